@@ -1,0 +1,175 @@
+/*
+ * fgfrft_b200.h -- C ABI of the B200-native FGFRFT hot path (libfgfrft_b200.so).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++/torch types. The C++
+ * drop-in header include/fgfrft/transform.hpp (same names and semantics as the reference
+ * header proj/include/fgfrft/transform.hpp) forwards every call here; a ctypes / cgo /
+ * JNI binding would bind exactly these symbols.
+ *
+ * Matrix convention (identical to Eigen::MatrixXcd, which the reference uses):
+ *   column-major, interleaved (re, im) doubles; element (i, j) of an n x n matrix is at
+ *   doubles [2*(i + j*n)] and [2*(i + j*n) + 1]. Signal blocks X are n x b, column-major.
+ *   complex64 caches take/return the same complex128 host buffers; storage and arithmetic
+ *   on the device are complex64 (fgfrft_dtype FGFRFT_C64).
+ *
+ * Series layout (identical to SincCoeffs, proj/include/fgfrft/sinc.hpp:40-48): arrays of
+ *   2L+1 doubles where entry [n + L] holds term n, n = -L..L.
+ *
+ * Errors: every function returns an fgfrft_status; no C++ exception crosses this boundary.
+ * The message of the last failure on the calling thread is fgfrft_last_error().
+ * Mapping to the reference exception taxonomy (proj/include/fgfrft/errors.hpp:36-62):
+ *   FGFRFT_PARAMETER -> parameter_error, FGFRFT_SHAPE -> shape_error,
+ *   FGFRFT_CAPACITY -> capacity_error, FGFRFT_NUMERICAL / FGFRFT_CUDA / FGFRFT_NCCL ->
+ *   numerical_error.
+ *
+ * Threading: calls on one handle are serialised by the handle; distinct handles may be
+ * used concurrently. Every call is synchronous with respect to host buffers. Calls taking
+ * device pointers (the *_dev variants) enqueue on the handle's stream and return without
+ * synchronising; fgfrft_cache_set_stream selects that stream.
+ */
+#ifndef FGFRFT_B200_H
+#define FGFRFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fgfrft_status {
+    FGFRFT_OK = 0,
+    FGFRFT_PARAMETER = 1,
+    FGFRFT_SHAPE = 2,
+    FGFRFT_CAPACITY = 3,
+    FGFRFT_NUMERICAL = 4,
+    FGFRFT_CUDA = 5,
+    FGFRFT_NCCL = 6
+} fgfrft_status;
+
+typedef enum fgfrft_dtype { FGFRFT_C128 = 0, FGFRFT_C64 = 1 } fgfrft_dtype;
+
+typedef enum fgfrft_which { FGFRFT_Q = 0, FGFRFT_DQ = 1 } fgfrft_which;
+
+/* Default budget of transform.hpp:17 (4 GiB). */
+#define FGFRFT_DEFAULT_MEMORY_BUDGET (4ULL << 30)
+
+typedef struct fgfrft_cache fgfrft_cache;
+
+/* ---- library ----------------------------------------------------------------------- */
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* fgfrft_last_error(void);
+
+/* Version string of the library ("0.1.0-b200"). */
+const char* fgfrft_version(void);
+
+/* Number of kernel launches this process has issued through the library (monotone). */
+uint64_t fgfrft_launch_count(void);
+
+/* sinc.hpp:50-63. c, dc: 2l+1 doubles each (either may be NULL). l < 1 -> PARAMETER. */
+int fgfrft_sinc_coeffs(double alpha, int l, double* c, double* dc);
+
+/* FNV-1a-64 over nbytes (rng.hpp:59-67), the cache fingerprint (gft.hpp:46-48). */
+uint64_t fgfrft_fnv1a64(const void* data, size_t nbytes);
+
+/* ---- power cache: replaces PowerCache (transform.hpp:41-80) ------------------------- */
+
+/*
+ * Build P_k = F^k, k = 1..l, on device `device` (transform.hpp:43-59): budget check
+ * l*n*n*elem > memory_budget -> CAPACITY (elem = 16 for C128, 8 for C64), FNV-1a
+ * fingerprint of f, P_1 = F, P_k = F P_{k-1} on FP64 tensor cores (DMMA).
+ * f: n x n host matrix (see convention). l < 1 or n < 1 -> PARAMETER.
+ */
+int fgfrft_cache_create(const double* f, int64_t n, int l, uint64_t memory_budget, int dtype,
+                        int device, fgfrft_cache** out);
+
+/* Same, but from host-built powers (l slabs, slab k-1 = F^k) -- no recursion on device. */
+int fgfrft_cache_create_from_powers(const double* powers, const double* f, int64_t n, int l,
+                                    uint64_t memory_budget, int dtype, int device,
+                                    fgfrft_cache** out);
+
+int fgfrft_cache_destroy(fgfrft_cache* cache);
+
+/* n, l, fingerprint, dtype, device (any pointer may be NULL). */
+int fgfrft_cache_info(const fgfrft_cache* cache, int64_t* n, int* l, uint64_t* fingerprint,
+                      int* dtype, int* device);
+
+/* transform.hpp:131-134: copy F^k (1 <= k <= l, else PARAMETER) to host (n x n). */
+int fgfrft_cache_power(fgfrft_cache* cache, int k, double* out);
+
+/* transform.hpp:136-139: NUMERICAL if fnv1a64(f) != stored fingerprint. */
+int fgfrft_cache_verify(const fgfrft_cache* cache, const double* f);
+
+/* Stream for subsequent calls on this handle (cudaStream_t as void*; NULL = handle's own). */
+int fgfrft_cache_set_stream(fgfrft_cache* cache, void* stream);
+
+/* Device pointer to slab k-1 (= F^k) and the device memory held by the handle. */
+int fgfrft_cache_device_slab(fgfrft_cache* cache, int k, void** dptr);
+int fgfrft_cache_device_bytes(const fgfrft_cache* cache, uint64_t* bytes);
+
+/* ---- series synthesis: replaces fgfrft_matrix / fgfrft_grad (transform.hpp:111-136) -- */
+
+/*
+ * For each of n_alpha orders: Q = c_0 I + sum_{k=1..L'} (c_k F^k + c_{-k} (F^k)^H) with
+ * c = sinc coefficients (which = FGFRFT_Q) or their alpha-derivatives (FGFRFT_DQ).
+ * L' = truncation (0 -> cache l; L' > l or < 0 -> PARAMETER; DQ always uses the full l).
+ * out: n_alpha consecutive n x n host matrices.
+ */
+int fgfrft_synthesize(fgfrft_cache* cache, const double* alphas, int n_alpha, int truncation,
+                      int which, double* out);
+
+/* Device variant: out_dev = n_alpha consecutive n x n device matrices of the cache dtype. */
+int fgfrft_synthesize_dev(fgfrft_cache* cache, const double* alphas, int n_alpha,
+                          int truncation, int which, void* out_dev);
+
+/* ---- apply: replaces apply_forward / apply_inverse (transform.hpp:138-148) ----------- */
+
+/*
+ * Y_a = Q(alpha_a) X (inverse = 0) or Q(alpha_a)^H X (inverse = 1) for n_alpha orders,
+ * Q synthesised on the device and consumed by the DMMA complex GEMM without a host
+ * round trip. x: n x b host; y: n_alpha consecutive n x b host blocks.
+ */
+int fgfrft_apply(fgfrft_cache* cache, const double* alphas, int n_alpha, int truncation,
+                 int inverse, const double* x, int64_t b, double* y);
+int fgfrft_apply_dev(fgfrft_cache* cache, const double* alphas, int n_alpha, int truncation,
+                     int inverse, const void* x_dev, int64_t b, void* y_dev);
+
+/*
+ * Plain apply of a materialised operator (FracOperator.q) -- apply_forward(op, X) exactly:
+ * Y = Q X (inverse = 0) or Q^H X (inverse = 1), Q: n x n host, X: n x b host, complex128.
+ * Runs the same DMMA GEMM on device `device`.
+ */
+int fgfrft_apply_matrix(const double* q, int64_t n, int inverse, const double* x, int64_t b,
+                        double* y, int device);
+
+/* ---- order gradient: dL/dalpha = sum_k c'_k(alpha) Re<G, F^k X> (learn.hpp:88-92) ---- */
+
+/*
+ * For each order a: s_{a,k} = Re<G_a, F^k X> for k = -L..L (written to s, n_alpha x (2L+1),
+ * may be NULL) and dlda[a] = sum_k c'_k(alpha_a) s_{a,k}. g: n_alpha consecutive n x b
+ * cotangents (dL/dconj(Y) convention of learn.hpp:92: L = ||R||^2 -> G = 2R / norm).
+ */
+int fgfrft_dlda(fgfrft_cache* cache, const double* alphas, int n_alpha, const double* g,
+                const double* x, int64_t b, double* s, double* dlda);
+int fgfrft_dlda_dev(fgfrft_cache* cache, const double* alphas, int n_alpha, const void* g_dev,
+                    const void* x_dev, int64_t b, double* s, double* dlda);
+
+/*
+ * MSE denoising step over an order sweep (the BASELINE config-2 workload): for each order a,
+ * Y_a = Q(alpha_a) X, loss_a = ||Y_a - Xc||_F^2 / (n b), G_a = 2 (Y_a - Xc) / (n b) and
+ * dlda_a = dloss_a/dalpha = sum_k c'_k(alpha_a) Re<G_a, F^k X>.
+ * Host variant: x, xc host (pinned for full speed), y host or NULL; loss, dlda host arrays of
+ * n_alpha; synchronous. Device variant: all pointers device, enqueued on the handle stream.
+ */
+int fgfrft_mse_step(fgfrft_cache* cache, const double* alphas, int n_alpha, const double* x,
+                    const double* xc, int64_t b, double* y, double* loss, double* dlda);
+int fgfrft_mse_step_dev(fgfrft_cache* cache, const double* alphas, int n_alpha,
+                        const void* x_dev, const void* xc_dev, int64_t b, void* y_dev,
+                        void* loss_dev, void* dlda_dev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FGFRFT_B200_H */

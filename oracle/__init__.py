@@ -1,0 +1,358 @@
+"""CPU oracle for the FGFRFT hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline / ``--impl
+reference`` leg may import this package; it is the checker, never the product. The product
+path (``paper_2602_20870_b200`` -> ``libfgfrft_b200.so``) neither imports nor links it.
+
+Pinning: the reference C++ library cannot be compiled here (Eigen3,
+CLI11, Catch2 absent; no network). Its std-only headers ARE compiled where they lie
+(oracle/ref_shim.cpp -> oracle/_ref/), which pins ``sinc_coeffs`` and the input RNG bit-exactly;
+the matrix parts are pinned by the reference's own known-answer tests
+(test_transform.cpp, test_sinc.cpp, acceptance.cpp criteria 1-6) re-run against this
+restatement in tests/test_oracle.py, and by committed golden vectors under tests/golden/.
+
+Restated reference functions (file:line under /root/reference/proj/include/fgfrft/):
+  sinc, sinc_deriv, sinc_coeffs      sinc.hpp:15-63          (C, fgfrft_oracle.c)
+  content_fingerprint / fnv1a64      gft.hpp:46-48, rng.hpp:59-67 (C)
+  PowerCache                         transform.hpp:41-80     (numpy GEMM recursion P_k = F P_{k-1})
+  fgfrft_matrix / fgfrft_grad        transform.hpp:21-34, 111-136 (C, 96x96 pair blocks)
+  apply_forward / apply_inverse      transform.hpp:138-148   (numpy zgemm)
+  eigendecompose_unitary             spectral.hpp:55-155     (numpy eigh, cluster refinement)
+  exact_gfrft / exact_gfrft_grad     spectral.hpp:158-174
+  phase_margin                       spectral.hpp:179-195
+  matrix_errors                      metrics.hpp:21-34
+  cascade dL/dalpha (K=1)            learn.hpp:88-92
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+import warnings
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+DEFAULT_MEMORY_BUDGET = 4 << 30  # transform.hpp:17
+
+
+class ParameterError(ValueError):
+    pass
+
+
+class ShapeError(ParameterError):
+    pass
+
+
+class CapacityError(ParameterError):
+    pass
+
+
+class NumericalError(ArithmeticError):
+    pass
+
+
+def build() -> str:
+    out = os.path.join(_HERE, "liboracle_fgfrft.so")
+    src = os.path.join(_HERE, "fgfrft_oracle.c")
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        subprocess.check_call(["make", "-s", "-C", _HERE, "all"])
+    return out
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        l = ctypes.CDLL(build())
+        d, i, i64, vp = ctypes.c_double, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+        l.oracle_sinc.restype = d
+        l.oracle_sinc.argtypes = [d]
+        l.oracle_sinc_deriv.restype = d
+        l.oracle_sinc_deriv.argtypes = [d]
+        l.oracle_sinc_coeffs.restype = i
+        l.oracle_sinc_coeffs.argtypes = [d, i, vp, vp]
+        l.oracle_fnv1a64.restype = ctypes.c_uint64
+        l.oracle_fnv1a64.argtypes = [vp, ctypes.c_size_t, ctypes.c_uint64]
+        l.oracle_synthesize.argtypes = [vp, i64, i, vp, vp, i]
+        l.oracle_power_dots.argtypes = [vp, i64, i, vp, vp]
+        l.oracle_max_threads.restype = i
+        _LIB = l
+    return _LIB
+
+
+# ----------------------------------------------------------------------------- sinc.hpp
+
+def sinc(x: float) -> float:
+    return lib().oracle_sinc(float(x))
+
+
+def sinc_deriv(x: float) -> float:
+    return lib().oracle_sinc_deriv(float(x))
+
+
+def sinc_coeffs(alpha: float, l: int):
+    """sinc.hpp:50-63 -> (c, dc), each 2l+1 doubles with entry [n + l] = term n."""
+    if l < 1:
+        raise ParameterError("sinc_coeffs: truncation order must be >= 1")
+    c = np.empty(2 * l + 1)
+    dc = np.empty(2 * l + 1)
+    lib().oracle_sinc_coeffs(float(alpha), int(l), c.ctypes.data, dc.ctypes.data)
+    return c, dc
+
+
+def content_fingerprint(f: np.ndarray) -> int:
+    """gft.hpp:46-48: FNV-1a-64 over the column-major interleaved complex128 bytes."""
+    buf = np.ascontiguousarray(np.asfortranarray(f, dtype=np.complex128).T)
+    return int(lib().oracle_fnv1a64(buf.ctypes.data, buf.nbytes, 0xCBF29CE484222325))
+
+
+# ----------------------------------------------------------------------------- transform.hpp
+
+class PowerCache:
+    """transform.hpp:41-80. Slabs are stored as a C-contiguous [l, n, n] array whose slab k-1
+    is P_k^T in row-major, i.e. P_k in column-major (the Eigen layout)."""
+
+    def __init__(self, f: np.ndarray, l: int, memory_budget: int = DEFAULT_MEMORY_BUDGET):
+        if l < 1:
+            raise ParameterError("PowerCache: truncation order must be >= 1")
+        f = np.asfortranarray(f, dtype=np.complex128)
+        n = f.shape[0]
+        nbytes = l * n * n * 16
+        if nbytes > memory_budget:
+            raise CapacityError(f"PowerCache: {l} powers of a {n}x{n} matrix need {nbytes} bytes, "
+                                f"over the {memory_budget}-byte budget")
+        self.l = l
+        self.n = n
+        self.fingerprint = content_fingerprint(f)
+        self.slabs = np.empty((l, n, n), dtype=np.complex128)
+        self.slabs[0] = f.T
+        for k in range(2, l + 1):
+            # P_k = F @ P_{k-1} (left multiply, transform.hpp:58); stored transposed:
+            # P_k^T = P_{k-1}^T @ F^T
+            np.matmul(self.slabs[k - 2], f.T, out=self.slabs[k - 1])
+
+    def power(self, k: int) -> np.ndarray:
+        if k < 1 or k > self.l:
+            raise ParameterError("PowerCache: power index out of range")
+        return self.slabs[k - 1].T
+
+    def verify(self, f: np.ndarray) -> None:
+        if content_fingerprint(f) != self.fingerprint:
+            raise NumericalError("PowerCache: fingerprint mismatch, cache is stale for this matrix")
+
+
+def _warn_window(alpha: float, l: int) -> None:
+    if abs(alpha) > l + 1.0:  # transform.hpp:97-104
+        warnings.warn(f"order alpha = {alpha} lies outside the series window [-{l + 1}, {l + 1}]; "
+                      "coefficient mass concentrates in dropped terms")
+
+
+def _synth(cache: PowerCache, coef: np.ndarray, l: int, nthreads: int = 1) -> np.ndarray:
+    q_t = np.empty((cache.n, cache.n), dtype=np.complex128)  # Q^T row-major == Q column-major
+    lib().oracle_synthesize(cache.slabs.ctypes.data, cache.n, l, np.ascontiguousarray(coef).ctypes.data,
+                            q_t.ctypes.data, nthreads)
+    return q_t.T
+
+
+def fgfrft_matrix(cache: PowerCache, alpha: float, truncation: int = 0, nthreads: int = 1) -> np.ndarray:
+    """transform.hpp:111-123 -> Q (n x n, column-major view)."""
+    l = cache.l if truncation == 0 else truncation
+    if l < 1 or l > cache.l:
+        raise ParameterError("fgfrft_matrix: truncation exceeds the cached power set")
+    _warn_window(alpha, l)
+    c, _ = sinc_coeffs(alpha, l)
+    return _synth(cache, c, l, nthreads)
+
+
+def fgfrft_grad(cache: PowerCache, alpha: float, nthreads: int = 1) -> np.ndarray:
+    """transform.hpp:127-136 -> dQ/dalpha."""
+    _warn_window(alpha, cache.l)
+    _, dc = sinc_coeffs(alpha, cache.l)
+    return _synth(cache, dc, cache.l, nthreads)
+
+
+def apply_forward(q: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """transform.hpp:138-141."""
+    if x.shape[0] != q.shape[1]:
+        raise ShapeError("apply_forward: signal length does not match operator")
+    return q @ x
+
+
+def apply_inverse(q: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """transform.hpp:145-148: Q^H x."""
+    if x.shape[0] != q.shape[0]:
+        raise ShapeError("apply_inverse: signal length does not match operator")
+    return q.conj().T @ x
+
+
+def power_dots(cache: PowerCache, m: np.ndarray) -> np.ndarray:
+    """s_k = Re<M, F^k> for k = -L..L ([k + L] layout), so that Re<G, F^k X> = s_k with
+    M = G X^H, and dL/dalpha = sum_k c'_k s_k (definition: learn.hpp:88-92)."""
+    mt = np.ascontiguousarray(np.asfortranarray(m, dtype=np.complex128).T)
+    out = np.empty(2 * cache.l + 1)
+    lib().oracle_power_dots(cache.slabs.ctypes.data, cache.n, cache.l, mt.ctypes.data, out.ctypes.data)
+    return out
+
+
+def dlda_mse(cache: PowerCache, alpha: float, x: np.ndarray, x_clean: np.ndarray):
+    """MSE denoising loss L = ||Q^a X - Xc||_F^2 / (N B) and dL/dalpha, evaluated the way the
+    reference's cascade does (learn.hpp:82-92 with K=1): dL/da = Re sum conj(G) o (dQ X),
+    G = 2 (Y - Xc) / (N B). Returns (loss, dlda, Y)."""
+    n, b = x.shape
+    q = fgfrft_matrix(cache, alpha)
+    y = q @ x
+    r = y - x_clean
+    loss = float(np.vdot(r, r).real) / (n * b)
+    g = 2.0 * r / (n * b)
+    dq = fgfrft_grad(cache, alpha)
+    dlda = float(np.sum(np.conj(g) * (dq @ x)).real)
+    return loss, dlda, y
+
+
+# ----------------------------------------------------------------------------- spectral.hpp
+
+K_CLUSTER_GAP = 1e-5  # spectral.hpp:43
+
+
+def _wrap_phase(lam: np.ndarray) -> np.ndarray:
+    t = np.arctan2(lam.imag, lam.real)  # spectral.hpp:34-38
+    t[t <= -math.pi] = math.pi
+    return t
+
+
+def _refine_clusters(cosv, w, fw, skew):
+    """spectral.hpp:55-82."""
+    n = w.shape[0]
+    lam = np.empty(n, dtype=np.complex128)
+    lo = 0
+    while lo < n:
+        hi = lo
+        while hi + 1 < n and cosv[hi + 1] - cosv[hi] <= K_CLUSTER_GAP:
+            hi += 1
+        k = hi - lo + 1
+        if k > 1:
+            m = skew(w, lo, k)
+            _, u = np.linalg.eigh(m)
+            w[:, lo:hi + 1] = w[:, lo:hi + 1] @ u
+            fw[:, lo:hi + 1] = fw[:, lo:hi + 1] @ u
+        for c in range(lo, hi + 1):
+            lam[c] = np.vdot(w[:, c], fw[:, c])
+        lo = hi + 1
+    return w, fw, lam
+
+
+def is_real(f: np.ndarray, tol: float = 1e-13) -> bool:
+    return float(np.abs(f.imag).max()) <= tol  # gft.hpp:34-36
+
+
+def eigendecompose_unitary(f: np.ndarray, known=None):
+    """spectral.hpp:121-155 -> (V, theta ascending). ``known`` = (V, theta) short-circuit."""
+    if known is not None:
+        return known
+    f = np.asarray(f, dtype=np.complex128)
+    if is_real(f):  # spectral.hpp:84-98
+        fr = f.real
+        s = 0.5 * (fr + fr.T)
+        cosv, ev = np.linalg.eigh(s)
+        b = 0.5 * (fr - fr.T)
+        w = ev.astype(np.complex128)
+        fw = (fr @ ev).astype(np.complex128)
+
+        def skew(wcur, lo, k):
+            wc = wcur[:, lo:lo + k].real
+            return (wc.T @ (b @ wc)).astype(np.complex128) * (-1j)
+    else:  # spectral.hpp:100-112
+        a = 0.5 * (f + f.conj().T)
+        cosv, w = np.linalg.eigh(a)
+        b = (f - f.conj().T) * (-0.5j)
+        fw = f @ w
+
+        def skew(wcur, lo, k):
+            wc = wcur[:, lo:lo + k]
+            return wc.conj().T @ (b @ wc)
+    w, fw, lam = _refine_clusters(cosv, np.array(w, dtype=np.complex128), np.array(fw), skew)
+    theta = _wrap_phase(lam)
+    order = np.argsort(theta, kind="stable")
+    v = w[:, order]
+    theta = theta[order]
+    resid = fw[:, order] - np.exp(1j * theta)[None, :] * v
+    rel = np.linalg.norm(resid) / max(np.linalg.norm(f), 1e-300)
+    if rel > 1e-6:
+        raise NumericalError(f"eigendecompose_unitary: reconstruction residual {rel} exceeds 1e-6")
+    return v, theta
+
+
+def exact_gfrft(eig, alpha: float) -> np.ndarray:
+    """spectral.hpp:158-166: V diag(e^{j alpha theta}) V^H."""
+    v, theta = eig
+    return (v * np.exp(1j * alpha * theta)[None, :]) @ v.conj().T
+
+
+def exact_gfrft_grad(eig, alpha: float) -> np.ndarray:
+    """spectral.hpp:169-174."""
+    v, theta = eig
+    return (v * (1j * theta * np.exp(1j * alpha * theta))[None, :]) @ v.conj().T
+
+
+def phase_margin(theta: np.ndarray) -> float:
+    """spectral.hpp:179-195."""
+    margin = float(np.min(math.pi - np.abs(theta))) if len(theta) else math.pi
+    margin = min(margin, math.pi)
+    if margin < 0.05 * math.pi:
+        warnings.warn(f"phase margin {margin} is below 0.05*pi; series approximation accuracy is at risk")
+    return margin
+
+
+# ----------------------------------------------------------------------------- metrics.hpp
+
+def matrix_errors(approx: np.ndarray, reference: np.ndarray):
+    """metrics.hpp:21-34 -> dict(mse, mae, nmse)."""
+    if approx.shape != reference.shape:
+        raise ShapeError("matrix_errors: shape mismatch")
+    ref_sq = float(np.vdot(reference, reference).real)
+    if ref_sq == 0.0:
+        raise NumericalError("matrix_errors: NMSE undefined for all-zero reference")
+    d = approx - reference
+    cnt = float(d.size)
+    sq = float(np.vdot(d, d).real)
+    return {"mse": sq / cnt, "mae": float(np.abs(d).sum()) / cnt, "nmse": sq / ref_sq}
+
+
+# ----------------------------------------------------------------------------- tests/oracles.hpp
+
+def scalar_series(theta: float, alpha: float, l: int) -> complex:
+    """tests/oracles.hpp:23-30."""
+    acc = 0j
+    for n in range(-l, l + 1):
+        x = alpha - n
+        s = (1.0 if x == 0 else 0.0) if x == round(x) else math.sin(math.pi * x) / (math.pi * x)
+        acc += s * complex(math.cos(n * theta), math.sin(n * theta))
+    return acc
+
+
+def truncation_bound(thetas, alpha: float, l: int) -> float:
+    """tests/oracles.hpp:31-41."""
+    return max(abs(complex(math.cos(alpha * t), math.sin(alpha * t)) - scalar_series(t, alpha, l))
+               for t in thetas)
+
+
+def spectral_norm(m: np.ndarray) -> float:
+    return float(np.linalg.svd(m, compute_uv=False)[0])
+
+
+def matrix_power(f: np.ndarray, m: int) -> np.ndarray:
+    """tests/oracles.hpp:50-56."""
+    acc = np.eye(f.shape[0], dtype=np.complex128)
+    base = f if m >= 0 else f.conj().T
+    for _ in range(abs(m)):
+        acc = base @ acc
+    return acc
+
+
+def rotation2(phi: float) -> np.ndarray:
+    """tests/oracles.hpp:43-48."""
+    return np.array([[math.cos(phi), -math.sin(phi)], [math.sin(phi), math.cos(phi)]], dtype=np.complex128)

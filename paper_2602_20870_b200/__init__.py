@@ -1,0 +1,327 @@
+"""B200-native FGFRFT hot path -- Python binding of the C ABI (include/fgfrft_b200.h).
+
+The product is ``libfgfrft_b200.so`` (hand-written sm_100a kernels behind an ``extern "C"``
+boundary); the C++ drop-in header ``include/fgfrft/transform.hpp`` is the reference-facing
+API. This module is a thin ctypes binding with the same names and error behaviour as the
+reference (proj/include/fgfrft/transform.hpp:41-148, sinc.hpp:50-63, errors.hpp:36-62) so
+tests and bench.py read like the reference's own tests. There is no CPU fallback: if the
+shared library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import warnings
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "ParameterError", "ShapeError", "CapacityError", "NumericalError", "DEFAULT_MEMORY_BUDGET",
+    "C128", "C64", "lib", "sinc_coeffs", "fnv1a64", "PowerCache", "build_power_cache",
+    "FracOperator", "fgfrft_matrix", "fgfrft_grad", "apply_forward", "apply_inverse",
+    "apply_series", "dlda", "mse_step", "launch_count",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfgfrft_b200.so")
+DEFAULT_MEMORY_BUDGET = 4 << 30  # transform.hpp:17
+C128, C64 = 0, 1
+Q, DQ = 0, 1
+
+
+class ParameterError(ValueError):
+    """errors.hpp:36 parameter_error."""
+
+
+class ShapeError(ParameterError):
+    """errors.hpp:40 shape_error."""
+
+
+class CapacityError(ParameterError):
+    """errors.hpp:44 capacity_error."""
+
+
+class NumericalError(ArithmeticError):
+    """errors.hpp:48 numerical_error (also CUDA / NCCL failures)."""
+
+
+_STATUS = {1: ParameterError, 2: ShapeError, 3: CapacityError, 4: NumericalError, 5: NumericalError,
+           6: NumericalError}
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfgfrft_b200.so (raises if it has not been built: no silent fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() or paper_2602_20870_b200/build.sh")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i, i64, u64, d = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "fgfrft_last_error": (ctypes.c_char_p, []),
+        "fgfrft_version": (ctypes.c_char_p, []),
+        "fgfrft_launch_count": (u64, []),
+        "fgfrft_sinc_coeffs": (i, [d, i, vp, vp]),
+        "fgfrft_fnv1a64": (u64, [vp, ctypes.c_size_t]),
+        "fgfrft_cache_create": (i, [vp, i64, i, u64, i, i, pp]),
+        "fgfrft_cache_create_from_powers": (i, [vp, vp, i64, i, u64, i, i, pp]),
+        "fgfrft_cache_destroy": (i, [vp]),
+        "fgfrft_cache_info": (i, [vp, vp, vp, vp, vp, vp]),
+        "fgfrft_cache_power": (i, [vp, i, vp]),
+        "fgfrft_cache_verify": (i, [vp, vp]),
+        "fgfrft_cache_set_stream": (i, [vp, vp]),
+        "fgfrft_cache_device_slab": (i, [vp, i, pp]),
+        "fgfrft_cache_device_bytes": (i, [vp, vp]),
+        "fgfrft_synthesize": (i, [vp, vp, i, i, i, vp]),
+        "fgfrft_synthesize_dev": (i, [vp, vp, i, i, i, vp]),
+        "fgfrft_apply": (i, [vp, vp, i, i, i, vp, i64, vp]),
+        "fgfrft_apply_dev": (i, [vp, vp, i, i, i, vp, i64, vp]),
+        "fgfrft_apply_matrix": (i, [vp, i64, i, vp, i64, vp, i]),
+        "fgfrft_dlda": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
+        "fgfrft_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
+        "fgfrft_mse_step": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
+        "fgfrft_mse_step_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = L
+    return L
+
+
+def exported_symbols():
+    return [
+        "fgfrft_last_error", "fgfrft_version", "fgfrft_launch_count", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
+        "fgfrft_cache_create", "fgfrft_cache_create_from_powers", "fgfrft_cache_destroy", "fgfrft_cache_info",
+        "fgfrft_cache_power", "fgfrft_cache_verify", "fgfrft_cache_set_stream", "fgfrft_cache_device_slab",
+        "fgfrft_cache_device_bytes", "fgfrft_synthesize", "fgfrft_synthesize_dev", "fgfrft_apply",
+        "fgfrft_apply_dev", "fgfrft_apply_matrix", "fgfrft_dlda", "fgfrft_dlda_dev", "fgfrft_mse_step",
+        "fgfrft_mse_step_dev",
+    ]
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().fgfrft_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, NumericalError)(msg)
+
+
+def launch_count() -> int:
+    return int(lib().fgfrft_launch_count())
+
+
+def _cm(a: np.ndarray) -> np.ndarray:
+    """Column-major complex128 view/copy (the Eigen::MatrixXcd layout)."""
+    a = np.asarray(a)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    return np.asfortranarray(a, dtype=np.complex128)
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _alphas(alphas) -> np.ndarray:
+    return np.ascontiguousarray(np.atleast_1d(np.asarray(alphas, dtype=np.float64)))
+
+
+# ----------------------------------------------------------------------------- sinc.hpp
+
+def sinc_coeffs(alpha: float, l: int):
+    """sinc.hpp:50-63 -> (c, dc) with entry [n + l] = term n."""
+    c = np.empty(max(2 * l + 1, 1))
+    dc = np.empty(max(2 * l + 1, 1))
+    _check(lib().fgfrft_sinc_coeffs(float(alpha), int(l), _ptr(c), _ptr(dc)))
+    return c, dc
+
+
+def fnv1a64(buf: np.ndarray) -> int:
+    b = np.ascontiguousarray(buf)
+    return int(lib().fgfrft_fnv1a64(_ptr(b), b.nbytes))
+
+
+def content_fingerprint(f: np.ndarray) -> int:
+    """gft.hpp:46-48 over the column-major bytes."""
+    fc = _cm(f)
+    return fnv1a64(np.ascontiguousarray(fc.T))
+
+
+# ----------------------------------------------------------------------------- transform.hpp
+
+class PowerCache:
+    """transform.hpp:41-80 on the GPU. ``PowerCache(f, l, memory_budget)`` builds P_k = F^k,
+    k = 1..l on device (DMMA GEMM chain). Move-only in spirit: the handle owns device memory."""
+
+    def __init__(self, f: np.ndarray, l: int, memory_budget: int = DEFAULT_MEMORY_BUDGET, dtype: int = C128,
+                 device: int = 0, powers: Optional[np.ndarray] = None):
+        self._h = ctypes.c_void_p()
+        fc = _cm(f)
+        if fc.shape[0] != fc.shape[1]:
+            raise ShapeError("PowerCache: F must be square")
+        n = fc.shape[0]
+        if powers is None:
+            _check(lib().fgfrft_cache_create(_ptr(fc), n, int(l), int(memory_budget), dtype, device,
+                                             ctypes.byref(self._h)))
+        else:
+            p = np.ascontiguousarray(powers, dtype=np.complex128)  # [l, n, n] slabs of P_k^T (col-major P_k)
+            _check(lib().fgfrft_cache_create_from_powers(_ptr(p), _ptr(fc), n, int(l), int(memory_budget), dtype,
+                                                         device, ctypes.byref(self._h)))
+        self._n, self._l, self.dtype, self.device = n, int(l), dtype, device
+        fp = ctypes.c_uint64()
+        _check(lib().fgfrft_cache_info(self._h, None, None, ctypes.addressof(fp), None, None))
+        self._fp = fp.value
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().fgfrft_cache_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def l(self) -> int:
+        return self._l
+
+    def n(self) -> int:
+        return self._n
+
+    def fingerprint(self) -> int:
+        return self._fp
+
+    def power(self, k: int) -> np.ndarray:
+        out = np.empty((self._n, self._n), dtype=np.complex128, order="F")
+        _check(lib().fgfrft_cache_power(self._h, int(k), _ptr(out)))
+        return out
+
+    def verify(self, f: np.ndarray) -> None:
+        fc = _cm(f)
+        _check(lib().fgfrft_cache_verify(self._h, _ptr(fc)))
+
+    def set_stream(self, stream_handle: int) -> None:
+        _check(lib().fgfrft_cache_set_stream(self._h, ctypes.c_void_p(stream_handle)))
+
+    def device_bytes(self) -> int:
+        b = ctypes.c_uint64()
+        _check(lib().fgfrft_cache_device_bytes(self._h, ctypes.addressof(b)))
+        return b.value
+
+
+def build_power_cache(f, l, memory_budget=DEFAULT_MEMORY_BUDGET, **kw) -> PowerCache:
+    """transform.hpp:82-85."""
+    return PowerCache(f, l, memory_budget, **kw)
+
+
+class FracOperator:
+    """transform.hpp:89-93: {q, alpha, l}; l = 0 marks an exact spectral operator."""
+
+    def __init__(self, q: np.ndarray, alpha: float, l: int):
+        self.q, self.alpha, self.l = q, alpha, l
+
+
+def _warn_window(alpha: float, l: int) -> None:
+    if abs(alpha) > l + 1.0:  # transform.hpp:97-104
+        warnings.warn(f"order alpha = {alpha:g} lies outside the series window [-{l + 1}, {l + 1}]; "
+                      "coefficient mass concentrates in dropped terms")
+
+
+def synthesize(cache: PowerCache, alphas, truncation: int = 0, which: int = Q) -> np.ndarray:
+    """Multi-order synthesis: returns [A, n, n] with out[a] = Q(alpha_a) (column-major views)."""
+    al = _alphas(alphas)
+    buf = np.empty((len(al), cache.n(), cache.n()), dtype=np.complex128)  # slab a = Q_a^T row-major
+    _check(lib().fgfrft_synthesize(cache.handle, _ptr(al), len(al), int(truncation), which, _ptr(buf)))
+    return np.transpose(buf, (0, 2, 1))
+
+
+def fgfrft_matrix(cache: PowerCache, alpha: float, truncation: int = 0) -> FracOperator:
+    """transform.hpp:111-123."""
+    l = cache.l() if truncation == 0 else truncation
+    if l < 1 or l > cache.l():
+        raise ParameterError("fgfrft_matrix: truncation exceeds the cached power set")
+    _warn_window(alpha, l)
+    return FracOperator(synthesize(cache, [alpha], truncation, Q)[0], float(alpha), l)
+
+
+def fgfrft_grad(cache: PowerCache, alpha: float) -> np.ndarray:
+    """transform.hpp:127-136."""
+    _warn_window(alpha, cache.l())
+    return synthesize(cache, [alpha], 0, DQ)[0]
+
+
+def apply_forward(op: FracOperator, x: np.ndarray, device: int = 0) -> np.ndarray:
+    """transform.hpp:138-141: Q X on the DMMA GEMM."""
+    xc = _cm(x)
+    q = _cm(op.q)
+    if xc.shape[0] != q.shape[1]:
+        raise ShapeError("apply_forward: signal length does not match operator")
+    y = np.empty_like(xc, order="F")
+    _check(lib().fgfrft_apply_matrix(_ptr(q), q.shape[0], 0, _ptr(xc), xc.shape[1], _ptr(y), device))
+    return y
+
+
+def apply_inverse(op: FracOperator, x: np.ndarray, device: int = 0) -> np.ndarray:
+    """transform.hpp:145-148: Q^H X."""
+    xc = _cm(x)
+    q = _cm(op.q)
+    if xc.shape[0] != q.shape[0]:
+        raise ShapeError("apply_inverse: signal length does not match operator")
+    y = np.empty_like(xc, order="F")
+    _check(lib().fgfrft_apply_matrix(_ptr(q), q.shape[0], 1, _ptr(xc), xc.shape[1], _ptr(y), device))
+    return y
+
+
+def apply_series(cache: PowerCache, alphas, x: np.ndarray, truncation: int = 0, inverse: bool = False) -> np.ndarray:
+    """Extension: Y_a = Q(alpha_a) X (or Q^H X) for many orders without a host round trip of Q.
+    Returns [A, n, b] where out[a] is column-major n x b."""
+    al = _alphas(alphas)
+    xc = _cm(x)
+    if xc.shape[0] != cache.n():
+        raise ShapeError("apply_forward: signal length does not match operator")
+    b = xc.shape[1]
+    y = np.empty((len(al), b, cache.n()), dtype=np.complex128)
+    _check(lib().fgfrft_apply(cache.handle, _ptr(al), len(al), int(truncation), int(inverse), _ptr(xc), b, _ptr(y)))
+    return np.transpose(y, (0, 2, 1))
+
+
+def dlda(cache: PowerCache, alphas, g: Sequence[np.ndarray], x: np.ndarray):
+    """Extension: s[a, k + L] = Re<G_a, F^k X> and dL/dalpha_a = sum_k c'_k s[a, k + L]."""
+    al = _alphas(alphas)
+    xc = _cm(x)
+    b = xc.shape[1]
+    gs = np.stack([np.ascontiguousarray(_cm(gi).T) for gi in g]) if len(al) else np.empty(0)
+    if gs.shape != (len(al), b, cache.n()) or xc.shape[0] != cache.n():
+        raise ShapeError("dlda: cotangent / signal shape mismatch")
+    s = np.empty((len(al), 2 * cache.l() + 1))
+    out = np.empty(len(al))
+    _check(lib().fgfrft_dlda(cache.handle, _ptr(al), len(al), _ptr(gs), _ptr(xc), b, _ptr(s), _ptr(out)))
+    return out, s
+
+
+def mse_step(cache: PowerCache, alphas, x: np.ndarray, x_clean: np.ndarray, want_y: bool = False):
+    """Extension: for each order, loss = ||Q X - Xc||^2/(n b) and dloss/dalpha (host buffers)."""
+    al = _alphas(alphas)
+    xc = _cm(x)
+    xcl = _cm(x_clean)
+    if xc.shape != xcl.shape or xc.shape[0] != cache.n():
+        raise ShapeError("mse_step: signal shape mismatch")
+    b = xc.shape[1]
+    loss = np.empty(len(al))
+    dl = np.empty(len(al))
+    y = np.empty((len(al), b, cache.n()), dtype=np.complex128) if want_y else None
+    _check(lib().fgfrft_mse_step(cache.handle, _ptr(al), len(al), _ptr(xc), _ptr(xcl), b,
+                                 _ptr(y) if want_y else None, _ptr(loss), _ptr(dl)))
+    return loss, dl, (np.transpose(y, (0, 2, 1)) if want_y else None)

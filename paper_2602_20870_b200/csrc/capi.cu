@@ -1,0 +1,738 @@
+// capi.cu -- the C ABI (include/fgfrft_b200.h): handle lifetime, validation with the
+// reference's error semantics, host<->device staging and orchestration of the kernels.
+//
+// Reference interfaces replaced (proj/include/fgfrft/):
+//   PowerCache ctor / power / verify / fingerprint  transform.hpp:43-74   -> fgfrft_cache_*
+//   fgfrft_matrix / fgfrft_grad                     transform.hpp:111-136 -> fgfrft_synthesize*
+//   apply_forward / apply_inverse                   transform.hpp:138-148 -> fgfrft_apply*, _matrix
+//   sinc_coeffs                                     sinc.hpp:50-63        -> fgfrft_sinc_coeffs
+//   dL/dalpha contraction                           learn.hpp:88-94       -> fgfrft_dlda*, mse_step*
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fgfrft_b200.h"
+
+namespace fgb {
+double host_sinc(double);
+double host_sinc_deriv(double);
+void host_sinc_coeffs(double alpha, int l, double* c, double* dc);
+uint64_t host_fnv1a64(const void* data, size_t nbytes);
+template <typename R>
+cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                         cudaStream_t stream);
+cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
+                         int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
+                         bool accumulate, cudaStream_t stream);
+cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                              double* partial, double* s_out, cudaStream_t stream);
+size_t dots_partial_elems(int n, int l, int n_alpha);
+cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, int n_alpha, double g_scale,
+                                double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream);
+size_t mse_partial_elems(int n_alpha);
+cudaError_t launch_demote(const void* src, void* dst, int64_t count, cudaStream_t stream);
+cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int width, double* out,
+                            cudaStream_t stream);
+}  // namespace fgb
+
+using namespace fgb;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define FGB_CUDA(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess) {                                                                \
+            cudaGetLastError();                                                                 \
+            return fail(FGFRFT_CUDA, std::string(#expr) + " failed: " + cudaGetErrorString(e_)); \
+        }                                                                                       \
+    } while (0)
+
+#define FGB_LAUNCH(expr, nlaunch)  \
+    do {                           \
+        FGB_CUDA(expr);            \
+        g_launches += (nlaunch);   \
+    } while (0)
+
+#define FGB_GUARD_BEGIN try {
+#define FGB_GUARD_END                                                        \
+    }                                                                        \
+    catch (const std::bad_alloc&) {                                          \
+        return fail(FGFRFT_CAPACITY, "host allocation failed");              \
+    }                                                                        \
+    catch (const std::exception& ex) {                                       \
+        return fail(FGFRFT_NUMERICAL, ex.what());                            \
+    }                                                                        \
+    catch (...) {                                                            \
+        return fail(FGFRFT_NUMERICAL, "unknown exception");                  \
+    }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct fgfrft_cache {
+    int64_t n = 0;
+    int l = 0;
+    int dtype = FGFRFT_C128;
+    int device = 0;
+    uint64_t fingerprint = 0;
+    void* slabs = nullptr;
+    size_t elem = 16;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    // workspaces
+    DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda;
+    double* coef_h = nullptr;  // pinned staging for the coefficient tables
+    size_t coef_h_cap = 0;
+    cudaEvent_t coef_evt = nullptr;
+
+    size_t slab_elems() const { return (size_t)n * (size_t)n; }
+    size_t slab_bytes() const { return slab_elems() * elem; }
+    void* slab(int k) const { return static_cast<char*>(slabs) + (size_t)(k - 1) * slab_bytes(); }
+};
+
+namespace {
+
+int check_handle(const fgfrft_cache* c) {
+    if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_cache handle");
+    return FGFRFT_OK;
+}
+
+// Orders per device chunk: keep a chunk's Q / M workspace L2-resident (~64 MiB) when possible.
+int alpha_chunk(const fgfrft_cache* c, int n_alpha) {
+    if (const char* env = std::getenv("FGFRFT_ALPHA_CHUNK")) {
+        const int v = std::atoi(env);
+        if (v > 0) return v < n_alpha ? v : n_alpha;
+    }
+    const size_t budget = (size_t)64 << 20;
+    size_t a = budget / (c->slab_elems() * 16);
+    if (a < 1) a = 1;
+    if (a > (size_t)n_alpha) a = (size_t)n_alpha;
+    return (int)a;
+}
+
+// Compute [c | dc] tables for the orders (layout [2][n_alpha][2l+1]) into pinned memory and
+// upload them on the handle stream. The previous upload must have completed before the
+// pinned staging is rewritten (it is enqueued ahead of the kernels that read it).
+int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, double** dev) {
+    const size_t width = (size_t)(2 * l + 1);
+    const size_t count = 2 * (size_t)n_alpha * width;
+    if (c->coef_evt) FGB_CUDA(cudaEventSynchronize(c->coef_evt));
+    if (c->coef_h_cap < count) {
+        if (c->coef_h) cudaFreeHost(c->coef_h);
+        c->coef_h = nullptr;
+        c->coef_h_cap = 0;
+        FGB_CUDA(cudaMallocHost(&c->coef_h, count * sizeof(double)));
+        c->coef_h_cap = count;
+    }
+    for (int a = 0; a < n_alpha; ++a)
+        host_sinc_coeffs(alphas[a], l, c->coef_h + a * width, c->coef_h + ((size_t)n_alpha + a) * width);
+    FGB_CUDA(c->coef.ensure(count * sizeof(double)));
+    FGB_CUDA(cudaMemcpyAsync(c->coef.p, c->coef_h, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (!c->coef_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->coef_evt, cudaEventDisableTiming));
+    FGB_CUDA(cudaEventRecord(c->coef_evt, c->stream));
+    *dev = c->coef.as<double>();
+    return FGFRFT_OK;
+}
+
+int check_alphas(const double* alphas, int n_alpha) {
+    if (n_alpha < 1 || !alphas) return fail(FGFRFT_PARAMETER, "need at least one order");
+    for (int a = 0; a < n_alpha; ++a)
+        if (!std::isfinite(alphas[a])) return fail(FGFRFT_PARAMETER, "order alpha must be finite");
+    return FGFRFT_OK;
+}
+
+int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out) {
+    if (c->dtype == FGFRFT_C128)
+        FGB_LAUNCH(launch_synth<double>(c->slabs, (int)c->n, l_used, coef_dev, n_alpha, out, c->stream), 1);
+    else
+        FGB_LAUNCH(launch_synth<float>(c->slabs, (int)c->n, l_used, coef_dev, n_alpha, out, c->stream), 1);
+    return FGFRFT_OK;
+}
+
+int require_c128(const fgfrft_cache* c, const char* what) {
+    if (c->dtype != FGFRFT_C128)
+        return fail(FGFRFT_PARAMETER, std::string(what) + ": complex64 caches support synthesis only in this build");
+    return FGFRFT_OK;
+}
+
+int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype, int device, fgfrft_cache** out,
+                  fgfrft_cache** made) {
+    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
+    *out = nullptr;
+    if (l < 1) return fail(FGFRFT_PARAMETER, "PowerCache: truncation order must be >= 1");
+    if (n < 1 || !f) return fail(FGFRFT_PARAMETER, "PowerCache: matrix must be non-empty");
+    if (n > (1 << 30) / 2) return fail(FGFRFT_CAPACITY, "PowerCache: n exceeds the 32-bit tile index range");
+    if (dtype != FGFRFT_C128 && dtype != FGFRFT_C64) return fail(FGFRFT_PARAMETER, "unknown dtype");
+    if (dtype == FGFRFT_C64 && (n % 2) != 0)
+        return fail(FGFRFT_PARAMETER, "complex64 caches need an even n (16-byte TMA column alignment)");
+    const uint64_t elem = dtype == FGFRFT_C128 ? 16 : 8;
+    const unsigned __int128 bytes = (unsigned __int128)l * (uint64_t)n * (uint64_t)n * elem;
+    if (bytes > budget) {
+        std::ostringstream msg;
+        msg << "PowerCache: " << l << " powers of a " << n << "x" << n << " matrix need "
+            << (unsigned long long)bytes << " bytes, over the " << budget << "-byte budget";
+        return fail(FGFRFT_CAPACITY, msg.str());
+    }
+    int ndev = 0;
+    FGB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(FGFRFT_PARAMETER, "device index out of range");
+    auto* c = new fgfrft_cache();
+    c->n = n;
+    c->l = l;
+    c->dtype = dtype;
+    c->device = device;
+    c->elem = elem;
+    c->fingerprint = host_fnv1a64(f, (size_t)n * (size_t)n * 16);
+    DeviceGuard dg(device);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    c->stream = c->own_stream;
+    e = cudaMalloc(&c->slabs, (size_t)bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamDestroy(c->own_stream);
+        delete c;
+        std::ostringstream msg;
+        msg << "PowerCache: device allocation of " << (unsigned long long)bytes
+            << " bytes failed (" << cudaGetErrorString(e) << ")";
+        return fail(FGFRFT_CAPACITY, msg.str());
+    }
+    *made = c;
+    return FGFRFT_OK;
+}
+
+void destroy_cache(fgfrft_cache* c) {
+    if (!c) return;
+    DeviceGuard dg(c->device);
+    if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+    if (c->stream && c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
+                      &c->loss, &c->dlda})
+        b->release();
+    if (c->coef_h) cudaFreeHost(c->coef_h);
+    if (c->coef_evt) cudaEventDestroy(c->coef_evt);
+    if (c->slabs) cudaFree(c->slabs);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+// Device cache build: P_1 = F, P_k = F P_{k-1} (transform.hpp:57-58) with the DMMA GEMM.
+// complex64 caches are built in complex128 and demoted slab by slab (error does not compound
+// through a complex64 recursion).
+int build_powers(fgfrft_cache* c, const double* f) {
+    const size_t sl = c->slab_elems();
+    const int n = (int)c->n;
+    if (c->dtype == FGFRFT_C128) {
+        FGB_CUDA(cudaMemcpyAsync(c->slab(1), f, sl * 16, cudaMemcpyHostToDevice, c->stream));
+        for (int k = 2; k <= c->l; ++k)
+            FGB_LAUNCH(launch_zgemm(n, n, n, c->slab(1), n, 0, false, c->slab(k - 1), n, 0, false, c->slab(k), n, 0,
+                                    1, false, c->stream),
+                       1);
+    } else {
+        FGB_CUDA(c->q.ensure(3 * sl * 16));
+        double2* fbuf = c->q.as<double2>();
+        double2* prev = fbuf + sl;
+        double2* cur = fbuf + 2 * sl;
+        FGB_CUDA(cudaMemcpyAsync(fbuf, f, sl * 16, cudaMemcpyHostToDevice, c->stream));
+        FGB_LAUNCH(launch_demote(fbuf, c->slab(1), (int64_t)sl, c->stream), 1);
+        FGB_CUDA(cudaMemcpyAsync(prev, fbuf, sl * 16, cudaMemcpyDeviceToDevice, c->stream));
+        for (int k = 2; k <= c->l; ++k) {
+            FGB_LAUNCH(launch_zgemm(n, n, n, fbuf, n, 0, false, prev, n, 0, false, cur, n, 0, 1, false, c->stream), 1);
+            FGB_LAUNCH(launch_demote(cur, c->slab(k), (int64_t)sl, c->stream), 1);
+            std::swap(prev, cur);
+        }
+    }
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    return FGFRFT_OK;
+}
+
+int upload_powers(fgfrft_cache* c, const double* powers) {
+    const size_t sl = c->slab_elems();
+    if (c->dtype == FGFRFT_C128) {
+        FGB_CUDA(cudaMemcpyAsync(c->slabs, powers, sl * 16 * c->l, cudaMemcpyHostToDevice, c->stream));
+    } else {
+        FGB_CUDA(c->q.ensure(sl * 16));
+        for (int k = 1; k <= c->l; ++k) {
+            FGB_CUDA(cudaMemcpyAsync(c->q.p, powers + 2 * sl * (k - 1), sl * 16, cudaMemcpyHostToDevice, c->stream));
+            FGB_LAUNCH(launch_demote(c->q.p, c->slab(k), (int64_t)sl, c->stream), 1);
+        }
+    }
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    return FGFRFT_OK;
+}
+
+// Copy n_alpha device results of the cache dtype to complex128 host matrices.
+int download_as_c128(fgfrft_cache* c, const void* dev, size_t elems, double* host) {
+    if (c->dtype == FGFRFT_C128) {
+        FGB_CUDA(cudaMemcpyAsync(host, dev, elems * 16, cudaMemcpyDeviceToHost, c->stream));
+        FGB_CUDA(cudaStreamSynchronize(c->stream));
+        return FGFRFT_OK;
+    }
+    std::vector<float> tmp(2 * elems);
+    FGB_CUDA(cudaMemcpyAsync(tmp.data(), dev, elems * 8, cudaMemcpyDeviceToHost, c->stream));
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < 2 * elems; ++i) host[i] = (double)tmp[i];
+    return FGFRFT_OK;
+}
+
+int resolve_truncation(const fgfrft_cache* c, int truncation, int which, int* l_used) {
+    const int l = (which == FGFRFT_DQ || truncation == 0) ? c->l : truncation;
+    if (l < 1 || l > c->l) return fail(FGFRFT_PARAMETER, "fgfrft_matrix: truncation exceeds the cached power set");
+    *l_used = l;
+    return FGFRFT_OK;
+}
+
+// Y[a] = op(Q(alpha_a)) X for all orders; x_dev n x b, y_dev n_alpha blocks of n x b.
+int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used, bool inverse, const void* x_dev,
+                 int64_t b, void* y_dev) {
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
+    const int n = (int)c->n;
+    const size_t sl = c->slab_elems();
+    const int chunk = alpha_chunk(c, n_alpha);
+    FGB_CUDA(c->q.ensure((size_t)chunk * sl * 16));
+    const size_t width = (size_t)(2 * l_used + 1);
+    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
+        const int na = std::min(chunk, n_alpha - a0);
+        if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p)) return st;
+        FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, inverse, x_dev, n, 0, false,
+                                static_cast<double2*>(y_dev) + (size_t)a0 * n * b, n, (int64_t)n * b, na, false,
+                                c->stream),
+                   1);
+    }
+    return FGFRFT_OK;
+}
+
+// s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
+int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
+    const int n = (int)c->n;
+    const size_t sl = c->slab_elems();
+    const int chunk = alpha_chunk(c, n_alpha);
+    FGB_CUDA(c->m.ensure((size_t)chunk * sl * 16));
+    FGB_CUDA(c->partial.ensure(dots_partial_elems(n, c->l, chunk) * sizeof(double)));
+    const size_t width = (size_t)(2 * c->l + 1);
+    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
+        const int na = std::min(chunk, n_alpha - a0);
+        // M_a = G_a X^H  (n x n, K = b)
+        FGB_LAUNCH(launch_zgemm(n, n, (int)b, static_cast<const double2*>(g_dev) + (size_t)a0 * n * b, n,
+                                (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na, false,
+                                c->stream),
+                   1);
+        FGB_LAUNCH(launch_power_dots(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
+                                     s_dev + a0 * width, c->stream),
+                   2);
+    }
+    return FGFRFT_OK;
+}
+
+}  // namespace
+
+// ===================================================================================== C ABI
+
+extern "C" {
+
+const char* fgfrft_last_error(void) { return g_err.c_str(); }
+
+const char* fgfrft_version(void) { return "0.1.0-b200"; }
+
+uint64_t fgfrft_launch_count(void) { return g_launches.load(); }
+
+int fgfrft_sinc_coeffs(double alpha, int l, double* c, double* dc) {
+    if (l < 1) return fail(FGFRFT_PARAMETER, "sinc_coeffs: truncation order must be >= 1");
+    host_sinc_coeffs(alpha, l, c, dc);
+    return FGFRFT_OK;
+}
+
+uint64_t fgfrft_fnv1a64(const void* data, size_t nbytes) { return host_fnv1a64(data, nbytes); }
+
+int fgfrft_cache_create(const double* f, int64_t n, int l, uint64_t memory_budget, int dtype, int device,
+                        fgfrft_cache** out) {
+    FGB_GUARD_BEGIN
+    fgfrft_cache* c = nullptr;
+    if (int st = create_common(f, n, l, memory_budget, dtype, device, out, &c)) return st;
+    DeviceGuard dg(device);
+    if (int st = build_powers(c, f)) {
+        destroy_cache(c);
+        return st;
+    }
+    *out = c;
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_cache_create_from_powers(const double* powers, const double* f, int64_t n, int l, uint64_t memory_budget,
+                                    int dtype, int device, fgfrft_cache** out) {
+    FGB_GUARD_BEGIN
+    if (!powers) return fail(FGFRFT_PARAMETER, "null powers");
+    fgfrft_cache* c = nullptr;
+    if (int st = create_common(f, n, l, memory_budget, dtype, device, out, &c)) return st;
+    DeviceGuard dg(device);
+    if (int st = upload_powers(c, powers)) {
+        destroy_cache(c);
+        return st;
+    }
+    *out = c;
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_cache_destroy(fgfrft_cache* cache) {
+    FGB_GUARD_BEGIN
+    destroy_cache(cache);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_cache_info(const fgfrft_cache* c, int64_t* n, int* l, uint64_t* fingerprint, int* dtype, int* device) {
+    if (int st = check_handle(c)) return st;
+    if (n) *n = c->n;
+    if (l) *l = c->l;
+    if (fingerprint) *fingerprint = c->fingerprint;
+    if (dtype) *dtype = c->dtype;
+    if (device) *device = c->device;
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_power(fgfrft_cache* c, int k, double* out) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (k < 1 || k > c->l) return fail(FGFRFT_PARAMETER, "PowerCache: power index out of range");
+    if (!out) return fail(FGFRFT_PARAMETER, "null output");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    return download_as_c128(c, c->slab(k), c->slab_elems(), out);
+    FGB_GUARD_END
+}
+
+int fgfrft_cache_verify(const fgfrft_cache* c, const double* f) {
+    if (int st = check_handle(c)) return st;
+    if (!f) return fail(FGFRFT_PARAMETER, "null matrix");
+    if (host_fnv1a64(f, c->slab_elems() * 16) != c->fingerprint)
+        return fail(FGFRFT_NUMERICAL, "PowerCache: fingerprint mismatch, cache is stale for this matrix");
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_set_stream(fgfrft_cache* c, void* stream) {
+    if (int st = check_handle(c)) return st;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_device_slab(fgfrft_cache* c, int k, void** dptr) {
+    if (int st = check_handle(c)) return st;
+    if (k < 1 || k > c->l) return fail(FGFRFT_PARAMETER, "PowerCache: power index out of range");
+    *dptr = c->slab(k);
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_device_bytes(const fgfrft_cache* c, uint64_t* bytes) {
+    if (int st = check_handle(c)) return st;
+    *bytes = (uint64_t)c->slab_bytes() * (uint64_t)c->l;
+    return FGFRFT_OK;
+}
+
+int fgfrft_synthesize_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int truncation, int which,
+                          void* out_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (which != FGFRFT_Q && which != FGFRFT_DQ) return fail(FGFRFT_PARAMETER, "which must be FGFRFT_Q or FGFRFT_DQ");
+    int l_used = 0;
+    if (int st = resolve_truncation(c, truncation, which, &l_used)) return st;
+    if (!out_dev) return fail(FGFRFT_PARAMETER, "null output");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
+    const double* table = which == FGFRFT_Q ? coef : coef + (size_t)n_alpha * (2 * l_used + 1);
+    return synth_into(c, table, n_alpha, l_used, out_dev);
+    FGB_GUARD_END
+}
+
+int fgfrft_synthesize(fgfrft_cache* c, const double* alphas, int n_alpha, int truncation, int which, double* out) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (!out) return fail(FGFRFT_PARAMETER, "null output");
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard dg(c->device);
+        FGB_CUDA(c->y.ensure((size_t)n_alpha * c->slab_bytes()));
+    }
+    if (int st = fgfrft_synthesize_dev(c, alphas, n_alpha, truncation, which, c->y.p)) return st;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    return download_as_c128(c, c->y.p, (size_t)n_alpha * c->slab_elems(), out);
+    FGB_GUARD_END
+}
+
+int fgfrft_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int truncation, int inverse,
+                     const void* x_dev, int64_t b, void* y_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = require_c128(c, "fgfrft_apply")) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
+    int l_used = 0;
+    if (int st = resolve_truncation(c, truncation, FGFRFT_Q, &l_used)) return st;
+    if (b == 0) return FGFRFT_OK;
+    if (!x_dev || !y_dev) return fail(FGFRFT_PARAMETER, "null signal buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    return apply_device(c, alphas, n_alpha, l_used, inverse != 0, x_dev, b, y_dev);
+    FGB_GUARD_END
+}
+
+int fgfrft_apply(fgfrft_cache* c, const double* alphas, int n_alpha, int truncation, int inverse, const double* x,
+                 int64_t b, double* y) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = require_c128(c, "fgfrft_apply")) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
+    int l_used = 0;
+    if (int st = resolve_truncation(c, truncation, FGFRFT_Q, &l_used)) return st;
+    if (b == 0) return FGFRFT_OK;
+    if (!x || !y) return fail(FGFRFT_PARAMETER, "null signal buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    const size_t xb = (size_t)c->n * b * 16;
+    FGB_CUDA(c->x.ensure(xb));
+    FGB_CUDA(c->y.ensure(xb * n_alpha));
+    FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xb, cudaMemcpyHostToDevice, c->stream));
+    if (int st = apply_device(c, alphas, n_alpha, l_used, inverse != 0, c->x.p, b, c->y.p)) return st;
+    FGB_CUDA(cudaMemcpyAsync(y, c->y.p, xb * n_alpha, cudaMemcpyDeviceToHost, c->stream));
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_apply_matrix(const double* q, int64_t n, int inverse, const double* x, int64_t b, double* y, int device) {
+    FGB_GUARD_BEGIN
+    if (n < 1 || b < 0) return fail(FGFRFT_SHAPE, "apply_forward: signal length does not match operator");
+    if (b == 0) return FGFRFT_OK;
+    if (!q || !x || !y) return fail(FGFRFT_PARAMETER, "null buffer");
+    DeviceGuard dg(device);
+    DevBuf dq, dx, dy;
+    const size_t qb = (size_t)n * n * 16, xb = (size_t)n * b * 16;
+    cudaStream_t st = nullptr;
+    FGB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int rc = FGFRFT_OK;
+    do {
+        if (dq.ensure(qb) || dx.ensure(xb) || dy.ensure(xb)) {
+            rc = fail(FGFRFT_CAPACITY, "device allocation failed");
+            break;
+        }
+        if (cudaMemcpyAsync(dq.p, q, qb, cudaMemcpyHostToDevice, st) ||
+            cudaMemcpyAsync(dx.p, x, xb, cudaMemcpyHostToDevice, st)) {
+            rc = fail(FGFRFT_CUDA, "upload failed");
+            break;
+        }
+        cudaError_t e = launch_zgemm((int)n, (int)b, (int)n, dq.p, n, 0, inverse != 0, dx.p, n, 0, false, dy.p, n, 0, 1,
+                                     false, st);
+        if (e != cudaSuccess) {
+            rc = fail(FGFRFT_CUDA, std::string("zgemm: ") + cudaGetErrorString(e));
+            break;
+        }
+        g_launches += 1;
+        if (cudaMemcpyAsync(y, dy.p, xb, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st)) {
+            rc = fail(FGFRFT_CUDA, "download failed");
+            break;
+        }
+    } while (false);
+    dq.release();
+    dx.release();
+    dy.release();
+    cudaStreamDestroy(st);
+    return rc;
+    FGB_GUARD_END
+}
+
+int fgfrft_dlda_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* g_dev, const void* x_dev,
+                    int64_t b, double* s, double* dlda) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = require_c128(c, "fgfrft_dlda")) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 0) return fail(FGFRFT_SHAPE, "negative signal count");
+    if (!g_dev || !x_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    const size_t width = (size_t)(2 * c->l + 1);
+    FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
+    if (b == 0) {
+        FGB_CUDA(cudaMemsetAsync(c->s.p, 0, (size_t)n_alpha * width * sizeof(double), c->stream));
+    } else if (int st = dots_device(c, n_alpha, g_dev, x_dev, b, c->s.as<double>())) {
+        return st;
+    }
+    std::vector<double> sh((size_t)n_alpha * width);
+    FGB_CUDA(cudaMemcpyAsync(sh.data(), c->s.p, sh.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<double> dc(width);
+    for (int a = 0; a < n_alpha; ++a) {
+        host_sinc_coeffs(alphas[a], c->l, nullptr, dc.data());
+        double acc = 0.0;
+        for (size_t k = 0; k < width; ++k) acc += dc[k] * sh[a * width + k];
+        if (dlda) dlda[a] = acc;
+    }
+    if (s) std::memcpy(s, sh.data(), sh.size() * sizeof(double));
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_dlda(fgfrft_cache* c, const double* alphas, int n_alpha, const double* g, const double* x, int64_t b,
+                double* s, double* dlda) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = require_c128(c, "fgfrft_dlda")) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 0) return fail(FGFRFT_SHAPE, "negative signal count");
+    if ((!g || !x) && b > 0) return fail(FGFRFT_PARAMETER, "null buffer");
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard dg(c->device);
+        const size_t xb = (size_t)c->n * (b > 0 ? b : 1) * 16;
+        FGB_CUDA(c->x.ensure(xb));
+        FGB_CUDA(c->g.ensure(xb * n_alpha));
+        if (b > 0) {
+            FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xb, cudaMemcpyHostToDevice, c->stream));
+            FGB_CUDA(cudaMemcpyAsync(c->g.p, g, xb * n_alpha, cudaMemcpyHostToDevice, c->stream));
+        }
+    }
+    return fgfrft_dlda_dev(c, alphas, n_alpha, c->g.p, c->x.p, b, s, dlda);
+    FGB_GUARD_END
+}
+
+int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_dev,
+                        int64_t b, void* y_dev, void* loss_dev, void* dlda_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = require_c128(c, "fgfrft_mse_step")) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
+    if (!x_dev || !xc_dev || !loss_dev || !dlda_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    const int n = (int)c->n;
+    const int l = c->l;
+    const size_t width = (size_t)(2 * l + 1);
+    const size_t blk = (size_t)n * b;
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
+    const double* dc_dev = coef + (size_t)n_alpha * width;
+    const int chunk = alpha_chunk(c, n_alpha);
+    const size_t sl = c->slab_elems();
+    FGB_CUDA(c->q.ensure((size_t)chunk * sl * 16));
+    FGB_CUDA(c->g.ensure((size_t)chunk * blk * 16));
+    FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
+    FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
+    if (!y_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * 16));
+    const double norm = 1.0 / ((double)n * (double)b);
+    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
+        const int na = std::min(chunk, n_alpha - a0);
+        double2* ya = y_dev ? static_cast<double2*>(y_dev) + (size_t)a0 * blk : c->y.as<double2>();
+        if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p)) return st;
+        FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n, (int64_t)blk,
+                                na, false, c->stream),
+                   1);
+        FGB_LAUNCH(launch_mse_residual(ya, xc_dev, (int64_t)blk, na, 2.0 * norm, norm, c->g.p, c->lpart.as<double>(),
+                                       static_cast<double*>(loss_dev) + a0, c->stream),
+                   2);
+        if (int st = dots_device(c, na, c->g.p, x_dev, b, c->s.as<double>() + a0 * width)) return st;
+    }
+    FGB_LAUNCH(launch_coef_dot(dc_dev, c->s.as<double>(), n_alpha, (int)width, static_cast<double*>(dlda_dev),
+                               c->stream),
+               1);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const double* x, const double* xc, int64_t b,
+                    double* y, double* loss, double* dlda) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (int st = require_c128(c, "fgfrft_mse_step")) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
+    if (!x || !xc || !loss || !dlda) return fail(FGFRFT_PARAMETER, "null buffer");
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard dg(c->device);
+        const size_t xb = (size_t)c->n * b * 16;
+        FGB_CUDA(c->x.ensure(xb));
+        FGB_CUDA(c->xc.ensure(xb));
+        FGB_CUDA(c->loss.ensure((size_t)n_alpha * 2 * sizeof(double)));
+        if (y) FGB_CUDA(c->y.ensure(xb * n_alpha));
+        FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xb, cudaMemcpyHostToDevice, c->stream));
+        FGB_CUDA(cudaMemcpyAsync(c->xc.p, xc, xb, cudaMemcpyHostToDevice, c->stream));
+    }
+    double* ld = c->loss.as<double>();
+    if (int st = fgfrft_mse_step_dev(c, alphas, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha))
+        return st;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    std::vector<double> out(2 * (size_t)n_alpha);
+    FGB_CUDA(cudaMemcpyAsync(out.data(), ld, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (y) FGB_CUDA(cudaMemcpyAsync(y, c->y.p, (size_t)c->n * b * 16 * n_alpha, cudaMemcpyDeviceToHost, c->stream));
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    std::memcpy(loss, out.data(), n_alpha * sizeof(double));
+    std::memcpy(dlda, out.data() + n_alpha, n_alpha * sizeof(double));
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+"""GPU parity: every hot-path entry point of libfgfrft_b200.so against the CPU oracle on the
+same inputs, plus the reference's known-answer tests re-run through the C ABI.
+
+Tolerances (BASELINE north star): complex128 within 1e-10 relative Frobenius; the series
+synthesis is evaluated in the reference's operation order without FMA contraction, so it is
+asserted BIT-EXACT against the oracle. dL/dalpha: |g - g_ref| <= 1e-10 * sum_k |c'_k s_k|.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2602_20870_b200 as fg
+import prep
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _cache_pair(f, l, **kw):
+    return fg.PowerCache(f, l, **kw), O.PowerCache(f, l, kw.get("memory_budget", O.DEFAULT_MEMORY_BUDGET))
+
+
+# --------------------------------------------------------------------------- power cache (K1)
+
+@pytest.mark.parametrize("n,l", [(1, 3), (2, 4), (24, 10), (48, 10), (100, 7), (256, 8)])
+def test_cache_build_matches_oracle(n, l):
+    f = prep.random_unitary(n, 77 + n)
+    g, o = _cache_pair(f, l)
+    assert g.fingerprint() == o.fingerprint == fg.content_fingerprint(f)
+    assert np.array_equal(g.power(1), f)                   # P_1 = F copied bit-exactly
+    for k in range(2, l + 1):
+        assert rel(g.power(k), o.power(k)) <= 1e-12
+        step = f @ g.power(k - 1)
+        assert np.linalg.norm(g.power(k) - step) <= 1e-9 * np.linalg.norm(step)   # test_transform.cpp:33-42
+    assert prep.unitarity_residual(g.power(l)) <= 1e-8
+
+
+def test_cache_identity_and_rotation():  # test_transform.cpp:20-31
+    c = fg.PowerCache(np.eye(8, dtype=complex), 3)
+    for k in (1, 2, 3):
+        assert np.abs(c.power(k) - np.eye(8)).max() == 0.0
+    r = fg.PowerCache(O.rotation2(math.pi / 4), 4)
+    assert np.abs(r.power(4) + np.eye(2)).max() < 1e-14
+
+
+def test_cache_fingerprint_and_errors():  # test_transform.cpp:44-58
+    f, other = prep.random_unitary(16, 5), prep.random_unitary(16, 6)
+    c = fg.PowerCache(f, 4)
+    c.verify(f)
+    with pytest.raises(fg.NumericalError):
+        c.verify(other)
+    for k in (0, 5):
+        with pytest.raises(fg.ParameterError):
+            c.power(k)
+    with pytest.raises(fg.CapacityError):
+        fg.PowerCache(prep.random_unitary(64, 1), 10, 1024)
+    fg.PowerCache(prep.random_unitary(64, 1), 2, 8 << 20)
+
+
+# --------------------------------------------------------------------------- synthesis (K2)
+
+@pytest.mark.parametrize("n,l", [(1, 2), (2, 10), (24, 10), (40, 10), (33, 5), (64, 24), (97, 12), (256, 32)])
+def test_synthesis_bit_exact(n, l):
+    f = prep.random_unitary(n, 1000 + n)
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l, powers=o.slabs)  # identical cache bytes -> bit-exact comparison
+    alphas = [0.37, -0.7, 1.5, 0.0, 2.0, 3.3, 1.0000004]
+    qs = fg.synthesize(g, alphas)
+    for a, q in zip(alphas, qs):
+        assert np.array_equal(q, O.fgfrft_matrix(o, a)), a
+    dqs = fg.synthesize(g, alphas, which=fg.DQ)
+    for a, dq in zip(alphas, dqs):
+        assert np.array_equal(dq, O.fgfrft_grad(o, a)), a
+
+
+def test_synthesis_truncation_and_sweep_chunks():
+    f = prep.random_unitary(70, 3)
+    o = O.PowerCache(f, 16)
+    g = fg.PowerCache(f, 16, powers=o.slabs)
+    alphas = list(np.linspace(0, 2, 11))
+    for t in (1, 5, 16):
+        for a, q in zip(alphas, fg.synthesize(g, alphas, truncation=t)):
+            assert np.array_equal(q, O.fgfrft_matrix(o, a, t))
+    with pytest.raises(fg.ParameterError):
+        fg.synthesize(g, [0.5], truncation=17)
+
+
+def test_kats_through_the_c_abi():
+    # order 0 -> identity exactly (test_transform.cpp:60-65)
+    c = fg.PowerCache(prep.random_unitary(32, 9), 6)
+    assert np.linalg.norm(fg.fgfrft_matrix(c, 0.0).q - np.eye(32)) == 0.0
+    # integer orders (test_transform.cpp:67-75)
+    f = prep.random_unitary(24, 31)
+    c = fg.PowerCache(f, 10)
+    for m in range(-3, 4):
+        e = O.matrix_power(f, m)
+        assert np.linalg.norm(fg.fgfrft_matrix(c, float(m)).q - e) <= 1e-10 * np.linalg.norm(e)
+    # conjugate symmetry, bit-exact here (test_transform.cpp:77-85 bounds it by 1e-14)
+    c = fg.PowerCache(prep.random_unitary(40, 13), 10)
+    for a in (0.3, 0.7, 1.5, 2.2):
+        assert np.array_equal(fg.fgfrft_matrix(c, -a).q, fg.fgfrft_matrix(c, a).q.conj().T)
+    # spectral-error identity (test_transform.cpp:98-112)
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(64, 0.05 * math.pi, 23), 40)
+    eig = O.eigendecompose_unitary(f)
+    c = fg.PowerCache(f, 24)
+    for a, l in ((0.5, 10), (0.3, 16), (0.85, 12), (1.4, 20), (0.15, 24)):
+        lhs = O.spectral_norm(fg.fgfrft_matrix(c, a, l).q - O.exact_gfrft(eig, a))
+        assert lhs == pytest.approx(O.truncation_bound(th, a, l), abs=1e-8)
+    # gradient vs finite differences (test_transform.cpp:151-160)
+    f, _, _ = prep.synthetic_unitary(prep.spread_phases(32, 0.1 * math.pi, 3), 15)
+    c = fg.PowerCache(f, 10)
+    for a in (0.15, 0.55, 1.0, 1.5):
+        fd = (fg.fgfrft_matrix(c, a + 1e-4).q - fg.fgfrft_matrix(c, a - 1e-4).q) / 2e-4
+        assert rel(fg.fgfrft_grad(c, a), fd) <= 1e-6
+    # identity spectrum gradient (test_transform.cpp:162-174)
+    c = fg.PowerCache(np.eye(6, dtype=complex), 8)
+    assert np.abs(fg.fgfrft_grad(c, 0.0)).max() == 0.0
+
+
+def test_window_warning():
+    c = fg.PowerCache(prep.random_unitary(8, 3), 4)
+    with pytest.warns(UserWarning, match="window"):
+        fg.fgfrft_matrix(c, 9.0)
+    assert fg.fgfrft_matrix(c, 0.5, 2).l == 2
+
+
+# --------------------------------------------------------------------------- apply (K3)
+
+@pytest.mark.parametrize("n,b", [(1, 1), (8, 3), (40, 1), (130, 70), (256, 1), (300, 257)])
+def test_apply_matrix_matches_oracle(n, b):
+    rng = np.random.default_rng(n)
+    q = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    op = fg.FracOperator(np.asfortranarray(q), 0.3, 4)
+    assert rel(fg.apply_forward(op, x), O.apply_forward(q, x)) <= 1e-13
+    assert rel(fg.apply_inverse(op, x), O.apply_inverse(q, x)) <= 1e-13
+    with pytest.raises(fg.ShapeError):
+        fg.apply_forward(op, np.zeros((n + 1, 1)))
+
+
+def test_apply_series_matches_oracle():
+    f = prep.random_unitary(150, 8)
+    o = O.PowerCache(f, 12)
+    g = fg.PowerCache(f, 12)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((150, 33)) + 1j * rng.standard_normal((150, 33))
+    alphas = [0.0, 0.37, 1.0, 1.9]
+    ys = fg.apply_series(g, alphas, x)
+    yi = fg.apply_series(g, alphas, x, inverse=True)
+    for a, y, z in zip(alphas, ys, yi):
+        q = O.fgfrft_matrix(o, a)
+        assert rel(y, q @ x) <= 1e-12
+        assert rel(z, q.conj().T @ x) <= 1e-12
+    assert np.array_equal(ys[0], x.astype(complex)) or rel(ys[0], x) <= 1e-15   # order 0 is the identity
+
+
+def test_forward_inverse_roundtrip():  # test_transform.cpp:176-203
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(64, 0.05 * math.pi, 23), 40)
+    c = fg.PowerCache(f, 12)
+    rng = prep.Rng(55)
+    x = np.array([complex(rng.gaussian(), rng.gaussian()) for _ in range(64)]).reshape(64, 1)
+    q0 = fg.fgfrft_matrix(c, 0.0)
+    assert np.linalg.norm(fg.apply_forward(q0, x) - x) == 0.0
+    q1 = fg.fgfrft_matrix(c, 1.0)
+    assert np.linalg.norm(fg.apply_inverse(q1, fg.apply_forward(q1, x)) - x) <= 1e-10 * np.linalg.norm(x)
+
+
+# --------------------------------------------------------------------------- dL/dalpha (K4)
+
+def test_dlda_matches_oracle():
+    f = prep.random_unitary(90, 21)
+    o = O.PowerCache(f, 9)
+    g = fg.PowerCache(f, 9)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((90, 17)) + 1j * rng.standard_normal((90, 17))
+    alphas = [0.37, 1.2, -0.4, 0.0, 2.0]
+    gs = [rng.standard_normal((90, 17)) + 1j * rng.standard_normal((90, 17)) for _ in alphas]
+    dl, s = fg.dlda(g, alphas, gs, x)
+    for i, a in enumerate(alphas):
+        s_ref = O.power_dots(o, gs[i] @ x.conj().T)
+        assert np.abs(s[i] - s_ref).max() <= 1e-10 * np.abs(s_ref).sum()
+        _, dc = O.sinc_coeffs(a, 9)
+        ref = float(np.sum(np.conj(gs[i]) * (O.fgfrft_grad(o, a) @ x)).real)
+        assert abs(dl[i] - ref) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+def test_mse_step_config1():
+    cfg = prep.config1()
+    o = O.PowerCache(cfg.f, cfg.l)
+    g = fg.PowerCache(cfg.f, cfg.l)
+    rng = np.random.default_rng(5)
+    clean = cfg.x + 0.1 * rng.standard_normal(cfg.x.shape)
+    loss, dl, y = fg.mse_step(g, cfg.alphas, cfg.x, clean, want_y=True)
+    lr, dr, yr = O.dlda_mse(o, cfg.alphas[0], cfg.x, clean)
+    assert rel(y[0], yr) <= 1e-10
+    assert loss[0] == pytest.approx(lr, rel=1e-10)
+    _, dc = O.sinc_coeffs(cfg.alphas[0], cfg.l)
+    s_ref = O.power_dots(o, (2 * (yr - clean) / yr.size) @ cfg.x.conj().T)
+    assert abs(dl[0] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))

@@ -1,0 +1,260 @@
+"""The CPU oracle (oracle/) against the reference's own known-answer tests and golden vectors.
+
+KATs re-expressed from proj/tests/test_sinc.cpp, test_transform.cpp and acceptance.cpp
+(criteria 1-5); golden vectors in tests/golden/ come from the reference's sinc.hpp / rng.hpp
+compiled where they lie (oracle/_ref, tests/golden/make_golden.py).
+"""
+import json
+import math
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+import oracle as O
+import prep
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _hex(v):
+    return float.fromhex(v)
+
+
+# ----------------------------------------------------------------------- sinc (test_sinc.cpp)
+
+def test_sinc_golden_bit_exact():
+    data = json.load(open(os.path.join(GOLDEN, "sinc_coeffs.json")))
+    for case in data["cases"]:
+        c, dc = O.sinc_coeffs(_hex(case["alpha"]), case["l"])
+        assert [float(v).hex() for v in c] == case["c"]
+        assert [float(v).hex() for v in dc] == case["dc"]
+
+
+def test_integer_orders_are_kronecker():  # test_sinc.cpp:9-22
+    c0, _ = O.sinc_coeffs(0.0, 2)
+    assert list(c0) == [0.0, 0.0, 1.0, 0.0, 0.0]
+    c1, _ = O.sinc_coeffs(1.0, 2)
+    assert list(c1) == [0.0, 0.0, 0.0, 1.0, 0.0]
+    cm3, _ = O.sinc_coeffs(-3.0, 5)
+    assert all(v == (1.0 if n == -3 else 0.0) for n, v in zip(range(-5, 6), cm3))
+
+
+def test_half_order_closed_forms():  # test_sinc.cpp:24-30
+    c, _ = O.sinc_coeffs(0.5, 2)
+    assert c[2] == pytest.approx(2 / math.pi, rel=1e-13)
+    assert c[3] == pytest.approx(2 / math.pi, rel=1e-13)
+    assert c[1] == pytest.approx(-2 / (3 * math.pi), rel=1e-13)
+    assert c[4] == pytest.approx(-2 / (3 * math.pi), rel=1e-13)
+
+
+def test_parity_bit_exact():  # test_sinc.cpp:40-46
+    for a in (0.3, 0.55, 1.0, 1.0000004, 2.5, 1e-8, 7.3):
+        p, _ = O.sinc_coeffs(a, 6)
+        m, _ = O.sinc_coeffs(-a, 6)
+        assert list(m) == list(p[::-1])
+
+
+def test_derivative_finite_differences():  # test_sinc.cpp:48-54
+    for x in (0.37, -1.22, 2.9, 1.0 + 3e-5, -2.0 - 3e-5, 5e-7, 2e-6):
+        fd = (O.sinc(x + 1e-4) - O.sinc(x - 1e-4)) / 2e-4
+        assert abs(O.sinc_deriv(x) - fd) <= 2e-7
+
+
+def test_derivative_integer_closed_form():  # test_sinc.cpp:56-61
+    assert O.sinc_deriv(0.0) == 0.0
+    assert O.sinc_deriv(1.0) == pytest.approx(-1.0, rel=1e-13)
+    assert O.sinc_deriv(2.0) == pytest.approx(0.5, rel=1e-13)
+    assert O.sinc_deriv(-3.0) == pytest.approx(1 / 3, rel=1e-13)
+
+
+def test_series_seam_continuity():  # test_sinc.cpp:63-69
+    eps = 1e-9
+    assert abs(O.sinc(1e-6 - eps) - O.sinc(1e-6 + eps)) <= 1e-12
+    assert abs(O.sinc_deriv(1e-6 - eps) - O.sinc_deriv(1e-6 + eps)) <= 2e-8
+
+
+def test_truncation_must_be_positive():  # test_sinc.cpp:71-73
+    with pytest.raises(O.ParameterError):
+        O.sinc_coeffs(0.5, 0)
+
+
+def test_fnv_golden():
+    data = json.load(open(os.path.join(GOLDEN, "fnv1a64.json")))
+    lib = O.lib()
+    for case in data["cases"]:
+        n = case["n"]
+        buf = (np.arange(n, dtype=np.uint64) * 2654435761 % 251).astype(np.uint8)
+        assert int(lib.oracle_fnv1a64(buf.ctypes.data, n, 0xCBF29CE484222325)) == int(case["value"])
+
+
+# ----------------------------------------------------------------------- transform (test_transform.cpp)
+
+def test_identity_and_quarter_rotation_cache():  # :20-31
+    cache = O.PowerCache(np.eye(8, dtype=complex), 3)
+    for k in (1, 2, 3):
+        assert np.abs(cache.power(k) - np.eye(8)).max() == 0.0
+    r = O.PowerCache(O.rotation2(math.pi / 4), 4)
+    assert np.abs(r.power(4) + np.eye(2)).max() < 1e-14
+
+
+def test_recursion_and_unitarity():  # :33-42
+    f = prep.random_unitary(48, 77)
+    cache = O.PowerCache(f, 10)
+    assert np.array_equal(cache.power(1), f)
+    for k in range(2, 11):
+        step = f @ cache.power(k - 1)
+        assert np.linalg.norm(cache.power(k) - step) <= 1e-9 * np.linalg.norm(step)
+    assert prep.unitarity_residual(cache.power(10)) <= 1e-8
+
+
+def test_fingerprint_and_index_errors():  # :44-52
+    f, other = prep.random_unitary(16, 5), prep.random_unitary(16, 6)
+    cache = O.PowerCache(f, 4)
+    cache.verify(f)
+    with pytest.raises(O.NumericalError):
+        cache.verify(other)
+    for k in (0, 5):
+        with pytest.raises(O.ParameterError):
+            cache.power(k)
+
+
+def test_memory_budget():  # :54-58
+    f = prep.random_unitary(64, 1)
+    with pytest.raises(O.CapacityError):
+        O.PowerCache(f, 10, 1024)
+    O.PowerCache(f, 2, 8 << 20)
+
+
+def test_order_zero_identity_exact():  # :60-65
+    cache = O.PowerCache(prep.random_unitary(32, 9), 6)
+    assert np.linalg.norm(O.fgfrft_matrix(cache, 0.0) - np.eye(32)) == 0.0
+
+
+def test_integer_orders_exact():  # :67-75
+    f = prep.random_unitary(24, 31)
+    cache = O.PowerCache(f, 10)
+    for m in range(-3, 4):
+        e = O.matrix_power(f, m)
+        assert np.linalg.norm(O.fgfrft_matrix(cache, float(m)) - e) <= 1e-10 * np.linalg.norm(e)
+
+
+def test_conjugate_symmetry():  # :77-85
+    cache = O.PowerCache(prep.random_unitary(40, 13), 10)
+    for a in (0.3, 0.7, 1.5, 2.2):
+        assert np.abs(O.fgfrft_matrix(cache, -a) - O.fgfrft_matrix(cache, a).conj().T).max() <= 1e-14
+
+
+def test_quarter_rotation_scalar_error():  # :87-96
+    cache = O.PowerCache(O.rotation2(math.pi / 2), 10)
+    q = O.fgfrft_matrix(cache, 0.5)
+    exact = O.rotation2(math.pi / 4)
+    err = O.scalar_series(math.pi / 2, 0.5, 10)
+    scalar_err = abs(complex(math.cos(math.pi / 4), math.sin(math.pi / 4)) - err)
+    assert O.spectral_norm(q - exact) == pytest.approx(scalar_err, abs=1e-12)
+
+
+def test_spectral_error_identity():  # :98-112 and acceptance criterion 5
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(64, 0.05 * math.pi, 23), 40)
+    eig = O.eigendecompose_unitary(f)
+    cache = O.PowerCache(f, 24)
+    for a, l in ((0.5, 10), (0.3, 16), (0.85, 12), (1.4, 20), (0.15, 24)):
+        lhs = O.spectral_norm(O.fgfrft_matrix(cache, a, l) - O.exact_gfrft(eig, a))
+        assert lhs == pytest.approx(O.truncation_bound(th, a, l), abs=1e-8)
+
+
+def test_nmse_monotone_in_l():  # :114-127
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(64, 0.1 * math.pi, 12), 81)
+    eig = O.eigendecompose_unitary(f)
+    cache = O.PowerCache(f, 100)
+    exact = O.exact_gfrft(eig, 0.5)
+    prev = math.inf
+    for l in range(10, 101, 10):
+        d = O.fgfrft_matrix(cache, 0.5, l) - exact
+        nmse = np.vdot(d, d).real / np.vdot(exact, exact).real
+        assert nmse <= prev + 1e-12
+        prev = nmse
+
+
+def test_grad_matches_finite_differences():  # :151-160
+    f, _, _ = prep.synthetic_unitary(prep.spread_phases(32, 0.1 * math.pi, 3), 15)
+    cache = O.PowerCache(f, 10)
+    for a in (0.15, 0.35, 0.55, 0.75, 0.95, 1.0, 1.5):
+        fd = (O.fgfrft_matrix(cache, a + 1e-4) - O.fgfrft_matrix(cache, a - 1e-4)) / 2e-4
+        an = O.fgfrft_grad(cache, a)
+        assert np.linalg.norm(an - fd) / np.linalg.norm(fd) <= 1e-6
+
+
+def test_identity_gradient_is_coefficient_sum():  # :162-174
+    cache = O.PowerCache(np.eye(6, dtype=complex), 8)
+    assert np.abs(O.fgfrft_grad(cache, 0.0)).max() == 0.0
+    _, dc = O.sinc_coeffs(0.4, 8)
+    g = O.fgfrft_grad(cache, 0.4)
+    assert abs(g[2, 2].real - dc.sum()) < 1e-14
+    assert abs(g[0, 1]) < 1e-14
+
+
+def test_window_warning_and_truncation():  # :205-221
+    cache = O.PowerCache(prep.random_unitary(8, 3), 4)
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        O.fgfrft_matrix(cache, 9.0)
+    assert any("window" in str(x.message) for x in w)
+    with pytest.raises(O.ParameterError):
+        O.fgfrft_matrix(cache, 0.5, 5)
+
+
+def test_power_dots_definition():
+    """s_k = Re<G, F^k X> (learn.hpp:88-92 contraction) via M = G X^H."""
+    f = prep.random_unitary(20, 4)
+    cache = O.PowerCache(f, 5)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((20, 3)) + 1j * rng.standard_normal((20, 3))
+    g = rng.standard_normal((20, 3)) + 1j * rng.standard_normal((20, 3))
+    s = O.power_dots(cache, g @ x.conj().T)
+    for k in range(-5, 6):
+        ref = np.sum(np.conj(g) * (O.matrix_power(f, k) @ x)).real
+        assert s[k + 5] == pytest.approx(ref, rel=1e-12, abs=1e-12)
+    loss, dl, _ = O.dlda_mse(cache, 0.37, x, g)
+    h = 1e-5
+    lp, _, _ = O.dlda_mse(cache, 0.37 + h, x, g)
+    lm, _, _ = O.dlda_mse(cache, 0.37 - h, x, g)
+    assert dl == pytest.approx((lp - lm) / (2 * h), rel=1e-6)
+
+
+# ----------------------------------------------------------------------- acceptance.cpp
+
+def test_acceptance_1_integer_order():  # :54-66
+    f = prep.random_unitary(256, 7)
+    cache = O.PowerCache(f, 10)
+    assert np.linalg.norm(O.fgfrft_matrix(cache, 1.0) - f) <= 1e-10 * np.linalg.norm(f)
+    assert np.linalg.norm(O.fgfrft_matrix(cache, 0.0) - np.eye(256)) <= 1e-12 * math.sqrt(256)
+
+
+def test_acceptance_3_table_magnitudes():  # :81-101 (N=1000 Haar, L=10)
+    f = prep.random_unitary(1000, 42)
+    eig = O.eigendecompose_unitary(f)
+    cache = O.PowerCache(f, 10)
+    alphas = (0.15, 0.35, 0.55, 0.75, 0.95)
+    errs = [O.matrix_errors(O.fgfrft_matrix(cache, a, nthreads=8), O.exact_gfrft(eig, a)) for a in alphas]
+    nmse = sum(e["nmse"] for e in errs) / len(errs)
+    mae = sum(e["mae"] for e in errs) / len(errs)
+    assert 2.05e-2 / 3 <= nmse <= 2.05e-2 * 3
+    assert 4.00e-3 / 3 <= mae <= 4.00e-3 * 3
+
+
+def test_acceptance_4_monotone_convergence():  # :103-117
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(512, 0.1 * math.pi, 23), 63)
+    eig = (v, th)  # known spectrum short-circuit (spectral.hpp:122)
+    order = np.argsort(th)
+    eig = (v[:, order], th[order])
+    cache = O.PowerCache(f, 30)
+    exact = O.exact_gfrft(eig, 0.5)
+    prev = -1.0
+    for l in (10, 20, 30):
+        d = O.fgfrft_matrix(cache, 0.5, l, nthreads=8) - exact
+        nmse = np.vdot(d, d).real / np.vdot(exact, exact).real
+        if prev >= 0:
+            assert nmse <= 0.9 * prev
+        prev = nmse
