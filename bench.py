@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""FGFRFT hot-path benchmark (BASELINE.json metric) on B200.
+
+Workload (BASELINE config 2, configs[1]): N=1024 Gaussian-weighted k-NN sensor graph, L=64
+(cache = 64 complex128 powers, 1.07 GB > L2), B=256 noisy bandlimited signals, 64 orders
+swept over [0, 2]. One STEP = for every order: Y = F^alpha X (series synthesis + DMMA GEMM),
+MSE loss against the clean signals, and dL/dalpha (M = G X^H on DMMA + per-power reductions).
+`value` is whole-job signal-nodes/s = N * B * A * ranks / step time, inputs resident in HBM;
+`e2e` is the same step through the C ABI with pinned host buffers (H2D of X, Xc and D2H of the
+per-order losses and gradients inside the timed region).
+
+Extra objects: `roofline` for the dominant kernel (the DMMA complex GEMM; FP64 tensor bound),
+`synthesis` (F^alpha synthesis GB/s vs HBM peak, the metric's first half, 64-order sweep and
+single order), `cache_build` (K1 TFLOP/s), `cpu_baseline` (the oracle on this host, bounded
+sample), `clocks` (nvidia-smi during the timed region), `gpu_launches`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun (N > 1) every rank runs an independent replica of the workload (different
+signal seed; the path shards by independent problems, no data-path collective): weak scaling.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "F^α synthesis GB/s vs HBM peak; F^α·X signal-nodes/s (complex128)"
+UNIT = "signal-nodes/s"
+
+
+def _peaks():
+    hbm, src = None, None
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm, src = float(mp["hbm_gbs"]), "MEASURED_PEAKS.json:hbm_gbs (measured copy)"
+    except Exception:
+        hbm, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
+    return {"hbm_gbs": hbm, "hbm_src": src, "fp64_tflops": float(fp64["dmma_m8n8k4_tflops"]),
+            "fp64_src": "profiles/r01_fp64_peaks.json:dmma_m8n8k4_tflops (measured DMMA microbenchmark; "
+                        "MEASURED_PEAKS.json has no FP64 figure)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _config(rank: int):
+    import prep
+    cfg = prep.config2(seed=1)  # graph / F identical on every rank
+    if rank:
+        # independent replica: same graph, signals from a rank-derived stream
+        rng = prep.Rng(prep.Rng.derive(1, 100 + rank))
+        n, b = cfg.x.shape
+        coef = np.zeros((n, b))
+        coef[:50, :] = rng.gaussians(50 * b).reshape(b, 50).T
+        clean = cfg.f.conj().T @ coef.astype(np.complex128)
+        cfg.x = np.asfortranarray(clean + 0.1 * rng.gaussians(n * b).reshape(b, n).T)
+        cfg.x_clean = np.asfortranarray(clean)
+    return cfg
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's CPU path (oracle port; the reference itself cannot be
+    built here -- Eigen3 absent) on all host threads, each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    cfg = _config(0)
+    cores = os.cpu_count() or 1
+    n, b = cfg.x.shape
+    sample = [float(a) for a in cfg.alphas[:: max(1, len(cfg.alphas) // 2)][:2]]
+    with threadpool_limits(cores):
+        cache = O.PowerCache(cfg.f, cfg.l)
+
+        def step():
+            for a in sample:
+                q = O.fgfrft_matrix(cache, a, nthreads=cores)
+                y = q @ cfg.x
+                r = y - cfg.x_clean
+                g = 2.0 * r / (n * b)
+                dq = O.fgfrft_grad(cache, a, nthreads=cores)
+                _ = float(np.sum(np.conj(g) * (dq @ cfg.x)).real)
+
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dt = (time.perf_counter() - t0) / args.steps
+    value = n * b * len(sample) / dt
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+           "config": {"workload": "BASELINE config 2: N=1024 Gaussian k-NN sensor graph, L=64, B=256, "
+                                  "orders linspace(0,2,64); sample of %d orders per step" % len(sample)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": f"{len(sample)} of 64 orders per step (alphas {sample}): fgfrft_matrix + "
+                                      "apply (OpenBLAS zgemm) + fgfrft_grad + <G, dQ X>, oracle restatement of "
+                                      "transform.hpp; reference C++ unbuildable (no Eigen3)"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    """Oracle port on this host, bounded sample (rank 0, N=1 only)."""
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    cores = os.cpu_count() or 1
+    n, b = cfg.x.shape
+    with threadpool_limits(cores):
+        cache = O.PowerCache(cfg.f, cfg.l)
+        done, t0 = 0, time.perf_counter()
+        for a in cfg.alphas:
+            q = O.fgfrft_matrix(cache, float(a), nthreads=cores)
+            y = q @ cfg.x
+            g = 2.0 * (y - cfg.x_clean) / (n * b)
+            dq = O.fgfrft_grad(cache, float(a), nthreads=cores)
+            _ = float(np.sum(np.conj(g) * (dq @ cfg.x)).real)
+            done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+    return {"value": n * b * done / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {done} of 64 orders of the config-2 sweep (~{dt:.1f} s): oracle fgfrft_matrix + "
+                      "OpenBLAS apply + fgfrft_grad + <G, dQ X>; reference C++ unbuildable here (Eigen3 absent)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = _dist()
+
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import torch
+    import paper_2602_20870_b200 as fg
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = _peaks()
+    cfg = _config(rank)
+    n, b = cfg.x.shape
+    A, L = len(cfg.alphas), cfg.l
+    alphas = np.ascontiguousarray(cfg.alphas, dtype=np.float64)
+    stream = torch.cuda.Stream()
+
+    # ---- K1: power cache built on device (DMMA GEMM chain), timed with events on the default stream
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cache = fg.PowerCache(cfg.f, L, memory_budget=8 << 30, device=local)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    build_flops = (L - 1) * 8.0 * n ** 3
+    cache.set_stream(stream.cuda_stream)
+
+    xd = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).to(f"cuda:{local}")      # column-major n x b
+    xcd = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).to(f"cuda:{local}")
+    loss_d = torch.empty(A, dtype=torch.float64, device=f"cuda:{local}")
+    dlda_d = torch.empty(A, dtype=torch.float64, device=f"cuda:{local}")
+    L_ = fg.lib()
+
+    def step_dev():
+        fg._check(L_.fgfrft_mse_step_dev(cache.handle, alphas.ctypes.data, A, xd.data_ptr(), xcd.data_ptr(), b,
+                                         None, loss_d.data_ptr(), dlda_d.data_ptr()))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: device-resident step, CUDA events on the library stream
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step_dev()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    fg.profile_enable(True)
+    fg.profile_read(reset=True)
+    launches0 = fg.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step_dev()
+    ev1.record(stream)
+    ev1.synchronize()
+    launches = fg.launch_count() - launches0
+    prof = fg.profile_read(reset=True)
+    fg.profile_enable(False)
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = n * b * A * ws / (ms * 1e-3)
+
+    # loss / gradient sanity against the oracle on one order (rank 0, cheap)
+    check = None
+    if rank == 0:
+        import oracle as O
+        ocache = O.PowerCache(cfg.f, L)
+        i = 23
+        lr, dr, _ = O.dlda_mse(ocache, float(alphas[i]), cfg.x, cfg.x_clean)
+        check = {"alpha": float(alphas[i]), "loss_rel_err": abs(float(loss_d[i]) - lr) / abs(lr),
+                 "dlda_abs_err": abs(float(dlda_d[i]) - dr), "dlda_ref": dr}
+        del ocache
+
+    # ---- dominant kernel roofline: the DMMA complex GEMM (Q X and G X^H per order)
+    gemm_ms, gemm_n = prof["dmma_zgemm"]
+    gemm_flops_step = 2 * A * 8.0 * n * n * b
+    gemm_tflops = gemm_flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+    tot_prof = sum(v[0] for v in prof.values())
+    shares = {k: (v[0] / tot_prof if tot_prof else None) for k, v in prof.items()}
+
+    # ---- synthesis GB/s (metric's first half): 64-order sweep and a single order, device output
+    qbuf = torch.empty((A, n, n), dtype=torch.complex128, device=f"cuda:{local}")
+
+    def synth(al):
+        fg._check(L_.fgfrft_synthesize_dev(cache.handle, al.ctypes.data, len(al), 0, 0, qbuf.data_ptr()))
+
+    syn = {}
+    for tag, al in (("sweep64", alphas), ("single", alphas[23:24].copy())):
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                synth(al)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record(stream)
+        for _ in range(reps):
+            synth(al)
+        e1.record(stream)
+        e1.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        nbytes = (L + len(al)) * n * n * 16.0
+        syn[tag] = {"orders": len(al), "ms": t, "gbs": nbytes / (t * 1e-3) / 1e9,
+                    "frac_hbm": nbytes / (t * 1e-3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": nbytes,
+                    "flops": 8.0 * L * n * n * len(al)}
+    del qbuf
+
+    # ---- e2e: through the C ABI with pinned host buffers (H2D X, Xc + D2H loss, dL/dalpha)
+    xh = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).pin_memory()
+    xch = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).pin_memory()
+    lh = torch.empty(A, dtype=torch.float64).pin_memory()
+    dh = torch.empty(A, dtype=torch.float64).pin_memory()
+
+    def step_e2e():
+        fg._check(L_.fgfrft_mse_step(cache.handle, alphas.ctypes.data, A, xh.data_ptr(), xch.data_ptr(), b, None,
+                                     lh.data_ptr(), dh.data_ptr()))
+
+    for _ in range(args.warmup):
+        step_e2e()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e()
+    e1.record(stream)
+    e1.synchronize()
+    t_wall = (time.perf_counter() - t_wall) / args.steps
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, t_wall * 1e3))
+    e2e_value = n * b * A * ws / (e2e_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": "BASELINE config 2 (configs[1]): N=1024 Gaussian k-NN sensor graph, L=64, "
+                                   "B=256 noisy bandlimited signals, 64 orders linspace(0,2); step = forward "
+                                   "F^a X + MSE loss + dL/da for every order",
+                       "n": n, "l": L, "b": b, "orders": A, "cache_bytes": L * n * n * 16,
+                       "l2": "inputs larger than L2 (1.07 GB cache streamed every step)",
+                       "parallelism": f"replicas x{ws} (independent problems per rank)"},
+            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma_kernel (FP64 DMMA complex GEMM)",
+                         "achieved": gemm_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                         "frac": (gemm_tflops / peaks["fp64_tflops"]) if gemm_tflops else None,
+                         "traffic": None, "peak_source": peaks["fp64_src"],
+                         "algorithmic": "8*N^2*B flops per order per GEMM, 2 GEMMs per order",
+                         "launches_timed": gemm_n, "share_of_step": shares},
+            "synthesis": {"unit": "GB/s", "peak_hbm_gbs": peaks["hbm_gbs"], "peak_source": peaks["hbm_src"],
+                          "layout": "S = L stored slabs (F^-k read as conjugate-transposed tile pairs)", **syn},
+            "cache_build": {"seconds": build_s, "tflops": build_flops / build_s / 1e12,
+                            "frac_fp64": build_flops / build_s / 1e12 / peaks["fp64_tflops"],
+                            "note": "host wall clock incl. H2D of F and allocation"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 2 * n * b * 16, "d2h_bytes_per_step": 2 * A * 8},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "parity_check": check,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -67,6 +67,15 @@ const char* fgfrft_version(void);
 /* Number of kernel launches this process has issued through the library (monotone). */
 uint64_t fgfrft_launch_count(void);
 
+/*
+ * Per-kernel-class device timing (CUDA events on the launching stream), for benchmarks:
+ * classes 0 synthesis, 1 DMMA GEMM, 2 power dots, 3 elementwise. fgfrft_profile_read waits
+ * for the recorded events, writes total ms and launch counts per class (arrays of 4) and
+ * optionally resets.
+ */
+int fgfrft_profile_enable(int on);
+int fgfrft_profile_read(double* ms, int64_t* counts, int reset);
+
 /* sinc.hpp:50-63. c, dc: 2l+1 doubles each (either may be NULL). l < 1 -> PARAMETER. */
 int fgfrft_sinc_coeffs(double alpha, int l, double* c, double* dc);
 

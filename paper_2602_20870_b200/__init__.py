@@ -67,6 +67,8 @@ def lib() -> ctypes.CDLL:
         "fgfrft_last_error": (ctypes.c_char_p, []),
         "fgfrft_version": (ctypes.c_char_p, []),
         "fgfrft_launch_count": (u64, []),
+        "fgfrft_profile_enable": (i, [i]),
+        "fgfrft_profile_read": (i, [vp, vp, i]),
         "fgfrft_sinc_coeffs": (i, [d, i, vp, vp]),
         "fgfrft_fnv1a64": (u64, [vp, ctypes.c_size_t]),
         "fgfrft_cache_create": (i, [vp, i64, i, u64, i, i, pp]),
@@ -98,7 +100,8 @@ def lib() -> ctypes.CDLL:
 
 def exported_symbols():
     return [
-        "fgfrft_last_error", "fgfrft_version", "fgfrft_launch_count", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
+        "fgfrft_last_error", "fgfrft_version", "fgfrft_launch_count", "fgfrft_profile_enable",
+        "fgfrft_profile_read", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
         "fgfrft_cache_create", "fgfrft_cache_create_from_powers", "fgfrft_cache_destroy", "fgfrft_cache_info",
         "fgfrft_cache_power", "fgfrft_cache_verify", "fgfrft_cache_set_stream", "fgfrft_cache_device_slab",
         "fgfrft_cache_device_bytes", "fgfrft_synthesize", "fgfrft_synthesize_dev", "fgfrft_apply",
@@ -115,6 +118,21 @@ def _check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(lib().fgfrft_launch_count())
+
+
+KERNEL_CLASSES = ("synthesis", "dmma_zgemm", "power_dots", "elementwise")
+
+
+def profile_enable(on: bool = True) -> None:
+    _check(lib().fgfrft_profile_enable(int(on)))
+
+
+def profile_read(reset: bool = True):
+    """{class: (total_ms, launches)} from CUDA events recorded around each launch."""
+    ms = np.zeros(4)
+    cnt = np.zeros(4, dtype=np.int64)
+    _check(lib().fgfrft_profile_read(_ptr(ms), _ptr(cnt), int(reset)))
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
 
 
 def _cm(a: np.ndarray) -> np.ndarray:

@@ -38,6 +38,8 @@ cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, in
                                 double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream);
 size_t mse_partial_elems(int n_alpha);
 cudaError_t launch_demote(const void* src, void* dst, int64_t count, cudaStream_t stream);
+cudaError_t launch_to_tiled(const void* src, void* dst, int n, int elem_bytes_dst, cudaStream_t stream);
+cudaError_t launch_from_tiled(const void* src, void* dst, int n, int elem_bytes_src, cudaStream_t stream);
 cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int width, double* out,
                             cudaStream_t stream);
 }  // namespace fgb
@@ -48,6 +50,48 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+
+// Optional per-kernel-class timing with CUDA events recorded on the launching stream
+// (fgfrft_profile_*): bench.py uses it to time the dominant kernel inside its timed region.
+enum KernelClass { KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_COUNT = 4 };
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) {
+        cudaEvent_t e = g_prof_pool.back();
+        g_prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(int c, cudaStream_t s) : cls(c), st(s) {
+        if (!g_prof_on) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        a = prof_event();
+        cudaEventRecord(a, st);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        cudaEvent_t b = prof_event();
+        cudaEventRecord(b, st);
+        g_prof.push_back({cls, a, b});
+    }
+};
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -130,12 +174,16 @@ struct fgfrft_cache {
     cudaStream_t stream = nullptr;
     std::mutex mu;
     // workspaces
-    DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda;
+    DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda, tmp;
     double* coef_h = nullptr;  // pinned staging for the coefficient tables
     size_t coef_h_cap = 0;
     cudaEvent_t coef_evt = nullptr;
 
-    size_t slab_elems() const { return (size_t)n * (size_t)n; }
+    // Matrices at the API are n x n column-major; device slabs are tiled (common.cuh) and padded
+    // to npad = 32 * ceil(n / 32) per side.
+    size_t mat_elems() const { return (size_t)n * (size_t)n; }
+    size_t npad() const { return (size_t)ceil_div(n, kTile) * kTile; }
+    size_t slab_elems() const { return npad() * npad(); }
     size_t slab_bytes() const { return slab_elems() * elem; }
     void* slab(int k) const { return static_cast<char*>(slabs) + (size_t)(k - 1) * slab_bytes(); }
 };
@@ -153,8 +201,10 @@ int alpha_chunk(const fgfrft_cache* c, int n_alpha) {
         const int v = std::atoi(env);
         if (v > 0) return v < n_alpha ? v : n_alpha;
     }
-    const size_t budget = (size_t)64 << 20;
-    size_t a = budget / (c->slab_elems() * 16);
+    // All orders of a sweep in one chunk up to ~4 GiB of Q / M workspace: the synthesis and
+    // power-dot kernels then stream the cache from HBM once per call.
+    const size_t budget = (size_t)4 << 30;
+    size_t a = budget / (c->mat_elems() * 16);
     if (a < 1) a = 1;
     if (a > (size_t)n_alpha) a = (size_t)n_alpha;
     return (int)a;
@@ -192,6 +242,7 @@ int check_alphas(const double* alphas, int n_alpha) {
 }
 
 int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out) {
+    ProfScope ps(KC_SYNTH, c->stream);
     if (c->dtype == FGFRFT_C128)
         FGB_LAUNCH(launch_synth<double>(c->slabs, (int)c->n, l_used, coef_dev, n_alpha, out, c->stream), 1);
     else
@@ -240,13 +291,14 @@ int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype,
         return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
     }
     c->stream = c->own_stream;
-    e = cudaMalloc(&c->slabs, (size_t)bytes);
+    const size_t alloc = c->slab_bytes() * (size_t)l;
+    e = cudaMalloc(&c->slabs, alloc);
     if (e != cudaSuccess) {
         cudaGetLastError();
         cudaStreamDestroy(c->own_stream);
         delete c;
         std::ostringstream msg;
-        msg << "PowerCache: device allocation of " << (unsigned long long)bytes
+        msg << "PowerCache: device allocation of " << (unsigned long long)alloc
             << " bytes failed (" << cudaGetErrorString(e) << ")";
         return fail(FGFRFT_CAPACITY, msg.str());
     }
@@ -260,7 +312,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->stream && c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
-                      &c->loss, &c->dlda})
+                      &c->loss, &c->dlda, &c->tmp})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -269,48 +321,39 @@ void destroy_cache(fgfrft_cache* c) {
     delete c;
 }
 
-// Device cache build: P_1 = F, P_k = F P_{k-1} (transform.hpp:57-58) with the DMMA GEMM.
-// complex64 caches are built in complex128 and demoted slab by slab (error does not compound
-// through a complex64 recursion).
+// Device cache build: P_1 = F, P_k = F P_{k-1} (transform.hpp:57-58) with the DMMA GEMM in
+// column-major complex128 scratch, each power then written to its tiled slab (demoted to
+// complex64 for C64 caches, so the error does not compound through a complex64 recursion).
 int build_powers(fgfrft_cache* c, const double* f) {
-    const size_t sl = c->slab_elems();
+    const size_t ml = c->mat_elems();
     const int n = (int)c->n;
-    if (c->dtype == FGFRFT_C128) {
-        FGB_CUDA(cudaMemcpyAsync(c->slab(1), f, sl * 16, cudaMemcpyHostToDevice, c->stream));
-        for (int k = 2; k <= c->l; ++k)
-            FGB_LAUNCH(launch_zgemm(n, n, n, c->slab(1), n, 0, false, c->slab(k - 1), n, 0, false, c->slab(k), n, 0,
-                                    1, false, c->stream),
-                       1);
-    } else {
-        FGB_CUDA(c->q.ensure(3 * sl * 16));
-        double2* fbuf = c->q.as<double2>();
-        double2* prev = fbuf + sl;
-        double2* cur = fbuf + 2 * sl;
-        FGB_CUDA(cudaMemcpyAsync(fbuf, f, sl * 16, cudaMemcpyHostToDevice, c->stream));
-        FGB_LAUNCH(launch_demote(fbuf, c->slab(1), (int64_t)sl, c->stream), 1);
-        FGB_CUDA(cudaMemcpyAsync(prev, fbuf, sl * 16, cudaMemcpyDeviceToDevice, c->stream));
-        for (int k = 2; k <= c->l; ++k) {
-            FGB_LAUNCH(launch_zgemm(n, n, n, fbuf, n, 0, false, prev, n, 0, false, cur, n, 0, 1, false, c->stream), 1);
-            FGB_LAUNCH(launch_demote(cur, c->slab(k), (int64_t)sl, c->stream), 1);
-            std::swap(prev, cur);
-        }
+    FGB_CUDA(c->tmp.ensure(3 * ml * 16));
+    double2* fbuf = c->tmp.as<double2>();
+    double2* prev = fbuf + ml;
+    double2* cur = fbuf + 2 * ml;
+    FGB_CUDA(cudaMemcpyAsync(fbuf, f, ml * 16, cudaMemcpyHostToDevice, c->stream));
+    FGB_LAUNCH(launch_to_tiled(fbuf, c->slab(1), n, (int)c->elem, c->stream), 1);
+    const double2* p = fbuf;
+    for (int k = 2; k <= c->l; ++k) {
+        FGB_LAUNCH(launch_zgemm(n, n, n, fbuf, n, 0, false, p, n, 0, false, cur, n, 0, 1, false, c->stream), 1);
+        FGB_LAUNCH(launch_to_tiled(cur, c->slab(k), n, (int)c->elem, c->stream), 1);
+        p = cur;
+        std::swap(prev, cur);
     }
     FGB_CUDA(cudaStreamSynchronize(c->stream));
+    c->tmp.release();
     return FGFRFT_OK;
 }
 
 int upload_powers(fgfrft_cache* c, const double* powers) {
-    const size_t sl = c->slab_elems();
-    if (c->dtype == FGFRFT_C128) {
-        FGB_CUDA(cudaMemcpyAsync(c->slabs, powers, sl * 16 * c->l, cudaMemcpyHostToDevice, c->stream));
-    } else {
-        FGB_CUDA(c->q.ensure(sl * 16));
-        for (int k = 1; k <= c->l; ++k) {
-            FGB_CUDA(cudaMemcpyAsync(c->q.p, powers + 2 * sl * (k - 1), sl * 16, cudaMemcpyHostToDevice, c->stream));
-            FGB_LAUNCH(launch_demote(c->q.p, c->slab(k), (int64_t)sl, c->stream), 1);
-        }
+    const size_t ml = c->mat_elems();
+    FGB_CUDA(c->tmp.ensure(ml * 16));
+    for (int k = 1; k <= c->l; ++k) {
+        FGB_CUDA(cudaMemcpyAsync(c->tmp.p, powers + 2 * ml * (k - 1), ml * 16, cudaMemcpyHostToDevice, c->stream));
+        FGB_LAUNCH(launch_to_tiled(c->tmp.p, c->slab(k), (int)c->n, (int)c->elem, c->stream), 1);
     }
     FGB_CUDA(cudaStreamSynchronize(c->stream));
+    c->tmp.release();
     return FGFRFT_OK;
 }
 
@@ -341,13 +384,14 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
     const int n = (int)c->n;
-    const size_t sl = c->slab_elems();
+    const size_t sl = c->mat_elems();
     const int chunk = alpha_chunk(c, n_alpha);
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * 16));
     const size_t width = (size_t)(2 * l_used + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p)) return st;
+        ProfScope ps(KC_GEMM, c->stream);
         FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, inverse, x_dev, n, 0, false,
                                 static_cast<double2*>(y_dev) + (size_t)a0 * n * b, n, (int64_t)n * b, na, false,
                                 c->stream),
@@ -359,7 +403,7 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
 // s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
 int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
     const int n = (int)c->n;
-    const size_t sl = c->slab_elems();
+    const size_t sl = c->mat_elems();
     const int chunk = alpha_chunk(c, n_alpha);
     FGB_CUDA(c->m.ensure((size_t)chunk * sl * 16));
     FGB_CUDA(c->partial.ensure(dots_partial_elems(n, c->l, chunk) * sizeof(double)));
@@ -367,10 +411,14 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         // M_a = G_a X^H  (n x n, K = b)
+        {
+        ProfScope ps(KC_GEMM, c->stream);
         FGB_LAUNCH(launch_zgemm(n, n, (int)b, static_cast<const double2*>(g_dev) + (size_t)a0 * n * b, n,
                                 (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na, false,
                                 c->stream),
                    1);
+        }
+        ProfScope ps(KC_DOTS, c->stream);
         FGB_LAUNCH(launch_power_dots(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
                                      s_dev + a0 * width, c->stream),
                    2);
@@ -389,6 +437,36 @@ const char* fgfrft_last_error(void) { return g_err.c_str(); }
 const char* fgfrft_version(void) { return "0.1.0-b200"; }
 
 uint64_t fgfrft_launch_count(void) { return g_launches.load(); }
+
+int fgfrft_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    return FGFRFT_OK;
+}
+
+int fgfrft_profile_read(double* ms, int64_t* counts, int reset) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (int k = 0; k < KC_COUNT; ++k) {
+        if (ms) ms[k] = 0.0;
+        if (counts) counts[k] = 0;
+    }
+    for (const ProfRec& r : g_prof) {
+        if (r.cls < 0 || r.cls >= KC_COUNT) continue;
+        FGB_CUDA(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        FGB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+        if (ms) ms[r.cls] += t;
+        if (counts) counts[r.cls] += 1;
+    }
+    if (reset) {
+        for (const ProfRec& r : g_prof) {
+            g_prof_pool.push_back(r.a);
+            g_prof_pool.push_back(r.b);
+        }
+        g_prof.clear();
+    }
+    return FGFRFT_OK;
+}
 
 int fgfrft_sinc_coeffs(double alpha, int l, double* c, double* dc) {
     if (l < 1) return fail(FGFRFT_PARAMETER, "sinc_coeffs: truncation order must be >= 1");
@@ -453,14 +531,18 @@ int fgfrft_cache_power(fgfrft_cache* c, int k, double* out) {
     if (!out) return fail(FGFRFT_PARAMETER, "null output");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
-    return download_as_c128(c, c->slab(k), c->slab_elems(), out);
+    FGB_CUDA(c->tmp.ensure(c->mat_elems() * 16));
+    FGB_LAUNCH(launch_from_tiled(c->slab(k), c->tmp.p, (int)c->n, (int)c->elem, c->stream), 1);
+    FGB_CUDA(cudaMemcpyAsync(out, c->tmp.p, c->mat_elems() * 16, cudaMemcpyDeviceToHost, c->stream));
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    return FGFRFT_OK;
     FGB_GUARD_END
 }
 
 int fgfrft_cache_verify(const fgfrft_cache* c, const double* f) {
     if (int st = check_handle(c)) return st;
     if (!f) return fail(FGFRFT_PARAMETER, "null matrix");
-    if (host_fnv1a64(f, c->slab_elems() * 16) != c->fingerprint)
+    if (host_fnv1a64(f, c->mat_elems() * 16) != c->fingerprint)
         return fail(FGFRFT_NUMERICAL, "PowerCache: fingerprint mismatch, cache is stale for this matrix");
     return FGFRFT_OK;
 }
@@ -481,7 +563,7 @@ int fgfrft_cache_device_slab(fgfrft_cache* c, int k, void** dptr) {
 
 int fgfrft_cache_device_bytes(const fgfrft_cache* c, uint64_t* bytes) {
     if (int st = check_handle(c)) return st;
-    *bytes = (uint64_t)c->slab_bytes() * (uint64_t)c->l;
+    *bytes = (uint64_t)c->slab_bytes() * (uint64_t)c->l;  // padded tiled slabs
     return FGFRFT_OK;
 }
 
@@ -511,12 +593,12 @@ int fgfrft_synthesize(fgfrft_cache* c, const double* alphas, int n_alpha, int tr
     {
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
-        FGB_CUDA(c->y.ensure((size_t)n_alpha * c->slab_bytes()));
+        FGB_CUDA(c->y.ensure((size_t)n_alpha * c->mat_elems() * c->elem));
     }
     if (int st = fgfrft_synthesize_dev(c, alphas, n_alpha, truncation, which, c->y.p)) return st;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
-    return download_as_c128(c, c->y.p, (size_t)n_alpha * c->slab_elems(), out);
+    return download_as_c128(c, c->y.p, (size_t)n_alpha * c->mat_elems(), out);
     FGB_GUARD_END
 }
 
@@ -675,7 +757,7 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
     const double* dc_dev = coef + (size_t)n_alpha * width;
     const int chunk = alpha_chunk(c, n_alpha);
-    const size_t sl = c->slab_elems();
+    const size_t sl = c->mat_elems();
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * 16));
     FGB_CUDA(c->g.ensure((size_t)chunk * blk * 16));
     FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
@@ -686,12 +768,18 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
         const int na = std::min(chunk, n_alpha - a0);
         double2* ya = y_dev ? static_cast<double2*>(y_dev) + (size_t)a0 * blk : c->y.as<double2>();
         if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p)) return st;
-        FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n, (int64_t)blk,
-                                na, false, c->stream),
-                   1);
-        FGB_LAUNCH(launch_mse_residual(ya, xc_dev, (int64_t)blk, na, 2.0 * norm, norm, c->g.p, c->lpart.as<double>(),
-                                       static_cast<double*>(loss_dev) + a0, c->stream),
-                   2);
+        {
+            ProfScope ps(KC_GEMM, c->stream);
+            FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n,
+                                    (int64_t)blk, na, false, c->stream),
+                       1);
+        }
+        {
+            ProfScope ps(KC_ELEMWISE, c->stream);
+            FGB_LAUNCH(launch_mse_residual(ya, xc_dev, (int64_t)blk, na, 2.0 * norm, norm, c->g.p,
+                                           c->lpart.as<double>(), static_cast<double*>(loss_dev) + a0, c->stream),
+                       2);
+        }
         if (int st = dots_device(c, na, c->g.p, x_dev, b, c->s.as<double>() + a0 * width)) return st;
     }
     FGB_LAUNCH(launch_coef_dot(dc_dev, c->s.as<double>(), n_alpha, (int)width, static_cast<double*>(dlda_dev),

@@ -96,6 +96,22 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                  : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+// ---------------------------------------------------------------- tiled cache layout
+//
+// Device slabs of the power cache are stored TILED: the n x n matrix is padded to
+// npad = 32 * nt (zeros) and cut into 32x32 tiles; tile (I, J) occupies 1024 consecutive
+// elements at ((J * nt + I) * 1024), and tile element (i, j) sits at j * 32 + (i ^ j).
+// One tile = one contiguous TMA bulk copy (16 KB complex128), and the XOR swizzle makes both
+// the direct read (lanes along i) and the transposed read (lanes along j) of a staged tile
+// bank-conflict free without padding shared memory.
+constexpr int kTile = 32;
+constexpr int kTileElems = kTile * kTile;
+
+__host__ __device__ __forceinline__ int64_t tile_base(int I, int J, int nt) {
+    return ((int64_t)J * nt + I) * kTileElems;
+}
+__host__ __device__ __forceinline__ int swz(int i, int j) { return j * kTile + (i ^ j); }
+
 // ---------------------------------------------------------------- misc
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

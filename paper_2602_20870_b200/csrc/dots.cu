@@ -13,11 +13,10 @@
 
 namespace fgb {
 
-constexpr int kDotT = 32, kDotStages = 4, kDotThreads = 256, kDotLdt = 33;
+constexpr int kDotStages = 4, kDotThreads = 256;
 
 size_t dots_smem_bytes(int l, int ac) {
-    return (size_t)kDotStages * 2 * kDotT * kDotLdt * 16 + kDotStages * 8 +
-           (size_t)l * 8 * ac * 2 * sizeof(double) + 16;
+    return (size_t)kDotStages * 2 * kTileElems * 16 + kDotStages * 8 + (size_t)l * 8 * ac * 2 * sizeof(double) + 16;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -26,16 +25,17 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// partial layout: [pair][a][2l+1]
+// slabs: tiled layout (common.cuh). partial layout: [a][2l+1][pair] (pairs contiguous so the
+// fixed-order reduction over pairs is coalesced).
 template <int AC>
 __global__ void __launch_bounds__(kDotThreads, 1)
 power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_elems,
                   const double2* __restrict__ m, int64_t m_stride, int n_alpha, int n_achunks,
-                  double* __restrict__ partial, int nt) {
-    constexpr int T = kDotT, S = kDotStages, LDT = kDotLdt;
+                  double* __restrict__ partial, int nt, int npairs) {
+    constexpr int T = kTile, S = kDotStages;
     extern __shared__ __align__(128) unsigned char smem[];
     double2* tiles = reinterpret_cast<double2*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * T * LDT * 16);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 16);
     double* red = reinterpret_cast<double*>(full + S);  // [k-1][warp][a][2]
 
     const int chunk = blockIdx.x % n_achunks;
@@ -55,22 +55,23 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
     }
     __syncthreads();
 
-    const uint32_t stage_bytes = (uint32_t)((diag ? 1 : 2) * bi * bj * 16);
+    const uint32_t tile_bytes = (uint32_t)(kTileElems * 16);
+    const bool stream_once = n_achunks == 1;
     const uint64_t pol = policy_evict_first();
-    auto issue = [&](int k, int s) {
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], stage_bytes);
-        __syncwarp();
+    const int64_t off1 = tile_base(I, J, nt), off2 = tile_base(J, I, nt);
+    auto issue = [&](int k, int s) {  // one thread: one bulk copy per 32x32 tile
+        mbar_arrive_expect_tx(&full[s], (diag ? 1 : 2) * tile_bytes);
         const double2* slab = slabs + (int64_t)(k - 1) * slab_elems;
-        double2* t1 = tiles + (size_t)(s * 2) * T * LDT;
-        double2* t2 = t1 + T * LDT;
-        if (lane < bj)
-            bulk_g2s_hint(t1 + lane * LDT, slab + (int64_t)(J * T + lane) * n + I * T, (uint32_t)(bi * 16),
-                          &full[s], pol);
-        if (!diag && lane < bi)
-            bulk_g2s_hint(t2 + lane * LDT, slab + (int64_t)(I * T + lane) * n + J * T, (uint32_t)(bj * 16),
-                          &full[s], pol);
+        double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        if (stream_once) {
+            bulk_g2s_hint(t1, slab + off1, tile_bytes, &full[s], pol);
+            if (!diag) bulk_g2s_hint(t1 + kTileElems, slab + off2, tile_bytes, &full[s], pol);
+        } else {
+            bulk_g2s(t1, slab + off1, tile_bytes, &full[s]);
+            if (!diag) bulk_g2s(t1 + kTileElems, slab + off2, tile_bytes, &full[s]);
+        }
     };
-    if (warp == 0)
+    if (tid == 0)
         for (int s = 0; s < S && s < l; ++s) issue(s + 1, s);
 
     // M tiles for this pair, zero outside the matrix so garbage smem never contributes.
@@ -95,16 +96,16 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
     for (int k = 1; k <= l; ++k) {
         const int s = (k - 1) % S;
         mbar_wait(&full[s], ((k - 1) / S) & 1);
-        const double2* t1 = tiles + (size_t)(s * 2) * T * LDT;
-        const double2* t2 = diag ? t1 : t1 + T * LDT;
+        const double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        const double2* t2 = diag ? t1 : t1 + kTileElems;
         double sp[AC], sm[AC];
 #pragma unroll
         for (int a = 0; a < AC; ++a) sp[a] = sm[a] = 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = warp + 8 * i;
-            const double2 p1 = t1[c * LDT + r];  // P[I*T + r, J*T + c]
-            const double2 p2 = t2[r * LDT + c];  // P[J*T + c, I*T + r]
+            const double2 p1 = t1[swz(r, c)];  // P[I*T + r, J*T + c]
+            const double2 p2 = t2[swz(c, r)];  // P[J*T + c, I*T + r]
 #pragma unroll
             for (int a = 0; a < AC; ++a) {
                 // Re(conj(m) p) and Re(conj(m) conj(p^T))
@@ -126,7 +127,7 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
             }
         }
         __syncthreads();
-        if (warp == 0 && k + S <= l) issue(k + S, s);
+        if (tid == 0 && k + S <= l) issue(k + S, s);
     }
 
     // s0 partial: warp reduce then fixed-order sum over warps through the (now idle) stage ring.
@@ -148,34 +149,38 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
             const int sel = kk > l ? 0 : 1;
             for (int w = 0; w < 8; ++w) acc += red[(((size_t)(k - 1) * 8 + w) * AC + a) * 2 + sel];
         }
-        partial[((int64_t)pair * n_alpha + a0 + a) * width + kk] = acc;
+        partial[((int64_t)(a0 + a) * width + kk) * npairs + pair] = acc;
     }
 }
 
-// out[a][kk] = sum over pairs (ascending) of partial[pair][a][kk].
-__global__ void reduce_pairs_kernel(const double* __restrict__ partial, int npairs, int n_alpha, int width,
-                                    double* __restrict__ out) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n_alpha * width) return;
+// out[a][kk] = sum over tile pairs of partial[a][kk][pair]: one block per (a, kk), a fixed
+// strided split over 128 threads and a fixed shuffle tree -> deterministic.
+__global__ void __launch_bounds__(128) reduce_pairs_kernel(const double* __restrict__ partial, int npairs,
+                                                           double* __restrict__ out) {
+    const double* row = partial + (int64_t)blockIdx.x * npairs;
     double acc = 0.0;
-    for (int p = 0; p < npairs; ++p) acc += partial[(int64_t)p * n_alpha * width + idx];
-    out[idx] = acc;
+    for (int p = threadIdx.x; p < npairs; p += 128) acc += row[p];
+    acc = warp_sum(acc);
+    __shared__ double ws[4];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = (ws[0] + ws[1]) + (ws[2] + ws[3]);
 }
 
 size_t dots_partial_elems(int n, int l, int n_alpha) {
-    const int nt = (int)ceil_div(n, kDotT);
+    const int nt = (int)ceil_div(n, kTile);
     return (size_t)(nt * (nt + 1) / 2) * n_alpha * (2 * l + 1);
 }
 
 // s_out (device): [n_alpha][2l+1]; partial: device scratch of dots_partial_elems().
 cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
                               double* partial, double* s_out, cudaStream_t stream) {
-    const int nt = (int)ceil_div(n, kDotT);
+    const int nt = (int)ceil_div(n, kTile);
     const int npairs = nt * (nt + 1) / 2;
     const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
     const int nchunks = (int)ceil_div(n_alpha, ac);
     const size_t smem = dots_smem_bytes(l, ac);
-    const int64_t slab = (int64_t)n * n;
+    const int64_t slab = (int64_t)nt * nt * kTileElems;
     const dim3 grid((unsigned)((int64_t)nchunks * npairs));
 #define FGB_DOTS_CASE(ACV)                                                                                   \
     {                                                                                                        \
@@ -183,15 +188,14 @@ cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, in
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return e;                                                                      \
         kern<<<grid, kDotThreads, smem, stream>>>((const double2*)slabs, n, l, slab, (const double2*)m,     \
-                                                  m_stride, n_alpha, nchunks, partial, nt);                  \
+                                                  m_stride, n_alpha, nchunks, partial, nt, npairs);                  \
     }
     if (ac == 4) FGB_DOTS_CASE(4) else if (ac == 2) FGB_DOTS_CASE(2) else FGB_DOTS_CASE(1)
 #undef FGB_DOTS_CASE
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int total = n_alpha * (2 * l + 1);
-    reduce_pairs_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, stream>>>(partial, npairs, n_alpha, 2 * l + 1,
-                                                                           s_out);
+    reduce_pairs_kernel<<<(unsigned)total, 128, 0, stream>>>(partial, npairs, s_out);
     return cudaGetLastError();
 }
 

@@ -32,12 +32,18 @@ mse_residual_kernel(const double2* __restrict__ y, const double2* __restrict__ x
     }
 }
 
-__global__ void sum_rows_kernel(const double* __restrict__ partial, int cols, double scale, double* __restrict__ out) {
-    const int a = blockIdx.x;
-    if (threadIdx.x != 0) return;
+// out[a] = scale * sum_i partial[a][i]; fixed split over 128 threads + fixed tree (deterministic).
+__global__ void __launch_bounds__(128) sum_rows_kernel(const double* __restrict__ partial, int cols, double scale,
+                                                       double* __restrict__ out) {
+    const double* row = partial + (int64_t)blockIdx.x * cols;
     double s = 0.0;
-    for (int i = 0; i < cols; ++i) s += partial[(int64_t)a * cols + i];
-    out[a] = s * scale;
+    for (int i = threadIdx.x; i < cols; i += 128) s += row[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ double ws[4];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = ((ws[0] + ws[1]) + (ws[2] + ws[3])) * scale;
 }
 
 size_t mse_partial_elems(int n_alpha) { return (size_t)n_alpha * kResBlocks; }
@@ -50,7 +56,7 @@ cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, in
                                                                       count, g_scale, (double2*)g, partial);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    sum_rows_kernel<<<n_alpha, 32, 0, stream>>>(partial, kResBlocks, loss_scale, loss_out);
+    sum_rows_kernel<<<n_alpha, 128, 0, stream>>>(partial, kResBlocks, loss_scale, loss_out);
     return cudaGetLastError();
 }
 

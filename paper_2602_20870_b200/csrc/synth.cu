@@ -9,7 +9,9 @@
 //
 // Multi-order launches (A orders): a CTA accumulates AC orders in registers; CTAs of the
 // ceil(A/AC) order chunks of one tile pair are adjacent in the grid, so the chunks after the
-// first are served from L2.
+// first are served from L2. The cache is stored tiled + XOR-swizzled (common.cuh): each staged
+// tile is ONE contiguous 16 KB bulk copy and both the direct and the transposed shared-memory
+// reads are conflict free.
 //
 // Arithmetic: the reference's per-element update t = a*p_ij + b*conj(p_ji); q = q + t is
 // evaluated with explicit round-to-nearest multiplies/adds (no FMA contraction), so for
@@ -19,13 +21,8 @@
 
 namespace fgb {
 
-constexpr int kSynthT = 32;        // tile edge (complex elements)
 constexpr int kSynthStages = 4;    // TMA ring depth
 constexpr int kSynthThreads = 256;
-
-template <typename R> struct SynthLdt;
-template <> struct SynthLdt<double> { static constexpr int v = 33; };  // 528 B columns: odd quad stride
-template <> struct SynthLdt<float> { static constexpr int v = 34; };   // 272 B: 16-B aligned, 2-way
 
 template <typename R>
 __device__ __forceinline__ R rmul(R a, R b);
@@ -44,21 +41,21 @@ __device__ __forceinline__ void pair_update(C& q, R a, R b, const C& p, const C&
 }
 
 size_t synth_smem_bytes(int elem_bytes, int l_used, int ac) {
-    const int ldt = elem_bytes == 16 ? SynthLdt<double>::v : SynthLdt<float>::v;
-    return (size_t)kSynthStages * 2 * kSynthT * ldt * elem_bytes + kSynthStages * 8 +
-           (size_t)l_used * ac * 16 + (size_t)ac * 8 + 16;
+    return (size_t)kSynthStages * 2 * kTileElems * elem_bytes + kSynthStages * 8 + (size_t)l_used * ac * 16 +
+           (size_t)ac * 8 + 16;
 }
 
+// slabs: tiled layout (common.cuh), slab_elems = nt^2 * 1024 per power.
 template <typename R, int AC>
 __global__ void __launch_bounds__(kSynthThreads, 1)
 synth_pairs_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l_used, int64_t slab_elems,
                    const double* __restrict__ coef, int coef_ld, int lc, int n_alpha, int n_achunks,
                    cplx_t<R>* __restrict__ out, int64_t out_stride, int nt) {
     using C = cplx_t<R>;
-    constexpr int T = kSynthT, S = kSynthStages, LDT = SynthLdt<R>::v;
+    constexpr int T = kTile, S = kSynthStages;
     extern __shared__ __align__(128) unsigned char smem[];
     C* tiles = reinterpret_cast<C*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * T * LDT * sizeof(C));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * sizeof(C));
     double2* cs = reinterpret_cast<double2*>(full + S);
     double* c0s = reinterpret_cast<double*>(cs + (size_t)l_used * AC);
 
@@ -89,24 +86,25 @@ synth_pairs_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l_used, int64
     }
     __syncthreads();
 
-    const uint32_t stage_bytes = (uint32_t)((diag ? 1 : 2) * bi * bj * sizeof(C));
+    const uint32_t tile_bytes = (uint32_t)(kTileElems * sizeof(C));
+    // Single order: the cache is streamed once, mark it evict-first. Several order chunks:
+    // sibling CTAs of the same tile pair re-read it from L2, keep the default policy.
+    const bool stream_once = n_achunks == 1;
     const uint64_t pol = policy_evict_first();
-    // Warp 0 issues one bulk copy per tile column: tile1 = P[I-block rows, J-block cols],
-    // tile2 = P[J-block rows, I-block cols]; padded columns keep transposed reads conflict-free.
-    auto issue = [&](int k, int s) {
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], stage_bytes);
-        __syncwarp();
+    const int64_t off1 = tile_base(I, J, nt), off2 = tile_base(J, I, nt);
+    auto issue = [&](int k, int s) {  // one thread: one bulk copy per 32x32 tile
+        mbar_arrive_expect_tx(&full[s], (diag ? 1 : 2) * tile_bytes);
         const C* slab = slabs + (int64_t)(k - 1) * slab_elems;
-        C* t1 = tiles + (size_t)(s * 2) * T * LDT;
-        C* t2 = t1 + T * LDT;
-        if (lane < bj)
-            bulk_g2s_hint(t1 + lane * LDT, slab + (int64_t)(J * T + lane) * n + I * T,
-                          (uint32_t)(bi * sizeof(C)), &full[s], pol);
-        if (!diag && lane < bi)
-            bulk_g2s_hint(t2 + lane * LDT, slab + (int64_t)(I * T + lane) * n + J * T,
-                          (uint32_t)(bj * sizeof(C)), &full[s], pol);
+        C* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        if (stream_once) {
+            bulk_g2s_hint(t1, slab + off1, tile_bytes, &full[s], pol);
+            if (!diag) bulk_g2s_hint(t1 + kTileElems, slab + off2, tile_bytes, &full[s], pol);
+        } else {
+            bulk_g2s(t1, slab + off1, tile_bytes, &full[s]);
+            if (!diag) bulk_g2s(t1 + kTileElems, slab + off2, tile_bytes, &full[s]);
+        }
     };
-    if (warp == 0)
+    if (tid == 0)
         for (int s = 0; s < S && s < l_used; ++s) issue(s + 1, s);
 
     const int r = lane;
@@ -127,16 +125,16 @@ synth_pairs_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l_used, int64
     for (int k = 1; k <= l_used; ++k) {
         const int s = (k - 1) % S;
         mbar_wait(&full[s], ((k - 1) / S) & 1);
-        const C* t1 = tiles + (size_t)(s * 2) * T * LDT;
-        const C* t2 = diag ? t1 : t1 + T * LDT;
+        const C* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        const C* t2 = diag ? t1 : t1 + kTileElems;
         double2 ab[AC];
 #pragma unroll
         for (int a = 0; a < AC; ++a) ab[a] = cs[(k - 1) * AC + a];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = warp + 8 * i;
-            const C p1 = t1[c * LDT + r];
-            const C p2 = t2[r * LDT + c];
+            const C p1 = t1[swz(r, c)];  // P[I*T + r, J*T + c]
+            const C p2 = t2[swz(c, r)];  // P[J*T + c, I*T + r]
 #pragma unroll
             for (int a = 0; a < AC; ++a) {
                 pair_update<R>(q1[i][a], (R)ab[a].x, (R)ab[a].y, p1, p2);
@@ -144,7 +142,7 @@ synth_pairs_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l_used, int64
             }
         }
         __syncthreads();
-        if (warp == 0 && k + S <= l_used) issue(k + S, s);
+        if (tid == 0 && k + S <= l_used) issue(k + S, s);
     }
 
     // Q[I,J]: lanes run down a column -> coalesced stores straight from registers.
@@ -159,20 +157,20 @@ synth_pairs_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l_used, int64
         }
     }
     if (diag) return;
-    // Q[J,I]: transpose through shared memory (stage-0 buffer) so stores stay coalesced.
+    // Q[J,I]: transpose through shared memory (swizzled, conflict-free) so stores stay coalesced.
     C* buf = tiles;
 #pragma unroll
     for (int a = 0; a < AC; ++a) {
         if (a >= na) break;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) buf[r * LDT + warp + 8 * i] = q2[i][a];
+        for (int i = 0; i < 4; ++i) buf[swz(warp + 8 * i, r)] = q2[i][a];  // (row c, col r) of Q[J,I]
         __syncthreads();
         C* o = out + (int64_t)(a0 + a) * out_stride;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int col = warp + 8 * i;   // I-block column
-            const int row = lane;           // J-block row
-            if (row < bj && col < bi) o[(int64_t)(I * T + col) * n + J * T + row] = buf[col * LDT + row];
+            const int col = warp + 8 * i;  // I-block column
+            const int row = lane;          // J-block row
+            if (row < bj && col < bi) o[(int64_t)(I * T + col) * n + J * T + row] = buf[swz(row, col)];
         }
         __syncthreads();
     }
@@ -182,12 +180,12 @@ synth_pairs_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l_used, int64
 template <typename R>
 cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha,
                          void* out, cudaStream_t stream) {
-    const int nt = (int)ceil_div(n, kSynthT);
+    const int nt = (int)ceil_div(n, kTile);
     const int npairs = nt * (nt + 1) / 2;
     const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
     const int nchunks = (int)ceil_div(n_alpha, ac);
     const size_t smem = synth_smem_bytes(sizeof(cplx_t<R>), l_used, ac);
-    const int64_t slab = (int64_t)n * n;
+    const int64_t slab = (int64_t)nt * nt * kTileElems;
     const dim3 grid((unsigned)((int64_t)nchunks * npairs));
     const int coef_ld = 2 * l_used + 1;
 #define FGB_SYNTH_CASE(ACV)                                                                                  \
@@ -197,7 +195,7 @@ cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coe
         if (e != cudaSuccess) return e;                                                                      \
         kern<<<grid, kSynthThreads, smem, stream>>>((const cplx_t<R>*)slabs, n, l_used, slab, coef_dev,      \
                                                     coef_ld, l_used, n_alpha, nchunks, (cplx_t<R>*)out,      \
-                                                    slab, nt);                                               \
+                                                    (int64_t)n * n, nt);                                     \
     }
     if (ac == 4) FGB_SYNTH_CASE(4) else if (ac == 2) FGB_SYNTH_CASE(2) else FGB_SYNTH_CASE(1)
 #undef FGB_SYNTH_CASE

@@ -202,3 +202,13 @@ def test_mse_step_config1():
     _, dc = O.sinc_coeffs(cfg.alphas[0], cfg.l)
     s_ref = O.power_dots(o, (2 * (yr - clean) / yr.size) @ cfg.x.conj().T)
     assert abs(dl[0] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+def test_cpp_dropin_header_suite():
+    """The reference's transform/sinc test cases compiled against include/fgfrft/*.hpp."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_dropin")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
