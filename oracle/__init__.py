@@ -356,3 +356,43 @@ def matrix_power(f: np.ndarray, m: int) -> np.ndarray:
 def rotation2(phi: float) -> np.ndarray:
     """tests/oracles.hpp:43-48."""
     return np.array([[math.cos(phi), -math.sin(phi)], [math.sin(phi), math.cos(phi)]], dtype=np.complex128)
+
+
+# ----------------------------------------------------------------------------- large-N checker
+
+def series_apply_recursive(f: np.ndarray, alpha: float, l: int, x: np.ndarray, which: str = "c",
+                           inverse: bool = False) -> np.ndarray:
+    """Q(alpha) X (or Q^H X) for a FEW columns X without forming any power: the powers act by
+    repeated multiplication, F^k X = F (F^{k-1} X) and (F^H)^k X (tests/oracles.hpp:50-56's
+    matrix_power, applied to X), weighted by the reference coefficients (sinc.hpp:50-63),
+    summed in ascending k like transform.hpp:118-121. which = "c" (Q) or "dc" (dQ/dalpha).
+    Cost 2L n^2 |X|: an independent checker at sizes where the dense oracle cannot run."""
+    c, dc = sinc_coeffs(alpha, l)
+    coef = c if which == "c" else dc
+    if inverse:  # Q^H = sum conj(c_k) F^{-k}: swap the roles of +k and -k (real coefficients)
+        coef = coef[::-1]
+    x = np.asarray(x, dtype=np.complex128)
+    fh = np.ascontiguousarray(f.conj().T)
+    fp = np.ascontiguousarray(f)
+    acc = coef[l] * x
+    vp, vm = x, x
+    for k in range(1, l + 1):
+        vp = fp @ vp
+        vm = fh @ vm
+        acc = acc + (coef[l + k] * vp + coef[l - k] * vm)
+    return acc
+
+
+def power_dots_recursive(f: np.ndarray, l: int, g: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """s_k = Re<G, F^k X>, k = -L..L, by the same recursion (definition of learn.hpp:88-92)."""
+    out = np.empty(2 * l + 1)
+    fh = np.ascontiguousarray(f.conj().T)
+    fp = np.ascontiguousarray(f)
+    out[l] = float(np.vdot(g, x).real)
+    vp, vm = x.astype(np.complex128), x.astype(np.complex128)
+    for k in range(1, l + 1):
+        vp = fp @ vp
+        vm = fh @ vm
+        out[l + k] = float(np.vdot(g, vp).real)
+        out[l - k] = float(np.vdot(g, vm).real)
+    return out

@@ -34,6 +34,10 @@ cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_
 cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
                               double* partial, double* s_out, cudaStream_t stream);
 size_t dots_partial_elems(int n, int l, int n_alpha);
+size_t dots_mma_partial_elems(int n);
+int dots_mma_max_orders();
+cudaError_t launch_power_dots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                                  double* partial, double* s_out, cudaStream_t stream, int* launches);
 cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, int n_alpha, double g_scale,
                                 double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream);
 size_t mse_partial_elems(int n_alpha);
@@ -401,27 +405,38 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
 }
 
 // s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
+// Order sweeps (>= 8 orders) use the DMMA split-K contraction (every byte of M and of the cache
+// read once per 64 orders); a few orders use the scalar tile-pair kernel (HBM-bound).
 int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
-    const int chunk = alpha_chunk(c, n_alpha);
+    const bool mma = n_alpha >= 8;
+    const int chunk = mma ? std::min(alpha_chunk(c, n_alpha), dots_mma_max_orders()) : alpha_chunk(c, n_alpha);
     FGB_CUDA(c->m.ensure((size_t)chunk * sl * 16));
-    FGB_CUDA(c->partial.ensure(dots_partial_elems(n, c->l, chunk) * sizeof(double)));
+    FGB_CUDA(c->partial.ensure(std::max(mma ? dots_mma_partial_elems(n) : 0, dots_partial_elems(n, c->l, chunk)) *
+                               sizeof(double)));
     const size_t width = (size_t)(2 * c->l + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         // M_a = G_a X^H  (n x n, K = b)
         {
-        ProfScope ps(KC_GEMM, c->stream);
-        FGB_LAUNCH(launch_zgemm(n, n, (int)b, static_cast<const double2*>(g_dev) + (size_t)a0 * n * b, n,
-                                (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na, false,
-                                c->stream),
-                   1);
+            ProfScope ps(KC_GEMM, c->stream);
+            FGB_LAUNCH(launch_zgemm(n, n, (int)b, static_cast<const double2*>(g_dev) + (size_t)a0 * n * b, n,
+                                    (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na, false,
+                                    c->stream),
+                       1);
         }
         ProfScope ps(KC_DOTS, c->stream);
-        FGB_LAUNCH(launch_power_dots(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
-                                     s_dev + a0 * width, c->stream),
-                   2);
+        if (mma && na >= 8) {
+            int nl = 0;
+            FGB_CUDA(launch_power_dots_mma(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
+                                           s_dev + a0 * width, c->stream, &nl));
+            g_launches += nl;
+        } else {
+            FGB_LAUNCH(launch_power_dots(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
+                                         s_dev + a0 * width, c->stream),
+                       2);
+        }
     }
     return FGFRFT_OK;
 }

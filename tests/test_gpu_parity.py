@@ -212,3 +212,21 @@ def test_cpp_dropin_header_suite():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.parametrize("n,l,n_alpha,b", [(90, 9, 8, 17), (150, 70, 67, 5), (33, 3, 64, 40)])
+def test_dlda_sweep_dmma_path(n, l, n_alpha, b):
+    """>= 8 orders route to the DMMA split-K contraction (several power / order chunks)."""
+    f = prep.random_unitary(n, 500 + n)
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    alphas = list(np.linspace(-1.3, 2.1, n_alpha))
+    gs = [rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b)) for _ in alphas]
+    dl, s = fg.dlda(g, alphas, gs, x)
+    for i in range(0, n_alpha, max(1, n_alpha // 7)):
+        s_ref = O.power_dots(o, gs[i] @ x.conj().T)
+        assert np.abs(s[i] - s_ref).max() <= 1e-10 * np.abs(s_ref).sum()
+        _, dc = O.sinc_coeffs(alphas[i], l)
+        assert abs(dl[i] - float(np.dot(dc, s_ref))) <= 1e-10 * np.sum(np.abs(dc * s_ref))
