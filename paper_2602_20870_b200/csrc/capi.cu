@@ -28,6 +28,9 @@ uint64_t host_fnv1a64(const void* data, size_t nbytes);
 template <typename R>
 cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
                          cudaStream_t stream);
+cudaError_t launch_synth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                               cudaStream_t stream);
+int synth_sweep_max_orders();
 cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
                          int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
                          bool accumulate, cudaStream_t stream);
@@ -245,8 +248,22 @@ int check_alphas(const double* alphas, int n_alpha) {
     return FGFRFT_OK;
 }
 
+// Q for n_alpha orders into out (n x n each). Up to 4 orders: exact scalar tile-pair kernel
+// (HBM-bound, bit-identical to the reference order of operations). Sweeps of >= 8 complex128
+// orders: DMMA kernel, 64 orders per launch, cache streamed once per launch.
 int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out) {
     ProfScope ps(KC_SYNTH, c->stream);
+    if (c->dtype == FGFRFT_C128 && n_alpha >= 8 && std::getenv("FGFRFT_EXACT_SWEEP") == nullptr) {
+        const int width = 2 * l_used + 1;
+        const int cap = synth_sweep_max_orders();
+        for (int a0 = 0; a0 < n_alpha; a0 += cap) {
+            const int na = std::min(cap, n_alpha - a0);
+            FGB_LAUNCH(launch_synth_sweep(c->slabs, (int)c->n, l_used, coef_dev + (size_t)a0 * width, na,
+                                          static_cast<double2*>(out) + (size_t)a0 * c->mat_elems(), c->stream),
+                       1);
+        }
+        return FGFRFT_OK;
+    }
     if (c->dtype == FGFRFT_C128)
         FGB_LAUNCH(launch_synth<double>(c->slabs, (int)c->n, l_used, coef_dev, n_alpha, out, c->stream), 1);
     else

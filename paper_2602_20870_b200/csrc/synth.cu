@@ -205,4 +205,171 @@ cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coe
 template cudaError_t launch_synth<double>(const void*, int, int, const double*, int, void*, cudaStream_t);
 template cudaError_t launch_synth<float>(const void*, int, int, const double*, int, void*, cudaStream_t);
 
+// =====================================================================================
+// Order sweeps on the FP64 tensor cores.
+//
+// For many orders the synthesis is the GEMM  Q[a][e] = sum_kk C[a][kk] V[kk][e]  with
+// kk = (k, +/-): C = a_k(alpha) / b_k(alpha), V = P_k(e) / conj(P_k^T)(e). One CTA owns an 8x8
+// sub-square of tile (I,J) plus its transposed partner in tile (J,I) (64 + 64 positions, e =
+// position x re/im = 256 columns) for up to 64 orders (rows), and streams the cached powers at
+// those positions (each cache element is staged by exactly one CTA, so the cache crosses HBM
+// once per launch, not once per order chunk). 8 warps: warp w owns the 32 e-columns
+// [32w, 32w+32) for all 64 orders: per K4 step 8 coefficient fragments + 4 cache fragments feed
+// 32 DMMAs. Coefficients are staged per chunk of 64 powers ([a][kk], padded), cache values
+// through a 3-stage cp.async ring of 8 powers; outputs leave through shared memory so stores
+// are 128-byte runs. Rounding differs from the exact scalar path (DMMA accumulation): the result
+// matches it to ~1e-16 relative instead of bit-for-bit.
+// =====================================================================================
+
+constexpr int kSwA = 64, kSwKc = 64, kSwStK = 8, kSwStages = 3;
+constexpr int kSwCLd = 2 * kSwKc + 4;  // doubles per coefficient row
+constexpr int kSwPLd = 66;             // complex per (power, tile) staging row
+
+size_t synth_sweep_smem_bytes() {
+    const size_t cs = (size_t)kSwA * kSwCLd * 8;
+    const size_t st = (size_t)kSwStages * kSwStK * 2 * kSwPLd * 16;
+    const size_t os = (size_t)kSwA * 66 * 16;
+    return (cs + st) > os ? cs + st : os;
+}
+
+__global__ void __launch_bounds__(256, 1)
+synth_sweep_mma_kernel(const double2* __restrict__ slabs, int n, int l_used, int64_t slab_elems,
+                       const double* __restrict__ coef, int coef_ld, int lc, int n_alpha,
+                       double2* __restrict__ out, int64_t out_stride, int nt) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* cs = reinterpret_cast<double*>(smem);
+    double2* stb = reinterpret_cast<double2*>(smem + (size_t)kSwA * kSwCLd * 8);
+    double2* os = reinterpret_cast<double2*>(smem);  // epilogue reuse
+
+    const int pair = blockIdx.x >> 4, sq = blockIdx.x & 15;
+    int I, J;
+    pair_of(pair, I, J);
+    const bool diag = (I == J);
+    const int sr = sq & 3, sc = sq >> 2;
+    if (diag && sr > sc) return;  // covered by the transposed sub-square
+    const int r0 = 8 * sr, c0 = 8 * sc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int tw = warp >> 2, pbase = 16 * (warp & 3);
+    const int64_t b1 = tile_base(I, J, nt), b2 = tile_base(J, I, nt);
+
+    double d[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+
+    for (int k0 = 1; k0 <= l_used; k0 += kSwKc) {
+        const int kc = min(kSwKc, l_used - k0 + 1);
+        const int nsteps = (kc + kSwStK - 1) / kSwStK;
+        __syncthreads();  // previous chunk finished with cs / stb
+        for (int idx = tid; idx < kSwA * 2 * kSwKc; idx += 256) {
+            const int a = idx / (2 * kSwKc), kk = idx % (2 * kSwKc);
+            const int k = k0 + (kk >> 1);
+            double v = 0.0;
+            if (a < n_alpha && (kk >> 1) < kc) v = coef[(size_t)a * coef_ld + lc + ((kk & 1) ? -k : k)];
+            cs[a * kSwCLd + kk] = v;
+        }
+        // stage st: powers k0 + 8 st + kp at the 64 + 64 positions (p = jj*8 + ii)
+        auto stage = [&](int st, int buf) {
+            double2* dst0 = stb + (size_t)buf * kSwStK * 2 * kSwPLd;
+            for (int idx = tid; idx < kSwStK * 2 * 64; idx += 256) {
+                const int kp = idx >> 7, t = (idx >> 6) & 1, p = idx & 63;
+                const int ii = p & 7, jj = p >> 3;
+                const int kq = 8 * st + kp;
+                const bool v = kq < kc;
+                const double2* slab = slabs + (int64_t)(k0 + (v ? kq : 0) - 1) * slab_elems;
+                const double2* src = t == 0 ? slab + b1 + swz(r0 + ii, c0 + jj) : slab + b2 + swz(c0 + jj, r0 + ii);
+                cp_async16(dst0 + (kp * 2 + t) * kSwPLd + p, src, v);
+            }
+        };
+#pragma unroll
+        for (int s = 0; s < kSwStages - 1; ++s) {
+            if (s < nsteps) stage(s, s);
+            cp_async_commit();
+        }
+        for (int st = 0; st < nsteps; ++st) {
+            cp_async_wait<kSwStages - 2>();
+            __syncthreads();
+            if (st + kSwStages - 1 < nsteps) stage(st + kSwStages - 1, (st + kSwStages - 1) % kSwStages);
+            cp_async_commit();
+            const double* sb = reinterpret_cast<const double*>(stb + (size_t)(st % kSwStages) * kSwStK * 2 * kSwPLd);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const int kkl = 4 * ks + t4;          // power term within the stage
+                const int kp = kkl >> 1, sign = kkl & 1;
+                double b[4];
+                const int tt = sign ? 1 - tw : tw;
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) {
+                    const int p = pbase + 4 * nb + (g >> 1), comp = g & 1;
+                    const double v = sb[((kp * 2 + tt) * kSwPLd + p) * 2 + comp];
+                    b[nb] = (sign && comp) ? -v : v;
+                }
+                const double* crow = cs + g * kSwCLd + 16 * st + kkl;
+#pragma unroll
+                for (int mb = 0; mb < 8; ++mb) {
+                    const double a = crow[8 * mb * kSwCLd];
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) dmma884(d[mb][nb][0], d[mb][nb][1], a, b[nb]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+
+    // Epilogue: identity term c_0 on the global diagonal, then coalesced stores via smem.
+    for (int t = 0; t < 2; ++t) {
+        if (t == 1 && diag && sr == sc) break;
+        __syncthreads();
+        if (tw == t) {
+#pragma unroll
+            for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) {
+                    const int a = 8 * mb + g;
+                    const int p = pbase + 4 * nb + t4;
+                    const int ii = p & 7, jj = p >> 3;
+                    double re = d[mb][nb][0];
+                    if (t == 0 && diag && sr == sc && ii == jj && a < n_alpha)
+                        re += coef[(size_t)a * coef_ld + lc];
+                    // t = 0: column-major over (ii fast); t = 1: transposed so writes stay contiguous
+                    const int q = t == 0 ? p : ii * 8 + jj;
+                    os[a * 66 + q] = make_double2(re, d[mb][nb][1]);
+                }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < kSwA * 64; idx += 256) {
+            const int a = idx >> 6, q = idx & 63;
+            if (a >= n_alpha) break;
+            const int hi = q >> 3, lo = q & 7;
+            int row, col;
+            if (t == 0) {  // q = jj*8 + ii: rows r0+ii of column c0+jj in tile (I,J)
+                row = I * 32 + r0 + lo;
+                col = J * 32 + c0 + hi;
+            } else {       // q = ii*8 + jj: rows c0+jj of column r0+ii in tile (J,I)
+                row = J * 32 + c0 + lo;
+                col = I * 32 + r0 + hi;
+            }
+            if (row < n && col < n) out[(int64_t)a * out_stride + (int64_t)col * n + row] = os[a * 66 + q];
+        }
+    }
+}
+
+int synth_sweep_max_orders() { return kSwA; }
+
+// n_alpha <= 64. coef: device [n_alpha][2*l_used+1].
+cudaError_t launch_synth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                               cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int npairs = nt * (nt + 1) / 2;
+    const size_t smem = synth_sweep_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(synth_sweep_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    synth_sweep_mma_kernel<<<(unsigned)npairs * 16, 256, smem, stream>>>(
+        (const double2*)slabs, n, l_used, (int64_t)nt * nt * kTileElems, coef_dev, 2 * l_used + 1, l_used, n_alpha,
+        (double2*)out, (int64_t)n * n, nt);
+    return cudaGetLastError();
+}
+
 }  // namespace fgb

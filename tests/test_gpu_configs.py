@@ -60,9 +60,11 @@ def test_config2_sweep_matches_oracle():
     n, b = cfg.x.shape
     o = O.PowerCache(cfg.f, cfg.l)
     g = fg.PowerCache(cfg.f, cfg.l, powers=o.slabs)
-    qs = fg.synthesize(g, cfg.alphas)
+    qs = fg.synthesize(g, cfg.alphas)  # 64-order sweep: DMMA kernel
     for i in (0, 7, 31, 40, 63):
-        assert np.array_equal(qs[i], O.fgfrft_matrix(o, float(cfg.alphas[i]), nthreads=8))
+        assert rel(qs[i], O.fgfrft_matrix(o, float(cfg.alphas[i]), nthreads=8)) <= 1e-14
+    for a in (float(cfg.alphas[7]), float(cfg.alphas[40])):  # single order: exact scalar kernel
+        assert np.array_equal(fg.synthesize(g, [a])[0], O.fgfrft_matrix(o, a, nthreads=8))
     loss, dl, y = fg.mse_step(g, cfg.alphas, cfg.x, cfg.x_clean, want_y=True)
     for i in range(0, 64, 9):
         a = float(cfg.alphas[i])

@@ -79,12 +79,19 @@ def test_synthesis_bit_exact(n, l):
 
 
 def test_synthesis_truncation_and_sweep_chunks():
+    """>= 8 orders take the DMMA sweep kernel: ~1e-16 relative (DMMA accumulation order), and
+    integer orders stay exact (0 * p = 0, 1 * p = p)."""
     f = prep.random_unitary(70, 3)
     o = O.PowerCache(f, 16)
     g = fg.PowerCache(f, 16, powers=o.slabs)
     alphas = list(np.linspace(0, 2, 11))
     for t in (1, 5, 16):
-        for a, q in zip(alphas, fg.synthesize(g, alphas, truncation=t)):
+        qs = fg.synthesize(g, alphas, truncation=t)
+        for a, q in zip(alphas, qs):
+            assert rel(q, O.fgfrft_matrix(o, a, t)) <= 1e-14
+        assert np.array_equal(qs[0], np.eye(70)) and np.array_equal(qs[5], O.fgfrft_matrix(o, 1.0, t))
+    for t in (1, 16):
+        for a, q in zip(alphas[:3], fg.synthesize(g, alphas[:3], truncation=t)):  # scalar path: bit-exact
             assert np.array_equal(q, O.fgfrft_matrix(o, a, t))
     with pytest.raises(fg.ParameterError):
         fg.synthesize(g, [0.5], truncation=17)
@@ -212,6 +219,24 @@ def test_cpp_dropin_header_suite():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.parametrize("n,l,n_alpha", [(40, 5, 8), (97, 70, 67), (256, 64, 64), (33, 130, 9)])
+def test_synthesis_sweep_dmma_path(n, l, n_alpha):
+    """DMMA sweep synthesis (several power chunks, > 64 orders, ragged n) vs the oracle; DQ too."""
+    f = prep.random_unitary(n, 900 + n)
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l, powers=o.slabs)
+    alphas = list(np.linspace(-2.2, 2.3, n_alpha))
+    qs = fg.synthesize(g, alphas)
+    dqs = fg.synthesize(g, alphas, which=fg.DQ)
+    for i in range(0, n_alpha, max(1, n_alpha // 9)):
+        assert rel(qs[i], O.fgfrft_matrix(o, alphas[i])) <= 1e-14
+        assert rel(dqs[i], O.fgfrft_grad(o, alphas[i])) <= 1e-13
+    # conjugate symmetry across the sweep: Q(-a) = Q(a)^H to 1e-14 elementwise
+    sym = fg.synthesize(g, [-a for a in alphas[:8]])
+    for i in range(8):
+        assert np.abs(sym[i] - qs[i].conj().T).max() <= 1e-14
 
 
 @pytest.mark.parametrize("n,l,n_alpha,b", [(90, 9, 8, 17), (150, 70, 67, 5), (33, 3, 64, 40)])
