@@ -177,6 +177,36 @@ int fgfrft_mse_step_dev(fgfrft_cache* cache, const double* alphas, int n_alpha,
                         const void* x_dev, const void* xc_dev, int64_t b, void* y_dev,
                         void* loss_dev, void* dlda_dev);
 
+/* ---- row-slab shards for multi-GPU -------------------------------------
+ *
+ * A shard owns output rows R = [row_begin, row_end) (row_begin % 32 == 0; row_end % 32 == 0
+ * or row_end == n) and stores the row panels P_k[R,:] and column panels P_k[:,R], k = 1..l
+ * (the rows of F^k and of F^{-k}), built on device from the replicated F. Everything below is
+ * local to the shard; the caller combines ranks with one all-reduce of the 2l+1 partials (and
+ * the loss) and one gather of the rows. Budget: 2*l*rows*n*16 bytes. The handle type is
+ * fgfrft_cache; the non-shard entry points reject it (and vice versa).
+ * Row blocks are column-major with leading dimension rows = row_end - row_begin.
+ */
+int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, int64_t row_end,
+                        uint64_t memory_budget, int device, fgfrft_cache** out);
+int fgfrft_shard_destroy(fgfrft_cache* shard);
+int fgfrft_shard_info(const fgfrft_cache* shard, int64_t* n, int* l, int64_t* row_begin,
+                      int64_t* row_end, uint64_t* fingerprint);
+int fgfrft_shard_set_stream(fgfrft_cache* shard, void* stream);
+/* Q(alpha_a)[R,:] (or dQ) for n_alpha orders: out_dev = n_alpha blocks of rows x n. */
+int fgfrft_shard_synthesize_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, int which,
+                                void* out_dev);
+/* Y[R,:] = Q(alpha_a)[R,:] X; x_dev n x b (replicated), y_dev n_alpha blocks of rows x b. */
+int fgfrft_shard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
+                           const void* x_dev, int64_t b, void* y_dev);
+/* Per order: loss_partial[a] = ||Y[R,:] - Xc[R,:]||^2 (unnormalised), s_partial[a][k+l] =
+ * Re<G[R,:], (F^k X)[R,:]> with G = 2 (Y - Xc) / (n b). xc_rows_dev: rows x b. y_rows_dev may be
+ * NULL. All outputs are device arrays. Sum both over ranks; then loss = sum / (n b) and
+ * dL/dalpha = sum_k c'_k s_k. */
+int fgfrft_shard_mse_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
+                                 const void* x_dev, const void* xc_rows_dev, int64_t b,
+                                 void* y_rows_dev, void* loss_partial_dev, void* s_partial_dev);
+
 #ifdef __cplusplus
 }
 #endif

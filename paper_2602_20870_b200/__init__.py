@@ -89,6 +89,13 @@ def lib() -> ctypes.CDLL:
         "fgfrft_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
         "fgfrft_mse_step": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
         "fgfrft_mse_step_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
+        "fgfrft_shard_create": (i, [vp, i64, i, i64, i64, u64, i, pp]),
+        "fgfrft_shard_destroy": (i, [vp]),
+        "fgfrft_shard_info": (i, [vp, vp, vp, vp, vp, vp]),
+        "fgfrft_shard_set_stream": (i, [vp, vp]),
+        "fgfrft_shard_synthesize_dev": (i, [vp, vp, i, i, vp]),
+        "fgfrft_shard_apply_dev": (i, [vp, vp, i, vp, i64, vp]),
+        "fgfrft_shard_mse_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -106,7 +113,9 @@ def exported_symbols():
         "fgfrft_cache_power", "fgfrft_cache_verify", "fgfrft_cache_set_stream", "fgfrft_cache_device_slab",
         "fgfrft_cache_device_bytes", "fgfrft_synthesize", "fgfrft_synthesize_dev", "fgfrft_apply",
         "fgfrft_apply_dev", "fgfrft_apply_matrix", "fgfrft_dlda", "fgfrft_dlda_dev", "fgfrft_mse_step",
-        "fgfrft_mse_step_dev",
+        "fgfrft_mse_step_dev", "fgfrft_shard_create", "fgfrft_shard_destroy", "fgfrft_shard_info",
+        "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
+        "fgfrft_shard_mse_partial_dev",
     ]
 
 

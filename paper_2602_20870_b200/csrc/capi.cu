@@ -31,6 +31,12 @@ cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coe
 cudaError_t launch_synth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
                                cudaStream_t stream);
 int synth_sweep_max_orders();
+cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream);
+cudaError_t launch_synth_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l_used,
+                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream);
+cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l, const void* m,
+                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream);
+size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
 cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
                          int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
                          bool accumulate, cudaStream_t stream);
@@ -182,6 +188,11 @@ struct fgfrft_cache {
     std::mutex mu;
     // workspaces
     DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda, tmp;
+    // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
+    bool shard = false;
+    int64_t r0 = 0, r1 = 0;
+    void* colp = nullptr;
+    size_t panel_elems = 0;
     double* coef_h = nullptr;  // pinned staging for the coefficient tables
     size_t coef_h_cap = 0;
     cudaEvent_t coef_evt = nullptr;
@@ -199,6 +210,13 @@ namespace {
 
 int check_handle(const fgfrft_cache* c) {
     if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_cache handle");
+    if (c->shard) return fail(FGFRFT_PARAMETER, "row-shard handle: use the fgfrft_shard_* entry points");
+    return FGFRFT_OK;
+}
+
+int check_shard(const fgfrft_cache* c) {
+    if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_shard handle");
+    if (!c->shard) return fail(FGFRFT_PARAMETER, "not a row-shard handle");
     return FGFRFT_OK;
 }
 
@@ -338,6 +356,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
     if (c->slabs) cudaFree(c->slabs);
+    if (c->colp) cudaFree(c->colp);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -851,6 +870,246 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
     FGB_CUDA(cudaStreamSynchronize(c->stream));
     std::memcpy(loss, out.data(), n_alpha * sizeof(double));
     std::memcpy(dlda, out.data() + n_alpha, n_alpha * sizeof(double));
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+// ---------------------------------------------------------------------------- row shards
+
+int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, int64_t row_end, uint64_t memory_budget,
+                        int device, fgfrft_cache** out) {
+    FGB_GUARD_BEGIN
+    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
+    *out = nullptr;
+    if (l < 1) return fail(FGFRFT_PARAMETER, "PowerCache: truncation order must be >= 1");
+    if (n < 1 || !f) return fail(FGFRFT_PARAMETER, "PowerCache: matrix must be non-empty");
+    if (row_begin < 0 || row_end > n || row_begin >= row_end || row_begin % kTile != 0 ||
+        (row_end % kTile != 0 && row_end != n))
+        return fail(FGFRFT_PARAMETER, "shard rows must be [r0, r1) with r0 % 32 == 0 and r1 % 32 == 0 or r1 == n");
+    const int64_t rows = row_end - row_begin;
+    const unsigned __int128 bytes = (unsigned __int128)2 * l * (uint64_t)rows * (uint64_t)n * 16;
+    if (bytes > memory_budget) {
+        std::ostringstream msg;
+        msg << "PowerCache shard: " << l << " row and column panels of " << rows << "x" << n << " need "
+            << (unsigned long long)bytes << " bytes, over the " << memory_budget << "-byte budget";
+        return fail(FGFRFT_CAPACITY, msg.str());
+    }
+    int ndev = 0;
+    FGB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(FGFRFT_PARAMETER, "device index out of range");
+    DeviceGuard dg(device);
+    auto* c = new fgfrft_cache();
+    c->n = n;
+    c->l = l;
+    c->device = device;
+    c->shard = true;
+    c->r0 = row_begin;
+    c->r1 = row_end;
+    c->fingerprint = host_fnv1a64(f, (size_t)n * (size_t)n * 16);
+    const int nI = (int)ceil_div(rows, kTile), nt = (int)ceil_div(n, kTile);
+    c->panel_elems = (size_t)nI * nt * kTileElems;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    c->stream = c->own_stream;
+    const size_t pbytes = c->panel_elems * 16 * (size_t)l;
+    if (cudaMalloc(&c->slabs, pbytes) != cudaSuccess || cudaMalloc(&c->colp, pbytes) != cudaSuccess) {
+        cudaGetLastError();
+        destroy_cache(c);
+        return fail(FGFRFT_CAPACITY, "PowerCache shard: device allocation failed");
+    }
+    // Build: Rp_1 = F[R,:], Cp_1 = F[:,R]; Rp_k = Rp_{k-1} F, Cp_k = F Cp_{k-1} (column-major scratch).
+    int rc = FGFRFT_OK;
+    do {
+        const size_t ml = (size_t)n * n, pl = (size_t)rows * n;
+        if (c->tmp.ensure((ml + 4 * pl) * 16) != cudaSuccess) {
+            rc = fail(FGFRFT_CAPACITY, "PowerCache shard: scratch allocation failed");
+            break;
+        }
+        double2* fb = c->tmp.as<double2>();
+        double2 *rp = fb + ml, *rq = rp + pl, *cp = rq + pl, *cq = cp + pl;
+        if (cudaMemcpyAsync(fb, f, ml * 16, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
+            cudaMemcpy2DAsync(rp, rows * 16, fb + row_begin, n * 16, rows * 16, n, cudaMemcpyDeviceToDevice,
+                              c->stream) != cudaSuccess ||
+            cudaMemcpyAsync(cp, fb + (size_t)row_begin * n, pl * 16, cudaMemcpyDeviceToDevice, c->stream) !=
+                cudaSuccess) {
+            rc = fail(FGFRFT_CUDA, "PowerCache shard: staging copies failed");
+            break;
+        }
+        for (int k = 1; k <= l && rc == FGFRFT_OK; ++k) {
+            if (k > 1) {
+                if (launch_zgemm((int)rows, (int)n, (int)n, rp, rows, 0, false, fb, n, 0, false, rq, rows, 0, 1, false,
+                                 c->stream) != cudaSuccess ||
+                    launch_zgemm((int)n, (int)rows, (int)n, fb, n, 0, false, cp, n, 0, false, cq, n, 0, 1, false,
+                                 c->stream) != cudaSuccess) {
+                    rc = fail(FGFRFT_CUDA, "PowerCache shard: panel GEMM failed");
+                    break;
+                }
+                std::swap(rp, rq);
+                std::swap(cp, cq);
+                g_launches += 2;
+            }
+            if (launch_rect_to_tiled(rp, rows, (int)rows, (int)n,
+                                     static_cast<double2*>(c->slabs) + (size_t)(k - 1) * c->panel_elems,
+                                     c->stream) != cudaSuccess ||
+                launch_rect_to_tiled(cp, n, (int)n, (int)rows,
+                                     static_cast<double2*>(c->colp) + (size_t)(k - 1) * c->panel_elems,
+                                     c->stream) != cudaSuccess) {
+                rc = fail(FGFRFT_CUDA, "PowerCache shard: tiling failed");
+                break;
+            }
+            g_launches += 2;
+        }
+        if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
+            rc = fail(FGFRFT_CUDA, "PowerCache shard: build failed");
+    } while (false);
+    c->tmp.release();
+    if (rc != FGFRFT_OK) {
+        destroy_cache(c);
+        return rc;
+    }
+    *out = c;
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_shard_destroy(fgfrft_cache* c) {
+    FGB_GUARD_BEGIN
+    if (c && !c->shard) return fail(FGFRFT_PARAMETER, "not a row-shard handle");
+    destroy_cache(c);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_shard_info(const fgfrft_cache* c, int64_t* n, int* l, int64_t* row_begin, int64_t* row_end,
+                      uint64_t* fingerprint) {
+    if (int st = check_shard(c)) return st;
+    if (n) *n = c->n;
+    if (l) *l = c->l;
+    if (row_begin) *row_begin = c->r0;
+    if (row_end) *row_end = c->r1;
+    if (fingerprint) *fingerprint = c->fingerprint;
+    return FGFRFT_OK;
+}
+
+int fgfrft_shard_set_stream(fgfrft_cache* c, void* stream) {
+    if (int st = check_shard(c)) return st;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    return FGFRFT_OK;
+}
+
+int fgfrft_shard_synthesize_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int which, void* out_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_shard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (which != FGFRFT_Q && which != FGFRFT_DQ) return fail(FGFRFT_PARAMETER, "which must be FGFRFT_Q or FGFRFT_DQ");
+    if (!out_dev) return fail(FGFRFT_PARAMETER, "null output");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
+    const double* table = which == FGFRFT_Q ? coef : coef + (size_t)n_alpha * (2 * c->l + 1);
+    ProfScope ps(KC_SYNTH, c->stream);
+    FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, (int)c->n, (int)c->r0, (int)(c->r1 - c->r0), c->l, table, n_alpha,
+                                 out_dev, c->stream),
+               1);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_shard_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, int64_t b,
+                           void* y_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_shard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
+    if (b == 0) return FGFRFT_OK;
+    if (!x_dev || !y_dev) return fail(FGFRFT_PARAMETER, "null signal buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    const int n = (int)c->n, rows = (int)(c->r1 - c->r0);
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
+    const size_t width = (size_t)(2 * c->l + 1), qs = (size_t)rows * n;
+    const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)4 << 30) / (qs * 16))));
+    FGB_CUDA(c->q.ensure((size_t)chunk * qs * 16));
+    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
+        const int na = std::min(chunk, n_alpha - a0);
+        {
+            ProfScope ps(KC_SYNTH, c->stream);
+            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, c->l, coef + a0 * width, na, c->q.p,
+                                         c->stream),
+                       1);
+        }
+        ProfScope ps(KC_GEMM, c->stream);
+        FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false,
+                                static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, (int64_t)rows * b, na,
+                                false, c->stream),
+                   1);
+    }
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
+                                 const void* xc_rows_dev, int64_t b, void* y_rows_dev, void* loss_partial_dev,
+                                 void* s_partial_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_shard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
+    if (!x_dev || !xc_rows_dev || !loss_partial_dev || !s_partial_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    const int n = (int)c->n, rows = (int)(c->r1 - c->r0), l = c->l;
+    const size_t width = (size_t)(2 * l + 1), qs = (size_t)rows * n, blk = (size_t)rows * b;
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
+    const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)2 << 30) / (qs * 16))));
+    FGB_CUDA(c->q.ensure((size_t)chunk * qs * 16));
+    FGB_CUDA(c->m.ensure((size_t)chunk * qs * 16));
+    FGB_CUDA(c->g.ensure((size_t)chunk * blk * 16));
+    FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
+    FGB_CUDA(c->partial.ensure(dots_rows_partial_elems(n, rows, l, chunk) * sizeof(double)));
+    if (!y_rows_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * 16));
+    const double norm = 1.0 / ((double)n * (double)b);
+    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
+        const int na = std::min(chunk, n_alpha - a0);
+        double2* ya = y_rows_dev ? static_cast<double2*>(y_rows_dev) + (size_t)a0 * blk : c->y.as<double2>();
+        {
+            ProfScope ps(KC_SYNTH, c->stream);
+            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, coef + a0 * width, na, c->q.p,
+                                         c->stream),
+                       1);
+        }
+        {
+            ProfScope ps(KC_GEMM, c->stream);
+            FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false, ya, rows,
+                                    (int64_t)blk, na, false, c->stream),
+                       1);
+        }
+        {
+            ProfScope ps(KC_ELEMWISE, c->stream);
+            FGB_LAUNCH(launch_mse_residual(ya, xc_rows_dev, (int64_t)blk, na, 2.0 * norm, 1.0, c->g.p,
+                                           c->lpart.as<double>(), static_cast<double*>(loss_partial_dev) + a0,
+                                           c->stream),
+                       2);
+        }
+        {
+            ProfScope ps(KC_GEMM, c->stream);  // M[R,:] = G[R,:] X^H
+            FGB_LAUNCH(launch_zgemm(rows, n, (int)b, c->g.p, rows, (int64_t)blk, false, x_dev, n, 0, true, c->m.p, rows,
+                                    (int64_t)qs, na, false, c->stream),
+                       1);
+        }
+        ProfScope ps(KC_DOTS, c->stream);
+        FGB_LAUNCH(launch_dots_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, c->m.p, (int64_t)qs, na,
+                                    c->partial.as<double>(), static_cast<double*>(s_partial_dev) + a0 * width,
+                                    c->stream),
+                   2);
+    }
     return FGFRFT_OK;
     FGB_GUARD_END
 }

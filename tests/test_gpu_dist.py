@@ -1,0 +1,82 @@
+"""Row-slab shard kernels on one GPU: two shards of the same F (ranks emulated SEQUENTIALLY in
+one process -- no kernel waits on another) must combine to the unsharded results: summed
+partials = full loss / s_k, concatenated rows = full F^a and F^a X."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2602_20870_b200 as fg
+import prep
+from paper_2602_20870_b200 import dist as fgd
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("n,l,world,n_alpha", [(100, 7, 2, 3), (256, 32, 3, 5), (64, 4, 2, 1), (96, 6, 4, 2)])
+def test_shards_combine_to_unsharded(n, l, world, n_alpha):
+    f = prep.random_unitary(n, 40 + n)
+    o = O.PowerCache(f, l)
+    rng = np.random.default_rng(n)
+    b = 9
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    alphas = list(np.linspace(-0.8, 1.9, n_alpha))
+    plan = fgd.plan_rows(n, world)
+    loss = np.zeros(n_alpha)
+    s = np.zeros((n_alpha, 2 * l + 1))
+    y_rows, q_rows = [], []
+    for r0, r1 in plan:
+        if r1 == r0:
+            continue
+        sh = fgd.CudaShard(f, l, r0, r1)
+        lp, sp, _ = sh.mse_partial(alphas, x, xc[r0:r1])
+        loss += lp.cpu().numpy()
+        s += sp.cpu().numpy()
+        y_rows.append(sh.apply_rows(alphas, x).cpu().numpy().transpose(0, 2, 1))
+        q_rows.append(sh.synthesize_rows(alphas).cpu().numpy().transpose(0, 2, 1))
+        sh.close()
+    y = np.concatenate(y_rows, axis=1)
+    q = np.concatenate(q_rows, axis=1)
+    for i, a in enumerate(alphas):
+        qr = O.fgfrft_matrix(o, a)
+        assert rel(q[i], qr) <= 1e-12
+        assert rel(y[i], qr @ x) <= 1e-12
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert loss[i] / (n * b) == pytest.approx(lr, rel=1e-12)
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (qr @ x - xc) / (n * b)) @ x.conj().T)
+        assert np.abs(s[i] - s_ref).max() <= 1e-10 * np.abs(s_ref).sum()
+        assert abs(float(np.dot(dc, s[i])) - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+def test_shard_validation():
+    f = prep.random_unitary(64, 1)
+    with pytest.raises(fg.ParameterError):
+        fgd.CudaShard(f, 3, 10, 40)      # not tile aligned
+    with pytest.raises(fg.CapacityError):
+        fgd.CudaShard(f, 3, 0, 32, memory_budget=1024)
+    sh = fgd.CudaShard(f, 3, 32, 64)
+    h = sh._h
+    with pytest.raises(fg.ParameterError):  # a shard is not a full cache handle
+        fg._check(fg.lib().fgfrft_cache_power(h, 1, np.zeros((64, 64), complex).ctypes.data))
+    sh.close()
+
+
+def test_sharded_step_wrapper_single_rank():
+    """ShardedFGFRFT with world 1 (no process group): same numbers as the unsharded mse_step."""
+    cfg = prep.config1()
+    sh = fgd.CudaShard(cfg.f, cfg.l, 0, cfg.n)
+    w = fgd.ShardedFGFRFT(sh, cfg.n, cfg.l)
+    xc = cfg.x + 0.05
+    loss, dl = w.mse_step(cfg.alphas, cfg.x, xc)
+    g = fg.PowerCache(cfg.f, cfg.l)
+    l2, d2, _ = fg.mse_step(g, cfg.alphas, cfg.x, xc)
+    assert loss[0] == pytest.approx(l2[0], rel=1e-12)
+    assert dl[0] == pytest.approx(d2[0], rel=1e-9, abs=1e-14)
+    y = w.apply(cfg.alphas, cfg.x)
+    assert rel(y[0], fg.apply_series(g, cfg.alphas, cfg.x)[0]) <= 1e-13
