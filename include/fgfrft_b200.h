@@ -110,7 +110,8 @@ int fgfrft_cache_power(fgfrft_cache* cache, int k, double* out);
 /* transform.hpp:136-139: NUMERICAL if fnv1a64(f) != stored fingerprint. */
 int fgfrft_cache_verify(const fgfrft_cache* cache, const double* f);
 
-/* Stream for subsequent calls on this handle (cudaStream_t as void*; NULL = handle's own). */
+/* Stream for subsequent calls on this handle (cudaStream_t as void*; NULL = the CUDA default
+ * stream, as everywhere in CUDA). A new handle uses its own non-blocking stream. */
 int fgfrft_cache_set_stream(fgfrft_cache* cache, void* stream);
 
 /* Device pointer to slab k-1 (= F^k) and the device memory held by the handle. */
@@ -206,6 +207,27 @@ int fgfrft_shard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alph
 int fgfrft_shard_mse_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
                                  const void* x_dev, const void* xc_rows_dev, int64_t b,
                                  void* y_rows_dev, void* loss_partial_dev, void* s_partial_dev);
+
+/* ---- batches of small graphs (BASELINE config 5: fractional specformer) ----------------
+ *
+ * `graphs` independent GFT matrices (n <= 64, complex128 host input, graph-major), powers
+ * 1..l stored per graph in complex64 (built in complex128 on DMMA, then demoted). One CTA per
+ * graph. All step-time buffers are device arrays: alphas_dev [graphs][heads] (learnable orders
+ * live on the GPU; their sinc coefficients are evaluated on the device), x_dev
+ * [graphs][ch][n] complex64 (= per graph an n x ch column-major block), y_dev / g_dev
+ * [graphs][heads][ch][n] complex64, dlda_dev [graphs][heads] double.
+ *   forward:  Y_gh = Q(alpha_gh; F_g) X_g
+ *   dlda:     dL/dalpha_gh = sum_k c'_k(alpha_gh) Re<G_gh, F_g^k X_g>  (G = dL/dconj(Y) convention)
+ * heads 1..4, ch 1..64.
+ */
+int fgfrft_batch_create(const double* fs, int64_t graphs, int64_t n, int l, int device,
+                        fgfrft_cache** out);
+int fgfrft_batch_destroy(fgfrft_cache* batch);
+int fgfrft_batch_set_stream(fgfrft_cache* batch, void* stream);
+int fgfrft_batch_forward_dev(fgfrft_cache* batch, const double* alphas_dev, int heads,
+                             const void* x_dev, int64_t ch, void* y_dev);
+int fgfrft_batch_dlda_dev(fgfrft_cache* batch, const double* alphas_dev, int heads,
+                          const void* g_dev, const void* x_dev, int64_t ch, void* dlda_dev);
 
 #ifdef __cplusplus
 }

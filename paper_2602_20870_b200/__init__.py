@@ -96,6 +96,11 @@ def lib() -> ctypes.CDLL:
         "fgfrft_shard_synthesize_dev": (i, [vp, vp, i, i, vp]),
         "fgfrft_shard_apply_dev": (i, [vp, vp, i, vp, i64, vp]),
         "fgfrft_shard_mse_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
+        "fgfrft_batch_create": (i, [vp, i64, i64, i, i, pp]),
+        "fgfrft_batch_destroy": (i, [vp]),
+        "fgfrft_batch_set_stream": (i, [vp, vp]),
+        "fgfrft_batch_forward_dev": (i, [vp, vp, i, vp, i64, vp]),
+        "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -115,7 +120,8 @@ def exported_symbols():
         "fgfrft_apply_dev", "fgfrft_apply_matrix", "fgfrft_dlda", "fgfrft_dlda_dev", "fgfrft_mse_step",
         "fgfrft_mse_step_dev", "fgfrft_shard_create", "fgfrft_shard_destroy", "fgfrft_shard_info",
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
-        "fgfrft_shard_mse_partial_dev",
+        "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
+        "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev",
     ]
 
 
@@ -352,3 +358,47 @@ def mse_step(cache: PowerCache, alphas, x: np.ndarray, x_clean: np.ndarray, want
     _check(lib().fgfrft_mse_step(cache.handle, _ptr(al), len(al), _ptr(xc), _ptr(xcl), b,
                                  _ptr(y) if want_y else None, _ptr(loss), _ptr(dl)))
     return loss, dl, (np.transpose(y, (0, 2, 1)) if want_y else None)
+
+
+class GraphBatch:
+    """Config-5 shape: many independent small graphs (n <= 64), complex64, H orders per graph.
+    Device buffers are torch tensors; forward/dlda are stream-ordered with torch's current stream."""
+
+    def __init__(self, fs: np.ndarray, l: int, device: int = 0):
+        import torch
+        self.torch = torch
+        fs = np.ascontiguousarray(np.asarray(fs, dtype=np.complex128).transpose(0, 2, 1))  # column-major slabs
+        self.graphs, self.n = fs.shape[0], fs.shape[1]
+        self.l, self.device = int(l), device
+        self._h = ctypes.c_void_p()
+        _check(lib().fgfrft_batch_create(fs.ctypes.data, self.graphs, self.n, self.l, device, ctypes.byref(self._h)))
+        _check(lib().fgfrft_batch_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)))
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().fgfrft_batch_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, alphas, x):
+        """alphas: [G, H] float64 tensor (device); x: [G, C, n] complex64 tensor (device).
+        Returns y [G, H, C, n] complex64 (y[g, h] is the column-major n x C block)."""
+        t = self.torch
+        G, H = alphas.shape
+        C = x.shape[1]
+        y = t.empty((G, H, C, self.n), dtype=t.complex64, device=x.device)
+        _check(lib().fgfrft_batch_forward_dev(self._h, alphas.data_ptr(), H, x.data_ptr(), C, y.data_ptr()))
+        return y
+
+    def dlda(self, alphas, g, x):
+        t = self.torch
+        G, H = alphas.shape
+        out = t.empty((G, H), dtype=t.float64, device=x.device)
+        _check(lib().fgfrft_batch_dlda_dev(self._h, alphas.data_ptr(), H, g.data_ptr(), x.data_ptr(), x.shape[1],
+                                           out.data_ptr()))
+        return out

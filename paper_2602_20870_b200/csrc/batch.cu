@@ -1,0 +1,382 @@
+// batch.cu -- K5: many small graphs at once (BASELINE config 5, the fractional-specformer shape:
+// 4096 independent graphs, n <= 64, L = 16, H learnable orders per graph, C channels, complex64).
+//
+// One CTA per graph. Forward: the graph's L powers (tiled + swizzled, 32 KB each for n = 64)
+// stream through a 4-stage TMA ring while 512 threads accumulate Q_h = c_0 I + sum_k a_hk P_k +
+// b_hk P_k^H for all H heads in registers (each thread owns 8 elements x H heads; both P_ij and
+// P_ji come from the same staged tile); Q_h then moves to shared memory and Y_h = Q_h X_g runs on
+// the FP32 FFMA pipes from shared memory. Backward (dL/dalpha per graph and head): M_h = G_h X^H
+// in registers (same element ownership), then one more pass over the powers forms
+// s_hk = Re<M_h, P_k>, Re<M_h, P_k^H> with a transposing warp reduction, and
+// dL/dalpha_h = sum_k c'_k s_hk. Coefficients for the 4096 x H orders are evaluated on the device
+// (double precision, the sinc.hpp formulas; differences from glibc are ~1 ulp, far inside the
+// complex64 tolerance), so a step has no host-side O(graphs x heads x L) work.
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace fgb {
+
+constexpr int kBN = 64;          // padded graph size (2 x 2 tiles)
+constexpr int kBTh = 512;        // threads per graph CTA
+constexpr int kBStages = 4;
+constexpr int kBMaxHeads = 4;
+constexpr int kBMaxCh = 64;
+constexpr int kBSlab = 4 * kTileElems;  // elements per padded slab
+
+// ---------------------------------------------------------------- device sinc (sinc.hpp:15-36)
+__device__ __forceinline__ double dsinc(double x) {
+    if (x == nearbyint(x)) return x == 0.0 ? 1.0 : 0.0;
+    if (fabs(x) < 1e-6) {
+        const double px = CUDART_PI * x;
+        return 1.0 - px * px / 6.0;
+    }
+    return sin(CUDART_PI * x) / (CUDART_PI * x);
+}
+__device__ __forceinline__ double dsinc_deriv(double x) {
+    if (x == nearbyint(x)) {
+        if (x == 0.0) return 0.0;
+        const long long k = (long long)x;
+        return (k % 2 == 0 ? 1.0 : -1.0) / x;
+    }
+    if (fabs(x) < 1e-6) {
+        const double pi2 = CUDART_PI * CUDART_PI;
+        return -pi2 * x / 3.0 + pi2 * pi2 * x * x * x / 30.0;
+    }
+    const double px = CUDART_PI * x;
+    return cos(px) / x - sin(px) / (CUDART_PI * x * x);
+}
+
+// coef[o][2][2l+1] (c then dc) for every order o.
+__global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_orders, int l, double* __restrict__ coef) {
+    const int w = 2 * l + 1;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_orders * w) return;
+    const int o = idx / w, t = idx % w;
+    const double x = alphas[o] - (double)(t - l);
+    coef[(size_t)o * 2 * w + t] = dsinc(x);
+    coef[(size_t)o * 2 * w + w + t] = dsinc_deriv(x);
+}
+
+// [G] column-major n x n complex128 (stride n*n) -> [G][slab k] tiled complex64 padded to 64.
+__global__ void __launch_bounds__(256) batch_to_tiled_kernel(const double2* __restrict__ src, int n, int l, int k,
+                                                             float2* __restrict__ dst) {
+    const int g = blockIdx.y, tile = blockIdx.x;  // tile = I + 2*J
+    const int I = tile & 1, J = tile >> 1;
+    const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double2* s = src + (int64_t)g * n * n;
+    float2* t = dst + ((int64_t)g * l + (k - 1)) * kBSlab + (int64_t)tile * kTileElems;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = w + 8 * i, row = I * 32 + r, col = J * 32 + c;
+        float2 v = make_float2(0.f, 0.f);
+        if (row < n && col < n) {
+            const double2 x = s[(int64_t)col * n + row];
+            v = make_float2((float)x.x, (float)x.y);
+        }
+        t[swz(r, c)] = v;
+    }
+}
+
+// element (i, j) of a padded 64 x 64 tiled slab
+__device__ __forceinline__ int bidx(int i, int j) { return ((j >> 5) * 2 + (i >> 5)) * kTileElems + swz(i & 31, j & 31); }
+
+struct BatchSmem {
+    // region A: TMA stages during the power passes, then Q_h / G_h; then X; then the mbarriers
+    // and the per-power reduction table red[(l+1) x 16 warps x 8].
+    static constexpr size_t kA = (size_t)kBStages * kBSlab * 8;          // 128 KB
+    static constexpr size_t kX = (size_t)kBN * kBMaxCh * 8;              // 32 KB
+    static size_t bytes(int l) { return kA + kX + kBStages * 8 + (size_t)(l + 1) * 16 * 8 * 8 + 64; }
+};
+
+size_t batch_smem_bytes(int l) { return BatchSmem::bytes(l); }
+
+template <int H>
+__global__ void __launch_bounds__(kBTh, 1)
+batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
+                     const float2* __restrict__ x, int ch, float2* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float2* regA = reinterpret_cast<float2*>(smem);
+    float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
+    const int g = blockIdx.x, tid = threadIdx.x;
+    const int w = 2 * l + 1;
+    const float2* gs = slabs + (int64_t)g * l * kBSlab;
+    if (tid == 0) {
+        for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    // X_g (n x ch, column-major) -> xs[c * 64 + j], zero padded
+    for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
+        const int j = idx & 63, c = idx >> 6;
+        xs[idx] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    const uint32_t bytes = kBSlab * 8;
+    auto issue = [&](int k, int s) {
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < kBStages && s < l; ++s) issue(s + 1, s);
+    // element ownership: e = tid + 512 u -> i = e & 63 (= tid & 63), j = (tid >> 6) + 8 u
+    const int i = tid & 63, j0 = tid >> 6;
+    float2 q[8][H];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const float c0 = (float)coef[(size_t)(g * H + h) * 2 * w + l];
+            q[u][h] = make_float2((i == j0 + 8 * u) ? c0 : 0.f, 0.f);
+        }
+    for (int k = 1; k <= l; ++k) {
+        const int s = (k - 1) % kBStages;
+        mbar_wait(&full[s], ((k - 1) / kBStages) & 1);
+        const float2* t = regA + (size_t)s * kBSlab;
+        float a[H], b[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            a[h] = (float)coef[(size_t)(g * H + h) * 2 * w + l + k];
+            b[h] = (float)coef[(size_t)(g * H + h) * 2 * w + l - k];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 8 * u;
+            const float2 p = t[bidx(i, j)], pt = t[bidx(j, i)];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                q[u][h].x = fmaf(a[h], p.x, fmaf(b[h], pt.x, q[u][h].x));
+                q[u][h].y = fmaf(a[h], p.y, fmaf(-b[h], pt.y, q[u][h].y));
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && k + kBStages <= l) issue(k + kBStages, s);
+    }
+    // Q_h -> region A as column-major 64 x 64: qs[h][j * 64 + i]
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int h = 0; h < H; ++h) regA[(size_t)h * kBN * kBN + (j0 + 8 * u) * kBN + i] = q[u][h];
+    __syncthreads();
+    // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: thread -> rows 4*ib..4*ib+3, cols 2*cb, 2*cb+1
+    const int ib = tid & 15, cb = tid >> 4;
+    float acc[H][4][2][2];
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) acc[h][r][c][0] = acc[h][r][c][1] = 0.f;
+    for (int j = 0; j < kBN; ++j) {
+        const float2 x0 = xs[(2 * cb) * kBN + j], x1 = xs[(2 * cb + 1) * kBN + j];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const float4* qp = reinterpret_cast<const float4*>(regA + (size_t)h * kBN * kBN + j * kBN + 4 * ib);
+            const float4 v0 = qp[0], v1 = qp[1];
+            const float2 qv[4] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
+                                  make_float2(v1.z, v1.w)};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                acc[h][r][0][0] = fmaf(qv[r].x, x0.x, fmaf(-qv[r].y, x0.y, acc[h][r][0][0]));
+                acc[h][r][0][1] = fmaf(qv[r].x, x0.y, fmaf(qv[r].y, x0.x, acc[h][r][0][1]));
+                acc[h][r][1][0] = fmaf(qv[r].x, x1.x, fmaf(-qv[r].y, x1.y, acc[h][r][1][0]));
+                acc[h][r][1][1] = fmaf(qv[r].x, x1.y, fmaf(qv[r].y, x1.x, acc[h][r][1][1]));
+            }
+        }
+    }
+    // y[g][h] : n x ch column-major
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int col = 2 * cb + c;
+            if (col >= ch) continue;
+            float2* yo = y + (((int64_t)g * H + h) * ch + col) * n;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int row = 4 * ib + r;
+                if (row < n) yo[row] = make_float2(acc[h][r][c][0], acc[h][r][c][1]);
+            }
+        }
+}
+
+template <int H>
+__global__ void __launch_bounds__(kBTh, 1)
+batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
+                  const float2* __restrict__ gcot, const float2* __restrict__ x, int ch, double* __restrict__ dlda) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float2* regA = reinterpret_cast<float2*>(smem);
+    float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
+    double* red = reinterpret_cast<double*>(full + kBStages);  // [k 0..l][warp 16][8]
+    const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int w = 2 * l + 1;
+    const float2* gs = slabs + (int64_t)g * l * kBSlab;
+    if (tid == 0) {
+        for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    // stage X (xs[c*64 + j]) and G_h (regA[h][c*64 + i]), zero padded
+    for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
+        const int r = idx & 63, c = idx >> 6;
+        const bool v = r < n && c < ch;
+        xs[idx] = v ? x[((int64_t)g * ch + c) * n + r] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+            regA[(size_t)h * kBN * kBMaxCh + idx] =
+                v ? gcot[(((int64_t)g * H + h) * ch + c) * n + r] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    // M_h[i, j] = sum_c G_h[i, c] conj(X[j, c]) for the thread's 8 elements
+    const int i = tid & 63, j0 = tid >> 6;
+    float2 m[8][H];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int h = 0; h < H; ++h) m[u][h] = make_float2(0.f, 0.f);
+    for (int c = 0; c < kBMaxCh; ++c) {
+        float2 gv[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) gv[h] = regA[(size_t)h * kBN * kBMaxCh + c * kBN + i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float2 xv = xs[c * kBN + j0 + 8 * u];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {  // g * conj(x)
+                m[u][h].x = fmaf(gv[h].x, xv.x, fmaf(gv[h].y, xv.y, m[u][h].x));
+                m[u][h].y = fmaf(gv[h].y, xv.x, fmaf(-gv[h].x, xv.y, m[u][h].y));
+            }
+        }
+    }
+    __syncthreads();  // region A is reused for the power stages
+    const uint32_t bytes = kBSlab * 8;
+    auto issue = [&](int k, int s) {
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < kBStages && s < l; ++s) issue(s + 1, s);
+    // s_0 = Re tr(M_h)
+    {
+        double v[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) v[h] = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+                if (i == j0 + 8 * u) v[h] += (double)m[u][h].x;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            double t = v[h];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) red[(0 * 16 + warp) * 8 + h] = t;
+        }
+    }
+    for (int k = 1; k <= l; ++k) {
+        const int s = (k - 1) % kBStages;
+        mbar_wait(&full[s], ((k - 1) / kBStages) & 1);
+        const float2* t = regA + (size_t)s * kBSlab;
+        double v[8];  // [h][+/-] packed as 2h + sign
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 8 * u;
+            const float2 p = t[bidx(i, j)], pt = t[bidx(j, i)];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                v[2 * h] += (double)fmaf(m[u][h].x, p.x, m[u][h].y * p.y);
+                v[2 * h + 1] += (double)fmaf(m[u][h].x, pt.x, -m[u][h].y * pt.y);
+            }
+        }
+        // transposing warp reduction of 8 values: lane q (< 8) ends with the sum of value q
+#pragma unroll
+        for (int o = 4, half = 4; o >= 1; o >>= 1, half >>= 1) {
+            const bool hi = (lane & o) != 0;
+#pragma unroll
+            for (int q = 0; q < half; ++q) {
+                const double send = hi ? v[q] : v[q + half];
+                const double keep = hi ? v[q + half] : v[q];
+                v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 8);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+        if (lane < 8) red[(k * 16 + warp) * 8 + lane] = v[0];
+        __syncthreads();
+        if (tid == 0 && k + kBStages <= l) issue(k + kBStages, s);
+    }
+    __syncthreads();
+    if (tid < H) {
+        const int h = tid;
+        const double* dc = coef + (size_t)(g * H + h) * 2 * w + w;
+        double acc = 0.0;
+        for (int kk = 0; kk < w; ++kk) {  // ascending k = -l..l
+            const int k = kk - l;
+            const int idx = k == 0 ? 2 * h : (k > 0 ? 2 * h : 2 * h + 1);
+            const int kr = k >= 0 ? k : -k;
+            double sk = 0.0;
+            for (int wp = 0; wp < 16; ++wp) sk += red[(kr * 16 + wp) * 8 + (k == 0 ? h : idx)];
+            acc += dc[kk] * sk;
+        }
+        dlda[(int64_t)g * H + h] = acc;
+    }
+}
+
+cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream) {
+    const int total = n_orders * (2 * l + 1);
+    batch_coef_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, stream>>>(alphas_dev, n_orders, l, coef_dev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream) {
+    batch_to_tiled_kernel<<<dim3(4, graphs), 256, 0, stream>>>((const double2*)src, n, l, k, (float2*)dst);
+    return cudaGetLastError();
+}
+
+#define FGB_BATCH_HEADS(MACRO) \
+    switch (heads) {           \
+        case 1: MACRO(1); break; \
+        case 2: MACRO(2); break; \
+        case 3: MACRO(3); break; \
+        default: MACRO(4); break; \
+    }
+
+cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
+                                 const void* x, int ch, void* y, cudaStream_t stream) {
+    const size_t smem = batch_smem_bytes(l);
+#define FGB_BF(HV)                                                                                             \
+    {                                                                                                          \
+        auto kern = batch_forward_kernel<HV>;                                                                  \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+        if (e != cudaSuccess) return e;                                                                        \
+        kern<<<graphs, kBTh, smem, stream>>>((const float2*)slabs, n, l, coef, (const float2*)x, ch, (float2*)y); \
+    }
+    FGB_BATCH_HEADS(FGB_BF)
+#undef FGB_BF
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
+                              const void* gcot, const void* x, int ch, double* dlda, cudaStream_t stream) {
+    const size_t smem = batch_smem_bytes(l);
+#define FGB_BD(HV)                                                                                            \
+    {                                                                                                         \
+        auto kern = batch_dlda_kernel<HV>;                                                                    \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+        if (e != cudaSuccess) return e;                                                                       \
+        kern<<<graphs, kBTh, smem, stream>>>((const float2*)slabs, n, l, coef, (const float2*)gcot,           \
+                                             (const float2*)x, ch, dlda);                                     \
+    }
+    FGB_BATCH_HEADS(FGB_BD)
+#undef FGB_BD
+    return cudaGetLastError();
+}
+
+int batch_max_heads() { return kBMaxHeads; }
+int batch_max_channels() { return kBMaxCh; }
+int batch_max_n() { return kBN; }
+
+}  // namespace fgb

@@ -37,18 +37,32 @@ cudaError_t launch_synth_rows(const void* rowp, const void* colp, int n, int r0,
 cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l, const void* m,
                              int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream);
 size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
+cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream);
+cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream);
+cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
+                                 const void* x, int ch, void* y, cudaStream_t stream);
+cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
+                              const void* gcot, const void* x, int ch, double* dlda, cudaStream_t stream);
+int batch_max_heads();
+int batch_max_channels();
+int batch_max_n();
 cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
                          int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
                          bool accumulate, cudaStream_t stream);
 cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
-                              double* partial, double* s_out, cudaStream_t stream);
+                              double* partial, double* s_out, cudaStream_t stream, int elem_bytes);
+cudaError_t launch_cgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
+                         int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
+                         bool accumulate, cudaStream_t stream);
+cudaError_t launch_promote(const void* src, void* dst, int64_t count, cudaStream_t stream);
 size_t dots_partial_elems(int n, int l, int n_alpha);
 size_t dots_mma_partial_elems(int n);
 int dots_mma_max_orders();
 cudaError_t launch_power_dots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
                                   double* partial, double* s_out, cudaStream_t stream, int* launches);
 cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, int n_alpha, double g_scale,
-                                double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream);
+                                double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream,
+                                int elem_bytes);
 size_t mse_partial_elems(int n_alpha);
 cudaError_t launch_demote(const void* src, void* dst, int64_t count, cudaStream_t stream);
 cudaError_t launch_to_tiled(const void* src, void* dst, int n, int elem_bytes_dst, cudaStream_t stream);
@@ -190,6 +204,7 @@ struct fgfrft_cache {
     DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda, tmp;
     // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
     bool shard = false;
+    int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
     int64_t r0 = 0, r1 = 0;
     void* colp = nullptr;
     size_t panel_elems = 0;
@@ -211,12 +226,19 @@ namespace {
 int check_handle(const fgfrft_cache* c) {
     if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_cache handle");
     if (c->shard) return fail(FGFRFT_PARAMETER, "row-shard handle: use the fgfrft_shard_* entry points");
+    if (c->graphs > 0) return fail(FGFRFT_PARAMETER, "graph-batch handle: use the fgfrft_batch_* entry points");
+    return FGFRFT_OK;
+}
+
+int check_batch(const fgfrft_cache* c) {
+    if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_batch handle");
+    if (c->graphs <= 0) return fail(FGFRFT_PARAMETER, "not a graph-batch handle");
     return FGFRFT_OK;
 }
 
 int check_shard(const fgfrft_cache* c) {
     if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_shard handle");
-    if (!c->shard) return fail(FGFRFT_PARAMETER, "not a row-shard handle");
+    if (!c->shard || c->graphs > 0) return fail(FGFRFT_PARAMETER, "not a row-shard handle");
     return FGFRFT_OK;
 }
 
@@ -289,11 +311,6 @@ int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used,
     return FGFRFT_OK;
 }
 
-int require_c128(const fgfrft_cache* c, const char* what) {
-    if (c->dtype != FGFRFT_C128)
-        return fail(FGFRFT_PARAMETER, std::string(what) + ": complex64 caches support synthesis only in this build");
-    return FGFRFT_OK;
-}
 
 int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype, int device, fgfrft_cache** out,
                   fgfrft_cache** made) {
@@ -349,7 +366,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (!c) return;
     DeviceGuard dg(c->device);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
-    if (c->stream && c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
+    if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
                       &c->loss, &c->dlda, &c->tmp})
         b->release();
@@ -418,6 +435,39 @@ int resolve_truncation(const fgfrft_cache* c, int truncation, int which, int* l_
     return FGFRFT_OK;
 }
 
+// Complex GEMM in the cache's arithmetic: DMMA complex128 or FP32 complex64.
+cudaError_t gemm(const fgfrft_cache* c, int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a,
+                 const void* B, int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch) {
+    if (c->dtype == FGFRFT_C128)
+        return launch_zgemm(M, N, K, A, lda, sA, conj_a, B, ldb, sB, conj_b, C, ldc, sC, batch, false, c->stream);
+    return launch_cgemm(M, N, K, A, lda, sA, conj_a, B, ldb, sB, conj_b, C, ldc, sC, batch, false, c->stream);
+}
+
+// Host complex128 block -> device buffer of the cache dtype (complex64: staged + demoted).
+int upload_signal(fgfrft_cache* c, const double* host, size_t elems, void* dst) {
+    if (c->dtype == FGFRFT_C128) {
+        FGB_CUDA(cudaMemcpyAsync(dst, host, elems * 16, cudaMemcpyHostToDevice, c->stream));
+        return FGFRFT_OK;
+    }
+    FGB_CUDA(c->tmp.ensure(elems * 16));
+    FGB_CUDA(cudaMemcpyAsync(c->tmp.p, host, elems * 16, cudaMemcpyHostToDevice, c->stream));
+    FGB_LAUNCH(launch_demote(c->tmp.p, dst, (int64_t)elems, c->stream), 1);
+    return FGFRFT_OK;
+}
+
+// Device buffer of the cache dtype -> host complex128 (synchronises the stream).
+int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host) {
+    if (c->dtype == FGFRFT_C128) {
+        FGB_CUDA(cudaMemcpyAsync(host, src, elems * 16, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        FGB_CUDA(c->tmp.ensure(elems * 16));
+        FGB_LAUNCH(launch_promote(src, c->tmp.p, (int64_t)elems, c->stream), 1);
+        FGB_CUDA(cudaMemcpyAsync(host, c->tmp.p, elems * 16, cudaMemcpyDeviceToHost, c->stream));
+    }
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    return FGFRFT_OK;
+}
+
 // Y[a] = op(Q(alpha_a)) X for all orders; x_dev n x b, y_dev n_alpha blocks of n x b.
 int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used, bool inverse, const void* x_dev,
                  int64_t b, void* y_dev) {
@@ -426,15 +476,14 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
     const int chunk = alpha_chunk(c, n_alpha);
-    FGB_CUDA(c->q.ensure((size_t)chunk * sl * 16));
+    FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
     const size_t width = (size_t)(2 * l_used + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p)) return st;
         ProfScope ps(KC_GEMM, c->stream);
-        FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, inverse, x_dev, n, 0, false,
-                                static_cast<double2*>(y_dev) + (size_t)a0 * n * b, n, (int64_t)n * b, na, false,
-                                c->stream),
+        FGB_LAUNCH(gemm(c, n, (int)b, n, c->q.p, n, (int64_t)sl, inverse, x_dev, n, 0, false,
+                        static_cast<char*>(y_dev) + (size_t)a0 * n * b * c->elem, n, (int64_t)n * b, na),
                    1);
     }
     return FGFRFT_OK;
@@ -446,9 +495,9 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
 int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
-    const bool mma = n_alpha >= 8;
+    const bool mma = n_alpha >= 8 && c->dtype == FGFRFT_C128;
     const int chunk = mma ? std::min(alpha_chunk(c, n_alpha), dots_mma_max_orders()) : alpha_chunk(c, n_alpha);
-    FGB_CUDA(c->m.ensure((size_t)chunk * sl * 16));
+    FGB_CUDA(c->m.ensure((size_t)chunk * sl * c->elem));
     FGB_CUDA(c->partial.ensure(std::max(mma ? dots_mma_partial_elems(n) : 0, dots_partial_elems(n, c->l, chunk)) *
                                sizeof(double)));
     const size_t width = (size_t)(2 * c->l + 1);
@@ -457,9 +506,8 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
         // M_a = G_a X^H  (n x n, K = b)
         {
             ProfScope ps(KC_GEMM, c->stream);
-            FGB_LAUNCH(launch_zgemm(n, n, (int)b, static_cast<const double2*>(g_dev) + (size_t)a0 * n * b, n,
-                                    (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na, false,
-                                    c->stream),
+            FGB_LAUNCH(gemm(c, n, n, (int)b, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->elem, n,
+                            (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na),
                        1);
         }
         ProfScope ps(KC_DOTS, c->stream);
@@ -470,7 +518,7 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
             g_launches += nl;
         } else {
             FGB_LAUNCH(launch_power_dots(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
-                                         s_dev + a0 * width, c->stream),
+                                         s_dev + a0 * width, c->stream, (int)c->elem),
                        2);
         }
     }
@@ -601,7 +649,7 @@ int fgfrft_cache_verify(const fgfrft_cache* c, const double* f) {
 int fgfrft_cache_set_stream(fgfrft_cache* c, void* stream) {
     if (int st = check_handle(c)) return st;
     std::lock_guard<std::mutex> lk(c->mu);
-    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
     return FGFRFT_OK;
 }
 
@@ -657,7 +705,6 @@ int fgfrft_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int tru
                      const void* x_dev, int64_t b, void* y_dev) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
-    if (int st = require_c128(c, "fgfrft_apply")) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
     int l_used = 0;
@@ -674,7 +721,6 @@ int fgfrft_apply(fgfrft_cache* c, const double* alphas, int n_alpha, int truncat
                  int64_t b, double* y) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
-    if (int st = require_c128(c, "fgfrft_apply")) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
     int l_used = 0;
@@ -683,14 +729,12 @@ int fgfrft_apply(fgfrft_cache* c, const double* alphas, int n_alpha, int truncat
     if (!x || !y) return fail(FGFRFT_PARAMETER, "null signal buffer");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
-    const size_t xb = (size_t)c->n * b * 16;
-    FGB_CUDA(c->x.ensure(xb));
-    FGB_CUDA(c->y.ensure(xb * n_alpha));
-    FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xb, cudaMemcpyHostToDevice, c->stream));
+    const size_t xe = (size_t)c->n * b;
+    FGB_CUDA(c->x.ensure(xe * c->elem));
+    FGB_CUDA(c->y.ensure(xe * c->elem * n_alpha));
+    if (int st = upload_signal(c, x, xe, c->x.p)) return st;
     if (int st = apply_device(c, alphas, n_alpha, l_used, inverse != 0, c->x.p, b, c->y.p)) return st;
-    FGB_CUDA(cudaMemcpyAsync(y, c->y.p, xb * n_alpha, cudaMemcpyDeviceToHost, c->stream));
-    FGB_CUDA(cudaStreamSynchronize(c->stream));
-    return FGFRFT_OK;
+    return download_signal(c, c->y.p, xe * n_alpha, y);
     FGB_GUARD_END
 }
 
@@ -739,7 +783,6 @@ int fgfrft_dlda_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const vo
                     int64_t b, double* s, double* dlda) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
-    if (int st = require_c128(c, "fgfrft_dlda")) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 0) return fail(FGFRFT_SHAPE, "negative signal count");
     if (!g_dev || !x_dev) return fail(FGFRFT_PARAMETER, "null buffer");
@@ -771,19 +814,18 @@ int fgfrft_dlda(fgfrft_cache* c, const double* alphas, int n_alpha, const double
                 double* s, double* dlda) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
-    if (int st = require_c128(c, "fgfrft_dlda")) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 0) return fail(FGFRFT_SHAPE, "negative signal count");
     if ((!g || !x) && b > 0) return fail(FGFRFT_PARAMETER, "null buffer");
     {
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
-        const size_t xb = (size_t)c->n * (b > 0 ? b : 1) * 16;
-        FGB_CUDA(c->x.ensure(xb));
-        FGB_CUDA(c->g.ensure(xb * n_alpha));
+        const size_t xe = (size_t)c->n * (b > 0 ? b : 1);
+        FGB_CUDA(c->x.ensure(xe * c->elem));
+        FGB_CUDA(c->g.ensure(xe * c->elem * n_alpha));
         if (b > 0) {
-            FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xb, cudaMemcpyHostToDevice, c->stream));
-            FGB_CUDA(cudaMemcpyAsync(c->g.p, g, xb * n_alpha, cudaMemcpyHostToDevice, c->stream));
+            if (int st = upload_signal(c, x, xe, c->x.p)) return st;
+            if (int st = upload_signal(c, g, xe * n_alpha, c->g.p)) return st;
         }
     }
     return fgfrft_dlda_dev(c, alphas, n_alpha, c->g.p, c->x.p, b, s, dlda);
@@ -794,7 +836,6 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
                         int64_t b, void* y_dev, void* loss_dev, void* dlda_dev) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
-    if (int st = require_c128(c, "fgfrft_mse_step")) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
     if (!x_dev || !xc_dev || !loss_dev || !dlda_dev) return fail(FGFRFT_PARAMETER, "null buffer");
@@ -809,26 +850,26 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     const double* dc_dev = coef + (size_t)n_alpha * width;
     const int chunk = alpha_chunk(c, n_alpha);
     const size_t sl = c->mat_elems();
-    FGB_CUDA(c->q.ensure((size_t)chunk * sl * 16));
-    FGB_CUDA(c->g.ensure((size_t)chunk * blk * 16));
+    FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
+    FGB_CUDA(c->g.ensure((size_t)chunk * blk * c->elem));
     FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
     FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
-    if (!y_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * 16));
+    if (!y_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * c->elem));
     const double norm = 1.0 / ((double)n * (double)b);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
-        double2* ya = y_dev ? static_cast<double2*>(y_dev) + (size_t)a0 * blk : c->y.as<double2>();
+        void* ya = y_dev ? static_cast<char*>(y_dev) + (size_t)a0 * blk * c->elem : c->y.p;
         if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p)) return st;
         {
             ProfScope ps(KC_GEMM, c->stream);
-            FGB_LAUNCH(launch_zgemm(n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n,
-                                    (int64_t)blk, na, false, c->stream),
+            FGB_LAUNCH(gemm(c, n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n, (int64_t)blk, na),
                        1);
         }
         {
             ProfScope ps(KC_ELEMWISE, c->stream);
             FGB_LAUNCH(launch_mse_residual(ya, xc_dev, (int64_t)blk, na, 2.0 * norm, norm, c->g.p,
-                                           c->lpart.as<double>(), static_cast<double*>(loss_dev) + a0, c->stream),
+                                           c->lpart.as<double>(), static_cast<double*>(loss_dev) + a0, c->stream,
+                                           (int)c->elem),
                        2);
         }
         if (int st = dots_device(c, na, c->g.p, x_dev, b, c->s.as<double>() + a0 * width)) return st;
@@ -844,20 +885,19 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
                     double* y, double* loss, double* dlda) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
-    if (int st = require_c128(c, "fgfrft_mse_step")) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
     if (!x || !xc || !loss || !dlda) return fail(FGFRFT_PARAMETER, "null buffer");
     {
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
-        const size_t xb = (size_t)c->n * b * 16;
-        FGB_CUDA(c->x.ensure(xb));
-        FGB_CUDA(c->xc.ensure(xb));
+        const size_t xe = (size_t)c->n * b;
+        FGB_CUDA(c->x.ensure(xe * c->elem));
+        FGB_CUDA(c->xc.ensure(xe * c->elem));
         FGB_CUDA(c->loss.ensure((size_t)n_alpha * 2 * sizeof(double)));
-        if (y) FGB_CUDA(c->y.ensure(xb * n_alpha));
-        FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xb, cudaMemcpyHostToDevice, c->stream));
-        FGB_CUDA(cudaMemcpyAsync(c->xc.p, xc, xb, cudaMemcpyHostToDevice, c->stream));
+        if (y) FGB_CUDA(c->y.ensure(xe * c->elem * n_alpha));
+        if (int st = upload_signal(c, x, xe, c->x.p)) return st;
+        if (int st = upload_signal(c, xc, xe, c->xc.p)) return st;
     }
     double* ld = c->loss.as<double>();
     if (int st = fgfrft_mse_step_dev(c, alphas, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha))
@@ -866,7 +906,9 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
     DeviceGuard dg(c->device);
     std::vector<double> out(2 * (size_t)n_alpha);
     FGB_CUDA(cudaMemcpyAsync(out.data(), ld, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (y) FGB_CUDA(cudaMemcpyAsync(y, c->y.p, (size_t)c->n * b * 16 * n_alpha, cudaMemcpyDeviceToHost, c->stream));
+    if (y) {
+        if (int st = download_signal(c, c->y.p, (size_t)c->n * b * n_alpha, y)) return st;
+    }
     FGB_CUDA(cudaStreamSynchronize(c->stream));
     std::memcpy(loss, out.data(), n_alpha * sizeof(double));
     std::memcpy(dlda, out.data() + n_alpha, n_alpha * sizeof(double));
@@ -997,7 +1039,7 @@ int fgfrft_shard_info(const fgfrft_cache* c, int64_t* n, int* l, int64_t* row_be
 int fgfrft_shard_set_stream(fgfrft_cache* c, void* stream) {
     if (int st = check_shard(c)) return st;
     std::lock_guard<std::mutex> lk(c->mu);
-    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
     return FGFRFT_OK;
 }
 
@@ -1095,7 +1137,7 @@ int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_al
             ProfScope ps(KC_ELEMWISE, c->stream);
             FGB_LAUNCH(launch_mse_residual(ya, xc_rows_dev, (int64_t)blk, na, 2.0 * norm, 1.0, c->g.p,
                                            c->lpart.as<double>(), static_cast<double*>(loss_partial_dev) + a0,
-                                           c->stream),
+                                           c->stream, 16),
                        2);
         }
         {
@@ -1110,6 +1152,148 @@ int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_al
                                     c->stream),
                    2);
     }
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+// ---------------------------------------------------------------------------- graph batches
+
+int fgfrft_batch_create(const double* fs, int64_t graphs, int64_t n, int l, int device, fgfrft_cache** out) {
+    FGB_GUARD_BEGIN
+    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
+    *out = nullptr;
+    if (l < 1) return fail(FGFRFT_PARAMETER, "PowerCache: truncation order must be >= 1");
+    if (graphs < 1 || graphs > 65535 || !fs) return fail(FGFRFT_PARAMETER, "graph batch: need 1..65535 graphs");
+    if (n < 1 || n > batch_max_n()) return fail(FGFRFT_PARAMETER, "graph batch: n must be in 1..64");
+    if (l > 255) return fail(FGFRFT_PARAMETER, "graph batch: l must be <= 255");
+    int ndev = 0;
+    FGB_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(FGFRFT_PARAMETER, "device index out of range");
+    DeviceGuard dg(device);
+    auto* c = new fgfrft_cache();
+    c->n = n;
+    c->l = l;
+    c->device = device;
+    c->dtype = FGFRFT_C64;
+    c->elem = 8;
+    c->graphs = graphs;
+    c->fingerprint = host_fnv1a64(fs, (size_t)graphs * n * n * 16);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    c->stream = c->own_stream;
+    const size_t slab = 4 * (size_t)kTileElems;  // padded 64 x 64
+    if (cudaMalloc(&c->slabs, (size_t)graphs * l * slab * 8) != cudaSuccess) {
+        cudaGetLastError();
+        destroy_cache(c);
+        return fail(FGFRFT_CAPACITY, "graph batch: device allocation failed");
+    }
+    int rc = FGFRFT_OK;
+    const size_t ml = (size_t)n * n;
+    do {
+        if (c->tmp.ensure(3 * graphs * ml * 16) != cudaSuccess) {
+            rc = fail(FGFRFT_CAPACITY, "graph batch: scratch allocation failed");
+            break;
+        }
+        double2* fb = c->tmp.as<double2>();
+        double2* prev = fb + graphs * ml;
+        double2* cur = prev + graphs * ml;
+        if (cudaMemcpyAsync(fb, fs, graphs * ml * 16, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+            rc = fail(FGFRFT_CUDA, "graph batch: upload failed");
+            break;
+        }
+        const double2* p = fb;
+        for (int k = 1; k <= l; ++k) {
+            if (k > 1) {  // P_k = F P_{k-1} for every graph (batched DMMA GEMM)
+                if (launch_zgemm((int)n, (int)n, (int)n, fb, n, (int64_t)ml, false, p, n, (int64_t)ml, false, cur, n,
+                                 (int64_t)ml, (int)graphs, false, c->stream) != cudaSuccess) {
+                    rc = fail(FGFRFT_CUDA, "graph batch: GEMM failed");
+                    break;
+                }
+                p = cur;
+                std::swap(prev, cur);
+                g_launches += 1;
+            }
+            if (launch_batch_to_tiled(p, (int)graphs, (int)n, l, k, c->slabs, c->stream) != cudaSuccess) {
+                rc = fail(FGFRFT_CUDA, "graph batch: tiling failed");
+                break;
+            }
+            g_launches += 1;
+        }
+        if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
+            rc = fail(FGFRFT_CUDA, "graph batch: build failed");
+    } while (false);
+    c->tmp.release();
+    if (rc != FGFRFT_OK) {
+        destroy_cache(c);
+        return rc;
+    }
+    *out = c;
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_batch_destroy(fgfrft_cache* c) {
+    FGB_GUARD_BEGIN
+    if (c && c->graphs <= 0) return fail(FGFRFT_PARAMETER, "not a graph-batch handle");
+    destroy_cache(c);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_batch_set_stream(fgfrft_cache* c, void* stream) {
+    if (int st = check_batch(c)) return st;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
+    return FGFRFT_OK;
+}
+
+namespace {
+int batch_coefs(fgfrft_cache* c, const double* alphas_dev, int heads, double** coef) {
+    const size_t orders = (size_t)c->graphs * heads;
+    FGB_CUDA(c->coef.ensure(orders * 2 * (2 * c->l + 1) * sizeof(double)));
+    FGB_LAUNCH(launch_batch_coef(alphas_dev, (int)orders, c->l, c->coef.as<double>(), c->stream), 1);
+    *coef = c->coef.as<double>();
+    return FGFRFT_OK;
+}
+}  // namespace
+
+int fgfrft_batch_forward_dev(fgfrft_cache* c, const double* alphas_dev, int heads, const void* x_dev, int64_t ch,
+                             void* y_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_batch(c)) return st;
+    if (heads < 1 || heads > batch_max_heads()) return fail(FGFRFT_PARAMETER, "graph batch: heads must be 1..4");
+    if (ch < 1 || ch > batch_max_channels()) return fail(FGFRFT_SHAPE, "graph batch: channels must be 1..64");
+    if (!alphas_dev || !x_dev || !y_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    double* coef = nullptr;
+    if (int st = batch_coefs(c, alphas_dev, heads, &coef)) return st;
+    ProfScope ps(KC_SYNTH, c->stream);
+    FGB_LAUNCH(launch_batch_forward(c->slabs, (int)c->graphs, (int)c->n, c->l, coef, heads, x_dev, (int)ch, y_dev,
+                                    c->stream),
+               1);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_batch_dlda_dev(fgfrft_cache* c, const double* alphas_dev, int heads, const void* g_dev, const void* x_dev,
+                          int64_t ch, void* dlda_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_batch(c)) return st;
+    if (heads < 1 || heads > batch_max_heads()) return fail(FGFRFT_PARAMETER, "graph batch: heads must be 1..4");
+    if (ch < 1 || ch > batch_max_channels()) return fail(FGFRFT_SHAPE, "graph batch: channels must be 1..64");
+    if (!alphas_dev || !g_dev || !x_dev || !dlda_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    double* coef = nullptr;
+    if (int st = batch_coefs(c, alphas_dev, heads, &coef)) return st;
+    ProfScope ps(KC_DOTS, c->stream);
+    FGB_LAUNCH(launch_batch_dlda(c->slabs, (int)c->graphs, (int)c->n, c->l, coef, heads, g_dev, x_dev, (int)ch,
+                                 static_cast<double*>(dlda_dev), c->stream),
+               1);
     return FGFRFT_OK;
     FGB_GUARD_END
 }

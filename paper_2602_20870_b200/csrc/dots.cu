@@ -15,8 +15,9 @@ namespace fgb {
 
 constexpr int kDotStages = 4, kDotThreads = 256;
 
-size_t dots_smem_bytes(int l, int ac) {
-    return (size_t)kDotStages * 2 * kTileElems * 16 + kDotStages * 8 + (size_t)l * 8 * ac * 2 * sizeof(double) + 16;
+size_t dots_smem_bytes(int l, int ac, int elem_bytes) {
+    return (size_t)kDotStages * 2 * kTileElems * elem_bytes + kDotStages * 8 + (size_t)l * 8 * ac * 2 * sizeof(double) +
+           16;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -27,15 +28,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // slabs: tiled layout (common.cuh). partial layout: [a][2l+1][pair] (pairs contiguous so the
 // fixed-order reduction over pairs is coalesced).
-template <int AC>
+__device__ __forceinline__ double2 to_d2(const double2& v) { return v; }
+__device__ __forceinline__ double2 to_d2(const float2& v) { return make_double2((double)v.x, (double)v.y); }
+
+template <typename R, int AC>
 __global__ void __launch_bounds__(kDotThreads, 1)
-power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_elems,
-                  const double2* __restrict__ m, int64_t m_stride, int n_alpha, int n_achunks,
+power_dots_kernel(const cplx_t<R>* __restrict__ slabs, int n, int l, int64_t slab_elems,
+                  const cplx_t<R>* __restrict__ m, int64_t m_stride, int n_alpha, int n_achunks,
                   double* __restrict__ partial, int nt, int npairs) {
+    using C = cplx_t<R>;
     constexpr int T = kTile, S = kDotStages;
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* tiles = reinterpret_cast<double2*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 16);
+    C* tiles = reinterpret_cast<C*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * sizeof(C));
     double* red = reinterpret_cast<double*>(full + S);  // [k-1][warp][a][2]
 
     const int chunk = blockIdx.x % n_achunks;
@@ -55,14 +60,14 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
     }
     __syncthreads();
 
-    const uint32_t tile_bytes = (uint32_t)(kTileElems * 16);
+    const uint32_t tile_bytes = (uint32_t)(kTileElems * sizeof(C));
     const bool stream_once = n_achunks == 1;
     const uint64_t pol = policy_evict_first();
     const int64_t off1 = tile_base(I, J, nt), off2 = tile_base(J, I, nt);
     auto issue = [&](int k, int s) {  // one thread: one bulk copy per 32x32 tile
         mbar_arrive_expect_tx(&full[s], (diag ? 1 : 2) * tile_bytes);
-        const double2* slab = slabs + (int64_t)(k - 1) * slab_elems;
-        double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        const C* slab = slabs + (int64_t)(k - 1) * slab_elems;
+        C* t1 = tiles + (size_t)(s * 2) * kTileElems;
         if (stream_once) {
             bulk_g2s_hint(t1, slab + off1, tile_bytes, &full[s], pol);
             if (!diag) bulk_g2s_hint(t1 + kTileElems, slab + off2, tile_bytes, &full[s], pol);
@@ -85,10 +90,10 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
         const bool v = r < bi && c < bj;
 #pragma unroll
         for (int a = 0; a < AC; ++a) {
-            const double2* ma = m + (int64_t)(a0 + (a < na ? a : 0)) * m_stride;
+            const C* ma = m + (int64_t)(a0 + (a < na ? a : 0)) * m_stride;
             const bool va = v && a < na;
-            m1[i][a] = va ? ma[(int64_t)(J * T + c) * n + I * T + r] : make_double2(0.0, 0.0);
-            m2[i][a] = (va && !diag) ? ma[(int64_t)(I * T + r) * n + J * T + c] : make_double2(0.0, 0.0);
+            m1[i][a] = va ? to_d2(ma[(int64_t)(J * T + c) * n + I * T + r]) : make_double2(0.0, 0.0);
+            m2[i][a] = (va && !diag) ? to_d2(ma[(int64_t)(I * T + r) * n + J * T + c]) : make_double2(0.0, 0.0);
             if (diag && r == c) s0[a] += m1[i][a].x;
         }
     }
@@ -108,13 +113,13 @@ power_dots_kernel(const double2* __restrict__ slabs, int n, int l, int64_t slab_
             if (k > l) break;
             const int s = (k - 1) % S;
             mbar_wait(&full[s], ((k - 1) / S) & 1);
-            const double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
-            const double2* t2 = diag ? t1 : t1 + kTileElems;
+            const C* t1 = tiles + (size_t)(s * 2) * kTileElems;
+            const C* t2 = diag ? t1 : t1 + kTileElems;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int c = warp + 8 * i;
-                const double2 p1 = t1[swz(r, c)];  // P[I*T + r, J*T + c]
-                const double2 p2 = t2[swz(c, r)];  // P[J*T + c, I*T + r]
+                const double2 p1 = to_d2(t1[swz(r, c)]);  // P[I*T + r, J*T + c]
+                const double2 p2 = to_d2(t2[swz(c, r)]);  // P[J*T + c, I*T + r]
 #pragma unroll
                 for (int a = 0; a < AC; ++a) {
                     double& sp = v[(g * AC + a) * 2 + 0];
@@ -192,24 +197,29 @@ size_t dots_partial_elems(int n, int l, int n_alpha) {
 }
 
 // s_out (device): [n_alpha][2l+1]; partial: device scratch of dots_partial_elems().
+// elem_bytes: 16 (complex128 cache and M) or 8 (complex64).
 cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
-                              double* partial, double* s_out, cudaStream_t stream) {
+                              double* partial, double* s_out, cudaStream_t stream, int elem_bytes) {
     const int nt = (int)ceil_div(n, kTile);
     const int npairs = nt * (nt + 1) / 2;
     const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
     const int nchunks = (int)ceil_div(n_alpha, ac);
-    const size_t smem = dots_smem_bytes(l, ac);
+    const size_t smem = dots_smem_bytes(l, ac, elem_bytes);
     const int64_t slab = (int64_t)nt * nt * kTileElems;
     const dim3 grid((unsigned)((int64_t)nchunks * npairs));
-#define FGB_DOTS_CASE(ACV)                                                                                   \
+#define FGB_DOTS_CASE(RT, ACV)                                                                               \
     {                                                                                                        \
-        auto kern = power_dots_kernel<ACV>;                                                                  \
+        auto kern = power_dots_kernel<RT, ACV>;                                                              \
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return e;                                                                      \
-        kern<<<grid, kDotThreads, smem, stream>>>((const double2*)slabs, n, l, slab, (const double2*)m,     \
-                                                  m_stride, n_alpha, nchunks, partial, nt, npairs);                  \
+        kern<<<grid, kDotThreads, smem, stream>>>((const cplx_t<RT>*)slabs, n, l, slab, (const cplx_t<RT>*)m, \
+                                                  m_stride, n_alpha, nchunks, partial, nt, npairs);          \
     }
-    if (ac == 4) FGB_DOTS_CASE(4) else if (ac == 2) FGB_DOTS_CASE(2) else FGB_DOTS_CASE(1)
+    if (elem_bytes == 16) {
+        if (ac == 4) FGB_DOTS_CASE(double, 4) else if (ac == 2) FGB_DOTS_CASE(double, 2) else FGB_DOTS_CASE(double, 1)
+    } else {
+        if (ac == 4) FGB_DOTS_CASE(float, 4) else if (ac == 2) FGB_DOTS_CASE(float, 2) else FGB_DOTS_CASE(float, 1)
+    }
 #undef FGB_DOTS_CASE
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -217,7 +227,6 @@ cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, in
     reduce_pairs_kernel<<<(unsigned)total, 128, 0, stream>>>(partial, npairs, s_out);
     return cudaGetLastError();
 }
-
 
 // =====================================================================================
 // Sweep variant on the FP64 tensor cores.

@@ -6,19 +6,22 @@ namespace fgb {
 
 constexpr int kResBlocks = 4 * FGFRFT_SMS;  // per order, fixed -> deterministic partition
 
-// For order a (blockIdx.y): R = Y_a - Xc, G_a = scale * R, loss partial per block = sum |R|^2.
+// For order a (blockIdx.y): R = Y_a - Xc, G_a = scale * R, loss partial per block = sum |R|^2
+// (accumulated in double for both element types).
+template <typename C>
 __global__ void __launch_bounds__(256)
-mse_residual_kernel(const double2* __restrict__ y, const double2* __restrict__ xc, int64_t count,
-                    double scale, double2* __restrict__ g, double* __restrict__ partial) {
+mse_residual_kernel(const C* __restrict__ y, const C* __restrict__ xc, int64_t count, double scale,
+                    C* __restrict__ g, double* __restrict__ partial) {
     const int a = blockIdx.y;
-    const double2* ya = y + (int64_t)a * count;
-    double2* ga = g + (int64_t)a * count;
+    const C* ya = y + (int64_t)a * count;
+    C* ga = g + (int64_t)a * count;
     double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 yv = ya[i], xv = xc[i];
-        const double rx = yv.x - xv.x, ry = yv.y - xv.y;
+        const C yv = ya[i], xv = xc[i];
+        const double rx = (double)yv.x - (double)xv.x, ry = (double)yv.y - (double)xv.y;
         acc = fma(rx, rx, fma(ry, ry, acc));
-        ga[i] = make_double2(scale * rx, scale * ry);
+        ga[i].x = scale * rx;
+        ga[i].y = scale * ry;
     }
     __shared__ double wsum[8];
 #pragma unroll
@@ -51,9 +54,13 @@ size_t mse_partial_elems(int n_alpha) { return (size_t)n_alpha * kResBlocks; }
 // loss_out[a] = ||Y_a - Xc||^2 * loss_scale ; g = g_scale (Y_a - Xc).
 cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, int n_alpha, double g_scale,
                                 double loss_scale, void* g, double* partial, double* loss_out,
-                                cudaStream_t stream) {
-    mse_residual_kernel<<<dim3(kResBlocks, n_alpha), 256, 0, stream>>>((const double2*)y, (const double2*)xc,
-                                                                      count, g_scale, (double2*)g, partial);
+                                cudaStream_t stream, int elem_bytes) {
+    if (elem_bytes == 16)
+        mse_residual_kernel<double2><<<dim3(kResBlocks, n_alpha), 256, 0, stream>>>(
+            (const double2*)y, (const double2*)xc, count, g_scale, (double2*)g, partial);
+    else
+        mse_residual_kernel<float2><<<dim3(kResBlocks, n_alpha), 256, 0, stream>>>(
+            (const float2*)y, (const float2*)xc, count, g_scale, (float2*)g, partial);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     sum_rows_kernel<<<n_alpha, 128, 0, stream>>>(partial, kResBlocks, loss_scale, loss_out);

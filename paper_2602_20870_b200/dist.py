@@ -67,6 +67,8 @@ class CudaShard(RankCompute):
                                          ctypes.byref(self._h)))
         self._lib = lib()
         self._check = _check
+        # order the shard's kernels with torch's work on this device (outputs are torch tensors)
+        self.set_stream(torch.cuda.current_stream(device).cuda_stream)
 
     def close(self):
         h, self._h = getattr(self, "_h", None), None

@@ -148,3 +148,26 @@ def test_config4_point_cloud_full_size():
         _sampled_checks(cfg, cache, cols=slice(0, 6), budget_cols=4)
     finally:
         cache.close()
+
+
+@pytest.mark.skipif(not HEAVY, reason="FGFRFT_SKIP_HEAVY=1")
+def test_config3_complex64_full_size():
+    """Config 3 in complex64 (8.6 GB cache): within 1e-4 of the fp64 checker on sampled columns."""
+    cfg = prep.config3()
+    a = float(cfg.alphas[0])
+    cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=16 << 30, dtype=fg.C64)
+    try:
+        x = np.asfortranarray(cfg.x[:, :16])
+        xc = np.asfortranarray(cfg.x_clean[:, :16])
+        y = fg.apply_series(cache, [a], x)[0]
+        yr = O.series_apply_recursive(cfg.f, a, cfg.l, x)
+        assert rel(y, yr) <= 1e-4
+        loss, dl, _ = fg.mse_step(cache, [a], x, xc)
+        r = yr - xc
+        nb = x.size
+        assert abs(loss[0] - float(np.vdot(r, r).real) / nb) <= 1e-4 * float(np.vdot(r, r).real) / nb
+        s_ref = O.power_dots_recursive(cfg.f, cfg.l, 2.0 * r / nb, x)
+        _, dc = O.sinc_coeffs(a, cfg.l)
+        assert abs(dl[0] - float(np.dot(dc, s_ref))) <= 1e-4 * float(np.sum(np.abs(dc * s_ref)))
+    finally:
+        cache.close()

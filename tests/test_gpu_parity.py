@@ -255,3 +255,36 @@ def test_dlda_sweep_dmma_path(n, l, n_alpha, b):
         assert np.abs(s[i] - s_ref).max() <= 1e-10 * np.abs(s_ref).sum()
         _, dc = O.sinc_coeffs(alphas[i], l)
         assert abs(dl[i] - float(np.dot(dc, s_ref))) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+# --------------------------------------------------------------------------- complex64 path
+
+@pytest.mark.parametrize("n,l,b", [(64, 8, 5), (150, 16, 33), (256, 32, 64)])
+def test_complex64_path_within_1e4_of_fp64_oracle(n, l, b):
+    """North star: the optional complex64 path within 1e-4 of the fp64 oracle. The c64 cache is
+    built in complex128 (DMMA) and demoted per power; synthesis, FP32 GEMM and the gradient
+    contraction run on complex64 data."""
+    f = prep.random_unitary(n, 70 + n)
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l, dtype=fg.C64)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    alphas = [0.37, -0.8, 1.0, 0.0]
+    for a, q in zip(alphas, fg.synthesize(g, alphas)):
+        assert rel(q, O.fgfrft_matrix(o, a)) <= 1e-4
+    ys = fg.apply_series(g, alphas, x)
+    yi = fg.apply_series(g, alphas, x, inverse=True)
+    loss, dl, _ = fg.mse_step(g, alphas, x, xc)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        assert rel(ys[i], q @ x) <= 1e-4
+        assert rel(yi[i], q.conj().T @ x) <= 1e-4
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert abs(loss[i] - lr) <= 1e-4 * lr
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
+        assert abs(dl[i] - dr) <= 1e-4 * np.sum(np.abs(dc * s_ref))
+    assert np.array_equal(fg.synthesize(g, [0.0])[0], np.eye(n))  # order 0 still exact
+    with pytest.raises(fg.ParameterError):
+        fg.PowerCache(prep.random_unitary(7, 1), 2, dtype=fg.C64)  # odd n: TMA alignment

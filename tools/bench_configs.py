@@ -37,27 +37,29 @@ def timed(stream, fn, reps=5, warm=3):
     return e0.elapsed_time(e1) / reps
 
 
-def run(name, cfg, peaks, budget):
+def run(name, cfg, peaks, budget, dtype=0):
     n, b, L = cfg.n, cfg.b, cfg.l
+    es = 16 if dtype == 0 else 8
+    ct = torch.complex128 if dtype == 0 else torch.complex64
     A = len(cfg.alphas)
     stream = torch.cuda.Stream()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cache = fg.PowerCache(cfg.f, L, memory_budget=budget)
+    cache = fg.PowerCache(cfg.f, L, memory_budget=budget, dtype=dtype)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     cache.set_stream(stream.cuda_stream)
     lib = fg.lib()
     al = np.ascontiguousarray(cfg.alphas, dtype=np.float64)
     one = al[:1].copy()
-    q = torch.empty((1, n, n), dtype=torch.complex128, device="cuda")
+    q = torch.empty((1, n, n), dtype=ct, device="cuda")
     t_syn = timed(stream, lambda: fg._check(lib.fgfrft_synthesize_dev(cache.handle, one.ctypes.data, 1, 0, 0,
                                                                        q.data_ptr())))
-    syn_bytes = (L + 1) * n * n * 16.0
+    syn_bytes = (L + 1) * n * n * float(es)
     del q
-    x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda()
-    xc = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda()
-    y = torch.empty((A, b, n), dtype=torch.complex128, device="cuda")
+    x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda().to(ct)
+    xc = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda().to(ct)
+    y = torch.empty((A, b, n), dtype=ct, device="cuda")
     t_app = timed(stream, lambda: fg._check(lib.fgfrft_apply_dev(cache.handle, al.ctypes.data, A, 0, 0, x.data_ptr(),
                                                                   b, y.data_ptr())))
     loss = torch.empty(A, dtype=torch.float64, device="cuda")
@@ -66,7 +68,8 @@ def run(name, cfg, peaks, budget):
                                                                       xc.data_ptr(), b, None, loss.data_ptr(),
                                                                       dl.data_ptr())))
     out = {
-        "config": name, "n": n, "l": L, "b": b, "orders": A, "cache_gb": L * n * n * 16 / 1e9,
+        "config": name, "dtype": "c128" if dtype == 0 else "c64", "n": n, "l": L, "b": b, "orders": A,
+        "cache_gb": L * n * n * es / 1e9,
         "cache_build": {"s": build_s, "tflops": (L - 1) * 8.0 * n ** 3 / build_s / 1e12},
         "synthesis_one_order": {"ms": t_syn, "gbs": syn_bytes / (t_syn * 1e-3) / 1e9,
                                 "frac_hbm": syn_bytes / (t_syn * 1e-3) / 1e9 / peaks["hbm"]},
@@ -76,6 +79,38 @@ def run(name, cfg, peaks, budget):
     }
     cache.close()
     return out
+
+
+def run_c5(peaks):
+    """C5: 4096 ER(64, 0.1) graphs, L=16, 4 orders per graph, 64 channels, complex64.
+    Step = forward Y_gh = F_g^{a_gh} X_g for all graphs/heads + dL/da_gh for a cotangent G."""
+    t0 = time.perf_counter()
+    fs, orders, feats, l = prep.config5()
+    prep_s = time.perf_counter() - t0
+    G, n, C = feats.shape
+    H = orders.shape[1]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    batch = fg.GraphBatch(fs, l)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    a_d = torch.from_numpy(orders).cuda()
+    x_d = torch.from_numpy(np.ascontiguousarray(feats.transpose(0, 2, 1)).astype(np.complex64)).cuda()
+    g_d = torch.randn((G, H, C, n), dtype=torch.complex64, device="cuda")
+    t_fwd = timed(stream, lambda: batch.forward(a_d, x_d))
+    t_bwd = timed(stream, lambda: batch.dlda(a_d, g_d, x_d))
+    nodes = G * H * n * C
+    # FP32 work: synthesis 8*L*n^2*H, apply 8*n^2*C*H, M = G X^H 8*n^2*C*H, dots 8*L*n^2*H (per graph)
+    flops = G * (8 * l * n * n * H * 2 + 8 * n * n * C * H * 2)
+    cache_bytes = G * l * 64 * 64 * 8
+    return {"config": "C5", "graphs": G, "n": n, "l": l, "heads": H, "channels": C, "dtype": "c64",
+            "cache_gb": cache_bytes / 1e9, "prep_s": prep_s, "cache_build_s": build_s,
+            "forward": {"ms": t_fwd, "signal_nodes_per_s": nodes / (t_fwd * 1e-3),
+                        "cache_gbs": cache_bytes / (t_fwd * 1e-3) / 1e9},
+            "dlda": {"ms": t_bwd},
+            "step": {"ms": t_fwd + t_bwd, "signal_nodes_per_s": nodes / ((t_fwd + t_bwd) * 1e-3),
+                     "fp32_tflops": flops / ((t_fwd + t_bwd) * 1e-3) / 1e12}}
 
 
 def main():
@@ -92,11 +127,18 @@ def main():
             "4": (prep.config4, 140 << 30)}
     fh = open(args.out, "a") if args.out else None
     for c in args.configs.split(","):
-        gen, budget = gens[c]
+        if c == "5":
+            line = json.dumps(run_c5(peaks))
+            print(line, flush=True)
+            if fh:
+                fh.write(line + "\n")
+            continue
+        dtype = 1 if c.endswith("c64") else 0
+        gen, budget = gens[c.replace("c64", "")]
         t0 = time.perf_counter()
         cfg = gen()
         prep_s = time.perf_counter() - t0
-        res = run("C" + c, cfg, peaks, budget)
+        res = run("C" + c, cfg, peaks, budget, dtype)
         res["prep_s"] = prep_s
         line = json.dumps(res)
         print(line, flush=True)
