@@ -1,0 +1,94 @@
+"""Config 4 on 1..8 GPUs with the row-slab sharded cache (strong scaling: total work fixed).
+
+  python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+      --master-port 29511 tools/bench_sharded.py [--steps K] [--warmup W] [--n 8192 --l 128 --replicas 512]
+
+Rank g owns rows R_g (paper_2602_20870_b200.dist.plan_rows) and holds P_k[R_g,:], P_k[:,R_g]
+(2 * 137/N GB at N=8192, L=128). One step = F^a X for the B = 1536 point-cloud signals, the MSE
+loss and dL/da: local shard kernels + ONE all_reduce of (loss, 2L+1 partials) over NCCL. Timed
+with CUDA events per rank, max over ranks. Rank 0 prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--l", type=int, default=128)
+    ap.add_argument("--replicas", type=int, default=512)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import prep
+    from paper_2602_20870_b200 import dist as fgd
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # rank 0 builds and persists F (eigendecomposition is host input prep); the others load it
+    if rank == 0:
+        cfg = prep.config4(n=args.n, replicas=args.replicas, l=args.l)
+    if ws > 1:
+        dist.barrier()
+    if rank != 0:
+        cfg = prep.config4(n=args.n, replicas=args.replicas, l=args.l)
+    n, b, L = cfg.n, cfg.b, cfg.l
+    plan = fgd.plan_rows(n, ws)
+    r0, r1 = plan[rank]
+    t0 = time.perf_counter()
+    shard = fgd.CudaShard(cfg.f, L, r0, r1, device=local)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    step_obj = fgd.ShardedFGFRFT(shard, n, L)
+    x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda()
+    xc_rows = torch.from_numpy(np.ascontiguousarray(cfg.x_clean[r0:r1].T)).cuda()
+    alphas = np.array([0.37])
+
+    def step():
+        return step_obj.mse_step(alphas, x, xc_rows)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        loss, dl = step()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "F^a X + MSE + dL/da, config 4 row-sharded", "value": n * b / (ms * 1e-3),
+            "unit": "signal-nodes/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "dtype": "c128", "data": "synthetic",
+            "config": {"workload": "BASELINE config 4", "n": n, "l": L, "b": b, "rows_per_rank": r1 - r0,
+                       "shard_bytes_per_rank": 2 * L * (r1 - r0) * n * 16},
+            "build_s_rank0": build_s, "loss": float(loss[0]), "dlda": float(dl[0])}), flush=True)
+    shard.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
