@@ -278,9 +278,11 @@ def main():
                  "dlda_abs_err": abs(float(dlda_d[i]) - dr), "dlda_ref": dr}
         del ocache
 
-    # ---- dominant kernel roofline: the DMMA complex GEMM (Q X and G X^H per order)
+    # ---- dominant kernel roofline: the DMMA GEMMs (Q X and G X^H per order). With a real F
+    # (graph GFT) they are real x complex: 4 n^2 B flops each (2 n^2 per real column, 2B columns).
+    real = cache.is_real()
     gemm_ms, gemm_n = prof["dmma_zgemm"]
-    gemm_flops_step = 2 * A * 8.0 * n * n * b
+    gemm_flops_step = 2 * A * (4.0 if real else 8.0) * n * n * b
     gemm_tflops = gemm_flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
     tot_prof = sum(v[0] for v in prof.values())
     shares = {k: (v[0] / tot_prof if tot_prof else None) for k, v in prof.items()}
@@ -304,7 +306,7 @@ def main():
         e1.record(stream)
         e1.synchronize()
         t = e0.elapsed_time(e1) / reps
-        nbytes = (L + len(al)) * n * n * 16.0
+        nbytes = (L * (8.0 if real else 16.0) + len(al) * 16.0) * n * n
         syn[tag] = {"orders": len(al), "ms": t, "gbs": nbytes / (t * 1e-3) / 1e9,
                     "frac_hbm": nbytes / (t * 1e-3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": nbytes,
                     "flops": 8.0 * L * n * n * len(al)}
@@ -347,17 +349,25 @@ def main():
             "config": {"workload": "BASELINE config 2 (configs[1]): N=1024 Gaussian k-NN sensor graph, L=64, "
                                    "B=256 noisy bandlimited signals, 64 orders linspace(0,2); step = forward "
                                    "F^a X + MSE loss + dL/da for every order",
-                       "n": n, "l": L, "b": b, "orders": A, "cache_bytes": L * n * n * 16,
+                       "n": n, "l": L, "b": b, "orders": A, "cache_bytes": L * n * n * (8 if real else 16),
+                       "real_f": real,
                        "l2": "inputs larger than L2 (1.07 GB cache streamed every step)",
                        "parallelism": f"replicas x{ws} (independent problems per rank)"},
-            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma_kernel (FP64 DMMA complex GEMM)",
+            "roofline": {"bound": "tensor",
+                         "kernel": ("rgemm_kernel (FP64 DMMA, real Q x complex X)" if real
+                                    else "zgemm_dmma_kernel (FP64 DMMA complex GEMM)"),
                          "achieved": gemm_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                          "frac": (gemm_tflops / peaks["fp64_tflops"]) if gemm_tflops else None,
                          "traffic": None, "peak_source": peaks["fp64_src"],
-                         "algorithmic": "8*N^2*B flops per order per GEMM, 2 GEMMs per order",
+                         "algorithmic": ("4*N^2*B flops per order per GEMM (real F: real x complex), "
+                                         "2 GEMMs per order" if real else
+                                         "8*N^2*B flops per order per GEMM, 2 GEMMs per order"),
                          "launches_timed": gemm_n, "share_of_step": shares},
             "synthesis": {"unit": "GB/s", "peak_hbm_gbs": peaks["hbm_gbs"], "peak_source": peaks["hbm_src"],
-                          "layout": "S = L stored slabs (F^-k read as conjugate-transposed tile pairs)", **syn},
+                          "layout": "S = L stored slabs (F^-k read as conjugate-transposed tile pairs); "
+                                    + ("real F: slabs stored as real doubles (8 B/element), output complex128"
+                                       if real else "complex128 slabs"),
+                          **syn},
             "cache_build": {"seconds": build_s, "tflops": build_flops / build_s / 1e12,
                             "frac_fp64": build_flops / build_s / 1e12 / peaks["fp64_tflops"],
                             "note": "host wall clock incl. H2D of F and allocation"},

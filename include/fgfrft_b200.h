@@ -104,6 +104,11 @@ int fgfrft_cache_destroy(fgfrft_cache* cache);
 int fgfrft_cache_info(const fgfrft_cache* cache, int64_t* n, int* l, uint64_t* fingerprint,
                       int* dtype, int* device);
 
+/* 1 if F's imaginary part is exactly zero: the cache is stored as real doubles and the real-F
+ * kernels run (half the bytes and flops; results equal the complex path's up to rounding).
+ * Set FGFRFT_NO_REAL=1 in the environment to force the complex kernels. */
+int fgfrft_cache_is_real(const fgfrft_cache* cache, int* real);
+
 /* transform.hpp:131-134: copy F^k (1 <= k <= l, else PARAMETER) to host (n x n). */
 int fgfrft_cache_power(fgfrft_cache* cache, int k, double* out);
 

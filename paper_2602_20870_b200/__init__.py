@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cache_destroy": (i, [vp]),
         "fgfrft_cache_info": (i, [vp, vp, vp, vp, vp, vp]),
         "fgfrft_cache_power": (i, [vp, i, vp]),
+        "fgfrft_cache_is_real": (i, [vp, vp]),
         "fgfrft_cache_verify": (i, [vp, vp]),
         "fgfrft_cache_set_stream": (i, [vp, vp]),
         "fgfrft_cache_device_slab": (i, [vp, i, pp]),
@@ -115,6 +116,7 @@ def exported_symbols():
         "fgfrft_last_error", "fgfrft_version", "fgfrft_launch_count", "fgfrft_profile_enable",
         "fgfrft_profile_read", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
         "fgfrft_cache_create", "fgfrft_cache_create_from_powers", "fgfrft_cache_destroy", "fgfrft_cache_info",
+        "fgfrft_cache_is_real",
         "fgfrft_cache_power", "fgfrft_cache_verify", "fgfrft_cache_set_stream", "fgfrft_cache_device_slab",
         "fgfrft_cache_device_bytes", "fgfrft_synthesize", "fgfrft_synthesize_dev", "fgfrft_apply",
         "fgfrft_apply_dev", "fgfrft_apply_matrix", "fgfrft_dlda", "fgfrft_dlda_dev", "fgfrft_mse_step",
@@ -235,6 +237,11 @@ class PowerCache:
 
     def fingerprint(self) -> int:
         return self._fp
+
+    def is_real(self) -> bool:
+        v = ctypes.c_int()
+        _check(lib().fgfrft_cache_is_real(self._h, ctypes.addressof(v)))
+        return bool(v.value)
 
     def power(self, k: int) -> np.ndarray:
         out = np.empty((self._n, self._n), dtype=np.complex128, order="F")

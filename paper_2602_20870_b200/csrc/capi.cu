@@ -46,6 +46,22 @@ cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const
 int batch_max_heads();
 int batch_max_channels();
 int batch_max_n();
+cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void* A, int64_t lda, int64_t sA,
+                         const void* B, int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int batch,
+                         cudaStream_t stream);
+cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t stream);
+cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream);
+cudaError_t launch_real_part(const void* src, void* dst, int64_t count, cudaStream_t stream);
+cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                          bool out_complex, cudaStream_t stream);
+cudaError_t launch_rsynth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                                bool out_complex, cudaStream_t stream);
+int rsweep_max_orders();
+cudaError_t launch_rdots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha, double* partial,
+                         double* s_out, cudaStream_t stream);
+cudaError_t launch_rdots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                             double* partial, double* s_out, cudaStream_t stream, int* launches);
+size_t rdots_mma_partial_elems(int n);
 cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
                          int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
                          bool accumulate, cudaStream_t stream);
@@ -193,6 +209,8 @@ struct fgfrft_cache {
     int64_t n = 0;
     int l = 0;
     int dtype = FGFRFT_C128;
+    bool real = false;  // F has an exactly zero imaginary part: real cache, real Q, real x complex GEMMs
+    size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
     int device = 0;
     uint64_t fingerprint = 0;
     void* slabs = nullptr;
@@ -291,8 +309,25 @@ int check_alphas(const double* alphas, int n_alpha) {
 // Q for n_alpha orders into out (n x n each). Up to 4 orders: exact scalar tile-pair kernel
 // (HBM-bound, bit-identical to the reference order of operations). Sweeps of >= 8 complex128
 // orders: DMMA kernel, 64 orders per launch, cache streamed once per launch.
-int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out) {
+int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out, bool internal = false) {
     ProfScope ps(KC_SYNTH, c->stream);
+    if (c->real) {  // complex output (imag 0) for the API, real Q for the internal GEMMs
+        const bool oc = !internal;
+        const size_t oe = oc ? 16 : 8;
+        if (n_alpha >= 8 && std::getenv("FGFRFT_EXACT_SWEEP") == nullptr) {
+            const int width = 2 * l_used + 1, cap = rsweep_max_orders();
+            for (int a0 = 0; a0 < n_alpha; a0 += cap) {
+                const int na = std::min(cap, n_alpha - a0);
+                FGB_LAUNCH(launch_rsynth_sweep(c->slabs, (int)c->n, l_used, coef_dev + (size_t)a0 * width, na,
+                                               static_cast<char*>(out) + (size_t)a0 * c->mat_elems() * oe, oc,
+                                               c->stream),
+                           1);
+            }
+        } else {
+            FGB_LAUNCH(launch_rsynth(c->slabs, (int)c->n, l_used, coef_dev, n_alpha, out, oc, c->stream), 1);
+        }
+        return FGFRFT_OK;
+    }
     if (c->dtype == FGFRFT_C128 && n_alpha >= 8 && std::getenv("FGFRFT_EXACT_SWEEP") == nullptr) {
         const int width = 2 * l_used + 1;
         const int cap = synth_sweep_max_orders();
@@ -339,7 +374,16 @@ int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype,
     c->dtype = dtype;
     c->device = device;
     c->elem = elem;
+    c->sig = elem;
     c->fingerprint = host_fnv1a64(f, (size_t)n * (size_t)n * 16);
+    if (dtype == FGFRFT_C128 && std::getenv("FGFRFT_NO_REAL") == nullptr) {
+        bool real = true;
+        for (size_t i = 0; i < (size_t)n * (size_t)n && real; ++i) real = f[2 * i + 1] == 0.0;
+        if (real) {
+            c->real = true;
+            c->elem = 8;
+        }
+    }
     DeviceGuard dg(device);
     cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -384,6 +428,25 @@ void destroy_cache(fgfrft_cache* c) {
 int build_powers(fgfrft_cache* c, const double* f) {
     const size_t ml = c->mat_elems();
     const int n = (int)c->n;
+    if (c->real) {  // P_k = F P_{k-1} as a real DMMA GEMM (2 n^3 flops per power)
+        FGB_CUDA(c->tmp.ensure(ml * 16 + 2 * ml * 8));
+        double* fr = reinterpret_cast<double*>(c->tmp.as<double2>() + ml);
+        double* cur = fr + ml;
+        FGB_CUDA(cudaMemcpyAsync(c->tmp.p, f, ml * 16, cudaMemcpyHostToDevice, c->stream));
+        FGB_LAUNCH(launch_real_part(c->tmp.p, fr, (int64_t)ml, c->stream), 1);
+        FGB_LAUNCH(launch_rto_tiled(fr, c->slab(1), n, c->stream), 1);
+        double* prev = reinterpret_cast<double*>(c->tmp.p);  // the complex staging is free now: reuse
+        const double* p = fr;
+        for (int k = 2; k <= c->l; ++k) {
+            FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, fr, n, 0, p, n, 0, cur, n, 0, 1, c->stream), 1);
+            FGB_LAUNCH(launch_rto_tiled(cur, c->slab(k), n, c->stream), 1);
+            p = cur;
+            std::swap(prev, cur);
+        }
+        FGB_CUDA(cudaStreamSynchronize(c->stream));
+        c->tmp.release();
+        return FGFRFT_OK;
+    }
     FGB_CUDA(c->tmp.ensure(3 * ml * 16));
     double2* fbuf = c->tmp.as<double2>();
     double2* prev = fbuf + ml;
@@ -404,10 +467,16 @@ int build_powers(fgfrft_cache* c, const double* f) {
 
 int upload_powers(fgfrft_cache* c, const double* powers) {
     const size_t ml = c->mat_elems();
-    FGB_CUDA(c->tmp.ensure(ml * 16));
+    FGB_CUDA(c->tmp.ensure(ml * 16 + ml * 8));
     for (int k = 1; k <= c->l; ++k) {
         FGB_CUDA(cudaMemcpyAsync(c->tmp.p, powers + 2 * ml * (k - 1), ml * 16, cudaMemcpyHostToDevice, c->stream));
-        FGB_LAUNCH(launch_to_tiled(c->tmp.p, c->slab(k), (int)c->n, (int)c->elem, c->stream), 1);
+        if (c->real) {
+            double* fr = reinterpret_cast<double*>(c->tmp.as<double2>() + ml);
+            FGB_LAUNCH(launch_real_part(c->tmp.p, fr, (int64_t)ml, c->stream), 1);
+            FGB_LAUNCH(launch_rto_tiled(fr, c->slab(k), (int)c->n, c->stream), 1);
+        } else {
+            FGB_LAUNCH(launch_to_tiled(c->tmp.p, c->slab(k), (int)c->n, (int)c->elem, c->stream), 1);
+        }
     }
     FGB_CUDA(cudaStreamSynchronize(c->stream));
     c->tmp.release();
@@ -480,11 +549,17 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
     const size_t width = (size_t)(2 * l_used + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
-        if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p)) return st;
+        if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p, true)) return st;
         ProfScope ps(KC_GEMM, c->stream);
-        FGB_LAUNCH(gemm(c, n, (int)b, n, c->q.p, n, (int64_t)sl, inverse, x_dev, n, 0, false,
-                        static_cast<char*>(y_dev) + (size_t)a0 * n * b * c->elem, n, (int64_t)n * b, na),
-                   1);
+        if (c->real)  // Y = Q X or Q^T X with real Q: real DMMA GEMM over the (re, im) columns
+            FGB_LAUNCH(launch_rgemm(inverse ? 1 : 0, 1, 1, n, 2 * (int)b, n, c->q.p, n, (int64_t)sl, x_dev, n, 0,
+                                    static_cast<char*>(y_dev) + (size_t)a0 * n * b * c->sig, n, (int64_t)2 * n * b, na,
+                                    c->stream),
+                       1);
+        else
+            FGB_LAUNCH(gemm(c, n, (int)b, n, c->q.p, n, (int64_t)sl, inverse, x_dev, n, 0, false,
+                            static_cast<char*>(y_dev) + (size_t)a0 * n * b * c->sig, n, (int64_t)n * b, na),
+                       1);
     }
     return FGFRFT_OK;
 }
@@ -495,23 +570,41 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
 int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
-    const bool mma = n_alpha >= 8 && c->dtype == FGFRFT_C128;
+    const bool mma = n_alpha >= 8 && c->dtype == FGFRFT_C128;  // real caches: rdots_mma (same cap)
     const int chunk = mma ? std::min(alpha_chunk(c, n_alpha), dots_mma_max_orders()) : alpha_chunk(c, n_alpha);
     FGB_CUDA(c->m.ensure((size_t)chunk * sl * c->elem));
-    FGB_CUDA(c->partial.ensure(std::max(mma ? dots_mma_partial_elems(n) : 0, dots_partial_elems(n, c->l, chunk)) *
+    FGB_CUDA(c->partial.ensure(std::max(mma ? std::max(dots_mma_partial_elems(n), rdots_mma_partial_elems(n)) : 0,
+                                        dots_partial_elems(n, c->l, chunk)) *
                                sizeof(double)));
     const size_t width = (size_t)(2 * c->l + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
-        // M_a = G_a X^H  (n x n, K = b)
+        // M_a = G_a X^H  (n x n, K = b); real cache: only M_re = Re(G X^H) is needed
         {
             ProfScope ps(KC_GEMM, c->stream);
-            FGB_LAUNCH(gemm(c, n, n, (int)b, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->elem, n,
-                            (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na),
-                       1);
+            if (c->real)
+                FGB_LAUNCH(launch_rgemm(2, 2, 0, n, n, 2 * (int)b,
+                                        static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, n,
+                                        (int64_t)2 * n * b, x_dev, n, 0, c->m.p, n, (int64_t)sl, na, c->stream),
+                           1);
+            else
+                FGB_LAUNCH(gemm(c, n, n, (int)b, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, n,
+                                (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na),
+                           1);
         }
         ProfScope ps(KC_DOTS, c->stream);
-        if (mma && na >= 8) {
+        if (c->real) {
+            if (na >= 8) {
+                int nl = 0;
+                FGB_CUDA(launch_rdots_mma(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
+                                          s_dev + a0 * width, c->stream, &nl));
+                g_launches += nl;
+            } else {
+                FGB_LAUNCH(launch_rdots(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
+                                        s_dev + a0 * width, c->stream),
+                           2);
+            }
+        } else if (mma && na >= 8) {
             int nl = 0;
             FGB_CUDA(launch_power_dots_mma(c->slabs, n, c->l, c->m.p, (int64_t)sl, na, c->partial.as<double>(),
                                            s_dev + a0 * width, c->stream, &nl));
@@ -623,6 +716,12 @@ int fgfrft_cache_info(const fgfrft_cache* c, int64_t* n, int* l, uint64_t* finge
     return FGFRFT_OK;
 }
 
+int fgfrft_cache_is_real(const fgfrft_cache* c, int* real) {
+    if (int st = check_handle(c)) return st;
+    if (real) *real = c->real ? 1 : 0;
+    return FGFRFT_OK;
+}
+
 int fgfrft_cache_power(fgfrft_cache* c, int k, double* out) {
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
@@ -631,7 +730,10 @@ int fgfrft_cache_power(fgfrft_cache* c, int k, double* out) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
     FGB_CUDA(c->tmp.ensure(c->mat_elems() * 16));
-    FGB_LAUNCH(launch_from_tiled(c->slab(k), c->tmp.p, (int)c->n, (int)c->elem, c->stream), 1);
+    if (c->real)
+        FGB_LAUNCH(launch_rfrom_tiled(c->slab(k), c->tmp.p, (int)c->n, c->stream), 1);
+    else
+        FGB_LAUNCH(launch_from_tiled(c->slab(k), c->tmp.p, (int)c->n, (int)c->elem, c->stream), 1);
     FGB_CUDA(cudaMemcpyAsync(out, c->tmp.p, c->mat_elems() * 16, cudaMemcpyDeviceToHost, c->stream));
     FGB_CUDA(cudaStreamSynchronize(c->stream));
     return FGFRFT_OK;
@@ -692,7 +794,7 @@ int fgfrft_synthesize(fgfrft_cache* c, const double* alphas, int n_alpha, int tr
     {
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
-        FGB_CUDA(c->y.ensure((size_t)n_alpha * c->mat_elems() * c->elem));
+        FGB_CUDA(c->y.ensure((size_t)n_alpha * c->mat_elems() * (c->real ? 16 : c->elem)));
     }
     if (int st = fgfrft_synthesize_dev(c, alphas, n_alpha, truncation, which, c->y.p)) return st;
     std::lock_guard<std::mutex> lk(c->mu);
@@ -730,8 +832,8 @@ int fgfrft_apply(fgfrft_cache* c, const double* alphas, int n_alpha, int truncat
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
     const size_t xe = (size_t)c->n * b;
-    FGB_CUDA(c->x.ensure(xe * c->elem));
-    FGB_CUDA(c->y.ensure(xe * c->elem * n_alpha));
+    FGB_CUDA(c->x.ensure(xe * c->sig));
+    FGB_CUDA(c->y.ensure(xe * c->sig * n_alpha));
     if (int st = upload_signal(c, x, xe, c->x.p)) return st;
     if (int st = apply_device(c, alphas, n_alpha, l_used, inverse != 0, c->x.p, b, c->y.p)) return st;
     return download_signal(c, c->y.p, xe * n_alpha, y);
@@ -821,8 +923,8 @@ int fgfrft_dlda(fgfrft_cache* c, const double* alphas, int n_alpha, const double
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
         const size_t xe = (size_t)c->n * (b > 0 ? b : 1);
-        FGB_CUDA(c->x.ensure(xe * c->elem));
-        FGB_CUDA(c->g.ensure(xe * c->elem * n_alpha));
+        FGB_CUDA(c->x.ensure(xe * c->sig));
+        FGB_CUDA(c->g.ensure(xe * c->sig * n_alpha));
         if (b > 0) {
             if (int st = upload_signal(c, x, xe, c->x.p)) return st;
             if (int st = upload_signal(c, g, xe * n_alpha, c->g.p)) return st;
@@ -851,25 +953,31 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     const int chunk = alpha_chunk(c, n_alpha);
     const size_t sl = c->mat_elems();
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
-    FGB_CUDA(c->g.ensure((size_t)chunk * blk * c->elem));
+    FGB_CUDA(c->g.ensure((size_t)chunk * blk * c->sig));
     FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
     FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
-    if (!y_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * c->elem));
+    if (!y_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * c->sig));
     const double norm = 1.0 / ((double)n * (double)b);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
-        void* ya = y_dev ? static_cast<char*>(y_dev) + (size_t)a0 * blk * c->elem : c->y.p;
-        if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p)) return st;
+        void* ya = y_dev ? static_cast<char*>(y_dev) + (size_t)a0 * blk * c->sig : c->y.p;
+        if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p, true)) return st;
         {
             ProfScope ps(KC_GEMM, c->stream);
-            FGB_LAUNCH(gemm(c, n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n, (int64_t)blk, na),
-                       1);
+            if (c->real)
+                FGB_LAUNCH(launch_rgemm(0, 1, 1, n, 2 * (int)b, n, c->q.p, n, (int64_t)sl, x_dev, n, 0, ya, n,
+                                        (int64_t)2 * blk, na, c->stream),
+                           1);
+            else
+                FGB_LAUNCH(gemm(c, n, (int)b, n, c->q.p, n, (int64_t)sl, false, x_dev, n, 0, false, ya, n, (int64_t)blk,
+                                na),
+                           1);
         }
         {
             ProfScope ps(KC_ELEMWISE, c->stream);
             FGB_LAUNCH(launch_mse_residual(ya, xc_dev, (int64_t)blk, na, 2.0 * norm, norm, c->g.p,
                                            c->lpart.as<double>(), static_cast<double*>(loss_dev) + a0, c->stream,
-                                           (int)c->elem),
+                                           (int)c->sig),
                        2);
         }
         if (int st = dots_device(c, na, c->g.p, x_dev, b, c->s.as<double>() + a0 * width)) return st;
@@ -892,10 +1000,10 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
         const size_t xe = (size_t)c->n * b;
-        FGB_CUDA(c->x.ensure(xe * c->elem));
-        FGB_CUDA(c->xc.ensure(xe * c->elem));
+        FGB_CUDA(c->x.ensure(xe * c->sig));
+        FGB_CUDA(c->xc.ensure(xe * c->sig));
         FGB_CUDA(c->loss.ensure((size_t)n_alpha * 2 * sizeof(double)));
-        if (y) FGB_CUDA(c->y.ensure(xe * c->elem * n_alpha));
+        if (y) FGB_CUDA(c->y.ensure(xe * c->sig * n_alpha));
         if (int st = upload_signal(c, x, xe, c->x.p)) return st;
         if (int st = upload_signal(c, xc, xe, c->xc.p)) return st;
     }

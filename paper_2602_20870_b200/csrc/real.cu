@@ -1,0 +1,846 @@
+// real.cu -- real-F specialisation of the hot path (complex128 API, real arithmetic).
+//
+// Every BASELINE config uses a graph-derived F = V^T (real orthogonal), so every cached power
+// P_k = F^k is exactly real and so are Q(alpha) and dQ/dalpha (real series coefficients). The
+// reference itself specialises real F in its fast denoise engine (learn.hpp:449-451). When the
+// imaginary part of F is exactly zero the library stores the cache as REAL doubles (half the
+// bytes), synthesises real Q (half the bytes / flops), and runs the products with a complex
+// operand as real DMMA GEMMs over the interleaved (re, im) columns (half the flops):
+//   Y = Q X            : D(m, 2j+c) = sum_k Q(m,k) X(k,j).c
+//   M_re = Re(G X^H)   : D(i, l)    = sum_{j,c} G(i,j).c X(l,j).c
+//   s_k  = Re<M, P_k>  = sum M_re .* P_k ,  s_{-k} = sum M_re .* P_k^T.
+// Results equal the complex path's up to rounding (the complex path adds exact zeros).
+//
+// Kernels: rgemm_kernel (real DMMA GEMM with operand modes), rsynth_pairs_kernel (exact scalar
+// synthesis, tile pairs, TMA ring), rsynth_sweep_kernel (DMMA sweep synthesis), rdots_kernel
+// (scalar per-power reductions) and rdots_mma_kernel (DMMA split-K contraction for sweeps).
+#include "common.cuh"
+
+namespace fgb {
+
+// =====================================================================================
+// Real DMMA GEMM: D (M x N) = A (M x K) * B (K x N), operand modes
+//   AM 0: A(m,k) = A[m + k*lda]                 (real, column-major)
+//   AM 1: A(m,k) = A[k + m*lda]                 (real, transposed storage: Q^T)
+//   AM 2: A(m,k) = G[(m + (k>>1)*lda)*2 + (k&1)]  (complex G viewed as M x 2B)
+//   BM 0: B(k,n) = B[k + n*ldb]                 (real, column-major)
+//   BM 1: B(k,n) = X[(k + (n>>1)*ldb)*2 + (n&1)]  (complex X viewed as K x 2B)
+//   BM 2: B(k,n) = X[(n + (k>>1)*ldb)*2 + (k&1)]  (complex X viewed as (2B x N)^T)
+//   CM 0: C[m + n*ldc] = D(m,n)                  (real)
+//   CM 1: C[(m + (n>>1)*ldc)*2 + (n&1)] = D(m,n)  (complex merge: columns (2j, 2j+1) -> Y(m,j))
+// CTA 128 x 128, BK = 16, 8 warps as 4 (m) x 2 (n), warp tile 32 x 64 (4 x 8 DMMA tiles),
+// 4-stage cp.async ring of 8-byte elements, fragment loads conflict free (ld = 136 doubles).
+// =====================================================================================
+constexpr int kRgBM = 128, kRgBN = 128, kRgBK = 16, kRgLd = 136, kRgStages = 4;
+
+size_t rgemm_smem_bytes() { return (size_t)kRgStages * 2 * kRgBK * kRgLd * 8; }
+
+template <int AM, int BM, int CM>
+__global__ void __launch_bounds__(256, 1)
+rgemm_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t sA, const double* __restrict__ B,
+             int64_t ldb, int64_t sB, double* __restrict__ C, int64_t ldc, int64_t sC) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* As = reinterpret_cast<double*>(smem);                   // [stage][k][m]
+    double* Bs = As + (size_t)kRgStages * kRgBK * kRgLd;            // [stage][k][n]
+    const int bz = blockIdx.z;
+    A += bz * sA;
+    B += bz * sB;
+    C += bz * sC;
+    const int m0 = blockIdx.x * kRgBM, n0 = blockIdx.y * kRgBN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
+    const int nk = (K + kRgBK - 1) / kRgBK;
+
+    auto a_addr = [&](int m, int k) -> int64_t {
+        if (AM == 0) return (int64_t)m + (int64_t)k * lda;
+        if (AM == 1) return (int64_t)k + (int64_t)m * lda;
+        return ((int64_t)m + (int64_t)(k >> 1) * lda) * 2 + (k & 1);
+    };
+    auto b_addr = [&](int k, int n) -> int64_t {
+        if (BM == 0) return (int64_t)k + (int64_t)n * ldb;
+        if (BM == 1) return ((int64_t)k + (int64_t)(n >> 1) * ldb) * 2 + (n & 1);
+        return ((int64_t)n + (int64_t)(k >> 1) * ldb) * 2 + (k & 1);
+    };
+    auto load_stage = [&](int kt, int s) {
+        const int k0 = kt * kRgBK;
+        double* as = As + (size_t)s * kRgBK * kRgLd;
+        double* bs = Bs + (size_t)s * kRgBK * kRgLd;
+#pragma unroll
+        for (int j = 0; j < (kRgBM * kRgBK) / 256; ++j) {
+            const int idx = tid + 256 * j;
+            // AM 0 / 2: m fastest (contiguous in memory for AM 0); AM 1: k fastest
+            const int m = AM == 1 ? idx / kRgBK : idx % kRgBM;
+            const int k = AM == 1 ? idx % kRgBK : idx / kRgBM;
+            const bool v = (m0 + m < M) && (k0 + k < K);
+            cp_async8(as + k * kRgLd + m, v ? A + a_addr(m0 + m, k0 + k) : A, v);
+        }
+#pragma unroll
+        for (int j = 0; j < (kRgBN * kRgBK) / 256; ++j) {
+            const int idx = tid + 256 * j;
+            // BM 0: k fastest (contiguous); BM 1 / 2: n fastest
+            const int n = BM == 0 ? idx / kRgBK : idx % kRgBN;
+            const int k = BM == 0 ? idx % kRgBK : idx / kRgBN;
+            const bool v = (n0 + n < N) && (k0 + k < K);
+            cp_async8(bs + k * kRgLd + n, v ? B + b_addr(k0 + k, n0 + n) : B, v);
+        }
+    };
+
+    double acc[4][8][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kRgStages - 1; ++s) {
+        if (s < nk) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<kRgStages - 2>();
+        __syncthreads();
+        {
+            const int nx = kt + kRgStages - 1;
+            if (nx < nk) load_stage(nx, nx % kRgStages);
+            cp_async_commit();
+        }
+        const double* as = As + (size_t)(kt % kRgStages) * kRgBK * kRgLd;
+        const double* bs = Bs + (size_t)(kt % kRgStages) * kRgBK * kRgLd;
+#pragma unroll
+        for (int kk = 0; kk < kRgBK; kk += 4) {
+            double a[4], b[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = as[(kk + t) * kRgLd + wm * 32 + i * 8 + g];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = bs[(kk + t) * kRgLd + wn * 64 + j * 8 + g];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + wm * 32 + i * 8 + g;
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int col = n0 + wn * 64 + j * 8 + 2 * t;  // even: (col, col+1) = (re, im) in CM 1
+            if (CM == 1) {
+                if (col < N) {
+                    double2* dst = reinterpret_cast<double2*>(C) + (int64_t)row + (int64_t)(col >> 1) * ldc;
+                    *dst = make_double2(acc[i][j][0], acc[i][j][1]);
+                }
+            } else {
+                if (col < N) C[(int64_t)row + (int64_t)col * ldc] = acc[i][j][0];
+                if (col + 1 < N) C[(int64_t)row + (int64_t)(col + 1) * ldc] = acc[i][j][1];
+            }
+        }
+    }
+}
+
+cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void* A, int64_t lda, int64_t sA,
+                         const void* B, int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int batch,
+                         cudaStream_t stream) {
+    if (M <= 0 || N <= 0 || batch <= 0) return cudaSuccess;
+    const dim3 grid((unsigned)ceil_div(M, kRgBM), (unsigned)ceil_div(N, kRgBN), (unsigned)batch);
+    const size_t smem = rgemm_smem_bytes();
+#define FGB_RG(AMV, BMV, CMV)                                                                                \
+    {                                                                                                        \
+        auto kern = rgemm_kernel<AMV, BMV, CMV>;                                                             \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                      \
+        kern<<<grid, 256, smem, stream>>>(M, N, K, (const double*)A, lda, sA, (const double*)B, ldb, sB,     \
+                                          (double*)C, ldc, sC);                                              \
+        return cudaGetLastError();                                                                           \
+    }
+    if (am == 0 && bm == 0 && cm == 0) FGB_RG(0, 0, 0)  // cache build P_k = F P_{k-1}
+    if (am == 0 && bm == 1 && cm == 1) FGB_RG(0, 1, 1)  // Y = Q X
+    if (am == 1 && bm == 1 && cm == 1) FGB_RG(1, 1, 1)  // Y = Q^T X
+    if (am == 2 && bm == 2 && cm == 0) FGB_RG(2, 2, 0)  // M_re = Re(G X^H)
+#undef FGB_RG
+    return cudaErrorInvalidValue;
+}
+
+// =====================================================================================
+// Real tiled layout (same tiling / swizzle as common.cuh, 8-byte elements, 8 KB tiles).
+// =====================================================================================
+__global__ void __launch_bounds__(256) rto_tiled_kernel(const double* __restrict__ src, double* __restrict__ dst, int n,
+                                                        int nt) {
+    const int I = blockIdx.x % nt, J = blockIdx.x / nt;
+    const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* t = dst + tile_base(I, J, nt);
+    const int row = I * kTile + r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = w + 8 * i, col = J * kTile + c;
+        t[swz(r, c)] = (row < n && col < n) ? src[(int64_t)col * n + row] : 0.0;
+    }
+}
+
+// tiled real -> column-major complex (imag 0)
+__global__ void __launch_bounds__(256) rfrom_tiled_kernel(const double* __restrict__ src, double2* __restrict__ dst,
+                                                          int n, int nt) {
+    const int I = blockIdx.x % nt, J = blockIdx.x / nt;
+    const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double* t = src + tile_base(I, J, nt);
+    const int row = I * kTile + r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = w + 8 * i, col = J * kTile + c;
+        if (row < n && col < n) dst[(int64_t)col * n + row] = make_double2(t[swz(r, c)], 0.0);
+    }
+}
+
+// complex (imag ignored) column-major -> real column-major
+__global__ void real_part_kernel(const double2* __restrict__ src, double* __restrict__ dst, int64_t count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i].x;
+}
+
+// real -> complex (imag 0)
+__global__ void real_to_complex_kernel(const double* __restrict__ src, double2* __restrict__ dst, int64_t count) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = make_double2(src[i], 0.0);
+}
+
+cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    rto_tiled_kernel<<<nt * nt, 256, 0, stream>>>((const double*)src, (double*)dst, n, nt);
+    return cudaGetLastError();
+}
+cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    rfrom_tiled_kernel<<<nt * nt, 256, 0, stream>>>((const double*)src, (double2*)dst, n, nt);
+    return cudaGetLastError();
+}
+cudaError_t launch_real_part(const void* src, void* dst, int64_t count, cudaStream_t stream) {
+    real_part_kernel<<<8 * FGFRFT_SMS, 256, 0, stream>>>((const double2*)src, (double*)dst, count);
+    return cudaGetLastError();
+}
+cudaError_t launch_real_to_complex(const void* src, void* dst, int64_t count, cudaStream_t stream) {
+    real_to_complex_kernel<<<8 * FGFRFT_SMS, 256, 0, stream>>>((const double*)src, (double2*)dst, count);
+    return cudaGetLastError();
+}
+
+// =====================================================================================
+// Exact scalar synthesis on real tiles (tile pairs, TMA ring), AC orders per CTA.
+// q += a*p + b*pt with round-to-nearest ops: identical to the real part of the complex path,
+// and the imaginary part the reference produces is exactly +0 (a*0 + b*(-0) = +0 after q + t).
+// OUTC: write complex output (imag 0) for the API, else real Q for the internal GEMM.
+// =====================================================================================
+constexpr int kRsStages = 6;
+
+size_t rsynth_smem_bytes(int l_used, int ac) {
+    return (size_t)kRsStages * 2 * kTileElems * 8 + kRsStages * 8 + (size_t)l_used * ac * 16 + (size_t)ac * 8 + 16;
+}
+
+template <int AC, bool OUTC>
+__global__ void __launch_bounds__(256, 1)
+rsynth_pairs_kernel(const double* __restrict__ slabs, int n, int l_used, int64_t slab_elems,
+                    const double* __restrict__ coef, int coef_ld, int n_alpha, int n_achunks, void* __restrict__ out,
+                    int64_t out_stride, int nt) {
+    constexpr int S = kRsStages;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* tiles = reinterpret_cast<double*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 8);
+    double2* cs = reinterpret_cast<double2*>(full + S);
+    double* c0s = reinterpret_cast<double*>(cs + (size_t)l_used * AC);
+    const int chunk = blockIdx.x % n_achunks, pair = blockIdx.x / n_achunks;
+    int I, J;
+    pair_of(pair, I, J);
+    const int a0 = chunk * AC, na = min(AC, n_alpha - a0);
+    const int bi = min(kTile, n - I * kTile), bj = min(kTile, n - J * kTile);
+    const bool diag = (I == J);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lc = l_used;
+    for (int idx = tid; idx < l_used * AC; idx += 256) {
+        const int k = idx / AC + 1, a = idx % AC;
+        double ak = 0.0, bk = 0.0;
+        if (a < na) {
+            ak = coef[(size_t)(a0 + a) * coef_ld + lc + k];
+            bk = coef[(size_t)(a0 + a) * coef_ld + lc - k];
+        }
+        cs[idx] = make_double2(ak, bk);
+    }
+    if (tid < AC) c0s[tid] = tid < na ? coef[(size_t)(a0 + tid) * coef_ld + lc] : 0.0;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t tb = kTileElems * 8;
+    const bool once = n_achunks == 1;
+    const uint64_t pol = policy_evict_first();
+    const int64_t off1 = tile_base(I, J, nt), off2 = tile_base(J, I, nt);
+    auto issue = [&](int k, int s) {
+        mbar_arrive_expect_tx(&full[s], (diag ? 1 : 2) * tb);
+        const double* slab = slabs + (int64_t)(k - 1) * slab_elems;
+        double* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        if (once) {
+            bulk_g2s_hint(t1, slab + off1, tb, &full[s], pol);
+            if (!diag) bulk_g2s_hint(t1 + kTileElems, slab + off2, tb, &full[s], pol);
+        } else {
+            bulk_g2s(t1, slab + off1, tb, &full[s]);
+            if (!diag) bulk_g2s(t1 + kTileElems, slab + off2, tb, &full[s]);
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < S && s < l_used; ++s) issue(s + 1, s);
+    const int r = lane;
+    double q1[4][AC], q2[4][AC];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int a = 0; a < AC; ++a) {
+            q1[i][a] = (diag && r == warp + 8 * i) ? c0s[a] : 0.0;
+            q2[i][a] = 0.0;
+        }
+    for (int k = 1; k <= l_used; ++k) {
+        const int s = (k - 1) % S;
+        mbar_wait(&full[s], ((k - 1) / S) & 1);
+        const double* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        const double* t2 = diag ? t1 : t1 + kTileElems;
+        double2 ab[AC];
+#pragma unroll
+        for (int a = 0; a < AC; ++a) ab[a] = cs[(k - 1) * AC + a];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = warp + 8 * i;
+            const double p1 = t1[swz(r, c)], p2 = t2[swz(c, r)];
+#pragma unroll
+            for (int a = 0; a < AC; ++a) {
+                q1[i][a] = __dadd_rn(q1[i][a], __dadd_rn(__dmul_rn(ab[a].x, p1), __dmul_rn(ab[a].y, p2)));
+                if (!diag) q2[i][a] = __dadd_rn(q2[i][a], __dadd_rn(__dmul_rn(ab[a].x, p2), __dmul_rn(ab[a].y, p1)));
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && k + S <= l_used) issue(k + S, s);
+    }
+    auto put = [&](int a, int64_t idx, double v) {
+        if (OUTC) reinterpret_cast<double2*>(out)[(int64_t)(a0 + a) * out_stride + idx] = make_double2(v, 0.0);
+        else reinterpret_cast<double*>(out)[(int64_t)(a0 + a) * out_stride + idx] = v;
+    };
+#pragma unroll
+    for (int a = 0; a < AC; ++a) {
+        if (a >= na) break;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = warp + 8 * i;
+            if (r < bi && c < bj) put(a, (int64_t)(J * kTile + c) * n + I * kTile + r, q1[i][a]);
+        }
+    }
+    if (diag) return;
+    double* buf = tiles;
+#pragma unroll
+    for (int a = 0; a < AC; ++a) {
+        if (a >= na) break;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) buf[swz(warp + 8 * i, r)] = q2[i][a];
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int col = warp + 8 * i, row = lane;
+            if (row < bj && col < bi) put(a, (int64_t)(I * kTile + col) * n + J * kTile + row, buf[swz(row, col)]);
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                          bool out_complex, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int npairs = nt * (nt + 1) / 2;
+    const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
+    const int nch = (int)ceil_div(n_alpha, ac);
+    const size_t smem = rsynth_smem_bytes(l_used, ac);
+    const int64_t slab = (int64_t)nt * nt * kTileElems;
+    const dim3 grid((unsigned)((int64_t)nch * npairs));
+#define FGB_RS(ACV, OC)                                                                                     \
+    {                                                                                                       \
+        auto kern = rsynth_pairs_kernel<ACV, OC>;                                                           \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                     \
+        kern<<<grid, 256, smem, stream>>>((const double*)slabs, n, l_used, slab, coef_dev, 2 * l_used + 1,  \
+                                          n_alpha, nch, out, (int64_t)n * n, nt);                           \
+    }
+    if (out_complex) {
+        if (ac == 4) FGB_RS(4, true) else if (ac == 2) FGB_RS(2, true) else FGB_RS(1, true)
+    } else {
+        if (ac == 4) FGB_RS(4, false) else if (ac == 2) FGB_RS(2, false) else FGB_RS(1, false)
+    }
+#undef FGB_RS
+    return cudaGetLastError();
+}
+
+// =====================================================================================
+// DMMA sweep synthesis on real tiles: Q[a][e] = sum_kk C[a][kk] V[kk][e], e = 128 positions
+// (an 8x8 sub-square of tile (I,J) + its transpose in (J,I)), up to 64 orders per launch,
+// 8 warps x 16 e-columns, 64 powers per coefficient chunk, 3-stage ring of 8 powers.
+// =====================================================================================
+constexpr int kRwA = 64, kRwKc = 64, kRwStK = 8, kRwStages = 3;
+constexpr int kRwCLd = 2 * kRwKc + 4;
+constexpr int kRwPLd = 136;  // doubles per staged power: 2 x 64 positions + pad
+
+size_t rsweep_smem_bytes() {
+    const size_t cs = (size_t)kRwA * kRwCLd * 8, st = (size_t)kRwStages * kRwStK * kRwPLd * 8;
+    const size_t os = (size_t)kRwA * 66 * 8;
+    return (cs + st) > os ? cs + st : os;
+}
+
+template <bool OUTC>
+__global__ void __launch_bounds__(256, 1)
+rsynth_sweep_kernel(const double* __restrict__ slabs, int n, int l_used, int64_t slab_elems,
+                    const double* __restrict__ coef, int coef_ld, int n_alpha, void* __restrict__ out, int64_t out_stride,
+                    int nt) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* cs = reinterpret_cast<double*>(smem);
+    double* stb = cs + (size_t)kRwA * kRwCLd;
+    double* os = reinterpret_cast<double*>(smem);
+    const int pair = blockIdx.x >> 4, sq = blockIdx.x & 15;
+    int I, J;
+    pair_of(pair, I, J);
+    const bool diag = (I == J);
+    const int sr = sq & 3, sc = sq >> 2;
+    if (diag && sr > sc) return;
+    const int r0 = 8 * sr, c0 = 8 * sc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int tw = warp >> 2, pbase = 16 * (warp & 3);  // warp: tile tw, positions pbase..pbase+15
+    const int64_t b1 = tile_base(I, J, nt), b2 = tile_base(J, I, nt);
+    const int lc = l_used;
+    double d[8][2][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+    for (int k0 = 1; k0 <= l_used; k0 += kRwKc) {
+        const int kc = min(kRwKc, l_used - k0 + 1);
+        const int nsteps = (kc + kRwStK - 1) / kRwStK;
+        __syncthreads();
+        for (int idx = tid; idx < kRwA * 2 * kRwKc; idx += 256) {
+            const int a = idx / (2 * kRwKc), kk = idx % (2 * kRwKc);
+            const int k = k0 + (kk >> 1);
+            double v = 0.0;
+            if (a < n_alpha && (kk >> 1) < kc) v = coef[(size_t)a * coef_ld + lc + ((kk & 1) ? -k : k)];
+            cs[a * kRwCLd + kk] = v;
+        }
+        auto stage = [&](int st, int buf) {
+            double* dst0 = stb + (size_t)buf * kRwStK * kRwPLd;
+            for (int idx = tid; idx < kRwStK * 128; idx += 256) {
+                const int kp = idx >> 7, t = (idx >> 6) & 1, p = idx & 63;
+                const int ii = p & 7, jj = p >> 3;
+                const int kq = 8 * st + kp;
+                const bool v = kq < kc;
+                const double* slab = slabs + (int64_t)(k0 + (v ? kq : 0) - 1) * slab_elems;
+                const double* src = t == 0 ? slab + b1 + swz(r0 + ii, c0 + jj) : slab + b2 + swz(c0 + jj, r0 + ii);
+                cp_async8(dst0 + kp * kRwPLd + t * 64 + p, src, v);
+            }
+        };
+#pragma unroll
+        for (int s = 0; s < kRwStages - 1; ++s) {
+            if (s < nsteps) stage(s, s);
+            cp_async_commit();
+        }
+        for (int st = 0; st < nsteps; ++st) {
+            cp_async_wait<kRwStages - 2>();
+            __syncthreads();
+            if (st + kRwStages - 1 < nsteps) stage(st + kRwStages - 1, (st + kRwStages - 1) % kRwStages);
+            cp_async_commit();
+            const double* sb = stb + (size_t)(st % kRwStages) * kRwStK * kRwPLd;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const int kkl = 4 * ks + t4, kp = kkl >> 1, sign = kkl & 1;
+                const int tt = sign ? 1 - tw : tw;  // (k,+): own tile; (k,-): the transposed partner
+                double b[2];
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb) b[nb] = sb[kp * kRwPLd + tt * 64 + pbase + 8 * nb + g];
+                const double* crow = cs + g * kRwCLd + 16 * st + kkl;
+#pragma unroll
+                for (int mb = 0; mb < 8; ++mb) {
+                    const double a = crow[8 * mb * kRwCLd];
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb) dmma884(d[mb][nb][0], d[mb][nb][1], a, b[nb]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    for (int t = 0; t < 2; ++t) {
+        if (t == 1 && diag && sr == sc) break;
+        __syncthreads();
+        if (tw == t) {
+#pragma unroll
+            for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int a = 8 * mb + g, p = pbase + 8 * nb + 2 * t4 + h;
+                        const int ii = p & 7, jj = p >> 3;
+                        double v = d[mb][nb][h];
+                        if (t == 0 && diag && sr == sc && ii == jj && a < n_alpha) v += coef[(size_t)a * coef_ld + lc];
+                        os[a * 66 + (t == 0 ? p : ii * 8 + jj)] = v;
+                    }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < kRwA * 64; idx += 256) {
+            const int a = idx >> 6, q = idx & 63;
+            if (a >= n_alpha) break;
+            const int hi = q >> 3, lo = q & 7;
+            const int row = t == 0 ? I * 32 + r0 + lo : J * 32 + c0 + lo;
+            const int col = t == 0 ? J * 32 + c0 + hi : I * 32 + r0 + hi;
+            if (row < n && col < n) {
+                const int64_t o = (int64_t)a * out_stride + (int64_t)col * n + row;
+                if (OUTC) reinterpret_cast<double2*>(out)[o] = make_double2(os[a * 66 + q], 0.0);
+                else reinterpret_cast<double*>(out)[o] = os[a * 66 + q];
+            }
+        }
+    }
+}
+
+int rsweep_max_orders() { return kRwA; }
+
+cudaError_t launch_rsynth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                                bool out_complex, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int npairs = nt * (nt + 1) / 2;
+    const size_t smem = rsweep_smem_bytes();
+    const int64_t slab = (int64_t)nt * nt * kTileElems;
+    if (out_complex) {
+        cudaError_t e =
+            cudaFuncSetAttribute(rsynth_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        rsynth_sweep_kernel<true><<<(unsigned)npairs * 16, 256, smem, stream>>>(
+            (const double*)slabs, n, l_used, slab, coef_dev, 2 * l_used + 1, n_alpha, out, (int64_t)n * n, nt);
+    } else {
+        cudaError_t e =
+            cudaFuncSetAttribute(rsynth_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        rsynth_sweep_kernel<false><<<(unsigned)npairs * 16, 256, smem, stream>>>(
+            (const double*)slabs, n, l_used, slab, coef_dev, 2 * l_used + 1, n_alpha, out, (int64_t)n * n, nt);
+    }
+    return cudaGetLastError();
+}
+
+// =====================================================================================
+// Real per-power reductions.
+//   Scalar (few orders): tile pairs, TMA ring, M_re pair tiles in registers, s_+ = sum M P,
+//   s_- = sum M P^T, grouped transposing warp reductions.
+//   DMMA (sweeps): D[a][kk] = sum_e M_re[a][e] V[e][kk], e = 32 positions of a 4x4 sub-square
+//   pair per block (K = 32 -> 8 DMMA K-steps), up to 64 orders x 64 powers per launch.
+// =====================================================================================
+constexpr int kRdStages = 6;
+
+size_t rdots_smem_bytes(int l, int ac) {
+    return (size_t)kRdStages * 2 * kTileElems * 8 + kRdStages * 8 + (size_t)l * 8 * ac * 2 * 8 + 16;
+}
+
+template <int AC>
+__global__ void __launch_bounds__(256, 1)
+rdots_kernel(const double* __restrict__ slabs, int n, int l, int64_t slab_elems, const double* __restrict__ m,
+             int64_t m_stride, int n_alpha, int n_achunks, double* __restrict__ partial, int nt, int npairs) {
+    constexpr int S = kRdStages;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* tiles = reinterpret_cast<double*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 8);
+    double* red = reinterpret_cast<double*>(full + S);
+    const int chunk = blockIdx.x % n_achunks, pair = blockIdx.x / n_achunks;
+    int I, J;
+    pair_of(pair, I, J);
+    const int a0 = chunk * AC, na = min(AC, n_alpha - a0);
+    const int bi = min(kTile, n - I * kTile), bj = min(kTile, n - J * kTile);
+    const bool diag = (I == J);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, r = lane;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t tb = kTileElems * 8;
+    const bool once = n_achunks == 1;
+    const uint64_t pol = policy_evict_first();
+    const int64_t off1 = tile_base(I, J, nt), off2 = tile_base(J, I, nt);
+    auto issue = [&](int k, int s) {
+        mbar_arrive_expect_tx(&full[s], (diag ? 1 : 2) * tb);
+        const double* slab = slabs + (int64_t)(k - 1) * slab_elems;
+        double* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        if (once) {
+            bulk_g2s_hint(t1, slab + off1, tb, &full[s], pol);
+            if (!diag) bulk_g2s_hint(t1 + kTileElems, slab + off2, tb, &full[s], pol);
+        } else {
+            bulk_g2s(t1, slab + off1, tb, &full[s]);
+            if (!diag) bulk_g2s(t1 + kTileElems, slab + off2, tb, &full[s]);
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < S && s < l; ++s) issue(s + 1, s);
+    double m1[4][AC], m2[4][AC], s0[AC];
+#pragma unroll
+    for (int a = 0; a < AC; ++a) s0[a] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = warp + 8 * i;
+        const bool v = r < bi && c < bj;
+#pragma unroll
+        for (int a = 0; a < AC; ++a) {
+            const double* ma = m + (int64_t)(a0 + (a < na ? a : 0)) * m_stride;
+            const bool va = v && a < na;
+            m1[i][a] = va ? ma[(int64_t)(J * kTile + c) * n + I * kTile + r] : 0.0;
+            m2[i][a] = (va && !diag) ? ma[(int64_t)(I * kTile + r) * n + J * kTile + c] : 0.0;
+            if (diag && r == c) s0[a] += m1[i][a];
+        }
+    }
+    constexpr int NV = 16, G = NV / (2 * AC);
+    for (int k0 = 1; k0 <= l; k0 += G) {
+        double v[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = 0.0;
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+            const int k = k0 + gg;
+            if (k > l) break;
+            const int s = (k - 1) % S;
+            mbar_wait(&full[s], ((k - 1) / S) & 1);
+            const double* t1 = tiles + (size_t)(s * 2) * kTileElems;
+            const double* t2 = diag ? t1 : t1 + kTileElems;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int c = warp + 8 * i;
+                const double p1 = t1[swz(r, c)], p2 = t2[swz(c, r)];
+#pragma unroll
+                for (int a = 0; a < AC; ++a) {
+                    double& sp = v[(gg * AC + a) * 2 + 0];
+                    double& sm = v[(gg * AC + a) * 2 + 1];
+                    sp = fma(m1[i][a], p1, sp);
+                    sm = fma(m1[i][a], p2, sm);
+                    if (!diag) {
+                        sp = fma(m2[i][a], p2, sp);
+                        sm = fma(m2[i][a], p1, sm);
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0 && k + S <= l) issue(k + S, s);
+        }
+#pragma unroll
+        for (int o = 8, half = NV / 2; o >= 1; o >>= 1, half >>= 1) {
+            const bool hi = (lane & o) != 0;
+#pragma unroll
+            for (int q = 0; q < half; ++q) {
+                const double send = hi ? v[q] : v[q + half];
+                const double keep = hi ? v[q + half] : v[q];
+                v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+        const int q = lane & (NV - 1);
+        const int gq = q / (2 * AC), a = (q / 2) % AC, sgn = q & 1;
+        if (lane < NV && k0 + gq <= l) red[(((size_t)(k0 + gq - 1) * 8 + warp) * AC + a) * 2 + sgn] = v[0];
+    }
+    __syncthreads();
+    double* s0buf = tiles;
+#pragma unroll
+    for (int a = 0; a < AC; ++a) {
+        double t = s0[a];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) s0buf[warp * AC + a] = t;
+    }
+    __syncthreads();
+    const int width = 2 * l + 1;
+    for (int idx = tid; idx < na * width; idx += 256) {
+        const int a = idx / width, kk = idx % width;
+        double acc = 0.0;
+        if (kk == l) {
+            for (int w = 0; w < 8; ++w) acc += s0buf[w * AC + a];
+        } else {
+            const int k = kk > l ? kk - l : l - kk, sel = kk > l ? 0 : 1;
+            for (int w = 0; w < 8; ++w) acc += red[(((size_t)(k - 1) * 8 + w) * AC + a) * 2 + sel];
+        }
+        partial[((int64_t)(a0 + a) * width + kk) * npairs + pair] = acc;
+    }
+}
+
+__device__ __forceinline__ double rwarp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(128) rreduce_pairs_kernel(const double* __restrict__ partial, int npairs,
+                                                            double* __restrict__ out) {
+    const double* row = partial + (int64_t)blockIdx.x * npairs;
+    double acc = 0.0;
+    for (int p = threadIdx.x; p < npairs; p += 128) acc += row[p];
+    acc = rwarp_sum(acc);
+    __shared__ double ws[4];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = (ws[0] + ws[1]) + (ws[2] + ws[3]);
+}
+
+cudaError_t launch_rdots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha, double* partial,
+                         double* s_out, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int npairs = nt * (nt + 1) / 2;
+    const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
+    const int nch = (int)ceil_div(n_alpha, ac);
+    const size_t smem = rdots_smem_bytes(l, ac);
+    const int64_t slab = (int64_t)nt * nt * kTileElems;
+    const dim3 grid((unsigned)((int64_t)nch * npairs));
+#define FGB_RD(ACV)                                                                                         \
+    {                                                                                                       \
+        auto kern = rdots_kernel<ACV>;                                                                      \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return e;                                                                     \
+        kern<<<grid, 256, smem, stream>>>((const double*)slabs, n, l, slab, (const double*)m, m_stride,     \
+                                          n_alpha, nch, partial, nt, npairs);                               \
+    }
+    if (ac == 4) FGB_RD(4) else if (ac == 2) FGB_RD(2) else FGB_RD(1)
+#undef FGB_RD
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    rreduce_pairs_kernel<<<(unsigned)(n_alpha * (2 * l + 1)), 128, 0, stream>>>(partial, npairs, s_out);
+    return cudaGetLastError();
+}
+
+constexpr int kRdmA = 64, kRdmK = 64, kRdmLd = 36, kRdmStages = 3;
+
+size_t rdots_mma_smem_bytes() { return (size_t)kRdmStages * (kRdmA + kRdmK) * kRdmLd * 8; }
+
+// partial layout [pair][a (64)][kk (128)]
+__global__ void __launch_bounds__(256, 1)
+rdots_mma_kernel(const double* __restrict__ slabs, int n, int k_begin, int k_count, int64_t slab_elems,
+                 const double* __restrict__ m, int64_t m_stride, int n_alpha, double* __restrict__ partial, int nt) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* base = reinterpret_cast<double*>(smem);
+    const int pair = blockIdx.x;
+    int I, J;
+    pair_of(pair, I, J);
+    const bool diag = (I == J);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3, wa = warp & 1, wk = warp >> 1;
+    const int64_t b1 = tile_base(I, J, nt), b2 = tile_base(J, I, nt);
+    // block blk: sub-square r0 = 4*(blk%8), c0 = 4*(blk/8); position p = t*16 + jj*4 + ii
+    auto stage = [&](int blk, int s) {
+        double* st = base + (size_t)s * (kRdmA + kRdmK) * kRdmLd;
+        const int r0 = 4 * (blk & 7), c0 = 4 * (blk >> 3);
+        for (int idx = tid; idx < (kRdmA + kRdmK) * 32; idx += 256) {
+            const int row = idx >> 5, p = idx & 31;
+            const int t = p >> 4, jj = (p >> 2) & 3, ii = p & 3;
+            const int li = r0 + ii, lj = c0 + jj;
+            double* dst = st + row * kRdmLd + p;
+            if (row < kRdmA) {
+                const int gi = t == 0 ? I * 32 + li : J * 32 + lj;
+                const int gj = t == 0 ? J * 32 + lj : I * 32 + li;
+                const bool v = row < n_alpha && gi < n && gj < n && !(diag && t == 1);
+                cp_async8(dst, v ? m + (int64_t)row * m_stride + (int64_t)gj * n + gi : m, v);
+            } else {
+                const int kq = row - kRdmA;
+                const bool v = kq < k_count;
+                const double* slab = slabs + (int64_t)(k_begin + (v ? kq : 0) - 1) * slab_elems;
+                cp_async8(dst, t == 0 ? slab + b1 + swz(li, lj) : slab + b2 + swz(lj, li), v);
+            }
+        }
+    };
+    double d[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[i][j][0] = d[i][j][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kRdmStages - 1; ++s) {
+        stage(s, s);
+        cp_async_commit();
+    }
+    for (int blk = 0; blk < 64; ++blk) {
+        cp_async_wait<kRdmStages - 2>();
+        __syncthreads();
+        if (blk + kRdmStages - 1 < 64) stage(blk + kRdmStages - 1, (blk + kRdmStages - 1) % kRdmStages);
+        cp_async_commit();
+        const double* st = base + (size_t)(blk % kRdmStages) * (kRdmA + kRdmK) * kRdmLd;
+        const double* ms = st;
+        const double* ps = st + kRdmA * kRdmLd;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const int p = 4 * ks + t4, pt = p ^ 16;
+            double a[4], b[4];
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb) a[mb] = ms[(32 * wa + 8 * mb + g) * kRdmLd + p];
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb) {
+                const int kk = 32 * wk + 8 * nb + g, kq = kk >> 1;
+                b[nb] = ps[kq * kRdmLd + ((kk & 1) ? pt : p)];
+            }
+#pragma unroll
+            for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) dmma884(d[mb][nb][0], d[mb][nb][1], a[mb], b[nb]);
+        }
+    }
+    cp_async_wait<0>();
+    double* out = partial + (int64_t)pair * kRdmA * (2 * kRdmK);
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+            const int a = 32 * wa + 8 * mb + g, kk = 32 * wk + 8 * nb + 2 * t4;
+            *reinterpret_cast<double2*>(out + a * (2 * kRdmK) + kk) = make_double2(d[mb][nb][0], d[mb][nb][1]);
+        }
+}
+
+__global__ void __launch_bounds__(128) rreduce_mma_kernel(const double* __restrict__ partial, int npairs, int k_begin,
+                                                          int k_count, int l, double* __restrict__ s_out) {
+    const int a = blockIdx.x / (2 * k_count), kk = blockIdx.x % (2 * k_count);
+    double acc = 0.0;
+    for (int p = threadIdx.x; p < npairs; p += 128) acc += partial[((int64_t)p * kRdmA + a) * (2 * kRdmK) + kk];
+    acc = rwarp_sum(acc);
+    __shared__ double ws[4];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int k = k_begin + (kk >> 1);
+        s_out[(int64_t)a * (2 * l + 1) + ((kk & 1) ? l - k : l + k)] = (ws[0] + ws[1]) + (ws[2] + ws[3]);
+    }
+}
+
+__global__ void __launch_bounds__(128) rtrace_kernel(const double* __restrict__ m, int64_t m_stride, int n, int l,
+                                                     double* __restrict__ s_out) {
+    const int a = blockIdx.x;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += 128) acc += m[(int64_t)a * m_stride + (int64_t)i * n + i];
+    acc = rwarp_sum(acc);
+    __shared__ double ws[4];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) s_out[(int64_t)a * (2 * l + 1) + l] = (ws[0] + ws[1]) + (ws[2] + ws[3]);
+}
+
+size_t rdots_mma_partial_elems(int n) {
+    const int nt = (int)ceil_div(n, kTile);
+    return (size_t)(nt * (nt + 1) / 2) * kRdmA * 2 * kRdmK;
+}
+
+cudaError_t launch_rdots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                             double* partial, double* s_out, cudaStream_t stream, int* launches) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int npairs = nt * (nt + 1) / 2;
+    const int64_t slab = (int64_t)nt * nt * kTileElems;
+    const size_t smem = rdots_mma_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(rdots_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int nl = 0;
+    for (int k0 = 1; k0 <= l; k0 += kRdmK) {
+        const int kc = min(kRdmK, l - k0 + 1);
+        rdots_mma_kernel<<<npairs, 256, smem, stream>>>((const double*)slabs, n, k0, kc, slab, (const double*)m,
+                                                        m_stride, n_alpha, partial, nt);
+        rreduce_mma_kernel<<<n_alpha * 2 * kc, 128, 0, stream>>>(partial, npairs, k0, kc, l, s_out);
+        nl += 2;
+    }
+    rtrace_kernel<<<n_alpha, 128, 0, stream>>>((const double*)m, m_stride, n, l, s_out);
+    if (launches) *launches = nl + 1;
+    return cudaGetLastError();
+}
+
+}  // namespace fgb

@@ -288,3 +288,52 @@ def test_complex64_path_within_1e4_of_fp64_oracle(n, l, b):
     assert np.array_equal(fg.synthesize(g, [0.0])[0], np.eye(n))  # order 0 still exact
     with pytest.raises(fg.ParameterError):
         fg.PowerCache(prep.random_unitary(7, 1), 2, dtype=fg.C64)  # odd n: TMA alignment
+
+
+# --------------------------------------------------------------------------- real-F path
+
+@pytest.mark.parametrize("n,l,b", [(64, 8, 5), (100, 12, 33), (256, 32, 17)])
+def test_real_f_path_matches_complex_path_and_oracle(n, l, b, monkeypatch):
+    """Graph-derived F is real: the cache is stored real and the real kernels run. They must agree
+    with the oracle (bit-exact single-order synthesis) and with the forced complex path."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 7 + n)))
+    assert np.all(f.imag == 0)
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    assert g.is_real()
+    monkeypatch.setenv("FGFRFT_NO_REAL", "1")
+    gc = fg.PowerCache(f, l)
+    monkeypatch.delenv("FGFRFT_NO_REAL")
+    assert not gc.is_real()
+    ge = fg.PowerCache(f, l, powers=o.slabs)
+    assert ge.is_real()
+    for k in (1, 2, l):
+        assert rel(g.power(k), o.power(k)) <= 1e-13
+        assert np.all(g.power(k).imag == 0)
+    for a in (0.37, -1.1, 0.0, 2.0):  # scalar exact path on identical cache bytes
+        q = fg.synthesize(ge, [a])[0]
+        assert np.array_equal(q, O.fgfrft_matrix(o, a))
+        assert np.array_equal(fg.synthesize(ge, [a], which=fg.DQ)[0], O.fgfrft_grad(o, a))
+    alphas = list(np.linspace(-0.5, 1.9, 12))  # sweep: DMMA kernels
+    qs, qc = fg.synthesize(g, alphas), fg.synthesize(gc, alphas)
+    for i, a in enumerate(alphas):
+        assert rel(qs[i], O.fgfrft_matrix(o, a)) <= 1e-13
+        assert rel(qs[i], qc[i]) <= 1e-13
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    for al in ([0.37], alphas):
+        y, yc = fg.apply_series(g, al, x), fg.apply_series(gc, al, x)
+        yi = fg.apply_series(g, al, x, inverse=True)
+        loss, dl, _ = fg.mse_step(g, al, x, xc)
+        lc, dlc, _ = fg.mse_step(gc, al, x, xc)
+        for i, a in enumerate(al):
+            q = O.fgfrft_matrix(o, a)
+            assert rel(y[i], q @ x) <= 1e-13 and rel(y[i], yc[i]) <= 1e-13
+            assert rel(yi[i], q.T @ x) <= 1e-13
+            lr, dr, _ = O.dlda_mse(o, a, x, xc)
+            assert abs(loss[i] - lr) <= 1e-12 * lr and abs(loss[i] - lc[i]) <= 1e-12 * lr
+            _, dc = O.sinc_coeffs(a, l)
+            s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
+            tol = 1e-10 * np.sum(np.abs(dc * s_ref))
+            assert abs(dl[i] - dr) <= tol and abs(dl[i] - dlc[i]) <= tol

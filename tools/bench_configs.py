@@ -55,7 +55,8 @@ def run(name, cfg, peaks, budget, dtype=0):
     q = torch.empty((1, n, n), dtype=ct, device="cuda")
     t_syn = timed(stream, lambda: fg._check(lib.fgfrft_synthesize_dev(cache.handle, one.ctypes.data, 1, 0, 0,
                                                                        q.data_ptr())))
-    syn_bytes = (L + 1) * n * n * float(es)
+    real = cache.is_real()
+    syn_bytes = (L * (8.0 if real else float(es)) + float(es)) * n * n
     del q
     x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda().to(ct)
     xc = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda().to(ct)
@@ -68,13 +69,13 @@ def run(name, cfg, peaks, budget, dtype=0):
                                                                       xc.data_ptr(), b, None, loss.data_ptr(),
                                                                       dl.data_ptr())))
     out = {
-        "config": name, "dtype": "c128" if dtype == 0 else "c64", "n": n, "l": L, "b": b, "orders": A,
-        "cache_gb": L * n * n * es / 1e9,
-        "cache_build": {"s": build_s, "tflops": (L - 1) * 8.0 * n ** 3 / build_s / 1e12},
+        "config": name, "dtype": "c128" if dtype == 0 else "c64", "real_f": real, "n": n, "l": L, "b": b,
+        "orders": A, "cache_gb": L * n * n * (8 if real else es) / 1e9,
+        "cache_build": {"s": build_s, "tflops": (L - 1) * (2.0 if real else 8.0) * n ** 3 / build_s / 1e12},
         "synthesis_one_order": {"ms": t_syn, "gbs": syn_bytes / (t_syn * 1e-3) / 1e9,
                                 "frac_hbm": syn_bytes / (t_syn * 1e-3) / 1e9 / peaks["hbm"]},
         "apply": {"ms": t_app, "signal_nodes_per_s": n * b * A / (t_app * 1e-3),
-                  "gemm_tflops_equiv": 8.0 * n * n * b * A / (t_app * 1e-3) / 1e12},
+                  "gemm_tflops_equiv": (4.0 if real else 8.0) * n * n * b * A / (t_app * 1e-3) / 1e12},
         "mse_step": {"ms": t_step, "signal_nodes_per_s": n * b * A / (t_step * 1e-3)},
     }
     cache.close()
