@@ -31,17 +31,23 @@ namespace fgb {
 // CTA 128 x 128, BK = 16, 8 warps as 4 (m) x 2 (n), warp tile 32 x 64 (4 x 8 DMMA tiles),
 // 4-stage cp.async ring of 8-byte elements, fragment loads conflict free (ld = 136 doubles).
 // =====================================================================================
-constexpr int kRgBM = 128, kRgBN = 128, kRgBK = 16, kRgLd = 136, kRgStages = 4;
+constexpr int kRgBM = 128, kRgBN = 128, kRgBK = 16, kRgStages = 4;
+constexpr int kRgLdW = 136;  // [k][m] / [k][n] layouts: 128 + 8 doubles (row stride = 8 mod 16 banks pairs)
+constexpr int kRgLdN = 20;   // [m][k] / [n][k] layouts: 16 + 4 doubles
+constexpr int kRgOp = 2560;  // doubles per operand stage (max of 16 x 136 and 128 x 20)
 
-size_t rgemm_smem_bytes() { return (size_t)kRgStages * 2 * kRgBK * kRgLd * 8; }
+size_t rgemm_smem_bytes() { return (size_t)kRgStages * 2 * kRgOp * 8; }
 
+// Staging: every mode reads global memory in contiguous runs (a warp covers 256 B) and writes
+// shared memory contiguously; the layout per mode keeps the DMMA fragment reads at the minimum
+// two wavefronts. A: AM 0 / 2 -> [k][m], AM 1 -> [m][k]. B: BM 0 / 1 -> [n][k], BM 2 -> [k][n].
 template <int AM, int BM, int CM>
 __global__ void __launch_bounds__(256, 1)
 rgemm_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda, int64_t sA, const double* __restrict__ B,
              int64_t ldb, int64_t sB, double* __restrict__ C, int64_t ldc, int64_t sC) {
     extern __shared__ __align__(128) unsigned char smem[];
-    double* As = reinterpret_cast<double*>(smem);                   // [stage][k][m]
-    double* Bs = As + (size_t)kRgStages * kRgBK * kRgLd;            // [stage][k][n]
+    double* As = reinterpret_cast<double*>(smem);
+    double* Bs = As + (size_t)kRgStages * kRgOp;
     const int bz = blockIdx.z;
     A += bz * sA;
     B += bz * sB;
@@ -51,37 +57,60 @@ rgemm_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda, int
     const int wm = warp & 3, wn = warp >> 2, g = lane >> 2, t = lane & 3;
     const int nk = (K + kRgBK - 1) / kRgBK;
 
-    auto a_addr = [&](int m, int k) -> int64_t {
-        if (AM == 0) return (int64_t)m + (int64_t)k * lda;
-        if (AM == 1) return (int64_t)k + (int64_t)m * lda;
-        return ((int64_t)m + (int64_t)(k >> 1) * lda) * 2 + (k & 1);
-    };
-    auto b_addr = [&](int k, int n) -> int64_t {
-        if (BM == 0) return (int64_t)k + (int64_t)n * ldb;
-        if (BM == 1) return ((int64_t)k + (int64_t)(n >> 1) * ldb) * 2 + (n & 1);
-        return ((int64_t)n + (int64_t)(k >> 1) * ldb) * 2 + (k & 1);
-    };
     auto load_stage = [&](int kt, int s) {
         const int k0 = kt * kRgBK;
-        double* as = As + (size_t)s * kRgBK * kRgLd;
-        double* bs = Bs + (size_t)s * kRgBK * kRgLd;
+        double* as = As + (size_t)s * kRgOp;
+        double* bs = Bs + (size_t)s * kRgOp;
 #pragma unroll
         for (int j = 0; j < (kRgBM * kRgBK) / 256; ++j) {
             const int idx = tid + 256 * j;
-            // AM 0 / 2: m fastest (contiguous in memory for AM 0); AM 1: k fastest
-            const int m = AM == 1 ? idx / kRgBK : idx % kRgBM;
-            const int k = AM == 1 ? idx % kRgBK : idx / kRgBM;
+            int m, k;
+            int64_t src;
+            double* dst;
+            if (AM == 0) {  // A(m,k) = A[m + k*lda]: m fastest
+                m = idx & 127;
+                k = idx >> 7;
+                src = (int64_t)(m0 + m) + (int64_t)(k0 + k) * lda;
+                dst = as + k * kRgLdW + m;
+            } else if (AM == 1) {  // A(m,k) = A[k + m*lda]: k fastest, [m][k]
+                k = idx & 15;
+                m = idx >> 4;
+                src = (int64_t)(k0 + k) + (int64_t)(m0 + m) * lda;
+                dst = as + m * kRgLdN + k;
+            } else {  // complex G(m, j).c with k = 2j + c: 16 m per c, the (re, im) halves of 16 elements
+                const int c = (idx >> 4) & 1;
+                m = (idx & 15) + 16 * ((idx >> 5) & 7);
+                k = 2 * (idx >> 8) + c;
+                src = ((int64_t)(m0 + m) + (int64_t)((k0 + k) >> 1) * lda) * 2 + c;
+                dst = as + k * kRgLdW + m;
+            }
             const bool v = (m0 + m < M) && (k0 + k < K);
-            cp_async8(as + k * kRgLd + m, v ? A + a_addr(m0 + m, k0 + k) : A, v);
+            cp_async8(dst, v ? A + src : A, v);
         }
 #pragma unroll
         for (int j = 0; j < (kRgBN * kRgBK) / 256; ++j) {
             const int idx = tid + 256 * j;
-            // BM 0: k fastest (contiguous); BM 1 / 2: n fastest
-            const int n = BM == 0 ? idx / kRgBK : idx % kRgBN;
-            const int k = BM == 0 ? idx % kRgBK : idx / kRgBN;
+            int n, k;
+            int64_t src;
+            double* dst;
+            if (BM == 0) {  // B(k,n) = B[k + n*ldb]: k fastest, [n][k]
+                k = idx & 15;
+                n = idx >> 4;
+                src = (int64_t)(k0 + k) + (int64_t)(n0 + n) * ldb;
+            } else if (BM == 1) {  // complex X(k, j).c with n = 2j + c: 16 k per c, [n][k]
+                const int c = (idx >> 4) & 1;
+                k = idx & 15;
+                n = 2 * (idx >> 5) + c;
+                src = ((int64_t)(k0 + k) + (int64_t)((n0 + n) >> 1) * ldb) * 2 + c;
+            } else {  // complex X(n, j).c with k = 2j + c: 16 n per c, [k][n]
+                const int c = (idx >> 4) & 1;
+                n = (idx & 15) + 16 * ((idx >> 5) & 7);
+                k = 2 * (idx >> 8) + c;
+                src = ((int64_t)(n0 + n) + (int64_t)((k0 + k) >> 1) * ldb) * 2 + c;
+            }
+            dst = BM == 2 ? bs + k * kRgLdW + n : bs + n * kRgLdN + k;
             const bool v = (n0 + n < N) && (k0 + k < K);
-            cp_async8(bs + k * kRgLd + n, v ? B + b_addr(k0 + k, n0 + n) : B, v);
+            cp_async8(dst, v ? B + src : B, v);
         }
     };
 
@@ -103,15 +132,21 @@ rgemm_kernel(int M, int N, int K, const double* __restrict__ A, int64_t lda, int
             if (nx < nk) load_stage(nx, nx % kRgStages);
             cp_async_commit();
         }
-        const double* as = As + (size_t)(kt % kRgStages) * kRgBK * kRgLd;
-        const double* bs = Bs + (size_t)(kt % kRgStages) * kRgBK * kRgLd;
+        const double* as = As + (size_t)(kt % kRgStages) * kRgOp;
+        const double* bs = Bs + (size_t)(kt % kRgStages) * kRgOp;
 #pragma unroll
         for (int kk = 0; kk < kRgBK; kk += 4) {
             double a[4], b[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = as[(kk + t) * kRgLd + wm * 32 + i * 8 + g];
+            for (int i = 0; i < 4; ++i) {
+                const int m = wm * 32 + i * 8 + g;
+                a[i] = AM == 1 ? as[m * kRgLdN + kk + t] : as[(kk + t) * kRgLdW + m];
+            }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) b[j] = bs[(kk + t) * kRgLd + wn * 64 + j * 8 + g];
+            for (int j = 0; j < 8; ++j) {
+                const int n = wn * 64 + j * 8 + g;
+                b[j] = BM == 2 ? bs[(kk + t) * kRgLdW + n] : bs[n * kRgLdN + kk + t];
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll

@@ -2,9 +2,8 @@
 
   python tools/profile_kernels.py            # plain run (must exit 0 before ncu is used)
   ncu --set full -k regex:'synth|zgemm|power_dots' ... python tools/profile_kernels.py
-Order of launches after the cache build: synth<double,1> (one order), synth<double,4>
-(64-order sweep), zgemm_dmma<0,0> (Q X, 64 orders batched), zgemm_dmma<0,1> (G X^H),
-power_dots<4>.
+Config 2's F is real, so the real-F kernels run: rsynth_pairs (one order), rsynth_sweep
+(64-order sweep), rgemm<0,1,1> (Q X, 64 orders batched), rgemm<2,2,0> (Re G X^H), rdots_mma.
 """
 import os
 import sys
