@@ -245,10 +245,13 @@ cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, in
 
 constexpr int kDmA = 64;        // orders per launch (rows of D)
 constexpr int kDmK = 64;        // powers per launch (kk = 128 columns of D)
-constexpr int kDmLd = 34;       // complex elements per staged row (32 + pad)
+constexpr int kDmLd = 34;       // complex elements per staged M row (32 + pad)
+constexpr int kDmLdP = 36;      // power rows: [t=0: 16][pad 2][t=1: 16][pad 2] complex; 64-bit fragment
+constexpr int kDmPT1 = 18;      // loads of one half-warp then hit 16 distinct bank pairs
 constexpr int kDmStages = 3;
+constexpr int kDmStage = kDmA * kDmLd + kDmK * kDmLdP;  // complex elements per stage
 
-size_t dots_mma_smem_bytes() { return (size_t)kDmStages * (kDmA + kDmK) * kDmLd * 16; }
+size_t dots_mma_smem_bytes() { return (size_t)kDmStages * kDmStage * 16; }
 
 // partial layout: [pair][a (kDmA)][kk (2*kDmK)]
 __global__ void __launch_bounds__(256, 1)
@@ -271,13 +274,14 @@ power_dots_mma_kernel(const double2* __restrict__ slabs, int n, int k_begin, int
     // Position index p = t*16 + jj*4 + ii: t = 0 -> (I*32+r0+ii, J*32+c0+jj); t = 1 -> its
     // transpose (J*32+c0+jj, I*32+r0+ii).
     auto stage = [&](int blk, int s) {
-        double2* st = stage_base + (size_t)s * (kDmA + kDmK) * kDmLd;
+        double2* st = stage_base + (size_t)s * kDmStage;
         const int r0 = 4 * (blk & 7), c0 = 4 * (blk >> 3);
         for (int idx = tid; idx < (kDmA + kDmK) * 32; idx += 256) {
             const int row = idx >> 5, p = idx & 31;
             const int t = p >> 4, jj = (p >> 2) & 3, ii = p & 3;
             const int li = r0 + ii, lj = c0 + jj;  // local (row, col) in tile (I,J)
-            double2* dst = st + row * kDmLd + p;
+            double2* dst = row < kDmA ? st + row * kDmLd + p
+                                      : st + kDmA * kDmLd + (row - kDmA) * kDmLdP + t * kDmPT1 + (p & 15);
             if (row < kDmA) {
                 const int a = row;
                 const int gi = t == 0 ? I * 32 + li : J * 32 + lj;
@@ -312,14 +316,14 @@ power_dots_mma_kernel(const double2* __restrict__ slabs, int n, int k_begin, int
         __syncthreads();
         if (blk + kDmStages - 1 < nblk) stage(blk + kDmStages - 1, (blk + kDmStages - 1) % kDmStages);
         cp_async_commit();
-        const double2* st = stage_base + (size_t)(blk % kDmStages) * (kDmA + kDmK) * kDmLd;
+        const double2* st = stage_base + (size_t)(blk % kDmStages) * kDmStage;
         const double* ms = reinterpret_cast<const double*>(st);
         const double* ps = reinterpret_cast<const double*>(st + kDmA * kDmLd);
 #pragma unroll
         for (int ks = 0; ks < 16; ++ks) {
             const int e = 4 * ks + t4;             // K index: (position p = e >> 1, component e & 1)
             const int p = e >> 1, comp = e & 1;
-            const int pt = p ^ 16;                 // transposed partner position
+            const int tp = p >> 4, pl = p & 15;    // transposed partner: same pl, other half
             double a[4], b[4];
 #pragma unroll
             for (int mb = 0; mb < 4; ++mb) a[mb] = ms[((32 * wa + 8 * mb + g) * kDmLd + p) * 2 + comp];
@@ -327,7 +331,7 @@ power_dots_mma_kernel(const double2* __restrict__ slabs, int n, int k_begin, int
             for (int nb = 0; nb < 4; ++nb) {
                 const int kk = 32 * wk + 8 * nb + g;
                 const int kq = kk >> 1;
-                const double v = (kk & 1) ? ps[(kq * kDmLd + pt) * 2 + comp] : ps[(kq * kDmLd + p) * 2 + comp];
+                const double v = ps[(kq * kDmLdP + (tp ^ (kk & 1)) * kDmPT1 + pl) * 2 + comp];
                 b[nb] = ((kk & 1) && comp) ? -v : v;
             }
 #pragma unroll

@@ -29,12 +29,14 @@ namespace fgb {
 //   CM 0: C[m + n*ldc] = D(m,n)                  (real)
 //   CM 1: C[(m + (n>>1)*ldc)*2 + (n&1)] = D(m,n)  (complex merge: columns (2j, 2j+1) -> Y(m,j))
 // CTA 128 x 128, BK = 16, 8 warps as 4 (m) x 2 (n), warp tile 32 x 64 (4 x 8 DMMA tiles),
-// 4-stage cp.async ring of 8-byte elements, fragment loads conflict free (ld = 136 doubles).
+// 4-stage cp.async ring of 8-byte elements, fragment loads conflict free (see kRgLdW).
 // =====================================================================================
 constexpr int kRgBM = 128, kRgBN = 128, kRgBK = 16, kRgStages = 4;
-constexpr int kRgLdW = 136;  // [k][m] / [k][n] layouts: 128 + 8 doubles (row stride = 8 mod 16 banks pairs)
+// 64-bit shared loads are serviced per half-warp (16 lanes = g 0..3 x t 0..3): strides are
+// chosen = 4 (mod 16) doubles so those 16 lanes hit 16 distinct bank pairs.
+constexpr int kRgLdW = 132;  // [k][m] / [k][n] layouts: 128 + 4 doubles
 constexpr int kRgLdN = 20;   // [m][k] / [n][k] layouts: 16 + 4 doubles
-constexpr int kRgOp = 2560;  // doubles per operand stage (max of 16 x 136 and 128 x 20)
+constexpr int kRgOp = 2560;  // doubles per operand stage (max of 16 x 132 and 128 x 20)
 
 size_t rgemm_smem_bytes() { return (size_t)kRgStages * 2 * kRgOp * 8; }
 
@@ -415,7 +417,8 @@ cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* co
 // =====================================================================================
 constexpr int kRwA = 64, kRwKc = 64, kRwStK = 8, kRwStages = 3;
 constexpr int kRwCLd = 2 * kRwKc + 4;
-constexpr int kRwPLd = 136;  // doubles per staged power: 2 x 64 positions + pad
+constexpr int kRwPLd = 136;  // doubles per staged power: [t=0: 64][pad 4][t=1: 64][pad 4]
+constexpr int kRwT1 = 68;    // offset of the transposed half: (k,+)/(k,-) rows land 4 banks apart
 
 size_t rsweep_smem_bytes() {
     const size_t cs = (size_t)kRwA * kRwCLd * 8, st = (size_t)kRwStages * kRwStK * kRwPLd * 8;
@@ -469,7 +472,7 @@ rsynth_sweep_kernel(const double* __restrict__ slabs, int n, int l_used, int64_t
                 const bool v = kq < kc;
                 const double* slab = slabs + (int64_t)(k0 + (v ? kq : 0) - 1) * slab_elems;
                 const double* src = t == 0 ? slab + b1 + swz(r0 + ii, c0 + jj) : slab + b2 + swz(c0 + jj, r0 + ii);
-                cp_async8(dst0 + kp * kRwPLd + t * 64 + p, src, v);
+                cp_async8(dst0 + kp * kRwPLd + t * kRwT1 + p, src, v);
             }
         };
 #pragma unroll
@@ -489,7 +492,7 @@ rsynth_sweep_kernel(const double* __restrict__ slabs, int n, int l_used, int64_t
                 const int tt = sign ? 1 - tw : tw;  // (k,+): own tile; (k,-): the transposed partner
                 double b[2];
 #pragma unroll
-                for (int nb = 0; nb < 2; ++nb) b[nb] = sb[kp * kRwPLd + tt * 64 + pbase + 8 * nb + g];
+                for (int nb = 0; nb < 2; ++nb) b[nb] = sb[kp * kRwPLd + tt * kRwT1 + pbase + 8 * nb + g];
                 const double* crow = cs + g * kRwCLd + 16 * st + kkl;
 #pragma unroll
                 for (int mb = 0; mb < 8; ++mb) {
@@ -741,8 +744,10 @@ cudaError_t launch_rdots(const void* slabs, int n, int l, const void* m, int64_t
 }
 
 constexpr int kRdmA = 64, kRdmK = 64, kRdmLd = 36, kRdmStages = 3;
+constexpr int kRdmLdP = 40, kRdmPT1 = 20;  // power rows: [t=0: 16][pad 4][t=1: 16][pad 4]
+constexpr int kRdmStage = kRdmA * kRdmLd + kRdmK * kRdmLdP;
 
-size_t rdots_mma_smem_bytes() { return (size_t)kRdmStages * (kRdmA + kRdmK) * kRdmLd * 8; }
+size_t rdots_mma_smem_bytes() { return (size_t)kRdmStages * kRdmStage * 8; }
 
 // partial layout [pair][a (64)][kk (128)]
 __global__ void __launch_bounds__(256, 1)
@@ -759,13 +764,14 @@ rdots_mma_kernel(const double* __restrict__ slabs, int n, int k_begin, int k_cou
     const int64_t b1 = tile_base(I, J, nt), b2 = tile_base(J, I, nt);
     // block blk: sub-square r0 = 4*(blk%8), c0 = 4*(blk/8); position p = t*16 + jj*4 + ii
     auto stage = [&](int blk, int s) {
-        double* st = base + (size_t)s * (kRdmA + kRdmK) * kRdmLd;
+        double* st = base + (size_t)s * kRdmStage;
         const int r0 = 4 * (blk & 7), c0 = 4 * (blk >> 3);
         for (int idx = tid; idx < (kRdmA + kRdmK) * 32; idx += 256) {
             const int row = idx >> 5, p = idx & 31;
             const int t = p >> 4, jj = (p >> 2) & 3, ii = p & 3;
             const int li = r0 + ii, lj = c0 + jj;
-            double* dst = st + row * kRdmLd + p;
+            double* dst = row < kRdmA ? st + row * kRdmLd + p
+                                      : st + kRdmA * kRdmLd + (row - kRdmA) * kRdmLdP + t * kRdmPT1 + (p & 15);
             if (row < kRdmA) {
                 const int gi = t == 0 ? I * 32 + li : J * 32 + lj;
                 const int gj = t == 0 ? J * 32 + lj : I * 32 + li;
@@ -794,19 +800,19 @@ rdots_mma_kernel(const double* __restrict__ slabs, int n, int k_begin, int k_cou
         __syncthreads();
         if (blk + kRdmStages - 1 < 64) stage(blk + kRdmStages - 1, (blk + kRdmStages - 1) % kRdmStages);
         cp_async_commit();
-        const double* st = base + (size_t)(blk % kRdmStages) * (kRdmA + kRdmK) * kRdmLd;
+        const double* st = base + (size_t)(blk % kRdmStages) * kRdmStage;
         const double* ms = st;
         const double* ps = st + kRdmA * kRdmLd;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-            const int p = 4 * ks + t4, pt = p ^ 16;
+            const int p = 4 * ks + t4, tp = p >> 4, pl = p & 15;
             double a[4], b[4];
 #pragma unroll
             for (int mb = 0; mb < 4; ++mb) a[mb] = ms[(32 * wa + 8 * mb + g) * kRdmLd + p];
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb) {
                 const int kk = 32 * wk + 8 * nb + g, kq = kk >> 1;
-                b[nb] = ps[kq * kRdmLd + ((kk & 1) ? pt : p)];
+                b[nb] = ps[kq * kRdmLdP + (tp ^ (kk & 1)) * kRdmPT1 + pl];
             }
 #pragma unroll
             for (int mb = 0; mb < 4; ++mb)
