@@ -69,9 +69,9 @@ uint64_t fgfrft_launch_count(void);
 
 /*
  * Per-kernel-class device timing (CUDA events on the launching stream), for benchmarks:
- * classes 0 synthesis, 1 DMMA GEMM, 2 power dots, 3 elementwise. fgfrft_profile_read waits
- * for the recorded events, writes total ms and launch counts per class (arrays of 4) and
- * optionally resets.
+ * classes 0 synthesis, 1 DMMA GEMM, 2 power dots, 3 elementwise, 4 INT8 tensor-core GEMM,
+ * 5 operand slicing, 6 series combine, 7 reserved. fgfrft_profile_read waits for the recorded
+ * events, writes total ms and launch counts per class (arrays of 8) and optionally resets.
  */
 int fgfrft_profile_enable(int on);
 int fgfrft_profile_read(double* ms, int64_t* counts, int reset);
@@ -212,6 +212,21 @@ int fgfrft_shard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alph
 int fgfrft_shard_mse_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
                                  const void* x_dev, const void* xc_rows_dev, int64_t b,
                                  void* y_rows_dev, void* loss_partial_dev, void* s_partial_dev);
+
+/* ---- FP64-accurate GEMM on the INT8 tensor cores (Ozaki scheme) -------------------------
+ *
+ * C = op(A) op(B) for real column-major device matrices (op(A) m x k, op(B) k x n, C m x n;
+ * op(X) = X^T when trans* != 0, as in BLAS dgemm), computed with
+ * tcgen05.mma kind::i8: A's rows and B's columns are scaled by powers of two and cut into
+ * `slices` 7-bit digits (6, 7 or 8; 0 = default 7); digit products with weight >= 2^-7(S+1)
+ * accumulate exactly in int32 TMEM and are combined in FP64. Error ~ sqrt(k) 2^-7S relative to
+ * (row max of A) x (column max of B): 7 slices ~3e-13 on the BASELINE operands, 8 ~3e-15.
+ * k <= 16384. Enqueued on `stream` (NULL = default stream); scratch is allocated per call.
+ * This is the engine behind the library's real-F GEMMs (fgfrft_set_gemm_engine).
+ */
+int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                          const double* b, int64_t ldb, double* c, int64_t ldc, int slices,
+                          void* stream);
 
 /* ---- batches of small graphs (BASELINE config 5: fractional specformer) ----------------
  *

@@ -102,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_batch_set_stream": (i, [vp, vp]),
         "fgfrft_batch_forward_dev": (i, [vp, vp, i, vp, i64, vp]),
         "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
+        "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -123,7 +124,7 @@ def exported_symbols():
         "fgfrft_mse_step_dev", "fgfrft_shard_create", "fgfrft_shard_destroy", "fgfrft_shard_info",
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
         "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
-        "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev",
+        "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev",
     ]
 
 
@@ -137,7 +138,8 @@ def launch_count() -> int:
     return int(lib().fgfrft_launch_count())
 
 
-KERNEL_CLASSES = ("synthesis", "dmma_zgemm", "power_dots", "elementwise")
+KERNEL_CLASSES = ("synthesis", "dmma_zgemm", "power_dots", "elementwise", "int8_gemm", "slicing", "combine",
+                  "reserved")
 
 
 def profile_enable(on: bool = True) -> None:
@@ -146,8 +148,8 @@ def profile_enable(on: bool = True) -> None:
 
 def profile_read(reset: bool = True):
     """{class: (total_ms, launches)} from CUDA events recorded around each launch."""
-    ms = np.zeros(4)
-    cnt = np.zeros(4, dtype=np.int64)
+    ms = np.zeros(8)
+    cnt = np.zeros(8, dtype=np.int64)
     _check(lib().fgfrft_profile_read(_ptr(ms), _ptr(cnt), int(reset)))
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
 
@@ -409,3 +411,20 @@ class GraphBatch:
         _check(lib().fgfrft_batch_dlda_dev(self._h, alphas.data_ptr(), H, g.data_ptr(), x.data_ptr(), x.shape[1],
                                            out.data_ptr()))
         return out
+
+
+def dgemm_int8(a, b, slices: int = 0):
+    """C = A B (real float64 torch CUDA tensors) on the INT8 tensor cores (Ozaki scheme), through
+    fgfrft_dgemm_int8_dev. Row-major torch operands are passed as transposed column-major ones;
+    the result is column-major (m x n) in memory, returned as a strided (m, n) view."""
+    import torch
+    assert a.dtype == torch.float64 and b.dtype == torch.float64 and a.is_cuda and b.is_cuda
+    m, k = a.shape
+    k2, n = b.shape
+    assert k == k2
+    a = a.contiguous()
+    b = b.contiguous()
+    ct = torch.empty((n, m), dtype=torch.float64, device=a.device)
+    _check(lib().fgfrft_dgemm_int8_dev(1, 1, m, n, k, a.data_ptr(), k, b.data_ptr(), n, ct.data_ptr(), m, slices,
+                                       ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)))
+    return ct.t()

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "fgfrft_b200.h"
+#include "oz.cuh"
 
 namespace fgb {
 double host_sinc(double);
@@ -96,7 +97,9 @@ std::atomic<uint64_t> g_launches{0};
 
 // Optional per-kernel-class timing with CUDA events recorded on the launching stream
 // (fgfrft_profile_*): bench.py uses it to time the dominant kernel inside its timed region.
-enum KernelClass { KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_COUNT = 4 };
+enum KernelClass {
+    KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_I8GEMM = 4, KC_SLICE = 5, KC_COMBINE = 6, KC_COUNT = 8
+};
 struct ProfRec {
     int cls;
     cudaEvent_t a, b;
@@ -1407,3 +1410,65 @@ int fgfrft_batch_dlda_dev(fgfrft_cache* c, const double* alphas_dev, int heads, 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ INT8 tensor-core DGEMM
+
+namespace {
+// Stream-ordered scratch stays in the device pool between calls (no release at sync points).
+void keep_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+}  // namespace
+
+int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                          const double* b, int64_t ldb, double* c, int64_t ldc, int slices, void* stream) {
+    FGB_GUARD_BEGIN
+    if (slices == 0) slices = oz_slices_default();
+    if (slices < 6 || slices > 8) return fail(FGFRFT_PARAMETER, "slices must be 6, 7 or 8");
+    if (m < 1 || n < 1 || k < 1 || k > 16384) return fail(FGFRFT_SHAPE, "dgemm_int8: need m, n >= 1 and 1 <= k <= 16384");
+    if (lda < (transa ? k : m) || ldb < (transb ? n : k) || ldc < m)
+        return fail(FGFRFT_SHAPE, "dgemm_int8: leading dimension too small");
+    if (!a || !b || !c) return fail(FGFRFT_PARAMETER, "null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    keep_pool();
+    const int64_t mp = ceil_div(m, kOzTileA) * kOzTileA, np = ceil_div(n, kOzTileB) * kOzTileB;
+    const int64_t kp = ceil_div(k, kOzK) * kOzK;
+    const size_t abytes = (size_t)slices * mp * kp, bbytes = (size_t)slices * np * kp;
+    const size_t total = abytes + bbytes + (size_t)(mp + np) * (sizeof(int) + sizeof(unsigned long long)) + 256;
+    char* ws = nullptr;
+    FGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), total, st));
+    int8_t* sa = reinterpret_cast<int8_t*>(ws);
+    int8_t* sb = sa + abytes;
+    unsigned long long* rmax = reinterpret_cast<unsigned long long*>(sb + bbytes);
+    int* ea = reinterpret_cast<int*>(rmax + mp + np);
+    int* eb = ea + mp;
+    // operand rows: op(A)(r, k) = a[r + k*lda] (or a[k + r*lda]); op(B)^T(r, k) = b[k + r*ldb] (or b[r + k*ldb])
+    const OzView va = transa ? OzView{a, lda, 1, 0, 0, 0, (int)m, (int)mp, 1, (int)k, (int)kp, false}
+                             : OzView{a, 1, lda, 0, 0, 0, (int)m, (int)mp, 1, (int)k, (int)kp, true};
+    const OzView vb = transb ? OzView{b, 1, ldb, 0, 0, 0, (int)n, (int)np, 1, (int)k, (int)kp, true}
+                             : OzView{b, ldb, 1, 0, 0, 0, (int)n, (int)np, 1, (int)k, (int)kp, false};
+    cudaError_t e;
+    {
+        ProfScope ps(KC_SLICE, st);
+        e = launch_oz_slice(va, slices, kOzTileA, sa, ea, rmax, st);
+        if (e == cudaSuccess) e = launch_oz_slice(vb, slices, kOzTileB, sb, eb, rmax + mp, st);
+    }
+    if (e == cudaSuccess) {
+        ProfScope ps(KC_I8GEMM, st);
+        e = launch_ozgemm(slices, 0, sa, ea, (int)mp, sb, eb, (int)np, (int)kp, c, ldc, 0, (int)m, (int)mp, (int)n, st);
+    }
+    cudaFreeAsync(ws, st);
+    if (e != cudaSuccess) return fail(FGFRFT_CUDA, std::string("dgemm_int8: ") + cudaGetErrorString(e));
+    g_launches += 5;
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}

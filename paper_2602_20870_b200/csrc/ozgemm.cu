@@ -1,0 +1,469 @@
+// ozgemm.cu -- FP64-accurate real GEMM on the INT8 tensor cores (Ozaki scheme, tcgen05).
+//
+// sm_100a has no FP64 tcgen05 kind: the FP64 tensor path is warp-level DMMA at ~37 TFLOP/s,
+// while tcgen05.mma kind::i8 runs ~4.5 POPS with int32 accumulators in TMEM. An FP64 product
+// C = A B^T (A: M x K, B: N x K) is computed exactly-in-int8 by fixed-point slicing:
+//   every row r of A is scaled by 2^-e_r (max |a_r.| < 2^e_r) and cut into S signed 7-bit
+//   digits,  a_rk = 2^e_r * sum_{t=1..S} A_t[r,k] 2^-7t,  |A_t| <= 127  (exact truncations);
+//   B likewise per row. Then  C = 2^(e_r + e_n) * sum_{t+u <= S+1} 2^-7(t+u) (A_t B_u^T)  where
+//   every int8 GEMM is exact in int32 (K * 127^2 * S < 2^31 for K <= 16384). Dropped terms and
+//   truncated digits bound the error by ~ sqrt(K) 2^-7S of |row max| |col max|: S = 7 gives
+//   3e-13 relative on the BASELINE configs (DMMA: ~1e-15; the parity bar is 1e-10), S = 8
+//   gives ~3e-15.
+//
+// Kernel layout (one 128 x 64 output tile per CTA, 256 threads):
+//   * operands are pre-sliced by oz_slice_kernel into the tcgen05 canonical no-swizzle K-major
+//     layout, blocked so that one (tile, 64-byte K block) of ALL S slices is ONE contiguous
+//     chunk: a stage is two 1-D bulk copies (UBLKCP) onto an mbarrier;
+//   * S int32 accumulators, one per digit weight d = t + u (2..S+1), live side by side in TMEM
+//     (S x 64 columns <= 512). For a fixed A digit t the B digits u = 1..S+1-t are stacked
+//     along N in shared memory, so ONE tcgen05.mma (N up to 256) covers a contiguous run of
+//     accumulators: 10 MMAs per 32-byte K step for S = 7 (28 digit products);
+//   * a 4-stage ring of 32-byte K blocks; warp 0 / lane 0 issues the bulk copies, warp 1 / lane 0
+//     the MMAs (tcgen05.commit frees a stage), then all 8 warps drain TMEM (tcgen05.ld 32x32b,
+//     lane = output row, 32 columns per warp) and combine the S accumulators in FP64 (Horner
+//     in 2^-7, exact scalings) into the output.
+#include "oz.cuh"
+
+#include <cstdlib>
+
+namespace fgb {
+
+constexpr int kOzBM = 128;  // rows of the A tile (TMEM lanes)
+constexpr int kOzBN = 64;   // rows of the B tile (N of one digit product)
+constexpr int kOzBK = 32;   // bytes (= int8 elements) of K per stage = one MMA K step
+constexpr int kOzStages = 4;
+constexpr int kOzSbo = kOzBK / 16 * 128;  // bytes between 8-row groups of one slice block
+
+template <int S> struct OzCfg {
+    static constexpr int a_stage = S * kOzBM * kOzBK;
+    static constexpr int b_stage = S * kOzBN * kOzBK;
+    static constexpr int stage = a_stage + b_stage;
+    static constexpr int smem = kOzStages * stage + 1024;  // + barriers / scratch
+};
+
+// ---------------------------------------------------------------- tcgen05 helpers
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // SWIZZLE_NONE K-major canonical layout: ((8, m), (16 B, 2)) : ((16 B, SBO), (1, LBO));
+    // version 1 (sm_100), base offset 0, layout type 0.
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+    // c_format S32 (2) [4,6); a/b format signed int8 (1) [7,10) / [10,13); K-major A and B;
+    // n_dim = N >> 3 [17,23); m_dim = M >> 4 [24,29).
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Same, arriving on the barrier at this offset in every CTA of `mask` (cluster multicast).
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+
+// 1-D bulk copy global -> the same shared offset in every CTA of `mask`, completing on each
+// CTA's barrier at `bar`'s offset.
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 32 consecutive TMEM columns of this thread's lane -> 32 registers.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ double pow2(int e) {  // exact 2^e for -1022 <= e <= 1023
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// ---------------------------------------------------------------- operand views and slicing (OzView: oz.cuh)
+
+__device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
+    const int bt = row / v.rp, r = row - bt * v.rp;
+    if (r >= v.rv || k >= v.kv) return 0.0;
+    return v.src[bt * v.sbatch + (int64_t)(r >> v.ra) * v.rs + (r & v.ra) + (int64_t)(k >> v.ka) * v.ks + (k & v.ka)];
+}
+
+// 64 x 64 tile of the operand -> shared [64][65], coalesced along the contiguous direction.
+__device__ __forceinline__ void oz_tile_load(const OzView& v, int row0, int k0, double (*t)[65]) {
+    for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+        const int a = idx & 63, b = idx >> 6;
+        const int r = v.rfast ? a : b, k = v.rfast ? b : a;
+        t[r][k] = oz_load(v, row0 + r, k0 + k);
+    }
+}
+
+// Pass 1: per-row max |a| (as ordered bits of a non-negative double) via atomicMax.
+__global__ void __launch_bounds__(256) oz_rowmax_kernel(OzView v, unsigned long long* rowmax) {
+    __shared__ double t[64][65];
+    const int row0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
+    oz_tile_load(v, row0, k0, t);
+    __syncthreads();
+    const int r = threadIdx.x >> 2, q = threadIdx.x & 3;  // 4 threads per row
+    double m = 0.0;
+#pragma unroll 4
+    for (int k = q; k < 64; k += 4) m = fmax(m, fabs(t[r][k]));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    if (q == 0 && m > 0.0) atomicMax(rowmax + row0 + r, (unsigned long long)__double_as_longlong(m));
+}
+
+// Pass 2: digits. Output chunk for (row tile rt of TR rows, 32-byte K block kb):
+//   dst + ((rt * KB + kb) * S + t) * TR * 32  +  g * 256 + c * 128 + r8 * 16 + (k & 15)
+// with g = (row % TR) / 8, r8 = row % 8, c = (k % 32) / 16 -- the canonical no-swizzle K-major
+// layout with SBO = 256 B (8-row groups) and LBO = 128 B (16-byte K chunks). All S slices of
+// one (row tile, K block) are contiguous: one bulk copy per operand and pipeline stage.
+template <int S>
+__global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned long long* rowmax, int tr,
+                                                       int8_t* __restrict__ dst, int* __restrict__ exps) {
+    __shared__ double t[64][65];
+    const int row0 = blockIdx.x * 64, k0 = blockIdx.y * 64;
+    oz_tile_load(v, row0, k0, t);
+    __syncthreads();
+    const int u = threadIdx.x;  // (g_local, c, r8): one 16-byte digit run per thread and slice
+    const int gl = u >> 5, c = (u >> 3) & 3, r8 = u & 7;
+    const int rl = gl * 8 + r8, row = row0 + rl;
+    const double mx = __longlong_as_double((long long)rowmax[row]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    if (blockIdx.y == 0 && c == 0) exps[row] = e;
+    const double sc = mx > 0.0 ? pow2(-e) : 0.0;
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = t[rl][c * 16 + i] * sc;
+    const int kb_count = v.kp / kOzBK;
+    const int rt = row / tr, rr = row - rt * tr;
+    const int kb = (blockIdx.y * 64 + c * 16) / kOzBK, cl = c & (kOzBK / 16 - 1);
+    int8_t* base = dst + ((int64_t)rt * kb_count + kb) * S * tr * kOzBK + (rr >> 3) * kOzSbo + cl * 128 + r8 * 16;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double y = x[q * 4 + i] * 128.0;  // exact
+                const double d = trunc(y);
+                x[q * 4 + i] = y - d;             // exact
+                packed |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * i);
+            }
+            w[q] = packed;
+        }
+        *reinterpret_cast<uint4*>(base + (int64_t)s * tr * kOzBK) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// ---------------------------------------------------------------- the GEMM
+
+// Output addressing: row m -> (batch block bm = m / mp, i = m % mp), valid when i < mv, n < nv.
+//   CM 0: C[bm * sC + i + n * ldc]                       (real, column-major)
+//   CM 1: C[bm * sC + (i + (n >> 1) * ldc) * 2 + (n & 1)]  (complex merge of column pairs)
+struct OzOut {
+    double* c;
+    int64_t ldc, sc;
+    int mv, mp, nv;
+};
+
+constexpr int kOzEpiWarps = 8;                        // 4 TMEM lane groups x 2 column halves
+constexpr int kOzThreads = 32 * (2 + kOzEpiWarps);    // producer warp, MMA warp, epilogue warps
+
+// Persistent, clusters of CL CTAs along N (CL = 2 by default): cluster c owns work units u = c, c + clusters, ...
+// (unit = one A row tile x CL adjacent N tiles; CTA rank r computes N tile r of the unit).
+// Every A stage is fetched ONCE per cluster: CTA r bulk-copies slice r/CL of it with
+// .multicast::cluster into all CL CTAs; each CTA's MMA commit arrives on every CTA's `empty`
+// barrier (count CL), so a stage is refilled only after the whole cluster consumed it.
+// Warp 0 streams K blocks of consecutive units through the stage ring without a break; warp 1
+// issues the MMAs of a tile once the epilogue has drained the previous accumulators
+// (tmem_empty); warps 2..9 drain TMEM, fold the S int32 accumulators into two exact int64
+// partial sums, release TMEM and only then convert, scale and store -- so the FP64 epilogue
+// overlaps the next tile's MMAs.
+template <int S, int CM, int CL>
+__global__ void __launch_bounds__(kOzThreads, 1)
+ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const int8_t* __restrict__ b,
+              const int* __restrict__ eb, int kblocks, int mtiles, int ntiles, OzOut out) {
+    using Cfg = OzCfg<S>;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* sa = smem;
+    unsigned char* sb = smem + kOzStages * Cfg::a_stage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * Cfg::stage);
+    uint64_t* empty = full + kOzStages;
+    uint64_t* tfull = empty + kOzStages;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = CL > 1 ? (int)cluster_rank() : 0;
+    const int cid = blockIdx.x / CL, nclusters = gridDim.x / CL;
+    const int ngroups = ntiles / CL, units = mtiles * ngroups;
+    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
+    constexpr int kAPart = Cfg::a_stage / CL;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kOzStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, CL);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, kOzEpiWarps);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    if (CL > 1) cluster_sync_all(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t keep = policy_evict_last();  // B (the small operand) is reread by every A tile
+            int it = 0;  // global K-block counter across units
+            for (int u = cid; u < units; u += nclusters) {
+                const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
+                const unsigned char* ga = reinterpret_cast<const unsigned char*>(a) + (int64_t)mt * kblocks * Cfg::a_stage;
+                const unsigned char* gb = reinterpret_cast<const unsigned char*>(b) + (int64_t)nt * kblocks * Cfg::b_stage;
+                for (int kb = 0; kb < kblocks; ++kb, ++it) {
+                    const int s = it % kOzStages;
+                    if (it >= kOzStages) mbar_wait(empty + s, ((it / kOzStages) - 1) & 1);
+                    mbar_arrive_expect_tx(full + s, Cfg::stage);
+                    if (CL > 1)
+                        bulk_g2s_mc(sa + s * Cfg::a_stage + rank * kAPart, ga + (int64_t)kb * Cfg::a_stage + rank * kAPart,
+                                    kAPart, full + s, kMask);
+                    else
+                        bulk_g2s(sa + s * Cfg::a_stage, ga + (int64_t)kb * Cfg::a_stage, Cfg::a_stage, full + s);
+                    bulk_g2s_hint(sb + s * Cfg::b_stage, gb + (int64_t)kb * Cfg::b_stage, Cfg::b_stage, full + s, keep);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int it = 0, tcount = 0;
+            for (int u = cid; u < units; u += nclusters, ++tcount) {
+                if (tcount > 0) mbar_wait(tempty, (tcount - 1) & 1);  // epilogue drained TMEM
+                tc_fence_after();
+                for (int kb = 0; kb < kblocks; ++kb, ++it) {
+                    const int s = it % kOzStages;
+                    mbar_wait(full + s, (it / kOzStages) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sa + s * Cfg::a_stage), b0 = smem_u32(sb + s * Cfg::b_stage);
+#pragma unroll
+                    for (int t = 1; t <= S; ++t) {
+                        const uint64_t ad = umma_desc(a0 + (t - 1) * kOzBM * kOzBK, 128, kOzSbo);
+#pragma unroll
+                        for (int u0 = 1; u0 <= S + 1 - t; u0 += 4) {
+                            const int cnt = (S + 1 - t - u0 + 1) < 4 ? (S + 1 - t - u0 + 1) : 4;
+                            const uint64_t bd = umma_desc(b0 + (u0 - 1) * kOzBN * kOzBK, 128, kOzSbo);
+                            const uint32_t col = tmem + (uint32_t)((t + u0 - 2) * kOzBN);
+                            mma_i8(col, ad, bd, idesc_i8(kOzBM, cnt * kOzBN), (kb > 0 || t > 1) ? 1u : 0u);
+                        }
+                    }
+                    if (CL > 1) mma_commit_mc(empty + s, kMask); else mma_commit(empty + s);
+                }
+                mma_commit(tfull);
+            }
+        }
+    } else {
+        // epilogue warps 2..9: lane group (warp % 4) = TMEM lanes / output rows, column half
+        const int ew = warp - 2, lg = warp & 3, h = ew >> 2;
+        const int lrow = lg * 32 + lane;
+        const uint32_t lane_addr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * 32);
+        int tcount = 0;
+        for (int u = cid; u < units; u += nclusters, ++tcount) {
+            const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
+            mbar_wait(tfull, tcount & 1);
+            tc_fence_after();
+            // exact integer fold: hi = sum_{d<=4} acc_d 2^(7(4-d)), lo = sum_{d>=5} acc_d 2^(7(S+1-d))
+            long long hi[32], lo[32];
+#pragma unroll
+            for (int d = 2; d <= S + 1; ++d) {
+                int32_t v[32];
+                tmem_ld32(lane_addr + (uint32_t)((d - 2) * kOzBN), v);
+                tmem_wait_ld();
+                if (d <= 4) {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) hi[q] = (d == 2) ? (long long)v[q] : (hi[q] << 7) + v[q];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) lo[q] = (d == 5) ? (long long)v[q] : (lo[q] << 7) + v[q];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+            // value = (hi + lo 2^-7(S-3)) * 2^(e_r - 28) * 2^(e_n)
+            const int m = mt * kOzBM + lrow;
+            const int bm = m / out.mp, i = m - bm * out.mp;
+            if (i < out.mv) {
+                const double ra = pow2(ea[m] - 28);
+                const double lo_w = pow2(-7 * (S - 3));
+                double* cb = out.c + (int64_t)bm * out.sc;
+                const int* ebt = eb + nt * kOzBN + h * 32;
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    const int n = nt * kOzBN + h * 32 + c;
+                    if (n >= out.nv) break;
+                    const double v0 = ((double)hi[c] + (double)lo[c] * lo_w) * ra * pow2(ebt[c]);
+                    const double v1 = ((double)hi[c + 1] + (double)lo[c + 1] * lo_w) * ra * pow2(ebt[c + 1]);
+                    if (CM == 0) {
+                        __stcs(cb + i + (int64_t)n * out.ldc, v0);
+                        if (n + 1 < out.nv) __stcs(cb + i + (int64_t)(n + 1) * out.ldc, v1);
+                    } else {
+                        __stcs(reinterpret_cast<double2*>(cb + (i + (int64_t)(n >> 1) * out.ldc) * 2), make_double2(v0, v1));
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    if (CL > 1) cluster_sync_all(); else __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------- host launchers
+
+int oz_slices_default() { return 7; }
+
+size_t oz_operand_bytes(int slices, int64_t rows_padded, int64_t kp) { return (size_t)slices * rows_padded * kp; }
+
+cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, int* exps, unsigned long long* rowmax,
+                            cudaStream_t stream) {
+    const int rows = v.nb * v.rp;
+    if (rows % 64 || v.kp % 64 || v.rp % tr) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(rowmax, 0, (size_t)rows * sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    dim3 grid(rows / 64, v.kp / 64);
+    oz_rowmax_kernel<<<grid, 256, 0, stream>>>(v, rowmax);
+    if (slices == 7)
+        oz_slice_kernel<7><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
+    else if (slices == 8)
+        oz_slice_kernel<8><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
+    else if (slices == 6)
+        oz_slice_kernel<6><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+template <int S, int CM, int CL>
+static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, const int8_t* b, const int* eb, int ntiles,
+                                int kp, const OzOut& out, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             OzCfg<S>::smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int units = mtiles * (ntiles / CL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kOzThreads);
+    cfg.dynamicSmemBytes = OzCfg<S>::smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // persistent grid = the clusters that are co-resident (GPC sizes are not multiples of CL)
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
+        cfg.gridDim = dim3(FGFRFT_SMS / CL * CL);
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, ozgemm_kernel<S, CM, CL>, &cfg) != cudaSuccess || mc <= 0) {
+            cudaGetLastError();
+            mc = FGFRFT_SMS / CL;
+        }
+        max_clusters = mc;
+    }
+    const int clusters = units < max_clusters ? units : max_clusters;
+    cfg.gridDim = dim3(clusters * CL);
+    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL>, a, ea, b, eb, kp / kOzBK, mtiles, ntiles, out);
+}
+
+template <int S, int CM>
+static cudaError_t oz_launch(const int8_t* a, const int* ea, int mrows, const int8_t* b, const int* eb, int nrows,
+                             int kp, const OzOut& out, cudaStream_t stream) {
+    const int mtiles = mrows / kOzBM, ntiles = nrows / kOzBN;
+    static const int forced = [] {
+        const char* e = std::getenv("FGFRFT_OZ_CLUSTER");
+        return e ? std::atoi(e) : 0;
+    }();
+    // Measured on B200 (tools/bench_int8gemm.py): pairs win (3.13 vs 3.05 POPS unclustered);
+    // clusters of 4 / 8 lose co-residency (GPC sizes) more than they save in L2 traffic.
+    int cl = ntiles % 2 == 0 ? 2 : 1;
+    if (forced > 0 && forced <= cl && ntiles % forced == 0) cl = forced;
+    switch (cl) {
+        case 8: return oz_launch_cl<S, CM, 8>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
+        case 4: return oz_launch_cl<S, CM, 4>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
+        case 2: return oz_launch_cl<S, CM, 2>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
+        default: return oz_launch_cl<S, CM, 1>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
+    }
+}
+
+// C (from OzOut) = A_sliced (mrows x kp) * B_sliced (nrows x kp)^T; mrows % 128 == 0, nrows % 64 == 0.
+cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
+                          const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
+                          cudaStream_t stream) {
+    if (mrows % kOzBM || nrows % kOzBN || kp % 64 || mp <= 0) return cudaErrorInvalidValue;
+    const OzOut out{c, ldc, sc, mv, mp, nv};
+#define FGB_OZ(S_)                                                                     \
+    if (slices == S_) {                                                                \
+        if (cm == 0) return oz_launch<S_, 0>(a, ea, mrows, b, eb, nrows, kp, out, stream); \
+        return oz_launch<S_, 1>(a, ea, mrows, b, eb, nrows, kp, out, stream);              \
+    }
+    FGB_OZ(6)
+    FGB_OZ(7)
+    FGB_OZ(8)
+#undef FGB_OZ
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace fgb
