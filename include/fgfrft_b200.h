@@ -51,6 +51,15 @@ typedef enum fgfrft_dtype { FGFRFT_C128 = 0, FGFRFT_C64 = 1 } fgfrft_dtype;
 
 typedef enum fgfrft_which { FGFRFT_Q = 0, FGFRFT_DQ = 1 } fgfrft_which;
 
+/*
+ * GEMM engine of a handle (fgfrft_cache_set_engine). DMMA: FP64 tensor cores (mma.sync f64),
+ * every order synthesised then multiplied. INT8: for real F, order sweeps run through the
+ * power products F^k X computed by one Ozaki-scheme GEMM on the INT8 tensor cores
+ * (tcgen05 kind::i8; ~3e-13 relative, see fgfrft_dgemm_int8_dev). AUTO (default, or the
+ * FGFRFT_ENGINE=dmma|int8 environment variable): INT8 power products when 2 n_alpha >= L.
+ */
+typedef enum fgfrft_engine { FGFRFT_ENGINE_AUTO = 0, FGFRFT_ENGINE_DMMA = 1, FGFRFT_ENGINE_INT8 = 2 } fgfrft_engine;
+
 /* Default budget of transform.hpp:17 (4 GiB). */
 #define FGFRFT_DEFAULT_MEMORY_BUDGET (4ULL << 30)
 
@@ -120,6 +129,10 @@ int fgfrft_cache_verify(const fgfrft_cache* cache, const double* f);
 int fgfrft_cache_set_stream(fgfrft_cache* cache, void* stream);
 
 /* Device pointer to slab k-1 (= F^k) and the device memory held by the handle. */
+int fgfrft_cache_set_engine(fgfrft_cache* cache, int engine);
+/* Build lazily-built device structures now (the INT8 digit slices of the stacked cache for the
+ * power-product route); a no-op for handles that never use them. Synchronises. */
+int fgfrft_cache_prepare(fgfrft_cache* cache);
 int fgfrft_cache_device_slab(fgfrft_cache* cache, int k, void** dptr);
 int fgfrft_cache_device_bytes(const fgfrft_cache* cache, uint64_t* bytes);
 

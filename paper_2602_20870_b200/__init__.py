@@ -102,6 +102,8 @@ def lib() -> ctypes.CDLL:
         "fgfrft_batch_set_stream": (i, [vp, vp]),
         "fgfrft_batch_forward_dev": (i, [vp, vp, i, vp, i64, vp]),
         "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
+        "fgfrft_cache_set_engine": (i, [vp, i]),
+        "fgfrft_cache_prepare": (i, [vp]),
         "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
     }
     for name, (res, args) in sig.items():
@@ -124,7 +126,8 @@ def exported_symbols():
         "fgfrft_mse_step_dev", "fgfrft_shard_create", "fgfrft_shard_destroy", "fgfrft_shard_info",
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
         "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
-        "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev",
+        "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
+        "fgfrft_cache_prepare",
     ]
 
 
@@ -137,6 +140,8 @@ def _check(rc: int) -> None:
 def launch_count() -> int:
     return int(lib().fgfrft_launch_count())
 
+
+ENGINE_AUTO, ENGINE_DMMA, ENGINE_INT8 = 0, 1, 2
 
 KERNEL_CLASSES = ("synthesis", "dmma_zgemm", "power_dots", "elementwise", "int8_gemm", "slicing", "combine",
                   "reserved")
@@ -256,6 +261,15 @@ class PowerCache:
 
     def set_stream(self, stream_handle: int) -> None:
         _check(lib().fgfrft_cache_set_stream(self._h, ctypes.c_void_p(stream_handle)))
+
+    def set_engine(self, engine: int) -> None:
+        """ENGINE_AUTO, ENGINE_DMMA (FP64 tensor cores, synthesis + GEMM per order) or ENGINE_INT8
+        (real F: INT8 tensor-core power products, see fgfrft_cache_set_engine)."""
+        _check(lib().fgfrft_cache_set_engine(self._h, int(engine)))
+
+    def prepare(self) -> None:
+        """Build lazily-built device structures (INT8 digit slices of the cache) now."""
+        _check(lib().fgfrft_cache_prepare(self._h))
 
     def device_bytes(self) -> int:
         b = ctypes.c_uint64()

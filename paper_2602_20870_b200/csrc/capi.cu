@@ -86,6 +86,11 @@ cudaError_t launch_to_tiled(const void* src, void* dst, int n, int elem_bytes_ds
 cudaError_t launch_from_tiled(const void* src, void* dst, int n, int elem_bytes_src, cudaStream_t stream);
 cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int width, double* out,
                             cudaStream_t stream);
+int combine_max_terms();
+size_t combine_partial_elems(int tp);
+cudaError_t launch_combine(const double* z, const double* x, const double* xc, int64_t count, int l,
+                           const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
+                           double* loss, cudaStream_t stream);
 }  // namespace fgb
 
 using namespace fgb;
@@ -223,6 +228,11 @@ struct fgfrft_cache {
     std::mutex mu;
     // workspaces
     DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda, tmp;
+    // Power-product route (real F): the stacked cache [P_1..P_L; P_1^T..P_L^T] as INT8 Ozaki
+    // digit slices (built lazily, once), the per-call slices of X and the products Z = P X.
+    int engine = FGFRFT_ENGINE_AUTO;
+    int ps_slices = 0;
+    DevBuf ps, pe, prm, xsl, xex, z;
     // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
     bool shard = false;
     int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
@@ -567,6 +577,104 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
     return FGFRFT_OK;
 }
 
+// ------------------------------------------------------------------ power-product route
+//
+// For an order sweep over a real cache, F^a X = sum_k c_k(a) F^k X: the 2L products
+// Z_k = P_k X, W_k = P_k^T X are ONE INT8 tensor-core GEMM of the stacked sliced cache with X,
+// after which each order is a (2L+1)-term combination (combine.cu). Used when it is cheaper than
+// synthesising every Q(a): 2L products against 2 GEMMs (Q X and G X^H) per order.
+int engine_of(const fgfrft_cache* c) {
+    if (c->engine != FGFRFT_ENGINE_AUTO) return c->engine;
+    static const int env = [] {
+        const char* e = std::getenv("FGFRFT_ENGINE");
+        if (!e) return (int)FGFRFT_ENGINE_AUTO;
+        if (!std::strcmp(e, "dmma")) return (int)FGFRFT_ENGINE_DMMA;
+        if (!std::strcmp(e, "int8")) return (int)FGFRFT_ENGINE_INT8;
+        return (int)FGFRFT_ENGINE_AUTO;
+    }();
+    return env;
+}
+
+bool use_power_route(const fgfrft_cache* c, int n_alpha) {
+    if (!c->real || c->dtype != FGFRFT_C128 || 2 * c->l + 1 > combine_max_terms() || c->n > 16384) return false;
+    const int eng = engine_of(c);
+    if (eng == FGFRFT_ENGINE_DMMA) return false;
+    if (eng == FGFRFT_ENGINE_INT8) return true;
+    return 2 * n_alpha >= c->l;  // auto: 2L products amortised over the orders
+}
+
+int64_t pad_rows(int64_t n) { return ceil_div(n, kOzTileA) * kOzTileA; }
+int64_t pad_k(int64_t n) { return ceil_div(n, kOzK) * kOzK; }
+
+int ensure_power_slices(fgfrft_cache* c) {
+    const int S = oz_slices_default();
+    if (c->ps_slices == S) return FGFRFT_OK;
+    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(n), rows = 2 * (int64_t)c->l * np;
+    FGB_CUDA(c->ps.ensure((size_t)S * rows * kp));
+    FGB_CUDA(c->pe.ensure((size_t)rows * sizeof(int)));
+    FGB_CUDA(c->prm.ensure((size_t)rows * sizeof(unsigned long long)));
+    const int nt = (int)ceil_div(n, kTile);
+    for (int half = 0; half < 2; ++half) {
+        OzView v{static_cast<const double*>(c->slabs), 0, 0, (int64_t)c->slab_elems(), 0, 0, (int)n, (int)np, c->l,
+                 (int)n, (int)kp, half == 0};
+        v.tiled = half == 0 ? 1 : 2;
+        v.nt = nt;
+        const int64_t r0 = half * (int64_t)c->l * np;
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->ps.as<int8_t>() + (size_t)S * r0 * kp, c->pe.as<int>() + r0,
+                                   c->prm.as<unsigned long long>(), c->stream),
+                   3);
+    }
+    c->ps_slices = S;
+    return FGFRFT_OK;
+}
+
+// z <- [P_1 X; ..; P_L X; P_1^T X; ..; P_L^T X], 2L blocks of n x b complex (column-major).
+int power_products(fgfrft_cache* c, const void* x_dev, int64_t b) {
+    if (int st = ensure_power_slices(c)) return st;
+    const int S = c->ps_slices;
+    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(n), rows = 2 * (int64_t)c->l * np;
+    const int64_t bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
+    FGB_CUDA(c->xsl.ensure((size_t)S * bp * kp));
+    FGB_CUDA(c->xex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
+    FGB_CUDA(c->z.ensure((size_t)2 * c->l * n * b * 16));
+    int* xe = c->xex.as<int>();
+    unsigned long long* xr = reinterpret_cast<unsigned long long*>(xe + bp);
+    {
+        // B operand rows r = 2j + comp (column j of X, re / im), K = signal index i
+        const OzView v{static_cast<const double*>(x_dev), 2 * n, 2, 0, 1, 0, (int)(2 * b), (int)bp, 1, (int)n,
+                       (int)kp, false};
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->xsl.as<int8_t>(), xe, xr, c->stream), 3);
+    }
+    ProfScope ps(KC_I8GEMM, c->stream);
+    FGB_LAUNCH(launch_ozgemm(S, 1, c->ps.as<int8_t>(), c->pe.as<int>(), (int)rows, c->xsl.as<int8_t>(), xe, (int)bp,
+                             (int)kp, c->z.as<double>(), n, 2 * n * b, (int)n, (int)np, (int)(2 * b), c->stream),
+               1);
+    return FGFRFT_OK;
+}
+
+// MSE step over the power products: loss, s (2L+1 per order) and optionally Y.
+int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev,
+                    int64_t b, void* y_dev, double* loss_dev, double* s_dev) {
+    if (int st = power_products(c, x_dev, b)) return st;
+    const int l = c->l;
+    const size_t width = (size_t)(2 * l + 1);
+    const int64_t count = 2 * c->n * b;
+    const double norm = 1.0 / ((double)c->n * (double)b);
+    FGB_CUDA(c->partial.ensure(combine_partial_elems(combine_max_terms()) * sizeof(double)));
+    for (int a0 = 0; a0 < n_alpha; a0 += 64) {
+        const int na = std::min(64, n_alpha - a0);
+        ProfScope ps(KC_COMBINE, c->stream);
+        FGB_LAUNCH(launch_combine(c->z.as<double>(), static_cast<const double*>(x_dev),
+                                  static_cast<const double*>(xc_dev), count, l, coef + (size_t)a0 * width, na, norm,
+                                  y_dev ? static_cast<double*>(y_dev) + (size_t)a0 * count : nullptr,
+                                  c->partial.as<double>(), s_dev + (size_t)a0 * width, loss_dev + a0, c->stream),
+                   2);
+    }
+    return FGFRFT_OK;
+}
+
 // s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
 // Order sweeps (>= 8 orders) use the DMMA split-K contraction (every byte of M and of the cache
 // read once per 64 orders); a few orders use the scalar tile-pair kernel (HBM-bound).
@@ -756,6 +864,27 @@ int fgfrft_cache_set_stream(fgfrft_cache* c, void* stream) {
     std::lock_guard<std::mutex> lk(c->mu);
     c->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
     return FGFRFT_OK;
+}
+
+int fgfrft_cache_set_engine(fgfrft_cache* c, int engine) {
+    if (int st = check_handle(c)) return st;
+    if (engine < FGFRFT_ENGINE_AUTO || engine > FGFRFT_ENGINE_INT8) return fail(FGFRFT_PARAMETER, "unknown engine");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->engine = engine;
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_prepare(fgfrft_cache* c) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    if (c->real && c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA &&
+        2 * c->l + 1 <= combine_max_terms())
+        if (int st = ensure_power_slices(c)) return st;
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    return FGFRFT_OK;
+    FGB_GUARD_END
 }
 
 int fgfrft_cache_device_slab(fgfrft_cache* c, int k, void** dptr) {
@@ -953,6 +1082,16 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
     const double* dc_dev = coef + (size_t)n_alpha * width;
+    if (use_power_route(c, n_alpha)) {
+        FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
+        if (int st = mse_power_route(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
+                                     c->s.as<double>()))
+            return st;
+        FGB_LAUNCH(launch_coef_dot(dc_dev, c->s.as<double>(), n_alpha, (int)width, static_cast<double*>(dlda_dev),
+                                   c->stream),
+                   1);
+        return FGFRFT_OK;
+    }
     const int chunk = alpha_chunk(c, n_alpha);
     const size_t sl = c->mat_elems();
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));

@@ -6,6 +6,7 @@ namespace fgb {
 
 // Logical operand (R rows x K): element (r, k) of batch block bt sits at
 //   src[bt * sbatch + (r >> ra) * rs + (r & ra) + (k >> ka) * ks + (k & ka)]
+// or, for a tiled cache slab (tiled = 1 / 2), at the tiled position of P(r, k) / P(k, r).
 // (ra / ka = 1 split a complex dimension into its (re, im) halves). Rows are grouped in batch
 // blocks of rv valid rows padded to rp (a multiple of the tile rows); the sliced operand holds
 // nb * rp rows. Padding rows / columns are zero.
@@ -16,6 +17,9 @@ struct OzView {
     int rv, rp, nb;  // valid rows per block, padded rows per block, blocks
     int kv, kp;      // valid K, padded K (multiple of kOzBK)
     bool rfast;      // rows are the contiguous direction of the source
+    int tiled = 0;   // 1: src is a tiled cache slab (common.cuh), element (r, k) = P(r, k);
+                     // 2: the same slab read transposed, element (r, k) = P(k, r)
+    int nt = 0;      // tiles per side of a tiled slab
 };
 
 

@@ -124,6 +124,10 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e for -1022 <= e <= 
 __device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
     const int bt = row / v.rp, r = row - bt * v.rp;
     if (r >= v.rv || k >= v.kv) return 0.0;
+    if (v.tiled) {
+        const int i = v.tiled == 1 ? r : k, j = v.tiled == 1 ? k : r;
+        return v.src[bt * v.sbatch + tile_base(i >> 5, j >> 5, v.nt) + swz(i & 31, j & 31)];
+    }
     return v.src[bt * v.sbatch + (int64_t)(r >> v.ra) * v.rs + (r & v.ra) + (int64_t)(k >> v.ka) * v.ks + (k & v.ka)];
 }
 
@@ -439,7 +443,7 @@ static cudaError_t oz_launch(const int8_t* a, const int* ea, int mrows, const in
     // Measured on B200 (tools/bench_int8gemm.py): pairs win (3.13 vs 3.05 POPS unclustered);
     // clusters of 4 / 8 lose co-residency (GPC sizes) more than they save in L2 traffic.
     int cl = ntiles % 2 == 0 ? 2 : 1;
-    if (forced > 0 && forced <= cl && ntiles % forced == 0) cl = forced;
+    if ((forced == 1 || forced == 2 || forced == 4 || forced == 8) && ntiles % forced == 0) cl = forced;
     switch (cl) {
         case 8: return oz_launch_cl<S, CM, 8>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
         case 4: return oz_launch_cl<S, CM, 4>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);

@@ -307,6 +307,8 @@ def test_real_f_path_matches_complex_path_and_oracle(n, l, b, monkeypatch):
     assert not gc.is_real()
     ge = fg.PowerCache(f, l, powers=o.slabs)
     assert ge.is_real()
+    g.set_engine(fg.ENGINE_DMMA)  # this test pins the synthesis + DMMA GEMM route
+    gc.set_engine(fg.ENGINE_DMMA)
     for k in (1, 2, l):
         assert rel(g.power(k), o.power(k)) <= 1e-13
         assert np.all(g.power(k).imag == 0)
@@ -337,3 +339,40 @@ def test_real_f_path_matches_complex_path_and_oracle(n, l, b, monkeypatch):
             s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
             tol = 1e-10 * np.sum(np.abs(dc * s_ref))
             assert abs(dl[i] - dr) <= tol and abs(dl[i] - dlc[i]) <= tol
+
+
+# --------------------------------------------------------------------------- power-product route (INT8)
+
+@pytest.mark.parametrize("n,l,b,n_alpha", [(64, 8, 5, 9), (100, 12, 33, 12), (256, 32, 17, 40), (200, 64, 3, 70)])
+def test_power_route_matches_oracle(n, l, b, n_alpha):
+    """Real F, order sweep through Z_k = F^k X on the INT8 tensor cores (Ozaki, 7 digits) and the
+    DMMA combination: F^a X, the MSE loss and dL/dalpha within the north-star bar (1e-10) of the
+    oracle's series; typically ~1e-13."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 11 + n)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    assert g.is_real()
+    g.set_engine(fg.ENGINE_INT8)
+    rng = np.random.default_rng(n + b)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    alphas = list(np.linspace(-0.9, 2.0, n_alpha))
+    loss, dl, y = fg.mse_step(g, alphas, x, xc, want_y=True)
+    worst = 0.0
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        yr = q @ x
+        e = rel(y[i], yr)
+        worst = max(worst, e)
+        assert e <= 1e-10
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (yr - xc) / (n * b)) @ x.conj().T)
+        assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+    assert worst <= 5e-12  # the INT8 products are far inside the bar
+    # the DMMA engine on the same handle agrees
+    g.set_engine(fg.ENGINE_DMMA)
+    loss2, dl2, y2 = fg.mse_step(g, alphas, x, xc, want_y=True)
+    assert np.max(np.abs(loss2 - loss) / loss) <= 1e-10
+    assert all(rel(y2[i], y[i]) <= 1e-10 for i in range(len(alphas)))
