@@ -3,13 +3,16 @@
 
 Workload (BASELINE config 2, configs[1]): N=1024 Gaussian-weighted k-NN sensor graph, L=64
 (cache = 64 complex128 powers, 1.07 GB > L2), B=256 noisy bandlimited signals, 64 orders
-swept over [0, 2]. One STEP = for every order: Y = F^alpha X (series synthesis + DMMA GEMM),
-MSE loss against the clean signals, and dL/dalpha (M = G X^H on DMMA + per-power reductions).
+swept over [0, 2]. One STEP = for every order: Y = F^alpha X, the MSE loss against the clean
+signals and dL/dalpha. With a real F (every BASELINE config) the library runs the power-product
+route: Z_k = F^k X for k = +-1..+-L in ONE INT8 tensor-core GEMM (Ozaki scheme) over the stacked
+cache, then per order Y = sum_k c_k Z_k, the loss and s_k = Re<G, Z_k> on DMMA
+(dmma_engine_ms_per_step: the same step on the FP64-tensor-core synthesis route).
 `value` is whole-job signal-nodes/s = N * B * A * ranks / step time, inputs resident in HBM;
 `e2e` is the same step through the C ABI with pinned host buffers (H2D of X, Xc and D2H of the
 per-order losses and gradients inside the timed region).
 
-Extra objects: `roofline` for the dominant kernel (the DMMA complex GEMM; FP64 tensor bound),
+Extra objects: `roofline` for the dominant kernel (the INT8 Ozaki GEMM, or the DMMA GEMM),
 `synthesis` (F^alpha synthesis GB/s vs HBM peak, the metric's first half, 64-order sweep and
 single order), `cache_build` (K1 TFLOP/s), `cpu_baseline` (the oracle on this host, bounded
 sample), `clocks` (nvidia-smi during the timed region), `gpu_launches`.
@@ -44,9 +47,13 @@ def _peaks():
     except Exception:
         hbm, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     fp64 = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")))
+    i8 = json.load(open(os.path.join(ROOT, "profiles", "r01_int8_peak.json")))
     return {"hbm_gbs": hbm, "hbm_src": src, "fp64_tflops": float(fp64["dmma_m8n8k4_tflops"]),
             "fp64_src": "profiles/r01_fp64_peaks.json:dmma_m8n8k4_tflops (measured DMMA microbenchmark; "
-                        "MEASURED_PEAKS.json has no FP64 figure)"}
+                        "MEASURED_PEAKS.json has no FP64 figure)",
+            "int8_tops": float(i8["cublas_int8_8192_tops"]),
+            "int8_src": "profiles/r01_int8_peak.json:cublas_int8_8192_tops (measured cuBLAS int8 GEMM 8192^3 on "
+                        "this pool, tools/peaks/int8_peak.cu; nominal dense 4500)"}
 
 
 class ClockSampler:
@@ -218,6 +225,11 @@ def main():
     build_s = time.perf_counter() - t0
     build_flops = (L - 1) * 8.0 * n ** 3
     cache.set_stream(stream.cuda_stream)
+    # INT8 digit slices of the stacked cache for the power-product route (built once per cache,
+    # like the cache itself; outside the timed region)
+    t0 = time.perf_counter()
+    cache.prepare()
+    slices_s = time.perf_counter() - t0
 
     xd = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).to(f"cuda:{local}")      # column-major n x b
     xcd = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).to(f"cuda:{local}")
@@ -278,14 +290,64 @@ def main():
                  "dlda_abs_err": abs(float(dlda_d[i]) - dr), "dlda_ref": dr}
         del ocache
 
-    # ---- dominant kernel roofline: the DMMA GEMMs (Q X and G X^H per order). With a real F
-    # (graph GFT) they are real x complex: 4 n^2 B flops each (2 n^2 per real column, 2B columns).
+    # ---- dominant kernel roofline.
+    # Power-product route (real F, INT8 engine): ozgemm_kernel computes Z = [P_1..P_L; P_1^T..P_L^T] X,
+    #   2 * (2L n) * 2B * n FP64-equivalent flops per step (real x complex: 2B real columns), as
+    #   28 int8 digit-product GEMMs (Ozaki, 7 digits): x28 int8 ops. combine_kernel: 2 DMMA GEMMs
+    #   of 2 * A * (2L+1) * 2nB flops each.
+    # Synthesis route (DMMA engine): the DMMA GEMMs Q X and G X^H, 4 n^2 B flops each (real F).
     real = cache.is_real()
-    gemm_ms, gemm_n = prof["dmma_zgemm"]
-    gemm_flops_step = 2 * A * (4.0 if real else 8.0) * n * n * b
-    gemm_tflops = gemm_flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
     tot_prof = sum(v[0] for v in prof.values())
     shares = {k: (v[0] / tot_prof if tot_prof else None) for k, v in prof.items()}
+    i8_ms, i8_n = prof["int8_gemm"]
+    power_route = i8_n > 0
+    if power_route:
+        fp64eq = 2.0 * (2 * L * n) * (2 * b) * n
+        i8_ops = fp64eq * 28
+        achieved = i8_ops * args.steps / (i8_ms * 1e-3) / 1e12
+        cb_ms, cb_n = prof["combine"]
+        roof = {"bound": "tensor", "kernel": "ozgemm_kernel<7,1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
+                "achieved": achieved, "peak": peaks["int8_tops"], "unit": "TOPS",
+                "frac": achieved / peaks["int8_tops"], "traffic": None, "peak_source": peaks["int8_src"],
+                "algorithmic": "per step 2*(2L*N)*(2B)*N FP64-equivalent flops (Z = F^k X, k = +-1..+-L, real F x "
+                               "complex X) = 28 int8 digit-product GEMMs of that size (Ozaki scheme, 7 digits)",
+                "fp64_equivalent_tflops": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12,
+                "fp64_equivalent_frac_of_dmma_peak": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12 / peaks["fp64_tflops"],
+                "dmma_peak_tflops": peaks["fp64_tflops"],
+                "launches_timed": i8_n, "share_of_step": shares,
+                "combine_kernel": {"ms_per_step": cb_ms / args.steps,
+                                   "tflops": 2 * 2.0 * A * (2 * L + 1) * 2 * n * b * args.steps / (cb_ms * 1e-3) / 1e12,
+                                   "peak_dmma_tflops": peaks["fp64_tflops"]}}
+    else:
+        gemm_ms, gemm_n = prof["dmma_zgemm"]
+        gemm_flops_step = 2 * A * (4.0 if real else 8.0) * n * n * b
+        gemm_tflops = gemm_flops_step * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+        roof = {"bound": "tensor",
+                "kernel": ("rgemm_kernel (FP64 DMMA, real Q x complex X)" if real
+                           else "zgemm_dmma_kernel (FP64 DMMA complex GEMM)"),
+                "achieved": gemm_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": (gemm_tflops / peaks["fp64_tflops"]) if gemm_tflops else None,
+                "traffic": None, "peak_source": peaks["fp64_src"],
+                "algorithmic": ("4*N^2*B flops per order per GEMM (real F: real x complex), "
+                                "2 GEMMs per order" if real else
+                                "8*N^2*B flops per order per GEMM, 2 GEMMs per order"),
+                "launches_timed": gemm_n, "share_of_step": shares}
+
+    # ---- the same step on the FP64-tensor-core (DMMA) engine, for comparison
+    dmma_ms = None
+    if power_route:
+        cache.set_engine(fg.ENGINE_DMMA)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                step_dev()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            step_dev()
+        e1.record(stream)
+        e1.synchronize()
+        dmma_ms = e0.elapsed_time(e1) / 5
+        cache.set_engine(fg.ENGINE_AUTO)
 
     # ---- synthesis GB/s (metric's first half): 64-order sweep and a single order, device output
     qbuf = torch.empty((A, n, n), dtype=torch.complex128, device=f"cuda:{local}")
@@ -353,16 +415,11 @@ def main():
                        "real_f": real,
                        "l2": "inputs larger than L2 (1.07 GB cache streamed every step)",
                        "parallelism": f"replicas x{ws} (independent problems per rank)"},
-            "roofline": {"bound": "tensor",
-                         "kernel": ("rgemm_kernel (FP64 DMMA, real Q x complex X)" if real
-                                    else "zgemm_dmma_kernel (FP64 DMMA complex GEMM)"),
-                         "achieved": gemm_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                         "frac": (gemm_tflops / peaks["fp64_tflops"]) if gemm_tflops else None,
-                         "traffic": None, "peak_source": peaks["fp64_src"],
-                         "algorithmic": ("4*N^2*B flops per order per GEMM (real F: real x complex), "
-                                         "2 GEMMs per order" if real else
-                                         "8*N^2*B flops per order per GEMM, 2 GEMMs per order"),
-                         "launches_timed": gemm_n, "share_of_step": shares},
+            "roofline": roof,
+            "route": ("power products: Z = F^k X by one INT8 tensor-core Ozaki GEMM over the stacked cache, "
+                      "then per-order combination + MSE + dL/da on DMMA" if power_route else
+                      "per-order synthesis Q(a) + DMMA GEMMs"),
+            "dmma_engine_ms_per_step": dmma_ms,
             "synthesis": {"unit": "GB/s", "peak_hbm_gbs": peaks["hbm_gbs"], "peak_source": peaks["hbm_src"],
                           "layout": "S = L stored slabs (F^-k read as conjugate-transposed tile pairs); "
                                     + ("real F: slabs stored as real doubles (8 B/element), output complex128"
@@ -370,7 +427,8 @@ def main():
                           **syn},
             "cache_build": {"seconds": build_s, "tflops": build_flops / build_s / 1e12,
                             "frac_fp64": build_flops / build_s / 1e12 / peaks["fp64_tflops"],
-                            "note": "host wall clock incl. H2D of F and allocation"},
+                            "note": "host wall clock incl. H2D of F and allocation",
+                            "int8_slices_seconds": slices_s},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 2 * n * b * 16, "d2h_bytes_per_step": 2 * A * 8},
             "gpu_launches": launches,
