@@ -233,6 +233,7 @@ struct fgfrft_cache {
     int engine = FGFRFT_ENGINE_AUTO;
     int ps_slices = 0;
     DevBuf ps, pe, prm, xsl, xex, z;
+    DevBuf qsl, qex;  // per-call INT8 slices of Q(a) (or G) for the synthesis route
     // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
     bool shard = false;
     int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
@@ -550,6 +551,11 @@ int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host
     return FGFRFT_OK;
 }
 
+// INT8 tensor-core (Ozaki) versions of the real-F synthesis route's two GEMMs (defined below).
+bool use_int8_gemm(const fgfrft_cache* c);
+int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
+int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
+
 // Y[a] = op(Q(alpha_a)) X for all orders; x_dev n x b, y_dev n_alpha blocks of n x b.
 int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used, bool inverse, const void* x_dev,
                  int64_t b, void* y_dev) {
@@ -563,6 +569,12 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p, true)) return st;
+        if (use_int8_gemm(c)) {
+            if (int st = int8_qx(c, na, inverse, c->q.p, x_dev, b,
+                                 static_cast<char*>(y_dev) + (size_t)a0 * n * b * c->sig))
+                return st;
+            continue;
+        }
         ProfScope ps(KC_GEMM, c->stream);
         if (c->real)  // Y = Q X or Q^T X with real Q: real DMMA GEMM over the (re, im) columns
             FGB_LAUNCH(launch_rgemm(inverse ? 1 : 0, 1, 1, n, 2 * (int)b, n, c->q.p, n, (int64_t)sl, x_dev, n, 0,
@@ -675,6 +687,85 @@ int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void
     return FGFRFT_OK;
 }
 
+bool use_int8_gemm(const fgfrft_cache* c) {
+    return c->real && c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA && c->n <= 16384 &&
+           !c->shard && c->graphs == 0;
+}
+
+// Slice the signal block X (n x b complex) as the B operand: rows 2j + comp, K = signal index.
+int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out) {
+    const int S = oz_slices_default();
+    const int64_t n = c->n, kp = pad_k(n), bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
+    FGB_CUDA(c->xsl.ensure((size_t)S * bp * kp));
+    FGB_CUDA(c->xex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
+    int* xe = c->xex.as<int>();
+    const OzView v{static_cast<const double*>(x_dev), 2 * n, 2, 0, 1, 0, (int)(2 * b), (int)bp, 1, (int)n, (int)kp,
+                   false};
+    ProfScope ps(KC_SLICE, c->stream);
+    FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->xsl.as<int8_t>(), xe,
+                               reinterpret_cast<unsigned long long*>(xe + bp), c->stream),
+               3);
+    *bp_out = bp;
+    return FGFRFT_OK;
+}
+
+// Y_a = op(Q_a) X for na real n x n matrices Q_a (column-major, stride n^2), complex X.
+int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y) {
+    const int S = oz_slices_default();
+    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(n), rows = (int64_t)na * np;
+    FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
+    FGB_CUDA(c->qex.ensure((size_t)rows * (sizeof(int) + sizeof(unsigned long long))));
+    int* qe = c->qex.as<int>();
+    {
+        const double* src = static_cast<const double*>(q);
+        const OzView v = inverse ? OzView{src, n, 1, n * n, 0, 0, (int)n, (int)np, na, (int)n, (int)kp, false}
+                                 : OzView{src, 1, n, n * n, 0, 0, (int)n, (int)np, na, (int)n, (int)kp, true};
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->qsl.as<int8_t>(), qe,
+                                   reinterpret_cast<unsigned long long*>(qe + rows), c->stream),
+                   3);
+    }
+    int64_t bp = 0;
+    if (int st = slice_signal_rows(c, x_dev, b, &bp)) return st;
+    ProfScope ps(KC_I8GEMM, c->stream);
+    FGB_LAUNCH(launch_ozgemm(S, 1, c->qsl.as<int8_t>(), qe, (int)rows, c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
+                             (int)kp, static_cast<double*>(y), n, 2 * n * b, (int)n, (int)np, (int)(2 * b), c->stream),
+               1);
+    return FGFRFT_OK;
+}
+
+// M_a = Re(G_a X^H) (real n x n, column-major, stride n^2) for na blocks G_a (n x b complex).
+int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m) {
+    const int S = oz_slices_default();
+    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(2 * b), rows = (int64_t)na * np;
+    const int64_t xp = ceil_div(n, kOzTileB) * kOzTileB;
+    FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
+    FGB_CUDA(c->qex.ensure((size_t)rows * (sizeof(int) + sizeof(unsigned long long))));
+    FGB_CUDA(c->xsl.ensure((size_t)S * xp * kp));
+    FGB_CUDA(c->xex.ensure((size_t)xp * (sizeof(int) + sizeof(unsigned long long))));
+    int* ge = c->qex.as<int>();
+    int* xe = c->xex.as<int>();
+    {
+        // G_a(i, 2j + comp) and X(l, 2j + comp): K = the (re, im) columns of the signal block
+        const OzView vg{static_cast<const double*>(g), 2, 2 * n, 2 * n * b, 0, 1, (int)n, (int)np, na, (int)(2 * b),
+                        (int)kp, true};
+        const OzView vx{static_cast<const double*>(x_dev), 2, 2 * n, 0, 0, 1, (int)n, (int)xp, 1, (int)(2 * b),
+                        (int)kp, true};
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(vg, S, kOzTileA, c->qsl.as<int8_t>(), ge,
+                                   reinterpret_cast<unsigned long long*>(ge + rows), c->stream),
+                   3);
+        FGB_LAUNCH(launch_oz_slice(vx, S, kOzTileB, c->xsl.as<int8_t>(), xe,
+                                   reinterpret_cast<unsigned long long*>(xe + xp), c->stream),
+                   3);
+    }
+    ProfScope ps(KC_I8GEMM, c->stream);
+    FGB_LAUNCH(launch_ozgemm(S, 0, c->qsl.as<int8_t>(), ge, (int)rows, c->xsl.as<int8_t>(), xe, (int)xp, (int)kp,
+                             static_cast<double*>(m), n, n * n, (int)n, (int)np, (int)n, c->stream),
+               1);
+    return FGFRFT_OK;
+}
+
 // s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
 // Order sweeps (>= 8 orders) use the DMMA split-K contraction (every byte of M and of the cache
 // read once per 64 orders); a few orders use the scalar tile-pair kernel (HBM-bound).
@@ -691,7 +782,11 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         // M_a = G_a X^H  (n x n, K = b); real cache: only M_re = Re(G X^H) is needed
-        {
+        if (use_int8_gemm(c)) {
+            if (int st = int8_gx(c, na, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, x_dev, b,
+                                 c->m.p))
+                return st;
+        } else {
             ProfScope ps(KC_GEMM, c->stream);
             if (c->real)
                 FGB_LAUNCH(launch_rgemm(2, 2, 0, n, n, 2 * (int)b,
@@ -1104,7 +1199,9 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
         const int na = std::min(chunk, n_alpha - a0);
         void* ya = y_dev ? static_cast<char*>(y_dev) + (size_t)a0 * blk * c->sig : c->y.p;
         if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p, true)) return st;
-        {
+        if (use_int8_gemm(c)) {
+            if (int st = int8_qx(c, na, false, c->q.p, x_dev, b, ya)) return st;
+        } else {
             ProfScope ps(KC_GEMM, c->stream);
             if (c->real)
                 FGB_LAUNCH(launch_rgemm(0, 1, 1, n, 2 * (int)b, n, c->q.p, n, (int64_t)sl, x_dev, n, 0, ya, n,

@@ -75,6 +75,7 @@ def test_sharded_step_wrapper_single_rank():
     xc = cfg.x + 0.05
     loss, dl = w.mse_step(cfg.alphas, cfg.x, xc)
     g = fg.PowerCache(cfg.f, cfg.l)
+    g.set_engine(fg.ENGINE_DMMA)  # the shards run the DMMA kernels: compare like with like
     l2, d2, _ = fg.mse_step(g, cfg.alphas, cfg.x, xc)
     assert loss[0] == pytest.approx(l2[0], rel=1e-12)
     assert dl[0] == pytest.approx(d2[0], rel=1e-9, abs=1e-14)

@@ -376,3 +376,35 @@ def test_power_route_matches_oracle(n, l, b, n_alpha):
     loss2, dl2, y2 = fg.mse_step(g, alphas, x, xc, want_y=True)
     assert np.max(np.abs(loss2 - loss) / loss) <= 1e-10
     assert all(rel(y2[i], y[i]) <= 1e-10 for i in range(len(alphas)))
+
+
+@pytest.mark.parametrize("n,l,b", [(96, 8, 7), (300, 16, 40), (512, 24, 129)])
+def test_int8_synthesis_route_matches_oracle(n, l, b):
+    """Real F, few orders (synthesis route) with the INT8 engine: op(Q) X and Re(G X^H) are Ozaki
+    GEMMs on the INT8 tensor cores; forward, inverse, loss and dL/dalpha within 1e-10 of the
+    oracle, and within 1e-10 of the DMMA engine."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.08, 3 + n)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    g.set_engine(fg.ENGINE_INT8)
+    rng = np.random.default_rng(b)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    alphas = [0.37, -1.3]  # 2 orders < L / 2: synthesis route
+    y = fg.apply_series(g, alphas, x)
+    yi = fg.apply_series(g, alphas, x, inverse=True)
+    loss, dl, _ = fg.mse_step(g, alphas, x, xc)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        assert rel(y[i], q @ x) <= 2e-12
+        assert rel(yi[i], q.T @ x) <= 2e-12
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
+        assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+    g.set_engine(fg.ENGINE_DMMA)
+    y2 = fg.apply_series(g, alphas, x)
+    loss2, dl2, _ = fg.mse_step(g, alphas, x, xc)
+    assert all(rel(y2[i], y[i]) <= 2e-12 for i in range(2))
+    assert np.max(np.abs(loss2 - loss) / loss) <= 1e-10
