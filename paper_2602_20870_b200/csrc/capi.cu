@@ -88,7 +88,7 @@ cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int 
                             cudaStream_t stream);
 int combine_max_terms();
 size_t combine_partial_elems(int tp);
-cudaError_t launch_combine(const double* z, const double* x, const double* xc, int64_t count, int l,
+cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
                            double* loss, cudaStream_t stream);
 }  // namespace fgb
@@ -555,11 +555,21 @@ int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host
 bool use_int8_gemm(const fgfrft_cache* c);
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
+bool use_power_route(const fgfrft_cache* c, int n_alpha);
+int apply_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, int64_t b, void* y_dev);
 
 // Y[a] = op(Q(alpha_a)) X for all orders; x_dev n x b, y_dev n_alpha blocks of n x b.
 int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used, bool inverse, const void* x_dev,
                  int64_t b, void* y_dev) {
     double* coef = nullptr;
+    if (l_used == c->l && use_power_route(c, n_alpha)) {
+        // Q(a)^T = Q(-a) bit-exactly (the coefficients mirror exactly, sinc.hpp / test_sinc.cpp:40-46)
+        std::vector<double> al(alphas, alphas + n_alpha);
+        if (inverse)
+            for (double& v : al) v = -v;
+        if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
+        return apply_power_route(c, coef, n_alpha, x_dev, b, y_dev);
+    }
     if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
@@ -678,7 +688,7 @@ int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void
     for (int a0 = 0; a0 < n_alpha; a0 += 64) {
         const int na = std::min(64, n_alpha - a0);
         ProfScope ps(KC_COMBINE, c->stream);
-        FGB_LAUNCH(launch_combine(c->z.as<double>(), static_cast<const double*>(x_dev),
+        FGB_LAUNCH(launch_combine(0, c->z.as<double>(), static_cast<const double*>(x_dev),
                                   static_cast<const double*>(xc_dev), count, l, coef + (size_t)a0 * width, na, norm,
                                   y_dev ? static_cast<double*>(y_dev) + (size_t)a0 * count : nullptr,
                                   c->partial.as<double>(), s_dev + (size_t)a0 * width, loss_dev + a0, c->stream),
@@ -766,10 +776,45 @@ int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b
     return FGFRFT_OK;
 }
 
+// Y_a = F^(alpha_a) X over the power products (coef: the orders' c tables, inverse already folded
+// in by the caller as alpha -> -alpha).
+int apply_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, int64_t b, void* y_dev) {
+    if (int st = power_products(c, x_dev, b)) return st;
+    const size_t width = (size_t)(2 * c->l + 1);
+    const int64_t count = 2 * c->n * b;
+    for (int a0 = 0; a0 < n_alpha; a0 += 64) {
+        const int na = std::min(64, n_alpha - a0);
+        ProfScope ps(KC_COMBINE, c->stream);
+        FGB_LAUNCH(launch_combine(1, c->z.as<double>(), static_cast<const double*>(x_dev), nullptr, count, c->l,
+                                  coef + (size_t)a0 * width, na, 0.0, static_cast<double*>(y_dev) + (size_t)a0 * count,
+                                  nullptr, nullptr, nullptr, c->stream),
+                   1);
+    }
+    return FGFRFT_OK;
+}
+
+// s_aq = Re<G_a, F^(q-L) X> for all orders over the power products.
+int dots_power_route(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
+    if (int st = power_products(c, x_dev, b)) return st;
+    const size_t width = (size_t)(2 * c->l + 1);
+    const int64_t count = 2 * c->n * b;
+    FGB_CUDA(c->partial.ensure(combine_partial_elems(combine_max_terms()) * sizeof(double)));
+    for (int a0 = 0; a0 < n_alpha; a0 += 64) {
+        const int na = std::min(64, n_alpha - a0);
+        ProfScope ps(KC_COMBINE, c->stream);
+        FGB_LAUNCH(launch_combine(2, c->z.as<double>(), static_cast<const double*>(x_dev),
+                                  static_cast<const double*>(g_dev) + (size_t)a0 * count, count, c->l, nullptr, na, 0.0,
+                                  nullptr, c->partial.as<double>(), s_dev + (size_t)a0 * width, nullptr, c->stream),
+                   2);
+    }
+    return FGFRFT_OK;
+}
+
 // s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
 // Order sweeps (>= 8 orders) use the DMMA split-K contraction (every byte of M and of the cache
 // read once per 64 orders); a few orders use the scalar tile-pair kernel (HBM-bound).
 int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_dev, int64_t b, double* s_dev) {
+    if (use_power_route(c, n_alpha)) return dots_power_route(c, n_alpha, g_dev, x_dev, b, s_dev);
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
     const bool mma = n_alpha >= 8 && c->dtype == FGFRFT_C128;  // real caches: rdots_mma (same cap)

@@ -24,44 +24,45 @@ constexpr int kCbMaxT = 136;  // padded terms (2L + 1 <= 129 -> L <= 64), multip
 __host__ __device__ constexpr int cb_ldc(int tp) { return tp + ((4 - tp % 16) + 16) % 16; }  // = 4 mod 16
 
 size_t combine_smem_bytes(int tp) {
-    return ((size_t)kCbA * cb_ldc(tp) + (size_t)tp * kCbLdP + (size_t)kCbA * kCbLdP + kCbP) * sizeof(double);
+    return ((size_t)kCbA * cb_ldc(tp) + 2 * (size_t)tp * kCbLdP + 2 * kCbP) * sizeof(double);
 }
 
 int combine_max_terms() { return kCbMaxT; }
 
 // z: 2L blocks of `count` doubles: block j < L holds F^(j+1) X, block L + j holds F^-(j+1) X.
-template <bool STORE_Y>
+// Warp w owns orders 8w..8w+7 for both GEMMs, so G never leaves the warp: the Y accumulators
+// are turned into the A fragments of S += G Z^T with quad shuffles. The chunk ring is double
+// buffered (cp.async prefetch of chunk i+1 while chunk i is multiplied): one barrier per chunk.
+// MODE 0: MSE step (Y, loss, S; Y stored when y != null). MODE 1: apply (Y only, stored).
+// MODE 2: dots (S += G Z^T for a caller's G = `xc`, A blocks of `count`; no Y).
+template <int MODE>
 __global__ void __launch_bounds__(256, 1)
 combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const double* __restrict__ xc,
                int64_t count, int l, int tp, const double* __restrict__ coef, int n_alpha, double g_scale,
                double* __restrict__ y, double* __restrict__ spart, double* __restrict__ lpart) {
+    constexpr bool kY = MODE != 2, kS = MODE != 1;
     extern __shared__ __align__(16) double sm[];
     const int ldc = cb_ldc(tp);
-    double* cf = sm;                       // [64][ldc]   coefficients c_aq (zero padded)
-    double* zc = cf + kCbA * ldc;          // [tp][68]    chunk of every term
-    double* gs = zc + tp * kCbLdP;         // [64][68]    G chunk
-    double* xs = gs + kCbA * kCbLdP;       // [64]        Xc chunk
+    double* cf = sm;                       // [64][ldc]      coefficients c_aq (zero padded)
+    double* zb = cf + kCbA * ldc;          // 2 x [tp][68]   chunk of every term
+    double* xb = zb + 2 * tp * kCbLdP;     // 2 x [64]       Xc chunk
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int T = 2 * l + 1;
 
     for (int idx = tid; idx < kCbA * ldc; idx += 256) {
         const int a = idx / ldc, q = idx - a * ldc;
-        cf[idx] = (a < n_alpha && q < T) ? coef[(int64_t)a * T + q] : 0.0;
+        cf[idx] = (coef && a < n_alpha && q < T) ? coef[(int64_t)a * T + q] : 0.0;
     }
-    for (int idx = tid; idx < (tp - T) * kCbLdP; idx += 256) zc[T * kCbLdP + idx] = 0.0;
-
-    double sacc[kCbMaxT / 8][2];
-    const int nqb = tp / 8;
-#pragma unroll
-    for (int qb = 0; qb < kCbMaxT / 8; ++qb) sacc[qb][0] = sacc[qb][1] = 0.0;
-    double lacc = 0.0;  // sum of R^2 over this thread's (order g of warp, positions)
+    for (int idx = tid; idx < (tp - T) * kCbLdP; idx += 256) {
+        zb[T * kCbLdP + idx] = 0.0;
+        zb[(tp + T) * kCbLdP + idx] = 0.0;
+    }
 
     const int64_t nchunks = (count + kCbP - 1) / kCbP;
-    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    auto stage = [&](int64_t ch, int buf) {
         const int64_t p0 = ch * kCbP;
         const int pv = (int)((count - p0) < kCbP ? (count - p0) : kCbP);
-        __syncthreads();  // previous chunk's readers are done
-        // stage the chunk of every term (16-byte cp.async; count is a multiple of 2)
+        double* zc = zb + buf * tp * kCbLdP;
         for (int idx = tid; idx < T * (kCbP / 2); idx += 256) {
             const int q = idx / (kCbP / 2), c2 = idx - q * (kCbP / 2);
             const double* src;
@@ -71,50 +72,98 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
             const bool v = 2 * c2 < pv;
             cp_async16(zc + q * kCbLdP + 2 * c2, src + p0 + (v ? 2 * c2 : 0), v);
         }
-        if (tid < kCbP / 2) cp_async16(xs + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
-        cp_async_commit();
+        if (MODE == 0 && tid < kCbP / 2)
+            cp_async16(xb + buf * kCbP + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
+    };
+
+    double sacc[kCbMaxT / 8][2];
+    const int nqb = tp / 8;
+#pragma unroll
+    for (int qb = 0; qb < kCbMaxT / 8; ++qb) sacc[qb][0] = sacc[qb][1] = 0.0;
+    double lacc = 0.0;  // sum of R^2 over this thread's (order g of warp, positions)
+    const int a = 8 * warp + g;
+    const bool a_ok = a < n_alpha;
+    const double* crow = cf + a * ldc;
+
+    int buf = 0;
+    if (blockIdx.x < nchunks) stage(blockIdx.x, 0);
+    cp_async_commit();
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, buf ^= 1) {
+        const int64_t p0 = ch * kCbP;
+        const int pv = (int)((count - p0) < kCbP ? (count - p0) : kCbP);
         cp_async_wait<0>();
-        __syncthreads();
+        __syncthreads();  // chunk `buf` landed for everyone; everyone is done with buffer buf^1
+        if (ch + gridDim.x < nchunks) stage(ch + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        const double* zc = zb + buf * tp * kCbLdP;
+        const double* xs = xb + buf * kCbP;
 
         // Y (orders 8w..8w+7) x (64 positions) = C Z_chunk
         double yacc[8][2];
 #pragma unroll
         for (int pb = 0; pb < 8; ++pb) yacc[pb][0] = yacc[pb][1] = 0.0;
-        const double* crow = cf + (8 * warp + g) * ldc;
-        for (int q0 = 0; q0 < tp; q0 += 4) {
-            const double av = crow[q0 + t];
-            const double* zrow = zc + (q0 + t) * kCbLdP + g;
+        if (kY) {
+            for (int q0 = 0; q0 < tp; q0 += 4) {
+                const double av = crow[q0 + t];
+                const double* zrow = zc + (q0 + t) * kCbLdP + g;
 #pragma unroll
-            for (int pb = 0; pb < 8; ++pb) dmma884(yacc[pb][0], yacc[pb][1], av, zrow[8 * pb]);
+                for (int pb = 0; pb < 8; ++pb) dmma884(yacc[pb][0], yacc[pb][1], av, zrow[8 * pb]);
+            }
         }
-        // residual, loss, G; optional Y store
-        const int a = 8 * warp + g;
+        if (MODE == 0) {
+            // residual, loss, G (in place of Y), optional Y store
+#pragma unroll
+            for (int pb = 0; pb < 8; ++pb) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int p = 8 * pb + 2 * t + e;
+                    const bool ok = p < pv && a_ok;
+                    if (y && ok) y[(int64_t)a * count + p0 + p] = yacc[pb][e];
+                    const double r = ok ? yacc[pb][e] - xs[p] : 0.0;
+                    lacc += r * r;
+                    yacc[pb][e] = r * g_scale;
+                }
+            }
+        } else if (MODE == 1) {
+#pragma unroll
+            for (int pb = 0; pb < 8; ++pb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int p = 8 * pb + 2 * t + e;
+                    if (p < pv && a_ok) y[(int64_t)a * count + p0 + p] = yacc[pb][e];
+                }
+            continue;
+        } else {
+            // the caller's G, loaded in the accumulator layout (rows a, positions 8pb + 2t + e)
+#pragma unroll
+            for (int pb = 0; pb < 8; ++pb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int p = 8 * pb + 2 * t + e;
+                    yacc[pb][e] = (p < pv && a_ok) ? xc[(int64_t)a * count + p0 + p] : 0.0;
+                }
+        }
+        // S (orders 8w..8w+7) x (terms) += G_chunk Z_chunk^T. A fragment of k-step (pb, h):
+        // lane (g, t) needs G[g][8pb + 4h + t], held by lane (g, 2h + (t >> 1)) as element t & 1.
 #pragma unroll
         for (int pb = 0; pb < 8; ++pb) {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int p = 8 * pb + 2 * t + e;
-                const bool ok = p < pv && a < n_alpha;
-                const double r = ok ? yacc[pb][e] - xs[p] : 0.0;
-                lacc += r * r;
-                gs[a * kCbLdP + p] = r * g_scale;
-                if (STORE_Y && ok) y[(int64_t)a * count + p0 + p] = yacc[pb][e];
+            for (int h = 0; h < 2; ++h) {
+                const int src = (lane & ~3) | (2 * h + (t >> 1));
+                const double v0 = __shfl_sync(0xffffffffu, yacc[pb][0], src);
+                const double v1 = __shfl_sync(0xffffffffu, yacc[pb][1], src);
+                const double av = (t & 1) ? v1 : v0;
+                const double* zcol = zc + g * kCbLdP + 8 * pb + 4 * h + t;
+#pragma unroll
+                for (int qb = 0; qb < kCbMaxT / 8; ++qb)
+                    if (qb < nqb) dmma884(sacc[qb][0], sacc[qb][1], av, zcol[8 * qb * kCbLdP]);
             }
         }
-        __syncthreads();
-        // S (orders 8w..8w+7) x (terms) += G_chunk Z_chunk^T
-        const double* grow = gs + (8 * warp + g) * kCbLdP;
-        for (int p4 = 0; p4 < kCbP; p4 += 4) {
-            const double av = grow[p4 + t];
-            const double* zcol = zc + g * kCbLdP + p4 + t;
-#pragma unroll
-            for (int qb = 0; qb < kCbMaxT / 8; ++qb)
-                if (qb < nqb) dmma884(sacc[qb][0], sacc[qb][1], av, zcol[8 * qb * kCbLdP]);
-        }
     }
+    cp_async_wait<0>();
+    if (!kS) return;
     // partials: spart[cta][a][q] (q < tp), lpart[cta][a]
     double* sp = spart + (int64_t)blockIdx.x * kCbA * tp;
-    const int a = 8 * warp + g;
 #pragma unroll
     for (int qb = 0; qb < kCbMaxT / 8; ++qb)
         if (qb < nqb) {
@@ -137,7 +186,7 @@ __global__ void combine_reduce_kernel(const double* __restrict__ spart, const do
         for (int c = 0; c < ctas; ++c) acc += spart[((int64_t)c * kCbA + a) * tp + q];
         s[idx] = acc;
     }
-    if (idx < n_alpha) {
+    if (loss && idx < n_alpha) {
         double acc = 0.0;
         for (int c = 0; c < ctas; ++c) acc += lpart[(int64_t)c * kCbA + idx];
         loss[idx] = acc * norm;
@@ -148,37 +197,51 @@ int combine_ctas() { return FGFRFT_SMS; }
 
 size_t combine_partial_elems(int tp) { return (size_t)FGFRFT_SMS * kCbA * (tp + 1); }
 
-// n_alpha <= 64, 2l + 1 <= 136; count = 2 N B (even). spart >= combine_partial_elems doubles.
-cudaError_t launch_combine(const double* z, const double* x, const double* xc, int64_t count, int l,
+template <int MODE>
+static cudaError_t combine_attr() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(combine_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)combine_smem_bytes(kCbMaxT));
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
+// mode 0 (MSE: xc = clean signals, y optional), 1 (apply: y required), 2 (dots: xc = G, A blocks).
+// n_alpha <= 64, 2l + 1 <= 136; count = 2 N B (even). partial >= combine_partial_elems doubles.
+cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
                            double* loss, cudaStream_t stream) {
     const int T = 2 * l + 1, tp = (T + 7) / 8 * 8;
-    if (n_alpha < 1 || n_alpha > kCbA || tp > kCbMaxT || count % 2) return cudaErrorInvalidValue;
+    if (n_alpha < 1 || n_alpha > kCbA || tp > kCbMaxT || count % 2 || mode < 0 || mode > 2) return cudaErrorInvalidValue;
     const size_t smem = combine_smem_bytes(tp);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(combine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)combine_smem_bytes(kCbMaxT));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(combine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)combine_smem_bytes(kCbMaxT));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
     const int64_t nchunks = (count + kCbP - 1) / kCbP;
     const int ctas = (int)(nchunks < FGFRFT_SMS ? nchunks : FGFRFT_SMS);
     double* spart = partial;
     double* lpart = partial + (size_t)ctas * kCbA * tp;
-    if (y)
-        combine_kernel<true><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 2.0 * norm, y, spart,
-                                                          lpart);
-    else
-        combine_kernel<false><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 2.0 * norm, y,
-                                                           spart, lpart);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+    switch (mode) {
+        case 0:
+            if ((e = combine_attr<0>()) != cudaSuccess) return e;
+            combine_kernel<0><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 2.0 * norm, y, spart,
+                                                           lpart);
+            break;
+        case 1:
+            if ((e = combine_attr<1>()) != cudaSuccess) return e;
+            combine_kernel<1><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 0.0, y, spart,
+                                                           lpart);
+            return cudaGetLastError();
+        default:
+            if ((e = combine_attr<2>()) != cudaSuccess) return e;
+            combine_kernel<2><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 0.0, y, spart,
+                                                           lpart);
+            break;
+    }
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int threads = 256, blocks = (n_alpha * T + threads - 1) / threads;
-    combine_reduce_kernel<<<blocks, threads, 0, stream>>>(spart, lpart, ctas, tp, T, n_alpha, norm, s, loss);
+    combine_reduce_kernel<<<blocks, threads, 0, stream>>>(spart, lpart, ctas, tp, T, n_alpha, norm, s,
+                                                          mode == 0 ? loss : nullptr);
     return cudaGetLastError();
 }
 

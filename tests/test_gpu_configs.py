@@ -144,7 +144,8 @@ def test_config4_point_cloud_full_size():
     assert cfg.n == 8192 and cfg.l == 128 and cfg.b == 1536
     cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=140 << 30)
     try:
-        assert cache.device_bytes() == 128 * 8192 * 8192 * 16
+        assert cache.is_real()  # graph GFT: real orthogonal F -> real cache (8 B per element)
+        assert cache.device_bytes() == 128 * 8192 * 8192 * 8
         _sampled_checks(cfg, cache, cols=slice(0, 6), budget_cols=4)
     finally:
         cache.close()

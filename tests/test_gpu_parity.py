@@ -408,3 +408,28 @@ def test_int8_synthesis_route_matches_oracle(n, l, b):
     loss2, dl2, _ = fg.mse_step(g, alphas, x, xc)
     assert all(rel(y2[i], y[i]) <= 2e-12 for i in range(2))
     assert np.max(np.abs(loss2 - loss) / loss) <= 1e-10
+
+
+@pytest.mark.parametrize("n,l,b,n_alpha", [(64, 8, 5, 9), (256, 32, 17, 40)])
+def test_power_route_apply_and_dlda(n, l, b, n_alpha):
+    """Order sweeps of apply_forward / apply_inverse and of the dL/dalpha contraction through the
+    power products (INT8 engine): within 1e-10 of the oracle; Q(a)^T X is Q(-a) X."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 21 + n)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    g.set_engine(fg.ENGINE_INT8)
+    rng = np.random.default_rng(7 * n + b)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    gr = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    alphas = list(np.linspace(-1.7, 2.3, n_alpha))
+    y = fg.apply_series(g, alphas, x)
+    yi = fg.apply_series(g, alphas, x, inverse=True)
+    dl, s = fg.dlda(g, alphas, np.broadcast_to(gr, (n_alpha, n, b)), x)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        assert rel(y[i], q @ x) <= 1e-11
+        assert rel(yi[i], q.T @ x) <= 1e-11
+        s_ref = O.power_dots(o, gr @ x.conj().T)
+        _, dc = O.sinc_coeffs(a, l)
+        assert np.max(np.abs(s[i] - s_ref)) <= 1e-10 * np.max(np.abs(s_ref))
+        assert abs(dl[i] - float(np.dot(dc, s_ref))) <= 1e-10 * np.sum(np.abs(dc * s_ref))
