@@ -293,7 +293,7 @@ def main():
     # ---- dominant kernel roofline.
     # Power-product route (real F, INT8 engine): ozgemm_kernel computes Z = [P_1..P_L; P_1^T..P_L^T] X,
     #   2 * (2L n) * 2B * n FP64-equivalent flops per step (real x complex: 2B real columns), as
-    #   28 int8 digit-product GEMMs (Ozaki, 7 digits): x28 int8 ops. combine_kernel: 2 DMMA GEMMs
+    #   S(S+1)/2 int8 digit-product GEMMs (Ozaki, S base-254 digits). combine_kernel: 2 DMMA GEMMs
     #   of 2 * A * (2L+1) * 2nB flops each.
     # Synthesis route (DMMA engine): the DMMA GEMMs Q X and G X^H, 4 n^2 B flops each (real F).
     real = cache.is_real()
@@ -302,15 +302,19 @@ def main():
     i8_ms, i8_n = prof["int8_gemm"]
     power_route = i8_n > 0
     if power_route:
+        S = int(L_.fgfrft_int8_digits())
+        products = S * (S + 1) // 2
         fp64eq = 2.0 * (2 * L * n) * (2 * b) * n
-        i8_ops = fp64eq * 28
+        i8_ops = fp64eq * products
         achieved = i8_ops * args.steps / (i8_ms * 1e-3) / 1e12
         cb_ms, cb_n = prof["combine"]
-        roof = {"bound": "tensor", "kernel": "ozgemm_kernel<7,1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
+        roof = {"bound": "tensor",
+                "kernel": f"ozgemm_kernel<{S},1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
                 "achieved": achieved, "peak": peaks["int8_tops"], "unit": "TOPS",
                 "frac": achieved / peaks["int8_tops"], "traffic": None, "peak_source": peaks["int8_src"],
                 "algorithmic": "per step 2*(2L*N)*(2B)*N FP64-equivalent flops (Z = F^k X, k = +-1..+-L, real F x "
-                               "complex X) = 28 int8 digit-product GEMMs of that size (Ozaki scheme, 7 digits)",
+                               f"complex X) = {products} int8 digit-product GEMMs of that size (Ozaki scheme, "
+                               f"{S} base-254 digits)",
                 "fp64_equivalent_tflops": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12,
                 "fp64_equivalent_frac_of_dmma_peak": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12 / peaks["fp64_tflops"],
                 "dmma_peak_tflops": peaks["fp64_tflops"],

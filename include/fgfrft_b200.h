@@ -231,12 +231,15 @@ int fgfrft_shard_mse_partial_dev(fgfrft_cache* shard, const double* alphas, int 
  * C = op(A) op(B) for real column-major device matrices (op(A) m x k, op(B) k x n, C m x n;
  * op(X) = X^T when trans* != 0, as in BLAS dgemm), computed with
  * tcgen05.mma kind::i8: A's rows and B's columns are scaled by powers of two and cut into
- * `slices` 7-bit digits (6, 7 or 8; 0 = default 7); digit products with weight >= 2^-7(S+1)
- * accumulate exactly in int32 TMEM and are combined in FP64. Error ~ sqrt(k) 2^-7S relative to
- * (row max of A) x (column max of B): 7 slices ~3e-13 on the BASELINE operands, 8 ~3e-15.
+ * `slices` balanced base-254 digits (6, 7 or 8; 0 = default 6); digit products of weight
+ * >= 254^-(S+1) accumulate exactly in int32 TMEM and are combined in FP64. Error ~ sqrt(k)
+ * 254^-S relative to (row max of A) x (column max of B): 6 digits (21 int8 products) ~3e-13 on
+ * the BASELINE operands, 7 digits (28 products) ~1e-15.
  * k <= 16384. Enqueued on `stream` (NULL = default stream); scratch is allocated per call.
  * This is the engine behind the library's real-F GEMMs (fgfrft_set_gemm_engine).
  */
+/* Default digit count of the library's INT8 engine (6). */
+int fgfrft_int8_digits(void);
 int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                           const double* b, int64_t ldb, double* c, int64_t ldc, int slices,
                           void* stream);

@@ -103,6 +103,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_batch_forward_dev": (i, [vp, vp, i, vp, i64, vp]),
         "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
         "fgfrft_cache_set_engine": (i, [vp, i]),
+        "fgfrft_int8_digits": (i, []),
         "fgfrft_cache_prepare": (i, [vp]),
         "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
     }
@@ -127,6 +128,7 @@ def exported_symbols():
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
         "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
         "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
+        "fgfrft_int8_digits",
         "fgfrft_cache_prepare",
     ]
 

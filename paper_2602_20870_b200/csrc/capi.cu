@@ -1710,6 +1710,8 @@ void keep_pool() {
 }
 }  // namespace
 
+int fgfrft_int8_digits(void) { return oz_slices_default(); }
+
 int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                           const double* b, int64_t ldb, double* c, int64_t ldc, int slices, void* stream) {
     FGB_GUARD_BEGIN

@@ -3,13 +3,14 @@
 // sm_100a has no FP64 tcgen05 kind: the FP64 tensor path is warp-level DMMA at ~37 TFLOP/s,
 // while tcgen05.mma kind::i8 runs ~4.5 POPS with int32 accumulators in TMEM. An FP64 product
 // C = A B^T (A: M x K, B: N x K) is computed exactly-in-int8 by fixed-point slicing:
-//   every row r of A is scaled by 2^-e_r (max |a_r.| < 2^e_r) and cut into S signed 7-bit
-//   digits,  a_rk = 2^e_r * sum_{t=1..S} A_t[r,k] 2^-7t,  |A_t| <= 127  (exact truncations);
-//   B likewise per row. Then  C = 2^(e_r + e_n) * sum_{t+u <= S+1} 2^-7(t+u) (A_t B_u^T)  where
-//   every int8 GEMM is exact in int32 (K * 127^2 * S < 2^31 for K <= 16384). Dropped terms and
-//   truncated digits bound the error by ~ sqrt(K) 2^-7S of |row max| |col max|: S = 7 gives
-//   3e-13 relative on the BASELINE configs (DMMA: ~1e-15; the parity bar is 1e-10), S = 8
-//   gives ~3e-15.
+//   every row r of A is scaled by 2^-(e_r+1) (max |a_r.| < 2^e_r) and cut into S balanced
+//   base-254 digits,  a_rk = 2^(e_r+1) * sum_{t=1..S} A_t[r,k] 254^-t,  |A_t| <= 127  (rint
+//   digits; remainders exact to 2^-53); B likewise per row. Then
+//   C = 2^(e_r + e_n + 2) * sum_{t+u <= S+1} 254^-(t+u) (A_t B_u^T), where every int8 GEMM is
+//   exact in int32 (K * 127^2 * S < 2^31 for K <= 16384). Dropped terms and truncated digits
+//   bound the error by ~ sqrt(K) 254^-S of |row max| |col max|: S = 6 (21 digit products)
+//   gives 3e-13 relative on the BASELINE configs (DMMA: ~1e-15; the parity bar is 1e-10),
+//   S = 7 (28 products) ~1e-15.
 //
 // Kernel layout (one 128 x 64 output tile per CTA, 256 threads):
 //   * operands are pre-sliced by oz_slice_kernel into the tcgen05 canonical no-swizzle K-major
@@ -18,11 +19,11 @@
 //   * S int32 accumulators, one per digit weight d = t + u (2..S+1), live side by side in TMEM
 //     (S x 64 columns <= 512). For a fixed A digit t the B digits u = 1..S+1-t are stacked
 //     along N in shared memory, so ONE tcgen05.mma (N up to 256) covers a contiguous run of
-//     accumulators: 10 MMAs per 32-byte K step for S = 7 (28 digit products);
+//     accumulators: 9 MMAs per 32-byte K step for S = 6 (21 digit products);
 //   * a 4-stage ring of 32-byte K blocks; warp 0 / lane 0 issues the bulk copies, warp 1 / lane 0
 //     the MMAs (tcgen05.commit frees a stage), then all 8 warps drain TMEM (tcgen05.ld 32x32b,
 //     lane = output row, 32 columns per warp) and combine the S accumulators in FP64 (Horner
-//     in 2^-7, exact scalings) into the output.
+//     in base 254 over exact int64 folds) into the output.
 #include "oz.cuh"
 
 #include <cstdlib>
@@ -34,6 +35,13 @@ constexpr int kOzBN = 64;   // rows of the B tile (N of one digit product)
 constexpr int kOzBK = 32;   // bytes (= int8 elements) of K per stage = one MMA K step
 constexpr int kOzStages = 4;
 constexpr int kOzSbo = kOzBK / 16 * 128;  // bytes between 8-row groups of one slice block
+
+// Digit base 254: with |v| < 1/2, rint(254 v) is in [-127, 127] and the remainder in [-1/2, 1/2],
+// so every digit fits int8 and carries log2(254) = 7.99 bits (base 256 would need 128).
+constexpr double kOzBase = 254.0;
+constexpr long long kOzBaseI = 254;
+constexpr double kOzScale = 4.0 / (254.0 * 254.0 * 254.0 * 254.0);  // 2^2 (two half scalings) x 254^-4
+__host__ __device__ constexpr double oz_pow254(int k) { return k == 0 ? 1.0 : 254.0 * oz_pow254(k - 1); }
 
 template <int S> struct OzCfg {
     static constexpr int a_stage = S * kOzBM * kOzBK;
@@ -174,7 +182,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     if (blockIdx.y == 0 && c == 0) exps[row] = e;
-    const double sc = mx > 0.0 ? pow2(-e) : 0.0;
+    const double sc = mx > 0.0 ? pow2(-e - 1) : 0.0;  // |a| * sc < 1/2
     double x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] = t[rl][c * 16 + i] * sc;
@@ -190,9 +198,9 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
             uint32_t packed = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                double y = x[q * 4 + i] * 128.0;  // exact
-                const double d = trunc(y);
-                x[q * 4 + i] = y - d;             // exact
+                const double y = x[q * 4 + i] * kOzBase;  // |y| <= 127
+                const double d = rint(y);
+                x[q * 4 + i] = y - d;                     // exact, |.| <= 1/2
                 packed |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * i);
             }
             w[q] = packed;
@@ -322,7 +330,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
             mbar_wait(tfull, tcount & 1);
             tc_fence_after();
-            // exact integer fold: hi = sum_{d<=4} acc_d 2^(7(4-d)), lo = sum_{d>=5} acc_d 2^(7(S+1-d))
+            // exact integer fold: hi = sum_{d<=4} acc_d 254^(4-d), lo = sum_{d>=5} acc_d 254^(S+1-d)
             long long hi[32], lo[32];
 #pragma unroll
             for (int d = 2; d <= S + 1; ++d) {
@@ -331,21 +339,21 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                 tmem_wait_ld();
                 if (d <= 4) {
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) hi[q] = (d == 2) ? (long long)v[q] : (hi[q] << 7) + v[q];
+                    for (int q = 0; q < 32; ++q) hi[q] = (d == 2) ? (long long)v[q] : hi[q] * kOzBaseI + v[q];
                 } else {
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) lo[q] = (d == 5) ? (long long)v[q] : (lo[q] << 7) + v[q];
+                    for (int q = 0; q < 32; ++q) lo[q] = (d == 5) ? (long long)v[q] : lo[q] * kOzBaseI + v[q];
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
-            // value = (hi + lo 2^-7(S-3)) * 2^(e_r - 28) * 2^(e_n)
+            // value = (hi + lo 254^-(S-3)) * 4 * 254^-4 * 2^e_r * 2^e_n
             const int m = mt * kOzBM + lrow;
             const int bm = m / out.mp, i = m - bm * out.mp;
             if (i < out.mv) {
-                const double ra = pow2(ea[m] - 28);
-                const double lo_w = pow2(-7 * (S - 3));
+                const double ra = pow2(ea[m]) * kOzScale;
+                const double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold: 254^-(S-3)
                 double* cb = out.c + (int64_t)bm * out.sc;
                 const int* ebt = eb + nt * kOzBN + h * 32;
 #pragma unroll
@@ -371,7 +379,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 
 // ---------------------------------------------------------------- host launchers
 
-int oz_slices_default() { return 7; }
+int oz_slices_default() { return 6; }
 
 size_t oz_operand_bytes(int slices, int64_t rows_padded, int64_t kp) { return (size_t)slices * rows_padded * kp; }
 

@@ -18,24 +18,26 @@ def _exactish(a, b):
 
 @pytest.mark.parametrize("m,n,k", [(128, 64, 64), (256, 128, 1024), (300, 70, 100), (1, 1, 1), (129, 65, 65), (384, 256, 200), (256, 320, 64),
                                    (1024, 512, 1024)])
-@pytest.mark.parametrize("slices", [7, 8])
+@pytest.mark.parametrize("slices", [6, 7, 8])
 def test_int8_gemm_accuracy(m, n, k, slices):
     rng = np.random.default_rng(m * 1000 + n * 10 + k)
     a = rng.standard_normal((m, k))
     b = rng.standard_normal((k, n))
     c = fg.dgemm_int8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), slices).cpu().numpy()
     ref = _exactish(a, b)
-    tol = 2e-12 if slices == 7 else 5e-14
+    tol = {6: 2e-12, 7: 2e-14, 8: 2e-15}[slices]
     assert np.linalg.norm(c - ref) <= tol * np.linalg.norm(ref)
 
 
-def test_int8_gemm_small_integers_exact():
-    # |entries| < 2^6 with power-of-two row maxima: every product is a single exact digit pair
+def test_int8_gemm_small_integers():
+    # integer inputs: the base-254 digits reconstruct them to ~2^-53, so 7 digits give the exact
+    # integer products after rounding
     rng = np.random.default_rng(5)
     a = rng.integers(-63, 64, size=(256, 192)).astype(np.float64)
     b = rng.integers(-63, 64, size=(192, 128)).astype(np.float64)
     c = fg.dgemm_int8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 7).cpu().numpy()
-    assert np.array_equal(c, a @ b)
+    assert np.abs(c - a @ b).max() <= 1e-9
+    assert np.array_equal(np.rint(c), a @ b)
 
 
 def test_int8_gemm_scaled_rows_and_zeros():
@@ -44,7 +46,7 @@ def test_int8_gemm_scaled_rows_and_zeros():
     a[7] = 0.0
     b = rng.standard_normal((300, 90)) * np.exp2(rng.integers(-30, 30, size=(1, 90)))
     b[:, 3] = 0.0
-    c = fg.dgemm_int8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 7).cpu().numpy()
+    c = fg.dgemm_int8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 6).cpu().numpy()
     ref = a @ b
     # row/column scaling is exact: relative error per (row, col) block is scale free
     err = np.abs(c - ref) / (np.abs(a).max(1, keepdims=True) * np.abs(b).max(0, keepdims=True) + 1e-300)
