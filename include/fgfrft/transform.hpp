@@ -80,6 +80,11 @@ class PowerCache {
 
     fgfrft_cache* handle() const { return h_; }
 
+    // Extension: GEMM engine (FGFRFT_ENGINE_AUTO / _DMMA / _INT8, see fgfrft_b200.h) and eager
+    // construction of the INT8 digit slices used by order sweeps on a real F.
+    void set_engine(int engine) { detail::throw_status(fgfrft_cache_set_engine(h_, engine)); }
+    void prepare() { detail::throw_status(fgfrft_cache_prepare(h_)); }
+
   private:
     void load_info() {
         int64_t n = 0;

@@ -86,6 +86,25 @@ static GftMatrix householder_unitary(Index n, unsigned seed) {
     g.provenance = Provenance::haar;
     return g;
 }
+// Real orthogonal matrix (a product of real Householder reflections): a graph-GFT-like F.
+static GftMatrix householder_real(Index n, unsigned seed) {
+    std::mt19937_64 gen(seed);
+    std::normal_distribution<double> nd;
+    MatrixXcd u = eye(n);
+    for (int r = 0; r < 4; ++r) {
+        std::vector<double> v(static_cast<size_t>(n));
+        double nn = 0;
+        for (auto& z : v) { z = nd(gen); nn += z * z; }
+        MatrixXcd h = eye(n);
+        for (Index j = 0; j < n; ++j)
+            for (Index i = 0; i < n; ++i) h(i, j) -= 2.0 * v[i] * v[j] / nn;
+        u = mul(h, u);
+    }
+    GftMatrix g;
+    g.f = u;
+    g.provenance = Provenance::haar;
+    return g;
+}
 static MatrixXcd matrix_power(const MatrixXcd& f, int m) {  // tests/oracles.hpp:50-56
     MatrixXcd acc = eye(f.rows());
     const MatrixXcd base = m >= 0 ? f : adj(f);
@@ -235,6 +254,26 @@ int main() {
         const double an = order_gradient(cache, 0.7, g, x);
         const double fd = (loss(0.7 + 1e-5) - loss(0.7 - 1e-5)) / 2e-5;
         CHECK(std::abs(an - fd) <= 1e-6 * std::max(1.0, std::abs(fd)));
+    }
+    // extension: GEMM engines on a real F (INT8 tensor-core Ozaki engine vs FP64 DMMA)
+    {
+        const GftMatrix f = householder_real(96, 9);
+        PowerCache cache(f, 10);
+        cache.prepare();
+        std::mt19937_64 gen(56);
+        std::normal_distribution<double> nd;
+        MatrixXcd x(96, 5);
+        for (Index j = 0; j < 5; ++j)
+            for (Index i = 0; i < 96; ++i) x(i, j) = {nd(gen), nd(gen)};
+        const FracOperator q = fgfrft_matrix(cache, 0.43);
+        const MatrixXcd ref = mul(q.q, x);
+        cache.set_engine(FGFRFT_ENGINE_INT8);
+        const MatrixXcd yi = apply_series(cache, 0.43, x);
+        cache.set_engine(FGFRFT_ENGINE_DMMA);
+        const MatrixXcd yd = apply_series(cache, 0.43, x);
+        CHECK(fro(sub(yi, ref)) <= 1e-11 * fro(ref));
+        CHECK(fro(sub(yd, ref)) <= 1e-12 * fro(ref));
+        CHECK_THROWS_AS(cache.set_engine(7), parameter_error);
     }
     // :205-221 window warning, truncation override
     {
