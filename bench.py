@@ -308,6 +308,13 @@ def main():
         i8_ops = fp64eq * products
         achieved = i8_ops * args.steps / (i8_ms * 1e-3) / 1e12
         cb_ms, cb_n = prof["combine"]
+        # combine: Y = C Z (2*A*(2L+1)*2nB DMMA flops) + either S = G Z^T (same again) or, for an
+        # orthogonal F, the 2(2L+1) dot products R_q = <Xc, Z_q>, gamma(d) = <X, F^d X> (FP64 FMA)
+        gram = cache.orthogonality() is not None and 0 <= cache.orthogonality() <= 1e-12
+        y_flops = 2.0 * A * (2 * L + 1) * 2 * n * b
+        cb_flops = y_flops + (2.0 * 2 * (2 * L + 1) * 2 * n * b if gram else y_flops)
+        cb_form = ("Y = C Z (DMMA) + Gram sequence / R dot products (F orthogonal: "
+                   f"residual {cache.orthogonality():.2e})" if gram else "Y = C Z and S = G Z^T (DMMA)")
         roof = {"bound": "tensor",
                 "kernel": f"ozgemm_kernel<{S},1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
                 "achieved": achieved, "peak": peaks["int8_tops"], "unit": "TOPS",
@@ -320,7 +327,9 @@ def main():
                 "dmma_peak_tflops": peaks["fp64_tflops"],
                 "launches_timed": i8_n, "share_of_step": shares,
                 "combine_kernel": {"ms_per_step": cb_ms / args.steps,
-                                   "tflops": 2 * 2.0 * A * (2 * L + 1) * 2 * n * b * args.steps / (cb_ms * 1e-3) / 1e12,
+                                   "flops_per_step": cb_flops,
+                                   "tflops": cb_flops * args.steps / (cb_ms * 1e-3) / 1e12,
+                                   "form": cb_form,
                                    "peak_dmma_tflops": peaks["fp64_tflops"]}}
     else:
         gemm_ms, gemm_n = prof["dmma_zgemm"]

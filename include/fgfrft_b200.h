@@ -130,6 +130,10 @@ int fgfrft_cache_set_stream(fgfrft_cache* cache, void* stream);
 
 /* Device pointer to slab k-1 (= F^k) and the device memory held by the handle. */
 int fgfrft_cache_set_engine(fgfrft_cache* cache, int engine);
+/* ||F^T F - I||_F / sqrt(n) measured on the device when a real cache is built (gft.hpp:39-44
+ * normalisation); -1 for complex caches. <= 1e-12 enables the Gram form of the power-product
+ * MSE step (s_k from <X, F^d X>). */
+int fgfrft_cache_orthogonality(const fgfrft_cache* cache, double* residual);
 /* Build lazily-built device structures now (the INT8 digit slices of the stacked cache for the
  * power-product route); a no-op for handles that never use them. Synchronises. */
 int fgfrft_cache_prepare(fgfrft_cache* cache);

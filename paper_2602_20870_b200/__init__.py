@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
         "fgfrft_cache_set_engine": (i, [vp, i]),
         "fgfrft_int8_digits": (i, []),
+        "fgfrft_cache_orthogonality": (i, [vp, vp]),
         "fgfrft_cache_prepare": (i, [vp]),
         "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
     }
@@ -128,7 +129,7 @@ def exported_symbols():
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
         "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
         "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
-        "fgfrft_int8_digits",
+        "fgfrft_int8_digits", "fgfrft_cache_orthogonality",
         "fgfrft_cache_prepare",
     ]
 
@@ -268,6 +269,12 @@ class PowerCache:
         """ENGINE_AUTO, ENGINE_DMMA (FP64 tensor cores, synthesis + GEMM per order) or ENGINE_INT8
         (real F: INT8 tensor-core power products, see fgfrft_cache_set_engine)."""
         _check(lib().fgfrft_cache_set_engine(self._h, int(engine)))
+
+    def orthogonality(self) -> float:
+        """||F^T F - I||_F / sqrt(n) measured at build (real caches; -1 otherwise)."""
+        r = ctypes.c_double()
+        _check(lib().fgfrft_cache_orthogonality(self._h, ctypes.addressof(r)))
+        return r.value
 
     def prepare(self) -> None:
         """Build lazily-built device structures (INT8 digit slices of the cache) now."""

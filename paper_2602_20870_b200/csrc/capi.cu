@@ -87,6 +87,7 @@ cudaError_t launch_from_tiled(const void* src, void* dst, int n, int elem_bytes_
 cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int width, double* out,
                             cudaStream_t stream);
 int combine_max_terms();
+cudaError_t launch_ortho_residual(const double* g, int n, double* out, cudaStream_t stream);
 size_t combine_partial_elems(int tp);
 cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
@@ -231,6 +232,10 @@ struct fgfrft_cache {
     // Power-product route (real F): the stacked cache [P_1..P_L; P_1^T..P_L^T] as INT8 Ozaki
     // digit slices (built lazily, once), the per-call slices of X and the products Z = P X.
     int engine = FGFRFT_ENGINE_AUTO;
+    // F^T F = I to rounding (unitarity residual of gft.hpp:39-44 <= 1e-12, checked on device at
+    // build): the power-product MSE step may then take s_k from the Gram sequence <X, F^d X>.
+    bool orthogonal = false;
+    double ortho_residual = -1.0;
     int ps_slices = 0;
     DevBuf ps, pe, prm, xsl, xex, z;
     DevBuf qsl, qex;  // per-call INT8 slices of Q(a) (or G) for the synthesis route
@@ -439,6 +444,20 @@ void destroy_cache(fgfrft_cache* c) {
 // Device cache build: P_1 = F, P_k = F P_{k-1} (transform.hpp:57-58) with the DMMA GEMM in
 // column-major complex128 scratch, each power then written to its tiled slab (demoted to
 // complex64 for C64 caches, so the error does not compound through a complex64 recursion).
+// ||F^T F - I||_F / sqrt(n) on the device (2 n^3 DMMA flops, once per cache; real F only).
+int check_orthogonal(fgfrft_cache* c, const double* fr, double* scratch) {
+    const int n = (int)c->n;
+    FGB_LAUNCH(launch_rgemm(1, 0, 0, n, n, n, fr, n, 0, fr, n, 0, scratch, n, 0, 1, c->stream), 1);
+    FGB_CUDA(c->lpart.ensure(sizeof(double)));
+    FGB_LAUNCH(launch_ortho_residual(scratch, n, c->lpart.as<double>(), c->stream), 1);
+    double r2 = 0.0;
+    FGB_CUDA(cudaMemcpyAsync(&r2, c->lpart.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    c->ortho_residual = std::sqrt(r2 / (double)n);
+    c->orthogonal = c->ortho_residual <= 1e-12;
+    return FGFRFT_OK;
+}
+
 int build_powers(fgfrft_cache* c, const double* f) {
     const size_t ml = c->mat_elems();
     const int n = (int)c->n;
@@ -450,6 +469,7 @@ int build_powers(fgfrft_cache* c, const double* f) {
         FGB_LAUNCH(launch_real_part(c->tmp.p, fr, (int64_t)ml, c->stream), 1);
         FGB_LAUNCH(launch_rto_tiled(fr, c->slab(1), n, c->stream), 1);
         double* prev = reinterpret_cast<double*>(c->tmp.p);  // the complex staging is free now: reuse
+        if (int st = check_orthogonal(c, fr, prev)) return st;
         const double* p = fr;
         for (int k = 2; k <= c->l; ++k) {
             FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, fr, n, 0, p, n, 0, cur, n, 0, 1, c->stream), 1);
@@ -488,6 +508,8 @@ int upload_powers(fgfrft_cache* c, const double* powers) {
             double* fr = reinterpret_cast<double*>(c->tmp.as<double2>() + ml);
             FGB_LAUNCH(launch_real_part(c->tmp.p, fr, (int64_t)ml, c->stream), 1);
             FGB_LAUNCH(launch_rto_tiled(fr, c->slab(k), (int)c->n, c->stream), 1);
+            if (k == 1)
+                if (int st = check_orthogonal(c, fr, reinterpret_cast<double*>(c->tmp.p))) return st;
         } else {
             FGB_LAUNCH(launch_to_tiled(c->tmp.p, c->slab(k), (int)c->n, (int)c->elem, c->stream), 1);
         }
@@ -676,6 +698,11 @@ int power_products(fgfrft_cache* c, const void* x_dev, int64_t b) {
     return FGFRFT_OK;
 }
 
+bool gram_route(const fgfrft_cache* c) {
+    static const bool off = std::getenv("FGFRFT_NO_GRAM") != nullptr;
+    return c->orthogonal && !off;
+}
+
 // MSE step over the power products: loss, s (2L+1 per order) and optionally Y.
 int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev,
                     int64_t b, void* y_dev, double* loss_dev, double* s_dev) {
@@ -688,7 +715,7 @@ int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void
     for (int a0 = 0; a0 < n_alpha; a0 += 64) {
         const int na = std::min(64, n_alpha - a0);
         ProfScope ps(KC_COMBINE, c->stream);
-        FGB_LAUNCH(launch_combine(0, c->z.as<double>(), static_cast<const double*>(x_dev),
+        FGB_LAUNCH(launch_combine(gram_route(c) ? 3 : 0, c->z.as<double>(), static_cast<const double*>(x_dev),
                                   static_cast<const double*>(xc_dev), count, l, coef + (size_t)a0 * width, na, norm,
                                   y_dev ? static_cast<double*>(y_dev) + (size_t)a0 * count : nullptr,
                                   c->partial.as<double>(), s_dev + (size_t)a0 * width, loss_dev + a0, c->stream),
@@ -1011,6 +1038,12 @@ int fgfrft_cache_set_engine(fgfrft_cache* c, int engine) {
     if (engine < FGFRFT_ENGINE_AUTO || engine > FGFRFT_ENGINE_INT8) return fail(FGFRFT_PARAMETER, "unknown engine");
     std::lock_guard<std::mutex> lk(c->mu);
     c->engine = engine;
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_orthogonality(const fgfrft_cache* c, double* residual) {
+    if (int st = check_handle(c)) return st;
+    if (residual) *residual = c->ortho_residual;
     return FGFRFT_OK;
 }
 

@@ -35,12 +35,16 @@ int combine_max_terms() { return kCbMaxT; }
 // buffered (cp.async prefetch of chunk i+1 while chunk i is multiplied): one barrier per chunk.
 // MODE 0: MSE step (Y, loss, S; Y stored when y != null). MODE 1: apply (Y only, stored).
 // MODE 2: dots (S += G Z^T for a caller's G = `xc`, A blocks of `count`; no Y).
+// MODE 3: MSE step for a verified-orthogonal F: Y and the loss as in MODE 0, but instead of the
+//   S GEMM the 2L+1 products R_q = <Xc, Z_q> and the Gram sequence gamma(d) = <X, F^d X>,
+//   d = 0..2L, are accumulated (258 dot products per chunk on the FP64 pipe); S follows from
+//   <Y_a, Z_q> = sum_q' c_aq' <Z_q', Z_q> = sum_q' c_aq' gamma(|q - q'|) (F^T F = I).
 template <int MODE>
 __global__ void __launch_bounds__(256, 1)
 combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const double* __restrict__ xc,
                int64_t count, int l, int tp, const double* __restrict__ coef, int n_alpha, double g_scale,
                double* __restrict__ y, double* __restrict__ spart, double* __restrict__ lpart) {
-    constexpr bool kY = MODE != 2, kS = MODE != 1;
+    constexpr bool kY = MODE != 2, kS = MODE != 1 && MODE != 3, kMse = MODE == 0 || MODE == 3;
     extern __shared__ __align__(16) double sm[];
     const int ldc = cb_ldc(tp);
     double* cf = sm;                       // [64][ldc]      coefficients c_aq (zero padded)
@@ -72,7 +76,7 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
             const bool v = 2 * c2 < pv;
             cp_async16(zc + q * kCbLdP + 2 * c2, src + p0 + (v ? 2 * c2 : 0), v);
         }
-        if (MODE == 0 && tid < kCbP / 2)
+        if (kMse && tid < kCbP / 2)
             cp_async16(xb + buf * kCbP + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
     };
 
@@ -81,6 +85,7 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
 #pragma unroll
     for (int qb = 0; qb < kCbMaxT / 8; ++qb) sacc[qb][0] = sacc[qb][1] = 0.0;
     double lacc = 0.0;  // sum of R^2 over this thread's (order g of warp, positions)
+    double dacc[2] = {0.0, 0.0};  // MODE 3: dot products tid and tid + 256 of the 2 (2L + 1) list
     const int a = 8 * warp + g;
     const bool a_ok = a < n_alpha;
     const double* crow = cf + a * ldc;
@@ -110,7 +115,33 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
                 for (int pb = 0; pb < 8; ++pb) dmma884(yacc[pb][0], yacc[pb][1], av, zrow[8 * pb]);
             }
         }
-        if (MODE == 0) {
+        if (MODE == 3) {
+            // R_q = <Xc, Z_q> (j < T) and gamma(d) (j = T + d): rows (L, L + d) for d <= L, else
+            // (0, d). Position order rotated by j: the 32 lanes read 32 rows without bank conflicts.
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = tid + 256 * h;
+                if (j < 2 * T) {
+                    const double *u, *v;
+                    if (j < T) {
+                        u = xs;
+                        v = zc + j * kCbLdP;
+                    } else {
+                        const int d = j - T;
+                        u = zc + (d <= l ? l : 0) * kCbLdP;
+                        v = zc + (d <= l ? l + d : d) * kCbLdP;
+                    }
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int i = 0; i < kCbP; ++i) {
+                        const int p = (i + j) & (kCbP - 1);
+                        acc = fma(u[p], v[p], acc);
+                    }
+                    dacc[h] += acc;
+                }
+            }
+        }
+        if (kMse) {
             // residual, loss, G (in place of Y), optional Y store
 #pragma unroll
             for (int pb = 0; pb < 8; ++pb) {
@@ -143,6 +174,7 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
                     yacc[pb][e] = (p < pv && a_ok) ? xc[(int64_t)a * count + p0 + p] : 0.0;
                 }
         }
+        if (MODE == 3) continue;
         // S (orders 8w..8w+7) x (terms) += G_chunk Z_chunk^T. A fragment of k-step (pb, h):
         // lane (g, t) needs G[g][8pb + 4h + t], held by lane (g, 2h + (t >> 1)) as element t & 1.
 #pragma unroll
@@ -161,6 +193,16 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
         }
     }
     cp_async_wait<0>();
+    if (MODE == 3) {
+        double* dp = spart + (int64_t)blockIdx.x * 2 * T;  // [cta][R_0..R_2L, gamma_0..gamma_2L]
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (tid + 256 * h < 2 * T) dp[tid + 256 * h] = dacc[h];
+        lacc += __shfl_xor_sync(0xffffffffu, lacc, 1);
+        lacc += __shfl_xor_sync(0xffffffffu, lacc, 2);
+        if (t == 0) lpart[(int64_t)blockIdx.x * kCbA + a] = lacc;
+        return;
+    }
     if (!kS) return;
     // partials: spart[cta][a][q] (q < tp), lpart[cta][a]
     double* sp = spart + (int64_t)blockIdx.x * kCbA * tp;
@@ -193,9 +235,65 @@ __global__ void combine_reduce_kernel(const double* __restrict__ spart, const do
     }
 }
 
+// MODE 3: rg[0..2T) = sum_cta of (R, gamma) partials, loss as in combine_reduce_kernel.
+__global__ void gram_reduce_kernel(const double* __restrict__ dpart, const double* __restrict__ lpart, int ctas, int T,
+                                   int n_alpha, double norm, double* __restrict__ rg, double* __restrict__ loss) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < 2 * T) {
+        double acc = 0.0;
+        for (int c = 0; c < ctas; ++c) acc += dpart[(int64_t)c * 2 * T + idx];
+        rg[idx] = acc;
+    }
+    if (idx < n_alpha) {
+        double acc = 0.0;
+        for (int c = 0; c < ctas; ++c) acc += lpart[(int64_t)c * kCbA + idx];
+        loss[idx] = acc * norm;
+    }
+}
+
+// s[a][q] = g_scale * (sum_q' c_aq' gamma(|q - q'|) - R_q): one CTA per order.
+__global__ void gram_s_kernel(const double* __restrict__ coef, const double* __restrict__ rg, int T, double g_scale,
+                              double* __restrict__ s) {
+    const int a = blockIdx.x;
+    const double* c = coef + (int64_t)a * T;
+    const double* gam = rg + T;
+    for (int q = threadIdx.x; q < T; q += blockDim.x) {
+        double acc = 0.0;
+        for (int q2 = 0; q2 < T; ++q2) acc = fma(c[q2], gam[q > q2 ? q - q2 : q2 - q], acc);
+        s[(int64_t)a * T + q] = g_scale * (acc - rg[q]);
+    }
+}
+
 int combine_ctas() { return FGFRFT_SMS; }
 
-size_t combine_partial_elems(int tp) { return (size_t)FGFRFT_SMS * kCbA * (tp + 1); }
+// out += sum_ij (G_ij - delta_ij)^2 over an n x n column-major G (orthogonality residual of F).
+__global__ void ortho_residual_kernel(const double* __restrict__ g, int n, double* out) {
+    double acc = 0.0;
+    const int64_t total = (int64_t)n * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % n, j = idx / n;
+        const double v = g[idx] - (i == j ? 1.0 : 0.0);
+        acc = fma(v, v, acc);
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) atomicAdd(out, acc);
+    }
+}
+
+cudaError_t launch_ortho_residual(const double* g, int n, double* out, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), stream);
+    if (e != cudaSuccess) return e;
+    ortho_residual_kernel<<<2 * FGFRFT_SMS, 256, 0, stream>>>(g, n, out);
+    return cudaGetLastError();
+}
+
+size_t combine_partial_elems(int tp) { return (size_t)FGFRFT_SMS * kCbA * (tp + 1) + 4 * (size_t)tp; }
 
 template <int MODE>
 static cudaError_t combine_attr() {
@@ -213,7 +311,7 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
                            double* loss, cudaStream_t stream) {
     const int T = 2 * l + 1, tp = (T + 7) / 8 * 8;
-    if (n_alpha < 1 || n_alpha > kCbA || tp > kCbMaxT || count % 2 || mode < 0 || mode > 2) return cudaErrorInvalidValue;
+    if (n_alpha < 1 || n_alpha > kCbA || tp > kCbMaxT || count % 2 || mode < 0 || mode > 3) return cudaErrorInvalidValue;
     const size_t smem = combine_smem_bytes(tp);
     const int64_t nchunks = (count + kCbP - 1) / kCbP;
     const int ctas = (int)(nchunks < FGFRFT_SMS ? nchunks : FGFRFT_SMS);
@@ -231,6 +329,17 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
             combine_kernel<1><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 0.0, y, spart,
                                                            lpart);
             return cudaGetLastError();
+        case 3: {
+            if ((e = combine_attr<3>()) != cudaSuccess) return e;
+            combine_kernel<3><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 2.0 * norm, y, spart,
+                                                           lpart);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            double* rg = lpart + (size_t)ctas * kCbA;
+            const int threads = 256, blocks = (2 * T + threads - 1) / threads;
+            gram_reduce_kernel<<<blocks, threads, 0, stream>>>(spart, lpart, ctas, T, n_alpha, norm, rg, loss);
+            gram_s_kernel<<<n_alpha, 128, 0, stream>>>(coef, rg, T, 2.0 * norm, s);
+            return cudaGetLastError();
+        }
         default:
             if ((e = combine_attr<2>()) != cudaSuccess) return e;
             combine_kernel<2><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 0.0, y, spart,

@@ -20,7 +20,7 @@
 //     (S x 64 columns <= 512). For a fixed A digit t the B digits u = 1..S+1-t are stacked
 //     along N in shared memory, so ONE tcgen05.mma (N up to 256) covers a contiguous run of
 //     accumulators: 9 MMAs per 32-byte K step for S = 6 (21 digit products);
-//   * a 4-stage ring of 32-byte K blocks; warp 0 / lane 0 issues the bulk copies, warp 1 / lane 0
+//   * a 3-4 stage ring of 64- / 32-byte K blocks; warp 0 / lane 0 issues the bulk copies, warp 1 / lane 0
 //     the MMAs (tcgen05.commit frees a stage), then all 8 warps drain TMEM (tcgen05.ld 32x32b,
 //     lane = output row, 32 columns per warp) and combine the S accumulators in FP64 (Horner
 //     in base 254 over exact int64 folds) into the output.
@@ -32,9 +32,6 @@ namespace fgb {
 
 constexpr int kOzBM = 128;  // rows of the A tile (TMEM lanes)
 constexpr int kOzBN = 64;   // rows of the B tile (N of one digit product)
-constexpr int kOzBK = 32;   // bytes (= int8 elements) of K per stage = one MMA K step
-constexpr int kOzStages = 4;
-constexpr int kOzSbo = kOzBK / 16 * 128;  // bytes between 8-row groups of one slice block
 
 // Digit base 254: with |v| < 1/2, rint(254 v) is in [-127, 127] and the remainder in [-1/2, 1/2],
 // so every digit fits int8 and carries log2(254) = 7.99 bits (base 256 would need 128).
@@ -43,11 +40,16 @@ constexpr long long kOzBaseI = 254;
 constexpr double kOzScale = 4.0 / (254.0 * 254.0 * 254.0 * 254.0);  // 2^2 (two half scalings) x 254^-4
 __host__ __device__ constexpr double oz_pow254(int k) { return k == 0 ? 1.0 : 254.0 * oz_pow254(k - 1); }
 
+// Stage geometry per digit count: 6 digits -> 64-byte K blocks (two MMA K steps, 18 MMAs per
+// stage) in a 3-stage ring; 7-8 digits -> 32-byte K blocks in a 4-stage ring (<= 197 KB smem).
 template <int S> struct OzCfg {
-    static constexpr int a_stage = S * kOzBM * kOzBK;
-    static constexpr int b_stage = S * kOzBN * kOzBK;
+    static constexpr int bk = S <= 6 ? 64 : 32;        // bytes (= int8 elements) of K per stage
+    static constexpr int stages = S <= 6 ? 3 : 4;
+    static constexpr int sbo = bk / 16 * 128;          // bytes between 8-row groups of a slice block
+    static constexpr int a_stage = S * kOzBM * bk;
+    static constexpr int b_stage = S * kOzBN * bk;
     static constexpr int stage = a_stage + b_stage;
-    static constexpr int smem = kOzStages * stage + 1024;  // + barriers / scratch
+    static constexpr int smem = stages * stage + 1024;  // + barriers / scratch
 };
 
 // ---------------------------------------------------------------- tcgen05 helpers
@@ -121,6 +123,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ double pow2(int e) {  // exact 2^e for -1022 <= e <= 1023
@@ -186,10 +196,11 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
     double x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] = t[rl][c * 16 + i] * sc;
-    const int kb_count = v.kp / kOzBK;
+    constexpr int kBK = OzCfg<S>::bk;
+    const int kb_count = v.kp / kBK;
     const int rt = row / tr, rr = row - rt * tr;
-    const int kb = (blockIdx.y * 64 + c * 16) / kOzBK, cl = c & (kOzBK / 16 - 1);
-    int8_t* base = dst + ((int64_t)rt * kb_count + kb) * S * tr * kOzBK + (rr >> 3) * kOzSbo + cl * 128 + r8 * 16;
+    const int kb = (blockIdx.y * 64 + c * 16) / kBK, cl = c & (kBK / 16 - 1);
+    int8_t* base = dst + ((int64_t)rt * kb_count + kb) * S * tr * kBK + (rr >> 3) * OzCfg<S>::sbo + cl * 128 + r8 * 16;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         uint32_t w[4];
@@ -205,7 +216,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
             }
             w[q] = packed;
         }
-        *reinterpret_cast<uint4*>(base + (int64_t)s * tr * kOzBK) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(base + (int64_t)s * tr * kBK) = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -238,6 +249,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
 ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const int8_t* __restrict__ b,
               const int* __restrict__ eb, int kblocks, int mtiles, int ntiles, OzOut out) {
     using Cfg = OzCfg<S>;
+    constexpr int kOzStages = Cfg::stages;
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* sa = smem;
     unsigned char* sb = smem + kOzStages * Cfg::a_stage;
@@ -305,14 +317,17 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sa + s * Cfg::a_stage), b0 = smem_u32(sb + s * Cfg::b_stage);
 #pragma unroll
-                    for (int t = 1; t <= S; ++t) {
-                        const uint64_t ad = umma_desc(a0 + (t - 1) * kOzBM * kOzBK, 128, kOzSbo);
+                    for (int j = 0; j < Cfg::bk / 32; ++j) {
 #pragma unroll
-                        for (int u0 = 1; u0 <= S + 1 - t; u0 += 4) {
-                            const int cnt = (S + 1 - t - u0 + 1) < 4 ? (S + 1 - t - u0 + 1) : 4;
-                            const uint64_t bd = umma_desc(b0 + (u0 - 1) * kOzBN * kOzBK, 128, kOzSbo);
-                            const uint32_t col = tmem + (uint32_t)((t + u0 - 2) * kOzBN);
-                            mma_i8(col, ad, bd, idesc_i8(kOzBM, cnt * kOzBN), (kb > 0 || t > 1) ? 1u : 0u);
+                        for (int t = 1; t <= S; ++t) {
+                            const uint64_t ad = umma_desc(a0 + (t - 1) * kOzBM * Cfg::bk + j * 256, 128, Cfg::sbo);
+#pragma unroll
+                            for (int u0 = 1; u0 <= S + 1 - t; u0 += 4) {
+                                const int cnt = (S + 1 - t - u0 + 1) < 4 ? (S + 1 - t - u0 + 1) : 4;
+                                const uint64_t bd = umma_desc(b0 + (u0 - 1) * kOzBN * Cfg::bk + j * 256, 128, Cfg::sbo);
+                                const uint32_t col = tmem + (uint32_t)((t + u0 - 2) * kOzBN);
+                                mma_i8(col, ad, bd, idesc_i8(kOzBM, cnt * kOzBN), (kb > 0 || j > 0 || t > 1) ? 1u : 0u);
+                            }
                         }
                     }
                     if (CL > 1) mma_commit_mc(empty + s, kMask); else mma_commit(empty + s);
@@ -330,20 +345,28 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
             mbar_wait(tfull, tcount & 1);
             tc_fence_after();
-            // exact integer fold: hi = sum_{d<=4} acc_d 254^(4-d), lo = sum_{d>=5} acc_d 254^(S+1-d)
-            long long hi[32], lo[32];
+            // exact integer fold per column: hi = sum_{d<=4} acc_d 254^(4-d), lo = sum_{d>=5}
+            // acc_d 254^(S+1-d); val = hi + lo 254^-(S-3). Two 16-column halves bound the registers.
+            constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
+            double val[32];
 #pragma unroll
-            for (int d = 2; d <= S + 1; ++d) {
-                int32_t v[32];
-                tmem_ld32(lane_addr + (uint32_t)((d - 2) * kOzBN), v);
-                tmem_wait_ld();
-                if (d <= 4) {
+            for (int hf = 0; hf < 2; ++hf) {
+                long long hi[16], lo[16];
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) hi[q] = (d == 2) ? (long long)v[q] : hi[q] * kOzBaseI + v[q];
-                } else {
+                for (int d = 2; d <= S + 1; ++d) {
+                    int32_t v[16];
+                    tmem_ld16(lane_addr + (uint32_t)((d - 2) * kOzBN + hf * 16), v);
+                    tmem_wait_ld();
+                    if (d <= 4) {
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) lo[q] = (d == 5) ? (long long)v[q] : lo[q] * kOzBaseI + v[q];
+                        for (int q = 0; q < 16; ++q) hi[q] = (d == 2) ? (long long)v[q] : hi[q] * kOzBaseI + v[q];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) lo[q] = (d == 5) ? (long long)v[q] : lo[q] * kOzBaseI + v[q];
+                    }
                 }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) val[hf * 16 + q] = (double)hi[q] + (double)lo[q] * lo_w;
             }
             tc_fence_before();
             __syncwarp();
@@ -353,15 +376,14 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             const int bm = m / out.mp, i = m - bm * out.mp;
             if (i < out.mv) {
                 const double ra = pow2(ea[m]) * kOzScale;
-                const double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold: 254^-(S-3)
                 double* cb = out.c + (int64_t)bm * out.sc;
                 const int* ebt = eb + nt * kOzBN + h * 32;
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {
                     const int n = nt * kOzBN + h * 32 + c;
                     if (n >= out.nv) break;
-                    const double v0 = ((double)hi[c] + (double)lo[c] * lo_w) * ra * pow2(ebt[c]);
-                    const double v1 = ((double)hi[c + 1] + (double)lo[c + 1] * lo_w) * ra * pow2(ebt[c + 1]);
+                    const double v0 = val[c] * ra * pow2(ebt[c]);
+                    const double v1 = val[c + 1] * ra * pow2(ebt[c + 1]);
                     if (CM == 0) {
                         __stcs(cb + i + (int64_t)n * out.ldc, v0);
                         if (n + 1 < out.nv) __stcs(cb + i + (int64_t)(n + 1) * out.ldc, v1);
@@ -437,7 +459,7 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
     }
     const int clusters = units < max_clusters ? units : max_clusters;
     cfg.gridDim = dim3(clusters * CL);
-    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL>, a, ea, b, eb, kp / kOzBK, mtiles, ntiles, out);
+    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL>, a, ea, b, eb, kp / OzCfg<S>::bk, mtiles, ntiles, out);
 }
 
 template <int S, int CM>

@@ -195,6 +195,7 @@ cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void
     if (am == 0 && bm == 1 && cm == 1) FGB_RG(0, 1, 1)  // Y = Q X
     if (am == 1 && bm == 1 && cm == 1) FGB_RG(1, 1, 1)  // Y = Q^T X
     if (am == 2 && bm == 2 && cm == 0) FGB_RG(2, 2, 0)  // M_re = Re(G X^H)
+    if (am == 1 && bm == 0 && cm == 0) FGB_RG(1, 0, 0)  // F^T F (orthogonality check)
 #undef FGB_RG
     return cudaErrorInvalidValue;
 }

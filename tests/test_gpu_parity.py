@@ -352,6 +352,7 @@ def test_power_route_matches_oracle(n, l, b, n_alpha):
     o = O.PowerCache(f, l)
     g = fg.PowerCache(f, l)
     assert g.is_real()
+    assert 0 <= g.orthogonality() <= 1e-12  # graph GFT: the Gram form of the step is used
     g.set_engine(fg.ENGINE_INT8)
     rng = np.random.default_rng(n + b)
     x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
@@ -433,3 +434,26 @@ def test_power_route_apply_and_dlda(n, l, b, n_alpha):
         _, dc = O.sinc_coeffs(a, l)
         assert np.max(np.abs(s[i] - s_ref)) <= 1e-10 * np.max(np.abs(s_ref))
         assert abs(dl[i] - float(np.dot(dc, s_ref))) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+def test_power_route_non_orthogonal_real_f():
+    """A real but non-orthogonal F (0.97 x a graph GFT): the power-product MSE step must not use the
+    Gram identity; s_k = Re<G, F^k X> is contracted directly and matches the oracle."""
+    n, l, b = 128, 16, 9
+    f = 0.97 * prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 5)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    assert g.orthogonality() > 1e-3
+    g.set_engine(fg.ENGINE_INT8)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = 0.9 * x
+    alphas = list(np.linspace(0.1, 1.9, 20))
+    loss, dl, _ = fg.mse_step(g, alphas, x, xc)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
+        assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
