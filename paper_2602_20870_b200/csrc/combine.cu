@@ -217,6 +217,155 @@ combine_kernel(const double* __restrict__ z, const double* __restrict__ x, const
     if (t == 0) lpart[(int64_t)blockIdx.x * kCbA + a] = lacc;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Y-only forms for an orthogonal F (MODE 3) and for apply (MODE 1), two CTAs per SM:
+// the coefficient fragments live in registers (34 per lane), the chunk ring holds 32 positions of
+// every term (2 x 39 KB), and the three Gram/residual rows <X, Z_q>, <Z_-L, Z_q>, <Xc, Z_q> are
+// one extra DMMA GEMV per chunk (rows of the A fragment: X, Z_-L, Xc).
+constexpr int kCyP = 32;    // positions per chunk
+constexpr int kCyLd = 36;   // doubles per staged row (= 4 mod 16)
+
+size_t combine_y_smem_bytes(int tp) { return (2 * (size_t)tp * kCyLd + 2 * kCyP) * sizeof(double); }
+
+template <bool GRAM>
+__global__ void __launch_bounds__(256, 2)
+combine_y_kernel(const double* __restrict__ z, const double* __restrict__ x, const double* __restrict__ xc,
+                 int64_t count, int l, int tp, const double* __restrict__ coef, int n_alpha, double* __restrict__ y,
+                 double* __restrict__ dpart, double* __restrict__ lpart) {
+    extern __shared__ __align__(16) double sm[];
+    double* zb = sm;                       // 2 x [tp][36]
+    double* xb = zb + 2 * tp * kCyLd;      // 2 x [32]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int T = 2 * l + 1;
+    const int a = 8 * warp + g;
+    const bool a_ok = a < n_alpha;
+    const int nks = tp / 4;
+
+    double creg[kCbMaxT / 4];
+#pragma unroll
+    for (int k = 0; k < kCbMaxT / 4; ++k) {
+        const int q = 4 * k + t;
+        creg[k] = (a_ok && q < T) ? coef[(int64_t)a * T + q] : 0.0;
+    }
+    for (int idx = tid; idx < (tp - T) * kCyLd; idx += 256) {
+        zb[T * kCyLd + idx] = 0.0;
+        zb[(tp + T) * kCyLd + idx] = 0.0;
+    }
+
+    const int64_t nchunks = (count + kCyP - 1) / kCyP;
+    auto stage = [&](int64_t ch, int buf) {
+        const int64_t p0 = ch * kCyP;
+        const int pv = (int)((count - p0) < kCyP ? (count - p0) : kCyP);
+        double* zc = zb + buf * tp * kCyLd;
+        for (int idx = tid; idx < T * (kCyP / 2); idx += 256) {
+            const int q = idx / (kCyP / 2), c2 = idx - q * (kCyP / 2);
+            const double* src;
+            if (q == l) src = x;
+            else if (q > l) src = z + (int64_t)(q - l - 1) * count;
+            else src = z + (int64_t)(l + (l - q) - 1) * count;
+            const bool v = 2 * c2 < pv;
+            cp_async16(zc + q * kCyLd + 2 * c2, src + p0 + (v ? 2 * c2 : 0), v);
+        }
+        if (GRAM && tid < kCyP / 2)
+            cp_async16(xb + buf * kCyP + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
+    };
+
+    double lacc = 0.0;
+    double dacc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // q-blocks warp, warp + 8, warp + 16
+    int buf = 0;
+    if (blockIdx.x < nchunks) stage(blockIdx.x, 0);
+    cp_async_commit();
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, buf ^= 1) {
+        const int64_t p0 = ch * kCyP;
+        const int pv = (int)((count - p0) < kCyP ? (count - p0) : kCyP);
+        cp_async_wait<0>();
+        __syncthreads();
+        if (ch + gridDim.x < nchunks) stage(ch + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        const double* zc = zb + buf * tp * kCyLd;
+        const double* xs = xb + buf * kCyP;
+
+        double yacc[4][2];
+#pragma unroll
+        for (int pb = 0; pb < 4; ++pb) yacc[pb][0] = yacc[pb][1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < kCbMaxT / 4; ++k) {
+            if (k < nks) {
+                const double* zrow = zc + (4 * k + t) * kCyLd + g;
+#pragma unroll
+                for (int pb = 0; pb < 4; ++pb) dmma884(yacc[pb][0], yacc[pb][1], creg[k], zrow[8 * pb]);
+            }
+        }
+#pragma unroll
+        for (int pb = 0; pb < 4; ++pb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int p = 8 * pb + 2 * t + e;
+                const bool ok = p < pv && a_ok;
+                if (y && ok) y[(int64_t)a * count + p0 + p] = yacc[pb][e];
+                if (GRAM) {
+                    const double r = ok ? yacc[pb][e] - xs[p] : 0.0;
+                    lacc += r * r;
+                }
+            }
+        if (GRAM) {
+            // rows: g = 0 -> X (term L), g = 1 -> Z_-L (term 0), g = 2 -> Xc, else 0
+#pragma unroll
+            for (int p4 = 0; p4 < kCyP; p4 += 4) {
+                const double av = g == 0 ? zc[l * kCyLd + p4 + t] : g == 1 ? zc[p4 + t] : g == 2 ? xs[p4 + t] : 0.0;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    const int qb = warp + 8 * r;
+                    if (8 * qb < tp) dmma884(dacc[r][0], dacc[r][1], av, zc[(8 * qb + g) * kCyLd + p4 + t]);
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if (!GRAM) return;
+    // partials: dpart[cta][row 0..2][tp], lpart[cta][a]
+    double* dp = dpart + (int64_t)blockIdx.x * 3 * tp;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const int qb = warp + 8 * r;
+        if (8 * qb < tp && g < 3) {
+            dp[g * tp + 8 * qb + 2 * t] = dacc[r][0];
+            dp[g * tp + 8 * qb + 2 * t + 1] = dacc[r][1];
+        }
+    }
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, 1);
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, 2);
+    if (t == 0) lpart[(int64_t)blockIdx.x * kCbA + a] = lacc;
+}
+
+// rg[0..T) = R_q = <Xc, Z_q>, rg[T + d] = gamma(d): <X, Z_d> (row 0, q = L + d) for d <= L,
+// <Z_-L, Z_(d-L)> (row 1, q = d) for d > L. loss as in combine_reduce_kernel.
+__global__ void gram3_reduce_kernel(const double* __restrict__ dpart, const double* __restrict__ lpart, int ctas,
+                                    int tp, int l, int n_alpha, double norm, double* __restrict__ rg,
+                                    double* __restrict__ loss) {
+    const int T = 2 * l + 1;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < 2 * T) {
+        int row, col;
+        if (idx < T) {
+            row = 2;
+            col = idx;
+        } else {
+            const int d = idx - T;
+            row = d <= l ? 0 : 1;
+            col = d <= l ? l + d : d;
+        }
+        double acc = 0.0;
+        for (int c = 0; c < ctas; ++c) acc += dpart[((int64_t)c * 3 + row) * tp + col];
+        rg[idx] = acc;
+    }
+    if (idx < n_alpha) {
+        double acc = 0.0;
+        for (int c = 0; c < ctas; ++c) acc += lpart[(int64_t)c * kCbA + idx];
+        loss[idx] = acc * norm;
+    }
+}
+
 // s[a][q] = sum_cta spart (fixed order), loss[a] = norm * sum_cta lpart
 __global__ void combine_reduce_kernel(const double* __restrict__ spart, const double* __restrict__ lpart, int ctas,
                                       int tp, int T, int n_alpha, double norm, double* __restrict__ s,
@@ -293,7 +442,11 @@ cudaError_t launch_ortho_residual(const double* g, int n, double* out, cudaStrea
     return cudaGetLastError();
 }
 
-size_t combine_partial_elems(int tp) { return (size_t)FGFRFT_SMS * kCbA * (tp + 1) + 4 * (size_t)tp; }
+size_t combine_partial_elems(int tp) {
+    const size_t a = (size_t)FGFRFT_SMS * kCbA * (tp + 1) + 4 * (size_t)tp;
+    const size_t b = (size_t)2 * FGFRFT_SMS * (3 * tp + kCbA) + 4 * (size_t)tp;
+    return a > b ? a : b;
+}
 
 template <int MODE>
 static cudaError_t combine_attr() {
@@ -325,18 +478,32 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
                                                            lpart);
             break;
         case 1:
-            if ((e = combine_attr<1>()) != cudaSuccess) return e;
-            combine_kernel<1><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 0.0, y, spart,
-                                                           lpart);
-            return cudaGetLastError();
         case 3: {
-            if ((e = combine_attr<3>()) != cudaSuccess) return e;
-            combine_kernel<3><<<ctas, 256, smem, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, 2.0 * norm, y, spart,
-                                                           lpart);
+            const size_t ysm = combine_y_smem_bytes(tp);
+            static bool yattr = false;
+            if (!yattr) {
+                if ((e = cudaFuncSetAttribute(combine_y_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)combine_y_smem_bytes(kCbMaxT))) != cudaSuccess)
+                    return e;
+                if ((e = cudaFuncSetAttribute(combine_y_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)combine_y_smem_bytes(kCbMaxT))) != cudaSuccess)
+                    return e;
+                yattr = true;
+            }
+            const int64_t ych = (count + kCyP - 1) / kCyP;
+            const int yctas = (int)(ych < 2 * FGFRFT_SMS ? ych : 2 * FGFRFT_SMS);
+            if (mode == 1) {
+                combine_y_kernel<false><<<yctas, 256, ysm, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, y, nullptr,
+                                                                    nullptr);
+                return cudaGetLastError();
+            }
+            double* dpart = partial;                                 // [yctas][3][tp]
+            double* lp = partial + (size_t)yctas * 3 * tp;           // [yctas][64]
+            double* rg = lp + (size_t)yctas * kCbA;                  // [2T]
+            combine_y_kernel<true><<<yctas, 256, ysm, stream>>>(z, x, xc, count, l, tp, coef, n_alpha, y, dpart, lp);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
-            double* rg = lpart + (size_t)ctas * kCbA;
             const int threads = 256, blocks = (2 * T + threads - 1) / threads;
-            gram_reduce_kernel<<<blocks, threads, 0, stream>>>(spart, lpart, ctas, T, n_alpha, norm, rg, loss);
+            gram3_reduce_kernel<<<blocks, threads, 0, stream>>>(dpart, lp, yctas, tp, l, n_alpha, norm, rg, loss);
             gram_s_kernel<<<n_alpha, 128, 0, stream>>>(coef, rg, T, 2.0 * norm, s);
             return cudaGetLastError();
         }
