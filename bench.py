@@ -409,7 +409,8 @@ def main():
     e1.record(stream)
     e1.synchronize()
     t_wall = (time.perf_counter() - t_wall) / args.steps
-    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, t_wall * 1e3))
+    e2e_dev_ms = e0.elapsed_time(e1) / args.steps
+    e2e_ms = max_over_ranks(max(e2e_dev_ms, t_wall * 1e3))
     e2e_value = n * b * A * ws / (e2e_ms * 1e-3)
 
     cpu = None
@@ -443,6 +444,7 @@ def main():
                             "note": "host wall clock incl. H2D of F and allocation",
                             "int8_slices_seconds": slices_s},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                    "device_ms": e2e_dev_ms, "wall_ms": t_wall * 1e3,
                     "h2d_bytes_per_step": 2 * n * b * 16, "d2h_bytes_per_step": 2 * A * 8},
             "gpu_launches": launches,
             "clocks": clk,

@@ -245,6 +245,11 @@ struct fgfrft_cache {
     int64_t r0 = 0, r1 = 0;
     void* colp = nullptr;
     size_t panel_elems = 0;
+    // Host-buffer MSE step: Xc is uploaded on a side stream while the power products run; the
+    // step waits on xc_evt right before its first use of Xc.
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t xc_evt = nullptr;
+    bool xc_pending = false;
     double* coef_h = nullptr;  // pinned staging for the coefficient tables
     size_t coef_h_cap = 0;
     cudaEvent_t coef_evt = nullptr;
@@ -308,6 +313,9 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
         FGB_CUDA(cudaMallocHost(&c->coef_h, count * sizeof(double)));
         c->coef_h_cap = count;
     }
+    // 2 (2L+1) libm evaluations per order: spread an order sweep over the host cores
+    const int nthr = std::min(8, std::max(1, n_alpha / 8));
+#pragma omp parallel for schedule(static) num_threads(nthr) if (nthr > 1)
     for (int a = 0; a < n_alpha; ++a)
         host_sinc_coeffs(alphas[a], l, c->coef_h + a * width, c->coef_h + ((size_t)n_alpha + a) * width);
     FGB_CUDA(c->coef.ensure(count * sizeof(double)));
@@ -430,11 +438,15 @@ void destroy_cache(fgfrft_cache* c) {
     DeviceGuard dg(c->device);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
+    if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
-                      &c->loss, &c->dlda, &c->tmp})
+                      &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
+                      &c->qex})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
+    if (c->xc_evt) cudaEventDestroy(c->xc_evt);
+    if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
     if (c->slabs) cudaFree(c->slabs);
     if (c->colp) cudaFree(c->colp);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -698,6 +710,13 @@ int power_products(fgfrft_cache* c, const void* x_dev, int64_t b) {
     return FGFRFT_OK;
 }
 
+int wait_xc(fgfrft_cache* c) {
+    if (!c->xc_pending) return FGFRFT_OK;
+    c->xc_pending = false;
+    FGB_CUDA(cudaStreamWaitEvent(c->stream, c->xc_evt, 0));
+    return FGFRFT_OK;
+}
+
 bool gram_route(const fgfrft_cache* c) {
     static const bool off = std::getenv("FGFRFT_NO_GRAM") != nullptr;
     return c->orthogonal && !off;
@@ -712,6 +731,7 @@ int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void
     const int64_t count = 2 * c->n * b;
     const double norm = 1.0 / ((double)c->n * (double)b);
     FGB_CUDA(c->partial.ensure(combine_partial_elems(combine_max_terms()) * sizeof(double)));
+    if (int st = wait_xc(c)) return st;
     for (int a0 = 0; a0 < n_alpha; a0 += 64) {
         const int na = std::min(64, n_alpha - a0);
         ProfScope ps(KC_COMBINE, c->stream);
@@ -1290,6 +1310,7 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
                                 na),
                            1);
         }
+        if (int st = wait_xc(c)) return st;
         {
             ProfScope ps(KC_ELEMWISE, c->stream);
             FGB_LAUNCH(launch_mse_residual(ya, xc_dev, (int64_t)blk, na, 2.0 * norm, norm, c->g.p,
@@ -1322,7 +1343,18 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
         FGB_CUDA(c->loss.ensure((size_t)n_alpha * 2 * sizeof(double)));
         if (y) FGB_CUDA(c->y.ensure(xe * c->sig * n_alpha));
         if (int st = upload_signal(c, x, xe, c->x.p)) return st;
-        if (int st = upload_signal(c, xc, xe, c->xc.p)) return st;
+        if (c->dtype == FGFRFT_C128) {
+            if (!c->aux_stream) FGB_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+            if (!c->xc_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->xc_evt, cudaEventDisableTiming));
+            // the side stream must not overwrite Xc while a previous step may still read it
+            FGB_CUDA(cudaEventRecord(c->xc_evt, c->stream));
+            FGB_CUDA(cudaStreamWaitEvent(c->aux_stream, c->xc_evt, 0));
+            FGB_CUDA(cudaMemcpyAsync(c->xc.p, xc, xe * 16, cudaMemcpyHostToDevice, c->aux_stream));
+            FGB_CUDA(cudaEventRecord(c->xc_evt, c->aux_stream));
+            c->xc_pending = true;
+        } else if (int st = upload_signal(c, xc, xe, c->xc.p)) {
+            return st;
+        }
     }
     double* ld = c->loss.as<double>();
     if (int st = fgfrft_mse_step_dev(c, alphas, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha))

@@ -33,11 +33,21 @@ double host_sinc_deriv(double x) {
     return std::cos(px) / x - std::sin(px) / (M_PI * x * x);
 }
 
+// Both tables at once: the generic branch of sinc and sinc' shares one sin(pi x) and one
+// cos(pi x) evaluation per term (the same libm calls on the same argument as host_sinc /
+// host_sinc_deriv, so the values are bit-identical to evaluating them separately).
 void host_sinc_coeffs(double alpha, int l, double* c, double* dc) {
     for (int n = -l; n <= l; ++n) {
         const double x = alpha - static_cast<double>(n);
-        if (c) c[n + l] = host_sinc(x);
-        if (dc) dc[n + l] = host_sinc_deriv(x);
+        if (x == std::nearbyint(x) || std::fabs(x) < 1e-6) {
+            if (c) c[n + l] = host_sinc(x);
+            if (dc) dc[n + l] = host_sinc_deriv(x);
+            continue;
+        }
+        const double px = M_PI * x;
+        const double sn = std::sin(px);
+        if (c) c[n + l] = sn / (M_PI * x);
+        if (dc) dc[n + l] = std::cos(px) / x - sn / (M_PI * x * x);
     }
 }
 
