@@ -58,7 +58,14 @@ typedef enum fgfrft_which { FGFRFT_Q = 0, FGFRFT_DQ = 1 } fgfrft_which;
  * (tcgen05 kind::i8; ~3e-13 relative, see fgfrft_dgemm_int8_dev). AUTO (default, or the
  * FGFRFT_ENGINE=dmma|int8 environment variable): INT8 power products when 2 n_alpha >= L.
  */
-typedef enum fgfrft_engine { FGFRFT_ENGINE_AUTO = 0, FGFRFT_ENGINE_DMMA = 1, FGFRFT_ENGINE_INT8 = 2 } fgfrft_engine;
+typedef enum fgfrft_engine {
+    FGFRFT_ENGINE_AUTO = 0,
+    FGFRFT_ENGINE_DMMA = 1,
+    FGFRFT_ENGINE_INT8 = 2,
+    /* INT8, and for an orthogonal F with 32 <= L <= 64 also the per-order combination Y = C Z on
+     * the INT8 tensor cores (Z written as digits by the power-product GEMM). Experimental. */
+    FGFRFT_ENGINE_INT8_COMBINE = 3
+} fgfrft_engine;
 
 /* Default budget of transform.hpp:17 (4 GiB). */
 #define FGFRFT_DEFAULT_MEMORY_BUDGET (4ULL << 30)

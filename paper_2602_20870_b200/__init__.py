@@ -144,7 +144,7 @@ def launch_count() -> int:
     return int(lib().fgfrft_launch_count())
 
 
-ENGINE_AUTO, ENGINE_DMMA, ENGINE_INT8 = 0, 1, 2
+ENGINE_AUTO, ENGINE_DMMA, ENGINE_INT8, ENGINE_INT8_COMBINE = 0, 1, 2, 3
 
 KERNEL_CLASSES = ("synthesis", "dmma_zgemm", "power_dots", "elementwise", "int8_gemm", "slicing", "combine",
                   "reserved")

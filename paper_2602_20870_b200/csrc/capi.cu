@@ -52,6 +52,7 @@ cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void
                          cudaStream_t stream);
 cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t stream);
 cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream);
+cudaError_t launch_rfrom_tiled_real(const void* src, void* dst, int n, cudaStream_t stream);
 cudaError_t launch_real_part(const void* src, void* dst, int64_t count, cudaStream_t stream);
 cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
                           bool out_complex, cudaStream_t stream);
@@ -88,6 +89,14 @@ cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int 
                             cudaStream_t stream);
 int combine_max_terms();
 cudaError_t launch_ortho_residual(const double* g, int n, double* out, cudaStream_t stream);
+cudaError_t launch_colstats(const double* x, const double* xc, int n, int b, double* colsq, double* colxc, int* ecol,
+                            double* rg, int l, cudaStream_t st);
+cudaError_t launch_gram_s_dlda(const double* coef, const double* dcoef, const double* rg, int n_alpha, int l,
+                               double norm, double* s, double* dlda, cudaStream_t st);
+cudaError_t launch_gram_terms(const double* part, int ctas, int tp2, int l, double* rg, cudaStream_t st);
+cudaError_t launch_loss3(const double* part, int ctas, int n_alpha, double norm, double* loss, cudaStream_t st);
+cudaError_t launch_gram_s(const double* coef, const double* rg, int n_alpha, int l, double norm, double* s,
+                          cudaStream_t st);
 size_t combine_partial_elems(int tp);
 cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
@@ -239,6 +248,10 @@ struct fgfrft_cache {
     int ps_slices = 0;
     DevBuf ps, pe, prm, xsl, xex, z;
     DevBuf qsl, qex;  // per-call INT8 slices of Q(a) (or G) for the synthesis route
+    // Orthogonal-F sweep with the combination on the INT8 tensor cores: the stacked cache sliced
+    // in (signal row, term) interleaved order, P_L in column-major form, and per-call buffers.
+    int ps3_slices = 0;
+    DevBuf ps3, pe3, plr, zd, zaux, cdig, cex;
     // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
     bool shard = false;
     int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
@@ -441,7 +454,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
-                      &c->qex})
+                      &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -587,6 +600,7 @@ int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host
 
 // INT8 tensor-core (Ozaki) versions of the real-F synthesis route's two GEMMs (defined below).
 bool use_int8_gemm(const fgfrft_cache* c);
+int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out);
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
 bool use_power_route(const fgfrft_cache* c, int n_alpha);
@@ -655,7 +669,7 @@ bool use_power_route(const fgfrft_cache* c, int n_alpha) {
     if (!c->real || c->dtype != FGFRFT_C128 || 2 * c->l + 1 > combine_max_terms() || c->n > 16384) return false;
     const int eng = engine_of(c);
     if (eng == FGFRFT_ENGINE_DMMA) return false;
-    if (eng == FGFRFT_ENGINE_INT8) return true;
+    if (eng == FGFRFT_ENGINE_INT8 || eng == FGFRFT_ENGINE_INT8_COMBINE) return true;
     return 2 * n_alpha >= c->l;  // auto: 2L products amortised over the orders
 }
 
@@ -720,6 +734,136 @@ int wait_xc(fgfrft_cache* c) {
 bool gram_route(const fgfrft_cache* c) {
     static const bool off = std::getenv("FGFRFT_NO_GRAM") != nullptr;
     return c->orthogonal && !off;
+}
+
+// ---- INT8 combination (orthogonal F, 32 <= L <= 64): Z = F^k X never exists in FP64. The
+// Z GEMM epilogue writes base-254 digits of Z (2^e_j > |x_j| >= |Z_k[i, j]|) straight into the
+// A-operand layout of the combine GEMM Y = C Z, and accumulates <X, Z_k>, <Xc, Z_k>, <Z_L, Z_k>
+// for the Gram form of s_k; the combine GEMM adds c_0 X, stores Y if asked and sums the loss.
+int tp2_of(const fgfrft_cache* c) { return 2 * c->l <= 64 ? 64 : 128; }
+
+// Opt-in (FGFRFT_ENGINE_INT8_COMBINE): measured on B200 it does not beat the DMMA combination at
+// K = 2L = 128 -- the digit fold of the Ozaki epilogue (~60 instructions per output) outweighs
+// the 2L-deep int8 products; it pays off only for much longer series.
+bool use_int8_combine(const fgfrft_cache* c) {
+    return engine_of(c) == FGFRFT_ENGINE_INT8_COMBINE && gram_route(c) && c->l >= 32 && c->l <= 64 &&
+           c->n % 64 == 0;
+}
+
+int ensure_power_slices3(fgfrft_cache* c) {
+    const int S = oz_slices_default();
+    if (c->ps3_slices == S) return FGFRFT_OK;
+    const int64_t n = c->n, kp = pad_k(n), tp2 = tp2_of(c);
+    const int64_t rows = ceil_div(n * tp2, kOzTileA) * kOzTileA;
+    FGB_CUDA(c->ps3.ensure((size_t)S * rows * kp));
+    FGB_CUDA(c->pe3.ensure((size_t)rows * sizeof(int)));
+    FGB_CUDA(c->prm.ensure((size_t)std::max<int64_t>(rows, 2 * c->l * pad_rows(n)) * sizeof(unsigned long long)));
+    OzView v{static_cast<const double*>(c->slabs), 0, 0, (int64_t)c->slab_elems(), 0, 0, (int)n, (int)rows, 1,
+             (int)n, (int)kp, false};
+    v.tiled = 3;
+    v.nt = (int)ceil_div(n, kTile);
+    v.l = c->l;
+    v.tp2 = (int)tp2;
+    {
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->ps3.as<int8_t>(), c->pe3.as<int>(),
+                                   c->prm.as<unsigned long long>(), c->stream),
+                   3);
+    }
+    c->ps3_slices = S;
+    return FGFRFT_OK;
+}
+
+int mse_int8_combine(fgfrft_cache* c, const double* coef, const double* dcoef, int n_alpha, const void* x_dev,
+                     const void* xc_dev, int64_t b, void* y_dev, double* loss_dev, double* s_dev, double* dlda_dev) {
+    if (int st = ensure_power_slices3(c)) return st;
+    const int S = c->ps3_slices, l = c->l, T = 2 * l + 1;
+    const int64_t n = c->n, kp = pad_k(n), tp2 = tp2_of(c);
+    const int64_t rows = ceil_div(n * tp2, kOzTileA) * kOzTileA;
+    const int64_t count = 2 * n * b, count_pad = ceil_div(count, kOzTileA) * kOzTileA;
+    const double norm = 1.0 / ((double)n * (double)b);
+    const double* x = static_cast<const double*>(x_dev);
+    const double* xc = static_cast<const double*>(xc_dev);
+    // aux layout: colsq[b] colxc[b] | rg[2T] | gpart[148*4*128*3] | lpart[148*4*4*16] | ecol[b]
+    const size_t n_dbl = 2 * (size_t)b + 2 * (size_t)T + (size_t)FGFRFT_SMS * 4 * 128 * 3 +
+                         (size_t)FGFRFT_SMS * 4 * 4 * 16;
+    FGB_CUDA(c->zaux.ensure(n_dbl * sizeof(double) + (size_t)b * sizeof(int)));
+    double* colsq = c->zaux.as<double>();
+    double* colxc = colsq + b;
+    double* rg = colxc + b;
+    double* gpart = rg + 2 * T;
+    double* lpart = gpart + (size_t)FGFRFT_SMS * 4 * 128 * 3;
+    int* ecol = reinterpret_cast<int*>(lpart + (size_t)FGFRFT_SMS * 4 * 4 * 16);
+    const int SZ = oz_zdigits();  // Z digits (bounded by column norms: one digit more than the cache)
+    FGB_CUDA(c->zd.ensure((size_t)SZ * count_pad * tp2));
+    // B operand of the Z GEMM (X digits) -- before waiting for Xc
+    int64_t bp = 0;
+    if (int st = slice_signal_rows(c, x_dev, b, &bp)) return st;
+    if (int st = wait_xc(c)) return st;
+    {
+        ProfScope ps(KC_ELEMWISE, c->stream);
+        FGB_LAUNCH(launch_colstats(x, xc, (int)n, (int)b, colsq, colxc, ecol, rg, l, c->stream), 2);
+    }
+    {
+        OzOut o;
+        o.nv = (int)(2 * b);
+        o.x = x;
+        o.xc = xc;
+        o.l = l;
+        o.epos = ecol;
+        o.zd = c->zd.as<int8_t>();
+        o.part = gpart;
+        o.n = (int)n;
+        o.tp2 = (int)tp2;
+        o.kbz = (int)(tp2 / oz_bk(SZ));
+        ProfScope ps(KC_I8GEMM, c->stream);
+        FGB_CUDA(cudaMemsetAsync(gpart, 0, (size_t)FGFRFT_SMS * 4 * 128 * 3 * sizeof(double), c->stream));
+        FGB_LAUNCH(launch_ozgemm_ex(S, 2, c->ps3.as<int8_t>(), c->pe3.as<int>(), (int)rows, c->xsl.as<int8_t>(),
+                                    c->xex.as<int>(), (int)bp, (int)kp, o, c->stream),
+                   1);
+    }
+    {
+        ProfScope ps(KC_COMBINE, c->stream);
+        FGB_LAUNCH(launch_gram_terms(gpart, FGFRFT_SMS, (int)tp2, l, rg, c->stream), 1);
+    }
+    FGB_CUDA(c->cdig.ensure((size_t)SZ * 64 * tp2));
+    FGB_CUDA(c->cex.ensure(64 * (sizeof(int) + sizeof(unsigned long long))));
+    const size_t width = (size_t)T;
+    for (int a0 = 0; a0 < n_alpha; a0 += 64) {
+        const int na = std::min(64, n_alpha - a0);
+        const double* cf = coef + (size_t)a0 * width;
+        int* ce = c->cex.as<int>();
+        {
+            OzView v{cf, (int64_t)T, 1, 0, 0, 0, na, 64, 1, (int)tp2, (int)tp2, false};
+            v.tiled = 4;
+            v.l = l;
+            ProfScope ps(KC_SLICE, c->stream);
+            FGB_LAUNCH(launch_oz_slice(v, SZ, kOzTileB, c->cdig.as<int8_t>(), ce,
+                                       reinterpret_cast<unsigned long long*>(ce + 64), c->stream),
+                       3);
+        }
+        OzOut o;
+        o.c = y_dev ? static_cast<double*>(y_dev) + (size_t)a0 * count : nullptr;
+        o.nv = na;
+        o.x = x;
+        o.xc = xc;
+        o.part = lpart;
+        o.c0 = cf + l;
+        o.c0s = T;
+        o.count = count;
+        o.n = (int)n;
+        o.epos = ecol;
+        ProfScope ps(KC_COMBINE, c->stream);
+        FGB_CUDA(cudaMemsetAsync(lpart, 0, (size_t)FGFRFT_SMS * 4 * 4 * 16 * sizeof(double), c->stream));
+        FGB_LAUNCH(launch_ozgemm_ex(SZ, 3, c->zd.as<int8_t>(), nullptr, (int)count_pad, c->cdig.as<int8_t>(), ce, 64,
+                                    (int)tp2, o, c->stream),
+                   1);
+        FGB_LAUNCH(launch_loss3(lpart, FGFRFT_SMS, na, norm, loss_dev + a0, c->stream), 1);
+        FGB_LAUNCH(launch_gram_s_dlda(cf, dcoef + (size_t)a0 * width, rg, na, l, norm, s_dev + (size_t)a0 * width,
+                                      dlda_dev + a0, c->stream),
+                   1);
+    }
+    return FGFRFT_OK;
 }
 
 // MSE step over the power products: loss, s (2L+1 per order) and optionally Y.
@@ -1055,7 +1199,8 @@ int fgfrft_cache_set_stream(fgfrft_cache* c, void* stream) {
 
 int fgfrft_cache_set_engine(fgfrft_cache* c, int engine) {
     if (int st = check_handle(c)) return st;
-    if (engine < FGFRFT_ENGINE_AUTO || engine > FGFRFT_ENGINE_INT8) return fail(FGFRFT_PARAMETER, "unknown engine");
+    if (engine < FGFRFT_ENGINE_AUTO || engine > FGFRFT_ENGINE_INT8_COMBINE)
+        return fail(FGFRFT_PARAMETER, "unknown engine");
     std::lock_guard<std::mutex> lk(c->mu);
     c->engine = engine;
     return FGFRFT_OK;
@@ -1073,8 +1218,11 @@ int fgfrft_cache_prepare(fgfrft_cache* c) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
     if (c->real && c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA &&
-        2 * c->l + 1 <= combine_max_terms())
+        2 * c->l + 1 <= combine_max_terms()) {
         if (int st = ensure_power_slices(c)) return st;
+        if (use_int8_combine(c))
+            if (int st = ensure_power_slices3(c)) return st;
+    }
     FGB_CUDA(cudaStreamSynchronize(c->stream));
     return FGFRFT_OK;
     FGB_GUARD_END
@@ -1275,6 +1423,11 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
     const double* dc_dev = coef + (size_t)n_alpha * width;
+    if (use_power_route(c, n_alpha) && use_int8_combine(c)) {
+        FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
+        return mse_int8_combine(c, coef, dc_dev, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
+                                c->s.as<double>(), static_cast<double*>(dlda_dev));
+    }
     if (use_power_route(c, n_alpha)) {
         FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
         if (int st = mse_power_route(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),

@@ -522,3 +522,173 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
 }
 
 }  // namespace fgb
+
+namespace fgb {
+
+// ---------------------------------------------------------------------------------------------
+// Orthogonal-F sweep with the combination on the INT8 tensor cores (see capi.cu power route):
+// per signal column j: colsq = |x_j|^2, colxc = Re<xc_j, x_j>; one CTA per column.
+__global__ void __launch_bounds__(256) colstats_kernel(const double* __restrict__ x, const double* __restrict__ xc,
+                                                       int n, double* __restrict__ colsq, double* __restrict__ colxc) {
+    const int j = blockIdx.x;
+    const double* xj = x + (int64_t)j * 2 * n;
+    const double* cj = xc + (int64_t)j * 2 * n;
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < 2 * n; i += 256) {
+        a = fma(xj[i], xj[i], a);
+        b = fma(xj[i], cj[i], b);
+    }
+    __shared__ double ra[8], rb[8];
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        ra[threadIdx.x >> 5] = a;
+        rb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sa = 0.0, sb = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            sa += ra[w];
+            sb += rb[w];
+        }
+        colsq[j] = sa;
+        colxc[j] = sb;
+    }
+}
+
+// e_j: 2^e_j > |x_j| (1 + 2^-20) >= every |(F^k X)[i, j]| for orthogonal F (the combine GEMM
+// reads the row exponent of position p as e_(p / 2n)); rg[T + 0] = gamma(0) = |X|^2 and
+// rg[L] = R_0 = <Xc, X> (fixed-order sums).
+__global__ void expo_kernel(const double* __restrict__ colsq, const double* __restrict__ colxc, int b,
+                            int* __restrict__ ecol, double* __restrict__ rg, int l) {
+    for (int j = threadIdx.x; j < b; j += blockDim.x) {
+        int e = 0;
+        const double nrm = sqrt(colsq[j]) * (1.0 + 0x1p-20);
+        if (nrm > 0.0) frexp(nrm, &e);
+        ecol[j] = e;
+    }
+    if (threadIdx.x == 0) {
+        double g0 = 0.0, r0 = 0.0;
+        for (int j = 0; j < b; ++j) {
+            g0 += colsq[j];
+            r0 += colxc[j];
+        }
+        const int T = 2 * l + 1;
+        rg[T] = g0;
+        rg[l] = r0;
+    }
+}
+
+// dlda[a] = sum_q dc[a][q] s[a][q] with s from the Gram form (gram_s_kernel fused): one CTA per order.
+__global__ void gram_s_dlda_kernel(const double* __restrict__ coef, const double* __restrict__ dcoef,
+                                   const double* __restrict__ rg, int T, double g_scale, double* __restrict__ s,
+                                   double* __restrict__ dlda) {
+    const int a = blockIdx.x;
+    const double* c = coef + (int64_t)a * T;
+    const double* gam = rg + T;
+    __shared__ double sv[272];
+    for (int q = threadIdx.x; q < T; q += blockDim.x) {
+        double acc = 0.0;
+        for (int q2 = 0; q2 < T; ++q2) acc = fma(c[q2], gam[q > q2 ? q - q2 : q2 - q], acc);
+        const double v = g_scale * (acc - rg[q]);
+        sv[q] = v;
+        if (s) s[(int64_t)a * T + q] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // ascending q, as coef_dot_kernel
+        const double* dc = dcoef + (int64_t)a * T;
+        double acc = 0.0;
+        for (int q = 0; q < T; ++q) acc += dc[q] * sv[q];
+        dlda[a] = acc;
+    }
+}
+
+// Gram partials [cta][4][128][3] (thread row lrow -> term kk = lrow % tp2) -> rg:
+//   R_q (q = k + L): k > 0 -> <Xc, Z_k> = part1[kk = k - 1]; k < 0 -> part1[kk = L - k - 1]
+//   gamma(d): 1 <= d <= L -> <X, Z_d> = part0[kk = d - 1]; L < d <= 2L -> <Z_-L, Z_(d-L)> =
+//   part2[kk = d - L - 1] (F^T F = I: <F^-L X, F^k X> = <X, F^(k+L) X>)
+__device__ __forceinline__ double block_sum128(double v, double* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    const double s = red[0] + red[1] + red[2] + red[3];  // fixed order
+    __syncthreads();
+    return s;
+}
+
+// one CTA (128 threads) per term kk; entries (cta, h, r = kk + m tp2) strided over the threads
+__global__ void __launch_bounds__(128) gram_terms_kernel(const double* __restrict__ part, int ctas, int tp2, int l,
+                                                         double* __restrict__ rg) {
+    const int kk = blockIdx.x;
+    const int per = 128 / tp2, entries = ctas * 4 * per;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int e = threadIdx.x; e < entries; e += 128) {
+        const int c = e / (4 * per), rem = e - c * 4 * per, h = rem / per, m = rem - h * per;
+        const double* p = part + (((int64_t)c * 4 + h) * 128 + kk + m * tp2) * 3;
+        s0 += p[0];
+        s1 += p[1];
+        s2 += p[2];
+    }
+    __shared__ double red[4];
+    s0 = block_sum128(s0, red);
+    s1 = block_sum128(s1, red);
+    s2 = block_sum128(s2, red);
+    if (threadIdx.x != 0) return;
+    const int T = 2 * l + 1;
+    const int k = kk < l ? kk + 1 : -(kk - l + 1);
+    rg[l + k] = s1;                       // R_(L+k)
+    if (k > 0) {
+        rg[T + k] = s0;                   // gamma(k), k = 1..L
+        rg[T + l + k] = s2;               // gamma(L + k) = <Z_-L, Z_k>
+    }
+}
+
+// loss[a] = norm * sum over [cta][4][4][16] partials (order a = q * 16 + c)
+__global__ void __launch_bounds__(128) loss3_kernel(const double* __restrict__ part, int ctas, int n_alpha,
+                                                    double norm, double* __restrict__ loss) {
+    const int a = blockIdx.x;
+    const int h = a >> 4, c = a & 15;
+    double acc = 0.0;
+    for (int e = threadIdx.x; e < ctas * 4; e += 128) {
+        const int t = e >> 2, lg = e & 3;
+        acc += part[(((int64_t)t * 4 + h) * 4 + lg) * 16 + c];
+    }
+    __shared__ double red[4];
+    acc = block_sum128(acc, red);
+    if (threadIdx.x == 0) loss[a] = acc * norm;
+}
+
+cudaError_t launch_colstats(const double* x, const double* xc, int n, int b, double* colsq, double* colxc, int* ecol,
+                            double* rg, int l, cudaStream_t st) {
+    colstats_kernel<<<b, 256, 0, st>>>(x, xc, n, colsq, colxc);
+    expo_kernel<<<1, 256, 0, st>>>(colsq, colxc, b, ecol, rg, l);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_s_dlda(const double* coef, const double* dcoef, const double* rg, int n_alpha, int l,
+                               double norm, double* s, double* dlda, cudaStream_t st) {
+    if (2 * l + 1 > 272) return cudaErrorInvalidValue;
+    gram_s_dlda_kernel<<<n_alpha, 128, 0, st>>>(coef, dcoef, rg, 2 * l + 1, 2.0 * norm, s, dlda);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_terms(const double* part, int ctas, int tp2, int l, double* rg, cudaStream_t st) {
+    gram_terms_kernel<<<2 * l, 128, 0, st>>>(part, ctas, tp2, l, rg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss3(const double* part, int ctas, int n_alpha, double norm, double* loss, cudaStream_t st) {
+    loss3_kernel<<<n_alpha, 128, 0, st>>>(part, ctas, n_alpha, norm, loss);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram_s(const double* coef, const double* rg, int n_alpha, int l, double norm, double* s,
+                          cudaStream_t st) {
+    gram_s_kernel<<<n_alpha, 128, 0, st>>>(coef, rg, 2 * l + 1, 2.0 * norm, s);
+    return cudaGetLastError();
+}
+
+}  // namespace fgb

@@ -18,10 +18,39 @@ struct OzView {
     int kv, kp;      // valid K, padded K (multiple of kOzBK)
     bool rfast;      // rows are the contiguous direction of the source
     int tiled = 0;   // 1: src is a tiled cache slab (common.cuh), element (r, k) = P(r, k);
-                     // 2: the same slab read transposed, element (r, k) = P(k, r)
+                     // 2: the same slab read transposed, element (r, k) = P(k, r);
+                     // 3: interleaved stacked cache, row r = i * tp2 + kk: term kk < L is
+                     //    P_(kk+1)(i, k), L <= kk < 2L is P_(kk-L+1)(k, i), else 0;
+                     // 4: coefficient table (rows = orders, row stride rs = 2L+1) in term order kk
     int nt = 0;      // tiles per side of a tiled slab
+    int l = 0, tp2 = 0;  // modes 3 / 4: L and the padded term count (64 or 128)
 };
 
+
+// Output addressing: row m -> (batch block bm = m / mp, i = m % mp), valid when i < mv, n < nv.
+//   CM 0: C[bm * sC + i + n * ldc]                       (real, column-major)
+//   CM 1: C[bm * sC + (i + (n >> 1) * ldc) * 2 + (n & 1)]  (complex merge of column pairs)
+//   CM 2: power products of the orthogonal-F sweep -> base-254 digits of Z for the combine GEMM
+//         plus Gram partials (rows m = i * tp2 + kk: signal row i, term kk; columns 2j + comp)
+//   CM 3: the combine GEMM Y = C Z (rows = flat positions p, columns = orders) + c_0 X, the
+//         optional store of Y and the per-order MSE loss partials.
+struct OzOut {
+    double* c;
+    int64_t ldc, sc;
+    int mv, mp, nv;
+    // CM 2 / CM 3 extras
+    const double* x = nullptr;   // X, flat 2 n b doubles
+    const double* xc = nullptr;  // clean signals (CM 3) / Xc (CM 2 Gram partials)
+    const double* zl = nullptr;  // unused (kept for layout stability)
+    const int* epos = nullptr;   // CM 2: exponent per signal column j: |Z_k[i, j]| < 2^e
+    int8_t* zd = nullptr;        // CM 2: digits, A operand layout of the combine GEMM
+    double* part = nullptr;      // CM 2: [cta][2][128][3] Gram partials; CM 3: [cta][2][4][32] loss
+    const double* c0 = nullptr;  // CM 3: c_0 of order a at c0[a * c0s]
+    int64_t c0s = 1;
+    int64_t count = 0;           // 2 n b
+    int n = 0, tp2 = 0, kbz = 0; // signal length, padded terms (64 | 128), K blocks of the combine
+    int l = 0;                   // CM 2: L (row kk = 2L-1 holds Z_-L)
+};
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)
 constexpr int kOzTileB = 64;   // B operand row tile (output columns per CTA)
@@ -34,6 +63,10 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
                             cudaStream_t stream);
 // C = A B^T over sliced operands; cm 0: C[bm*sc + i + n*ldc], cm 1: complex merge of column
 // pairs C[bm*sc + (i + (n>>1)*ldc)*2 + (n&1)], with m = bm * mp + i (i < mv), n < nv.
+cudaError_t launch_ozgemm_ex(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
+                             const int* eb, int nrows, int kp, const OzOut& out, cudaStream_t stream);
+int oz_bk(int slices);  // bytes of K per stage / per digit block of the sliced layout
+int oz_zdigits();       // digits of Z written by the CM 2 epilogue (the combine GEMM's digit count)
 cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                           const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
                           cudaStream_t stream);

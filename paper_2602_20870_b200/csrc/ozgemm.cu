@@ -37,19 +37,21 @@ constexpr int kOzBN = 64;   // rows of the B tile (N of one digit product)
 // so every digit fits int8 and carries log2(254) = 7.99 bits (base 256 would need 128).
 constexpr double kOzBase = 254.0;
 constexpr long long kOzBaseI = 254;
+constexpr double kOzMagic = 6755399441055744.0;  // 1.5 * 2^52: x + magic rounds x (|x| < 2^51) to an integer
+constexpr int kOzZDigits = 7;  // digits of Z written by the CM 2 epilogue (bounded by column norms: +1 digit)
 constexpr double kOzScale = 4.0 / (254.0 * 254.0 * 254.0 * 254.0);  // 2^2 (two half scalings) x 254^-4
 __host__ __device__ constexpr double oz_pow254(int k) { return k == 0 ? 1.0 : 254.0 * oz_pow254(k - 1); }
 
 // Stage geometry per digit count: 6 digits -> 64-byte K blocks (two MMA K steps, 18 MMAs per
-// stage) in a 3-stage ring; 7-8 digits -> 32-byte K blocks in a 4-stage ring (<= 197 KB smem).
+// stage) in a 3-stage ring; 7-8 digits -> 32-byte K blocks in a 5- / 4-stage ring (<= 219 KB smem).
 template <int S> struct OzCfg {
     static constexpr int bk = S <= 6 ? 64 : 32;        // bytes (= int8 elements) of K per stage
-    static constexpr int stages = S <= 6 ? 3 : 4;
+    static constexpr int stages = S <= 6 ? 3 : (S == 7 ? 5 : 4);
     static constexpr int sbo = bk / 16 * 128;          // bytes between 8-row groups of a slice block
     static constexpr int a_stage = S * kOzBM * bk;
     static constexpr int b_stage = S * kOzBN * bk;
     static constexpr int stage = a_stage + b_stage;
-    static constexpr int smem = stages * stage + 1024;  // + barriers / scratch
+    static constexpr int smem = stages * stage + 1024 + 2048;  // + barriers / scratch + CM 2 exchange
 };
 
 // ---------------------------------------------------------------- tcgen05 helpers
@@ -123,6 +125,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -140,8 +147,22 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e for -1022 <= e <= 
 // ---------------------------------------------------------------- operand views and slicing (OzView: oz.cuh)
 
 __device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
+    if (v.tiled == 3) {  // rv = n (signal rows), rows beyond n * tp2 are padding
+        const int i = row / v.tp2, kk = row - i * v.tp2;
+        if (i >= v.rv || kk >= 2 * v.l || k >= v.kv) return 0.0;
+        const bool tr = kk >= v.l;
+        const int slab = tr ? kk - v.l : kk;
+        const int a = tr ? k : i, b = tr ? i : k;
+        return v.src[slab * v.sbatch + tile_base(a >> 5, b >> 5, v.nt) + swz(a & 31, b & 31)];
+    }
     const int bt = row / v.rp, r = row - bt * v.rp;
     if (r >= v.rv || k >= v.kv) return 0.0;
+    if (v.tiled == 4) {
+        const int kk = k;
+        if (kk >= 2 * v.l) return 0.0;
+        const int q = kk < v.l ? v.l + 1 + kk : 2 * v.l - 1 - kk;
+        return v.src[(int64_t)r * v.rs + q];
+    }
     if (v.tiled) {
         const int i = v.tiled == 1 ? r : k, j = v.tiled == 1 ? k : r;
         return v.src[bt * v.sbatch + tile_base(i >> 5, j >> 5, v.nt) + swz(i & 31, j & 31)];
@@ -210,9 +231,9 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const double y = x[q * 4 + i] * kOzBase;  // |y| <= 127
-                const double d = rint(y);
-                x[q * 4 + i] = y - d;                     // exact, |.| <= 1/2
-                packed |= ((uint32_t)(int32_t)d & 0xFFu) << (8 * i);
+                const double t = y + kOzMagic;            // rint(y) in the low word
+                x[q * 4 + i] = y - (t - kOzMagic);        // exact, |.| <= 1/2
+                packed |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * i);
             }
             w[q] = packed;
         }
@@ -222,16 +243,11 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
 
 // ---------------------------------------------------------------- the GEMM
 
-// Output addressing: row m -> (batch block bm = m / mp, i = m % mp), valid when i < mv, n < nv.
-//   CM 0: C[bm * sC + i + n * ldc]                       (real, column-major)
-//   CM 1: C[bm * sC + (i + (n >> 1) * ldc) * 2 + (n & 1)]  (complex merge of column pairs)
-struct OzOut {
-    double* c;
-    int64_t ldc, sc;
-    int mv, mp, nv;
-};
 
-constexpr int kOzEpiWarps = 8;                        // 4 TMEM lane groups x 2 column halves
+
+constexpr int kOzEpiWarps = 16;                       // 4 TMEM lane groups x 4 column quarters
+constexpr int kOzEpiQ = kOzEpiWarps / 4;              // column groups
+constexpr int kOzEC = kOzBN / kOzEpiQ;                // columns per epilogue thread (16)
 constexpr int kOzThreads = 32 * (2 + kOzEpiWarps);    // producer warp, MMA warp, epilogue warps
 
 // Persistent, clusters of CL CTAs along N (CL = 2 by default): cluster c owns work units u = c, c + clusters, ...
@@ -258,6 +274,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     uint64_t* tfull = empty + kOzStages;
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    double* xchg = reinterpret_cast<double*>(smem + kOzStages * Cfg::stage + 1024);  // CM 2: 2 x [2][64]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = CL > 1 ? (int)cluster_rank() : 0;
@@ -336,51 +353,133 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             }
         }
     } else {
-        // epilogue warps 2..9: lane group (warp % 4) = TMEM lanes / output rows, column half
+        // epilogue warps 2..17: lane group (warp % 4) = TMEM lanes / output rows, column quarter
         const int ew = warp - 2, lg = warp & 3, h = ew >> 2;
         const int lrow = lg * 32 + lane;
-        const uint32_t lane_addr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * 32);
+        const uint32_t lane_addr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * kOzEC);
         int tcount = 0;
+        double gacc[3] = {0.0, 0.0, 0.0};  // CM 2: <X, Z_kk>, <Xc, Z_kk>, <Z_L, Z_kk> over this thread's tiles
+        double lacc[kOzEC];                // CM 3: sum (Y - Xc)^2 per order column
+        if (CM == 3) {
+#pragma unroll
+            for (int c = 0; c < kOzEC; ++c) lacc[c] = 0.0;
+        }
         for (int u = cid; u < units; u += nclusters, ++tcount) {
             const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
             mbar_wait(tfull, tcount & 1);
             tc_fence_after();
             // exact integer fold per column: hi = sum_{d<=4} acc_d 254^(4-d), lo = sum_{d>=5}
-            // acc_d 254^(S+1-d); val = hi + lo 254^-(S-3). Two 16-column halves bound the registers.
+            // acc_d 254^(S+1-d); val = hi + lo 254^-(S-3). TMEM is drained 8 columns at a time, all S
+            // accumulators in flight per wait.
             constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
-            double val[32];
+            double val[kOzEC];
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                long long hi[16], lo[16];
+            for (int g8 = 0; g8 < kOzEC / 8; ++g8) {
+                // all S accumulators of 8 columns in flight, one wait
+                int32_t v[S][8];
 #pragma unroll
-                for (int d = 2; d <= S + 1; ++d) {
-                    int32_t v[16];
-                    tmem_ld16(lane_addr + (uint32_t)((d - 2) * kOzBN + hf * 16), v);
-                    tmem_wait_ld();
-                    if (d <= 4) {
+                for (int d = 0; d < S; ++d) tmem_ld8(lane_addr + (uint32_t)(d * kOzBN + g8 * 8), v[d]);
+                tmem_wait_ld();
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) hi[q] = (d == 2) ? (long long)v[q] : hi[q] * kOzBaseI + v[q];
-                    } else {
+                for (int q = 0; q < 8; ++q) {
+                    long long hi = v[0][q], lo = v[3][q];
+                    hi = hi * kOzBaseI + v[1][q];
+                    hi = hi * kOzBaseI + v[2][q];
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) lo[q] = (d == 5) ? (long long)v[q] : lo[q] * kOzBaseI + v[q];
-                    }
+                    for (int d = 4; d < S; ++d) lo = lo * kOzBaseI + v[d][q];
+                    val[g8 * 8 + q] = (double)hi + (double)lo * lo_w;
                 }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) val[hf * 16 + q] = (double)hi[q] + (double)lo[q] * lo_w;
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
             // value = (hi + lo 254^-(S-3)) * 4 * 254^-4 * 2^e_r * 2^e_n
             const int m = mt * kOzBM + lrow;
+            if (CM == 2) {
+                // Z_kk[i, col] for this thread's 32 columns: Gram partials + base-254 digits. The row
+                // kk = 2L-1 (Z_-L) of each signal row i in the tile is published through shared
+                // memory for the <Z_-L, Z_k> partials (one named barrier of the 8 epilogue warps).
+                const int i = m / out.tp2, kk = m - i * out.tp2, il = lrow / out.tp2;
+                const bool row_ok = i < out.n;
+                const double ra = pow2(ea[m]) * kOzScale;
+                const int* ebt = eb + nt * kOzBN + h * kOzEC;
+                double* xs = xchg + (tcount & 1) * 128 + il * 64 + h * kOzEC;
+#pragma unroll
+                for (int c = 0; c < kOzEC; ++c) {
+                    const int col = nt * kOzBN + h * kOzEC + c;
+                    val[c] = (row_ok && col < out.nv) ? val[c] * ra * pow2(ebt[c]) : 0.0;
+                    if (kk == 2 * out.l - 1) xs[c] = val[c];
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kOzEpiWarps) : "memory");
+                if (row_ok) {
+                    // n % 64 == 0: position p = 2i + comp + 2n j has the same (p & 127) for every j,
+                    // so the digit address of column pair j is base(comp) + j * jstride.
+                    using YC = OzCfg<kOzZDigits>;
+                    constexpr int kDig = kOzBM * YC::bk;  // bytes between the digit planes of a block
+                    const int rr0 = (2 * i) & 127, pt0 = (2 * i) >> 7;
+                    const int64_t jstride = (int64_t)(2 * out.n / 128) * out.kbz * kOzZDigits * kDig;
+                    const int64_t kofs = (int64_t)(kk / YC::bk) * kOzZDigits * kDig + ((kk % YC::bk) >> 4) * 128 + (kk & 15);
+                    int8_t* base0 = out.zd + (int64_t)pt0 * out.kbz * kOzZDigits * kDig + kofs +
+                                    (rr0 >> 3) * YC::sbo + (rr0 & 7) * 16;
+                    int8_t* base1 = out.zd + (int64_t)pt0 * out.kbz * kOzZDigits * kDig + kofs +
+                                    ((rr0 + 1) >> 3) * YC::sbo + ((rr0 + 1) & 7) * 16;
+                    const int j0 = (nt * kOzBN + h * kOzEC) >> 1;
+#pragma unroll
+                    for (int c2 = 0; c2 < kOzEC / 2; ++c2) {
+                        const int j = j0 + c2;
+                        if (2 * j >= out.nv) continue;
+                        const int64_t p = ((int64_t)i + (int64_t)j * out.n) * 2;
+                        const double2 xv = *reinterpret_cast<const double2*>(out.x + p);
+                        const double2 cv = *reinterpret_cast<const double2*>(out.xc + p);
+                        const double v0 = val[2 * c2], v1 = val[2 * c2 + 1];
+                        gacc[0] = fma(xv.x, v0, fma(xv.y, v1, gacc[0]));
+                        gacc[1] = fma(cv.x, v0, fma(cv.y, v1, gacc[1]));
+                        gacc[2] = fma(xs[2 * c2], v0, fma(xs[2 * c2 + 1], v1, gacc[2]));
+                        const double sc = pow2(-out.epos[j] - 1);
+                        double r0 = v0 * sc, r1 = v1 * sc;  // |r| < 1/2
+                        int8_t* d0 = base0 + j * jstride;
+                        int8_t* d1 = base1 + j * jstride;
+#pragma unroll
+                        for (int t = 0; t < kOzZDigits; ++t) {
+                            const double y0 = r0 * kOzBase, y1 = r1 * kOzBase;
+                            const double t0 = y0 + kOzMagic, t1 = y1 + kOzMagic;  // rint in the low word
+                            r0 = y0 - (t0 - kOzMagic);
+                            r1 = y1 - (t1 - kOzMagic);
+                            d0[t * kDig] = (int8_t)__double2loint(t0);
+                            d1[t * kDig] = (int8_t)__double2loint(t1);
+                        }
+                    }
+                }
+                continue;
+            }
+            if (CM == 3) {
+                // Y_a[p] = (C Z)[p, a] + c_0(a) X[p]; loss partial per order
+                const int64_t p = m;
+                if (p < out.count) {
+                    const double ra = pow2(out.epos[m / (2 * out.n)]) * kOzScale;
+                    const int* ebt = eb + nt * kOzBN + h * kOzEC;
+                    const double xp = out.x[p], xcp = out.xc[p];
+#pragma unroll
+                    for (int c = 0; c < kOzEC; ++c) {
+                        const int a = nt * kOzBN + h * kOzEC + c;
+                        if (a < out.nv) {
+                            const double yv = fma(out.c0[(int64_t)a * out.c0s], xp, val[c] * ra * pow2(ebt[c]));
+                            if (out.c) __stcs(out.c + (int64_t)a * out.count + p, yv);
+                            const double r = yv - xcp;
+                            lacc[c] = fma(r, r, lacc[c]);
+                        }
+                    }
+                }
+                continue;
+            }
             const int bm = m / out.mp, i = m - bm * out.mp;
             if (i < out.mv) {
                 const double ra = pow2(ea[m]) * kOzScale;
                 double* cb = out.c + (int64_t)bm * out.sc;
-                const int* ebt = eb + nt * kOzBN + h * 32;
+                const int* ebt = eb + nt * kOzBN + h * kOzEC;
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                    const int n = nt * kOzBN + h * 32 + c;
+                for (int c = 0; c < kOzEC; c += 2) {
+                    const int n = nt * kOzBN + h * kOzEC + c;
                     if (n >= out.nv) break;
                     const double v0 = val[c] * ra * pow2(ebt[c]);
                     const double v1 = val[c + 1] * ra * pow2(ebt[c + 1]);
@@ -393,6 +492,26 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                 }
             }
         }
+        if (CM == 2) {
+            double* gp = out.part + (((int64_t)blockIdx.x * kOzEpiQ + h) * kOzBM + lrow) * 3;
+            gp[0] = gacc[0];
+            gp[1] = gacc[1];
+            gp[2] = gacc[2];
+        }
+        if (CM == 3) {
+#pragma unroll
+            for (int c = 0; c < kOzEC; ++c) {
+                double v = lacc[c];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                lacc[c] = v;
+            }
+            if (lane == 0) {
+                double* lp = out.part + (((int64_t)blockIdx.x * kOzEpiQ + h) * 4 + lg) * kOzEC;
+#pragma unroll
+                for (int c = 0; c < kOzEC; ++c) lp[c] = lacc[c];
+            }
+        }
     }
     tc_fence_before();
     if (CL > 1) cluster_sync_all(); else __syncthreads();
@@ -402,6 +521,10 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 // ---------------------------------------------------------------- host launchers
 
 int oz_slices_default() { return 6; }
+
+int oz_zdigits() { return kOzZDigits; }
+
+int oz_bk(int slices) { return slices <= 6 ? OzCfg<6>::bk : OzCfg<7>::bk; }
 
 size_t oz_operand_bytes(int slices, int64_t rows_padded, int64_t kp) { return (size_t)slices * rows_padded * kp; }
 
@@ -483,21 +606,39 @@ static cudaError_t oz_launch(const int8_t* a, const int* ea, int mrows, const in
 }
 
 // C (from OzOut) = A_sliced (mrows x kp) * B_sliced (nrows x kp)^T; mrows % 128 == 0, nrows % 64 == 0.
-cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
-                          const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
-                          cudaStream_t stream) {
-    if (mrows % kOzBM || nrows % kOzBN || kp % 64 || mp <= 0) return cudaErrorInvalidValue;
-    const OzOut out{c, ldc, sc, mv, mp, nv};
-#define FGB_OZ(S_)                                                                     \
-    if (slices == S_) {                                                                \
-        if (cm == 0) return oz_launch<S_, 0>(a, ea, mrows, b, eb, nrows, kp, out, stream); \
-        return oz_launch<S_, 1>(a, ea, mrows, b, eb, nrows, kp, out, stream);              \
+cudaError_t launch_ozgemm_ex(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
+                             const int* eb, int nrows, int kp, const OzOut& out, cudaStream_t stream) {
+    if (mrows % kOzBM || nrows % kOzBN || kp % 64) return cudaErrorInvalidValue;
+    if (cm <= 1 && out.mp <= 0) return cudaErrorInvalidValue;
+#define FGB_OZ(S_)                                                                       \
+    if (slices == S_) {                                                                  \
+        switch (cm) {                                                                    \
+            case 0: return oz_launch<S_, 0>(a, ea, mrows, b, eb, nrows, kp, out, stream); \
+            case 1: return oz_launch<S_, 1>(a, ea, mrows, b, eb, nrows, kp, out, stream); \
+            case 2: return oz_launch<S_, 2>(a, ea, mrows, b, eb, nrows, kp, out, stream); \
+            case 3: return oz_launch<S_, 3>(a, ea, mrows, b, eb, nrows, kp, out, stream); \
+            default: return cudaErrorInvalidValue;                                       \
+        }                                                                                \
     }
     FGB_OZ(6)
     FGB_OZ(7)
     FGB_OZ(8)
 #undef FGB_OZ
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
+                          const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
+                          cudaStream_t stream) {
+    if (cm > 1) return cudaErrorInvalidValue;
+    OzOut out;
+    out.c = c;
+    out.ldc = ldc;
+    out.sc = sc;
+    out.mv = mv;
+    out.mp = mp;
+    out.nv = nv;
+    return launch_ozgemm_ex(slices, cm, a, ea, mrows, b, eb, nrows, kp, out, stream);
 }
 
 }  // namespace fgb

@@ -247,6 +247,26 @@ cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t str
     rto_tiled_kernel<<<nt * nt, 256, 0, stream>>>((const double*)src, (double*)dst, n, nt);
     return cudaGetLastError();
 }
+// Same, real column-major output (8-byte elements).
+__global__ void __launch_bounds__(256) rfrom_tiled_real_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                               int n, int nt) {
+    const int I = blockIdx.x % nt, J = blockIdx.x / nt;
+    const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const double* t = src + tile_base(I, J, nt);
+    const int row = I * kTile + r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = w + 8 * i, col = J * kTile + c;
+        if (row < n && col < n) dst[(int64_t)col * n + row] = t[swz(r, c)];
+    }
+}
+
+cudaError_t launch_rfrom_tiled_real(const void* src, void* dst, int n, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    rfrom_tiled_real_kernel<<<nt * nt, 256, 0, stream>>>((const double*)src, (double*)dst, n, nt);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream) {
     const int nt = (int)ceil_div(n, kTile);
     rfrom_tiled_kernel<<<nt * nt, 256, 0, stream>>>((const double*)src, (double2*)dst, n, nt);

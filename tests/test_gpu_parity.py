@@ -457,3 +457,28 @@ def test_power_route_non_orthogonal_real_f():
         _, dc = O.sinc_coeffs(a, l)
         s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
         assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+@pytest.mark.parametrize("n,l,b,n_alpha", [(256, 32, 17, 40), (128, 64, 6, 64)])
+def test_int8_combine_engine(n, l, b, n_alpha):
+    """Experimental engine: the per-order combination Y = C Z also on the INT8 tensor cores (Z as
+    base-254 digits bounded by the column norms of X), Gram form of s_k. Within 1e-10 of the
+    oracle and of the DMMA engine."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 31 + n)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    g.set_engine(fg.ENGINE_INT8_COMBINE)
+    rng = np.random.default_rng(n * b)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    alphas = list(np.linspace(-0.4, 1.8, n_alpha))
+    loss, dl, y = fg.mse_step(g, alphas, x, xc, want_y=True)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        yr = q @ x
+        assert rel(y[i], yr) <= 1e-11
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (yr - xc) / (n * b)) @ x.conj().T)
+        assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
