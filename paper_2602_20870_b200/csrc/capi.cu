@@ -495,9 +495,36 @@ int build_powers(fgfrft_cache* c, const double* f) {
         FGB_LAUNCH(launch_rto_tiled(fr, c->slab(1), n, c->stream), 1);
         double* prev = reinterpret_cast<double*>(c->tmp.p);  // the complex staging is free now: reuse
         if (int st = check_orthogonal(c, fr, prev)) return st;
+        // Small n: one n^3 GEMM per power leaves most SMs idle (n = 1024: 64 CTA tiles), so build by
+        // doubling, P_(s+j) = P_j P_s for j = 1..s: log2(L) levels of batched GEMMs over all
+        // powers, same (L-1) products. The reference left-multiplies (transform.hpp:58); the
+        // results agree to rounding (and the recursion depth drops from L-1 to log2 L).
+        static const bool chain_only = std::getenv("FGFRFT_BUILD_CHAIN") != nullptr;
+        if (!chain_only && n <= 2048 && c->l >= 4) {
+            DevBuf rect;  // all L powers column-major (L n^2 doubles; <= 2 GB at n = 2048, L = 64)
+            FGB_CUDA(rect.ensure(ml * 8 * (size_t)c->l));
+            double* R = rect.as<double>();
+            FGB_CUDA(cudaMemcpyAsync(R, fr, ml * 8, cudaMemcpyDeviceToDevice, c->stream));
+            for (int s = 1; s < c->l; s *= 2) {
+                const int cnt = std::min(s, c->l - s);
+                ProfScope ps(KC_GEMM, c->stream);
+                FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, R, n, (int64_t)ml, R + (size_t)(s - 1) * ml, n, 0,
+                                        R + (size_t)s * ml, n, (int64_t)ml, cnt, c->stream),
+                           1);
+            }
+            for (int k = 2; k <= c->l; ++k)
+                FGB_LAUNCH(launch_rto_tiled(R + (size_t)(k - 1) * ml, c->slab(k), n, c->stream), 1);
+            FGB_CUDA(cudaStreamSynchronize(c->stream));
+            rect.release();
+            c->tmp.release();
+            return FGFRFT_OK;
+        }
         const double* p = fr;
         for (int k = 2; k <= c->l; ++k) {
-            FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, fr, n, 0, p, n, 0, cur, n, 0, 1, c->stream), 1);
+            {
+                ProfScope ps(KC_GEMM, c->stream);
+                FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, fr, n, 0, p, n, 0, cur, n, 0, 1, c->stream), 1);
+            }
             FGB_LAUNCH(launch_rto_tiled(cur, c->slab(k), n, c->stream), 1);
             p = cur;
             std::swap(prev, cur);
