@@ -53,6 +53,10 @@ cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void
 cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t stream);
 cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream);
 cudaError_t launch_rfrom_tiled_real(const void* src, void* dst, int n, cudaStream_t stream);
+size_t rapply_fused_part_elems(int n, int n_alpha);
+int rapply_fused_max_cols();
+cudaError_t launch_rapply_fused(const void* slabs, int n, int l_used, const double* coef_dev, int coef_ld, int n_alpha,
+                                const double* x, int b, double* part, double* y, cudaStream_t stream);
 cudaError_t launch_real_part(const void* src, void* dst, int64_t count, cudaStream_t stream);
 cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
                           bool out_complex, cudaStream_t stream);
@@ -626,11 +630,13 @@ int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host
 }
 
 // INT8 tensor-core (Ozaki) versions of the real-F synthesis route's two GEMMs (defined below).
-bool use_int8_gemm(const fgfrft_cache* c);
+bool use_int8_gemm(const fgfrft_cache* c, int64_t b);
+bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b);
 int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out);
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
 bool use_power_route(const fgfrft_cache* c, int n_alpha);
+int engine_of(const fgfrft_cache* c);
 int apply_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, int64_t b, void* y_dev);
 
 // Y[a] = op(Q(alpha_a)) X for all orders; x_dev n x b, y_dev n_alpha blocks of n x b.
@@ -648,13 +654,28 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
     if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
     const int n = (int)c->n;
     const size_t sl = c->mat_elems();
+    if (use_fused_apply(c, n_alpha, b)) {
+        // small batch: fused synthesis + product, Q never materialised (K3)
+        FGB_CUDA(c->partial.ensure(rapply_fused_part_elems(n, n_alpha) * sizeof(double)));
+        const size_t width = (size_t)(2 * l_used + 1);
+        std::vector<double> al(alphas, alphas + n_alpha);
+        if (inverse) {  // Q(a)^T = Q(-a) bit-exactly
+            for (double& v : al) v = -v;
+            if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
+        }
+        ProfScope ps(KC_SYNTH, c->stream);
+        FGB_LAUNCH(launch_rapply_fused(c->slabs, n, l_used, coef, (int)width, n_alpha, static_cast<const double*>(x_dev),
+                                       (int)b, c->partial.as<double>(), static_cast<double*>(y_dev), c->stream),
+                   2);
+        return FGFRFT_OK;
+    }
     const int chunk = alpha_chunk(c, n_alpha);
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
     const size_t width = (size_t)(2 * l_used + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         if (int st = synth_into(c, coef + a0 * width, na, l_used, c->q.p, true)) return st;
-        if (use_int8_gemm(c)) {
+        if (use_int8_gemm(c, b)) {
             if (int st = int8_qx(c, na, inverse, c->q.p, x_dev, b,
                                  static_cast<char*>(y_dev) + (size_t)a0 * n * b * c->sig))
                 return st;
@@ -915,9 +936,20 @@ int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void
     return FGFRFT_OK;
 }
 
-bool use_int8_gemm(const fgfrft_cache* c) {
-    return c->real && c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA && c->n <= 16384 &&
-           !c->shard && c->graphs == 0;
+// INT8 engine for the synthesis route's GEMMs: forced, or (auto) when the products are large
+// enough to amortise the per-call digit slicing of Q / G and X.
+bool use_int8_gemm(const fgfrft_cache* c, int64_t b) {
+    if (!c->real || c->dtype != FGFRFT_C128 || c->n > 16384 || c->shard || c->graphs > 0) return false;
+    const int eng = engine_of(c);
+    if (eng == FGFRFT_ENGINE_DMMA) return false;
+    if (eng != FGFRFT_ENGINE_AUTO) return true;
+    return c->n >= 512 && 2 * b >= 64;
+}
+
+// Small signal batches on a real cache: the fused synthesis + product kernel (Q never in HBM).
+bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b) {
+    return c->real && c->dtype == FGFRFT_C128 && 2 * b <= rapply_fused_max_cols() && c->n <= 2048 &&
+           n_alpha <= 4 && engine_of(c) == FGFRFT_ENGINE_AUTO && !c->shard && c->graphs == 0;
 }
 
 // Slice the signal block X (n x b complex) as the B operand: rows 2j + comp, K = signal index.
@@ -1045,7 +1077,7 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         // M_a = G_a X^H  (n x n, K = b); real cache: only M_re = Re(G X^H) is needed
-        if (use_int8_gemm(c)) {
+        if (use_int8_gemm(c, b)) {
             if (int st = int8_gx(c, na, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, x_dev, b,
                                  c->m.p))
                 return st;
@@ -1476,8 +1508,16 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         void* ya = y_dev ? static_cast<char*>(y_dev) + (size_t)a0 * blk * c->sig : c->y.p;
-        if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p, true)) return st;
-        if (use_int8_gemm(c)) {
+        if (use_fused_apply(c, na, b)) {
+            FGB_CUDA(c->partial.ensure(rapply_fused_part_elems(n, na) * sizeof(double)));
+            ProfScope ps(KC_SYNTH, c->stream);
+            FGB_LAUNCH(launch_rapply_fused(c->slabs, n, l, coef + a0 * width, (int)width, na,
+                                           static_cast<const double*>(x_dev), (int)b, c->partial.as<double>(),
+                                           static_cast<double*>(ya), c->stream),
+                       2);
+        } else if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p, true)) {
+            return st;
+        } else if (use_int8_gemm(c, b)) {
             if (int st = int8_qx(c, na, false, c->q.p, x_dev, b, ya)) return st;
         } else {
             ProfScope ps(KC_GEMM, c->stream);

@@ -289,7 +289,7 @@ cudaError_t launch_real_to_complex(const void* src, void* dst, int64_t count, cu
 // =====================================================================================
 constexpr int kRsStages = 6;
 
-size_t rsynth_smem_bytes(int l_used, int ac) {
+__host__ __device__ size_t rsynth_smem_bytes(int l_used, int ac) {
     return (size_t)kRsStages * 2 * kTileElems * 8 + kRsStages * 8 + (size_t)l_used * ac * 16 + (size_t)ac * 8 + 16;
 }
 
@@ -428,6 +428,157 @@ cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* co
         if (ac == 4) FGB_RS(4, false) else if (ac == 2) FGB_RS(2, false) else FGB_RS(1, false)
     }
 #undef FGB_RS
+    return cudaGetLastError();
+}
+
+// =====================================================================================
+// Fused apply for small signal batches (north-star K3): Y = Q(alpha) X without Q ever reaching
+// HBM. One CTA per (tile pair {(I,J),(J,I)}, order): the cache tiles stream through the same TMA
+// ring as rsynth_pairs_kernel and are scaled and accumulated in registers (identical, exactly
+// rounded pair updates), the two Q tiles go to shared memory and are multiplied straight away by
+// the staged 32-row blocks of X:  part[pair][0] = Q[I,J] X[J],  part[pair][1] = Q[J,I] X[I].
+// rapply_reduce_kernel then sums, per 32-row block, its nt contributions in a fixed order
+// (deterministic). 2B <= 64 real columns (B <= 32 complex signals).
+// =====================================================================================
+constexpr int kRfCols = 64;  // max real columns (2B)
+
+size_t rapply_fused_smem_bytes(int l_used) {
+    return rsynth_smem_bytes(l_used, 1) + (size_t)(2 * kTileElems + 2 * kTile * kRfCols) * 8;
+}
+
+__global__ void __launch_bounds__(256, 1)
+rapply_fused_kernel(const double* __restrict__ slabs, int n, int l_used, int64_t slab_elems,
+                    const double* __restrict__ coef, int coef_ld, const double* __restrict__ x, int b,
+                    double* __restrict__ part, int nt, int npairs) {
+    constexpr int S = kRsStages;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* tiles = reinterpret_cast<double*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 8);
+    double2* cs = reinterpret_cast<double2*>(full + S);
+    double* c0s = reinterpret_cast<double*>(cs + (size_t)l_used);
+    double* qt = reinterpret_cast<double*>(smem + rsynth_smem_bytes(l_used, 1));  // Q[I,J], Q[J,I] (swizzled)
+    double* xs = qt + 2 * kTileElems;                                               // X[J rows], X[I rows]
+    const int pair = blockIdx.x, a = blockIdx.y;
+    int I, J;
+    pair_of(pair, I, J);
+    const bool diag = (I == J);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lc = l_used, cols = 2 * b;
+    for (int idx = tid; idx < l_used; idx += 256)
+        cs[idx] = make_double2(coef[(size_t)a * coef_ld + lc + idx + 1], coef[(size_t)a * coef_ld + lc - idx - 1]);
+    if (tid == 0) {
+        c0s[0] = coef[(size_t)a * coef_ld + lc];
+        for (int s2 = 0; s2 < S; ++s2) mbar_init(&full[s2], 1);
+        fence_mbar_init();
+    }
+    // stage X rows of blocks J and I: xs[blk][row][col], col = 2j + comp
+    for (int idx = tid; idx < 2 * kTile * cols; idx += 256) {
+        const int blk = idx / (kTile * cols), rem = idx - blk * kTile * cols;
+        const int col = rem % cols, row = rem / cols;
+        const int gi = (blk == 0 ? J : I) * kTile + row;
+        xs[(blk * kTile + row) * kRfCols + col] = gi < n ? x[((int64_t)gi + (int64_t)(col >> 1) * n) * 2 + (col & 1)] : 0.0;
+    }
+    __syncthreads();
+    const uint32_t tb = kTileElems * 8;
+    const int64_t off1 = tile_base(I, J, nt), off2 = tile_base(J, I, nt);
+    auto issue = [&](int k, int s2) {
+        mbar_arrive_expect_tx(&full[s2], (diag ? 1 : 2) * tb);
+        const double* slab = slabs + (int64_t)(k - 1) * slab_elems;
+        double* t1 = tiles + (size_t)(s2 * 2) * kTileElems;
+        bulk_g2s(t1, slab + off1, tb, &full[s2]);
+        if (!diag) bulk_g2s(t1 + kTileElems, slab + off2, tb, &full[s2]);
+    };
+    if (tid == 0)
+        for (int s2 = 0; s2 < S && s2 < l_used; ++s2) issue(s2 + 1, s2);
+    const int r = lane;
+    double q1[4], q2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        q1[i] = (diag && r == warp + 8 * i) ? c0s[0] : 0.0;
+        q2[i] = 0.0;
+    }
+    for (int k = 1; k <= l_used; ++k) {
+        const int s2 = (k - 1) % S;
+        mbar_wait(&full[s2], ((k - 1) / S) & 1);
+        const double* t1 = tiles + (size_t)(s2 * 2) * kTileElems;
+        const double* t2 = diag ? t1 : t1 + kTileElems;
+        const double2 ab = cs[k - 1];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = warp + 8 * i;
+            const double p1 = t1[swz(r, c)], p2 = t2[swz(c, r)];
+            q1[i] = __dadd_rn(q1[i], __dadd_rn(__dmul_rn(ab.x, p1), __dmul_rn(ab.y, p2)));
+            if (!diag) q2[i] = __dadd_rn(q2[i], __dadd_rn(__dmul_rn(ab.x, p2), __dmul_rn(ab.y, p1)));
+        }
+        __syncthreads();
+        if (tid == 0 && k + S <= l_used) issue(k + S, s2);
+    }
+    // q1[i] = Q[I*32 + r, J*32 + c], q2[i] = Q[J*32 + c, I*32 + r] (c = warp + 8 i)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = warp + 8 * i;
+        qt[swz(r, c)] = q1[i];                     // tile 0: (row r, col c) of Q[I,J]
+        qt[kTileElems + swz(c, r)] = q2[i];        // tile 1: (row c, col r) of Q[J,I]
+    }
+    __syncthreads();
+    // part[pair][0][row][col] = sum_c Q[I,J](row, c) X[J*32 + c, col]; [1] = Q[J,I] X[I]
+    double* out = part + (int64_t)(a * npairs + pair) * 2 * kTile * kRfCols;
+    const int nprod = diag ? 1 : 2;
+    for (int idx = tid; idx < nprod * kTile * cols; idx += 256) {
+        const int pr = idx / (kTile * cols), rem = idx - pr * kTile * cols;
+        const int row = rem / cols, col = rem - row * cols;
+        const double* q = qt + pr * kTileElems;
+        const double* xb = xs + (pr == 0 ? 0 : kTile) * kRfCols + col;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < kTile; ++c) acc = fma(q[swz(row, c)], xb[c * kRfCols], acc);
+        out[(pr * kTile + row) * kRfCols + col] = acc;
+    }
+}
+
+// Y[a][row block I] = sum over the pairs touching I, in ascending partner order.
+__global__ void rapply_reduce_kernel(const double* __restrict__ part, int n, int b, int nt, int npairs,
+                                     double* __restrict__ y) {
+    const int a = blockIdx.y, cols = 2 * b;
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (row, col) of the n x 2b output
+    if (idx >= n * cols) return;
+    const int row = idx / cols, col = idx - row * cols;
+    const int I = row / kTile, rr = row - I * kTile;
+    double acc = 0.0;
+    for (int K = 0; K < nt; ++K) {
+        int p, slot;
+        if (K >= I) {  // pair (I, K): slot 0
+            p = K * (K + 1) / 2 + I;
+            slot = 0;
+        } else {       // pair (K, I): slot 1
+            p = I * (I + 1) / 2 + K;
+            slot = 1;
+        }
+        acc += part[((int64_t)(a * npairs + p) * 2 + slot) * kTile * kRfCols + rr * kRfCols + col];
+    }
+    y[(int64_t)a * n * cols + ((int64_t)row + (int64_t)(col >> 1) * n) * 2 + (col & 1)] = acc;
+}
+
+size_t rapply_fused_part_elems(int n, int n_alpha) {
+    const int64_t nt = ceil_div(n, kTile);
+    return (size_t)n_alpha * (size_t)(nt * (nt + 1) / 2) * 2 * kTile * kRfCols;
+}
+
+int rapply_fused_max_cols() { return kRfCols; }
+
+cudaError_t launch_rapply_fused(const void* slabs, int n, int l_used, const double* coef_dev, int coef_ld, int n_alpha,
+                                const double* x, int b, double* part, double* y, cudaStream_t stream) {
+    if (2 * b > kRfCols || b < 1) return cudaErrorInvalidValue;
+    const int nt = (int)ceil_div(n, kTile), npairs = nt * (nt + 1) / 2;
+    const size_t smem = rapply_fused_smem_bytes(l_used);
+    cudaError_t e = cudaFuncSetAttribute(rapply_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    rapply_fused_kernel<<<dim3((unsigned)npairs, (unsigned)n_alpha), 256, smem, stream>>>(
+        (const double*)slabs, n, l_used, (int64_t)nt * nt * kTileElems, coef_dev, coef_ld, x, b, part, nt, npairs);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int tot = n * 2 * b;
+    rapply_reduce_kernel<<<dim3((unsigned)ceil_div(tot, 256), (unsigned)n_alpha), 256, 0, stream>>>(part, n, b, nt,
+                                                                                                     npairs, y);
     return cudaGetLastError();
 }
 

@@ -482,3 +482,26 @@ def test_int8_combine_engine(n, l, b, n_alpha):
         _, dc = O.sinc_coeffs(a, l)
         s_ref = O.power_dots(o, (2.0 * (yr - xc) / (n * b)) @ x.conj().T)
         assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+
+
+@pytest.mark.parametrize("n,l,b", [(256, 32, 1), (100, 12, 7), (64, 8, 32), (1024, 16, 3)])
+def test_fused_small_batch_apply(n, l, b):
+    """Small signal batches (2B <= 64): fused synthesis + product, Q(alpha) never leaves the SM.
+    Forward and inverse against the oracle (1e-12) and against the synthesis + DMMA GEMM route."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 41 + n)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l)
+    rng = np.random.default_rng(n + 3 * b)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    alphas = [0.37, 1.0, -0.81]
+    launches = fg.launch_count()
+    y = fg.apply_series(g, alphas, x)
+    yi = fg.apply_series(g, alphas, x, inverse=True)
+    assert fg.launch_count() - launches <= 2 * 4   # fused + reduce per call (+ coefficient upload)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        assert rel(y[i], q @ x) <= 1e-12
+        assert rel(yi[i], q.T @ x) <= 1e-12
+    g.set_engine(fg.ENGINE_DMMA)
+    y2 = fg.apply_series(g, alphas, x)
+    assert all(rel(y2[i], y[i]) <= 1e-13 for i in range(len(alphas)))
