@@ -32,11 +32,14 @@ cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coe
 cudaError_t launch_synth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
                                cudaStream_t stream);
 int synth_sweep_max_orders();
-cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream);
+cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream,
+                                 bool real);
 cudaError_t launch_synth_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l_used,
-                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream);
+                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream, bool real,
+                              bool out_complex);
 cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l, const void* m,
-                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream);
+                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream,
+                             bool real);
 size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
 cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream);
 cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream);
@@ -635,6 +638,10 @@ bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b);
 int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out);
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
+int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
+                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy);
+int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
+                int64_t sm);
 bool use_power_route(const fgfrft_cache* c, int n_alpha);
 int engine_of(const fgfrft_cache* c);
 int apply_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, int64_t b, void* y_dev);
@@ -939,7 +946,7 @@ int mse_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void
 // INT8 engine for the synthesis route's GEMMs: forced, or (auto) when the products are large
 // enough to amortise the per-call digit slicing of Q / G and X.
 bool use_int8_gemm(const fgfrft_cache* c, int64_t b) {
-    if (!c->real || c->dtype != FGFRFT_C128 || c->n > 16384 || c->shard || c->graphs > 0) return false;
+    if (!c->real || c->dtype != FGFRFT_C128 || c->n > 16384 || c->graphs > 0) return false;
     const int eng = engine_of(c);
     if (eng == FGFRFT_ENGINE_DMMA) return false;
     if (eng != FGFRFT_ENGINE_AUTO) return true;
@@ -969,17 +976,19 @@ int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp
     return FGFRFT_OK;
 }
 
-// Y_a = op(Q_a) X for na real n x n matrices Q_a (column-major, stride n^2), complex X.
-int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y) {
+// Y_a = op(Q_a) X for na real m x n matrices Q_a (column-major, leading dimension ldq, stride sq
+// doubles), complex X (n x b); Y_a complex m x b (leading dimension ldy, stride sy doubles).
+int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
+                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy) {
     const int S = oz_slices_default();
-    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(n), rows = (int64_t)na * np;
+    const int64_t n = c->n, mp = pad_rows(m), kp = pad_k(n), rows = (int64_t)na * mp;
     FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
     FGB_CUDA(c->qex.ensure((size_t)rows * (sizeof(int) + sizeof(unsigned long long))));
     int* qe = c->qex.as<int>();
     {
         const double* src = static_cast<const double*>(q);
-        const OzView v = inverse ? OzView{src, n, 1, n * n, 0, 0, (int)n, (int)np, na, (int)n, (int)kp, false}
-                                 : OzView{src, 1, n, n * n, 0, 0, (int)n, (int)np, na, (int)n, (int)kp, true};
+        const OzView v = inverse ? OzView{src, ldq, 1, sq, 0, 0, (int)m, (int)mp, na, (int)n, (int)kp, false}
+                                 : OzView{src, 1, ldq, sq, 0, 0, (int)m, (int)mp, na, (int)n, (int)kp, true};
         ProfScope ps(KC_SLICE, c->stream);
         FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->qsl.as<int8_t>(), qe,
                                    reinterpret_cast<unsigned long long*>(qe + rows), c->stream),
@@ -989,15 +998,21 @@ int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_
     if (int st = slice_signal_rows(c, x_dev, b, &bp)) return st;
     ProfScope ps(KC_I8GEMM, c->stream);
     FGB_LAUNCH(launch_ozgemm(S, 1, c->qsl.as<int8_t>(), qe, (int)rows, c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
-                             (int)kp, static_cast<double*>(y), n, 2 * n * b, (int)n, (int)np, (int)(2 * b), c->stream),
+                             (int)kp, static_cast<double*>(y), ldy, sy, (int)m, (int)mp, (int)(2 * b), c->stream),
                1);
     return FGFRFT_OK;
 }
 
-// M_a = Re(G_a X^H) (real n x n, column-major, stride n^2) for na blocks G_a (n x b complex).
-int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m) {
+int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y) {
+    return int8_qx_gen(c, na, inverse, q, c->n, c->n, c->n * c->n, x_dev, b, y, c->n, 2 * c->n * b);
+}
+
+// M_a = Re(G_a X^H) (real m x n, column-major ld m, stride sm) for na blocks G_a (m x b complex,
+// ld m, stride 2 m b doubles), X n x b.
+int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
+                int64_t sm) {
     const int S = oz_slices_default();
-    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(2 * b), rows = (int64_t)na * np;
+    const int64_t n = c->n, mp = pad_rows(m), kp = pad_k(2 * b), rows = (int64_t)na * mp;
     const int64_t xp = ceil_div(n, kOzTileB) * kOzTileB;
     FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
     FGB_CUDA(c->qex.ensure((size_t)rows * (sizeof(int) + sizeof(unsigned long long))));
@@ -1007,7 +1022,7 @@ int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b
     int* xe = c->xex.as<int>();
     {
         // G_a(i, 2j + comp) and X(l, 2j + comp): K = the (re, im) columns of the signal block
-        const OzView vg{static_cast<const double*>(g), 2, 2 * n, 2 * n * b, 0, 1, (int)n, (int)np, na, (int)(2 * b),
+        const OzView vg{static_cast<const double*>(g), 2, 2 * m, 2 * m * b, 0, 1, (int)m, (int)mp, na, (int)(2 * b),
                         (int)kp, true};
         const OzView vx{static_cast<const double*>(x_dev), 2, 2 * n, 0, 0, 1, (int)n, (int)xp, 1, (int)(2 * b),
                         (int)kp, true};
@@ -1021,9 +1036,13 @@ int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b
     }
     ProfScope ps(KC_I8GEMM, c->stream);
     FGB_LAUNCH(launch_ozgemm(S, 0, c->qsl.as<int8_t>(), ge, (int)rows, c->xsl.as<int8_t>(), xe, (int)xp, (int)kp,
-                             static_cast<double*>(m), n, n * n, (int)n, (int)np, (int)n, c->stream),
+                             static_cast<double*>(out), m, sm, (int)m, (int)mp, (int)n, c->stream),
                1);
     return FGFRFT_OK;
+}
+
+int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m) {
+    return int8_gx_gen(c, na, g, c->n, x_dev, b, m, c->n * c->n);
 }
 
 // Y_a = F^(alpha_a) X over the power products (coef: the orders' c tables, inverse already folded
@@ -1606,7 +1625,10 @@ int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, in
         (row_end % kTile != 0 && row_end != n))
         return fail(FGFRFT_PARAMETER, "shard rows must be [r0, r1) with r0 % 32 == 0 and r1 % 32 == 0 or r1 == n");
     const int64_t rows = row_end - row_begin;
-    const unsigned __int128 bytes = (unsigned __int128)2 * l * (uint64_t)rows * (uint64_t)n * 16;
+    // real F (graph GFT): real panels, real kernels (as the full cache, learn.hpp:449-451)
+    bool real = std::getenv("FGFRFT_NO_REAL") == nullptr;
+    for (size_t i = 0; i < (size_t)n * (size_t)n && real; ++i) real = f[2 * i + 1] == 0.0;
+    const unsigned __int128 bytes = (unsigned __int128)2 * l * (uint64_t)rows * (uint64_t)n * (real ? 8 : 16);
     if (bytes > memory_budget) {
         std::ostringstream msg;
         msg << "PowerCache shard: " << l << " row and column panels of " << rows << "x" << n << " need "
@@ -1622,6 +1644,8 @@ int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, in
     c->l = l;
     c->device = device;
     c->shard = true;
+    c->real = real;
+    c->elem = real ? 8 : 16;
     c->r0 = row_begin;
     c->r1 = row_end;
     c->fingerprint = host_fnv1a64(f, (size_t)n * (size_t)n * 16);
@@ -1633,7 +1657,7 @@ int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, in
         return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
     }
     c->stream = c->own_stream;
-    const size_t pbytes = c->panel_elems * 16 * (size_t)l;
+    const size_t pbytes = c->panel_elems * c->elem * (size_t)l;
     if (cudaMalloc(&c->slabs, pbytes) != cudaSuccess || cudaMalloc(&c->colp, pbytes) != cudaSuccess) {
         cudaGetLastError();
         destroy_cache(c);
@@ -1657,25 +1681,59 @@ int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, in
             rc = fail(FGFRFT_CUDA, "PowerCache shard: staging copies failed");
             break;
         }
+        // real: real copies of F and of the panels (8-byte elements) in their own scratch
+        DevBuf rs;
+        double *fre = nullptr, *rpr = nullptr, *rqr = nullptr, *cpr = nullptr, *cqr = nullptr;
+        if (real) {
+            if (rs.ensure((ml + 4 * pl) * 8) != cudaSuccess) {
+                rc = fail(FGFRFT_CAPACITY, "PowerCache shard: scratch allocation failed");
+                break;
+            }
+            fre = rs.as<double>();
+            rpr = fre + ml;
+            rqr = rpr + pl;
+            cpr = rqr + pl;
+            cqr = cpr + pl;
+            if (launch_real_part(fb, fre, (int64_t)ml, c->stream) != cudaSuccess ||
+                launch_real_part(rp, rpr, (int64_t)pl, c->stream) != cudaSuccess ||
+                launch_real_part(cp, cpr, (int64_t)pl, c->stream) != cudaSuccess) {
+                rc = fail(FGFRFT_CUDA, "PowerCache shard: real staging failed");
+                rs.release();
+                break;
+            }
+        }
         for (int k = 1; k <= l && rc == FGFRFT_OK; ++k) {
             if (k > 1) {
-                if (launch_zgemm((int)rows, (int)n, (int)n, rp, rows, 0, false, fb, n, 0, false, rq, rows, 0, 1, false,
-                                 c->stream) != cudaSuccess ||
-                    launch_zgemm((int)n, (int)rows, (int)n, fb, n, 0, false, cp, n, 0, false, cq, n, 0, 1, false,
-                                 c->stream) != cudaSuccess) {
+                cudaError_t e1, e2;
+                if (real) {
+                    e1 = launch_rgemm(0, 0, 0, (int)rows, (int)n, (int)n, rpr, rows, 0, fre, n, 0, rqr, rows, 0, 1,
+                                      c->stream);
+                    e2 = launch_rgemm(0, 0, 0, (int)n, (int)rows, (int)n, fre, n, 0, cpr, n, 0, cqr, n, 0, 1,
+                                      c->stream);
+                } else {
+                    e1 = launch_zgemm((int)rows, (int)n, (int)n, rp, rows, 0, false, fb, n, 0, false, rq, rows, 0, 1,
+                                      false, c->stream);
+                    e2 = launch_zgemm((int)n, (int)rows, (int)n, fb, n, 0, false, cp, n, 0, false, cq, n, 0, 1, false,
+                                      c->stream);
+                }
+                if (e1 != cudaSuccess || e2 != cudaSuccess) {
                     rc = fail(FGFRFT_CUDA, "PowerCache shard: panel GEMM failed");
                     break;
                 }
                 std::swap(rp, rq);
                 std::swap(cp, cq);
+                std::swap(rpr, rqr);
+                std::swap(cpr, cqr);
                 g_launches += 2;
             }
-            if (launch_rect_to_tiled(rp, rows, (int)rows, (int)n,
-                                     static_cast<double2*>(c->slabs) + (size_t)(k - 1) * c->panel_elems,
-                                     c->stream) != cudaSuccess ||
-                launch_rect_to_tiled(cp, n, (int)n, (int)rows,
-                                     static_cast<double2*>(c->colp) + (size_t)(k - 1) * c->panel_elems,
-                                     c->stream) != cudaSuccess) {
+            const void* rsrc = real ? static_cast<const void*>(rpr) : static_cast<const void*>(rp);
+            const void* csrc = real ? static_cast<const void*>(cpr) : static_cast<const void*>(cp);
+            if (launch_rect_to_tiled(rsrc, rows, (int)rows, (int)n,
+                                     static_cast<char*>(c->slabs) + (size_t)(k - 1) * c->panel_elems * c->elem,
+                                     c->stream, real) != cudaSuccess ||
+                launch_rect_to_tiled(csrc, n, (int)n, (int)rows,
+                                     static_cast<char*>(c->colp) + (size_t)(k - 1) * c->panel_elems * c->elem,
+                                     c->stream, real) != cudaSuccess) {
                 rc = fail(FGFRFT_CUDA, "PowerCache shard: tiling failed");
                 break;
             }
@@ -1683,6 +1741,7 @@ int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, in
         }
         if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
             rc = fail(FGFRFT_CUDA, "PowerCache shard: build failed");
+        rs.release();
     } while (false);
     c->tmp.release();
     if (rc != FGFRFT_OK) {
@@ -1733,7 +1792,7 @@ int fgfrft_shard_synthesize_dev(fgfrft_cache* c, const double* alphas, int n_alp
     const double* table = which == FGFRFT_Q ? coef : coef + (size_t)n_alpha * (2 * c->l + 1);
     ProfScope ps(KC_SYNTH, c->stream);
     FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, (int)c->n, (int)c->r0, (int)(c->r1 - c->r0), c->l, table, n_alpha,
-                                 out_dev, c->stream),
+                                 out_dev, c->stream, c->real, true),
                1);
     return FGFRFT_OK;
     FGB_GUARD_END
@@ -1760,14 +1819,26 @@ int fgfrft_shard_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, c
         {
             ProfScope ps(KC_SYNTH, c->stream);
             FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, c->l, coef + a0 * width, na, c->q.p,
-                                         c->stream),
+                                         c->stream, c->real, false),
                        1);
         }
+        if (use_int8_gemm(c, b)) {
+            if (int st = int8_qx_gen(c, na, false, c->q.p, rows, rows, (int64_t)qs, x_dev, b,
+                                     static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, 2 * (int64_t)rows * b))
+                return st;
+            continue;
+        }
         ProfScope ps(KC_GEMM, c->stream);
-        FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false,
-                                static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, (int64_t)rows * b, na,
-                                false, c->stream),
-                   1);
+        if (c->real)  // Y[R,:] = Q[R,:] X, real Q rows panel (ld = rows) x complex X
+            FGB_LAUNCH(launch_rgemm(0, 1, 1, rows, 2 * (int)b, n, c->q.p, rows, (int64_t)qs, x_dev, n, 0,
+                                    static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, (int64_t)2 * rows * b,
+                                    na, c->stream),
+                       1);
+        else
+            FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false,
+                                    static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, (int64_t)rows * b, na,
+                                    false, c->stream),
+                       1);
     }
     return FGFRFT_OK;
     FGB_GUARD_END
@@ -1801,14 +1872,23 @@ int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_al
         {
             ProfScope ps(KC_SYNTH, c->stream);
             FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, coef + a0 * width, na, c->q.p,
-                                         c->stream),
+                                         c->stream, c->real, false),
                        1);
         }
-        {
+        if (use_int8_gemm(c, b)) {
+            if (int st = int8_qx_gen(c, na, false, c->q.p, rows, rows, (int64_t)qs, x_dev, b, ya, rows,
+                                     2 * (int64_t)blk))
+                return st;
+        } else {
             ProfScope ps(KC_GEMM, c->stream);
-            FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false, ya, rows,
-                                    (int64_t)blk, na, false, c->stream),
-                       1);
+            if (c->real)
+                FGB_LAUNCH(launch_rgemm(0, 1, 1, rows, 2 * (int)b, n, c->q.p, rows, (int64_t)qs, x_dev, n, 0, ya, rows,
+                                        (int64_t)2 * blk, na, c->stream),
+                           1);
+            else
+                FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false, ya, rows,
+                                        (int64_t)blk, na, false, c->stream),
+                           1);
         }
         {
             ProfScope ps(KC_ELEMWISE, c->stream);
@@ -1817,16 +1897,23 @@ int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_al
                                            c->stream, 16),
                        2);
         }
-        {
-            ProfScope ps(KC_GEMM, c->stream);  // M[R,:] = G[R,:] X^H
-            FGB_LAUNCH(launch_zgemm(rows, n, (int)b, c->g.p, rows, (int64_t)blk, false, x_dev, n, 0, true, c->m.p, rows,
-                                    (int64_t)qs, na, false, c->stream),
-                       1);
+        if (use_int8_gemm(c, b)) {
+            if (int st = int8_gx_gen(c, na, c->g.p, rows, x_dev, b, c->m.p, (int64_t)qs)) return st;
+        } else {
+            ProfScope ps(KC_GEMM, c->stream);  // M[R,:] = G[R,:] X^H (real F: only Re M is needed)
+            if (c->real)
+                FGB_LAUNCH(launch_rgemm(2, 2, 0, rows, n, 2 * (int)b, c->g.p, rows, (int64_t)2 * blk, x_dev, n, 0, c->m.p,
+                                        rows, (int64_t)qs, na, c->stream),
+                           1);
+            else
+                FGB_LAUNCH(launch_zgemm(rows, n, (int)b, c->g.p, rows, (int64_t)blk, false, x_dev, n, 0, true, c->m.p,
+                                        rows, (int64_t)qs, na, false, c->stream),
+                           1);
         }
         ProfScope ps(KC_DOTS, c->stream);
         FGB_LAUNCH(launch_dots_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, c->m.p, (int64_t)qs, na,
                                     c->partial.as<double>(), static_cast<double*>(s_partial_dev) + a0 * width,
-                                    c->stream),
+                                    c->stream, c->real),
                    2);
     }
     return FGFRFT_OK;

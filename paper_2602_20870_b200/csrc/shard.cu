@@ -20,22 +20,29 @@ namespace fgb {
 constexpr int kRowStages = 4;
 
 // Rectangular column-major (m x ncols, ld) -> tiled with tile (I, J) at (J * ntm + I) * 1024.
-__global__ void __launch_bounds__(256) rect_to_tiled_kernel(const double2* __restrict__ src, int64_t ld, int m,
-                                                            int ncols, double2* __restrict__ dst, int ntm) {
+template <typename T>
+__global__ void __launch_bounds__(256) rect_to_tiled_kernel(const T* __restrict__ src, int64_t ld, int m, int ncols,
+                                                            T* __restrict__ dst, int ntm) {
     const int I = blockIdx.x % ntm, J = blockIdx.x / ntm;
     const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double2* t = dst + ((int64_t)J * ntm + I) * kTileElems;
+    T* t = dst + ((int64_t)J * ntm + I) * kTileElems;
     const int row = I * kTile + r;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int c = w + 8 * i, col = J * kTile + c;
-        t[swz(r, c)] = (row < m && col < ncols) ? src[(int64_t)col * ld + row] : make_double2(0.0, 0.0);
+        t[swz(r, c)] = (row < m && col < ncols) ? src[(int64_t)col * ld + row] : T{};
     }
 }
 
-cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream) {
+cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream,
+                                 bool real) {
     const int ntm = (int)ceil_div(m, kTile), ntn = (int)ceil_div(ncols, kTile);
-    rect_to_tiled_kernel<<<ntm * ntn, 256, 0, stream>>>((const double2*)src, ld, m, ncols, (double2*)dst, ntm);
+    if (real)
+        rect_to_tiled_kernel<double><<<ntm * ntn, 256, 0, stream>>>((const double*)src, ld, m, ncols, (double*)dst,
+                                                                    ntm);
+    else
+        rect_to_tiled_kernel<double2><<<ntm * ntn, 256, 0, stream>>>((const double2*)src, ld, m, ncols,
+                                                                     (double2*)dst, ntm);
     return cudaGetLastError();
 }
 
@@ -45,20 +52,28 @@ __device__ __forceinline__ void pair_update_d(double2& q, double a, double b, co
     q.y = __dadd_rn(q.y, __dadd_rn(__dmul_rn(a, p.y), __dmul_rn(b, -pt.y)));
 }
 
-size_t rows_smem_bytes(int l, int ac) {
-    return (size_t)kRowStages * 2 * kTileElems * 16 + kRowStages * 8 + (size_t)l * ac * 16 + (size_t)ac * 8 + 16;
+__device__ __forceinline__ void pair_update_d(double& q, double a, double b, const double& p, const double& pt) {
+    q = __dadd_rn(q, __dadd_rn(__dmul_rn(a, p), __dmul_rn(b, pt)));
 }
 
+__host__ __device__ inline size_t rows_smem_bytes(int l, int ac, int esz) {
+    return (size_t)kRowStages * 2 * kTileElems * esz + kRowStages * 8 + (size_t)l * ac * 16 + (size_t)ac * 8 + 16;
+}
+
+template <typename T> __device__ __forceinline__ T zero_of(double v);
+template <> __device__ __forceinline__ double2 zero_of<double2>(double v) { return make_double2(v, 0.0); }
+template <> __device__ __forceinline__ double zero_of<double>(double v) { return v; }
+
 // CTA per (order chunk, tile (I0 + i, J)); output rows panel (ld = rows).
-template <int AC>
+template <typename T, int AC, bool OUTC>
 __global__ void __launch_bounds__(256, 1)
-synth_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ colp, int64_t panel_elems, int n,
+synth_rows_kernel(const T* __restrict__ rowp, const T* __restrict__ colp, int64_t panel_elems, int n,
                   int r0, int rows, int l_used, const double* __restrict__ coef, int coef_ld, int n_alpha,
-                  int n_achunks, double2* __restrict__ out, int64_t out_stride, int nI, int nt) {
+                  int n_achunks, void* __restrict__ out, int64_t out_stride, int nI, int nt) {
     constexpr int S = kRowStages;
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* tiles = reinterpret_cast<double2*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 16);
+    T* tiles = reinterpret_cast<T*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * sizeof(T));
     double2* cs = reinterpret_cast<double2*>(full + S);
     double* c0s = reinterpret_cast<double*>(cs + (size_t)l_used * AC);
     const int chunk = blockIdx.x % n_achunks, tidx = blockIdx.x / n_achunks;
@@ -81,12 +96,12 @@ synth_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ 
         fence_mbar_init();
     }
     __syncthreads();
-    const uint32_t tb = kTileElems * 16;
+    const uint32_t tb = kTileElems * sizeof(T);
     const uint64_t pol = policy_evict_first();
     const int64_t off1 = ((int64_t)J * nI + i) * kTileElems, off2 = ((int64_t)i * nt + J) * kTileElems;
     auto issue = [&](int k, int s) {
         mbar_arrive_expect_tx(&full[s], 2 * tb);
-        double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        T* t1 = tiles + (size_t)(s * 2) * kTileElems;
         bulk_g2s_hint(t1, rowp + (int64_t)(k - 1) * panel_elems + off1, tb, &full[s], pol);
         bulk_g2s_hint(t1 + kTileElems, colp + (int64_t)(k - 1) * panel_elems + off2, tb, &full[s], pol);
     };
@@ -94,26 +109,26 @@ synth_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ 
         for (int s = 0; s < S && s < l_used; ++s) issue(s + 1, s);
     const int gI = r0 / kTile + i;  // global block row
     const int r = lane;
-    double2 q[4][AC];
+    T q[4][AC];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int c = warp + 8 * u;
 #pragma unroll
-        for (int a = 0; a < AC; ++a) q[u][a] = make_double2((gI == J && r == c) ? c0s[a] : 0.0, 0.0);
+        for (int a = 0; a < AC; ++a) q[u][a] = zero_of<T>((gI == J && r == c) ? c0s[a] : 0.0);
     }
     for (int k = 1; k <= l_used; ++k) {
         const int s = (k - 1) % S;
         mbar_wait(&full[s], ((k - 1) / S) & 1);
-        const double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
-        const double2* t2 = t1 + kTileElems;
+        const T* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        const T* t2 = t1 + kTileElems;
         double2 ab[AC];
 #pragma unroll
         for (int a = 0; a < AC; ++a) ab[a] = cs[(k - 1) * AC + a];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = warp + 8 * u;
-            const double2 p1 = t1[swz(r, c)];  // P[gI*32 + r, J*32 + c]
-            const double2 p2 = t2[swz(c, r)];  // P[J*32 + c, gI*32 + r]
+            const T p1 = t1[swz(r, c)];  // P[gI*32 + r, J*32 + c]
+            const T p2 = t2[swz(c, r)];  // P[J*32 + c, gI*32 + r]
 #pragma unroll
             for (int a = 0; a < AC; ++a) pair_update_d(q[u][a], ab[a].x, ab[a].y, p1, p2);
         }
@@ -127,29 +142,41 @@ synth_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ 
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int col = J * kTile + warp + 8 * u;
-            if (lrow < rows && col < n) out[(int64_t)(a0 + a) * out_stride + (int64_t)col * rows + lrow] = q[u][a];
+            if (lrow < rows && col < n) {
+                const int64_t o = (int64_t)(a0 + a) * out_stride + (int64_t)col * rows + lrow;
+                if constexpr (OUTC && sizeof(T) == 8) reinterpret_cast<double2*>(out)[o] = make_double2(q[u][a], 0.0);
+                else reinterpret_cast<T*>(out)[o] = q[u][a];
+            }
         }
     }
 }
 
+// real: real panels; out_complex: write complex128 (API output) even from real panels.
 cudaError_t launch_synth_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l_used,
-                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream) {
+                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream, bool real,
+                              bool out_complex) {
     const int nI = (int)ceil_div(rows, kTile), nt = (int)ceil_div(n, kTile);
     const int64_t panel = (int64_t)nI * nt * kTileElems;
     const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
     const int nch = (int)ceil_div(n_alpha, ac);
-    const size_t smem = rows_smem_bytes(l_used, ac);
+    const size_t smem = rows_smem_bytes(l_used, ac, real ? 8 : 16);
     const dim3 grid((unsigned)((int64_t)nch * nI * nt));
-#define FGB_ROWS_CASE(ACV)                                                                                   \
+#define FGB_ROWS_CASE(TT, ACV, OC)                                                                           \
     {                                                                                                        \
-        auto kern = synth_rows_kernel<ACV>;                                                                  \
+        auto kern = synth_rows_kernel<TT, ACV, OC>;                                                          \
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return e;                                                                      \
-        kern<<<grid, 256, smem, stream>>>((const double2*)rowp, (const double2*)colp, panel, n, r0, rows,    \
-                                          l_used, coef_dev, 2 * l_used + 1, n_alpha, nch, (double2*)out,     \
-                                          (int64_t)rows * n, nI, nt);                                        \
+        kern<<<grid, 256, smem, stream>>>((const TT*)rowp, (const TT*)colp, panel, n, r0, rows, l_used,      \
+                                          coef_dev, 2 * l_used + 1, n_alpha, nch, out, (int64_t)rows * n, nI, \
+                                          nt);                                                               \
     }
-    if (ac == 4) FGB_ROWS_CASE(4) else if (ac == 2) FGB_ROWS_CASE(2) else FGB_ROWS_CASE(1)
+    if (!real) {
+        if (ac == 4) FGB_ROWS_CASE(double2, 4, true) else if (ac == 2) FGB_ROWS_CASE(double2, 2, true) else FGB_ROWS_CASE(double2, 1, true)
+    } else if (out_complex) {
+        if (ac == 4) FGB_ROWS_CASE(double, 4, true) else if (ac == 2) FGB_ROWS_CASE(double, 2, true) else FGB_ROWS_CASE(double, 1, true)
+    } else {
+        if (ac == 4) FGB_ROWS_CASE(double, 4, false) else if (ac == 2) FGB_ROWS_CASE(double, 2, false) else FGB_ROWS_CASE(double, 1, false)
+    }
 #undef FGB_ROWS_CASE
     return cudaGetLastError();
 }
@@ -162,15 +189,26 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
-template <int AC>
+__device__ __forceinline__ double re_dot(const double2& m, const double2& p, double acc) {
+    return fma(m.x, p.x, fma(m.y, p.y, acc));
+}
+__device__ __forceinline__ double re_dot_conj(const double2& m, const double2& p, double acc) {
+    return fma(m.x, p.x, fma(-m.y, p.y, acc));
+}
+__device__ __forceinline__ double re_dot(const double& m, const double& p, double acc) { return fma(m, p, acc); }
+__device__ __forceinline__ double re_dot_conj(const double& m, const double& p, double acc) { return fma(m, p, acc); }
+__device__ __forceinline__ double re_of(const double2& v) { return v.x; }
+__device__ __forceinline__ double re_of(const double& v) { return v; }
+
+template <typename T, int AC>
 __global__ void __launch_bounds__(256, 1)
-dots_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ colp, int64_t panel_elems, int n,
-                 int r0, int rows, int l, const double2* __restrict__ m, int64_t m_stride, int n_alpha,
+dots_rows_kernel(const T* __restrict__ rowp, const T* __restrict__ colp, int64_t panel_elems, int n,
+                 int r0, int rows, int l, const T* __restrict__ m, int64_t m_stride, int n_alpha,
                  int n_achunks, double* __restrict__ partial, int nI, int nt) {
     constexpr int S = kRowStages;
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* tiles = reinterpret_cast<double2*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * 16);
+    T* tiles = reinterpret_cast<T*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * 2 * kTileElems * sizeof(T));
     double* red = reinterpret_cast<double*>(full + S);  // [k-1][warp][a][2]
     const int chunk = blockIdx.x % n_achunks, tidx = blockIdx.x / n_achunks;
     const int i = tidx % nI, J = tidx / nI;
@@ -182,19 +220,19 @@ dots_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ c
         fence_mbar_init();
     }
     __syncthreads();
-    const uint32_t tb = kTileElems * 16;
+    const uint32_t tb = kTileElems * sizeof(T);
     const uint64_t pol = policy_evict_first();
     const int64_t off1 = ((int64_t)J * nI + i) * kTileElems, off2 = ((int64_t)i * nt + J) * kTileElems;
     auto issue = [&](int k, int s) {
         mbar_arrive_expect_tx(&full[s], 2 * tb);
-        double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        T* t1 = tiles + (size_t)(s * 2) * kTileElems;
         bulk_g2s_hint(t1, rowp + (int64_t)(k - 1) * panel_elems + off1, tb, &full[s], pol);
         bulk_g2s_hint(t1 + kTileElems, colp + (int64_t)(k - 1) * panel_elems + off2, tb, &full[s], pol);
     };
     if (tid == 0)
         for (int s = 0; s < S && s < l; ++s) issue(s + 1, s);
     const int gI = r0 / kTile + i;
-    double2 mv[4][AC];
+    T mv[4][AC];
     double s0[AC];
 #pragma unroll
     for (int a = 0; a < AC; ++a) s0[a] = 0.0;
@@ -205,27 +243,27 @@ dots_rows_kernel(const double2* __restrict__ rowp, const double2* __restrict__ c
 #pragma unroll
         for (int a = 0; a < AC; ++a) {
             const bool v = a < na && lrow < rows && col < n;
-            mv[u][a] = v ? m[(int64_t)(a0 + a) * m_stride + (int64_t)col * rows + lrow] : make_double2(0.0, 0.0);
-            if (gI == J && r == c) s0[a] += mv[u][a].x;
+            mv[u][a] = v ? m[(int64_t)(a0 + a) * m_stride + (int64_t)col * rows + lrow] : T{};
+            if (gI == J && r == c) s0[a] += re_of(mv[u][a]);
         }
     }
     for (int k = 1; k <= l; ++k) {
         const int s = (k - 1) % S;
         mbar_wait(&full[s], ((k - 1) / S) & 1);
-        const double2* t1 = tiles + (size_t)(s * 2) * kTileElems;
-        const double2* t2 = t1 + kTileElems;
+        const T* t1 = tiles + (size_t)(s * 2) * kTileElems;
+        const T* t2 = t1 + kTileElems;
         double sp[AC], sm[AC];
 #pragma unroll
         for (int a = 0; a < AC; ++a) sp[a] = sm[a] = 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = warp + 8 * u;
-            const double2 p1 = t1[swz(r, c)];
-            const double2 p2 = t2[swz(c, r)];
+            const T p1 = t1[swz(r, c)];
+            const T p2 = t2[swz(c, r)];
 #pragma unroll
             for (int a = 0; a < AC; ++a) {
-                sp[a] = fma(mv[u][a].x, p1.x, fma(mv[u][a].y, p1.y, sp[a]));
-                sm[a] = fma(mv[u][a].x, p2.x, fma(-mv[u][a].y, p2.y, sm[a]));
+                sp[a] = re_dot(mv[u][a], p1, sp[a]);
+                sm[a] = re_dot_conj(mv[u][a], p2, sm[a]);
             }
         }
 #pragma unroll
@@ -277,22 +315,28 @@ size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha) {
 }
 
 cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l, const void* m,
-                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream) {
+                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream,
+                             bool real) {
     const int nI = (int)ceil_div(rows, kTile), nt = (int)ceil_div(n, kTile);
     const int64_t panel = (int64_t)nI * nt * kTileElems;
     const int ac = n_alpha >= 4 ? 4 : (n_alpha >= 2 ? 2 : 1);
     const int nch = (int)ceil_div(n_alpha, ac);
-    const size_t smem = (size_t)kRowStages * 2 * kTileElems * 16 + kRowStages * 8 + (size_t)l * 8 * ac * 2 * 8 + 16;
+    const size_t esz = real ? 8 : 16;
+    const size_t smem = (size_t)kRowStages * 2 * kTileElems * esz + kRowStages * 8 + (size_t)l * 8 * ac * 2 * 8 + 16;
     const dim3 grid((unsigned)((int64_t)nch * nI * nt));
-#define FGB_DR_CASE(ACV)                                                                                     \
+#define FGB_DR_CASE(TT, ACV)                                                                                 \
     {                                                                                                        \
-        auto kern = dots_rows_kernel<ACV>;                                                                   \
+        auto kern = dots_rows_kernel<TT, ACV>;                                                               \
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return e;                                                                      \
-        kern<<<grid, 256, smem, stream>>>((const double2*)rowp, (const double2*)colp, panel, n, r0, rows, l, \
-                                          (const double2*)m, m_stride, n_alpha, nch, partial, nI, nt);       \
+        kern<<<grid, 256, smem, stream>>>((const TT*)rowp, (const TT*)colp, panel, n, r0, rows, l,           \
+                                          (const TT*)m, m_stride, n_alpha, nch, partial, nI, nt);            \
     }
-    if (ac == 4) FGB_DR_CASE(4) else if (ac == 2) FGB_DR_CASE(2) else FGB_DR_CASE(1)
+    if (real) {
+        if (ac == 4) FGB_DR_CASE(double, 4) else if (ac == 2) FGB_DR_CASE(double, 2) else FGB_DR_CASE(double, 1)
+    } else {
+        if (ac == 4) FGB_DR_CASE(double2, 4) else if (ac == 2) FGB_DR_CASE(double2, 2) else FGB_DR_CASE(double2, 1)
+    }
 #undef FGB_DR_CASE
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

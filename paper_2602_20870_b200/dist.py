@@ -36,6 +36,18 @@ def plan_rows(n: int, world: int) -> List[Tuple[int, int]]:
     return out
 
 
+def _signals(x) -> int:
+    """Number of signals b: host arrays are n x b; device tensors are stored transposed, b x n
+    (the column-major n x b block)."""
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            return int(x.shape[0])
+    except ImportError:
+        pass
+    return int(np.asarray(x).shape[1])
+
+
 class RankCompute:
     """Per-rank work on rows [r0, r1). All arrays are numpy/torch on the rank's device."""
 
@@ -94,7 +106,7 @@ class CudaShard(RankCompute):
     def mse_partial(self, alphas, x, xc_rows, want_y: bool = False):
         t = self.torch
         al = np.ascontiguousarray(alphas, dtype=np.float64)
-        A, b = len(al), x.shape[1]
+        A, b = len(al), _signals(x)
         xd = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(np.asarray(x).T)).to(self._dev())
         xcd = xc_rows if isinstance(xc_rows, t.Tensor) else \
             t.from_numpy(np.ascontiguousarray(np.asarray(xc_rows).T)).to(self._dev())
@@ -109,7 +121,7 @@ class CudaShard(RankCompute):
     def apply_rows(self, alphas, x):
         t = self.torch
         al = np.ascontiguousarray(alphas, dtype=np.float64)
-        A, b = len(al), x.shape[1]
+        A, b = len(al), _signals(x)
         xd = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(np.asarray(x).T)).to(self._dev())
         y = t.empty((A, b, self.rows), dtype=t.complex128, device=self._dev())
         self._check(self._lib.fgfrft_shard_apply_dev(self._h, al.ctypes.data, A, xd.data_ptr(), b, y.data_ptr()))
@@ -147,7 +159,7 @@ class ShardedFGFRFT:
             dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)  # the only data collective
         packed = packed.cpu().numpy()
         A = len(alphas)
-        b = x.shape[1]
+        b = _signals(x)
         loss = packed[:A] / (self.n * b)
         s = packed[A:].reshape(A, 2 * self.l + 1)
         dl = np.array([float(np.dot(sinc_coeffs(float(a), self.l)[1], s[i])) for i, a in enumerate(alphas)])

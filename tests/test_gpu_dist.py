@@ -17,12 +17,18 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("n,l,world,n_alpha", [(100, 7, 2, 3), (256, 32, 3, 5), (64, 4, 2, 1), (96, 6, 4, 2)])
-def test_shards_combine_to_unsharded(n, l, world, n_alpha):
-    f = prep.random_unitary(n, 40 + n)
+@pytest.mark.parametrize("kind", ["haar", "graph"])
+@pytest.mark.parametrize("n,l,world,n_alpha,b", [(100, 7, 2, 3, 9), (256, 32, 3, 5, 9), (64, 4, 2, 1, 9),
+                                                 (96, 6, 4, 2, 9), (512, 8, 2, 2, 40)])
+def test_shards_combine_to_unsharded(n, l, world, n_alpha, b, kind):
+    """kind = graph: a real orthogonal F (graph GFT) -> real panels and real shard kernels; with
+    n >= 512 and 2b >= 64 the shard GEMMs run on the INT8 engine."""
+    if kind == "haar":
+        f = prep.random_unitary(n, 40 + n)
+    else:
+        f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 40 + n)))
     o = O.PowerCache(f, l)
     rng = np.random.default_rng(n)
-    b = 9
     x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
     xc = x + 0.1 * rng.standard_normal((n, b))
     alphas = list(np.linspace(-0.8, 1.9, n_alpha))

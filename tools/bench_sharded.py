@@ -83,7 +83,7 @@ def main():
             "unit": "signal-nodes/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "dtype": "c128", "data": "synthetic",
             "config": {"workload": "BASELINE config 4", "n": n, "l": L, "b": b, "rows_per_rank": r1 - r0,
-                       "shard_bytes_per_rank": 2 * L * (r1 - r0) * n * 16},
+                       "shard_bytes_per_rank": 2 * L * (r1 - r0) * n * (8 if np.all(cfg.f.imag == 0) else 16)},
             "build_s_rank0": build_s, "loss": float(loss[0]), "dlda": float(dl[0])}), flush=True)
     shard.close()
     if ws > 1:
