@@ -121,6 +121,19 @@ def _config(rank: int):
     return cfg
 
 
+def workload_config(cfg, ws):
+    """The `config` object of both arms (ours and --impl reference): the same workload."""
+    n, b = cfg.x.shape
+    real = bool(np.all(cfg.f.imag == 0))
+    return {"workload": "BASELINE config 2 (configs[1]): N=1024 Gaussian k-NN sensor graph, L=64, "
+                        "B=256 noisy bandlimited signals, 64 orders linspace(0,2); step = forward "
+                        "F^a X + MSE loss + dL/da for every order",
+            "n": n, "l": cfg.l, "b": b, "orders": len(cfg.alphas),
+            "cache_bytes": cfg.l * n * n * (8 if real else 16), "real_f": real,
+            "l2": "inputs larger than L2 (0.54 GB real cache + 0.8 GB INT8 digits streamed every step)",
+            "parallelism": f"replicas x{ws} (independent problems per rank)"}
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the reference's CPU path (oracle port; the reference itself cannot be
     built here -- Eigen3 absent) on all host threads, each step a bounded sample of the workload."""
@@ -154,8 +167,7 @@ def run_reference(args, ws, rank):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-           "config": {"workload": "BASELINE config 2: N=1024 Gaussian k-NN sensor graph, L=64, B=256, "
-                                  "orders linspace(0,2,64); sample of %d orders per step" % len(sample)},
+           "config": workload_config(cfg, ws),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                             "sample": f"{len(sample)} of 64 orders per step (alphas {sample}): fgfrft_matrix + "
                                       "apply (OpenBLAS zgemm) + fgfrft_grad + <G, dQ X>, oracle restatement of "
@@ -427,13 +439,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": "BASELINE config 2 (configs[1]): N=1024 Gaussian k-NN sensor graph, L=64, "
-                                   "B=256 noisy bandlimited signals, 64 orders linspace(0,2); step = forward "
-                                   "F^a X + MSE loss + dL/da for every order",
-                       "n": n, "l": L, "b": b, "orders": A, "cache_bytes": L * n * n * (8 if real else 16),
-                       "real_f": real,
-                       "l2": "inputs larger than L2 (1.07 GB cache streamed every step)",
-                       "parallelism": f"replicas x{ws} (independent problems per rank)"},
+            "config": workload_config(cfg, ws),
             "roofline": roof,
             "route": ("power products: Z = F^k X by one INT8 tensor-core Ozaki GEMM over the stacked cache, "
                       "then per-order combination + MSE + dL/da on DMMA" if power_route else
