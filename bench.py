@@ -121,6 +121,24 @@ def _config(rank: int):
     return cfg
 
 
+def ncu_traffic(kernel_prefix: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel from the committed ncu
+    --set full summary (profiles/r01_ncu_final_summary.csv), or None."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_ncu_final_summary.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        h, u = rows[0], rows[1]
+        ki, ri, wi = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for r in rows[2:]:
+            if r[ki].startswith(kernel_prefix):
+                return float(r[ri]) * scale[u[ri]] + float(r[wi]) * scale[u[wi]]
+    except Exception:
+        return None
+    return None
+
+
 def workload_config(cfg, ws):
     """The `config` object of both arms (ours and --impl reference): the same workload."""
     n, b = cfg.x.shape
@@ -332,10 +350,15 @@ def main():
         cb_flops = y_flops + (2.0 * 2 * (2 * L + 1) * 2 * n * b if gram else y_flops)
         cb_form = ("Y = C Z (DMMA) + Gram sequence / R dot products (F orthogonal: "
                    f"residual {cache.orthogonality():.2e})" if gram else "Y = C Z and S = G Z^T (DMMA)")
+        traffic = ncu_traffic(f"void ozgemm_kernel<{S}, 1, 2>")
         roof = {"bound": "tensor",
                 "kernel": f"ozgemm_kernel<{S},1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
                 "achieved": achieved, "peak": peaks["int8_tops"], "unit": "TOPS",
-                "frac": achieved / peaks["int8_tops"], "traffic": None, "peak_source": peaks["int8_src"],
+                "frac": achieved / peaks["int8_tops"], "traffic": traffic,
+                "traffic_note": ("bytes per launch, DRAM read + write from profiles/r01_ncu_final_summary.csv "
+                                 "(ncu --set full); algorithmic: sliced cache 2L*N*N*S bytes read once + Z "
+                                 "2L*N*2B*8 written = %.3g" % (2 * L * n * n * S + 2 * L * n * 2 * b * 8)),
+                "peak_source": peaks["int8_src"],
                 "algorithmic": "per step 2*(2L*N)*(2B)*N FP64-equivalent flops (Z = F^k X, k = +-1..+-L, real F x "
                                f"complex X) = {products} int8 digit-product GEMMs of that size (Ozaki scheme, "
                                f"{S} base-254 digits)",
