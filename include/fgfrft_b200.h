@@ -255,6 +255,29 @@ int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
                           const double* b, int64_t ldb, double* c, int64_t ldc, int slices,
                           void* stream);
 
+/* ---- GPU-resident denoising learner (learn.hpp:291-516, adam.hpp) -------------------------
+ *
+ * The paper's denoising workload on the device for a real F (graph GFT): the signal-side powers
+ * F^m y are built once; every evaluation applies Q(alpha) = sum c_m F^m through power products
+ * (one INT8 tensor-core GEMM each for F^m (h o u) and F^m r) and combinations, exactly the
+ * quantities of the reference's fast engine:
+ *   u = Q y, w = Q^H (h o u), loss = |w - x|^2, grad_h = 2 rowsum(Q r o u),
+ *   grad_alpha = 2 <r, dQ^H/dalpha (h o u)> + 2 <Q r, h o dQ/dalpha y>,  r = w - x.
+ * y, x_ref, reconstruction: n x channels real, column-major (host). fit runs Adam (lr, beta
+ * 0.9 / 0.999, eps 1e-8) over [alpha, h] from [init_alpha, 1..1] for `epochs` steps, evaluating
+ * once more at the end (trajectories have epochs + 1 entries) and tracking the best loss, all on
+ * the device. Coefficients of the device-resident alpha come from device sin / cos (~1 ulp).
+ */
+typedef struct fgfrft_denoise fgfrft_denoise;
+int fgfrft_denoise_create(fgfrft_cache* cache, const double* y, const double* x_ref, int64_t channels,
+                          fgfrft_denoise** out);
+int fgfrft_denoise_destroy(fgfrft_denoise* problem);
+int fgfrft_denoise_eval(fgfrft_denoise* problem, double alpha, const double* h, double* loss,
+                        double* grad_alpha, double* grad_h);
+int fgfrft_denoise_fit(fgfrft_denoise* problem, int epochs, double lr, double init_alpha,
+                       double* traj_loss, double* traj_alpha, double* alpha_best, double* h_best,
+                       double* loss_best, int* best_epoch, double* reconstruction);
+
 /* ---- batches of small graphs (BASELINE config 5: fractional specformer) ----------------
  *
  * `graphs` independent GFT matrices (n <= 64, complex128 host input, graph-major), powers

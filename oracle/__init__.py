@@ -22,6 +22,7 @@ Restated reference functions (file:line under /root/reference/proj/include/fgfrf
   phase_margin                       spectral.hpp:179-195
   matrix_errors                      metrics.hpp:21-34
   cascade dL/dalpha (K=1)            learn.hpp:88-92
+  FastDenoiseEngine (real F), Adam   learn.hpp:291-413, learn.hpp:471-516, adam.hpp:34-53
 """
 from __future__ import annotations
 
@@ -396,3 +397,84 @@ def power_dots_recursive(f: np.ndarray, l: int, g: np.ndarray, x: np.ndarray) ->
         out[l + k] = float(np.vdot(g, vp).real)
         out[l - k] = float(np.vdot(g, vm).real)
     return out
+
+
+# ------------------------------------------------------------------ denoising learner (real F)
+
+class FastDenoise:
+    """learn.hpp:291-413 FastDenoiseEngine<MatrixXd> (real F): matrix-free Q^alpha through
+    iterated products with F / F^T; the signal-side powers F^n y are precomputed (learn.hpp:300-305)."""
+
+    def __init__(self, y: np.ndarray, x: np.ndarray, f: np.ndarray, l: int):
+        self.y, self.x, self.f, self.l = np.asarray(y, float), np.asarray(x, float), np.asarray(f, float), int(l)
+        self.spow = self._powers(self.y)
+
+    def _powers(self, v: np.ndarray) -> dict:
+        p = {0: v}
+        for m in range(1, self.l + 1):  # at(m) = F at(m-1), at(-m) = F^H at(-(m-1))
+            p[m] = self.f @ p[m - 1]
+            p[-m] = self.f.T @ p[-(m - 1)]
+        return p
+
+    def _run(self, c: np.ndarray, h: np.ndarray):
+        l = self.l
+        u = c[l] * self.spow[0]
+        for m in range(1, l + 1):
+            u = u + (c[l + m] * self.spow[m] + c[l - m] * self.spow[-m])
+        v = h[:, None] * u
+        tpow = self._powers(v)
+        w = c[l] * tpow[0]
+        for m in range(1, l + 1):  # Q^H v = sum_m c_{-m} F^m v
+            w = w + (c[l - m] * tpow[m] + c[l + m] * tpow[-m])
+        cot = w - self.x
+        return u, tpow, w, cot, float(np.sum(cot * cot))
+
+    def eval(self, alpha: float, h: np.ndarray):
+        """-> (loss, grad_alpha, grad_h), learn.hpp:306-338."""
+        l = self.l
+        c, dc = sinc_coeffs(alpha, l)
+        u, tpow, w, cot, loss = self._run(c, h)
+        gpow = self._powers(cot)
+        qr = c[l] * gpow[0]
+        for m in range(1, l + 1):
+            qr = qr + (c[l + m] * gpow[m] + c[l - m] * gpow[-m])
+        grad_h = 2.0 * np.sum(qr * u, axis=1)
+        dqh_v = dc[l] * tpow[0]
+        for m in range(1, l + 1):
+            dqh_v = dqh_v + (dc[l - m] * tpow[m] + dc[l + m] * tpow[-m])
+        du = dc[l] * self.spow[0]
+        for m in range(1, l + 1):
+            du = du + (dc[l + m] * self.spow[m] + dc[l - m] * self.spow[-m])
+        ga = 2.0 * float(np.sum(cot * dqh_v)) + 2.0 * float(np.sum(qr * (h[:, None] * du)))
+        return loss, ga, grad_h
+
+    def reconstruct(self, alpha: float, h: np.ndarray) -> np.ndarray:
+        c, _ = sinc_coeffs(alpha, self.l)
+        return self._run(c, h)[2]
+
+
+def adam_step(params, m, v, grad, step, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """adam.hpp:34-53 (step = the new step count)."""
+    m = beta1 * m + (1.0 - beta1) * grad
+    v = beta2 * v + (1.0 - beta2) * grad * grad
+    c1 = 1.0 - beta1 ** step
+    c2 = 1.0 - beta2 ** step
+    return params - lr * (m / c1) / (np.sqrt(v / c2) + eps), m, v
+
+
+def denoise_fit(problem: FastDenoise, epochs: int, lr: float, init_alpha: float):
+    """learn.hpp:471-516: Adam over [alpha, h] from [init_alpha, 1..1]; returns (trajectory
+    [(loss, alpha)] of epochs + 1 entries, alpha_best, h_best, loss_best, best_epoch)."""
+    n = problem.y.shape[0]
+    params = np.ones(n + 1)
+    params[0] = init_alpha
+    m, v = np.zeros(n + 1), np.zeros(n + 1)
+    traj, best = [], (math.inf, None, -1)
+    for epoch in range(epochs + 1):
+        loss, ga, gh = problem.eval(float(params[0]), params[1:])
+        traj.append((loss, float(params[0])))
+        if loss < best[0]:
+            best = (loss, params.copy(), epoch)
+        if epoch < epochs:
+            params, m, v = adam_step(params, m, v, np.concatenate([[ga], gh]), epoch + 1, lr)
+    return traj, float(best[1][0]), best[1][1:], best[0], best[2]

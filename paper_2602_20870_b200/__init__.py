@@ -104,6 +104,10 @@ def lib() -> ctypes.CDLL:
         "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
         "fgfrft_cache_set_engine": (i, [vp, i]),
         "fgfrft_int8_digits": (i, []),
+        "fgfrft_denoise_create": (i, [vp, vp, vp, i64, pp]),
+        "fgfrft_denoise_destroy": (i, [vp]),
+        "fgfrft_denoise_eval": (i, [vp, d, vp, vp, vp, vp]),
+        "fgfrft_denoise_fit": (i, [vp, i, d, d, vp, vp, vp, vp, vp, vp, vp]),
         "fgfrft_cache_orthogonality": (i, [vp, vp]),
         "fgfrft_cache_prepare": (i, [vp]),
         "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
@@ -129,7 +133,8 @@ def exported_symbols():
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
         "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
         "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
-        "fgfrft_int8_digits", "fgfrft_cache_orthogonality",
+        "fgfrft_int8_digits", "fgfrft_cache_orthogonality", "fgfrft_denoise_create", "fgfrft_denoise_destroy",
+        "fgfrft_denoise_eval", "fgfrft_denoise_fit",
         "fgfrft_cache_prepare",
     ]
 
@@ -451,3 +456,49 @@ def dgemm_int8(a, b, slices: int = 0):
     _check(lib().fgfrft_dgemm_int8_dev(1, 1, m, n, k, a.data_ptr(), k, b.data_ptr(), n, ct.data_ptr(), m, slices,
                                        ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)))
     return ct.t()
+
+
+class DenoiseProblem:
+    """GPU-resident denoising learner (learn.hpp:291-516 on the device, real F): y, x_ref are
+    n x C real host arrays; eval(alpha, h) -> (loss, grad_alpha, grad_h); fit(...) runs Adam."""
+
+    def __init__(self, cache: PowerCache, y: np.ndarray, x_ref: np.ndarray):
+        y = np.asfortranarray(np.asarray(y, dtype=np.float64))
+        x = np.asfortranarray(np.asarray(x_ref, dtype=np.float64))
+        if y.shape != x.shape or y.shape[0] != cache.n():
+            raise ShapeError("denoise: signal shape mismatch")
+        self.n, self.ch = y.shape
+        self.cache = cache  # keeps the cache alive
+        self._h = ctypes.c_void_p()
+        _check(lib().fgfrft_denoise_create(cache.handle, y.ctypes.data, x.ctypes.data, self.ch,
+                                           ctypes.byref(self._h)))
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().fgfrft_denoise_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def eval(self, alpha: float, h: np.ndarray):
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        loss, ga = ctypes.c_double(), ctypes.c_double()
+        gh = np.empty(self.n)
+        _check(lib().fgfrft_denoise_eval(self._h, float(alpha), h.ctypes.data, ctypes.addressof(loss),
+                                         ctypes.addressof(ga), gh.ctypes.data))
+        return loss.value, ga.value, gh
+
+    def fit(self, epochs: int, lr: float = 0.01, init_alpha: float = 0.5, want_reconstruction: bool = False):
+        tl, ta = np.empty(epochs + 1), np.empty(epochs + 1)
+        hb = np.empty(self.n)
+        ab, lb, be = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        rec = np.empty((self.n, self.ch), order="F") if want_reconstruction else None
+        _check(lib().fgfrft_denoise_fit(self._h, int(epochs), float(lr), float(init_alpha), tl.ctypes.data,
+                                        ta.ctypes.data, ctypes.addressof(ab), hb.ctypes.data, ctypes.addressof(lb),
+                                        ctypes.addressof(be), rec.ctypes.data if rec is not None else None))
+        return {"traj_loss": tl, "traj_alpha": ta, "alpha_best": ab.value, "h_best": hb, "loss_best": lb.value,
+                "best_epoch": be.value, "reconstruction": rec}

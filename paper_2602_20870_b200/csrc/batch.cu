@@ -24,29 +24,6 @@ constexpr int kBMaxHeads = 4;
 constexpr int kBMaxCh = 64;
 constexpr int kBSlab = 4 * kTileElems;  // elements per padded slab
 
-// ---------------------------------------------------------------- device sinc (sinc.hpp:15-36)
-__device__ __forceinline__ double dsinc(double x) {
-    if (x == nearbyint(x)) return x == 0.0 ? 1.0 : 0.0;
-    if (fabs(x) < 1e-6) {
-        const double px = CUDART_PI * x;
-        return 1.0 - px * px / 6.0;
-    }
-    return sin(CUDART_PI * x) / (CUDART_PI * x);
-}
-__device__ __forceinline__ double dsinc_deriv(double x) {
-    if (x == nearbyint(x)) {
-        if (x == 0.0) return 0.0;
-        const long long k = (long long)x;
-        return (k % 2 == 0 ? 1.0 : -1.0) / x;
-    }
-    if (fabs(x) < 1e-6) {
-        const double pi2 = CUDART_PI * CUDART_PI;
-        return -pi2 * x / 3.0 + pi2 * pi2 * x * x * x / 30.0;
-    }
-    const double px = CUDART_PI * x;
-    return cos(px) / x - sin(px) / (CUDART_PI * x * x);
-}
-
 // coef[o][2][2l+1] (c then dc) for every order o.
 __global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_orders, int l, double* __restrict__ coef) {
     const int w = 2 * l + 1;

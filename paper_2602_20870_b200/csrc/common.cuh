@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #ifndef FGFRFT_SMS
 #define FGFRFT_SMS 148
@@ -115,6 +116,30 @@ __host__ __device__ __forceinline__ int64_t tile_base(int I, int J, int nt) {
     return ((int64_t)J * nt + I) * kTileElems;
 }
 __host__ __device__ __forceinline__ int swz(int i, int j) { return j * kTile + (i ^ j); }
+
+// ---------------------------------------------------------------- device sinc (sinc.hpp:15-36)
+// (device libm: within ~1 ulp of the host coefficients; used where orders live on the device)
+__device__ __forceinline__ double dsinc(double x) {
+    if (x == nearbyint(x)) return x == 0.0 ? 1.0 : 0.0;
+    if (fabs(x) < 1e-6) {
+        const double px = CUDART_PI * x;
+        return 1.0 - px * px / 6.0;
+    }
+    return sin(CUDART_PI * x) / (CUDART_PI * x);
+}
+__device__ __forceinline__ double dsinc_deriv(double x) {
+    if (x == nearbyint(x)) {
+        if (x == 0.0) return 0.0;
+        const long long k = (long long)x;
+        return (k % 2 == 0 ? 1.0 : -1.0) / x;
+    }
+    if (fabs(x) < 1e-6) {
+        const double pi2 = CUDART_PI * CUDART_PI;
+        return -pi2 * x / 3.0 + pi2 * pi2 * x * x * x / 30.0;
+    }
+    const double px = CUDART_PI * x;
+    return cos(px) / x - sin(px) / (CUDART_PI * x * x);
+}
 
 // ---------------------------------------------------------------- misc
 

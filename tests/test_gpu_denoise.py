@@ -1,0 +1,63 @@
+"""GPU-resident denoising learner: evaluations and short Adam fits against
+the oracle restatement of the reference's fast engine (learn.hpp:291-516, adam.hpp:34-53)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2602_20870_b200 as fg
+import prep
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(n, l, ch, seed):
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.08, seed)))
+    rng = np.random.default_rng(seed)
+    coef = np.zeros((n, ch))
+    coef[: n // 8] = rng.standard_normal((n // 8, ch))
+    x = f.real.T @ coef                       # smooth (band-limited) clean signals
+    y = x + 0.1 * rng.standard_normal((n, ch))
+    return f, x, y
+
+
+@pytest.mark.parametrize("n,l,ch", [(128, 8, 3), (256, 32, 16), (512, 64, 64)])
+def test_denoise_eval_matches_reference_engine(n, l, ch):
+    f, x, y = _problem(n, l, ch, 5 + n)
+    ref = O.FastDenoise(y, x, f.real, l)
+    g = fg.PowerCache(f, l)
+    dp = fg.DenoiseProblem(g, y, x)
+    rng = np.random.default_rng(n)
+    for alpha in (0.5, 0.83, -0.4):
+        h = 1.0 + 0.1 * rng.standard_normal(n)
+        loss, ga, gh = dp.eval(alpha, h)
+        lr, gar, ghr = ref.eval(alpha, h)
+        assert abs(loss - lr) <= 1e-10 * lr
+        assert abs(ga - gar) <= 1e-9 * max(1.0, abs(gar))
+        assert np.linalg.norm(gh - ghr) <= 1e-9 * np.linalg.norm(ghr)
+
+
+def test_denoise_fit_matches_reference_loop():
+    n, l, ch, epochs = 128, 16, 4, 12
+    f, x, y = _problem(n, l, ch, 77)
+    ref = O.FastDenoise(y, x, f.real, l)
+    traj, ab, hb, lb, be = O.denoise_fit(ref, epochs, 0.01, 0.5)
+    g = fg.PowerCache(f, l)
+    dp = fg.DenoiseProblem(g, y, x)
+    out = dp.fit(epochs, lr=0.01, init_alpha=0.5, want_reconstruction=True)
+    tl = np.array([t[0] for t in traj])
+    ta = np.array([t[1] for t in traj])
+    assert np.max(np.abs(out["traj_loss"] - tl) / tl) <= 1e-8
+    assert np.max(np.abs(out["traj_alpha"] - ta)) <= 1e-9
+    assert out["best_epoch"] == be
+    assert abs(out["alpha_best"] - ab) <= 1e-9 and abs(out["loss_best"] - lb) <= 1e-8 * lb
+    assert np.max(np.abs(out["h_best"] - hb)) <= 1e-8
+    rec = ref.reconstruct(ab, hb)
+    assert np.linalg.norm(out["reconstruction"] - rec) <= 1e-8 * np.linalg.norm(rec)
+    assert out["traj_loss"][-1] < out["traj_loss"][0]  # it learns
+
+
+def test_denoise_rejects_complex_f():
+    f = prep.random_unitary(64, 3)
+    g = fg.PowerCache(f, 4)
+    with pytest.raises(fg.ParameterError):
+        fg.DenoiseProblem(g, np.zeros((64, 2)), np.zeros((64, 2)))
