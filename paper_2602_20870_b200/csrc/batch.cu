@@ -135,7 +135,8 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
 #pragma unroll
         for (int h = 0; h < H; ++h) regA[(size_t)h * kBN * kBN + (j0 + 8 * u) * kBN + i] = q[u][h];
     __syncthreads();
-    // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: thread -> rows 4*ib..4*ib+3, cols 2*cb, 2*cb+1
+    // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: thread -> rows 2ib, 2ib+1, 32+2ib, 33+2ib and cols 2cb, 2cb+1
+    // (the 16 lanes of a half-warp read 256 contiguous bytes of a Q column per LDS.128: conflict-free)
     const int ib = tid & 15, cb = tid >> 4;
     float acc[H][4][2][2];
 #pragma unroll
@@ -148,8 +149,8 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
         const float2 x0 = xs[(2 * cb) * kBN + j], x1 = xs[(2 * cb + 1) * kBN + j];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            const float4* qp = reinterpret_cast<const float4*>(regA + (size_t)h * kBN * kBN + j * kBN + 4 * ib);
-            const float4 v0 = qp[0], v1 = qp[1];
+            const float4* qp = reinterpret_cast<const float4*>(regA + (size_t)h * kBN * kBN + j * kBN + 2 * ib);
+            const float4 v0 = qp[0], v1 = qp[16];
             const float2 qv[4] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
                                   make_float2(v1.z, v1.w)};
 #pragma unroll
@@ -171,7 +172,7 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
             float2* yo = y + (((int64_t)g * H + h) * ch + col) * n;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const int row = 4 * ib + r;
+                const int row = 2 * ib + (r & 1) + 32 * (r >> 1);
                 if (row < n) yo[row] = make_float2(acc[h][r][c][0], acc[h][r][c][1]);
             }
         }
@@ -255,19 +256,24 @@ batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* 
         const int s = (k - 1) % kBStages;
         mbar_wait(&full[s], ((k - 1) / kBStages) & 1);
         const float2* t = regA + (size_t)s * kBSlab;
-        double v[8];  // [h][+/-] packed as 2h + sign
+        // [h][+/-] packed as 2h + sign; the thread's 8 terms are summed in FP32 (one F2F per value
+        // instead of one per product), the cross-thread reduction is FP64
+        float vf[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = 0.0;
+        for (int q = 0; q < 8; ++q) vf[q] = 0.f;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int j = j0 + 8 * u;
             const float2 p = t[bidx(i, j)], pt = t[bidx(j, i)];
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                v[2 * h] += (double)fmaf(m[u][h].x, p.x, m[u][h].y * p.y);
-                v[2 * h + 1] += (double)fmaf(m[u][h].x, pt.x, -m[u][h].y * pt.y);
+                vf[2 * h] += fmaf(m[u][h].x, p.x, m[u][h].y * p.y);
+                vf[2 * h + 1] += fmaf(m[u][h].x, pt.x, -m[u][h].y * pt.y);
             }
         }
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = (double)vf[q];
         // transposing warp reduction of 8 values: lane q (< 8) ends with the sum of value q
 #pragma unroll
         for (int o = 4, half = 4; o >= 1; o >>= 1, half >>= 1) {
