@@ -20,7 +20,7 @@
  * Mapping to the reference exception taxonomy (proj/include/fgfrft/errors.hpp:36-62):
  *   FGFRFT_PARAMETER -> parameter_error, FGFRFT_SHAPE -> shape_error,
  *   FGFRFT_CAPACITY -> capacity_error, FGFRFT_NUMERICAL / FGFRFT_CUDA / FGFRFT_NCCL ->
- *   numerical_error.
+ *   numerical_error, FGFRFT_OPTIMIZER -> optimizer_error (a numerical_error).
  *
  * Threading: calls on one handle are serialised by the handle; distinct handles may be
  * used concurrently. Every call is synchronous with respect to host buffers. Calls taking
@@ -44,7 +44,8 @@ typedef enum fgfrft_status {
     FGFRFT_CAPACITY = 3,
     FGFRFT_NUMERICAL = 4,
     FGFRFT_CUDA = 5,
-    FGFRFT_NCCL = 6
+    FGFRFT_NCCL = 6,
+    FGFRFT_OPTIMIZER = 7 /* non-finite loss / gradient in a learner (optimizer_error) */
 } fgfrft_status;
 
 typedef enum fgfrft_dtype { FGFRFT_C128 = 0, FGFRFT_C64 = 1 } fgfrft_dtype;
@@ -277,6 +278,51 @@ int fgfrft_denoise_eval(fgfrft_denoise* problem, double alpha, const double* h, 
 int fgfrft_denoise_fit(fgfrft_denoise* problem, int epochs, double lr, double init_alpha,
                        double* traj_loss, double* traj_alpha, double* alpha_best, double* h_best,
                        double* loss_best, int* best_epoch, double* reconstruction);
+
+/* ---- spectral form and the exact GFRFT (spectral.hpp:19-195) ------------------------------
+ *
+ * fgfrft_spectrum holds F = V diag(e^{j theta}) V^H on a device: V n x n complex128, theta
+ * ascending in (-pi, pi]. create: a recorded spectrum (KnownSpectrum, gft.hpp:21-25), stored as
+ * given. decompose: eigendecompose_unitary (spectral.hpp:121-155) of a host F -- Hermitian part
+ * (F + F^H)/2 by cuSOLVER (real F: the real symmetric solver), clusters of cos(theta) within 1e-5
+ * rediagonalised against -i (F - F^H)/2, phases from Rayleigh quotients, sorted ascending, and
+ * the reconstruction residual checked (> 1e-6 -> FGFRFT_NUMERICAL). theta is returned by
+ * spectrum_info (n doubles), V by spectrum_vectors (n x n complex128).
+ * exact[_dev]: out[a] = V diag(e^{j a theta}) V^H (FGFRFT_Q, exact_gfrft, spectral.hpp:158-166) or
+ * V diag(j theta e^{j a theta}) V^H (FGFRFT_DQ, exact_gfrft_grad, :169-174) for every order; one
+ * column scaling and one FP64 tensor-core GEMM per order. out: n_alpha blocks of n x n.
+ */
+typedef struct fgfrft_spectrum fgfrft_spectrum;
+int fgfrft_spectrum_create(const double* v, const double* theta, int64_t n, int device,
+                           fgfrft_spectrum** out);
+int fgfrft_spectrum_decompose(const double* f, int64_t n, int device, fgfrft_spectrum** out);
+int fgfrft_spectrum_destroy(fgfrft_spectrum* spectrum);
+int fgfrft_spectrum_info(const fgfrft_spectrum* spectrum, int64_t* n, double* theta);
+int fgfrft_spectrum_vectors(fgfrft_spectrum* spectrum, double* v);
+int fgfrft_spectrum_set_stream(fgfrft_spectrum* spectrum, void* stream);
+int fgfrft_exact(fgfrft_spectrum* spectrum, const double* alphas, int n_alpha, int which, double* out);
+int fgfrft_exact_dev(fgfrft_spectrum* spectrum, const double* alphas, int n_alpha, int which,
+                     void* out_dev);
+
+/* ---- cascaded transform-order learning (learn.hpp:29-166) ----------------------------------
+ *
+ * CascadeProblem on the device: Yhat = Q_K ... Q_1 (X = I), target F^{target_order} (exact, from
+ * the spectrum), loss = |Yhat - target|_F^2 / N^2, per-layer gradients accumulated in reverse
+ * through the product (learn.hpp:72-97). Backend fast: Q_l, dQ_l/dalpha synthesised from `cache`
+ * (complex128); exact: cache == NULL, Q_l and dQ_l from the spectrum. All products are FP64
+ * tensor-core complex GEMMs; the gradient of layer l is 2/N^2 Re<b prefix_{l-1}^H, dQ_l>.
+ * learn: learn_orders (learn.hpp:124-166), Adam (lr, 0.9, 0.999, 1e-8) from init_order for
+ * `epochs` steps plus a final evaluation; traj_loss has epochs + 1 entries, traj_alphas
+ * (epochs + 1) x depth. Non-finite loss or gradient -> FGFRFT_OPTIMIZER.
+ */
+typedef struct fgfrft_cascade fgfrft_cascade;
+int fgfrft_cascade_create(fgfrft_cache* cache, fgfrft_spectrum* spectrum, double target_order, int depth,
+                          fgfrft_cascade** out);
+int fgfrft_cascade_destroy(fgfrft_cascade* problem);
+int fgfrft_cascade_eval(fgfrft_cascade* problem, const double* alphas, double* loss, double* grad);
+int fgfrft_cascade_learn(fgfrft_cascade* problem, double init_order, int epochs, double lr,
+                         double* traj_loss, double* traj_alphas, double* final_loss,
+                         double* final_alphas);
 
 /* ---- batches of small graphs (BASELINE config 5: fractional specformer) ----------------
  *

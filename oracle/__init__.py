@@ -22,6 +22,7 @@ Restated reference functions (file:line under /root/reference/proj/include/fgfrf
   phase_margin                       spectral.hpp:179-195
   matrix_errors                      metrics.hpp:21-34
   cascade dL/dalpha (K=1)            learn.hpp:88-92
+  Cascade / learn_orders             learn.hpp:55-166 (any depth, fast and exact backends)
   FastDenoiseEngine (real F), Adam   learn.hpp:291-413, learn.hpp:471-516, adam.hpp:34-53
 """
 from __future__ import annotations
@@ -478,3 +479,68 @@ def denoise_fit(problem: FastDenoise, epochs: int, lr: float, init_alpha: float)
         if epoch < epochs:
             params, m, v = adam_step(params, m, v, np.concatenate([[ga], gh]), epoch + 1, lr)
     return traj, float(best[1][0]), best[1][1:], best[0], best[2]
+
+
+# ----------------------------------------------------------------------------- learn.hpp cascade
+
+class Cascade:
+    """learn.hpp:55-116 (CascadeProblem): Yhat = Q_K ... Q_1 (X = I), target = exact
+    F^{target_order}, loss = |Yhat - target|^2 / N^2, reverse-accumulated order gradients.
+    backend "fast": Q from fgfrft_matrix / fgfrft_grad of a PowerCache; "exact": exact_gfrft."""
+
+    def __init__(self, f, depth: int, target_order: float, truncation: int, backend: str = "fast", eig=None,
+                 cache=None):
+        if depth < 1 or truncation < 1:
+            raise ParameterError("CascadeConfig: depth and truncation must be >= 1")
+        self.n = f.shape[0]
+        self.eig = eig if eig is not None else eigendecompose_unitary(f)
+        self.target = exact_gfrft(self.eig, target_order)  # learn.hpp:61
+        self.backend = backend
+        self.cache = None
+        if backend == "fast":
+            self.cache = cache if cache is not None else PowerCache(np.asarray(f, dtype=np.complex128), truncation)
+
+    def _op(self, a):
+        return fgfrft_matrix(self.cache, a) if self.backend == "fast" else exact_gfrft(self.eig, a)
+
+    def _grad_op(self, a):
+        return fgfrft_grad(self.cache, a) if self.backend == "fast" else exact_gfrft_grad(self.eig, a)
+
+    def eval(self, alphas):
+        """learn.hpp:72-97."""
+        k = len(alphas)
+        nn = float(self.n) * float(self.n)
+        ops = [self._op(float(a)) for a in alphas]
+        prefix = []
+        for l in range(k):
+            prefix.append(ops[0] if l == 0 else ops[l] @ prefix[l - 1])
+        resid = prefix[k - 1] - self.target
+        loss = float(np.vdot(resid, resid).real) / nn
+        grad = np.empty(k)
+        b = resid
+        for l in range(k - 1, -1, -1):
+            dq = self._grad_op(float(alphas[l]))
+            dyhat = dq if l == 0 else dq @ prefix[l - 1]
+            grad[l] = 2.0 / nn * float(np.sum(b.conj() * dyhat).real)
+            if l > 0:
+                b = ops[l].conj().T @ b
+        return loss, grad
+
+
+def learn_orders(problem: Cascade, depth: int, init_order: float, epochs: int, lr: float):
+    """learn.hpp:124-166: Adam from init_order; returns (traj_loss [epochs+1], traj_alphas
+    [epochs+1, depth], final_loss, final_alphas)."""
+    params = np.full(depth, float(init_order))
+    m, v = np.zeros(depth), np.zeros(depth)
+    tl, ta = [], []
+    for epoch in range(epochs):
+        loss, grad = problem.eval(params)
+        if not math.isfinite(loss):
+            raise NumericalError(f"learn_orders: non-finite loss at epoch {epoch}")
+        tl.append(loss)
+        ta.append(params.copy())
+        params, m, v = adam_step(params, m, v, grad, epoch + 1, lr)
+    loss, _ = problem.eval(params)
+    tl.append(loss)
+    ta.append(params.copy())
+    return np.array(tl), np.array(ta), loss, params

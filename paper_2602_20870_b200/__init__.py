@@ -47,8 +47,12 @@ class NumericalError(ArithmeticError):
     """errors.hpp:48 numerical_error (also CUDA / NCCL failures)."""
 
 
+class OptimizerError(NumericalError):
+    """errors.hpp optimizer_error: non-finite loss or gradient inside a learner."""
+
+
 _STATUS = {1: ParameterError, 2: ShapeError, 3: CapacityError, 4: NumericalError, 5: NumericalError,
-           6: NumericalError}
+           6: NumericalError, 7: OptimizerError}
 
 _LIB = None
 
@@ -111,6 +115,18 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cache_orthogonality": (i, [vp, vp]),
         "fgfrft_cache_prepare": (i, [vp]),
         "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
+        "fgfrft_spectrum_create": (i, [vp, vp, i64, i, pp]),
+        "fgfrft_spectrum_decompose": (i, [vp, i64, i, pp]),
+        "fgfrft_spectrum_destroy": (i, [vp]),
+        "fgfrft_spectrum_info": (i, [vp, vp, vp]),
+        "fgfrft_spectrum_vectors": (i, [vp, vp]),
+        "fgfrft_spectrum_set_stream": (i, [vp, vp]),
+        "fgfrft_exact": (i, [vp, vp, i, i, vp]),
+        "fgfrft_exact_dev": (i, [vp, vp, i, i, vp]),
+        "fgfrft_cascade_create": (i, [vp, vp, d, i, pp]),
+        "fgfrft_cascade_destroy": (i, [vp]),
+        "fgfrft_cascade_eval": (i, [vp, vp, vp, vp]),
+        "fgfrft_cascade_learn": (i, [vp, d, i, d, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -135,7 +151,10 @@ def exported_symbols():
         "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
         "fgfrft_int8_digits", "fgfrft_cache_orthogonality", "fgfrft_denoise_create", "fgfrft_denoise_destroy",
         "fgfrft_denoise_eval", "fgfrft_denoise_fit",
-        "fgfrft_cache_prepare",
+        "fgfrft_cache_prepare", "fgfrft_spectrum_create", "fgfrft_spectrum_decompose", "fgfrft_spectrum_destroy",
+        "fgfrft_spectrum_info", "fgfrft_spectrum_vectors", "fgfrft_spectrum_set_stream", "fgfrft_exact",
+        "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
+        "fgfrft_cascade_learn",
     ]
 
 
@@ -502,3 +521,172 @@ class DenoiseProblem:
                                         ctypes.addressof(be), rec.ctypes.data if rec is not None else None))
         return {"traj_loss": tl, "traj_alpha": ta, "alpha_best": ab.value, "h_best": hb, "loss_best": lb.value,
                 "best_epoch": be.value, "reconstruction": rec}
+
+
+# ----------------------------------------------------------------------------- spectral.hpp / learn.hpp
+
+
+class UnitaryEigen:
+    """spectral.hpp:19-31 on the GPU: F = V diag(e^{j theta}) V^H, V resident in HBM.
+
+    ``UnitaryEigen(v=..., theta=...)`` stores a recorded spectrum (KnownSpectrum);
+    ``eigendecompose_unitary(f)`` computes one on the device."""
+
+    def __init__(self, v: Optional[np.ndarray] = None, theta: Optional[np.ndarray] = None, device: int = 0,
+                 _handle=None):
+        self._h = ctypes.c_void_p()
+        if _handle is not None:
+            self._h = _handle
+        else:
+            vc = _cm(v)
+            th = np.ascontiguousarray(theta, dtype=np.float64)
+            if vc.shape[0] != vc.shape[1] or th.shape != (vc.shape[0],):
+                raise ShapeError("spectrum: V must be n x n and theta of length n")
+            _check(lib().fgfrft_spectrum_create(_ptr(vc), _ptr(th), vc.shape[0], device, ctypes.byref(self._h)))
+        n = ctypes.c_int64()
+        _check(lib().fgfrft_spectrum_info(self._h, ctypes.addressof(n), None))
+        self._n = n.value
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def n(self) -> int:
+        return self._n
+
+    @property
+    def theta(self) -> np.ndarray:
+        th = np.empty(self._n)
+        _check(lib().fgfrft_spectrum_info(self._h, None, _ptr(th)))
+        return th
+
+    @property
+    def v(self) -> np.ndarray:
+        buf = np.empty((self._n, self._n), dtype=np.complex128)  # row-major buffer of V^T
+        _check(lib().fgfrft_spectrum_vectors(self._h, _ptr(buf)))
+        return buf.T
+
+    def eigenvalues(self) -> np.ndarray:
+        return np.exp(1j * self.theta)
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().fgfrft_spectrum_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def eigendecompose_unitary(f: np.ndarray, device: int = 0) -> UnitaryEigen:
+    """spectral.hpp:121-155 with the large products and the Hermitian eigensolve on the GPU."""
+    fc = _cm(f)
+    if fc.shape[0] != fc.shape[1]:
+        raise ShapeError("eigendecompose_unitary: F must be square")
+    h = ctypes.c_void_p()
+    _check(lib().fgfrft_spectrum_decompose(_ptr(fc), fc.shape[0], device, ctypes.byref(h)))
+    return UnitaryEigen(device=device, _handle=h)
+
+
+def exact_matrices(eig: UnitaryEigen, alphas, which: int = Q) -> np.ndarray:
+    """[A, n, n]: V diag(e^{j a theta}) V^H (which Q) or its a-derivative (DQ) for every order."""
+    al = _alphas(alphas)
+    buf = np.empty((len(al), eig.n(), eig.n()), dtype=np.complex128)
+    _check(lib().fgfrft_exact(eig.handle, _ptr(al), len(al), which, _ptr(buf)))
+    return np.transpose(buf, (0, 2, 1))
+
+
+def exact_gfrft(eig: UnitaryEigen, alpha: float) -> FracOperator:
+    """spectral.hpp:158-166."""
+    return FracOperator(exact_matrices(eig, [alpha], Q)[0], float(alpha), 0)
+
+
+def exact_gfrft_grad(eig: UnitaryEigen, alpha: float) -> np.ndarray:
+    """spectral.hpp:169-174."""
+    return exact_matrices(eig, [alpha], DQ)[0]
+
+
+def phase_margin(eig: UnitaryEigen) -> float:
+    """spectral.hpp:179-195 (min_k pi - |theta_k|, warning below 0.05 pi)."""
+    margin = float(np.min(np.pi - np.abs(eig.theta))) if eig.n() else float(np.pi)
+    margin = min(margin, float(np.pi))
+    if margin < 0.05 * np.pi:
+        warnings.warn(f"phase margin {margin} is below 0.05*pi; series approximation accuracy is at risk")
+    return margin
+
+
+FAST, EXACT = "fast", "exact"
+
+
+class CascadeProblem:
+    """learn.hpp:55-116 on the GPU. ``backend`` "fast" synthesises the layer operators from a
+    PowerCache of F (built here with ``truncation`` unless ``cache`` is given); "exact" uses the
+    spectrum. eval(alphas) -> (loss, grad)."""
+
+    def __init__(self, f: Optional[np.ndarray], depth: int = 1, target_order: float = 1.5, truncation: int = 10,
+                 backend: str = FAST, memory_budget: int = DEFAULT_MEMORY_BUDGET, eig: Optional[UnitaryEigen] = None,
+                 cache: Optional[PowerCache] = None, device: int = 0):
+        if depth < 1:
+            raise ParameterError("CascadeConfig: depth must be >= 1")
+        if truncation < 1:
+            raise ParameterError("CascadeConfig: truncation must be >= 1")
+        if backend not in (FAST, EXACT):
+            raise ParameterError(f"unknown backend {backend!r}")
+        self.eig = eig if eig is not None else eigendecompose_unitary(f, device)
+        self.cache = None
+        if backend == FAST:
+            self.cache = cache if cache is not None else PowerCache(f, truncation, memory_budget, device=device)
+        self.depth, self.backend = int(depth), backend
+        self._h = ctypes.c_void_p()
+        _check(lib().fgfrft_cascade_create(self.cache.handle if self.cache is not None else None, self.eig.handle,
+                                           float(target_order), self.depth, ctypes.byref(self._h)))
+
+    def n(self) -> int:
+        return self.eig.n()
+
+    def eval(self, alphas):
+        al = _alphas(alphas)
+        if len(al) != self.depth:
+            raise ShapeError("cascade: need one order per layer")
+        loss, grad = ctypes.c_double(), np.empty(self.depth)
+        _check(lib().fgfrft_cascade_eval(self._h, _ptr(al), ctypes.addressof(loss), _ptr(grad)))
+        return loss.value, grad
+
+    def learn(self, init_order: float = 0.1, epochs: int = 200, lr: float = 0.01):
+        """learn_orders (learn.hpp:124-166): trajectory of (loss, alphas) for epochs + 1 points."""
+        tl = np.empty(epochs + 1) if epochs >= 1 else np.empty(1)
+        ta = np.empty((max(epochs, 0) + 1, self.depth))
+        fl, fa = ctypes.c_double(), np.empty(self.depth)
+        _check(lib().fgfrft_cascade_learn(self._h, float(init_order), int(epochs), float(lr), _ptr(tl), _ptr(ta),
+                                          ctypes.addressof(fl), _ptr(fa)))
+        return {"traj_loss": tl, "traj_alphas": ta, "final_loss": fl.value, "final_alphas": fa,
+                "final_alpha_sum": float(fa.sum())}
+
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().fgfrft_cascade_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def learn_orders(f: np.ndarray, depth: int = 1, init_order: float = 0.1, target_order: float = 1.5,
+                 truncation: int = 10, epochs: int = 200, lr: float = 0.01, backend: str = FAST, device: int = 0):
+    """learn.hpp:124-166 (CascadeConfig fields as keyword arguments)."""
+    if epochs < 1:
+        raise ParameterError("CascadeConfig: epochs must be >= 1")
+    if not lr > 0:
+        raise ParameterError("CascadeConfig: lr must be positive")
+    prob = CascadeProblem(f, depth, target_order, truncation, backend, device=device)
+    try:
+        return prob.learn(init_order, epochs, lr)
+    finally:
+        prob.close()

