@@ -11,9 +11,16 @@ namespace fgfrft {
 
 enum class Provenance { graph, haar, synthetic };
 
+// Eigenbasis and eigenphases recorded at construction time (gft.hpp:21-25).
+struct KnownSpectrum {
+    MatrixXcd v;     // unitary eigenvector matrix
+    VectorXd theta;  // phases in (-pi, pi)
+};
+
 struct GftMatrix {
     MatrixXcd f;
     Provenance provenance = Provenance::graph;
+    std::optional<KnownSpectrum> known_spectrum;
 
     Index n() const { return f.rows(); }
 

@@ -13,6 +13,7 @@
 #include <Eigen/Dense>
 namespace fgfrft {
 using MatrixXcd = Eigen::MatrixXcd;
+using VectorXd = Eigen::VectorXd;
 using Index = Eigen::Index;
 }  // namespace fgfrft
 #define FGFRFT_HAVE_EIGEN 1
@@ -96,6 +97,35 @@ class MatrixXcd {
   private:
     Index r_ = 0, c_ = 0;
     std::vector<Scalar> d_;
+};
+
+// Real vector with the Eigen::VectorXd members the learning API uses.
+class VectorXd {
+  public:
+    VectorXd() = default;
+    explicit VectorXd(Index n) : d_(static_cast<size_t>(n), 0.0) {}
+    static VectorXd Zero(Index n) { return VectorXd(n); }
+    static VectorXd Constant(Index n, double v) {
+        VectorXd x(n);
+        for (auto& e : x.d_) e = v;
+        return x;
+    }
+    Index size() const { return static_cast<Index>(d_.size()); }
+    double* data() { return d_.data(); }
+    const double* data() const { return d_.data(); }
+    double& operator()(Index i) { return d_[static_cast<size_t>(i)]; }
+    const double& operator()(Index i) const { return d_[static_cast<size_t>(i)]; }
+    double& operator[](Index i) { return d_[static_cast<size_t>(i)]; }
+    const double& operator[](Index i) const { return d_[static_cast<size_t>(i)]; }
+    void resize(Index n) { d_.assign(static_cast<size_t>(n), 0.0); }
+    double sum() const {
+        double s = 0.0;
+        for (double v : d_) s += v;
+        return s;
+    }
+
+  private:
+    std::vector<double> d_;
 };
 
 }  // namespace fgfrft

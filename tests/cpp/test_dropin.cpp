@@ -296,6 +296,88 @@ int main() {
         const std::vector<MatrixXcd> qs = fgfrft_matrices(cache, {0.0, 1.0});
         CHECK(qs[0] == fgfrft_matrix(cache, 0.0).q && qs[1] == fgfrft_matrix(cache, 1.0).q);
     }
+    // spectral.hpp: test_spectral.cpp:34-71, 96-127 through the drop-in header
+    {
+        const GftMatrix f = householder_unitary(24, 3);
+        const UnitaryEigen e = eigendecompose_unitary(f);
+        bool ascending = true;
+        for (Index k = 1; k < e.theta.size(); ++k) ascending = ascending && e.theta(k - 1) <= e.theta(k);
+        CHECK(ascending);
+        CHECK(fro(sub(mul(adj(e.v), e.v), eye(24))) <= 1e-12 * std::sqrt(24.0));
+        MatrixXcd vd = e.v;
+        for (Index j = 0; j < 24; ++j)
+            for (Index i = 0; i < 24; ++i) vd(i, j) *= std::polar(1.0, e.theta(j));
+        CHECK(fro(sub(mul(f.f, e.v), vd)) <= 1e-9 * fro(f.f));
+        CHECK(fro(sub(exact_gfrft(e, 1.0).q, f.f)) <= 1e-12 * fro(f.f));
+        CHECK(fro(sub(exact_gfrft(e, 0.0).q, eye(24))) <= 1e-13 * std::sqrt(24.0));
+        CHECK(fro(sub(exact_gfrft(e, 2.0).q, mul(f.f, f.f))) <= 1e-12 * fro(f.f));
+        const MatrixXcd fd = (exact_gfrft(e, 0.6 + 1e-4).q - exact_gfrft(e, 0.6 - 1e-4).q) * (1.0 / 2e-4);
+        CHECK(fro(sub(exact_gfrft_grad(e, 0.6), fd)) <= 1e-6 * fro(fd));
+        GftMatrix rot;
+        rot.f = MatrixXcd(2, 2);
+        const double c = std::cos(M_PI / 4), s = std::sin(M_PI / 4);
+        rot.f(0, 0) = c;
+        rot.f(0, 1) = -s;
+        rot.f(1, 0) = s;
+        rot.f(1, 1) = c;
+        const UnitaryEigen er = eigendecompose_unitary(rot);
+        CHECK(std::fabs(er.theta(0) + M_PI / 4) <= 1e-14 && std::fabs(er.theta(1) - M_PI / 4) <= 1e-14);
+        GftMatrix known = f;
+        known.known_spectrum = KnownSpectrum{e.v, e.theta};
+        const UnitaryEigen ek = eigendecompose_unitary(known);
+        CHECK(ek.v == e.v);
+        CHECK(fro(sub(exact_gfrft(ek, 0.37).q, exact_gfrft(e, 0.37).q)) <= 1e-13 * std::sqrt(24.0));
+        MatrixXcd bad = eye(8);
+        bad(0, 1) = 0.5;
+        GftMatrix gb;
+        gb.f = bad;
+        CHECK_THROWS_AS(eigendecompose_unitary(gb), numerical_error);
+    }
+    // learn.hpp cascade: test_learn.cpp:62-102
+    {
+        const GftMatrix f = householder_unitary(24, 3);
+        for (Backend backend : {Backend::fast, Backend::exact}) {
+            for (int k : {1, 3}) {
+                CascadeConfig cfg;
+                cfg.depth = k;
+                cfg.truncation = 8;
+                const CascadeProblem problem(f, cfg, backend);
+                std::mt19937_64 gen(71 + k);
+                std::uniform_real_distribution<double> ud(-0.5, 1.8);
+                for (int state = 0; state < 5; ++state) {
+                    VectorXd alphas(k);
+                    for (int l = 0; l < k; ++l) alphas(l) = ud(gen);
+                    const auto ev = problem.eval(alphas);
+                    for (int l = 0; l < k; ++l) {
+                        VectorXd ap = alphas, am = alphas;
+                        ap(l) += 1e-4;
+                        am(l) -= 1e-4;
+                        const double fdl = (problem.eval(ap).loss - problem.eval(am).loss) / 2e-4;
+                        CHECK(std::fabs(ev.grad(l) - fdl) / std::max(std::fabs(fdl), 1e-12) <= 1e-5);
+                    }
+                }
+            }
+        }
+        CascadeConfig cfg;
+        cfg.depth = 1;
+        cfg.init_order = 0.7;
+        cfg.target_order = 0.7;
+        cfg.epochs = 10;
+        const OrderLearnResult res = learn_orders(householder_unitary(20, 8), cfg, Backend::exact);
+        CHECK(res.final_loss == 0.0);
+        CHECK(res.trajectory.size() == 11);
+        for (const OrderTrajectoryPoint& p : res.trajectory) CHECK(p.loss == 0.0 && p.alphas[0] == 0.7);
+        CascadeConfig c2;
+        c2.depth = 2;
+        c2.truncation = 30;
+        const OrderLearnResult r2 = learn_orders(householder_unitary(48, 21), c2, Backend::fast);
+        std::printf("cascade k=2 fast: final loss %.3e, sum(alpha) %.5f\n", r2.final_loss, r2.final_alpha_sum);
+        CHECK(std::fabs(r2.final_alpha_sum - 1.5) <= 0.01);
+        CHECK(r2.trajectory.back().loss < r2.trajectory.front().loss);
+        CascadeConfig bad;
+        bad.depth = 0;
+        CHECK_THROWS_AS(learn_orders(f, bad, Backend::fast), parameter_error);
+    }
     std::printf("drop-in C++ tests: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }
