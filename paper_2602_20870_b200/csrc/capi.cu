@@ -99,8 +99,9 @@ cudaError_t launch_eig_residual(const void* fw, const void* w, const double* the
                                 double* part, double* out2, cudaStream_t st);
 cudaError_t launch_spec_scale(const void* v, const double* theta, const double* alphas, int na, int which, int n,
                               void* w, cudaStream_t st);
-cudaError_t launch_cdiff_sq(const void* y, const void* t, int64_t count, void* b, double* part, cudaStream_t st);
-cudaError_t launch_cre_dot(const void* m, const void* d, int64_t count, double* part, cudaStream_t st);
+cudaError_t launch_cdiff_sq(const void* y, bool real_y, const void* t, int64_t count, void* b, double* part,
+                            cudaStream_t st);
+cudaError_t launch_cre_dot(const void* m, const void* d, bool real_d, int64_t count, double* part, cudaStream_t st);
 cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s1, double* out, cudaStream_t st);
 size_t dots_partial_elems(int n, int l, int n_alpha);
 size_t dots_mma_partial_elems(int n);
@@ -2759,52 +2760,82 @@ void spectrum_free(fgfrft_spectrum* s) {
 
 // loss and per-layer gradients at the host orders: out_host[0] = loss, out_host[1 + l] = grad_l.
 //   forward: prefix_l = Q_l prefix_{l-1}, resid = prefix_{K-1} - target, loss = |resid|^2 / N^2
-//   reverse: grad_l = 2/N^2 Re<b, dQ_l prefix_{l-1}> = 2/N^2 Re<b prefix_{l-1}^H, dQ_l>,
-//            b <- Q_l^H b                                           (learn.hpp:72-97)
+//   reverse: grad_l = 2/N^2 Re<b, dQ_l prefix_{l-1}>, b <- Q_l^H b           (learn.hpp:72-97)
+// Complex F: Re<b, dQ X> is taken as Re<b X^H, dQ> (complex GEMMs on the FP64 tensor cores).
+// Real F (fast backend): Q_l, dQ_l and the prefixes are real, so the products are real DMMA GEMMs
+// (dQ_l prefix_{l-1} real x real, Q_l^T b real x complex): a third of the complex flops.
 int cascade_eval_device(fgfrft_cascade* cs, const double* alphas, double* out_host) {
     const int K = cs->k;
     const int n = (int)cs->n;
     const size_t nn = (size_t)n * n;
     cudaStream_t st = cs->stream();
-    double2* ops = cs->ops.as<double2>();
-    double2* dops = cs->dops.as<double2>();
+    const bool real = cs->cache && cs->cache->real;
+    const size_t es = real ? 8 : 16;
+    char* ops = cs->ops.as<char>();
+    char* dops = cs->dops.as<char>();
     if (cs->cache) {
         fgfrft_cache* c = cs->cache;
         double* coef = nullptr;
         if (int e = upload_coefs(c, alphas, K, c->l, &coef)) return e;
-        if (int e = synth_into(c, coef, K, c->l, ops)) return e;
-        if (int e = synth_into(c, coef + (size_t)K * (2 * c->l + 1), K, c->l, dops)) return e;
+        if (int e = synth_into(c, coef, K, c->l, ops, real)) return e;
+        if (int e = synth_into(c, coef + (size_t)K * (2 * c->l + 1), K, c->l, dops, real)) return e;
     } else {
         if (int e = exact_into(cs->spec, alphas, K, FGFRFT_Q, ops, st)) return e;
         if (int e = exact_into(cs->spec, alphas, K, FGFRFT_DQ, dops, st)) return e;
     }
-    auto prefix = [&](int l) { return l == 0 ? ops : cs->prefix.as<double2>() + (size_t)l * nn; };
-    for (int l = 1; l < K; ++l) {
+    auto op = [&](char* base, int l) { return static_cast<void*>(base + (size_t)l * nn * es); };
+    auto prefix = [&](int l) { return l == 0 ? op(ops, 0) : op(cs->prefix.as<char>(), l); };
+    // real x real products: INT8 Ozaki engine where the cache's engine selects it, else DMMA
+    const bool i8 = real && use_int8_gemm(cs->cache, n);
+    auto real_mm = [&](const void* a, const void* bb, void* cc) -> int {
+        if (i8)
+            return fgfrft_dgemm_int8_dev(0, 0, n, n, n, static_cast<const double*>(a), n,
+                                         static_cast<const double*>(bb), n, static_cast<double*>(cc), n, 0, st);
         ProfScope ps(KC_GEMM, st);
-        FGB_LAUNCH(launch_zgemm(n, n, n, ops + (size_t)l * nn, n, 0, false, prefix(l - 1), n, 0, false, prefix(l), n,
-                                0, 1, false, st),
+        FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, a, n, 0, bb, n, 0, cc, n, 0, 1, st), 1);
+        return FGFRFT_OK;
+    };
+    for (int l = 1; l < K; ++l) {
+        if (real) {
+            if (int e = real_mm(op(ops, l), prefix(l - 1), prefix(l))) return e;
+            continue;
+        }
+        ProfScope ps(KC_GEMM, st);
+        FGB_LAUNCH(launch_zgemm(n, n, n, op(ops, l), n, 0, false, prefix(l - 1), n, 0, false, prefix(l), n, 0, 1,
+                                false, st),
                    1);
     }
     double* part = cs->part.as<double>();
     const size_t G = sp_part_elems();
     double2* b = cs->b.as<double2>();
     double2* nb = cs->nb.as<double2>();
-    FGB_LAUNCH(launch_cdiff_sq(prefix(K - 1), cs->target.p, (int64_t)nn, b, part, st), 1);
+    FGB_LAUNCH(launch_cdiff_sq(prefix(K - 1), real, cs->target.p, (int64_t)nn, b, part, st), 1);
     for (int l = K - 1; l >= 0; --l) {
         if (l > 0) {
             {
                 ProfScope ps(KC_GEMM, st);
-                FGB_LAUNCH(launch_zgemm(n, n, n, b, n, 0, false, prefix(l - 1), n, 0, true, cs->m.p, n, 0, 1, false,
-                                        st),
-                           1);
+                if (real) {  // dY = dQ_l prefix_{l-1}
+                    if (int e = real_mm(op(dops, l), prefix(l - 1), cs->m.p)) return e;
+                } else {  // M = b prefix_{l-1}^H
+                    FGB_LAUNCH(launch_zgemm(n, n, n, b, n, 0, false, prefix(l - 1), n, 0, true, cs->m.p, n, 0, 1,
+                                            false, st),
+                               1);
+                }
             }
-            FGB_LAUNCH(launch_cre_dot(cs->m.p, dops + (size_t)l * nn, (int64_t)nn, part + (1 + l) * G, st), 1);
+            if (real)
+                FGB_LAUNCH(launch_cre_dot(b, cs->m.p, true, (int64_t)nn, part + (1 + l) * G, st), 1);
+            else
+                FGB_LAUNCH(launch_cre_dot(cs->m.p, op(dops, l), false, (int64_t)nn, part + (1 + l) * G, st), 1);
             ProfScope ps(KC_GEMM, st);
-            FGB_LAUNCH(launch_zgemm(n, n, n, ops + (size_t)l * nn, n, 0, true, b, n, 0, false, nb, n, 0, 1, false, st),
-                       1);
+            if (i8) {  // b <- Q_l^T b
+                if (int e = int8_qx(cs->cache, 1, true, op(ops, l), b, n, nb)) return e;
+            } else if (real) {  // over the (re, im) columns
+                FGB_LAUNCH(launch_rgemm(1, 1, 1, n, 2 * n, n, op(ops, l), n, 0, b, n, 0, nb, n, 0, 1, st), 1);
+            } else
+                FGB_LAUNCH(launch_zgemm(n, n, n, op(ops, l), n, 0, true, b, n, 0, false, nb, n, 0, 1, false, st), 1);
             std::swap(b, nb);
         } else {
-            FGB_LAUNCH(launch_cre_dot(b, dops, (int64_t)nn, part + G, st), 1);
+            FGB_LAUNCH(launch_cre_dot(b, dops, real, (int64_t)nn, part + G, st), 1);
         }
     }
     const double inv = 1.0 / ((double)n * (double)n);

@@ -151,14 +151,17 @@ __global__ void spec_scale_kernel(const double2* __restrict__ v, const double* _
 
 // ---- cascade reductions (learn.hpp:85-92)
 
-// b = y - t, part[blk] = sum |b|^2
-__global__ void __launch_bounds__(kSpRedThreads) cdiff_sq_kernel(const double2* __restrict__ y,
+// b = y - t, part[blk] = sum |b|^2 (REAL_Y: y is a real n x n matrix, the real-F fast backend)
+template <bool REAL_Y>
+__global__ void __launch_bounds__(kSpRedThreads) cdiff_sq_kernel(const void* __restrict__ yv,
                                                                  const double2* __restrict__ t, int64_t count,
                                                                  double2* __restrict__ b, double* __restrict__ part) {
     __shared__ double red[kSpRedThreads / 32];
     double acc = 0.0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x) {
-        const double2 d = make_double2(y[p].x - t[p].x, y[p].y - t[p].y);
+        const double2 y = REAL_Y ? make_double2(static_cast<const double*>(yv)[p], 0.0)
+                                 : static_cast<const double2*>(yv)[p];
+        const double2 d = make_double2(y.x - t[p].x, y.y - t[p].y);
         b[p] = d;
         acc = fma(d.x, d.x, fma(d.y, d.y, acc));
     }
@@ -166,14 +169,21 @@ __global__ void __launch_bounds__(kSpRedThreads) cdiff_sq_kernel(const double2* 
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-// part[blk] = Re sum conj(m) o d
+// part[blk] = Re sum conj(m) o d (REAL_D: d is real)
+template <bool REAL_D>
 __global__ void __launch_bounds__(kSpRedThreads) cre_dot_kernel(const double2* __restrict__ m,
-                                                                const double2* __restrict__ d, int64_t count,
+                                                                const void* __restrict__ dv, int64_t count,
                                                                 double* __restrict__ part) {
     __shared__ double red[kSpRedThreads / 32];
     double acc = 0.0;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x)
-        acc = fma(m[p].x, d[p].x, fma(m[p].y, d[p].y, acc));
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x) {
+        if (REAL_D) {
+            acc = fma(m[p].x, static_cast<const double*>(dv)[p], acc);
+        } else {
+            const double2 d = static_cast<const double2*>(dv)[p];
+            acc = fma(m[p].x, d.x, fma(m[p].y, d.y, acc));
+        }
+    }
     acc = block_sum(acc, red);
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
@@ -236,13 +246,19 @@ cudaError_t launch_spec_scale(const void* v, const double* theta, const double* 
                                                                         n, (double2*)w);
     return cudaGetLastError();
 }
-cudaError_t launch_cdiff_sq(const void* y, const void* t, int64_t count, void* b, double* part, cudaStream_t st) {
-    cdiff_sq_kernel<<<kSpRedBlocks, kSpRedThreads, 0, st>>>((const double2*)y, (const double2*)t, count,
-                                                           (double2*)b, part);
+cudaError_t launch_cdiff_sq(const void* y, bool real_y, const void* t, int64_t count, void* b, double* part,
+                            cudaStream_t st) {
+    if (real_y)
+        cdiff_sq_kernel<true><<<kSpRedBlocks, kSpRedThreads, 0, st>>>(y, (const double2*)t, count, (double2*)b, part);
+    else
+        cdiff_sq_kernel<false><<<kSpRedBlocks, kSpRedThreads, 0, st>>>(y, (const double2*)t, count, (double2*)b, part);
     return cudaGetLastError();
 }
-cudaError_t launch_cre_dot(const void* m, const void* d, int64_t count, double* part, cudaStream_t st) {
-    cre_dot_kernel<<<kSpRedBlocks, kSpRedThreads, 0, st>>>((const double2*)m, (const double2*)d, count, part);
+cudaError_t launch_cre_dot(const void* m, const void* d, bool real_d, int64_t count, double* part, cudaStream_t st) {
+    if (real_d)
+        cre_dot_kernel<true><<<kSpRedBlocks, kSpRedThreads, 0, st>>>((const double2*)m, d, count, part);
+    else
+        cre_dot_kernel<false><<<kSpRedBlocks, kSpRedThreads, 0, st>>>((const double2*)m, d, count, part);
     return cudaGetLastError();
 }
 cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s1, double* out, cudaStream_t st) {
