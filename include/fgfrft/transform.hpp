@@ -13,6 +13,7 @@
 #include <complex>
 #include <cstdint>
 #include <sstream>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -85,7 +86,19 @@ class PowerCache {
     void set_engine(int engine) { detail::throw_status(fgfrft_cache_set_engine(h_, engine)); }
     void prepare() { detail::throw_status(fgfrft_cache_prepare(h_)); }
 
+    // Extension: persist F and the resident powers; load() restores the
+    // cache without the O(L n^3) recursion (io_error / parse_error / capacity_error /
+    // numerical_error on a missing, malformed, over-budget or corrupt file).
+    void save(const std::string& path) const { detail::throw_status(fgfrft_cache_save(h_, path.c_str())); }
+    static PowerCache load(const std::string& path, std::uint64_t memory_budget = kDefaultMemoryBudget,
+                           int device = 0) {
+        fgfrft_cache* h = nullptr;
+        detail::throw_status(fgfrft_cache_load(path.c_str(), memory_budget, device, &h));
+        return PowerCache(h, memory_budget);
+    }
+
   private:
+    PowerCache(fgfrft_cache* h, std::uint64_t budget) : h_(h), budget_(budget) { load_info(); }
     void load_info() {
         int64_t n = 0;
         detail::throw_status(fgfrft_cache_info(h_, &n, &l_, &fp_, nullptr, nullptr));

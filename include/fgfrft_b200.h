@@ -20,7 +20,8 @@
  * Mapping to the reference exception taxonomy (proj/include/fgfrft/errors.hpp:36-62):
  *   FGFRFT_PARAMETER -> parameter_error, FGFRFT_SHAPE -> shape_error,
  *   FGFRFT_CAPACITY -> capacity_error, FGFRFT_NUMERICAL / FGFRFT_CUDA / FGFRFT_NCCL ->
- *   numerical_error, FGFRFT_OPTIMIZER -> optimizer_error (a numerical_error).
+ *   numerical_error, FGFRFT_OPTIMIZER -> optimizer_error (a numerical_error), FGFRFT_IO ->
+ *   io_error, FGFRFT_PARSE -> parse_error.
  *
  * Threading: calls on one handle are serialised by the handle; distinct handles may be
  * used concurrently. Every call is synchronous with respect to host buffers. Calls taking
@@ -45,7 +46,9 @@ typedef enum fgfrft_status {
     FGFRFT_NUMERICAL = 4,
     FGFRFT_CUDA = 5,
     FGFRFT_NCCL = 6,
-    FGFRFT_OPTIMIZER = 7 /* non-finite loss / gradient in a learner (optimizer_error) */
+    FGFRFT_OPTIMIZER = 7, /* non-finite loss / gradient in a learner (optimizer_error) */
+    FGFRFT_IO = 8,        /* file cannot be opened / written (io_error) */
+    FGFRFT_PARSE = 9      /* malformed or truncated file (parse_error) */
 } fgfrft_status;
 
 typedef enum fgfrft_dtype { FGFRFT_C128 = 0, FGFRFT_C64 = 1 } fgfrft_dtype;
@@ -278,6 +281,19 @@ int fgfrft_denoise_eval(fgfrft_denoise* problem, double alpha, const double* h, 
 int fgfrft_denoise_fit(fgfrft_denoise* problem, int epochs, double lr, double init_alpha,
                        double* traj_loss, double* traj_alpha, double* alpha_best, double* h_best,
                        double* loss_best, int* best_epoch, double* reconstruction);
+
+/* ---- on-disk power cache ----------------------------------------------
+ *
+ * save: header (magic "FGFRFTC\1", dtype, storage, n, L, fingerprint), F as n x n complex128
+ * column-major (the bytes content_fingerprint hashes), the resident slabs as they lie in HBM, and
+ * a 64-bit device checksum of the slabs. load: rebuilds the handle without the O(L n^3) build --
+ * budget check as in the constructor (FGFRFT_CAPACITY), F re-fingerprinted against the header
+ * and the slab checksum re-computed on the device (mismatch -> FGFRFT_NUMERICAL), bad magic /
+ * truncation -> FGFRFT_PARSE, open / write failures -> FGFRFT_IO. File IO overlaps the copies
+ * through two pinned staging buffers.
+ */
+int fgfrft_cache_save(fgfrft_cache* cache, const char* path);
+int fgfrft_cache_load(const char* path, uint64_t memory_budget, int device, fgfrft_cache** out);
 
 /* ---- spectral form and the exact GFRFT (spectral.hpp:19-195) ------------------------------
  *

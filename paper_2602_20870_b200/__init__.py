@@ -51,8 +51,16 @@ class OptimizerError(NumericalError):
     """errors.hpp optimizer_error: non-finite loss or gradient inside a learner."""
 
 
+class IoError(RuntimeError):
+    """errors.hpp io_error: a file cannot be opened or written."""
+
+
+class ParseError(IoError):
+    """errors.hpp parse_error: a malformed or truncated file."""
+
+
 _STATUS = {1: ParameterError, 2: ShapeError, 3: CapacityError, 4: NumericalError, 5: NumericalError,
-           6: NumericalError, 7: OptimizerError}
+           6: NumericalError, 7: OptimizerError, 8: IoError, 9: ParseError}
 
 _LIB = None
 
@@ -127,6 +135,8 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cascade_destroy": (i, [vp]),
         "fgfrft_cascade_eval": (i, [vp, vp, vp, vp]),
         "fgfrft_cascade_learn": (i, [vp, d, i, d, vp, vp, vp, vp]),
+        "fgfrft_cache_save": (i, [vp, ctypes.c_char_p]),
+        "fgfrft_cache_load": (i, [ctypes.c_char_p, u64, i, pp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -154,7 +164,7 @@ def exported_symbols():
         "fgfrft_cache_prepare", "fgfrft_spectrum_create", "fgfrft_spectrum_decompose", "fgfrft_spectrum_destroy",
         "fgfrft_spectrum_info", "fgfrft_spectrum_vectors", "fgfrft_spectrum_set_stream", "fgfrft_exact",
         "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
-        "fgfrft_cascade_learn",
+        "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load",
     ]
 
 
@@ -308,6 +318,22 @@ class PowerCache:
         b = ctypes.c_uint64()
         _check(lib().fgfrft_cache_device_bytes(self._h, ctypes.addressof(b)))
         return b.value
+
+    def save(self, path: str) -> None:
+        """Write F, the resident slabs and their checksum (fgfrft_cache_save)."""
+        _check(lib().fgfrft_cache_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, memory_budget: int = DEFAULT_MEMORY_BUDGET, device: int = 0) -> "PowerCache":
+        """Rebuild a cache from a file written by save() (no power recursion)."""
+        self = cls.__new__(cls)
+        self._h = ctypes.c_void_p()
+        _check(lib().fgfrft_cache_load(os.fsencode(path), int(memory_budget), int(device), ctypes.byref(self._h)))
+        n, l, fp, dt = ctypes.c_int64(), ctypes.c_int(), ctypes.c_uint64(), ctypes.c_int()
+        _check(lib().fgfrft_cache_info(self._h, ctypes.addressof(n), ctypes.addressof(l), ctypes.addressof(fp),
+                                       ctypes.addressof(dt), None))
+        self._n, self._l, self._fp, self.dtype, self.device = n.value, l.value, fp.value, dt.value, device
+        return self
 
 
 def build_power_cache(f, l, memory_budget=DEFAULT_MEMORY_BUDGET, **kw) -> PowerCache:

@@ -378,6 +378,20 @@ int main() {
         bad.depth = 0;
         CHECK_THROWS_AS(learn_orders(f, bad, Backend::fast), parameter_error);
     }
+    // on-disk cache (extension): save / load round trip, corrupt and missing files
+    {
+        const GftMatrix f = householder_real(96, 11);
+        const PowerCache cache(f, 6);
+        const std::string path = "/tmp/fgfrft_dropin_cache.fgc";
+        cache.save(path);
+        const PowerCache back = PowerCache::load(path);
+        CHECK(back.l() == 6 && back.n() == 96 && back.fingerprint() == cache.fingerprint());
+        CHECK(back.power(6) == cache.power(6));
+        back.verify(f);
+        CHECK_THROWS_AS(PowerCache::load("/tmp/fgfrft_no_such_file.fgc"), io_error);
+        CHECK_THROWS_AS(PowerCache::load(path, 1024), capacity_error);
+        std::remove(path.c_str());
+    }
     std::printf("drop-in C++ tests: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }

@@ -505,3 +505,44 @@ def test_fused_small_batch_apply(n, l, b):
     g.set_engine(fg.ENGINE_DMMA)
     y2 = fg.apply_series(g, alphas, x)
     assert all(rel(y2[i], y[i]) <= 1e-13 for i in range(len(alphas)))
+
+
+# --------------------------------------------------------------------------- on-disk cache (8(f) rank 4)
+
+@pytest.mark.parametrize("kind,dtype", [("real", fg.C128), ("complex", fg.C128), ("complex", fg.C64)])
+def test_cache_save_load_round_trip(tmp_path, kind, dtype):
+    n, l = (300, 12) if kind == "real" else (130, 9)
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.05, 4))) if kind == "real" else prep.random_unitary(n, 8)
+    g = fg.PowerCache(f, l, dtype=dtype)
+    path = str(tmp_path / "cache.fgc")
+    g.save(path)
+    h = fg.PowerCache.load(path)
+    assert (h.n(), h.l(), h.fingerprint(), h.dtype) == (n, l, g.fingerprint(), dtype)
+    assert h.is_real() == g.is_real()
+    if kind == "real":
+        assert h.orthogonality() == pytest.approx(g.orthogonality(), rel=1e-9)
+    for k in (1, l // 2, l):
+        assert np.array_equal(h.power(k), g.power(k))
+    alphas = [0.31, 1.2]
+    assert np.array_equal(fg.synthesize(h, alphas), fg.synthesize(g, alphas))
+    h.verify(f) if dtype == fg.C128 else None
+    # budget check as in the constructor; corruption and truncation are detected
+    with pytest.raises(fg.CapacityError):
+        fg.PowerCache.load(path, memory_budget=1024)
+    raw = bytearray(open(path, "rb").read())
+    bad = str(tmp_path / "bad.fgc")
+    raw2 = bytearray(raw)
+    raw2[-100] ^= 0x40  # a slab byte
+    open(bad, "wb").write(raw2)
+    with pytest.raises(fg.NumericalError):
+        fg.PowerCache.load(bad)
+    open(bad, "wb").write(raw[: len(raw) // 2])
+    with pytest.raises(fg.ParseError):
+        fg.PowerCache.load(bad)
+    raw3 = bytearray(raw)
+    raw3[0] = ord("X")
+    open(bad, "wb").write(raw3)
+    with pytest.raises(fg.ParseError):
+        fg.PowerCache.load(bad)
+    with pytest.raises(fg.IoError):
+        fg.PowerCache.load(str(tmp_path / "missing.fgc"))
