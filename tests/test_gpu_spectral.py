@@ -161,3 +161,39 @@ def test_cascade_errors():
         prob.eval([0.1])
     with pytest.raises(fg.ParameterError):
         prob.learn(0.1, 0, 0.01)
+
+
+# --------------------------------------------------------------------------- acceptance 3-4 fully on the GPU
+
+def test_series_vs_exact_errors_on_gpu_three_digits():  # acceptance.cpp:81-101 + north star "3 digits"
+    f = prep.random_unitary(1000, 42)
+    alphas = [0.15, 0.35, 0.55, 0.75, 0.95]
+    eig = fg.eigendecompose_unitary(f)
+    cache = fg.PowerCache(f, 10)
+    qs = fg.synthesize(cache, alphas)
+    ex = fg.exact_matrices(eig, alphas)
+    ve, te = O.eigendecompose_unitary(f)
+    oc = O.PowerCache(f, 10)
+    gpu = [O.matrix_errors(qs[i], ex[i]) for i in range(len(alphas))]
+    ref = [O.matrix_errors(O.fgfrft_matrix(oc, a, nthreads=8), O.exact_gfrft((ve, te), a)) for a in alphas]
+    for g, r in zip(gpu, ref):
+        for key in ("mse", "nmse", "mae"):
+            assert float(f"{g[key]:.3e}") == float(f"{r[key]:.3e}")
+    nmse = sum(e["nmse"] for e in gpu) / len(gpu)
+    mae = sum(e["mae"] for e in gpu) / len(gpu)
+    assert 2.05e-2 / 3 <= nmse <= 2.05e-2 * 3
+    assert 4.00e-3 / 3 <= mae <= 4.00e-3 * 3
+
+
+def test_monotone_convergence_on_gpu():  # acceptance.cpp:103-117
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(512, 0.1 * math.pi, 23), 63)
+    eig = fg.UnitaryEigen(v=v, theta=th)
+    exact = fg.exact_gfrft(eig, 0.5).q
+    cache = fg.PowerCache(f, 30)
+    prev = None
+    for l in (10, 20, 30):
+        q = fg.fgfrft_matrix(cache, 0.5, l).q
+        nmse = np.linalg.norm(q - exact) ** 2 / np.linalg.norm(exact) ** 2
+        if prev is not None:
+            assert nmse <= 0.9 * prev
+        prev = nmse

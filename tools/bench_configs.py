@@ -23,18 +23,22 @@ import paper_2602_20870_b200 as fg  # noqa: E402
 import prep  # noqa: E402
 
 
-def timed(stream, fn, reps=5, warm=3):
+def timed(stream, fn, reps=5, warm=3, groups=5):
+    """Median over `groups` CUDA-event-timed groups of `reps` calls (ms per call)."""
     with torch.cuda.stream(stream):
         for _ in range(warm):
             fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        fn()
-    e1.record(stream)
-    e1.synchronize()
-    return e0.elapsed_time(e1) / reps
+    out = []
+    for _ in range(groups):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1) / reps)
+    return float(np.median(out))
 
 
 def run(name, cfg, peaks, budget, dtype=0):

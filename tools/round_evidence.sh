@@ -1,0 +1,9 @@
+set -x
+mkdir -p gpurun_out/ev
+python -m pytest tests -m gpu -q -x > gpurun_out/ev/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ev/pytest_gpu.log
+python bench.py > gpurun_out/ev/bench.json 2> gpurun_out/ev/bench.err
+python bench.py --impl reference > gpurun_out/ev/bench_ref.json 2> gpurun_out/ev/bench_ref.err
+python tools/bench_configs.py --configs 1,2,3,4,5 > gpurun_out/ev/configs_int8.jsonl 2> gpurun_out/ev/configs_int8.err
+FGFRFT_ENGINE=dmma python tools/bench_configs.py --configs 2,3,4 > gpurun_out/ev/configs_dmma.jsonl 2> gpurun_out/ev/configs_dmma.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ev/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ev/ncu_bench.log 2>&1
+tail -2 gpurun_out/ev/pytest_gpu.log
