@@ -104,6 +104,7 @@ cudaError_t launch_cdiff_sq(const void* y, bool real_y, const void* t, int64_t c
                             cudaStream_t st);
 cudaError_t launch_cre_dot(const void* m, const void* d, bool real_d, int64_t count, double* part, cudaStream_t st);
 cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s1, double* out, cudaStream_t st);
+cudaError_t launch_rdot(const double* a, const double* b, int64_t count, double* part, cudaStream_t st);
 // store.cu
 cudaError_t launch_checksum(const void* data, size_t bytes, unsigned long long* out, cudaStream_t st);
 size_t dots_partial_elems(int n, int l, int n_alpha);
@@ -1117,6 +1118,23 @@ int dots_power_route(fgfrft_cache* c, int n_alpha, const void* g_dev, const void
     return FGFRFT_OK;
 }
 
+// c->m[a] = M_a = G_a X^H (n x n, K = b) for na orders; real cache: only M_re = Re(G X^H).
+int gx_device(fgfrft_cache* c, int na, const void* g_dev, const void* x_dev, int64_t b) {
+    const int n = (int)c->n;
+    const size_t sl = c->mat_elems();
+    if (use_int8_gemm(c, b)) return int8_gx(c, na, g_dev, x_dev, b, c->m.p);
+    ProfScope ps(KC_GEMM, c->stream);
+    if (c->real)
+        FGB_LAUNCH(launch_rgemm(2, 2, 0, n, n, 2 * (int)b, g_dev, n, (int64_t)2 * n * b, x_dev, n, 0, c->m.p, n,
+                                (int64_t)sl, na, c->stream),
+                   1);
+    else
+        FGB_LAUNCH(gemm(c, n, n, (int)b, g_dev, n, (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl,
+                        na),
+                   1);
+    return FGFRFT_OK;
+}
+
 // s_dev[a][2l+1] = Re<G_a, F^k X> for all orders; g_dev n_alpha blocks of n x b.
 // Order sweeps (>= 8 orders) use the DMMA split-K contraction (every byte of M and of the cache
 // read once per 64 orders); a few orders use the scalar tile-pair kernel (HBM-bound).
@@ -1133,23 +1151,8 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
     const size_t width = (size_t)(2 * c->l + 1);
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
-        // M_a = G_a X^H  (n x n, K = b); real cache: only M_re = Re(G X^H) is needed
-        if (use_int8_gemm(c, b)) {
-            if (int st = int8_gx(c, na, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, x_dev, b,
-                                 c->m.p))
-                return st;
-        } else {
-            ProfScope ps(KC_GEMM, c->stream);
-            if (c->real)
-                FGB_LAUNCH(launch_rgemm(2, 2, 0, n, n, 2 * (int)b,
-                                        static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, n,
-                                        (int64_t)2 * n * b, x_dev, n, 0, c->m.p, n, (int64_t)sl, na, c->stream),
-                           1);
-            else
-                FGB_LAUNCH(gemm(c, n, n, (int)b, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, n,
-                                (int64_t)n * b, false, x_dev, n, 0, true, c->m.p, n, (int64_t)sl, na),
-                           1);
-        }
+        if (int st = gx_device(c, na, static_cast<const char*>(g_dev) + (size_t)a0 * n * b * c->sig, x_dev, b))
+            return st;
         ProfScope ps(KC_DOTS, c->stream);
         if (c->real) {
             if (na >= 8) {
@@ -1556,7 +1559,12 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     }
     const int chunk = alpha_chunk(c, n_alpha);
     const size_t sl = c->mat_elems();
-    FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
+    // One or two orders: synthesise Q and dQ/dalpha together (one pass over the cache, the pair
+    // kernel's 2 / 4-order form) and take dL/dalpha = Re<G, dQ X> = Re<G X^H, dQ> as one
+    // elementwise dot, instead of a second cache pass for the per-power dots s_k.
+    const bool dq_route = n_alpha <= 2 && chunk >= n_alpha && !use_fused_apply(c, n_alpha, b) &&
+                          c->dtype == FGFRFT_C128 && std::getenv("FGFRFT_DOTS_ROUTE") == nullptr;
+    FGB_CUDA(c->q.ensure((size_t)(dq_route ? 2 : 1) * chunk * sl * c->elem));
     FGB_CUDA(c->g.ensure((size_t)chunk * blk * c->sig));
     FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
     FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
@@ -1572,8 +1580,8 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
                                            static_cast<const double*>(x_dev), (int)b, c->partial.as<double>(),
                                            static_cast<double*>(ya), c->stream),
                        2);
-        } else if (int st = synth_into(c, coef + a0 * width, na, l, c->q.p, true)) {
-            return st;
+        } else if (int st = synth_into(c, coef + a0 * width, dq_route ? 2 * na : na, l, c->q.p, true)) {
+            return st;  // dq_route: rows [c(a) ..][c'(a) ..] are contiguous in the table (a0 = 0)
         } else if (use_int8_gemm(c, b)) {
             if (int st = int8_qx(c, na, false, c->q.p, x_dev, b, ya)) return st;
         } else {
@@ -1595,11 +1603,34 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
                                            (int)c->sig),
                        2);
         }
+        if (dq_route) {
+            FGB_CUDA(c->m.ensure((size_t)na * sl * c->elem));
+            if (int st = gx_device(c, na, c->g.p, x_dev, b)) return st;
+            FGB_CUDA(c->partial.ensure((size_t)na * sp_part_elems() * sizeof(double)));
+            double* part = c->partial.as<double>();
+            const char* dq = c->q.as<char>() + (size_t)na * sl * c->elem;
+            ProfScope ps(KC_ELEMWISE, c->stream);
+            for (int i = 0; i < na; ++i) {
+                const char* mi = c->m.as<char>() + (size_t)i * sl * c->elem;
+                if (c->real)
+                    FGB_LAUNCH(launch_rdot(reinterpret_cast<const double*>(mi),
+                                           reinterpret_cast<const double*>(dq + (size_t)i * sl * c->elem), (int64_t)sl,
+                                           part + (size_t)i * sp_part_elems(), c->stream),
+                               1);
+                else
+                    FGB_LAUNCH(launch_cre_dot(mi, dq + (size_t)i * sl * c->elem, false, (int64_t)sl,
+                                              part + (size_t)i * sp_part_elems(), c->stream),
+                               1);
+            }
+            FGB_LAUNCH(launch_sum_parts(part, na, 1.0, 1.0, static_cast<double*>(dlda_dev) + a0, c->stream), 1);
+            continue;
+        }
         if (int st = dots_device(c, na, c->g.p, x_dev, b, c->s.as<double>() + a0 * width)) return st;
     }
-    FGB_LAUNCH(launch_coef_dot(dc_dev, c->s.as<double>(), n_alpha, (int)width, static_cast<double*>(dlda_dev),
-                               c->stream),
-               1);
+    if (!dq_route)
+        FGB_LAUNCH(launch_coef_dot(dc_dev, c->s.as<double>(), n_alpha, (int)width, static_cast<double*>(dlda_dev),
+                                   c->stream),
+                   1);
     return FGFRFT_OK;
     FGB_GUARD_END
 }

@@ -188,6 +188,18 @@ __global__ void __launch_bounds__(kSpRedThreads) cre_dot_kernel(const double2* _
     if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
+// part[blk] = sum a o b (real)
+__global__ void __launch_bounds__(kSpRedThreads) rdot_kernel(const double* __restrict__ a,
+                                                             const double* __restrict__ b, int64_t count,
+                                                             double* __restrict__ part) {
+    __shared__ double red[kSpRedThreads / 32];
+    double acc = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x)
+        acc = fma(a[p], b[p], acc);
+    acc = block_sum(acc, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
 // out[g] = scale_g * sum_b part[g * G + b] (fixed order), scale_0 = s0, scale_{g>0} = s1
 __global__ void sum_parts_kernel(const double* __restrict__ part, int groups, double s0, double s1,
                                  double* __restrict__ out) {
@@ -259,6 +271,10 @@ cudaError_t launch_cre_dot(const void* m, const void* d, bool real_d, int64_t co
         cre_dot_kernel<true><<<kSpRedBlocks, kSpRedThreads, 0, st>>>((const double2*)m, d, count, part);
     else
         cre_dot_kernel<false><<<kSpRedBlocks, kSpRedThreads, 0, st>>>((const double2*)m, d, count, part);
+    return cudaGetLastError();
+}
+cudaError_t launch_rdot(const double* a, const double* b, int64_t count, double* part, cudaStream_t st) {
+    rdot_kernel<<<kSpRedBlocks, kSpRedThreads, 0, st>>>(a, b, count, part);
     return cudaGetLastError();
 }
 cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s1, double* out, cudaStream_t st) {
