@@ -240,6 +240,12 @@ int fgfrft_shard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alph
 int fgfrft_shard_mse_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
                                  const void* x_dev, const void* xc_rows_dev, int64_t b,
                                  void* y_rows_dev, void* loss_partial_dev, void* s_partial_dev);
+/* Same, returning dlda_partial[a] = sum_k c'_k(alpha_a) s_partial[a][k] directly (n_alpha doubles
+ * to all-reduce instead of n_alpha (2L+1)); one or two orders synthesise dQ/dalpha rows in the
+ * same pass over the panels as Q and take Re<M[R,:], dQ[R,:]>, no second pass. */
+int fgfrft_shard_mse_dlda_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
+                                      const void* x_dev, const void* xc_rows_dev, int64_t b,
+                                      void* y_rows_dev, void* loss_partial_dev, void* dlda_partial_dev);
 
 /* ---- FP64-accurate GEMM on the INT8 tensor cores (Ozaki scheme) -------------------------
  *

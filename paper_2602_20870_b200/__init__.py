@@ -136,6 +136,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cascade_eval": (i, [vp, vp, vp, vp]),
         "fgfrft_cascade_learn": (i, [vp, d, i, d, vp, vp, vp, vp]),
         "fgfrft_cache_save": (i, [vp, ctypes.c_char_p]),
+        "fgfrft_shard_mse_dlda_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
         "fgfrft_cache_load": (i, [ctypes.c_char_p, u64, i, pp]),
     }
     for name, (res, args) in sig.items():
@@ -164,7 +165,7 @@ def exported_symbols():
         "fgfrft_cache_prepare", "fgfrft_spectrum_create", "fgfrft_spectrum_decompose", "fgfrft_spectrum_destroy",
         "fgfrft_spectrum_info", "fgfrft_spectrum_vectors", "fgfrft_spectrum_set_stream", "fgfrft_exact",
         "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
-        "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load",
+        "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
     ]
 
 

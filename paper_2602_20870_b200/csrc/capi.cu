@@ -1913,35 +1913,40 @@ int fgfrft_shard_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, c
     FGB_GUARD_END
 }
 
-int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
-                                 const void* xc_rows_dev, int64_t b, void* y_rows_dev, void* loss_partial_dev,
-                                 void* s_partial_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_shard(c)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
-    if (!x_dev || !xc_rows_dev || !loss_partial_dev || !s_partial_dev) return fail(FGFRFT_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
+}  // extern "C"
+
+namespace {
+
+// Row-shard MSE step. s_partial (per-power partials, 2L+1 per order) when requested; otherwise
+// dlda_partial = sum_k c'_k s_k directly -- for one or two orders via dQ/dalpha rows synthesised
+// in the same cache pass as Q and Re<M[R,:], dQ[R,:]> (no second pass over the panels).
+int shard_mse_impl(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_rows_dev,
+                   int64_t b, void* y_rows_dev, void* loss_partial_dev, double* s_partial_dev,
+                   double* dlda_partial_dev) {
     const int n = (int)c->n, rows = (int)(c->r1 - c->r0), l = c->l;
     const size_t width = (size_t)(2 * l + 1), qs = (size_t)rows * n, blk = (size_t)rows * b;
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
     const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)2 << 30) / (qs * 16))));
-    FGB_CUDA(c->q.ensure((size_t)chunk * qs * 16));
+    const bool dq_route = !s_partial_dev && n_alpha <= 2 && chunk >= n_alpha &&
+                          std::getenv("FGFRFT_DOTS_ROUTE") == nullptr;
+    FGB_CUDA(c->q.ensure((size_t)(dq_route ? 2 : 1) * chunk * qs * 16));
     FGB_CUDA(c->m.ensure((size_t)chunk * qs * 16));
     FGB_CUDA(c->g.ensure((size_t)chunk * blk * 16));
     FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
-    FGB_CUDA(c->partial.ensure(dots_rows_partial_elems(n, rows, l, chunk) * sizeof(double)));
+    FGB_CUDA(c->partial.ensure(std::max(dots_rows_partial_elems(n, rows, l, chunk), 2 * sp_part_elems()) *
+                               sizeof(double)));
+    if (!s_partial_dev && !dq_route) FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
     if (!y_rows_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * 16));
     const double norm = 1.0 / ((double)n * (double)b);
+    const size_t qe = c->real ? 8 : 16;
     for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
         const int na = std::min(chunk, n_alpha - a0);
         double2* ya = y_rows_dev ? static_cast<double2*>(y_rows_dev) + (size_t)a0 * blk : c->y.as<double2>();
         {
-            ProfScope ps(KC_SYNTH, c->stream);
-            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, coef + a0 * width, na, c->q.p,
-                                         c->stream, c->real, false),
+            ProfScope ps(KC_SYNTH, c->stream);  // dq_route: table rows [c(a) ..][c'(a) ..] (a0 = 0)
+            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, coef + a0 * width,
+                                         dq_route ? 2 * na : na, c->q.p, c->stream, c->real, false),
                        1);
         }
         if (use_int8_gemm(c, b)) {
@@ -1979,13 +1984,69 @@ int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_al
                                         rows, (int64_t)qs, na, false, c->stream),
                            1);
         }
+        if (dq_route) {  // dlda_partial[a] = Re<M[R,:], dQ[R,:]>
+            double* part = c->partial.as<double>();
+            const char* dq = c->q.as<char>() + (size_t)na * qs * qe;
+            ProfScope ps(KC_ELEMWISE, c->stream);
+            for (int i = 0; i < na; ++i) {
+                const char* mi = c->m.as<char>() + (size_t)i * qs * qe;
+                if (c->real)
+                    FGB_LAUNCH(launch_rdot(reinterpret_cast<const double*>(mi),
+                                           reinterpret_cast<const double*>(dq + (size_t)i * qs * qe), (int64_t)qs,
+                                           part + (size_t)i * sp_part_elems(), c->stream),
+                               1);
+                else
+                    FGB_LAUNCH(launch_cre_dot(mi, dq + (size_t)i * qs * qe, false, (int64_t)qs,
+                                              part + (size_t)i * sp_part_elems(), c->stream),
+                               1);
+            }
+            FGB_LAUNCH(launch_sum_parts(part, na, 1.0, 1.0, dlda_partial_dev + a0, c->stream), 1);
+            continue;
+        }
+        double* sp = s_partial_dev ? s_partial_dev : c->s.as<double>();
         ProfScope ps(KC_DOTS, c->stream);
         FGB_LAUNCH(launch_dots_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, c->m.p, (int64_t)qs, na,
-                                    c->partial.as<double>(), static_cast<double*>(s_partial_dev) + a0 * width,
-                                    c->stream, c->real),
+                                    c->partial.as<double>(), sp + a0 * width, c->stream, c->real),
                    2);
     }
+    if (!s_partial_dev && !dq_route)
+        FGB_LAUNCH(launch_coef_dot(coef + (size_t)n_alpha * width, c->s.as<double>(), n_alpha, (int)width,
+                                   dlda_partial_dev, c->stream),
+                   1);
     return FGFRFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
+                                 const void* xc_rows_dev, int64_t b, void* y_rows_dev, void* loss_partial_dev,
+                                 void* s_partial_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_shard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
+    if (!x_dev || !xc_rows_dev || !loss_partial_dev || !s_partial_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    return shard_mse_impl(c, alphas, n_alpha, x_dev, xc_rows_dev, b, y_rows_dev, loss_partial_dev,
+                          static_cast<double*>(s_partial_dev), nullptr);
+    FGB_GUARD_END
+}
+
+int fgfrft_shard_mse_dlda_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
+                                      const void* xc_rows_dev, int64_t b, void* y_rows_dev, void* loss_partial_dev,
+                                      void* dlda_partial_dev) {
+    FGB_GUARD_BEGIN
+    if (int st = check_shard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
+    if (!x_dev || !xc_rows_dev || !loss_partial_dev || !dlda_partial_dev) return fail(FGFRFT_PARAMETER, "null buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    return shard_mse_impl(c, alphas, n_alpha, x_dev, xc_rows_dev, b, y_rows_dev, loss_partial_dev, nullptr,
+                          static_cast<double*>(dlda_partial_dev));
     FGB_GUARD_END
 }
 

@@ -5,7 +5,9 @@ powers are sharded by ROW SLABS. Rank g owns output rows R_g and stores P_k[R_g,
 P_k[:,R_g] (the rows of F^k and F^{-k}); F is replicated for the build. Everything else is
 local (libfgfrft_b200.so `fgfrft_shard_*`), and the only collectives are
 
-  * all_reduce(sum) of the per-order loss partials and the 2L+1 per-power partials s_k, and
+  * all_reduce(sum) of the per-order loss partials and dL/dalpha partials (device shards:
+    `fgfrft_shard_mse_dlda_partial_dev`; a RankCompute without it sends the 2L+1 per-power
+    partials s_k instead), and
   * an all_gather of the rows of Y = F^alpha X (only when the caller wants Y).
 
 Collectives go through torch.distributed (NCCL over NVLink on GPUs; gloo on CPU in the tests).
@@ -118,6 +120,21 @@ class CudaShard(RankCompute):
             loss.data_ptr(), s.data_ptr()))
         return loss, s, y
 
+    def mse_dlda_partial(self, alphas, x, xc_rows):
+        """-> (loss_partial [A], dlda_partial [A]) on the device: dL/dalpha per order without the
+        per-power partials (dQ/dalpha rows from the same pass over the panels for <= 2 orders)."""
+        t = self.torch
+        al = np.ascontiguousarray(alphas, dtype=np.float64)
+        A, b = len(al), _signals(x)
+        xd = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(np.asarray(x).T)).to(self._dev())
+        xcd = xc_rows if isinstance(xc_rows, t.Tensor) else \
+            t.from_numpy(np.ascontiguousarray(np.asarray(xc_rows).T)).to(self._dev())
+        out = t.empty(2 * A, dtype=t.float64, device=self._dev())
+        self._check(self._lib.fgfrft_shard_mse_dlda_partial_dev(
+            self._h, al.ctypes.data, A, xd.data_ptr(), xcd.data_ptr(), b, None, out.data_ptr(),
+            out[A:].data_ptr()))
+        return out
+
     def apply_rows(self, alphas, x):
         t = self.torch
         al = np.ascontiguousarray(alphas, dtype=np.float64)
@@ -151,6 +168,14 @@ class ShardedFGFRFT:
         from . import sinc_coeffs
         torch = __import__("torch")
         dist = self._dist()
+        A = len(alphas)
+        b = _signals(x)
+        if hasattr(self.compute, "mse_dlda_partial"):  # device: [loss partials | dL/dalpha partials]
+            packed = self.compute.mse_dlda_partial(np.asarray(alphas, dtype=np.float64), x, x_clean_rows)
+            if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+                dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)  # the only data collective
+            packed = packed.cpu().numpy()
+            return packed[:A] / (self.n * b), packed[A:].copy()
         loss_p, s_p, _ = self.compute.mse_partial(np.asarray(alphas, dtype=np.float64), x, x_clean_rows)
         loss_t = loss_p if isinstance(loss_p, torch.Tensor) else torch.from_numpy(np.asarray(loss_p))
         s_t = s_p if isinstance(s_p, torch.Tensor) else torch.from_numpy(np.asarray(s_p))
@@ -158,8 +183,6 @@ class ShardedFGFRFT:
         if dist.is_initialized() and dist.get_world_size(self.group) > 1:
             dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=self.group)  # the only data collective
         packed = packed.cpu().numpy()
-        A = len(alphas)
-        b = _signals(x)
         loss = packed[:A] / (self.n * b)
         s = packed[A:].reshape(A, 2 * self.l + 1)
         dl = np.array([float(np.dot(sinc_coeffs(float(a), self.l)[1], s[i])) for i, a in enumerate(alphas)])

@@ -35,6 +35,7 @@ def test_shards_combine_to_unsharded(n, l, world, n_alpha, b, kind):
     plan = fgd.plan_rows(n, world)
     loss = np.zeros(n_alpha)
     s = np.zeros((n_alpha, 2 * l + 1))
+    dl_direct = np.zeros(n_alpha)  # fgfrft_shard_mse_dlda_partial_dev (dQ rows for <= 2 orders)
     y_rows, q_rows = [], []
     for r0, r1 in plan:
         if r1 == r0:
@@ -43,6 +44,9 @@ def test_shards_combine_to_unsharded(n, l, world, n_alpha, b, kind):
         lp, sp, _ = sh.mse_partial(alphas, x, xc[r0:r1])
         loss += lp.cpu().numpy()
         s += sp.cpu().numpy()
+        packed = sh.mse_dlda_partial(alphas, x, xc[r0:r1]).cpu().numpy()
+        assert np.allclose(packed[:n_alpha], lp.cpu().numpy(), rtol=1e-13, atol=0)
+        dl_direct += packed[n_alpha:]
         y_rows.append(sh.apply_rows(alphas, x).cpu().numpy().transpose(0, 2, 1))
         q_rows.append(sh.synthesize_rows(alphas).cpu().numpy().transpose(0, 2, 1))
         sh.close()
@@ -58,6 +62,7 @@ def test_shards_combine_to_unsharded(n, l, world, n_alpha, b, kind):
         s_ref = O.power_dots(o, (2.0 * (qr @ x - xc) / (n * b)) @ x.conj().T)
         assert np.abs(s[i] - s_ref).max() <= 1e-10 * np.abs(s_ref).sum()
         assert abs(float(np.dot(dc, s[i])) - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+        assert abs(dl_direct[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
 
 
 def test_shard_validation():
