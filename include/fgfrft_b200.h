@@ -10,7 +10,9 @@
  *   column-major, interleaved (re, im) doubles; element (i, j) of an n x n matrix is at
  *   doubles [2*(i + j*n)] and [2*(i + j*n) + 1]. Signal blocks X are n x b, column-major.
  *   complex64 caches take/return the same complex128 host buffers; storage and arithmetic
- *   on the device are complex64 (fgfrft_dtype FGFRFT_C64).
+ *   on the device are complex64 (fgfrft_dtype FGFRFT_C64). For a real F (imaginary part exactly
+ *   zero) a C64 cache stores the powers as real doubles -- the same 8 bytes per element -- and
+ *   computes in FP64; its *_dev entry points still take and return complex64 device signals.
  *
  * Series layout (identical to SincCoeffs, proj/include/fgfrft/sinc.hpp:40-48): arrays of
  *   2L+1 doubles where entry [n + L] holds term n, n = -L..L.

@@ -154,6 +154,14 @@ using namespace fgb;
 namespace {
 
 thread_local std::string g_err;
+// Set by the host-buffer entry points around their call into a *_dev entry point: the device
+// buffers they pass are already in the internal (complex128) layout, no complex64 bridge.
+thread_local bool tl_internal_signals = false;
+struct InternalSignals {
+    bool prev;
+    InternalSignals() : prev(tl_internal_signals) { tl_internal_signals = true; }
+    ~InternalSignals() { tl_internal_signals = prev; }
+};
 std::atomic<uint64_t> g_launches{0};
 
 // Optional per-kernel-class timing with CUDA events recorded on the launching stream
@@ -274,6 +282,12 @@ struct fgfrft_cache {
     int l = 0;
     int dtype = FGFRFT_C128;
     bool real = false;  // F has an exactly zero imaginary part: real cache, real Q, real x complex GEMMs
+    // complex64 API over a real F: the powers are stored as real doubles (the same 8 bytes per
+    // element as complex64) and every kernel runs the real complex128 path; the *_dev entry points
+    // promote the caller's complex64 signals on entry and demote the results (dtype stays C128
+    // internally, fgfrft_cache_info reports C64).
+    bool api_c64 = false;
+    DevBuf bx, bxc, by;
     size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
     int device = 0;
     uint64_t fingerprint = 0;
@@ -462,12 +476,17 @@ int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype,
     c->elem = elem;
     c->sig = elem;
     c->fingerprint = host_fnv1a64(f, (size_t)n * (size_t)n * 16);
-    if (dtype == FGFRFT_C128 && std::getenv("FGFRFT_NO_REAL") == nullptr) {
+    if (std::getenv("FGFRFT_NO_REAL") == nullptr) {
         bool real = true;
         for (size_t i = 0; i < (size_t)n * (size_t)n && real; ++i) real = f[2 * i + 1] == 0.0;
         if (real) {
             c->real = true;
             c->elem = 8;
+            if (dtype == FGFRFT_C64) {  // same 8 bytes per element, FP64 real kernels (see api_c64)
+                c->api_c64 = true;
+                c->dtype = FGFRFT_C128;
+                c->sig = 16;
+            }
         }
     }
     DeviceGuard dg(device);
@@ -500,7 +519,8 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
-                      &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex})
+                      &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
+                      &c->by})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -1272,7 +1292,7 @@ int fgfrft_cache_info(const fgfrft_cache* c, int64_t* n, int* l, uint64_t* finge
     if (n) *n = c->n;
     if (l) *l = c->l;
     if (fingerprint) *fingerprint = c->fingerprint;
-    if (dtype) *dtype = c->dtype;
+    if (dtype) *dtype = c->api_c64 ? FGFRFT_C64 : c->dtype;
     if (device) *device = c->device;
     return FGFRFT_OK;
 }
@@ -1374,6 +1394,13 @@ int fgfrft_synthesize_dev(fgfrft_cache* c, const double* alphas, int n_alpha, in
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
     const double* table = which == FGFRFT_Q ? coef : coef + (size_t)n_alpha * (2 * l_used + 1);
+    if (c->api_c64 && !tl_internal_signals) {  // complex64 output
+        const size_t cnt = (size_t)n_alpha * c->mat_elems();
+        FGB_CUDA(c->by.ensure(cnt * 16));
+        if (int st = synth_into(c, table, n_alpha, l_used, c->by.p)) return st;
+        FGB_LAUNCH(launch_demote(c->by.p, out_dev, (int64_t)cnt, c->stream), 1);
+        return FGFRFT_OK;
+    }
     return synth_into(c, table, n_alpha, l_used, out_dev);
     FGB_GUARD_END
 }
@@ -1388,7 +1415,10 @@ int fgfrft_synthesize(fgfrft_cache* c, const double* alphas, int n_alpha, int tr
         DeviceGuard dg(c->device);
         FGB_CUDA(c->y.ensure((size_t)n_alpha * c->mat_elems() * (c->real ? 16 : c->elem)));
     }
-    if (int st = fgfrft_synthesize_dev(c, alphas, n_alpha, truncation, which, c->y.p)) return st;
+    {
+        InternalSignals internal;
+        if (int st = fgfrft_synthesize_dev(c, alphas, n_alpha, truncation, which, c->y.p)) return st;
+    }
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
     return download_as_c128(c, c->y.p, (size_t)n_alpha * c->mat_elems(), out);
@@ -1407,6 +1437,15 @@ int fgfrft_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int tru
     if (!x_dev || !y_dev) return fail(FGFRFT_PARAMETER, "null signal buffer");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
+    if (c->api_c64 && !tl_internal_signals) {  // complex64 signals in and out
+        const size_t xe = (size_t)c->n * b;
+        FGB_CUDA(c->bx.ensure(xe * 16));
+        FGB_CUDA(c->by.ensure(xe * n_alpha * 16));
+        FGB_LAUNCH(launch_promote(x_dev, c->bx.p, (int64_t)xe, c->stream), 1);
+        if (int st = apply_device(c, alphas, n_alpha, l_used, inverse != 0, c->bx.p, b, c->by.p)) return st;
+        FGB_LAUNCH(launch_demote(c->by.p, y_dev, (int64_t)(xe * n_alpha), c->stream), 1);
+        return FGFRFT_OK;
+    }
     return apply_device(c, alphas, n_alpha, l_used, inverse != 0, x_dev, b, y_dev);
     FGB_GUARD_END
 }
@@ -1486,6 +1525,13 @@ int fgfrft_dlda_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const vo
     FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
     if (b == 0) {
         FGB_CUDA(cudaMemsetAsync(c->s.p, 0, (size_t)n_alpha * width * sizeof(double), c->stream));
+    } else if (c->api_c64 && !tl_internal_signals) {  // complex64 G and X
+        const size_t xe = (size_t)c->n * b;
+        FGB_CUDA(c->bx.ensure(xe * 16));
+        FGB_CUDA(c->by.ensure(xe * n_alpha * 16));
+        FGB_LAUNCH(launch_promote(x_dev, c->bx.p, (int64_t)xe, c->stream), 1);
+        FGB_LAUNCH(launch_promote(g_dev, c->by.p, (int64_t)(xe * n_alpha), c->stream), 1);
+        if (int st = dots_device(c, n_alpha, c->by.p, c->bx.p, b, c->s.as<double>())) return st;
     } else if (int st = dots_device(c, n_alpha, g_dev, x_dev, b, c->s.as<double>())) {
         return st;
     }
@@ -1522,6 +1568,7 @@ int fgfrft_dlda(fgfrft_cache* c, const double* alphas, int n_alpha, const double
             if (int st = upload_signal(c, g, xe * n_alpha, c->g.p)) return st;
         }
     }
+    InternalSignals internal;
     return fgfrft_dlda_dev(c, alphas, n_alpha, c->g.p, c->x.p, b, s, dlda);
     FGB_GUARD_END
 }
@@ -1539,6 +1586,28 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     const int l = c->l;
     const size_t width = (size_t)(2 * l + 1);
     const size_t blk = (size_t)n * b;
+    void* y_c64 = nullptr;
+    if (c->api_c64 && !tl_internal_signals) {  // complex64 X, Xc (and Y) at the boundary
+        FGB_CUDA(c->bx.ensure(blk * 16));
+        FGB_CUDA(c->bxc.ensure(blk * 16));
+        FGB_LAUNCH(launch_promote(x_dev, c->bx.p, (int64_t)blk, c->stream), 1);
+        FGB_LAUNCH(launch_promote(xc_dev, c->bxc.p, (int64_t)blk, c->stream), 1);
+        x_dev = c->bx.p;
+        xc_dev = c->bxc.p;
+        if (y_dev) {
+            FGB_CUDA(c->by.ensure(blk * n_alpha * 16));
+            y_c64 = y_dev;
+            y_dev = c->by.p;
+        }
+    }
+    struct DemoteY {  // runs on every successful return below
+        fgfrft_cache* c;
+        void* dst;
+        size_t cnt;
+        ~DemoteY() {
+            if (dst) launch_demote(c->by.p, dst, (int64_t)cnt, c->stream);
+        }
+    } demote_y{c, y_c64, blk * n_alpha};
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
     const double* dc_dev = coef + (size_t)n_alpha * width;
@@ -1665,8 +1734,12 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
         }
     }
     double* ld = c->loss.as<double>();
-    if (int st = fgfrft_mse_step_dev(c, alphas, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha))
-        return st;
+    {
+        InternalSignals internal;
+        if (int st = fgfrft_mse_step_dev(c, alphas, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld,
+                                         ld + n_alpha))
+            return st;
+    }
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
     std::vector<double> out(2 * (size_t)n_alpha);
@@ -3279,7 +3352,7 @@ int fgfrft_cache_save(fgfrft_cache* c, const char* path) {
     CacheFileHeader h{};
     std::memcpy(h.magic, kCacheMagic, 8);
     h.version = 1;
-    h.dtype = (uint32_t)c->dtype;
+    h.dtype = (uint32_t)(c->api_c64 ? FGFRFT_C64 : c->dtype);
     h.real = c->real ? 1u : 0u;
     h.elem = (uint32_t)c->elem;
     h.n = c->n;

@@ -5,6 +5,7 @@ Tolerances (BASELINE north star): complex128 within 1e-10 relative Frobenius; th
 synthesis is evaluated in the reference's operation order without FMA contraction, so it is
 asserted BIT-EXACT against the oracle. dL/dalpha: |g - g_ref| <= 1e-10 * sum_k |c'_k s_k|.
 """
+import ctypes
 import math
 
 import numpy as np
@@ -546,3 +547,44 @@ def test_cache_save_load_round_trip(tmp_path, kind, dtype):
         fg.PowerCache.load(bad)
     with pytest.raises(fg.IoError):
         fg.PowerCache.load(str(tmp_path / "missing.fgc"))
+
+
+def test_complex64_api_over_real_f_runs_the_real_fp64_path():
+    """A real F under dtype C64: powers stored as real doubles (same 8 bytes per element), the real
+    FP64 kernels run, and the *_dev entry points take / return complex64 device buffers."""
+    import torch
+    n, l, b = 512, 16, 48
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.03, 5)))
+    g64 = fg.PowerCache(f, l, dtype=fg.C64)
+    g128 = fg.PowerCache(f, l)
+    dt = ctypes.c_int()
+    fg._check(fg.lib().fgfrft_cache_info(g64.handle, None, None, None, ctypes.addressof(dt), None))
+    assert dt.value == fg.C64 and g64.is_real() and g64.device_bytes() == g128.device_bytes()
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))).astype(np.complex64)
+    xc = (x + 0.1 * rng.standard_normal((n, b))).astype(np.complex64)
+    alphas = np.array([0.37, 1.21])
+    lib = fg.lib()
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    xcd = torch.from_numpy(np.ascontiguousarray(xc.T)).cuda()
+    y = torch.empty((2, b, n), dtype=torch.complex64, device="cuda")
+    fg._check(lib.fgfrft_apply_dev(g64.handle, alphas.ctypes.data, 2, 0, 0, xd.data_ptr(), b, y.data_ptr()))
+    q = torch.empty((2, n, n), dtype=torch.complex64, device="cuda")
+    fg._check(lib.fgfrft_synthesize_dev(g64.handle, alphas.ctypes.data, 2, 0, 0, q.data_ptr()))
+    loss = torch.empty(2, dtype=torch.float64, device="cuda")
+    dl = torch.empty(2, dtype=torch.float64, device="cuda")
+    fg._check(lib.fgfrft_mse_step_dev(g64.handle, alphas.ctypes.data, 2, xd.data_ptr(), xcd.data_ptr(), b, None,
+                                      loss.data_ptr(), dl.data_ptr()))
+    torch.cuda.synchronize()
+    x128, xc128 = x.astype(np.complex128), xc.astype(np.complex128)
+    y_ref = fg.apply_series(g128, alphas, x128)
+    q_ref = fg.synthesize(g128, alphas)
+    l_ref, d_ref, _ = fg.mse_step(g128, alphas, x128, xc128)
+    ys = y.cpu().numpy().transpose(0, 2, 1)
+    for i in range(2):
+        assert rel(ys[i], y_ref[i]) <= 1e-6                       # complex64 rounding of the output only
+        assert rel(q.cpu().numpy()[i].T, q_ref[i]) <= 1e-6
+    assert np.allclose(loss.cpu().numpy(), l_ref, rtol=1e-12)   # FP64 arithmetic on the same inputs
+    assert np.allclose(dl.cpu().numpy(), d_ref, rtol=1e-9, atol=1e-14)
+    # host-buffer entry points return complex128 as before
+    assert rel(fg.apply_series(g64, alphas, x128)[0], y_ref[0]) <= 1e-14
