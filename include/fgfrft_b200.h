@@ -242,6 +242,21 @@ int fgfrft_shard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alph
 int fgfrft_shard_mse_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
                                  const void* x_dev, const void* xc_rows_dev, int64_t b,
                                  void* y_rows_dev, void* loss_partial_dev, void* s_partial_dev);
+/* Fused all-gather of the apply (north star: "the final row gather"): rows [r0, r1) of
+ * Y_a = F^alpha_a X are written into y_full_dev (n_alpha blocks of n x b, column-major, the FULL
+ * result) AND, at the same offsets, into each of the n_peers peer buffers peer_y_full[q] -- the
+ * other ranks' y_full buffers mapped into this process (fgfrft_ipc_open) -- by the INT8 GEMM's
+ * epilogue itself (NVLink P2P stores interleaved with the tiles), or by a P2P push kernel after the
+ * DMMA GEMM. After every rank's call has completed (stream sync + a host barrier), every y_full
+ * holds all rows. n_peers <= 7. */
+int fgfrft_shard_apply_gather_dev(fgfrft_cache* shard, const double* alphas, int n_alpha,
+                                  const void* x_dev, int64_t b, void* y_full_dev,
+                                  void* const* peer_y_full, int n_peers);
+/* CUDA IPC for the peer mappings: handle (64 bytes) and the offset of dev_ptr inside its
+ * allocation; open maps a peer's allocation (base) on `device`; close unmaps it. */
+int fgfrft_ipc_get(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
+int fgfrft_ipc_open(const void* handle, int device, void** base_out);
+int fgfrft_ipc_close(void* base);
 /* Same, returning dlda_partial[a] = sum_k c'_k(alpha_a) s_partial[a][k] directly (n_alpha doubles
  * to all-reduce instead of n_alpha (2L+1)); one or two orders synthesise dQ/dalpha rows in the
  * same pass over the panels as Q and take Re<M[R,:], dQ[R,:]>, no second pass. */

@@ -137,6 +137,10 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cascade_learn": (i, [vp, d, i, d, vp, vp, vp, vp]),
         "fgfrft_cache_save": (i, [vp, ctypes.c_char_p]),
         "fgfrft_shard_mse_dlda_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
+        "fgfrft_shard_apply_gather_dev": (i, [vp, vp, i, vp, i64, vp, vp, i]),
+        "fgfrft_ipc_get": (i, [vp, vp, vp]),
+        "fgfrft_ipc_open": (i, [vp, i, pp]),
+        "fgfrft_ipc_close": (i, [vp]),
         "fgfrft_cache_load": (i, [ctypes.c_char_p, u64, i, pp]),
     }
     for name, (res, args) in sig.items():
@@ -166,6 +170,7 @@ def exported_symbols():
         "fgfrft_spectrum_info", "fgfrft_spectrum_vectors", "fgfrft_spectrum_set_stream", "fgfrft_exact",
         "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
         "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
+        "fgfrft_shard_apply_gather_dev", "fgfrft_ipc_get", "fgfrft_ipc_open", "fgfrft_ipc_close",
     ]
 
 

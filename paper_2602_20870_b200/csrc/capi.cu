@@ -107,6 +107,9 @@ cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s
 cudaError_t launch_rdot(const double* a, const double* b, int64_t count, double* part, cudaStream_t st);
 // store.cu
 cudaError_t launch_checksum(const void* data, size_t bytes, unsigned long long* out, cudaStream_t st);
+// shard.cu (fused row gather, DMMA path)
+cudaError_t launch_rows_push(const void* src, int64_t n, int r0, int rows, int64_t cols, void* const* dst_dev,
+                             int ndst, cudaStream_t stream);
 size_t dots_partial_elems(int n, int l, int n_alpha);
 size_t dots_mma_partial_elems(int n);
 int dots_mma_max_orders();
@@ -698,7 +701,8 @@ int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
 int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
-                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy);
+                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers = nullptr,
+                int npeers = 0);
 int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
                 int64_t sm);
 bool use_power_route(const fgfrft_cache* c, int n_alpha);
@@ -1038,7 +1042,7 @@ int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp
 // Y_a = op(Q_a) X for na real m x n matrices Q_a (column-major, leading dimension ldq, stride sq
 // doubles), complex X (n x b); Y_a complex m x b (leading dimension ldy, stride sy doubles).
 int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
-                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy) {
+                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers, int npeers) {
     const int S = oz_slices_default();
     const int64_t n = c->n, mp = pad_rows(m), kp = pad_k(n), rows = (int64_t)na * mp;
     FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
@@ -1057,7 +1061,8 @@ int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m,
     if (int st = slice_signal_rows(c, x_dev, b, &bp)) return st;
     ProfScope ps(KC_I8GEMM, c->stream);
     FGB_LAUNCH(launch_ozgemm(S, 1, c->qsl.as<int8_t>(), qe, (int)rows, c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
-                             (int)kp, static_cast<double*>(y), ldy, sy, (int)m, (int)mp, (int)(2 * b), c->stream),
+                             (int)kp, static_cast<double*>(y), ldy, sy, (int)m, (int)mp, (int)(2 * b), c->stream, peers,
+                             npeers),
                1);
     return FGFRFT_OK;
 }
@@ -1938,6 +1943,109 @@ int fgfrft_shard_synthesize_dev(fgfrft_cache* c, const double* alphas, int n_alp
                1);
     return FGFRFT_OK;
     FGB_GUARD_END
+}
+
+int fgfrft_shard_apply_gather_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, int64_t b,
+                                  void* y_full_dev, void* const* peer_y_full, int n_peers) {
+    FGB_GUARD_BEGIN
+    if (int st = check_shard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
+    if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !peer_y_full))
+        return fail(FGFRFT_PARAMETER, "apply_gather: 0..7 peer buffers");
+    if (b == 0) return FGFRFT_OK;
+    if (!x_dev || !y_full_dev) return fail(FGFRFT_PARAMETER, "null signal buffer");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    const int n = (int)c->n, rows = (int)(c->r1 - c->r0);
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
+    const size_t width = (size_t)(2 * c->l + 1), qs = (size_t)rows * n, blk = (size_t)n * b;
+    const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)4 << 30) / (qs * 16))));
+    FGB_CUDA(c->q.ensure((size_t)chunk * qs * 16));
+    FGB_CUDA(c->tmp.ensure(8 * sizeof(void*)));  // peer bases as a device array (push kernel)
+    const bool i8 = use_int8_gemm(c, b);
+    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
+        const int na = std::min(chunk, n_alpha - a0);
+        const size_t off = (size_t)a0 * blk + (size_t)c->r0;  // complex elements: order a0, row r0
+        double2* yl = static_cast<double2*>(y_full_dev) + off;
+        {
+            ProfScope ps(KC_SYNTH, c->stream);
+            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, c->l, coef + a0 * width, na, c->q.p,
+                                         c->stream, c->real, false),
+                       1);
+        }
+        if (i8) {  // rows of Y written locally and into every peer buffer by the GEMM epilogue
+            double* pp[7];
+            for (int q = 0; q < n_peers; ++q) pp[q] = reinterpret_cast<double*>(static_cast<double2*>(peer_y_full[q]) + off);
+            if (int st = int8_qx_gen(c, na, false, c->q.p, rows, rows, (int64_t)qs, x_dev, b, yl, n,
+                                     2 * (int64_t)blk, pp, n_peers))
+                return st;
+            continue;
+        }
+        {
+            ProfScope ps(KC_GEMM, c->stream);
+            if (c->real)
+                FGB_LAUNCH(launch_rgemm(0, 1, 1, rows, 2 * (int)b, n, c->q.p, rows, (int64_t)qs, x_dev, n, 0, yl, n,
+                                        (int64_t)2 * blk, na, c->stream),
+                           1);
+            else
+                FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false, yl, n,
+                                        (int64_t)blk, na, false, c->stream),
+                           1);
+        }
+        if (n_peers > 0) {  // DMMA epilogue writes locally: push the rows to the peers (P2P stores)
+            std::vector<void*> shifted((size_t)n_peers);
+            for (int q = 0; q < n_peers; ++q) shifted[q] = static_cast<double2*>(peer_y_full[q]) + (size_t)a0 * blk;
+            FGB_CUDA(cudaMemcpyAsync(c->tmp.p, shifted.data(), (size_t)n_peers * sizeof(void*),
+                                     cudaMemcpyHostToDevice, c->stream));
+            FGB_LAUNCH(launch_rows_push(static_cast<double2*>(y_full_dev) + (size_t)a0 * blk, n, (int)c->r0, rows,
+                                        (int64_t)na * b, c->tmp.as<void*>(), n_peers, c->stream),
+                       1);
+            FGB_CUDA(cudaStreamSynchronize(c->stream));  // `shifted` is host staging of the copy above
+        }
+    }
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+// CUDA IPC of a device buffer for the fused gather: handle (64 bytes) + offset of the pointer in
+// its allocation (allocator sub-allocations), and the mapping on a peer process.
+int fgfrft_ipc_get(const void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+    FGB_GUARD_BEGIN
+    if (!dev_ptr || !handle_out || !offset_out) return fail(FGFRFT_PARAMETER, "null argument");
+    using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static GetRange get_range = [] {
+        void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        return h ? reinterpret_cast<GetRange>(dlsym(h, "cuMemGetAddressRange_v2")) : nullptr;
+    }();
+    if (!get_range) return fail(FGFRFT_CUDA, "cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+        return fail(FGFRFT_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    FGB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle_out, &h, sizeof h);
+    *offset_out = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_ipc_open(const void* handle, int device, void** base_out) {
+    FGB_GUARD_BEGIN
+    if (!handle || !base_out) return fail(FGFRFT_PARAMETER, "null argument");
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    FGB_CUDA(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_ipc_close(void* base) {
+    if (base) cudaIpcCloseMemHandle(base);
+    return FGFRFT_OK;
 }
 
 int fgfrft_shard_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, int64_t b,

@@ -50,6 +50,10 @@ struct OzOut {
     int64_t count = 0;           // 2 n b
     int n = 0, tp2 = 0, kbz = 0; // signal length, padded terms (64 | 128), K blocks of the combine
     int l = 0;                   // CM 2: L (row kk = 2L-1 holds Z_-L)
+    // CM 0 / 1: the same tile also stored at these bases (peer GPUs' buffers mapped over NVLink:
+    // the all-gather of a row-sharded output fused into the GEMM epilogue). Offsets as for c.
+    double* peers[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int npeers = 0;
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)
@@ -69,6 +73,6 @@ int oz_bk(int slices);  // bytes of K per stage / per digit block of the sliced 
 int oz_zdigits();       // digits of Z written by the CM 2 epilogue (the combine GEMM's digit count)
 cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                           const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
-                          cudaStream_t stream);
+                          cudaStream_t stream, double* const* peers = nullptr, int npeers = 0);
 
 }  // namespace fgb

@@ -484,10 +484,18 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                     const double v0 = val[c] * ra * pow2(ebt[c]);
                     const double v1 = val[c + 1] * ra * pow2(ebt[c + 1]);
                     if (CM == 0) {
+                        const int64_t o0 = (int64_t)bm * out.sc + i + (int64_t)n * out.ldc;
                         __stcs(cb + i + (int64_t)n * out.ldc, v0);
                         if (n + 1 < out.nv) __stcs(cb + i + (int64_t)(n + 1) * out.ldc, v1);
+                        for (int q = 0; q < out.npeers; ++q) {  // fused all-gather: peer copies
+                            out.peers[q][o0] = v0;
+                            if (n + 1 < out.nv) out.peers[q][o0 + out.ldc] = v1;
+                        }
                     } else {
+                        const int64_t o = (int64_t)bm * out.sc + (i + (int64_t)(n >> 1) * out.ldc) * 2;
                         __stcs(reinterpret_cast<double2*>(cb + (i + (int64_t)(n >> 1) * out.ldc) * 2), make_double2(v0, v1));
+                        for (int q = 0; q < out.npeers; ++q)
+                            *reinterpret_cast<double2*>(out.peers[q] + o) = make_double2(v0, v1);
                     }
                 }
             }
@@ -629,9 +637,11 @@ cudaError_t launch_ozgemm_ex(int slices, int cm, const int8_t* a, const int* ea,
 
 cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                           const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
-                          cudaStream_t stream) {
-    if (cm > 1) return cudaErrorInvalidValue;
+                          cudaStream_t stream, double* const* peers, int npeers) {
+    if (cm > 1 || npeers < 0 || npeers > 7) return cudaErrorInvalidValue;
     OzOut out;
+    for (int q = 0; q < npeers; ++q) out.peers[q] = peers[q];
+    out.npeers = npeers;
     out.c = c;
     out.ldc = ldc;
     out.sc = sc;

@@ -344,4 +344,26 @@ cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, 
     return cudaGetLastError();
 }
 
+// Rows [r0, r0 + rows) of na blocks of n x b complex128 (column-major, block stride n b) from the
+// local full buffer to every peer's buffer (NVLink P2P stores): the all-gather of a row-sharded
+// result for the GEMMs that cannot write peers from their epilogue (DMMA path).
+__global__ void rows_push_kernel(const double2* __restrict__ src, int64_t n, int r0, int rows, int64_t cols,
+                                 double2* const* __restrict__ dst, int ndst) {
+    const int64_t total = (int64_t)rows * cols;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = idx / rows, i = idx - j * rows;
+        const int64_t o = j * n + r0 + i;
+        const double2 v = src[o];
+        for (int d = 0; d < ndst; ++d) dst[d][o] = v;
+    }
+}
+
+cudaError_t launch_rows_push(const void* src, int64_t n, int r0, int rows, int64_t cols, void* const* dst_dev,
+                             int ndst, cudaStream_t stream) {
+    if (ndst <= 0 || rows <= 0 || cols <= 0) return cudaSuccess;
+    rows_push_kernel<<<8 * FGFRFT_SMS, 256, 0, stream>>>((const double2*)src, n, r0, rows, cols,
+                                                         (double2* const*)dst_dev, ndst);
+    return cudaGetLastError();
+}
+
 }  // namespace fgb

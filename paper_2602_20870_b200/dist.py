@@ -8,7 +8,9 @@ local (libfgfrft_b200.so `fgfrft_shard_*`), and the only collectives are
   * all_reduce(sum) of the per-order loss partials and dL/dalpha partials (device shards:
     `fgfrft_shard_mse_dlda_partial_dev`; a RankCompute without it sends the 2L+1 per-power
     partials s_k instead), and
-  * an all_gather of the rows of Y = F^alpha X (only when the caller wants Y).
+  * an all_gather of the rows of Y = F^alpha X (only when the caller wants Y) -- either NCCL
+    (`apply`) or fused into the GEMM epilogue (`apply_fused`: every rank's kernel stores its rows
+    into every rank's Y buffer over NVLink through CUDA IPC mappings).
 
 Collectives go through torch.distributed (NCCL over NVLink on GPUs; gloo on CPU in the tests).
 The per-rank compute is the `RankCompute` interface: `CudaShard` is the product implementation;
@@ -135,6 +137,19 @@ class CudaShard(RankCompute):
             out[A:].data_ptr()))
         return out
 
+    def apply_gather(self, alphas, x, y_full, peers: Sequence[int] = ()):
+        """Rows [r0, r1) of Y into y_full ([A, b, n] device tensor = A column-major n x b blocks)
+        and, by the same GEMM epilogue, into every peer buffer (device pointers mapped over
+        NVLink, fgfrft_ipc_open): the fused all-gather of the row-sharded apply."""
+        t = self.torch
+        al = np.ascontiguousarray(alphas, dtype=np.float64)
+        b = _signals(x)
+        xd = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(np.asarray(x).T)).to(self._dev())
+        arr = (ctypes.c_void_p * max(1, len(peers)))(*[ctypes.c_void_p(int(p)) for p in peers])
+        self._check(self._lib.fgfrft_shard_apply_gather_dev(self._h, al.ctypes.data, len(al), xd.data_ptr(), b,
+                                                            y_full.data_ptr(), arr if peers else None, len(peers)))
+        return y_full
+
     def apply_rows(self, alphas, x):
         t = self.torch
         al = np.ascontiguousarray(alphas, dtype=np.float64)
@@ -187,6 +202,55 @@ class ShardedFGFRFT:
         s = packed[A:].reshape(A, 2 * self.l + 1)
         dl = np.array([float(np.dot(sinc_coeffs(float(a), self.l)[1], s[i])) for i, a in enumerate(alphas)])
         return loss, dl
+
+    def _peer_buffers(self, y_full):
+        """IPC-map every other rank's y_full once per buffer; returns their device pointers."""
+        from . import _check, lib
+        dist = self._dist()
+        key = (y_full.data_ptr(), tuple(y_full.shape))
+        cache = getattr(self, "_peer_cache", None)
+        if cache and cache[0] == key:
+            return cache[1]
+        for base in getattr(self, "_peer_bases", []):
+            lib().fgfrft_ipc_close(ctypes.c_void_p(base))
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_uint64()
+        _check(lib().fgfrft_ipc_get(ctypes.c_void_p(y_full.data_ptr()), h, ctypes.addressof(off)))
+        world, me = dist.get_world_size(self.group), dist.get_rank(self.group)
+        mine = (bytes(h), off.value)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=self.group)
+        ptrs, bases = [], []
+        for r, (hb, o) in enumerate(allh):
+            if r == me:
+                continue
+            base = ctypes.c_void_p()
+            _check(lib().fgfrft_ipc_open(ctypes.create_string_buffer(hb, 64), y_full.device.index,
+                                         ctypes.byref(base)))
+            bases.append(base.value)
+            ptrs.append(base.value + o)
+        self._peer_cache, self._peer_bases = (key, ptrs), bases
+        return ptrs
+
+    def apply_fused(self, alphas: Sequence[float], x):
+        """Full Y = F^alpha X on every rank with the all-gather fused into the GEMM epilogue: each
+        rank's kernel stores its rows into every rank's Y buffer over NVLink (CUDA IPC mappings),
+        then a host barrier. Returns the [A, b, n] device tensor (column-major n x b blocks)."""
+        torch = __import__("torch")
+        dist = self._dist()
+        A, b = len(alphas), _signals(x)
+        shape = (A, b, self.n)
+        y = getattr(self, "_yfull", None)
+        if y is None or tuple(y.shape) != shape:
+            y = torch.empty(shape, dtype=torch.complex128, device=self.compute._dev())
+            self._yfull = y
+        world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        peers = self._peer_buffers(y) if world > 1 else []
+        self.compute.apply_gather(np.asarray(alphas, dtype=np.float64), x, y, peers)
+        torch.cuda.synchronize(y.device)
+        if world > 1:
+            dist.barrier(group=self.group)  # every rank's rows have landed in every buffer
+        return y
 
     def apply(self, alphas: Sequence[float], x, plan: Optional[List[Tuple[int, int]]] = None):
         """Full Y = F^alpha X on every rank: local rows, then all_gather of the row blocks."""

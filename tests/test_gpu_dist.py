@@ -92,3 +92,101 @@ def test_sharded_step_wrapper_single_rank():
     assert dl[0] == pytest.approx(d2[0], rel=1e-9, abs=1e-14)
     y = w.apply(cfg.alphas, cfg.x)
     assert rel(y[0], fg.apply_series(g, cfg.alphas, cfg.x)[0]) <= 1e-13
+
+
+@pytest.mark.parametrize("kind,n,b,world", [("graph", 512, 40, 2), ("graph", 300, 9, 3), ("haar", 200, 9, 2),
+                                            ("graph", 1024, 64, 4)])
+def test_fused_gather_epilogue_writes_every_buffer(kind, n, b, world):
+    """fgfrft_shard_apply_gather_dev with the other 'ranks' buffers as peers (here local device
+    buffers standing in for NVLink mappings): after every shard's call, every buffer holds the
+    full Y. graph + n >= 512 + 2b >= 64 exercises the INT8 epilogue path, the rest the DMMA GEMM
+    + P2P push kernel."""
+    import torch
+    f = prep.random_unitary(n, 5) if kind == "haar" else prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.05, 6)))
+    l = 6
+    o = O.PowerCache(f, l)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    alphas = [0.3, 1.7, -0.45]
+    bufs = [torch.full((len(alphas), b, n), float("nan"), dtype=torch.complex128, device="cuda") for _ in range(world)]
+    for rank, (r0, r1) in enumerate(fgd.plan_rows(n, world)):
+        if r1 == r0:
+            continue
+        sh = fgd.CudaShard(f, l, r0, r1)
+        peers = [bufs[q].data_ptr() for q in range(world) if q != rank]
+        sh.apply_gather(alphas, x, bufs[rank], peers)
+        torch.cuda.synchronize()
+        sh.close()
+    for q in range(world):
+        y = bufs[q].cpu().numpy().transpose(0, 2, 1)
+        for i, a in enumerate(alphas):
+            assert rel(y[i], O.fgfrft_matrix(o, a) @ x) <= 1e-12
+
+
+def test_apply_fused_single_rank():
+    cfg = prep.config1()
+    sh = fgd.CudaShard(cfg.f, cfg.l, 0, cfg.n)
+    w = fgd.ShardedFGFRFT(sh, cfg.n, cfg.l)
+    y = w.apply_fused(cfg.alphas, cfg.x).cpu().numpy().transpose(0, 2, 1)
+    assert rel(y[0], w.apply(cfg.alphas, cfg.x)[0]) <= 1e-14
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import paper_2602_20870_b200.dist as fgd_
+    import prep as prep_
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # host collectives: handles, barrier
+    try:
+        n, l, b = 512, 6, 40
+        f = prep_.gft_from_shift(prep_.laplacian(prep_.er_graph(n, 0.05, 6)))
+        r0, r1 = fgd_.plan_rows(n, world)[rank]
+        sh = fgd_.CudaShard(f, l, r0, r1, device=0)
+        w = fgd_.ShardedFGFRFT(sh, n, l)
+        rng = np.random.default_rng(n)
+        x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+        y = w.apply_fused([0.3, 1.7], x)
+        y2 = w.apply_fused([0.3, 1.7], x)  # cached IPC mappings
+        q.put((rank, y.cpu().numpy(), y2.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_apply_fused_two_processes_ipc():
+    """Two ranks (processes) on the one GPU, gloo for the host collectives: the fused-gather apply
+    exchanges CUDA IPC handles, each rank's GEMM epilogue writes its rows into both Y buffers, and
+    both ranks end with the full Y. No kernel waits on the other rank (host barrier only)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(2):
+        rank, y, y2 = q.get(timeout=300)
+        out[rank] = (y, y2)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, l = 512, 6
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.05, 6)))
+    o = O.PowerCache(f, l)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 40)) + 1j * rng.standard_normal((n, 40))
+    for rank in (0, 1):
+        for y in out[rank]:
+            yy = y.transpose(0, 2, 1)
+            for i, a in enumerate([0.3, 1.7]):
+                assert rel(yy[i], O.fgfrft_matrix(o, a) @ x) <= 1e-12
