@@ -241,6 +241,75 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
     }
 }
 
+// Direct forms for plain strided views whose rows are the contiguous direction (rfast: Q, G and
+// the products' operands): one thread per row, 64 K values per block, loads coalesced across
+// the warp's consecutive rows, no shared-memory staging (the tile forms above were issue-bound).
+__device__ __forceinline__ const double* oz_row_ptr(const OzView& v, int row, bool* valid) {
+    const int bt = row / v.rp, rr = row - bt * v.rp;
+    *valid = rr < v.rv;
+    return v.src + (int64_t)bt * v.sbatch + (int64_t)(rr >> v.ra) * v.rs + (rr & v.ra);
+}
+
+__global__ void __launch_bounds__(64) oz_rowmax_direct_kernel(OzView v, unsigned long long* rowmax) {
+    const int row = blockIdx.x * 64 + threadIdx.x, k0 = blockIdx.y * 64;
+    bool ok;
+    const double* p = oz_row_ptr(v, row, &ok);
+    if (!ok) return;
+    const int kn = min(64, v.kv - k0);
+    double m = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < kn; ++i) {
+        const int k = k0 + i;
+        m = fmax(m, fabs(p[(int64_t)(k >> v.ka) * v.ks + (k & v.ka)]));
+    }
+    if (m > 0.0) atomicMax(rowmax + row, (unsigned long long)__double_as_longlong(m));
+}
+
+template <int S>
+__global__ void __launch_bounds__(64) oz_slice_direct_kernel(OzView v, const unsigned long long* rowmax, int tr,
+                                                             int8_t* __restrict__ dst, int* __restrict__ exps) {
+    const int row = blockIdx.x * 64 + threadIdx.x, k0 = blockIdx.y * 64;
+    bool ok;
+    const double* p = oz_row_ptr(v, row, &ok);
+    const double mx = __longlong_as_double((long long)rowmax[row]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    if (blockIdx.y == 0) exps[row] = e;
+    const double sc = mx > 0.0 ? pow2(-e - 1) : 0.0;  // |a| * sc < 1/2
+    constexpr int kBK = OzCfg<S>::bk;
+    const int kb_count = v.kp / kBK;
+    const int rt = row / tr, rr = row - rt * tr;
+    const int r8 = rr & 7;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {  // 16-byte digit runs: K = k0 + 16c .. +15
+        double x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int k = k0 + c * 16 + i;
+            x[i] = (ok && k < v.kv) ? p[(int64_t)(k >> v.ka) * v.ks + (k & v.ka)] * sc : 0.0;
+        }
+        const int kb = (k0 + c * 16) / kBK, cl = c & (kBK / 16 - 1);
+        int8_t* base = dst + ((int64_t)rt * kb_count + kb) * S * tr * kBK + (rr >> 3) * OzCfg<S>::sbo + cl * 128 + r8 * 16;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t packed = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double y = x[q * 4 + i] * kOzBase;
+                    const double t = y + kOzMagic;
+                    x[q * 4 + i] = y - (t - kOzMagic);
+                    packed |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * i);
+                }
+                w[q] = packed;
+            }
+            *reinterpret_cast<uint4*>(base + (int64_t)s * tr * kBK) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- the GEMM
 
 
@@ -543,6 +612,18 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
     cudaError_t e = cudaMemsetAsync(rowmax, 0, (size_t)rows * sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return e;
     dim3 grid(rows / 64, v.kp / 64);
+    if (!v.tiled && v.rfast) {
+        oz_rowmax_direct_kernel<<<grid, 64, 0, stream>>>(v, rowmax);
+        if (slices == 7)
+            oz_slice_direct_kernel<7><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);
+        else if (slices == 8)
+            oz_slice_direct_kernel<8><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);
+        else if (slices == 6)
+            oz_slice_direct_kernel<6><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);
+        else
+            return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
     oz_rowmax_kernel<<<grid, 256, 0, stream>>>(v, rowmax);
     if (slices == 7)
         oz_slice_kernel<7><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
