@@ -131,7 +131,7 @@ cudaError_t launch_dn_residual(const double* w, const double* x, double* r, int6
                                cudaStream_t st);
 cudaError_t launch_dn_grad(const double* u, const double* du, const double* h, const double* r, const double* dqhv,
                            const double* qr, int n, int ch, double* grad, double* part, double* loss, int* flag,
-                           cudaStream_t st);
+                           int epoch, cudaStream_t st);
 cudaError_t launch_dn_track(const double* loss, const double* params, int np, int epoch, double* traj, double* best,
                             int* best_epoch, cudaStream_t st);
 cudaError_t launch_dn_adam(double* params, double* m, double* v, const double* grad, int np, int64_t step, double lr,
@@ -2479,7 +2479,7 @@ int power_products_real(fgfrft_cache* c, const double* src, int64_t ch, double* 
 }
 
 // One evaluation at the device-resident params = [alpha, h_1..h_n]: loss, grad = [d/dalpha, d/dh].
-int denoise_eval_device(fgfrft_denoise* d, const double* params, double* loss, double* grad) {
+int denoise_eval_device(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch = -1) {
     fgfrft_cache* c = d->cache;
     const int l = d->l, T = 2 * l + 1;
     const int64_t cnt = d->n * d->ch, cp = d->cpad;
@@ -2512,7 +2512,7 @@ int denoise_eval_device(fgfrft_denoise* d, const double* params, double* loss, d
     }
     FGB_LAUNCH(launch_dn_grad(d->uu.as<double>(), d->uu.as<double>() + cp, h, d->r.as<double>(),
                               d->ww.as<double>() + cp, d->qr.as<double>(), (int)d->n, (int)d->ch, grad, part, loss,
-                              d->flag.as<int>(), c->stream),
+                              d->flag.as<int>(), epoch, c->stream),
                2);
     return FGFRFT_OK;
 }
@@ -2552,7 +2552,7 @@ int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref,
         d->gpow.ensure(2 * d->l * blk) || d->uu.ensure(2 * blk) || d->ww.ensure(2 * blk) || d->qr.ensure(blk) ||
         d->v.ensure(blk) || d->r.ensure(blk) || d->params.ensure(np * 8) || d->grad.ensure(np * 8) ||
         d->adam.ensure(2 * np * 8) || d->tab.ensure(4 * T * 8) || d->part.ensure(dn_part_elems() * 8) ||
-        d->scal.ensure(8 * 8) || d->best.ensure((np + 1) * 8) || d->flag.ensure(2 * sizeof(int)))
+        d->scal.ensure(8 * 8) || d->best.ensure((np + 1) * 8) || d->flag.ensure(4 * sizeof(int)))
         rc = fail(FGFRFT_CAPACITY, "denoise: device allocation failed");
     if (rc == FGFRFT_OK) {
         cudaMemsetAsync(d->y.p, 0, blk, c->stream);
@@ -2640,22 +2640,33 @@ int fgfrft_denoise_fit(fgfrft_denoise* d, int epochs, double lr, double init_alp
         FGB_CUDA(cudaMemcpyAsync(params, p0.data(), (size_t)np * 8, cudaMemcpyHostToDevice, c->stream));
         FGB_CUDA(cudaMemsetAsync(m, 0, (size_t)2 * np * 8, c->stream));
         FGB_CUDA(cudaMemcpyAsync(best, &inf, 8, cudaMemcpyHostToDevice, c->stream));
-        FGB_CUDA(cudaMemsetAsync(d->flag.p, 0, 2 * sizeof(int), c->stream));
-        FGB_CUDA(cudaStreamSynchronize(c->stream));  // p0 / inf are host stack buffers
+        const int fl0[4] = {0, 0, std::numeric_limits<int>::max(), std::numeric_limits<int>::max()};
+        FGB_CUDA(cudaMemcpyAsync(d->flag.p, fl0, sizeof fl0, cudaMemcpyHostToDevice, c->stream));
+        FGB_CUDA(cudaStreamSynchronize(c->stream));  // p0 / inf / fl0 are host stack buffers
     }
-    for (int e = 0; e <= epochs; ++e) {
-        if (int st = denoise_eval_device(d, params, sl, d->grad.as<double>())) return st;
+    for (int e = 0; e <= epochs; ++e) {  // the final evaluation (e == epochs) is not checked
+        if (int st = denoise_eval_device(d, params, sl, d->grad.as<double>(), e < epochs ? e : -1)) return st;
         FGB_LAUNCH(launch_dn_track(sl, params, np, e, d->traj.as<double>(), best, bep, c->stream), 1);
         if (e < epochs) FGB_LAUNCH(launch_dn_adam(params, m, m + np, d->grad.as<double>(), np, e + 1, lr, c->stream), 1);
     }
-    int flags[2] = {0, 0};
-    FGB_CUDA(cudaMemcpyAsync(flags, d->flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    int flags[4] = {0, 0, 0, 0};
+    FGB_CUDA(cudaMemcpyAsync(flags, d->flag.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     std::vector<double> tr((size_t)2 * (epochs + 1)), bb((size_t)np + 1);
     FGB_CUDA(cudaMemcpyAsync(tr.data(), d->traj.p, tr.size() * 8, cudaMemcpyDeviceToHost, c->stream));
     FGB_CUDA(cudaMemcpyAsync(bb.data(), best, bb.size() * 8, cudaMemcpyDeviceToHost, c->stream));
     FGB_CUDA(cudaStreamSynchronize(c->stream));
-    if (flags[0] & 1) return fail(FGFRFT_OPTIMIZER, "denoise: non-finite loss");
-    if (flags[0] & 2) return fail(FGFRFT_OPTIMIZER, "adam_step: non-finite gradient");
+    // the reference loop stops at the first failing check: loss of epoch e, then the Adam step's
+    // gradient check (step e + 1)
+    if ((flags[0] & 1) && (!(flags[0] & 2) || flags[2] <= flags[3])) {
+        std::ostringstream msg;
+        msg << "denoise: non-finite loss at epoch " << flags[2];
+        return fail(FGFRFT_OPTIMIZER, msg.str());
+    }
+    if (flags[0] & 2) {
+        std::ostringstream msg;
+        msg << "adam_step: non-finite gradient at step " << flags[3] + 1;
+        return fail(FGFRFT_OPTIMIZER, msg.str());
+    }
     for (int e = 0; e <= epochs; ++e) {
         if (traj_loss) traj_loss[e] = tr[2 * e];
         if (traj_alpha) traj_alpha[e] = tr[2 * e + 1];

@@ -85,9 +85,11 @@ __global__ void __launch_bounds__(256) dn_grad_kernel(const double* __restrict__
     if (threadIdx.x == 0) part[kDnBlocks + blockIdx.x] = acc;
 }
 
-// loss = sum part[0][:], grad_alpha = 2 sum part[1][:] (fixed order), non-finite -> flag
+// loss = sum part[0][:], grad_alpha = 2 sum part[1][:] (fixed order). For a training epoch
+// (epoch >= 0) a non-finite loss / gradient sets flag[0] bit 1 / 2 and the first such epoch in
+// flag[2] / flag[3] (learn.hpp:499-505 and adam.hpp:36-42 checks, evaluated after the loop).
 __global__ void dn_finish_kernel(const double* __restrict__ part, double* __restrict__ loss,
-                                 double* __restrict__ grad, int n, int* __restrict__ flag) {
+                                 double* __restrict__ grad, int n, int* __restrict__ flag, int epoch) {
     __shared__ double red[8];
     double a = 0.0, g = 0.0;
     for (int b = threadIdx.x; b < kDnBlocks; b += 256) {
@@ -99,10 +101,17 @@ __global__ void dn_finish_kernel(const double* __restrict__ part, double* __rest
     if (threadIdx.x == 0) {
         *loss = a;
         grad[0] = 2.0 * g;
-        if (!isfinite(a)) atomicOr(flag, 1);
+        if (epoch >= 0 && !isfinite(a)) {
+            atomicOr(flag, 1);
+            atomicMin(flag + 2, epoch);
+        }
     }
+    if (epoch < 0) return;
     for (int i = threadIdx.x; i < n + 1; i += 256)
-        if (!isfinite(grad[i])) atomicOr(flag, 2);
+        if (!isfinite(grad[i])) {
+            atomicOr(flag, 2);
+            atomicMin(flag + 3, epoch);
+        }
 }
 
 // trajectory[epoch] = (loss, alpha); best <- params when loss improves (learn.hpp:483-491)
@@ -154,11 +163,11 @@ cudaError_t launch_dn_residual(const double* w, const double* x, double* r, int6
 }
 cudaError_t launch_dn_grad(const double* u, const double* du, const double* h, const double* r, const double* dqhv,
                            const double* qr, int n, int ch, double* grad, double* part, double* loss, int* flag,
-                           cudaStream_t st) {
+                           int epoch, cudaStream_t st) {
     dn_grad_kernel<<<kDnBlocks, 256, 0, st>>>(u, du, h, r, dqhv, qr, n, ch, grad + 1, part);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dn_finish_kernel<<<1, 256, 0, st>>>(part, loss, grad, n, flag);
+    dn_finish_kernel<<<1, 256, 0, st>>>(part, loss, grad, n, flag, epoch);
     return cudaGetLastError();
 }
 cudaError_t launch_dn_track(const double* loss, const double* params, int np, int epoch, double* traj, double* best,

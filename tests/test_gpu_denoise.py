@@ -61,3 +61,15 @@ def test_denoise_rejects_complex_f():
     g = fg.PowerCache(f, 4)
     with pytest.raises(fg.ParameterError):
         fg.DenoiseProblem(g, np.zeros((64, 2)), np.zeros((64, 2)))
+
+
+def test_denoise_fit_non_finite_loss_reports_epoch():  # learn.hpp:499-505 (optimizer_error)
+    n, l, ch = 64, 6, 2
+    f, x, y = _problem(n, l, ch, 11)
+    y = y.copy()
+    y[3, 1] = np.nan
+    dp = fg.DenoiseProblem(fg.PowerCache(f, l), y, x)
+    loss, ga, gh = dp.eval(0.5, np.ones(n))
+    assert not np.isfinite(loss)                 # a single evaluation just reports it
+    with pytest.raises(fg.OptimizerError, match="non-finite loss at epoch 0"):
+        dp.fit(5, lr=0.01, init_alpha=0.5)
