@@ -77,6 +77,7 @@ typedef enum fgfrft_engine {
 #define FGFRFT_DEFAULT_MEMORY_BUDGET (4ULL << 30)
 
 typedef struct fgfrft_cache fgfrft_cache;
+typedef struct fgfrft_spectrum fgfrft_spectrum; /* spectral form of F, see below */
 
 /* ---- library ----------------------------------------------------------------------- */
 
@@ -304,6 +305,14 @@ int fgfrft_denoise_eval(fgfrft_denoise* problem, double alpha, const double* h, 
 int fgfrft_denoise_fit(fgfrft_denoise* problem, int epochs, double lr, double init_alpha,
                        double* traj_loss, double* traj_alpha, double* alpha_best, double* h_best,
                        double* loss_best, int* best_epoch, double* reconstruction);
+/* Exact backend (ExactDenoiseEngine, learn.hpp:205-289) on a device spectrum, any unitary F:
+ * F^a = V diag(e^{j a theta}) V^H, six FP64 tensor-core ZGEMMs per evaluation; loss on the
+ * complex residual, or on its real part when loss_on_real. eval / fit / reconstruct / destroy as
+ * for the fast backend. */
+int fgfrft_denoise_create_exact(fgfrft_spectrum* spectrum, const double* y, const double* x_ref,
+                                int64_t channels, int loss_on_real, fgfrft_denoise** out);
+/* Re(Q^{-alpha} h o Q^alpha y) at (alpha, h): n x channels real (learn.hpp:232-234, 405-408). */
+int fgfrft_denoise_reconstruct(fgfrft_denoise* problem, double alpha, const double* h, double* out);
 
 /* ---- on-disk power cache ----------------------------------------------
  *
@@ -331,7 +340,6 @@ int fgfrft_cache_load(const char* path, uint64_t memory_budget, int device, fgfr
  * V diag(j theta e^{j a theta}) V^H (FGFRFT_DQ, exact_gfrft_grad, :169-174) for every order; one
  * column scaling and one FP64 tensor-core GEMM per order. out: n_alpha blocks of n x n.
  */
-typedef struct fgfrft_spectrum fgfrft_spectrum;
 int fgfrft_spectrum_create(const double* v, const double* theta, int64_t n, int device,
                            fgfrft_spectrum** out);
 int fgfrft_spectrum_decompose(const double* f, int64_t n, int device, fgfrft_spectrum** out);

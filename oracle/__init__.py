@@ -24,6 +24,7 @@ Restated reference functions (file:line under /root/reference/proj/include/fgfrf
   cascade dL/dalpha (K=1)            learn.hpp:88-92
   Cascade / learn_orders             learn.hpp:55-166 (any depth, fast and exact backends)
   FastDenoiseEngine (real F), Adam   learn.hpp:291-413, learn.hpp:471-516, adam.hpp:34-53
+  ExactDenoiseEngine                 learn.hpp:205-289
 """
 from __future__ import annotations
 
@@ -452,6 +453,44 @@ class FastDenoise:
     def reconstruct(self, alpha: float, h: np.ndarray) -> np.ndarray:
         c, _ = sinc_coeffs(alpha, self.l)
         return self._run(c, h)[2]
+
+
+class ExactDenoise:
+    """learn.hpp:205-289 ExactDenoiseEngine: F^a = V diag(e^{j a theta}) V^H on the spectrum,
+    loss on the complex residual (or its real part with loss_on_real)."""
+
+    def __init__(self, y: np.ndarray, x: np.ndarray, eig, loss_on_real: bool = False):
+        self.y, self.x = np.asarray(y, float), np.asarray(x, float)
+        self.v, self.theta = eig
+        self.loss_on_real = bool(loss_on_real)
+        self.ytil = self.v.conj().T @ self.y.astype(np.complex128)
+
+    def _run(self, alpha: float, h: np.ndarray):
+        phase = np.exp(1j * alpha * self.theta)
+        u = self.v @ (phase[:, None] * self.ytil)
+        b = self.v.conj().T @ (h[:, None] * u)
+        w = self.v @ (phase.conj()[:, None] * b)
+        if self.loss_on_real:
+            r = w.real - self.x
+            return phase, u, b, w, r.astype(np.complex128), float(np.sum(r * r))
+        cot = w - self.x
+        return phase, u, b, w, cot, float(np.vdot(cot, cot).real)
+
+    def eval(self, alpha: float, h: np.ndarray):
+        """-> (loss, grad_alpha, grad_h), learn.hpp:211-229."""
+        phase, u, b, w, cot, loss = self._run(alpha, h)
+        vh_r = self.v.conj().T @ cot
+        far = self.v @ (phase[:, None] * vh_r)
+        grad_h = 2.0 * np.sum((far.conj() * u).real, axis=1)
+        jt = 1j * self.theta
+        t1 = (-jt * phase.conj())[:, None] * b
+        ga = 2.0 * float(np.sum((vh_r.conj() * t1).real))
+        q = self.v @ ((jt * phase)[:, None] * self.ytil)
+        ga += 2.0 * float(np.sum((far.conj() * (h[:, None] * q)).real))
+        return loss, ga, grad_h
+
+    def reconstruct(self, alpha: float, h: np.ndarray) -> np.ndarray:
+        return self._run(alpha, h)[3].real
 
 
 def adam_step(params, m, v, grad, step, lr, beta1=0.9, beta2=0.999, eps=1e-8):

@@ -138,6 +138,8 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cache_save": (i, [vp, ctypes.c_char_p]),
         "fgfrft_shard_mse_dlda_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
         "fgfrft_shard_apply_gather_dev": (i, [vp, vp, i, vp, i64, vp, vp, i]),
+        "fgfrft_denoise_create_exact": (i, [vp, vp, vp, i64, i, pp]),
+        "fgfrft_denoise_reconstruct": (i, [vp, d, vp, vp]),
         "fgfrft_ipc_get": (i, [vp, vp, vp]),
         "fgfrft_ipc_open": (i, [vp, i, pp]),
         "fgfrft_ipc_close": (i, [vp]),
@@ -171,6 +173,7 @@ def exported_symbols():
         "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
         "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
         "fgfrft_shard_apply_gather_dev", "fgfrft_ipc_get", "fgfrft_ipc_open", "fgfrft_ipc_close",
+        "fgfrft_denoise_create_exact", "fgfrft_denoise_reconstruct",
     ]
 
 
@@ -510,19 +513,37 @@ def dgemm_int8(a, b, slices: int = 0):
 
 
 class DenoiseProblem:
-    """GPU-resident denoising learner (learn.hpp:291-516 on the device, real F): y, x_ref are
-    n x C real host arrays; eval(alpha, h) -> (loss, grad_alpha, grad_h); fit(...) runs Adam."""
+    """GPU-resident denoising learner (learn.hpp:168-516 on the device): y, x_ref are n x C real
+    host arrays; eval(alpha, h) -> (loss, grad_alpha, grad_h); fit(...) runs Adam.
+    ``DenoiseProblem(cache, y, x)``: fast backend (real F, power products on the INT8 engine);
+    ``DenoiseProblem.exact(eig, y, x, loss_on_real)``: exact backend on a device spectrum."""
 
-    def __init__(self, cache: PowerCache, y: np.ndarray, x_ref: np.ndarray):
+    def __init__(self, cache: Optional[PowerCache], y: np.ndarray, x_ref: np.ndarray,
+                 eig: Optional["UnitaryEigen"] = None, loss_on_real: bool = False):
         y = np.asfortranarray(np.asarray(y, dtype=np.float64))
         x = np.asfortranarray(np.asarray(x_ref, dtype=np.float64))
-        if y.shape != x.shape or y.shape[0] != cache.n():
+        n = cache.n() if cache is not None else eig.n()
+        if y.shape != x.shape or y.shape[0] != n:
             raise ShapeError("denoise: signal shape mismatch")
         self.n, self.ch = y.shape
-        self.cache = cache  # keeps the cache alive
+        self.cache, self.eig = cache, eig  # keep the handles alive
         self._h = ctypes.c_void_p()
-        _check(lib().fgfrft_denoise_create(cache.handle, y.ctypes.data, x.ctypes.data, self.ch,
-                                           ctypes.byref(self._h)))
+        if cache is not None:
+            _check(lib().fgfrft_denoise_create(cache.handle, y.ctypes.data, x.ctypes.data, self.ch,
+                                               ctypes.byref(self._h)))
+        else:
+            _check(lib().fgfrft_denoise_create_exact(eig.handle, y.ctypes.data, x.ctypes.data, self.ch,
+                                                     int(bool(loss_on_real)), ctypes.byref(self._h)))
+
+    @classmethod
+    def exact(cls, eig: "UnitaryEigen", y: np.ndarray, x_ref: np.ndarray, loss_on_real: bool = False):
+        return cls(None, y, x_ref, eig=eig, loss_on_real=loss_on_real)
+
+    def reconstruct(self, alpha: float, h: np.ndarray) -> np.ndarray:
+        h = np.ascontiguousarray(h, dtype=np.float64)
+        out = np.empty((self.n, self.ch), order="F")
+        _check(lib().fgfrft_denoise_reconstruct(self._h, float(alpha), h.ctypes.data, out.ctypes.data))
+        return out
 
     def close(self):
         h, self._h = getattr(self, "_h", None), None

@@ -182,4 +182,114 @@ cudaError_t launch_dn_adam(double* params, double* m, double* v, const double* g
 }
 size_t dn_part_elems() { return 2 * (size_t)kDnBlocks; }
 
+// ---------------------------------------------------------------- exact backend (learn.hpp:205-289)
+//
+// F^a = V diag(e^{j a theta}) V^H on the device spectrum; every product with V / V^H is a DMMA
+// ZGEMM (capi.cu), these kernels are the diagonal scalings and the reductions around them. All
+// blocks are n x ch complex128, column-major; row i of a spectral-domain block is eigen index i.
+
+// phase = e^{j a theta}, jtp = j theta e^{j a theta}, jtc = -j theta e^{-j a theta}; a = params[0]
+__global__ void dnx_phase_kernel(const double* __restrict__ params, const double* __restrict__ theta, int n,
+                                 double2* __restrict__ phase, double2* __restrict__ jtp, double2* __restrict__ jtc) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double th = theta[k];
+    double s, c;
+    sincos(params[0] * th, &s, &c);
+    phase[k] = make_double2(c, s);
+    jtp[k] = make_double2(-th * s, th * c);  // (j th)(c + j s)
+    jtc[k] = make_double2(-th * s, -th * c); // (-j th)(c - j s)
+}
+
+// dst[i, c] = d[i] src[i, c] (conj_d: conj(d[i])); real_h: d is the real filter h = params + 1
+__global__ void dnx_rowscale_kernel(const double2* __restrict__ src, const double2* __restrict__ d,
+                                    const double* __restrict__ h, bool conj_d, int n, int64_t count,
+                                    double2* __restrict__ dst) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(p % n);
+        const double2 v = src[p];
+        if (h) {
+            dst[p] = make_double2(h[i] * v.x, h[i] * v.y);
+        } else {
+            const double dx = d[i].x, dy = conj_d ? -d[i].y : d[i].y;
+            dst[p] = make_double2(fma(dx, v.x, -dy * v.y), fma(dx, v.y, dy * v.x));
+        }
+    }
+}
+
+// cot = w - x (or Re w - x with loss_on_real), part[blk] = sum |cot|^2
+__global__ void __launch_bounds__(256) dnx_cot_kernel(const double2* __restrict__ w, const double* __restrict__ x,
+                                                      int64_t count, bool real_loss, double2* __restrict__ cot,
+                                                      double* __restrict__ part) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x) {
+        const double2 r = make_double2(w[p].x - x[p], real_loss ? 0.0 : w[p].y);
+        cot[p] = r;
+        acc = fma(r.x, r.x, fma(r.y, r.y, acc));
+    }
+    acc = block_sum256(acc, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// grad_h[i] = 2 sum_c Re(conj(far[i, c]) u[i, c]);
+// part[kDnBlocks + blk] = sum Re(conj(vhr) jtc o b) + Re(conj(far) h o q)  (grad_alpha / 2)
+__global__ void __launch_bounds__(256) dnx_grad_kernel(const double2* __restrict__ far, const double2* __restrict__ u,
+                                                       const double2* __restrict__ vhr, const double2* __restrict__ b,
+                                                       const double2* __restrict__ jtc, const double2* __restrict__ q,
+                                                       const double* __restrict__ h, int n, int ch,
+                                                       double* __restrict__ grad_h, double* __restrict__ part) {
+    __shared__ double red[8];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int c = 0; c < ch; ++c) {
+            const double2 f = far[i + (int64_t)c * n], uu = u[i + (int64_t)c * n];
+            acc = fma(f.x, uu.x, fma(f.y, uu.y, acc));
+        }
+        grad_h[i] = 2.0 * acc;
+    }
+    const int64_t count = (int64_t)n * ch;
+    double acc = 0.0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(p % n);
+        const double2 t = make_double2(fma(jtc[i].x, b[p].x, -jtc[i].y * b[p].y), fma(jtc[i].x, b[p].y, jtc[i].y * b[p].x));
+        acc = fma(vhr[p].x, t.x, fma(vhr[p].y, t.y, acc));
+        const double2 hq = make_double2(h[i] * q[p].x, h[i] * q[p].y);
+        acc = fma(far[p].x, hq.x, fma(far[p].y, hq.y, acc));
+    }
+    acc = block_sum256(acc, red);
+    if (threadIdx.x == 0) part[kDnBlocks + blockIdx.x] = acc;
+}
+
+cudaError_t launch_dnx_phase(const double* params, const double* theta, int n, void* phase, void* jtp, void* jtc,
+                             cudaStream_t st) {
+    dnx_phase_kernel<<<(n + 127) / 128, 128, 0, st>>>(params, theta, n, (double2*)phase, (double2*)jtp,
+                                                      (double2*)jtc);
+    return cudaGetLastError();
+}
+cudaError_t launch_dnx_rowscale(const void* src, const void* d, const double* h, bool conj_d, int n, int64_t count,
+                                void* dst, cudaStream_t st) {
+    dnx_rowscale_kernel<<<kDnBlocks, 256, 0, st>>>((const double2*)src, (const double2*)d, h, conj_d, n, count,
+                                                   (double2*)dst);
+    return cudaGetLastError();
+}
+cudaError_t launch_dnx_cot(const void* w, const double* x, int64_t count, bool real_loss, void* cot, double* part,
+                           cudaStream_t st) {
+    dnx_cot_kernel<<<kDnBlocks, 256, 0, st>>>((const double2*)w, x, count, real_loss, (double2*)cot, part);
+    return cudaGetLastError();
+}
+cudaError_t launch_dnx_grad(const void* far, const void* u, const void* vhr, const void* b, const void* jtc,
+                            const void* q, const double* h, int n, int ch, double* grad_h, double* part,
+                            cudaStream_t st) {
+    dnx_grad_kernel<<<kDnBlocks, 256, 0, st>>>((const double2*)far, (const double2*)u, (const double2*)vhr,
+                                               (const double2*)b, (const double2*)jtc, (const double2*)q, h, n, ch,
+                                               grad_h, part);
+    return cudaGetLastError();
+}
+cudaError_t launch_dn_finish(const double* part, double* loss, double* grad, int n, int* flag, int epoch,
+                             cudaStream_t st) {
+    dn_finish_kernel<<<1, 256, 0, st>>>(part, loss, grad, n, flag, epoch);
+    return cudaGetLastError();
+}
+
 }  // namespace fgb

@@ -73,3 +73,44 @@ def test_denoise_fit_non_finite_loss_reports_epoch():  # learn.hpp:499-505 (opti
     assert not np.isfinite(loss)                 # a single evaluation just reports it
     with pytest.raises(fg.OptimizerError, match="non-finite loss at epoch 0"):
         dp.fit(5, lr=0.01, init_alpha=0.5)
+
+
+@pytest.mark.parametrize("kind,loss_on_real", [("grid", False), ("synthetic", False), ("synthetic", True)])
+def test_exact_denoise_backend_matches_oracle(kind, loss_on_real):  # learn.hpp:205-289, acceptance.cpp:183-226
+    if kind == "grid":
+        f = prep.gft_from_shift(prep.laplacian(prep.grid_graph(8, 8)))
+        ve, te = O.eigendecompose_unitary(f)
+    else:
+        f, ve, te = prep.synthetic_unitary(prep.spread_phases(48, 0.2, 4), 21)
+    n = f.shape[0]
+    rng = np.random.default_rng(600)
+    x = rng.standard_normal((n, 3))
+    y = x + 0.5 * rng.standard_normal((n, 3))
+    ref = O.ExactDenoise(y, x, (ve, te), loss_on_real)
+    dp = fg.DenoiseProblem.exact(fg.UnitaryEigen(v=ve, theta=te), y, x, loss_on_real)
+    for alpha in (-1.0, 0.37, 1.6):
+        h = 1.0 + 0.3 * rng.standard_normal(n)
+        loss, ga, gh = dp.eval(alpha, h)
+        lr, gar, ghr = ref.eval(alpha, h)
+        assert abs(loss - lr) <= 1e-10 * lr
+        assert abs(ga - gar) <= 1e-9 * max(1.0, abs(gar))
+        assert np.linalg.norm(gh - ghr) <= 1e-9 * np.linalg.norm(ghr)
+        assert np.linalg.norm(dp.reconstruct(alpha, h) - ref.reconstruct(alpha, h)) <= 1e-10 * np.linalg.norm(y)
+        # finite differences of the device loss (acceptance.cpp:201-220)
+        fd = (dp.eval(alpha + 1e-4, h)[0] - dp.eval(alpha - 1e-4, h)[0]) / 2e-4
+        assert abs(ga - fd) / max(abs(fd), 1e-12) <= 1e-5
+
+
+def test_exact_denoise_fit_matches_reference_loop():
+    f, ve, te = prep.synthetic_unitary(prep.spread_phases(40, 0.2, 4), 21)
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((40, 2))
+    y = x + 0.3 * rng.standard_normal((40, 2))
+    ref = O.ExactDenoise(y, x, (ve, te))
+    traj, ab, hb, lb, be = O.denoise_fit(ref, 15, 0.01, 0.5)
+    dp = fg.DenoiseProblem.exact(fg.UnitaryEigen(v=ve, theta=te), y, x)
+    out = dp.fit(15, lr=0.01, init_alpha=0.5, want_reconstruction=True)
+    tl = np.array([t[0] for t in traj])
+    assert np.max(np.abs(out["traj_loss"] - tl) / tl) <= 1e-8
+    assert out["best_epoch"] == be
+    assert np.linalg.norm(out["reconstruction"] - ref.reconstruct(ab, hb)) <= 1e-8 * np.linalg.norm(y)

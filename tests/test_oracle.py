@@ -304,3 +304,24 @@ def test_cascade_learned_orders_additivity():  # test_learn.cpp:104-120 (k = 1)
     tl, ta, fl, fa = O.learn_orders(prob, 1, 0.1, 200, 0.01)
     assert fl <= 1e-4
     assert abs(fa.sum() - 1.5) <= 0.01
+
+
+@pytest.mark.parametrize("loss_on_real", [False, True])
+def test_exact_denoise_gradients_finite_differences(loss_on_real):  # acceptance.cpp:183-226 (exact)
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(24, 0.2, 4), 21)
+    rng = prep.Rng(600)
+    n = 24
+    x = np.array([[rng.gaussian()] for _ in range(n)])
+    y = x + 0.5 * np.array([[rng.gaussian()] for _ in range(n)])
+    prob = O.ExactDenoise(y, x, (v, th), loss_on_real)
+    alpha = 0.37
+    h = 1.0 + 0.3 * np.array([rng.gaussian() for _ in range(n)])
+    loss, ga, gh = prob.eval(alpha, h)
+    fd_a = _central(lambda a: prob.eval(a, h)[0], alpha)
+    assert _rel_err(ga, fd_a) <= 1e-5
+    for idx in (0, n // 2):
+        def lh(val, idx=idx):
+            hh = h.copy()
+            hh[idx] = val
+            return prob.eval(alpha, hh)[0]
+        assert _rel_err(gh[idx], _central(lh, h[idx])) <= 1e-5
