@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <limits>
 #include <memory>
 #include <optional>
 #include <vector>
@@ -116,6 +117,140 @@ inline OrderLearnResult learn_orders(const GftMatrix& f, const CascadeConfig& cf
     }
     out.final_alphas = fa;
     for (double a : fa) out.final_alpha_sum += a;
+    return out;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Joint order/filter denoising (learn.hpp:168-516)
+
+struct DenoiseConfig {  // learn.hpp:168-184
+    int truncation = 10;
+    int epochs = 300;
+    double lr = 0.01;
+    double init_alpha = 0.5;
+    double sigma = 0.0;
+    std::uint64_t seed = 0;
+    bool loss_on_real = false;
+
+    void validate() const {
+        if (truncation < 1) throw parameter_error("DenoiseConfig: truncation must be >= 1");
+        if (epochs < 1) throw parameter_error("DenoiseConfig: epochs must be >= 1");
+        if (!(lr > 0.0)) throw parameter_error("DenoiseConfig: lr must be positive");
+        if (sigma < 0.0) throw parameter_error("DenoiseConfig: sigma must be >= 0");
+    }
+};
+
+struct FilterDiag {
+    VectorXd h;
+};
+
+namespace detail {
+struct DenoiseEval {
+    double loss = 0.0;
+    double grad_alpha = 0.0;
+    VectorXd grad_h;
+};
+}  // namespace detail
+
+// Real n x C matrix at the denoising boundary (Eigen::MatrixXd when Eigen is present).
+#ifdef FGFRFT_HAVE_EIGEN
+using MatrixXdN = Eigen::MatrixXd;
+#else
+struct MatrixXdN {
+    MatrixXdN() = default;
+    MatrixXdN(Index r, Index c) : r_(r), c_(c), d_(static_cast<size_t>(r * c), 0.0) {}
+    Index rows() const { return r_; }
+    Index cols() const { return c_; }
+    double* data() { return d_.data(); }
+    const double* data() const { return d_.data(); }
+    double& operator()(Index i, Index j) { return d_[static_cast<size_t>(i + j * r_)]; }
+    const double& operator()(Index i, Index j) const { return d_[static_cast<size_t>(i + j * r_)]; }
+
+  private:
+    Index r_ = 0, c_ = 0;
+    std::vector<double> d_;
+};
+#endif
+
+class DenoiseProblem {  // learn.hpp:439-467
+  public:
+    DenoiseProblem(const MatrixXdN& y, const MatrixXdN& x_ref, const GftMatrix& f, const DenoiseConfig& cfg,
+                   Backend backend, std::shared_ptr<const UnitaryEigen> spectrum = nullptr, int device = 0)
+        : n_(f.n()), ch_(y.cols()) {
+        cfg.validate();
+        if (y.rows() != x_ref.rows() || y.cols() != x_ref.cols())
+            throw shape_error("denoise: noisy and reference signals have mismatched channels");
+        if (y.rows() != f.n()) throw shape_error("denoise: signal length does not match the graph");
+        fgfrft_denoise* h = nullptr;
+        if (backend == Backend::exact) {
+            if (!spectrum) spectrum = std::make_shared<UnitaryEigen>(eigendecompose_unitary(f, device));
+            spec_ = spectrum;
+            detail::throw_status(fgfrft_denoise_create_exact(spectrum->device_handle(device), y.data(), x_ref.data(),
+                                                             ch_, cfg.loss_on_real ? 1 : 0, &h));
+        } else {
+            if (!f.is_real())
+                throw parameter_error("denoise: the device fast backend needs a real F (use Backend::exact)");
+            cache_.emplace(f, cfg.truncation, std::uint64_t(1) << 40, device);
+            detail::throw_status(fgfrft_denoise_create(cache_->handle(), y.data(), x_ref.data(), ch_, &h));
+        }
+        h_.reset(h, [](fgfrft_denoise* p) { fgfrft_denoise_destroy(p); });
+    }
+
+    detail::DenoiseEval eval(double alpha, const VectorXd& h) const {
+        detail::DenoiseEval out;
+        out.grad_h = VectorXd(n_);
+        detail::throw_status(fgfrft_denoise_eval(h_.get(), alpha, h.data(), &out.loss, &out.grad_alpha,
+                                                 out.grad_h.data()));
+        return out;
+    }
+    MatrixXdN reconstruct(double alpha, const VectorXd& h) const {
+        MatrixXdN out(n_, ch_);
+        detail::throw_status(fgfrft_denoise_reconstruct(h_.get(), alpha, h.data(), out.data()));
+        return out;
+    }
+    Index n() const { return n_; }
+    fgfrft_denoise* handle() const { return h_.get(); }
+    Index channels() const { return ch_; }
+
+  private:
+    Index n_ = 0, ch_ = 0;
+    std::optional<PowerCache> cache_;
+    std::shared_ptr<const UnitaryEigen> spec_;
+    std::shared_ptr<fgfrft_denoise> h_;
+};
+
+struct DenoiseTrajectoryPoint {
+    int epoch = 0;
+    double loss = 0.0;
+    double alpha = 0.0;
+};
+
+struct DenoiseResult {  // learn.hpp:423-430
+    double alpha_best = 0.0;
+    FilterDiag filter_best;
+    MatrixXdN reconstruction;
+    std::vector<DenoiseTrajectoryPoint> trajectory;
+    double loss_best = 0.0;
+    int best_epoch = 0;
+};
+
+// learn.hpp:470-516: Adam over [alpha, h] from [init_alpha, 1..1] on the device.
+inline DenoiseResult denoise(const MatrixXdN& y, const MatrixXdN& x_ref, const GftMatrix& f, const DenoiseConfig& cfg,
+                             Backend backend, std::shared_ptr<const UnitaryEigen> spectrum = nullptr,
+                             int device = 0) {
+    cfg.validate();
+    const DenoiseProblem problem(y, x_ref, f, cfg, backend, std::move(spectrum), device);
+    const Index n = f.n();
+    const int e = cfg.epochs;
+    std::vector<double> tl(static_cast<size_t>(e + 1)), ta(static_cast<size_t>(e + 1));
+    DenoiseResult out;
+    out.filter_best.h = VectorXd(n);
+    out.reconstruction = MatrixXdN(n, problem.channels());
+    detail::throw_status(fgfrft_denoise_fit(problem.handle(), e, cfg.lr, cfg.init_alpha, tl.data(), ta.data(),
+                                            &out.alpha_best, out.filter_best.h.data(), &out.loss_best,
+                                            &out.best_epoch, out.reconstruction.data()));
+    out.trajectory.reserve(static_cast<size_t>(e + 1));
+    for (int i = 0; i <= e; ++i) out.trajectory.push_back({i, tl[static_cast<size_t>(i)], ta[static_cast<size_t>(i)]});
     return out;
 }
 

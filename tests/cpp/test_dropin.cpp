@@ -392,6 +392,45 @@ int main() {
         CHECK_THROWS_AS(PowerCache::load(path, 1024), capacity_error);
         std::remove(path.c_str());
     }
+    // learn.hpp denoising: both backends through the drop-in header (acceptance.cpp:183-226 style)
+    {
+        const GftMatrix f = householder_real(48, 5);
+        const Index n = 48;
+        std::mt19937_64 gen(600);
+        std::normal_distribution<double> nd;
+        MatrixXdN x(n, 1), y(n, 1);
+        for (Index i = 0; i < n; ++i) {
+            x(i, 0) = nd(gen);
+            y(i, 0) = x(i, 0) + 0.5 * nd(gen);
+        }
+        DenoiseConfig cfg;
+        cfg.truncation = 8;
+        for (Backend backend : {Backend::fast, Backend::exact}) {
+            const DenoiseProblem problem(y, x, f, cfg, backend);
+            for (int state = 0; state < 3; ++state) {
+                const double alpha = -0.5 + 0.9 * state;
+                VectorXd h(n);
+                for (Index i = 0; i < n; ++i) h(i) = 1.0 + 0.3 * nd(gen);
+                const auto ev = problem.eval(alpha, h);
+                const double fd = (problem.eval(alpha + 1e-4, h).loss - problem.eval(alpha - 1e-4, h).loss) / 2e-4;
+                CHECK(std::fabs(ev.grad_alpha - fd) / std::max(std::fabs(fd), 1e-12) <= 1e-5);
+                VectorXd hp = h, hm = h;
+                hp(n / 2) += 1e-4;
+                hm(n / 2) -= 1e-4;
+                const double fdh = (problem.eval(alpha, hp).loss - problem.eval(alpha, hm).loss) / 2e-4;
+                CHECK(std::fabs(ev.grad_h(n / 2) - fdh) / std::max(std::fabs(fdh), 1e-12) <= 1e-5);
+            }
+        }
+        cfg.epochs = 20;
+        const DenoiseResult r = denoise(y, x, f, cfg, Backend::fast);
+        CHECK(r.trajectory.size() == 21);
+        CHECK(r.loss_best <= r.trajectory.front().loss);
+        CHECK(r.reconstruction.rows() == n && r.reconstruction.cols() == 1);
+        CHECK_THROWS_AS(denoise(y, x, householder_unitary(48, 2), cfg, Backend::fast), parameter_error);
+        DenoiseConfig bad;
+        bad.epochs = 0;
+        CHECK_THROWS_AS(denoise(y, x, f, bad, Backend::fast), parameter_error);
+    }
     std::printf("drop-in C++ tests: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail;
 }
