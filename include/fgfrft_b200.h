@@ -279,6 +279,13 @@ int fgfrft_shard_mse_dlda_partial_dev(fgfrft_cache* shard, const double* alphas,
  */
 /* Default digit count of the library's INT8 engine (6). */
 int fgfrft_int8_digits(void);
+/* Complex128 GEMM on the same engine: C (m x n, column-major ldc) = op(A) op(B), trans 0 = N,
+ * 1 = T, 2 = C (conjugate transpose); interleaved (re, im) doubles. Computed as ONE real Ozaki
+ * GEMM with K doubled (A' = [Re, -Im], B' = [[Re, Im], [Im, -Re]] per element, the epilogue merges
+ * column pairs into (Re C, Im C)): 8 m n k FP64-equivalent flops. k <= 8192. */
+int fgfrft_zgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a,
+                          int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                          void* stream);
 int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                           const double* b, int64_t ldb, double* c, int64_t ldc, int slices,
                           void* stream);

@@ -139,6 +139,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_shard_mse_dlda_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
         "fgfrft_shard_apply_gather_dev": (i, [vp, vp, i, vp, i64, vp, vp, i]),
         "fgfrft_denoise_create_exact": (i, [vp, vp, vp, i64, i, pp]),
+        "fgfrft_zgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]),
         "fgfrft_denoise_reconstruct": (i, [vp, d, vp, vp]),
         "fgfrft_ipc_get": (i, [vp, vp, vp]),
         "fgfrft_ipc_open": (i, [vp, i, pp]),
@@ -173,7 +174,7 @@ def exported_symbols():
         "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
         "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
         "fgfrft_shard_apply_gather_dev", "fgfrft_ipc_get", "fgfrft_ipc_open", "fgfrft_ipc_close",
-        "fgfrft_denoise_create_exact", "fgfrft_denoise_reconstruct",
+        "fgfrft_denoise_create_exact", "fgfrft_denoise_reconstruct", "fgfrft_zgemm_int8_dev",
     ]
 
 
@@ -510,6 +511,28 @@ def dgemm_int8(a, b, slices: int = 0):
     _check(lib().fgfrft_dgemm_int8_dev(1, 1, m, n, k, a.data_ptr(), k, b.data_ptr(), n, ct.data_ptr(), m, slices,
                                        ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)))
     return ct.t()
+
+
+def zgemm_int8(a, b, op_a: str = "N", op_b: str = "N"):
+    """C = op(A) op(B) for complex128 torch CUDA tensors on the INT8 tensor cores (one real Ozaki
+    GEMM with K doubled), through fgfrft_zgemm_int8_dev. op: "N", "T" or "C" (conjugate
+    transpose). Operands are passed as column-major (a torch (r, c) row-major tensor is the
+    column-major c x r matrix of its transpose)."""
+    import torch
+    assert a.dtype == torch.complex128 and b.dtype == torch.complex128 and a.is_cuda and b.is_cuda
+    code = {"N": 0, "T": 1, "C": 2}
+    # column-major views: A_cm = a^T (shape (a.shape[1], a.shape[0])), likewise B
+    acm = a.contiguous()
+    bcm = b.contiguous()
+    ar, ac = acm.shape[1], acm.shape[0]   # column-major rows / cols
+    br, bc = bcm.shape[1], bcm.shape[0]
+    m, k = (ar, ac) if op_a == "N" else (ac, ar)
+    k2, n = (br, bc) if op_b == "N" else (bc, br)
+    assert k == k2
+    ct = torch.empty((n, m), dtype=torch.complex128, device=a.device)
+    _check(lib().fgfrft_zgemm_int8_dev(code[op_a], code[op_b], m, n, k, acm.data_ptr(), ar, bcm.data_ptr(), br,
+                                       ct.data_ptr(), m, ctypes.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)))
+    return ct  # column-major m x n (i.e. ct.T is C)
 
 
 class DenoiseProblem:

@@ -672,9 +672,20 @@ int resolve_truncation(const fgfrft_cache* c, int truncation, int which, int* l_
     return FGFRFT_OK;
 }
 
-// Complex GEMM in the cache's arithmetic: DMMA complex128 or FP32 complex64.
+int engine_of(const fgfrft_cache* c);
+bool complex_int8_default(int64_t m, int64_t n, int64_t k);
+int zgemm_auto(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda, int64_t sa,
+               const void* b, int64_t ldb, int64_t sb, void* c, int64_t ldc, int64_t sc, int batch, cudaStream_t st);
+
+// Complex GEMM in the cache's arithmetic: complex128 on the INT8 engine (large products, engine
+// not DMMA) or DMMA; FP32 for complex64.
 cudaError_t gemm(const fgfrft_cache* c, int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a,
                  const void* B, int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch) {
+    if (c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA && complex_int8_default(M, N, K)) {
+        const int r = zgemm_auto(conj_a ? 2 : 0, conj_b ? 2 : 0, M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch,
+                                 c->stream);
+        return r == FGFRFT_OK ? cudaSuccess : cudaErrorUnknown;
+    }
     if (c->dtype == FGFRFT_C128)
         return launch_zgemm(M, N, K, A, lda, sA, conj_a, B, ldb, sB, conj_b, C, ldc, sC, batch, false, c->stream);
     return launch_cgemm(M, N, K, A, lda, sA, conj_a, B, ldb, sB, conj_b, C, ldc, sC, batch, false, c->stream);
@@ -2450,6 +2461,93 @@ int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
     FGB_GUARD_END
 }
 
+namespace {
+
+// Complex product on the INT8 engine: C (m x n, column-major ldc, complex128) = op(A) op(B),
+// op 0 = N, 1 = T, 2 = C (conjugate transpose), as ONE real Ozaki GEMM with K doubled:
+// A'(r, 2k + e) = (Re, -Im)[e] of op(A)(r, k), B'(2j + c, 2k + e) = [[Re, Im], [Im, -Re]][c][e] of
+// op(B)(k, j), so A' B'^T holds (Re C, Im C) in column pairs (2j, 2j + 1) -- the CM 1 epilogue.
+int zgemm_int8(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda, const void* b,
+               int64_t ldb, void* c, int64_t ldc, cudaStream_t st) {
+    const int slices = oz_slices_default();
+    if (2 * k > 16384) return fail(FGFRFT_SHAPE, "zgemm_int8: k must be <= 8192");
+    keep_pool();
+    const int64_t mp = ceil_div(m, kOzTileA) * kOzTileA, np = ceil_div(2 * n, kOzTileB) * kOzTileB;
+    const int64_t kp = ceil_div(2 * k, kOzK) * kOzK;
+    const size_t abytes = (size_t)slices * mp * kp, bbytes = (size_t)slices * np * kp;
+    const size_t total = abytes + bbytes + (size_t)(mp + np) * (sizeof(int) + sizeof(unsigned long long)) + 256;
+    char* ws = nullptr;
+    FGB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), total, st));
+    int8_t* sa = reinterpret_cast<int8_t*>(ws);
+    int8_t* sb = sa + abytes;
+    unsigned long long* rmax = reinterpret_cast<unsigned long long*>(sb + bbytes);
+    int* ea = reinterpret_cast<int*>(rmax + mp + np);
+    int* eb = ea + mp;
+    OzView va{static_cast<const double*>(a), opa == 0 ? 1 : lda, opa == 0 ? lda : 1, 0, 0, opa == 2 ? 1 : 0, (int)m,
+              (int)mp, 1, (int)(2 * k), (int)kp, opa == 0};
+    va.tiled = 5;
+    OzView vb{static_cast<const double*>(b), opb == 0 ? ldb : 1, opb == 0 ? 1 : ldb, 0, 1, opb == 2 ? 1 : 0,
+              (int)(2 * n), (int)np, 1, (int)(2 * k), (int)kp, opb != 0};
+    vb.tiled = 5;
+    cudaError_t e;
+    {
+        ProfScope ps(KC_SLICE, st);
+        e = launch_oz_slice(va, slices, kOzTileA, sa, ea, rmax, st);
+        if (e == cudaSuccess) e = launch_oz_slice(vb, slices, kOzTileB, sb, eb, rmax + mp, st);
+    }
+    if (e == cudaSuccess) {
+        ProfScope ps(KC_I8GEMM, st);
+        e = launch_ozgemm(slices, 1, sa, ea, (int)mp, sb, eb, (int)np, (int)kp, static_cast<double*>(c), ldc, 0,
+                          (int)m, (int)mp, (int)(2 * n), st);
+    }
+    cudaFreeAsync(ws, st);
+    if (e != cudaSuccess) return fail(FGFRFT_CUDA, std::string("zgemm_int8: ") + cudaGetErrorString(e));
+    g_launches += 5;
+    return FGFRFT_OK;
+}
+
+// Complex GEMMs outside a cache handle (spectrum, cascade): the INT8 engine from n = 512 up unless
+// FGFRFT_ENGINE=dmma, else DMMA. op as above; batch of independent products with strides.
+bool complex_int8_default(int64_t m, int64_t n, int64_t k) {
+    static const bool dmma = [] {
+        const char* e = std::getenv("FGFRFT_ENGINE");
+        return e && !std::strcmp(e, "dmma");
+    }();
+    return !dmma && m >= 512 && n >= 256 && k >= 512 && k <= 8192;
+}
+
+int zgemm_auto(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda, int64_t sa,
+               const void* b, int64_t ldb, int64_t sb, void* c, int64_t ldc, int64_t sc, int batch, cudaStream_t st) {
+    if (opa == 1 || opb == 1) return fail(FGFRFT_PARAMETER, "zgemm_auto: plain transpose not used");
+    if (complex_int8_default(m, n, k)) {
+        for (int i = 0; i < batch; ++i)
+            if (int r = zgemm_int8(opa, opb, m, n, k, static_cast<const double2*>(a) + (size_t)i * sa, lda,
+                                   static_cast<const double2*>(b) + (size_t)i * sb, ldb,
+                                   static_cast<double2*>(c) + (size_t)i * sc, ldc, st))
+                return r;
+        return FGFRFT_OK;
+    }
+    ProfScope ps(KC_GEMM, st);
+    FGB_LAUNCH(launch_zgemm((int)m, (int)n, (int)k, a, lda, sa, opa == 2, b, ldb, sb, opb == 2, c, ldc, sc, batch,
+                            false, st),
+               1);
+    return FGFRFT_OK;
+}
+
+}  // namespace
+
+int fgfrft_zgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
+                          const double* b, int64_t ldb, double* c, int64_t ldc, void* stream) {
+    FGB_GUARD_BEGIN
+    if (transa < 0 || transa > 2 || transb < 0 || transb > 2) return fail(FGFRFT_PARAMETER, "trans must be 0, 1 or 2");
+    if (m < 1 || n < 1 || k < 1 || k > 8192) return fail(FGFRFT_SHAPE, "zgemm_int8: need m, n >= 1 and 1 <= k <= 8192");
+    if (lda < (transa ? k : m) || ldb < (transb ? n : k) || ldc < m)
+        return fail(FGFRFT_SHAPE, "zgemm_int8: leading dimension too small");
+    if (!a || !b || !c) return fail(FGFRFT_PARAMETER, "null buffer");
+    return zgemm_int8(transa, transb, m, n, k, a, lda, b, ldb, c, ldc, static_cast<cudaStream_t>(stream));
+    FGB_GUARD_END
+}
+
 // ------------------------------------------------------------------ GPU-resident denoising learner
 //
 // learn.hpp:291-413 (FastDenoiseEngine, real F) and learn.hpp:471-516 (denoise + Adam, adam.hpp)
@@ -2909,7 +3007,7 @@ int spectrum_decompose(fgfrft_spectrum* s, const double* f_host) {
         FGB_LAUNCH(launch_real_to_cplx(a.as<double>(), (int64_t)nn, w.p, st), 1);
     else
         FGB_CUDA(cudaMemcpyAsync(w.p, a.p, nn * 16, cudaMemcpyDeviceToDevice, st));
-    FGB_LAUNCH(launch_zgemm(n, n, n, f.p, n, 0, false, w.p, n, 0, false, fw.p, n, 0, 1, false, st), 1);  // F W
+    if (int e = zgemm_auto(0, 0, n, n, n, f.p, n, 0, w.p, n, 0, fw.p, n, 0, 1, st)) return e;  // F W
     std::vector<double> cv(n);
     FGB_CUDA(cudaMemcpyAsync(cv.data(), cosv.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
     FGB_CUDA(cudaStreamSynchronize(st));
@@ -2927,7 +3025,7 @@ int spectrum_decompose(fgfrft_spectrum* s, const double* f_host) {
         // M_c = W_c^H Bh W_c for every cluster of size > 1 (column-major k x k)
         if (t.ensure(nn * 16) || w2.ensure(nn * 16) || fw2.ensure(nn * 16))
             return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-        FGB_LAUNCH(launch_zgemm(n, n, n, bh.p, n, 0, false, w.p, n, 0, false, t.p, n, 0, 1, false, st), 1);
+        if (int e = zgemm_auto(0, 0, n, n, n, bh.p, n, 0, w.p, n, 0, t.p, n, 0, 1, st)) return e;
         std::vector<int> pr;
         for (const auto& c : clusters)
             if (c.second > 1)
@@ -3036,10 +3134,9 @@ int exact_into(fgfrft_spectrum* s, const double* alphas, int na, int which, void
         FGB_LAUNCH(launch_spec_scale(s->v.p, s->theta.as<double>(), s->alph.as<double>() + a0, nc, which, n, s->w.p,
                                      st),
                    1);
-        ProfScope ps(KC_GEMM, st);
-        FGB_LAUNCH(launch_zgemm(n, n, n, s->w.p, n, (int64_t)nn, false, s->v.p, n, 0, true,
-                                static_cast<double2*>(out) + (size_t)a0 * nn, n, (int64_t)nn, nc, false, st),
-                   1);
+        if (int e = zgemm_auto(0, 2, n, n, n, s->w.p, n, (int64_t)nn, s->v.p, n, 0,
+                               static_cast<double2*>(out) + (size_t)a0 * nn, n, (int64_t)nn, nc, st))
+            return e;
     }
     return FGFRFT_OK;
 }
@@ -3114,10 +3211,7 @@ int cascade_eval_device(fgfrft_cascade* cs, const double* alphas, double* out_ho
             if (int e = real_mm(op(ops, l), prefix(l - 1), prefix(l))) return e;
             continue;
         }
-        ProfScope ps(KC_GEMM, st);
-        FGB_LAUNCH(launch_zgemm(n, n, n, op(ops, l), n, 0, false, prefix(l - 1), n, 0, false, prefix(l), n, 0, 1,
-                                false, st),
-                   1);
+        if (int e = zgemm_auto(0, 0, n, n, n, op(ops, l), n, 0, prefix(l - 1), n, 0, prefix(l), n, 0, 1, st)) return e;
     }
     double* part = cs->part.as<double>();
     const size_t G = sp_part_elems();
@@ -3131,9 +3225,8 @@ int cascade_eval_device(fgfrft_cascade* cs, const double* alphas, double* out_ho
                 if (real) {  // dY = dQ_l prefix_{l-1}
                     if (int e = real_mm(op(dops, l), prefix(l - 1), cs->m.p)) return e;
                 } else {  // M = b prefix_{l-1}^H
-                    FGB_LAUNCH(launch_zgemm(n, n, n, b, n, 0, false, prefix(l - 1), n, 0, true, cs->m.p, n, 0, 1,
-                                            false, st),
-                               1);
+                    if (int e = zgemm_auto(0, 2, n, n, n, b, n, 0, prefix(l - 1), n, 0, cs->m.p, n, 0, 1, st))
+                        return e;
                 }
             }
             if (real)
@@ -3145,8 +3238,9 @@ int cascade_eval_device(fgfrft_cascade* cs, const double* alphas, double* out_ho
                 if (int e = int8_qx(cs->cache, 1, true, op(ops, l), b, n, nb)) return e;
             } else if (real) {  // over the (re, im) columns
                 FGB_LAUNCH(launch_rgemm(1, 1, 1, n, 2 * n, n, op(ops, l), n, 0, b, n, 0, nb, n, 0, 1, st), 1);
-            } else
-                FGB_LAUNCH(launch_zgemm(n, n, n, op(ops, l), n, 0, true, b, n, 0, false, nb, n, 0, 1, false, st), 1);
+            } else if (int e = zgemm_auto(2, 0, n, n, n, op(ops, l), n, 0, b, n, 0, nb, n, 0, 1, st)) {
+                return e;
+            }
             std::swap(b, nb);
         } else {
             FGB_LAUNCH(launch_cre_dot(b, dops, real, (int64_t)nn, part + G, st), 1);
@@ -3656,9 +3750,7 @@ int denoise_exact_eval(fgfrft_denoise* d, const double* params, double* loss, do
     double2* jtp = ph + n;
     double2* jtc = ph + 2 * n;
     auto zg = [&](bool adj, const void* b, void* c) -> int {  // c = V b or V^H b
-        ProfScope ps(KC_GEMM, st);
-        FGB_LAUNCH(launch_zgemm(n, ch, n, s->v.p, n, 0, adj, b, n, 0, false, c, n, 0, 1, false, st), 1);
-        return FGFRFT_OK;
+        return zgemm_auto(adj ? 2 : 0, 0, n, ch, n, s->v.p, n, 0, b, n, 0, c, n, 0, 1, st);
     };
     FGB_LAUNCH(launch_dnx_phase(params, s->theta.as<double>(), n, ph, jtp, jtc, st), 1);
     FGB_LAUNCH(launch_dnx_rowscale(d->xytil.p, ph, nullptr, false, n, cnt, d->xt.p, st), 1);

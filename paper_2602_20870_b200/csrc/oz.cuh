@@ -22,6 +22,11 @@ struct OzView {
                      // 3: interleaved stacked cache, row r = i * tp2 + kk: term kk < L is
                      //    P_(kk+1)(i, k), L <= kk < 2L is P_(kk-L+1)(k, i), else 0;
                      // 4: coefficient table (rows = orders, row stride rs = 2L+1) in term order kk
+                     // 5: an operand of a COMPLEX product as one real GEMM (ozgemm CM 1): z(r, k)
+                     //    = src complex element r * rs + k * ks (complex strides), K doubled:
+                     //    ra = 0 (A side): A'(r, 2k + e) = e ? -Im z : Re z
+                     //    ra = 1 (B side, rows 2j + c): B'(2j + c, 2k + e) = (Re, Im; Im, -Re)[c][e]
+                     //    ka = 1: conjugate z first
     int nt = 0;      // tiles per side of a tiled slab
     int l = 0, tp2 = 0;  // modes 3 / 4: L and the padded term count (64 or 128)
 };

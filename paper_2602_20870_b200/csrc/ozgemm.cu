@@ -147,6 +147,16 @@ __device__ __forceinline__ double pow2(int e) {  // exact 2^e for -1022 <= e <= 
 // ---------------------------------------------------------------- operand views and slicing (OzView: oz.cuh)
 
 __device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
+    if (v.tiled == 5) {  // complex product operand (see OzView)
+        const int bt = row / v.rp, r = row - bt * v.rp;
+        if (r >= v.rv || k >= v.kv) return 0.0;
+        const int kc = k >> 1, e = k & 1;
+        const int rc = v.ra ? r >> 1 : r, c = v.ra ? r & 1 : 0;
+        const double2 z = reinterpret_cast<const double2*>(v.src)[bt * v.sbatch + (int64_t)rc * v.rs + (int64_t)kc * v.ks];
+        const double zr = z.x, zi = v.ka ? -z.y : z.y;
+        if (!v.ra) return e ? -zi : zr;
+        return c == 0 ? (e ? zi : zr) : (e ? -zr : zi);
+    }
     if (v.tiled == 3) {  // rv = n (signal rows), rows beyond n * tp2 are padding
         const int i = row / v.tp2, kk = row - i * v.tp2;
         if (i >= v.rv || kk >= 2 * v.l || k >= v.kv) return 0.0;

@@ -52,3 +52,23 @@ def test_int8_gemm_scaled_rows_and_zeros():
     err = np.abs(c - ref) / (np.abs(a).max(1, keepdims=True) * np.abs(b).max(0, keepdims=True) + 1e-300)
     assert err.max() <= 1e-12 * np.sqrt(300)
     assert np.all(c[7] == 0.0) and np.all(c[:, 3] == 0.0)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (130, 70, 33), (512, 300, 1024), (1000, 257, 4096)])
+@pytest.mark.parametrize("op_a,op_b", [("N", "N"), ("C", "N"), ("N", "C"), ("T", "T")])
+def test_zgemm_int8_matches_fp64(m, n, k, op_a, op_b):
+    """Complex GEMM as one real Ozaki GEMM with K doubled: within 1e-12 of the FP64 product
+    (relative to |op(A)| |op(B)| norms), every op combination."""
+    import torch
+    rng = np.random.default_rng(m + 7 * n + k)
+    shp_a = (m, k) if op_a == "N" else (k, m)
+    shp_b = (k, n) if op_b == "N" else (n, k)
+    A = rng.standard_normal(shp_a) + 1j * rng.standard_normal(shp_a)
+    B = rng.standard_normal(shp_b) + 1j * rng.standard_normal(shp_b)
+    opf = {"N": lambda z: z, "T": lambda z: z.T, "C": lambda z: z.conj().T}
+    ref = opf[op_a](A) @ opf[op_b](B)
+    ta = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()   # column-major A in a row-major tensor
+    tb = torch.from_numpy(np.ascontiguousarray(B.T)).cuda()
+    c = fg.zgemm_int8(ta, tb, op_a, op_b).cpu().numpy().T
+    scale = np.linalg.norm(A) * np.linalg.norm(B)
+    assert np.linalg.norm(c - ref) <= 1e-12 * scale
