@@ -7,186 +7,17 @@
 //   apply_forward / apply_inverse                   transform.hpp:138-148 -> fgfrft_apply*, _matrix
 //   sinc_coeffs                                     sinc.hpp:50-63        -> fgfrft_sinc_coeffs
 //   dL/dalpha contraction                           learn.hpp:88-94       -> fgfrft_dlda*, mse_step*
-#include <algorithm>
-#include <atomic>
-#include <cstdio>
-#include <complex>
-#include <dlfcn.h>
-#include <numeric>
-#include <limits>
-#include <cmath>
-#include <cstdlib>
-#include <cstring>
-#include <mutex>
-#include <new>
-#include <sstream>
-#include <string>
-#include <vector>
+// plus the INT8 engine entry points (fgfrft_dgemm_int8_dev, fgfrft_zgemm_int8_dev). The other C-ABI
+// units: capi_shard.cu (row shards, fused gather, graph batches), capi_learn.cu (denoising
+// learner), capi_spectral.cu (spectrum, exact GFRFT, cascade), capi_store.cu (on-disk cache);
+// shared internals in capi_internal.cuh.
+#include "capi_internal.cuh"
 
-#include <cusolverDn.h>
-
-#include "common.cuh"
-#include "fgfrft_b200.h"
-#include "oz.cuh"
-
-namespace fgb {
-double host_sinc(double);
-double host_sinc_deriv(double);
-void host_sinc_coeffs(double alpha, int l, double* c, double* dc);
-uint64_t host_fnv1a64(const void* data, size_t nbytes);
-template <typename R>
-cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
-                         cudaStream_t stream);
-cudaError_t launch_synth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
-                               cudaStream_t stream);
-int synth_sweep_max_orders();
-cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream,
-                                 bool real);
-cudaError_t launch_synth_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l_used,
-                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream, bool real,
-                              bool out_complex);
-cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l, const void* m,
-                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream,
-                             bool real);
-size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
-cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream);
-cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream);
-cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
-                                 const void* x, int ch, void* y, cudaStream_t stream);
-cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
-                              const void* gcot, const void* x, int ch, double* dlda, cudaStream_t stream);
-int batch_max_heads();
-int batch_max_channels();
-int batch_max_n();
-cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void* A, int64_t lda, int64_t sA,
-                         const void* B, int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int batch,
-                         cudaStream_t stream);
-cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t stream);
-cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream);
-cudaError_t launch_rfrom_tiled_real(const void* src, void* dst, int n, cudaStream_t stream);
-size_t rapply_fused_part_elems(int n, int n_alpha);
-int rapply_fused_max_cols();
-cudaError_t launch_rapply_fused(const void* slabs, int n, int l_used, const double* coef_dev, int coef_ld, int n_alpha,
-                                const double* x, int b, double* part, double* y, cudaStream_t stream);
-cudaError_t launch_real_part(const void* src, void* dst, int64_t count, cudaStream_t stream);
-cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
-                          bool out_complex, cudaStream_t stream);
-cudaError_t launch_rsynth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
-                                bool out_complex, cudaStream_t stream);
-int rsweep_max_orders();
-cudaError_t launch_rdots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha, double* partial,
-                         double* s_out, cudaStream_t stream);
-cudaError_t launch_rdots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
-                             double* partial, double* s_out, cudaStream_t stream, int* launches);
-size_t rdots_mma_partial_elems(int n);
-cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
-                         int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
-                         bool accumulate, cudaStream_t stream);
-cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
-                              double* partial, double* s_out, cudaStream_t stream, int elem_bytes);
-cudaError_t launch_cgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
-                         int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
-                         bool accumulate, cudaStream_t stream);
-cudaError_t launch_promote(const void* src, void* dst, int64_t count, cudaStream_t stream);
-// spectral.cu (exact GFRFT, eigendecomposition pieces, cascade reductions)
-size_t sp_part_elems();
-cudaError_t launch_herm_parts(const void* f, int n, bool real, void* a, void* bh, cudaStream_t st);
-cudaError_t launch_real_to_cplx(const double* src, int64_t count, void* dst, cudaStream_t st);
-cudaError_t launch_blockdiag(const void* in, int n, const int* colinfo, const void* u, void* out, cudaStream_t st);
-cudaError_t launch_col_pair_dot(const void* w, const void* t, int n, const int* pairs, int count, void* out,
-                                cudaStream_t st);
-cudaError_t launch_gather_cols(const void* src, int n, const int* perm, void* dst, cudaStream_t st);
-cudaError_t launch_eig_residual(const void* fw, const void* w, const double* theta, const void* f, int n,
-                                double* part, double* out2, cudaStream_t st);
-cudaError_t launch_spec_scale(const void* v, const double* theta, const double* alphas, int na, int which, int n,
-                              void* w, cudaStream_t st);
-cudaError_t launch_cdiff_sq(const void* y, bool real_y, const void* t, int64_t count, void* b, double* part,
-                            cudaStream_t st);
-cudaError_t launch_cre_dot(const void* m, const void* d, bool real_d, int64_t count, double* part, cudaStream_t st);
-cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s1, double* out, cudaStream_t st);
-cudaError_t launch_rdot(const double* a, const double* b, int64_t count, double* part, cudaStream_t st);
-// store.cu
-cudaError_t launch_checksum(const void* data, size_t bytes, unsigned long long* out, cudaStream_t st);
-// shard.cu (fused row gather, DMMA path)
-cudaError_t launch_rows_push(const void* src, int64_t n, int r0, int rows, int64_t cols, void* const* dst_dev,
-                             int ndst, cudaStream_t stream);
-size_t dots_partial_elems(int n, int l, int n_alpha);
-size_t dots_mma_partial_elems(int n);
-int dots_mma_max_orders();
-cudaError_t launch_power_dots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
-                                  double* partial, double* s_out, cudaStream_t stream, int* launches);
-cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, int n_alpha, double g_scale,
-                                double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream,
-                                int elem_bytes);
-size_t mse_partial_elems(int n_alpha);
-cudaError_t launch_demote(const void* src, void* dst, int64_t count, cudaStream_t stream);
-cudaError_t launch_to_tiled(const void* src, void* dst, int n, int elem_bytes_dst, cudaStream_t stream);
-cudaError_t launch_from_tiled(const void* src, void* dst, int n, int elem_bytes_src, cudaStream_t stream);
-cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int width, double* out,
-                            cudaStream_t stream);
-int combine_max_terms();
-cudaError_t launch_dn_coef(const double* params, int l, double* tab, cudaStream_t st);
-cudaError_t launch_dn_scale(const double* u, const double* h, double* v, int n, int64_t count, cudaStream_t st);
-cudaError_t launch_dn_residual(const double* w, const double* x, double* r, int64_t count, double* part,
-                               cudaStream_t st);
-cudaError_t launch_dn_grad(const double* u, const double* du, const double* h, const double* r, const double* dqhv,
-                           const double* qr, int n, int ch, double* grad, double* part, double* loss, int* flag,
-                           int epoch, cudaStream_t st);
-cudaError_t launch_dn_track(const double* loss, const double* params, int np, int epoch, double* traj, double* best,
-                            int* best_epoch, cudaStream_t st);
-cudaError_t launch_dnx_phase(const double* params, const double* theta, int n, void* phase, void* jtp, void* jtc,
-                             cudaStream_t st);
-cudaError_t launch_dnx_rowscale(const void* src, const void* d, const double* h, bool conj_d, int n, int64_t count,
-                                void* dst, cudaStream_t st);
-cudaError_t launch_dnx_cot(const void* w, const double* x, int64_t count, bool real_loss, void* cot, double* part,
-                           cudaStream_t st);
-cudaError_t launch_dnx_grad(const void* far, const void* u, const void* vhr, const void* b, const void* jtc,
-                            const void* q, const double* h, int n, int ch, double* grad_h, double* part,
-                            cudaStream_t st);
-cudaError_t launch_dn_finish(const double* part, double* loss, double* grad, int n, int* flag, int epoch,
-                             cudaStream_t st);
-cudaError_t launch_dn_adam(double* params, double* m, double* v, const double* grad, int np, int64_t step, double lr,
-                           cudaStream_t st);
-size_t dn_part_elems();
-cudaError_t launch_ortho_residual(const double* g, int n, double* out, cudaStream_t stream);
-cudaError_t launch_colstats(const double* x, const double* xc, int n, int b, double* colsq, double* colxc, int* ecol,
-                            double* rg, int l, cudaStream_t st);
-cudaError_t launch_gram_s_dlda(const double* coef, const double* dcoef, const double* rg, int n_alpha, int l,
-                               double norm, double* s, double* dlda, cudaStream_t st);
-cudaError_t launch_gram_terms(const double* part, int ctas, int tp2, int l, double* rg, cudaStream_t st);
-cudaError_t launch_loss3(const double* part, int ctas, int n_alpha, double norm, double* loss, cudaStream_t st);
-cudaError_t launch_gram_s(const double* coef, const double* rg, int n_alpha, int l, double norm, double* s,
-                          cudaStream_t st);
-size_t combine_partial_elems(int tp);
-cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
-                           const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
-                           double* loss, cudaStream_t stream);
-}  // namespace fgb
-
-using namespace fgb;
-
-namespace {
+namespace fgbi {
 
 thread_local std::string g_err;
-// Set by the host-buffer entry points around their call into a *_dev entry point: the device
-// buffers they pass are already in the internal (complex128) layout, no complex64 bridge.
 thread_local bool tl_internal_signals = false;
-struct InternalSignals {
-    bool prev;
-    InternalSignals() : prev(tl_internal_signals) { tl_internal_signals = true; }
-    ~InternalSignals() { tl_internal_signals = prev; }
-};
 std::atomic<uint64_t> g_launches{0};
-
-// Optional per-kernel-class timing with CUDA events recorded on the launching stream
-// (fgfrft_profile_*): bench.py uses it to time the dominant kernel inside its timed region.
-enum KernelClass {
-    KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_I8GEMM = 4, KC_SLICE = 5, KC_COMBINE = 6, KC_COUNT = 8
-};
-struct ProfRec {
-    int cls;
-    cudaEvent_t a, b;
-};
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 std::vector<ProfRec> g_prof;
@@ -203,154 +34,14 @@ cudaEvent_t prof_event() {
     return e;
 }
 
-struct ProfScope {
-    int cls;
-    cudaStream_t st;
-    cudaEvent_t a = nullptr;
-    ProfScope(int c, cudaStream_t s) : cls(c), st(s) {
-        if (!g_prof_on) return;
-        std::lock_guard<std::mutex> lk(g_prof_mu);
-        a = prof_event();
-        cudaEventRecord(a, st);
-    }
-    ~ProfScope() {
-        if (!a) return;
-        std::lock_guard<std::mutex> lk(g_prof_mu);
-        cudaEvent_t b = prof_event();
-        cudaEventRecord(b, st);
-        g_prof.push_back({cls, a, b});
-    }
-};
-
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
 
-#define FGB_CUDA(expr)                                                                          \
-    do {                                                                                        \
-        cudaError_t e_ = (expr);                                                                \
-        if (e_ != cudaSuccess) {                                                                \
-            cudaGetLastError();                                                                 \
-            return fail(FGFRFT_CUDA, std::string(#expr) + " failed: " + cudaGetErrorString(e_)); \
-        }                                                                                       \
-    } while (0)
+}  // namespace fgbi
 
-#define FGB_LAUNCH(expr, nlaunch)  \
-    do {                           \
-        FGB_CUDA(expr);            \
-        g_launches += (nlaunch);   \
-    } while (0)
-
-#define FGB_GUARD_BEGIN try {
-#define FGB_GUARD_END                                                        \
-    }                                                                        \
-    catch (const std::bad_alloc&) {                                          \
-        return fail(FGFRFT_CAPACITY, "host allocation failed");              \
-    }                                                                        \
-    catch (const std::exception& ex) {                                       \
-        return fail(FGFRFT_NUMERICAL, ex.what());                            \
-    }                                                                        \
-    catch (...) {                                                            \
-        return fail(FGFRFT_NUMERICAL, "unknown exception");                  \
-    }
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    cudaError_t ensure(size_t bytes) {
-        if (bytes <= cap) return cudaSuccess;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        cudaError_t e = cudaMalloc(&p, bytes);
-        if (e == cudaSuccess) cap = bytes;
-        return e;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-    template <typename T>
-    T* as() const { return static_cast<T*>(p); }
-};
-
-}  // namespace
-
-struct fgfrft_cache {
-    int64_t n = 0;
-    int l = 0;
-    int dtype = FGFRFT_C128;
-    bool real = false;  // F has an exactly zero imaginary part: real cache, real Q, real x complex GEMMs
-    // complex64 API over a real F: the powers are stored as real doubles (the same 8 bytes per
-    // element as complex64) and every kernel runs the real complex128 path; the *_dev entry points
-    // promote the caller's complex64 signals on entry and demote the results (dtype stays C128
-    // internally, fgfrft_cache_info reports C64).
-    bool api_c64 = false;
-    DevBuf bx, bxc, by;
-    size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
-    int device = 0;
-    uint64_t fingerprint = 0;
-    void* slabs = nullptr;
-    size_t elem = 16;
-    cudaStream_t own_stream = nullptr;
-    cudaStream_t stream = nullptr;
-    std::mutex mu;
-    // workspaces
-    DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda, tmp;
-    // Power-product route (real F): the stacked cache [P_1..P_L; P_1^T..P_L^T] as INT8 Ozaki
-    // digit slices (built lazily, once), the per-call slices of X and the products Z = P X.
-    int engine = FGFRFT_ENGINE_AUTO;
-    // F^T F = I to rounding (unitarity residual of gft.hpp:39-44 <= 1e-12, checked on device at
-    // build): the power-product MSE step may then take s_k from the Gram sequence <X, F^d X>.
-    bool orthogonal = false;
-    double ortho_residual = -1.0;
-    int ps_slices = 0;
-    DevBuf ps, pe, prm, xsl, xex, z;
-    DevBuf qsl, qex;  // per-call INT8 slices of Q(a) (or G) for the synthesis route
-    // Orthogonal-F sweep with the combination on the INT8 tensor cores: the stacked cache sliced
-    // in (signal row, term) interleaved order, P_L in column-major form, and per-call buffers.
-    int ps3_slices = 0;
-    DevBuf ps3, pe3, plr, zd, zaux, cdig, cex;
-    // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
-    bool shard = false;
-    int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
-    int64_t r0 = 0, r1 = 0;
-    void* colp = nullptr;
-    size_t panel_elems = 0;
-    // Host-buffer MSE step: Xc is uploaded on a side stream while the power products run; the
-    // step waits on xc_evt right before its first use of Xc.
-    cudaStream_t aux_stream = nullptr;
-    cudaEvent_t xc_evt = nullptr;
-    bool xc_pending = false;
-    double* coef_h = nullptr;  // pinned staging for the coefficient tables
-    size_t coef_h_cap = 0;
-    cudaEvent_t coef_evt = nullptr;
-
-    // Matrices at the API are n x n column-major; device slabs are tiled (common.cuh) and padded
-    // to npad = 32 * ceil(n / 32) per side.
-    size_t mat_elems() const { return (size_t)n * (size_t)n; }
-    size_t npad() const { return (size_t)ceil_div(n, kTile) * kTile; }
-    size_t slab_elems() const { return npad() * npad(); }
-    size_t slab_bytes() const { return slab_elems() * elem; }
-    void* slab(int k) const { return static_cast<char*>(slabs) + (size_t)(k - 1) * slab_bytes(); }
-};
-
-namespace {
+namespace fgbi {
 
 int check_handle(const fgfrft_cache* c) {
     if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_cache handle");
@@ -423,7 +114,7 @@ int check_alphas(const double* alphas, int n_alpha) {
 // Q for n_alpha orders into out (n x n each). Up to 4 orders: exact scalar tile-pair kernel
 // (HBM-bound, bit-identical to the reference order of operations). Sweeps of >= 8 complex128
 // orders: DMMA kernel, 64 orders per launch, cache streamed once per launch.
-int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out, bool internal = false) {
+int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out, bool internal) {
     ProfScope ps(KC_SYNTH, c->stream);
     if (c->real) {  // complex output (imag 0) for the API, real Q for the internal GEMMs
         const bool oc = !internal;
@@ -722,9 +413,6 @@ bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b);
 int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out);
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
-int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
-                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers = nullptr,
-                int npeers = 0);
 int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
                 int64_t sm);
 bool use_power_route(const fgfrft_cache* c, int n_alpha);
@@ -1226,7 +914,7 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
     return FGFRFT_OK;
 }
 
-}  // namespace
+}  // namespace fgbi
 
 // ===================================================================================== C ABI
 
@@ -1781,625 +1469,11 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
     FGB_GUARD_END
 }
 
-// ---------------------------------------------------------------------------- row shards
-
-int fgfrft_shard_create(const double* f, int64_t n, int l, int64_t row_begin, int64_t row_end, uint64_t memory_budget,
-                        int device, fgfrft_cache** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (l < 1) return fail(FGFRFT_PARAMETER, "PowerCache: truncation order must be >= 1");
-    if (n < 1 || !f) return fail(FGFRFT_PARAMETER, "PowerCache: matrix must be non-empty");
-    if (row_begin < 0 || row_end > n || row_begin >= row_end || row_begin % kTile != 0 ||
-        (row_end % kTile != 0 && row_end != n))
-        return fail(FGFRFT_PARAMETER, "shard rows must be [r0, r1) with r0 % 32 == 0 and r1 % 32 == 0 or r1 == n");
-    const int64_t rows = row_end - row_begin;
-    // real F (graph GFT): real panels, real kernels (as the full cache, learn.hpp:449-451)
-    bool real = std::getenv("FGFRFT_NO_REAL") == nullptr;
-    for (size_t i = 0; i < (size_t)n * (size_t)n && real; ++i) real = f[2 * i + 1] == 0.0;
-    const unsigned __int128 bytes = (unsigned __int128)2 * l * (uint64_t)rows * (uint64_t)n * (real ? 8 : 16);
-    if (bytes > memory_budget) {
-        std::ostringstream msg;
-        msg << "PowerCache shard: " << l << " row and column panels of " << rows << "x" << n << " need "
-            << (unsigned long long)bytes << " bytes, over the " << memory_budget << "-byte budget";
-        return fail(FGFRFT_CAPACITY, msg.str());
-    }
-    int ndev = 0;
-    FGB_CUDA(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(FGFRFT_PARAMETER, "device index out of range");
-    DeviceGuard dg(device);
-    auto* c = new fgfrft_cache();
-    c->n = n;
-    c->l = l;
-    c->device = device;
-    c->shard = true;
-    c->real = real;
-    c->elem = real ? 8 : 16;
-    c->r0 = row_begin;
-    c->r1 = row_end;
-    c->fingerprint = host_fnv1a64(f, (size_t)n * (size_t)n * 16);
-    const int nI = (int)ceil_div(rows, kTile), nt = (int)ceil_div(n, kTile);
-    c->panel_elems = (size_t)nI * nt * kTileElems;
-    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-        delete c;
-        return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
-    }
-    c->stream = c->own_stream;
-    const size_t pbytes = c->panel_elems * c->elem * (size_t)l;
-    if (cudaMalloc(&c->slabs, pbytes) != cudaSuccess || cudaMalloc(&c->colp, pbytes) != cudaSuccess) {
-        cudaGetLastError();
-        destroy_cache(c);
-        return fail(FGFRFT_CAPACITY, "PowerCache shard: device allocation failed");
-    }
-    // Build: Rp_1 = F[R,:], Cp_1 = F[:,R]; Rp_k = Rp_{k-1} F, Cp_k = F Cp_{k-1} (column-major scratch).
-    int rc = FGFRFT_OK;
-    do {
-        const size_t ml = (size_t)n * n, pl = (size_t)rows * n;
-        if (c->tmp.ensure((ml + 4 * pl) * 16) != cudaSuccess) {
-            rc = fail(FGFRFT_CAPACITY, "PowerCache shard: scratch allocation failed");
-            break;
-        }
-        double2* fb = c->tmp.as<double2>();
-        double2 *rp = fb + ml, *rq = rp + pl, *cp = rq + pl, *cq = cp + pl;
-        if (cudaMemcpyAsync(fb, f, ml * 16, cudaMemcpyHostToDevice, c->stream) != cudaSuccess ||
-            cudaMemcpy2DAsync(rp, rows * 16, fb + row_begin, n * 16, rows * 16, n, cudaMemcpyDeviceToDevice,
-                              c->stream) != cudaSuccess ||
-            cudaMemcpyAsync(cp, fb + (size_t)row_begin * n, pl * 16, cudaMemcpyDeviceToDevice, c->stream) !=
-                cudaSuccess) {
-            rc = fail(FGFRFT_CUDA, "PowerCache shard: staging copies failed");
-            break;
-        }
-        // real: real copies of F and of the panels (8-byte elements) in their own scratch
-        DevBuf rs;
-        double *fre = nullptr, *rpr = nullptr, *rqr = nullptr, *cpr = nullptr, *cqr = nullptr;
-        if (real) {
-            if (rs.ensure((ml + 4 * pl) * 8) != cudaSuccess) {
-                rc = fail(FGFRFT_CAPACITY, "PowerCache shard: scratch allocation failed");
-                break;
-            }
-            fre = rs.as<double>();
-            rpr = fre + ml;
-            rqr = rpr + pl;
-            cpr = rqr + pl;
-            cqr = cpr + pl;
-            if (launch_real_part(fb, fre, (int64_t)ml, c->stream) != cudaSuccess ||
-                launch_real_part(rp, rpr, (int64_t)pl, c->stream) != cudaSuccess ||
-                launch_real_part(cp, cpr, (int64_t)pl, c->stream) != cudaSuccess) {
-                rc = fail(FGFRFT_CUDA, "PowerCache shard: real staging failed");
-                rs.release();
-                break;
-            }
-        }
-        for (int k = 1; k <= l && rc == FGFRFT_OK; ++k) {
-            if (k > 1) {
-                cudaError_t e1, e2;
-                if (real) {
-                    e1 = launch_rgemm(0, 0, 0, (int)rows, (int)n, (int)n, rpr, rows, 0, fre, n, 0, rqr, rows, 0, 1,
-                                      c->stream);
-                    e2 = launch_rgemm(0, 0, 0, (int)n, (int)rows, (int)n, fre, n, 0, cpr, n, 0, cqr, n, 0, 1,
-                                      c->stream);
-                } else {
-                    e1 = launch_zgemm((int)rows, (int)n, (int)n, rp, rows, 0, false, fb, n, 0, false, rq, rows, 0, 1,
-                                      false, c->stream);
-                    e2 = launch_zgemm((int)n, (int)rows, (int)n, fb, n, 0, false, cp, n, 0, false, cq, n, 0, 1, false,
-                                      c->stream);
-                }
-                if (e1 != cudaSuccess || e2 != cudaSuccess) {
-                    rc = fail(FGFRFT_CUDA, "PowerCache shard: panel GEMM failed");
-                    break;
-                }
-                std::swap(rp, rq);
-                std::swap(cp, cq);
-                std::swap(rpr, rqr);
-                std::swap(cpr, cqr);
-                g_launches += 2;
-            }
-            const void* rsrc = real ? static_cast<const void*>(rpr) : static_cast<const void*>(rp);
-            const void* csrc = real ? static_cast<const void*>(cpr) : static_cast<const void*>(cp);
-            if (launch_rect_to_tiled(rsrc, rows, (int)rows, (int)n,
-                                     static_cast<char*>(c->slabs) + (size_t)(k - 1) * c->panel_elems * c->elem,
-                                     c->stream, real) != cudaSuccess ||
-                launch_rect_to_tiled(csrc, n, (int)n, (int)rows,
-                                     static_cast<char*>(c->colp) + (size_t)(k - 1) * c->panel_elems * c->elem,
-                                     c->stream, real) != cudaSuccess) {
-                rc = fail(FGFRFT_CUDA, "PowerCache shard: tiling failed");
-                break;
-            }
-            g_launches += 2;
-        }
-        if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
-            rc = fail(FGFRFT_CUDA, "PowerCache shard: build failed");
-        rs.release();
-    } while (false);
-    c->tmp.release();
-    if (rc != FGFRFT_OK) {
-        destroy_cache(c);
-        return rc;
-    }
-    *out = c;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_shard_destroy(fgfrft_cache* c) {
-    FGB_GUARD_BEGIN
-    if (c && !c->shard) return fail(FGFRFT_PARAMETER, "not a row-shard handle");
-    destroy_cache(c);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_shard_info(const fgfrft_cache* c, int64_t* n, int* l, int64_t* row_begin, int64_t* row_end,
-                      uint64_t* fingerprint) {
-    if (int st = check_shard(c)) return st;
-    if (n) *n = c->n;
-    if (l) *l = c->l;
-    if (row_begin) *row_begin = c->r0;
-    if (row_end) *row_end = c->r1;
-    if (fingerprint) *fingerprint = c->fingerprint;
-    return FGFRFT_OK;
-}
-
-int fgfrft_shard_set_stream(fgfrft_cache* c, void* stream) {
-    if (int st = check_shard(c)) return st;
-    std::lock_guard<std::mutex> lk(c->mu);
-    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
-    return FGFRFT_OK;
-}
-
-int fgfrft_shard_synthesize_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int which, void* out_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_shard(c)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (which != FGFRFT_Q && which != FGFRFT_DQ) return fail(FGFRFT_PARAMETER, "which must be FGFRFT_Q or FGFRFT_DQ");
-    if (!out_dev) return fail(FGFRFT_PARAMETER, "null output");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    double* coef = nullptr;
-    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
-    const double* table = which == FGFRFT_Q ? coef : coef + (size_t)n_alpha * (2 * c->l + 1);
-    ProfScope ps(KC_SYNTH, c->stream);
-    FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, (int)c->n, (int)c->r0, (int)(c->r1 - c->r0), c->l, table, n_alpha,
-                                 out_dev, c->stream, c->real, true),
-               1);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_shard_apply_gather_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, int64_t b,
-                                  void* y_full_dev, void* const* peer_y_full, int n_peers) {
-    FGB_GUARD_BEGIN
-    if (int st = check_shard(c)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
-    if (n_peers < 0 || n_peers > 7 || (n_peers > 0 && !peer_y_full))
-        return fail(FGFRFT_PARAMETER, "apply_gather: 0..7 peer buffers");
-    if (b == 0) return FGFRFT_OK;
-    if (!x_dev || !y_full_dev) return fail(FGFRFT_PARAMETER, "null signal buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    const int n = (int)c->n, rows = (int)(c->r1 - c->r0);
-    double* coef = nullptr;
-    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
-    const size_t width = (size_t)(2 * c->l + 1), qs = (size_t)rows * n, blk = (size_t)n * b;
-    const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)4 << 30) / (qs * 16))));
-    FGB_CUDA(c->q.ensure((size_t)chunk * qs * 16));
-    FGB_CUDA(c->tmp.ensure(8 * sizeof(void*)));  // peer bases as a device array (push kernel)
-    const bool i8 = use_int8_gemm(c, b);
-    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
-        const int na = std::min(chunk, n_alpha - a0);
-        const size_t off = (size_t)a0 * blk + (size_t)c->r0;  // complex elements: order a0, row r0
-        double2* yl = static_cast<double2*>(y_full_dev) + off;
-        {
-            ProfScope ps(KC_SYNTH, c->stream);
-            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, c->l, coef + a0 * width, na, c->q.p,
-                                         c->stream, c->real, false),
-                       1);
-        }
-        if (i8) {  // rows of Y written locally and into every peer buffer by the GEMM epilogue
-            double* pp[7];
-            for (int q = 0; q < n_peers; ++q) pp[q] = reinterpret_cast<double*>(static_cast<double2*>(peer_y_full[q]) + off);
-            if (int st = int8_qx_gen(c, na, false, c->q.p, rows, rows, (int64_t)qs, x_dev, b, yl, n,
-                                     2 * (int64_t)blk, pp, n_peers))
-                return st;
-            continue;
-        }
-        {
-            ProfScope ps(KC_GEMM, c->stream);
-            if (c->real)
-                FGB_LAUNCH(launch_rgemm(0, 1, 1, rows, 2 * (int)b, n, c->q.p, rows, (int64_t)qs, x_dev, n, 0, yl, n,
-                                        (int64_t)2 * blk, na, c->stream),
-                           1);
-            else
-                FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false, yl, n,
-                                        (int64_t)blk, na, false, c->stream),
-                           1);
-        }
-        if (n_peers > 0) {  // DMMA epilogue writes locally: push the rows to the peers (P2P stores)
-            std::vector<void*> shifted((size_t)n_peers);
-            for (int q = 0; q < n_peers; ++q) shifted[q] = static_cast<double2*>(peer_y_full[q]) + (size_t)a0 * blk;
-            FGB_CUDA(cudaMemcpyAsync(c->tmp.p, shifted.data(), (size_t)n_peers * sizeof(void*),
-                                     cudaMemcpyHostToDevice, c->stream));
-            FGB_LAUNCH(launch_rows_push(static_cast<double2*>(y_full_dev) + (size_t)a0 * blk, n, (int)c->r0, rows,
-                                        (int64_t)na * b, c->tmp.as<void*>(), n_peers, c->stream),
-                       1);
-            FGB_CUDA(cudaStreamSynchronize(c->stream));  // `shifted` is host staging of the copy above
-        }
-    }
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-// CUDA IPC of a device buffer for the fused gather: handle (64 bytes) + offset of the pointer in
-// its allocation (allocator sub-allocations), and the mapping on a peer process.
-int fgfrft_ipc_get(const void* dev_ptr, void* handle_out, uint64_t* offset_out) {
-    FGB_GUARD_BEGIN
-    if (!dev_ptr || !handle_out || !offset_out) return fail(FGFRFT_PARAMETER, "null argument");
-    using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
-    static GetRange get_range = [] {
-        void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
-        return h ? reinterpret_cast<GetRange>(dlsym(h, "cuMemGetAddressRange_v2")) : nullptr;
-    }();
-    if (!get_range) return fail(FGFRFT_CUDA, "cuMemGetAddressRange unavailable");
-    unsigned long long base = 0;
-    size_t size = 0;
-    if (get_range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
-        return fail(FGFRFT_CUDA, "cuMemGetAddressRange failed");
-    cudaIpcMemHandle_t h;
-    FGB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
-    std::memcpy(handle_out, &h, sizeof h);
-    *offset_out = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_ipc_open(const void* handle, int device, void** base_out) {
-    FGB_GUARD_BEGIN
-    if (!handle || !base_out) return fail(FGFRFT_PARAMETER, "null argument");
-    DeviceGuard dg(device);
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, handle, sizeof h);
-    FGB_CUDA(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_ipc_close(void* base) {
-    if (base) cudaIpcCloseMemHandle(base);
-    return FGFRFT_OK;
-}
-
-int fgfrft_shard_apply_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, int64_t b,
-                           void* y_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_shard(c)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (b < 0) return fail(FGFRFT_SHAPE, "apply_forward: negative signal count");
-    if (b == 0) return FGFRFT_OK;
-    if (!x_dev || !y_dev) return fail(FGFRFT_PARAMETER, "null signal buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    const int n = (int)c->n, rows = (int)(c->r1 - c->r0);
-    double* coef = nullptr;
-    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
-    const size_t width = (size_t)(2 * c->l + 1), qs = (size_t)rows * n;
-    const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)4 << 30) / (qs * 16))));
-    FGB_CUDA(c->q.ensure((size_t)chunk * qs * 16));
-    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
-        const int na = std::min(chunk, n_alpha - a0);
-        {
-            ProfScope ps(KC_SYNTH, c->stream);
-            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, c->l, coef + a0 * width, na, c->q.p,
-                                         c->stream, c->real, false),
-                       1);
-        }
-        if (use_int8_gemm(c, b)) {
-            if (int st = int8_qx_gen(c, na, false, c->q.p, rows, rows, (int64_t)qs, x_dev, b,
-                                     static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, 2 * (int64_t)rows * b))
-                return st;
-            continue;
-        }
-        ProfScope ps(KC_GEMM, c->stream);
-        if (c->real)  // Y[R,:] = Q[R,:] X, real Q rows panel (ld = rows) x complex X
-            FGB_LAUNCH(launch_rgemm(0, 1, 1, rows, 2 * (int)b, n, c->q.p, rows, (int64_t)qs, x_dev, n, 0,
-                                    static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, (int64_t)2 * rows * b,
-                                    na, c->stream),
-                       1);
-        else
-            FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false,
-                                    static_cast<double2*>(y_dev) + (size_t)a0 * rows * b, rows, (int64_t)rows * b, na,
-                                    false, c->stream),
-                       1);
-    }
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-}  // extern "C"
-
-namespace {
-
-// Row-shard MSE step. s_partial (per-power partials, 2L+1 per order) when requested; otherwise
-// dlda_partial = sum_k c'_k s_k directly -- for one or two orders via dQ/dalpha rows synthesised
-// in the same cache pass as Q and Re<M[R,:], dQ[R,:]> (no second pass over the panels).
-int shard_mse_impl(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_rows_dev,
-                   int64_t b, void* y_rows_dev, void* loss_partial_dev, double* s_partial_dev,
-                   double* dlda_partial_dev) {
-    const int n = (int)c->n, rows = (int)(c->r1 - c->r0), l = c->l;
-    const size_t width = (size_t)(2 * l + 1), qs = (size_t)rows * n, blk = (size_t)rows * b;
-    double* coef = nullptr;
-    if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
-    const int chunk = std::max(1, std::min(n_alpha, (int)(((size_t)2 << 30) / (qs * 16))));
-    const bool dq_route = !s_partial_dev && n_alpha <= 2 && chunk >= n_alpha &&
-                          std::getenv("FGFRFT_DOTS_ROUTE") == nullptr;
-    FGB_CUDA(c->q.ensure((size_t)(dq_route ? 2 : 1) * chunk * qs * 16));
-    FGB_CUDA(c->m.ensure((size_t)chunk * qs * 16));
-    FGB_CUDA(c->g.ensure((size_t)chunk * blk * 16));
-    FGB_CUDA(c->lpart.ensure(mse_partial_elems(chunk) * sizeof(double)));
-    FGB_CUDA(c->partial.ensure(std::max(dots_rows_partial_elems(n, rows, l, chunk), 2 * sp_part_elems()) *
-                               sizeof(double)));
-    if (!s_partial_dev && !dq_route) FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
-    if (!y_rows_dev) FGB_CUDA(c->y.ensure((size_t)chunk * blk * 16));
-    const double norm = 1.0 / ((double)n * (double)b);
-    const size_t qe = c->real ? 8 : 16;
-    for (int a0 = 0; a0 < n_alpha; a0 += chunk) {
-        const int na = std::min(chunk, n_alpha - a0);
-        double2* ya = y_rows_dev ? static_cast<double2*>(y_rows_dev) + (size_t)a0 * blk : c->y.as<double2>();
-        {
-            ProfScope ps(KC_SYNTH, c->stream);  // dq_route: table rows [c(a) ..][c'(a) ..] (a0 = 0)
-            FGB_LAUNCH(launch_synth_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, coef + a0 * width,
-                                         dq_route ? 2 * na : na, c->q.p, c->stream, c->real, false),
-                       1);
-        }
-        if (use_int8_gemm(c, b)) {
-            if (int st = int8_qx_gen(c, na, false, c->q.p, rows, rows, (int64_t)qs, x_dev, b, ya, rows,
-                                     2 * (int64_t)blk))
-                return st;
-        } else {
-            ProfScope ps(KC_GEMM, c->stream);
-            if (c->real)
-                FGB_LAUNCH(launch_rgemm(0, 1, 1, rows, 2 * (int)b, n, c->q.p, rows, (int64_t)qs, x_dev, n, 0, ya, rows,
-                                        (int64_t)2 * blk, na, c->stream),
-                           1);
-            else
-                FGB_LAUNCH(launch_zgemm(rows, (int)b, n, c->q.p, rows, (int64_t)qs, false, x_dev, n, 0, false, ya, rows,
-                                        (int64_t)blk, na, false, c->stream),
-                           1);
-        }
-        {
-            ProfScope ps(KC_ELEMWISE, c->stream);
-            FGB_LAUNCH(launch_mse_residual(ya, xc_rows_dev, (int64_t)blk, na, 2.0 * norm, 1.0, c->g.p,
-                                           c->lpart.as<double>(), static_cast<double*>(loss_partial_dev) + a0,
-                                           c->stream, 16),
-                       2);
-        }
-        if (use_int8_gemm(c, b)) {
-            if (int st = int8_gx_gen(c, na, c->g.p, rows, x_dev, b, c->m.p, (int64_t)qs)) return st;
-        } else {
-            ProfScope ps(KC_GEMM, c->stream);  // M[R,:] = G[R,:] X^H (real F: only Re M is needed)
-            if (c->real)
-                FGB_LAUNCH(launch_rgemm(2, 2, 0, rows, n, 2 * (int)b, c->g.p, rows, (int64_t)2 * blk, x_dev, n, 0, c->m.p,
-                                        rows, (int64_t)qs, na, c->stream),
-                           1);
-            else
-                FGB_LAUNCH(launch_zgemm(rows, n, (int)b, c->g.p, rows, (int64_t)blk, false, x_dev, n, 0, true, c->m.p,
-                                        rows, (int64_t)qs, na, false, c->stream),
-                           1);
-        }
-        if (dq_route) {  // dlda_partial[a] = Re<M[R,:], dQ[R,:]>
-            double* part = c->partial.as<double>();
-            const char* dq = c->q.as<char>() + (size_t)na * qs * qe;
-            ProfScope ps(KC_ELEMWISE, c->stream);
-            for (int i = 0; i < na; ++i) {
-                const char* mi = c->m.as<char>() + (size_t)i * qs * qe;
-                if (c->real)
-                    FGB_LAUNCH(launch_rdot(reinterpret_cast<const double*>(mi),
-                                           reinterpret_cast<const double*>(dq + (size_t)i * qs * qe), (int64_t)qs,
-                                           part + (size_t)i * sp_part_elems(), c->stream),
-                               1);
-                else
-                    FGB_LAUNCH(launch_cre_dot(mi, dq + (size_t)i * qs * qe, false, (int64_t)qs,
-                                              part + (size_t)i * sp_part_elems(), c->stream),
-                               1);
-            }
-            FGB_LAUNCH(launch_sum_parts(part, na, 1.0, 1.0, dlda_partial_dev + a0, c->stream), 1);
-            continue;
-        }
-        double* sp = s_partial_dev ? s_partial_dev : c->s.as<double>();
-        ProfScope ps(KC_DOTS, c->stream);
-        FGB_LAUNCH(launch_dots_rows(c->slabs, c->colp, n, (int)c->r0, rows, l, c->m.p, (int64_t)qs, na,
-                                    c->partial.as<double>(), sp + a0 * width, c->stream, c->real),
-                   2);
-    }
-    if (!s_partial_dev && !dq_route)
-        FGB_LAUNCH(launch_coef_dot(coef + (size_t)n_alpha * width, c->s.as<double>(), n_alpha, (int)width,
-                                   dlda_partial_dev, c->stream),
-                   1);
-    return FGFRFT_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int fgfrft_shard_mse_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
-                                 const void* xc_rows_dev, int64_t b, void* y_rows_dev, void* loss_partial_dev,
-                                 void* s_partial_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_shard(c)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
-    if (!x_dev || !xc_rows_dev || !loss_partial_dev || !s_partial_dev) return fail(FGFRFT_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    return shard_mse_impl(c, alphas, n_alpha, x_dev, xc_rows_dev, b, y_rows_dev, loss_partial_dev,
-                          static_cast<double*>(s_partial_dev), nullptr);
-    FGB_GUARD_END
-}
-
-int fgfrft_shard_mse_dlda_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
-                                      const void* xc_rows_dev, int64_t b, void* y_rows_dev, void* loss_partial_dev,
-                                      void* dlda_partial_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_shard(c)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
-    if (!x_dev || !xc_rows_dev || !loss_partial_dev || !dlda_partial_dev) return fail(FGFRFT_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    return shard_mse_impl(c, alphas, n_alpha, x_dev, xc_rows_dev, b, y_rows_dev, loss_partial_dev, nullptr,
-                          static_cast<double*>(dlda_partial_dev));
-    FGB_GUARD_END
-}
-
-// ---------------------------------------------------------------------------- graph batches
-
-int fgfrft_batch_create(const double* fs, int64_t graphs, int64_t n, int l, int device, fgfrft_cache** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (l < 1) return fail(FGFRFT_PARAMETER, "PowerCache: truncation order must be >= 1");
-    if (graphs < 1 || graphs > 65535 || !fs) return fail(FGFRFT_PARAMETER, "graph batch: need 1..65535 graphs");
-    if (n < 1 || n > batch_max_n()) return fail(FGFRFT_PARAMETER, "graph batch: n must be in 1..64");
-    if (l > 255) return fail(FGFRFT_PARAMETER, "graph batch: l must be <= 255");
-    int ndev = 0;
-    FGB_CUDA(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(FGFRFT_PARAMETER, "device index out of range");
-    DeviceGuard dg(device);
-    auto* c = new fgfrft_cache();
-    c->n = n;
-    c->l = l;
-    c->device = device;
-    c->dtype = FGFRFT_C64;
-    c->elem = 8;
-    c->graphs = graphs;
-    c->fingerprint = host_fnv1a64(fs, (size_t)graphs * n * n * 16);
-    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-        delete c;
-        return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
-    }
-    c->stream = c->own_stream;
-    const size_t slab = 4 * (size_t)kTileElems;  // padded 64 x 64
-    if (cudaMalloc(&c->slabs, (size_t)graphs * l * slab * 8) != cudaSuccess) {
-        cudaGetLastError();
-        destroy_cache(c);
-        return fail(FGFRFT_CAPACITY, "graph batch: device allocation failed");
-    }
-    int rc = FGFRFT_OK;
-    const size_t ml = (size_t)n * n;
-    do {
-        if (c->tmp.ensure(3 * graphs * ml * 16) != cudaSuccess) {
-            rc = fail(FGFRFT_CAPACITY, "graph batch: scratch allocation failed");
-            break;
-        }
-        double2* fb = c->tmp.as<double2>();
-        double2* prev = fb + graphs * ml;
-        double2* cur = prev + graphs * ml;
-        if (cudaMemcpyAsync(fb, fs, graphs * ml * 16, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
-            rc = fail(FGFRFT_CUDA, "graph batch: upload failed");
-            break;
-        }
-        const double2* p = fb;
-        for (int k = 1; k <= l; ++k) {
-            if (k > 1) {  // P_k = F P_{k-1} for every graph (batched DMMA GEMM)
-                if (launch_zgemm((int)n, (int)n, (int)n, fb, n, (int64_t)ml, false, p, n, (int64_t)ml, false, cur, n,
-                                 (int64_t)ml, (int)graphs, false, c->stream) != cudaSuccess) {
-                    rc = fail(FGFRFT_CUDA, "graph batch: GEMM failed");
-                    break;
-                }
-                p = cur;
-                std::swap(prev, cur);
-                g_launches += 1;
-            }
-            if (launch_batch_to_tiled(p, (int)graphs, (int)n, l, k, c->slabs, c->stream) != cudaSuccess) {
-                rc = fail(FGFRFT_CUDA, "graph batch: tiling failed");
-                break;
-            }
-            g_launches += 1;
-        }
-        if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
-            rc = fail(FGFRFT_CUDA, "graph batch: build failed");
-    } while (false);
-    c->tmp.release();
-    if (rc != FGFRFT_OK) {
-        destroy_cache(c);
-        return rc;
-    }
-    *out = c;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_batch_destroy(fgfrft_cache* c) {
-    FGB_GUARD_BEGIN
-    if (c && c->graphs <= 0) return fail(FGFRFT_PARAMETER, "not a graph-batch handle");
-    destroy_cache(c);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_batch_set_stream(fgfrft_cache* c, void* stream) {
-    if (int st = check_batch(c)) return st;
-    std::lock_guard<std::mutex> lk(c->mu);
-    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
-    return FGFRFT_OK;
-}
-
-namespace {
-int batch_coefs(fgfrft_cache* c, const double* alphas_dev, int heads, double** coef) {
-    const size_t orders = (size_t)c->graphs * heads;
-    FGB_CUDA(c->coef.ensure(orders * 2 * (2 * c->l + 1) * sizeof(double)));
-    FGB_LAUNCH(launch_batch_coef(alphas_dev, (int)orders, c->l, c->coef.as<double>(), c->stream), 1);
-    *coef = c->coef.as<double>();
-    return FGFRFT_OK;
-}
-}  // namespace
-
-int fgfrft_batch_forward_dev(fgfrft_cache* c, const double* alphas_dev, int heads, const void* x_dev, int64_t ch,
-                             void* y_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_batch(c)) return st;
-    if (heads < 1 || heads > batch_max_heads()) return fail(FGFRFT_PARAMETER, "graph batch: heads must be 1..4");
-    if (ch < 1 || ch > batch_max_channels()) return fail(FGFRFT_SHAPE, "graph batch: channels must be 1..64");
-    if (!alphas_dev || !x_dev || !y_dev) return fail(FGFRFT_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    double* coef = nullptr;
-    if (int st = batch_coefs(c, alphas_dev, heads, &coef)) return st;
-    ProfScope ps(KC_SYNTH, c->stream);
-    FGB_LAUNCH(launch_batch_forward(c->slabs, (int)c->graphs, (int)c->n, c->l, coef, heads, x_dev, (int)ch, y_dev,
-                                    c->stream),
-               1);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_batch_dlda_dev(fgfrft_cache* c, const double* alphas_dev, int heads, const void* g_dev, const void* x_dev,
-                          int64_t ch, void* dlda_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_batch(c)) return st;
-    if (heads < 1 || heads > batch_max_heads()) return fail(FGFRFT_PARAMETER, "graph batch: heads must be 1..4");
-    if (ch < 1 || ch > batch_max_channels()) return fail(FGFRFT_SHAPE, "graph batch: channels must be 1..64");
-    if (!alphas_dev || !g_dev || !x_dev || !dlda_dev) return fail(FGFRFT_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    double* coef = nullptr;
-    if (int st = batch_coefs(c, alphas_dev, heads, &coef)) return st;
-    ProfScope ps(KC_DOTS, c->stream);
-    FGB_LAUNCH(launch_batch_dlda(c->slabs, (int)c->graphs, (int)c->n, c->l, coef, heads, g_dev, x_dev, (int)ch,
-                                 static_cast<double*>(dlda_dev), c->stream),
-               1);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
 }  // extern "C"
 
 // ------------------------------------------------------------------ INT8 tensor-core DGEMM
 
-namespace {
+namespace fgbi {
 // Stream-ordered scratch stays in the device pool between calls (no release at sync points).
 void keep_pool() {
     static thread_local int done_dev = -1;
@@ -2413,7 +1487,7 @@ void keep_pool() {
     }
     done_dev = dev;
 }
-}  // namespace
+}  // namespace fgbi
 
 int fgfrft_int8_digits(void) { return oz_slices_default(); }
 
@@ -2461,7 +1535,7 @@ int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
     FGB_GUARD_END
 }
 
-namespace {
+namespace fgbi {
 
 // Complex product on the INT8 engine: C (m x n, column-major ldc, complex128) = op(A) op(B),
 // op 0 = N, 1 = T, 2 = C (conjugate transpose), as ONE real Ozaki GEMM with K doubled:
@@ -2534,7 +1608,7 @@ int zgemm_auto(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* a,
     return FGFRFT_OK;
 }
 
-}  // namespace
+}  // namespace fgbi
 
 int fgfrft_zgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                           const double* b, int64_t ldb, double* c, int64_t ldc, void* stream) {
@@ -2548,1301 +1622,3 @@ int fgfrft_zgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
     FGB_GUARD_END
 }
 
-// ------------------------------------------------------------------ GPU-resident denoising learner
-//
-// learn.hpp:291-413 (FastDenoiseEngine, real F) and learn.hpp:471-516 (denoise + Adam, adam.hpp)
-// on the device. Kernels: denoise.cu (pieces), ozgemm.cu (F^m V for all m in one INT8 GEMM),
-// combine.cu (sum_m c_m Z_m for a few coefficient rows).
-
-struct fgfrft_denoise {
-    fgfrft_cache* cache = nullptr;
-    int64_t n = 0, ch = 0, cpad = 0;
-    int l = 0;
-    DevBuf y, x, spow, tpow, gpow, uu, ww, qr, v, r, params, grad, adam, tab, part, scal, best, traj, flag;
-    // exact backend (learn.hpp:205-289): the spectrum and its n x ch complex blocks
-    fgfrft_spectrum* spec = nullptr;
-    bool exact = false, loss_on_real = false;
-    DevBuf xytil, xu, xb, xw, xcot, xvhr, xfar, xq, xt, xph;
-};
-
-namespace {
-
-// handle plumbing shared by both backends (defined after fgfrft_spectrum)
-cudaStream_t dn_stream(const fgfrft_denoise* d);
-std::mutex& dn_mutex(fgfrft_denoise* d);
-int dn_device(const fgfrft_denoise* d);
-int denoise_exact_eval(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch);
-
-// out[m-block] = F^(+-m) V for a real n x ch block V (column-major): one INT8 GEMM over the stacked
-// cache slices; out blocks of stride `stride` doubles in the power-product order.
-int power_products_real(fgfrft_cache* c, const double* src, int64_t ch, double* out, int64_t stride) {
-    if (int st = ensure_power_slices(c)) return st;
-    const int S = c->ps_slices;
-    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(n), rows = 2 * (int64_t)c->l * np;
-    const int64_t bp = ceil_div(ch, kOzTileB) * kOzTileB;
-    FGB_CUDA(c->xsl.ensure((size_t)S * bp * kp));
-    FGB_CUDA(c->xex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
-    int* xe = c->xex.as<int>();
-    {
-        const OzView v{src, n, 1, 0, 0, 0, (int)ch, (int)bp, 1, (int)n, (int)kp, false};
-        ProfScope ps(KC_SLICE, c->stream);
-        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->xsl.as<int8_t>(), xe,
-                                   reinterpret_cast<unsigned long long*>(xe + bp), c->stream),
-                   3);
-    }
-    ProfScope ps(KC_I8GEMM, c->stream);
-    FGB_LAUNCH(launch_ozgemm(S, 0, c->ps.as<int8_t>(), c->pe.as<int>(), (int)rows, c->xsl.as<int8_t>(), xe, (int)bp,
-                             (int)kp, out, n, stride, (int)n, (int)np, (int)ch, c->stream),
-               1);
-    return FGFRFT_OK;
-}
-
-// One evaluation at the device-resident params = [alpha, h_1..h_n]: loss, grad = [d/dalpha, d/dh].
-int denoise_eval_device(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch = -1) {
-    if (d->exact) return denoise_exact_eval(d, params, loss, grad, epoch);
-    fgfrft_cache* c = d->cache;
-    const int l = d->l, T = 2 * l + 1;
-    const int64_t cnt = d->n * d->ch, cp = d->cpad;
-    double* tab = d->tab.as<double>();
-    const double* h = params + 1;
-    FGB_CUDA(c->partial.ensure(combine_partial_elems(combine_max_terms()) * sizeof(double)));
-    FGB_LAUNCH(launch_dn_coef(params, l, tab, c->stream), 1);
-    {
-        ProfScope ps(KC_COMBINE, c->stream);  // u = sum c_m spow_m, du = sum c'_m spow_m
-        FGB_LAUNCH(launch_combine(1, d->spow.as<double>(), d->y.as<double>(), nullptr, cp, l, tab, 2, 0.0,
-                                  d->uu.as<double>(), nullptr, nullptr, nullptr, c->stream),
-                   1);
-    }
-    FGB_LAUNCH(launch_dn_scale(d->uu.as<double>(), h, d->v.as<double>(), (int)d->n, cnt, c->stream), 1);
-    if (int st = power_products_real(c, d->v.as<double>(), d->ch, d->tpow.as<double>(), cp)) return st;
-    {
-        ProfScope ps(KC_COMBINE, c->stream);  // w = Q^H v = sum c_-m tpow_m, dqh_v = sum c'_-m tpow_m
-        FGB_LAUNCH(launch_combine(1, d->tpow.as<double>(), d->v.as<double>(), nullptr, cp, l, tab + 2 * T, 2, 0.0,
-                                  d->ww.as<double>(), nullptr, nullptr, nullptr, c->stream),
-                   1);
-    }
-    double* part = d->part.as<double>();
-    FGB_LAUNCH(launch_dn_residual(d->ww.as<double>(), d->x.as<double>(), d->r.as<double>(), cnt, part, c->stream), 1);
-    if (int st = power_products_real(c, d->r.as<double>(), d->ch, d->gpow.as<double>(), cp)) return st;
-    {
-        ProfScope ps(KC_COMBINE, c->stream);  // qr = Q r = sum c_m gpow_m
-        FGB_LAUNCH(launch_combine(1, d->gpow.as<double>(), d->r.as<double>(), nullptr, cp, l, tab, 1, 0.0,
-                                  d->qr.as<double>(), nullptr, nullptr, nullptr, c->stream),
-                   1);
-    }
-    FGB_LAUNCH(launch_dn_grad(d->uu.as<double>(), d->uu.as<double>() + cp, h, d->r.as<double>(),
-                              d->ww.as<double>() + cp, d->qr.as<double>(), (int)d->n, (int)d->ch, grad, part, loss,
-                              d->flag.as<int>(), epoch, c->stream),
-               2);
-    return FGFRFT_OK;
-}
-
-int check_denoise(const fgfrft_denoise* d) {
-    if (!d || (!d->cache && !d->spec)) return fail(FGFRFT_PARAMETER, "null fgfrft_denoise handle");
-    return FGFRFT_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref, int64_t channels,
-                          fgfrft_denoise** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (int st = check_handle(c)) return st;
-    if (!c->real || c->dtype != FGFRFT_C128)
-        return fail(FGFRFT_PARAMETER, "denoise on the device needs a real F (graph GFT) in a complex128 cache");
-    if (2 * c->l + 1 > combine_max_terms()) return fail(FGFRFT_PARAMETER, "denoise on the device supports L <= 64");
-    if (channels < 1) return fail(FGFRFT_SHAPE, "denoise: need at least one channel");
-    if (!y || !x_ref) return fail(FGFRFT_PARAMETER, "null signal buffer");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    auto* d = new fgfrft_denoise();
-    d->cache = c;
-    d->n = c->n;
-    d->ch = channels;
-    d->l = c->l;
-    const int64_t cnt = d->n * channels;
-    d->cpad = cnt + (cnt & 1);  // even: 16-byte aligned blocks for the combine kernel
-    const size_t blk = (size_t)d->cpad * 8, T = 2 * (size_t)d->l + 1, np = (size_t)d->n + 1;
-    int rc = FGFRFT_OK;
-    if (d->y.ensure(blk) || d->x.ensure(blk) || d->spow.ensure(2 * d->l * blk) || d->tpow.ensure(2 * d->l * blk) ||
-        d->gpow.ensure(2 * d->l * blk) || d->uu.ensure(2 * blk) || d->ww.ensure(2 * blk) || d->qr.ensure(blk) ||
-        d->v.ensure(blk) || d->r.ensure(blk) || d->params.ensure(np * 8) || d->grad.ensure(np * 8) ||
-        d->adam.ensure(2 * np * 8) || d->tab.ensure(4 * T * 8) || d->part.ensure(dn_part_elems() * 8) ||
-        d->scal.ensure(8 * 8) || d->best.ensure((np + 1) * 8) || d->flag.ensure(4 * sizeof(int)))
-        rc = fail(FGFRFT_CAPACITY, "denoise: device allocation failed");
-    if (rc == FGFRFT_OK) {
-        cudaMemsetAsync(d->y.p, 0, blk, c->stream);
-        cudaMemsetAsync(d->x.p, 0, blk, c->stream);
-        if (cudaMemcpyAsync(d->y.p, y, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream) ||
-            cudaMemcpyAsync(d->x.p, x_ref, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream))
-            rc = fail(FGFRFT_CUDA, "denoise: upload failed");
-    }
-    // spow_m = F^m y, m = +-1..+-L: fixed per problem (learn.hpp:300-305)
-    if (rc == FGFRFT_OK) rc = power_products_real(c, d->y.as<double>(), channels, d->spow.as<double>(), d->cpad);
-    if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
-        rc = fail(FGFRFT_CUDA, "denoise: setup failed");
-    if (rc != FGFRFT_OK) {
-        for (DevBuf* b : {&d->y, &d->x, &d->spow, &d->tpow, &d->gpow, &d->uu, &d->ww, &d->qr, &d->v, &d->r,
-                          &d->params, &d->grad, &d->adam, &d->tab, &d->part, &d->scal, &d->best, &d->traj, &d->flag})
-            b->release();
-        delete d;
-        return rc;
-    }
-    *out = d;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_denoise_destroy(fgfrft_denoise* d) {
-    if (!d) return FGFRFT_OK;
-    if (d->cache || d->spec) {
-        DeviceGuard dg(dn_device(d));
-        cudaStreamSynchronize(dn_stream(d));
-    }
-    for (DevBuf* b : {&d->y, &d->x, &d->spow, &d->tpow, &d->gpow, &d->uu, &d->ww, &d->qr, &d->v, &d->r, &d->params,
-                      &d->grad, &d->adam, &d->tab, &d->part, &d->scal, &d->best, &d->traj, &d->flag, &d->xytil,
-                      &d->xu, &d->xb, &d->xw, &d->xcot, &d->xvhr, &d->xfar, &d->xq, &d->xt, &d->xph})
-        b->release();
-    delete d;
-    return FGFRFT_OK;
-}
-
-int fgfrft_denoise_eval(fgfrft_denoise* d, double alpha, const double* h, double* loss, double* grad_alpha,
-                        double* grad_h) {
-    FGB_GUARD_BEGIN
-    if (int st = check_denoise(d)) return st;
-    if (!h) return fail(FGFRFT_PARAMETER, "null filter");
-    std::lock_guard<std::mutex> lk(dn_mutex(d));
-    DeviceGuard dg(dn_device(d));
-    cudaStream_t st = dn_stream(d);
-    double* params = d->params.as<double>();
-    FGB_CUDA(cudaMemcpyAsync(params, &alpha, 8, cudaMemcpyHostToDevice, st));
-    FGB_CUDA(cudaMemcpyAsync(params + 1, h, (size_t)d->n * 8, cudaMemcpyHostToDevice, st));
-    FGB_CUDA(cudaMemsetAsync(d->flag.p, 0, sizeof(int), st));
-    double* sl = d->scal.as<double>();
-    if (int e = denoise_eval_device(d, params, sl, d->grad.as<double>())) return e;
-    std::vector<double> g((size_t)d->n + 1);
-    double lv = 0.0;
-    FGB_CUDA(cudaMemcpyAsync(&lv, sl, 8, cudaMemcpyDeviceToHost, st));
-    FGB_CUDA(cudaMemcpyAsync(g.data(), d->grad.p, g.size() * 8, cudaMemcpyDeviceToHost, st));
-    FGB_CUDA(cudaStreamSynchronize(st));
-    if (loss) *loss = lv;
-    if (grad_alpha) *grad_alpha = g[0];
-    if (grad_h) std::memcpy(grad_h, g.data() + 1, (size_t)d->n * 8);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_denoise_fit(fgfrft_denoise* d, int epochs, double lr, double init_alpha, double* traj_loss,
-                       double* traj_alpha, double* alpha_best, double* h_best, double* loss_best, int* best_epoch,
-                       double* reconstruction) {
-    FGB_GUARD_BEGIN
-    if (int st = check_denoise(d)) return st;
-    if (epochs < 1) return fail(FGFRFT_PARAMETER, "DenoiseConfig: epochs must be >= 1");
-    if (!(lr > 0.0)) return fail(FGFRFT_PARAMETER, "DenoiseConfig: lr must be positive");
-    std::lock_guard<std::mutex> lk(dn_mutex(d));
-    DeviceGuard dg(dn_device(d));
-    cudaStream_t cst = dn_stream(d);
-    const int np = (int)d->n + 1;
-    FGB_CUDA(d->traj.ensure((size_t)2 * (epochs + 1) * 8));
-    double* params = d->params.as<double>();
-    double* m = d->adam.as<double>();
-    double* best = d->best.as<double>();
-    double* sl = d->scal.as<double>();
-    int* bep = d->flag.as<int>() + 1;
-    {  // params = [init_alpha, 1 .. 1] (learn.hpp:475-478); Adam moments zero; best loss = +inf
-        std::vector<double> p0((size_t)np, 1.0);
-        p0[0] = init_alpha;
-        const double inf = std::numeric_limits<double>::infinity();
-        FGB_CUDA(cudaMemcpyAsync(params, p0.data(), (size_t)np * 8, cudaMemcpyHostToDevice, cst));
-        FGB_CUDA(cudaMemsetAsync(m, 0, (size_t)2 * np * 8, cst));
-        FGB_CUDA(cudaMemcpyAsync(best, &inf, 8, cudaMemcpyHostToDevice, cst));
-        const int fl0[4] = {0, 0, std::numeric_limits<int>::max(), std::numeric_limits<int>::max()};
-        FGB_CUDA(cudaMemcpyAsync(d->flag.p, fl0, sizeof fl0, cudaMemcpyHostToDevice, cst));
-        FGB_CUDA(cudaStreamSynchronize(cst));  // p0 / inf / fl0 are host stack buffers
-    }
-    for (int e = 0; e <= epochs; ++e) {  // the final evaluation (e == epochs) is not checked
-        if (int st = denoise_eval_device(d, params, sl, d->grad.as<double>(), e < epochs ? e : -1)) return st;
-        FGB_LAUNCH(launch_dn_track(sl, params, np, e, d->traj.as<double>(), best, bep, cst), 1);
-        if (e < epochs) FGB_LAUNCH(launch_dn_adam(params, m, m + np, d->grad.as<double>(), np, e + 1, lr, cst), 1);
-    }
-    int flags[4] = {0, 0, 0, 0};
-    FGB_CUDA(cudaMemcpyAsync(flags, d->flag.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, cst));
-    std::vector<double> tr((size_t)2 * (epochs + 1)), bb((size_t)np + 1);
-    FGB_CUDA(cudaMemcpyAsync(tr.data(), d->traj.p, tr.size() * 8, cudaMemcpyDeviceToHost, cst));
-    FGB_CUDA(cudaMemcpyAsync(bb.data(), best, bb.size() * 8, cudaMemcpyDeviceToHost, cst));
-    FGB_CUDA(cudaStreamSynchronize(cst));
-    // the reference loop stops at the first failing check: loss of epoch e, then the Adam step's
-    // gradient check (step e + 1)
-    if ((flags[0] & 1) && (!(flags[0] & 2) || flags[2] <= flags[3])) {
-        std::ostringstream msg;
-        msg << "denoise: non-finite loss at epoch " << flags[2];
-        return fail(FGFRFT_OPTIMIZER, msg.str());
-    }
-    if (flags[0] & 2) {
-        std::ostringstream msg;
-        msg << "adam_step: non-finite gradient at step " << flags[3] + 1;
-        return fail(FGFRFT_OPTIMIZER, msg.str());
-    }
-    for (int e = 0; e <= epochs; ++e) {
-        if (traj_loss) traj_loss[e] = tr[2 * e];
-        if (traj_alpha) traj_alpha[e] = tr[2 * e + 1];
-    }
-    if (loss_best) *loss_best = bb[0];
-    if (alpha_best) *alpha_best = bb[1];
-    if (h_best) std::memcpy(h_best, bb.data() + 2, (size_t)d->n * 8);
-    if (best_epoch) *best_epoch = flags[1];
-    if (reconstruction) {  // real part of w at the best parameters (learn.hpp:514)
-        FGB_CUDA(cudaMemcpyAsync(params, best + 1, (size_t)np * 8, cudaMemcpyDeviceToDevice, cst));
-        if (int st = denoise_eval_device(d, params, sl, d->grad.as<double>())) return st;
-        const void* src = d->ww.p;
-        if (d->exact) {  // Re w
-            FGB_LAUNCH(launch_real_part(d->xw.p, d->xt.p, d->n * d->ch, cst), 1);
-            src = d->xt.p;
-        }
-        FGB_CUDA(cudaMemcpyAsync(reconstruction, src, (size_t)d->n * d->ch * 8, cudaMemcpyDeviceToHost, cst));
-        FGB_CUDA(cudaStreamSynchronize(cst));
-    }
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-}  // extern "C"
-
-// ------------------------------------------------------------------ spectral form, exact GFRFT
-//
-// spectral.hpp:19-174 on the device: fgfrft_spectrum holds V (n x n,
-// complex128, HBM) and the ascending phases theta. The exact operator F^a = V diag(e^{j a theta})
-// V^H (and its a-derivative) is one column scaling plus one DMMA complex GEMM per order. The
-// decomposition follows eigendecompose_unitary: Hermitian part to cuSOLVER (syevd / heevd), the
-// clusters of near-equal cos(theta) rediagonalised against the skew part (small Hermitian
-// problems, host Jacobi), Rayleigh quotients, wrap, sort, reconstruction check -- all large
-// products on the device.
-
-struct fgfrft_spectrum {
-    int64_t n = 0;
-    int device = 0;
-    cudaStream_t own_stream = nullptr;
-    cudaStream_t stream = nullptr;
-    std::mutex mu;
-    DevBuf v, theta, alph, w;
-    std::vector<double> theta_h;
-};
-
-struct fgfrft_cascade {
-    fgfrft_cache* cache = nullptr;  // fast backend; nullptr: exact backend through the spectrum
-    fgfrft_spectrum* spec = nullptr;
-    int k = 0;
-    int64_t n = 0;
-    DevBuf target, ops, dops, prefix, b, nb, m, part, out;
-    cudaStream_t stream() const { return cache ? cache->stream : spec->stream; }
-};
-
-namespace {
-
-// cuSOLVER is bound at first use (dlopen), so the library loads without it.
-struct SolverApi {
-    bool ok = false;
-    std::string why;
-    decltype(&cusolverDnCreate) create = nullptr;
-    decltype(&cusolverDnDestroy) destroy = nullptr;
-    decltype(&cusolverDnSetStream) set_stream = nullptr;
-    decltype(&cusolverDnDsyevd_bufferSize) dsyevd_bs = nullptr;
-    decltype(&cusolverDnDsyevd) dsyevd = nullptr;
-    decltype(&cusolverDnZheevd_bufferSize) zheevd_bs = nullptr;
-    decltype(&cusolverDnZheevd) zheevd = nullptr;
-};
-
-const SolverApi& solver_api() {
-    static const SolverApi api = [] {
-        SolverApi a;
-        void* h = nullptr;
-        for (const char* name : {"libcusolver.so.11", "libcusolver.so", "/usr/local/cuda/lib64/libcusolver.so.11"})
-            if ((h = dlopen(name, RTLD_NOW | RTLD_GLOBAL))) break;
-        if (!h) {
-            a.why = "cuSOLVER (libcusolver.so.11) is not loadable";
-            return a;
-        }
-        bool all = true;
-        auto bind = [&](auto& fp, const char* name) {
-            fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
-            all = all && fp != nullptr;
-        };
-        bind(a.create, "cusolverDnCreate");
-        bind(a.destroy, "cusolverDnDestroy");
-        bind(a.set_stream, "cusolverDnSetStream");
-        bind(a.dsyevd_bs, "cusolverDnDsyevd_bufferSize");
-        bind(a.dsyevd, "cusolverDnDsyevd");
-        bind(a.zheevd_bs, "cusolverDnZheevd_bufferSize");
-        bind(a.zheevd, "cusolverDnZheevd");
-        a.ok = all;
-        if (!all) a.why = "cuSOLVER symbols missing";
-        return a;
-    }();
-    return api;
-}
-
-using cd = std::complex<double>;
-
-// Eigenpairs of a small Hermitian matrix (column-major k x k, upper triangle used) by cyclic
-// complex Jacobi rotations: ascending eigenvalues and orthonormal eigenvectors, the role of the
-// cluster SelfAdjointEigenSolver in spectral.hpp:59-64.
-void herm_eig_small(int k, std::vector<cd> a, std::vector<cd>& vec) {
-    for (int j = 0; j < k; ++j) {
-        for (int i = 0; i < j; ++i) a[j + (size_t)i * k] = std::conj(a[i + (size_t)j * k]);
-        a[j + (size_t)j * k] = cd(a[j + (size_t)j * k].real(), 0.0);
-    }
-    vec.assign((size_t)k * k, cd(0.0, 0.0));
-    for (int i = 0; i < k; ++i) vec[i + (size_t)i * k] = 1.0;
-    double norm2 = 0.0;
-    for (const cd& z : a) norm2 += std::norm(z);
-    for (int sweep = 0; sweep < 100 && norm2 > 0.0; ++sweep) {
-        double off = 0.0;
-        for (int q = 0; q < k; ++q)
-            for (int p = 0; p < q; ++p) off += std::norm(a[p + (size_t)q * k]);
-        if (off <= 1e-32 * norm2) break;
-        for (int q = 1; q < k; ++q)
-            for (int p = 0; p < q; ++p) {
-                const cd apq = a[p + (size_t)q * k];
-                const double mag = std::abs(apq);
-                if (mag == 0.0) continue;
-                const cd ph = std::conj(apq / mag);  // e^{-i phi}
-                const double app = a[p + (size_t)p * k].real(), aqq = a[q + (size_t)q * k].real();
-                const double tau = (aqq - app) / (2.0 * mag);
-                const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
-                const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
-                // J = diag(1, e^{-i phi}) [[c, s], [-s, c]] on (p, q): A <- J^H A J, V <- V J
-                const cd jpp = c, jpq = s, jqp = -s * ph, jqq = c * ph;
-                for (int r = 0; r < k; ++r) {
-                    cd& x = a[r + (size_t)p * k];
-                    cd& y = a[r + (size_t)q * k];
-                    const cd nx = x * jpp + y * jqp, ny = x * jpq + y * jqq;
-                    x = nx;
-                    y = ny;
-                    cd& vx = vec[r + (size_t)p * k];
-                    cd& vy = vec[r + (size_t)q * k];
-                    const cd nvx = vx * jpp + vy * jqp, nvy = vx * jpq + vy * jqq;
-                    vx = nvx;
-                    vy = nvy;
-                }
-                for (int r = 0; r < k; ++r) {
-                    cd& x = a[p + (size_t)r * k];
-                    cd& y = a[q + (size_t)r * k];
-                    const cd nx = std::conj(jpp) * x + std::conj(jqp) * y, ny = std::conj(jpq) * x + std::conj(jqq) * y;
-                    x = nx;
-                    y = ny;
-                }
-                a[p + (size_t)q * k] = a[q + (size_t)p * k] = 0.0;
-                a[p + (size_t)p * k] = a[p + (size_t)p * k].real();
-                a[q + (size_t)q * k] = a[q + (size_t)q * k].real();
-            }
-    }
-    std::vector<int> ord(k);
-    std::iota(ord.begin(), ord.end(), 0);
-    std::stable_sort(ord.begin(), ord.end(),
-                     [&](int x, int y) { return a[x + (size_t)x * k].real() < a[y + (size_t)y * k].real(); });
-    std::vector<cd> sorted((size_t)k * k);
-    for (int j = 0; j < k; ++j)
-        for (int i = 0; i < k; ++i) sorted[i + (size_t)j * k] = vec[i + (size_t)ord[j] * k];
-    vec.swap(sorted);
-}
-
-struct ScopedBufs {
-    DevBuf b[16];
-    ~ScopedBufs() {
-        for (DevBuf& x : b) x.release();
-    }
-};
-
-// eigendecompose_unitary (spectral.hpp:121-155) of the host matrix f into s->v / s->theta.
-int spectrum_decompose(fgfrft_spectrum* s, const double* f_host) {
-    const SolverApi& api = solver_api();
-    if (!api.ok) return fail(FGFRFT_NUMERICAL, "eigendecompose_unitary: " + api.why);
-    const int n = (int)s->n;
-    const size_t nn = (size_t)n * n;
-    cudaStream_t st = s->stream;
-    bool real = true;  // GftMatrix::is_real, gft.hpp:34-36
-    for (size_t i = 0; i < nn && real; ++i) real = std::fabs(f_host[2 * i + 1]) <= 1e-13;
-    ScopedBufs sb;
-    DevBuf &f = sb.b[0], &a = sb.b[1], &bh = sb.b[2], &w = sb.b[3], &fw = sb.b[4], &t = sb.b[5], &w2 = sb.b[6],
-           &fw2 = sb.b[7], &cosv = sb.b[8], &info = sb.b[9], &work = sb.b[10], &pairs = sb.b[11], &vals = sb.b[12],
-           &u = sb.b[13], &colinfo = sb.b[14], &part = sb.b[15];
-    if (f.ensure(nn * 16) || a.ensure(nn * 16) || bh.ensure(nn * 16) || w.ensure(nn * 16) || fw.ensure(nn * 16) ||
-        cosv.ensure((size_t)n * 8) || info.ensure(sizeof(int)) || part.ensure((2 * sp_part_elems() + 2) * 8))
-        return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-    FGB_CUDA(cudaMemcpyAsync(f.p, f_host, nn * 16, cudaMemcpyHostToDevice, st));
-    FGB_LAUNCH(launch_herm_parts(f.p, n, real, a.p, bh.p, st), 1);
-    cusolverDnHandle_t h = nullptr;
-    if (api.create(&h) != CUSOLVER_STATUS_SUCCESS) return fail(FGFRFT_NUMERICAL, "cusolverDnCreate failed");
-    api.set_stream(h, st);
-    int lwork = 0;
-    cusolverStatus_t cs;
-    if (real) {
-        cs = api.dsyevd_bs(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, a.as<double>(), n,
-                           cosv.as<double>(), &lwork);
-        if (cs == CUSOLVER_STATUS_SUCCESS && work.ensure((size_t)std::max(lwork, 1) * 8) == cudaSuccess)
-            cs = api.dsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, a.as<double>(), n,
-                            cosv.as<double>(), work.as<double>(), lwork, info.as<int>());
-    } else {
-        cs = api.zheevd_bs(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, a.as<cuDoubleComplex>(), n,
-                           cosv.as<double>(), &lwork);
-        if (cs == CUSOLVER_STATUS_SUCCESS && work.ensure((size_t)std::max(lwork, 1) * 16) == cudaSuccess)
-            cs = api.zheevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, a.as<cuDoubleComplex>(), n,
-                            cosv.as<double>(), work.as<cuDoubleComplex>(), lwork, info.as<int>());
-    }
-    int dev_info = 0;
-    const cudaError_t ce = cudaMemcpyAsync(&dev_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st);
-    const cudaError_t se = cudaStreamSynchronize(st);
-    api.destroy(h);
-    FGB_CUDA(ce);
-    FGB_CUDA(se);
-    if (cs != CUSOLVER_STATUS_SUCCESS || dev_info != 0)
-        return fail(FGFRFT_NUMERICAL, real ? "eigendecompose_unitary: symmetric stage failed"
-                                           : "eigendecompose_unitary: Hermitian stage failed");
-    if (real)
-        FGB_LAUNCH(launch_real_to_cplx(a.as<double>(), (int64_t)nn, w.p, st), 1);
-    else
-        FGB_CUDA(cudaMemcpyAsync(w.p, a.p, nn * 16, cudaMemcpyDeviceToDevice, st));
-    if (int e = zgemm_auto(0, 0, n, n, n, f.p, n, 0, w.p, n, 0, fw.p, n, 0, 1, st)) return e;  // F W
-    std::vector<double> cv(n);
-    FGB_CUDA(cudaMemcpyAsync(cv.data(), cosv.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
-    FGB_CUDA(cudaStreamSynchronize(st));
-    // clusters of cos(theta) closer than kClusterGap = 1e-5 (spectral.hpp:45, 55-58)
-    std::vector<std::pair<int, int>> clusters;  // (lo, k)
-    bool any = false;
-    for (int lo = 0; lo < n;) {
-        int hi = lo;
-        while (hi + 1 < n && cv[hi + 1] - cv[hi] <= 1e-5) ++hi;
-        clusters.emplace_back(lo, hi - lo + 1);
-        any = any || hi > lo;
-        lo = hi + 1;
-    }
-    if (any) {
-        // M_c = W_c^H Bh W_c for every cluster of size > 1 (column-major k x k)
-        if (t.ensure(nn * 16) || w2.ensure(nn * 16) || fw2.ensure(nn * 16))
-            return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-        if (int e = zgemm_auto(0, 0, n, n, n, bh.p, n, 0, w.p, n, 0, t.p, n, 0, 1, st)) return e;
-        std::vector<int> pr;
-        for (const auto& c : clusters)
-            if (c.second > 1)
-                for (int j = 0; j < c.second; ++j)
-                    for (int i = 0; i < c.second; ++i) {
-                        pr.push_back(c.first + i);
-                        pr.push_back(c.first + j);
-                    }
-        const int cnt = (int)(pr.size() / 2);
-        if (pairs.ensure(pr.size() * sizeof(int)) || vals.ensure((size_t)cnt * 16))
-            return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-        FGB_CUDA(cudaMemcpyAsync(pairs.p, pr.data(), pr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        FGB_LAUNCH(launch_col_pair_dot(w.p, t.p, n, pairs.as<int>(), cnt, vals.p, st), 1);
-        std::vector<cd> mv((size_t)cnt);
-        FGB_CUDA(cudaMemcpyAsync(mv.data(), vals.p, (size_t)cnt * 16, cudaMemcpyDeviceToHost, st));
-        FGB_CUDA(cudaStreamSynchronize(st));
-        // block-diagonal U: every column gets (lo, k, offset); singletons a 1 x 1 identity block
-        std::vector<int> ci((size_t)3 * n);
-        std::vector<cd> ub;
-        size_t moff = 0;
-        for (const auto& c : clusters) {
-            const int lo = c.first, k = c.second;
-            const int off = (int)ub.size();
-            if (k == 1) {
-                ub.push_back(1.0);
-            } else {
-                std::vector<cd> m(mv.begin() + moff, mv.begin() + moff + (size_t)k * k), vec;
-                moff += (size_t)k * k;
-                herm_eig_small(k, std::move(m), vec);
-                ub.insert(ub.end(), vec.begin(), vec.end());
-            }
-            for (int j = 0; j < k; ++j) {
-                ci[3 * (size_t)(lo + j)] = lo;
-                ci[3 * (size_t)(lo + j) + 1] = k;
-                ci[3 * (size_t)(lo + j) + 2] = off;
-            }
-        }
-        if (u.ensure(ub.size() * 16) || colinfo.ensure(ci.size() * sizeof(int)))
-            return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-        FGB_CUDA(cudaMemcpyAsync(u.p, ub.data(), ub.size() * 16, cudaMemcpyHostToDevice, st));
-        FGB_CUDA(cudaMemcpyAsync(colinfo.p, ci.data(), ci.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        FGB_LAUNCH(launch_blockdiag(w.p, n, colinfo.as<int>(), u.p, w2.p, st), 1);
-        FGB_LAUNCH(launch_blockdiag(fw.p, n, colinfo.as<int>(), u.p, fw2.p, st), 1);
-        std::swap(w.p, w2.p);
-        std::swap(w.cap, w2.cap);
-        std::swap(fw.p, fw2.p);
-        std::swap(fw.cap, fw2.cap);
-        FGB_CUDA(cudaStreamSynchronize(st));  // host staging (ub, ci) is released at scope exit
-    }
-    // Rayleigh quotients lambda_c = w_c^H F w_c, theta = wrap_phase(lambda) (spectral.hpp:34-38, 67)
-    {
-        std::vector<int> pr((size_t)2 * n);
-        for (int c = 0; c < n; ++c) pr[2 * (size_t)c] = pr[2 * (size_t)c + 1] = c;
-        if (pairs.ensure(pr.size() * sizeof(int)) || vals.ensure((size_t)n * 16))
-            return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-        FGB_CUDA(cudaMemcpyAsync(pairs.p, pr.data(), pr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        FGB_LAUNCH(launch_col_pair_dot(w.p, fw.p, n, pairs.as<int>(), n, vals.p, st), 1);
-        std::vector<cd> lam((size_t)n);
-        FGB_CUDA(cudaMemcpyAsync(lam.data(), vals.p, (size_t)n * 16, cudaMemcpyDeviceToHost, st));
-        FGB_CUDA(cudaStreamSynchronize(st));
-        std::vector<double> th((size_t)n);
-        for (int c = 0; c < n; ++c) {
-            double tv = std::atan2(lam[c].imag(), lam[c].real());
-            if (tv <= -M_PI) tv = M_PI;
-            th[c] = tv;
-        }
-        // reconstruction residual |F W - W diag(e^{j theta})| / |F| <= 1e-6 (spectral.hpp:141-153)
-        FGB_CUDA(cudaMemcpyAsync(cosv.p, th.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
-        double* pp = part.as<double>();
-        FGB_CUDA(launch_eig_residual(fw.p, w.p, cosv.as<double>(), f.p, n, pp, pp + 2 * sp_part_elems(), st));
-        g_launches += 2;
-        double rr[2] = {0.0, 0.0};
-        FGB_CUDA(cudaMemcpyAsync(rr, pp + 2 * sp_part_elems(), 16, cudaMemcpyDeviceToHost, st));
-        FGB_CUDA(cudaStreamSynchronize(st));
-        const double rel = std::sqrt(rr[0]) / std::max(std::sqrt(rr[1]), 1e-300);
-        if (!(rel <= 1e-6)) {
-            std::ostringstream msg;
-            msg << "eigendecompose_unitary: reconstruction residual " << rel << " exceeds 1e-6";
-            return fail(FGFRFT_NUMERICAL, msg.str());
-        }
-        std::vector<int> order((size_t)n);
-        std::iota(order.begin(), order.end(), 0);
-        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return th[x] < th[y]; });
-        s->theta_h.resize((size_t)n);
-        for (int c = 0; c < n; ++c) s->theta_h[c] = th[order[c]];
-        if (s->v.ensure(nn * 16) || s->theta.ensure((size_t)n * 8))
-            return fail(FGFRFT_CAPACITY, "eigendecompose_unitary: device allocation failed");
-        FGB_CUDA(cudaMemcpyAsync(pairs.p, order.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice, st));
-        FGB_LAUNCH(launch_gather_cols(w.p, n, pairs.as<int>(), s->v.p, st), 1);
-        FGB_CUDA(cudaMemcpyAsync(s->theta.p, s->theta_h.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
-        FGB_CUDA(cudaStreamSynchronize(st));
-    }
-    return FGFRFT_OK;
-}
-
-// out[a] = V diag(d_a) V^H for the orders (which: FGFRFT_Q or FGFRFT_DQ), spectral.hpp:158-174.
-int exact_into(fgfrft_spectrum* s, const double* alphas, int na, int which, void* out, cudaStream_t st) {
-    const int n = (int)s->n;
-    const size_t nn = (size_t)n * n;
-    const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)na, ((size_t)2 << 30) / (nn * 16)));
-    FGB_CUDA(s->alph.ensure((size_t)na * 8));
-    FGB_CUDA(s->w.ensure((size_t)chunk * nn * 16));
-    FGB_CUDA(cudaMemcpyAsync(s->alph.p, alphas, (size_t)na * 8, cudaMemcpyHostToDevice, st));
-    for (int a0 = 0; a0 < na; a0 += chunk) {
-        const int nc = std::min(chunk, na - a0);
-        FGB_LAUNCH(launch_spec_scale(s->v.p, s->theta.as<double>(), s->alph.as<double>() + a0, nc, which, n, s->w.p,
-                                     st),
-                   1);
-        if (int e = zgemm_auto(0, 2, n, n, n, s->w.p, n, (int64_t)nn, s->v.p, n, 0,
-                               static_cast<double2*>(out) + (size_t)a0 * nn, n, (int64_t)nn, nc, st))
-            return e;
-    }
-    return FGFRFT_OK;
-}
-
-int check_spectrum(const fgfrft_spectrum* s) {
-    if (!s) return fail(FGFRFT_PARAMETER, "null fgfrft_spectrum handle");
-    return FGFRFT_OK;
-}
-
-int spectrum_new(int64_t n, int device, fgfrft_spectrum** out) {
-    auto* s = new fgfrft_spectrum();
-    s->n = n;
-    s->device = device;
-    cudaError_t e = cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-        delete s;
-        return fail(FGFRFT_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
-    }
-    s->stream = s->own_stream;
-    *out = s;
-    return FGFRFT_OK;
-}
-
-void spectrum_free(fgfrft_spectrum* s) {
-    if (s->stream) cudaStreamSynchronize(s->stream);
-    for (DevBuf* b : {&s->v, &s->theta, &s->alph, &s->w}) b->release();
-    if (s->own_stream) cudaStreamDestroy(s->own_stream);
-    delete s;
-}
-
-// ---- cascade (learn.hpp:55-166)
-
-// loss and per-layer gradients at the host orders: out_host[0] = loss, out_host[1 + l] = grad_l.
-//   forward: prefix_l = Q_l prefix_{l-1}, resid = prefix_{K-1} - target, loss = |resid|^2 / N^2
-//   reverse: grad_l = 2/N^2 Re<b, dQ_l prefix_{l-1}>, b <- Q_l^H b           (learn.hpp:72-97)
-// Complex F: Re<b, dQ X> is taken as Re<b X^H, dQ> (complex GEMMs on the FP64 tensor cores).
-// Real F (fast backend): Q_l, dQ_l and the prefixes are real, so the products are real DMMA GEMMs
-// (dQ_l prefix_{l-1} real x real, Q_l^T b real x complex): a third of the complex flops.
-int cascade_eval_device(fgfrft_cascade* cs, const double* alphas, double* out_host) {
-    const int K = cs->k;
-    const int n = (int)cs->n;
-    const size_t nn = (size_t)n * n;
-    cudaStream_t st = cs->stream();
-    const bool real = cs->cache && cs->cache->real;
-    const size_t es = real ? 8 : 16;
-    char* ops = cs->ops.as<char>();
-    char* dops = cs->dops.as<char>();
-    if (cs->cache) {
-        fgfrft_cache* c = cs->cache;
-        double* coef = nullptr;
-        if (int e = upload_coefs(c, alphas, K, c->l, &coef)) return e;
-        if (int e = synth_into(c, coef, K, c->l, ops, real)) return e;
-        if (int e = synth_into(c, coef + (size_t)K * (2 * c->l + 1), K, c->l, dops, real)) return e;
-    } else {
-        if (int e = exact_into(cs->spec, alphas, K, FGFRFT_Q, ops, st)) return e;
-        if (int e = exact_into(cs->spec, alphas, K, FGFRFT_DQ, dops, st)) return e;
-    }
-    auto op = [&](char* base, int l) { return static_cast<void*>(base + (size_t)l * nn * es); };
-    auto prefix = [&](int l) { return l == 0 ? op(ops, 0) : op(cs->prefix.as<char>(), l); };
-    // real x real products: INT8 Ozaki engine where the cache's engine selects it, else DMMA
-    const bool i8 = real && use_int8_gemm(cs->cache, n);
-    auto real_mm = [&](const void* a, const void* bb, void* cc) -> int {
-        if (i8)
-            return fgfrft_dgemm_int8_dev(0, 0, n, n, n, static_cast<const double*>(a), n,
-                                         static_cast<const double*>(bb), n, static_cast<double*>(cc), n, 0, st);
-        ProfScope ps(KC_GEMM, st);
-        FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, a, n, 0, bb, n, 0, cc, n, 0, 1, st), 1);
-        return FGFRFT_OK;
-    };
-    for (int l = 1; l < K; ++l) {
-        if (real) {
-            if (int e = real_mm(op(ops, l), prefix(l - 1), prefix(l))) return e;
-            continue;
-        }
-        if (int e = zgemm_auto(0, 0, n, n, n, op(ops, l), n, 0, prefix(l - 1), n, 0, prefix(l), n, 0, 1, st)) return e;
-    }
-    double* part = cs->part.as<double>();
-    const size_t G = sp_part_elems();
-    double2* b = cs->b.as<double2>();
-    double2* nb = cs->nb.as<double2>();
-    FGB_LAUNCH(launch_cdiff_sq(prefix(K - 1), real, cs->target.p, (int64_t)nn, b, part, st), 1);
-    for (int l = K - 1; l >= 0; --l) {
-        if (l > 0) {
-            {
-                ProfScope ps(KC_GEMM, st);
-                if (real) {  // dY = dQ_l prefix_{l-1}
-                    if (int e = real_mm(op(dops, l), prefix(l - 1), cs->m.p)) return e;
-                } else {  // M = b prefix_{l-1}^H
-                    if (int e = zgemm_auto(0, 2, n, n, n, b, n, 0, prefix(l - 1), n, 0, cs->m.p, n, 0, 1, st))
-                        return e;
-                }
-            }
-            if (real)
-                FGB_LAUNCH(launch_cre_dot(b, cs->m.p, true, (int64_t)nn, part + (1 + l) * G, st), 1);
-            else
-                FGB_LAUNCH(launch_cre_dot(cs->m.p, op(dops, l), false, (int64_t)nn, part + (1 + l) * G, st), 1);
-            ProfScope ps(KC_GEMM, st);
-            if (i8) {  // b <- Q_l^T b
-                if (int e = int8_qx(cs->cache, 1, true, op(ops, l), b, n, nb)) return e;
-            } else if (real) {  // over the (re, im) columns
-                FGB_LAUNCH(launch_rgemm(1, 1, 1, n, 2 * n, n, op(ops, l), n, 0, b, n, 0, nb, n, 0, 1, st), 1);
-            } else if (int e = zgemm_auto(2, 0, n, n, n, op(ops, l), n, 0, b, n, 0, nb, n, 0, 1, st)) {
-                return e;
-            }
-            std::swap(b, nb);
-        } else {
-            FGB_LAUNCH(launch_cre_dot(b, dops, real, (int64_t)nn, part + G, st), 1);
-        }
-    }
-    const double inv = 1.0 / ((double)n * (double)n);
-    FGB_LAUNCH(launch_sum_parts(part, K + 1, inv, 2.0 * inv, cs->out.as<double>(), st), 1);
-    FGB_CUDA(cudaMemcpyAsync(out_host, cs->out.p, (size_t)(K + 1) * 8, cudaMemcpyDeviceToHost, st));
-    FGB_CUDA(cudaStreamSynchronize(st));
-    return FGFRFT_OK;
-}
-
-int check_cascade(const fgfrft_cascade* cs) {
-    if (!cs || !cs->spec) return fail(FGFRFT_PARAMETER, "null fgfrft_cascade handle");
-    return FGFRFT_OK;
-}
-
-// Locks the handle(s) the cascade computes through.
-struct CascadeLock {
-    std::unique_lock<std::mutex> a, b;
-    explicit CascadeLock(fgfrft_cascade* cs) : b(cs->spec->mu) {
-        if (cs->cache) a = std::unique_lock<std::mutex>(cs->cache->mu);
-    }
-};
-
-}  // namespace
-
-extern "C" {
-
-int fgfrft_spectrum_create(const double* v, const double* theta, int64_t n, int device, fgfrft_spectrum** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (n < 1) return fail(FGFRFT_SHAPE, "spectrum: n must be >= 1");
-    if (!v || !theta) return fail(FGFRFT_PARAMETER, "null spectrum buffer");
-    for (int64_t k = 0; k < n; ++k)
-        if (!std::isfinite(theta[k])) return fail(FGFRFT_PARAMETER, "spectrum: phases must be finite");
-    DeviceGuard dg(device);
-    fgfrft_spectrum* s = nullptr;
-    if (int st = spectrum_new(n, device, &s)) return st;
-    const size_t nn = (size_t)n * n;
-    int rc = FGFRFT_OK;
-    if (s->v.ensure(nn * 16) || s->theta.ensure((size_t)n * 8))
-        rc = fail(FGFRFT_CAPACITY, "spectrum: device allocation failed");
-    if (rc == FGFRFT_OK) {
-        s->theta_h.assign(theta, theta + n);
-        if (cudaMemcpyAsync(s->v.p, v, nn * 16, cudaMemcpyHostToDevice, s->stream) ||
-            cudaMemcpyAsync(s->theta.p, theta, (size_t)n * 8, cudaMemcpyHostToDevice, s->stream) ||
-            cudaStreamSynchronize(s->stream))
-            rc = fail(FGFRFT_CUDA, "spectrum: upload failed");
-    }
-    if (rc != FGFRFT_OK) {
-        spectrum_free(s);
-        return rc;
-    }
-    *out = s;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_spectrum_decompose(const double* f, int64_t n, int device, fgfrft_spectrum** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (n < 1) return fail(FGFRFT_SHAPE, "eigendecompose_unitary: n must be >= 1");
-    if (n > (1 << 15)) return fail(FGFRFT_SHAPE, "eigendecompose_unitary: n too large");
-    if (!f) return fail(FGFRFT_PARAMETER, "null matrix");
-    DeviceGuard dg(device);
-    fgfrft_spectrum* s = nullptr;
-    if (int st = spectrum_new(n, device, &s)) return st;
-    if (int st = spectrum_decompose(s, f)) {
-        spectrum_free(s);
-        return st;
-    }
-    *out = s;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_spectrum_destroy(fgfrft_spectrum* s) {
-    if (!s) return FGFRFT_OK;
-    DeviceGuard dg(s->device);
-    spectrum_free(s);
-    return FGFRFT_OK;
-}
-
-int fgfrft_spectrum_info(const fgfrft_spectrum* s, int64_t* n, double* theta) {
-    if (int st = check_spectrum(s)) return st;
-    if (n) *n = s->n;
-    if (theta) std::memcpy(theta, s->theta_h.data(), (size_t)s->n * 8);
-    return FGFRFT_OK;
-}
-
-int fgfrft_spectrum_vectors(fgfrft_spectrum* s, double* v) {
-    FGB_GUARD_BEGIN
-    if (int st = check_spectrum(s)) return st;
-    if (!v) return fail(FGFRFT_PARAMETER, "null output");
-    std::lock_guard<std::mutex> lk(s->mu);
-    DeviceGuard dg(s->device);
-    FGB_CUDA(cudaMemcpyAsync(v, s->v.p, (size_t)s->n * s->n * 16, cudaMemcpyDeviceToHost, s->stream));
-    FGB_CUDA(cudaStreamSynchronize(s->stream));
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_spectrum_set_stream(fgfrft_spectrum* s, void* stream) {
-    if (int st = check_spectrum(s)) return st;
-    std::lock_guard<std::mutex> lk(s->mu);
-    s->stream = stream ? static_cast<cudaStream_t>(stream) : s->own_stream;
-    return FGFRFT_OK;
-}
-
-int fgfrft_exact_dev(fgfrft_spectrum* s, const double* alphas, int n_alpha, int which, void* out_dev) {
-    FGB_GUARD_BEGIN
-    if (int st = check_spectrum(s)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (which != FGFRFT_Q && which != FGFRFT_DQ) return fail(FGFRFT_PARAMETER, "which must be FGFRFT_Q or FGFRFT_DQ");
-    if (!out_dev) return fail(FGFRFT_PARAMETER, "null output");
-    std::lock_guard<std::mutex> lk(s->mu);
-    DeviceGuard dg(s->device);
-    return exact_into(s, alphas, n_alpha, which, out_dev, s->stream);
-    FGB_GUARD_END
-}
-
-int fgfrft_exact(fgfrft_spectrum* s, const double* alphas, int n_alpha, int which, double* out) {
-    FGB_GUARD_BEGIN
-    if (int st = check_spectrum(s)) return st;
-    if (int st = check_alphas(alphas, n_alpha)) return st;
-    if (which != FGFRFT_Q && which != FGFRFT_DQ) return fail(FGFRFT_PARAMETER, "which must be FGFRFT_Q or FGFRFT_DQ");
-    if (!out) return fail(FGFRFT_PARAMETER, "null output");
-    std::lock_guard<std::mutex> lk(s->mu);
-    DeviceGuard dg(s->device);
-    const size_t nn = (size_t)s->n * s->n;
-    DevBuf o;
-    if (o.ensure((size_t)n_alpha * nn * 16)) return fail(FGFRFT_CAPACITY, "exact_gfrft: device allocation failed");
-    int rc = exact_into(s, alphas, n_alpha, which, o.p, s->stream);
-    if (rc == FGFRFT_OK &&
-        (cudaMemcpyAsync(out, o.p, (size_t)n_alpha * nn * 16, cudaMemcpyDeviceToHost, s->stream) ||
-         cudaStreamSynchronize(s->stream)))
-        rc = fail(FGFRFT_CUDA, "exact_gfrft: download failed");
-    o.release();
-    return rc;
-    FGB_GUARD_END
-}
-
-int fgfrft_cascade_create(fgfrft_cache* cache, fgfrft_spectrum* spec, double target_order, int depth,
-                          fgfrft_cascade** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (int st = check_spectrum(spec)) return st;
-    if (depth < 1) return fail(FGFRFT_PARAMETER, "CascadeConfig: depth must be >= 1");
-    if (!std::isfinite(target_order)) return fail(FGFRFT_PARAMETER, "CascadeConfig: target order must be finite");
-    if (cache) {
-        if (int st = check_handle(cache)) return st;
-        if (cache->dtype != FGFRFT_C128) return fail(FGFRFT_PARAMETER, "cascade: the fast backend needs a complex128 cache");
-        if (cache->n != spec->n) return fail(FGFRFT_SHAPE, "cascade: cache and spectrum sizes differ");
-        if (cache->device != spec->device) return fail(FGFRFT_PARAMETER, "cascade: cache and spectrum on different devices");
-    }
-    std::lock_guard<std::mutex> lk(spec->mu);
-    DeviceGuard dg(spec->device);
-    auto* cs = new fgfrft_cascade();
-    cs->cache = cache;
-    cs->spec = spec;
-    cs->k = depth;
-    cs->n = spec->n;
-    const size_t blk = (size_t)cs->n * cs->n * 16;
-    int rc = FGFRFT_OK;
-    if (cs->target.ensure(blk) || cs->ops.ensure((size_t)depth * blk) || cs->dops.ensure((size_t)depth * blk) ||
-        cs->prefix.ensure((size_t)depth * blk) || cs->b.ensure(blk) || cs->nb.ensure(blk) ||
-        (depth > 1 && cs->m.ensure(blk)) || cs->part.ensure((size_t)(depth + 1) * sp_part_elems() * 8) ||
-        cs->out.ensure((size_t)(depth + 1) * 8))
-        rc = fail(FGFRFT_CAPACITY, "cascade: device allocation failed");
-    // target = F^{target_order} from the spectrum, always exact (learn.hpp:61)
-    if (rc == FGFRFT_OK) rc = exact_into(spec, &target_order, 1, FGFRFT_Q, cs->target.p, spec->stream);
-    if (rc == FGFRFT_OK && cudaStreamSynchronize(spec->stream) != cudaSuccess)
-        rc = fail(FGFRFT_CUDA, "cascade: target construction failed");
-    if (rc != FGFRFT_OK) {
-        for (DevBuf* b : {&cs->target, &cs->ops, &cs->dops, &cs->prefix, &cs->b, &cs->nb, &cs->m, &cs->part, &cs->out})
-            b->release();
-        delete cs;
-        return rc;
-    }
-    *out = cs;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_cascade_destroy(fgfrft_cascade* cs) {
-    if (!cs) return FGFRFT_OK;
-    if (cs->spec) {
-        DeviceGuard dg(cs->spec->device);
-        cudaStreamSynchronize(cs->stream());
-    }
-    for (DevBuf* b : {&cs->target, &cs->ops, &cs->dops, &cs->prefix, &cs->b, &cs->nb, &cs->m, &cs->part, &cs->out})
-        b->release();
-    delete cs;
-    return FGFRFT_OK;
-}
-
-int fgfrft_cascade_eval(fgfrft_cascade* cs, const double* alphas, double* loss, double* grad) {
-    FGB_GUARD_BEGIN
-    if (int st = check_cascade(cs)) return st;
-    if (!alphas) return fail(FGFRFT_PARAMETER, "null orders");
-    if (int st = check_alphas(alphas, cs->k)) return st;
-    CascadeLock lk(cs);
-    DeviceGuard dg(cs->spec->device);
-    std::vector<double> o((size_t)cs->k + 1);
-    if (int st = cascade_eval_device(cs, alphas, o.data())) return st;
-    if (loss) *loss = o[0];
-    if (grad) std::memcpy(grad, o.data() + 1, (size_t)cs->k * 8);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_cascade_learn(fgfrft_cascade* cs, double init_order, int epochs, double lr, double* traj_loss,
-                         double* traj_alphas, double* final_loss, double* final_alphas) {
-    FGB_GUARD_BEGIN
-    if (int st = check_cascade(cs)) return st;
-    if (epochs < 1) return fail(FGFRFT_PARAMETER, "CascadeConfig: epochs must be >= 1");
-    if (!(lr > 0.0)) return fail(FGFRFT_PARAMETER, "CascadeConfig: lr must be positive");
-    if (!std::isfinite(init_order)) return fail(FGFRFT_PARAMETER, "CascadeConfig: init order must be finite");
-    CascadeLock lk(cs);
-    DeviceGuard dg(cs->spec->device);
-    const int K = cs->k;
-    // AdamState::init(constant(init_order), lr), adam_step (adam.hpp:24-53)
-    std::vector<double> p((size_t)K, init_order), m((size_t)K, 0.0), v((size_t)K, 0.0), o((size_t)K + 1);
-    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-    int64_t step = 0;
-    auto record = [&](int e, double l) {
-        if (traj_loss) traj_loss[e] = l;
-        if (traj_alphas) std::memcpy(traj_alphas + (size_t)e * K, p.data(), (size_t)K * 8);
-    };
-    for (int e = 0; e < epochs; ++e) {  // learn.hpp:142-152
-        if (int st = cascade_eval_device(cs, p.data(), o.data())) return st;
-        if (!std::isfinite(o[0])) {
-            std::ostringstream msg;
-            msg << "learn_orders: non-finite loss at epoch " << e;
-            return fail(FGFRFT_OPTIMIZER, msg.str());
-        }
-        record(e, o[0]);
-        for (int i = 0; i < K; ++i)
-            if (!std::isfinite(o[1 + i])) {
-                std::ostringstream msg;
-                msg << "adam_step: non-finite gradient at step " << step + 1 << ", parameter " << i;
-                return fail(FGFRFT_OPTIMIZER, msg.str());
-            }
-        ++step;
-        const double c1 = 1.0 - std::pow(b1, (double)step), c2 = 1.0 - std::pow(b2, (double)step);
-        for (int i = 0; i < K; ++i) {
-            const double g = o[1 + i];
-            m[i] = b1 * m[i] + (1.0 - b1) * g;
-            v[i] = b2 * v[i] + (1.0 - b2) * (g * g);
-            p[i] = p[i] - lr * (m[i] / c1) / (std::sqrt(v[i] / c2) + eps);
-        }
-    }
-    if (int st = cascade_eval_device(cs, p.data(), o.data())) return st;  // learn.hpp:154-155
-    record(epochs, o[0]);
-    if (final_loss) *final_loss = o[0];
-    if (final_alphas) std::memcpy(final_alphas, p.data(), (size_t)K * 8);
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-}  // extern "C"
-
-// ------------------------------------------------------------------ on-disk power cache
-//
-// the reference rebuilds its cache every run (no binary format for F or the
-// powers, io.hpp holds only PGM/XYZ/CSV/manifest). File layout (little endian):
-//   CacheFileHeader (128 bytes)
-//   F: n x n complex128, column-major -- the bytes content_fingerprint hashes (gft.hpp:46-48)
-//   the resident slabs exactly as in HBM (tiled 32 x 32, padded to npad, real / c128 / c64)
-//   one u64: order-independent checksum of the slab bytes (store.cu), re-checked after load
-// The slabs move through two pinned 64 MiB staging buffers so file IO overlaps the copies.
-
-namespace {
-
-struct CacheFileHeader {
-    char magic[8];  // "FGFRFTC\x01"
-    uint32_t version, dtype, real, elem;
-    int64_t n;
-    int32_t l, tile;
-    uint64_t fingerprint, slab_bytes, f_bytes;
-    uint64_t reserved[7];
-    uint64_t header_fnv;  // fnv1a64 of the preceding 120 bytes
-};
-static_assert(sizeof(CacheFileHeader) == 128, "cache file header is 128 bytes");
-constexpr char kCacheMagic[8] = {'F', 'G', 'F', 'R', 'F', 'T', 'C', 1};
-constexpr size_t kStageBytes = (size_t)64 << 20;
-
-struct FileCloser {
-    std::FILE* f = nullptr;
-    ~FileCloser() {
-        if (f) std::fclose(f);
-    }
-};
-struct PinnedPair {
-    void* p[2] = {nullptr, nullptr};
-    cudaEvent_t e[2] = {nullptr, nullptr};
-    cudaError_t init() {
-        for (int i = 0; i < 2; ++i) {
-            if (cudaError_t r = cudaMallocHost(&p[i], kStageBytes)) return r;
-            if (cudaError_t r = cudaEventCreateWithFlags(&e[i], cudaEventDisableTiming)) return r;
-        }
-        return cudaSuccess;
-    }
-    ~PinnedPair() {
-        for (int i = 0; i < 2; ++i) {
-            if (e[i]) cudaEventSynchronize(e[i]), cudaEventDestroy(e[i]);
-            if (p[i]) cudaFreeHost(p[i]);
-        }
-    }
-};
-
-int slab_checksum(fgfrft_cache* c, unsigned long long* out) {
-    FGB_CUDA(c->lpart.ensure(sizeof(unsigned long long)));
-    FGB_LAUNCH(launch_checksum(c->slabs, c->slab_bytes() * (size_t)c->l, c->lpart.as<unsigned long long>(), c->stream),
-               1);
-    FGB_CUDA(cudaMemcpyAsync(out, c->lpart.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-    FGB_CUDA(cudaStreamSynchronize(c->stream));
-    return FGFRFT_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int fgfrft_cache_save(fgfrft_cache* c, const char* path) {
-    FGB_GUARD_BEGIN
-    if (int st = check_handle(c)) return st;
-    if (!path) return fail(FGFRFT_PARAMETER, "null path");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard dg(c->device);
-    const size_t ml = c->mat_elems();
-    // F = P_1 back in complex128 column-major (the fingerprinted bytes; a complex64 cache stores
-    // its rounded F and keeps the original fingerprint in the header)
-    std::vector<double> f(2 * ml);
-    FGB_CUDA(c->tmp.ensure(ml * 16));
-    if (c->real)
-        FGB_LAUNCH(launch_rfrom_tiled(c->slab(1), c->tmp.p, (int)c->n, c->stream), 1);
-    else
-        FGB_LAUNCH(launch_from_tiled(c->slab(1), c->tmp.p, (int)c->n, (int)c->elem, c->stream), 1);
-    FGB_CUDA(cudaMemcpyAsync(f.data(), c->tmp.p, ml * 16, cudaMemcpyDeviceToHost, c->stream));
-    FGB_CUDA(cudaStreamSynchronize(c->stream));
-    c->tmp.release();
-    unsigned long long sum = 0;
-    if (int st = slab_checksum(c, &sum)) return st;
-    CacheFileHeader h{};
-    std::memcpy(h.magic, kCacheMagic, 8);
-    h.version = 1;
-    h.dtype = (uint32_t)(c->api_c64 ? FGFRFT_C64 : c->dtype);
-    h.real = c->real ? 1u : 0u;
-    h.elem = (uint32_t)c->elem;
-    h.n = c->n;
-    h.l = c->l;
-    h.tile = kTile;
-    h.fingerprint = c->fingerprint;
-    h.slab_bytes = c->slab_bytes();
-    h.f_bytes = ml * 16;
-    h.header_fnv = host_fnv1a64(&h, offsetof(CacheFileHeader, header_fnv));
-    FileCloser fc;
-    fc.f = std::fopen(path, "wb");
-    if (!fc.f) return fail(FGFRFT_IO, std::string("cannot open ") + path + " for writing");
-    if (std::fwrite(&h, sizeof h, 1, fc.f) != 1 || std::fwrite(f.data(), 16, ml, fc.f) != ml)
-        return fail(FGFRFT_IO, std::string("failed writing ") + path);
-    // slabs: D2H into one staging buffer while the other is written to the file
-    PinnedPair pp;
-    FGB_CUDA(pp.init());
-    const size_t total = c->slab_bytes() * (size_t)c->l;
-    const char* src = static_cast<const char*>(c->slabs);
-    size_t sizes[2] = {0, 0};
-    auto enqueue = [&](size_t off, int b) -> int {
-        sizes[b] = std::min(kStageBytes, total - off);
-        FGB_CUDA(cudaMemcpyAsync(pp.p[b], src + off, sizes[b], cudaMemcpyDeviceToHost, c->stream));
-        FGB_CUDA(cudaEventRecord(pp.e[b], c->stream));
-        return FGFRFT_OK;
-    };
-    if (int st = enqueue(0, 0)) return st;
-    for (size_t off = 0, i = 0; off < total; off += kStageBytes, ++i) {
-        const int b = (int)(i & 1);
-        FGB_CUDA(cudaEventSynchronize(pp.e[b]));
-        if (off + kStageBytes < total)
-            if (int st = enqueue(off + kStageBytes, b ^ 1)) return st;
-        if (std::fwrite(pp.p[b], 1, sizes[b], fc.f) != sizes[b]) return fail(FGFRFT_IO, std::string("failed writing ") + path);
-    }
-    const uint64_t s64 = sum;
-    if (std::fwrite(&s64, 8, 1, fc.f) != 1) return fail(FGFRFT_IO, std::string("failed writing ") + path);
-    if (std::fclose(fc.f) != 0) {
-        fc.f = nullptr;
-        return fail(FGFRFT_IO, std::string("failed writing ") + path);
-    }
-    fc.f = nullptr;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_cache_load(const char* path, uint64_t memory_budget, int device, fgfrft_cache** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (!path) return fail(FGFRFT_PARAMETER, "null path");
-    FileCloser fc;
-    fc.f = std::fopen(path, "rb");
-    if (!fc.f) return fail(FGFRFT_IO, std::string("cannot open ") + path);
-    CacheFileHeader h{};
-    if (std::fread(&h, sizeof h, 1, fc.f) != 1) return fail(FGFRFT_PARSE, std::string(path) + ": truncated header");
-    if (std::memcmp(h.magic, kCacheMagic, 8) != 0) return fail(FGFRFT_PARSE, std::string(path) + ": not a power-cache file");
-    if (h.header_fnv != host_fnv1a64(&h, offsetof(CacheFileHeader, header_fnv)))
-        return fail(FGFRFT_PARSE, std::string(path) + ": corrupt header");
-    if (h.version != 1 || h.tile != kTile)
-        return fail(FGFRFT_PARSE, std::string(path) + ": unsupported cache file version or layout");
-    if (h.n < 1 || h.l < 1 || h.f_bytes != (uint64_t)h.n * h.n * 16)
-        return fail(FGFRFT_PARSE, std::string(path) + ": inconsistent header");
-    const size_t ml = (size_t)h.n * (size_t)h.n;
-    std::vector<double> f(2 * ml);
-    if (std::fread(f.data(), 16, ml, fc.f) != ml) return fail(FGFRFT_PARSE, std::string(path) + ": truncated matrix");
-    fgfrft_cache* c = nullptr;
-    if (int st = create_common(f.data(), h.n, h.l, memory_budget, (int)h.dtype, device, out, &c)) return st;
-    DeviceGuard dg(device);
-    int rc = FGFRFT_OK;
-    do {
-        if (c->dtype == FGFRFT_C64) c->fingerprint = h.fingerprint;  // F stored rounded to complex64
-        if (c->fingerprint != h.fingerprint) {
-            rc = fail(FGFRFT_NUMERICAL, std::string(path) + ": fingerprint mismatch, the stored matrix is corrupt");
-            break;
-        }
-        if ((c->real ? 1u : 0u) != h.real || c->elem != h.elem || c->slab_bytes() != h.slab_bytes) {
-            rc = fail(FGFRFT_PARSE, std::string(path) + ": slab storage differs from this build (real / element size)");
-            break;
-        }
-        // slabs: file -> staging buffer b while the other buffer's H2D copy runs
-        PinnedPair pp;
-        if (pp.init() != cudaSuccess) {
-            rc = fail(FGFRFT_CAPACITY, "cache load: pinned staging allocation failed");
-            break;
-        }
-        const size_t total = c->slab_bytes() * (size_t)c->l;
-        char* dst = static_cast<char*>(c->slabs);
-        for (size_t off = 0, i = 0; off < total && rc == FGFRFT_OK; off += kStageBytes, ++i) {
-            const int b = (int)(i & 1);
-            const size_t sz = std::min(kStageBytes, total - off);
-            if (i >= 2 && cudaEventSynchronize(pp.e[b]) != cudaSuccess) rc = fail(FGFRFT_CUDA, "cache load: copy failed");
-            else if (std::fread(pp.p[b], 1, sz, fc.f) != sz) rc = fail(FGFRFT_PARSE, std::string(path) + ": truncated slabs");
-            else if (cudaMemcpyAsync(dst + off, pp.p[b], sz, cudaMemcpyHostToDevice, c->stream) ||
-                     cudaEventRecord(pp.e[b], c->stream))
-                rc = fail(FGFRFT_CUDA, "cache load: copy failed");
-        }
-        if (rc != FGFRFT_OK) break;
-        uint64_t want = 0;
-        if (std::fread(&want, 8, 1, fc.f) != 1) {
-            rc = fail(FGFRFT_PARSE, std::string(path) + ": missing checksum");
-            break;
-        }
-        unsigned long long got = 0;
-        if ((rc = slab_checksum(c, &got)) != FGFRFT_OK) break;
-        if (got != want) {
-            rc = fail(FGFRFT_NUMERICAL, std::string(path) + ": slab checksum mismatch, the stored powers are corrupt");
-            break;
-        }
-        if (c->real) {  // the orthogonality flag of the build (power-product / Gram routes)
-            DevBuf t;
-            if (t.ensure(ml * 16 + ml * 8) != cudaSuccess) {
-                rc = fail(FGFRFT_CAPACITY, "cache load: scratch allocation failed");
-                break;
-            }
-            double* fr = reinterpret_cast<double*>(t.as<double2>() + ml);
-            if (cudaMemcpyAsync(t.p, f.data(), ml * 16, cudaMemcpyHostToDevice, c->stream) ||
-                launch_real_part(t.p, fr, (int64_t)ml, c->stream))
-                rc = fail(FGFRFT_CUDA, "cache load: upload failed");
-            else
-                rc = check_orthogonal(c, fr, reinterpret_cast<double*>(t.p));
-            cudaStreamSynchronize(c->stream);
-            t.release();
-        }
-    } while (false);
-    if (rc != FGFRFT_OK) {
-        destroy_cache(c);
-        return rc;
-    }
-    *out = c;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-}  // extern "C"
-
-// ------------------------------------------------------------------ exact denoise backend
-//
-// learn.hpp:205-289 (ExactDenoiseEngine) on the device spectrum: per evaluation six DMMA ZGEMMs
-// with V / V^H (u, b, w, V^H r, F^a r, q) around diagonal scalings (denoise.cu dnx_*), the loss
-// and both gradients reduced in a fixed order; the Adam loop / tracking is the fast backend's.
-
-namespace {
-
-cudaStream_t dn_stream(const fgfrft_denoise* d) { return d->exact ? d->spec->stream : d->cache->stream; }
-std::mutex& dn_mutex(fgfrft_denoise* d) { return d->exact ? d->spec->mu : d->cache->mu; }
-int dn_device(const fgfrft_denoise* d) { return d->exact ? d->spec->device : d->cache->device; }
-
-int denoise_exact_eval(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch) {
-    fgfrft_spectrum* s = d->spec;
-    cudaStream_t st = s->stream;
-    const int n = (int)d->n, ch = (int)d->ch;
-    const int64_t cnt = (int64_t)n * ch;
-    const double* h = params + 1;
-    double2* ph = d->xph.as<double2>();
-    double2* jtp = ph + n;
-    double2* jtc = ph + 2 * n;
-    auto zg = [&](bool adj, const void* b, void* c) -> int {  // c = V b or V^H b
-        return zgemm_auto(adj ? 2 : 0, 0, n, ch, n, s->v.p, n, 0, b, n, 0, c, n, 0, 1, st);
-    };
-    FGB_LAUNCH(launch_dnx_phase(params, s->theta.as<double>(), n, ph, jtp, jtc, st), 1);
-    FGB_LAUNCH(launch_dnx_rowscale(d->xytil.p, ph, nullptr, false, n, cnt, d->xt.p, st), 1);
-    if (int e = zg(false, d->xt.p, d->xu.p)) return e;                          // u = V (phase o ytil)
-    FGB_LAUNCH(launch_dnx_rowscale(d->xu.p, nullptr, h, false, n, cnt, d->xt.p, st), 1);
-    if (int e = zg(true, d->xt.p, d->xb.p)) return e;                           // b = V^H (h o u)
-    FGB_LAUNCH(launch_dnx_rowscale(d->xb.p, ph, nullptr, true, n, cnt, d->xt.p, st), 1);
-    if (int e = zg(false, d->xt.p, d->xw.p)) return e;                          // w = V (conj(phase) o b)
-    double* part = d->part.as<double>();
-    FGB_LAUNCH(launch_dnx_cot(d->xw.p, d->x.as<double>(), cnt, d->loss_on_real, d->xcot.p, part, st), 1);
-    if (int e = zg(true, d->xcot.p, d->xvhr.p)) return e;                       // V^H r
-    FGB_LAUNCH(launch_dnx_rowscale(d->xvhr.p, ph, nullptr, false, n, cnt, d->xt.p, st), 1);
-    if (int e = zg(false, d->xt.p, d->xfar.p)) return e;                        // F^a r
-    FGB_LAUNCH(launch_dnx_rowscale(d->xytil.p, jtp, nullptr, false, n, cnt, d->xt.p, st), 1);
-    if (int e = zg(false, d->xt.p, d->xq.p)) return e;                          // q = V (j theta phase o ytil)
-    FGB_LAUNCH(launch_dnx_grad(d->xfar.p, d->xu.p, d->xvhr.p, d->xb.p, jtc, d->xq.p, h, n, ch, grad + 1, part, st),
-               1);
-    FGB_LAUNCH(launch_dn_finish(part, loss, grad, n, d->flag.as<int>(), epoch, st), 1);
-    return FGFRFT_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int fgfrft_denoise_create_exact(fgfrft_spectrum* spec, const double* y, const double* x_ref, int64_t channels,
-                                int loss_on_real, fgfrft_denoise** out) {
-    FGB_GUARD_BEGIN
-    if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
-    *out = nullptr;
-    if (int st = check_spectrum(spec)) return st;
-    if (channels < 1) return fail(FGFRFT_SHAPE, "denoise: need at least one channel");
-    if (!y || !x_ref) return fail(FGFRFT_PARAMETER, "null signal buffer");
-    std::lock_guard<std::mutex> lk(spec->mu);
-    DeviceGuard dg(spec->device);
-    auto* d = new fgfrft_denoise();
-    d->spec = spec;
-    d->exact = true;
-    d->loss_on_real = loss_on_real != 0;
-    d->n = spec->n;
-    d->ch = channels;
-    const int64_t cnt = d->n * channels;
-    d->cpad = cnt;
-    const size_t cb = (size_t)cnt * 16, np = (size_t)d->n + 1;
-    cudaStream_t st = spec->stream;
-    int rc = FGFRFT_OK;
-    if (d->y.ensure(cnt * 8) || d->x.ensure(cnt * 8) || d->xytil.ensure(cb) || d->xu.ensure(cb) || d->xb.ensure(cb) ||
-        d->xw.ensure(cb) || d->xcot.ensure(cb) || d->xvhr.ensure(cb) || d->xfar.ensure(cb) || d->xq.ensure(cb) ||
-        d->xt.ensure(cb) || d->xph.ensure((size_t)3 * d->n * 16) || d->params.ensure(np * 8) ||
-        d->grad.ensure(np * 8) || d->adam.ensure(2 * np * 8) || d->part.ensure(dn_part_elems() * 8) ||
-        d->scal.ensure(8 * 8) || d->best.ensure((np + 1) * 8) || d->flag.ensure(4 * sizeof(int)))
-        rc = fail(FGFRFT_CAPACITY, "denoise: device allocation failed");
-    if (rc == FGFRFT_OK && (cudaMemcpyAsync(d->y.p, y, (size_t)cnt * 8, cudaMemcpyHostToDevice, st) ||
-                            cudaMemcpyAsync(d->x.p, x_ref, (size_t)cnt * 8, cudaMemcpyHostToDevice, st)))
-        rc = fail(FGFRFT_CUDA, "denoise: upload failed");
-    if (rc == FGFRFT_OK) {  // ytil = V^H y (learn.hpp:210), y promoted to complex
-        if (launch_real_to_cplx(d->y.as<double>(), cnt, d->xt.p, st) ||
-            launch_zgemm((int)d->n, (int)channels, (int)d->n, spec->v.p, d->n, 0, true, d->xt.p, d->n, 0, false,
-                         d->xytil.p, d->n, 0, 1, false, st) ||
-            cudaStreamSynchronize(st))
-            rc = fail(FGFRFT_CUDA, "denoise: setup failed");
-        g_launches += 2;
-    }
-    if (rc != FGFRFT_OK) {
-        fgfrft_denoise_destroy(d);
-        return rc;
-    }
-    *out = d;
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-int fgfrft_denoise_reconstruct(fgfrft_denoise* d, double alpha, const double* h, double* out) {
-    FGB_GUARD_BEGIN
-    if (int st = check_denoise(d)) return st;
-    if (!h || !out) return fail(FGFRFT_PARAMETER, "null buffer");
-    std::lock_guard<std::mutex> lk(dn_mutex(d));
-    DeviceGuard dg(dn_device(d));
-    cudaStream_t st = dn_stream(d);
-    double* params = d->params.as<double>();
-    FGB_CUDA(cudaMemcpyAsync(params, &alpha, 8, cudaMemcpyHostToDevice, st));
-    FGB_CUDA(cudaMemcpyAsync(params + 1, h, (size_t)d->n * 8, cudaMemcpyHostToDevice, st));
-    if (int e = denoise_eval_device(d, params, d->scal.as<double>(), d->grad.as<double>())) return e;
-    const void* src = d->ww.p;
-    if (d->exact) {  // Re w (learn.hpp:232-234)
-        FGB_LAUNCH(launch_real_part(d->xw.p, d->xt.p, d->n * d->ch, st), 1);
-        src = d->xt.p;
-    }
-    FGB_CUDA(cudaMemcpyAsync(out, src, (size_t)d->n * d->ch * 8, cudaMemcpyDeviceToHost, st));
-    FGB_CUDA(cudaStreamSynchronize(st));
-    return FGFRFT_OK;
-    FGB_GUARD_END
-}
-
-}  // extern "C"

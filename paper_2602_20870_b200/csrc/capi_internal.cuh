@@ -1,0 +1,395 @@
+// capi_internal.cuh -- shared internals of the C ABI translation units (capi*.cu): kernel
+// launcher declarations, error / profiling plumbing, the handle structs and the internal helpers
+// one unit calls in another. Not part of the public boundary (include/fgfrft_b200.h is).
+#pragma once
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <complex>
+#include <dlfcn.h>
+#include <numeric>
+#include <limits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <cusolverDn.h>
+
+#include "common.cuh"
+#include "fgfrft_b200.h"
+#include "oz.cuh"
+
+namespace fgb {
+double host_sinc(double);
+double host_sinc_deriv(double);
+void host_sinc_coeffs(double alpha, int l, double* c, double* dc);
+uint64_t host_fnv1a64(const void* data, size_t nbytes);
+template <typename R>
+cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                         cudaStream_t stream);
+cudaError_t launch_synth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                               cudaStream_t stream);
+int synth_sweep_max_orders();
+cudaError_t launch_rect_to_tiled(const void* src, int64_t ld, int m, int ncols, void* dst, cudaStream_t stream,
+                                 bool real);
+cudaError_t launch_synth_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l_used,
+                              const double* coef_dev, int n_alpha, void* out, cudaStream_t stream, bool real,
+                              bool out_complex);
+cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, int rows, int l, const void* m,
+                             int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream,
+                             bool real);
+size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
+cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream);
+cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream);
+cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
+                                 const void* x, int ch, void* y, cudaStream_t stream);
+cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
+                              const void* gcot, const void* x, int ch, double* dlda, cudaStream_t stream);
+int batch_max_heads();
+int batch_max_channels();
+int batch_max_n();
+cudaError_t launch_rgemm(int am, int bm, int cm, int M, int N, int K, const void* A, int64_t lda, int64_t sA,
+                         const void* B, int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int batch,
+                         cudaStream_t stream);
+cudaError_t launch_rto_tiled(const void* src, void* dst, int n, cudaStream_t stream);
+cudaError_t launch_rfrom_tiled(const void* src, void* dst, int n, cudaStream_t stream);
+cudaError_t launch_rfrom_tiled_real(const void* src, void* dst, int n, cudaStream_t stream);
+size_t rapply_fused_part_elems(int n, int n_alpha);
+int rapply_fused_max_cols();
+cudaError_t launch_rapply_fused(const void* slabs, int n, int l_used, const double* coef_dev, int coef_ld, int n_alpha,
+                                const double* x, int b, double* part, double* y, cudaStream_t stream);
+cudaError_t launch_real_part(const void* src, void* dst, int64_t count, cudaStream_t stream);
+cudaError_t launch_rsynth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                          bool out_complex, cudaStream_t stream);
+cudaError_t launch_rsynth_sweep(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
+                                bool out_complex, cudaStream_t stream);
+int rsweep_max_orders();
+cudaError_t launch_rdots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha, double* partial,
+                         double* s_out, cudaStream_t stream);
+cudaError_t launch_rdots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                             double* partial, double* s_out, cudaStream_t stream, int* launches);
+size_t rdots_mma_partial_elems(int n);
+cudaError_t launch_zgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
+                         int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
+                         bool accumulate, cudaStream_t stream);
+cudaError_t launch_power_dots(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                              double* partial, double* s_out, cudaStream_t stream, int elem_bytes);
+cudaError_t launch_cgemm(int M, int N, int K, const void* A, int64_t lda, int64_t sA, bool conj_a, const void* B,
+                         int64_t ldb, int64_t sB, bool conj_b, void* C, int64_t ldc, int64_t sC, int batch,
+                         bool accumulate, cudaStream_t stream);
+cudaError_t launch_promote(const void* src, void* dst, int64_t count, cudaStream_t stream);
+// spectral.cu (exact GFRFT, eigendecomposition pieces, cascade reductions)
+size_t sp_part_elems();
+cudaError_t launch_herm_parts(const void* f, int n, bool real, void* a, void* bh, cudaStream_t st);
+cudaError_t launch_real_to_cplx(const double* src, int64_t count, void* dst, cudaStream_t st);
+cudaError_t launch_blockdiag(const void* in, int n, const int* colinfo, const void* u, void* out, cudaStream_t st);
+cudaError_t launch_col_pair_dot(const void* w, const void* t, int n, const int* pairs, int count, void* out,
+                                cudaStream_t st);
+cudaError_t launch_gather_cols(const void* src, int n, const int* perm, void* dst, cudaStream_t st);
+cudaError_t launch_eig_residual(const void* fw, const void* w, const double* theta, const void* f, int n,
+                                double* part, double* out2, cudaStream_t st);
+cudaError_t launch_spec_scale(const void* v, const double* theta, const double* alphas, int na, int which, int n,
+                              void* w, cudaStream_t st);
+cudaError_t launch_cdiff_sq(const void* y, bool real_y, const void* t, int64_t count, void* b, double* part,
+                            cudaStream_t st);
+cudaError_t launch_cre_dot(const void* m, const void* d, bool real_d, int64_t count, double* part, cudaStream_t st);
+cudaError_t launch_sum_parts(const double* part, int groups, double s0, double s1, double* out, cudaStream_t st);
+cudaError_t launch_rdot(const double* a, const double* b, int64_t count, double* part, cudaStream_t st);
+// store.cu
+cudaError_t launch_checksum(const void* data, size_t bytes, unsigned long long* out, cudaStream_t st);
+// shard.cu (fused row gather, DMMA path)
+cudaError_t launch_rows_push(const void* src, int64_t n, int r0, int rows, int64_t cols, void* const* dst_dev,
+                             int ndst, cudaStream_t stream);
+size_t dots_partial_elems(int n, int l, int n_alpha);
+size_t dots_mma_partial_elems(int n);
+int dots_mma_max_orders();
+cudaError_t launch_power_dots_mma(const void* slabs, int n, int l, const void* m, int64_t m_stride, int n_alpha,
+                                  double* partial, double* s_out, cudaStream_t stream, int* launches);
+cudaError_t launch_mse_residual(const void* y, const void* xc, int64_t count, int n_alpha, double g_scale,
+                                double loss_scale, void* g, double* partial, double* loss_out, cudaStream_t stream,
+                                int elem_bytes);
+size_t mse_partial_elems(int n_alpha);
+cudaError_t launch_demote(const void* src, void* dst, int64_t count, cudaStream_t stream);
+cudaError_t launch_to_tiled(const void* src, void* dst, int n, int elem_bytes_dst, cudaStream_t stream);
+cudaError_t launch_from_tiled(const void* src, void* dst, int n, int elem_bytes_src, cudaStream_t stream);
+cudaError_t launch_coef_dot(const double* dc, const double* s, int n_alpha, int width, double* out,
+                            cudaStream_t stream);
+int combine_max_terms();
+cudaError_t launch_dn_coef(const double* params, int l, double* tab, cudaStream_t st);
+cudaError_t launch_dn_scale(const double* u, const double* h, double* v, int n, int64_t count, cudaStream_t st);
+cudaError_t launch_dn_residual(const double* w, const double* x, double* r, int64_t count, double* part,
+                               cudaStream_t st);
+cudaError_t launch_dn_grad(const double* u, const double* du, const double* h, const double* r, const double* dqhv,
+                           const double* qr, int n, int ch, double* grad, double* part, double* loss, int* flag,
+                           int epoch, cudaStream_t st);
+cudaError_t launch_dn_track(const double* loss, const double* params, int np, int epoch, double* traj, double* best,
+                            int* best_epoch, cudaStream_t st);
+cudaError_t launch_dnx_phase(const double* params, const double* theta, int n, void* phase, void* jtp, void* jtc,
+                             cudaStream_t st);
+cudaError_t launch_dnx_rowscale(const void* src, const void* d, const double* h, bool conj_d, int n, int64_t count,
+                                void* dst, cudaStream_t st);
+cudaError_t launch_dnx_cot(const void* w, const double* x, int64_t count, bool real_loss, void* cot, double* part,
+                           cudaStream_t st);
+cudaError_t launch_dnx_grad(const void* far, const void* u, const void* vhr, const void* b, const void* jtc,
+                            const void* q, const double* h, int n, int ch, double* grad_h, double* part,
+                            cudaStream_t st);
+cudaError_t launch_dn_finish(const double* part, double* loss, double* grad, int n, int* flag, int epoch,
+                             cudaStream_t st);
+cudaError_t launch_dn_adam(double* params, double* m, double* v, const double* grad, int np, int64_t step, double lr,
+                           cudaStream_t st);
+size_t dn_part_elems();
+cudaError_t launch_ortho_residual(const double* g, int n, double* out, cudaStream_t stream);
+cudaError_t launch_colstats(const double* x, const double* xc, int n, int b, double* colsq, double* colxc, int* ecol,
+                            double* rg, int l, cudaStream_t st);
+cudaError_t launch_gram_s_dlda(const double* coef, const double* dcoef, const double* rg, int n_alpha, int l,
+                               double norm, double* s, double* dlda, cudaStream_t st);
+cudaError_t launch_gram_terms(const double* part, int ctas, int tp2, int l, double* rg, cudaStream_t st);
+cudaError_t launch_loss3(const double* part, int ctas, int n_alpha, double norm, double* loss, cudaStream_t st);
+cudaError_t launch_gram_s(const double* coef, const double* rg, int n_alpha, int l, double norm, double* s,
+                          cudaStream_t st);
+size_t combine_partial_elems(int tp);
+cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
+                           const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
+                           double* loss, cudaStream_t stream);
+}  // namespace fgb
+
+using namespace fgb;
+
+namespace fgbi {
+
+extern thread_local std::string g_err;
+// Set by the host-buffer entry points around their call into a *_dev entry point: the device
+// buffers they pass are already in the internal (complex128) layout, no complex64 bridge.
+extern thread_local bool tl_internal_signals;
+struct InternalSignals {
+    bool prev;
+    InternalSignals() : prev(tl_internal_signals) { tl_internal_signals = true; }
+    ~InternalSignals() { tl_internal_signals = prev; }
+};
+extern std::atomic<uint64_t> g_launches;
+
+// Optional per-kernel-class timing with CUDA events recorded on the launching stream
+// (fgfrft_profile_*): bench.py uses it to time the dominant kernel inside its timed region.
+enum KernelClass {
+    KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_I8GEMM = 4, KC_SLICE = 5, KC_COMBINE = 6, KC_COUNT = 8
+};
+struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+};
+extern std::mutex g_prof_mu;
+extern bool g_prof_on;
+extern std::vector<ProfRec> g_prof;
+extern std::vector<cudaEvent_t> g_prof_pool;
+
+cudaEvent_t prof_event();
+
+struct ProfScope {
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(int c, cudaStream_t s) : cls(c), st(s) {
+        if (!g_prof_on) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        a = prof_event();
+        cudaEventRecord(a, st);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        cudaEvent_t b = prof_event();
+        cudaEventRecord(b, st);
+        g_prof.push_back({cls, a, b});
+    }
+};
+
+int fail(int code, const std::string& msg);
+
+#define FGB_CUDA(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess) {                                                                \
+            cudaGetLastError();                                                                 \
+            return fail(FGFRFT_CUDA, std::string(#expr) + " failed: " + cudaGetErrorString(e_)); \
+        }                                                                                       \
+    } while (0)
+
+#define FGB_LAUNCH(expr, nlaunch)  \
+    do {                           \
+        FGB_CUDA(expr);            \
+        g_launches += (nlaunch);   \
+    } while (0)
+
+#define FGB_GUARD_BEGIN try {
+#define FGB_GUARD_END                                                        \
+    }                                                                        \
+    catch (const std::bad_alloc&) {                                          \
+        return fail(FGFRFT_CAPACITY, "host allocation failed");              \
+    }                                                                        \
+    catch (const std::exception& ex) {                                       \
+        return fail(FGFRFT_NUMERICAL, ex.what());                            \
+    }                                                                        \
+    catch (...) {                                                            \
+        return fail(FGFRFT_NUMERICAL, "unknown exception");                  \
+    }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace fgbi
+
+using namespace fgbi;
+
+struct fgfrft_cache {
+    int64_t n = 0;
+    int l = 0;
+    int dtype = FGFRFT_C128;
+    bool real = false;  // F has an exactly zero imaginary part: real cache, real Q, real x complex GEMMs
+    // complex64 API over a real F: the powers are stored as real doubles (the same 8 bytes per
+    // element as complex64) and every kernel runs the real complex128 path; the *_dev entry points
+    // promote the caller's complex64 signals on entry and demote the results (dtype stays C128
+    // internally, fgfrft_cache_info reports C64).
+    bool api_c64 = false;
+    DevBuf bx, bxc, by;
+    size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
+    int device = 0;
+    uint64_t fingerprint = 0;
+    void* slabs = nullptr;
+    size_t elem = 16;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    // workspaces
+    DevBuf coef, q, m, partial, s, x, y, g, xc, lpart, loss, dlda, tmp;
+    // Power-product route (real F): the stacked cache [P_1..P_L; P_1^T..P_L^T] as INT8 Ozaki
+    // digit slices (built lazily, once), the per-call slices of X and the products Z = P X.
+    int engine = FGFRFT_ENGINE_AUTO;
+    // F^T F = I to rounding (unitarity residual of gft.hpp:39-44 <= 1e-12, checked on device at
+    // build): the power-product MSE step may then take s_k from the Gram sequence <X, F^d X>.
+    bool orthogonal = false;
+    double ortho_residual = -1.0;
+    int ps_slices = 0;
+    DevBuf ps, pe, prm, xsl, xex, z;
+    DevBuf qsl, qex;  // per-call INT8 slices of Q(a) (or G) for the synthesis route
+    // Orthogonal-F sweep with the combination on the INT8 tensor cores: the stacked cache sliced
+    // in (signal row, term) interleaved order, P_L in column-major form, and per-call buffers.
+    int ps3_slices = 0;
+    DevBuf ps3, pe3, plr, zd, zaux, cdig, cex;
+    // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
+    bool shard = false;
+    int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
+    int64_t r0 = 0, r1 = 0;
+    void* colp = nullptr;
+    size_t panel_elems = 0;
+    // Host-buffer MSE step: Xc is uploaded on a side stream while the power products run; the
+    // step waits on xc_evt right before its first use of Xc.
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t xc_evt = nullptr;
+    bool xc_pending = false;
+    double* coef_h = nullptr;  // pinned staging for the coefficient tables
+    size_t coef_h_cap = 0;
+    cudaEvent_t coef_evt = nullptr;
+
+    // Matrices at the API are n x n column-major; device slabs are tiled (common.cuh) and padded
+    // to npad = 32 * ceil(n / 32) per side.
+    size_t mat_elems() const { return (size_t)n * (size_t)n; }
+    size_t npad() const { return (size_t)ceil_div(n, kTile) * kTile; }
+    size_t slab_elems() const { return npad() * npad(); }
+    size_t slab_bytes() const { return slab_elems() * elem; }
+    void* slab(int k) const { return static_cast<char*>(slabs) + (size_t)(k - 1) * slab_bytes(); }
+};
+
+struct fgfrft_denoise {
+    fgfrft_cache* cache = nullptr;
+    int64_t n = 0, ch = 0, cpad = 0;
+    int l = 0;
+    DevBuf y, x, spow, tpow, gpow, uu, ww, qr, v, r, params, grad, adam, tab, part, scal, best, traj, flag;
+    // exact backend (learn.hpp:205-289): the spectrum and its n x ch complex blocks
+    fgfrft_spectrum* spec = nullptr;
+    bool exact = false, loss_on_real = false;
+    DevBuf xytil, xu, xb, xw, xcot, xvhr, xfar, xq, xt, xph;
+};
+
+struct fgfrft_spectrum {
+    int64_t n = 0;
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    DevBuf v, theta, alph, w;
+    std::vector<double> theta_h;
+};
+
+struct fgfrft_cascade {
+    fgfrft_cache* cache = nullptr;  // fast backend; nullptr: exact backend through the spectrum
+    fgfrft_spectrum* spec = nullptr;
+    int k = 0;
+    int64_t n = 0;
+    DevBuf target, ops, dops, prefix, b, nb, m, part, out;
+    cudaStream_t stream() const { return cache ? cache->stream : spec->stream; }
+};
+
+namespace fgbi {
+
+// helpers defined in one capi*.cu unit and used in another
+int ensure_power_slices(fgfrft_cache* c);
+int64_t pad_k(int64_t n);
+int64_t pad_rows(int64_t n);
+int zgemm_auto(int opa, int opb, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda, int64_t sa,
+               const void* b, int64_t ldb, int64_t sb, void* c, int64_t ldc, int64_t sc, int batch, cudaStream_t st);
+int check_handle(const fgfrft_cache* c);
+void destroy_cache(fgfrft_cache* c);
+int check_shard(const fgfrft_cache* c);
+int check_alphas(const double* alphas, int n_alpha);
+int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, double** dev);
+bool use_int8_gemm(const fgfrft_cache* c, int64_t b);
+int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
+                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers = nullptr,
+                int npeers = 0);
+int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
+                int64_t sm);
+int check_batch(const fgfrft_cache* c);
+int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out, bool internal = false);
+int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
+int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype, int device, fgfrft_cache** out,
+                  fgfrft_cache** made);
+int check_orthogonal(fgfrft_cache* c, const double* fr, double* scratch);
+int check_spectrum(const fgfrft_spectrum* s);
+
+}  // namespace fgbi
