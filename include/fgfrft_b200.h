@@ -292,16 +292,16 @@ int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
 
 /* ---- GPU-resident denoising learner (learn.hpp:291-516, adam.hpp) -------------------------
  *
- * The paper's denoising workload on the device for a real F (graph GFT): the signal-side powers
- * F^m y are built once; every evaluation applies Q(alpha) = sum c_m F^m through power products
- * (one INT8 tensor-core GEMM each for F^m (h o u) and F^m r) and combinations, exactly the
- * quantities of the reference's fast engine:
+ * The paper's denoising workload on the device for a real F (graph GFT): every evaluation
+ * synthesises Q(alpha) and dQ/dalpha from the cache in one pass (alpha lives on the device; its
+ * sinc coefficients are evaluated there, ~1 ulp from glibc) and forms, with five n x n x C GEMMs
+ * (INT8 engine or DMMA), the quantities of the reference's fast engine:
  *   u = Q y, w = Q^H (h o u), loss = |w - x|^2, grad_h = 2 rowsum(Q r o u),
  *   grad_alpha = 2 <r, dQ^H/dalpha (h o u)> + 2 <Q r, h o dQ/dalpha y>,  r = w - x.
  * y, x_ref, reconstruction: n x channels real, column-major (host). fit runs Adam (lr, beta
  * 0.9 / 0.999, eps 1e-8) over [alpha, h] from [init_alpha, 1..1] for `epochs` steps, evaluating
  * once more at the end (trajectories have epochs + 1 entries) and tracking the best loss, all on
- * the device. Coefficients of the device-resident alpha come from device sin / cos (~1 ulp).
+ * the device; a non-finite loss / gradient inside the loop -> FGFRFT_OPTIMIZER naming the epoch.
  */
 typedef struct fgfrft_denoise fgfrft_denoise;
 int fgfrft_denoise_create(fgfrft_cache* cache, const double* y, const double* x_ref, int64_t channels,

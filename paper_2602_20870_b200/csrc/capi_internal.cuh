@@ -339,7 +339,7 @@ struct fgfrft_denoise {
     fgfrft_cache* cache = nullptr;
     int64_t n = 0, ch = 0, cpad = 0;
     int l = 0;
-    DevBuf y, x, spow, tpow, gpow, uu, ww, qr, v, r, params, grad, adam, tab, part, scal, best, traj, flag;
+    DevBuf y, x, qd, uu, ww, qr, v, r, params, grad, adam, tab, part, scal, best, traj, flag;  // qd = [Q | dQ]
     // exact backend (learn.hpp:205-289): the spectrum and its n x ch complex blocks
     fgfrft_spectrum* spec = nullptr;
     bool exact = false, loss_on_real = false;

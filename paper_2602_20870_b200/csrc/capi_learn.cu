@@ -1,12 +1,12 @@
-// capi_learn.cu -- the GPU-resident denoising learner: fast (power products) and exact (device
-// spectrum) backends, Adam on the device (fgfrft_denoise_*).
+// capi_learn.cu -- the GPU-resident denoising learner: fast (synthesised Q, dQ from the power
+// cache) and exact (device spectrum) backends, Adam on the device (fgfrft_denoise_*).
 #include "capi_internal.cuh"
 
 // ------------------------------------------------------------------ GPU-resident denoising learner
 //
 // learn.hpp:291-413 (FastDenoiseEngine, real F) and learn.hpp:471-516 (denoise + Adam, adam.hpp)
-// on the device. Kernels: denoise.cu (pieces), ozgemm.cu (F^m V for all m in one INT8 GEMM),
-// combine.cu (sum_m c_m Z_m for a few coefficient rows).
+// on the device. Kernels: denoise.cu (pieces), the pair synthesis (Q and dQ/dalpha from the
+// cache), the INT8 / DMMA real GEMMs.
 
 
 namespace fgbi {
@@ -17,66 +17,49 @@ std::mutex& dn_mutex(fgfrft_denoise* d);
 int dn_device(const fgfrft_denoise* d);
 int denoise_exact_eval(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch);
 
-// out[m-block] = F^(+-m) V for a real n x ch block V (column-major): one INT8 GEMM over the stacked
-// cache slices; out blocks of stride `stride` doubles in the power-product order.
-int power_products_real(fgfrft_cache* c, const double* src, int64_t ch, double* out, int64_t stride) {
-    if (int st = ensure_power_slices(c)) return st;
-    const int S = c->ps_slices;
-    const int64_t n = c->n, np = pad_rows(n), kp = pad_k(n), rows = 2 * (int64_t)c->l * np;
-    const int64_t bp = ceil_div(ch, kOzTileB) * kOzTileB;
-    FGB_CUDA(c->xsl.ensure((size_t)S * bp * kp));
-    FGB_CUDA(c->xex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
-    int* xe = c->xex.as<int>();
-    {
-        const OzView v{src, n, 1, 0, 0, 0, (int)ch, (int)bp, 1, (int)n, (int)kp, false};
-        ProfScope ps(KC_SLICE, c->stream);
-        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->xsl.as<int8_t>(), xe,
-                                   reinterpret_cast<unsigned long long*>(xe + bp), c->stream),
-                   3);
-    }
-    ProfScope ps(KC_I8GEMM, c->stream);
-    FGB_LAUNCH(launch_ozgemm(S, 0, c->ps.as<int8_t>(), c->pe.as<int>(), (int)rows, c->xsl.as<int8_t>(), xe, (int)bp,
-                             (int)kp, out, n, stride, (int)n, (int)np, (int)ch, c->stream),
+// C (n x ch) = op(A) B for real n x n A (op: A or A^T) and real n x ch B, column-major: the INT8
+// engine where the cache's engine selects it, else a real DMMA GEMM.
+int dn_gemm(fgfrft_cache* c, bool trans, const double* a, const double* b, double* out, int64_t ch) {
+    const int64_t n = c->n;
+    if (use_int8_gemm(c, (ch + 1) / 2))
+        return fgfrft_dgemm_int8_dev(trans ? 1 : 0, 0, n, ch, n, a, n, b, n, out, n, 0, c->stream);
+    ProfScope ps(KC_GEMM, c->stream);
+    FGB_LAUNCH(launch_rgemm(trans ? 1 : 0, 0, 0, (int)n, (int)ch, (int)n, a, n, 0, b, n, 0, out, n, 0, 1, c->stream),
                1);
     return FGFRFT_OK;
 }
 
 // One evaluation at the device-resident params = [alpha, h_1..h_n]: loss, grad = [d/dalpha, d/dh].
+// The reference's matrix-free engine (learn.hpp:291-413) applies Q = sum_m c_m F^m through 4L
+// products with F per evaluation; here Q and dQ/dalpha are synthesised together from the device
+// cache (one pass, the pair kernel's 2-order form: exact, P_-m = P_m^T) and every "sum_m c_m F^m
+// applied to a block" becomes one GEMM:
+//   u = Q y, du = dQ y, v = h o u, w = Q^T v (= sum c_-m F^m v), dqh_v = dQ^T v, r = w - x,
+//   qr = Q r, grad_h = 2 rowsum(qr o u), grad_alpha = 2 <r, dqh_v> + 2 <qr, h o du>.
 int denoise_eval_device(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch = -1) {
     if (d->exact) return denoise_exact_eval(d, params, loss, grad, epoch);
     fgfrft_cache* c = d->cache;
-    const int l = d->l, T = 2 * l + 1;
-    const int64_t cnt = d->n * d->ch, cp = d->cpad;
+    const int l = d->l;
+    const int64_t cnt = d->n * d->ch, cp = d->cpad, ch = d->ch;
+    const size_t nn = (size_t)d->n * d->n;
     double* tab = d->tab.as<double>();
     const double* h = params + 1;
-    FGB_CUDA(c->partial.ensure(combine_partial_elems(combine_max_terms()) * sizeof(double)));
-    FGB_LAUNCH(launch_dn_coef(params, l, tab, c->stream), 1);
-    {
-        ProfScope ps(KC_COMBINE, c->stream);  // u = sum c_m spow_m, du = sum c'_m spow_m
-        FGB_LAUNCH(launch_combine(1, d->spow.as<double>(), d->y.as<double>(), nullptr, cp, l, tab, 2, 0.0,
-                                  d->uu.as<double>(), nullptr, nullptr, nullptr, c->stream),
-                   1);
-    }
-    FGB_LAUNCH(launch_dn_scale(d->uu.as<double>(), h, d->v.as<double>(), (int)d->n, cnt, c->stream), 1);
-    if (int st = power_products_real(c, d->v.as<double>(), d->ch, d->tpow.as<double>(), cp)) return st;
-    {
-        ProfScope ps(KC_COMBINE, c->stream);  // w = Q^H v = sum c_-m tpow_m, dqh_v = sum c'_-m tpow_m
-        FGB_LAUNCH(launch_combine(1, d->tpow.as<double>(), d->v.as<double>(), nullptr, cp, l, tab + 2 * T, 2, 0.0,
-                                  d->ww.as<double>(), nullptr, nullptr, nullptr, c->stream),
-                   1);
-    }
+    double* q = d->qd.as<double>();
+    double* dq = q + nn;
+    double* uu = d->uu.as<double>();
+    double* ww = d->ww.as<double>();
+    FGB_LAUNCH(launch_dn_coef(params, l, tab, c->stream), 1);  // rows c(alpha), c'(alpha)
+    if (int st = synth_into(c, tab, 2, l, q, true)) return st;
+    if (int st = dn_gemm(c, false, q, d->y.as<double>(), uu, ch)) return st;        // u
+    if (int st = dn_gemm(c, false, dq, d->y.as<double>(), uu + cp, ch)) return st;  // du
+    FGB_LAUNCH(launch_dn_scale(uu, h, d->v.as<double>(), (int)d->n, cnt, c->stream), 1);
+    if (int st = dn_gemm(c, true, q, d->v.as<double>(), ww, ch)) return st;         // w = Q^T v
+    if (int st = dn_gemm(c, true, dq, d->v.as<double>(), ww + cp, ch)) return st;   // dQ^T v
     double* part = d->part.as<double>();
-    FGB_LAUNCH(launch_dn_residual(d->ww.as<double>(), d->x.as<double>(), d->r.as<double>(), cnt, part, c->stream), 1);
-    if (int st = power_products_real(c, d->r.as<double>(), d->ch, d->gpow.as<double>(), cp)) return st;
-    {
-        ProfScope ps(KC_COMBINE, c->stream);  // qr = Q r = sum c_m gpow_m
-        FGB_LAUNCH(launch_combine(1, d->gpow.as<double>(), d->r.as<double>(), nullptr, cp, l, tab, 1, 0.0,
-                                  d->qr.as<double>(), nullptr, nullptr, nullptr, c->stream),
-                   1);
-    }
-    FGB_LAUNCH(launch_dn_grad(d->uu.as<double>(), d->uu.as<double>() + cp, h, d->r.as<double>(),
-                              d->ww.as<double>() + cp, d->qr.as<double>(), (int)d->n, (int)d->ch, grad, part, loss,
-                              d->flag.as<int>(), epoch, c->stream),
+    FGB_LAUNCH(launch_dn_residual(ww, d->x.as<double>(), d->r.as<double>(), cnt, part, c->stream), 1);
+    if (int st = dn_gemm(c, false, q, d->r.as<double>(), d->qr.as<double>(), ch)) return st;  // qr = Q r
+    FGB_LAUNCH(launch_dn_grad(uu, uu + cp, h, d->r.as<double>(), ww + cp, d->qr.as<double>(), (int)d->n, (int)d->ch,
+                              grad, part, loss, d->flag.as<int>(), epoch, c->stream),
                2);
     return FGFRFT_OK;
 }
@@ -98,7 +81,6 @@ int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref,
     if (int st = check_handle(c)) return st;
     if (!c->real || c->dtype != FGFRFT_C128)
         return fail(FGFRFT_PARAMETER, "denoise on the device needs a real F (graph GFT) in a complex128 cache");
-    if (2 * c->l + 1 > combine_max_terms()) return fail(FGFRFT_PARAMETER, "denoise on the device supports L <= 64");
     if (channels < 1) return fail(FGFRFT_SHAPE, "denoise: need at least one channel");
     if (!y || !x_ref) return fail(FGFRFT_PARAMETER, "null signal buffer");
     std::lock_guard<std::mutex> lk(c->mu);
@@ -112,8 +94,8 @@ int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref,
     d->cpad = cnt + (cnt & 1);  // even: 16-byte aligned blocks for the combine kernel
     const size_t blk = (size_t)d->cpad * 8, T = 2 * (size_t)d->l + 1, np = (size_t)d->n + 1;
     int rc = FGFRFT_OK;
-    if (d->y.ensure(blk) || d->x.ensure(blk) || d->spow.ensure(2 * d->l * blk) || d->tpow.ensure(2 * d->l * blk) ||
-        d->gpow.ensure(2 * d->l * blk) || d->uu.ensure(2 * blk) || d->ww.ensure(2 * blk) || d->qr.ensure(blk) ||
+    if (d->y.ensure(blk) || d->x.ensure(blk) || d->qd.ensure(2 * (size_t)d->n * d->n * 8) || d->uu.ensure(2 * blk) ||
+        d->ww.ensure(2 * blk) || d->qr.ensure(blk) ||
         d->v.ensure(blk) || d->r.ensure(blk) || d->params.ensure(np * 8) || d->grad.ensure(np * 8) ||
         d->adam.ensure(2 * np * 8) || d->tab.ensure(4 * T * 8) || d->part.ensure(dn_part_elems() * 8) ||
         d->scal.ensure(8 * 8) || d->best.ensure((np + 1) * 8) || d->flag.ensure(4 * sizeof(int)))
@@ -125,12 +107,10 @@ int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref,
             cudaMemcpyAsync(d->x.p, x_ref, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream))
             rc = fail(FGFRFT_CUDA, "denoise: upload failed");
     }
-    // spow_m = F^m y, m = +-1..+-L: fixed per problem (learn.hpp:300-305)
-    if (rc == FGFRFT_OK) rc = power_products_real(c, d->y.as<double>(), channels, d->spow.as<double>(), d->cpad);
     if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
         rc = fail(FGFRFT_CUDA, "denoise: setup failed");
     if (rc != FGFRFT_OK) {
-        for (DevBuf* b : {&d->y, &d->x, &d->spow, &d->tpow, &d->gpow, &d->uu, &d->ww, &d->qr, &d->v, &d->r,
+        for (DevBuf* b : {&d->y, &d->x, &d->qd, &d->uu, &d->ww, &d->qr, &d->v, &d->r,
                           &d->params, &d->grad, &d->adam, &d->tab, &d->part, &d->scal, &d->best, &d->traj, &d->flag})
             b->release();
         delete d;
@@ -147,7 +127,7 @@ int fgfrft_denoise_destroy(fgfrft_denoise* d) {
         DeviceGuard dg(dn_device(d));
         cudaStreamSynchronize(dn_stream(d));
     }
-    for (DevBuf* b : {&d->y, &d->x, &d->spow, &d->tpow, &d->gpow, &d->uu, &d->ww, &d->qr, &d->v, &d->r, &d->params,
+    for (DevBuf* b : {&d->y, &d->x, &d->qd, &d->uu, &d->ww, &d->qr, &d->v, &d->r, &d->params,
                       &d->grad, &d->adam, &d->tab, &d->part, &d->scal, &d->best, &d->traj, &d->flag, &d->xytil,
                       &d->xu, &d->xb, &d->xw, &d->xcot, &d->xvhr, &d->xfar, &d->xq, &d->xt, &d->xph})
         b->release();
