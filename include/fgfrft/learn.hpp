@@ -188,10 +188,9 @@ class DenoiseProblem {  // learn.hpp:439-467
             detail::throw_status(fgfrft_denoise_create_exact(spectrum->device_handle(device), y.data(), x_ref.data(),
                                                              ch_, cfg.loss_on_real ? 1 : 0, &h));
         } else {
-            if (!f.is_real())
-                throw parameter_error("denoise: the device fast backend needs a real F (use Backend::exact)");
             cache_.emplace(f, cfg.truncation, std::uint64_t(1) << 40, device);
-            detail::throw_status(fgfrft_denoise_create(cache_->handle(), y.data(), x_ref.data(), ch_, &h));
+            detail::throw_status(fgfrft_denoise_create_ex(cache_->handle(), y.data(), x_ref.data(), ch_,
+                                                          cfg.loss_on_real ? 1 : 0, &h));
         }
         h_.reset(h, [](fgfrft_denoise* p) { fgfrft_denoise_destroy(p); });
     }

@@ -292,7 +292,7 @@ int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
 
 /* ---- GPU-resident denoising learner (learn.hpp:291-516, adam.hpp) -------------------------
  *
- * The paper's denoising workload on the device for a real F (graph GFT): every evaluation
+ * The paper's denoising workload on the device (fast backend; real or complex F): every evaluation
  * synthesises Q(alpha) and dQ/dalpha from the cache in one pass (alpha lives on the device; its
  * sinc coefficients are evaluated there, ~1 ulp from glibc) and forms, with five n x n x C GEMMs
  * (INT8 engine or DMMA), the quantities of the reference's fast engine:
@@ -306,6 +306,11 @@ int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t 
 typedef struct fgfrft_denoise fgfrft_denoise;
 int fgfrft_denoise_create(fgfrft_cache* cache, const double* y, const double* x_ref, int64_t channels,
                           fgfrft_denoise** out);
+/* Same with the loss on the real part of the reconstruction (loss_on_real, learn.hpp:389-403;
+ * only differs from the plain form for a complex F). A complex F runs the same five products as
+ * complex GEMMs. */
+int fgfrft_denoise_create_ex(fgfrft_cache* cache, const double* y, const double* x_ref, int64_t channels,
+                             int loss_on_real, fgfrft_denoise** out);
 int fgfrft_denoise_destroy(fgfrft_denoise* problem);
 int fgfrft_denoise_eval(fgfrft_denoise* problem, double alpha, const double* h, double* loss,
                         double* grad_alpha, double* grad_h);

@@ -404,18 +404,25 @@ def power_dots_recursive(f: np.ndarray, l: int, g: np.ndarray, x: np.ndarray) ->
 # ------------------------------------------------------------------ denoising learner (real F)
 
 class FastDenoise:
-    """learn.hpp:291-413 FastDenoiseEngine<MatrixXd> (real F): matrix-free Q^alpha through
-    iterated products with F / F^T; the signal-side powers F^n y are precomputed (learn.hpp:300-305)."""
+    """learn.hpp:291-413 FastDenoiseEngine<MatrixXd> (real F) / <MatrixXcd> (complex F): matrix-free
+    Q^alpha through iterated products with F / F^H; the signal-side powers F^n y are precomputed
+    (learn.hpp:300-305). Complex F: loss on the complex residual, or on its real part with
+    loss_on_real (learn.hpp:389-403)."""
 
-    def __init__(self, y: np.ndarray, x: np.ndarray, f: np.ndarray, l: int):
-        self.y, self.x, self.f, self.l = np.asarray(y, float), np.asarray(x, float), np.asarray(f, float), int(l)
-        self.spow = self._powers(self.y)
+    def __init__(self, y: np.ndarray, x: np.ndarray, f: np.ndarray, l: int, loss_on_real: bool = False):
+        self.cplx = bool(np.iscomplexobj(f) and np.any(np.imag(f) != 0))
+        dt = np.complex128 if self.cplx else float
+        self.y, self.x = np.asarray(y, float), np.asarray(x, float)
+        self.f = np.asarray(f, dt) if self.cplx else np.asarray(np.real(f), float)
+        self.l, self.loss_on_real = int(l), bool(loss_on_real)
+        self.spow = self._powers(self.y.astype(dt))
 
     def _powers(self, v: np.ndarray) -> dict:
         p = {0: v}
+        fh = self.f.conj().T
         for m in range(1, self.l + 1):  # at(m) = F at(m-1), at(-m) = F^H at(-(m-1))
             p[m] = self.f @ p[m - 1]
-            p[-m] = self.f.T @ p[-(m - 1)]
+            p[-m] = fh @ p[-(m - 1)]
         return p
 
     def _run(self, c: np.ndarray, h: np.ndarray):
@@ -428,8 +435,11 @@ class FastDenoise:
         w = c[l] * tpow[0]
         for m in range(1, l + 1):  # Q^H v = sum_m c_{-m} F^m v
             w = w + (c[l - m] * tpow[m] + c[l + m] * tpow[-m])
+        if self.cplx and self.loss_on_real:
+            r = w.real - self.x
+            return u, tpow, w, r.astype(np.complex128), float(np.sum(r * r))
         cot = w - self.x
-        return u, tpow, w, cot, float(np.sum(cot * cot))
+        return u, tpow, w, cot, float(np.vdot(cot, cot).real)
 
     def eval(self, alpha: float, h: np.ndarray):
         """-> (loss, grad_alpha, grad_h), learn.hpp:306-338."""
@@ -440,19 +450,19 @@ class FastDenoise:
         qr = c[l] * gpow[0]
         for m in range(1, l + 1):
             qr = qr + (c[l + m] * gpow[m] + c[l - m] * gpow[-m])
-        grad_h = 2.0 * np.sum(qr * u, axis=1)
+        grad_h = 2.0 * np.sum((np.conj(qr) * u).real, axis=1)
         dqh_v = dc[l] * tpow[0]
         for m in range(1, l + 1):
             dqh_v = dqh_v + (dc[l - m] * tpow[m] + dc[l + m] * tpow[-m])
         du = dc[l] * self.spow[0]
         for m in range(1, l + 1):
             du = du + (dc[l + m] * self.spow[m] + dc[l - m] * self.spow[-m])
-        ga = 2.0 * float(np.sum(cot * dqh_v)) + 2.0 * float(np.sum(qr * (h[:, None] * du)))
+        ga = 2.0 * float(np.sum((np.conj(cot) * dqh_v).real)) + 2.0 * float(np.sum((np.conj(qr) * (h[:, None] * du)).real))
         return loss, ga, grad_h
 
     def reconstruct(self, alpha: float, h: np.ndarray) -> np.ndarray:
         c, _ = sinc_coeffs(alpha, self.l)
-        return self._run(c, h)[2]
+        return np.real(self._run(c, h)[2])
 
 
 class ExactDenoise:

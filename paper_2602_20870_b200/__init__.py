@@ -139,6 +139,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_shard_mse_dlda_partial_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp, vp]),
         "fgfrft_shard_apply_gather_dev": (i, [vp, vp, i, vp, i64, vp, vp, i]),
         "fgfrft_denoise_create_exact": (i, [vp, vp, vp, i64, i, pp]),
+        "fgfrft_denoise_create_ex": (i, [vp, vp, vp, i64, i, pp]),
         "fgfrft_zgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp]),
         "fgfrft_denoise_reconstruct": (i, [vp, d, vp, vp]),
         "fgfrft_ipc_get": (i, [vp, vp, vp]),
@@ -175,6 +176,7 @@ def exported_symbols():
         "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
         "fgfrft_shard_apply_gather_dev", "fgfrft_ipc_get", "fgfrft_ipc_open", "fgfrft_ipc_close",
         "fgfrft_denoise_create_exact", "fgfrft_denoise_reconstruct", "fgfrft_zgemm_int8_dev",
+        "fgfrft_denoise_create_ex",
     ]
 
 
@@ -538,7 +540,8 @@ def zgemm_int8(a, b, op_a: str = "N", op_b: str = "N"):
 class DenoiseProblem:
     """GPU-resident denoising learner (learn.hpp:168-516 on the device): y, x_ref are n x C real
     host arrays; eval(alpha, h) -> (loss, grad_alpha, grad_h); fit(...) runs Adam.
-    ``DenoiseProblem(cache, y, x)``: fast backend (real F, power products on the INT8 engine);
+    ``DenoiseProblem(cache, y, x, loss_on_real=False)``: fast backend (Q and dQ synthesised from the
+    cache, five GEMMs per evaluation; real or complex F);
     ``DenoiseProblem.exact(eig, y, x, loss_on_real)``: exact backend on a device spectrum."""
 
     def __init__(self, cache: Optional[PowerCache], y: np.ndarray, x_ref: np.ndarray,
@@ -552,8 +555,8 @@ class DenoiseProblem:
         self.cache, self.eig = cache, eig  # keep the handles alive
         self._h = ctypes.c_void_p()
         if cache is not None:
-            _check(lib().fgfrft_denoise_create(cache.handle, y.ctypes.data, x.ctypes.data, self.ch,
-                                               ctypes.byref(self._h)))
+            _check(lib().fgfrft_denoise_create_ex(cache.handle, y.ctypes.data, x.ctypes.data, self.ch,
+                                                  int(bool(loss_on_real)), ctypes.byref(self._h)))
         else:
             _check(lib().fgfrft_denoise_create_exact(eig.handle, y.ctypes.data, x.ctypes.data, self.ch,
                                                      int(bool(loss_on_real)), ctypes.byref(self._h)))

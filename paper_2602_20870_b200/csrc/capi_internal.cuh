@@ -343,6 +343,7 @@ struct fgfrft_denoise {
     // exact backend (learn.hpp:205-289): the spectrum and its n x ch complex blocks
     fgfrft_spectrum* spec = nullptr;
     bool exact = false, loss_on_real = false;
+    bool cplx = false;  // fast backend over a complex F: complex blocks in the x* buffers
     DevBuf xytil, xu, xb, xw, xcot, xvhr, xfar, xq, xt, xph;
 };
 

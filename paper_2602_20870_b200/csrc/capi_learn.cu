@@ -36,8 +36,42 @@ int dn_gemm(fgfrft_cache* c, bool trans, const double* a, const double* b, doubl
 // applied to a block" becomes one GEMM:
 //   u = Q y, du = dQ y, v = h o u, w = Q^T v (= sum c_-m F^m v), dqh_v = dQ^T v, r = w - x,
 //   qr = Q r, grad_h = 2 rowsum(qr o u), grad_alpha = 2 <r, dqh_v> + 2 <qr, h o du>.
+// Complex F (FastDenoiseEngine<MatrixXcd>): the same five products as complex GEMMs (INT8 engine
+// from n = 512, else DMMA), Q^H / dQ^H as conjugate-transposed operands; the scalings and
+// reductions are the exact backend's kernels (dnx_*; the "jtc" diagonal is all ones here).
+int denoise_fast_complex_eval(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch) {
+    fgfrft_cache* c = d->cache;
+    cudaStream_t st = c->stream;
+    const int n = (int)d->n, ch = (int)d->ch;
+    const int64_t cnt = (int64_t)n * ch;
+    const size_t nn = (size_t)n * n;
+    const double* h = params + 1;
+    double* tab = d->tab.as<double>();
+    double2* q = d->qd.as<double2>();
+    double2* dq = q + nn;
+    auto zg = [&](int opa, const void* a, const void* b, void* out) {
+        return zgemm_auto(opa, 0, n, ch, n, a, n, 0, b, n, 0, out, n, 0, 1, st);
+    };
+    FGB_LAUNCH(launch_dn_coef(params, d->l, tab, st), 1);
+    if (int e = synth_into(c, tab, 2, d->l, q, true)) return e;
+    if (int e = zg(0, q, d->xytil.p, d->xu.p)) return e;                  // u = Q y
+    if (int e = zg(0, dq, d->xytil.p, d->xb.p)) return e;                 // du = dQ y
+    FGB_LAUNCH(launch_dnx_rowscale(d->xu.p, nullptr, h, false, n, cnt, d->xq.p, st), 1);  // v = h o u
+    if (int e = zg(2, q, d->xq.p, d->xw.p)) return e;                     // w = Q^H v
+    if (int e = zg(2, dq, d->xq.p, d->xvhr.p)) return e;                  // dQ^H v
+    double* part = d->part.as<double>();
+    FGB_LAUNCH(launch_dnx_cot(d->xw.p, d->x.as<double>(), cnt, d->loss_on_real, d->xcot.p, part, st), 1);
+    if (int e = zg(0, q, d->xcot.p, d->xfar.p)) return e;                 // qr = Q r
+    FGB_LAUNCH(launch_dnx_grad(d->xfar.p, d->xu.p, d->xcot.p, d->xvhr.p, d->xph.p, d->xb.p, h, n, ch, grad + 1, part,
+                               st),
+               1);
+    FGB_LAUNCH(launch_dn_finish(part, loss, grad, n, d->flag.as<int>(), epoch, st), 1);
+    return FGFRFT_OK;
+}
+
 int denoise_eval_device(fgfrft_denoise* d, const double* params, double* loss, double* grad, int epoch = -1) {
     if (d->exact) return denoise_exact_eval(d, params, loss, grad, epoch);
+    if (d->cplx) return denoise_fast_complex_eval(d, params, loss, grad, epoch);
     fgfrft_cache* c = d->cache;
     const int l = d->l;
     const int64_t cnt = d->n * d->ch, cp = d->cpad, ch = d->ch;
@@ -75,12 +109,17 @@ extern "C" {
 
 int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref, int64_t channels,
                           fgfrft_denoise** out) {
+    return fgfrft_denoise_create_ex(c, y, x_ref, channels, 0, out);
+}
+
+int fgfrft_denoise_create_ex(fgfrft_cache* c, const double* y, const double* x_ref, int64_t channels,
+                             int loss_on_real, fgfrft_denoise** out) {
     FGB_GUARD_BEGIN
     if (!out) return fail(FGFRFT_PARAMETER, "null output handle pointer");
     *out = nullptr;
     if (int st = check_handle(c)) return st;
-    if (!c->real || c->dtype != FGFRFT_C128)
-        return fail(FGFRFT_PARAMETER, "denoise on the device needs a real F (graph GFT) in a complex128 cache");
+    if (c->dtype != FGFRFT_C128 || c->api_c64)
+        return fail(FGFRFT_PARAMETER, "denoise on the device needs a complex128 cache");
     if (channels < 1) return fail(FGFRFT_SHAPE, "denoise: need at least one channel");
     if (!y || !x_ref) return fail(FGFRFT_PARAMETER, "null signal buffer");
     std::lock_guard<std::mutex> lk(c->mu);
@@ -91,10 +130,20 @@ int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref,
     d->ch = channels;
     d->l = c->l;
     const int64_t cnt = d->n * channels;
-    d->cpad = cnt + (cnt & 1);  // even: 16-byte aligned blocks for the combine kernel
+    d->cpad = cnt + (cnt & 1);  // even: 16-byte aligned blocks
+    d->cplx = !c->real;
+    d->loss_on_real = loss_on_real != 0;
     const size_t blk = (size_t)d->cpad * 8, T = 2 * (size_t)d->l + 1, np = (size_t)d->n + 1;
     int rc = FGFRFT_OK;
-    if (d->y.ensure(blk) || d->x.ensure(blk) || d->qd.ensure(2 * (size_t)d->n * d->n * 8) || d->uu.ensure(2 * blk) ||
+    if (d->cplx) {  // complex blocks (the exact backend's buffers), [Q | dQ] complex, a ones diagonal
+        const size_t cb = (size_t)cnt * 16;
+        if (d->xytil.ensure(cb) || d->xu.ensure(cb) || d->xb.ensure(cb) || d->xw.ensure(cb) || d->xcot.ensure(cb) ||
+            d->xvhr.ensure(cb) || d->xfar.ensure(cb) || d->xq.ensure(cb) || d->xt.ensure(cb) ||
+            d->xph.ensure((size_t)d->n * 16))
+            rc = fail(FGFRFT_CAPACITY, "denoise: device allocation failed");
+    }
+    if (rc != FGFRFT_OK || d->y.ensure(blk) || d->x.ensure(blk) ||
+        d->qd.ensure(2 * (size_t)d->n * d->n * (d->cplx ? 16 : 8)) || d->uu.ensure(2 * blk) ||
         d->ww.ensure(2 * blk) || d->qr.ensure(blk) ||
         d->v.ensure(blk) || d->r.ensure(blk) || d->params.ensure(np * 8) || d->grad.ensure(np * 8) ||
         d->adam.ensure(2 * np * 8) || d->tab.ensure(4 * T * 8) || d->part.ensure(dn_part_elems() * 8) ||
@@ -107,13 +156,18 @@ int fgfrft_denoise_create(fgfrft_cache* c, const double* y, const double* x_ref,
             cudaMemcpyAsync(d->x.p, x_ref, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream))
             rc = fail(FGFRFT_CUDA, "denoise: upload failed");
     }
+    if (rc == FGFRFT_OK && d->cplx) {  // y as complex; the all-ones diagonal for dnx_grad
+        std::vector<double2> ones((size_t)d->n, make_double2(1.0, 0.0));
+        if (launch_real_to_cplx(d->y.as<double>(), cnt, d->xytil.p, c->stream) ||
+            cudaMemcpyAsync(d->xph.p, ones.data(), ones.size() * 16, cudaMemcpyHostToDevice, c->stream) ||
+            cudaStreamSynchronize(c->stream))
+            rc = fail(FGFRFT_CUDA, "denoise: setup failed");
+        g_launches += 1;
+    }
     if (rc == FGFRFT_OK && cudaStreamSynchronize(c->stream) != cudaSuccess)
         rc = fail(FGFRFT_CUDA, "denoise: setup failed");
     if (rc != FGFRFT_OK) {
-        for (DevBuf* b : {&d->y, &d->x, &d->qd, &d->uu, &d->ww, &d->qr, &d->v, &d->r,
-                          &d->params, &d->grad, &d->adam, &d->tab, &d->part, &d->scal, &d->best, &d->traj, &d->flag})
-            b->release();
-        delete d;
+        fgfrft_denoise_destroy(d);
         return rc;
     }
     *out = d;
@@ -224,7 +278,7 @@ int fgfrft_denoise_fit(fgfrft_denoise* d, int epochs, double lr, double init_alp
         FGB_CUDA(cudaMemcpyAsync(params, best + 1, (size_t)np * 8, cudaMemcpyDeviceToDevice, cst));
         if (int st = denoise_eval_device(d, params, sl, d->grad.as<double>())) return st;
         const void* src = d->ww.p;
-        if (d->exact) {  // Re w
+        if (d->exact || d->cplx) {  // Re w
             FGB_LAUNCH(launch_real_part(d->xw.p, d->xt.p, d->n * d->ch, cst), 1);
             src = d->xt.p;
         }
@@ -344,7 +398,7 @@ int fgfrft_denoise_reconstruct(fgfrft_denoise* d, double alpha, const double* h,
     FGB_CUDA(cudaMemcpyAsync(params + 1, h, (size_t)d->n * 8, cudaMemcpyHostToDevice, st));
     if (int e = denoise_eval_device(d, params, d->scal.as<double>(), d->grad.as<double>())) return e;
     const void* src = d->ww.p;
-    if (d->exact) {  // Re w (learn.hpp:232-234)
+    if (d->exact || d->cplx) {  // Re w (learn.hpp:232-234, 405-408)
         FGB_LAUNCH(launch_real_part(d->xw.p, d->xt.p, d->n * d->ch, st), 1);
         src = d->xt.p;
     }

@@ -426,7 +426,8 @@ int main() {
         CHECK(r.trajectory.size() == 21);
         CHECK(r.loss_best <= r.trajectory.front().loss);
         CHECK(r.reconstruction.rows() == n && r.reconstruction.cols() == 1);
-        CHECK_THROWS_AS(denoise(y, x, householder_unitary(48, 2), cfg, Backend::fast), parameter_error);
+        const DenoiseResult rc = denoise(y, x, householder_unitary(48, 2), cfg, Backend::fast);  // complex F
+        CHECK(rc.trajectory.size() == 21 && rc.loss_best <= rc.trajectory.front().loss);
         DenoiseConfig bad;
         bad.epochs = 0;
         CHECK_THROWS_AS(denoise(y, x, f, bad, Backend::fast), parameter_error);

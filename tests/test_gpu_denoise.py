@@ -56,11 +56,13 @@ def test_denoise_fit_matches_reference_loop():
     assert out["traj_loss"][-1] < out["traj_loss"][0]  # it learns
 
 
-def test_denoise_rejects_complex_f():
+def test_denoise_rejects_complex64_cache():
     f = prep.random_unitary(64, 3)
-    g = fg.PowerCache(f, 4)
+    g = fg.PowerCache(f, 4, dtype=fg.C64)
     with pytest.raises(fg.ParameterError):
         fg.DenoiseProblem(g, np.zeros((64, 2)), np.zeros((64, 2)))
+    with pytest.raises(fg.ShapeError):
+        fg.DenoiseProblem(fg.PowerCache(f, 4), np.zeros((63, 2)), np.zeros((63, 2)))
 
 
 def test_denoise_fit_non_finite_loss_reports_epoch():  # learn.hpp:499-505 (optimizer_error)
@@ -114,3 +116,23 @@ def test_exact_denoise_fit_matches_reference_loop():
     assert np.max(np.abs(out["traj_loss"] - tl) / tl) <= 1e-8
     assert out["best_epoch"] == be
     assert np.linalg.norm(out["reconstruction"] - ref.reconstruct(ab, hb)) <= 1e-8 * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("loss_on_real", [False, True])
+@pytest.mark.parametrize("n", [48, 520])
+def test_fast_denoise_complex_f_matches_oracle(n, loss_on_real):  # FastDenoiseEngine<MatrixXcd>
+    f = prep.random_unitary(n, 13)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 3))
+    y = x + 0.4 * rng.standard_normal((n, 3))
+    l = 10
+    ref = O.FastDenoise(y, x, f, l, loss_on_real)
+    dp = fg.DenoiseProblem(fg.PowerCache(f, l), y, x, loss_on_real=loss_on_real)
+    for alpha in (0.3, 1.1):
+        h = 1.0 + 0.2 * rng.standard_normal(n)
+        loss, ga, gh = dp.eval(alpha, h)
+        lr, gar, ghr = ref.eval(alpha, h)
+        assert abs(loss - lr) <= 1e-10 * lr
+        assert abs(ga - gar) <= 1e-9 * max(1.0, abs(gar))
+        assert np.linalg.norm(gh - ghr) <= 1e-9 * np.linalg.norm(ghr)
+        assert np.linalg.norm(dp.reconstruct(alpha, h) - ref.reconstruct(alpha, h)) <= 1e-10 * np.linalg.norm(y)

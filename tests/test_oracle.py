@@ -325,3 +325,23 @@ def test_exact_denoise_gradients_finite_differences(loss_on_real):  # acceptance
             hh[idx] = val
             return prob.eval(alpha, hh)[0]
         assert _rel_err(gh[idx], _central(lh, h[idx])) <= 1e-5
+
+
+@pytest.mark.parametrize("loss_on_real", [False, True])
+def test_fast_denoise_complex_f_finite_differences(loss_on_real):  # learn.hpp:291-413 (MatrixXcd)
+    f, v, th = prep.synthetic_unitary(prep.spread_phases(20, 0.2, 4), 21)
+    rng = prep.Rng(601)
+    n = 20
+    x = np.array([[rng.gaussian(), rng.gaussian()] for _ in range(n)])
+    y = x + 0.5 * np.array([[rng.gaussian(), rng.gaussian()] for _ in range(n)])
+    prob = O.FastDenoise(y, x, f, 8, loss_on_real)
+    alpha = 0.41
+    h = 1.0 + 0.3 * np.array([rng.gaussian() for _ in range(n)])
+    loss, ga, gh = prob.eval(alpha, h)
+    assert _rel_err(ga, _central(lambda a: prob.eval(a, h)[0], alpha)) <= 1e-5
+    for idx in (0, n // 2):
+        def lh(val, idx=idx):
+            hh = h.copy()
+            hh[idx] = val
+            return prob.eval(alpha, hh)[0]
+        assert _rel_err(gh[idx], _central(lh, h[idx])) <= 1e-5
