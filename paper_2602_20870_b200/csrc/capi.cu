@@ -290,9 +290,18 @@ int build_powers(fgfrft_cache* c, const double* f) {
             c->tmp.release();
             return FGFRFT_OK;
         }
+        // Large n: the chain P_k = F P_(k-1), on the INT8 engine with 7 digits (~1e-15 per product,
+        // the DMMA rounding level) unless the engine is forced to DMMA (FGFRFT_ENGINE=dmma).
+        static const bool dmma_only = [] {
+            const char* e = std::getenv("FGFRFT_ENGINE");
+            return e && !std::strcmp(e, "dmma");
+        }();
+        const bool i8 = !dmma_only && n <= 16384;
         const double* p = fr;
         for (int k = 2; k <= c->l; ++k) {
-            {
+            if (i8) {
+                if (int st = fgfrft_dgemm_int8_dev(0, 0, n, n, n, fr, n, p, n, cur, n, 7, c->stream)) return st;
+            } else {
                 ProfScope ps(KC_GEMM, c->stream);
                 FGB_LAUNCH(launch_rgemm(0, 0, 0, n, n, n, fr, n, 0, p, n, 0, cur, n, 0, 1, c->stream), 1);
             }

@@ -146,6 +146,12 @@ def test_config4_point_cloud_full_size():
     try:
         assert cache.is_real()  # graph GFT: real orthogonal F -> real cache (8 B per element)
         assert cache.device_bytes() == 128 * 8192 * 8192 * 8
+        col = np.zeros((cfg.n, 1))
+        col[7, 0] = 1.0
+        ref = col
+        for _ in range(128):  # the 127-product build chain against repeated products on the host
+            ref = cfg.f.real @ ref
+        assert rel(cache.power(128)[:, 7:8], ref) <= 1e-12
         _sampled_checks(cfg, cache, cols=slice(0, 6), budget_cols=4)
     finally:
         cache.close()
