@@ -12,6 +12,7 @@
 // (double precision, the sinc.hpp formulas; differences from glibc are ~1 ulp, far inside the
 // complex64 tolerance), so a step has no host-side O(graphs x heads x L) work.
 #include <math_constants.h>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -35,23 +36,25 @@ __global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_order
     coef[(size_t)o * 2 * w + w + t] = dsinc_deriv(x);
 }
 
-// [G] column-major n x n complex128 (stride n*n) -> [G][slab k] tiled complex64 padded to 64.
+// [G] column-major n x n complex128 (stride n*n) -> [G][slab k] tiled complex64 padded to 64
+// (REAL: a real F's slabs as float, half the bytes and half the FMAs downstream).
+template <bool REAL>
 __global__ void __launch_bounds__(256) batch_to_tiled_kernel(const double2* __restrict__ src, int n, int l, int k,
-                                                             float2* __restrict__ dst) {
+                                                             void* __restrict__ dstv) {
     const int g = blockIdx.y, tile = blockIdx.x;  // tile = I + 2*J
     const int I = tile & 1, J = tile >> 1;
     const int r = threadIdx.x & 31, w = threadIdx.x >> 5;
     const double2* s = src + (int64_t)g * n * n;
-    float2* t = dst + ((int64_t)g * l + (k - 1)) * kBSlab + (int64_t)tile * kTileElems;
+    const int64_t off = ((int64_t)g * l + (k - 1)) * kBSlab + (int64_t)tile * kTileElems;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int c = w + 8 * i, row = I * 32 + r, col = J * 32 + c;
-        float2 v = make_float2(0.f, 0.f);
-        if (row < n && col < n) {
-            const double2 x = s[(int64_t)col * n + row];
-            v = make_float2((float)x.x, (float)x.y);
-        }
-        t[swz(r, c)] = v;
+        double2 x = make_double2(0.0, 0.0);
+        if (row < n && col < n) x = s[(int64_t)col * n + row];
+        if (REAL)
+            static_cast<float*>(dstv)[off + swz(r, c)] = (float)x.x;
+        else
+            static_cast<float2*>(dstv)[off + swz(r, c)] = make_float2((float)x.x, (float)x.y);
     }
 }
 
@@ -68,17 +71,19 @@ struct BatchSmem {
 
 size_t batch_smem_bytes(int l) { return BatchSmem::bytes(l); }
 
-template <int H>
+// R: real slabs (a real F: Q real, half the bytes streamed and half the FMAs in both phases).
+template <int H, bool R>
 __global__ void __launch_bounds__(kBTh, 1)
-batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
+batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
                      const float2* __restrict__ x, int ch, float2* __restrict__ y) {
+    using ST = typename std::conditional<R, float, float2>::type;  // slab / Q element
     extern __shared__ __align__(128) unsigned char smem[];
-    float2* regA = reinterpret_cast<float2*>(smem);
+    ST* regA = reinterpret_cast<ST*>(smem);
     float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
     const int g = blockIdx.x, tid = threadIdx.x;
     const int w = 2 * l + 1;
-    const float2* gs = slabs + (int64_t)g * l * kBSlab;
+    const ST* gs = static_cast<const ST*>(slabs) + (int64_t)g * l * kBSlab;
     if (tid == 0) {
         for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
@@ -89,7 +94,7 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
         xs[idx] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    const uint32_t bytes = kBSlab * 8;
+    const uint32_t bytes = kBSlab * sizeof(ST);
     auto issue = [&](int k, int s) {
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
@@ -98,18 +103,19 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
         for (int s = 0; s < kBStages && s < l; ++s) issue(s + 1, s);
     // element ownership: e = tid + 512 u -> i = e & 63 (= tid & 63), j = (tid >> 6) + 8 u
     const int i = tid & 63, j0 = tid >> 6;
-    float2 q[8][H];
+    ST q[8][H];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            const float c0 = (float)coef[(size_t)(g * H + h) * 2 * w + l];
-            q[u][h] = make_float2((i == j0 + 8 * u) ? c0 : 0.f, 0.f);
+            const float c0 = (i == j0 + 8 * u) ? (float)coef[(size_t)(g * H + h) * 2 * w + l] : 0.f;
+            if constexpr (R) q[u][h] = c0;
+            else q[u][h] = make_float2(c0, 0.f);
         }
     for (int k = 1; k <= l; ++k) {
         const int s = (k - 1) % kBStages;
         mbar_wait(&full[s], ((k - 1) / kBStages) & 1);
-        const float2* t = regA + (size_t)s * kBSlab;
+        const ST* t = regA + (size_t)s * kBSlab;
         float a[H], b[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
@@ -119,11 +125,15 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int j = j0 + 8 * u;
-            const float2 p = t[bidx(i, j)], pt = t[bidx(j, i)];
+            const ST p = t[bidx(i, j)], pt = t[bidx(j, i)];
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                q[u][h].x = fmaf(a[h], p.x, fmaf(b[h], pt.x, q[u][h].x));
-                q[u][h].y = fmaf(a[h], p.y, fmaf(-b[h], pt.y, q[u][h].y));
+                if constexpr (R) {
+                    q[u][h] = fmaf(a[h], p, fmaf(b[h], pt, q[u][h]));
+                } else {
+                    q[u][h].x = fmaf(a[h], p.x, fmaf(b[h], pt.x, q[u][h].x));
+                    q[u][h].y = fmaf(a[h], p.y, fmaf(-b[h], pt.y, q[u][h].y));
+                }
             }
         }
         __syncthreads();
@@ -136,7 +146,7 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
         for (int h = 0; h < H; ++h) regA[(size_t)h * kBN * kBN + (j0 + 8 * u) * kBN + i] = q[u][h];
     __syncthreads();
     // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: thread -> rows 2ib, 2ib+1, 32+2ib, 33+2ib and cols 2cb, 2cb+1
-    // (the 16 lanes of a half-warp read 256 contiguous bytes of a Q column per LDS.128: conflict-free)
+    // (the 16 lanes of a half-warp read contiguous bytes of a Q column: conflict-free)
     const int ib = tid & 15, cb = tid >> 4;
     float acc[H][4][2][2];
 #pragma unroll
@@ -149,16 +159,29 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
         const float2 x0 = xs[(2 * cb) * kBN + j], x1 = xs[(2 * cb + 1) * kBN + j];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            const float4* qp = reinterpret_cast<const float4*>(regA + (size_t)h * kBN * kBN + j * kBN + 2 * ib);
-            const float4 v0 = qp[0], v1 = qp[16];
-            const float2 qv[4] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
-                                  make_float2(v1.z, v1.w)};
+            if constexpr (R) {
+                const float2* qp = reinterpret_cast<const float2*>(regA + (size_t)h * kBN * kBN + j * kBN + 2 * ib);
+                const float2 v0 = qp[0], v1 = qp[16];
+                const float qv[4] = {v0.x, v0.y, v1.x, v1.y};
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                acc[h][r][0][0] = fmaf(qv[r].x, x0.x, fmaf(-qv[r].y, x0.y, acc[h][r][0][0]));
-                acc[h][r][0][1] = fmaf(qv[r].x, x0.y, fmaf(qv[r].y, x0.x, acc[h][r][0][1]));
-                acc[h][r][1][0] = fmaf(qv[r].x, x1.x, fmaf(-qv[r].y, x1.y, acc[h][r][1][0]));
-                acc[h][r][1][1] = fmaf(qv[r].x, x1.y, fmaf(qv[r].y, x1.x, acc[h][r][1][1]));
+                for (int r = 0; r < 4; ++r) {
+                    acc[h][r][0][0] = fmaf(qv[r], x0.x, acc[h][r][0][0]);
+                    acc[h][r][0][1] = fmaf(qv[r], x0.y, acc[h][r][0][1]);
+                    acc[h][r][1][0] = fmaf(qv[r], x1.x, acc[h][r][1][0]);
+                    acc[h][r][1][1] = fmaf(qv[r], x1.y, acc[h][r][1][1]);
+                }
+            } else {
+                const float4* qp = reinterpret_cast<const float4*>(regA + (size_t)h * kBN * kBN + j * kBN + 2 * ib);
+                const float4 v0 = qp[0], v1 = qp[16];
+                const float2 qv[4] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
+                                      make_float2(v1.z, v1.w)};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    acc[h][r][0][0] = fmaf(qv[r].x, x0.x, fmaf(-qv[r].y, x0.y, acc[h][r][0][0]));
+                    acc[h][r][0][1] = fmaf(qv[r].x, x0.y, fmaf(qv[r].y, x0.x, acc[h][r][0][1]));
+                    acc[h][r][1][0] = fmaf(qv[r].x, x1.x, fmaf(-qv[r].y, x1.y, acc[h][r][1][0]));
+                    acc[h][r][1][1] = fmaf(qv[r].x, x1.y, fmaf(qv[r].y, x1.x, acc[h][r][1][1]));
+                }
             }
         }
     }
@@ -178,18 +201,20 @@ batch_forward_kernel(const float2* __restrict__ slabs, int n, int l, const doubl
         }
 }
 
-template <int H>
+template <int H, bool R>
 __global__ void __launch_bounds__(kBTh, 1)
-batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
+batch_dlda_kernel(const void* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
                   const float2* __restrict__ gcot, const float2* __restrict__ x, int ch, double* __restrict__ dlda) {
+    using ST = typename std::conditional<R, float, float2>::type;  // slab element; M element (Re M for R)
     extern __shared__ __align__(128) unsigned char smem[];
     float2* regA = reinterpret_cast<float2*>(smem);
+    ST* regS = reinterpret_cast<ST*>(smem);  // the same region as power stages
     float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
     double* red = reinterpret_cast<double*>(full + kBStages);  // [k 0..l][warp 16][8]
     const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = 2 * l + 1;
-    const float2* gs = slabs + (int64_t)g * l * kBSlab;
+    const ST* gs = static_cast<const ST*>(slabs) + (int64_t)g * l * kBSlab;
     if (tid == 0) {
         for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
@@ -207,11 +232,14 @@ batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* 
     __syncthreads();
     // M_h[i, j] = sum_c G_h[i, c] conj(X[j, c]) for the thread's 8 elements
     const int i = tid & 63, j0 = tid >> 6;
-    float2 m[8][H];
+    ST m[8][H];  // R: only Re M = Gr Xr^T + Gi Xi^T is needed against real powers
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int h = 0; h < H; ++h) m[u][h] = make_float2(0.f, 0.f);
+        for (int h = 0; h < H; ++h) {
+            if constexpr (R) m[u][h] = 0.f;
+            else m[u][h] = make_float2(0.f, 0.f);
+        }
     for (int c = 0; c < kBMaxCh; ++c) {
         float2 gv[H];
 #pragma unroll
@@ -221,16 +249,20 @@ batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* 
             const float2 xv = xs[c * kBN + j0 + 8 * u];
 #pragma unroll
             for (int h = 0; h < H; ++h) {  // g * conj(x)
-                m[u][h].x = fmaf(gv[h].x, xv.x, fmaf(gv[h].y, xv.y, m[u][h].x));
-                m[u][h].y = fmaf(gv[h].y, xv.x, fmaf(-gv[h].x, xv.y, m[u][h].y));
+                if constexpr (R) {
+                    m[u][h] = fmaf(gv[h].x, xv.x, fmaf(gv[h].y, xv.y, m[u][h]));
+                } else {
+                    m[u][h].x = fmaf(gv[h].x, xv.x, fmaf(gv[h].y, xv.y, m[u][h].x));
+                    m[u][h].y = fmaf(gv[h].y, xv.x, fmaf(-gv[h].x, xv.y, m[u][h].y));
+                }
             }
         }
     }
     __syncthreads();  // region A is reused for the power stages
-    const uint32_t bytes = kBSlab * 8;
+    const uint32_t bytes = kBSlab * sizeof(ST);
     auto issue = [&](int k, int s) {
         mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
+        bulk_g2s(regS + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
     };
     if (tid == 0)
         for (int s = 0; s < kBStages && s < l; ++s) issue(s + 1, s);
@@ -243,7 +275,10 @@ batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* 
         for (int u = 0; u < 8; ++u)
 #pragma unroll
             for (int h = 0; h < H; ++h)
-                if (i == j0 + 8 * u) v[h] += (double)m[u][h].x;
+                if (i == j0 + 8 * u) {
+                    if constexpr (R) v[h] += (double)m[u][h];
+                    else v[h] += (double)m[u][h].x;
+                }
 #pragma unroll
         for (int h = 0; h < H; ++h) {
             double t = v[h];
@@ -255,7 +290,7 @@ batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* 
     for (int k = 1; k <= l; ++k) {
         const int s = (k - 1) % kBStages;
         mbar_wait(&full[s], ((k - 1) / kBStages) & 1);
-        const float2* t = regA + (size_t)s * kBSlab;
+        const ST* t = regS + (size_t)s * kBSlab;
         // [h][+/-] packed as 2h + sign; the thread's 8 terms are summed in FP32 (one F2F per value
         // instead of one per product), the cross-thread reduction is FP64
         float vf[8];
@@ -264,11 +299,16 @@ batch_dlda_kernel(const float2* __restrict__ slabs, int n, int l, const double* 
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int j = j0 + 8 * u;
-            const float2 p = t[bidx(i, j)], pt = t[bidx(j, i)];
+            const ST p = t[bidx(i, j)], pt = t[bidx(j, i)];
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                vf[2 * h] += fmaf(m[u][h].x, p.x, m[u][h].y * p.y);
-                vf[2 * h + 1] += fmaf(m[u][h].x, pt.x, -m[u][h].y * pt.y);
+                if constexpr (R) {
+                    vf[2 * h] = fmaf(m[u][h], p, vf[2 * h]);
+                    vf[2 * h + 1] = fmaf(m[u][h], pt, vf[2 * h + 1]);
+                } else {
+                    vf[2 * h] += fmaf(m[u][h].x, p.x, m[u][h].y * p.y);
+                    vf[2 * h + 1] += fmaf(m[u][h].x, pt.x, -m[u][h].y * pt.y);
+                }
             }
         }
         double v[8];
@@ -314,8 +354,12 @@ cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, dou
     return cudaGetLastError();
 }
 
-cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream) {
-    batch_to_tiled_kernel<<<dim3(4, graphs), 256, 0, stream>>>((const double2*)src, n, l, k, (float2*)dst);
+cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, bool real,
+                                  cudaStream_t stream) {
+    if (real)
+        batch_to_tiled_kernel<true><<<dim3(4, graphs), 256, 0, stream>>>((const double2*)src, n, l, k, dst);
+    else
+        batch_to_tiled_kernel<false><<<dim3(4, graphs), 256, 0, stream>>>((const double2*)src, n, l, k, dst);
     return cudaGetLastError();
 }
 
@@ -328,14 +372,14 @@ cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int
     }
 
 cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
-                                 const void* x, int ch, void* y, cudaStream_t stream) {
+                                 const void* x, int ch, void* y, bool real, cudaStream_t stream) {
     const size_t smem = batch_smem_bytes(l);
 #define FGB_BF(HV)                                                                                             \
     {                                                                                                          \
-        auto kern = batch_forward_kernel<HV>;                                                                  \
+        auto kern = real ? batch_forward_kernel<HV, true> : batch_forward_kernel<HV, false>;                    \
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
         if (e != cudaSuccess) return e;                                                                        \
-        kern<<<graphs, kBTh, smem, stream>>>((const float2*)slabs, n, l, coef, (const float2*)x, ch, (float2*)y); \
+        kern<<<graphs, kBTh, smem, stream>>>(slabs, n, l, coef, (const float2*)x, ch, (float2*)y);              \
     }
     FGB_BATCH_HEADS(FGB_BF)
 #undef FGB_BF
@@ -343,15 +387,15 @@ cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, co
 }
 
 cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
-                              const void* gcot, const void* x, int ch, double* dlda, cudaStream_t stream) {
+                              const void* gcot, const void* x, int ch, double* dlda, bool real, cudaStream_t stream) {
     const size_t smem = batch_smem_bytes(l);
 #define FGB_BD(HV)                                                                                            \
     {                                                                                                         \
-        auto kern = batch_dlda_kernel<HV>;                                                                    \
+        auto kern = real ? batch_dlda_kernel<HV, true> : batch_dlda_kernel<HV, false>;                        \
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
         if (e != cudaSuccess) return e;                                                                       \
-        kern<<<graphs, kBTh, smem, stream>>>((const float2*)slabs, n, l, coef, (const float2*)gcot,           \
-                                             (const float2*)x, ch, dlda);                                     \
+        kern<<<graphs, kBTh, smem, stream>>>(slabs, n, l, coef, (const float2*)gcot, (const float2*)x, ch,    \
+                                             dlda);                                                           \
     }
     FGB_BATCH_HEADS(FGB_BD)
 #undef FGB_BD

@@ -45,11 +45,12 @@ cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, 
                              bool real);
 size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
 cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream);
-cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, cudaStream_t stream);
+cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, bool real,
+                                  cudaStream_t stream);
 cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
-                                 const void* x, int ch, void* y, cudaStream_t stream);
+                                 const void* x, int ch, void* y, bool real, cudaStream_t stream);
 cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
-                              const void* gcot, const void* x, int ch, double* dlda, cudaStream_t stream);
+                              const void* gcot, const void* x, int ch, double* dlda, bool real, cudaStream_t stream);
 int batch_max_heads();
 int batch_max_channels();
 int batch_max_n();

@@ -498,6 +498,12 @@ int fgfrft_batch_create(const double* fs, int64_t graphs, int64_t n, int l, int 
     c->elem = 8;
     c->graphs = graphs;
     c->fingerprint = host_fnv1a64(fs, (size_t)graphs * n * n * 16);
+    if (std::getenv("FGFRFT_NO_REAL") == nullptr) {  // every F real: real float slabs (half the bytes)
+        bool real = true;
+        for (size_t i = 0; i < (size_t)graphs * n * n && real; ++i) real = fs[2 * i + 1] == 0.0;
+        c->real = real;
+        if (real) c->elem = 4;
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete c;
@@ -505,7 +511,7 @@ int fgfrft_batch_create(const double* fs, int64_t graphs, int64_t n, int l, int 
     }
     c->stream = c->own_stream;
     const size_t slab = 4 * (size_t)kTileElems;  // padded 64 x 64
-    if (cudaMalloc(&c->slabs, (size_t)graphs * l * slab * 8) != cudaSuccess) {
+    if (cudaMalloc(&c->slabs, (size_t)graphs * l * slab * c->elem) != cudaSuccess) {
         cudaGetLastError();
         destroy_cache(c);
         return fail(FGFRFT_CAPACITY, "graph batch: device allocation failed");
@@ -536,7 +542,7 @@ int fgfrft_batch_create(const double* fs, int64_t graphs, int64_t n, int l, int 
                 std::swap(prev, cur);
                 g_launches += 1;
             }
-            if (launch_batch_to_tiled(p, (int)graphs, (int)n, l, k, c->slabs, c->stream) != cudaSuccess) {
+            if (launch_batch_to_tiled(p, (int)graphs, (int)n, l, k, c->slabs, c->real, c->stream) != cudaSuccess) {
                 rc = fail(FGFRFT_CUDA, "graph batch: tiling failed");
                 break;
             }
@@ -593,7 +599,7 @@ int fgfrft_batch_forward_dev(fgfrft_cache* c, const double* alphas_dev, int head
     if (int st = batch_coefs(c, alphas_dev, heads, &coef)) return st;
     ProfScope ps(KC_SYNTH, c->stream);
     FGB_LAUNCH(launch_batch_forward(c->slabs, (int)c->graphs, (int)c->n, c->l, coef, heads, x_dev, (int)ch, y_dev,
-                                    c->stream),
+                                    c->real, c->stream),
                1);
     return FGFRFT_OK;
     FGB_GUARD_END
@@ -612,7 +618,7 @@ int fgfrft_batch_dlda_dev(fgfrft_cache* c, const double* alphas_dev, int heads, 
     if (int st = batch_coefs(c, alphas_dev, heads, &coef)) return st;
     ProfScope ps(KC_DOTS, c->stream);
     FGB_LAUNCH(launch_batch_dlda(c->slabs, (int)c->graphs, (int)c->n, c->l, coef, heads, g_dev, x_dev, (int)ch,
-                                 static_cast<double*>(dlda_dev), c->stream),
+                                 static_cast<double*>(dlda_dev), c->real, c->stream),
                1);
     return FGFRFT_OK;
     FGB_GUARD_END

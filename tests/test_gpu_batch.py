@@ -15,10 +15,16 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+@pytest.mark.parametrize("kind", ["graph", "unitary"])
 @pytest.mark.parametrize("graphs,n,l,heads,ch", [(24, 64, 16, 4, 64), (9, 40, 5, 2, 17), (5, 64, 16, 1, 64),
                                                  (3, 33, 30, 3, 8)])
-def test_graph_batch_forward_and_gradient(graphs, n, l, heads, ch):
-    fs = np.stack([prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 100 + g))) for g in range(graphs)])
+def test_graph_batch_forward_and_gradient(graphs, n, l, heads, ch, kind):
+    """kind graph: every F real (ER graph GFTs) -> real float slabs and the real kernels; unitary:
+    complex F (Haar) -> complex64 slabs."""
+    if kind == "graph":
+        fs = np.stack([prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 100 + g))) for g in range(graphs)])
+    else:
+        fs = np.stack([prep.random_unitary(n, 200 + g) for g in range(graphs)])
     rng = np.random.default_rng(graphs)
     alphas = rng.uniform(0.5, 1.5, (graphs, heads))
     x = (rng.standard_normal((graphs, n, ch)) + 1j * rng.standard_normal((graphs, n, ch))).astype(np.complex64)

@@ -108,7 +108,7 @@ def run_c5(peaks):
     nodes = G * H * n * C
     # FP32 work: synthesis 8*L*n^2*H, apply 8*n^2*C*H, M = G X^H 8*n^2*C*H, dots 8*L*n^2*H (per graph)
     flops = G * (8 * l * n * n * H * 2 + 8 * n * n * C * H * 2)
-    cache_bytes = G * l * 64 * 64 * 8
+    cache_bytes = G * l * 64 * 64 * (4 if np.all(np.imag(fs) == 0) else 8)  # real F: float slabs
     return {"config": "C5", "graphs": G, "n": n, "l": l, "heads": H, "channels": C, "dtype": "c64",
             "cache_gb": cache_bytes / 1e9, "prep_s": prep_s, "cache_build_s": build_s,
             "forward": {"ms": t_fwd, "signal_nodes_per_s": nodes / (t_fwd * 1e-3),
