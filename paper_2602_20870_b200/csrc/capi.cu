@@ -296,7 +296,7 @@ int build_powers(fgfrft_cache* c, const double* f) {
             const char* e = std::getenv("FGFRFT_ENGINE");
             return e && !std::strcmp(e, "dmma");
         }();
-        const bool i8 = !dmma_only && n <= 16384;
+        const bool i8 = !dmma_only && n > 2048 && n <= 16384;
         const double* p = fr;
         for (int k = 2; k <= c->l; ++k) {
             if (i8) {
