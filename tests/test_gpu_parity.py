@@ -588,3 +588,38 @@ def test_complex64_api_over_real_f_runs_the_real_fp64_path():
     assert np.allclose(dl.cpu().numpy(), d_ref, rtol=1e-9, atol=1e-14)
     # host-buffer entry points return complex128 as before
     assert rel(fg.apply_series(g64, alphas, x128)[0], y_ref[0]) <= 1e-14
+
+
+def test_concurrent_handles_from_threads():
+    """Distinct handles used from concurrent host threads (ctypes releases the GIL): results equal
+    the sequential ones; one handle shared by two threads is serialised by the handle."""
+    import threading
+    fa = prep.gft_from_shift(prep.laplacian(prep.er_graph(600, 0.02, 1)))
+    fb = prep.random_unitary(300, 2)
+    rng = np.random.default_rng(3)
+    xa = rng.standard_normal((600, 40)) + 1j * rng.standard_normal((600, 40))
+    xb = rng.standard_normal((300, 20)) + 1j * rng.standard_normal((300, 20))
+    ga, gb = fg.PowerCache(fa, 16), fg.PowerCache(fb, 12)
+    alphas = list(np.linspace(0.1, 1.9, 12))
+    ref_a = fg.mse_step(ga, alphas, xa, xa + 0.1)
+    ref_b = fg.apply_series(gb, alphas[:3], xb)
+    out, errs = {}, []
+
+    def work(key, fn):
+        try:
+            for _ in range(5):
+                out[key] = fn()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=("a", lambda: fg.mse_step(ga, alphas, xa, xa + 0.1))),
+          threading.Thread(target=work, args=("b", lambda: fg.apply_series(gb, alphas[:3], xb))),
+          threading.Thread(target=work, args=("a2", lambda: fg.mse_step(ga, alphas, xa, xa + 0.1)))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for key in ("a", "a2"):
+        assert np.array_equal(out[key][0], ref_a[0]) and np.array_equal(out[key][1], ref_a[1])
+    assert np.array_equal(out["b"], ref_b)
