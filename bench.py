@@ -15,7 +15,8 @@ per-order losses and gradients inside the timed region).
 Extra objects: `roofline` for the dominant kernel (the INT8 Ozaki GEMM, or the DMMA GEMM),
 `synthesis` (F^alpha synthesis GB/s vs HBM peak, the metric's first half, 64-order sweep and
 single order), `cache_build` (K1 TFLOP/s), `cpu_baseline` (the oracle on this host, bounded
-sample), `clocks` (nvidia-smi during the timed region), `gpu_launches`.
+sample; `cpu_baseline_single_thread` the same at 1 thread, the reference's own configuration),
+`clocks` (nvidia-smi during the timed region), `gpu_launches`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Under torchrun (N > 1) every rank runs an independent replica of the workload (different
@@ -194,11 +195,12 @@ def run_reference(args, ws, rank):
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(cfg, budget_s=20.0):
-    """Oracle port on this host, bounded sample (rank 0, N=1 only)."""
+def cpu_baseline(cfg, budget_s=20.0, cores=None):
+    """Oracle port on this host, bounded sample (rank 0, N=1 only). cores=None: all host cores;
+    cores=1: the reference's single-threaded configuration (proj/README.md:47-48)."""
     import oracle as O
     from threadpoolctl import threadpool_limits
-    cores = os.cpu_count() or 1
+    cores = cores or os.cpu_count() or 1
     n, b = cfg.x.shape
     with threadpool_limits(cores):
         cache = O.PowerCache(cfg.f, cfg.l)
@@ -453,9 +455,10 @@ def main():
     e2e_ms = max_over_ranks(max(e2e_dev_ms, t_wall * 1e3))
     e2e_value = n * b * A * ws / (e2e_ms * 1e-3)
 
-    cpu = None
+    cpu = cpu1 = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg)
+        cpu1 = cpu_baseline(cfg, budget_s=8.0, cores=1)  # the reference's single-threaded configuration
 
     if rank == 0:
         out = {
@@ -490,6 +493,7 @@ def main():
             "clocks": clk,
             "parity_check": check,
             "cpu_baseline": cpu,
+            "cpu_baseline_single_thread": cpu1,
         }
         print(json.dumps(out), flush=True)
     if dist is not None:
