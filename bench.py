@@ -337,8 +337,44 @@ def main():
     tot_prof = sum(v[0] for v in prof.values())
     shares = {k: (v[0] / tot_prof if tot_prof else None) for k, v in prof.items()}
     i8_ms, i8_n = prof["int8_gemm"]
+    route, nodes = cache.route_info()
     power_route = i8_n > 0
-    if power_route:
+    if power_route and route == 2:
+        # Node route: W_j = Q(a_j) for r Chebyshev nodes by one INT8 GEMM over the 2L terms
+        # (n^2 element rows x r node rows x K = 2L), then Z'_j = W_j X (r n x 2B x n), both as
+        # S(S+1)/2 int8 digit-product GEMMs; node_combine: Y and dY rows (2 A x r x 2nB DMMA flops
+        # each) with the loss and dL/da.
+        S = int(L_.fgfrft_int8_digits())
+        products = S * (S + 1) // 2
+        r = nodes
+        fp_basis = 2.0 * n * n * r * (2 * L)
+        fp_prod = 2.0 * (r * n) * (2 * b) * n
+        fp64eq = fp_basis + fp_prod
+        i8_ops = fp64eq * products
+        achieved = i8_ops * args.steps / (i8_ms * 1e-3) / 1e12
+        cb_ms, cb_n = prof["combine"]
+        cb_flops = 2 * (2.0 * A * r * 2 * n * b)
+        traffic = ncu_traffic("void ozgemm_kernel<6, 1, 2>")
+        roof = {"bound": "tensor",
+                "kernel": f"ozgemm_kernel<{S},0,1> + <{S},1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
+                "achieved": achieved, "peak": peaks["int8_tops"], "unit": "TOPS",
+                "frac": achieved / peaks["int8_tops"], "traffic": traffic,
+                "traffic_note": ("bytes per launch of the product GEMM, DRAM read + write from the committed "
+                                 "ncu --set full capture"),
+                "peak_source": peaks["int8_src"],
+                "route": f"node interpolation, r = {r} Chebyshev nodes on [{alphas.min():.3g}, {alphas.max():.3g}]",
+                "algorithmic": (f"per step 2*N^2*r*2L (node operators) + 2*(r*N)*(2B)*N (W_j X) FP64-equivalent "
+                                f"flops = {fp64eq:.4g}, as {products} int8 digit-product GEMMs (Ozaki scheme, "
+                                f"{S} base-254 digits)"),
+                "fp64_equivalent_tflops": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12,
+                "fp64_equivalent_frac_of_dmma_peak": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12 / peaks["fp64_tflops"],
+                "dmma_peak_tflops": peaks["fp64_tflops"],
+                "launches_timed": i8_n, "share_of_step": shares,
+                "combine_kernel": {"ms_per_step": cb_ms / args.steps, "flops_per_step": cb_flops,
+                                   "tflops": cb_flops * args.steps / (cb_ms * 1e-3) / 1e12,
+                                   "form": "Y = P_C Z', dY = P_D Z' (DMMA) + loss and dL/da",
+                                   "peak_dmma_tflops": peaks["fp64_tflops"]}}
+    elif power_route:
         S = int(L_.fgfrft_int8_digits())
         products = S * (S + 1) // 2
         fp64eq = 2.0 * (2 * L * n) * (2 * b) * n
@@ -467,7 +503,11 @@ def main():
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": workload_config(cfg, ws),
             "roofline": roof,
-            "route": ("power products: Z = F^k X by one INT8 tensor-core Ozaki GEMM over the stacked cache, "
+            "route": (f"node interpolation: Q(a) through r = {nodes} Chebyshev nodes of the order interval; the "
+                      "node operators W_j by one INT8 tensor-core Ozaki GEMM over the cache's 2L terms, Z'_j = W_j X "
+                      "by a second, then Y, dY, loss and dL/da for every order by one DMMA pass"
+                      if route == 2 else
+                      "power products: Z = F^k X by one INT8 tensor-core Ozaki GEMM over the stacked cache, "
                       "then per-order combination + MSE + dL/da on DMMA" if power_route else
                       "per-order synthesis Q(a) + DMMA GEMMs"),
             "dmma_engine_ms_per_step": dmma_ms,

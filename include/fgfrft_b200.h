@@ -131,6 +131,10 @@ int fgfrft_cache_info(const fgfrft_cache* cache, int64_t* n, int* l, uint64_t* f
  * kernels run (half the bytes and flops; results equal the complex path's up to rounding).
  * Set FGFRFT_NO_REAL=1 in the environment to force the complex kernels. */
 int fgfrft_cache_is_real(const fgfrft_cache* cache, int* real);
+/* Route taken by the last fgfrft_mse_step* on this handle: 0 synthesis (one GEMM pair per order),
+ * 1 power products (2L products F^k X), 2 node interpolation (nodes = its r node operators); -1
+ * before the first step. For benchmarks and diagnostics. */
+int fgfrft_cache_route_info(const fgfrft_cache* cache, int* route, int* nodes);
 
 /* transform.hpp:131-134: copy F^k (1 <= k <= l, else PARAMETER) to host (n x n). */
 int fgfrft_cache_power(fgfrft_cache* cache, int k, double* out);

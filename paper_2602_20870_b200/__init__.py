@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_cache_info": (i, [vp, vp, vp, vp, vp, vp]),
         "fgfrft_cache_power": (i, [vp, i, vp]),
         "fgfrft_cache_is_real": (i, [vp, vp]),
+        "fgfrft_cache_route_info": (i, [vp, vp, vp]),
         "fgfrft_cache_verify": (i, [vp, vp]),
         "fgfrft_cache_set_stream": (i, [vp, vp]),
         "fgfrft_cache_device_slab": (i, [vp, i, pp]),
@@ -160,7 +161,7 @@ def exported_symbols():
         "fgfrft_last_error", "fgfrft_version", "fgfrft_launch_count", "fgfrft_profile_enable",
         "fgfrft_profile_read", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
         "fgfrft_cache_create", "fgfrft_cache_create_from_powers", "fgfrft_cache_destroy", "fgfrft_cache_info",
-        "fgfrft_cache_is_real",
+        "fgfrft_cache_is_real", "fgfrft_cache_route_info",
         "fgfrft_cache_power", "fgfrft_cache_verify", "fgfrft_cache_set_stream", "fgfrft_cache_device_slab",
         "fgfrft_cache_device_bytes", "fgfrft_synthesize", "fgfrft_synthesize_dev", "fgfrft_apply",
         "fgfrft_apply_dev", "fgfrft_apply_matrix", "fgfrft_dlda", "fgfrft_dlda_dev", "fgfrft_mse_step",
@@ -293,6 +294,12 @@ class PowerCache:
 
     def fingerprint(self) -> int:
         return self._fp
+
+    def route_info(self):
+        """(route, nodes) of the last MSE step: 0 synthesis, 1 power products, 2 node interpolation."""
+        r, k = ctypes.c_int(), ctypes.c_int()
+        _check(lib().fgfrft_cache_route_info(self._h, ctypes.addressof(r), ctypes.addressof(k)))
+        return r.value, k.value
 
     def is_real(self) -> bool:
         v = ctypes.c_int()

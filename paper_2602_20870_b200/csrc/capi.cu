@@ -86,6 +86,8 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
     if (c->coef_evt) FGB_CUDA(cudaEventSynchronize(c->coef_evt));
     if (c->coef_h_cap < count) {
         if (c->coef_h) cudaFreeHost(c->coef_h);
+    if (c->nd_h) cudaFreeHost(c->nd_h);
+    if (c->nd_evt) cudaEventDestroy(c->nd_evt);
         c->coef_h = nullptr;
         c->coef_h_cap = 0;
         FGB_CUDA(cudaMallocHost(&c->coef_h, count * sizeof(double)));
@@ -225,7 +227,8 @@ void destroy_cache(fgfrft_cache* c) {
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
                       &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
-                      &c->by})
+                      &c->by, &c->es, &c->ee, &c->erm, &c->nd_tab, &c->nd_p, &c->nd_d0, &c->nd_bsl, &c->nd_bex,
+                      &c->nd_w, &c->nd_z})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -427,6 +430,9 @@ int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x
 bool use_power_route(const fgfrft_cache* c, int n_alpha);
 int engine_of(const fgfrft_cache* c);
 int apply_power_route(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, int64_t b, void* y_dev);
+bool use_node_route(const fgfrft_cache* c, int n_alpha, int64_t b);
+int mse_node_route(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_dev,
+                   int64_t b, void* y_dev, double* loss_dev, double* dlda_dev, bool need_d, bool* ran);
 
 // Y[a] = op(Q(alpha_a)) X for all orders; x_dev n x b, y_dev n_alpha blocks of n x b.
 int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used, bool inverse, const void* x_dev,
@@ -438,6 +444,12 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
         if (inverse)
             for (double& v : al) v = -v;
         if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
+        if (use_node_route(c, n_alpha, b)) {
+            bool ran = false;
+            if (int st = mse_node_route(c, al.data(), n_alpha, x_dev, nullptr, b, y_dev, nullptr, nullptr, false, &ran))
+                return st;
+            if (ran) return FGFRFT_OK;
+        }
         return apply_power_route(c, coef, n_alpha, x_dev, b, y_dev);
     }
     if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
@@ -512,6 +524,230 @@ bool use_power_route(const fgfrft_cache* c, int n_alpha) {
 
 int64_t pad_rows(int64_t n) { return ceil_div(n, kOzTileA) * kOzTileA; }
 int64_t pad_k(int64_t n) { return ceil_div(n, kOzK) * kOzK; }
+
+int wait_xc(fgfrft_cache* c);
+
+// ------------------------------------------------------------------ node route
+//
+// For an order sweep on [lo, hi], Q(a) = sum_k c_k(a) P_k is an entire function of a, so it is
+// interpolated to rounding by a degree-(r-1) polynomial through r Chebyshev nodes a_j of the
+// interval (r = 32 for a width-2 sweep, measured 1e-14 on the coefficients, 2e-12 on their
+// derivatives): F^a X = sum_j l_j(a) W_j X and dF^a/da X = sum_j l_j'(a) W_j X with the node
+// operators W_j = Q(a_j). The W_j come from ONE INT8 GEMM over the cache's 2L terms (element-row
+// digit slices of the stacked cache x the node coefficient rows), the products W_j X from a
+// second one, and the per-order Y, dY, loss and dL/da from one DMMA pass over the r products
+// (node_combine_kernel) -- r products instead of the power route's 2L. Every call re-plans
+// (nodes, barycentric weights, an interpolation check against the exact coefficients on a
+// subset of the orders); a failed check or r > 48 falls back to the power route.
+bool use_node_route(const fgfrft_cache* c, int n_alpha, int64_t b) {
+    static const int mode = [] {
+        const char* e = std::getenv("FGFRFT_ROUTE");
+        return (e && !std::strcmp(e, "power")) ? 0 : 1;
+    }();
+    return mode == 1 && use_power_route(c, n_alpha) && engine_of(c) == FGFRFT_ENGINE_AUTO && use_int8_gemm(c, b) &&
+           n_alpha >= 16 && n_alpha <= 64 && c->n <= 46340;
+}
+
+int ensure_elem_slices(fgfrft_cache* c) {
+    const int S = oz_slices_default();
+    if (c->es_slices == S) return FGFRFT_OK;
+    const int64_t n = c->n, rows = pad_rows(n * n), kp = pad_k(2 * (int64_t)c->l);
+    FGB_CUDA(c->es.ensure((size_t)S * rows * kp));
+    FGB_CUDA(c->ee.ensure((size_t)rows * sizeof(int)));
+    FGB_CUDA(c->erm.ensure((size_t)rows * sizeof(unsigned long long)));
+    OzView v{static_cast<const double*>(c->slabs), 0, 0, (int64_t)c->slab_elems(), 0, 0, (int)(n * n), (int)rows, 1,
+             2 * c->l, (int)kp, true};
+    v.tiled = 6;
+    v.nt = (int)ceil_div(n, kTile);
+    v.l = c->l;
+    v.tp2 = (int)n;
+    ProfScope ps(KC_SLICE, c->stream);
+    FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->es.as<int8_t>(), c->ee.as<int>(), c->erm.as<unsigned long long>(),
+                               c->stream),
+               3);
+    c->es_slices = S;
+    return FGFRFT_OK;
+}
+
+// Plan: nodes, node coefficient rows (r x T), interpolation weights P = [l_j(a); l_j'(a)] (rows x rp).
+// coef_h holds the exact [c | c'] tables of the orders (upload_coefs). false: not interpolable.
+bool node_plan(const double* alphas, int na, int l, bool need_d, const double* coef_h, std::vector<double>& tab,
+               std::vector<double>& d0, std::vector<double>& pw, int* r_out, int* rp_out) {
+    const int T = 2 * l + 1;
+    double lo = alphas[0], hi = alphas[0];
+    for (int a = 1; a < na; ++a) {
+        lo = std::min(lo, alphas[a]);
+        hi = std::max(hi, alphas[a]);
+    }
+    const double w = hi - lo;
+    if (!(w > 1e-9)) return false;
+    const int r = (int)std::ceil(12.0 + 10.0 * w);
+    if (r > node_max_terms()) return false;
+    const int rp = (r + 3) / 4 * 4;
+    const double mid = 0.5 * (lo + hi), half = 0.5 * w;
+    std::vector<double> xn((size_t)r), bw((size_t)r);
+    for (int j = 0; j < r; ++j) {  // Chebyshev points of the first kind and their barycentric weights
+        const double th = M_PI * (2.0 * j + 1.0) / (2.0 * r);
+        xn[j] = mid + half * std::cos(th);
+        bw[j] = ((j & 1) ? -1.0 : 1.0) * std::sin(th);
+    }
+    tab.assign((size_t)r * T, 0.0);
+    d0.assign((size_t)r, 0.0);
+    std::vector<double> scratch((size_t)T);
+    for (int j = 0; j < r; ++j) {
+        host_sinc_coeffs(xn[j], l, &tab[(size_t)j * T], scratch.data());
+        d0[j] = tab[(size_t)j * T + l];
+    }
+    const int rows = need_d ? 2 * na : na;
+    pw.assign((size_t)rows * rp, 0.0);
+    for (int a = 0; a < na; ++a) {
+        const double x = alphas[a];
+        double* lj = &pw[(size_t)a * rp];
+        double* dj = need_d ? &pw[(size_t)(na + a) * rp] : nullptr;
+        int hit = -1;
+        for (int j = 0; j < r; ++j)
+            if (std::fabs(x - xn[j]) < 1e-14 * std::max(1.0, std::fabs(x))) hit = j;
+        if (hit >= 0) {  // on a node: Kronecker weights, the derivative row of the differentiation matrix
+            lj[hit] = 1.0;
+            if (dj) {
+                double diag = 0.0;
+                for (int j = 0; j < r; ++j)
+                    if (j != hit) {
+                        dj[j] = (bw[j] / bw[hit]) / (xn[hit] - xn[j]);
+                        diag -= dj[j];
+                    }
+                dj[hit] = diag;
+            }
+            continue;
+        }
+        double sw = 0.0, sw2 = 0.0;
+        for (int j = 0; j < r; ++j) {
+            const double t = bw[j] / (x - xn[j]);
+            sw += t;
+            sw2 += t / (x - xn[j]);
+        }
+        for (int j = 0; j < r; ++j) {
+            const double t = bw[j] / (x - xn[j]);
+            lj[j] = t / sw;
+            if (dj) dj[j] = lj[j] * (-1.0 / (x - xn[j]) + sw2 / sw);
+        }
+    }
+    // check the interpolated coefficients against the exact ones on every 4th order
+    double cmax = 0.0, dmax = 0.0, ce = 0.0, de = 0.0;
+    for (int a = 0; a < na; a += 4) {
+        const double* c = coef_h + (size_t)a * T;
+        const double* dc = coef_h + (size_t)(na + a) * T;
+        for (int q = 0; q < T; ++q) {
+            double vc = 0.0, vd = 0.0;
+            for (int j = 0; j < r; ++j) {
+                vc += pw[(size_t)a * rp + j] * tab[(size_t)j * T + q];
+                if (need_d) vd += pw[(size_t)(na + a) * rp + j] * tab[(size_t)j * T + q];
+            }
+            cmax = std::max(cmax, std::fabs(c[q]));
+            ce = std::max(ce, std::fabs(vc - c[q]));
+            if (need_d) {
+                dmax = std::max(dmax, std::fabs(dc[q]));
+                de = std::max(de, std::fabs(vd - dc[q]));
+            }
+        }
+    }
+    if (!(ce <= 1e-13 * cmax) || (need_d && !(de <= 1e-10 * std::max(dmax, 1e-300)))) return false;
+    *r_out = r;
+    *rp_out = rp;
+    return true;
+}
+
+// W_j = sum_k c_k(a_j) P_k (INT8 GEMM over the element-row slices) and Z'_j = W_j X.
+int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0, int r,
+                  const void* x_dev, int64_t b) {
+    if (int st = ensure_elem_slices(c)) return st;
+    const int S = c->es_slices;
+    const int T = 2 * c->l + 1;
+    const int64_t n = c->n, rows = pad_rows(n * n), kp = pad_k(2 * (int64_t)c->l), bp = kOzTileB;
+    FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
+    FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
+    FGB_CUDA(cudaMemcpyAsync(c->nd_tab.p, c->nd_h, tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    FGB_CUDA(cudaMemcpyAsync(c->nd_d0.p, c->nd_h + tab.size(), d0.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    FGB_CUDA(c->nd_bsl.ensure((size_t)S * bp * kp));
+    FGB_CUDA(c->nd_bex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
+    int* be = c->nd_bex.as<int>();
+    {  // node coefficient rows in the stacked term order (operand mode 4)
+        OzView v{c->nd_tab.as<double>(), T, 0, 0, 0, 0, r, (int)bp, 1, 2 * c->l, (int)kp, false};
+        v.tiled = 4;
+        v.l = c->l;
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->nd_bsl.as<int8_t>(), be,
+                                   reinterpret_cast<unsigned long long*>(be + bp), c->stream),
+                   3);
+    }
+    const size_t nn = (size_t)n * n;
+    FGB_CUDA(c->nd_w.ensure((size_t)r * nn * 8));
+    {
+        ProfScope ps(KC_I8GEMM, c->stream);
+        FGB_LAUNCH(launch_ozgemm(S, 0, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(), be,
+                                 (int)bp, (int)kp, c->nd_w.as<double>(), (int64_t)nn, 0, (int)nn, (int)rows, r,
+                                 c->stream),
+                   1);
+    }
+    FGB_LAUNCH(launch_add_diag(c->nd_w.as<double>(), (int)n, (int64_t)nn, c->nd_d0.as<double>(), r, c->stream), 1);
+    FGB_CUDA(c->nd_z.ensure((size_t)r * n * b * 16));
+    return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p);
+}
+
+// Copy the plan's tables into the pinned staging (after the previous call's uploads have read
+// it) and upload the interpolation weights; node_products uploads the rest from the same staging.
+int node_stage(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0,
+               const std::vector<double>& pw) {
+    const size_t need = tab.size() + d0.size() + pw.size();
+    if (c->nd_evt) FGB_CUDA(cudaEventSynchronize(c->nd_evt));
+    if (c->nd_h_cap < need) {
+        if (c->nd_h) cudaFreeHost(c->nd_h);
+        c->nd_h = nullptr;
+        c->nd_h_cap = 0;
+        FGB_CUDA(cudaMallocHost(&c->nd_h, need * 8));
+        c->nd_h_cap = need;
+    }
+    std::memcpy(c->nd_h, tab.data(), tab.size() * 8);
+    std::memcpy(c->nd_h + tab.size(), d0.data(), d0.size() * 8);
+    std::memcpy(c->nd_h + tab.size() + d0.size(), pw.data(), pw.size() * 8);
+    FGB_CUDA(c->nd_p.ensure(pw.size() * 8));
+    FGB_CUDA(cudaMemcpyAsync(c->nd_p.p, c->nd_h + tab.size() + d0.size(), pw.size() * 8, cudaMemcpyHostToDevice,
+                             c->stream));
+    return FGFRFT_OK;
+}
+
+// record that the staging may be reused once the uploads enqueued so far have run
+int node_staged(fgfrft_cache* c) {
+    if (!c->nd_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->nd_evt, cudaEventDisableTiming));
+    FGB_CUDA(cudaEventRecord(c->nd_evt, c->stream));
+    return FGFRFT_OK;
+}
+
+// Y (optional), loss, dL/da of an order sweep through the node route; false in *ran when the
+// sweep is not interpolable (the caller falls back).
+int mse_node_route(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_dev,
+                   int64_t b, void* y_dev, double* loss_dev, double* dlda_dev, bool need_d, bool* ran) {
+    *ran = false;
+    std::vector<double> tab, d0, pw;
+    int r = 0, rp = 0;
+    if (!node_plan(alphas, n_alpha, c->l, need_d, c->coef_h, tab, d0, pw, &r, &rp)) return FGFRFT_OK;
+    if (int st = node_stage(c, tab, d0, pw)) return st;
+    if (int st = node_products(c, tab, d0, r, x_dev, b)) return st;
+    if (int st = node_staged(c)) return st;
+    if (xc_dev && !need_d) return fail(FGFRFT_PARAMETER, "node route: the MSE form needs the derivative rows");
+    if (xc_dev)
+        if (int st = wait_xc(c)) return st;
+    FGB_CUDA(c->partial.ensure(node_partial_elems() * sizeof(double)));
+    ProfScope ps(KC_COMBINE, c->stream);
+    FGB_LAUNCH(launch_node_combine(c->nd_z.as<double>(), static_cast<const double*>(xc_dev), 2 * c->n * b, r, rp,
+                                   c->nd_p.as<double>(), n_alpha, static_cast<double*>(y_dev), c->partial.as<double>(),
+                                   1.0 / ((double)c->n * (double)b), loss_dev, dlda_dev, c->stream),
+               xc_dev ? 2 : 1);
+    *ran = true;
+    c->last_route = 2;
+    c->last_nodes = r;
+    return FGFRFT_OK;
+}
 
 int ensure_power_slices(fgfrft_cache* c) {
     const int S = oz_slices_default();
@@ -1021,6 +1257,13 @@ int fgfrft_cache_info(const fgfrft_cache* c, int64_t* n, int* l, uint64_t* finge
     return FGFRFT_OK;
 }
 
+int fgfrft_cache_route_info(const fgfrft_cache* c, int* route, int* nodes) {
+    if (int st = check_handle(c)) return st;
+    if (route) *route = c->last_route;
+    if (nodes) *nodes = c->last_nodes;
+    return FGFRFT_OK;
+}
+
 int fgfrft_cache_is_real(const fgfrft_cache* c, int* real) {
     if (int st = check_handle(c)) return st;
     if (real) *real = c->real ? 1 : 0;
@@ -1340,6 +1583,15 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
         return mse_int8_combine(c, coef, dc_dev, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
                                 c->s.as<double>(), static_cast<double*>(dlda_dev));
     }
+    if (use_node_route(c, n_alpha, b)) {
+        bool ran = false;
+        if (int st = mse_node_route(c, alphas, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
+                                    static_cast<double*>(dlda_dev), true, &ran))
+            return st;
+        if (ran) return FGFRFT_OK;
+    }
+    c->last_route = use_power_route(c, n_alpha) ? 1 : 0;
+    c->last_nodes = 0;
     if (use_power_route(c, n_alpha)) {
         FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
         if (int st = mse_power_route(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),

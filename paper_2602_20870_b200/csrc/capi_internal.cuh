@@ -154,6 +154,12 @@ cudaError_t launch_loss3(const double* part, int ctas, int n_alpha, double norm,
 cudaError_t launch_gram_s(const double* coef, const double* rg, int n_alpha, int l, double norm, double* s,
                           cudaStream_t st);
 size_t combine_partial_elems(int tp);
+size_t node_partial_elems();
+int node_max_terms();
+cudaError_t launch_add_diag(double* w, int n, int64_t stride, const double* d, int r, cudaStream_t stream);
+cudaError_t launch_node_combine(const double* zin, const double* xc, int64_t count, int r, int rp, const double* pc,
+                                int n_alpha, double* y, double* partial, double norm, double* loss, double* dlda,
+                                cudaStream_t stream);
 cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
                            double* loss, cudaStream_t stream);
@@ -288,6 +294,15 @@ struct fgfrft_cache {
     // internally, fgfrft_cache_info reports C64).
     bool api_c64 = false;
     DevBuf bx, bxc, by;
+    // Node route of order sweeps (real F): the stacked cache as element-row INT8 digit slices
+    // (built once), the per-call node coefficient table / interpolation weights, the node
+    // operators W_j and their products Z'_j = W_j X.
+    int last_route = -1, last_nodes = 0;  // route of the last sweep (fgfrft_cache_route_info)
+    int es_slices = 0;
+    DevBuf es, ee, erm, nd_tab, nd_p, nd_d0, nd_bsl, nd_bex, nd_w, nd_z;
+    double* nd_h = nullptr;  // pinned staging of the per-call node tables
+    size_t nd_h_cap = 0;
+    cudaEvent_t nd_evt = nullptr;
     size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
     int device = 0;
     uint64_t fingerprint = 0;

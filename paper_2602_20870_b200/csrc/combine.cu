@@ -692,3 +692,172 @@ cudaError_t launch_gram_s(const double* coef, const double* rg, int n_alpha, int
 }
 
 }  // namespace fgb
+
+namespace fgb {
+
+// ---------------------------------------------------------------------------------------------
+// Node route of an order sweep (capi.cu): the series operator is polynomial-interpolated in the
+// order over r Chebyshev nodes a_j of the sweep's interval, Q(a) = sum_j l_j(a) Q(a_j) + O(1e-15),
+// dQ/da(a) = sum_j l_j'(a) Q(a_j); with Z'_j = Q(a_j) X formed by one INT8 GEMM, per order a over
+// the flat (re, im) positions p of the N x B block:
+//   Y_a = sum_j P[a][j] Z'_j,  dY_a = sum_j P[A + a][j] Z'_j,
+//   loss_a = |Y_a - Xc|^2 / (N B),  dL/da = 2/(N B) Re<Y_a - Xc, dY_a>.
+// Warp w owns orders 8w..8w+7 of both Y and dY (coefficient fragments in registers), so the
+// residual and both reductions stay in the accumulators' lanes; 32-position chunks double
+// buffered through cp.async, two CTAs per SM. MSE = false: Y only (apply).
+constexpr int kNdMaxR = 48;
+constexpr int kNdP = 32;
+constexpr int kNdLd = 36;  // = 4 mod 16: the DMMA B-fragment loads are conflict free
+
+size_t node_smem_bytes(int rp) { return (2 * (size_t)rp * kNdLd + 2 * kNdP) * sizeof(double); }
+int node_max_terms() { return kNdMaxR; }
+
+template <bool MSE>
+__global__ void __launch_bounds__(256, 2)
+node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ xc, int64_t count, int r, int rp,
+                    const double* __restrict__ pc, int n_alpha, double* __restrict__ y, double* __restrict__ lpart,
+                    double* __restrict__ dpart) {
+    extern __shared__ __align__(16) double sm[];
+    double* zb = sm;                   // 2 x [rp][36]
+    double* xb = zb + 2 * rp * kNdLd;  // 2 x [32]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int a = 8 * warp + g;
+    const bool a_ok = a < n_alpha;
+    const int nks = rp / 4;
+    double cy[kNdMaxR / 4], cd[kNdMaxR / 4];
+#pragma unroll
+    for (int k = 0; k < kNdMaxR / 4; ++k) {
+        const int q = 4 * k + t;
+        cy[k] = (a_ok && q < r) ? pc[(int64_t)a * rp + q] : 0.0;
+        cd[k] = (MSE && a_ok && q < r) ? pc[(int64_t)(n_alpha + a) * rp + q] : 0.0;
+    }
+    for (int idx = tid; idx < (rp - r) * kNdLd; idx += 256) {  // padded terms stay zero
+        zb[r * kNdLd + idx] = 0.0;
+        zb[(rp + r) * kNdLd + idx] = 0.0;
+    }
+    const int64_t nchunks = (count + kNdP - 1) / kNdP;
+    auto stage = [&](int64_t ch, int buf) {
+        const int64_t p0 = ch * kNdP;
+        const int pv = (int)((count - p0) < kNdP ? (count - p0) : kNdP);
+        double* zc = zb + buf * rp * kNdLd;
+        for (int idx = tid; idx < r * (kNdP / 2); idx += 256) {
+            const int q = idx / (kNdP / 2), c2 = idx - q * (kNdP / 2);
+            const bool v = 2 * c2 < pv;
+            cp_async16(zc + q * kNdLd + 2 * c2, zin + (int64_t)q * count + p0 + (v ? 2 * c2 : 0), v);
+        }
+        if (MSE && tid < kNdP / 2)
+            cp_async16(xb + buf * kNdP + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
+    };
+    double lacc = 0.0, gacc = 0.0;
+    int buf = 0;
+    if (blockIdx.x < nchunks) stage(blockIdx.x, 0);
+    cp_async_commit();
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, buf ^= 1) {
+        const int64_t p0 = ch * kNdP;
+        const int pv = (int)((count - p0) < kNdP ? (count - p0) : kNdP);
+        cp_async_wait<0>();
+        __syncthreads();
+        if (ch + gridDim.x < nchunks) stage(ch + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        const double* zc = zb + buf * rp * kNdLd;
+        const double* xs = xb + buf * kNdP;
+        double yacc[4][2], dacc[4][2];
+#pragma unroll
+        for (int pb = 0; pb < 4; ++pb) yacc[pb][0] = yacc[pb][1] = dacc[pb][0] = dacc[pb][1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < kNdMaxR / 4; ++k) {
+            if (k < nks) {
+                const double* zrow = zc + (4 * k + t) * kNdLd + g;
+#pragma unroll
+                for (int pb = 0; pb < 4; ++pb) {
+                    const double zv = zrow[8 * pb];
+                    dmma884(yacc[pb][0], yacc[pb][1], cy[k], zv);
+                    if (MSE) dmma884(dacc[pb][0], dacc[pb][1], cd[k], zv);
+                }
+            }
+        }
+#pragma unroll
+        for (int pb = 0; pb < 4; ++pb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int p = 8 * pb + 2 * t + e;
+                const bool ok = p < pv && a_ok;
+                if (y && ok) y[(int64_t)a * count + p0 + p] = yacc[pb][e];
+                if (MSE) {
+                    const double res = ok ? yacc[pb][e] - xs[p] : 0.0;
+                    lacc = fma(res, res, lacc);
+                    gacc = fma(res, ok ? dacc[pb][e] : 0.0, gacc);
+                }
+            }
+    }
+    cp_async_wait<0>();
+    if (!MSE) return;
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, 1);
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, 2);
+    gacc += __shfl_xor_sync(0xffffffffu, gacc, 1);
+    gacc += __shfl_xor_sync(0xffffffffu, gacc, 2);
+    if (t == 0) {
+        lpart[(int64_t)blockIdx.x * kCbA + a] = lacc;
+        dpart[(int64_t)blockIdx.x * kCbA + a] = gacc;
+    }
+}
+
+// loss[a] = norm sum_cta lpart, dlda[a] = 2 norm sum_cta dpart (fixed order)
+__global__ void node_reduce_kernel(const double* __restrict__ lpart, const double* __restrict__ dpart, int ctas,
+                                   int n_alpha, double norm, double* __restrict__ loss, double* __restrict__ dlda) {
+    const int a = threadIdx.x;
+    if (a >= n_alpha) return;
+    double l = 0.0, d = 0.0;
+    for (int c = 0; c < ctas; ++c) {
+        l += lpart[(int64_t)c * kCbA + a];
+        d += dpart[(int64_t)c * kCbA + a];
+    }
+    loss[a] = norm * l;
+    dlda[a] = 2.0 * norm * d;
+}
+
+// W_j[i, i] += d[j] for r row-stacked n x n operators (the identity term of the series)
+__global__ void add_diag_kernel(double* __restrict__ w, int n, int64_t stride, const double* __restrict__ d, int r) {
+    const int j = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && j < r) w[(int64_t)j * stride + (int64_t)i * n + i] += d[j];
+}
+
+size_t node_partial_elems() { return 2 * (size_t)(2 * FGFRFT_SMS) * kCbA; }
+
+cudaError_t launch_add_diag(double* w, int n, int64_t stride, const double* d, int r, cudaStream_t stream) {
+    add_diag_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)r), 256, 0, stream>>>(w, n, stride, d, r);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_node_combine(const double* zin, const double* xc, int64_t count, int r, int rp, const double* pc,
+                                int n_alpha, double* y, double* partial, double norm, double* loss, double* dlda,
+                                cudaStream_t stream) {
+    if (n_alpha > kCbA || rp > kNdMaxR || rp % 4 || r > rp) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(node_combine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)node_smem_bytes(kNdMaxR));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(node_combine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)node_smem_bytes(kNdMaxR));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int64_t nch = (count + kNdP - 1) / kNdP;
+    const int ctas = (int)(nch < 2 * FGFRFT_SMS ? nch : 2 * FGFRFT_SMS);
+    const size_t smem = node_smem_bytes(rp);
+    if (!xc) {
+        node_combine_kernel<false><<<ctas, 256, smem, stream>>>(zin, nullptr, count, r, rp, pc, n_alpha, y, nullptr,
+                                                                nullptr);
+        return cudaGetLastError();
+    }
+    double* lp = partial;
+    double* dp = partial + (size_t)ctas * kCbA;
+    node_combine_kernel<true><<<ctas, 256, smem, stream>>>(zin, xc, count, r, rp, pc, n_alpha, y, lp, dp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    node_reduce_kernel<<<1, kCbA, 0, stream>>>(lp, dp, ctas, n_alpha, norm, loss, dlda);
+    return cudaGetLastError();
+}
+
+}  // namespace fgb

@@ -27,6 +27,9 @@ struct OzView {
                      //    ra = 0 (A side): A'(r, 2k + e) = e ? -Im z : Re z
                      //    ra = 1 (B side, rows 2j + c): B'(2j + c, 2k + e) = (Re, Im; Im, -Re)[c][e]
                      //    ka = 1: conjugate z first
+                     // 6: element rows of the stacked cache (the basis synthesis GEMM): row
+                     //    e = i + j n (rv = n^2, tp2 = n), K term kk < L: P_(kk+1)(i, j), L <= kk < 2L:
+                     //    P_(kk-L+1)(j, i); one batch block (nb = 1, rp = padded n^2)
     int nt = 0;      // tiles per side of a tiled slab
     int l = 0, tp2 = 0;  // modes 3 / 4: L and the padded term count (64 or 128)
 };

@@ -157,6 +157,14 @@ __device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
         if (!v.ra) return e ? -zi : zr;
         return c == 0 ? (e ? zi : zr) : (e ? -zr : zi);
     }
+    if (v.tiled == 6) {  // element rows of the stacked cache: row e = i + j n, K term kk (see OzView)
+        if (row >= v.rv || k >= v.kv || k >= 2 * v.l) return 0.0;
+        const int n = v.tp2, i = row % n, j = row / n;
+        const bool tr = k >= v.l;
+        const int slab = tr ? k - v.l : k;
+        const int a = tr ? j : i, b = tr ? i : j;
+        return v.src[slab * v.sbatch + tile_base(a >> 5, b >> 5, v.nt) + swz(a & 31, b & 31)];
+    }
     if (v.tiled == 3) {  // rv = n (signal rows), rows beyond n * tp2 are padding
         const int i = row / v.tp2, kk = row - i * v.tp2;
         if (i >= v.rv || kk >= 2 * v.l || k >= v.kv) return 0.0;

@@ -623,3 +623,37 @@ def test_concurrent_handles_from_threads():
     for key in ("a", "a2"):
         assert np.array_equal(out[key][0], ref_a[0]) and np.array_equal(out[key][1], ref_a[1])
     assert np.array_equal(out["b"], ref_b)
+
+
+@pytest.mark.parametrize("n,l,b,lo,hi,na", [(512, 16, 40, 0.0, 2.0, 64), (600, 24, 33, -0.7, 0.4, 16),
+                                             (520, 12, 64, 1.0, 4.5, 20), (1024, 64, 48, 0.2, 0.3, 32),
+                                             (512, 10, 40, -3.0, 3.0, 40)])
+def test_node_route_sweeps_match_oracle(n, l, b, lo, hi, na):
+    """Order sweeps on a real F through the node route (Chebyshev interpolation of Q(a) over the
+    sweep's interval, INT8 node operators; wide intervals fall back to the power route) against
+    the oracle: F^a X, Q(a)^H X, loss and dL/da within 1e-10."""
+    f = prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 6.0 / n, n + l)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l, powers=o.slabs)
+    rng = np.random.default_rng(n + na)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    alphas = list(np.linspace(lo, hi, na))
+    loss, dl, ym = fg.mse_step(g, alphas, x, xc, want_y=True)
+    route, nodes = g.route_info()
+    assert route in (1, 2)
+    ys = fg.apply_series(g, alphas, x)
+    yi = fg.apply_series(g, alphas, x, inverse=True)
+    for i in range(0, na, max(1, na // 8)):
+        a = alphas[i]
+        q = O.fgfrft_matrix(o, a)
+        assert rel(ys[i], q @ x) <= 1e-10
+        assert rel(yi[i], q.T @ x) <= 1e-10
+        assert rel(ym[i], q @ x) <= 1e-10
+        lr, dr, _ = O.dlda_mse(o, a, x, xc)
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        _, dc = O.sinc_coeffs(a, l)
+        s_ref = O.power_dots(o, (2.0 * (q @ x - xc) / (n * b)) @ x.conj().T)
+        assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s_ref))
+    if hi - lo <= 2.0:
+        assert route == 2 and nodes == int(np.ceil(12 + 10 * (hi - lo)))
