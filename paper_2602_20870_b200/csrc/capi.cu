@@ -86,8 +86,6 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
     if (c->coef_evt) FGB_CUDA(cudaEventSynchronize(c->coef_evt));
     if (c->coef_h_cap < count) {
         if (c->coef_h) cudaFreeHost(c->coef_h);
-    if (c->nd_h) cudaFreeHost(c->nd_h);
-    if (c->nd_evt) cudaEventDestroy(c->nd_evt);
         c->coef_h = nullptr;
         c->coef_h_cap = 0;
         FGB_CUDA(cudaMallocHost(&c->coef_h, count * sizeof(double)));
@@ -232,6 +230,8 @@ void destroy_cache(fgfrft_cache* c) {
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
+    if (c->nd_h) cudaFreeHost(c->nd_h);
+    if (c->nd_evt) cudaEventDestroy(c->nd_evt);
     if (c->xc_evt) cudaEventDestroy(c->xc_evt);
     if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
     if (c->slabs) cudaFree(c->slabs);
@@ -531,14 +531,14 @@ int wait_xc(fgfrft_cache* c);
 //
 // For an order sweep on [lo, hi], Q(a) = sum_k c_k(a) P_k is an entire function of a, so it is
 // interpolated to rounding by a degree-(r-1) polynomial through r Chebyshev nodes a_j of the
-// interval (r = 32 for a width-2 sweep, measured 1e-14 on the coefficients, 2e-12 on their
-// derivatives): F^a X = sum_j l_j(a) W_j X and dF^a/da X = sum_j l_j'(a) W_j X with the node
+// interval (r = 19 for a width-2 sweep: 4e-15 on the coefficients, 2e-12 on their derivatives,
+// checked per call): F^a X = sum_j l_j(a) W_j X and dF^a/da X = sum_j l_j'(a) W_j X with the node
 // operators W_j = Q(a_j). The W_j come from ONE INT8 GEMM over the cache's 2L terms (element-row
 // digit slices of the stacked cache x the node coefficient rows), the products W_j X from a
 // second one, and the per-order Y, dY, loss and dL/da from one DMMA pass over the r products
 // (node_combine_kernel) -- r products instead of the power route's 2L. Every call re-plans
-// (nodes, barycentric weights, an interpolation check against the exact coefficients on a
-// subset of the orders); a failed check or r > 48 falls back to the power route.
+// (memoised on the order set): nodes, barycentric weights, an interpolation check against the
+// exact coefficients of every order; no r <= 48 passing the check falls back to the power route.
 bool use_node_route(const fgfrft_cache* c, int n_alpha, int64_t b) {
     static const int mode = [] {
         const char* e = std::getenv("FGFRFT_ROUTE");
@@ -570,9 +570,12 @@ int ensure_elem_slices(fgfrft_cache* c) {
 }
 
 // Plan: nodes, node coefficient rows (r x T), interpolation weights P = [l_j(a); l_j'(a)] (rows x rp).
-// coef_h holds the exact [c | c'] tables of the orders (upload_coefs). false: not interpolable.
-bool node_plan(const double* alphas, int na, int l, bool need_d, const double* coef_h, std::vector<double>& tab,
-               std::vector<double>& d0, std::vector<double>& pw, int* r_out, int* rp_out) {
+// coef_h holds the exact [c | c'] tables of the orders (upload_coefs). The node count is the
+// smallest r (from an estimate upward) whose interpolated coefficients match the exact ones on
+// every order to 4e-15 of the largest coefficient (2e-12 for the derivatives) -- about 9 + 5w for
+// a width-w sweep (19 for [0, 2]). false: not interpolable within node_max_terms() nodes.
+static bool node_plan_r(const double* alphas, int na, int l, bool need_d, const double* coef_h, int r,
+                        std::vector<double>& tab, std::vector<double>& d0, std::vector<double>& pw, int* rp_out) {
     const int T = 2 * l + 1;
     double lo = alphas[0], hi = alphas[0];
     for (int a = 1; a < na; ++a) {
@@ -580,9 +583,6 @@ bool node_plan(const double* alphas, int na, int l, bool need_d, const double* c
         hi = std::max(hi, alphas[a]);
     }
     const double w = hi - lo;
-    if (!(w > 1e-9)) return false;
-    const int r = (int)std::ceil(12.0 + 10.0 * w);
-    if (r > node_max_terms()) return false;
     const int rp = (r + 3) / 4 * 4;
     const double mid = 0.5 * (lo + hi), half = 0.5 * w;
     std::vector<double> xn((size_t)r), bw((size_t)r);
@@ -632,29 +632,62 @@ bool node_plan(const double* alphas, int na, int l, bool need_d, const double* c
             if (dj) dj[j] = lj[j] * (-1.0 / (x - xn[j]) + sw2 / sw);
         }
     }
-    // check the interpolated coefficients against the exact ones on every 4th order
+    // check the interpolated coefficients against the exact ones on every order
     double cmax = 0.0, dmax = 0.0, ce = 0.0, de = 0.0;
-    for (int a = 0; a < na; a += 4) {
+    std::vector<double> vc((size_t)T), vd((size_t)T);
+    for (int a = 0; a < na; ++a) {
         const double* c = coef_h + (size_t)a * T;
         const double* dc = coef_h + (size_t)(na + a) * T;
-        for (int q = 0; q < T; ++q) {
-            double vc = 0.0, vd = 0.0;
-            for (int j = 0; j < r; ++j) {
-                vc += pw[(size_t)a * rp + j] * tab[(size_t)j * T + q];
-                if (need_d) vd += pw[(size_t)(na + a) * rp + j] * tab[(size_t)j * T + q];
+        std::fill(vc.begin(), vc.end(), 0.0);
+        std::fill(vd.begin(), vd.end(), 0.0);
+        for (int j = 0; j < r; ++j) {
+            const double* tj = &tab[(size_t)j * T];
+            const double pl = pw[(size_t)a * rp + j], pd = need_d ? pw[(size_t)(na + a) * rp + j] : 0.0;
+            for (int q = 0; q < T; ++q) {
+                vc[q] += pl * tj[q];
+                vd[q] += pd * tj[q];
             }
+        }
+        for (int q = 0; q < T; ++q) {
             cmax = std::max(cmax, std::fabs(c[q]));
-            ce = std::max(ce, std::fabs(vc - c[q]));
+            ce = std::max(ce, std::fabs(vc[q] - c[q]));
             if (need_d) {
                 dmax = std::max(dmax, std::fabs(dc[q]));
-                de = std::max(de, std::fabs(vd - dc[q]));
+                de = std::max(de, std::fabs(vd[q] - dc[q]));
             }
         }
     }
-    if (!(ce <= 1e-13 * cmax) || (need_d && !(de <= 1e-10 * std::max(dmax, 1e-300)))) return false;
-    *r_out = r;
     *rp_out = rp;
-    return true;
+    return ce <= 4e-15 * cmax && (!need_d || de <= 2e-12 * std::max(dmax, 1e-300));
+}
+
+bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* r_out, int* rp_out) {
+    auto& p = c->nd_plan;
+    if (p.need_d == need_d && p.alphas.size() == (size_t)na &&
+        !std::memcmp(p.alphas.data(), alphas, (size_t)na * sizeof(double))) {
+        *r_out = p.r;
+        *rp_out = p.rp;
+        return p.ok;
+    }
+    p.alphas.assign(alphas, alphas + na);
+    p.need_d = need_d;
+    p.ok = false;
+    double lo = alphas[0], hi = alphas[0];
+    for (int a = 1; a < na; ++a) {
+        lo = std::min(lo, alphas[a]);
+        hi = std::max(hi, alphas[a]);
+    }
+    const double w = hi - lo;
+    if (!(w > 1e-9)) return false;
+    for (int r = std::max(6, (int)std::floor(8.0 + 4.2 * w)); r <= node_max_terms(); ++r)
+        if (node_plan_r(alphas, na, c->l, need_d, c->coef_h, r, p.tab, p.d0, p.pw, &p.rp)) {
+            p.r = r;
+            p.ok = true;
+            break;
+        }
+    *r_out = p.r;
+    *rp_out = p.rp;
+    return p.ok;
 }
 
 // W_j = sum_k c_k(a_j) P_k (INT8 GEMM over the element-row slices) and Z'_j = W_j X.
@@ -728,11 +761,11 @@ int node_staged(fgfrft_cache* c) {
 int mse_node_route(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_dev,
                    int64_t b, void* y_dev, double* loss_dev, double* dlda_dev, bool need_d, bool* ran) {
     *ran = false;
-    std::vector<double> tab, d0, pw;
     int r = 0, rp = 0;
-    if (!node_plan(alphas, n_alpha, c->l, need_d, c->coef_h, tab, d0, pw, &r, &rp)) return FGFRFT_OK;
-    if (int st = node_stage(c, tab, d0, pw)) return st;
-    if (int st = node_products(c, tab, d0, r, x_dev, b)) return st;
+    if (!node_plan(c, alphas, n_alpha, need_d, &r, &rp)) return FGFRFT_OK;
+    const auto& p = c->nd_plan;
+    if (int st = node_stage(c, p.tab, p.d0, p.pw)) return st;
+    if (int st = node_products(c, p.tab, p.d0, r, x_dev, b)) return st;
     if (int st = node_staged(c)) return st;
     if (xc_dev && !need_d) return fail(FGFRFT_PARAMETER, "node route: the MSE form needs the derivative rows");
     if (xc_dev)

@@ -303,6 +303,11 @@ struct fgfrft_cache {
     double* nd_h = nullptr;  // pinned staging of the per-call node tables
     size_t nd_h_cap = 0;
     cudaEvent_t nd_evt = nullptr;
+    struct NodePlan {  // memoised plan of the last sweep (a pure function of the orders)
+        std::vector<double> alphas, tab, d0, pw;
+        bool need_d = false, ok = false;
+        int r = 0, rp = 0;
+    } nd_plan;
     size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
     int device = 0;
     uint64_t fingerprint = 0;
