@@ -340,39 +340,53 @@ def main():
     route, nodes = cache.route_info()
     power_route = i8_n > 0
     if power_route and route == 2:
-        # Node route: W_j = Q(a_j) for r Chebyshev nodes by one INT8 GEMM over the 2L terms
-        # (n^2 element rows x r node rows x K = 2L), then Z'_j = W_j X (r n x 2B x n), both as
-        # S(S+1)/2 int8 digit-product GEMMs; node_combine: Y and dY rows (2 A x r x 2nB DMMA flops
-        # each) with the loss and dL/da.
+        # Node route. Two INT8 Ozaki GEMMs (S(S+1)/2 digit products each):
+        #  * node operators W_j = Q(a_j), j < r: n^2 element rows of the sliced cache (K = 2L terms)
+        #    x r node coefficient rows. A skinny GEMM (r <= 48 output columns): bound by streaming
+        #    the S-digit element-row slices (S * n^2 * 2L bytes) and writing W (r n^2 doubles);
+        #  * node products Z'_j = W_j X (r n x 2B x n): tensor-bound.
+        # node_combine: Y rows (2 A r 2nB DMMA flops) + the node Gram [Z'; Xc][Z'; Xc]^T.
         S = int(L_.fgfrft_int8_digits())
         products = S * (S + 1) // 2
         r = nodes
+        nodeop_ms, nodeop_n = prof["node_operators"]
         fp_basis = 2.0 * n * n * r * (2 * L)
         fp_prod = 2.0 * (r * n) * (2 * b) * n
-        fp64eq = fp_basis + fp_prod
-        i8_ops = fp64eq * products
-        achieved = i8_ops * args.steps / (i8_ms * 1e-3) / 1e12
+        basis_bytes = float(S * n * n * 2 * L + r * n * n * 8)
+        basis_cache_bytes = float((L if real else 2 * L) * n * n * (8 if real else 16) + r * n * n * 8)
+        prod_tops = fp_prod * products * args.steps / (i8_ms * 1e-3) / 1e12
+        basis_gbs = basis_bytes * args.steps / (nodeop_ms * 1e-3) / 1e9
         cb_ms, cb_n = prof["combine"]
-        cb_flops = 2 * (2.0 * A * r * 2 * n * b)
-        traffic = ncu_traffic("void ozgemm_kernel<6, 1, 2>")
-        roof = {"bound": "tensor",
-                "kernel": f"ozgemm_kernel<{S},0,1> + <{S},1,2> (tcgen05.mma kind::i8, TMEM digit accumulators)",
-                "achieved": achieved, "peak": peaks["int8_tops"], "unit": "TOPS",
-                "frac": achieved / peaks["int8_tops"], "traffic": traffic,
-                "traffic_note": ("bytes per launch of the product GEMM, DRAM read + write from the committed "
-                                 "ncu --set full capture"),
-                "peak_source": peaks["int8_src"],
+        cb_flops = 2.0 * A * r * 2 * n * b + 2.0 * (r + 1) * (r + 2) / 2 * 2 * n * b
+        traffic = ncu_traffic("void ozgemm_kernel<6, 0, 1>")
+        hbm_peak = peaks["hbm_gbs"]
+        roof = {"bound": "hbm",
+                "kernel": f"ozgemm_kernel<{S},0,1> (node operators: tcgen05.mma kind::i8 over the element-row "
+                          f"digit slices of the cache, r = {r} output columns)",
+                "achieved": basis_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": basis_gbs / hbm_peak,
+                "traffic": traffic,
+                "traffic_note": "DRAM read + write per launch of the node-operator GEMM (ncu --set full capture)",
+                "peak_source": peaks["hbm_src"],
+                "algorithmic": (f"per launch: S*N^2*2L digit bytes of the element-row slices read + r*N^2*8 "
+                                f"bytes of W written = {basis_bytes:.4g} B ({basis_cache_bytes:.4g} B counting "
+                                f"the FP64 cache itself instead of its digits)"),
                 "route": f"node interpolation, r = {r} Chebyshev nodes on [{alphas.min():.3g}, {alphas.max():.3g}]",
-                "algorithmic": (f"per step 2*N^2*r*2L (node operators) + 2*(r*N)*(2B)*N (W_j X) FP64-equivalent "
-                                f"flops = {fp64eq:.4g}, as {products} int8 digit-product GEMMs (Ozaki scheme, "
-                                f"{S} base-254 digits)"),
-                "fp64_equivalent_tflops": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12,
-                "fp64_equivalent_frac_of_dmma_peak": fp64eq * args.steps / (i8_ms * 1e-3) / 1e12 / peaks["fp64_tflops"],
-                "dmma_peak_tflops": peaks["fp64_tflops"],
-                "launches_timed": i8_n, "share_of_step": shares,
+                "share_of_step": shares,
+                "node_operator_gemm": {"ms_per_step": nodeop_ms / args.steps, "gbs": basis_gbs,
+                                       "gbs_vs_fp64_cache_bytes": basis_cache_bytes * args.steps
+                                       / (nodeop_ms * 1e-3) / 1e9,
+                                       "fp64_equivalent_flops": fp_basis},
+                "node_product_gemm": {"kernel": f"ozgemm_kernel<{S},1,2>", "bound": "tensor",
+                                      "ms_per_step": i8_ms / args.steps, "achieved_tops": prod_tops,
+                                      "peak_tops": peaks["int8_tops"], "frac": prod_tops / peaks["int8_tops"],
+                                      "peak_source": peaks["int8_src"],
+                                      "algorithmic": f"2*(r*N)*(2B)*N = {fp_prod:.4g} FP64-equivalent flops x "
+                                                     f"{products} digit products",
+                                      "fp64_equivalent_tflops": fp_prod * args.steps / (i8_ms * 1e-3) / 1e12,
+                                      "dmma_peak_tflops": peaks["fp64_tflops"]},
                 "combine_kernel": {"ms_per_step": cb_ms / args.steps, "flops_per_step": cb_flops,
                                    "tflops": cb_flops * args.steps / (cb_ms * 1e-3) / 1e12,
-                                   "form": "Y = P_C Z', dY = P_D Z' (DMMA) + loss and dL/da",
+                                   "form": "Y = P_C Z' (DMMA) + loss; dL/da from the node Gram of [Z'; Xc]",
                                    "peak_dmma_tflops": peaks["fp64_tflops"]}}
     elif power_route:
         S = int(L_.fgfrft_int8_digits())
@@ -505,7 +519,8 @@ def main():
             "roofline": roof,
             "route": (f"node interpolation: Q(a) through r = {nodes} Chebyshev nodes of the order interval; the "
                       "node operators W_j by one INT8 tensor-core Ozaki GEMM over the cache's 2L terms, Z'_j = W_j X "
-                      "by a second, then Y, dY, loss and dL/da for every order by one DMMA pass"
+                      "by a second, then Y and the loss of every order by one DMMA pass that also forms the node Gram, "
+                      "from which dL/da follows for every order"
                       if route == 2 else
                       "power products: Z = F^k X by one INT8 tensor-core Ozaki GEMM over the stacked cache, "
                       "then per-order combination + MSE + dL/da on DMMA" if power_route else

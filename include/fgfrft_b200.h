@@ -93,7 +93,7 @@ uint64_t fgfrft_launch_count(void);
 /*
  * Per-kernel-class device timing (CUDA events on the launching stream), for benchmarks:
  * classes 0 synthesis, 1 DMMA GEMM, 2 power dots, 3 elementwise, 4 INT8 tensor-core GEMM,
- * 5 operand slicing, 6 series combine, 7 reserved. fgfrft_profile_read waits for the recorded
+ * 5 operand slicing, 6 series combine, 7 node operators (order-sweep node route). fgfrft_profile_read waits for the recorded
  * events, writes total ms and launch counts per class (arrays of 8) and optionally resets.
  */
 int fgfrft_profile_enable(int on);

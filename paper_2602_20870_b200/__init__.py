@@ -194,7 +194,7 @@ def launch_count() -> int:
 ENGINE_AUTO, ENGINE_DMMA, ENGINE_INT8, ENGINE_INT8_COMBINE = 0, 1, 2, 3
 
 KERNEL_CLASSES = ("synthesis", "dmma_zgemm", "power_dots", "elementwise", "int8_gemm", "slicing", "combine",
-                  "reserved")
+                  "node_operators")
 
 
 def profile_enable(on: bool = True) -> None:

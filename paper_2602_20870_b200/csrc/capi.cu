@@ -716,7 +716,7 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
     const size_t nn = (size_t)n * n;
     FGB_CUDA(c->nd_w.ensure((size_t)r * nn * 8));
     {
-        ProfScope ps(KC_I8GEMM, c->stream);
+        ProfScope ps(KC_NODEOP, c->stream);
         FGB_LAUNCH(launch_ozgemm(S, 0, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(), be,
                                  (int)bp, (int)kp, c->nd_w.as<double>(), (int64_t)nn, 0, (int)nn, (int)rows, r,
                                  c->stream),

@@ -183,7 +183,7 @@ extern std::atomic<uint64_t> g_launches;
 // Optional per-kernel-class timing with CUDA events recorded on the launching stream
 // (fgfrft_profile_*): bench.py uses it to time the dominant kernel inside its timed region.
 enum KernelClass {
-    KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_I8GEMM = 4, KC_SLICE = 5, KC_COMBINE = 6, KC_COUNT = 8
+    KC_SYNTH = 0, KC_GEMM = 1, KC_DOTS = 2, KC_ELEMWISE = 3, KC_I8GEMM = 4, KC_SLICE = 5, KC_COMBINE = 6, KC_NODEOP = 7, KC_COUNT = 8
 };
 struct ProfRec {
     int cls;

@@ -700,55 +700,63 @@ namespace fgb {
 // order over r Chebyshev nodes a_j of the sweep's interval, Q(a) = sum_j l_j(a) Q(a_j) + O(1e-15),
 // dQ/da(a) = sum_j l_j'(a) Q(a_j); with Z'_j = Q(a_j) X formed by one INT8 GEMM, per order a over
 // the flat (re, im) positions p of the N x B block:
-//   Y_a = sum_j P[a][j] Z'_j,  dY_a = sum_j P[A + a][j] Z'_j,
-//   loss_a = |Y_a - Xc|^2 / (N B),  dL/da = 2/(N B) Re<Y_a - Xc, dY_a>.
-// Warp w owns orders 8w..8w+7 of both Y and dY (coefficient fragments in registers), so the
-// residual and both reductions stay in the accumulators' lanes; 32-position chunks double
-// buffered through cp.async, two CTAs per SM. MSE = false: Y only (apply).
+//   Y_a = sum_j P[a][j] Z'_j,  loss_a = |Y_a - Xc|^2 / (N B),
+//   dL/da = 2/(N B) <Y_a - Xc, dY_a> = 2/(N B) sum_j P[A + a][j] ((G P[a])_j - h_j)
+// with the node Gram G = Z'^T Z' (r x r) and h = Z'^T Xc: dY is never formed. Warp w owns orders
+// 8w..8w+7 of Y (coefficient fragments in registers), so the residual and the loss stay in the
+// accumulators' lanes; the Gram [Z'; Xc] [Z'; Xc]^T (Xc staged as row r of the chunk) is
+// accumulated by upper-triangular 8x8 DMMA tiles, warp w taking positions 4w..4w+3 of every
+// chunk. 32-position chunks double buffered through cp.async, two CTAs per SM. MSE = false: Y only.
 constexpr int kNdMaxR = 48;
 constexpr int kNdP = 32;
-constexpr int kNdLd = 36;  // = 4 mod 16: the DMMA B-fragment loads are conflict free
+constexpr int kNdLd = 36;                          // = 4 mod 16: the DMMA fragment loads are conflict free
+constexpr int kNdT = (kNdMaxR + 1 + 7) / 8;        // 8-row tiles of [Z'; Xc]
+constexpr int kNdPairs = kNdT * (kNdT + 1) / 2;    // upper-triangular tile pairs of the Gram
 
-size_t node_smem_bytes(int rp) { return (2 * (size_t)rp * kNdLd + 2 * kNdP) * sizeof(double); }
+__host__ __device__ inline int node_rows8(int r) { return (r + 1 + 7) / 8 * 8; }
+size_t node_smem_bytes(int r) { return 2 * (size_t)node_rows8(r) * kNdLd * sizeof(double); }
 int node_max_terms() { return kNdMaxR; }
 
-template <bool MSE>
+template <bool MSE, int T>  // T = node_rows8(r) / 8
 __global__ void __launch_bounds__(256, 2)
 node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ xc, int64_t count, int r, int rp,
                     const double* __restrict__ pc, int n_alpha, double* __restrict__ y, double* __restrict__ lpart,
-                    double* __restrict__ dpart) {
+                    double* __restrict__ gpart) {
     extern __shared__ __align__(16) double sm[];
-    double* zb = sm;                   // 2 x [rp][36]
-    double* xb = zb + 2 * rp * kNdLd;  // 2 x [32]
+    constexpr int r8 = 8 * T, t8 = T;
+    double* zb = sm;  // 2 x [r8][36]: rows 0..r-1 Z', row r Xc, the rest zero
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int a = 8 * warp + g;
     const bool a_ok = a < n_alpha;
     const int nks = rp / 4;
-    double cy[kNdMaxR / 4], cd[kNdMaxR / 4];
+    double cy[2 * T];
 #pragma unroll
-    for (int k = 0; k < kNdMaxR / 4; ++k) {
+    for (int k = 0; k < 2 * T; ++k) {
         const int q = 4 * k + t;
         cy[k] = (a_ok && q < r) ? pc[(int64_t)a * rp + q] : 0.0;
-        cd[k] = (MSE && a_ok && q < r) ? pc[(int64_t)(n_alpha + a) * rp + q] : 0.0;
     }
-    for (int idx = tid; idx < (rp - r) * kNdLd; idx += 256) {  // padded terms stay zero
-        zb[r * kNdLd + idx] = 0.0;
-        zb[(rp + r) * kNdLd + idx] = 0.0;
+    const int zrow0 = MSE ? r + 1 : r;
+    for (int idx = tid; idx < (r8 - zrow0) * kNdLd; idx += 256) {  // padded rows stay zero
+        zb[zrow0 * kNdLd + idx] = 0.0;
+        zb[(r8 + zrow0) * kNdLd + idx] = 0.0;
     }
     const int64_t nchunks = (count + kNdP - 1) / kNdP;
     auto stage = [&](int64_t ch, int buf) {
         const int64_t p0 = ch * kNdP;
         const int pv = (int)((count - p0) < kNdP ? (count - p0) : kNdP);
-        double* zc = zb + buf * rp * kNdLd;
+        double* zc = zb + buf * r8 * kNdLd;
         for (int idx = tid; idx < r * (kNdP / 2); idx += 256) {
             const int q = idx / (kNdP / 2), c2 = idx - q * (kNdP / 2);
             const bool v = 2 * c2 < pv;
             cp_async16(zc + q * kNdLd + 2 * c2, zin + (int64_t)q * count + p0 + (v ? 2 * c2 : 0), v);
         }
         if (MSE && tid < kNdP / 2)
-            cp_async16(xb + buf * kNdP + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
+            cp_async16(zc + r * kNdLd + 2 * tid, xc + p0 + (2 * tid < pv ? 2 * tid : 0), 2 * tid < pv);
     };
-    double lacc = 0.0, gacc = 0.0;
+    double lacc = 0.0;
+    double gacc[T * (T + 1) / 2][2];
+#pragma unroll
+    for (int i = 0; i < T * (T + 1) / 2; ++i) gacc[i][0] = gacc[i][1] = 0.0;
     int buf = 0;
     if (blockIdx.x < nchunks) stage(blockIdx.x, 0);
     cp_async_commit();
@@ -759,21 +767,27 @@ node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ x
         __syncthreads();
         if (ch + gridDim.x < nchunks) stage(ch + gridDim.x, buf ^ 1);
         cp_async_commit();
-        const double* zc = zb + buf * rp * kNdLd;
-        const double* xs = xb + buf * kNdP;
-        double yacc[4][2], dacc[4][2];
+        const double* zc = zb + buf * r8 * kNdLd;
+        const double* xs = zc + r * kNdLd;
+        double yacc[4][2];
 #pragma unroll
-        for (int pb = 0; pb < 4; ++pb) yacc[pb][0] = yacc[pb][1] = dacc[pb][0] = dacc[pb][1] = 0.0;
+        for (int pb = 0; pb < 4; ++pb) yacc[pb][0] = yacc[pb][1] = 0.0;
 #pragma unroll
-        for (int k = 0; k < kNdMaxR / 4; ++k) {
+        for (int k = 0; k < 2 * T; ++k) {
             if (k < nks) {
                 const double* zrow = zc + (4 * k + t) * kNdLd + g;
 #pragma unroll
-                for (int pb = 0; pb < 4; ++pb) {
-                    const double zv = zrow[8 * pb];
-                    dmma884(yacc[pb][0], yacc[pb][1], cy[k], zv);
-                    if (MSE) dmma884(dacc[pb][0], dacc[pb][1], cd[k], zv);
-                }
+                for (int pb = 0; pb < 4; ++pb) dmma884(yacc[pb][0], yacc[pb][1], cy[k], zrow[8 * pb]);
+            }
+        }
+        if (MSE) {
+            int pi = 0;
+#pragma unroll
+            for (int mt = 0; mt < T; ++mt) {
+                const double av = mt < t8 ? zc[(8 * mt + g) * kNdLd + 4 * warp + t] : 0.0;
+#pragma unroll
+                for (int nt = mt; nt < T; ++nt, ++pi)
+                    if (nt < t8) dmma884(gacc[pi][0], gacc[pi][1], av, zc[(8 * nt + g) * kNdLd + 4 * warp + t]);
             }
         }
 #pragma unroll
@@ -786,7 +800,6 @@ node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ x
                 if (MSE) {
                     const double res = ok ? yacc[pb][e] - xs[p] : 0.0;
                     lacc = fma(res, res, lacc);
-                    gacc = fma(res, ok ? dacc[pb][e] : 0.0, gacc);
                 }
             }
     }
@@ -794,26 +807,80 @@ node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ x
     if (!MSE) return;
     lacc += __shfl_xor_sync(0xffffffffu, lacc, 1);
     lacc += __shfl_xor_sync(0xffffffffu, lacc, 2);
-    gacc += __shfl_xor_sync(0xffffffffu, gacc, 1);
-    gacc += __shfl_xor_sync(0xffffffffu, gacc, 2);
-    if (t == 0) {
-        lpart[(int64_t)blockIdx.x * kCbA + a] = lacc;
-        dpart[(int64_t)blockIdx.x * kCbA + a] = gacc;
+    if (t == 0) lpart[(int64_t)blockIdx.x * kCbA + a] = lacc;
+    // the 8 warps' Gram tiles summed in warp order through shared memory (deterministic)
+    const int npairs = t8 * (t8 + 1) / 2;
+    __syncthreads();
+    double* gs = zb;  // npairs x 64 <= 2 r8 kNdLd
+    for (int w = 0; w < 8; ++w) {
+        if (warp == w) {
+            int pi = 0, pc2 = 0;
+#pragma unroll
+            for (int mt = 0; mt < T; ++mt)
+#pragma unroll
+                for (int nt = mt; nt < T; ++nt, ++pi)
+                    if (nt < t8 && mt < t8) {
+                        pc2 = (mt * (2 * t8 - mt + 1)) / 2 + (nt - mt);  // compact pair index
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            double* d = gs + pc2 * 64 + g * 8 + 2 * t + e;
+                            *d = (w == 0 ? 0.0 : *d) + gacc[pi][e];
+                        }
+                    }
+        }
+        __syncthreads();
     }
+    for (int idx = tid; idx < npairs * 64; idx += 256) gpart[(int64_t)blockIdx.x * kNdPairs * 64 + idx] = gs[idx];
 }
 
-// loss[a] = norm sum_cta lpart, dlda[a] = 2 norm sum_cta dpart (fixed order)
-__global__ void node_reduce_kernel(const double* __restrict__ lpart, const double* __restrict__ dpart, int ctas,
-                                   int n_alpha, double norm, double* __restrict__ loss, double* __restrict__ dlda) {
-    const int a = threadIdx.x;
-    if (a >= n_alpha) return;
-    double l = 0.0, d = 0.0;
-    for (int c = 0; c < ctas; ++c) {
-        l += lpart[(int64_t)c * kCbA + a];
-        d += dpart[(int64_t)c * kCbA + a];
+// G = sum over CTAs of the Gram partials (fixed order), one thread per tile element
+__global__ void node_gram_reduce_kernel(const double* __restrict__ gpart, int ctas, int elems,
+                                        double* __restrict__ gsum) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= elems) return;
+    double s0 = 0.0, s1 = 0.0;
+    int c = 0;
+    for (; c + 1 < ctas; c += 2) {
+        s0 += gpart[(int64_t)c * kNdPairs * 64 + i];
+        s1 += gpart[(int64_t)(c + 1) * kNdPairs * 64 + i];
     }
-    loss[a] = norm * l;
-    dlda[a] = 2.0 * norm * d;
+    if (c < ctas) s0 += gpart[(int64_t)c * kNdPairs * 64 + i];
+    gsum[i] = s0 + s1;
+}
+
+// one CTA per order: loss from the per-CTA partials (fixed-order tree), dL/da from the Gram
+__global__ void __launch_bounds__(128) node_reduce_kernel(const double* __restrict__ lpart,
+                                                          const double* __restrict__ gsum, int ctas, int r, int rp,
+                                                          const double* __restrict__ pc, int n_alpha, double norm,
+                                                          double* __restrict__ loss, double* __restrict__ dlda) {
+    __shared__ double sl[4], sv[kNdMaxR + 1];
+    const int a = blockIdx.x, t = threadIdx.x;
+    const int t8 = node_rows8(r) / 8;
+    auto gval = [&](int i, int j) {  // G[i][j] from the compact upper-triangular tiles
+        if (i / 8 > j / 8) {
+            const int s = i;
+            i = j;
+            j = s;
+        }
+        const int mt = i / 8, nt = j / 8, pcx = (mt * (2 * t8 - mt + 1)) / 2 + (nt - mt);
+        return gsum[pcx * 64 + (i & 7) * 8 + (j & 7)];
+    };
+    double l = 0.0;
+    for (int c = t; c < ctas; c += 128) l += lpart[(int64_t)c * kCbA + a];
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if ((t & 31) == 0) sl[t >> 5] = l;
+    if (t < r) {  // v_j = (G P[a])_j - h_j = <Z'_j, Y_a - Xc>
+        double v = -gval(t, r);
+        for (int k = 0; k < r; ++k) v = fma(pc[(int64_t)a * rp + k], gval(t, k), v);
+        sv[t] = v;
+    }
+    __syncthreads();
+    if (t == 0) {
+        double d = 0.0;
+        for (int j = 0; j < r; ++j) d = fma(pc[(int64_t)(n_alpha + a) * rp + j], sv[j], d);
+        loss[a] = norm * ((sl[0] + sl[1]) + (sl[2] + sl[3]));
+        dlda[a] = 2.0 * norm * d;
+    }
 }
 
 // W_j[i, i] += d[j] for r row-stacked n x n operators (the identity term of the series)
@@ -822,41 +889,65 @@ __global__ void add_diag_kernel(double* __restrict__ w, int n, int64_t stride, c
     if (i < n && j < r) w[(int64_t)j * stride + (int64_t)i * n + i] += d[j];
 }
 
-size_t node_partial_elems() { return 2 * (size_t)(2 * FGFRFT_SMS) * kCbA; }
+size_t node_partial_elems() { return (size_t)(2 * FGFRFT_SMS) * (kCbA + kNdPairs * 64) + kNdPairs * 64; }
 
 cudaError_t launch_add_diag(double* w, int n, int64_t stride, const double* d, int r, cudaStream_t stream) {
     add_diag_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)r), 256, 0, stream>>>(w, n, stride, d, r);
     return cudaGetLastError();
 }
 
-cudaError_t launch_node_combine(const double* zin, const double* xc, int64_t count, int r, int rp, const double* pc,
-                                int n_alpha, double* y, double* partial, double norm, double* loss, double* dlda,
-                                cudaStream_t stream) {
-    if (n_alpha > kCbA || rp > kNdMaxR || rp % 4 || r > rp) return cudaErrorInvalidValue;
+template <bool MSE, int T>
+static cudaError_t node_combine_t(int ctas, size_t smem, cudaStream_t st, const double* zin, const double* xc,
+                                  int64_t count, int r, int rp, const double* pc, int n_alpha, double* y, double* lp,
+                                  double* gp) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(node_combine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)node_smem_bytes(kNdMaxR));
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(node_combine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)node_smem_bytes(kNdMaxR));
+        cudaError_t e = cudaFuncSetAttribute(node_combine_kernel<MSE, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)node_smem_bytes(8 * T - 1));
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    node_combine_kernel<MSE, T><<<ctas, 256, smem, st>>>(zin, xc, count, r, rp, pc, n_alpha, y, lp, gp);
+    return cudaGetLastError();
+}
+
+template <bool MSE>
+static cudaError_t node_combine_dispatch(int t8, int ctas, size_t smem, cudaStream_t st, const double* zin,
+                                         const double* xc, int64_t count, int r, int rp, const double* pc,
+                                         int n_alpha, double* y, double* lp, double* gp) {
+    switch (t8) {
+#define FGB_ND(T) \
+    case T: return node_combine_t<MSE, T>(ctas, smem, st, zin, xc, count, r, rp, pc, n_alpha, y, lp, gp);
+        FGB_ND(1) FGB_ND(2) FGB_ND(3) FGB_ND(4) FGB_ND(5) FGB_ND(6) FGB_ND(7)
+#undef FGB_ND
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_node_combine(const double* zin, const double* xc, int64_t count, int r, int rp, const double* pc,
+                                int n_alpha, double* y, double* partial, double norm, double* loss, double* dlda,
+                                cudaStream_t stream) {
+    if (n_alpha > kCbA || r > kNdMaxR || rp > kNdMaxR || rp % 4 || r > rp) return cudaErrorInvalidValue;
     const int64_t nch = (count + kNdP - 1) / kNdP;
     const int ctas = (int)(nch < 2 * FGFRFT_SMS ? nch : 2 * FGFRFT_SMS);
-    const size_t smem = node_smem_bytes(rp);
+    const size_t smem = node_smem_bytes(r);
+    const int t8 = node_rows8(r) / 8;
+    cudaError_t e = cudaSuccess;
     if (!xc) {
-        node_combine_kernel<false><<<ctas, 256, smem, stream>>>(zin, nullptr, count, r, rp, pc, n_alpha, y, nullptr,
-                                                                nullptr);
-        return cudaGetLastError();
+        e = node_combine_dispatch<false>(t8, ctas, smem, stream, zin, nullptr, count, r, rp, pc, n_alpha, y, nullptr,
+                                         nullptr);
+        return e;
     }
     double* lp = partial;
-    double* dp = partial + (size_t)ctas * kCbA;
-    node_combine_kernel<true><<<ctas, 256, smem, stream>>>(zin, xc, count, r, rp, pc, n_alpha, y, lp, dp);
-    cudaError_t e = cudaGetLastError();
+    double* gp = partial + (size_t)ctas * kCbA;
+    double* gs = gp + (size_t)ctas * kNdPairs * 64;
+    e = node_combine_dispatch<true>(t8, ctas, smem, stream, zin, xc, count, r, rp, pc, n_alpha, y, lp, gp);
     if (e != cudaSuccess) return e;
-    node_reduce_kernel<<<1, kCbA, 0, stream>>>(lp, dp, ctas, n_alpha, norm, loss, dlda);
+    const int elems = t8 * (t8 + 1) / 2 * 64;
+    node_gram_reduce_kernel<<<(elems + 127) / 128, 128, 0, stream>>>(gp, ctas, elems, gs);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    node_reduce_kernel<<<n_alpha, 128, 0, stream>>>(lp, gs, ctas, r, rp, pc, n_alpha, norm, loss, dlda);
     return cudaGetLastError();
 }
 
