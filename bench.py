@@ -124,19 +124,20 @@ def _config(rank: int):
 
 def ncu_traffic(kernel_prefix: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel from the committed ncu
-    --set full summary (profiles/r01_ncu_final_summary.csv), or None."""
+    --set full summaries (newest first: profiles/r01_ncu_node_summary.csv, r01_ncu_final_summary.csv),
+    or None."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01_ncu_final_summary.csv")
-    try:
-        rows = list(csv.reader(open(path)))
-        h, u = rows[0], rows[1]
-        ki, ri, wi = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
-        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        for r in rows[2:]:
-            if r[ki].startswith(kernel_prefix):
-                return float(r[ri]) * scale[u[ri]] + float(r[wi]) * scale[u[wi]]
-    except Exception:
-        return None
+    for name in ("r01_ncu_node_summary.csv", "r01_ncu_final_summary.csv"):
+        try:
+            rows = list(csv.reader(open(os.path.join(ROOT, "profiles", name))))
+            h, u = rows[0], rows[1]
+            ki, ri, wi = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            for r in rows[2:]:
+                if r[ki].startswith(kernel_prefix):
+                    return float(r[ri]) * scale[u[ri]] + float(r[wi]) * scale[u[wi]]
+        except Exception:
+            continue
     return None
 
 
