@@ -299,8 +299,6 @@ def main():
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    fg.profile_enable(True)
-    fg.profile_read(reset=True)
     launches0 = fg.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -309,12 +307,20 @@ def main():
     ev1.record(stream)
     ev1.synchronize()
     launches = fg.launch_count() - launches0
-    prof = fg.profile_read(reset=True)
-    fg.profile_enable(False)
     clk = clocks.stop()
     torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    # per-kernel-class device time (CUDA events around each class inside the library) from a
+    # separate pass of the same K steps, so the event records stay out of the timed region
+    fg.profile_enable(True)
+    fg.profile_read(reset=True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step_dev()
+    torch.cuda.synchronize()
+    prof = fg.profile_read(reset=True)
+    fg.profile_enable(False)
     value = n * b * A * ws / (ms * 1e-3)
 
     # loss / gradient sanity against the oracle on one order (rank 0, cheap)

@@ -83,6 +83,12 @@ int alpha_chunk(const fgfrft_cache* c, int n_alpha) {
 int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, double** dev) {
     const size_t width = (size_t)(2 * l + 1);
     const size_t count = 2 * (size_t)n_alpha * width;
+    if (c->coef_l == l && c->coef_alphas.size() == (size_t)n_alpha &&
+        !std::memcmp(c->coef_alphas.data(), alphas, (size_t)n_alpha * sizeof(double))) {
+        *dev = c->coef.as<double>();  // same orders as the tables already on the device: no host work
+        return FGFRFT_OK;
+    }
+    c->coef_l = -1;
     if (c->coef_evt) FGB_CUDA(cudaEventSynchronize(c->coef_evt));
     if (c->coef_h_cap < count) {
         if (c->coef_h) cudaFreeHost(c->coef_h);
@@ -100,6 +106,8 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
     FGB_CUDA(cudaMemcpyAsync(c->coef.p, c->coef_h, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     if (!c->coef_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->coef_evt, cudaEventDisableTiming));
     FGB_CUDA(cudaEventRecord(c->coef_evt, c->stream));
+    c->coef_alphas.assign(alphas, alphas + n_alpha);
+    c->coef_l = l;
     *dev = c->coef.as<double>();
     return FGFRFT_OK;
 }
@@ -672,6 +680,7 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
     p.alphas.assign(alphas, alphas + na);
     p.need_d = need_d;
     p.ok = false;
+    p.staged = false;
     double lo = alphas[0], hi = alphas[0];
     for (int a = 1; a < na; ++a) {
         lo = std::min(lo, alphas[a]);
@@ -692,15 +701,17 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
 
 // W_j = sum_k c_k(a_j) P_k (INT8 GEMM over the element-row slices) and Z'_j = W_j X.
 int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0, int r,
-                  const void* x_dev, int64_t b) {
+                  const void* x_dev, int64_t b, bool upload) {
     if (int st = ensure_elem_slices(c)) return st;
     const int S = c->es_slices;
     const int T = 2 * c->l + 1;
     const int64_t n = c->n, rows = pad_rows(n * n), kp = pad_k(2 * (int64_t)c->l), bp = kOzTileB;
-    FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
-    FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
-    FGB_CUDA(cudaMemcpyAsync(c->nd_tab.p, c->nd_h, tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
-    FGB_CUDA(cudaMemcpyAsync(c->nd_d0.p, c->nd_h + tab.size(), d0.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    if (upload) {
+        FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
+        FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
+        FGB_CUDA(cudaMemcpyAsync(c->nd_tab.p, c->nd_h, tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        FGB_CUDA(cudaMemcpyAsync(c->nd_d0.p, c->nd_h + tab.size(), d0.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    }
     FGB_CUDA(c->nd_bsl.ensure((size_t)S * bp * kp));
     FGB_CUDA(c->nd_bex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
     int* be = c->nd_bex.as<int>();
@@ -763,10 +774,17 @@ int mse_node_route(fgfrft_cache* c, const double* alphas, int n_alpha, const voi
     *ran = false;
     int r = 0, rp = 0;
     if (!node_plan(c, alphas, n_alpha, need_d, &r, &rp)) return FGFRFT_OK;
-    const auto& p = c->nd_plan;
-    if (int st = node_stage(c, p.tab, p.d0, p.pw)) return st;
-    if (int st = node_products(c, p.tab, p.d0, r, x_dev, b)) return st;
-    if (int st = node_staged(c)) return st;
+    auto& p = c->nd_plan;
+    // a memoised plan's tables are still on the device from the call that staged them: no host
+    // staging, no wait on that call's uploads
+    const bool upload = !p.staged;
+    if (upload)
+        if (int st = node_stage(c, p.tab, p.d0, p.pw)) return st;
+    if (int st = node_products(c, p.tab, p.d0, r, x_dev, b, upload)) return st;
+    if (upload) {
+        if (int st = node_staged(c)) return st;
+        p.staged = true;
+    }
     if (xc_dev && !need_d) return fail(FGFRFT_PARAMETER, "node route: the MSE form needs the derivative rows");
     if (xc_dev)
         if (int st = wait_xc(c)) return st;

@@ -306,6 +306,7 @@ struct fgfrft_cache {
     struct NodePlan {  // memoised plan of the last sweep (a pure function of the orders)
         std::vector<double> alphas, tab, d0, pw;
         bool need_d = false, ok = false;
+        bool staged = false;  // tab / d0 / pw of this plan already resident in nd_tab / nd_d0 / nd_p
         int r = 0, rp = 0;
     } nd_plan;
     size_t sig = 16;    // bytes per signal element (X, Y, G): 16 complex128, 8 complex64
@@ -346,6 +347,8 @@ struct fgfrft_cache {
     double* coef_h = nullptr;  // pinned staging for the coefficient tables
     size_t coef_h_cap = 0;
     cudaEvent_t coef_evt = nullptr;
+    std::vector<double> coef_alphas;  // orders of the tables now in `coef` / coef_h (memo)
+    int coef_l = -1;
 
     // Matrices at the API are n x n column-major; device slabs are tiled (common.cuh) and padded
     // to npad = 32 * ceil(n / 32) per side.

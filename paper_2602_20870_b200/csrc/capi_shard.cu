@@ -579,6 +579,7 @@ int fgfrft_batch_set_stream(fgfrft_cache* c, void* stream) {
 namespace fgbi {
 int batch_coefs(fgfrft_cache* c, const double* alphas_dev, int heads, double** coef) {
     const size_t orders = (size_t)c->graphs * heads;
+    c->coef_l = -1;  // the host-table memo no longer describes `coef`
     FGB_CUDA(c->coef.ensure(orders * 2 * (2 * c->l + 1) * sizeof(double)));
     FGB_LAUNCH(launch_batch_coef(alphas_dev, (int)orders, c->l, c->coef.as<double>(), c->stream), 1);
     *coef = c->coef.as<double>();

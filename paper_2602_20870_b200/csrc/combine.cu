@@ -833,19 +833,26 @@ node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ x
     for (int idx = tid; idx < npairs * 64; idx += 256) gpart[(int64_t)blockIdx.x * kNdPairs * 64 + idx] = gs[idx];
 }
 
-// G = sum over CTAs of the Gram partials (fixed order), one thread per tile element
-__global__ void node_gram_reduce_kernel(const double* __restrict__ gpart, int ctas, int elems,
-                                        double* __restrict__ gsum) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= elems) return;
-    double s0 = 0.0, s1 = 0.0;
-    int c = 0;
-    for (; c + 1 < ctas; c += 2) {
-        s0 += gpart[(int64_t)c * kNdPairs * 64 + i];
-        s1 += gpart[(int64_t)(c + 1) * kNdPairs * 64 + i];
+// G = sum over CTAs of the Gram partials (fixed order): a block per 32 tile elements, lane =
+// element (coalesced), warp w sums the CTAs c = w mod 16 (independent loads), then a fixed-order
+// sum over the 16 warps -- the serial per-element chain over ~300 partials was latency-bound.
+__global__ void __launch_bounds__(512) node_gram_reduce_kernel(const double* __restrict__ gpart, int ctas, int elems,
+                                                               double* __restrict__ gsum) {
+    __shared__ double red[16][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, i = blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (i < elems) {
+#pragma unroll 4
+        for (int c = w; c < ctas; c += 16) s += gpart[(int64_t)c * kNdPairs * 64 + i];
     }
-    if (c < ctas) s0 += gpart[(int64_t)c * kNdPairs * 64 + i];
-    gsum[i] = s0 + s1;
+    red[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && i < elems) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) t += red[q][lane];
+        gsum[i] = t;
+    }
 }
 
 // one CTA per order: loss from the per-CTA partials (fixed-order tree), dL/da from the Gram
@@ -944,7 +951,7 @@ cudaError_t launch_node_combine(const double* zin, const double* xc, int64_t cou
     e = node_combine_dispatch<true>(t8, ctas, smem, stream, zin, xc, count, r, rp, pc, n_alpha, y, lp, gp);
     if (e != cudaSuccess) return e;
     const int elems = t8 * (t8 + 1) / 2 * 64;
-    node_gram_reduce_kernel<<<(elems + 127) / 128, 128, 0, stream>>>(gp, ctas, elems, gs);
+    node_gram_reduce_kernel<<<(elems + 31) / 32, 512, 0, stream>>>(gp, ctas, elems, gs);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     node_reduce_kernel<<<n_alpha, 128, 0, stream>>>(lp, gs, ctas, r, rp, pc, n_alpha, norm, loss, dlda);

@@ -283,6 +283,46 @@ __global__ void __launch_bounds__(64) oz_rowmax_direct_kernel(OzView v, unsigned
     if (m > 0.0) atomicMax(rowmax + row, (unsigned long long)__double_as_longlong(m));
 }
 
+// S digit slices of one 16-byte run (K = k0 .. k0 + 15 of row (rt, rr)) from its scaled values.
+template <int S>
+__device__ __forceinline__ void oz_write_digits(double (&x)[16], int kp, int k0, int tr, int rt, int rr,
+                                                int8_t* __restrict__ dst) {
+    constexpr int kBK = OzCfg<S>::bk;
+    const int kb_count = kp / kBK;
+    const int kb = k0 / kBK, cl = (k0 >> 4) & (kBK / 16 - 1);
+    int8_t* base = dst + ((int64_t)rt * kb_count + kb) * S * tr * kBK + (rr >> 3) * OzCfg<S>::sbo + cl * 128 + (rr & 7) * 16;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double y = x[q * 4 + i] * kOzBase;
+                const double t = y + kOzMagic;
+                x[q * 4 + i] = y - (t - kOzMagic);
+                packed |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * i);
+            }
+            w[q] = packed;
+        }
+        *reinterpret_cast<uint4*>(base + (int64_t)s * tr * kBK) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// One 16-byte digit run of a plain strided view -> S digit slices.
+template <int S>
+__device__ __forceinline__ void oz_digit_run(const OzView& v, const double* p, bool ok, double sc, int k0, int tr,
+                                             int rt, int rr, int8_t* __restrict__ dst) {
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int k = k0 + i;
+        x[i] = (ok && k < v.kv) ? p[(int64_t)(k >> v.ka) * v.ks + (k & v.ka)] * sc : 0.0;
+    }
+    oz_write_digits<S>(x, v.kp, k0, tr, rt, rr, dst);
+}
+
 template <int S>
 __global__ void __launch_bounds__(64) oz_slice_direct_kernel(OzView v, const unsigned long long* rowmax, int tr,
                                                              int8_t* __restrict__ dst, int* __restrict__ exps) {
@@ -294,37 +334,101 @@ __global__ void __launch_bounds__(64) oz_slice_direct_kernel(OzView v, const uns
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     if (blockIdx.y == 0) exps[row] = e;
     const double sc = mx > 0.0 ? pow2(-e - 1) : 0.0;  // |a| * sc < 1/2
-    constexpr int kBK = OzCfg<S>::bk;
-    const int kb_count = v.kp / kBK;
     const int rt = row / tr, rr = row - rt * tr;
-    const int r8 = rr & 7;
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {  // 16-byte digit runs: K = k0 + 16c .. +15
-        double x[16];
+    for (int c = 0; c < 4; ++c) oz_digit_run<S>(v, p, ok, sc, k0 + c * 16, tr, rt, rr, dst);  // K = k0 + 16c ..
+}
+
+// Row max and digits in ONE kernel for tall row-contiguous views (the node operators W_j: 19n
+// rows): a CTA owns 32 rows and all of K, its 8 warps take interleaved 64-wide K blocks (lanes =
+// consecutive rows, coalesced), reduce the row max through shared memory, then slice the same
+// blocks -- the second read of the CTA's 32 rows is an L2 hit, so W crosses HBM once instead of
+// twice, and there is no rowmax memset / atomic pass.
+template <int S>
+__global__ void __launch_bounds__(256) oz_rowslice_direct_kernel(OzView v, int tr, int8_t* __restrict__ dst,
+                                                                 int* __restrict__ exps) {
+    __shared__ double wmax[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int row = blockIdx.x * 32 + lane, kblocks = v.kp / 64;
+    bool ok;
+    const double* p = oz_row_ptr(v, row, &ok);
+    double m = 0.0;
+    if (ok)
+        for (int kb = w; kb < kblocks; kb += 8) {
+            const int k0 = kb * 64, kn = min(64, v.kv - k0);
+#pragma unroll 8
+            for (int i = 0; i < kn; ++i) {
+                const int k = k0 + i;
+                m = fmax(m, fabs(p[(int64_t)(k >> v.ka) * v.ks + (k & v.ka)]));
+            }
+        }
+    wmax[w][lane] = m;
+    __syncthreads();
+    double mx = wmax[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) mx = fmax(mx, wmax[q][lane]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    if (w == 0) exps[row] = e;
+    const double sc = mx > 0.0 ? pow2(-e - 1) : 0.0;  // |a| * sc < 1/2
+    const int rt = row / tr, rr = row - rt * tr;
+    // slice in the reverse order of the max pass: the most recently read K blocks are the likeliest
+    // L2 hits
+    for (int kb = w + (kblocks - 1 - w) / 8 * 8; kb >= 0; kb -= 8)
+#pragma unroll 1
+        for (int c = 3; c >= 0; --c) oz_digit_run<S>(v, p, ok, sc, kb * 64 + c * 16, tr, rt, rr, dst);
+}
+
+// Complex signal columns as B-operand row pairs (rows 2j, 2j + 1 = Re, Im of column j, K = the
+// signal index, interleaved (re, im) in memory): one warp per column, lane = 16-wide K runs, each
+// run read as 16 double2 loads; the row max of both rows by shuffles, then the
+// digits from a second read of the (L1/L2-resident) column. One kernel, no memset / atomics.
+template <int S>
+__global__ void __launch_bounds__(256) oz_rowslice_pairs_kernel(OzView v, int tr, int8_t* __restrict__ dst,
+                                                                int* __restrict__ exps) {
+    const int lane = threadIdx.x & 31, j = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int r0 = 2 * j;
+    if (r0 >= v.nb * v.rp) return;
+    const bool ok = r0 < v.rv;  // rv even (2 x columns)
+    const double2* col = reinterpret_cast<const double2*>(v.src + (int64_t)j * v.rs);
+    const int runs = v.kp / 16;
+    double m0 = 0.0, m1 = 0.0;
+    if (ok)
+        for (int q = lane; q < runs; q += 32)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int k = q * 16 + i;
+                if (k < v.kv) {
+                    const double2 z = col[k];
+                    m0 = fmax(m0, fabs(z.x));
+                    m1 = fmax(m1, fabs(z.y));
+                }
+            }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    int e0 = 0, e1 = 0;
+    if (m0 > 0.0) frexp(m0, &e0);
+    if (m1 > 0.0) frexp(m1, &e1);
+    if (lane == 0) {
+        exps[r0] = e0;
+        exps[r0 + 1] = e1;
+    }
+    const double s0 = m0 > 0.0 ? pow2(-e0 - 1) : 0.0, s1 = m1 > 0.0 ? pow2(-e1 - 1) : 0.0;
+    const int rt0 = r0 / tr, rr0 = r0 - rt0 * tr, rt1 = (r0 + 1) / tr, rr1 = r0 + 1 - rt1 * tr;
+    for (int q = lane; q < runs; q += 32) {
+        double x0[16], x1[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int k = k0 + c * 16 + i;
-            x[i] = (ok && k < v.kv) ? p[(int64_t)(k >> v.ka) * v.ks + (k & v.ka)] * sc : 0.0;
+            const int k = q * 16 + i;
+            const double2 z = (ok && k < v.kv) ? col[k] : make_double2(0.0, 0.0);
+            x0[i] = z.x * s0;
+            x1[i] = z.y * s1;
         }
-        const int kb = (k0 + c * 16) / kBK, cl = c & (kBK / 16 - 1);
-        int8_t* base = dst + ((int64_t)rt * kb_count + kb) * S * tr * kBK + (rr >> 3) * OzCfg<S>::sbo + cl * 128 + r8 * 16;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            uint32_t w[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t packed = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const double y = x[q * 4 + i] * kOzBase;
-                    const double t = y + kOzMagic;
-                    x[q * 4 + i] = y - (t - kOzMagic);
-                    packed |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * i);
-                }
-                w[q] = packed;
-            }
-            *reinterpret_cast<uint4*>(base + (int64_t)s * tr * kBK) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        oz_write_digits<S>(x0, v.kp, q * 16, tr, rt0, rr0, dst);
+        oz_write_digits<S>(x1, v.kp, q * 16, tr, rt1, rr1, dst);
     }
 }
 
@@ -455,10 +559,50 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
             mbar_wait(tfull, tcount & 1);
             tc_fence_after();
+            constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
+            if (CM == 0 && out.npeers == 0 && out.nv - nt * kOzBN <= 32) {
+                // Skinny output (the node operators: r <= 32 of the 64 tile columns are real): warp h
+                // owns the 8 columns 8h..8h+7, so only the live groups are drained and folded. All S
+                // accumulators of the group are read before TMEM is released, so the next unit's MMAs
+                // overlap the whole fold + store instead of waiting for it.
+                const int c0 = h * 8, live = out.nv - nt * kOzBN - c0;
+                double val8[8];
+                if (live > 0) {
+                    int32_t v[S][8];
+#pragma unroll
+                    for (int d = 0; d < S; ++d)
+                        tmem_ld8(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * kOzBN + c0), v[d]);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        long long hi = v[0][q], lo = v[3][q];
+                        hi = hi * kOzBaseI + v[1][q];
+                        hi = hi * kOzBaseI + v[2][q];
+#pragma unroll
+                        for (int d = 4; d < S; ++d) lo = lo * kOzBaseI + v[d][q];
+                        val8[q] = (double)hi + (double)lo * lo_w;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty);
+                if (live <= 0) continue;
+                const int m = mt * kOzBM + lrow;
+                const int bm = m / out.mp, i = m - bm * out.mp;
+                if (i >= out.mv) continue;
+                const double ra = pow2(ea[m]) * kOzScale;
+                double* cb = out.c + (int64_t)bm * out.sc + i;
+                const int* ebt = eb + nt * kOzBN + c0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (q >= live) break;
+                    __stcs(cb + (int64_t)(nt * kOzBN + c0 + q) * out.ldc, val8[q] * ra * pow2(ebt[q]));
+                }
+                continue;
+            }
             // exact integer fold per column: hi = sum_{d<=4} acc_d 254^(4-d), lo = sum_{d>=5}
             // acc_d 254^(S+1-d); val = hi + lo 254^-(S-3). TMEM is drained 8 columns at a time, all S
             // accumulators in flight per wait.
-            constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
             double val[kOzEC];
 #pragma unroll
             for (int g8 = 0; g8 < kOzEC / 8; ++g8) {
@@ -627,6 +771,30 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
                             cudaStream_t stream) {
     const int rows = v.nb * v.rp;
     if (rows % 64 || v.kp % 64 || v.rp % tr) return cudaErrorInvalidValue;
+    if (!v.tiled && !v.rfast && v.ra == 1 && v.ka == 0 && v.ks == 2 && v.rv % 2 == 0 && v.nb == 1) {
+        // complex signal columns (re / im row pairs): one fused pass
+        const unsigned blocks = (unsigned)((rows / 2 + 7) / 8);
+        if (slices == 7)
+            oz_rowslice_pairs_kernel<7><<<blocks, 256, 0, stream>>>(v, tr, dst, exps);
+        else if (slices == 8)
+            oz_rowslice_pairs_kernel<8><<<blocks, 256, 0, stream>>>(v, tr, dst, exps);
+        else if (slices == 6)
+            oz_rowslice_pairs_kernel<6><<<blocks, 256, 0, stream>>>(v, tr, dst, exps);
+        else
+            return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
+    if (!v.tiled && v.rfast && rows / 32 >= 2 * FGFRFT_SMS) {  // tall: one fused pass
+        if (slices == 7)
+            oz_rowslice_direct_kernel<7><<<rows / 32, 256, 0, stream>>>(v, tr, dst, exps);
+        else if (slices == 8)
+            oz_rowslice_direct_kernel<8><<<rows / 32, 256, 0, stream>>>(v, tr, dst, exps);
+        else if (slices == 6)
+            oz_rowslice_direct_kernel<6><<<rows / 32, 256, 0, stream>>>(v, tr, dst, exps);
+        else
+            return cudaErrorInvalidValue;
+        return cudaGetLastError();
+    }
     cudaError_t e = cudaMemsetAsync(rowmax, 0, (size_t)rows * sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return e;
     dim3 grid(rows / 64, v.kp / 64);
