@@ -431,7 +431,6 @@ int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host
 bool use_int8_gemm(const fgfrft_cache* c, int64_t b);
 bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b);
 int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out);
-int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
 int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
                 int64_t sm);
@@ -715,27 +714,64 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
     FGB_CUDA(c->nd_bsl.ensure((size_t)S * bp * kp));
     FGB_CUDA(c->nd_bex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
     int* be = c->nd_bex.as<int>();
+    // r <= 32 nodes: the narrow GEMM form (32-row B tiles, double-buffered TMEM accumulators)
+    const bool narrow = r <= kOzTileNarrow;
     {  // node coefficient rows in the stacked term order (operand mode 4)
         OzView v{c->nd_tab.as<double>(), T, 0, 0, 0, 0, r, (int)bp, 1, 2 * c->l, (int)kp, false};
         v.tiled = 4;
         v.l = c->l;
         ProfScope ps(KC_SLICE, c->stream);
-        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->nd_bsl.as<int8_t>(), be,
+        FGB_LAUNCH(launch_oz_slice(v, S, narrow ? kOzTileNarrow : kOzTileB, c->nd_bsl.as<int8_t>(), be,
                                    reinterpret_cast<unsigned long long*>(be + bp), c->stream),
                    3);
     }
     const size_t nn = (size_t)n * n;
     FGB_CUDA(c->nd_w.ensure((size_t)r * nn * 8));
-    {
-        ProfScope ps(KC_NODEOP, c->stream);
-        FGB_LAUNCH(launch_ozgemm(S, 0, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(), be,
-                                 (int)bp, (int)kp, c->nd_w.as<double>(), (int64_t)nn, 0, (int)nn, (int)rows, r,
-                                 c->stream),
-                   1);
-    }
-    FGB_LAUNCH(launch_add_diag(c->nd_w.as<double>(), (int)n, (int64_t)nn, c->nd_d0.as<double>(), r, c->stream), 1);
     FGB_CUDA(c->nd_z.ensure((size_t)r * n * b * 16));
-    return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p);
+    // n % 128 == 0: the node-operator GEMM also adds the diagonal and leaves the row maxima of W
+    // for the product GEMM's slicing (one pass over W instead of two)
+    // (the GEMM's grid becomes a multiple of the n / 128 row blocks: only when that keeps >= 90% of
+    // the SMs)
+    const int64_t ibs = n / kOzTileA;
+    static const bool fuse_ok = [] {
+        const char* e = std::getenv("FGFRFT_NODE_FUSED_ROWMAX");
+        return !e || std::atoi(e) != 0;
+    }();
+    const bool fused = fuse_ok && n % kOzTileA == 0 && rows == (int64_t)nn &&
+                       (FGFRFT_SMS / ibs) * ibs * 10 >= FGFRFT_SMS * 9;
+    const int64_t wrows = (int64_t)r * pad_rows(n);
+    if (fused) {
+        FGB_CUDA(c->qsl.ensure((size_t)S * wrows * pad_k(n)));
+        FGB_CUDA(c->qex.ensure((size_t)wrows * (sizeof(int) + sizeof(unsigned long long))));
+        FGB_CUDA(cudaMemsetAsync(c->qex.as<int>() + wrows, 0, (size_t)wrows * sizeof(unsigned long long), c->stream));
+    }
+    {
+        OzOut out;
+        out.c = c->nd_w.as<double>();
+        out.ldc = (int64_t)nn;
+        out.sc = 0;
+        out.mv = (int)nn;
+        out.mp = (int)rows;
+        out.nv = r;
+        if (fused) {
+            out.rmax = reinterpret_cast<unsigned long long*>(c->qex.as<int>() + wrows);
+            out.dg = c->nd_d0.as<double>();
+            out.rn = (int)n;
+            out.rnp = (int)pad_rows(n);
+        }
+        ProfScope ps(KC_NODEOP, c->stream);
+        if (narrow)
+            FGB_LAUNCH(launch_ozgemm_narrow(S, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(),
+                                            be, kOzTileNarrow, (int)kp, out, c->stream),
+                       1);
+        else
+            FGB_LAUNCH(launch_ozgemm_ex(S, 0, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(),
+                                        be, (int)bp, (int)kp, out, c->stream),
+                       1);
+    }
+    if (!fused)
+        FGB_LAUNCH(launch_add_diag(c->nd_w.as<double>(), (int)n, (int64_t)nn, c->nd_d0.as<double>(), r, c->stream), 1);
+    return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, fused);
 }
 
 // Copy the plan's tables into the pinned staging (after the previous call's uploads have read
@@ -1048,7 +1084,8 @@ int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp
 // Y_a = op(Q_a) X for na real m x n matrices Q_a (column-major, leading dimension ldq, stride sq
 // doubles), complex X (n x b); Y_a complex m x b (leading dimension ldy, stride sy doubles).
 int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
-                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers, int npeers) {
+                const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers, int npeers,
+                bool rowmax_ready) {
     const int S = oz_slices_default();
     const int64_t n = c->n, mp = pad_rows(m), kp = pad_k(n), rows = (int64_t)na * mp;
     FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
@@ -1059,9 +1096,14 @@ int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m,
         const OzView v = inverse ? OzView{src, ldq, 1, sq, 0, 0, (int)m, (int)mp, na, (int)n, (int)kp, false}
                                  : OzView{src, 1, ldq, sq, 0, 0, (int)m, (int)mp, na, (int)n, (int)kp, true};
         ProfScope ps(KC_SLICE, c->stream);
-        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->qsl.as<int8_t>(), qe,
-                                   reinterpret_cast<unsigned long long*>(qe + rows), c->stream),
-                   3);
+        if (rowmax_ready)  // the producer of q left the row maxima in the rowmax half of qex
+            FGB_LAUNCH(launch_oz_slice_ready(v, S, kOzTileA, c->qsl.as<int8_t>(), qe,
+                                             reinterpret_cast<const unsigned long long*>(qe + rows), c->stream),
+                       1);
+        else
+            FGB_LAUNCH(launch_oz_slice(v, S, kOzTileA, c->qsl.as<int8_t>(), qe,
+                                       reinterpret_cast<unsigned long long*>(qe + rows), c->stream),
+                       3);
     }
     int64_t bp = 0;
     if (int st = slice_signal_rows(c, x_dev, b, &bp)) return st;
@@ -1073,8 +1115,10 @@ int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m,
     return FGFRFT_OK;
 }
 
-int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y) {
-    return int8_qx_gen(c, na, inverse, q, c->n, c->n, c->n * c->n, x_dev, b, y, c->n, 2 * c->n * b);
+int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y,
+            bool rowmax_ready) {
+    return int8_qx_gen(c, na, inverse, q, c->n, c->n, c->n * c->n, x_dev, b, y, c->n, 2 * c->n * b, nullptr, 0,
+                       rowmax_ready);
 }
 
 // M_a = Re(G_a X^H) (real m x n, column-major ld m, stride sm) for na blocks G_a (m x b complex,

@@ -62,9 +62,17 @@ struct OzOut {
     // the all-gather of a row-sharded output fused into the GEMM epilogue). Offsets as for c.
     double* peers[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int npeers = 0;
+    // CM 0, skinny (nv <= 32) node operators over element rows m = i + j rn (rn % 128 == 0): the
+    // grid is a multiple of rn / 128 so each CTA stays in one row block; adds dg[col] on the diagonal
+    // (i == j) and leaves max_j |C[i + j rn, col]| in rmax[col * rnp + i] (atomicMax on the bits of
+    // a non-negative double; zeroed by the caller) -- the row max the product GEMM's slicing needs.
+    unsigned long long* rmax = nullptr;
+    const double* dg = nullptr;
+    int rn = 0, rnp = 0;
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)
+constexpr int kOzTileNarrow = 32;  // B row tile of the skinny node-operator GEMM
 constexpr int kOzTileB = 64;   // B operand row tile (output columns per CTA)
 constexpr int kOzK = 64;       // K padding granule
 
@@ -75,6 +83,10 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
                             cudaStream_t stream);
 // C = A B^T over sliced operands; cm 0: C[bm*sc + i + n*ldc], cm 1: complex merge of column
 // pairs C[bm*sc + (i + (n>>1)*ldc)*2 + (n&1)], with m = bm * mp + i (i < mv), n < nv.
+cudaError_t launch_ozgemm_narrow(int slices, const int8_t* a, const int* ea, int mrows, const int8_t* b,
+                                 const int* eb, int nrows, int kp, const OzOut& out, cudaStream_t stream);
+cudaError_t launch_oz_slice_ready(const OzView& v, int slices, int tr, int8_t* dst, int* exps,
+                                  const unsigned long long* rowmax, cudaStream_t stream);
 cudaError_t launch_ozgemm_ex(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                              const int* eb, int nrows, int kp, const OzOut& out, cudaStream_t stream);
 int oz_bk(int slices);  // bytes of K per stage / per digit block of the sliced layout

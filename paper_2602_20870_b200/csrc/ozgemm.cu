@@ -44,12 +44,12 @@ __host__ __device__ constexpr double oz_pow254(int k) { return k == 0 ? 1.0 : 25
 
 // Stage geometry per digit count: 6 digits -> 64-byte K blocks (two MMA K steps, 18 MMAs per
 // stage) in a 3-stage ring; 7-8 digits -> 32-byte K blocks in a 5- / 4-stage ring (<= 219 KB smem).
-template <int S> struct OzCfg {
+template <int S, int BN = kOzBN> struct OzCfg {
     static constexpr int bk = S <= 6 ? 64 : 32;        // bytes (= int8 elements) of K per stage
     static constexpr int stages = S <= 6 ? 3 : (S == 7 ? 5 : 4);
     static constexpr int sbo = bk / 16 * 128;          // bytes between 8-row groups of a slice block
     static constexpr int a_stage = S * kOzBM * bk;
-    static constexpr int b_stage = S * kOzBN * bk;
+    static constexpr int b_stage = S * BN * bk;
     static constexpr int stage = a_stage + b_stage;
     static constexpr int smem = stages * stage + 1024 + 2048;  // + barriers / scratch + CM 2 exchange
 };
@@ -380,21 +380,21 @@ __global__ void __launch_bounds__(256) oz_rowslice_direct_kernel(OzView v, int t
 }
 
 // Complex signal columns as B-operand row pairs (rows 2j, 2j + 1 = Re, Im of column j, K = the
-// signal index, interleaved (re, im) in memory): one warp per column, lane = 16-wide K runs, each
-// run read as 16 double2 loads; the row max of both rows by shuffles, then the
-// digits from a second read of the (L1/L2-resident) column. One kernel, no memset / atomics.
+// signal index, interleaved (re, im) in memory): a 64-thread block per column, thread = 16-wide K
+// runs; the row max of both rows by shuffles + shared memory, then the digits from a second read
+// of the (L1/L2-resident) column. One kernel, no memset / atomics.
 template <int S>
-__global__ void __launch_bounds__(256) oz_rowslice_pairs_kernel(OzView v, int tr, int8_t* __restrict__ dst,
-                                                                int* __restrict__ exps) {
-    const int lane = threadIdx.x & 31, j = blockIdx.x * 8 + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(64) oz_rowslice_pairs_kernel(OzView v, int tr, int8_t* __restrict__ dst,
+                                                               int* __restrict__ exps) {
+    __shared__ double wm[2][2];
+    const int t = threadIdx.x, lane = t & 31, j = blockIdx.x;
     const int r0 = 2 * j;
-    if (r0 >= v.nb * v.rp) return;
     const bool ok = r0 < v.rv;  // rv even (2 x columns)
     const double2* col = reinterpret_cast<const double2*>(v.src + (int64_t)j * v.rs);
     const int runs = v.kp / 16;
     double m0 = 0.0, m1 = 0.0;
     if (ok)
-        for (int q = lane; q < runs; q += 32)
+        for (int q = t; q < runs; q += 64)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int k = q * 16 + i;
@@ -409,16 +409,23 @@ __global__ void __launch_bounds__(256) oz_rowslice_pairs_kernel(OzView v, int tr
         m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
         m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
     }
+    if (lane == 0) {
+        wm[t >> 5][0] = m0;
+        wm[t >> 5][1] = m1;
+    }
+    __syncthreads();
+    m0 = fmax(wm[0][0], wm[1][0]);
+    m1 = fmax(wm[0][1], wm[1][1]);
     int e0 = 0, e1 = 0;
     if (m0 > 0.0) frexp(m0, &e0);
     if (m1 > 0.0) frexp(m1, &e1);
-    if (lane == 0) {
+    if (t == 0) {
         exps[r0] = e0;
         exps[r0 + 1] = e1;
     }
     const double s0 = m0 > 0.0 ? pow2(-e0 - 1) : 0.0, s1 = m1 > 0.0 ? pow2(-e1 - 1) : 0.0;
     const int rt0 = r0 / tr, rr0 = r0 - rt0 * tr, rt1 = (r0 + 1) / tr, rr1 = r0 + 1 - rt1 * tr;
-    for (int q = lane; q < runs; q += 32) {
+    for (int q = t; q < runs; q += 64) {
         double x0[16], x1[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -451,20 +458,26 @@ constexpr int kOzThreads = 32 * (2 + kOzEpiWarps);    // producer warp, MMA warp
 // (tmem_empty); warps 2..9 drain TMEM, fold the S int32 accumulators into two exact int64
 // partial sums, release TMEM and only then convert, scale and store -- so the FP64 epilogue
 // overlaps the next tile's MMAs.
-template <int S, int CM, int CL>
+// BN = 32 (CM 0 only): the skinny node-operator form -- B tiles of 32 rows (r <= 32 live output
+// columns), S x 32 TMEM columns per accumulator set, so two sets fit and the MMAs of unit u + 1
+// run while the epilogue drains unit u (tfull / tempty per buffer).
+template <int S, int CM, int CL, int BN = kOzBN>
 __global__ void __launch_bounds__(kOzThreads, 1)
 ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const int8_t* __restrict__ b,
               const int* __restrict__ eb, int kblocks, int mtiles, int ntiles, OzOut out) {
-    using Cfg = OzCfg<S>;
+    static_assert(BN == kOzBN || (BN == 32 && CM == 0), "narrow tiles: node operators only");
+    using Cfg = OzCfg<S, BN>;
+    constexpr int NB = BN == kOzBN ? 1 : 2;        // TMEM accumulator buffers
+    constexpr uint32_t kBufCols = BN == kOzBN ? 0 : 256;
     constexpr int kOzStages = Cfg::stages;
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* sa = smem;
     unsigned char* sb = smem + kOzStages * Cfg::a_stage;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzStages * Cfg::stage);
     uint64_t* empty = full + kOzStages;
-    uint64_t* tfull = empty + kOzStages;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tfull = empty + kOzStages;  // [NB]
+    uint64_t* tempty = tfull + 2;         // [NB]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     double* xchg = reinterpret_cast<double*>(smem + kOzStages * Cfg::stage + 1024);  // CM 2: 2 x [2][64]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -479,8 +492,10 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             mbar_init(full + s, 1);
             mbar_init(empty + s, CL);
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, kOzEpiWarps);
+        for (int q = 0; q < NB; ++q) {
+            mbar_init(tfull + q, 1);
+            mbar_init(tempty + q, kOzEpiWarps);
+        }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -491,13 +506,20 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     if (CL > 1) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // unit schedule: strided over the clusters. Row-max node operators (out.rmax): the host sizes
+    // the grid as a multiple of the row blocks per column (rn / 128), so every unit of a CTA lies in
+    // the same row block and the row max stays in registers until one flush at the end
+    const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr;
+    const int ub = cid, ue = units, us = nclusters;
+    auto unit_mt = [&](int u) { return u / ngroups; };
+    auto unit_nt = [&](int u) { return (u % ngroups) * CL + rank; };
 
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();  // B (the small operand) is reread by every A tile
             int it = 0;  // global K-block counter across units
-            for (int u = cid; u < units; u += nclusters) {
-                const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
+            for (int u = ub; u < ue; u += us) {
+                const int mt = unit_mt(u), nt = unit_nt(u);
                 const unsigned char* ga = reinterpret_cast<const unsigned char*>(a) + (int64_t)mt * kblocks * Cfg::a_stage;
                 const unsigned char* gb = reinterpret_cast<const unsigned char*>(b) + (int64_t)nt * kblocks * Cfg::b_stage;
                 for (int kb = 0; kb < kblocks; ++kb, ++it) {
@@ -516,9 +538,11 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     } else if (warp == 1) {
         if (lane == 0) {
             int it = 0, tcount = 0;
-            for (int u = cid; u < units; u += nclusters, ++tcount) {
-                if (tcount > 0) mbar_wait(tempty, (tcount - 1) & 1);  // epilogue drained TMEM
+            for (int u = ub; u < ue; u += us, ++tcount) {
+                const int buf = tcount % NB;
+                if (tcount >= NB) mbar_wait(tempty + buf, ((tcount / NB) - 1) & 1);  // epilogue drained it
                 tc_fence_after();
+                const uint32_t acc = tmem + (uint32_t)buf * kBufCols;
                 for (int kb = 0; kb < kblocks; ++kb, ++it) {
                     const int s = it % kOzStages;
                     mbar_wait(full + s, (it / kOzStages) & 1);
@@ -532,15 +556,15 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
                             for (int u0 = 1; u0 <= S + 1 - t; u0 += 4) {
                                 const int cnt = (S + 1 - t - u0 + 1) < 4 ? (S + 1 - t - u0 + 1) : 4;
-                                const uint64_t bd = umma_desc(b0 + (u0 - 1) * kOzBN * Cfg::bk + j * 256, 128, Cfg::sbo);
-                                const uint32_t col = tmem + (uint32_t)((t + u0 - 2) * kOzBN);
-                                mma_i8(col, ad, bd, idesc_i8(kOzBM, cnt * kOzBN), (kb > 0 || j > 0 || t > 1) ? 1u : 0u);
+                                const uint64_t bd = umma_desc(b0 + (u0 - 1) * BN * Cfg::bk + j * 256, 128, Cfg::sbo);
+                                const uint32_t col = acc + (uint32_t)((t + u0 - 2) * BN);
+                                mma_i8(col, ad, bd, idesc_i8(kOzBM, cnt * BN), (kb > 0 || j > 0 || t > 1) ? 1u : 0u);
                             }
                         }
                     }
                     if (CL > 1) mma_commit_mc(empty + s, kMask); else mma_commit(empty + s);
                 }
-                mma_commit(tfull);
+                mma_commit(tfull + buf);
             }
         }
     } else {
@@ -555,26 +579,41 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
             for (int c = 0; c < kOzEC; ++c) lacc[c] = 0.0;
         }
-        for (int u = cid; u < units; u += nclusters, ++tcount) {
-            const int mt = u / ngroups, nt = (u % ngroups) * CL + rank;
-            mbar_wait(tfull, tcount & 1);
+        double rmx[8];  // chunk mode: running row max of this thread's 8 columns over the row block
+        int rib = -1;
+        auto flush_rmax = [&](int live) {
+            if (rib < 0) return;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < live && rmx[q] > 0.0)
+                    atomicMax(out.rmax + (int64_t)(h * ((out.nv + 3) >> 2) + q) * out.rnp + rib * kOzBM + lrow,
+                              (unsigned long long)__double_as_longlong(rmx[q]));
+        };
+        for (int u = ub; u < ue; u += us, ++tcount) {
+            const int mt = unit_mt(u), nt = unit_nt(u);
+            const int buf = tcount % NB;
+            mbar_wait(tfull + buf, (tcount / NB) & 1);
             tc_fence_after();
             constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
-            if (CM == 0 && out.npeers == 0 && out.nv - nt * kOzBN <= 32) {
-                // Skinny output (the node operators: r <= 32 of the 64 tile columns are real): warp h
-                // owns the 8 columns 8h..8h+7, so only the live groups are drained and folded. All S
-                // accumulators of the group are read before TMEM is released, so the next unit's MMAs
+            if (BN != kOzBN || (CM == 0 && out.npeers == 0 && out.nv - nt * kOzBN <= 32)) {
+                // Skinny output (the node operators: r <= 32 of the 64 tile columns are real): the w
+                // live columns are split evenly over the 4 column warps (warp h owns cw = ceil(w / 4)
+                // columns from h cw), so only live columns are drained and folded and the per-unit
+                // epilogue (the critical path of this HBM-streaming GEMM) is ceil(w / 4) columns deep.
+                // All S accumulators are read before TMEM is released, so the next unit's MMAs
                 // overlap the whole fold + store instead of waiting for it.
-                const int c0 = h * 8, live = out.nv - nt * kOzBN - c0;
+                const int wl = min(out.nv - nt * BN, 32), cw = (wl + 3) >> 2;
+                const int c0 = h * cw, live = min(cw, wl - c0);
                 double val8[8];
                 if (live > 0) {
                     int32_t v[S][8];
 #pragma unroll
                     for (int d = 0; d < S; ++d)
-                        tmem_ld8(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * kOzBN + c0), v[d]);
+                        tmem_ld8(tmem + buf * kBufCols + ((uint32_t)(lg * 32) << 16) + (uint32_t)(d * BN + c0), v[d]);
                     tmem_wait_ld();
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
+                        if (q >= live) break;
                         long long hi = v[0][q], lo = v[3][q];
                         hi = hi * kOzBaseI + v[1][q];
                         hi = hi * kOzBaseI + v[2][q];
@@ -585,21 +624,40 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(tempty);
+                if (lane == 0) mbar_arrive(tempty + buf);
                 if (live <= 0) continue;
                 const int m = mt * kOzBM + lrow;
                 const int bm = m / out.mp, i = m - bm * out.mp;
                 if (i >= out.mv) continue;
                 const double ra = pow2(ea[m]) * kOzScale;
                 double* cb = out.c + (int64_t)bm * out.sc + i;
-                const int* ebt = eb + nt * kOzBN + c0;
+                const int* ebt = eb + nt * BN + c0;
+                if (chunk) {
+                    const int ibs = out.rn / kOzBM, rj = mt / ibs, ib = mt - rj * ibs, ri = ib * kOzBM + lrow;
+                    if (ib != rib) {
+                        flush_rmax(live);
+                        rib = ib;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) rmx[q] = 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (q >= live) break;
+                        double y = val8[q] * ra * pow2(ebt[q]);
+                        if (ri == rj) y += out.dg[c0 + q];  // the c_0 I term of the series
+                        rmx[q] = fmax(rmx[q], fabs(y));
+                        __stcs(cb + (int64_t)(c0 + q) * out.ldc, y);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (q >= live) break;
-                    __stcs(cb + (int64_t)(nt * kOzBN + c0 + q) * out.ldc, val8[q] * ra * pow2(ebt[q]));
+                    __stcs(cb + (int64_t)(nt * BN + c0 + q) * out.ldc, val8[q] * ra * pow2(ebt[q]));
                 }
                 continue;
             }
+            if constexpr (BN == kOzBN) {
             // exact integer fold per column: hi = sum_{d<=4} acc_d 254^(4-d), lo = sum_{d>=5}
             // acc_d 254^(S+1-d); val = hi + lo 254^-(S-3). TMEM is drained 8 columns at a time, all S
             // accumulators in flight per wait.
@@ -623,7 +681,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty);
+            if (lane == 0) mbar_arrive(tempty + buf);
             // value = (hi + lo 254^-(S-3)) * 4 * 254^-4 * 2^e_r * 2^e_n
             const int m = mt * kOzBM + lrow;
             if (CM == 2) {
@@ -730,7 +788,9 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                     }
                 }
             }
+            }  // BN == kOzBN
         }
+        if (chunk) flush_rmax(min((out.nv + 3) >> 2, out.nv - h * ((out.nv + 3) >> 2)));
         if (CM == 2) {
             double* gp = out.part + (((int64_t)blockIdx.x * kOzEpiQ + h) * kOzBM + lrow) * 3;
             gp[0] = gacc[0];
@@ -773,13 +833,13 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
     if (rows % 64 || v.kp % 64 || v.rp % tr) return cudaErrorInvalidValue;
     if (!v.tiled && !v.rfast && v.ra == 1 && v.ka == 0 && v.ks == 2 && v.rv % 2 == 0 && v.nb == 1) {
         // complex signal columns (re / im row pairs): one fused pass
-        const unsigned blocks = (unsigned)((rows / 2 + 7) / 8);
+        const unsigned blocks = (unsigned)(rows / 2);
         if (slices == 7)
-            oz_rowslice_pairs_kernel<7><<<blocks, 256, 0, stream>>>(v, tr, dst, exps);
+            oz_rowslice_pairs_kernel<7><<<blocks, 64, 0, stream>>>(v, tr, dst, exps);
         else if (slices == 8)
-            oz_rowslice_pairs_kernel<8><<<blocks, 256, 0, stream>>>(v, tr, dst, exps);
+            oz_rowslice_pairs_kernel<8><<<blocks, 64, 0, stream>>>(v, tr, dst, exps);
         else if (slices == 6)
-            oz_rowslice_pairs_kernel<6><<<blocks, 256, 0, stream>>>(v, tr, dst, exps);
+            oz_rowslice_pairs_kernel<6><<<blocks, 64, 0, stream>>>(v, tr, dst, exps);
         else
             return cudaErrorInvalidValue;
         return cudaGetLastError();
@@ -822,20 +882,42 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
     return cudaGetLastError();
 }
 
-template <int S, int CM, int CL>
+// Digits only, from row maxima already in `rowmax` (e.g. left by the node-operator GEMM).
+cudaError_t launch_oz_slice_ready(const OzView& v, int slices, int tr, int8_t* dst, int* exps,
+                                  const unsigned long long* rowmax, cudaStream_t stream) {
+    const int rows = v.nb * v.rp;
+    if (rows % 64 || v.kp % 64 || v.rp % tr) return cudaErrorInvalidValue;
+    dim3 grid(rows / 64, v.kp / 64);
+    const bool direct = !v.tiled && v.rfast;
+#define FGB_SL(S_)                                                                                  \
+    if (slices == S_) {                                                                             \
+        if (direct)                                                                                 \
+            oz_slice_direct_kernel<S_><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);          \
+        else                                                                                        \
+            oz_slice_kernel<S_><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);                \
+        return cudaGetLastError();                                                                  \
+    }
+    FGB_SL(6)
+    FGB_SL(7)
+    FGB_SL(8)
+#undef FGB_SL
+    return cudaErrorInvalidValue;
+}
+
+template <int S, int CM, int CL, int BN = kOzBN>
 static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, const int8_t* b, const int* eb, int ntiles,
                                 int kp, const OzOut& out, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             OzCfg<S>::smem);
+        cudaError_t e = cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (OzCfg<S, BN>::smem));
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const int units = mtiles * (ntiles / CL);
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kOzThreads);
-    cfg.dynamicSmemBytes = OzCfg<S>::smem;
+    cfg.dynamicSmemBytes = (OzCfg<S, BN>::smem);
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -849,15 +931,19 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
     if (max_clusters == 0) {
         cfg.gridDim = dim3(FGFRFT_SMS / CL * CL);
         int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, ozgemm_kernel<S, CM, CL>, &cfg) != cudaSuccess || mc <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&mc, ozgemm_kernel<S, CM, CL, BN>, &cfg) != cudaSuccess || mc <= 0) {
             cudaGetLastError();
             mc = FGFRFT_SMS / CL;
         }
         max_clusters = mc;
     }
-    const int clusters = units < max_clusters ? units : max_clusters;
+    int clusters = units < max_clusters ? units : max_clusters;
+    if (CM == 0 && CL == 1 && out.rmax) {  // row-max mode: a multiple of the row blocks per column
+        const int ibs = out.rn / kOzBM;
+        if (clusters >= ibs) clusters = clusters / ibs * ibs;
+    }
     cfg.gridDim = dim3(clusters * CL);
-    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL>, a, ea, b, eb, kp / OzCfg<S>::bk, mtiles, ntiles, out);
+    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL, BN>, a, ea, b, eb, kp / OzCfg<S, BN>::bk, mtiles, ntiles, out);
 }
 
 template <int S, int CM>
@@ -878,6 +964,19 @@ static cudaError_t oz_launch(const int8_t* a, const int* ea, int mrows, const in
         case 2: return oz_launch_cl<S, CM, 2>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
         default: return oz_launch_cl<S, CM, 1>(a, ea, mtiles, b, eb, ntiles, kp, out, stream);
     }
+}
+
+// Skinny CM 0 product (out.nv <= 32, no peers): B sliced with 32-row tiles (launch_oz_slice tr =
+// kOzTileNarrow), nrows == 32; narrow TMEM accumulators, double-buffered.
+cudaError_t launch_ozgemm_narrow(int slices, const int8_t* a, const int* ea, int mrows, const int8_t* b,
+                                 const int* eb, int nrows, int kp, const OzOut& out, cudaStream_t stream) {
+    if (mrows % kOzBM || nrows != kOzTileNarrow || kp % 64 || out.nv > kOzTileNarrow || out.npeers)
+        return cudaErrorInvalidValue;
+    const int mtiles = mrows / kOzBM;
+    if (slices == 6) return oz_launch_cl<6, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, 1, kp, out, stream);
+    if (slices == 7) return oz_launch_cl<7, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, 1, kp, out, stream);
+    if (slices == 8) return oz_launch_cl<8, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, 1, kp, out, stream);
+    return cudaErrorInvalidValue;
 }
 
 // C (from OzOut) = A_sliced (mrows x kp) * B_sliced (nrows x kp)^T; mrows % 128 == 0, nrows % 64 == 0.
