@@ -66,7 +66,8 @@ struct BatchSmem {
     // and the per-power reduction table red[(l+1) x 16 warps x 8].
     static constexpr size_t kA = (size_t)kBStages * kBSlab * 8;          // 128 KB
     static constexpr size_t kX = (size_t)kBN * kBMaxCh * 8;              // 32 KB
-    static size_t bytes(int l) { return kA + kX + kBStages * 8 + (size_t)(l + 1) * 16 * 8 * 8 + 64; }
+    // + one more mbarrier (X / G bulk copy) before the table: forward keeps its coefficients there
+    static size_t bytes(int l) { return kA + kX + (kBStages + 1) * 8 + (size_t)(l + 1) * 16 * 8 * 8 + 64; }
 };
 
 size_t batch_smem_bytes(int l) { return BatchSmem::bytes(l); }
@@ -81,26 +82,42 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
     ST* regA = reinterpret_cast<ST*>(smem);
     float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
+    uint64_t* xbar = full + kBStages;
     const int g = blockIdx.x, tid = threadIdx.x;
     const int w = 2 * l + 1;
+    float* cs = reinterpret_cast<float*>(xbar + 1);  // [h][w]: this graph's series coefficients
     const ST* gs = static_cast<const ST*>(slabs) + (int64_t)g * l * kBSlab;
-    if (tid == 0) {
-        for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-    }
-    // X_g (n x ch, column-major) -> xs[c * 64 + j], zero padded
-    for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
-        const int j = idx & 63, c = idx >> 6;
-        xs[idx] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
     const uint32_t bytes = kBSlab * sizeof(ST);
     auto issue = [&](int k, int s) {
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
     };
-    if (tid == 0)
+    // Full-size graphs (n = 64, 64 channels): X_g is one contiguous 32 KB block in the xs layout,
+    // bulk-copied at kernel start; it is first needed by the Y phase, so the copy overlaps the
+    // whole power pass instead of exposing a global-load latency per element.
+    const bool xbulk = n == kBN && ch == kBMaxCh && ((uintptr_t)x & 15) == 0;
+    if (tid == 0) {
+        for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
+        mbar_init(xbar, 1);
+        fence_mbar_init();
         for (int s = 0; s < kBStages && s < l; ++s) issue(s + 1, s);
+        if (xbulk) {
+            mbar_arrive_expect_tx(xbar, kBN * kBMaxCh * sizeof(float2));
+            bulk_g2s(xs, x + (int64_t)g * ch * n, kBN * kBMaxCh * sizeof(float2), xbar);
+        }
+    }
+    // coefficients once into shared memory (the power loop used to re-load them from global)
+    for (int idx = tid; idx < H * w; idx += kBTh) {
+        const int h = idx / w, t = idx - h * w;
+        cs[idx] = (float)coef[(size_t)(g * H + h) * 2 * w + t];
+    }
+    // X_g (n x ch, column-major) -> xs[c * 64 + j], zero padded
+    if (!xbulk)
+        for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
+            const int j = idx & 63, c = idx >> 6;
+            xs[idx] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
+        }
+    __syncthreads();
     // element ownership: e = tid + 512 u -> i = e & 63 (= tid & 63), j = (tid >> 6) + 8 u
     const int i = tid & 63, j0 = tid >> 6;
     ST q[8][H];
@@ -108,7 +125,7 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
     for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            const float c0 = (i == j0 + 8 * u) ? (float)coef[(size_t)(g * H + h) * 2 * w + l] : 0.f;
+            const float c0 = (i == j0 + 8 * u) ? cs[h * w + l] : 0.f;
             if constexpr (R) q[u][h] = c0;
             else q[u][h] = make_float2(c0, 0.f);
         }
@@ -119,8 +136,8 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
         float a[H], b[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            a[h] = (float)coef[(size_t)(g * H + h) * 2 * w + l + k];
-            b[h] = (float)coef[(size_t)(g * H + h) * 2 * w + l - k];
+            a[h] = cs[h * w + l + k];
+            b[h] = cs[h * w + l - k];
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -144,6 +161,7 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
     for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int h = 0; h < H; ++h) regA[(size_t)h * kBN * kBN + (j0 + 8 * u) * kBN + i] = q[u][h];
+    if (xbulk) mbar_wait(xbar, 0);
     __syncthreads();
     // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: thread -> rows 2ib, 2ib+1, 32+2ib, 33+2ib and cols 2cb, 2cb+1
     // (the 16 lanes of a half-warp read contiguous bytes of a Q column: conflict-free)
@@ -211,25 +229,38 @@ batch_dlda_kernel(const void* __restrict__ slabs, int n, int l, const double* __
     ST* regS = reinterpret_cast<ST*>(smem);  // the same region as power stages
     float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
-    double* red = reinterpret_cast<double*>(full + kBStages);  // [k 0..l][warp 16][8]
+    uint64_t* xbar = full + kBStages;
+    double* red = reinterpret_cast<double*>(xbar + 1);  // [k 0..l][warp 16][8]
     const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = 2 * l + 1;
     const ST* gs = static_cast<const ST*>(slabs) + (int64_t)g * l * kBSlab;
+    // full-size graphs: X_g and the H gradient blocks G_h are contiguous in the staged layouts, so
+    // two bulk copies replace the per-element loads
+    const bool bulk = n == kBN && ch == kBMaxCh && ((uintptr_t)x & 15) == 0 && ((uintptr_t)gcot & 15) == 0;
     if (tid == 0) {
         for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
+        mbar_init(xbar, 1);
         fence_mbar_init();
+        if (bulk) {
+            constexpr uint32_t blk = kBN * kBMaxCh * sizeof(float2);
+            mbar_arrive_expect_tx(xbar, (H + 1) * blk);
+            bulk_g2s(xs, x + (int64_t)g * ch * n, blk, xbar);
+            bulk_g2s(regA, gcot + (int64_t)g * H * ch * n, H * blk, xbar);
+        }
     }
     // stage X (xs[c*64 + j]) and G_h (regA[h][c*64 + i]), zero padded
-    for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
-        const int r = idx & 63, c = idx >> 6;
-        const bool v = r < n && c < ch;
-        xs[idx] = v ? x[((int64_t)g * ch + c) * n + r] : make_float2(0.f, 0.f);
+    if (!bulk)
+        for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
+            const int r = idx & 63, c = idx >> 6;
+            const bool v = r < n && c < ch;
+            xs[idx] = v ? x[((int64_t)g * ch + c) * n + r] : make_float2(0.f, 0.f);
 #pragma unroll
-        for (int h = 0; h < H; ++h)
-            regA[(size_t)h * kBN * kBMaxCh + idx] =
-                v ? gcot[(((int64_t)g * H + h) * ch + c) * n + r] : make_float2(0.f, 0.f);
-    }
+            for (int h = 0; h < H; ++h)
+                regA[(size_t)h * kBN * kBMaxCh + idx] =
+                    v ? gcot[(((int64_t)g * H + h) * ch + c) * n + r] : make_float2(0.f, 0.f);
+        }
     __syncthreads();
+    if (bulk) mbar_wait(xbar, 0);
     // M_h[i, j] = sum_c G_h[i, c] conj(X[j, c]) for the thread's 8 elements
     const int i = tid & 63, j0 = tid >> 6;
     ST m[8][H];  // R: only Re M = Gr Xr^T + Gi Xi^T is needed against real powers
