@@ -20,7 +20,8 @@ namespace fgb {
 
 constexpr int kBN = 64;          // padded graph size (2 x 2 tiles)
 constexpr int kBTh = 512;        // threads per graph CTA
-constexpr int kBStages = 4;
+constexpr int kBStages = 4;      // power ring slots in region A for complex slabs (32 KB each)
+constexpr int kBStagesR = 8;     // forward, real float slabs (16 KB each): the same 128 KB, twice the depth
 constexpr int kBMaxHeads = 4;
 constexpr int kBMaxCh = 64;
 constexpr int kBSlab = 4 * kTileElems;  // elements per padded slab
@@ -67,7 +68,7 @@ struct BatchSmem {
     static constexpr size_t kA = (size_t)kBStages * kBSlab * 8;          // 128 KB
     static constexpr size_t kX = (size_t)kBN * kBMaxCh * 8;              // 32 KB
     // + one more mbarrier (X / G bulk copy) before the table: forward keeps its coefficients there
-    static size_t bytes(int l) { return kA + kX + (kBStages + 1) * 8 + (size_t)(l + 1) * 16 * 8 * 8 + 64; }
+    static size_t bytes(int l) { return kA + kX + (kBStagesR + 1) * 8 + (size_t)(l + 1) * 16 * 8 * 8 + 64; }
 };
 
 size_t batch_smem_bytes(int l) { return BatchSmem::bytes(l); }
@@ -82,7 +83,8 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
     ST* regA = reinterpret_cast<ST*>(smem);
     float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
-    uint64_t* xbar = full + kBStages;
+    constexpr int NS = R ? kBStagesR : kBStages;
+    uint64_t* xbar = full + kBStagesR;
     const int g = blockIdx.x, tid = threadIdx.x;
     const int w = 2 * l + 1;
     float* cs = reinterpret_cast<float*>(xbar + 1);  // [h][w]: this graph's series coefficients
@@ -97,10 +99,10 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
     // whole power pass instead of exposing a global-load latency per element.
     const bool xbulk = n == kBN && ch == kBMaxCh && ((uintptr_t)x & 15) == 0;
     if (tid == 0) {
-        for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         mbar_init(xbar, 1);
         fence_mbar_init();
-        for (int s = 0; s < kBStages && s < l; ++s) issue(s + 1, s);
+        for (int s = 0; s < NS && s < l; ++s) issue(s + 1, s);
         if (xbulk) {
             mbar_arrive_expect_tx(xbar, kBN * kBMaxCh * sizeof(float2));
             bulk_g2s(xs, x + (int64_t)g * ch * n, kBN * kBMaxCh * sizeof(float2), xbar);
@@ -130,8 +132,8 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
             else q[u][h] = make_float2(c0, 0.f);
         }
     for (int k = 1; k <= l; ++k) {
-        const int s = (k - 1) % kBStages;
-        mbar_wait(&full[s], ((k - 1) / kBStages) & 1);
+        const int s = (k - 1) % NS;
+        mbar_wait(&full[s], ((k - 1) / NS) & 1);
         const ST* t = regA + (size_t)s * kBSlab;
         float a[H], b[H];
 #pragma unroll
@@ -154,7 +156,7 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
             }
         }
         __syncthreads();
-        if (tid == 0 && k + kBStages <= l) issue(k + kBStages, s);
+        if (tid == 0 && k + NS <= l) issue(k + NS, s);
     }
     // Q_h -> region A as column-major 64 x 64: qs[h][j * 64 + i]
 #pragma unroll
@@ -229,7 +231,7 @@ batch_dlda_kernel(const void* __restrict__ slabs, int n, int l, const double* __
     ST* regS = reinterpret_cast<ST*>(smem);  // the same region as power stages
     float2* xs = reinterpret_cast<float2*>(smem + BatchSmem::kA);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BatchSmem::kA + BatchSmem::kX);
-    uint64_t* xbar = full + kBStages;
+    uint64_t* xbar = full + kBStagesR;
     double* red = reinterpret_cast<double*>(xbar + 1);  // [k 0..l][warp 16][8]
     const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = 2 * l + 1;
