@@ -365,17 +365,24 @@ batch_dlda_kernel(const void* __restrict__ slabs, int n, int l, const double* __
         if (tid == 0 && k + kBStages <= l) issue(k + kBStages, s);
     }
     __syncthreads();
+    // per-power totals over the 16 warps, one thread per (power, value), in place in warp 0's row
+    // (only this thread touches its column); then dL/da_h = sum_k c'_k s_hk by H threads
+    for (int t = tid; t < (l + 1) * 8; t += kBTh) {
+        const int kr = t >> 3, q = t & 7;
+        double sk = 0.0;
+#pragma unroll
+        for (int wp = 0; wp < 16; ++wp) sk += red[(kr * 16 + wp) * 8 + q];
+        red[(kr * 16) * 8 + q] = sk;
+    }
+    __syncthreads();
     if (tid < H) {
         const int h = tid;
         const double* dc = coef + (size_t)(g * H + h) * 2 * w + w;
         double acc = 0.0;
         for (int kk = 0; kk < w; ++kk) {  // ascending k = -l..l
             const int k = kk - l;
-            const int idx = k == 0 ? 2 * h : (k > 0 ? 2 * h : 2 * h + 1);
             const int kr = k >= 0 ? k : -k;
-            double sk = 0.0;
-            for (int wp = 0; wp < 16; ++wp) sk += red[(kr * 16 + wp) * 8 + (k == 0 ? h : idx)];
-            acc += dc[kk] * sk;
+            acc += dc[kk] * red[(kr * 16) * 8 + (k == 0 ? h : (k > 0 ? 2 * h : 2 * h + 1))];
         }
         dlda[(int64_t)g * H + h] = acc;
     }
