@@ -737,7 +737,8 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
         const char* e = std::getenv("FGFRFT_NODE_FUSED_ROWMAX");
         return !e || std::atoi(e) != 0;
     }();
-    const bool fused = fuse_ok && n % kOzTileA == 0 && rows == (int64_t)nn &&
+    // (only the narrow, r <= 32, epilogue implements the fusion)
+    const bool fused = fuse_ok && narrow && n % kOzTileA == 0 && rows == (int64_t)nn &&
                        (FGFRFT_SMS / ibs) * ibs * 10 >= FGFRFT_SMS * 9;
     const int64_t wrows = (int64_t)r * pad_rows(n);
     if (fused) {

@@ -509,7 +509,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     // unit schedule: strided over the clusters. Row-max node operators (out.rmax): the host sizes
     // the grid as a multiple of the row blocks per column (rn / 128), so every unit of a CTA lies in
     // the same row block and the row max stays in registers until one flush at the end
-    const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr;
+    const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32;  // (the skinny epilogue)
     const int ub = cid, ue = units, us = nclusters;
     auto unit_mt = [&](int u) { return u / ngroups; };
     auto unit_nt = [&](int u) { return (u % ngroups) * CL + rank; };

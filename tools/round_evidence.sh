@@ -10,3 +10,4 @@ FGFRFT_ENGINE=dmma python tools/bench_configs.py --configs 2,3,4 > gpurun_out/ev
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ev/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ev/ncu_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"ozgemm_kernel|node_combine|rsynth|rapply_fused" -c 12 -o gpurun_out/ev/prof python tools/profile_kernels.py > gpurun_out/ev/ncu_full.log 2>&1
 tail -2 gpurun_out/ev/pytest_gpu.log
+ncu --set full --clock-control none --import-source on -k regex:"batch_forward|batch_dlda" -c 2 -o gpurun_out/ev/prof_c5 python tools/bench_configs.py --configs 5 > gpurun_out/ev/ncu_c5.log 2>&1
