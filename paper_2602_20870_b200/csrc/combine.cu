@@ -708,8 +708,8 @@ namespace fgb {
 // accumulated by upper-triangular 8x8 DMMA tiles, warp w taking positions 4w..4w+3 of every
 // chunk. 32-position chunks double buffered through cp.async, two CTAs per SM. MSE = false: Y only.
 constexpr int kNdMaxR = 48;
-constexpr int kNdP = 32;
-constexpr int kNdLd = 36;                          // = 4 mod 16: the DMMA fragment loads are conflict free
+constexpr int kNdP = 64;                           // positions per chunk (one __syncthreads per chunk)
+constexpr int kNdLd = 68;                          // = 4 mod 16: the DMMA fragment loads are conflict free
 constexpr int kNdT = (kNdMaxR + 1 + 7) / 8;        // 8-row tiles of [Z'; Xc]
 constexpr int kNdPairs = kNdT * (kNdT + 1) / 2;    // upper-triangular tile pairs of the Gram
 
@@ -769,29 +769,34 @@ node_combine_kernel(const double* __restrict__ zin, const double* __restrict__ x
         cp_async_commit();
         const double* zc = zb + buf * r8 * kNdLd;
         const double* xs = zc + r * kNdLd;
-        double yacc[4][2];
+        constexpr int PB = kNdP / 8;  // 8-position blocks per chunk
+        double yacc[PB][2];
 #pragma unroll
-        for (int pb = 0; pb < 4; ++pb) yacc[pb][0] = yacc[pb][1] = 0.0;
+        for (int pb = 0; pb < PB; ++pb) yacc[pb][0] = yacc[pb][1] = 0.0;
 #pragma unroll
         for (int k = 0; k < 2 * T; ++k) {
             if (k < nks) {
                 const double* zrow = zc + (4 * k + t) * kNdLd + g;
 #pragma unroll
-                for (int pb = 0; pb < 4; ++pb) dmma884(yacc[pb][0], yacc[pb][1], cy[k], zrow[8 * pb]);
+                for (int pb = 0; pb < PB; ++pb) dmma884(yacc[pb][0], yacc[pb][1], cy[k], zrow[8 * pb]);
             }
         }
         if (MSE) {
-            int pi = 0;
 #pragma unroll
-            for (int mt = 0; mt < T; ++mt) {
-                const double av = mt < t8 ? zc[(8 * mt + g) * kNdLd + 4 * warp + t] : 0.0;
+            for (int cg = 0; cg < kNdP / 32; ++cg) {  // K = 4 positions per warp per 32-position group
+                const int col = 32 * cg + 4 * warp + t;
+                int pi = 0;
 #pragma unroll
-                for (int nt = mt; nt < T; ++nt, ++pi)
-                    if (nt < t8) dmma884(gacc[pi][0], gacc[pi][1], av, zc[(8 * nt + g) * kNdLd + 4 * warp + t]);
+                for (int mt = 0; mt < T; ++mt) {
+                    const double av = mt < t8 ? zc[(8 * mt + g) * kNdLd + col] : 0.0;
+#pragma unroll
+                    for (int nt = mt; nt < T; ++nt, ++pi)
+                        if (nt < t8) dmma884(gacc[pi][0], gacc[pi][1], av, zc[(8 * nt + g) * kNdLd + col]);
+                }
             }
         }
 #pragma unroll
-        for (int pb = 0; pb < 4; ++pb)
+        for (int pb = 0; pb < PB; ++pb)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int p = 8 * pb + 2 * t + e;
