@@ -175,6 +175,7 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
         for (int r = 0; r < 4; ++r)
 #pragma unroll
             for (int c = 0; c < 2; ++c) acc[h][r][c][0] = acc[h][r][c][1] = 0.f;
+#pragma unroll 2
     for (int j = 0; j < kBN; ++j) {
         const float2 x0 = xs[(2 * cb) * kBN + j], x1 = xs[(2 * cb + 1) * kBN + j];
 #pragma unroll
