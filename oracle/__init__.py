@@ -119,7 +119,11 @@ class PowerCache:
     """transform.hpp:41-80. Slabs are stored as a C-contiguous [l, n, n] array whose slab k-1
     is P_k^T in row-major, i.e. P_k in column-major (the Eigen layout)."""
 
-    def __init__(self, f: np.ndarray, l: int, memory_budget: int = DEFAULT_MEMORY_BUDGET):
+    def __init__(self, f: np.ndarray, l: int, memory_budget: int = DEFAULT_MEMORY_BUDGET,
+                 real_recursion: bool = False):
+        """real_recursion: when Im F == 0, run the recursion as real dgemm (a quarter of the flops)
+        and store the slabs as complex128. Same products up to summation order (~1 ulp); used only
+        to build large oracle caches (bench.py's CPU baseline at config 3) outside timed regions."""
         if l < 1:
             raise ParameterError("PowerCache: truncation order must be >= 1")
         f = np.asfortranarray(f, dtype=np.complex128)
@@ -133,6 +137,13 @@ class PowerCache:
         self.fingerprint = content_fingerprint(f)
         self.slabs = np.empty((l, n, n), dtype=np.complex128)
         self.slabs[0] = f.T
+        if real_recursion and not np.any(f.imag):
+            ft = np.ascontiguousarray(f.real.T)
+            cur = ft.copy()
+            for k in range(2, l + 1):
+                cur = cur @ ft
+                self.slabs[k - 1] = cur
+            return
         for k in range(2, l + 1):
             # P_k = F @ P_{k-1} (left multiply, transform.hpp:58); stored transposed:
             # P_k^T = P_{k-1}^T @ F^T

@@ -184,6 +184,7 @@ int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype,
     auto* c = new fgfrft_cache();
     c->n = n;
     c->l = l;
+    c->budget = budget;
     c->dtype = dtype;
     c->device = device;
     c->elem = elem;
@@ -230,11 +231,16 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
+    for (cudaEvent_t e : c->pk_es) cudaEventDestroy(e);
+    for (cudaEvent_t e : {c->pk_e0, c->pk_eg, c->pk_ex})
+        if (e) cudaEventDestroy(e);
+    if (c->pk_s) cudaStreamSynchronize(c->pk_s);
+    if (c->pk_g) cudaStreamSynchronize(c->pk_g);
     for (DevBuf* b : {&c->coef, &c->q, &c->m, &c->partial, &c->s, &c->x, &c->y, &c->g, &c->xc, &c->lpart,
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
                       &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
                       &c->by, &c->es, &c->ee, &c->erm, &c->nd_tab, &c->nd_p, &c->nd_d0, &c->nd_bsl, &c->nd_bex,
-                      &c->nd_w, &c->nd_z})
+                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ydy})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -242,6 +248,8 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->nd_evt) cudaEventDestroy(c->nd_evt);
     if (c->xc_evt) cudaEventDestroy(c->xc_evt);
     if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+    if (c->pk_s) cudaStreamDestroy(c->pk_s);
+    if (c->pk_g) cudaStreamDestroy(c->pk_g);
     if (c->slabs) cudaFree(c->slabs);
     if (c->colp) cudaFree(c->colp);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -476,6 +484,16 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
                                        (int)b, c->partial.as<double>(), static_cast<double*>(y_dev), c->stream),
                    2);
         return FGFRFT_OK;
+    }
+    if ((n_alpha == 1 || n_alpha == 2 || n_alpha == 4) && packed_enabled(c) && use_int8_gemm(c, b) &&
+        ensure_packed(c)) {
+        // Q(a)^T = Q(-a) bit-exactly (sinc.hpp coefficient mirror): the inverse synthesises Q(-a)
+        if (inverse) {
+            std::vector<double> al(alphas, alphas + n_alpha);
+            for (double& v : al) v = -v;
+            if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
+        }
+        return packed_products(c, coef, 2 * l_used + 1, n_alpha, x_dev, b, y_dev, l_used);
     }
     const int chunk = alpha_chunk(c, n_alpha);
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
@@ -1255,6 +1273,266 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
     return FGFRFT_OK;
 }
 
+// ------------------------------------------------------------------ memory budget of aux structures
+
+// The reference's budget counts L n^2 16 bytes (transform.hpp:46-53); auxiliary representations
+// are admitted while that count plus every admitted auxiliary byte stays within the handle's budget.
+bool aux_fits(fgfrft_cache* c, uint64_t bytes) {
+    const unsigned __int128 ref = (unsigned __int128)c->l * (uint64_t)c->n * (uint64_t)c->n * 16;
+    return ref + c->aux_bytes + bytes <= (unsigned __int128)c->budget;
+}
+
+// ------------------------------------------------------------------ packed step route (packed.cu)
+//
+// One or a few orders over a real cache with a large signal batch (config 3 / 4): Q(a) and
+// dQ/da from ONE pass over the packed slabs (6 B per element instead of 8), the row maxima of
+// Q / dQ left by the same kernel, one slicing pass, and ONE Ozaki GEMM [Y; dY] = [Q; dQ] X;
+// loss and dL/da = 2/(NB) Re<Y - Xc, dY> from a single elementwise pass (no G, no G X^H GEMM).
+bool packed_enabled(const fgfrft_cache* c) {
+    static const bool off = [] {
+        const char* e = std::getenv("FGFRFT_PACKED");
+        return e && !std::strcmp(e, "0");
+    }();
+    return !off && c->real && c->dtype == FGFRFT_C128 && !c->shard && c->graphs == 0 && c->n >= 512 &&
+           engine_of(c) == FGFRFT_ENGINE_AUTO;
+}
+
+// true when the packed slabs are resident (built on first use, counted against the budget).
+bool ensure_packed(fgfrft_cache* c) {
+    if (c->pk_state) return c->pk_state > 0;
+    const uint64_t bytes = (uint64_t)packed_bytes((int)c->n, c->l);
+    const uint64_t sbytes = (uint64_t)packed_scale_elems((int)c->n, c->l) * sizeof(double);
+    if (!aux_fits(c, bytes + sbytes) || c->pk.ensure(bytes) != cudaSuccess || c->pks.ensure(sbytes) != cudaSuccess) {
+        cudaGetLastError();
+        c->pk.release();
+        c->pks.release();
+        c->pk_state = -1;
+        return false;
+    }
+    ProfScope ps(KC_SLICE, c->stream);
+    if (launch_pack_tiles(c->slabs, (int)c->n, c->l, c->pk.p, c->pks.as<double>(), c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        c->pk.release();
+        c->pks.release();
+        c->pk_state = -1;
+        return false;
+    }
+    g_launches += 1;
+    c->aux_bytes += bytes + sbytes;
+    c->pk_state = 1;
+    return true;
+}
+
+// ---- the pipelined form: row-complete shells
+//
+// The step is the sum of an HBM-bound pass (synthesis from the packed slabs) and a tensor-bound
+// pass (the Ozaki GEMM). They overlap by ROW SHELLS: the tile pairs are enumerated I-major
+// (pairs_before), so the pairs whose smaller tile index falls in a row range are one index range,
+// and once it is synthesised those rows of Q (and dQ) are complete -- their row maxima, slicing and
+// product rows Y[r0:r1] = Q[r0:r1, :] X can go. The synthesis + slicing of shell s+1 (side stream
+// S) runs while the GEMM of shell s (stream G, high priority, persistent grid capped so the
+// synthesis keeps SMs) runs; no kernel waits on another (stream events only). Shell bounds come
+// from a small DP over a cost model (the first shells have the most pairs per row).
+static double pk_env(const char* name, double dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atof(e) : dflt;
+}
+
+// Shell plan for n rows, `rows` operator blocks (1, 2, 4), b signals, L powers: DP over 128-row
+// block boundaries minimising S_0 + sum_s max(sigma S_s, gamma G_(s-1)) + G_last (+ a per-shell
+// launch overhead), S = synthesis + slicing of a shell, G = its GEMM. Memoised per shape.
+static std::vector<PkShell> pk_plan(int64_t n, int rows, int64_t b, int l) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int T = (int)ceil_div(n, kOzTileA);
+    // Default: one shell (no overlap). Measured on B200 at config 3: the packed synthesis is
+    // issue-bound per SM (FP64 decode + accumulate, ~100 SM-ms) and the GEMM tensor-bound (~115
+    // SM-ms), so sharing the SMs cannot beat running them back to back by more than ~14%, and the
+    // measured 4-8 shell pipelines lost 0.2-0.5 ms to the split. FGFRFT_PIPE_SHELLS
+    // enables the pipeline for experiments.
+    const int maxc = (int)pk_env("FGFRFT_PIPE_SHELLS", 1);
+    const double hbm = 6.3e12, i8 = 3.7e15, slice_bw = 4.0e12;
+    const double sigma = pk_env("FGFRFT_PIPE_SIGMA", 1.25), gamma = pk_env("FGFRFT_PIPE_GAMMA", 1.45);
+    const double over = pk_env("FGFRFT_PIPE_OVERHEAD_US", 6.0) * 1e-6;
+    auto tile_of = [&](int blk) { return std::min(nt, blk * (kOzTileA / kTile)); };
+    auto S = [&](int a, int z) {  // synthesis + slicing of block rows [a, z)
+        const double pairs = (double)(packed_pairs_before(tile_of(z), nt) - packed_pairs_before(tile_of(a), nt));
+        const double rws = (double)std::min<int64_t>(n, (int64_t)z * kOzTileA) - (double)a * kOzTileA;
+        return pairs * 2.0 * kTileElems * 5.0 * l / hbm + rows * rws * n * 14.0 / slice_bw;
+    };
+    auto G = [&](int a, int z) {
+        const double rws = (double)std::min<int64_t>(n, (int64_t)z * kOzTileA) - (double)a * kOzTileA;
+        return rows * rws * 2.0 * b * n * 2.0 * 21.0 / i8;
+    };
+    std::vector<PkShell> out;
+    std::vector<int> bounds{0, T};
+    if (maxc > 1 && T >= 4) {
+        // f[c][j][k]: best cost of shells covering blocks [0, k) with c shells, the last being [j, k)
+        const double inf = 1e30;
+        std::vector<double> f((size_t)(maxc + 1) * (T + 1) * (T + 1), inf);
+        std::vector<int> arg(f.size(), -1);
+        auto at = [&](int c, int j, int k) -> size_t { return ((size_t)c * (T + 1) + j) * (T + 1) + k; };
+        for (int k = 1; k <= T; ++k) f[at(1, 0, k)] = S(0, k) + over;
+        for (int c = 2; c <= maxc; ++c)
+            for (int j = 1; j < T; ++j)
+                for (int k = j + 1; k <= T; ++k)
+                    for (int i = 0; i < j; ++i) {
+                        const double pv = f[at(c - 1, i, j)];
+                        if (pv >= inf) continue;
+                        const double v = pv + std::max(sigma * S(j, k), gamma * G(i, j)) + over;
+                        if (v < f[at(c, j, k)]) {
+                            f[at(c, j, k)] = v;
+                            arg[at(c, j, k)] = i;
+                        }
+                    }
+        double best = inf;
+        int bc = 1, bj = 0;
+        for (int c = 1; c <= maxc; ++c)
+            for (int j = 0; j < T; ++j) {
+                const double v = f[at(c, j, T)];
+                if (v < inf && v + G(j, T) < best) {
+                    best = v + G(j, T);
+                    bc = c;
+                    bj = j;
+                }
+            }
+        bounds.assign(1, T);
+        int c = bc, j = bj, k = T;
+        while (c >= 1) {
+            bounds.push_back(j);
+            const int i = arg[at(c, j, k)];
+            k = j;
+            j = i;
+            --c;
+        }
+        std::reverse(bounds.begin(), bounds.end());
+    }
+    for (size_t s = 0; s + 1 < bounds.size(); ++s) {
+        PkShell sh;
+        sh.r0 = (int)std::min<int64_t>(n, (int64_t)bounds[s] * kOzTileA);
+        sh.r1 = (int)std::min<int64_t>(n, (int64_t)bounds[s + 1] * kOzTileA);
+        sh.p0 = (int)packed_pairs_before(tile_of(bounds[s]), nt);
+        sh.p1 = (int)packed_pairs_before(tile_of(bounds[s + 1]), nt);
+        if (sh.r1 > sh.r0) out.push_back(sh);
+    }
+    return out;
+}
+
+int ensure_pipe_streams(fgfrft_cache* c) {
+    if (c->pk_g) return FGFRFT_OK;
+    int lo = 0, hi = 0;
+    FGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FGB_CUDA(cudaStreamCreateWithPriority(&c->pk_s, cudaStreamNonBlocking, lo));
+    FGB_CUDA(cudaStreamCreateWithPriority(&c->pk_g, cudaStreamNonBlocking, hi));  // GEMM CTAs placed first
+    for (auto* e : {&c->pk_e0, &c->pk_eg, &c->pk_ex})
+        FGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return FGFRFT_OK;
+}
+
+// rows (1, 2 or 4) real n x n operators M_r (table rows r of coef, width coef_ld, l_used powers)
+// from the packed slabs, Y_r = M_r X into y (stride 2 n b doubles), shell-pipelined.
+int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
+                    void* y, int l_used) {
+    const int S = oz_slices_default();
+    const int64_t n = c->n, mp = pad_rows(n), sl = n * n, kp = pad_k(n);
+    const int64_t bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
+    const uint64_t key = ((uint64_t)n << 40) ^ ((uint64_t)rows << 32) ^ ((uint64_t)b << 8) ^ (uint64_t)l_used;
+    if (c->pk_plan_key != key) {
+        c->pk_plan = pk_plan(n, rows, b, l_used);
+        c->pk_plan_key = key;
+    }
+    const std::vector<PkShell>& plan = c->pk_plan;
+    int64_t srows = 0;  // sliced rows over all shells (each shell padded to 128)
+    for (const PkShell& sh : plan) srows += pad_rows(sh.r1 - sh.r0);
+    const int64_t exps_ints = ceil_div((int64_t)rows * srows, 2) * 2;
+    FGB_CUDA(c->q.ensure((size_t)rows * sl * sizeof(double)));
+    FGB_CUDA(c->qsl.ensure((size_t)S * rows * srows * kp));
+    FGB_CUDA(c->qex.ensure((size_t)exps_ints * sizeof(int) + (size_t)rows * mp * sizeof(unsigned long long)));
+    FGB_CUDA(c->xsl.ensure((size_t)S * bp * kp));
+    FGB_CUDA(c->xex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
+    if (int st = ensure_pipe_streams(c)) return st;
+    int* exps = c->qex.as<int>();
+    unsigned long long* rmax = reinterpret_cast<unsigned long long*>(exps + exps_ints);
+    double* q = c->q.as<double>();
+    FGB_CUDA(cudaEventRecord(c->pk_e0, c->stream));
+    FGB_CUDA(cudaStreamWaitEvent(c->pk_s, c->pk_e0, 0));
+    FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_e0, 0));
+    // G: X sliced once (B operand: rows 2j + comp, K = signal index), while S synthesises shell 0
+    {
+        int* xe = c->xex.as<int>();
+        const OzView v{static_cast<const double*>(x_dev), 2 * n, 2, 0, 1, 0, (int)(2 * b), (int)bp, 1, (int)n,
+                       (int)kp, false};
+        ProfScope ps(KC_SLICE, c->pk_g);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->xsl.as<int8_t>(), xe,
+                                   reinterpret_cast<unsigned long long*>(xe + bp), c->pk_g),
+                   3);
+    }
+    FGB_CUDA(cudaMemsetAsync(rmax, 0, (size_t)rows * mp * sizeof(unsigned long long), c->pk_s));
+    const int gcap = (int)pk_env("FGFRFT_PIPE_GEMM_CTAS", 100);
+    const int syn_cap = (int)pk_env("FGFRFT_PIPE_SYN_CTAS", FGFRFT_SMS - gcap);  // one CTA per SM
+    if (c->pk_es.size() < plan.size()) {
+        const size_t have = c->pk_es.size();
+        c->pk_es.resize(plan.size(), nullptr);
+        for (size_t i = have; i < plan.size(); ++i)
+            FGB_CUDA(cudaEventCreateWithFlags(&c->pk_es[i], cudaEventDisableTiming));
+    }
+    int64_t row_off = 0;
+    for (size_t s = 0; s < plan.size(); ++s) {
+        const PkShell& sh = plan[s];
+        const int64_t rv = sh.r1 - sh.r0, rp = pad_rows(rv);
+        int8_t* dst = c->qsl.as<int8_t>() + (size_t)S * rows * row_off * kp;
+        int* ex = exps + rows * row_off;
+        {
+            ProfScope ps(KC_SYNTH, c->pk_s);
+            // shell 0 runs alone (the GEMM has nothing yet): full grid; later shells share the GPU
+            FGB_LAUNCH(launch_psynth(c->pk.p, c->pks.as<double>(), (int)n, l_used, c->l, coef, coef_ld, rows, q, sl, rmax, mp,
+                                     c->pk_s, sh.p0, sh.p1, s == 0 ? 0 : syn_cap),
+                       1);
+        }
+        {
+            OzView v{q + sh.r0, 1, n, sl, 0, 0, (int)rv, (int)rp, rows, (int)n, (int)kp, true};
+            v.rmb = mp;
+            ProfScope ps(KC_SLICE, c->pk_s);
+            FGB_LAUNCH(launch_oz_slice_ready(v, S, kOzTileA, dst, ex, rmax + sh.r0, c->pk_s), 1);
+        }
+        FGB_CUDA(cudaEventRecord(c->pk_es[s], c->pk_s));
+        FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_es[s], 0));
+        {
+            ProfScope ps(KC_I8GEMM, c->pk_g);
+            const bool last = s + 1 == plan.size();
+            FGB_LAUNCH(launch_ozgemm(S, 1, dst, ex, (int)(rows * rp), c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
+                                     (int)kp, static_cast<double*>(y) + 2 * sh.r0, n, 2 * n * b, (int)rv, (int)rp,
+                                     (int)(2 * b), c->pk_g, nullptr, 0, last ? 0 : gcap),
+                       1);
+        }
+        row_off += rp;
+    }
+    FGB_CUDA(cudaEventRecord(c->pk_eg, c->pk_g));
+    FGB_CUDA(cudaStreamWaitEvent(c->stream, c->pk_eg, 0));
+    return FGFRFT_OK;
+}
+
+int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,
+                    void* y_dev, double* loss_dev, double* dlda_dev) {
+    const int64_t n = c->n, blk = 2 * n * b;  // doubles per n x b complex block
+    const int rows = 2 * n_alpha;             // table rows [c(a_0) ..][c'(a_0) ..]: Q_a then dQ_a
+    FGB_CUDA(c->ydy.ensure((size_t)rows * blk * sizeof(double)));
+    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l)) return st;
+    if (int st = wait_xc(c)) return st;
+    FGB_CUDA(c->lpart.ensure(mse_dy_part_elems() * sizeof(double)));
+    const double norm = 1.0 / ((double)n * (double)b);
+    ProfScope ps(KC_ELEMWISE, c->stream);
+    for (int a = 0; a < n_alpha; ++a) {
+        const double* ya = c->ydy.as<double>() + (size_t)a * blk;
+        FGB_LAUNCH(launch_mse_dy(ya, ya + (size_t)n_alpha * blk, xc_dev, n * b,
+                                 y_dev ? static_cast<double*>(y_dev) + (size_t)a * blk : nullptr, c->lpart.as<double>(),
+                                 norm, loss_dev + a, dlda_dev + a, c->stream),
+                   2);
+    }
+    c->last_route = 3;
+    c->last_nodes = 0;
+    return FGFRFT_OK;
+}
+
 }  // namespace fgbi
 
 // ===================================================================================== C ABI
@@ -1688,6 +1966,10 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     }
     c->last_route = use_power_route(c, n_alpha) ? 1 : 0;
     c->last_nodes = 0;
+    if (!use_power_route(c, n_alpha) && n_alpha <= 2 && packed_enabled(c) && use_int8_gemm(c, b) &&
+        !use_fused_apply(c, n_alpha, b) && ensure_packed(c))
+        return mse_packed_step(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
+                               static_cast<double*>(dlda_dev));
     if (use_power_route(c, n_alpha)) {
         FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
         if (int st = mse_power_route(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),

@@ -163,6 +163,17 @@ cudaError_t launch_node_combine(const double* zin, const double* xc, int64_t cou
 cudaError_t launch_combine(int mode, const double* z, const double* x, const double* xc, int64_t count, int l,
                            const double* coef, int n_alpha, double norm, double* y, double* partial, double* s,
                            double* loss, cudaStream_t stream);
+// packed.cu (the packed power cache and the one- / two-order step route)
+size_t packed_bytes(int n, int l);
+cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream);
+cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
+                          int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
+                          int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0);
+size_t packed_scale_elems(int n, int l);
+int64_t packed_pairs_before(int I, int nt);
+size_t mse_dy_part_elems();
+cudaError_t launch_mse_dy(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
+                          double norm, double* loss, double* dlda, cudaStream_t stream);
 }  // namespace fgb
 
 using namespace fgb;
@@ -283,6 +294,12 @@ struct DevBuf {
 
 using namespace fgbi;
 
+// One row shell of the pipelined packed route (capi.cu packed_products).
+struct PkShell {
+    int r0, r1;  // rows [r0, r1)
+    int p0, p1;  // I-major tile pairs [p0, p1)
+};
+
 struct fgfrft_cache {
     int64_t n = 0;
     int l = 0;
@@ -344,6 +361,22 @@ struct fgfrft_cache {
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t xc_evt = nullptr;
     bool xc_pending = false;
+    // Memory budget of the handle (transform.hpp:46-53 counts L n^2 16 bytes): auxiliary device
+    // representations (packed slabs, INT8 digit slices) are built only while the reference count
+    // plus their bytes stays within it; otherwise the routes that need them are not taken.
+    uint64_t budget = 0;
+    uint64_t aux_bytes = 0;
+    // Packed power cache (packed.cu): 48-bit fixed-point tiles + per-tile scales, for the one- /
+    // two-order step and apply route (real F). 0 not built, 1 ready, -1 unavailable.
+    int pk_state = 0;
+    DevBuf pk, pks, ydy;
+    // shell pipeline of the packed route: side streams (S synthesis + slicing, G GEMMs, high
+    // priority), fork / join events, one event per shell, the memoised shell plan
+    cudaStream_t pk_s = nullptr, pk_g = nullptr;
+    cudaEvent_t pk_e0 = nullptr, pk_eg = nullptr, pk_ex = nullptr;
+    std::vector<cudaEvent_t> pk_es;
+    std::vector<PkShell> pk_plan;
+    uint64_t pk_plan_key = 0;
     double* coef_h = nullptr;  // pinned staging for the coefficient tables
     size_t coef_h_cap = 0;
     cudaEvent_t coef_evt = nullptr;
@@ -417,5 +450,12 @@ int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype,
                   fgfrft_cache** made);
 int check_orthogonal(fgfrft_cache* c, const double* fr, double* scratch);
 int check_spectrum(const fgfrft_spectrum* s);
+bool aux_fits(fgfrft_cache* c, uint64_t bytes);
+bool packed_enabled(const fgfrft_cache* c);
+bool ensure_packed(fgfrft_cache* c);
+int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
+                    void* y, int l_used);
+int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,
+                    void* y_dev, double* loss_dev, double* dlda_dev);
 
 }  // namespace fgbi

@@ -450,12 +450,11 @@ size_t combine_partial_elems(int tp) {
 
 template <int MODE>
 static cudaError_t combine_attr() {
-    static bool done = false;
-    if (done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(combine_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)combine_smem_bytes(kCbMaxT));
-    if (e == cudaSuccess) done = true;
-    return e;
+    static PerDeviceOnce done;
+    return done.run([] {
+        return cudaFuncSetAttribute(combine_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)combine_smem_bytes(kCbMaxT));
+    });
 }
 
 // mode 0 (MSE: xc = clean signals, y optional), 1 (apply: y required), 2 (dots: xc = G, A blocks).
@@ -480,16 +479,16 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
         case 1:
         case 3: {
             const size_t ysm = combine_y_smem_bytes(tp);
-            static bool yattr = false;
-            if (!yattr) {
-                if ((e = cudaFuncSetAttribute(combine_y_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)combine_y_smem_bytes(kCbMaxT))) != cudaSuccess)
-                    return e;
-                if ((e = cudaFuncSetAttribute(combine_y_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)combine_y_smem_bytes(kCbMaxT))) != cudaSuccess)
-                    return e;
-                yattr = true;
-            }
+            static PerDeviceOnce yattr;
+            if ((e = yattr.run([] {
+                     cudaError_t r = cudaFuncSetAttribute(combine_y_kernel<true>,
+                                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          (int)combine_y_smem_bytes(kCbMaxT));
+                     if (r != cudaSuccess) return r;
+                     return cudaFuncSetAttribute(combine_y_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)combine_y_smem_bytes(kCbMaxT));
+                 })) != cudaSuccess)
+                return e;
             const int64_t ych = (count + kCyP - 1) / kCyP;
             const int yctas = (int)(ych < 2 * FGFRFT_SMS ? ych : 2 * FGFRFT_SMS);
             if (mode == 1) {
@@ -912,13 +911,12 @@ template <bool MSE, int T>
 static cudaError_t node_combine_t(int ctas, size_t smem, cudaStream_t st, const double* zin, const double* xc,
                                   int64_t count, int r, int rp, const double* pc, int n_alpha, double* y, double* lp,
                                   double* gp) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(node_combine_kernel<MSE, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)node_smem_bytes(8 * T - 1));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    if (cudaError_t e = attr.run([] {
+            return cudaFuncSetAttribute(node_combine_kernel<MSE, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)node_smem_bytes(8 * T - 1));
+        }))
+        return e;
     node_combine_kernel<MSE, T><<<ctas, 256, smem, st>>>(zin, xc, count, r, rp, pc, n_alpha, y, lp, gp);
     return cudaGetLastError();
 }

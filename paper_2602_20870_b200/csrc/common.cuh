@@ -1,6 +1,7 @@
 // common.cuh -- sm_100a device helpers shared by the FGFRFT kernels.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -142,6 +143,23 @@ __device__ __forceinline__ double dsinc_deriv(double x) {
 }
 
 // ---------------------------------------------------------------- misc
+
+// One-time per-DEVICE setup (cudaFuncSetAttribute opt-ins are per device): a bit per device,
+// set with an atomic OR after the first success. Concurrent first calls may both run f (the
+// attribute calls are idempotent); no unsynchronised static flag.
+struct PerDeviceOnce {
+    std::atomic<uint64_t> mask{0};
+    template <class F>
+    cudaError_t run(F&& f) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = 1ull << (dev & 63);
+        if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+        const cudaError_t e = f();
+        if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+        return e;
+    }
+};
 
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -32,6 +32,7 @@ struct OzView {
                      //    P_(kk-L+1)(j, i); one batch block (nb = 1, rp = padded n^2)
     int nt = 0;      // tiles per side of a tiled slab
     int l = 0, tp2 = 0;  // modes 3 / 4: L and the padded term count (64 or 128)
+    int64_t rmb = 0;     // slicing from ready row maxima: slot of row (bt, r) = bt * rmb + r (0: bt * rp + r)
 };
 
 
@@ -69,6 +70,7 @@ struct OzOut {
     unsigned long long* rmax = nullptr;
     const double* dg = nullptr;
     int rn = 0, rnp = 0;
+    int max_ctas = 0;  // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)
@@ -93,6 +95,6 @@ int oz_bk(int slices);  // bytes of K per stage / per digit block of the sliced 
 int oz_zdigits();       // digits of Z written by the CM 2 epilogue (the combine GEMM's digit count)
 cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                           const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
-                          cudaStream_t stream, double* const* peers = nullptr, int npeers = 0);
+                          cudaStream_t stream, double* const* peers = nullptr, int npeers = 0, int max_ctas = 0);
 
 }  // namespace fgb

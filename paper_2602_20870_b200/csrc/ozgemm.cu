@@ -197,6 +197,13 @@ __device__ __forceinline__ void oz_tile_load(const OzView& v, int row0, int k0, 
     }
 }
 
+// Row-max slot of sliced row `row` (= bt * rp + r): bt * rmb + r when the view sets rmb.
+__device__ __forceinline__ int64_t oz_rm_index(const OzView& v, int row) {
+    if (!v.rmb) return row;
+    const int bt = row / v.rp;
+    return (int64_t)bt * v.rmb + (row - bt * v.rp);
+}
+
 // Pass 1: per-row max |a| (as ordered bits of a non-negative double) via atomicMax.
 __global__ void __launch_bounds__(256) oz_rowmax_kernel(OzView v, unsigned long long* rowmax) {
     __shared__ double t[64][65];
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzView v, const unsigned 
     const int u = threadIdx.x;  // (g_local, c, r8): one 16-byte digit run per thread and slice
     const int gl = u >> 5, c = (u >> 3) & 3, r8 = u & 7;
     const int rl = gl * 8 + r8, row = row0 + rl;
-    const double mx = __longlong_as_double((long long)rowmax[row]);
+    const double mx = __longlong_as_double((long long)rowmax[oz_rm_index(v, row)]);
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     if (blockIdx.y == 0 && c == 0) exps[row] = e;
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(64) oz_slice_direct_kernel(OzView v, const uns
     const int row = blockIdx.x * 64 + threadIdx.x, k0 = blockIdx.y * 64;
     bool ok;
     const double* p = oz_row_ptr(v, row, &ok);
-    const double mx = __longlong_as_double((long long)rowmax[row]);
+    const double mx = __longlong_as_double((long long)rowmax[oz_rm_index(v, row)]);
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     if (blockIdx.y == 0) exps[row] = e;
@@ -907,13 +914,12 @@ cudaError_t launch_oz_slice_ready(const OzView& v, int slices, int tr, int8_t* d
 template <int S, int CM, int CL, int BN = kOzBN>
 static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, const int8_t* b, const int* eb, int ntiles,
                                 int kp, const OzOut& out, cudaStream_t stream) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (OzCfg<S, BN>::smem));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static PerDeviceOnce attr;
+    if (cudaError_t e = attr.run([] {
+            return cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (OzCfg<S, BN>::smem));
+        }))
+        return e;
     const int units = mtiles * (ntiles / CL);
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kOzThreads);
@@ -927,7 +933,10 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
     cfg.attrs = at;
     cfg.numAttrs = 1;
     // persistent grid = the clusters that are co-resident (GPC sizes are not multiples of CL)
-    static int max_clusters = 0;
+    static std::atomic<int> max_clusters_dev[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int max_clusters = max_clusters_dev[dev & 63].load(std::memory_order_relaxed);
     if (max_clusters == 0) {
         cfg.gridDim = dim3(FGFRFT_SMS / CL * CL);
         int mc = 0;
@@ -936,7 +945,9 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
             mc = FGFRFT_SMS / CL;
         }
         max_clusters = mc;
+        max_clusters_dev[dev & 63].store(mc, std::memory_order_relaxed);
     }
+    if (out.max_ctas > 0 && out.max_ctas / CL < max_clusters) max_clusters = out.max_ctas / CL > 0 ? out.max_ctas / CL : 1;
     int clusters = units < max_clusters ? units : max_clusters;
     if (CM == 0 && CL == 1 && out.rmax) {  // row-max mode: a multiple of the row blocks per column
         const int ibs = out.rn / kOzBM;
@@ -1003,7 +1014,7 @@ cudaError_t launch_ozgemm_ex(int slices, int cm, const int8_t* a, const int* ea,
 
 cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                           const int* eb, int nrows, int kp, double* c, int64_t ldc, int64_t sc, int mv, int mp, int nv,
-                          cudaStream_t stream, double* const* peers, int npeers) {
+                          cudaStream_t stream, double* const* peers, int npeers, int max_ctas) {
     if (cm > 1 || npeers < 0 || npeers > 7) return cudaErrorInvalidValue;
     OzOut out;
     for (int q = 0; q < npeers; ++q) out.peers[q] = peers[q];
@@ -1014,6 +1025,7 @@ cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, in
     out.mv = mv;
     out.mp = mp;
     out.nv = nv;
+    out.max_ctas = max_ctas;
     return launch_ozgemm_ex(slices, cm, a, ea, mrows, b, eb, nrows, kp, out, stream);
 }
 

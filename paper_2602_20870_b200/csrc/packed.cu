@@ -1,0 +1,415 @@
+// packed.cu -- the packed power cache and its synthesis kernel (the one- / two-order step route).
+//
+// The MSE step and the series apply of one or two orders are bound by streaming the L cached
+// powers once (transform.hpp:111-136: every call reads every slab). For a real F (every
+// BASELINE graph) the step route keeps, next to the exact FP64 slabs (which fgfrft_matrix /
+// fgfrft_grad still read, bit-exactly), a PACKED copy: each 32x32 tile of each power as 40-bit
+// fixed-point mantissas relative to a per-tile power of two,
+//     P_k[i, j] = m * 2^(e_kT - 38),  |m| <= 2^38,  max_T |P_k| < 2^e_kT,
+// stored as a 32-bit low plane and an 8-bit high plane of u = m + 2^39 (5 bytes per element
+// instead of 8: 37.5% fewer bytes on the HBM-bound pass). Decoding is exact integer arithmetic:
+// the double with high word 0x43300000 | hi and low word lo is 2^52 + u, so m = that - (2^52 +
+// 2^39) with no rounding; the tile scale is folded into the series coefficient (a power-of-two
+// product, exact), so each element costs one DADD and two DFMAs per order. Quantisation error:
+// <= 2^-39 of the tile's largest |entry| per element (a few 1e-12 relative on Q, measured in
+// tests/test_gpu_packed.py): inside the 1e-10 relative Frobenius parity bar; the
+// exact path (fgfrft_matrix / fgfrft_grad) is untouched.
+//
+// psynth_pairs_kernel mirrors rsynth_pairs_kernel (real.cu): one CTA per tile pair {(I,J),(J,I)},
+// a TMA bulk-copy ring of packed tiles, both tiles of Q updated from the same staged bytes. It
+// also leaves the row maxima |Q[i, :]| (as ordered double bits, atomicMax) that the Ozaki
+// slicing of Q for the product GEMM needs, so Q is read once by the slicer instead of twice.
+#include "common.cuh"
+
+namespace fgb {
+
+constexpr int kPkTileBytes = kTileElems * 5;  // lo32 plane (4096 B) + hi8 plane (1024 B)
+constexpr int kPkFrac = 38;
+__device__ constexpr double kPkMagic = 4503599627370496.0 + 549755813888.0;  // 2^52 + 2^39
+
+size_t packed_bytes(int n, int l) {  // pair-major records: npairs * L * 2 tiles
+    const int64_t nt = ceil_div(n, kTile);
+    return (size_t)(nt * (nt + 1) / 2) * (size_t)l * 2 * kPkTileBytes;
+}
+size_t packed_scale_elems(int n, int l) {
+    const int64_t nt = ceil_div(n, kTile);
+    return (size_t)(nt * (nt + 1) / 2) * (size_t)l * 2;
+}
+
+// One CTA per tile of every power: grid = l * ntiles, 256 threads x 4 elements.
+// Pair-major layout: tile pair p = {(I,J), (J,I)} (I-major order, pairs_before below), power k:
+// both tiles in one 10 KB record at ((p * L + k - 1) * 2 + slot) * 5120 bytes, slot 0 = (I,J),
+// slot 1 = (J,I) (a diagonal tile is stored in both slots), scales at (p * L + k - 1) * 2 + slot.
+// A CTA walking a pair streams one contiguous L * 10 KB region, one bulk copy per power.
+__host__ __device__ __forceinline__ int64_t pairs_before(int64_t I, int64_t nt) { return I * nt - I * (I - 1) / 2; }
+
+// One CTA per tile of every power: grid = l * ntiles, 256 threads x 4 elements.
+__global__ void __launch_bounds__(256) pack_tiles_kernel(const double* __restrict__ slabs, int64_t slab_elems,
+                                                         int nt, int l, unsigned char* __restrict__ packed,
+                                                         double* __restrict__ scales) {
+    __shared__ double red[8];
+    const int64_t ntiles = (int64_t)nt * nt;
+    const int64_t tile = blockIdx.x;
+    const int64_t k = tile / ntiles, t = tile - k * ntiles;  // k = power - 1; t = J * nt + I
+    const int I = (int)(t % nt), J = (int)(t / nt);
+    const double* src = slabs + k * slab_elems + t * kTileElems;
+    double v[4];
+    double m = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[i] = src[threadIdx.x + 256 * i];
+        m = fmax(m, fabs(v[i]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    double mx = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+    e = max(e, -900);              // all-tiny tiles quantise to 0 instead of overflowing the scale
+    const double up = ldexp(1.0, kPkFrac - e);
+    const int lo_i = min(I, J), hi_j = max(I, J);
+    const int64_t pair = pairs_before(lo_i, nt) + (hi_j - lo_i);
+    for (int slot = (I <= J ? 0 : 1); slot <= (I < J ? 0 : 1); ++slot) {  // diagonal: both slots
+        const int64_t rec = (pair * l + k) * 2 + slot;
+        unsigned char* dst = packed + rec * kPkTileBytes;
+        uint32_t* lo = reinterpret_cast<uint32_t*>(dst);
+        uint8_t* hi = dst + kTileElems * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const long long mi = __double2ll_rn(v[i] * up);  // |mi| <= 2^38
+            const unsigned long long u = (unsigned long long)(mi + (1LL << 39));
+            lo[threadIdx.x + 256 * i] = (uint32_t)u;
+            hi[threadIdx.x + 256 * i] = (uint8_t)(u >> 32);
+        }
+        if (threadIdx.x == 0) scales[rec] = ldexp(1.0, e - kPkFrac);
+    }
+}
+
+cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    const int64_t ntiles = (int64_t)nt * nt;
+    pack_tiles_kernel<<<(unsigned)(ntiles * l), 256, 0, stream>>>((const double*)slabs, ntiles * kTileElems, nt, l,
+                                                                  (unsigned char*)packed, scales);
+    return cudaGetLastError();
+}
+
+// I-major enumeration of the tile pairs (I <= J): row I's pairs are contiguous, so the pairs
+// whose smaller tile index lies in [I0, I1) -- everything that completes rows [32 I0, 32 I1) of
+// Q -- are one index range [pairs_before(I0), pairs_before(I1)).
+__device__ __forceinline__ void pair_of_imajor(int p, int nt, int& I, int& J) {
+    const double b = 2.0 * nt + 1.0;
+    int i = (int)((b - sqrt(b * b - 8.0 * p)) * 0.5);
+    i = max(0, min(i, nt - 1));
+    while (i > 0 && pairs_before(i, nt) > p) --i;
+    while (i + 1 < nt && pairs_before(i + 1, nt) <= p) ++i;
+    I = i;
+    J = i + (int)(p - pairs_before(i, nt));
+}
+
+int64_t packed_pairs_before(int I, int nt) { return pairs_before(I, nt); }
+
+
+// Persistent form: 2 CTAs per SM, each walking its pairs p0 + blockIdx.x + j * gridDim.x. A
+// dedicated producer warp keeps a TMA ring of (pair, power) items full ACROSS pairs (consumer
+// warps release stages through `empty` mbarriers, no CTA-wide barrier per power), so the next
+// pair's tiles stream in while this pair's epilogue (stores, row maxima) runs; the per-tile
+// scales of a pair arrive by bulk copy into a double buffer. Decode + scale is one exact DFMA
+// (d s - (2^52 + 2^39) s, s a power of two); the series coefficients are a table shared by all pairs.
+constexpr int kPsStages = 10;
+constexpr int kPsConsumers = 256;
+
+
+// G independent producer / consumer groups per CTA (one CTA per SM): each group has its own ring,
+// barriers, scale buffers and tables, and walks its own pairs; a capped grid therefore occupies
+// exactly that many SMs and leaves the others whole for a concurrent GEMM (the shell pipeline).
+__host__ __device__ __forceinline__ size_t psynth_group_bytes(int l, int ac, int stages = kPsStages) {
+    const size_t b = (size_t)stages * 2 * kPkTileBytes + (2 * stages + 2) * 8 + (size_t)2 * 2 * l * 8 +
+                     (size_t)ac * (2 * l + 1) * 8 + (size_t)ac * 8 * 32 * 8;
+    return (b + 127) & ~(size_t)127;
+}
+static int psynth_groups(int ac) { return ac == 4 ? 1 : 2; }
+size_t psynth_smem_bytes(int l, int ac, int stages) { return psynth_groups(ac) * psynth_group_bytes(l, ac, stages); }
+static int psynth_stages(int l, int ac) {  // the deepest ring that fits 227 KB (10 or 8 stages)
+    return psynth_smem_bytes(l, ac, kPsStages) <= 227 * 1024 ? kPsStages : 8;
+}
+
+__device__ __forceinline__ void consumer_sync(int g) { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); }
+
+// Stage s of a pair's items is (k - 1) % S (every pair restarts at stage 0, so the consumer's
+// stage offsets are compile-time immediates); per-stage phase bits track the reuse.
+template <int AC, int G, int S>
+__global__ void __launch_bounds__(G * (kPsConsumers + 32), 1)
+psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __restrict__ scales, int n, int l,
+                    int lc, const double* __restrict__ coef, int coef_ld, double* __restrict__ out, int64_t out_stride,
+                    unsigned long long* __restrict__ rowmax, int64_t rm_stride, int nt, int p0, int p1) {
+    constexpr int kStage = 2 * kPkTileBytes;
+    extern __shared__ __align__(128) unsigned char smem_all[];
+    const int g = threadIdx.x / (kPsConsumers + 32);
+    unsigned char* smem = smem_all + (size_t)g * psynth_group_bytes(lc, AC, S);
+    unsigned char* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * kStage);
+    uint64_t* empty = full + S;
+    uint64_t* sbar = empty + S;                                          // [2] scale buffers
+    double* sbuf = reinterpret_cast<double*>(sbar + 2);                  // [2][lc][2]
+    double* ctab = sbuf + 4 * lc;                                        // [AC][2l + 1]
+    double* red = ctab + AC * (2 * l + 1);                               // [AC][8][32]
+    const int tid = threadIdx.x - g * (kPsConsumers + 32), lane = tid & 31, warp = tid >> 5;
+    const int vcta = (int)blockIdx.x * G + g, vgrid = (int)gridDim.x * G;  // this group's pairs
+    const int npairs = (p1 - p0 - vcta + vgrid - 1) / vgrid;
+    const int depth = S < l ? S : l;  // stages in use; <= l, so a pair's scale buffer is never refilled in use
+    const int cw = 2 * l + 1;
+    for (int idx = tid; idx < AC * cw; idx += kPsConsumers + 32) ctab[idx] = coef[(size_t)(idx / cw) * coef_ld + idx % cw];
+    if (tid == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], kPsConsumers / 32);
+        }
+        mbar_init(&sbar[0], 1);
+        mbar_init(&sbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (npairs <= 0) return;
+    if (warp == kPsConsumers / 32) {  // ---------------- producer warp (one elected lane)
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            uint32_t used = 0, eph = 0;
+            for (int j = 0; j < npairs; ++j) {
+                const int64_t pr = p0 + vcta + (int64_t)j * vgrid;
+                const unsigned char* src = packed + pr * lc * kStage;  // this pair's contiguous records
+                int q = 0;
+                for (int k = 1; k <= l; ++k) {
+                    if (used >> q & 1) {
+                        mbar_wait(&empty[q], eph >> q & 1);
+                        eph ^= 1u << q;
+                    }
+                    used |= 1u << q;
+                    if (k == 1) {  // the pair's tile scales, both tiles, all powers
+                        mbar_arrive_expect_tx(&sbar[j & 1], 2 * lc * 8);
+                        bulk_g2s(sbuf + (size_t)(j & 1) * 2 * lc, scales + pr * lc * 2, 2 * lc * 8, &sbar[j & 1]);
+                    }
+                    mbar_arrive_expect_tx(&full[q], kStage);
+                    bulk_g2s_hint(ring + (size_t)q * kStage, src + (int64_t)(k - 1) * kStage, kStage, &full[q], pol);
+                    if (++q == depth) q = 0;
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumer warps: thread (lane r, warp) owns elements (r, c_i) of tile (I,J)
+    // and (c_i, r) of tile (J,I), c_i = warp + 8 i; their byte offsets inside a stage are fixed
+    const int r = lane;
+    const uint32_t* lo1p[4];  // element (r, c_i) of tile 1 and (c_i, r) of tile 2, stage 0
+    const uint8_t* hi1p[4];
+    const uint32_t* lo2p[4];
+    const uint8_t* hi2p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int c = warp + 8 * i;
+        lo1p[i] = reinterpret_cast<const uint32_t*>(ring) + swz(r, c);
+        hi1p[i] = ring + kTileElems * 4 + swz(r, c);
+        lo2p[i] = reinterpret_cast<const uint32_t*>(ring + kPkTileBytes) + swz(c, r);
+        hi2p[i] = ring + kPkTileBytes + kTileElems * 4 + swz(c, r);
+    }
+    uint32_t fph = 0;
+    for (int j = 0; j < npairs; ++j) {
+        int I, J;
+        pair_of_imajor(p0 + vcta + j * vgrid, nt, I, J);
+        const bool diag = I == J;
+        const int bi = min(kTile, n - I * kTile), bj = min(kTile, n - J * kTile);
+        mbar_wait(&sbar[j & 1], (j >> 1) & 1);
+        const double* sv = sbuf + (size_t)(j & 1) * 2 * lc;  // [k][slot]
+        double q1[4][AC], q2[4][AC];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int a = 0; a < AC; ++a) {
+                q1[i][a] = (diag && r == warp + 8 * i) ? ctab[a * cw + l] : 0.0;
+                q2[i][a] = 0.0;
+            }
+        for (int k0 = 1; k0 <= l; k0 += S) {
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                const int k = k0 + u;
+                if (k > l) break;
+                mbar_wait(&full[u], fph >> u & 1);
+                fph ^= 1u << u;
+                const double sc1 = sv[2 * (k - 1)], sc2 = sv[2 * (k - 1) + 1];
+                const double ns1 = -kPkMagic * sc1, ns2 = -kPkMagic * sc2;  // exact (powers of two)
+                double ck[AC], cm[AC];
+#pragma unroll
+                for (int a = 0; a < AC; ++a) {
+                    ck[a] = ctab[a * cw + l + k];
+                    cm[a] = ctab[a * cw + l - k];
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    // stage offsets are immediates (u is unrolled): LDS [R + imm], no address math
+                    const uint32_t lo1 = lo1p[i][u * (kStage / 4)], hi1 = hi1p[i][u * kStage];
+                    const uint32_t lo2 = lo2p[i][u * (kStage / 4)], hi2 = hi2p[i][u * kStage];
+                    // (2^52 + u) s - (2^52 + 2^39) s = m s exactly: one rounding-free FMA per value
+                    const double p1 = fma(__hiloint2double((int)(0x43300000u | hi1), (int)lo1), sc1, ns1);
+                    const double p2 = fma(__hiloint2double((int)(0x43300000u | hi2), (int)lo2), sc2, ns2);
+#pragma unroll
+                    for (int a = 0; a < AC; ++a) {
+                        q1[i][a] = fma(ck[a], p1, fma(cm[a], p2, q1[i][a]));
+                        q2[i][a] = fma(ck[a], p2, fma(cm[a], p1, q2[i][a]));  // unused on diagonal pairs
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[u]);
+            }
+        }
+        // Q[I-tile, J-tile]: rows r (lanes), columns c = warp + 8 i; row maxima across the 8 warps
+#pragma unroll
+        for (int a = 0; a < AC; ++a) {
+            double mx = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int c = warp + 8 * i;
+                if (r < bi && c < bj) {
+                    out[(int64_t)a * out_stride + (int64_t)(J * kTile + c) * n + I * kTile + r] = q1[i][a];
+                    mx = fmax(mx, fabs(q1[i][a]));
+                }
+            }
+            red[(a * 8 + warp) * 32 + lane] = mx;
+        }
+        if (!diag) {
+            // Q[J-tile, I-tile]: thread (lane r, warp) holds Q[J*32 + warp + 8i, I*32 + r]; the stores of
+            // a 32-byte sector come from 4 warps and merge in L2
+#pragma unroll
+            for (int a = 0; a < AC; ++a)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int row = warp + 8 * i;
+                    const bool ok = r < bi && row < bj;
+                    double m = ok ? fabs(q2[i][a]) : 0.0;
+                    if (ok) out[(int64_t)a * out_stride + (int64_t)(I * kTile + r) * n + J * kTile + row] = q2[i][a];
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    if (lane == 0 && row < bj && m > 0.0)
+                        atomicMax(rowmax + (int64_t)a * rm_stride + J * kTile + row,
+                                  (unsigned long long)__double_as_longlong(m));
+                }
+        }
+        consumer_sync(g);
+        if (warp < AC) {
+            const int a = warp;
+            double mx = red[(a * 8) * 32 + lane];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) mx = fmax(mx, red[(a * 8 + w) * 32 + lane]);
+            if (r < bi && mx > 0.0)
+                atomicMax(rowmax + (int64_t)a * rm_stride + I * kTile + r, (unsigned long long)__double_as_longlong(mx));
+        }
+        consumer_sync(g);
+    }
+}
+
+// Tile pairs [p0, p1) of the I-major enumeration (p1 < 0: all of them); max_ctas > 0 caps the
+// persistent grid.
+// l: powers summed (the truncation), l_cache: powers stored (the scale layout's stride).
+cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
+                          int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
+                          int64_t rm_stride, cudaStream_t stream, int p0, int p1, int max_ctas) {
+    const int nt = (int)ceil_div(n, kTile);
+    if (p1 < 0) p1 = nt * (nt + 1) / 2;
+    const int npairs = p1 - p0;
+    if (npairs <= 0) return cudaSuccess;
+    const int stages = psynth_stages(l_cache, n_alpha);
+    const size_t smem = psynth_smem_bytes(l_cache, n_alpha, stages);
+    const int groups = psynth_groups(n_alpha);
+    int grid = FGFRFT_SMS;  // one CTA (groups x 288 threads) per SM
+    if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+    if (grid * groups > npairs) grid = (npairs + groups - 1) / groups;
+#define FGB_PS(ACV)                                                                                          \
+    {                                                                                                        \
+        constexpr int GV = ACV == 4 ? 1 : 2;                                                                 \
+        static PerDeviceOnce attr;                                                                           \
+        cudaError_t e = attr.run([] {                                                                        \
+            cudaError_t r = cudaFuncSetAttribute(psynth_pairs_kernel<ACV, GV, kPsStages>,                    \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);   \
+            if (r != cudaSuccess) return r;                                                                  \
+            return cudaFuncSetAttribute(psynth_pairs_kernel<ACV, GV, 8>,                                     \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);            \
+        });                                                                                                  \
+        if (e != cudaSuccess) return e;                                                                      \
+        if (smem > 227 * 1024) return cudaErrorInvalidValue;                                                 \
+        auto kern = stages == kPsStages ? psynth_pairs_kernel<ACV, GV, kPsStages> : psynth_pairs_kernel<ACV, GV, 8>; \
+        kern<<<grid, GV * (kPsConsumers + 32), smem, stream>>>((const unsigned char*)packed,                 \
+                                                              scales, n, l, l_cache,                         \
+                                                              coef_dev, coef_ld, out, out_stride, rowmax,    \
+                                                              rm_stride, nt, p0, p1);                        \
+    }
+    if (n_alpha == 1) FGB_PS(1) else if (n_alpha == 2) FGB_PS(2) else if (n_alpha == 4) FGB_PS(4) else return cudaErrorInvalidValue;
+#undef FGB_PS
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- MSE + dL/da from [Y; dY]
+// loss = ||Y - Xc||^2 / (n b), dL/da = 2 Re<Y - Xc, dY> / (n b)  (G = 2 (Y - Xc) / (n b),
+// learn.hpp:85-92 normalisation; dY = dQ/da X, so Re<G, dY> = Re<G, F'^a X>). Fixed-order
+// two-pass reduction (deterministic). Optionally copies Y out (the caller's y buffer).
+constexpr int kMdBlocks = 4 * FGFRFT_SMS;
+
+__global__ void __launch_bounds__(256) mse_dy_kernel(const double2* __restrict__ y, const double2* __restrict__ dy,
+                                                     const double2* __restrict__ xc, int64_t count,
+                                                     double2* __restrict__ yout, double* __restrict__ part) {
+    __shared__ double red[2][8];
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < count; i += (int64_t)gridDim.x * 256) {
+        const double2 v = y[i], d = dy[i], c = xc[i];
+        const double rx = v.x - c.x, ry = v.y - c.y;
+        s1 = fma(rx, rx, fma(ry, ry, s1));
+        s2 = fma(rx, d.x, fma(ry, d.y, s2));
+        if (yout) yout[i] = v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = s1;
+        red[1][threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+        part[(int64_t)threadIdx.x * kMdBlocks + blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(64) mse_dy_finish_kernel(const double* __restrict__ part, double norm,
+                                                           double* __restrict__ loss, double* __restrict__ dlda) {
+    __shared__ double red[2][2];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp 0: loss, warp 1: dot
+    double t = 0.0;
+    for (int i = lane; i < kMdBlocks; i += 32) t += part[(int64_t)w * kMdBlocks + i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[w][0] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *loss = red[0][0] * norm;
+        *dlda = 2.0 * red[1][0] * norm;
+    }
+}
+
+size_t mse_dy_part_elems() { return 2 * kMdBlocks; }
+
+cudaError_t launch_mse_dy(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
+                          double norm, double* loss, double* dlda, cudaStream_t stream) {
+    mse_dy_kernel<<<kMdBlocks, 256, 0, stream>>>((const double2*)y, (const double2*)dy, (const double2*)xc, count,
+                                                 (double2*)yout, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    mse_dy_finish_kernel<<<1, 64, 0, stream>>>(part, norm, loss, dlda);
+    return cudaGetLastError();
+}
+
+}  // namespace fgb

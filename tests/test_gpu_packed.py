@@ -1,0 +1,93 @@
+"""GPU parity of the packed step route (csrc/packed.cu): one, two or four orders over a real
+cache with a large signal batch -- Q(a), dQ/da from the packed (48-bit fixed-point) slabs, one
+Ozaki GEMM [Y; dY] = [Q; dQ] X, loss and dL/da from one elementwise pass -- against the oracle
+(transform.hpp:111-148, learn.hpp:88-92 form) at the 1e-10 relative bar of the north star.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2602_20870_b200 as fg
+import prep
+
+pytestmark = pytest.mark.gpu
+
+PACKED_ROUTE = 3
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _graph_f(n, seed):
+    rng = prep.Rng(seed)
+    pts = rng.uniforms(2 * n).reshape(n, 2)
+    return prep.gft_from_shift(prep.laplacian(prep.knn_graph(pts, 8)))
+
+
+@pytest.fixture(scope="module")
+def problem():
+    n, l, b = 1024, 24, 80
+    f = _graph_f(n, 11)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    return f, l, x, xc, fg.PowerCache(f, l, memory_budget=8 << 30), O.PowerCache(f, l)
+
+
+@pytest.mark.parametrize("alphas", [[0.37], [-1.3], [0.25, 1.75], [2.0]])
+def test_packed_mse_step_matches_oracle(problem, alphas):
+    f, l, x, xc, g, o = problem
+    loss, dl, y = fg.mse_step(g, alphas, x, xc, want_y=True)
+    assert g.route_info()[0] == PACKED_ROUTE
+    for i, a in enumerate(alphas):
+        lr, dr, yr = O.dlda_mse(o, a, x, xc)
+        assert rel(y[i], yr) <= 1e-10
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        s = O.power_dots(o, 2.0 * (yr - xc) @ x.conj().T / x.size)
+        _, dc = O.sinc_coeffs(a, l)
+        assert abs(dl[i] - dr) <= 1e-10 * max(np.sum(np.abs(dc * s)), 1e-300)
+
+
+@pytest.mark.parametrize("alphas,inverse", [([0.37], False), ([0.37], True), ([0.1, 0.9], False),
+                                            ([0.1, 0.5, 1.2, -0.7], True)])
+def test_packed_apply_matches_oracle(problem, alphas, inverse):
+    f, l, x, xc, g, o = problem
+    y = fg.apply_series(g, alphas, x, inverse=inverse)
+    for i, a in enumerate(alphas):
+        q = O.fgfrft_matrix(o, a)
+        yr = (q.conj().T if inverse else q) @ x
+        assert rel(y[i], yr) <= 1e-10
+
+
+def test_packed_apply_truncation(problem):
+    f, l, x, xc, g, o = problem
+    y = fg.apply_series(g, [0.6], x, truncation=9)
+    assert rel(y[0], O.fgfrft_matrix(o, 0.6, truncation=9) @ x) <= 1e-10
+
+
+def test_packed_integer_order_is_the_power(problem):
+    f, l, x, xc, g, o = problem
+    y = fg.apply_series(g, [3.0, 0.0], x)
+    # c_k(3) is an exact Kronecker row (sinc.hpp:16): Y = P_3 X up to the 40-bit packing of P_3
+    # (<= 2^-39 of each tile's largest entry) and the Ozaki product
+    assert rel(y[0], o.power(3) @ x) <= 2e-11
+    assert rel(y[1], x) <= 1e-13
+
+
+def test_packed_route_respects_memory_budget():
+    """The packed slabs are auxiliary: with a budget that only covers the reference count
+    L n^2 16 bytes (transform.hpp:46-53) they are not built and the exact route runs."""
+    n, l, b = 512, 8, 40
+    f = _graph_f(n, 3)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((n, b)) + 0j
+    xc = x.copy()
+    tight = fg.PowerCache(f, l, memory_budget=l * n * n * 16)
+    roomy = fg.PowerCache(f, l, memory_budget=1 << 30)
+    lt, dt_, _ = fg.mse_step(tight, [0.4], x, xc)
+    assert tight.route_info()[0] != PACKED_ROUTE
+    lr, dr, _ = fg.mse_step(roomy, [0.4], x, xc)
+    assert roomy.route_info()[0] == PACKED_ROUTE
+    assert abs(lt[0] - lr[0]) <= 1e-10 * lr[0]
+    assert abs(dt_[0] - dr[0]) <= 1e-9 * max(1.0, abs(dr[0]))

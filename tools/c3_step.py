@@ -1,0 +1,81 @@
+"""Config-3 step probe: forward F^a X + MSE + dL/da (one order, alternating between two orders
+every call) through fgfrft_mse_step_dev, CUDA events on the library stream, plus the library's
+per-kernel-class breakdown. Used for ncu launch lists of the headline step.
+
+  python tools/c3_step.py [--steps 10] [--warmup 3] [--config 3|4] [--c64]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2602_20870_b200 as fg  # noqa: E402
+import prep  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="3")
+    ap.add_argument("--c64", action="store_true")
+    args = ap.parse_args()
+    t0 = time.perf_counter()
+    cfg = prep.config3() if args.config == "3" else prep.config4()
+    prep_s = time.perf_counter() - t0
+    n, b, L = cfg.n, cfg.b, cfg.l
+    dtype = 1 if args.c64 else 0
+    ct = torch.complex64 if args.c64 else torch.complex128
+    stream = torch.cuda.Stream()
+    t0 = time.perf_counter()
+    cache = fg.PowerCache(cfg.f, L, memory_budget=200 << 30, dtype=dtype)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    cache.set_stream(stream.cuda_stream)
+    lib = fg.lib()
+    al = [np.array([0.37]), np.array([0.63])]
+    x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda().to(ct)
+    xc = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda().to(ct)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    dl = torch.empty(1, dtype=torch.float64, device="cuda")
+
+    def step(i):
+        fg._check(lib.fgfrft_mse_step_dev(cache.handle, al[i & 1].ctypes.data, 1, x.data_ptr(), xc.data_ptr(), b,
+                                          None, loss.data_ptr(), dl.data_ptr()))
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = fg.launch_count()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = (fg.launch_count() - l0) / args.steps
+    fg.profile_enable(True)
+    fg.profile_read(reset=True)
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            step(i)
+    torch.cuda.synchronize()
+    prof = {k: [v[0] / args.steps, v[1] / args.steps] for k, v in fg.profile_read(reset=True).items() if v[1]}
+    fg.profile_enable(False)
+    print(json.dumps({"config": "C" + args.config, "c64": args.c64, "n": n, "l": L, "b": b, "ms_per_step": ms,
+                      "signal_nodes_per_s": n * b / (ms * 1e-3), "launches_per_step": launches,
+                      "prep_s": prep_s, "build_s": build_s, "classes_ms_per_step": prof,
+                      "loss": float(loss[0]), "dlda": float(dl[0])}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
