@@ -357,46 +357,62 @@ def main():
     tot = sum(v[0] for v in prof.values()) or 1.0
     classes = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                    "share": v[0] / tot} for k, v in prof.items() if v[1]}
-    route_desc = cache.step_route() if hasattr(cache, "step_route") else {}
 
     # ---- roofline of the dominant kernel class.
-    # synthesis (HBM): reads the L stored power slabs once and writes Q and dQ/da (real doubles for a
-    #   real F): SURVEY 8(d) bytes (S*e + A*e) * N^2 with S = L, e = 8, A = 2 outputs.
-    # int8_gemm (tensor): [Y; dY] = [Q; dQ] X or Y = Q X and M = G X^H, 2*N*(2B)*N FP64-equivalent
-    #   flops per N-row product, S(S+1)/2 int8 digit GEMMs of that size (Ozaki, S base-254 digits).
+    # synthesis (HBM): Q(a) and dQ/da from ONE pass over the stored powers. On the packed route
+    #   (route 3, real F) the stored powers are the packed slabs: 5 B per element (40-bit fixed point
+    #   + one scale per 32x32 tile and power), pair-major, the diagonal tiles twice; algorithmic bytes
+    #   per launch = packed slabs + scales read + Q, dQ written (real doubles). The SURVEY 8(d) FP64
+    #   form, (S*e + A*e)*N^2 with S = L slabs of e = 8 B, is reported beside it
+    #   (`fp64_equivalent_*`: the bytes the exact FP64 cache would move for the same launch).
+    # int8_gemm (tensor): [Y; dY] = [Q; dQ] X, 2 * (2N) * (2B) * N FP64-equivalent flops per step
+    #   (real F x complex X), S(S+1)/2 int8 digit GEMMs of that size (Ozaki, S base-254 digits).
     S = int(L_.fgfrft_int8_digits())
     products = S * (S + 1) // 2
     e = 8 if real else 16
-    syn_bytes = (L * e + 2 * e) * n * n
+    route, _nodes = cache.route_info()
+    nt = -(-n // 32)
+    npairs = nt * (nt + 1) // 2
+    packed_bytes = npairs * L * 2 * 32 * 32 * 5 + npairs * L * 2 * 8
+    fp64_bytes = (L * e + 2 * e) * n * n
+    syn_bytes = (packed_bytes + 2 * 8 * n * n) if route == 3 else fp64_bytes
     dom = max(classes, key=lambda k: classes[k]["ms_per_step"])
-    syn = classes.get("synthesis") or classes.get("packed_synthesis")
+    syn = classes.get("synthesis")
     roof = None
     if syn:
         per_launch_ms = syn["ms_per_step"] / syn["launches_per_step"]
         ach = syn_bytes / syn["launches_per_step"] / (per_launch_ms * 1e-3) / 1e9
-        nc = ncu_summary(r"synth")
-        roof = {"bound": "hbm", "kernel_class": "synthesis (Q and dQ/da from one pass over the cache)",
+        fp64_ach = fp64_bytes / syn["launches_per_step"] / (per_launch_ms * 1e-3) / 1e9
+        nc = ncu_summary(r"psynth" if route == 3 else r"rsynth_pairs")
+        roof = {"bound": "hbm",
+                "kernel": ("psynth_pairs_kernel<2> (packed slabs -> Q and dQ/da, one pass, TMA ring)" if route == 3
+                           else "rsynth_pairs_kernel (FP64 slabs -> Q and dQ/da)"),
                 "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
                 "traffic": nc["traffic"] if nc else None,
                 "traffic_source": (f"{nc['file']}: dram__bytes_read.sum + dram__bytes_write.sum of "
-                                   f"'{nc['kernel']}' (ncu --set full, one launch)") if nc else None,
+                                   f"'{nc['kernel'][:60]}' (ncu --set full, one launch)") if nc else None,
                 "algorithmic_bytes_per_launch": syn_bytes / syn["launches_per_step"],
-                "algorithmic": (f"SURVEY 8(d): (S*e + A*e)*N^2 with S = L = {L} stored slabs (F^-k read as the "
-                                f"transposed tile of F^k), e = {e} B ({'real F stored as real doubles' if real else 'c128'}),"
-                                f" A = 2 outputs (Q, dQ/da) = {syn_bytes:.4g} B"),
+                "algorithmic": (f"packed slabs {packed_bytes:.4g} B (npairs*L*2 tiles*5 KB + scales; 5 B per element, "
+                                f"diagonal tiles twice) read + Q, dQ 2*N^2*8 B written = {syn_bytes:.4g} B"
+                                if route == 3 else
+                                f"SURVEY 8(d): (S*e + A*e)*N^2, S = L = {L}, e = {e}, A = 2 = {syn_bytes:.4g} B"),
+                "fp64_equivalent_bytes": fp64_bytes,
+                "fp64_equivalent_gbs": fp64_ach, "fp64_equivalent_frac": fp64_ach / peaks["hbm_gbs"],
+                "fp64_equivalent_note": ("SURVEY 8(d) bytes of the exact FP64 cache, (S*e + A*e)*N^2 with S = L, "
+                                         "e = 8, A = 2: what the same launch would move on 8-byte slabs"),
                 "peak_source": peaks["hbm_src"], "share_of_step": syn["share"],
                 "ms_per_launch": per_launch_ms}
     i8 = classes.get("int8_gemm")
     gemm = None
     if i8:
-        fp = 2.0 * 2 * n * (2 * b) * n  # two N x 2B x N real products per step (real F x complex X)
+        fp = 2.0 * 2 * n * (2 * b) * n  # [Q; dQ] (2N rows, real) x X (2B real columns), K = N
         tops = fp * products / (i8["ms_per_step"] * 1e-3) / 1e12
-        nc = ncu_summary(r"ozgemm_kernel")
-        gemm = {"bound": "tensor", "kernel_class": "INT8 Ozaki GEMMs (tcgen05.mma kind::i8, TMEM accumulators)",
+        nc = ncu_summary(r"ozgemm_kernel<6")
+        gemm = {"bound": "tensor", "kernel": f"ozgemm_kernel<{S},1,2> (tcgen05.mma kind::i8, TMEM accumulators)",
                 "achieved": tops, "peak": peaks["int8_tops"], "unit": "TOPS", "frac": tops / peaks["int8_tops"],
                 "fp64_equivalent_tflops": fp / (i8["ms_per_step"] * 1e-3) / 1e12,
                 "dmma_peak_tflops": peaks["fp64_tflops"],
-                "algorithmic": f"2 products of 2*N*(2B)*N = {fp / 2:.4g} FP64-equivalent flops x {products} digit GEMMs",
+                "algorithmic": f"2*(2N)*(2B)*N = {fp:.4g} FP64-equivalent flops x {products} int8 digit GEMMs",
                 "traffic": nc["traffic"] if nc else None, "peak_source": peaks["int8_src"],
                 "share_of_step": i8["share"]}
     if roof is None or (gemm and dom == "int8_gemm"):
@@ -404,6 +420,9 @@ def main():
     if roof is not None:
         roof["other_kernel"] = gemm
         roof["dominant_class"] = dom
+    route_desc = {"route": {0: "synthesis (exact FP64 slabs)", 1: "power products", 2: "node interpolation",
+                            3: "packed: Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X"}.get(route),
+                  "int8_digits": S}
 
     # ---- parity of the timed step against the oracle (rank 0; the oracle cache is reused by the CPU
     # baseline below)

@@ -269,6 +269,55 @@ int fgfrft_shard_mse_dlda_partial_dev(fgfrft_cache* shard, const double* alphas,
                                       const void* x_dev, const void* xc_rows_dev, int64_t b,
                                       void* y_rows_dev, void* loss_partial_dev, void* dlda_partial_dev);
 
+/* ---- Multi-GPU: NCCL communicator + pair shards of the packed cache ----------------------
+ *
+ * Replaces the single-GPU PowerCache (transform.hpp:43-59) + MSE step for caches sharded over
+ * the GPUs of one node, without PyTorch: the library owns the NCCL communicator (libnccl.so.2,
+ * loaded at first use). Bootstrap like NCCL itself: rank 0 calls fgfrft_comm_unique_id and the
+ * launcher hands the 128 bytes to every rank (MPI, a TCP store, torch.distributed, ...); or one
+ * process drives all devices with fgfrft_comm_create_all (ncclCommInitAll).
+ *
+ * A pair shard owns the tile pairs {(I,J),(J,I)}, I <= J, with I in its contiguous band (about
+ * 1/G of the pairs; fgfrft_pshard_plan gives the bands), stores only their packed powers (5 B
+ * per element, built from its row / column panels -- F is broadcast from rank 0, the only
+ * collective of the build), synthesises Q, dQ/da on its tiles and multiplies them with X locally.
+ * Per MSE step: one reduce-scatter of [Y; dY] by signal-column chunks and one all-reduce of 2A
+ * doubles. Real F (graph GFTs) only; a complex F uses the row shards above.
+ */
+#define FGFRFT_COMM_ID_BYTES 128
+typedef struct fgfrft_comm fgfrft_comm;
+int fgfrft_comm_unique_id(void* id_out /* FGFRFT_COMM_ID_BYTES */);
+int fgfrft_comm_create(const void* id, int world, int rank, int device, fgfrft_comm** out);
+int fgfrft_comm_create_all(int ndev, const int* devices, fgfrft_comm** out /* ndev handles */);
+int fgfrft_comm_destroy(fgfrft_comm* comm);
+int fgfrft_comm_info(const fgfrft_comm* comm, int* world, int* rank, int* device);
+
+/* Tile-row band boundaries (world + 1 ints, in 32-row tiles) of the pair shards of an n x n F. */
+int fgfrft_pshard_plan(int64_t n, int world, int* tile_rows);
+/* f: n x n complex128 column-major on every rank, or NULL on ranks != 0 (broadcast from rank 0). */
+int fgfrft_pshard_create(const double* f, int64_t n, int l, uint64_t memory_budget, fgfrft_comm* comm,
+                         fgfrft_cache** out);
+/* A shard of rank `rank` of `world` with no communicator (partials only: tests, custom reductions). */
+int fgfrft_pshard_create_local(const double* f, int64_t n, int l, uint64_t memory_budget, int world, int rank,
+                               int device, fgfrft_cache** out);
+int fgfrft_pshard_destroy(fgfrft_cache* shard);
+int fgfrft_pshard_info(const fgfrft_cache* shard, int* world, int* rank, int64_t* pair_begin, int64_t* pair_end,
+                       int64_t* row_begin, int64_t* row_end, uint64_t* device_bytes);
+int fgfrft_pshard_set_stream(fgfrft_cache* shard, void* stream);
+/* This rank's partial products (sum over ranks = the full result): with_dq 1 -> 2 n_alpha blocks
+ * [Y_g(a..); dY_g(a..)], 0 -> n_alpha blocks Y_g(a..), each n x b complex (stride 2 n b doubles). */
+int fgfrft_pshard_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, int with_dq,
+                              const void* x_dev, int64_t b, void* out_dev);
+/* MSE step (one or two orders) over the communicator; full X, Xc on every rank; loss and
+ * dL/dalpha of every order on every rank. */
+int fgfrft_pshard_mse_step_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, const void* x_dev,
+                               const void* xc_dev, int64_t b, void* loss_dev, void* dlda_dev);
+int fgfrft_pshard_mse_step(fgfrft_cache* shard, const double* alphas, int n_alpha, const double* x,
+                           const double* xc, int64_t b, double* loss, double* dlda);
+/* Y = F^alpha X (inverse: the conjugate transpose) for 1, 2 or 4 orders, the full Y on every rank. */
+int fgfrft_pshard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, int inverse,
+                            const void* x_dev, int64_t b, void* y_dev);
+
 /* ---- FP64-accurate GEMM on the INT8 tensor cores (Ozaki scheme) -------------------------
  *
  * C = op(A) op(B) for real column-major device matrices (op(A) m x k, op(B) k x n, C m x n;

@@ -147,6 +147,21 @@ def lib() -> ctypes.CDLL:
         "fgfrft_ipc_open": (i, [vp, i, pp]),
         "fgfrft_ipc_close": (i, [vp]),
         "fgfrft_cache_load": (i, [ctypes.c_char_p, u64, i, pp]),
+        "fgfrft_comm_unique_id": (i, [vp]),
+        "fgfrft_comm_create": (i, [vp, i, i, i, pp]),
+        "fgfrft_comm_create_all": (i, [i, vp, vp]),
+        "fgfrft_comm_destroy": (i, [vp]),
+        "fgfrft_comm_info": (i, [vp, vp, vp, vp]),
+        "fgfrft_pshard_plan": (i, [i64, i, vp]),
+        "fgfrft_pshard_create": (i, [vp, i64, i, u64, vp, pp]),
+        "fgfrft_pshard_create_local": (i, [vp, i64, i, u64, i, i, i, pp]),
+        "fgfrft_pshard_destroy": (i, [vp]),
+        "fgfrft_pshard_info": (i, [vp, vp, vp, vp, vp, vp, vp, vp]),
+        "fgfrft_pshard_set_stream": (i, [vp, vp]),
+        "fgfrft_pshard_partial_dev": (i, [vp, vp, i, i, vp, i64, vp]),
+        "fgfrft_pshard_mse_step_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
+        "fgfrft_pshard_mse_step": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
+        "fgfrft_pshard_apply_dev": (i, [vp, vp, i, i, vp, i64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -177,7 +192,11 @@ def exported_symbols():
         "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
         "fgfrft_shard_apply_gather_dev", "fgfrft_ipc_get", "fgfrft_ipc_open", "fgfrft_ipc_close",
         "fgfrft_denoise_create_exact", "fgfrft_denoise_reconstruct", "fgfrft_zgemm_int8_dev",
-        "fgfrft_denoise_create_ex",
+        "fgfrft_denoise_create_ex", "fgfrft_comm_unique_id", "fgfrft_comm_create", "fgfrft_comm_create_all",
+        "fgfrft_comm_destroy", "fgfrft_comm_info", "fgfrft_pshard_plan", "fgfrft_pshard_create",
+        "fgfrft_pshard_create_local", "fgfrft_pshard_destroy", "fgfrft_pshard_info", "fgfrft_pshard_set_stream",
+        "fgfrft_pshard_partial_dev", "fgfrft_pshard_mse_step_dev", "fgfrft_pshard_mse_step",
+        "fgfrft_pshard_apply_dev",
     ]
 
 
@@ -296,7 +315,8 @@ class PowerCache:
         return self._fp
 
     def route_info(self):
-        """(route, nodes) of the last MSE step: 0 synthesis, 1 power products, 2 node interpolation."""
+        """(route, nodes) of the last MSE step: 0 synthesis, 1 power products, 2 node interpolation,
+        3 packed (Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X)."""
         r, k = ctypes.c_int(), ctypes.c_int()
         _check(lib().fgfrft_cache_route_info(self._h, ctypes.addressof(r), ctypes.addressof(k)))
         return r.value, k.value

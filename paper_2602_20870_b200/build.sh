@@ -12,7 +12,7 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompil
        -Xcompiler -ffp-contract=off -Xcompiler -fopenmp -I"$ROOT/include" -I"$SRC" --expt-relaxed-constexpr)
 [ -n "${FGFRFT_PTXAS_VERBOSE:-}" ] && FLAGS+=(-Xptxas -v)
 pids=()
-for f in capi capi_shard capi_learn capi_spectral capi_store synth zgemm cgemm dots ops layout shard batch real ozgemm combine denoise spectral store packed; do
+for f in capi capi_shard capi_learn capi_spectral capi_store synth zgemm cgemm dots ops layout shard batch real ozgemm combine denoise spectral store packed capi_pshard; do
   "$NVCC" "${FLAGS[@]}" -c "$SRC/$f.cu" -o "$OBJ/$f.o" & pids+=($!)
 done
 "$NVCC" "${FLAGS[@]}" -x cu -c "$SRC/sinc_host.cpp" -o "$OBJ/sinc_host.o" & pids+=($!)

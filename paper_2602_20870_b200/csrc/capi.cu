@@ -46,6 +46,7 @@ namespace fgbi {
 int check_handle(const fgfrft_cache* c) {
     if (!c) return fail(FGFRFT_PARAMETER, "null fgfrft_cache handle");
     if (c->shard) return fail(FGFRFT_PARAMETER, "row-shard handle: use the fgfrft_shard_* entry points");
+    if (c->pshard) return fail(FGFRFT_PARAMETER, "pair-shard handle: use the fgfrft_pshard_* entry points");
     if (c->graphs > 0) return fail(FGFRFT_PARAMETER, "graph-batch handle: use the fgfrft_batch_* entry points");
     return FGFRFT_OK;
 }
@@ -232,6 +233,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->stream != c->own_stream) cudaStreamSynchronize(c->stream);
     if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     for (cudaEvent_t e : c->pk_es) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->xh_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->pk_e0, c->pk_eg, c->pk_ex})
         if (e) cudaEventDestroy(e);
     if (c->pk_s) cudaStreamSynchronize(c->pk_s);
@@ -240,7 +242,7 @@ void destroy_cache(fgfrft_cache* c) {
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
                       &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
                       &c->by, &c->es, &c->ee, &c->erm, &c->nd_tab, &c->nd_p, &c->nd_d0, &c->nd_bsl, &c->nd_bex,
-                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ydy})
+                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ydy, &c->pp, &c->ppc})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -1430,8 +1432,11 @@ int ensure_pipe_streams(fgfrft_cache* c) {
 
 // rows (1, 2 or 4) real n x n operators M_r (table rows r of coef, width coef_ld, l_used powers)
 // from the packed slabs, Y_r = M_r X into y (stride 2 n b doubles), shell-pipelined.
+// x_host != nullptr: X is still on the host -- it is copied into x_dev in column chunks on the
+// aux stream, and the GEMM runs per chunk as its columns land, so the host->device transfer
+// overlaps the synthesis (which does not need X) and the earlier chunks' products.
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
-                    void* y, int l_used) {
+                    void* y, int l_used, const double* x_host) {
     const int S = oz_slices_default();
     const int64_t n = c->n, mp = pad_rows(n), sl = n * n, kp = pad_k(n);
     const int64_t bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
@@ -1439,6 +1444,10 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
     if (c->pk_plan_key != key) {
         c->pk_plan = pk_plan(n, rows, b, l_used);
         c->pk_plan_key = key;
+    }
+    if (x_host && c->pk_plan.size() > 1) {  // the chunked host-X form runs one shell
+        c->pk_plan.assign(1, PkShell{0, (int)n, 0, -1});
+        c->pk_plan_key = 0;
     }
     const std::vector<PkShell>& plan = c->pk_plan;
     int64_t srows = 0;  // sliced rows over all shells (each shell padded to 128)
@@ -1456,8 +1465,30 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
     FGB_CUDA(cudaEventRecord(c->pk_e0, c->stream));
     FGB_CUDA(cudaStreamWaitEvent(c->pk_s, c->pk_e0, 0));
     FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_e0, 0));
+    // host X: column chunks of >= 32 signals (64 B-operand rows) copied on the aux stream
+    const int nch = x_host ? (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)pk_env("FGFRFT_E2E_CHUNKS", 4),
+                                                                        ceil_div(b, 32)))
+                           : 0;
+    const int64_t cw = x_host ? ceil_div(ceil_div(b, nch), 32) * 32 : b;
+    if (x_host) {
+        if (!c->aux_stream) FGB_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        FGB_CUDA(cudaStreamWaitEvent(c->aux_stream, c->pk_e0, 0));  // the previous call's readers are done
+        if (c->xh_ev.size() < (size_t)nch) {
+            const size_t have = c->xh_ev.size();
+            c->xh_ev.resize(nch, nullptr);
+            for (size_t i = have; i < (size_t)nch; ++i)
+                FGB_CUDA(cudaEventCreateWithFlags(&c->xh_ev[i], cudaEventDisableTiming));
+        }
+        for (int ch = 0; ch < nch; ++ch) {
+            const int64_t j0 = ch * cw, j1 = std::min<int64_t>(b, j0 + cw);
+            if (j1 <= j0) break;
+            FGB_CUDA(cudaMemcpyAsync(static_cast<double*>(const_cast<void*>(x_dev)) + j0 * 2 * n, x_host + j0 * 2 * n,
+                                     (size_t)(j1 - j0) * n * 16, cudaMemcpyHostToDevice, c->aux_stream));
+            FGB_CUDA(cudaEventRecord(c->xh_ev[ch], c->aux_stream));
+        }
+    }
     // G: X sliced once (B operand: rows 2j + comp, K = signal index), while S synthesises shell 0
-    {
+    if (!x_host) {
         int* xe = c->xex.as<int>();
         const OzView v{static_cast<const double*>(x_dev), 2 * n, 2, 0, 1, 0, (int)(2 * b), (int)bp, 1, (int)n,
                        (int)kp, false};
@@ -1495,6 +1526,30 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
             FGB_LAUNCH(launch_oz_slice_ready(v, S, kOzTileA, dst, ex, rmax + sh.r0, c->pk_s), 1);
         }
         FGB_CUDA(cudaEventRecord(c->pk_es[s], c->pk_s));
+        if (x_host) {  // one shell: per X chunk, slice its columns, then their products
+            for (int ch = 0; ch < nch; ++ch) {
+                const int64_t j0 = ch * cw, j1 = std::min<int64_t>(b, j0 + cw);
+                if (j1 <= j0) break;
+                const int64_t crows = 2 * (j1 - j0), cp = ceil_div(crows, kOzTileB) * kOzTileB;
+                int* xe = c->xex.as<int>() + 2 * j0;
+                int8_t* xd = c->xsl.as<int8_t>() + (size_t)2 * j0 * kp * S;
+                FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->xh_ev[ch], 0));
+                {
+                    const OzView v{static_cast<const double*>(x_dev) + j0 * 2 * n, 2 * n, 2, 0, 1, 0, (int)crows,
+                                   (int)cp, 1, (int)n, (int)kp, false};
+                    ProfScope ps(KC_SLICE, c->pk_g);
+                    FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, xd, xe, nullptr, c->pk_g), 1);
+                }
+                if (ch == 0) FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_es[s], 0));
+                ProfScope ps(KC_I8GEMM, c->pk_g);
+                FGB_LAUNCH(launch_ozgemm(S, 1, dst, ex, (int)(rows * rp), xd, xe, (int)cp, (int)kp,
+                                         static_cast<double*>(y) + 2 * sh.r0 + j0 * 2 * n, n, 2 * n * b, (int)rv,
+                                         (int)rp, (int)crows, c->pk_g, nullptr, 0, 0),
+                           1);
+            }
+            row_off += rp;
+            continue;
+        }
         FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_es[s], 0));
         {
             ProfScope ps(KC_I8GEMM, c->pk_g);
@@ -1512,11 +1567,18 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
 }
 
 int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,
-                    void* y_dev, double* loss_dev, double* dlda_dev) {
+                    void* y_dev, double* loss_dev, double* dlda_dev, const double* x_host, const double* xc_host) {
     const int64_t n = c->n, blk = 2 * n * b;  // doubles per n x b complex block
     const int rows = 2 * n_alpha;             // table rows [c(a_0) ..][c'(a_0) ..]: Q_a then dQ_a
     FGB_CUDA(c->ydy.ensure((size_t)rows * blk * sizeof(double)));
-    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l)) return st;
+    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l, x_host)) return st;
+    if (xc_host) {  // Xc behind X on the aux stream: only the final loss pass needs it
+        if (!c->xc_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->xc_evt, cudaEventDisableTiming));
+        FGB_CUDA(cudaMemcpyAsync(const_cast<void*>(xc_dev), xc_host, (size_t)n * b * 16, cudaMemcpyHostToDevice,
+                                 c->aux_stream));
+        FGB_CUDA(cudaEventRecord(c->xc_evt, c->aux_stream));
+        c->xc_pending = true;
+    }
     if (int st = wait_xc(c)) return st;
     FGB_CUDA(c->lpart.ensure(mse_dy_part_elems() * sizeof(double)));
     const double norm = 1.0 / ((double)n * (double)b);
@@ -2065,6 +2127,35 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
     if (int st = check_alphas(alphas, n_alpha)) return st;
     if (b < 1) return fail(FGFRFT_SHAPE, "mse_step: need at least one signal");
     if (!x || !xc || !loss || !dlda) return fail(FGFRFT_PARAMETER, "null buffer");
+    {
+        // Packed route (one or two orders, real F, large batch): X goes up in column chunks that
+        // overlap the synthesis and the earlier chunks' products, Xc behind it (mse_packed_step).
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard dg(c->device);
+        if (c->dtype == FGFRFT_C128 && !c->api_c64 && n_alpha <= 2 && packed_enabled(c) && use_int8_gemm(c, b) &&
+            !use_fused_apply(c, n_alpha, b) && !use_power_route(c, n_alpha) && ensure_packed(c)) {
+            const size_t xe = (size_t)c->n * b;
+            FGB_CUDA(c->x.ensure(xe * 16));
+            FGB_CUDA(c->xc.ensure(xe * 16));
+            FGB_CUDA(c->loss.ensure((size_t)n_alpha * 2 * sizeof(double)));
+            if (y) FGB_CUDA(c->y.ensure(xe * 16 * n_alpha));
+            double* coef = nullptr;
+            if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
+            double* ld = c->loss.as<double>();
+            if (int st = mse_packed_step(c, coef, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha,
+                                         x, xc))
+                return st;
+            std::vector<double> out(2 * (size_t)n_alpha);
+            FGB_CUDA(cudaMemcpyAsync(out.data(), ld, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            if (y) {
+                if (int st = download_signal(c, c->y.p, xe * n_alpha, y)) return st;
+            }
+            FGB_CUDA(cudaStreamSynchronize(c->stream));
+            std::memcpy(loss, out.data(), n_alpha * sizeof(double));
+            std::memcpy(dlda, out.data() + n_alpha, n_alpha * sizeof(double));
+            return FGFRFT_OK;
+        }
+    }
     {
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);

@@ -168,7 +168,12 @@ size_t packed_bytes(int n, int l);
 cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream);
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
-                          int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0);
+                          int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0,
+                          int pbase = 0);
+cudaError_t launch_pack_pairs_from_panels(const double* rp, int64_t ld_r, const double* cp, int64_t ld_c, int n, int I0,
+                                          int pbase, int npairs_local, int k, int l, void* packed, double* scales,
+                                          cudaStream_t stream);
+size_t packed_bytes_pairs(int64_t npairs, int l);
 size_t packed_scale_elems(int n, int l);
 int64_t packed_pairs_before(int I, int nt);
 size_t mse_dy_part_elems();
@@ -350,6 +355,16 @@ struct fgfrft_cache {
     // in (signal row, term) interleaved order, P_L in column-major form, and per-call buffers.
     int ps3_slices = 0;
     DevBuf ps3, pe3, plr, zd, zaux, cdig, cex;
+    // Pair shard (fgfrft_pshard_*, capi_pshard.cu): tile pairs [pbase, pend) = tile-row band
+    // [I0, I1) of `world`; the packed slabs (pk, pks) hold only those pairs; pp = this rank's
+    // partial [Y; dY] (zero outside its rows), ppc = the reduce-scatter's column chunk.
+    bool pshard = false;
+    int world = 1, rank = 0, I0 = 0, I1 = 0;
+    int64_t pbase = 0, pend = 0;
+    struct fgfrft_comm* comm = nullptr;
+    DevBuf pp, ppc;
+    int64_t pp_b = -1;
+    int pp_rows = -1;
     // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
     bool shard = false;
     int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64
@@ -375,6 +390,7 @@ struct fgfrft_cache {
     cudaStream_t pk_s = nullptr, pk_g = nullptr;
     cudaEvent_t pk_e0 = nullptr, pk_eg = nullptr, pk_ex = nullptr;
     std::vector<cudaEvent_t> pk_es;
+    std::vector<cudaEvent_t> xh_ev;  // host-X column chunks landed (chunked host MSE step)
     std::vector<PkShell> pk_plan;
     uint64_t pk_plan_key = 0;
     double* coef_h = nullptr;  // pinned staging for the coefficient tables
@@ -454,8 +470,9 @@ bool aux_fits(fgfrft_cache* c, uint64_t bytes);
 bool packed_enabled(const fgfrft_cache* c);
 bool ensure_packed(fgfrft_cache* c);
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
-                    void* y, int l_used);
+                    void* y, int l_used, const double* x_host = nullptr);
 int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,
-                    void* y_dev, double* loss_dev, double* dlda_dev);
+                    void* y_dev, double* loss_dev, double* dlda_dev, const double* x_host = nullptr,
+                    const double* xc_host = nullptr);
 
 }  // namespace fgbi

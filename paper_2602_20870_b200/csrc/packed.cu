@@ -145,7 +145,8 @@ template <int AC, int G, int S>
 __global__ void __launch_bounds__(G * (kPsConsumers + 32), 1)
 psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __restrict__ scales, int n, int l,
                     int lc, const double* __restrict__ coef, int coef_ld, double* __restrict__ out, int64_t out_stride,
-                    unsigned long long* __restrict__ rowmax, int64_t rm_stride, int nt, int p0, int p1) {
+                    unsigned long long* __restrict__ rowmax, int64_t rm_stride, int nt, int p0, int p1,
+                    int pbase) {
     constexpr int kStage = 2 * kPkTileBytes;
     extern __shared__ __align__(128) unsigned char smem_all[];
     const int g = threadIdx.x / (kPsConsumers + 32);
@@ -179,8 +180,8 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
             const uint64_t pol = policy_evict_first();
             uint32_t used = 0, eph = 0;
             for (int j = 0; j < npairs; ++j) {
-                const int64_t pr = p0 + vcta + (int64_t)j * vgrid;
-                const unsigned char* src = packed + pr * lc * kStage;  // this pair's contiguous records
+                const int64_t pr = p0 + vcta + (int64_t)j * vgrid - pbase;  // local record index
+                const unsigned char* src = packed + pr * lc * kStage;       // this pair's contiguous records
                 int q = 0;
                 for (int k = 1; k <= l; ++k) {
                     if (used >> q & 1) {
@@ -314,7 +315,7 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
 // l: powers summed (the truncation), l_cache: powers stored (the scale layout's stride).
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
-                          int64_t rm_stride, cudaStream_t stream, int p0, int p1, int max_ctas) {
+                          int64_t rm_stride, cudaStream_t stream, int p0, int p1, int max_ctas, int pbase) {
     const int nt = (int)ceil_div(n, kTile);
     if (p1 < 0) p1 = nt * (nt + 1) / 2;
     const int npairs = p1 - p0;
@@ -342,12 +343,81 @@ cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l
         kern<<<grid, GV * (kPsConsumers + 32), smem, stream>>>((const unsigned char*)packed,                 \
                                                               scales, n, l, l_cache,                         \
                                                               coef_dev, coef_ld, out, out_stride, rowmax,    \
-                                                              rm_stride, nt, p0, p1);                        \
+                                                              rm_stride, nt, p0, p1, pbase);                 \
     }
     if (n_alpha == 1) FGB_PS(1) else if (n_alpha == 2) FGB_PS(2) else if (n_alpha == 4) FGB_PS(4) else return cudaErrorInvalidValue;
 #undef FGB_PS
     return cudaGetLastError();
 }
+
+// Pair-sharded build (capi_pshard.cu): rank g owns the pairs whose smaller tile index lies in
+// [I0, I1) and never holds the full cache. Per power k it keeps the row panel P_k[R, :] and the
+// column panel P_k[:, R] (R = rows [32 I0, 32 I1), real, column-major, ld_r = |R|, ld_c = n) and
+// packs its pairs' records for that power from them: slot 0 = tile (I, J) from the row panel,
+// slot 1 = tile (J, I) from the column panel. Records are local: index (pair - pbase).
+__global__ void __launch_bounds__(256) pack_pairs_from_panels_kernel(const double* __restrict__ rp, int64_t ld_r,
+                                                                     const double* __restrict__ cp, int64_t ld_c,
+                                                                     int n, int nt, int I0, int pbase, int k, int l,
+                                                                     unsigned char* __restrict__ packed,
+                                                                     double* __restrict__ scales) {
+    __shared__ double red[8];
+    const int local = (int)(blockIdx.x >> 1), slot = (int)(blockIdx.x & 1);
+    int I, J;
+    pair_of_imajor(pbase + local, nt, I, J);
+    const int r0 = I0 * kTile;
+    double v[4];
+    double m = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int t = threadIdx.x + 256 * q;            // tile position t = j * 32 + (i ^ j)
+        const int jj = t >> 5, ii = (t & 31) ^ jj;      // element (ii, jj) of the tile
+        double x = 0.0;
+        if (slot == 0) {                                 // tile (I, J): rows I*32 + ii of the row panel
+            const int gr = I * kTile + ii, gc = J * kTile + jj;
+            if (gr < n && gc < n) x = rp[(int64_t)(gr - r0) + (int64_t)gc * ld_r];
+        } else {                                         // tile (J, I): columns I*32 + jj of the column panel
+            const int gr = J * kTile + ii, gc = I * kTile + jj;
+            if (gr < n && gc < n) x = cp[(int64_t)gr + (int64_t)(gc - r0) * ld_c];
+        }
+        v[q] = x;
+        m = fmax(m, fabs(x));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    double mx = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    e = max(e, -900);
+    const double up = ldexp(1.0, kPkFrac - e);
+    const int64_t rec = ((int64_t)local * l + k) * 2 + slot;
+    unsigned char* dst = packed + rec * kPkTileBytes;
+    uint32_t* lo = reinterpret_cast<uint32_t*>(dst);
+    uint8_t* hi = dst + kTileElems * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long mi = __double2ll_rn(v[q] * up);
+        const unsigned long long u = (unsigned long long)(mi + (1LL << 39));
+        lo[threadIdx.x + 256 * q] = (uint32_t)u;
+        hi[threadIdx.x + 256 * q] = (uint8_t)(u >> 32);
+    }
+    if (threadIdx.x == 0) scales[rec] = ldexp(1.0, e - kPkFrac);
+}
+
+cudaError_t launch_pack_pairs_from_panels(const double* rp, int64_t ld_r, const double* cp, int64_t ld_c, int n, int I0,
+                                          int pbase, int npairs_local, int k, int l, void* packed, double* scales,
+                                          cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    if (npairs_local <= 0) return cudaSuccess;
+    pack_pairs_from_panels_kernel<<<(unsigned)(2 * npairs_local), 256, 0, stream>>>(
+        rp, ld_r, cp, ld_c, n, nt, I0, pbase, k, l, (unsigned char*)packed, scales);
+    return cudaGetLastError();
+}
+
+size_t packed_bytes_pairs(int64_t npairs, int l) { return (size_t)npairs * (size_t)l * 2 * kPkTileBytes; }
 
 // ---------------------------------------------------------------- MSE + dL/da from [Y; dY]
 // loss = ||Y - Xc||^2 / (n b), dL/da = 2 Re<Y - Xc, dY> / (n b)  (G = 2 (Y - Xc) / (n b),

@@ -235,7 +235,12 @@ class ShardedFGFRFT:
     def apply_fused(self, alphas: Sequence[float], x):
         """Full Y = F^alpha X on every rank with the all-gather fused into the GEMM epilogue: each
         rank's kernel stores its rows into every rank's Y buffer over NVLink (CUDA IPC mappings),
-        then a host barrier. Returns the [A, b, n] device tensor (column-major n x b blocks)."""
+        then a host barrier. Returns a NEW [A, b, n] device tensor (column-major n x b blocks) owned
+        by the caller; the IPC-mapped gather buffer itself is internal.
+
+        Ordering: a barrier before the GEMM (no rank writes into a peer's gather buffer while that
+        peer may still be copying out the previous call's result) and one after it (every rank's
+        rows have landed in every buffer)."""
         torch = __import__("torch")
         dist = self._dist()
         A, b = len(alphas), _signals(x)
@@ -246,11 +251,16 @@ class ShardedFGFRFT:
             self._yfull = y
         world = dist.get_world_size(self.group) if dist.is_initialized() else 1
         peers = self._peer_buffers(y) if world > 1 else []
+        if world > 1:
+            torch.cuda.synchronize(y.device)
+            dist.barrier(group=self.group)  # peers are done reading the previous call's rows
         self.compute.apply_gather(np.asarray(alphas, dtype=np.float64), x, y, peers)
         torch.cuda.synchronize(y.device)
         if world > 1:
             dist.barrier(group=self.group)  # every rank's rows have landed in every buffer
-        return y
+        out = y.clone()
+        torch.cuda.synchronize(y.device)  # the copy-out completes before any peer's next write
+        return out
 
     def apply(self, alphas: Sequence[float], x, plan: Optional[List[Tuple[int, int]]] = None):
         """Full Y = F^alpha X on every rank: local rows, then all_gather of the row blocks."""

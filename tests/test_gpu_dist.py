@@ -150,9 +150,10 @@ def _ipc_worker(rank, world, port, q):
         w = fgd_.ShardedFGFRFT(sh, n, l)
         rng = np.random.default_rng(n)
         x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
-        y = w.apply_fused([0.3, 1.7], x)
-        y2 = w.apply_fused([0.3, 1.7], x)  # cached IPC mappings
-        q.put((rank, y.cpu().numpy(), y2.cpu().numpy()))
+        y = w.apply_fused([0.3, 1.7], x).cpu().numpy()
+        y2 = w.apply_fused([0.9, -0.4], x)  # cached IPC mappings, different orders
+        y3 = w.apply_fused([0.3, 1.7], x)   # the first result is not aliased by later calls
+        q.put((rank, y, y2.cpu().numpy(), y3.cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -175,8 +176,8 @@ def test_apply_fused_two_processes_ipc():
         p.start()
     out = {}
     for _ in range(2):
-        rank, y, y2 = q.get(timeout=300)
-        out[rank] = (y, y2)
+        rank, y, y2, y3 = q.get(timeout=300)
+        out[rank] = ((y, [0.3, 1.7]), (y2, [0.9, -0.4]), (y3, [0.3, 1.7]))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -186,7 +187,7 @@ def test_apply_fused_two_processes_ipc():
     rng = np.random.default_rng(n)
     x = rng.standard_normal((n, 40)) + 1j * rng.standard_normal((n, 40))
     for rank in (0, 1):
-        for y in out[rank]:
+        for y, alphas in out[rank]:
             yy = y.transpose(0, 2, 1)
-            for i, a in enumerate([0.3, 1.7]):
+            for i, a in enumerate(alphas):
                 assert rel(yy[i], O.fgfrft_matrix(o, a) @ x) <= 1e-12

@@ -91,3 +91,23 @@ def test_packed_route_respects_memory_budget():
     assert roomy.route_info()[0] == PACKED_ROUTE
     assert abs(lt[0] - lr[0]) <= 1e-10 * lr[0]
     assert abs(dt_[0] - dr[0]) <= 1e-9 * max(1.0, abs(dr[0]))
+
+
+def test_packed_host_and_device_steps_agree(problem):
+    """fgfrft_mse_step (host buffers: X copied in column chunks overlapping the synthesis) and
+    fgfrft_mse_step_dev (device-resident X) run the same products: identical results."""
+    import torch
+    f, l, x, xc, g, o = problem
+    n, b = x.shape
+    al = np.array([0.81, -0.4])
+    loss_h, dl_h, _ = fg.mse_step(g, al, x, xc)
+    xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    xcd = torch.from_numpy(np.ascontiguousarray(xc.T)).cuda()
+    lo = torch.empty(2, dtype=torch.float64, device="cuda")
+    dl = torch.empty(2, dtype=torch.float64, device="cuda")
+    g.set_stream(torch.cuda.current_stream().cuda_stream)
+    fg._check(fg.lib().fgfrft_mse_step_dev(g.handle, al.ctypes.data, 2, xd.data_ptr(), xcd.data_ptr(), b, None,
+                                           lo.data_ptr(), dl.data_ptr()))
+    torch.cuda.synchronize()
+    assert np.allclose(lo.cpu().numpy(), loss_h, rtol=1e-14, atol=0)
+    assert np.allclose(dl.cpu().numpy(), dl_h, rtol=1e-12, atol=1e-300)
