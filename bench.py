@@ -266,6 +266,143 @@ def c2_sweep(fg, torch, stream, dev):
             "nodes": nodes}
 
 
+def run_sharded(args, ws, rank, local):
+    """--gpus N > 1 (torchrun): the config-3 step on N pair shards (strong scaling). The library owns
+    the NCCL communicator (fgfrft_comm_*); torch.distributed (gloo, host tensors) is used only to hand
+    out its 128-byte id, for barriers and for the max over ranks of the device-timed step."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_20870_b200 as fg
+    import prep
+    from paper_2602_20870_b200 import pshard as ps
+
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", str(rank)),
+                 ("WORLD_SIZE", str(ws))):
+        os.environ.setdefault(k, v)
+    dist.init_process_group("gloo")
+    peaks = _peaks()
+    uid = [ps.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = ps.Comm(uid[0], ws, rank, local)
+    cfg = prep.config3(seed=1)
+    n, b = cfg.x.shape
+    L = cfg.l
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    # F from rank 0 only: the library broadcasts it over the communicator (the build's one collective)
+    sh = ps.PairShard(cfg.f if rank == 0 else None, L, memory_budget=64 << 30, comm=comm, n=n)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream()
+    sh.set_stream(stream.cuda_stream)
+    xd = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).to(dev)
+    xcd = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).to(dev)
+    L_ = fg.lib()
+    al = [np.array([a]) for a in ALPHAS]
+    lo = torch.empty(2, dtype=torch.float64, device=dev)
+    dl = torch.empty(2, dtype=torch.float64, device=dev)
+
+    def step(i):
+        fg._check(L_.fgfrft_pshard_mse_step_dev(sh.handle, al[i & 1].ctypes.data, 1, xd.data_ptr(), xcd.data_ptr(),
+                                                b, lo[i & 1:].data_ptr(), dl[i & 1:].data_ptr()))
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    l0 = fg.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    e1.synchronize()
+    launches = fg.launch_count() - l0
+    clk = clocks.stop() if rank == 0 else None
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms_t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t[0])
+    res = (lo.cpu().numpy().copy(), dl.cpu().numpy().copy())
+    # per-rank synthesis class (CUDA events on the stream the kernels run on), separate pass
+    fg.profile_enable(True)
+    fg.profile_read(reset=True)
+    for i in range(args.steps):
+        step(i)
+    torch.cuda.synchronize()
+    prof = fg.profile_read(reset=True)
+    fg.profile_enable(False)
+    info = sh.info()
+    syn_ms, syn_n = prof["synthesis"]
+    local_pairs = info["pair_end"] - info["pair_begin"]
+    syn_bytes = local_pairs * L * 2 * (32 * 32 * 5 + 8)
+    syn_gbs = syn_bytes * syn_n / (syn_ms * 1e-3) / 1e9 if syn_ms else None
+    # e2e: host buffers through the C ABI (H2D of X, Xc inside the timed region)
+    xh = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).pin_memory()  # column-major n x b, pinned
+    xch = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).pin_memory()
+    lh, dh = np.empty(1), np.empty(1)
+
+    def step_e2e(i):
+        fg._check(L_.fgfrft_pshard_mse_step(sh.handle, al[i & 1].ctypes.data, 1, xh.data_ptr(), xch.data_ptr(), b,
+                                            lh.ctypes.data, dh.ctypes.data))
+
+    for i in range(2):
+        step_e2e(i)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step_e2e(i)
+    e2e_t = torch.tensor([(time.perf_counter() - t0) / args.steps * 1e3], dtype=torch.float64)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_t[0])
+    rows = torch.tensor([syn_gbs or 0.0, float(local_pairs)], dtype=torch.float64)
+    allrows = [torch.zeros_like(rows) for _ in range(ws)]
+    dist.all_gather(allrows, rows)
+    check = None
+    if rank == 0:  # the unsharded single-GPU step on the same inputs
+        cache = fg.PowerCache(cfg.f, L, memory_budget=64 << 30, device=local)
+        check = []
+        for i, a in enumerate(ALPHAS):
+            l1, d1, _ = fg.mse_step(cache, [a], cfg.x, cfg.x_clean)
+            check.append({"alpha": a, "loss": float(res[0][i]), "loss_unsharded": float(l1[0]),
+                          "loss_rel_diff": abs(float(res[0][i]) - float(l1[0])) / abs(float(l1[0])),
+                          "dlda": float(res[1][i]), "dlda_unsharded": float(d1[0]),
+                          "dlda_rel_diff": abs(float(res[1][i]) - float(d1[0])) / max(abs(float(d1[0])), 1e-300)})
+        cache.close()
+        out = {
+            "metric": METRIC, "value": n * b / (ms * 1e-3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded generators, prep/)",
+            "config": workload_config(n, b, L, True, ws),
+            "roofline": {"bound": "hbm", "kernel": "psynth_pairs_kernel<2> on each rank's pair band",
+                         "achieved": syn_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": syn_gbs / peaks["hbm_gbs"] if syn_gbs else None, "traffic": None,
+                         "algorithmic": "rank 0: its pairs x L x 2 tiles x (5 KB + 8 B scale) read",
+                         "per_rank_gbs": [float(r[0]) for r in allrows],
+                         "per_rank_pairs": [int(r[1]) for r in allrows], "peak_source": peaks["hbm_src"]},
+            "collectives": "per step: ncclReduceScatter of [Y; dY] (2 x N x B complex128, by signal-column chunks) "
+                           "+ ncclAllReduce of 2 doubles; build: ncclBroadcast of F",
+            "cache_build": {"seconds": build_s, "note": "per-rank panel recursion + packing of its pairs"},
+            "e2e": {"value": n * b / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 2 * n * b * 16, "d2h_bytes_per_step": 16,
+                    "note": "fgfrft_pshard_mse_step with host X, Xc on every rank; max over ranks of wall time"},
+            "gpu_launches": launches, "clocks": clk, "parity_check": check,
+        }
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    sh.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -274,6 +411,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="the pair-sharded path even at N = 1 (validation)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = _dist()
@@ -281,9 +419,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
-    if ws > 1:
-        import bench_sharded
-        bench_sharded.main(args, ws, rank, local)
+    if ws > 1 or args.sharded:
+        run_sharded(args, ws, rank, local)
         return
 
     import torch

@@ -14,6 +14,7 @@
 namespace fgfrft {
 using MatrixXcd = Eigen::MatrixXcd;
 using VectorXd = Eigen::VectorXd;
+using MatrixXd = Eigen::MatrixXd;
 using Index = Eigen::Index;
 }  // namespace fgfrft
 #define FGFRFT_HAVE_EIGEN 1
@@ -97,6 +98,38 @@ class MatrixXcd {
   private:
     Index r_ = 0, c_ = 0;
     std::vector<Scalar> d_;
+};
+
+// Real dense matrix (column-major) with the Eigen::MatrixXd members the graph / GFT fallbacks use.
+class MatrixXd {
+  public:
+    using Scalar = double;
+    MatrixXd() = default;
+    MatrixXd(Index r, Index c) : r_(r), c_(c), d_(static_cast<size_t>(r * c), 0.0) {}
+    static MatrixXd Zero(Index r, Index c) { return MatrixXd(r, c); }
+    Index rows() const { return r_; }
+    Index cols() const { return c_; }
+    Index size() const { return r_ * c_; }
+    double* data() { return d_.data(); }
+    const double* data() const { return d_.data(); }
+    double& operator()(Index i, Index j) { return d_[static_cast<size_t>(i + j * r_)]; }
+    const double& operator()(Index i, Index j) const { return d_[static_cast<size_t>(i + j * r_)]; }
+    double squaredNorm() const {
+        double s = 0.0;
+        for (double v : d_) s += v * v;
+        return s;
+    }
+    double norm() const { return std::sqrt(squaredNorm()); }
+    MatrixXd transpose() const {
+        MatrixXd t(c_, r_);
+        for (Index j = 0; j < c_; ++j)
+            for (Index i = 0; i < r_; ++i) t(j, i) = (*this)(i, j);
+        return t;
+    }
+
+  private:
+    Index r_ = 0, c_ = 0;
+    std::vector<double> d_;
 };
 
 // Real vector with the Eigen::VectorXd members the learning API uses.

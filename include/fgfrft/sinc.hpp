@@ -8,6 +8,10 @@
 
 #include "fgfrft/errors.hpp"
 
+#if defined(FGFRFT_HAVE_EIGEN) && __has_include_next(<fgfrft/sinc.hpp>)
+// integration builds: the reference's own (std-only, bit-identical) sinc.hpp
+#include_next <fgfrft/sinc.hpp>
+#else
 namespace fgfrft {
 
 struct SincCoeffs {
@@ -19,6 +23,18 @@ struct SincCoeffs {
     double coeff(int n) const { return c[static_cast<std::size_t>(n + l)]; }
     double dcoeff(int n) const { return dc[static_cast<std::size_t>(n + l)]; }
 };
+
+// sin(pi x) / (pi x) and its derivative (sinc.hpp:15-36): c_0 and c_0' of the order x.
+inline double sinc(double x) {
+    double c[3], dc[3];
+    detail::throw_status(fgfrft_sinc_coeffs(x, 1, c, dc));
+    return c[1];
+}
+inline double sinc_deriv(double x) {
+    double c[3], dc[3];
+    detail::throw_status(fgfrft_sinc_coeffs(x, 1, c, dc));
+    return dc[1];
+}
 
 inline SincCoeffs sinc_coeffs(double alpha, int l) {
     if (l < 1) throw parameter_error("sinc_coeffs: truncation order must be >= 1");
@@ -32,3 +48,4 @@ inline SincCoeffs sinc_coeffs(double alpha, int l) {
 }
 
 }  // namespace fgfrft
+#endif

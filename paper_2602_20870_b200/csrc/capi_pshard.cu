@@ -282,6 +282,7 @@ int pshard_partial(fgfrft_cache* c, const double* coef, int coef_ld, int rows, c
                                  c->stream, (int)c->pbase, (int)c->pend, 0, (int)c->pbase),
                    1);
     }
+    if (int st = wait_xc(c)) return st;  // host-buffer step: X (and Xc) uploaded on the aux stream
     {
         ProfScope ps(KC_SLICE, c->stream);
         OzView va{q + r0 + r0 * n, 1, n, sl, 0, 0, (int)rvA, (int)rpA, rows, (int)kvA, (int)kpA, true};
@@ -537,8 +538,17 @@ int fgfrft_pshard_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, c
         FGB_CUDA(c->x.ensure(xe * 16));
         FGB_CUDA(c->xc.ensure(xe * 16));
         FGB_CUDA(c->dlda.ensure((size_t)2 * n_alpha * 8));
-        FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xe * 16, cudaMemcpyHostToDevice, c->stream));
-        FGB_CUDA(cudaMemcpyAsync(c->xc.p, xc, xe * 16, cudaMemcpyHostToDevice, c->stream));
+        // X and Xc go up on the aux stream while the synthesis runs (it does not need them); the
+        // partial products wait for X right before its slicing, the loss pass for Xc (x_evt).
+        if (!c->aux_stream) FGB_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        if (!c->xc_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->xc_evt, cudaEventDisableTiming));
+        if (!c->pk_e0) FGB_CUDA(cudaEventCreateWithFlags(&c->pk_e0, cudaEventDisableTiming));
+        FGB_CUDA(cudaEventRecord(c->pk_e0, c->stream));  // the previous call's readers are done
+        FGB_CUDA(cudaStreamWaitEvent(c->aux_stream, c->pk_e0, 0));
+        FGB_CUDA(cudaMemcpyAsync(c->x.p, x, xe * 16, cudaMemcpyHostToDevice, c->aux_stream));
+        FGB_CUDA(cudaMemcpyAsync(c->xc.p, xc, xe * 16, cudaMemcpyHostToDevice, c->aux_stream));
+        FGB_CUDA(cudaEventRecord(c->xc_evt, c->aux_stream));
+        c->xc_pending = true;
     }
     double* out = c->dlda.as<double>();
     if (int st = fgfrft_pshard_mse_step_dev(c, alphas, n_alpha, c->x.p, c->xc.p, b, out, out + n_alpha)) return st;
