@@ -438,7 +438,8 @@ def main():
     # ---- K1: power cache built on device, outside the timed region (as transform.hpp:43-59)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cache = fg.PowerCache(cfg.f, L, memory_budget=64 << 30, device=local)
+    # budget: the reference count L N^2 16 B (17.2 GB) + the packed slabs (5.4 GB) the step route uses
+    cache = fg.PowerCache(cfg.f, L, memory_budget=24 << 30, device=local)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     real = cache.is_real()

@@ -541,7 +541,22 @@ int engine_of(const fgfrft_cache* c) {
     return env;
 }
 
-bool use_power_route(const fgfrft_cache* c, int n_alpha) {
+int64_t pad_rows(int64_t n) { return ceil_div(n, kOzTileA) * kOzTileA; }
+int64_t pad_k(int64_t n) { return ceil_div(n, kOzK) * kOzK; }
+
+// Device bytes of the INT8 digit slices the sweep routes build once per cache (counted against
+// the handle's memory budget, aux_fits): the stacked cache for the power route, its element rows
+// for the node route.
+uint64_t power_slice_bytes(const fgfrft_cache* c) {
+    const uint64_t rows = 2 * (uint64_t)c->l * pad_rows(c->n);
+    return (uint64_t)oz_slices_default() * rows * pad_k(c->n) + rows * 12;
+}
+uint64_t elem_slice_bytes(const fgfrft_cache* c) {
+    const uint64_t rows = pad_rows(c->n * c->n);
+    return (uint64_t)oz_slices_default() * rows * pad_k(2 * (int64_t)c->l) + rows * 12;
+}
+
+static bool power_route_shape(const fgfrft_cache* c, int n_alpha) {
     if (!c->real || c->dtype != FGFRFT_C128 || 2 * c->l + 1 > combine_max_terms() || c->n > 16384) return false;
     const int eng = engine_of(c);
     if (eng == FGFRFT_ENGINE_DMMA) return false;
@@ -549,8 +564,9 @@ bool use_power_route(const fgfrft_cache* c, int n_alpha) {
     return 2 * n_alpha >= c->l;  // auto: 2L products amortised over the orders
 }
 
-int64_t pad_rows(int64_t n) { return ceil_div(n, kOzTileA) * kOzTileA; }
-int64_t pad_k(int64_t n) { return ceil_div(n, kOzK) * kOzK; }
+bool use_power_route(const fgfrft_cache* c, int n_alpha) {
+    return power_route_shape(c, n_alpha) && (c->ps_slices || aux_fits(c, power_slice_bytes(c)));
+}
 
 int wait_xc(fgfrft_cache* c);
 
@@ -571,8 +587,8 @@ bool use_node_route(const fgfrft_cache* c, int n_alpha, int64_t b) {
         const char* e = std::getenv("FGFRFT_ROUTE");
         return (e && !std::strcmp(e, "power")) ? 0 : 1;
     }();
-    return mode == 1 && use_power_route(c, n_alpha) && engine_of(c) == FGFRFT_ENGINE_AUTO && use_int8_gemm(c, b) &&
-           n_alpha >= 16 && n_alpha <= 64 && c->n <= 46340;
+    return mode == 1 && power_route_shape(c, n_alpha) && engine_of(c) == FGFRFT_ENGINE_AUTO && use_int8_gemm(c, b) &&
+           n_alpha >= 16 && n_alpha <= 64 && c->n <= 46340 && (c->es_slices || aux_fits(c, elem_slice_bytes(c)));
 }
 
 int ensure_elem_slices(fgfrft_cache* c) {
@@ -593,6 +609,7 @@ int ensure_elem_slices(fgfrft_cache* c) {
                                c->stream),
                3);
     c->es_slices = S;
+    c->aux_bytes += elem_slice_bytes(c);
     return FGFRFT_OK;
 }
 
@@ -685,7 +702,17 @@ static bool node_plan_r(const double* alphas, int na, int l, bool need_d, const 
         }
     }
     *rp_out = rp;
-    return ce <= 4e-15 * cmax && (!need_d || de <= 2e-12 * std::max(dmax, 1e-300));
+    // The derivative weights l_j'(a) amplify the node operators' INT8 error (~5e-14 of |W_j|) by
+    // sum_j |l_j'(a)| ~ 420 / width: capped at 5000 (width >~ 0.08; the parity tests hold 1e-10 at
+    // width 0.1) -- narrower sweeps take the power route (2L products, no derivative amplification).
+    double lsum = 0.0;
+    if (need_d)
+        for (int a = 0; a < na; ++a) {
+            double t = 0.0;
+            for (int j = 0; j < r; ++j) t += std::fabs(pw[(size_t)(na + a) * rp + j]);
+            lsum = std::max(lsum, t);
+        }
+    return ce <= 4e-15 * cmax && (!need_d || (de <= 2e-12 * std::max(dmax, 1e-300) && lsum <= 5000.0));
 }
 
 bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* r_out, int* rp_out) {
@@ -851,6 +878,23 @@ int mse_node_route(fgfrft_cache* c, const double* alphas, int n_alpha, const voi
                                    c->nd_p.as<double>(), n_alpha, static_cast<double*>(y_dev), c->partial.as<double>(),
                                    1.0 / ((double)c->n * (double)b), loss_dev, dlda_dev, c->stream),
                xc_dev ? 2 : 1);
+    // alpha = 0 exactly: Q(0) = I (sinc.hpp:16 Kronecker coefficients, test_transform.cpp:60-65), so
+    // Y = X bit for bit and the loss is ||X - Xc||^2 / (N B) -- snapped instead of interpolated.
+    // (Other integer orders keep the INT8 product error, <= 3e-13 relative, like every order.)
+    for (int a = 0; a < n_alpha; ++a) {
+        if (alphas[a] != 0.0) continue;
+        const size_t blk = (size_t)2 * c->n * b;
+        if (y_dev)
+            FGB_CUDA(cudaMemcpyAsync(static_cast<double*>(y_dev) + (size_t)a * blk, x_dev, blk * 8,
+                                     cudaMemcpyDeviceToDevice, c->stream));
+        if (xc_dev && loss_dev) {
+            FGB_CUDA(c->lpart.ensure((mse_dy_part_elems() + 1) * sizeof(double)));
+            double* scratch = c->lpart.as<double>() + mse_dy_part_elems();  // the dot of X with itself: unused
+            FGB_LAUNCH(launch_mse_dy(x_dev, x_dev, xc_dev, c->n * b, nullptr, c->lpart.as<double>(),
+                                     1.0 / ((double)c->n * (double)b), loss_dev + a, scratch, c->stream),
+                       2);
+        }
+    }
     *ran = true;
     c->last_route = 2;
     c->last_nodes = r;
@@ -877,6 +921,7 @@ int ensure_power_slices(fgfrft_cache* c) {
                    3);
     }
     c->ps_slices = S;
+    c->aux_bytes += power_slice_bytes(c);
     return FGFRFT_OK;
 }
 
@@ -1279,7 +1324,7 @@ int dots_device(fgfrft_cache* c, int n_alpha, const void* g_dev, const void* x_d
 
 // The reference's budget counts L n^2 16 bytes (transform.hpp:46-53); auxiliary representations
 // are admitted while that count plus every admitted auxiliary byte stays within the handle's budget.
-bool aux_fits(fgfrft_cache* c, uint64_t bytes) {
+bool aux_fits(const fgfrft_cache* c, uint64_t bytes) {
     const unsigned __int128 ref = (unsigned __int128)c->l * (uint64_t)c->n * (uint64_t)c->n * 16;
     return ref + c->aux_bytes + bytes <= (unsigned __int128)c->budget;
 }
@@ -1759,9 +1804,16 @@ int fgfrft_cache_prepare(fgfrft_cache* c) {
     if (int st = check_handle(c)) return st;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard dg(c->device);
+    // every structure a route may build lazily, in the order the routes prefer them, each only while
+    // it fits the handle's memory budget (aux_fits): the packed slabs (one / two-order steps), the
+    // element-row digit slices (node-interpolated sweeps), the stacked digit slices (power route)
+    if (packed_enabled(c)) ensure_packed(c);
     if (c->real && c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA &&
         2 * c->l + 1 <= combine_max_terms()) {
-        if (int st = ensure_power_slices(c)) return st;
+        if (engine_of(c) == FGFRFT_ENGINE_AUTO && !c->es_slices && aux_fits(c, elem_slice_bytes(c)))
+            if (int st = ensure_elem_slices(c)) return st;
+        if (!c->ps_slices && aux_fits(c, power_slice_bytes(c)))
+            if (int st = ensure_power_slices(c)) return st;
         if (use_int8_combine(c))
             if (int st = ensure_power_slices3(c)) return st;
     }

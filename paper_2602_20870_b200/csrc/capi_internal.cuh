@@ -466,9 +466,12 @@ int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype,
                   fgfrft_cache** made);
 int check_orthogonal(fgfrft_cache* c, const double* fr, double* scratch);
 int check_spectrum(const fgfrft_spectrum* s);
-bool aux_fits(fgfrft_cache* c, uint64_t bytes);
+bool aux_fits(const fgfrft_cache* c, uint64_t bytes);
 int wait_xc(fgfrft_cache* c);
 bool packed_enabled(const fgfrft_cache* c);
+uint64_t power_slice_bytes(const fgfrft_cache* c);
+uint64_t elem_slice_bytes(const fgfrft_cache* c);
+int ensure_elem_slices(fgfrft_cache* c);
 bool ensure_packed(fgfrft_cache* c);
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
                     void* y, int l_used, const double* x_host = nullptr);

@@ -111,3 +111,32 @@ def test_packed_host_and_device_steps_agree(problem):
     torch.cuda.synchronize()
     assert np.allclose(lo.cpu().numpy(), loss_h, rtol=1e-14, atol=0)
     assert np.allclose(dl.cpu().numpy(), dl_h, rtol=1e-12, atol=1e-300)
+
+
+def test_node_sweep_snaps_order_zero_and_narrow_sweeps_fall_back():
+    """Node-interpolated sweeps (real F, 16-64 orders): alpha = 0 returns X bit for bit (Q(0) = I,
+    test_transform.cpp:60-65); a narrow sweep (width 0.01) whose derivative weights
+    would amplify the node operators' INT8 error takes the power route and stays at 1e-10."""
+    n, l, b = 512, 10, 40
+    f = _graph_f(n, 23)
+    g = fg.PowerCache(f, l, memory_budget=4 << 30)
+    o = O.PowerCache(f, l)
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    xc = x + 0.1 * rng.standard_normal((n, b))
+    wide = np.linspace(0.0, 2.0, 24)
+    loss, dl, y = fg.mse_step(g, wide, x, xc, want_y=True)
+    assert g.route_info()[0] == 2
+    assert np.array_equal(y[0], x)
+    assert loss[0] == np.vdot(x - xc, x - xc).real / (n * b) or abs(loss[0] - np.vdot(x - xc, x - xc).real / (n * b)) \
+        <= 1e-15 * loss[0]
+    narrow = np.linspace(0.7, 0.71, 32)
+    loss, dl, _ = fg.mse_step(g, narrow, x, xc)
+    assert g.route_info()[0] == 1  # power products: no derivative-weight amplification
+    for i in (0, 13, 31):
+        a = float(narrow[i])
+        lr, dr, yr = O.dlda_mse(o, a, x, xc)
+        s = O.power_dots(o, 2.0 * (yr - xc) @ x.conj().T / x.size)
+        _, dc = O.sinc_coeffs(a, l)
+        assert abs(loss[i] - lr) <= 1e-10 * lr
+        assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s))
