@@ -386,13 +386,21 @@ def series_apply_recursive(f: np.ndarray, alpha: float, l: int, x: np.ndarray, w
     if inverse:  # Q^H = sum conj(c_k) F^{-k}: swap the roles of +k and -k (real coefficients)
         coef = coef[::-1]
     x = np.asarray(x, dtype=np.complex128)
-    fh = np.ascontiguousarray(f.conj().T)
-    fp = np.ascontiguousarray(f)
+    if not np.any(f.imag):  # real F (graph GFTs): the same products as real GEMMs on (Re, Im)
+        fp, fh = np.ascontiguousarray(f.real), np.ascontiguousarray(f.real.T)
+
+        def mul(m, v):
+            return m @ v.real + 1j * (m @ v.imag)
+    else:
+        fp, fh = np.ascontiguousarray(f), np.ascontiguousarray(f.conj().T)
+
+        def mul(m, v):
+            return m @ v
     acc = coef[l] * x
     vp, vm = x, x
     for k in range(1, l + 1):
-        vp = fp @ vp
-        vm = fh @ vm
+        vp = mul(fp, vp)
+        vm = mul(fh, vm)
         acc = acc + (coef[l + k] * vp + coef[l - k] * vm)
     return acc
 

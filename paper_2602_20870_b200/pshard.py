@@ -134,9 +134,15 @@ class PairShard:
     def set_stream(self, stream_handle: int) -> None:
         _check(lib().fgfrft_pshard_set_stream(self._h, ctypes.c_void_p(stream_handle)))
 
+    def _torch_stream(self):
+        """Device calls are stream-ordered with torch's current stream (like the tensors they fill)."""
+        import torch
+        self.set_stream(torch.cuda.current_stream().cuda_stream)
+
     def partial(self, alphas: Sequence[float], x_dev, with_dq: bool = True):
         """This rank's partial products (device tensor [rows, b, n] complex128; column-major blocks)."""
         import torch
+        self._torch_stream()
         al = np.ascontiguousarray(alphas, dtype=np.float64)
         b = int(x_dev.shape[0])
         rows = len(al) * (2 if with_dq else 1)
@@ -148,6 +154,7 @@ class PairShard:
     def mse_step_dev(self, alphas: Sequence[float], x_dev, xc_dev):
         """(loss, dL/da) device tensors, every rank (reduce-scatter + all-reduce inside)."""
         import torch
+        self._torch_stream()
         al = np.ascontiguousarray(alphas, dtype=np.float64)
         lo = torch.empty(len(al), dtype=torch.float64, device=x_dev.device)
         dl = torch.empty(len(al), dtype=torch.float64, device=x_dev.device)
@@ -167,6 +174,7 @@ class PairShard:
     def apply_dev(self, alphas: Sequence[float], x_dev, inverse: bool = False):
         """Full Y = F^a X on every rank (all-reduce of the partials): [A, b, n] complex128."""
         import torch
+        self._torch_stream()
         al = np.ascontiguousarray(alphas, dtype=np.float64)
         b = int(x_dev.shape[0])
         y = torch.empty((len(al), b, self.n), dtype=torch.complex128, device=x_dev.device)

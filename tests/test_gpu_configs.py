@@ -178,3 +178,94 @@ def test_config3_complex64_full_size():
         assert abs(dl[0] - float(np.dot(dc, s_ref))) <= 1e-4 * float(np.sum(np.abs(dc * s_ref)))
     finally:
         cache.close()
+
+
+@pytest.mark.skipif(not HEAVY, reason="FGFRFT_SKIP_HEAVY=1")
+def test_config3_headline_step_full_batch_dense_oracle():
+    """The bench's headline step (config 3, the full B = 1024 batch, the packed route) against the
+    DENSE oracle on the same inputs: Y = F^a X, the loss and dL/da (transform.hpp:111-148,
+    learn.hpp:88-92 form) within 1e-10; plus the series-vs-eigendecomposition approximation error
+    (spectral.hpp:121-166, metrics.hpp:21-34) reproduced to 3 digits with the GPU spectrum."""
+    from threadpoolctl import threadpool_limits
+    cfg = prep.config3()
+    n, b = cfg.x.shape
+    cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=24 << 30)
+    try:
+        with threadpool_limits(os.cpu_count() or 1):
+            o = O.PowerCache(cfg.f, cfg.l, memory_budget=1 << 40, real_recursion=True)
+            for a in (0.37, -1.3):
+                loss, dl, y = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
+                assert cache.route_info()[0] == 3
+                q = O.fgfrft_matrix(o, a, nthreads=os.cpu_count() or 1)
+                yr = q @ cfg.x
+                r = yr - cfg.x_clean
+                lr = float(np.vdot(r, r).real) / (n * b)
+                dq = O.fgfrft_grad(o, a, nthreads=os.cpu_count() or 1)
+                dr = float(np.sum(np.conj(2.0 * r / (n * b)) * (dq @ cfg.x)).real)
+                assert rel(y[0], yr) <= 1e-10
+                assert abs(loss[0] - lr) <= 1e-10 * lr
+                assert abs(dl[0] - dr) <= 1e-10 * max(abs(dr), 1e-3)
+            # series vs exact: the GPU spectrum against the oracle's (CPU) decomposition
+            a = 0.37
+            eig_g = fg.eigendecompose_unitary(cfg.f)
+            e_gpu = O.matrix_errors(fg.fgfrft_matrix(cache, a).q, fg.exact_gfrft(eig_g, a).q)
+            eig_o = O.eigendecompose_unitary(cfg.f)
+            e_ref = O.matrix_errors(O.fgfrft_matrix(o, a, nthreads=os.cpu_count() or 1), O.exact_gfrft(eig_o, a))
+            for key in ("mse", "nmse"):  # unitarily invariant (SURVEY 8(c)): robust to eigenbasis choices
+                assert abs(e_gpu[key] - e_ref[key]) <= 5e-4 * e_ref[key], (key, e_gpu[key], e_ref[key])
+            del o
+    finally:
+        cache.close()
+
+
+def test_config2_series_vs_eig_three_digits():
+    """Config 2: the series-vs-eigendecomposition error of the device path (series synthesis and the
+    GPU spectrum's exact operator) equals the oracle's to 3 significant digits, over the sweep."""
+    cfg = prep.config2()
+    o = O.PowerCache(cfg.f, cfg.l)
+    g = fg.PowerCache(cfg.f, cfg.l, memory_budget=8 << 30)
+    eig_g = fg.eigendecompose_unitary(cfg.f)
+    eig_o = O.eigendecompose_unitary(cfg.f)
+    for a in (0.25, 0.73, 1.5):
+        e_gpu = O.matrix_errors(fg.fgfrft_matrix(g, a).q, fg.exact_gfrft(eig_g, a).q)
+        e_ref = O.matrix_errors(O.fgfrft_matrix(o, a, nthreads=8), O.exact_gfrft(eig_o, a))
+        for key in ("mse", "nmse"):
+            assert float(f"{e_gpu[key]:.3e}") == float(f"{e_ref[key]:.3e}"), (a, key, e_gpu[key], e_ref[key])
+
+
+@pytest.mark.skipif(not HEAVY, reason="FGFRFT_SKIP_HEAVY=1")
+def test_config4_packed_step_and_pair_shard_world1():
+    """Config 4 (N = 8192, L = 128, B = 1536) on one B200: the packed step at two orders, Y checked on
+    64 sampled signal columns against the recursive checker (repeated products with F), and the
+    full-batch loss / dL/da of the single-GPU packed step against the pair-sharded step (world 1:
+    a different build -- row / column panels -- and different kernels: two rectangle GEMMs)."""
+    import torch
+    from paper_2602_20870_b200 import pshard as ps
+    cfg = prep.config4()
+    n, b = cfg.x.shape
+    alphas = [0.37, 1.2]
+    cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=200 << 30)
+    try:
+        single = []
+        for a in alphas:
+            loss, dl, y = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
+            assert cache.route_info()[0] == 3
+            single.append((loss[0], dl[0]))
+            cols = np.random.default_rng(int(a * 100)).choice(b, size=64, replace=False)
+            yr = O.series_apply_recursive(cfg.f, a, cfg.l, np.asfortranarray(cfg.x[:, cols]))
+            assert rel(y[0][:, cols], yr) <= 1e-10
+    finally:
+        cache.close()
+    comm = ps.Comm(ps.Comm.unique_id(), 1, 0, 0)
+    sh = ps.PairShard(cfg.f, cfg.l, memory_budget=64 << 30, comm=comm)
+    try:
+        xd = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda()
+        xcd = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda()
+        lo, dl = sh.mse_step_dev(alphas, xd, xcd)
+        lo, dl = lo.cpu().numpy(), dl.cpu().numpy()
+        for i in range(2):
+            assert abs(lo[i] - single[i][0]) <= 1e-11 * single[i][0]
+            assert abs(dl[i] - single[i][1]) <= 1e-9 * max(abs(single[i][1]), 1e-3)
+    finally:
+        sh.close()
+        comm.close()
