@@ -308,6 +308,12 @@ int fgfrft_pshard_set_stream(fgfrft_cache* shard, void* stream);
  * [Y_g(a..); dY_g(a..)], 0 -> n_alpha blocks Y_g(a..), each n x b complex (stride 2 n b doubles). */
 int fgfrft_pshard_partial_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, int with_dq,
                               const void* x_dev, int64_t b, void* out_dev);
+/* The same partial products scattered by signal-column chunk straight from the GEMM epilogue (the
+ * data path of the fused reduce-scatter the MSE step runs over NVLink): dest[h] = this rank's
+ * receive slot in owner h's buffer, rows blocks of n x cb complex (cb = ceil(b / ndest), ndest <= 8);
+ * summing owner h's slots over the source ranks gives columns [h cb, (h+1) cb) of the result. */
+int fgfrft_pshard_partial_scatter_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, int with_dq,
+                                      const void* x_dev, int64_t b, void* const* dest, int ndest);
 /* MSE step (one or two orders) over the communicator; full X, Xc on every rank; loss and
  * dL/dalpha of every order on every rank. */
 int fgfrft_pshard_mse_step_dev(fgfrft_cache* shard, const double* alphas, int n_alpha, const void* x_dev,

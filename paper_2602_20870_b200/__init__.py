@@ -162,6 +162,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_pshard_mse_step_dev": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
         "fgfrft_pshard_mse_step": (i, [vp, vp, i, vp, vp, i64, vp, vp]),
         "fgfrft_pshard_apply_dev": (i, [vp, vp, i, i, vp, i64, vp]),
+        "fgfrft_pshard_partial_scatter_dev": (i, [vp, vp, i, i, vp, i64, vp, i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -196,7 +197,7 @@ def exported_symbols():
         "fgfrft_comm_destroy", "fgfrft_comm_info", "fgfrft_pshard_plan", "fgfrft_pshard_create",
         "fgfrft_pshard_create_local", "fgfrft_pshard_destroy", "fgfrft_pshard_info", "fgfrft_pshard_set_stream",
         "fgfrft_pshard_partial_dev", "fgfrft_pshard_mse_step_dev", "fgfrft_pshard_mse_step",
-        "fgfrft_pshard_apply_dev",
+        "fgfrft_pshard_apply_dev", "fgfrft_pshard_partial_scatter_dev",
     ]
 
 

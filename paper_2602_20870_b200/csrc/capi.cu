@@ -234,6 +234,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     for (cudaEvent_t e : c->pk_es) cudaEventDestroy(e);
     for (cudaEvent_t e : c->xh_ev) cudaEventDestroy(e);
+    for (void* p : c->rb_open) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t e : {c->pk_e0, c->pk_eg, c->pk_ex})
         if (e) cudaEventDestroy(e);
     if (c->pk_s) cudaStreamSynchronize(c->pk_s);
@@ -242,7 +243,7 @@ void destroy_cache(fgfrft_cache* c) {
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
                       &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
                       &c->by, &c->es, &c->ee, &c->erm, &c->nd_tab, &c->nd_p, &c->nd_d0, &c->nd_bsl, &c->nd_bex,
-                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ydy, &c->pp, &c->ppc})
+                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ydy, &c->pp, &c->ppc, &c->rb, &c->bar})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);

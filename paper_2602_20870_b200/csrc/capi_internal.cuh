@@ -174,6 +174,7 @@ cudaError_t launch_pack_pairs_from_panels(const double* rp, int64_t ld_r, const 
                                           int pbase, int npairs_local, int k, int l, void* packed, double* scales,
                                           cudaStream_t stream);
 size_t packed_bytes_pairs(int64_t npairs, int l);
+cudaError_t launch_sum_slots(const double* slots, int nslots, int64_t count, double* out, cudaStream_t stream);
 size_t packed_scale_elems(int n, int l);
 int64_t packed_pairs_before(int I, int nt);
 size_t mse_dy_part_elems();
@@ -365,6 +366,12 @@ struct fgfrft_cache {
     DevBuf pp, ppc;
     int64_t pp_b = -1;
     int pp_rows = -1;
+    // fused reduce-scatter: rb = this rank's receive slots [source rank][rows blocks][n x cb complex];
+    // rb_dest = every owner's slot for this rank (peers mapped through CUDA IPC), rb_open = mappings
+    DevBuf rb, bar;
+    std::vector<double*> rb_dest;
+    std::vector<void*> rb_open, rb_peer;
+    void* rb_for = nullptr;
     // Row-slab shard (fgfrft_shard_*): rows [r0, r1); slabs = row panels, colp = column panels.
     bool shard = false;
     int64_t graphs = 0;  // > 0: batch of small graphs (fgfrft_batch_*), n <= 64, complex64

@@ -29,6 +29,7 @@ struct NcclApi {
     decltype(&ncclAllReduce) all_reduce = nullptr;
     decltype(&ncclReduceScatter) reduce_scatter = nullptr;
     decltype(&ncclBroadcast) broadcast = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclGroupStart) group_start = nullptr;
     decltype(&ncclGroupEnd) group_end = nullptr;
     decltype(&ncclGetErrorString) error_string = nullptr;
@@ -50,12 +51,13 @@ const NcclApi* nccl_api() {
         FGB_SYM(all_reduce, "ncclAllReduce");
         FGB_SYM(reduce_scatter, "ncclReduceScatter");
         FGB_SYM(broadcast, "ncclBroadcast");
+        FGB_SYM(all_gather, "ncclAllGather");
         FGB_SYM(group_start, "ncclGroupStart");
         FGB_SYM(group_end, "ncclGroupEnd");
         FGB_SYM(error_string, "ncclGetErrorString");
 #undef FGB_SYM
         return api.get_unique_id && api.init_rank && api.init_all && api.destroy && api.all_reduce &&
-               api.reduce_scatter && api.broadcast && api.group_start && api.group_end && api.error_string;
+               api.reduce_scatter && api.broadcast && api.all_gather && api.group_start && api.group_end && api.error_string;
     }();
     return ok ? &api : nullptr;
 }
@@ -240,13 +242,17 @@ int pshard_create(const double* f, int64_t n, int l, uint64_t budget, int world,
 // This rank's partial products into c->pp: `rows` blocks (stride 2 n bpad doubles) of n x bpad
 // complex, bpad = world * ceil(b / world); only rows [32 I_g, N) and columns < b are ever written,
 // the rest stays zero.
-int pshard_partial(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b) {
+// dest != nullptr: the fused reduce-scatter -- the GEMM epilogue stores each output tile into the
+// receive slot (for this rank) of the rank owning its signal-column chunk (ndest owners, cb columns
+// each): dest[h] + block * 2 n cb + (row + (j - h cb) n) * 2. Otherwise into c->pp (see above).
+int pshard_partial(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
+                   double* const* dest = nullptr, int ndest = 0, int64_t cb = 0) {
     const int S = oz_slices_default();
     const int64_t n = c->n, mp = pad_rows(n), sl = n * n;
     const int64_t bpad = ceil_div(b, c->world) * c->world, blk = 2 * n * bpad;
     const int64_t r0 = (int64_t)c->I0 * kTile, r1 = std::min<int64_t>(n, (int64_t)c->I1 * kTile);
     const size_t pbytes = (size_t)rows * blk * sizeof(double);
-    if (c->pp.cap < pbytes || c->pp_b != b || c->pp_rows != rows) {
+    if (!dest && (c->pp.cap < pbytes || c->pp_b != b || c->pp_rows != rows)) {
         FGB_CUDA(c->pp.ensure(pbytes));
         FGB_CUDA(cudaMemsetAsync(c->pp.p, 0, pbytes, c->stream));
         c->pp_b = b;
@@ -301,6 +307,28 @@ int pshard_partial(fgfrft_cache* c, const double* coef, int coef_ld, int rows, c
         }
     }
     ProfScope ps(KC_I8GEMM, c->stream);
+    if (dest) {  // GEMM + reduce-scatter in one kernel: tiles go straight to their owners' slots
+        auto launch = [&](const int8_t* sa, const int* ea, int64_t rp, const int8_t* sx, const int* xe, int64_t kp,
+                          int64_t row0, int64_t rv) -> int {
+            OzOut o;
+            o.c = dest[0] + 2 * row0;
+            o.ldc = n;
+            o.sc = 2 * n * cb;
+            o.mv = (int)rv;
+            o.mp = (int)rp;
+            o.nv = (int)(2 * b);
+            o.scw = (int)cb;
+            o.ssc = 2 * n * cb;
+            o.sld = n;
+            for (int h = 0; h < ndest; ++h) o.dest[h] = dest[h] + 2 * row0;
+            FGB_LAUNCH(launch_ozgemm_ex(S, 1, sa, ea, (int)(rows * rp), sx, xe, (int)bp, (int)kp, o, c->stream), 1);
+            return FGFRFT_OK;
+        };
+        if (int st = launch(sA, exA, rpA, xA, xeA, kpA, r0, rvA)) return st;
+        if (rvB > 0)
+            if (int st = launch(sB, exB, rpB, xB, xeB, kpB, r1, rvB)) return st;
+        return FGFRFT_OK;
+    }
     double* pp = c->pp.as<double>();
     FGB_LAUNCH(launch_ozgemm(S, 1, sA, exA, (int)(rows * rpA), xA, xeA, (int)bp, (int)kpA, pp + 2 * r0, n, blk,
                              (int)rvA, (int)rpA, (int)(2 * b), c->stream),
@@ -309,6 +337,62 @@ int pshard_partial(fgfrft_cache* c, const double* coef, int coef_ld, int rows, c
         FGB_LAUNCH(launch_ozgemm(S, 1, sB, exB, (int)(rows * rpB), xB, xeB, (int)bp, (int)kpB, pp + 2 * r1, n, blk,
                                  (int)rvB, (int)rpB, (int)(2 * b), c->stream),
                    1);
+    return FGFRFT_OK;
+}
+
+// The receive slots of this rank (world x rows blocks x n x cb complex) and every owner's slot for
+// this rank: local for itself, CUDA IPC mappings of the peers' buffers (handles exchanged with one
+// ncclAllGather) for the others -- remapped only when the buffer changes.
+int pshard_map_slots(fgfrft_cache* c, int rows, int64_t cb) {
+    const int G = c->world;
+    const int64_t slot = (int64_t)rows * 2 * c->n * cb;  // doubles of one source rank's slot
+    const size_t need = (size_t)G * slot * sizeof(double);
+    if (c->rb.cap < need) {
+        for (void* p : c->rb_open) cudaIpcCloseMemHandle(p);
+        c->rb_open.clear();
+        c->rb_for = nullptr;
+        FGB_CUDA(c->rb.ensure(need));
+    }
+    c->rb_dest.assign(G, nullptr);
+    if (G == 1 || !c->comm) {
+        c->rb_dest[0] = c->rb.as<double>();
+        return FGFRFT_OK;
+    }
+    if (c->rb_for != c->rb.p) {
+        for (void* p : c->rb_open) cudaIpcCloseMemHandle(p);
+        c->rb_open.clear();
+        c->rb_peer.assign(G, nullptr);
+        cudaIpcMemHandle_t mine;
+        FGB_CUDA(cudaIpcGetMemHandle(&mine, c->rb.p));
+        DevBuf hb;
+        FGB_CUDA(hb.ensure((size_t)G * sizeof(mine)));
+        FGB_CUDA(cudaMemcpyAsync(hb.as<char>() + (size_t)c->rank * sizeof(mine), &mine, sizeof(mine),
+                                 cudaMemcpyHostToDevice, c->stream));
+        FGB_NCCL(nccl_api()->all_gather(hb.as<char>() + (size_t)c->rank * sizeof(mine), hb.p, sizeof(mine), ncclUint8,
+                                        c->comm->comm, c->stream));
+        std::vector<cudaIpcMemHandle_t> all(G);
+        FGB_CUDA(cudaMemcpyAsync(all.data(), hb.p, (size_t)G * sizeof(mine), cudaMemcpyDeviceToHost, c->stream));
+        FGB_CUDA(cudaStreamSynchronize(c->stream));
+        for (int h = 0; h < G; ++h) {
+            if (h == c->rank) {
+                c->rb_peer[h] = c->rb.p;
+                continue;
+            }
+            void* p = nullptr;
+            FGB_CUDA(cudaIpcOpenMemHandle(&p, all[h], cudaIpcMemLazyEnablePeerAccess));
+            c->rb_open.push_back(p);
+            c->rb_peer[h] = p;
+        }
+        c->rb_for = c->rb.p;
+    }
+    for (int h = 0; h < G; ++h) c->rb_dest[h] = static_cast<double*>(c->rb_peer[h]) + (int64_t)c->rank * slot;
+    return FGFRFT_OK;
+}
+
+// A stream-ordered barrier across the ranks: an all-reduce of one double.
+int pshard_barrier(fgfrft_cache* c) {
+    FGB_CUDA(c->bar.ensure(sizeof(double)));
+    FGB_NCCL(nccl_api()->all_reduce(c->bar.p, c->bar.p, 1, ncclFloat64, ncclSum, c->comm->comm, c->stream));
     return FGFRFT_OK;
 }
 
@@ -472,6 +556,29 @@ int fgfrft_pshard_partial_dev(fgfrft_cache* c, const double* alphas, int n_alpha
     FGB_GUARD_END
 }
 
+// This rank's partial products scattered by signal-column chunk straight from the GEMM epilogue:
+// dest[h] = this rank's receive slot in owner h's buffer (rows blocks x n x cb complex, cb =
+// ceil(b / ndest)); the fused reduce-scatter's data path without its barriers (tests, custom
+// transports). Sum over the source ranks of owner h's slots = columns [h cb, (h+1) cb) of the result.
+int fgfrft_pshard_partial_scatter_dev(fgfrft_cache* c, const double* alphas, int n_alpha, int with_dq,
+                                      const void* x_dev, int64_t b, void* const* dest, int ndest) {
+    FGB_GUARD_BEGIN
+    if (int st = check_pshard(c)) return st;
+    if (int st = check_alphas(alphas, n_alpha)) return st;
+    if (b < 1 || !x_dev || !dest || ndest < 1 || ndest > 8)
+        return fail(FGFRFT_PARAMETER, "pshard_partial_scatter: need X, b >= 1 and 1..8 destinations");
+    const int rows = with_dq ? 2 * n_alpha : n_alpha;
+    if (rows != 1 && rows != 2 && rows != 4) return fail(FGFRFT_PARAMETER, "pshard: 1 or 2 orders (4 without dQ)");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    double* coef = nullptr;
+    if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
+    std::vector<double*> d(ndest);
+    for (int h = 0; h < ndest; ++h) d[h] = static_cast<double*>(dest[h]);
+    return pshard_partial(c, coef, 2 * c->l + 1, rows, x_dev, b, d.data(), ndest, ceil_div(b, ndest));
+    FGB_GUARD_END
+}
+
 // The MSE step over the communicator: every rank passes the full X and Xc (device); loss and
 // dL/da of every order land on every rank (loss_dev, dlda_dev: n_alpha doubles each).
 int fgfrft_pshard_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev,
@@ -488,12 +595,35 @@ int fgfrft_pshard_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alph
     double* coef = nullptr;
     if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
     const int rows = 2 * n_alpha;
-    if (int st = pshard_partial(c, coef, 2 * c->l + 1, rows, x_dev, b)) return st;
     const int64_t n = c->n, bpad = ceil_div(b, c->world) * c->world, cb = bpad / c->world, blk = 2 * n * bpad;
     const int64_t chunk = 2 * n * cb;  // doubles of one rank's column chunk of one block
-    const double* yr = c->pp.as<double>();  // world 1: the whole (only) chunk
-    int64_t ystride = blk;
-    if (coll) {  // the reduce-scatter of [Y; dY] by signal-column chunks
+    static const bool nccl_rs = [] {
+        const char* e = std::getenv("FGFRFT_PSHARD_RS");
+        return e && !std::strcmp(e, "nccl");
+    }();
+    if (coll && !nccl_rs && c->world <= 8) {
+        // fused: the GEMM epilogue stores every tile into its owner's receive slot over NVLink; a
+        // barrier before (the owners are done with the previous step's slots) and after (every
+        // rank's tiles have landed), then the owner sums its slots in rank order
+        if (int st = pshard_map_slots(c, rows, cb)) return st;
+        if (int st = pshard_barrier(c)) return st;
+        if (int st = pshard_partial(c, coef, 2 * c->l + 1, rows, x_dev, b, c->rb_dest.data(), c->world, cb))
+            return st;
+        if (int st = pshard_barrier(c)) return st;
+        FGB_CUDA(c->ppc.ensure((size_t)rows * chunk * sizeof(double)));
+        {
+            ProfScope ps(KC_ELEMWISE, c->stream);
+            FGB_LAUNCH(launch_sum_slots(c->rb.as<double>(), c->world, (int64_t)rows * chunk, c->ppc.as<double>(),
+                                        c->stream),
+                       1);
+        }
+    } else if (int st = pshard_partial(c, coef, 2 * c->l + 1, rows, x_dev, b)) {
+        return st;
+    }
+    const bool fused = coll && !nccl_rs && c->world <= 8;
+    const double* yr = fused ? c->ppc.as<double>() : c->pp.as<double>();  // world 1: the whole (only) chunk
+    int64_t ystride = fused ? chunk : blk;
+    if (coll && !fused) {  // the NCCL reduce-scatter of [Y; dY] by signal-column chunks
         FGB_CUDA(c->ppc.ensure((size_t)rows * chunk * sizeof(double)));
         const NcclApi* api = nccl_api();
         FGB_NCCL(api->group_start());

@@ -71,6 +71,12 @@ struct OzOut {
     const double* dg = nullptr;
     int rn = 0, rnp = 0;
     int max_ctas = 0;  // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
+    // CM 1 fused reduce-scatter (pair shards): complex output column j goes to owner h = j / scw
+    // instead of c: dest[h] + bm * ssc + (i + (j - h scw) * sld) * 2 -- each owner's receive slot for
+    // this rank, local or a peer GPU's buffer mapped over NVLink (CUDA IPC). scw = 0: off.
+    double* dest[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int scw = 0;
+    int64_t ssc = 0, sld = 0;
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)

@@ -787,6 +787,10 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                             out.peers[q][o0] = v0;
                             if (n + 1 < out.nv) out.peers[q][o0 + out.ldc] = v1;
                         }
+                    } else if (out.scw > 0) {  // fused reduce-scatter: the owner's receive slot
+                        const int j = n >> 1, ho = j / out.scw;
+                        double* d = out.dest[ho] + (int64_t)bm * out.ssc + (i + (int64_t)(j - ho * out.scw) * out.sld) * 2;
+                        *reinterpret_cast<double2*>(d) = make_double2(v0, v1);
                     } else {
                         const int64_t o = (int64_t)bm * out.sc + (i + (int64_t)(n >> 1) * out.ldc) * 2;
                         __stcs(reinterpret_cast<double2*>(cb + (i + (int64_t)(n >> 1) * out.ldc) * 2), make_double2(v0, v1));
@@ -798,6 +802,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             }  // BN == kOzBN
         }
         if (chunk) flush_rmax(min((out.nv + 3) >> 2, out.nv - h * ((out.nv + 3) >> 2)));
+        if (CM == 1 && out.scw > 0) __threadfence_system();  // peer stores visible before the barrier
         if (CM == 2) {
             double* gp = out.part + (((int64_t)blockIdx.x * kOzEpiQ + h) * kOzBM + lrow) * 3;
             gp[0] = gacc[0];

@@ -417,6 +417,22 @@ cudaError_t launch_pack_pairs_from_panels(const double* rp, int64_t ld_r, const 
     return cudaGetLastError();
 }
 
+// The owner's side of the fused reduce-scatter: out[i] = sum_s slots[s][i] over the G receive
+// slots (one per source rank), in rank order (deterministic).
+__global__ void __launch_bounds__(256) sum_slots_kernel(const double* __restrict__ slots, int nslots, int64_t count,
+                                                        double* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < count; i += (int64_t)gridDim.x * 256) {
+        double v = slots[i];
+        for (int s = 1; s < nslots; ++s) v += slots[(int64_t)s * count + i];
+        out[i] = v;
+    }
+}
+
+cudaError_t launch_sum_slots(const double* slots, int nslots, int64_t count, double* out, cudaStream_t stream) {
+    sum_slots_kernel<<<4 * FGFRFT_SMS, 256, 0, stream>>>(slots, nslots, count, out);
+    return cudaGetLastError();
+}
+
 size_t packed_bytes_pairs(int64_t npairs, int l) { return (size_t)npairs * (size_t)l * 2 * kPkTileBytes; }
 
 // ---------------------------------------------------------------- MSE + dL/da from [Y; dY]

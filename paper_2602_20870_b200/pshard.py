@@ -151,6 +151,16 @@ class PairShard:
                                                out.data_ptr()))
         return out
 
+    def partial_scatter(self, alphas: Sequence[float], x_dev, dests, with_dq: bool = True) -> None:
+        """The fused reduce-scatter's data path: this rank's partial tiles stored by the GEMM epilogue
+        into dests[h] (device pointers: this rank's receive slot in owner h's buffer, rows blocks of
+        n x ceil(b / len(dests)) complex)."""
+        self._torch_stream()
+        al = np.ascontiguousarray(alphas, dtype=np.float64)
+        arr = (ctypes.c_void_p * len(dests))(*[ctypes.c_void_p(int(d)) for d in dests])
+        _check(lib().fgfrft_pshard_partial_scatter_dev(self._h, al.ctypes.data, len(al), int(with_dq),
+                                                       x_dev.data_ptr(), int(x_dev.shape[0]), arr, len(dests)))
+
     def mse_step_dev(self, alphas: Sequence[float], x_dev, xc_dev):
         """(loss, dL/da) device tensors, every rank (reduce-scatter + all-reduce inside)."""
         import torch

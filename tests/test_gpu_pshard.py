@@ -116,3 +116,31 @@ def test_pair_shard_errors(problem):
     with pytest.raises(fg.ParameterError):  # a local shard of a world > 1 has no communicator
         sh.mse_step_dev([0.5], xd, xd)
     sh.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_reduce_scatter_epilogue(problem, world):
+    """The fused reduce-scatter's data path, emulated on one GPU: every "rank" GEMM stores its tiles
+    into the receive slot it owns in each owner's buffer (here all local memory; on a node, peer
+    buffers mapped over NVLink); the owners' slot sums are the column chunks of the full products."""
+    import torch
+    f, l, x, xc, xd, xcd, o = problem
+    n, b = x.shape
+    cb = -(-b // world)
+    rows = 2  # [Y; dY] of one order
+    slot = rows * cb * n  # complex elements of one source rank's slot
+    rbs = [torch.zeros(world * slot, dtype=torch.complex128, device="cuda") for _ in range(world)]
+    for g in range(world):
+        sh = ps.PairShard(f, l, world=world, rank=g)
+        sh.partial_scatter([0.37], xd, [rb.data_ptr() + g * slot * 16 for rb in rbs])
+        sh.close()
+    torch.cuda.synchronize()
+    y = np.zeros((n, world * cb), dtype=complex)
+    dy = np.zeros_like(y)
+    for h in range(world):
+        tot = rbs[h].view(world, rows, cb, n).sum(dim=0).cpu().numpy()  # [rows][col][row]
+        y[:, h * cb:(h + 1) * cb] = tot[0].T
+        dy[:, h * cb:(h + 1) * cb] = tot[1].T
+    assert not np.any(y[:, b:]) and not np.any(dy[:, b:])  # padding columns never written
+    assert rel(y[:, :b], O.fgfrft_matrix(o, 0.37) @ x) <= 1e-10
+    assert rel(dy[:, :b], O.fgfrft_grad(o, 0.37) @ x) <= 1e-10

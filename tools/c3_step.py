@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="3")
     ap.add_argument("--c64", action="store_true")
+    ap.add_argument("--pshard", action="store_true", help="the pair-shard step at world 1 (NCCL communicator)")
     args = ap.parse_args()
     t0 = time.perf_counter()
     cfg = prep.config3() if args.config == "3" else prep.config4()
@@ -35,11 +36,18 @@ def main():
     ct = torch.complex64 if args.c64 else torch.complex128
     stream = torch.cuda.Stream()
     t0 = time.perf_counter()
-    cache = fg.PowerCache(cfg.f, L, memory_budget=200 << 30, dtype=dtype)
+    lib = fg.lib()
+    if args.pshard:
+        from paper_2602_20870_b200 import pshard as ps
+        comm = ps.Comm(ps.Comm.unique_id(), 1, 0, 0)
+        cache = ps.PairShard(cfg.f, L, memory_budget=120 << 30, comm=comm)
+        step_fn = lib.fgfrft_pshard_mse_step_dev
+    else:
+        cache = fg.PowerCache(cfg.f, L, memory_budget=200 << 30, dtype=dtype)
+        step_fn = None
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     cache.set_stream(stream.cuda_stream)
-    lib = fg.lib()
     al = [np.array([0.37]), np.array([0.63])]
     x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda().to(ct)
     xc = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda().to(ct)
@@ -47,6 +55,10 @@ def main():
     dl = torch.empty(1, dtype=torch.float64, device="cuda")
 
     def step(i):
+        if step_fn is not None:
+            fg._check(step_fn(cache.handle, al[i & 1].ctypes.data, 1, x.data_ptr(), xc.data_ptr(), b, loss.data_ptr(),
+                              dl.data_ptr()))
+            return
         fg._check(lib.fgfrft_mse_step_dev(cache.handle, al[i & 1].ctypes.data, 1, x.data_ptr(), xc.data_ptr(), b,
                                           None, loss.data_ptr(), dl.data_ptr()))
 
@@ -71,7 +83,7 @@ def main():
     torch.cuda.synchronize()
     prof = {k: [v[0] / args.steps, v[1] / args.steps] for k, v in fg.profile_read(reset=True).items() if v[1]}
     fg.profile_enable(False)
-    print(json.dumps({"config": "C" + args.config, "c64": args.c64, "n": n, "l": L, "b": b, "ms_per_step": ms,
+    print(json.dumps({"config": "C" + args.config, "c64": args.c64, "pshard": args.pshard, "n": n, "l": L, "b": b, "ms_per_step": ms,
                       "signal_nodes_per_s": n * b / (ms * 1e-3), "launches_per_step": launches,
                       "prep_s": prep_s, "build_s": build_s, "classes_ms_per_step": prof,
                       "loss": float(loss[0]), "dlda": float(dl[0])}), flush=True)
