@@ -116,6 +116,15 @@ def _dist():
 
 
 def cpu_model():
+    """The host CPU as lscpu names it (model, sockets x cores x threads, max MHz), /proc/cpuinfo otherwise."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {k.strip(): v.strip() for k, v in (ln.split(":", 1) for ln in out.splitlines() if ":" in ln)}
+        return (f"{kv.get('Model name', '?')}; {kv.get('Socket(s)', '?')} socket x {kv.get('Core(s) per socket', '?')} "
+                f"cores x {kv.get('Thread(s) per core', '?')} threads = {kv.get('CPU(s)', '?')} CPUs; "
+                f"max MHz {kv.get('CPU max MHz', 'n/a')}; flags avx512f={'avx512f' in kv.get('Flags', '')}")
+    except Exception:
+        pass
     try:
         for line in open("/proc/cpuinfo"):
             if line.startswith("model name"):

@@ -222,6 +222,145 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
         }
 }
 
+// Real-F forward with TWO CTAs per SM (one graph each), so one CTA's power stream overlaps the
+// other's FFMA-bound Y phase (the 1-CTA form serialised them: 0.64 ms at config 5). Region A is
+// 64 KB (a 4-slot ring of 16 KB real slabs, then Q_h of up to 4 heads), X is staged with a padded
+// row stride (68 float2: the two half-warps' X reads fall on different banks), and the Y phase runs
+// two heads at a time (32 accumulators per thread, so 512 threads fit 64 registers).
+constexpr int kBfStages = 4;
+constexpr int kBfXs = 68;
+constexpr size_t kBfA = (size_t)kBfStages * kBSlab * 4;  // 64 KB
+constexpr size_t kBfX = (size_t)kBMaxCh * kBfXs * 8;     // 34.8 KB
+
+size_t batch_forward_real_smem_bytes(int l, int heads) {
+    return kBfA + kBfX + (kBfStages + 1) * 8 + (size_t)heads * (2 * l + 1) * 4 + 64;
+}
+
+template <int H>
+__global__ void __launch_bounds__(kBTh, 2)
+batch_forward_real_kernel(const float* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
+                          const float2* __restrict__ x, int ch, float2* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* regA = reinterpret_cast<float*>(smem);
+    float2* xs = reinterpret_cast<float2*>(smem + kBfA);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBfA + kBfX);
+    uint64_t* xbar = full + kBfStages;
+    float* cs = reinterpret_cast<float*>(xbar + 1);  // [h][w]
+    const int g = blockIdx.x, tid = threadIdx.x;
+    const int w = 2 * l + 1;
+    const float* gs = slabs + (int64_t)g * l * kBSlab;
+    constexpr uint32_t bytes = kBSlab * sizeof(float);
+    auto issue = [&](int k, int s) {
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
+    };
+    const bool xbulk = n == kBN && ch == kBMaxCh && ((uintptr_t)x & 15) == 0;
+    if (tid == 0) {
+        for (int s = 0; s < kBfStages; ++s) mbar_init(&full[s], 1);
+        mbar_init(xbar, 1);
+        fence_mbar_init();
+        for (int s = 0; s < kBfStages && s < l; ++s) issue(s + 1, s);
+        if (xbulk) {  // 64 column copies into the padded layout, overlapping the power pass
+            mbar_arrive_expect_tx(xbar, kBN * kBMaxCh * sizeof(float2));
+            for (int c = 0; c < kBMaxCh; ++c)
+                bulk_g2s(xs + c * kBfXs, x + ((int64_t)g * ch + c) * n, kBN * sizeof(float2), xbar);
+        }
+    }
+    for (int idx = tid; idx < H * w; idx += kBTh) {
+        const int h = idx / w, t = idx - h * w;
+        cs[idx] = (float)coef[(size_t)(g * H + h) * 2 * w + t];
+    }
+    if (!xbulk)
+        for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
+            const int j = idx & 63, c = idx >> 6;
+            xs[c * kBfXs + j] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
+        }
+    __syncthreads();
+    const int i = tid & 63, j0 = tid >> 6;
+    float q[8][H];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int h = 0; h < H; ++h) q[u][h] = (i == j0 + 8 * u) ? cs[h * w + l] : 0.f;
+    for (int k = 1; k <= l; ++k) {
+        const int s = (k - 1) % kBfStages;
+        mbar_wait(&full[s], ((k - 1) / kBfStages) & 1);
+        const float* t = regA + (size_t)s * kBSlab;
+        float a[H], b[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            a[h] = cs[h * w + l + k];
+            b[h] = cs[h * w + l - k];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = j0 + 8 * u;
+            const float p = t[bidx(i, j)], pt = t[bidx(j, i)];
+#pragma unroll
+            for (int h = 0; h < H; ++h) q[u][h] = fmaf(a[h], p, fmaf(b[h], pt, q[u][h]));
+        }
+        __syncthreads();
+        if (tid == 0 && k + kBfStages <= l) issue(k + kBfStages, s);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int h = 0; h < H; ++h) regA[(size_t)h * kBN * kBN + (j0 + 8 * u) * kBN + i] = q[u][h];
+    if (xbulk) mbar_wait(xbar, 0);
+    __syncthreads();
+    // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: rows 2ib, 2ib+1, 32+2ib, 33+2ib, columns 2cb, 2cb+1
+    const int ib = tid & 15, cb = tid >> 4;
+#pragma unroll
+    for (int h0 = 0; h0 < H; h0 += 2) {
+        constexpr int HP = 2;
+        float acc[HP][4][2][2];
+#pragma unroll
+        for (int hh = 0; hh < HP; ++hh)
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) acc[hh][r][c][0] = acc[hh][r][c][1] = 0.f;
+#pragma unroll 2
+        for (int j = 0; j < kBN; ++j) {
+            const float2 x0 = xs[(2 * cb) * kBfXs + j], x1 = xs[(2 * cb + 1) * kBfXs + j];
+#pragma unroll
+            for (int hh = 0; hh < HP; ++hh) {
+                if (h0 + hh >= H) break;
+                const float2* qp = reinterpret_cast<const float2*>(regA + (size_t)(h0 + hh) * kBN * kBN + j * kBN + 2 * ib);
+                const float2 v0 = qp[0], v1 = qp[16];
+                const float qv[4] = {v0.x, v0.y, v1.x, v1.y};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    acc[hh][r][0][0] = fmaf(qv[r], x0.x, acc[hh][r][0][0]);
+                    acc[hh][r][0][1] = fmaf(qv[r], x0.y, acc[hh][r][0][1]);
+                    acc[hh][r][1][0] = fmaf(qv[r], x1.x, acc[hh][r][1][0]);
+                    acc[hh][r][1][1] = fmaf(qv[r], x1.y, acc[hh][r][1][1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int hh = 0; hh < HP; ++hh) {
+            const int h = h0 + hh;
+            if (h >= H) break;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int col = 2 * cb + c;
+                if (col >= ch) continue;
+                float2* yo = y + (((int64_t)g * H + h) * ch + col) * n;
+#pragma unroll
+                for (int r = 0; r < 4; r += 2) {  // rows 2ib, 2ib+1 (+32): one 16-byte store
+                    const int row = 2 * ib + 32 * (r >> 1);
+                    if (row + 1 < n)
+                        *reinterpret_cast<float4*>(yo + row) =
+                            make_float4(acc[hh][r][c][0], acc[hh][r][c][1], acc[hh][r + 1][c][0], acc[hh][r + 1][c][1]);
+                    else if (row < n)
+                        yo[row] = make_float2(acc[hh][r][c][0], acc[hh][r][c][1]);
+                }
+            }
+        }
+    }
+}
+
 template <int H, bool R>
 __global__ void __launch_bounds__(kBTh, 1)
 batch_dlda_kernel(const void* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
@@ -414,6 +553,24 @@ cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int
 
 cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
                                  const void* x, int ch, void* y, bool real, cudaStream_t stream) {
+    if (real && ((uintptr_t)y & 15) == 0 && n % 2 == 0) {  // two CTAs per SM (batch_forward_real_kernel)
+        const size_t sm = batch_forward_real_smem_bytes(l, heads);
+#define FGB_BFR(HV)                                                                                            \
+    {                                                                                                          \
+        static PerDeviceOnce attr;                                                                             \
+        cudaError_t e = attr.run([] {                                                                          \
+            return cudaFuncSetAttribute(batch_forward_real_kernel<HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        110 * 1024);                                                           \
+        });                                                                                                    \
+        if (e != cudaSuccess) return e;                                                                        \
+        batch_forward_real_kernel<HV><<<graphs, kBTh, sm, stream>>>((const float*)slabs, n, l, coef,            \
+                                                                    (const float2*)x, ch, (float2*)y);         \
+    }
+        if (sm > 110 * 1024) return cudaErrorInvalidValue;
+        FGB_BATCH_HEADS(FGB_BFR)
+#undef FGB_BFR
+        return cudaGetLastError();
+    }
     const size_t smem = batch_smem_bytes(l);
 #define FGB_BF(HV)                                                                                             \
     {                                                                                                          \
