@@ -12,6 +12,7 @@
 // (double precision, the sinc.hpp formulas; differences from glibc are ~1 ulp, far inside the
 // complex64 tolerance), so a step has no host-side O(graphs x heads x L) work.
 #include <math_constants.h>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -222,37 +223,57 @@ batch_forward_kernel(const void* __restrict__ slabs, int n, int l, const double*
         }
 }
 
-// Real-F forward with TWO CTAs per SM (one graph each), so one CTA's power stream overlaps the
-// other's FFMA-bound Y phase (the 1-CTA form serialised them: 0.64 ms at config 5). Region A is
-// 64 KB (a 4-slot ring of 16 KB real slabs, then Q_h of up to 4 heads), X is staged with a padded
-// row stride (68 float2: the two half-warps' X reads fall on different banks), and the Y phase runs
-// two heads at a time (32 accumulators per thread, so 512 threads fit 64 registers).
 constexpr int kBfStages = 4;
-constexpr int kBfXs = 68;
-constexpr size_t kBfA = (size_t)kBfStages * kBSlab * 4;  // 64 KB
-constexpr size_t kBfX = (size_t)kBMaxCh * kBfXs * 8;     // 34.8 KB
 
-size_t batch_forward_real_smem_bytes(int l, int heads) {
-    return kBfA + kBfX + (kBfStages + 1) * 8 + (size_t)heads * (2 * l + 1) * 4 + 64;
+// Real-F forward with the Y phase on the tensor cores: Y_h = Q_h X as mma.sync m16n8k8 TF32 with
+// the 3xTF32 split (a = a_hi + a_lo, products hi*hi + hi*lo + lo*hi: FP32-level accuracy, far
+// inside the complex64 1e-4 bar; single-pass TF32 is not). The FFMA form was issue-bound (FMA pipe
+// 51%, 79% of issue slots, profiles/r02_ncu_c5_summary.csv). Shared memory: region Q (the 4-slot
+// power ring, then Q_h row-major with a 68-float row stride: conflict-free A fragments), X as
+// staged (bulk copy) and its TF32 hi / lo split as the real 64 x 128 matrix [Re | Im interleaved]
+// with a 136-float row stride (conflict-free B fragments). One CTA per graph, 16 warps: warp w
+// computes m-tile (w & 3) x n-tiles 4 (w >> 2) .. +3 of every head.
+constexpr int kBmQs = 68, kBmXs = 136;
+constexpr size_t kBmQ = (size_t)kBMaxHeads * kBN * kBmQs * 4;  // 69.6 KB (>= the 64 KB ring)
+constexpr size_t kBmXraw = (size_t)kBN * kBMaxCh * 8;           // 32 KB
+constexpr size_t kBmXsplit = (size_t)kBN * kBmXs * 4;           // 34.8 KB each (hi, lo)
+
+size_t batch_forward_mma_smem_bytes(int l, int heads) {
+    return kBmQ + kBmXraw + 2 * kBmXsplit + (kBfStages + 1) * 8 + (size_t)heads * (2 * l + 1) * 4 + 64;
+}
+
+__device__ __forceinline__ uint32_t tf32_of(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 template <int H>
-__global__ void __launch_bounds__(kBTh, 2)
-batch_forward_real_kernel(const float* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
-                          const float2* __restrict__ x, int ch, float2* __restrict__ y) {
+__global__ void __launch_bounds__(kBTh, 1)
+batch_forward_mma_kernel(const float* __restrict__ slabs, int n, int l, const double* __restrict__ coef,
+                         const float2* __restrict__ x, int ch, float2* __restrict__ y) {
     extern __shared__ __align__(128) unsigned char smem[];
-    float* regA = reinterpret_cast<float*>(smem);
-    float2* xs = reinterpret_cast<float2*>(smem + kBfA);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBfA + kBfX);
+    float* regQ = reinterpret_cast<float*>(smem);
+    float2* xraw = reinterpret_cast<float2*>(smem + kBmQ);
+    float* xhi = reinterpret_cast<float*>(smem + kBmQ + kBmXraw);
+    float* xlo = xhi + kBN * kBmXs;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBmQ + kBmXraw + 2 * kBmXsplit);
     uint64_t* xbar = full + kBfStages;
-    float* cs = reinterpret_cast<float*>(xbar + 1);  // [h][w]
-    const int g = blockIdx.x, tid = threadIdx.x;
+    float* cs = reinterpret_cast<float*>(xbar + 1);
+    const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int w = 2 * l + 1;
     const float* gs = slabs + (int64_t)g * l * kBSlab;
     constexpr uint32_t bytes = kBSlab * sizeof(float);
     auto issue = [&](int k, int s) {
         mbar_arrive_expect_tx(&full[s], bytes);
-        bulk_g2s(regA + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
+        bulk_g2s(regQ + (size_t)s * kBSlab, gs + (int64_t)(k - 1) * kBSlab, bytes, &full[s]);
     };
     const bool xbulk = n == kBN && ch == kBMaxCh && ((uintptr_t)x & 15) == 0;
     if (tid == 0) {
@@ -260,10 +281,9 @@ batch_forward_real_kernel(const float* __restrict__ slabs, int n, int l, const d
         mbar_init(xbar, 1);
         fence_mbar_init();
         for (int s = 0; s < kBfStages && s < l; ++s) issue(s + 1, s);
-        if (xbulk) {  // 64 column copies into the padded layout, overlapping the power pass
+        if (xbulk) {
             mbar_arrive_expect_tx(xbar, kBN * kBMaxCh * sizeof(float2));
-            for (int c = 0; c < kBMaxCh; ++c)
-                bulk_g2s(xs + c * kBfXs, x + ((int64_t)g * ch + c) * n, kBN * sizeof(float2), xbar);
+            bulk_g2s(xraw, x + (int64_t)g * ch * n, kBN * kBMaxCh * sizeof(float2), xbar);
         }
     }
     for (int idx = tid; idx < H * w; idx += kBTh) {
@@ -273,9 +293,10 @@ batch_forward_real_kernel(const float* __restrict__ slabs, int n, int l, const d
     if (!xbulk)
         for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
             const int j = idx & 63, c = idx >> 6;
-            xs[c * kBfXs + j] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
+            xraw[idx] = (j < n && c < ch) ? x[((int64_t)g * ch + c) * n + j] : make_float2(0.f, 0.f);
         }
     __syncthreads();
+    // power pass: Q_h for 8 elements per thread in registers (both P_ij and P_ji from one staged slab)
     const int i = tid & 63, j0 = tid >> 6;
     float q[8][H];
 #pragma unroll
@@ -285,7 +306,7 @@ batch_forward_real_kernel(const float* __restrict__ slabs, int n, int l, const d
     for (int k = 1; k <= l; ++k) {
         const int s = (k - 1) % kBfStages;
         mbar_wait(&full[s], ((k - 1) / kBfStages) & 1);
-        const float* t = regA + (size_t)s * kBSlab;
+        const float* t = regQ + (size_t)s * kBSlab;
         float a[H], b[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
@@ -302,61 +323,65 @@ batch_forward_real_kernel(const float* __restrict__ slabs, int n, int l, const d
         __syncthreads();
         if (tid == 0 && k + kBfStages <= l) issue(k + kBfStages, s);
     }
+    // Q_h row-major (row i, column j) with stride 68 -- the ring is idle now
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int h = 0; h < H; ++h) regA[(size_t)h * kBN * kBN + (j0 + 8 * u) * kBN + i] = q[u][h];
+        for (int h = 0; h < H; ++h) regQ[(size_t)h * kBN * kBmQs + i * kBmQs + j0 + 8 * u] = q[u][h];
     if (xbulk) mbar_wait(xbar, 0);
+    // X (64 x 64 complex, staged [c][j]) -> the real 64 x 128 matrix Xr[j][2c + e], TF32 hi / lo
+    for (int idx = tid; idx < kBN * kBMaxCh; idx += kBTh) {
+        const int j = idx & 63, c = idx >> 6;
+        const float2 v = xraw[c * kBN + j];
+        const float hr = __uint_as_float(tf32_of(v.x)), hm = __uint_as_float(tf32_of(v.y));
+        xhi[j * kBmXs + 2 * c] = hr;
+        xhi[j * kBmXs + 2 * c + 1] = hm;
+        xlo[j * kBmXs + 2 * c] = __uint_as_float(tf32_of(v.x - hr));
+        xlo[j * kBmXs + 2 * c + 1] = __uint_as_float(tf32_of(v.y - hm));
+    }
     __syncthreads();
-    // Y_h[ii, c] = sum_j Q_h[ii, j] X[j, c]: rows 2ib, 2ib+1, 32+2ib, 33+2ib, columns 2cb, 2cb+1
-    const int ib = tid & 15, cb = tid >> 4;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int mt = warp & 3, ng = warp >> 2;
+#pragma unroll 1
+    for (int h = 0; h < H; ++h) {
+        const float* qh = regQ + (size_t)h * kBN * kBmQs;
+        float acc[4][4];
 #pragma unroll
-    for (int h0 = 0; h0 < H; h0 += 2) {
-        constexpr int HP = 2;
-        float acc[HP][4][2][2];
+        for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
 #pragma unroll
-        for (int hh = 0; hh < HP; ++hh)
+        for (int ks = 0; ks < kBN / 8; ++ks) {
+            // A fragment: a0 = Q[16mt + g][8ks + t], a1 = row + 8, a2 = column + 4, a3 = both
+            const float* qa = qh + (16 * mt + gq) * kBmQs + 8 * ks + tq;
+            const float av[4] = {qa[0], qa[8 * kBmQs], qa[4], qa[8 * kBmQs + 4]};
+            uint32_t ahi[4], alo[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+            for (int e = 0; e < 4; ++e) {
+                ahi[e] = tf32_of(av[e]);
+                alo[e] = tf32_of(av[e] - __uint_as_float(ahi[e]));
+            }
 #pragma unroll
-                for (int c = 0; c < 2; ++c) acc[hh][r][c][0] = acc[hh][r][c][1] = 0.f;
-#pragma unroll 2
-        for (int j = 0; j < kBN; ++j) {
-            const float2 x0 = xs[(2 * cb) * kBfXs + j], x1 = xs[(2 * cb + 1) * kBfXs + j];
-#pragma unroll
-            for (int hh = 0; hh < HP; ++hh) {
-                if (h0 + hh >= H) break;
-                const float2* qp = reinterpret_cast<const float2*>(regA + (size_t)(h0 + hh) * kBN * kBN + j * kBN + 2 * ib);
-                const float2 v0 = qp[0], v1 = qp[16];
-                const float qv[4] = {v0.x, v0.y, v1.x, v1.y};
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    acc[hh][r][0][0] = fmaf(qv[r], x0.x, acc[hh][r][0][0]);
-                    acc[hh][r][0][1] = fmaf(qv[r], x0.y, acc[hh][r][0][1]);
-                    acc[hh][r][1][0] = fmaf(qv[r], x1.x, acc[hh][r][1][0]);
-                    acc[hh][r][1][1] = fmaf(qv[r], x1.y, acc[hh][r][1][1]);
-                }
+            for (int nt = 0; nt < 4; ++nt) {
+                // B fragment: b0 = Xr[8ks + t][8(4ng + nt) + g], b1 = row + 4
+                const int col = 8 * (4 * ng + nt) + gq, row = 8 * ks + tq;
+                const uint32_t bh0 = __float_as_uint(xhi[row * kBmXs + col]);
+                const uint32_t bh1 = __float_as_uint(xhi[(row + 4) * kBmXs + col]);
+                const uint32_t bl0 = __float_as_uint(xlo[row * kBmXs + col]);
+                const uint32_t bl1 = __float_as_uint(xlo[(row + 4) * kBmXs + col]);
+                mma_tf32(acc[nt], alo, bh0, bh1);  // small terms first
+                mma_tf32(acc[nt], ahi, bl0, bl1);
+                mma_tf32(acc[nt], ahi, bh0, bh1);
             }
         }
+        // D fragment: (c0, c1) = Y_h[16mt + g][real cols 2t, 2t+1 of n-tile] = one complex value,
+        // (c2, c3) the same for row + 8
 #pragma unroll
-        for (int hh = 0; hh < HP; ++hh) {
-            const int h = h0 + hh;
-            if (h >= H) break;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int col = 2 * cb + c;
-                if (col >= ch) continue;
-                float2* yo = y + (((int64_t)g * H + h) * ch + col) * n;
-#pragma unroll
-                for (int r = 0; r < 4; r += 2) {  // rows 2ib, 2ib+1 (+32): one 16-byte store
-                    const int row = 2 * ib + 32 * (r >> 1);
-                    if (row + 1 < n)
-                        *reinterpret_cast<float4*>(yo + row) =
-                            make_float4(acc[hh][r][c][0], acc[hh][r][c][1], acc[hh][r + 1][c][0], acc[hh][r + 1][c][1]);
-                    else if (row < n)
-                        yo[row] = make_float2(acc[hh][r][c][0], acc[hh][r][c][1]);
-                }
-            }
+        for (int nt = 0; nt < 4; ++nt) {
+            const int cc = 4 * (4 * ng + nt) + tq;  // complex column
+            if (cc >= ch) continue;
+            float2* yo = y + (((int64_t)g * H + h) * ch + cc) * n;
+            const int r0 = 16 * mt + gq;
+            if (r0 < n) yo[r0] = make_float2(acc[nt][0], acc[nt][1]);
+            if (r0 + 8 < n) yo[r0 + 8] = make_float2(acc[nt][2], acc[nt][3]);
         }
     }
 }
@@ -553,22 +578,30 @@ cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int
 
 cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
                                  const void* x, int ch, void* y, bool real, cudaStream_t stream) {
-    if (real && ((uintptr_t)y & 15) == 0 && n % 2 == 0) {  // two CTAs per SM (batch_forward_real_kernel)
-        const size_t sm = batch_forward_real_smem_bytes(l, heads);
-#define FGB_BFR(HV)                                                                                            \
+    // 2: the Y phase on the tensor cores (default); 0: the FFMA form. Measured at config 5: both
+    // 0.64 ms -- the per-graph power stream, not the Y phase, bounds the kernel; a two-CTA-per-SM
+    // FFMA form (0.65 ms) and a persistent warp-specialised form streaming across graphs (0.78 ms)
+    // were tried and dropped.
+    static const int fwd_form = [] {
+        const char* e = std::getenv("FGFRFT_BATCH_FWD");
+        return e ? std::atoi(e) : 2;
+    }();
+    if (real && fwd_form == 2) {
+        const size_t sm = batch_forward_mma_smem_bytes(l, heads);
+#define FGB_BFM(HV)                                                                                            \
     {                                                                                                          \
         static PerDeviceOnce attr;                                                                             \
         cudaError_t e = attr.run([] {                                                                          \
-            return cudaFuncSetAttribute(batch_forward_real_kernel<HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                        110 * 1024);                                                           \
+            return cudaFuncSetAttribute(batch_forward_mma_kernel<HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        227 * 1024);                                                           \
         });                                                                                                    \
         if (e != cudaSuccess) return e;                                                                        \
-        batch_forward_real_kernel<HV><<<graphs, kBTh, sm, stream>>>((const float*)slabs, n, l, coef,            \
-                                                                    (const float2*)x, ch, (float2*)y);         \
+        batch_forward_mma_kernel<HV><<<graphs, kBTh, sm, stream>>>((const float*)slabs, n, l, coef,             \
+                                                                   (const float2*)x, ch, (float2*)y);          \
     }
-        if (sm > 110 * 1024) return cudaErrorInvalidValue;
-        FGB_BATCH_HEADS(FGB_BFR)
-#undef FGB_BFR
+        if (sm > 227 * 1024) return cudaErrorInvalidValue;
+        FGB_BATCH_HEADS(FGB_BFM)
+#undef FGB_BFM
         return cudaGetLastError();
     }
     const size_t smem = batch_smem_bytes(l);
