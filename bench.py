@@ -134,7 +134,7 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
-def ncu_summary(name_regex: str, files=("r02_ncu_c3_summary.csv",)):
+def ncu_summary(name_regex: str, files=("r02_ncu_c3_summary.csv", "r02_ncu_c3_gemm_summary.csv")):
     """The committed ncu --set full summary row (profiles/<file>) of the kernel whose name matches
     `name_regex`: {"traffic": dram read + write bytes per launch, "duration_us", "file"} or None."""
     rx = re.compile(name_regex)
@@ -271,7 +271,7 @@ def c2_sweep(fg, torch, stream, dev):
     cache.close()
     return {"workload": "BASELINE config 2: N=1024 k-NN graph, L=64, B=256, 64 orders on [0,2] per step "
                         "(orders change every step)", "ms_per_step": ms, "value": n * b * A / (ms * 1e-3),
-            "unit": UNIT, "route": {0: "synthesis", 1: "power products", 2: "node interpolation"}[route],
+            "unit": UNIT, "route": {0: "synthesis", 1: "power products", 2: "node interpolation"}.get(route, str(route)),
             "nodes": nodes}
 
 
@@ -514,15 +514,19 @@ def main():
     #   (`fp64_equivalent_*`: the bytes the exact FP64 cache would move for the same launch).
     # int8_gemm (tensor): [Y; dY] = [Q; dQ] X, 2 * (2N) * (2B) * N FP64-equivalent flops per step
     #   (real F x complex X), S(S+1)/2 int8 digit GEMMs of that size (Ozaki, S base-254 digits).
-    S = int(L_.fgfrft_int8_digits())
+    route, _nodes = cache.route_info()
+    S = int(L_.fgfrft_step_int8_digits() if route in (3, 4) else L_.fgfrft_int8_digits())
     products = S * (S + 1) // 2
     e = 8 if real else 16
-    route, _nodes = cache.route_info()
     nt = -(-n // 32)
     npairs = nt * (nt + 1) // 2
     packed_bytes = npairs * L * 2 * 32 * 32 * 5 + npairs * L * 2 * 8
+    # route 4: the digit cache -- npairs * 1024 element-pair rows x 2 pad64(L) powers x 5 digits,
+    # + one int32 exponent per row
+    dk_rows, dk_kp = npairs * 1024, 2 * (-(-L // 64) * 64)
+    digit_bytes = dk_rows * dk_kp * 5 + dk_rows * 4
     fp64_bytes = (L * e + 2 * e) * n * n
-    syn_bytes = (packed_bytes + 2 * 8 * n * n) if route == 3 else fp64_bytes
+    syn_bytes = {3: packed_bytes + 2 * 8 * n * n, 4: digit_bytes + 2 * 8 * n * n}.get(route, fp64_bytes)
     dom = max(classes, key=lambda k: classes[k]["ms_per_step"])
     syn = classes.get("synthesis")
     roof = None
@@ -530,19 +534,24 @@ def main():
         per_launch_ms = syn["ms_per_step"] / syn["launches_per_step"]
         ach = syn_bytes / syn["launches_per_step"] / (per_launch_ms * 1e-3) / 1e9
         fp64_ach = fp64_bytes / syn["launches_per_step"] / (per_launch_ms * 1e-3) / 1e9
-        nc = ncu_summary(r"psynth" if route == 3 else r"rsynth_pairs")
+        nc = ncu_summary({3: r"psynth", 4: r"dsynth_kernel"}.get(route, r"rsynth_pairs"))
         roof = {"bound": "hbm",
-                "kernel": ("psynth_pairs_kernel<2> (packed slabs -> Q and dQ/da, one pass, TMA ring)" if route == 3
-                           else "rsynth_pairs_kernel (FP64 slabs -> Q and dQ/da)"),
+                "kernel": {3: "psynth_pairs_kernel<2> (packed slabs -> Q and dQ/da, one pass, TMA ring)",
+                           4: ("dsynth_kernel<2,4> (digit cache -> Q and dQ/da on the INT8 tensor cores: TMA ring, "
+                               "2 MMA-issuing warps, TMEM accumulators, mirror pairs per row)")}.get(
+                               route, "rsynth_pairs_kernel (FP64 slabs -> Q and dQ/da)"),
                 "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
                 "traffic": nc["traffic"] if nc else None,
                 "traffic_source": (f"{nc['file']}: dram__bytes_read.sum + dram__bytes_write.sum of "
                                    f"'{nc['kernel'][:60]}' (ncu --set full, one launch)") if nc else None,
                 "algorithmic_bytes_per_launch": syn_bytes / syn["launches_per_step"],
-                "algorithmic": (f"packed slabs {packed_bytes:.4g} B (npairs*L*2 tiles*5 KB + scales; 5 B per element, "
-                                f"diagonal tiles twice) read + Q, dQ 2*N^2*8 B written = {syn_bytes:.4g} B"
-                                if route == 3 else
-                                f"SURVEY 8(d): (S*e + A*e)*N^2, S = L = {L}, e = {e}, A = 2 = {syn_bytes:.4g} B"),
+                "algorithmic": {3: (f"packed slabs {packed_bytes:.4g} B (npairs*L*2 tiles*5 KB + scales; 5 B per "
+                                    f"element, diagonal tiles twice) read + Q, dQ 2*N^2*8 B written = {syn_bytes:.4g} B"),
+                                4: (f"digit cache {digit_bytes:.4g} B (npairs*1024 element-pair rows x {dk_kp} powers "
+                                    f"(P_k(e) | P_k(e')) x 5 digits + 4 B exponent per row; 5 B per element and "
+                                    f"power, diagonal tiles twice) read + Q, dQ 2*N^2*8 B written = {syn_bytes:.4g} B")
+                                }.get(route, f"SURVEY 8(d): (S*e + A*e)*N^2, S = L = {L}, e = {e}, A = 2 = "
+                                             f"{syn_bytes:.4g} B"),
                 "fp64_equivalent_bytes": fp64_bytes,
                 "fp64_equivalent_gbs": fp64_ach, "fp64_equivalent_frac": fp64_ach / peaks["hbm_gbs"],
                 "fp64_equivalent_note": ("SURVEY 8(d) bytes of the exact FP64 cache, (S*e + A*e)*N^2 with S = L, "
@@ -554,7 +563,7 @@ def main():
     if i8:
         fp = 2.0 * 2 * n * (2 * b) * n  # [Q; dQ] (2N rows, real) x X (2B real columns), K = N
         tops = fp * products / (i8["ms_per_step"] * 1e-3) / 1e12
-        nc = ncu_summary(r"ozgemm_kernel<6")
+        nc = ncu_summary(rf"ozgemm_kernel<{S}")
         gemm = {"bound": "tensor", "kernel": f"ozgemm_kernel<{S},1,2> (tcgen05.mma kind::i8, TMEM accumulators)",
                 "achieved": tops, "peak": peaks["int8_tops"], "unit": "TOPS", "frac": tops / peaks["int8_tops"],
                 "fp64_equivalent_tflops": fp / (i8["ms_per_step"] * 1e-3) / 1e12,
@@ -568,7 +577,9 @@ def main():
         roof["other_kernel"] = gemm
         roof["dominant_class"] = dom
     route_desc = {"route": {0: "synthesis (exact FP64 slabs)", 1: "power products", 2: "node interpolation",
-                            3: "packed: Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X"}.get(route),
+                            3: "packed: Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X",
+                            4: ("packed step, tensor-core synthesis: Q, dQ/da from the digit cache on tcgen05 (kind::i8) "
+                                "+ one Ozaki GEMM [Y; dY] = [Q; dQ] X")}.get(route),
                   "int8_digits": S}
 
     # ---- parity of the timed step against the oracle (rank 0; the oracle cache is reused by the CPU

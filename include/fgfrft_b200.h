@@ -98,6 +98,9 @@ uint64_t fgfrft_launch_count(void);
  */
 int fgfrft_profile_enable(int on);
 int fgfrft_profile_read(double* ms, int64_t* counts, int reset);
+/* The recorded launches in order (before a reset): class, start and end in ms relative to the first
+ * record's start (CUDA events on the launching streams); up to cap records, *count = recorded. */
+int fgfrft_profile_trace(int* cls, double* t0, double* t1, int cap, int* count);
 
 /* sinc.hpp:50-63. c, dc: 2l+1 doubles each (either may be NULL). l < 1 -> PARAMETER. */
 int fgfrft_sinc_coeffs(double alpha, int l, double* c, double* dc);
@@ -132,8 +135,10 @@ int fgfrft_cache_info(const fgfrft_cache* cache, int64_t* n, int* l, uint64_t* f
  * Set FGFRFT_NO_REAL=1 in the environment to force the complex kernels. */
 int fgfrft_cache_is_real(const fgfrft_cache* cache, int* real);
 /* Route taken by the last fgfrft_mse_step* on this handle: 0 synthesis (one GEMM pair per order),
- * 1 power products (2L products F^k X), 2 node interpolation (nodes = its r node operators); -1
- * before the first step. For benchmarks and diagnostics. */
+ * 1 power products (2L products F^k X), 2 node interpolation (nodes = its r node operators),
+ * 3 packed step (Q, dQ/da from the packed 40-bit slabs, then one INT8 Ozaki GEMM), 4 the same step
+ * with Q, dQ/da synthesised on the INT8 tensor cores from the element-row digit cache; -1 before
+ * the first step. For benchmarks and diagnostics. */
 int fgfrft_cache_route_info(const fgfrft_cache* cache, int* route, int* nodes);
 
 /* transform.hpp:131-134: copy F^k (1 <= k <= l, else PARAMETER) to host (n x n). */
@@ -338,6 +343,9 @@ int fgfrft_pshard_apply_dev(fgfrft_cache* shard, const double* alphas, int n_alp
  */
 /* Default digit count of the library's INT8 engine (6). */
 int fgfrft_int8_digits(void);
+/* Digits per operand of the packed step route's product GEMM [Y; dY] = [Q; dQ] X (routes 3 / 4):
+ * 5 by default (Q carries the cache's ~2^-40 quantisation), FGFRFT_STEP_SLICES=6 for 6. */
+int fgfrft_step_int8_digits(void);
 /* Complex128 GEMM on the same engine: C (m x n, column-major ldc) = op(A) op(B), trans 0 = N,
  * 1 = T, 2 = C (conjugate transpose); interleaved (re, im) doubles. Computed as ONE real Ozaki
  * GEMM with K doubled (A' = [Re, -Im], B' = [[Re, Im], [Im, -Re]] per element, the epilogue merges

@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_launch_count": (u64, []),
         "fgfrft_profile_enable": (i, [i]),
         "fgfrft_profile_read": (i, [vp, vp, i]),
+        "fgfrft_profile_trace": (i, [vp, vp, vp, i, vp]),
         "fgfrft_sinc_coeffs": (i, [d, i, vp, vp]),
         "fgfrft_fnv1a64": (u64, [vp, ctypes.c_size_t]),
         "fgfrft_cache_create": (i, [vp, i64, i, u64, i, i, pp]),
@@ -117,6 +118,7 @@ def lib() -> ctypes.CDLL:
         "fgfrft_batch_dlda_dev": (i, [vp, vp, i, vp, vp, i64, vp]),
         "fgfrft_cache_set_engine": (i, [vp, i]),
         "fgfrft_int8_digits": (i, []),
+        "fgfrft_step_int8_digits": (i, []),
         "fgfrft_denoise_create": (i, [vp, vp, vp, i64, pp]),
         "fgfrft_denoise_destroy": (i, [vp]),
         "fgfrft_denoise_eval": (i, [vp, d, vp, vp, vp, vp]),
@@ -175,7 +177,7 @@ def lib() -> ctypes.CDLL:
 def exported_symbols():
     return [
         "fgfrft_last_error", "fgfrft_version", "fgfrft_launch_count", "fgfrft_profile_enable",
-        "fgfrft_profile_read", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
+        "fgfrft_profile_read", "fgfrft_profile_trace", "fgfrft_sinc_coeffs", "fgfrft_fnv1a64",
         "fgfrft_cache_create", "fgfrft_cache_create_from_powers", "fgfrft_cache_destroy", "fgfrft_cache_info",
         "fgfrft_cache_is_real", "fgfrft_cache_route_info",
         "fgfrft_cache_power", "fgfrft_cache_verify", "fgfrft_cache_set_stream", "fgfrft_cache_device_slab",
@@ -185,7 +187,7 @@ def exported_symbols():
         "fgfrft_shard_set_stream", "fgfrft_shard_synthesize_dev", "fgfrft_shard_apply_dev",
         "fgfrft_shard_mse_partial_dev", "fgfrft_batch_create", "fgfrft_batch_destroy", "fgfrft_batch_set_stream",
         "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
-        "fgfrft_int8_digits", "fgfrft_cache_orthogonality", "fgfrft_denoise_create", "fgfrft_denoise_destroy",
+        "fgfrft_int8_digits", "fgfrft_step_int8_digits", "fgfrft_cache_orthogonality", "fgfrft_denoise_create", "fgfrft_denoise_destroy",
         "fgfrft_denoise_eval", "fgfrft_denoise_fit",
         "fgfrft_cache_prepare", "fgfrft_spectrum_create", "fgfrft_spectrum_decompose", "fgfrft_spectrum_destroy",
         "fgfrft_spectrum_info", "fgfrft_spectrum_vectors", "fgfrft_spectrum_set_stream", "fgfrft_exact",
@@ -227,6 +229,16 @@ def profile_read(reset: bool = True):
     cnt = np.zeros(8, dtype=np.int64)
     _check(lib().fgfrft_profile_read(_ptr(ms), _ptr(cnt), int(reset)))
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def profile_trace(cap: int = 4096):
+    """[(class, start_ms, end_ms)] of the recorded launches (call before profile_read(reset=True))."""
+    cls = np.zeros(cap, dtype=np.int32)
+    t0, t1 = np.zeros(cap), np.zeros(cap)
+    cnt = ctypes.c_int()
+    _check(lib().fgfrft_profile_trace(_ptr(cls), _ptr(t0), _ptr(t1), cap, ctypes.addressof(cnt)))
+    m = min(cnt.value, cap)
+    return [(KERNEL_CLASSES[cls[i]], float(t0[i]), float(t1[i])) for i in range(m)]
 
 
 def _cm(a: np.ndarray) -> np.ndarray:
@@ -317,7 +329,8 @@ class PowerCache:
 
     def route_info(self):
         """(route, nodes) of the last MSE step: 0 synthesis, 1 power products, 2 node interpolation,
-        3 packed (Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X)."""
+        3 packed (Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X), 4 the same
+        step with Q, dQ/da synthesised on the INT8 tensor cores from the digit cache."""
         r, k = ctypes.c_int(), ctypes.c_int()
         _check(lib().fgfrft_cache_route_info(self._h, ctypes.addressof(r), ctypes.addressof(k)))
         return r.value, k.value

@@ -243,7 +243,7 @@ void destroy_cache(fgfrft_cache* c) {
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
                       &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
                       &c->by, &c->es, &c->ee, &c->erm, &c->nd_tab, &c->nd_p, &c->nd_d0, &c->nd_bsl, &c->nd_bex,
-                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ydy, &c->pp, &c->ppc, &c->rb, &c->bar})
+                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ds, &c->dse, &c->dsb, &c->ydy, &c->pp, &c->ppc, &c->rb, &c->bar})
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
@@ -489,7 +489,7 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
         return FGFRFT_OK;
     }
     if ((n_alpha == 1 || n_alpha == 2 || n_alpha == 4) && packed_enabled(c) && use_int8_gemm(c, b) &&
-        ensure_packed(c)) {
+        ensure_step_cache(c)) {
         // Q(a)^T = Q(-a) bit-exactly (sinc.hpp coefficient mirror): the inverse synthesises Q(-a)
         if (inverse) {
             std::vector<double> al(alphas, alphas + n_alpha);
@@ -1371,6 +1371,62 @@ bool ensure_packed(fgfrft_cache* c) {
     return true;
 }
 
+// The digit cache of the tensor-core synthesis (preferred over the packed slabs: same bytes per
+// element at L = 64, a fifth of the SM issue per element -- it can overlap the product GEMM).
+// FGFRFT_DSYNTH=0 keeps the packed route (read per call: the tests compare both).
+static bool dsynth_wanted() {
+    const char* e = std::getenv("FGFRFT_DSYNTH");
+    return !(e && !std::strcmp(e, "0"));
+}
+
+bool ensure_dsynth(fgfrft_cache* c) {
+    if (!dsynth_wanted()) return false;
+    if (c->ds_state) return c->ds_state > 0;
+    const int64_t rows = (int64_t)dsynth_cache_rows((int)c->n), kp = dsynth_kp(c->l);
+    const uint64_t bytes = (uint64_t)rows * kp * dsynth_slices(), ebytes = (uint64_t)rows * sizeof(int);
+    DevBuf tmp;
+    auto fail = [&] {
+        cudaGetLastError();
+        c->ds.release();
+        c->dse.release();
+        tmp.release();
+        c->ds_state = -1;
+        return false;
+    };
+    if (kp > 512 || !aux_fits(c, bytes + ebytes) || c->ds.ensure(bytes) != cudaSuccess ||
+        c->dse.ensure(ebytes) != cudaSuccess || tmp.ensure((size_t)rows * sizeof(unsigned long long)) != cudaSuccess ||
+        c->dsb.ensure(dsynth_coef_bytes((int)kp)) != cudaSuccess)
+        return fail();
+    {
+        ProfScope ps(KC_SLICE, c->stream);
+        if (launch_dsynth_build(static_cast<const double*>(c->slabs), (int)c->n, c->l, (int)kp, c->ds.as<int8_t>(), c->dse.as<int>(),
+                                tmp.as<unsigned long long>(), c->stream) != cudaSuccess)
+            return fail();
+    }
+    g_launches += 3;
+    cudaStreamSynchronize(c->stream);  // the row-max scratch is freed below
+    tmp.release();
+    c->aux_bytes += bytes + ebytes;
+    c->ds_state = 1;
+    return true;
+}
+
+// Digits per operand of the step route's product GEMM [Y; dY] = [Q; dQ] X. Q carries the cache's
+// ~2^-40 quantisation (packed 40-bit tiles / 5-digit element rows), so 5 base-254 digits (39.9
+// bits, 15 digit products) match it; 6 digits (21 products) buy nothing measurable. FGFRFT_STEP_SLICES
+// overrides (5 or 6).
+static int step_slices() {
+    static const int s = [] {
+        const char* e = std::getenv("FGFRFT_STEP_SLICES");
+        const int v = e ? std::atoi(e) : 5;
+        return v == 6 ? 6 : 5;
+    }();
+    return s;
+}
+
+// The step route's cache: the digit cache when wanted and it fits, else the packed slabs.
+bool ensure_step_cache(fgfrft_cache* c) { return ensure_dsynth(c) || ensure_packed(c); }
+
 // ---- the pipelined form: row-complete shells
 //
 // The step is the sum of an HBM-bound pass (synthesis from the packed slabs) and a tensor-bound
@@ -1413,7 +1469,17 @@ static std::vector<PkShell> pk_plan(int64_t n, int rows, int64_t b, int l) {
     };
     std::vector<PkShell> out;
     std::vector<int> bounds{0, T};
-    if (maxc > 1 && T >= 4) {
+    if (const char* sp = std::getenv("FGFRFT_PIPE_SPLIT")) {  // explicit row fractions "f1,f2,..."
+        bounds.assign(1, 0);
+        for (const char* q = sp; *q;) {
+            const double f = std::atof(q);
+            const int blk = (int)std::lround(f * T);
+            if (blk > bounds.back() && blk < T) bounds.push_back(blk);
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+        bounds.push_back(T);
+    } else if (maxc > 1 && T >= 4) {
         // f[c][j][k]: best cost of shells covering blocks [0, k) with c shells, the last being [j, k)
         const double inf = 1e30;
         std::vector<double> f((size_t)(maxc + 1) * (T + 1) * (T + 1), inf);
@@ -1483,10 +1549,13 @@ int ensure_pipe_streams(fgfrft_cache* c) {
 // overlaps the synthesis (which does not need X) and the earlier chunks' products.
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
                     void* y, int l_used, const double* x_host) {
-    const int S = oz_slices_default();
+    const int S = step_slices();
     const int64_t n = c->n, mp = pad_rows(n), sl = n * n, kp = pad_k(n);
     const int64_t bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
-    const uint64_t key = ((uint64_t)n << 40) ^ ((uint64_t)rows << 32) ^ ((uint64_t)b << 8) ^ (uint64_t)l_used;
+    const char* split = std::getenv("FGFRFT_PIPE_SPLIT");
+    const uint64_t key = ((uint64_t)n << 40) ^ ((uint64_t)rows << 32) ^ ((uint64_t)b << 8) ^ (uint64_t)l_used ^
+                         ((uint64_t)pk_env("FGFRFT_PIPE_SHELLS", 1) << 56) ^ ((uint64_t)dsynth_wanted() << 62) ^
+                         (split ? std::hash<std::string>{}(split) : 0);
     if (c->pk_plan_key != key) {
         c->pk_plan = pk_plan(n, rows, b, l_used);
         c->pk_plan_key = key;
@@ -1544,6 +1613,15 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
                    3);
     }
     FGB_CUDA(cudaMemsetAsync(rmax, 0, (size_t)rows * mp * sizeof(unsigned long long), c->pk_s));
+    // synthesis engine: tensor-core digits (dsynth) or the packed FP64 decode (psynth)
+    const bool tc = dsynth_wanted() && c->ds_state > 0;
+    c->pk_tc = tc;
+    if (!tc && !ensure_packed(c)) return FGFRFT_CAPACITY;
+    const int64_t dkp = dsynth_kp(c->l);
+    if (tc) {
+        ProfScope ps(KC_SYNTH, c->pk_s);
+        FGB_LAUNCH(launch_dsynth_coefs(coef, coef_ld, l_used, rows, (int)dkp, c->dsb.as<int8_t>(), c->pk_s), 1);
+    }
     const int gcap = (int)pk_env("FGFRFT_PIPE_GEMM_CTAS", 100);
     const int syn_cap = (int)pk_env("FGFRFT_PIPE_SYN_CTAS", FGFRFT_SMS - gcap);  // one CTA per SM
     if (c->pk_es.size() < plan.size()) {
@@ -1561,9 +1639,15 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         {
             ProfScope ps(KC_SYNTH, c->pk_s);
             // shell 0 runs alone (the GEMM has nothing yet): full grid; later shells share the GPU
-            FGB_LAUNCH(launch_psynth(c->pk.p, c->pks.as<double>(), (int)n, l_used, c->l, coef, coef_ld, rows, q, sl, rmax, mp,
-                                     c->pk_s, sh.p0, sh.p1, s == 0 ? 0 : syn_cap),
-                       1);
+            if (tc)
+                FGB_LAUNCH(launch_dsynth(c->ds.as<int8_t>(), c->dse.as<int>(), c->dsb.as<int8_t>(), (int)dkp, (int)n,
+                                         sh.p0, sh.p1, coef, coef_ld, l_used, rows, q, sl, rmax, mp,
+                                         s == 0 ? (int)pk_env("FGFRFT_SYN_CAP0", 0) : syn_cap, c->pk_s),
+                           1);
+            else
+                FGB_LAUNCH(launch_psynth(c->pk.p, c->pks.as<double>(), (int)n, l_used, c->l, coef, coef_ld, rows, q, sl,
+                                         rmax, mp, c->pk_s, sh.p0, sh.p1, s == 0 ? 0 : syn_cap),
+                           1);
         }
         {
             OzView v{q + sh.r0, 1, n, sl, 0, 0, (int)rv, (int)rp, rows, (int)n, (int)kp, true};
@@ -1636,7 +1720,7 @@ int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void
                                  norm, loss_dev + a, dlda_dev + a, c->stream),
                    2);
     }
-    c->last_route = 3;
+    c->last_route = c->pk_tc ? 4 : 3;
     c->last_nodes = 0;
     return FGFRFT_OK;
 }
@@ -1679,6 +1763,23 @@ int fgfrft_profile_read(double* ms, int64_t* counts, int reset) {
             g_prof_pool.push_back(r.b);
         }
         g_prof.clear();
+    }
+    return FGFRFT_OK;
+}
+
+int fgfrft_profile_trace(int* cls, double* t0, double* t1, int cap, int* count) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    const int m = (int)g_prof.size();
+    if (count) *count = m;
+    for (int i = 0; i < m && i < cap; ++i) {
+        const ProfRec& r = g_prof[i];
+        FGB_CUDA(cudaEventSynchronize(r.b));
+        float a = 0.f, b = 0.f;
+        FGB_CUDA(cudaEventElapsedTime(&a, g_prof[0].a, r.a));
+        FGB_CUDA(cudaEventElapsedTime(&b, g_prof[0].a, r.b));
+        if (cls) cls[i] = r.cls;
+        if (t0) t0[i] = a;
+        if (t1) t1[i] = b;
     }
     return FGFRFT_OK;
 }
@@ -1808,7 +1909,7 @@ int fgfrft_cache_prepare(fgfrft_cache* c) {
     // every structure a route may build lazily, in the order the routes prefer them, each only while
     // it fits the handle's memory budget (aux_fits): the packed slabs (one / two-order steps), the
     // element-row digit slices (node-interpolated sweeps), the stacked digit slices (power route)
-    if (packed_enabled(c)) ensure_packed(c);
+    if (packed_enabled(c)) ensure_step_cache(c);
     if (c->real && c->dtype == FGFRFT_C128 && engine_of(c) != FGFRFT_ENGINE_DMMA &&
         2 * c->l + 1 <= combine_max_terms()) {
         if (engine_of(c) == FGFRFT_ENGINE_AUTO && !c->es_slices && aux_fits(c, elem_slice_bytes(c)))
@@ -2082,7 +2183,7 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     c->last_route = use_power_route(c, n_alpha) ? 1 : 0;
     c->last_nodes = 0;
     if (!use_power_route(c, n_alpha) && n_alpha <= 2 && packed_enabled(c) && use_int8_gemm(c, b) &&
-        !use_fused_apply(c, n_alpha, b) && ensure_packed(c))
+        !use_fused_apply(c, n_alpha, b) && ensure_step_cache(c))
         return mse_packed_step(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
                                static_cast<double*>(dlda_dev));
     if (use_power_route(c, n_alpha)) {
@@ -2186,7 +2287,7 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
         if (c->dtype == FGFRFT_C128 && !c->api_c64 && n_alpha <= 2 && packed_enabled(c) && use_int8_gemm(c, b) &&
-            !use_fused_apply(c, n_alpha, b) && !use_power_route(c, n_alpha) && ensure_packed(c)) {
+            !use_fused_apply(c, n_alpha, b) && !use_power_route(c, n_alpha) && ensure_step_cache(c)) {
             const size_t xe = (size_t)c->n * b;
             FGB_CUDA(c->x.ensure(xe * 16));
             FGB_CUDA(c->xc.ensure(xe * 16));
@@ -2273,6 +2374,8 @@ void keep_pool() {
 }  // namespace fgbi
 
 int fgfrft_int8_digits(void) { return oz_slices_default(); }
+
+int fgfrft_step_int8_digits(void) { return step_slices(); }
 
 int fgfrft_dgemm_int8_dev(int transa, int transb, int64_t m, int64_t n, int64_t k, const double* a, int64_t lda,
                           const double* b, int64_t ldb, double* c, int64_t ldc, int slices, void* stream) {

@@ -388,10 +388,16 @@ struct fgfrft_cache {
     // plus their bytes stays within it; otherwise the routes that need them are not taken.
     uint64_t budget = 0;
     uint64_t aux_bytes = 0;
-    // Packed power cache (packed.cu): 48-bit fixed-point tiles + per-tile scales, for the one- /
+    // Packed power cache (packed.cu): 40-bit fixed-point tiles + per-tile scales, for the one- /
     // two-order step and apply route (real F). 0 not built, 1 ready, -1 unavailable.
     int pk_state = 0;
     DevBuf pk, pks, ydy;
+    // Digit cache of the INT8 tensor-core synthesis (ozgemm.cu dsynth_kernel): pair-major element
+    // rows x powers, 5 base-254 digits + one exponent per element row; the coefficient digits.
+    // Replaces the packed slabs on the step route when it fits. 0 not built, 1 ready, -1 unavailable.
+    int ds_state = 0;
+    bool pk_tc = false;  // the last packed_products synthesised on the tensor cores
+    DevBuf ds, dse, dsb;
     // shell pipeline of the packed route: side streams (S synthesis + slicing, G GEMMs, high
     // priority), fork / join events, one event per shell, the memoised shell plan
     cudaStream_t pk_s = nullptr, pk_g = nullptr;
@@ -480,6 +486,8 @@ uint64_t power_slice_bytes(const fgfrft_cache* c);
 uint64_t elem_slice_bytes(const fgfrft_cache* c);
 int ensure_elem_slices(fgfrft_cache* c);
 bool ensure_packed(fgfrft_cache* c);
+bool ensure_dsynth(fgfrft_cache* c);
+bool ensure_step_cache(fgfrft_cache* c);
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
                     void* y, int l_used, const double* x_host = nullptr);
 int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,

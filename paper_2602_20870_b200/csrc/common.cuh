@@ -172,4 +172,18 @@ __device__ __forceinline__ void pair_of(int p, int& I, int& J) {
     I = p - j * (j + 1) / 2;
 }
 
+// I-major enumeration of the tile pairs (I <= J): row I's pairs are contiguous, so the pairs
+// whose smaller tile index lies in [I0, I1) -- everything that completes rows [32 I0, 32 I1) of
+// a synthesised operator -- are one index range [pairs_before(I0), pairs_before(I1)).
+__host__ __device__ __forceinline__ int64_t pairs_before(int64_t I, int64_t nt) { return I * nt - I * (I - 1) / 2; }
+__device__ __forceinline__ void pair_of_imajor(int p, int nt, int& I, int& J) {
+    const double b = 2.0 * nt + 1.0;
+    int i = (int)((b - sqrt(b * b - 8.0 * p)) * 0.5);
+    i = max(0, min(i, nt - 1));
+    while (i > 0 && pairs_before(i, nt) > p) --i;
+    while (i + 1 < nt && pairs_before(i + 1, nt) <= p) ++i;
+    I = i;
+    J = i + (int)(p - pairs_before(i, nt));
+}
+
 }  // namespace fgb

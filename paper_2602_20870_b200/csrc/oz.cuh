@@ -27,6 +27,12 @@ struct OzView {
                      //    ra = 0 (A side): A'(r, 2k + e) = e ? -Im z : Re z
                      //    ra = 1 (B side, rows 2j + c): B'(2j + c, 2k + e) = (Re, Im; Im, -Re)[c][e]
                      //    ka = 1: conjugate z first
+                     // 7: element-pair rows of the PAIR-MAJOR digit cache (the INT8 synthesis,
+                     //    dsynth_kernel): row r -> M tile mt = r / 128, pair p = mt / 8, t = 128
+                     //    (mt % 8) + r % 128, (I, J) = pair_of_imajor(p), i = t % 32, j = t / 32;
+                     //    K < kp / 2: P_(K+1)(32 I + i, 32 J + j), K >= kp / 2: the mirror
+                     //    P_(K-kp/2+1)(32 J + j, 32 I + i) (tiled slabs: sbatch = slab elements,
+                     //    nt, l = L, tp2 = n)
                      // 6: element rows of the stacked cache (the basis synthesis GEMM): row
                      //    e = i + j n (rv = n^2, tp2 = n), K term kk < L: P_(kk+1)(i, j), L <= kk < 2L:
                      //    P_(kk-L+1)(j, i); one batch block (nb = 1, rp = padded n^2)
@@ -85,6 +91,21 @@ constexpr int kOzTileB = 64;   // B operand row tile (output columns per CTA)
 constexpr int kOzK = 64;       // K padding granule
 
 int oz_slices_default();
+// INT8 tensor-core synthesis (ozgemm.cu dsynth_kernel): operator rows x < ac of
+// Q_x = c_x0 I + sum_k c_xk P_k + c_x(-k) P_k^T for the tile pairs [p0, p1) (p1 < 0: all) from the
+// pair-major element-row digit cache (launch_dsynth_build) and the coefficient digits
+// (launch_dsynth_coefs); out + x out_stride: n x n column-major, rowmax + x mp: row maxima.
+size_t dsynth_cache_rows(int n);
+int dsynth_slices();
+int dsynth_kp(int l);  // K of the digit cache: 2 x pad64(L)
+size_t dsynth_coef_bytes(int kp);
+cudaError_t launch_dsynth_build(const double* slabs, int n, int l, int kp, int8_t* digits, int* exps,
+                                unsigned long long* rowmax_tmp, cudaStream_t stream);
+cudaError_t launch_dsynth_coefs(const double* coef, int coef_ld, int l_used, int ac, int kp, int8_t* bsl,
+                                cudaStream_t stream);
+cudaError_t launch_dsynth(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0, int p1,
+                          const double* coef, int coef_ld, int l_used, int ac, double* out, int64_t out_stride,
+                          unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream);
 // Slice a viewed operand into dst (slices * nb * rp * kp bytes) + exps (nb * rp ints);
 // rowmax: nb * rp scratch words. tr = kOzTileA for an A operand, kOzTileB for a B operand.
 cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, int* exps, unsigned long long* rowmax,

@@ -165,6 +165,20 @@ __device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
         const int a = tr ? j : i, b = tr ? i : j;
         return v.src[slab * v.sbatch + tile_base(a >> 5, b >> 5, v.nt) + swz(a & 31, b & 31)];
     }
+    if (v.tiled == 7) {  // element-pair rows of the digit cache (see OzView)
+        if (row >= v.rv || k >= v.kp) return 0.0;
+        const int mt = row >> 7, p = mt >> 3;
+        const int t = 128 * (mt & 7) + (row & 127), kh = v.kp >> 1;
+        const bool mirror = k >= kh;
+        const int kk = mirror ? k - kh : k;
+        if (kk >= v.l) return 0.0;
+        int I, J;
+        pair_of_imajor(p, v.nt, I, J);
+        const int i = t & 31, j = t >> 5;
+        const int gr = mirror ? J * 32 + j : I * 32 + i, gc = mirror ? I * 32 + i : J * 32 + j;
+        if (gr >= v.tp2 || gc >= v.tp2) return 0.0;
+        return v.src[(int64_t)kk * v.sbatch + tile_base(gr >> 5, gc >> 5, v.nt) + swz(gr & 31, gc & 31)];
+    }
     if (v.tiled == 3) {  // rv = n (signal rows), rows beyond n * tp2 are padding
         const int i = row / v.tp2, kk = row - i * v.tp2;
         if (i >= v.rv || kk >= 2 * v.l || k >= v.kv) return 0.0;
@@ -829,6 +843,307 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- INT8 tensor-core synthesis
+//
+// Q(a) = c_0 I + sum_k c_k P_k + c_-k P_k^T (and dQ/da with c'_k) for one tile pair {(I,J),(J,I)}
+// as a GEMM whose rows are ELEMENT PAIRS and whose K is the power index: row t of a pair holds the
+// powers of element e = (32I+i, 32J+j) in K [0, kh) and of its mirror e' = (32J+j, 32I+i) in
+// K [kh, 2 kh) (OzView mode 7: 5 base-254 digits, one exponent per row over all 2L values -- the
+// same ~2^-40 quantisation as the packed cache). B = per operator row two coefficient rows
+// [c_k | c_-k] and [c_-k | c_k] (6 digits, one 16-row tile loaded once per CTA), so accumulator
+// column 2x is Q_x[e] and column 2x + 1 is Q_x[e'] -- every thread owns both outputs of its row,
+// with no exchange between threads. The multiply-adds run on the tensor cores; the SMs stream
+// digits (TMA ring) and run a short fold per element, so the synthesis of one row shell can share
+// the GPU with the product GEMM of the previous one (capi.cu packed_products). One CTA per SM
+// walks whole pairs (8 M tiles of 128 rows): warp 0 = TMA producer, warps 1-2 = MMA issuers, then G
+// epilogue groups of 4 warps taking tiles round robin (TMEM: 4 accumulator buffers, 128 columns
+// apart, each 6 digit sums x 16 columns).
+constexpr int kDsBN = 16;
+constexpr int kDsSA = 5, kDsSB = 6;
+constexpr int kDsNB = 4;
+constexpr int kDsIssuers = 2;                  // MMA-issuing warps (kDsNB % kDsIssuers == 0); dbg & 2: 1
+constexpr int kDsAStage = kDsSA * kOzBM * 64;  // one M tile x one 64-byte K block (40 KB)
+constexpr int kDsTiles = 8;                    // M tiles per pair (1024 element pairs / 128)
+
+__host__ __device__ constexpr int ds_b_bytes(int kp) { return kDsSB * kDsBN * kp; }
+__host__ __device__ constexpr int ds_fixed_bytes(int kp) { return ds_b_bytes(kp) + 256; }  // B + barriers
+static int ds_stages(int kp) {
+    static const int forced = [] {
+        const char* e = std::getenv("FGFRFT_DS_STAGES");
+        return e ? std::atoi(e) : 0;
+    }();
+    int st = (227 * 1024 - ds_fixed_bytes(kp)) / kDsAStage;
+    if (forced > 0 && forced < st) st = forced;
+    return st > 5 ? 5 : st;
+}
+static int ds_smem(int kp) { return ds_stages(kp) * kDsAStage + ds_fixed_bytes(kp); }
+
+template <int W>
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, int32_t (&v)[W]) {
+    if constexpr (W == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(taddr));
+    } else if constexpr (W == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
+    } else {
+        static_assert(W == 8, "2, 4 or 8 columns");
+        tmem_ld8(taddr, v);
+    }
+}
+
+// c_x(s k) of table row x (c_k at l_used + k), 0 beyond the truncation
+__device__ __forceinline__ double ds_coef(const double* coef, int coef_ld, int l_used, int x, int k) {
+    return (k <= l_used && k >= -l_used) ? coef[(size_t)x * coef_ld + l_used + k] : 0.0;
+}
+
+// B operand: row 2x = [c_x(k) | c_x(-k)], row 2x + 1 = [c_x(-k) | c_x(k)] (K halves of kh = kp / 2,
+// k = kk + 1), the canonical K-major layout of a 16-row tile with 64-byte K blocks.
+__global__ void __launch_bounds__(512) dsynth_coef_kernel(const double* __restrict__ coef, int coef_ld, int l_used,
+                                                          int ac, int kp, int8_t* __restrict__ bd, int* __restrict__ eb) {
+    __shared__ unsigned long long mx[kDsBN];
+    const int kh = kp / 2, runs = kp / 16;  // one thread per (row, 16-byte K run)
+    const int r = threadIdx.x / runs, q = threadIdx.x - r * runs;
+    if (threadIdx.x < kDsBN) mx[threadIdx.x] = 0ull;
+    double x[16];
+    double m = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int kk = q * 16 + i;
+        const bool hi = kk >= kh;
+        const int k = (hi ? kk - kh : kk) + 1;
+        const bool neg = hi != (bool)(r & 1);
+        x[i] = r < 2 * ac ? ds_coef(coef, coef_ld, l_used, r >> 1, neg ? -k : k) : 0.0;
+        m = fmax(m, fabs(x[i]));
+    }
+    __syncthreads();
+    if (m > 0.0) atomicMax(mx + r, (unsigned long long)__double_as_longlong(m));
+    __syncthreads();
+    const double rm = __longlong_as_double((long long)mx[r]);
+    int e = 0;
+    if (rm > 0.0) frexp(rm, &e);
+    if (q == 0) eb[r] = e;
+    const double sc = rm > 0.0 ? pow2(-e - 1) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] *= sc;
+    const int k0 = q * 16, kb = k0 / 64, cl = (k0 >> 4) & 3;
+    int8_t* base = bd + (int64_t)kb * kDsSB * kDsBN * 64 + (r >> 3) * 512 + cl * 128 + (r & 7) * 16;
+#pragma unroll
+    for (int s2 = 0; s2 < kDsSB; ++s2) {
+        uint32_t w[4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double y = x[qq * 4 + i] * kOzBase;
+                const double tt = y + kOzMagic;
+                x[qq * 4 + i] = y - (tt - kOzMagic);
+                packed |= ((uint32_t)__double2loint(tt) & 0xFFu) << (8 * i);
+            }
+            w[qq] = packed;
+        }
+        *reinterpret_cast<uint4*>(base + s2 * kDsBN * 64) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// max of non-negative doubles over the warp by their high words (sign, exponent, 20 mantissa
+// bits): the slicer only takes the exponent of a row max, which the high word fixes exactly
+__device__ __forceinline__ unsigned long long ds_warp_max_hi(double v) {
+    const unsigned h = (unsigned)((unsigned long long)__double_as_longlong(v) >> 32);
+    return (unsigned long long)__reduce_max_sync(0xffffffffu, h) << 32;
+}
+
+template <int AC, int G>
+__global__ void __launch_bounds__(32 * (1 + kDsIssuers + 4 * G), 1)
+dsynth_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const int8_t* __restrict__ b,
+              const int* __restrict__ eb, int kblocks, int stages, int n, int nt, int p0, int p1,
+              const double* __restrict__ coef, int coef_ld, int l_used, double* __restrict__ out, int64_t ostride,
+              unsigned long long* __restrict__ rowmax, int64_t mp, int dbg) {
+    constexpr int W = 2 * AC;        // live B rows / accumulator columns
+    constexpr int TPG = kDsTiles / G;  // tiles of a pair per epilogue group
+    static_assert(kDsTiles % G == 0, "groups divide the tiles of a pair");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* sa = smem;
+    unsigned char* sb = smem + (size_t)stages * kDsAStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + ds_b_bytes(kblocks * 64));
+    uint64_t* empty = full + 5;
+    uint64_t* tfull = empty + 5;  // [NB]
+    uint64_t* tempty = tfull + kDsNB;
+    uint64_t* bfull = tempty + kDsNB;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t pstart = p0 + blockIdx.x;
+    const int tile_kb = kblocks;  // K blocks per M tile
+    const int nis = (dbg & 2) ? 1 : kDsIssuers;  // MMA issuers
+    const int sr = stages / nis;                 // stages per issuer ring
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int u = 0; u < kDsNB; ++u) {
+            mbar_init(tfull + u, 1);
+            mbar_init(tempty + u, 4);
+        }
+        mbar_init(bfull, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();  // the digits are read once per step (dsynth)
+            mbar_arrive_expect_tx(bfull, (uint32_t)ds_b_bytes(kblocks * 64));
+            bulk_g2s(sb, b, (uint32_t)ds_b_bytes(kblocks * 64), bfull);
+            // one stage ring per MMA issuer (issuer w consumes tiles w, w + nis, ...): a ring whose
+            // stages alternated between issuers would let one wait on a phase two ahead (parity alias)
+            int itr[kDsIssuers] = {};
+            int tcount = 0;
+            for (int64_t p = pstart; p < p1; p += gridDim.x) {
+                const unsigned char* ga = reinterpret_cast<const unsigned char*>(a) + p * kDsTiles * (int64_t)tile_kb * kDsAStage;
+                for (int sub = 0; sub < kDsTiles; ++sub, ++tcount) {  // a pair's tiles are contiguous
+                    const int r = tcount % nis;
+                    for (int kb = 0; kb < tile_kb; ++kb) {
+                        const int it = itr[r]++;
+                        const int s = r * sr + it % sr;
+                        if (it >= sr) mbar_wait(empty + s, ((it / sr) - 1) & 1);
+                        mbar_arrive_expect_tx(full + s, kDsAStage);
+                        bulk_g2s_hint(sa + (size_t)s * kDsAStage, ga + ((int64_t)sub * tile_kb + kb) * kDsAStage, kDsAStage,
+                                      full + s, pol);
+                    }
+                }
+            }
+        }
+    } else if (warp <= kDsIssuers) {
+        // MMA issuers: one tcgen05.mma costs its issuing thread ~75 cycles whatever N (measured,
+        // tools/probes/mma_probe.cu), more than the tensor pipe needs for these N <= 96 tiles, so
+        // kDsIssuers warps issue alternate tiles (issuer w: tiles w, w + kDsIssuers, ...)
+        const int me = warp - 1;
+        if (lane == 0 && me < nis) {
+            mbar_wait(bfull, 0);
+            tc_fence_after();
+            const uint32_t b0 = smem_u32(sb);
+            int it = 0, tcount = 0;
+            for (int64_t p = pstart; p < p1; p += gridDim.x)
+                for (int sub = 0; sub < kDsTiles; ++sub, ++tcount) {
+                    if (tcount % nis != me) continue;
+                    const int buf = tcount % kDsNB;
+                    if (tcount >= kDsNB) mbar_wait(tempty + buf, ((tcount / kDsNB) - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t acc = tmem + (uint32_t)buf * 128;
+                    for (int kb = 0; kb < tile_kb; ++kb, ++it) {
+                        const int s = me * sr + it % sr;
+                        mbar_wait(full + s, (it / sr) & 1);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sa + (size_t)s * kDsAStage);
+                        if (!(dbg & 1))
+#pragma unroll
+                            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                                for (int t = 1; t <= kDsSA; ++t) {
+                                    // A digit t x B digits 1 .. 7 - t -> digit sums t - 1 .. 5 (columns 16 (t-1) ..)
+                                    const uint64_t ad = umma_desc(a0 + (t - 1) * kOzBM * 64 + j * 256, 128, 512);
+                                    const uint64_t bd = umma_desc(b0 + kb * kDsSB * kDsBN * 64 + j * 256, 128, 512);
+                                    mma_i8(acc + (uint32_t)((t - 1) * kDsBN), ad, bd,
+                                           idesc_i8(kOzBM, (kDsSB + 1 - t) * kDsBN), (kb > 0 || j > 0 || t > 1) ? 1u : 0u);
+                                }
+                        mma_commit(empty + s);
+                    }
+                    mma_commit(tfull + buf);
+                }
+        }
+    } else {
+        const int grp = (warp - 1 - kDsIssuers) >> 2, lg = warp & 3;
+        const int lrow = lg * 32 + lane;
+        int ebv[W];
+        double c0v[AC];
+#pragma unroll
+        for (int c = 0; c < W; ++c) ebv[c] = eb[c];
+#pragma unroll
+        for (int x = 0; x < AC; ++x) c0v[x] = coef[(size_t)x * coef_ld + l_used];
+        constexpr double w1 = 1.0 / 254.0, w2 = w1 * w1, w3 = w2 * w1, w4 = w3 * w1, w5 = w4 * w1;
+        // this group's tiles of a pair are sub = G q + grp; their row exponents are loaded one pair
+        // ahead (a DRAM round trip under load is ~1-2 us)
+        int eaq[TPG], ean[TPG];
+        auto load_ea = [&](int64_t pp, int (&dst)[TPG]) {
+#pragma unroll
+            for (int q2 = 0; q2 < TPG; ++q2)
+                dst[q2] = pp < p1 ? __ldcs(ea + (pp * kDsTiles + G * q2 + grp) * kOzBM + lrow) : 0;
+        };
+        load_ea(pstart, eaq);
+        int jp = 0;
+        for (int64_t p = pstart; p < p1; p += gridDim.x, ++jp) {
+            load_ea(p + gridDim.x, ean);
+            int I, J;
+            pair_of_imajor((int)p, nt, I, J);
+            const bool diag = I == J;
+            const int i = lane, ri = I * kTile + i;  // this thread's row of Q_IJ (fixed over the pair)
+            double rij[AC];
+#pragma unroll
+            for (int x = 0; x < AC; ++x) rij[x] = 0.0;
+#pragma unroll
+            for (int q2 = 0; q2 < TPG; ++q2) {
+                const int sub = G * q2 + grp, tcount = jp * kDsTiles + sub;
+                const int buf = tcount % kDsNB;
+                const int j = 4 * sub + lg;  // t = 128 sub + 32 lg + lane = i + 32 j
+                const double ra = pow2(eaq[q2]) * (4.0 / (254.0 * 254.0));  // 2^2 x 254^-2: f = sum v_d 254^-d
+                mbar_wait(tfull + buf, (tcount / kDsNB) & 1);
+                tc_fence_after();
+                int32_t v[6][W];
+#pragma unroll
+                for (int d = 0; d < 6; ++d)
+                    tmem_ldw<W>(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * 128 + d * kDsBN), v[d]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + buf);
+                const int cj = J * kTile + j;
+                const bool ok = ri < n && cj < n;
+#pragma unroll
+                for (int x = 0; x < AC; ++x) {
+                    double val[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = 2 * x + h;  // |v| < 2^31: exact in double; 6 roundings ~ 2^-51 relative
+                        double f = fma((double)v[5][c], w5, (double)v[4][c] * w4);
+                        f = fma((double)v[3][c], w3, f);
+                        f = fma((double)v[2][c], w2, f);
+                        f = fma((double)v[1][c], w1, f);
+                        f += (double)v[0][c];
+                        val[h] = f * ra * pow2(ebv[c]);
+                        if (diag && i == j) val[h] += c0v[x];
+                    }
+                    double* o = out + x * ostride;
+                    if (ok) {
+                        __stcs(o + (int64_t)cj * n + ri, val[0]);  // Q[32I+i, 32J+j]: lanes along rows
+                        rij[x] = fmax(rij[x], fabs(val[0]));
+                    }
+                    if (!diag) {  // Q[32J+j, 32I+i]; row 32J+j's max over this warp's 32 columns
+                        if (ok) __stcs(o + (int64_t)ri * n + cj, val[1]);
+                        const unsigned long long m = ds_warp_max_hi(ok ? fabs(val[1]) : 0.0);
+                        if (lane == 0 && m && cj < n) atomicMax(rowmax + (int64_t)x * mp + cj, m);
+                    }
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < AC; ++x)
+                if (ri < n && rij[x] > 0.0)
+                    atomicMax(rowmax + (int64_t)x * mp + ri, (unsigned long long)__double_as_longlong(rij[x]));
+#pragma unroll
+            for (int q2 = 0; q2 < TPG; ++q2) eaq[q2] = ean[q2];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // ---------------------------------------------------------------- host launchers
 
 int oz_slices_default() { return 6; }
@@ -852,6 +1167,8 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
             oz_rowslice_pairs_kernel<8><<<blocks, 64, 0, stream>>>(v, tr, dst, exps);
         else if (slices == 6)
             oz_rowslice_pairs_kernel<6><<<blocks, 64, 0, stream>>>(v, tr, dst, exps);
+        else if (slices == 5)
+            oz_rowslice_pairs_kernel<5><<<blocks, 64, 0, stream>>>(v, tr, dst, exps);
         else
             return cudaErrorInvalidValue;
         return cudaGetLastError();
@@ -863,6 +1180,8 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
             oz_rowslice_direct_kernel<8><<<rows / 32, 256, 0, stream>>>(v, tr, dst, exps);
         else if (slices == 6)
             oz_rowslice_direct_kernel<6><<<rows / 32, 256, 0, stream>>>(v, tr, dst, exps);
+        else if (slices == 5)
+            oz_rowslice_direct_kernel<5><<<rows / 32, 256, 0, stream>>>(v, tr, dst, exps);
         else
             return cudaErrorInvalidValue;
         return cudaGetLastError();
@@ -878,12 +1197,16 @@ cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, in
             oz_slice_direct_kernel<8><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);
         else if (slices == 6)
             oz_slice_direct_kernel<6><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);
+        else if (slices == 5)
+            oz_slice_direct_kernel<5><<<grid, 64, 0, stream>>>(v, rowmax, tr, dst, exps);
         else
             return cudaErrorInvalidValue;
         return cudaGetLastError();
     }
     oz_rowmax_kernel<<<grid, 256, 0, stream>>>(v, rowmax);
-    if (slices == 7)
+    if (slices == 5)  // the synthesis digit cache (dsynth_kernel)
+        oz_slice_kernel<5><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
+    else if (slices == 7)
         oz_slice_kernel<7><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
     else if (slices == 8)
         oz_slice_kernel<8><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);
@@ -909,6 +1232,7 @@ cudaError_t launch_oz_slice_ready(const OzView& v, int slices, int tr, int8_t* d
             oz_slice_kernel<S_><<<grid, 256, 0, stream>>>(v, rowmax, tr, dst, exps);                \
         return cudaGetLastError();                                                                  \
     }
+    FGB_SL(5)
     FGB_SL(6)
     FGB_SL(7)
     FGB_SL(8)
@@ -1010,6 +1334,7 @@ cudaError_t launch_ozgemm_ex(int slices, int cm, const int8_t* a, const int* ea,
             default: return cudaErrorInvalidValue;                                       \
         }                                                                                \
     }
+    FGB_OZ(5)
     FGB_OZ(6)
     FGB_OZ(7)
     FGB_OZ(8)
@@ -1032,6 +1357,87 @@ cudaError_t launch_ozgemm(int slices, int cm, const int8_t* a, const int* ea, in
     out.nv = nv;
     out.max_ctas = max_ctas;
     return launch_ozgemm_ex(slices, cm, a, ea, mrows, b, eb, nrows, kp, out, stream);
+}
+
+
+size_t dsynth_cache_rows(int n) {
+    const int64_t nt = ceil_div(n, kTile);
+    return (size_t)(nt * (nt + 1) / 2) * kDsTiles * kOzBM;
+}
+int dsynth_slices() { return kDsSA; }
+int dsynth_kp(int l) { return (int)(2 * ceil_div(l, 64) * 64); }
+size_t dsynth_coef_bytes(int kp) { return (size_t)ds_b_bytes(kp) + kDsBN * sizeof(int); }
+
+// The digit cache from the tiled FP64 slabs: OzView mode 7, 5 digits, 128-row tiles.
+cudaError_t launch_dsynth_build(const double* slabs, int n, int l, int kp, int8_t* digits, int* exps,
+                                unsigned long long* rowmax_tmp, cudaStream_t stream) {
+    const int nt = (int)ceil_div(n, kTile);
+    OzView v{slabs, 0, 0, (int64_t)nt * nt * kTileElems, 0, 0, (int)dsynth_cache_rows(n), (int)dsynth_cache_rows(n),
+             1, kp, kp, true};
+    v.tiled = 7;
+    v.nt = nt;
+    v.l = l;
+    v.tp2 = n;
+    return launch_oz_slice(v, kDsSA, kOzBM, digits, exps, rowmax_tmp, stream);
+}
+
+// Coefficient digits for `ac` operator rows (table rows of width coef_ld, c_k at l_used + k) into
+// bsl (dsynth_coef_bytes(kp): digits, then 16 exponents).
+cudaError_t launch_dsynth_coefs(const double* coef, int coef_ld, int l_used, int ac, int kp, int8_t* bsl,
+                                cudaStream_t stream) {
+    if (ac != 1 && ac != 2 && ac != 4) return cudaErrorInvalidValue;
+    dsynth_coef_kernel<<<1, kDsBN * (kp / 16), 0, stream>>>(coef, coef_ld, l_used, ac, kp, bsl,
+                                             reinterpret_cast<int*>(bsl + ds_b_bytes(kp)));
+    return cudaGetLastError();
+}
+
+template <int AC, int G>
+static cudaError_t dsynth_launch(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0,
+                                 int p1, const double* coef, int coef_ld, int l_used, double* out, int64_t out_stride,
+                                 unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream) {
+    static PerDeviceOnce attr;
+    const int smem = ds_smem(kp);
+    if (cudaError_t e = attr.run([&] {
+            return cudaFuncSetAttribute(dsynth_kernel<AC, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        }))
+        return e;
+    const int pairs = p1 - p0;
+    int grid = FGFRFT_SMS;
+    if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+    if (pairs < grid) grid = pairs;
+    if (grid <= 0) return cudaSuccess;
+    const int nt = (int)ceil_div(n, kTile);
+    static const int dbg = [] {
+        const char* e = std::getenv("FGFRFT_DS_DEBUG");  // timing experiments only: 1 = skip the MMAs
+        return e ? std::atoi(e) : 0;
+    }();
+    dsynth_kernel<AC, G><<<grid, 32 * (1 + kDsIssuers + 4 * G), smem, stream>>>(
+        digits, exps, bsl, reinterpret_cast<const int*>(bsl + ds_b_bytes(kp)), kp / 64, ds_stages(kp), n, nt, p0, p1,
+        coef, coef_ld, l_used, out, out_stride, rowmax, mp, dbg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dsynth(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0, int p1,
+                          const double* coef, int coef_ld, int l_used, int ac, double* out, int64_t out_stride,
+                          unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream) {
+    if (kp % 128 || kp > 512) return cudaErrorInvalidValue;
+    if (p1 < 0) {
+        const int64_t nt = ceil_div(n, kTile);
+        p1 = (int)(nt * (nt + 1) / 2);
+    }
+    static const int groups = [] {
+        const char* e = std::getenv("FGFRFT_DS_GROUPS");
+        return e ? std::atoi(e) : 4;
+    }();
+    switch (ac * 10 + (groups == 2 ? 2 : 4)) {
+        case 12: return dsynth_launch<1, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        case 14: return dsynth_launch<1, 4>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        case 22: return dsynth_launch<2, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        case 24: return dsynth_launch<2, 4>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        case 42:
+        case 44: return dsynth_launch<4, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace fgb

@@ -41,7 +41,6 @@ size_t packed_scale_elems(int n, int l) {
 // both tiles in one 10 KB record at ((p * L + k - 1) * 2 + slot) * 5120 bytes, slot 0 = (I,J),
 // slot 1 = (J,I) (a diagonal tile is stored in both slots), scales at (p * L + k - 1) * 2 + slot.
 // A CTA walking a pair streams one contiguous L * 10 KB region, one bulk copy per power.
-__host__ __device__ __forceinline__ int64_t pairs_before(int64_t I, int64_t nt) { return I * nt - I * (I - 1) / 2; }
 
 // One CTA per tile of every power: grid = l * ntiles, 256 threads x 4 elements.
 __global__ void __launch_bounds__(256) pack_tiles_kernel(const double* __restrict__ slabs, int64_t slab_elems,
@@ -95,19 +94,6 @@ cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, dou
     pack_tiles_kernel<<<(unsigned)(ntiles * l), 256, 0, stream>>>((const double*)slabs, ntiles * kTileElems, nt, l,
                                                                   (unsigned char*)packed, scales);
     return cudaGetLastError();
-}
-
-// I-major enumeration of the tile pairs (I <= J): row I's pairs are contiguous, so the pairs
-// whose smaller tile index lies in [I0, I1) -- everything that completes rows [32 I0, 32 I1) of
-// Q -- are one index range [pairs_before(I0), pairs_before(I1)).
-__device__ __forceinline__ void pair_of_imajor(int p, int nt, int& I, int& J) {
-    const double b = 2.0 * nt + 1.0;
-    int i = (int)((b - sqrt(b * b - 8.0 * p)) * 0.5);
-    i = max(0, min(i, nt - 1));
-    while (i > 0 && pairs_before(i, nt) > p) --i;
-    while (i + 1 < nt && pairs_before(i + 1, nt) <= p) ++i;
-    I = i;
-    J = i + (int)(p - pairs_before(i, nt));
 }
 
 int64_t packed_pairs_before(int I, int nt) { return pairs_before(I, nt); }

@@ -195,7 +195,7 @@ def test_config3_headline_step_full_batch_dense_oracle():
             o = O.PowerCache(cfg.f, cfg.l, memory_budget=1 << 40, real_recursion=True)
             for a in (0.37, -1.3):
                 loss, dl, y = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
-                assert cache.route_info()[0] == 3
+                assert cache.route_info()[0] in (3, 4)  # packed step: FP64-decode or tensor-core synthesis
                 q = O.fgfrft_matrix(o, a, nthreads=os.cpu_count() or 1)
                 yr = q @ cfg.x
                 r = yr - cfg.x_clean
@@ -249,7 +249,7 @@ def test_config4_packed_step_and_pair_shard_world1():
         single = []
         for a in alphas:
             loss, dl, y = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
-            assert cache.route_info()[0] == 3
+            assert cache.route_info()[0] in (3, 4)  # packed step: FP64-decode or tensor-core synthesis
             single.append((loss[0], dl[0]))
             cols = np.random.default_rng(int(a * 100)).choice(b, size=64, replace=False)
             yr = O.series_apply_recursive(cfg.f, a, cfg.l, np.asfortranarray(cfg.x[:, cols]))

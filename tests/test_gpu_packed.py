@@ -1,8 +1,12 @@
-"""GPU parity of the packed step route (csrc/packed.cu): one, two or four orders over a real
-cache with a large signal batch -- Q(a), dQ/da from the packed (48-bit fixed-point) slabs, one
-Ozaki GEMM [Y; dY] = [Q; dQ] X, loss and dL/da from one elementwise pass -- against the oracle
-(transform.hpp:111-148, learn.hpp:88-92 form) at the 1e-10 relative bar of the north star.
+"""GPU parity of the packed step route (csrc/packed.cu, csrc/ozgemm.cu dsynth_kernel): one, two
+or four orders over a real cache with a large signal batch -- Q(a), dQ/da synthesised either from
+the packed 40-bit fixed-point slabs (FP64 decode, route 3) or on the INT8 tensor cores from the
+element-row digit cache (route 4), one Ozaki GEMM [Y; dY] = [Q; dQ] X, loss and dL/da from one
+elementwise pass -- against the oracle (transform.hpp:111-148, learn.hpp:88-92 form) at the 1e-10
+relative bar of the north star. Every test runs under both synthesis engines (FGFRFT_DSYNTH).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -12,7 +16,7 @@ import prep
 
 pytestmark = pytest.mark.gpu
 
-PACKED_ROUTE = 3
+ROUTES = {"packed": 3, "dsynth": 4}
 
 
 def rel(a, b):
@@ -25,21 +29,32 @@ def _graph_f(n, seed):
     return prep.gft_from_shift(prep.laplacian(prep.knn_graph(pts, 8)))
 
 
+@pytest.fixture(scope="module", params=["packed", "dsynth"])
+def engine(request):
+    old = os.environ.get("FGFRFT_DSYNTH")
+    os.environ["FGFRFT_DSYNTH"] = "1" if request.param == "dsynth" else "0"
+    yield ROUTES[request.param]
+    if old is None:
+        os.environ.pop("FGFRFT_DSYNTH", None)
+    else:
+        os.environ["FGFRFT_DSYNTH"] = old
+
+
 @pytest.fixture(scope="module")
-def problem():
+def problem(engine):
     n, l, b = 1024, 24, 80
     f = _graph_f(n, 11)
     rng = np.random.default_rng(5)
     x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
     xc = x + 0.1 * rng.standard_normal((n, b))
-    return f, l, x, xc, fg.PowerCache(f, l, memory_budget=8 << 30), O.PowerCache(f, l)
+    return f, l, x, xc, fg.PowerCache(f, l, memory_budget=8 << 30), O.PowerCache(f, l), engine
 
 
 @pytest.mark.parametrize("alphas", [[0.37], [-1.3], [0.25, 1.75], [2.0]])
 def test_packed_mse_step_matches_oracle(problem, alphas):
-    f, l, x, xc, g, o = problem
+    f, l, x, xc, g, o, route = problem
     loss, dl, y = fg.mse_step(g, alphas, x, xc, want_y=True)
-    assert g.route_info()[0] == PACKED_ROUTE
+    assert g.route_info()[0] == route
     for i, a in enumerate(alphas):
         lr, dr, yr = O.dlda_mse(o, a, x, xc)
         assert rel(y[i], yr) <= 1e-10
@@ -52,7 +67,7 @@ def test_packed_mse_step_matches_oracle(problem, alphas):
 @pytest.mark.parametrize("alphas,inverse", [([0.37], False), ([0.37], True), ([0.1, 0.9], False),
                                             ([0.1, 0.5, 1.2, -0.7], True)])
 def test_packed_apply_matches_oracle(problem, alphas, inverse):
-    f, l, x, xc, g, o = problem
+    f, l, x, xc, g, o, route = problem
     y = fg.apply_series(g, alphas, x, inverse=inverse)
     for i, a in enumerate(alphas):
         q = O.fgfrft_matrix(o, a)
@@ -61,21 +76,22 @@ def test_packed_apply_matches_oracle(problem, alphas, inverse):
 
 
 def test_packed_apply_truncation(problem):
-    f, l, x, xc, g, o = problem
+    f, l, x, xc, g, o, route = problem
     y = fg.apply_series(g, [0.6], x, truncation=9)
     assert rel(y[0], O.fgfrft_matrix(o, 0.6, truncation=9) @ x) <= 1e-10
 
 
 def test_packed_integer_order_is_the_power(problem):
-    f, l, x, xc, g, o = problem
+    f, l, x, xc, g, o, route = problem
     y = fg.apply_series(g, [3.0, 0.0], x)
-    # c_k(3) is an exact Kronecker row (sinc.hpp:16): Y = P_3 X up to the 40-bit packing of P_3
-    # (<= 2^-39 of each tile's largest entry) and the Ozaki product
-    assert rel(y[0], o.power(3) @ x) <= 2e-11
+    # c_k(3) is an exact Kronecker row (sinc.hpp:16): Y = P_3 X up to the 40-bit quantisation of P_3
+    # in the cache (<= 2^-39 of each tile's / element row's largest entry) and the 5-digit (39.9-bit)
+    # Ozaki product -- two ~2^-40 roundings, ~2e-11 relative; the series bar is 1e-10
+    assert rel(y[0], o.power(3) @ x) <= 5e-11
     assert rel(y[1], x) <= 1e-13
 
 
-def test_packed_route_respects_memory_budget():
+def test_packed_route_respects_memory_budget(engine):
     """The packed slabs are auxiliary: with a budget that only covers the reference count
     L n^2 16 bytes (transform.hpp:46-53) they are not built and the exact route runs."""
     n, l, b = 512, 8, 40
@@ -86,9 +102,9 @@ def test_packed_route_respects_memory_budget():
     tight = fg.PowerCache(f, l, memory_budget=l * n * n * 16)
     roomy = fg.PowerCache(f, l, memory_budget=1 << 30)
     lt, dt_, _ = fg.mse_step(tight, [0.4], x, xc)
-    assert tight.route_info()[0] != PACKED_ROUTE
+    assert tight.route_info()[0] not in (3, 4)
     lr, dr, _ = fg.mse_step(roomy, [0.4], x, xc)
-    assert roomy.route_info()[0] == PACKED_ROUTE
+    assert roomy.route_info()[0] == engine
     assert abs(lt[0] - lr[0]) <= 1e-10 * lr[0]
     assert abs(dt_[0] - dr[0]) <= 1e-9 * max(1.0, abs(dr[0]))
 
@@ -97,7 +113,7 @@ def test_packed_host_and_device_steps_agree(problem):
     """fgfrft_mse_step (host buffers: X copied in column chunks overlapping the synthesis) and
     fgfrft_mse_step_dev (device-resident X) run the same products: identical results."""
     import torch
-    f, l, x, xc, g, o = problem
+    f, l, x, xc, g, o, route = problem
     n, b = x.shape
     al = np.array([0.81, -0.4])
     loss_h, dl_h, _ = fg.mse_step(g, al, x, xc)
@@ -140,3 +156,32 @@ def test_node_sweep_snaps_order_zero_and_narrow_sweeps_fall_back():
         _, dc = O.sinc_coeffs(a, l)
         assert abs(loss[i] - lr) <= 1e-10 * lr
         assert abs(dl[i] - dr) <= 1e-10 * np.sum(np.abs(dc * s))
+
+
+def test_tensor_core_synthesis_matches_packed_synthesis():
+    """The two synthesis engines on one cache: Y = Q(a) X from the digit cache (5 digits per element
+    row over the powers) and from the packed 40-bit tiles agree to their common quantisation
+    (~2^-40 of the entries), odd n (ragged edge tiles) and a truncated series included."""
+    n, l, b = 1000, 20, 80
+    f = _graph_f(n, 31)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((n, b)) + 1j * rng.standard_normal((n, b))
+    o = O.PowerCache(f, l)
+    old = os.environ.get("FGFRFT_DSYNTH")
+    try:
+        out = {}
+        for eng in ("0", "1"):
+            os.environ["FGFRFT_DSYNTH"] = eng
+            g = fg.PowerCache(f, l, memory_budget=8 << 30)
+            out[eng] = (fg.apply_series(g, [0.43, -1.2], x), fg.apply_series(g, [0.8], x, truncation=7))
+        for a, ya, yb in zip([0.43, -1.2], out["0"][0], out["1"][0]):
+            yr = O.fgfrft_matrix(o, a) @ x
+            assert rel(yb, yr) <= 1e-10 and rel(ya, yr) <= 1e-10
+            assert rel(ya, yb) <= 1e-10
+        yr = O.fgfrft_matrix(o, 0.8, truncation=7) @ x
+        assert rel(out["1"][1][0], yr) <= 1e-10 and rel(out["0"][1][0], yr) <= 1e-10
+    finally:
+        if old is None:
+            os.environ.pop("FGFRFT_DSYNTH", None)
+        else:
+            os.environ["FGFRFT_DSYNTH"] = old

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--config", default="3")
     ap.add_argument("--c64", action="store_true")
     ap.add_argument("--pshard", action="store_true", help="the pair-shard step at world 1 (NCCL communicator)")
+    ap.add_argument("--sweep", default="", help="env settings to time in turn, e.g. "
+                    "'FGFRFT_PIPE_SHELLS=1;FGFRFT_PIPE_SHELLS=4&FGFRFT_PIPE_GEMM_CTAS=100'")
+    ap.add_argument("--trace", action="store_true", help="print the last step's launch timeline (sweep mode)")
     args = ap.parse_args()
     t0 = time.perf_counter()
     cfg = prep.config3() if args.config == "3" else prep.config4()
@@ -62,6 +65,44 @@ def main():
         fg._check(lib.fgfrft_mse_step_dev(cache.handle, al[i & 1].ctypes.data, 1, x.data_ptr(), xc.data_ptr(), b,
                                           None, loss.data_ptr(), dl.data_ptr()))
 
+    if args.sweep:
+        for setting in args.sweep.split(";"):
+            for kv in filter(None, setting.split("&")):
+                k, v = kv.split("=")
+                if v:
+                    os.environ[k] = v
+                else:
+                    os.environ.pop(k, None)
+            with torch.cuda.stream(stream):
+                for i in range(args.warmup):
+                    step(i)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.steps):
+                step(i)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            fg.profile_enable(True)
+            fg.profile_read(reset=True)
+            with torch.cuda.stream(stream):
+                for i in range(args.steps):
+                    step(i)
+            torch.cuda.synchronize()
+            tr = fg.profile_trace()
+            per = len(tr) // args.steps
+            trace = [(c, round(a, 3), round(b, 3)) for c, a, b in tr[-per:]]
+            t00 = trace[0][1] if trace else 0.0
+            trace = [(c, round(a - t00, 3), round(b - t00, 3)) for c, a, b in trace]
+            prof = {k: round(v[0] / args.steps, 4) for k, v in fg.profile_read(reset=True).items() if v[1]}
+            fg.profile_enable(False)
+            if args.trace:
+                print(json.dumps({"setting": setting, "trace": trace}), flush=True)
+            print(json.dumps({"setting": setting, "ms_per_step": ms, "classes": prof,
+                              "route": cache.route_info()[0] if not args.pshard else None,
+                              "loss": float(loss[0]), "dlda": float(dl[0])}), flush=True)
+        return
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
             step(i)
