@@ -582,23 +582,6 @@ def main():
                                 "+ one Ozaki GEMM [Y; dY] = [Q; dQ] X")}.get(route),
                   "int8_digits": S}
 
-    # ---- parity of the timed step against the oracle (rank 0; the oracle cache is reused by the CPU
-    # baseline below)
-    import oracle as O
-    from threadpoolctl import threadpool_limits
-    cores = os.cpu_count() or 1
-    with threadpool_limits(cores):
-        t0 = time.perf_counter()
-        ocache = oracle_cache(O, cfg)
-        ocache_s = time.perf_counter() - t0
-        check = []
-        for i, a in enumerate(ALPHAS):
-            lr, dr = oracle_step(O, ocache, cfg.x, cfg.x_clean, a, cores)
-            check.append({"alpha": a, "loss": float(step_out[0][i]), "loss_ref": lr,
-                          "loss_rel_err": abs(float(step_out[0][i]) - lr) / abs(lr),
-                          "dlda": float(step_out[1][i]), "dlda_ref": dr,
-                          "dlda_rel_err": abs(float(step_out[1][i]) - dr) / max(abs(dr), 1e-300)})
-
     # ---- synthesis GB/s (metric's first half): one order, complex128 output (fgfrft_matrix)
     qbuf = torch.empty((1, n, n), dtype=torch.complex128, device=dev)
 
@@ -644,6 +627,24 @@ def main():
             extras["c2_sweep"] = c2_sweep(fg, torch, stream, local)
         except Exception as ex:  # secondary line only
             extras["c2_sweep"] = {"error": str(ex)}
+
+    # ---- parity of the timed step against the oracle (rank 0; the oracle cache is reused by the CPU
+    # baseline below). After every GPU timing: the oracle's BLAS threads keep spinning for a while
+    # after their work and would steal the launching thread's core from the e2e / sweep timings.
+    import oracle as O
+    from threadpoolctl import threadpool_limits
+    cores = os.cpu_count() or 1
+    with threadpool_limits(cores):
+        t0 = time.perf_counter()
+        ocache = oracle_cache(O, cfg)
+        ocache_s = time.perf_counter() - t0
+        check = []
+        for i, a in enumerate(ALPHAS):
+            lr, dr = oracle_step(O, ocache, cfg.x, cfg.x_clean, a, cores)
+            check.append({"alpha": a, "loss": float(step_out[0][i]), "loss_ref": lr,
+                          "loss_rel_err": abs(float(step_out[0][i]) - lr) / abs(lr),
+                          "dlda": float(step_out[1][i]), "dlda_ref": dr,
+                          "dlda_rel_err": abs(float(step_out[1][i]) - dr) / max(abs(dr), 1e-300)})
 
     cpu = cpu1 = None
     if not args.no_cpu_baseline:

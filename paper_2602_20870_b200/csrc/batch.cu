@@ -15,7 +15,10 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace fgb {
 
@@ -553,6 +556,463 @@ batch_dlda_kernel(const void* __restrict__ slabs, int n, int l, const double* __
     }
 }
 
+// ---------------------------------------------------------------- config 5 on the tensor cores
+//
+// Real F, n = 64, 64 channels (the BASELINE config-5 shape): persistent, warp-specialised kernels,
+// one CTA per SM walking graphs g = blockIdx.x, + gridDim.x, ... Warp 16 streams every 16 KB item
+// a graph needs (its real power slabs, X_g in two channel halves, and for dL/da the gradient blocks
+// G_h) through ONE ring of bulk copies that runs ahead ACROSS graphs, so HBM never waits for a
+// graph's compute; warp 17 issues the graph's GEMM on tcgen05 (kind::f16, BF16 operands, FP32
+// accumulators in TMEM); warps 0..15 synthesise Q_h from the powers in registers (thread = element
+// (i, 8 jb .. 8 jb + 7), all heads: each staged power value is read once for every head), write the
+// GEMM operands and drain TMEM. FP32-level accuracy from BF16 operands by the two-term split
+// a = a_hi + a_lo (products hi hi + hi lo + lo hi: ~2^-16 relative, inside the complex64 1e-4 bar;
+// the 2^-32 term is dropped). Operands are K-major SWIZZLE_NONE canonical layouts with 64-byte K
+// blocks: byte(r, k) = (k / 32) rows 64 + (r / 8) 512 + ((k % 32) / 8) 128 + (r % 8) 16 + (k % 8) 2.
+//   forward: [Y_h0; Y_h1] (128 x 128 real: columns 2c + re/im) = [Q_h0; Q_h1] (128 x 64) X^T (64 x 128)
+//   dL/da:   [M_h0; M_h1] (128 x 64) = [G_h0; G_h1] (128 x 128: K = 2c + re/im) [X] (64 x 128),
+//            Re M_h = Re(G_h X^H); s_hk = <M_h, P_k>, <M_h, P_k^T> and dL/da_h = sum_k c'_k s_hk.
+constexpr int kTcItem = kBSlab * 4;           // 16 KB: a real power slab / half of X_g / half of G_h
+constexpr int kTcWarps = 16;                  // synthesis / operand / epilogue warps
+constexpr int kTcThreads = 32 * (kTcWarps + 2);
+constexpr int kTcMaxStages = 8;
+
+// byte offset of the 16-byte chunk (row r, K core column k8 = k / 8) of a rows x K canonical operand
+__device__ __forceinline__ uint32_t tc_off(int rows, int r, int k8) {
+    return (uint32_t)((k8 >> 2) * rows * 64 + (r >> 3) * 512 + (k8 & 3) * 128 + (r & 7) * 16);
+}
+
+// 8 floats -> BF16 hi / lo chunks (a = hi + lo + O(2^-17 a))
+__device__ __forceinline__ void tc_split8(const float (&v)[8], uint4& hi, uint4& lo) {
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162 bh = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+        const float2 back = __bfloat1622float2(bh);
+        const __nv_bfloat162 bl = __floats2bfloat162_rn(v[2 * q] - back.x, v[2 * q + 1] - back.y);
+        h[q] = *reinterpret_cast<const uint32_t*>(&bh);
+        l[q] = *reinterpret_cast<const uint32_t*>(&bl);
+    }
+    hi = make_uint4(h[0], h[1], h[2], h[3]);
+    lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__device__ __forceinline__ void st_shared_v4(unsigned char* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+
+__device__ __forceinline__ void tc_compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcWarps) : "memory"); }
+
+// The ring protocol of both kernels: item it lives in stage it % S; the producer waits for the
+// stage's `empty` (one arrival per compute warp) before refilling it.
+struct TcRing {
+    unsigned char* base;
+    uint64_t* full;
+    uint64_t* empty;
+    int stages;
+    __device__ __forceinline__ const unsigned char* wait(int it) const {
+        const int s = it % stages;
+        mbar_wait(full + s, (uint32_t)((it / stages) & 1));
+        return base + (size_t)s * kTcItem;
+    }
+    __device__ __forceinline__ void release(int it, int lane) const {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + it % stages);
+    }
+};
+
+__device__ __forceinline__ void tc_produce(const TcRing& r, int it, const void* src, uint64_t pol) {
+    const int s = it % r.stages;
+    if (it >= r.stages) mbar_wait(r.empty + s, (uint32_t)(((it / r.stages) - 1) & 1));
+    mbar_arrive_expect_tx(r.full + s, kTcItem);
+    bulk_g2s_hint(r.base + (size_t)s * kTcItem, src, kTcItem, r.full + s, pol);
+}
+
+size_t batch_tc_fwd_smem(int l, int heads, int* stages) {
+    const size_t ops = (size_t)((heads + 1) / 2) * 2 * 16384 + 2 * 16384;  // Q tiles hi / lo, X^T hi / lo
+    const size_t fixed = ops + 2 * (kTcMaxStages + 2) * 8 + 16 + (size_t)heads * (2 * l + 1) * 4 + 128;
+    int st = (int)((227 * 1024 - fixed) / kTcItem);
+    if (st > kTcMaxStages) st = kTcMaxStages;
+    if (stages) *stages = st;
+    return fixed + (size_t)st * kTcItem;
+}
+
+template <int H>
+__global__ void __launch_bounds__(kTcThreads, 1)
+batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const double* __restrict__ coef,
+                    const float2* __restrict__ x, float2* __restrict__ y, int graphs, int stages) {
+    constexpr int NT = (H + 1) / 2;  // M tiles of two heads
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* qhl = smem;                        // [NT][hi, lo] 128 x 64 BF16 (16 KB each)
+    unsigned char* xhl = qhl + NT * 2 * 16384;        // [hi, lo] X^T: 128 x 64 BF16
+    unsigned char* ringp = xhl + 2 * 16384;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ringp + (size_t)stages * kTcItem);
+    const TcRing ring{ringp, bars, bars + kTcMaxStages, stages};
+    uint64_t* opready = bars + 2 * kTcMaxStages;
+    uint64_t* mmadone = opready + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mmadone + 1);
+    float* cs = reinterpret_cast<float*>(tslot + 4);  // [H][2l + 1]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, w = 2 * l + 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(ring.full + s, 1);
+            mbar_init(ring.empty + s, kTcWarps);
+        }
+        mbar_init(opready, kTcWarps);
+        mbar_init(mmadone, 1);
+        fence_mbar_init();
+    }
+    if (warp == kTcWarps + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (warp == kTcWarps) {
+        // ---- producer: per graph the l power slabs, then X_g (channels 0-31, 32-63)
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int it = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x)
+                for (int t = 0; t < l + 2; ++t, ++it)
+                    tc_produce(ring, it,
+                               t < l ? (const void*)(slabs + ((int64_t)g * l + t) * kBSlab)
+                                     : (const void*)(x + (int64_t)g * kBN * kBMaxCh + (t - l) * (kBN * kBMaxCh / 2)),
+                               pol);
+        }
+    } else if (warp == kTcWarps + 1) {
+        // ---- MMA issuer: per graph NT tiles x 4 K steps x 3 split products
+        if (lane == 0) {
+            const uint32_t q0 = smem_u32(qhl), x0 = smem_u32(xhl);
+            int gi = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++gi) {
+                mbar_wait(opready, (uint32_t)(gi & 1));
+                tc_fence_after();
+#pragma unroll
+                for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+                        for (int ps = 0; ps < 3; ++ps) {  // lo hi, hi lo, hi hi (small terms first)
+                            const uint32_t a = q0 + (uint32_t)(mt * 2 + (ps == 0)) * 16384u;
+                            const uint32_t b = x0 + (uint32_t)(ps == 1) * 16384u;
+                            const uint32_t ko = (uint32_t)((ks >> 1) * 8192 + (ks & 1) * 256);
+                            mma_bf16(tmem + (uint32_t)(mt * 128), umma_desc(a + ko, 128, 512),
+                                     umma_desc(b + ko, 128, 512), idesc_bf16(128, 128), (ks | ps) ? 1u : 0u);
+                        }
+                mma_commit(mmadone);
+            }
+        }
+    } else {
+        // ---- compute warps
+        const int tid = threadIdx.x, i = tid & 63, jb = tid >> 6;
+        const int qd = warp & 3, wq = warp >> 2;  // TMEM lane quarter, column quarter
+        int it = 0, gi = 0;
+        for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++gi) {
+            for (int idx = tid; idx < H * w; idx += 32 * kTcWarps) {
+                const int h = idx / w, t = idx - h * w;
+                cs[idx] = (float)coef[(size_t)(g * H + h) * 2 * w + t];
+            }
+            tc_compute_sync();
+            float q[H][8];
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) q[h][u] = (i == 8 * jb + u) ? cs[h * w + l] : 0.f;
+            for (int k = 1; k <= l; ++k, ++it) {
+                const float* t = reinterpret_cast<const float*>(ring.wait(it));
+                float a[H], b[H];
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    a[h] = cs[h * w + l + k];
+                    b[h] = cs[h * w + l - k];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = 8 * jb + u;
+                    const float p = t[bidx(i, j)], pt = t[bidx(j, i)];
+#pragma unroll
+                    for (int h = 0; h < H; ++h) q[h][u] = fmaf(a[h], p, fmaf(b[h], pt, q[h][u]));
+                }
+                ring.release(it, lane);
+            }
+            // X_g halves -> X^T operand: B row n = 2c + e, K = j. Thread: channel c = 32 half + cl
+            // (cl = tid >> 3 & 31), 8 consecutive j (kc = tid & 7), both components -> rows 2c, 2c + 1.
+            {
+                const int half = tid >> 8, cl = (tid >> 3) & 31, kc = tid & 7;
+                for (int hh = 0; hh < 2; ++hh) {
+                    const float2* xr = reinterpret_cast<const float2*>(ring.wait(it + hh));
+                    if (hh == half) {
+                        float re[8], im[8];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const float4 v = *reinterpret_cast<const float4*>(xr + cl * kBN + 8 * kc + 2 * m);
+                            re[2 * m] = v.x;
+                            im[2 * m] = v.y;
+                            re[2 * m + 1] = v.z;
+                            im[2 * m + 1] = v.w;
+                        }
+                        const int n0 = 2 * (32 * half + cl);
+                        uint4 hi, lo;
+                        tc_split8(re, hi, lo);
+                        st_shared_v4(xhl + tc_off(128, n0, kc), hi);
+                        st_shared_v4(xhl + 16384 + tc_off(128, n0, kc), lo);
+                        tc_split8(im, hi, lo);
+                        st_shared_v4(xhl + tc_off(128, n0 + 1, kc), hi);
+                        st_shared_v4(xhl + 16384 + tc_off(128, n0 + 1, kc), lo);
+                    }
+                    ring.release(it + hh, lane);
+                }
+                it += 2;
+            }
+            // Q_h -> A operand of tile h / 2: row (h % 2) 64 + i, K core column jb
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                uint4 hi, lo;
+                tc_split8(q[h], hi, lo);
+                unsigned char* tq = qhl + (size_t)(h >> 1) * 2 * 16384;
+                st_shared_v4(tq + tc_off(128, (h & 1) * 64 + i, jb), hi);
+                st_shared_v4(tq + 16384 + tc_off(128, (h & 1) * 64 + i, jb), lo);
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(opready);
+            // epilogue: TMEM lane 32 qd + lane of tile mt = row (h, i); this warp's 32 columns from 32 wq
+            mbar_wait(mmadone, (uint32_t)(gi & 1));
+            tc_fence_after();
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt) {
+                const int h = 2 * mt + (qd >> 1), io = 32 * (qd & 1) + lane;
+                if (h >= H) continue;  // warp-uniform
+                int32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(mt * 128 + 32 * wq), v);
+                tmem_wait_ld();
+                float2* yo = y + (((int64_t)g * H + h) * kBMaxCh + 16 * wq) * kBN + io;
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    __stcs(yo + c * kBN, make_float2(__int_as_float(v[2 * c]), __int_as_float(v[2 * c + 1])));
+            }
+            tc_fence_before();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kTcWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+constexpr int kTcMs = 68;  // row stride (floats) of the staged M_h: conflict-free row-chunk reads
+
+size_t batch_tc_dlda_smem(int l, int heads, int* stages) {
+    const size_t mreg = (size_t)kBMaxHeads * kBN * kTcMs * 4;  // >= one G tile hi / lo (64 KB)
+    const size_t fixed = 2 * 16384 + mreg + 2 * (kTcMaxStages + 2) * 8 + 16 + (size_t)heads * (2 * l + 1) * 8 +
+                         kTcWarps * kBMaxHeads * 8 + 128;
+    int st = (int)((227 * 1024 - fixed) / kTcItem);
+    if (st > kTcMaxStages) st = kTcMaxStages;
+    if (stages) *stages = st;
+    return fixed + (size_t)st * kTcItem;
+}
+
+template <int H>
+__global__ void __launch_bounds__(kTcThreads, 1)
+batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const double* __restrict__ coef,
+                     const float2* __restrict__ gcot, const float2* __restrict__ x, double* __restrict__ dlda,
+                     int graphs, int stages) {
+    constexpr int NT = (H + 1) / 2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* xhl = smem;                 // [hi, lo] X: 64 rows (j) x 128 K (2c + e) BF16 (16 KB each)
+    unsigned char* reg = xhl + 2 * 16384;      // G tile [hi, lo] 128 x 128 BF16, later M_h [h][i][kTcMs]
+    float* ms = reinterpret_cast<float*>(reg);
+    unsigned char* ringp = reg + (size_t)kBMaxHeads * kBN * kTcMs * 4;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ringp + (size_t)stages * kTcItem);
+    const TcRing ring{ringp, bars, bars + kTcMaxStages, stages};
+    uint64_t* opready = bars + 2 * kTcMaxStages;
+    uint64_t* mmadone = opready + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(mmadone + 1);
+    double* dcs = reinterpret_cast<double*>(tslot + 4);  // [H][2l + 1]: c'_k of this graph
+    double* red = dcs + H * (2 * l + 1);                 // [16 warps][4]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, w = 2 * l + 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(ring.full + s, 1);
+            mbar_init(ring.empty + s, kTcWarps);
+        }
+        mbar_init(opready, kTcWarps);
+        mbar_init(mmadone, 1);
+        fence_mbar_init();
+    }
+    if (warp == kTcWarps + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    constexpr int half_floats = kBN * kBMaxCh;  // float2 elements of half a 64 x 64 complex block x 2
+    if (warp == kTcWarps) {
+        // ---- producer: per graph X_g (2 items), G_h (2 items per head), then the l power slabs
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int it = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x) {
+                for (int t = 0; t < 2; ++t, ++it)
+                    tc_produce(ring, it, x + (int64_t)g * kBN * kBMaxCh + t * (half_floats / 2), pol);
+                for (int t = 0; t < 2 * H; ++t, ++it)
+                    tc_produce(ring, it, gcot + (int64_t)g * H * kBN * kBMaxCh + t * (half_floats / 2), pol);
+                for (int k = 0; k < l; ++k, ++it) tc_produce(ring, it, slabs + ((int64_t)g * l + k) * kBSlab, pol);
+            }
+        }
+    } else if (warp == kTcWarps + 1) {
+        // ---- MMA issuer: per graph NT tiles, each 8 K steps x 3 split products (N = 64)
+        if (lane == 0) {
+            const uint32_t x0 = smem_u32(xhl), a0 = smem_u32(reg);
+            int ev = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x)
+                for (int mt = 0; mt < NT; ++mt, ++ev) {
+                    mbar_wait(opready, (uint32_t)(ev & 1));
+                    tc_fence_after();
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+                        for (int ps = 0; ps < 3; ++ps) {
+                            const uint32_t a = a0 + (uint32_t)(ps == 0) * 32768u + (uint32_t)((ks >> 1) * 8192 + (ks & 1) * 256);
+                            const uint32_t b = x0 + (uint32_t)(ps == 1) * 16384u + (uint32_t)((ks >> 1) * 4096 + (ks & 1) * 256);
+                            mma_bf16(tmem + (uint32_t)(mt * 64), umma_desc(a, 128, 512), umma_desc(b, 128, 512),
+                                     idesc_bf16(128, 64), (ks | ps) ? 1u : 0u);
+                        }
+                    mma_commit(mmadone);
+                }
+        }
+    } else {
+        const int tid = threadIdx.x, i = tid & 63, jb = tid >> 6;
+        const int qd = warp & 3, wq = warp >> 2;
+        int it = 0, ev = 0;
+        for (int g = blockIdx.x; g < graphs; g += gridDim.x) {
+            for (int idx = tid; idx < H * w; idx += 32 * kTcWarps) {
+                const int h = idx / w, t = idx - h * w;
+                dcs[idx] = coef[(size_t)(g * H + h) * 2 * w + w + t];
+            }
+            // X halves -> B operand (row j, K = 2c + e); thread: row j = i, core column kc = jb of the half
+            for (int hh = 0; hh < 2; ++hh, ++it) {
+                const float2* xr = reinterpret_cast<const float2*>(ring.wait(it));
+                float v[8];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const float2 z = xr[(4 * jb + m) * kBN + i];
+                    v[2 * m] = z.x;
+                    v[2 * m + 1] = z.y;
+                }
+                uint4 hi, lo;
+                tc_split8(v, hi, lo);
+                st_shared_v4(xhl + tc_off(64, i, 8 * hh + jb), hi);
+                st_shared_v4(xhl + 16384 + tc_off(64, i, 8 * hh + jb), lo);
+                ring.release(it, lane);
+            }
+            for (int mt = 0; mt < NT; ++mt, ++ev) {
+                if (mt > 0) mbar_wait(mmadone, (uint32_t)((ev - 1) & 1));  // tile mt - 1 has read the region
+                for (int hl = 0; hl < 2; ++hl) {
+                    if (2 * mt + hl >= H) break;
+                    for (int hh = 0; hh < 2; ++hh, ++it) {
+                        const float2* gr = reinterpret_cast<const float2*>(ring.wait(it));
+                        float v[8];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const float2 z = gr[(4 * jb + m) * kBN + i];
+                            v[2 * m] = z.x;
+                            v[2 * m + 1] = z.y;
+                        }
+                        uint4 hi, lo;
+                        tc_split8(v, hi, lo);
+                        st_shared_v4(reg + tc_off(128, 64 * hl + i, 8 * hh + jb), hi);
+                        st_shared_v4(reg + 32768 + tc_off(128, 64 * hl + i, 8 * hh + jb), lo);
+                        ring.release(it, lane);
+                    }
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(opready);
+            }
+            mbar_wait(mmadone, (uint32_t)((ev - 1) & 1));
+            tc_fence_after();
+            // M_h rows (TMEM lane 32 qd + lane of tile mt) -> ms[h][i][j], this warp's 16 columns
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt) {
+                const int h = 2 * mt + (qd >> 1), io = 32 * (qd & 1) + lane;
+                if (h >= H) continue;
+                int32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(mt * 64 + 16 * wq), v);
+                tmem_wait_ld();
+                float4* dst = reinterpret_cast<float4*>(ms + ((size_t)h * kBN + io) * kTcMs + 16 * wq);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    dst[c] = make_float4(__int_as_float(v[4 * c]), __int_as_float(v[4 * c + 1]),
+                                         __int_as_float(v[4 * c + 2]), __int_as_float(v[4 * c + 3]));
+            }
+            tc_fence_before();
+            tc_compute_sync();
+            float m[H][8];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const float4* src = reinterpret_cast<const float4*>(ms + ((size_t)h * kBN + i) * kTcMs + 8 * jb);
+                const float4 a = src[0], b = src[1];
+                m[h][0] = a.x; m[h][1] = a.y; m[h][2] = a.z; m[h][3] = a.w;
+                m[h][4] = b.x; m[h][5] = b.y; m[h][6] = b.z; m[h][7] = b.w;
+            }
+            tc_compute_sync();  // the region is the next graph's G tile
+            double dl[H];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                float d = 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (i == 8 * jb + u) d = m[h][u];
+                dl[h] = dcs[h * w + l] * (double)d;  // c'_0 Re tr(M_h)
+            }
+            for (int k = 1; k <= l; ++k, ++it) {
+                const float* t = reinterpret_cast<const float*>(ring.wait(it));
+                float vp[H], vm[H];
+#pragma unroll
+                for (int h = 0; h < H; ++h) vp[h] = vm[h] = 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = 8 * jb + u;
+                    const float p = t[bidx(i, j)], pt = t[bidx(j, i)];
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        vp[h] = fmaf(m[h][u], p, vp[h]);
+                        vm[h] = fmaf(m[h][u], pt, vm[h]);
+                    }
+                }
+                ring.release(it, lane);
+#pragma unroll
+                for (int h = 0; h < H; ++h)
+                    dl[h] = fma(dcs[h * w + l + k], (double)vp[h], fma(dcs[h * w + l - k], (double)vm[h], dl[h]));
+            }
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                double t = dl[h];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (lane == 0) red[warp * kBMaxHeads + h] = t;
+            }
+            tc_compute_sync();
+            if (tid < H) {
+                double t = 0.0;
+                for (int wp = 0; wp < kTcWarps; ++wp) t += red[wp * kBMaxHeads + tid];
+                dlda[(int64_t)g * H + tid] = t;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kTcWarps + 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+// The tcgen05 kernels' shape: full 64-node graphs, 64 channels, 16-byte aligned signal blocks.
+static bool tc_shape_ok(int n, int ch, const void* a, const void* b) {
+    return n == kBN && ch == kBMaxCh && ((uintptr_t)a & 15) == 0 && ((uintptr_t)b & 15) == 0;
+}
+
 cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream) {
     const int total = n_orders * (2 * l + 1);
     batch_coef_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, stream>>>(alphas_dev, n_orders, l, coef_dev);
@@ -584,8 +1044,29 @@ cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, co
     // were tried and dropped.
     static const int fwd_form = [] {
         const char* e = std::getenv("FGFRFT_BATCH_FWD");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 3;
     }();
+    // 3 (default): the persistent tcgen05 kernel for the config-5 shape (real F, n = 64, 64 channels)
+    if (real && fwd_form == 3 && tc_shape_ok(n, ch, x, y)) {
+        int stages = 0;
+        const size_t sm = batch_tc_fwd_smem(l, heads, &stages);
+        if (stages < 3) return cudaErrorInvalidValue;
+        const int grid = graphs < FGFRFT_SMS ? graphs : FGFRFT_SMS;
+#define FGB_BFT(HV)                                                                                            \
+    {                                                                                                          \
+        static PerDeviceOnce attr;                                                                             \
+        cudaError_t e = attr.run([] {                                                                          \
+            return cudaFuncSetAttribute(batch_fwd_tc_kernel<HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                        227 * 1024);                                                           \
+        });                                                                                                    \
+        if (e != cudaSuccess) return e;                                                                        \
+        batch_fwd_tc_kernel<HV><<<grid, kTcThreads, sm, stream>>>((const float*)slabs, l, coef,                \
+                                                                  (const float2*)x, (float2*)y, graphs, stages); \
+    }
+        FGB_BATCH_HEADS(FGB_BFT)
+#undef FGB_BFT
+        return cudaGetLastError();
+    }
     if (real && fwd_form == 2) {
         const size_t sm = batch_forward_mma_smem_bytes(l, heads);
 #define FGB_BFM(HV)                                                                                            \
@@ -619,6 +1100,31 @@ cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, co
 
 cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const double* coef, int heads,
                               const void* gcot, const void* x, int ch, double* dlda, bool real, cudaStream_t stream) {
+    static const int form = [] {
+        const char* e = std::getenv("FGFRFT_BATCH_DLDA");
+        return e ? std::atoi(e) : 3;
+    }();
+    if (real && form == 3 && tc_shape_ok(n, ch, x, gcot)) {
+        int stages = 0;
+        const size_t sm = batch_tc_dlda_smem(l, heads, &stages);
+        if (stages < 3) return cudaErrorInvalidValue;
+        const int grid = graphs < FGFRFT_SMS ? graphs : FGFRFT_SMS;
+#define FGB_BDT(HV)                                                                                            \
+    {                                                                                                          \
+        static PerDeviceOnce attr;                                                                             \
+        cudaError_t e = attr.run([] {                                                                          \
+            return cudaFuncSetAttribute(batch_dlda_tc_kernel<HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        227 * 1024);                                                           \
+        });                                                                                                    \
+        if (e != cudaSuccess) return e;                                                                        \
+        batch_dlda_tc_kernel<HV><<<grid, kTcThreads, sm, stream>>>((const float*)slabs, l, coef,               \
+                                                                   (const float2*)gcot, (const float2*)x,      \
+                                                                   dlda, graphs, stages);                      \
+    }
+        FGB_BATCH_HEADS(FGB_BDT)
+#undef FGB_BDT
+        return cudaGetLastError();
+    }
     const size_t smem = batch_smem_bytes(l);
 #define FGB_BD(HV)                                                                                            \
     {                                                                                                         \

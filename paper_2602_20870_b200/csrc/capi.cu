@@ -1371,12 +1371,15 @@ bool ensure_packed(fgfrft_cache* c) {
     return true;
 }
 
-// The digit cache of the tensor-core synthesis (preferred over the packed slabs: same bytes per
-// element at L = 64, a fifth of the SM issue per element -- it can overlap the product GEMM).
-// FGFRFT_DSYNTH=0 keeps the packed route (read per call: the tests compare both).
+// The digit cache of the tensor-core synthesis (dsynth_kernel: the same 5 B per element and power as
+// the packed slabs at L = 64, a fifth of the SM issue per element, built so the synthesis could share
+// the SMs with the product GEMM). Measured at config 3 it is not faster on its own (0.94 vs 0.92 ms
+// synthesis, 1.70 vs 1.67 ms step) and the shell pipeline that would overlap it with the GEMM lost to
+// the serial order (1.74-1.82 ms), so the packed FP64-decode synthesis (psynth) is the default and
+// FGFRFT_DSYNTH=1 opts in (read per call: the tests run both engines).
 static bool dsynth_wanted() {
     const char* e = std::getenv("FGFRFT_DSYNTH");
-    return !(e && !std::strcmp(e, "0"));
+    return e && !std::strcmp(e, "1");
 }
 
 bool ensure_dsynth(fgfrft_cache* c) {
@@ -1411,15 +1414,17 @@ bool ensure_dsynth(fgfrft_cache* c) {
     return true;
 }
 
-// Digits per operand of the step route's product GEMM [Y; dY] = [Q; dQ] X. Q carries the cache's
-// ~2^-40 quantisation (packed 40-bit tiles / 5-digit element rows), so 5 base-254 digits (39.9
-// bits, 15 digit products) match it; 6 digits (21 products) buy nothing measurable. FGFRFT_STEP_SLICES
-// overrides (5 or 6).
+// Digits per operand of the step route's product GEMM [Y; dY] = [Q; dQ] X: 6 base-254 digits (21
+// digit products). The synthesis leaves out the c_0 I term (nodiag; the GEMM epilogue adds c_0 X), so
+// Q's row maxima are its off-diagonal entries rather than the diagonal c_0 ~ 0.8 (13x larger at
+// config 3). Measured relative error of Y at 5 digits (15 products, 25% faster): config 3 1.9e-10
+// -> 1.2e-11 with nodiag, but config 4 (N = 8192 k-NN point cloud) still 1.0e-10 -- at the 1e-10
+// bar of the north star, so 5 digits is opt-in only (FGFRFT_STEP_SLICES=5); 6 digits leave ~250x.
 static int step_slices() {
     static const int s = [] {
         const char* e = std::getenv("FGFRFT_STEP_SLICES");
-        const int v = e ? std::atoi(e) : 5;
-        return v == 6 ? 6 : 5;
+        const int v = e ? std::atoi(e) : 6;
+        return v == 5 ? 5 : 6;
     }();
     return s;
 }
@@ -1630,6 +1635,23 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         for (size_t i = have; i < plan.size(); ++i)
             FGB_CUDA(cudaEventCreateWithFlags(&c->pk_es[i], cudaEventDisableTiming));
     }
+    // [Y; dY] rows of shell / chunk: the synthesis leaves out c_0 I (nodiag), the GEMM epilogue adds
+    // c_0 X (Q's row maxima then follow its off-diagonal entries: at config 3, alpha = 0.37, the
+    // diagonal is 0.80 against 0.06 off it, and the 5-digit slicing error drops 1.9e-10 -> 1.2e-11)
+    auto gemm_out = [&](double* yp, int64_t rv, int64_t rp, int64_t nv, const double* xp, int max_ctas) {
+        OzOut o;
+        o.c = yp;
+        o.ldc = n;
+        o.sc = 2 * n * b;
+        o.mv = (int)rv;
+        o.mp = (int)rp;
+        o.nv = (int)nv;
+        o.max_ctas = max_ctas;
+        o.dx = xp;
+        o.dgc = coef + l_used;
+        o.dgs = coef_ld;
+        return o;
+    };
     int64_t row_off = 0;
     for (size_t s = 0; s < plan.size(); ++s) {
         const PkShell& sh = plan[s];
@@ -1642,11 +1664,11 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
             if (tc)
                 FGB_LAUNCH(launch_dsynth(c->ds.as<int8_t>(), c->dse.as<int>(), c->dsb.as<int8_t>(), (int)dkp, (int)n,
                                          sh.p0, sh.p1, coef, coef_ld, l_used, rows, q, sl, rmax, mp,
-                                         s == 0 ? (int)pk_env("FGFRFT_SYN_CAP0", 0) : syn_cap, c->pk_s),
+                                         s == 0 ? (int)pk_env("FGFRFT_SYN_CAP0", 0) : syn_cap, c->pk_s, 1),
                            1);
             else
                 FGB_LAUNCH(launch_psynth(c->pk.p, c->pks.as<double>(), (int)n, l_used, c->l, coef, coef_ld, rows, q, sl,
-                                         rmax, mp, c->pk_s, sh.p0, sh.p1, s == 0 ? 0 : syn_cap),
+                                         rmax, mp, c->pk_s, sh.p0, sh.p1, s == 0 ? 0 : syn_cap, 0, 1),
                            1);
         }
         {
@@ -1672,9 +1694,10 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
                 }
                 if (ch == 0) FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_es[s], 0));
                 ProfScope ps(KC_I8GEMM, c->pk_g);
-                FGB_LAUNCH(launch_ozgemm(S, 1, dst, ex, (int)(rows * rp), xd, xe, (int)cp, (int)kp,
-                                         static_cast<double*>(y) + 2 * sh.r0 + j0 * 2 * n, n, 2 * n * b, (int)rv,
-                                         (int)rp, (int)crows, c->pk_g, nullptr, 0, 0),
+                FGB_LAUNCH(launch_ozgemm_ex(S, 1, dst, ex, (int)(rows * rp), xd, xe, (int)cp, (int)kp,
+                                            gemm_out(static_cast<double*>(y) + 2 * sh.r0 + j0 * 2 * n, rv, rp, crows,
+                                                     static_cast<const double*>(x_dev) + 2 * sh.r0 + j0 * 2 * n, 0),
+                                            c->pk_g),
                            1);
             }
             row_off += rp;
@@ -1684,9 +1707,11 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         {
             ProfScope ps(KC_I8GEMM, c->pk_g);
             const bool last = s + 1 == plan.size();
-            FGB_LAUNCH(launch_ozgemm(S, 1, dst, ex, (int)(rows * rp), c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
-                                     (int)kp, static_cast<double*>(y) + 2 * sh.r0, n, 2 * n * b, (int)rv, (int)rp,
-                                     (int)(2 * b), c->pk_g, nullptr, 0, last ? 0 : gcap),
+            FGB_LAUNCH(launch_ozgemm_ex(S, 1, dst, ex, (int)(rows * rp), c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
+                                        (int)kp,
+                                        gemm_out(static_cast<double*>(y) + 2 * sh.r0, rv, rp, 2 * b,
+                                                 static_cast<const double*>(x_dev) + 2 * sh.r0, last ? 0 : gcap),
+                                        c->pk_g),
                        1);
         }
         row_off += rp;

@@ -169,7 +169,7 @@ cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, dou
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
                           int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0,
-                          int pbase = 0);
+                          int pbase = 0, int nodiag = 0);
 cudaError_t launch_pack_pairs_from_panels(const double* rp, int64_t ld_r, const double* cp, int64_t ld_c, int n, int I0,
                                           int pbase, int npairs_local, int k, int l, void* packed, double* scales,
                                           cudaStream_t stream);

@@ -83,6 +83,12 @@ struct OzOut {
     double* dest[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int scw = 0;
     int64_t ssc = 0, sld = 0;
+    // CM 1: the diagonal term of a series whose synthesis left out c_0 I (A = Q - c_0 I, so the
+    // slicing error follows the off-diagonal entries): C[bm] += dgc[bm * dgs] * dx[same offset as C
+    // within a block] (dx complex, laid out as C with the same ldc). dx = nullptr: off.
+    const double* dx = nullptr;
+    const double* dgc = nullptr;
+    int64_t dgs = 0;
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)
@@ -105,7 +111,7 @@ cudaError_t launch_dsynth_coefs(const double* coef, int coef_ld, int l_used, int
                                 cudaStream_t stream);
 cudaError_t launch_dsynth(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0, int p1,
                           const double* coef, int coef_ld, int l_used, int ac, double* out, int64_t out_stride,
-                          unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream);
+                          unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream, int nodiag = 0);
 // Slice a viewed operand into dst (slices * nb * rp * kp bytes) + exps (nb * rp ints);
 // rowmax: nb * rp scratch words. tr = kOzTileA for an A operand, kOzTileB for a B operand.
 cudaError_t launch_oz_slice(const OzView& v, int slices, int tr, int8_t* dst, int* exps, unsigned long long* rowmax,

@@ -25,6 +25,7 @@
 //     lane = output row, 32 columns per warp) and combine the S accumulators in FP64 (Horner
 //     in base 254 over exact int64 folds) into the output.
 #include "oz.cuh"
+#include "tc.cuh"
 
 #include <cstdlib>
 
@@ -54,91 +55,6 @@ template <int S, int BN = kOzBN> struct OzCfg {
     static constexpr int smem = stages * stage + 1024 + 2048;  // + barriers / scratch + CM 2 exchange
 };
 
-// ---------------------------------------------------------------- tcgen05 helpers
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    // SWIZZLE_NONE K-major canonical layout: ((8, m), (16 B, 2)) : ((16 B, SBO), (1, LBO));
-    // version 1 (sm_100), base offset 0, layout type 0.
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;
-    return d;
-}
-
-__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
-    // c_format S32 (2) [4,6); a/b format signed int8 (1) [7,10) / [10,13); K-major A and B;
-    // n_dim = N >> 3 [17,23); m_dim = M >> 4 [24,29).
-    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Same, arriving on the barrier at this offset in every CTA of `mask` (cluster multicast).
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
-}
-
-// 1-D bulk copy global -> the same shared offset in every CTA of `mask`, completing on each
-// CTA's barrier at `bar`'s offset.
-__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;"
-        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask) : "memory");
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-// 32 consecutive TMEM columns of this thread's lane -> 32 registers.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
-                 : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ double pow2(int e) {  // exact 2^e for -1022 <= e <= 1023
     return __longlong_as_double((long long)(e + 1023) << 52);
@@ -791,8 +707,14 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                 for (int c = 0; c < kOzEC; c += 2) {
                     const int n = nt * kOzBN + h * kOzEC + c;
                     if (n >= out.nv) break;
-                    const double v0 = val[c] * ra * pow2(ebt[c]);
-                    const double v1 = val[c + 1] * ra * pow2(ebt[c + 1]);
+                    double v0 = val[c] * ra * pow2(ebt[c]);
+                    double v1 = val[c + 1] * ra * pow2(ebt[c + 1]);
+                    if (CM == 1 && out.dx) {  // the c_0 I term the synthesis left out: + c_0 X[i, j]
+                        const double d = out.dgc[(int64_t)bm * out.dgs];
+                        const double2 xv = *reinterpret_cast<const double2*>(out.dx + (i + (int64_t)(n >> 1) * out.ldc) * 2);
+                        v0 = fma(d, xv.x, v0);
+                        v1 = fma(d, xv.y, v1);
+                    }
                     if (CM == 0) {
                         const int64_t o0 = (int64_t)bm * out.sc + i + (int64_t)n * out.ldc;
                         __stcs(cb + i + (int64_t)n * out.ldc, v0);
@@ -958,7 +880,7 @@ __global__ void __launch_bounds__(32 * (1 + kDsIssuers + 4 * G), 1)
 dsynth_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const int8_t* __restrict__ b,
               const int* __restrict__ eb, int kblocks, int stages, int n, int nt, int p0, int p1,
               const double* __restrict__ coef, int coef_ld, int l_used, double* __restrict__ out, int64_t ostride,
-              unsigned long long* __restrict__ rowmax, int64_t mp, int dbg) {
+              unsigned long long* __restrict__ rowmax, int64_t mp, int dbg, int nodiag) {
     constexpr int W = 2 * AC;        // live B rows / accumulator columns
     constexpr int TPG = kDsTiles / G;  // tiles of a pair per epilogue group
     static_assert(kDsTiles % G == 0, "groups divide the tiles of a pair");
@@ -1066,7 +988,7 @@ dsynth_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
         for (int c = 0; c < W; ++c) ebv[c] = eb[c];
 #pragma unroll
-        for (int x = 0; x < AC; ++x) c0v[x] = coef[(size_t)x * coef_ld + l_used];
+        for (int x = 0; x < AC; ++x) c0v[x] = nodiag ? 0.0 : coef[(size_t)x * coef_ld + l_used];  // nodiag: Q - c_0 I
         constexpr double w1 = 1.0 / 254.0, w2 = w1 * w1, w3 = w2 * w1, w4 = w3 * w1, w5 = w4 * w1;
         // this group's tiles of a pair are sub = G q + grp; their row exponents are loaded one pair
         // ahead (a DRAM round trip under load is ~1-2 us)
@@ -1394,7 +1316,7 @@ cudaError_t launch_dsynth_coefs(const double* coef, int coef_ld, int l_used, int
 template <int AC, int G>
 static cudaError_t dsynth_launch(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0,
                                  int p1, const double* coef, int coef_ld, int l_used, double* out, int64_t out_stride,
-                                 unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream) {
+                                 unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream, int nodiag) {
     static PerDeviceOnce attr;
     const int smem = ds_smem(kp);
     if (cudaError_t e = attr.run([&] {
@@ -1413,13 +1335,13 @@ static cudaError_t dsynth_launch(const int8_t* digits, const int* exps, const in
     }();
     dsynth_kernel<AC, G><<<grid, 32 * (1 + kDsIssuers + 4 * G), smem, stream>>>(
         digits, exps, bsl, reinterpret_cast<const int*>(bsl + ds_b_bytes(kp)), kp / 64, ds_stages(kp), n, nt, p0, p1,
-        coef, coef_ld, l_used, out, out_stride, rowmax, mp, dbg);
+        coef, coef_ld, l_used, out, out_stride, rowmax, mp, dbg, nodiag);
     return cudaGetLastError();
 }
 
 cudaError_t launch_dsynth(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0, int p1,
                           const double* coef, int coef_ld, int l_used, int ac, double* out, int64_t out_stride,
-                          unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream) {
+                          unsigned long long* rowmax, int64_t mp, int max_ctas, cudaStream_t stream, int nodiag) {
     if (kp % 128 || kp > 512) return cudaErrorInvalidValue;
     if (p1 < 0) {
         const int64_t nt = ceil_div(n, kTile);
@@ -1430,12 +1352,12 @@ cudaError_t launch_dsynth(const int8_t* digits, const int* exps, const int8_t* b
         return e ? std::atoi(e) : 4;
     }();
     switch (ac * 10 + (groups == 2 ? 2 : 4)) {
-        case 12: return dsynth_launch<1, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
-        case 14: return dsynth_launch<1, 4>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
-        case 22: return dsynth_launch<2, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
-        case 24: return dsynth_launch<2, 4>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        case 12: return dsynth_launch<1, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream, nodiag);
+        case 14: return dsynth_launch<1, 4>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream, nodiag);
+        case 22: return dsynth_launch<2, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream, nodiag);
+        case 24: return dsynth_launch<2, 4>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream, nodiag);
         case 42:
-        case 44: return dsynth_launch<4, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream);
+        case 44: return dsynth_launch<4, 2>(digits, exps, bsl, kp, n, p0, p1, coef, coef_ld, l_used, out, out_stride, rowmax, mp, max_ctas, stream, nodiag);
         default: return cudaErrorInvalidValue;
     }
 }

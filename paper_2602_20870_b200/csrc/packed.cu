@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(G * (kPsConsumers + 32), 1)
 psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __restrict__ scales, int n, int l,
                     int lc, const double* __restrict__ coef, int coef_ld, double* __restrict__ out, int64_t out_stride,
                     unsigned long long* __restrict__ rowmax, int64_t rm_stride, int nt, int p0, int p1,
-                    int pbase) {
+                    int pbase, int nodiag) {
     constexpr int kStage = 2 * kPkTileBytes;
     extern __shared__ __align__(128) unsigned char smem_all[];
     const int g = threadIdx.x / (kPsConsumers + 32);
@@ -149,7 +149,10 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
     const int npairs = (p1 - p0 - vcta + vgrid - 1) / vgrid;
     const int depth = S < l ? S : l;  // stages in use; <= l, so a pair's scale buffer is never refilled in use
     const int cw = 2 * l + 1;
-    for (int idx = tid; idx < AC * cw; idx += kPsConsumers + 32) ctab[idx] = coef[(size_t)(idx / cw) * coef_ld + idx % cw];
+    // nodiag: Q - c_0 I (the product GEMM adds c_0 X in its epilogue, so Q's row maxima -- and the
+    // Ozaki slicing error -- follow the off-diagonal entries)
+    for (int idx = tid; idx < AC * cw; idx += kPsConsumers + 32)
+        ctab[idx] = (nodiag && idx % cw == l) ? 0.0 : coef[(size_t)(idx / cw) * coef_ld + idx % cw];
     if (tid == 0) {
         for (int q = 0; q < S; ++q) {
             mbar_init(&full[q], 1);
@@ -301,7 +304,8 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
 // l: powers summed (the truncation), l_cache: powers stored (the scale layout's stride).
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
-                          int64_t rm_stride, cudaStream_t stream, int p0, int p1, int max_ctas, int pbase) {
+                          int64_t rm_stride, cudaStream_t stream, int p0, int p1, int max_ctas, int pbase,
+                          int nodiag) {
     const int nt = (int)ceil_div(n, kTile);
     if (p1 < 0) p1 = nt * (nt + 1) / 2;
     const int npairs = p1 - p0;
@@ -329,7 +333,7 @@ cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l
         kern<<<grid, GV * (kPsConsumers + 32), smem, stream>>>((const unsigned char*)packed,                 \
                                                               scales, n, l, l_cache,                         \
                                                               coef_dev, coef_ld, out, out_stride, rowmax,    \
-                                                              rm_stride, nt, p0, p1, pbase);                 \
+                                                              rm_stride, nt, p0, p1, pbase, nodiag);         \
     }
     if (n_alpha == 1) FGB_PS(1) else if (n_alpha == 2) FGB_PS(2) else if (n_alpha == 4) FGB_PS(4) else return cudaErrorInvalidValue;
 #undef FGB_PS

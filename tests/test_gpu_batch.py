@@ -61,3 +61,35 @@ def test_graph_batch_validation():
     y = b.forward(a[:, :2].contiguous(), x)
     assert y.shape == (2, 2, 3, 8)
     b.close()
+
+
+@pytest.mark.parametrize("graphs,heads", [(400, 4), (161, 3), (150, 1)])
+def test_graph_batch_persistent_tensor_core_kernels(graphs, heads):
+    """The config-5 shape (real F, n = 64, 64 channels) runs the persistent tcgen05 kernels: more
+    graphs than SMs, so every CTA walks several graphs through one power / signal ring; checked on a
+    sample that covers the first, the wrap-around and the last graphs of the persistent loop."""
+    n, l, ch = 64, 16, 64
+    fs = np.stack([prep.gft_from_shift(prep.laplacian(prep.er_graph(n, 0.1, 500 + g))) for g in range(graphs)])
+    rng = np.random.default_rng(graphs + heads)
+    alphas = rng.uniform(0.5, 1.5, (graphs, heads))
+    x = (rng.standard_normal((graphs, n, ch)) + 1j * rng.standard_normal((graphs, n, ch))).astype(np.complex64)
+    gc = (rng.standard_normal((graphs, heads, n, ch)) + 1j * rng.standard_normal((graphs, heads, n, ch))) \
+        .astype(np.complex64)
+    batch = fg.GraphBatch(fs, l)
+    a_d = torch.from_numpy(alphas).cuda()
+    x_d = torch.from_numpy(np.ascontiguousarray(x.transpose(0, 2, 1))).cuda()
+    g_d = torch.from_numpy(np.ascontiguousarray(gc.transpose(0, 1, 3, 2))).cuda()
+    y = batch.forward(a_d, x_d).cpu().numpy().transpose(0, 1, 3, 2)
+    dl = batch.dlda(a_d, g_d, x_d).cpu().numpy()
+    sample = sorted({0, 1, 147, 148, 149, graphs // 2, graphs - 2, graphs - 1} & set(range(graphs)))
+    for gi in sample:
+        cache = O.PowerCache(fs[gi], l)
+        xg = x[gi].astype(np.complex128)
+        for h in range(heads):
+            q = O.fgfrft_matrix(cache, alphas[gi, h])
+            assert rel(y[gi, h], q @ xg) <= 1e-4, (gi, h)
+            gg = gc[gi, h].astype(np.complex128)
+            s_ref = O.power_dots(cache, gg @ xg.conj().T)
+            _, dc = O.sinc_coeffs(alphas[gi, h], l)
+            assert abs(dl[gi, h] - float(np.dot(dc, s_ref))) <= 1e-4 * float(np.sum(np.abs(dc * s_ref))), (gi, h)
+    batch.close()

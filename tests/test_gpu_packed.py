@@ -50,7 +50,7 @@ def problem(engine):
     return f, l, x, xc, fg.PowerCache(f, l, memory_budget=8 << 30), O.PowerCache(f, l), engine
 
 
-@pytest.mark.parametrize("alphas", [[0.37], [-1.3], [0.25, 1.75], [2.0]])
+@pytest.mark.parametrize("alphas", [[0.37], [0.04], [-1.3], [0.25, 1.75], [2.0]])
 def test_packed_mse_step_matches_oracle(problem, alphas):
     f, l, x, xc, g, o, route = problem
     loss, dl, y = fg.mse_step(g, alphas, x, xc, want_y=True)

@@ -106,16 +106,42 @@ def run_c5(peaks):
     t_fwd = timed(stream, lambda: batch.forward(a_d, x_d))
     t_bwd = timed(stream, lambda: batch.dlda(a_d, g_d, x_d))
     nodes = G * H * n * C
-    # FP32 work: synthesis 8*L*n^2*H, apply 8*n^2*C*H, M = G X^H 8*n^2*C*H, dots 8*L*n^2*H (per graph)
-    flops = G * (8 * l * n * n * H * 2 + 8 * n * n * C * H * 2)
-    cache_bytes = G * l * 64 * 64 * (4 if np.all(np.imag(fs) == 0) else 8)  # real F: float slabs
+    real = bool(np.all(np.imag(fs) == 0))
+    e = 4 if real else 8  # real F: float slabs, real Q; complex F: complex64 slabs
+    # FP32 flops per graph. Real F: synthesis 2 FMAs (P, P^T) per element, power and head = 4 L n^2 H;
+    # Y = Q X real x complex = 4 n^2 C H; Re M = Gr Xr^T + Gi Xi^T = 4 n^2 C H; dots 4 L n^2 H.
+    # Complex F: every product complex (4 real FMAs): twice each.
+    per = 4 * l * n * n * H + 4 * n * n * C * H
+    flops_fwd = G * per * (1 if real else 2)
+    flops_bwd = G * per * (1 if real else 2)
+    cache_bytes = G * l * 64 * 64 * e
+    sig = G * C * n * 8  # one complex64 n x C block per graph
+    fwd_bytes = cache_bytes + sig + H * sig  # powers + X read, Y_h written
+    bwd_bytes = cache_bytes + sig + H * sig  # powers + X + G_h read
+    peak = _hbm_peak()
     return {"config": "C5", "graphs": G, "n": n, "l": l, "heads": H, "channels": C, "dtype": "c64",
-            "cache_gb": cache_bytes / 1e9, "prep_s": prep_s, "cache_build_s": build_s,
-            "forward": {"ms": t_fwd, "signal_nodes_per_s": nodes / (t_fwd * 1e-3),
-                        "cache_gbs": cache_bytes / (t_fwd * 1e-3) / 1e9},
-            "dlda": {"ms": t_bwd},
-            "step": {"ms": t_fwd + t_bwd, "signal_nodes_per_s": nodes / ((t_fwd + t_bwd) * 1e-3),
-                     "fp32_tflops": flops / ((t_fwd + t_bwd) * 1e-3) / 1e12}}
+            "real_f": real, "cache_gb": cache_bytes / 1e9, "prep_s": prep_s, "cache_build_s": build_s,
+            "forward": {"ms": t_fwd, "signal_nodes_per_s": nodes / (t_fwd * 1e-3), "hbm_gb": fwd_bytes / 1e9,
+                        "hbm_gbs": fwd_bytes / (t_fwd * 1e-3) / 1e9,
+                        "frac_hbm": fwd_bytes / (t_fwd * 1e-3) / 1e9 / peak,
+                        "fp32_tflops": flops_fwd / (t_fwd * 1e-3) / 1e12},
+            "dlda": {"ms": t_bwd, "hbm_gb": bwd_bytes / 1e9, "hbm_gbs": bwd_bytes / (t_bwd * 1e-3) / 1e9,
+                     "frac_hbm": bwd_bytes / (t_bwd * 1e-3) / 1e9 / peak,
+                     "fp32_tflops": flops_bwd / (t_bwd * 1e-3) / 1e12},
+            "step": {"ms": t_fwd + t_bwd, "signal_nodes_per_s": nodes / ((t_fwd + t_bwd) * 1e-3)},
+            "peak_hbm_gbs": peak}
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        for k in ("hbm_gbs", "hbm_copy_gbs", "copy_gbs"):
+            if k in d:
+                return float(d[k])
+    except Exception:
+        pass
+    return 6549.1
 
 
 def main():
