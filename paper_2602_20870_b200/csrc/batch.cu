@@ -30,15 +30,23 @@ constexpr int kBMaxHeads = 4;
 constexpr int kBMaxCh = 64;
 constexpr int kBSlab = 4 * kTileElems;  // elements per padded slab
 
-// coef[o][2][2l+1] (c then dc) for every order o.
-__global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_orders, int l, double* __restrict__ coef) {
+// coef[o][2][2l+1] (c then dc) for every order o; heads > 0: also the FP32 copy the tcgen05 kernels
+// stream, [g][h][2][2l+1] at a 16-byte padded per-graph stride (tc_coef_stride), after the doubles.
+__global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_orders, int l, double* __restrict__ coef,
+                                  float* __restrict__ coef_f, int heads, int fstride) {
     const int w = 2 * l + 1;
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n_orders * w) return;
     const int o = idx / w, t = idx % w;
     const double x = alphas[o] - (double)(t - l);
-    coef[(size_t)o * 2 * w + t] = dsinc(x);
-    coef[(size_t)o * 2 * w + w + t] = dsinc_deriv(x);
+    const double c = dsinc(x), d = dsinc_deriv(x);
+    coef[(size_t)o * 2 * w + t] = c;
+    coef[(size_t)o * 2 * w + w + t] = d;
+    if (coef_f) {
+        float* f = coef_f + (size_t)(o / heads) * fstride + (o % heads) * 2 * w;
+        f[t] = (float)c;
+        f[w + t] = (float)d;
+    }
 }
 
 // [G] column-major n x n complex128 (stride n*n) -> [G][slab k] tiled complex64 padded to 64
@@ -601,43 +609,104 @@ __device__ __forceinline__ void st_shared_v4(unsigned char* p, uint4 v) { *reint
 
 __device__ __forceinline__ void tc_compute_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcWarps) : "memory"); }
 
-// The ring protocol of both kernels: item it lives in stage it % S; the producer waits for the
-// stage's `empty` (one arrival per compute warp) before refilling it.
+// Ring position: stage and phase parity advanced item by item (no division in the loops). The
+// producer waits on `empty` with the opposite parity, which a fresh barrier passes at once.
+struct TcCursor {
+    int s = 0;
+    uint32_t ph = 0;
+    __device__ __forceinline__ void next(int stages) {
+        if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+};
+
 struct TcRing {
     unsigned char* base;
     uint64_t* full;
     uint64_t* empty;
     int stages;
-    __device__ __forceinline__ const unsigned char* wait(int it) const {
-        const int s = it % stages;
-        mbar_wait(full + s, (uint32_t)((it / stages) & 1));
-        return base + (size_t)s * kTcItem;
+    __device__ __forceinline__ const unsigned char* wait(const TcCursor& c) const {
+        mbar_wait(full + c.s, c.ph);
+        return base + (size_t)c.s * kTcItem;
     }
-    __device__ __forceinline__ void release(int it, int lane) const {
+    __device__ __forceinline__ void release(const TcCursor& c, int lane) const {
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + it % stages);
+        if (lane == 0) mbar_arrive(empty + c.s);
+    }
+    __device__ __forceinline__ void produce(TcCursor& c, const void* src, uint64_t pol) const {
+        mbar_wait(empty + c.s, c.ph ^ 1u);
+        mbar_arrive_expect_tx(full + c.s, kTcItem);
+        bulk_g2s_hint(base + (size_t)c.s * kTcItem, src, kTcItem, full + c.s, pol);
+        c.next(stages);
     }
 };
 
-__device__ __forceinline__ void tc_produce(const TcRing& r, int it, const void* src, uint64_t pol) {
-    const int s = it % r.stages;
-    if (it >= r.stages) mbar_wait(r.empty + s, (uint32_t)(((it / r.stages) - 1) & 1));
-    mbar_arrive_expect_tx(r.full + s, kTcItem);
-    bulk_g2s_hint(r.base + (size_t)s * kTcItem, src, kTcItem, r.full + s, pol);
+// Per-graph series coefficients, FP32 (batch_coef_kernel's second table): [h][c | c'][2l + 1] at a
+// per-graph stride padded to 16 bytes, double-buffered in shared memory by graph parity and
+// bulk-copied by the producer ahead of the graph's first ring item (no CTA barrier per graph).
+__host__ __device__ constexpr int tc_coef_stride(int heads, int l) { return (2 * heads * (2 * l + 1) + 3) & ~3; }
+
+struct TcCoefs {
+    float* buf;      // [2][stride]
+    uint64_t* full;  // [2]
+    uint64_t* empty; // [2], one arrival per compute warp
+    int stride;
+    __device__ __forceinline__ const float* wait(int t) const {
+        mbar_wait(full + (t & 1), (uint32_t)((t >> 1) & 1));
+        return buf + (t & 1) * stride;
+    }
+    __device__ __forceinline__ void release(int t, int lane) const {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + (t & 1));
+    }
+    __device__ __forceinline__ void produce(int t, const float* src) const {
+        mbar_wait(empty + (t & 1), (uint32_t)(((t >> 1) & 1) ^ 1));
+        mbar_arrive_expect_tx(full + (t & 1), (uint32_t)stride * 4);
+        bulk_g2s(buf + (t & 1) * stride, src, (uint32_t)stride * 4, full + (t & 1));
+    }
+};
+
+// the coefficient buffers are bulk-copy destinations: 16-byte aligned
+__device__ __forceinline__ float* tc_align16(void* p) {
+    return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 15) & ~(uintptr_t)15);
+}
+
+// barriers: full[8], empty[8], cfull[2], cempty[2], opready, mmadone, tempty; then the TMEM slot
+constexpr int kTcBars = 2 * kTcMaxStages + 4 + 3;
+
+__device__ __forceinline__ void tc_init_barriers(uint64_t* bars, int stages, int op_count) {
+    for (int s = 0; s < stages; ++s) {
+        mbar_init(bars + s, 1);
+        mbar_init(bars + kTcMaxStages + s, kTcWarps);
+    }
+    uint64_t* c = bars + 2 * kTcMaxStages;
+    mbar_init(c + 0, 1);
+    mbar_init(c + 1, 1);
+    mbar_init(c + 2, kTcWarps);
+    mbar_init(c + 3, kTcWarps);
+    mbar_init(c + 4, op_count);  // opready
+    mbar_init(c + 5, 1);         // mmadone
+    mbar_init(c + 6, kTcWarps);  // tempty (unused by the current kernels' single TMEM buffer)
+    fence_mbar_init();
 }
 
 size_t batch_tc_fwd_smem(int l, int heads, int* stages) {
     const size_t ops = (size_t)((heads + 1) / 2) * 2 * 16384 + 2 * 16384;  // Q tiles hi / lo, X^T hi / lo
-    const size_t fixed = ops + 2 * (kTcMaxStages + 2) * 8 + 16 + (size_t)heads * (2 * l + 1) * 4 + 128;
+    const size_t fixed = ops + kTcBars * 8 + 16 + 2 * (size_t)tc_coef_stride(heads, l) * 4 + 128;
     int st = (int)((227 * 1024 - fixed) / kTcItem);
     if (st > kTcMaxStages) st = kTcMaxStages;
     if (stages) *stages = st;
     return fixed + (size_t)st * kTcItem;
 }
 
+// Forward. The compute warps run graph t's epilogue AFTER synthesising graph t + 1 (the MMA of t
+// overlaps that synthesis), then write t + 1's operands: operands and TMEM stay single-buffered
+// because graph t's accumulators are drained before t + 1's MMA is released.
 template <int H>
 __global__ void __launch_bounds__(kTcThreads, 1)
-batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const double* __restrict__ coef,
+batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const float* __restrict__ coef,
                     const float2* __restrict__ x, float2* __restrict__ y, int graphs, int stages) {
     constexpr int NT = (H + 1) / 2;  // M tiles of two heads
     extern __shared__ __align__(128) unsigned char smem[];
@@ -646,20 +715,13 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const double* __rest
     unsigned char* ringp = xhl + 2 * 16384;
     uint64_t* bars = reinterpret_cast<uint64_t*>(ringp + (size_t)stages * kTcItem);
     const TcRing ring{ringp, bars, bars + kTcMaxStages, stages};
-    uint64_t* opready = bars + 2 * kTcMaxStages;
+    uint64_t* opready = bars + 2 * kTcMaxStages + 4;
     uint64_t* mmadone = opready + 1;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(mmadone + 1);
-    float* cs = reinterpret_cast<float*>(tslot + 4);  // [H][2l + 1]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, w = 2 * l + 1;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < stages; ++s) {
-            mbar_init(ring.full + s, 1);
-            mbar_init(ring.empty + s, kTcWarps);
-        }
-        mbar_init(opready, kTcWarps);
-        mbar_init(mmadone, 1);
-        fence_mbar_init();
-    }
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kTcBars);
+    const int w = 2 * l + 1, cst = tc_coef_stride(H, l);
+    const TcCoefs cf{tc_align16(tslot + 4), bars + 2 * kTcMaxStages, bars + 2 * kTcMaxStages + 2, cst};
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) tc_init_barriers(bars, stages, kTcWarps);
     if (warp == kTcWarps + 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -669,24 +731,25 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const double* __rest
     tc_fence_after();
     const uint32_t tmem = *tslot;
     if (warp == kTcWarps) {
-        // ---- producer: per graph the l power slabs, then X_g (channels 0-31, 32-63)
+        // ---- producer: per graph its coefficients, the l power slabs, then X_g (channels 0-31, 32-63)
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            int it = 0;
-            for (int g = blockIdx.x; g < graphs; g += gridDim.x)
-                for (int t = 0; t < l + 2; ++t, ++it)
-                    tc_produce(ring, it,
-                               t < l ? (const void*)(slabs + ((int64_t)g * l + t) * kBSlab)
-                                     : (const void*)(x + (int64_t)g * kBN * kBMaxCh + (t - l) * (kBN * kBMaxCh / 2)),
-                               pol);
+            TcCursor c;
+            int t = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++t) {
+                cf.produce(t, coef + (size_t)g * cst);
+                for (int k = 0; k < l; ++k) ring.produce(c, slabs + ((int64_t)g * l + k) * kBSlab, pol);
+                for (int hh = 0; hh < 2; ++hh)
+                    ring.produce(c, x + (int64_t)g * kBN * kBMaxCh + hh * (kBN * kBMaxCh / 2), pol);
+            }
         }
     } else if (warp == kTcWarps + 1) {
         // ---- MMA issuer: per graph NT tiles x 4 K steps x 3 split products
         if (lane == 0) {
             const uint32_t q0 = smem_u32(qhl), x0 = smem_u32(xhl);
-            int gi = 0;
-            for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++gi) {
-                mbar_wait(opready, (uint32_t)(gi & 1));
+            int t = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++t) {
+                mbar_wait(opready, (uint32_t)(t & 1));
                 tc_fence_after();
 #pragma unroll
                 for (int mt = 0; mt < NT; ++mt)
@@ -707,41 +770,79 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const double* __rest
         // ---- compute warps
         const int tid = threadIdx.x, i = tid & 63, jb = tid >> 6;
         const int qd = warp & 3, wq = warp >> 2;  // TMEM lane quarter, column quarter
-        int it = 0, gi = 0;
-        for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++gi) {
-            for (int idx = tid; idx < H * w; idx += 32 * kTcWarps) {
-                const int h = idx / w, t = idx - h * w;
-                cs[idx] = (float)coef[(size_t)(g * H + h) * 2 * w + t];
+        // graph pg's Y from TMEM: lane 32 qd + lane of tile mt = row (h, i); this warp's 32 columns
+        auto epilogue = [&](int pg) {
+#pragma unroll
+            for (int mt = 0; mt < NT; ++mt) {
+                const int h = 2 * mt + (qd >> 1), io = 32 * (qd & 1) + lane;
+                if (h >= H) continue;  // warp-uniform
+                float2* yo = y + (((int64_t)pg * H + h) * kBMaxCh + 16 * wq) * kBN + io;
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {  // 16 columns at a time: the next graph's Q is live
+                    int32_t v[16];
+                    tmem_ld16(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(mt * 128 + 32 * wq + 16 * hf), v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        __stcs(yo + (8 * hf + c) * kBN,
+                               make_float2(__int_as_float(v[2 * c]), __int_as_float(v[2 * c + 1])));
+                }
             }
-            tc_compute_sync();
+        };
+        TcCursor rc;
+        int t = 0, pg = -1;
+        for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++t) {
+            const float* cs = cf.wait(t);  // [h][c (w) | c' (w)]
             float q[H][8];
 #pragma unroll
-            for (int h = 0; h < H; ++h)
+            for (int h = 0; h < H; ++h) {
+                const float c0 = cs[h * 2 * w + l];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) q[h][u] = (i == 8 * jb + u) ? cs[h * w + l] : 0.f;
-            for (int k = 1; k <= l; ++k, ++it) {
-                const float* t = reinterpret_cast<const float*>(ring.wait(it));
+                for (int u = 0; u < 8; ++u) q[h][u] = (i == 8 * jb + u) ? c0 : 0.f;
+            }
+            for (int k = 1; k <= l; ++k) {
+                const float* tp = reinterpret_cast<const float*>(ring.wait(rc));
                 float a[H], b[H];
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    a[h] = cs[h * w + l + k];
-                    b[h] = cs[h * w + l - k];
+                    a[h] = cs[h * 2 * w + l + k];
+                    b[h] = cs[h * 2 * w + l - k];
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int j = 8 * jb + u;
-                    const float p = t[bidx(i, j)], pt = t[bidx(j, i)];
+                    const float p = tp[bidx(i, j)], pt = tp[bidx(j, i)];
 #pragma unroll
                     for (int h = 0; h < H; ++h) q[h][u] = fmaf(a[h], p, fmaf(b[h], pt, q[h][u]));
                 }
-                ring.release(it, lane);
+                ring.release(rc, lane);
+                rc.next(stages);
+            }
+            cf.release(t, lane);
+            // the previous graph's MMA ran during this synthesis: once it is done, Q moves into the
+            // operand tiles (so the accumulators are not live during the epilogue), the previous
+            // graph's Y leaves TMEM, and X_g takes the operand the MMA has finished reading
+            if (pg >= 0) mbar_wait(mmadone, (uint32_t)((t - 1) & 1));
+            // Q_h -> A operand of tile h / 2: row (h % 2) 64 + i, K core column jb
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                uint4 hi, lo;
+                tc_split8(q[h], hi, lo);
+                unsigned char* tq = qhl + (size_t)(h >> 1) * 2 * 16384;
+                st_shared_v4(tq + tc_off(128, (h & 1) * 64 + i, jb), hi);
+                st_shared_v4(tq + 16384 + tc_off(128, (h & 1) * 64 + i, jb), lo);
+            }
+            if (pg >= 0) {
+                tc_fence_after();
+                epilogue(pg);
+                tc_fence_before();
             }
             // X_g halves -> X^T operand: B row n = 2c + e, K = j. Thread: channel c = 32 half + cl
             // (cl = tid >> 3 & 31), 8 consecutive j (kc = tid & 7), both components -> rows 2c, 2c + 1.
             {
                 const int half = tid >> 8, cl = (tid >> 3) & 31, kc = tid & 7;
                 for (int hh = 0; hh < 2; ++hh) {
-                    const float2* xr = reinterpret_cast<const float2*>(ring.wait(it + hh));
+                    const float2* xr = reinterpret_cast<const float2*>(ring.wait(rc));
                     if (hh == half) {
                         float re[8], im[8];
 #pragma unroll
@@ -761,37 +862,19 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const double* __rest
                         st_shared_v4(xhl + tc_off(128, n0 + 1, kc), hi);
                         st_shared_v4(xhl + 16384 + tc_off(128, n0 + 1, kc), lo);
                     }
-                    ring.release(it + hh, lane);
+                    ring.release(rc, lane);
+                    rc.next(stages);
                 }
-                it += 2;
-            }
-            // Q_h -> A operand of tile h / 2: row (h % 2) 64 + i, K core column jb
-#pragma unroll
-            for (int h = 0; h < H; ++h) {
-                uint4 hi, lo;
-                tc_split8(q[h], hi, lo);
-                unsigned char* tq = qhl + (size_t)(h >> 1) * 2 * 16384;
-                st_shared_v4(tq + tc_off(128, (h & 1) * 64 + i, jb), hi);
-                st_shared_v4(tq + 16384 + tc_off(128, (h & 1) * 64 + i, jb), lo);
             }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(opready);
-            // epilogue: TMEM lane 32 qd + lane of tile mt = row (h, i); this warp's 32 columns from 32 wq
-            mbar_wait(mmadone, (uint32_t)(gi & 1));
+            pg = g;
+        }
+        if (pg >= 0) {
+            mbar_wait(mmadone, (uint32_t)((t - 1) & 1));
             tc_fence_after();
-#pragma unroll
-            for (int mt = 0; mt < NT; ++mt) {
-                const int h = 2 * mt + (qd >> 1), io = 32 * (qd & 1) + lane;
-                if (h >= H) continue;  // warp-uniform
-                int32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(mt * 128 + 32 * wq), v);
-                tmem_wait_ld();
-                float2* yo = y + (((int64_t)g * H + h) * kBMaxCh + 16 * wq) * kBN + io;
-#pragma unroll
-                for (int c = 0; c < 16; ++c)
-                    __stcs(yo + c * kBN, make_float2(__int_as_float(v[2 * c]), __int_as_float(v[2 * c + 1])));
-            }
+            epilogue(pg);
             tc_fence_before();
         }
     }
@@ -804,7 +887,7 @@ constexpr int kTcMs = 68;  // row stride (floats) of the staged M_h: conflict-fr
 
 size_t batch_tc_dlda_smem(int l, int heads, int* stages) {
     const size_t mreg = (size_t)kBMaxHeads * kBN * kTcMs * 4;  // >= one G tile hi / lo (64 KB)
-    const size_t fixed = 2 * 16384 + mreg + 2 * (kTcMaxStages + 2) * 8 + 16 + (size_t)heads * (2 * l + 1) * 8 +
+    const size_t fixed = 2 * 16384 + mreg + kTcBars * 8 + 16 + 2 * (size_t)tc_coef_stride(heads, l) * 4 +
                          kTcWarps * kBMaxHeads * 8 + 128;
     int st = (int)((227 * 1024 - fixed) / kTcItem);
     if (st > kTcMaxStages) st = kTcMaxStages;
@@ -814,7 +897,7 @@ size_t batch_tc_dlda_smem(int l, int heads, int* stages) {
 
 template <int H>
 __global__ void __launch_bounds__(kTcThreads, 1)
-batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const double* __restrict__ coef,
+batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const float* __restrict__ coef,
                      const float2* __restrict__ gcot, const float2* __restrict__ x, double* __restrict__ dlda,
                      int graphs, int stages) {
     constexpr int NT = (H + 1) / 2;
@@ -825,21 +908,14 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const double* __res
     unsigned char* ringp = reg + (size_t)kBMaxHeads * kBN * kTcMs * 4;
     uint64_t* bars = reinterpret_cast<uint64_t*>(ringp + (size_t)stages * kTcItem);
     const TcRing ring{ringp, bars, bars + kTcMaxStages, stages};
-    uint64_t* opready = bars + 2 * kTcMaxStages;
+    uint64_t* opready = bars + 2 * kTcMaxStages + 4;
     uint64_t* mmadone = opready + 1;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(mmadone + 1);
-    double* dcs = reinterpret_cast<double*>(tslot + 4);  // [H][2l + 1]: c'_k of this graph
-    double* red = dcs + H * (2 * l + 1);                 // [16 warps][4]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, w = 2 * l + 1;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < stages; ++s) {
-            mbar_init(ring.full + s, 1);
-            mbar_init(ring.empty + s, kTcWarps);
-        }
-        mbar_init(opready, kTcWarps);
-        mbar_init(mmadone, 1);
-        fence_mbar_init();
-    }
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kTcBars);
+    const int w = 2 * l + 1, cst = tc_coef_stride(H, l);
+    const TcCoefs cf{tc_align16(tslot + 4), bars + 2 * kTcMaxStages, bars + 2 * kTcMaxStages + 2, cst};
+    double* red = reinterpret_cast<double*>(cf.buf + 2 * cst);  // [16 warps][4]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) tc_init_barriers(bars, stages, kTcWarps);
     if (warp == kTcWarps + 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -848,18 +924,19 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const double* __res
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    constexpr int half_floats = kBN * kBMaxCh;  // float2 elements of half a 64 x 64 complex block x 2
+    constexpr int kHalf = kBN * kBMaxCh / 2;  // float2 elements of half a 64 x 64 complex block
     if (warp == kTcWarps) {
-        // ---- producer: per graph X_g (2 items), G_h (2 items per head), then the l power slabs
+        // ---- producer: per graph its coefficients, X_g (2 items), G_h (2 items per head), the powers
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            int it = 0;
-            for (int g = blockIdx.x; g < graphs; g += gridDim.x) {
-                for (int t = 0; t < 2; ++t, ++it)
-                    tc_produce(ring, it, x + (int64_t)g * kBN * kBMaxCh + t * (half_floats / 2), pol);
-                for (int t = 0; t < 2 * H; ++t, ++it)
-                    tc_produce(ring, it, gcot + (int64_t)g * H * kBN * kBMaxCh + t * (half_floats / 2), pol);
-                for (int k = 0; k < l; ++k, ++it) tc_produce(ring, it, slabs + ((int64_t)g * l + k) * kBSlab, pol);
+            TcCursor c;
+            int t = 0;
+            for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++t) {
+                cf.produce(t, coef + (size_t)g * cst);
+                for (int hh = 0; hh < 2; ++hh) ring.produce(c, x + (int64_t)g * kBN * kBMaxCh + hh * kHalf, pol);
+                for (int hh = 0; hh < 2 * H; ++hh)
+                    ring.produce(c, gcot + (int64_t)g * H * kBN * kBMaxCh + hh * kHalf, pol);
+                for (int k = 0; k < l; ++k) ring.produce(c, slabs + ((int64_t)g * l + k) * kBSlab, pol);
             }
         }
     } else if (warp == kTcWarps + 1) {
@@ -886,47 +963,33 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const double* __res
     } else {
         const int tid = threadIdx.x, i = tid & 63, jb = tid >> 6;
         const int qd = warp & 3, wq = warp >> 2;
-        int it = 0, ev = 0;
-        for (int g = blockIdx.x; g < graphs; g += gridDim.x) {
-            for (int idx = tid; idx < H * w; idx += 32 * kTcWarps) {
-                const int h = idx / w, t = idx - h * w;
-                dcs[idx] = coef[(size_t)(g * H + h) * 2 * w + w + t];
-            }
-            // X halves -> B operand (row j, K = 2c + e); thread: row j = i, core column kc = jb of the half
-            for (int hh = 0; hh < 2; ++hh, ++it) {
-                const float2* xr = reinterpret_cast<const float2*>(ring.wait(it));
-                float v[8];
+        TcCursor rc;
+        int t = 0, ev = 0;
+        // one 16 KB half (channels 32 hh ..) of a complex 64 x 64 block -> 8 values of operand row r
+        // (K core column 8 hh + jb: channels 4 jb .. 4 jb + 3 of the half, re / im interleaved)
+        auto convert = [&](unsigned char* dst, int rows, int r, int hh, uint32_t lo_off) {
+            const float2* src = reinterpret_cast<const float2*>(ring.wait(rc));
+            float v[8];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const float2 z = xr[(4 * jb + m) * kBN + i];
-                    v[2 * m] = z.x;
-                    v[2 * m + 1] = z.y;
-                }
-                uint4 hi, lo;
-                tc_split8(v, hi, lo);
-                st_shared_v4(xhl + tc_off(64, i, 8 * hh + jb), hi);
-                st_shared_v4(xhl + 16384 + tc_off(64, i, 8 * hh + jb), lo);
-                ring.release(it, lane);
+            for (int m = 0; m < 4; ++m) {
+                const float2 z = src[(4 * jb + m) * kBN + i];
+                v[2 * m] = z.x;
+                v[2 * m + 1] = z.y;
             }
+            uint4 hi, lo;
+            tc_split8(v, hi, lo);
+            st_shared_v4(dst + tc_off(rows, r, 8 * hh + jb), hi);
+            st_shared_v4(dst + lo_off + tc_off(rows, r, 8 * hh + jb), lo);
+            ring.release(rc, lane);
+            rc.next(stages);
+        };
+        for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++t) {
+            for (int hh = 0; hh < 2; ++hh) convert(xhl, 64, i, hh, 16384);
             for (int mt = 0; mt < NT; ++mt, ++ev) {
                 if (mt > 0) mbar_wait(mmadone, (uint32_t)((ev - 1) & 1));  // tile mt - 1 has read the region
                 for (int hl = 0; hl < 2; ++hl) {
                     if (2 * mt + hl >= H) break;
-                    for (int hh = 0; hh < 2; ++hh, ++it) {
-                        const float2* gr = reinterpret_cast<const float2*>(ring.wait(it));
-                        float v[8];
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const float2 z = gr[(4 * jb + m) * kBN + i];
-                            v[2 * m] = z.x;
-                            v[2 * m + 1] = z.y;
-                        }
-                        uint4 hi, lo;
-                        tc_split8(v, hi, lo);
-                        st_shared_v4(reg + tc_off(128, 64 * hl + i, 8 * hh + jb), hi);
-                        st_shared_v4(reg + 32768 + tc_off(128, 64 * hl + i, 8 * hh + jb), lo);
-                        ring.release(it, lane);
-                    }
+                    for (int hh = 0; hh < 2; ++hh) convert(reg, 128, 64 * hl + i, hh, 32768);
                 }
                 fence_async_smem();
                 __syncwarp();
@@ -959,47 +1022,51 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const double* __res
                 m[h][4] = b.x; m[h][5] = b.y; m[h][6] = b.z; m[h][7] = b.w;
             }
             tc_compute_sync();  // the region is the next graph's G tile
-            double dl[H];
+            const float* dcs = cf.wait(t) + w;  // c'_k of head h at dcs[h 2w + l + k]
+            float dl[H];
 #pragma unroll
             for (int h = 0; h < H; ++h) {
                 float d = 0.f;
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
                     if (i == 8 * jb + u) d = m[h][u];
-                dl[h] = dcs[h * w + l] * (double)d;  // c'_0 Re tr(M_h)
+                dl[h] = dcs[h * 2 * w + l] * d;  // c'_0 Re tr(M_h)
             }
-            for (int k = 1; k <= l; ++k, ++it) {
-                const float* t = reinterpret_cast<const float*>(ring.wait(it));
+            for (int k = 1; k <= l; ++k) {
+                const float* tp = reinterpret_cast<const float*>(ring.wait(rc));
                 float vp[H], vm[H];
 #pragma unroll
                 for (int h = 0; h < H; ++h) vp[h] = vm[h] = 0.f;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int j = 8 * jb + u;
-                    const float p = t[bidx(i, j)], pt = t[bidx(j, i)];
+                    const float p = tp[bidx(i, j)], pt = tp[bidx(j, i)];
 #pragma unroll
                     for (int h = 0; h < H; ++h) {
                         vp[h] = fmaf(m[h][u], p, vp[h]);
                         vm[h] = fmaf(m[h][u], pt, vm[h]);
                     }
                 }
-                ring.release(it, lane);
+                ring.release(rc, lane);
+                rc.next(stages);
 #pragma unroll
                 for (int h = 0; h < H; ++h)
-                    dl[h] = fma(dcs[h * w + l + k], (double)vp[h], fma(dcs[h * w + l - k], (double)vm[h], dl[h]));
+                    dl[h] = fmaf(dcs[h * 2 * w + l + k], vp[h], fmaf(dcs[h * 2 * w + l - k], vm[h], dl[h]));
             }
+            cf.release(t, lane);
+            // FP32 per thread (8 elements x 2l + 1 terms), FP64 across the 512 threads
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                double t = dl[h];
+                double s2 = (double)dl[h];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                if (lane == 0) red[warp * kBMaxHeads + h] = t;
+                for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                if (lane == 0) red[warp * kBMaxHeads + h] = s2;
             }
             tc_compute_sync();
             if (tid < H) {
-                double t = 0.0;
-                for (int wp = 0; wp < kTcWarps; ++wp) t += red[wp * kBMaxHeads + tid];
-                dlda[(int64_t)g * H + tid] = t;
+                double s2 = 0.0;
+                for (int wp = 0; wp < kTcWarps; ++wp) s2 += red[wp * kBMaxHeads + tid];
+                dlda[(int64_t)g * H + tid] = s2;
             }
         }
     }
@@ -1013,9 +1080,23 @@ static bool tc_shape_ok(int n, int ch, const void* a, const void* b) {
     return n == kBN && ch == kBMaxCh && ((uintptr_t)a & 15) == 0 && ((uintptr_t)b & 15) == 0;
 }
 
-cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream) {
+static size_t batch_coef_dbytes(int n_orders, int l) { return ((size_t)n_orders * 2 * (2 * l + 1) * 8 + 15) & ~(size_t)15; }
+
+size_t batch_coef_bytes(int graphs, int heads, int l) {
+    return batch_coef_dbytes(graphs * heads, l) + (size_t)graphs * tc_coef_stride(heads, l) * 4;
+}
+
+static const float* batch_coef_f(const double* coef, int n_orders, int l) {
+    return reinterpret_cast<const float*>(reinterpret_cast<const char*>(coef) + batch_coef_dbytes(n_orders, l));
+}
+
+cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream,
+                              int heads) {
     const int total = n_orders * (2 * l + 1);
-    batch_coef_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, stream>>>(alphas_dev, n_orders, l, coef_dev);
+    float* cf = heads > 0 ? const_cast<float*>(batch_coef_f(coef_dev, n_orders, l)) : nullptr;
+    batch_coef_kernel<<<(unsigned)ceil_div(total, 256), 256, 0, stream>>>(alphas_dev, n_orders, l, coef_dev, cf,
+                                                                          heads > 0 ? heads : 1,
+                                                                          tc_coef_stride(heads > 0 ? heads : 1, l));
     return cudaGetLastError();
 }
 
@@ -1060,7 +1141,8 @@ cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, co
                                         227 * 1024);                                                           \
         });                                                                                                    \
         if (e != cudaSuccess) return e;                                                                        \
-        batch_fwd_tc_kernel<HV><<<grid, kTcThreads, sm, stream>>>((const float*)slabs, l, coef,                \
+        batch_fwd_tc_kernel<HV><<<grid, kTcThreads, sm, stream>>>((const float*)slabs, l,                      \
+                                                                  batch_coef_f(coef, graphs * HV, l),          \
                                                                   (const float2*)x, (float2*)y, graphs, stages); \
     }
         FGB_BATCH_HEADS(FGB_BFT)
@@ -1117,7 +1199,8 @@ cudaError_t launch_batch_dlda(const void* slabs, int graphs, int n, int l, const
                                         227 * 1024);                                                           \
         });                                                                                                    \
         if (e != cudaSuccess) return e;                                                                        \
-        batch_dlda_tc_kernel<HV><<<grid, kTcThreads, sm, stream>>>((const float*)slabs, l, coef,               \
+        batch_dlda_tc_kernel<HV><<<grid, kTcThreads, sm, stream>>>((const float*)slabs, l,                     \
+                                                                   batch_coef_f(coef, graphs * HV, l),         \
                                                                    (const float2*)gcot, (const float2*)x,      \
                                                                    dlda, graphs, stages);                      \
     }

@@ -44,7 +44,9 @@ cudaError_t launch_dots_rows(const void* rowp, const void* colp, int n, int r0, 
                              int64_t m_stride, int n_alpha, double* partial, double* s_out, cudaStream_t stream,
                              bool real);
 size_t dots_rows_partial_elems(int n, int rows, int l, int n_alpha);
-cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream);
+cudaError_t launch_batch_coef(const double* alphas_dev, int n_orders, int l, double* coef_dev, cudaStream_t stream,
+                              int heads = 0);
+size_t batch_coef_bytes(int graphs, int heads, int l);  // the doubles + the tcgen05 kernels' FP32 table
 cudaError_t launch_batch_to_tiled(const void* src, int graphs, int n, int l, int k, void* dst, bool real,
                                   cudaStream_t stream);
 cudaError_t launch_batch_forward(const void* slabs, int graphs, int n, int l, const double* coef, int heads,

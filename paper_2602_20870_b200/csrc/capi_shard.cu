@@ -580,8 +580,8 @@ namespace fgbi {
 int batch_coefs(fgfrft_cache* c, const double* alphas_dev, int heads, double** coef) {
     const size_t orders = (size_t)c->graphs * heads;
     c->coef_l = -1;  // the host-table memo no longer describes `coef`
-    FGB_CUDA(c->coef.ensure(orders * 2 * (2 * c->l + 1) * sizeof(double)));
-    FGB_LAUNCH(launch_batch_coef(alphas_dev, (int)orders, c->l, c->coef.as<double>(), c->stream), 1);
+    FGB_CUDA(c->coef.ensure(batch_coef_bytes((int)c->graphs, heads, c->l)));
+    FGB_LAUNCH(launch_batch_coef(alphas_dev, (int)orders, c->l, c->coef.as<double>(), c->stream, heads), 1);
     *coef = c->coef.as<double>();
     return FGFRFT_OK;
 }
