@@ -31,7 +31,8 @@ constexpr int kBMaxCh = 64;
 constexpr int kBSlab = 4 * kTileElems;  // elements per padded slab
 
 // coef[o][2][2l+1] (c then dc) for every order o; heads > 0: also the FP32 copy the tcgen05 kernels
-// stream, [g][h][2][2l+1] at a 16-byte padded per-graph stride (tc_coef_stride), after the doubles.
+// stream, per graph [c_k | c_-k | c'_k | c'_-k][k = 0..l][4 heads] (one 16-byte load per power and
+// table, heads padded to 4; tc_coef_stride floats), after the doubles.
 __global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_orders, int l, double* __restrict__ coef,
                                   float* __restrict__ coef_f, int heads, int fstride) {
     const int w = 2 * l + 1;
@@ -43,9 +44,14 @@ __global__ void batch_coef_kernel(const double* __restrict__ alphas, int n_order
     coef[(size_t)o * 2 * w + t] = c;
     coef[(size_t)o * 2 * w + w + t] = d;
     if (coef_f) {
-        float* f = coef_f + (size_t)(o / heads) * fstride + (o % heads) * 2 * w;
-        f[t] = (float)c;
-        f[w + t] = (float)d;
+        float* f = coef_f + (size_t)(o / heads) * fstride + (o % heads);
+        const int k = t - l, kk = k >= 0 ? k : -k, tb = k >= 0 ? 0 : 1, q = 4 * (l + 1);
+        f[tb * q + 4 * kk] = (float)c;
+        f[(2 + tb) * q + 4 * kk] = (float)d;
+        if (k == 0) {
+            f[q] = (float)c;
+            f[3 * q] = (float)d;
+        }
     }
 }
 
@@ -646,7 +652,7 @@ struct TcRing {
 // Per-graph series coefficients, FP32 (batch_coef_kernel's second table): [h][c | c'][2l + 1] at a
 // per-graph stride padded to 16 bytes, double-buffered in shared memory by graph parity and
 // bulk-copied by the producer ahead of the graph's first ring item (no CTA barrier per graph).
-__host__ __device__ constexpr int tc_coef_stride(int heads, int l) { return (2 * heads * (2 * l + 1) + 3) & ~3; }
+__host__ __device__ constexpr int tc_coef_stride(int heads, int l) { return 16 * (l + 1) + 0 * heads; }
 
 struct TcCoefs {
     float* buf;      // [2][stride]
@@ -692,11 +698,21 @@ __device__ __forceinline__ void tc_init_barriers(uint64_t* bars, int stages, int
     fence_mbar_init();
 }
 
+// ring depth cap (FGFRFT_TC_STAGES: experiments only)
+static int tc_max_stages() {
+    static const int v = [] {
+        const char* e = std::getenv("FGFRFT_TC_STAGES");
+        const int s = e ? std::atoi(e) : kTcMaxStages;
+        return s >= 3 && s <= kTcMaxStages ? s : kTcMaxStages;
+    }();
+    return v;
+}
+
 size_t batch_tc_fwd_smem(int l, int heads, int* stages) {
     const size_t ops = (size_t)((heads + 1) / 2) * 2 * 16384 + 2 * 16384;  // Q tiles hi / lo, X^T hi / lo
     const size_t fixed = ops + kTcBars * 8 + 16 + 2 * (size_t)tc_coef_stride(heads, l) * 4 + 128;
     int st = (int)((227 * 1024 - fixed) / kTcItem);
-    if (st > kTcMaxStages) st = kTcMaxStages;
+    if (st > tc_max_stages()) st = tc_max_stages();
     if (stages) *stages = st;
     return fixed + (size_t)st * kTcItem;
 }
@@ -792,22 +808,20 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const float* __restr
         TcCursor rc;
         int t = 0, pg = -1;
         for (int g = blockIdx.x; g < graphs; g += gridDim.x, ++t) {
-            const float* cs = cf.wait(t);  // [h][c (w) | c' (w)]
+            const float4* cs = reinterpret_cast<const float4*>(cf.wait(t));  // [c_k | c_-k][k][4 heads]
             float q[H][8];
+            {
+                const float4 c0 = cs[0];
+                const float c0v[4] = {c0.x, c0.y, c0.z, c0.w};
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
-                const float c0 = cs[h * 2 * w + l];
+                for (int h = 0; h < H; ++h)
 #pragma unroll
-                for (int u = 0; u < 8; ++u) q[h][u] = (i == 8 * jb + u) ? c0 : 0.f;
+                    for (int u = 0; u < 8; ++u) q[h][u] = (i == 8 * jb + u) ? c0v[h] : 0.f;
             }
             for (int k = 1; k <= l; ++k) {
                 const float* tp = reinterpret_cast<const float*>(ring.wait(rc));
-                float a[H], b[H];
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    a[h] = cs[h * 2 * w + l + k];
-                    b[h] = cs[h * 2 * w + l - k];
-                }
+                const float4 av = cs[k], bv = cs[l + 1 + k];
+                const float a[4] = {av.x, av.y, av.z, av.w}, b[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int j = 8 * jb + u;
@@ -844,10 +858,17 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const float* __restr
                 for (int hh = 0; hh < 2; ++hh) {
                     const float2* xr = reinterpret_cast<const float2*>(ring.wait(rc));
                     if (hh == half) {
+                        // chunk (m + kc / 2) % 4 first: the 8 lanes of a channel then hit 8 distinct
+                        // 16-byte bank groups (kc * 64 bytes alone covers only two)
+                        const int rot = kc >> 1;
+                        float4 ld[4];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+                            ld[m] = *reinterpret_cast<const float4*>(xr + cl * kBN + 8 * kc + 2 * ((m + rot) & 3));
                         float re[8], im[8];
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const float4 v = *reinterpret_cast<const float4*>(xr + cl * kBN + 8 * kc + 2 * m);
+                        for (int m = 0; m < 4; ++m) {  // chunk m was loaded as ld[(m - rot) & 3]
+                            const float4 v = rot == 0 ? ld[m] : rot == 1 ? ld[(m + 3) & 3] : rot == 2 ? ld[(m + 2) & 3] : ld[(m + 1) & 3];
                             re[2 * m] = v.x;
                             im[2 * m] = v.y;
                             re[2 * m + 1] = v.z;
@@ -890,7 +911,7 @@ size_t batch_tc_dlda_smem(int l, int heads, int* stages) {
     const size_t fixed = 2 * 16384 + mreg + kTcBars * 8 + 16 + 2 * (size_t)tc_coef_stride(heads, l) * 4 +
                          kTcWarps * kBMaxHeads * 8 + 128;
     int st = (int)((227 * 1024 - fixed) / kTcItem);
-    if (st > kTcMaxStages) st = kTcMaxStages;
+    if (st > tc_max_stages()) st = tc_max_stages();
     if (stages) *stages = st;
     return fixed + (size_t)st * kTcItem;
 }
@@ -1022,15 +1043,19 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const float* __rest
                 m[h][4] = b.x; m[h][5] = b.y; m[h][6] = b.z; m[h][7] = b.w;
             }
             tc_compute_sync();  // the region is the next graph's G tile
-            const float* dcs = cf.wait(t) + w;  // c'_k of head h at dcs[h 2w + l + k]
+            const float4* dcs = reinterpret_cast<const float4*>(cf.wait(t)) + 2 * (l + 1);  // [c'_k | c'_-k][k][4]
             float dl[H];
+            {
+                const float4 d0 = dcs[0];
+                const float d0v[4] = {d0.x, d0.y, d0.z, d0.w};
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
-                float d = 0.f;
+                for (int h = 0; h < H; ++h) {
+                    float d = 0.f;
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (i == 8 * jb + u) d = m[h][u];
-                dl[h] = dcs[h * 2 * w + l] * d;  // c'_0 Re tr(M_h)
+                    for (int u = 0; u < 8; ++u)
+                        if (i == 8 * jb + u) d = m[h][u];
+                    dl[h] = d0v[h] * d;  // c'_0 Re tr(M_h)
+                }
             }
             for (int k = 1; k <= l; ++k) {
                 const float* tp = reinterpret_cast<const float*>(ring.wait(rc));
@@ -1049,9 +1074,10 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const float* __rest
                 }
                 ring.release(rc, lane);
                 rc.next(stages);
+                const float4 dpv = dcs[k], dmv = dcs[l + 1 + k];
+                const float dp[4] = {dpv.x, dpv.y, dpv.z, dpv.w}, dm[4] = {dmv.x, dmv.y, dmv.z, dmv.w};
 #pragma unroll
-                for (int h = 0; h < H; ++h)
-                    dl[h] = fmaf(dcs[h * 2 * w + l + k], vp[h], fmaf(dcs[h * 2 * w + l - k], vm[h], dl[h]));
+                for (int h = 0; h < H; ++h) dl[h] = fmaf(dp[h], vp[h], fmaf(dm[h], vm[h], dl[h]));
             }
             cf.release(t, lane);
             // FP32 per thread (8 elements x 2l + 1 terms), FP64 across the 512 threads
