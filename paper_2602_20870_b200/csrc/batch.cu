@@ -734,7 +734,7 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const float* __restr
     uint64_t* opready = bars + 2 * kTcMaxStages + 4;
     uint64_t* mmadone = opready + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kTcBars);
-    const int w = 2 * l + 1, cst = tc_coef_stride(H, l);
+    const int cst = tc_coef_stride(H, l);
     const TcCoefs cf{tc_align16(tslot + 4), bars + 2 * kTcMaxStages, bars + 2 * kTcMaxStages + 2, cst};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) tc_init_barriers(bars, stages, kTcWarps);
@@ -932,7 +932,7 @@ batch_dlda_tc_kernel(const float* __restrict__ slabs, int l, const float* __rest
     uint64_t* opready = bars + 2 * kTcMaxStages + 4;
     uint64_t* mmadone = opready + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + kTcBars);
-    const int w = 2 * l + 1, cst = tc_coef_stride(H, l);
+    const int cst = tc_coef_stride(H, l);
     const TcCoefs cf{tc_align16(tslot + 4), bars + 2 * kTcMaxStages, bars + 2 * kTcMaxStages + 2, cst};
     double* red = reinterpret_cast<double*>(cf.buf + 2 * cst);  // [16 warps][4]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -247,8 +247,10 @@ void destroy_cache(fgfrft_cache* c) {
         b->release();
     if (c->coef_h) cudaFreeHost(c->coef_h);
     if (c->coef_evt) cudaEventDestroy(c->coef_evt);
-    if (c->nd_h) cudaFreeHost(c->nd_h);
-    if (c->nd_evt) cudaEventDestroy(c->nd_evt);
+    for (int q = 0; q < fgfrft_cache::kNdRing; ++q) {
+        if (c->nd_hr[q]) cudaFreeHost(c->nd_hr[q]);
+        if (c->nd_evr[q]) cudaEventDestroy(c->nd_evr[q]);
+    }
     if (c->xc_evt) cudaEventDestroy(c->xc_evt);
     if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
     if (c->pk_s) cudaStreamDestroy(c->pk_s);
@@ -552,7 +554,23 @@ uint64_t power_slice_bytes(const fgfrft_cache* c) {
     const uint64_t rows = 2 * (uint64_t)c->l * pad_rows(c->n);
     return (uint64_t)oz_slices_default() * rows * pad_k(c->n) + rows * 12;
 }
+// The node operators' A operand: element-PAIR rows by default (row = the element pair (i, j), (j, i)
+// of a tile pair, K = the L powers of both elements: half the bytes of the element-row form, whose
+// K stacked P_k(i, j) and P_k(j, i) for every element, so every power was stored twice) -- the
+// same values per row, so the same slicing error. FGFRFT_NODE_PAIRS=0: the element-row form.
+static bool node_pairs_wanted() {
+    static const bool v = [] {
+        const char* e = std::getenv("FGFRFT_NODE_PAIRS");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return v;
+}
+
 uint64_t elem_slice_bytes(const fgfrft_cache* c) {
+    if (node_pairs_wanted()) {
+        const uint64_t rows = dsynth_cache_rows((int)c->n);
+        return (uint64_t)oz_slices_default() * rows * dsynth_kp(c->l) + rows * 12;
+    }
     const uint64_t rows = pad_rows(c->n * c->n);
     return (uint64_t)oz_slices_default() * rows * pad_k(2 * (int64_t)c->l) + rows * 12;
 }
@@ -595,6 +613,21 @@ bool use_node_route(const fgfrft_cache* c, int n_alpha, int64_t b) {
 int ensure_elem_slices(fgfrft_cache* c) {
     const int S = oz_slices_default();
     if (c->es_slices == S) return FGFRFT_OK;
+    if (node_pairs_wanted()) {
+        const int64_t rows = (int64_t)dsynth_cache_rows((int)c->n), kp = dsynth_kp(c->l);
+        FGB_CUDA(c->es.ensure((size_t)S * rows * kp));
+        FGB_CUDA(c->ee.ensure((size_t)rows * sizeof(int)));
+        FGB_CUDA(c->erm.ensure((size_t)rows * sizeof(unsigned long long)));
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_dsynth_build(static_cast<const double*>(c->slabs), (int)c->n, c->l, (int)kp,
+                                       c->es.as<int8_t>(), c->ee.as<int>(), c->erm.as<unsigned long long>(), c->stream,
+                                       S),
+                   3);
+        c->es_slices = S;
+        c->es_pairs = true;
+        c->aux_bytes += elem_slice_bytes(c);
+        return FGFRFT_OK;
+    }
     const int64_t n = c->n, rows = pad_rows(n * n), kp = pad_k(2 * (int64_t)c->l);
     FGB_CUDA(c->es.ensure((size_t)S * rows * kp));
     FGB_CUDA(c->ee.ensure((size_t)rows * sizeof(int)));
@@ -735,7 +768,9 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
     }
     const double w = hi - lo;
     if (!(w > 1e-9)) return false;
-    for (int r = std::max(6, (int)std::floor(8.0 + 4.2 * w)); r <= node_max_terms(); ++r)
+    // the element-pair node operators hold 2r <= 64 output columns (one B tile)
+    const int rmax = node_pairs_wanted() ? std::min(node_max_terms(), kOzTileB / 2) : node_max_terms();
+    for (int r = std::max(6, (int)std::floor(8.0 + 4.2 * w)); r <= rmax; ++r)
         if (node_plan_r(alphas, na, c->l, need_d, c->coef_h, r, p.tab, p.d0, p.pw, &p.rp)) {
             p.r = r;
             p.ok = true;
@@ -746,12 +781,69 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
     return p.ok;
 }
 
+// The element-pair form of node_products: one INT8 GEMM over the pair-major slices (L terms per
+// element instead of 2L) with 2r output columns (W_j at the pair's element and at its mirror),
+// the diagonal and the row maxima of W fused into the epilogue (ozgemm pair mode).
+static int node_products_pairs(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0, int r,
+                               const void* x_dev, int64_t b, bool upload) {
+    const int S = c->es_slices;
+    const int64_t n = c->n, rows = (int64_t)dsynth_cache_rows((int)n), kp = dsynth_kp(c->l), bp = kOzTileB;
+    if (upload) {
+        FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
+        FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
+        FGB_CUDA(cudaMemcpyAsync(c->nd_tab.p, c->nd_h, tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        FGB_CUDA(cudaMemcpyAsync(c->nd_d0.p, c->nd_h + tab.size(), d0.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    }
+    FGB_CUDA(c->nd_bsl.ensure((size_t)S * bp * kp));
+    FGB_CUDA(c->nd_bex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
+    int* be = c->nd_bex.as<int>();
+    {  // B rows 2x + m: node x's coefficients in the pair order (OzView mode 8)
+        OzView v{c->nd_tab.as<double>(), 2 * c->l + 1, 0, 0, 0, 0, 2 * r, (int)bp, 1, (int)kp, (int)kp, false};
+        v.tiled = 8;
+        v.l = c->l;
+        ProfScope ps(KC_SLICE, c->stream);
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->nd_bsl.as<int8_t>(), be,
+                                   reinterpret_cast<unsigned long long*>(be + bp), c->stream),
+                   3);
+    }
+    const size_t nn = (size_t)n * n;
+    FGB_CUDA(c->nd_w.ensure((size_t)r * nn * 8));
+    FGB_CUDA(c->nd_z.ensure((size_t)r * n * b * 16));
+    const int64_t wrows = (int64_t)r * pad_rows(n);
+    FGB_CUDA(c->qsl.ensure((size_t)S * wrows * pad_k(n)));
+    FGB_CUDA(c->qex.ensure((size_t)wrows * (sizeof(int) + sizeof(unsigned long long))));
+    FGB_CUDA(cudaMemsetAsync(c->qex.as<int>() + wrows, 0, (size_t)wrows * sizeof(unsigned long long), c->stream));
+    {
+        OzOut out;
+        out.c = c->nd_w.as<double>();
+        out.ldc = (int64_t)nn;
+        out.sc = 0;
+        out.mv = (int)rows;
+        out.mp = (int)rows;
+        out.nv = 2 * r;
+        out.rmax = reinterpret_cast<unsigned long long*>(c->qex.as<int>() + wrows);
+        out.dg = c->nd_d0.as<double>();
+        out.rnp = (int)pad_rows(n);
+        out.pair_nt = (int)ceil_div(n, kTile);
+        out.pair_n = (int)n;
+        ProfScope ps(KC_NODEOP, c->stream);
+        FGB_LAUNCH(launch_ozgemm_ex(S, 0, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(), be,
+                                    (int)bp, (int)kp, out, c->stream),
+                   1);
+    }
+    return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, true);
+}
+
 // W_j = sum_k c_k(a_j) P_k (INT8 GEMM over the element-row slices) and Z'_j = W_j X.
 int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0, int r,
                   const void* x_dev, int64_t b, bool upload) {
     if (int st = ensure_elem_slices(c)) return st;
     const int S = c->es_slices;
     const int T = 2 * c->l + 1;
+    if (c->es_pairs) {
+        if (r > kOzTileB / 2) return fail(FGFRFT_NUMERICAL, "node route: more nodes than the pair form holds");
+        return node_products_pairs(c, tab, d0, r, x_dev, b, upload);
+    }
     const int64_t n = c->n, rows = pad_rows(n * n), kp = pad_k(2 * (int64_t)c->l), bp = kOzTileB;
     if (upload) {
         FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
@@ -823,19 +915,23 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
     return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, fused);
 }
 
-// Copy the plan's tables into the pinned staging (after the previous call's uploads have read
-// it) and upload the interpolation weights; node_products uploads the rest from the same staging.
+// Copy the plan's tables into the next pinned staging slot (after the uploads of the call that
+// last used it, kNdRing calls ago, have read it) and upload the interpolation weights;
+// node_products uploads the rest from the same slot.
 int node_stage(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0,
                const std::vector<double>& pw) {
     const size_t need = tab.size() + d0.size() + pw.size();
-    if (c->nd_evt) FGB_CUDA(cudaEventSynchronize(c->nd_evt));
-    if (c->nd_h_cap < need) {
-        if (c->nd_h) cudaFreeHost(c->nd_h);
-        c->nd_h = nullptr;
-        c->nd_h_cap = 0;
-        FGB_CUDA(cudaMallocHost(&c->nd_h, need * 8));
-        c->nd_h_cap = need;
+    const int q = (c->nd_slot + 1) % fgfrft_cache::kNdRing;
+    if (c->nd_evr[q]) FGB_CUDA(cudaEventSynchronize(c->nd_evr[q]));
+    if (c->nd_hr_cap[q] < need) {
+        if (c->nd_hr[q]) cudaFreeHost(c->nd_hr[q]);
+        c->nd_hr[q] = nullptr;
+        c->nd_hr_cap[q] = 0;
+        FGB_CUDA(cudaMallocHost(&c->nd_hr[q], need * 8));
+        c->nd_hr_cap[q] = need;
     }
+    c->nd_slot = q;
+    c->nd_h = c->nd_hr[q];
     std::memcpy(c->nd_h, tab.data(), tab.size() * 8);
     std::memcpy(c->nd_h + tab.size(), d0.data(), d0.size() * 8);
     std::memcpy(c->nd_h + tab.size() + d0.size(), pw.data(), pw.size() * 8);
@@ -847,8 +943,9 @@ int node_stage(fgfrft_cache* c, const std::vector<double>& tab, const std::vecto
 
 // record that the staging may be reused once the uploads enqueued so far have run
 int node_staged(fgfrft_cache* c) {
-    if (!c->nd_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->nd_evt, cudaEventDisableTiming));
-    FGB_CUDA(cudaEventRecord(c->nd_evt, c->stream));
+    cudaEvent_t& ev = c->nd_evr[c->nd_slot];
+    if (!ev) FGB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FGB_CUDA(cudaEventRecord(ev, c->stream));
     return FGFRFT_OK;
 }
 

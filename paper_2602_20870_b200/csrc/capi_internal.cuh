@@ -324,10 +324,17 @@ struct fgfrft_cache {
     // operators W_j and their products Z'_j = W_j X.
     int last_route = -1, last_nodes = 0;  // route of the last sweep (fgfrft_cache_route_info)
     int es_slices = 0;
+    bool es_pairs = false;  // es holds element-PAIR rows (pair-major, L terms per element) instead of element rows
     DevBuf es, ee, erm, nd_tab, nd_p, nd_d0, nd_bsl, nd_bex, nd_w, nd_z;
-    double* nd_h = nullptr;  // pinned staging of the per-call node tables
-    size_t nd_h_cap = 0;
-    cudaEvent_t nd_evt = nullptr;
+    // pinned staging of the per-call node tables: a ring of 3, so the host plans and stages the next
+    // calls while the device still runs this one (a single buffer made every call wait for the
+    // previous call's GEMMs, exposing the host planning on the device timeline)
+    static constexpr int kNdRing = 3;
+    double* nd_h = nullptr;  // the current slot's buffer
+    double* nd_hr[kNdRing] = {};
+    size_t nd_hr_cap[kNdRing] = {};
+    cudaEvent_t nd_evr[kNdRing] = {};
+    int nd_slot = 0;
     struct NodePlan {  // memoised plan of the last sweep (a pure function of the orders)
         std::vector<double> alphas, tab, d0, pw;
         bool need_d = false, ok = false;

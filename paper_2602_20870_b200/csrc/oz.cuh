@@ -33,6 +33,9 @@ struct OzView {
                      //    K < kp / 2: P_(K+1)(32 I + i, 32 J + j), K >= kp / 2: the mirror
                      //    P_(K-kp/2+1)(32 J + j, 32 I + i) (tiled slabs: sbatch = slab elements,
                      //    nt, l = L, tp2 = n)
+                     // 8: node coefficient rows for element-pair operands (ozgemm pair mode):
+                     //    row 2x + m, K < kp / 2: c_x(+-(K + 1)), K >= kp / 2: c_x(-+(K - kp/2 + 1))
+                     //    (+ for m = 0 in the first half); src = r x rs table, c_k at column l + k
                      // 6: element rows of the stacked cache (the basis synthesis GEMM): row
                      //    e = i + j n (rv = n^2, tp2 = n), K term kk < L: P_(kk+1)(i, j), L <= kk < 2L:
                      //    P_(kk-L+1)(j, i); one batch block (nb = 1, rp = padded n^2)
@@ -89,6 +92,12 @@ struct OzOut {
     const double* dx = nullptr;
     const double* dgc = nullptr;
     int64_t dgs = 0;
+    // CM 0 node operators over ELEMENT-PAIR rows (A = the pair-major slices of OzView mode 7, B =
+    // mode 8 coefficient rows): pair_nt > 0 = tiles per side. Output column 2x + m is node x's
+    // operator at element e (m = 0) or its mirror e' (m = 1), stored at c + x * ldc + column-major
+    // (pair_n x pair_n); dg[x] added on the diagonal; rmax[x * rnp + row] = the row maxima (zeroed
+    // by the caller). Each CTA takes the 8 M tiles of a tile pair in a row.
+    int pair_nt = 0, pair_n = 0;
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)
@@ -106,7 +115,8 @@ int dsynth_slices();
 int dsynth_kp(int l);  // K of the digit cache: 2 x pad64(L)
 size_t dsynth_coef_bytes(int kp);
 cudaError_t launch_dsynth_build(const double* slabs, int n, int l, int kp, int8_t* digits, int* exps,
-                                unsigned long long* rowmax_tmp, cudaStream_t stream);
+                                unsigned long long* rowmax_tmp, cudaStream_t stream, int slices = 0);
+size_t dsynth_cache_rows(int n);  // element-pair rows (128-row tiles, 8 per tile pair)
 cudaError_t launch_dsynth_coefs(const double* coef, int coef_ld, int l_used, int ac, int kp, int8_t* bsl,
                                 cudaStream_t stream);
 cudaError_t launch_dsynth(const int8_t* digits, const int* exps, const int8_t* bsl, int kp, int n, int p0, int p1,

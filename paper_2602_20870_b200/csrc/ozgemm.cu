@@ -105,6 +105,14 @@ __device__ __forceinline__ double oz_load(const OzView& v, int row, int k) {
     }
     const int bt = row / v.rp, r = row - bt * v.rp;
     if (r >= v.rv || k >= v.kv) return 0.0;
+    if (v.tiled == 8) {
+        const int x = r >> 1, kh = v.kp >> 1;
+        const bool hi = k >= kh;
+        const int kk = hi ? k - kh : k;
+        if (kk >= v.l) return 0.0;
+        const bool neg = hi != (bool)(r & 1);
+        return v.src[(int64_t)x * v.rs + v.l + (neg ? -(kk + 1) : kk + 1)];
+    }
     if (v.tiled == 4) {
         const int kk = k;
         if (kk >= 2 * v.l) return 0.0;
@@ -446,8 +454,12 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     // unit schedule: strided over the clusters. Row-max node operators (out.rmax): the host sizes
     // the grid as a multiple of the row blocks per column (rn / 128), so every unit of a CTA lies in
     // the same row block and the row max stays in registers until one flush at the end
-    const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32;  // (the skinny epilogue)
-    const int ub = cid, ue = units, us = nclusters;
+    // pair mode (out.pair_nt): a CTA takes the 8 M tiles of one tile pair in a row (row maxima of
+    // the pair's rows stay in registers across them)
+    const bool pairs = CM == 0 && CL == 1 && out.pair_nt > 0;
+    const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32 && !pairs;  // (the skinny epilogue)
+    const int ub = pairs ? cid * 8 : cid, ue = units, us = nclusters;
+    auto next_u = [&](int u) { return pairs ? ((u & 7) == 7 ? u + 8 * us - 7 : u + 1) : u + us; };
     auto unit_mt = [&](int u) { return u / ngroups; };
     auto unit_nt = [&](int u) { return (u % ngroups) * CL + rank; };
 
@@ -455,7 +467,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
         if (lane == 0) {
             const uint64_t keep = policy_evict_last();  // B (the small operand) is reread by every A tile
             int it = 0;  // global K-block counter across units
-            for (int u = ub; u < ue; u += us) {
+            for (int u = ub; u < ue; u = next_u(u)) {
                 const int mt = unit_mt(u), nt = unit_nt(u);
                 const unsigned char* ga = reinterpret_cast<const unsigned char*>(a) + (int64_t)mt * kblocks * Cfg::a_stage;
                 const unsigned char* gb = reinterpret_cast<const unsigned char*>(b) + (int64_t)nt * kblocks * Cfg::b_stage;
@@ -475,7 +487,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     } else if (warp == 1) {
         if (lane == 0) {
             int it = 0, tcount = 0;
-            for (int u = ub; u < ue; u += us, ++tcount) {
+            for (int u = ub; u < ue; u = next_u(u), ++tcount) {
                 const int buf = tcount % NB;
                 if (tcount >= NB) mbar_wait(tempty + buf, ((tcount / NB) - 1) & 1);  // epilogue drained it
                 tc_fence_after();
@@ -516,6 +528,18 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
             for (int c = 0; c < kOzEC; ++c) lacc[c] = 0.0;
         }
+        double prm[kOzEC / 2];  // pair mode: running max of rows 32I + i over the pair's tiles
+#pragma unroll
+        for (int q = 0; q < kOzEC / 2; ++q) prm[q] = 0.0;
+        // pair mode: the column scales 2^e_n and the diagonal terms in shared memory (the CM 2
+        // exchange region), the next unit's row exponent prefetched, the pair's (I, J) per pair
+        int ea_nx = 0, pI = 0, pJ = 0;
+        if (CM == 0 && pairs) {
+            for (int t = threadIdx.x - 64; t < kOzBN + 32; t += 32 * kOzEpiWarps)
+                xchg[t] = t < kOzBN ? pow2(eb[t]) : (t - kOzBN < out.nv / 2 ? out.dg[t - kOzBN] : 0.0);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kOzEpiWarps) : "memory");
+            if (ub < ue) ea_nx = ea[ub * kOzBM + lrow];
+        }
         double rmx[8];  // chunk mode: running row max of this thread's 8 columns over the row block
         int rib = -1;
         auto flush_rmax = [&](int live) {
@@ -526,13 +550,13 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                     atomicMax(out.rmax + (int64_t)(h * ((out.nv + 3) >> 2) + q) * out.rnp + rib * kOzBM + lrow,
                               (unsigned long long)__double_as_longlong(rmx[q]));
         };
-        for (int u = ub; u < ue; u += us, ++tcount) {
+        for (int u = ub; u < ue; u = next_u(u), ++tcount) {
             const int mt = unit_mt(u), nt = unit_nt(u);
             const int buf = tcount % NB;
             mbar_wait(tfull + buf, (tcount / NB) & 1);
             tc_fence_after();
             constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
-            if (BN != kOzBN || (CM == 0 && out.npeers == 0 && out.nv - nt * kOzBN <= 32)) {
+            if (BN != kOzBN || (CM == 0 && out.npeers == 0 && out.nv - nt * kOzBN <= 32 && !pairs)) {
                 // Skinny output (the node operators: r <= 32 of the 64 tile columns are real): the w
                 // live columns are split evenly over the 4 column warps (warp h owns cw = ceil(w / 4)
                 // columns from h cw), so only live columns are drained and folded and the per-unit
@@ -694,6 +718,55 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                             const double r = yv - xcp;
                             lacc[c] = fma(r, r, lacc[c]);
                         }
+                    }
+                }
+                continue;
+            }
+            if (CM == 0 && pairs) {
+                // element pair row m: tile pair p, t = 128 (mt % 8) + lrow -> (i, j) = (t % 32, t / 32)
+                const int t = m & 1023, pi = t & 31, pj = t >> 5;
+                if ((mt & 7) == 0 || tcount == 0) pair_of_imajor(m >> 10, out.pair_nt, pI, pJ);
+                const int I = pI, J = pJ;
+                const int ri = I * 32 + pi, cj = J * 32 + pj, nn = out.pair_n;
+                const bool ok = ri < nn && cj < nn, diag = I == J;
+                const double ra = pow2(ea_nx) * kOzScale;
+                {
+                    const int un = next_u(u);
+                    ea_nx = un < ue ? ea[un * kOzBM + lrow] : 0;
+                }
+                const double* sct = xchg + h * kOzEC;
+#pragma unroll
+                for (int q = 0; q < kOzEC / 2; ++q) {
+                    const int x = (nt * kOzBN + h * kOzEC) / 2 + q;
+                    if (2 * x >= out.nv) break;  // warp-uniform
+                    double w0 = val[2 * q] * ra * sct[2 * q];
+                    double w1 = val[2 * q + 1] * ra * sct[2 * q + 1];
+                    if (diag && pi == pj) {
+                        w0 += xchg[kOzBN + x];
+                        w1 += xchg[kOzBN + x];
+                    }
+                    double* o = out.c + (int64_t)x * out.ldc;
+                    if (ok) {
+                        __stcs(o + (int64_t)cj * nn + ri, w0);  // W_x[32I + i, 32J + j]: lanes along rows
+                        prm[q] = fmax(prm[q], fabs(w0));
+                    }
+                    if (!diag) {  // W_x[32J + j, 32I + i]; row 32J + j is warp-uniform
+                        if (ok) __stcs(o + (int64_t)ri * nn + cj, w1);
+                        if (out.rmax) {
+                            const unsigned hw = (unsigned)((unsigned long long)__double_as_longlong(ok ? fabs(w1) : 0.0) >> 32);
+                            const unsigned mx = __reduce_max_sync(0xffffffffu, hw);
+                            if (lane == 0 && mx && cj < nn)
+                                atomicMax(out.rmax + (int64_t)x * out.rnp + cj, (unsigned long long)mx << 32);
+                        }
+                    }
+                }
+                if ((mt & 7) == 7) {  // the pair's last tile: rows 32I + i are complete for this thread
+#pragma unroll
+                    for (int q = 0; q < kOzEC / 2; ++q) {
+                        const int x = (nt * kOzBN + h * kOzEC) / 2 + q;
+                        if (out.rmax && 2 * x < out.nv && prm[q] > 0.0 && ri < nn)
+                            atomicMax(out.rmax + (int64_t)x * out.rnp + ri, (unsigned long long)__double_as_longlong(prm[q]));
+                        prm[q] = 0.0;
                     }
                 }
                 continue;
@@ -1200,7 +1273,7 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
     }
     if (out.max_ctas > 0 && out.max_ctas / CL < max_clusters) max_clusters = out.max_ctas / CL > 0 ? out.max_ctas / CL : 1;
     int clusters = units < max_clusters ? units : max_clusters;
-    if (CM == 0 && CL == 1 && out.rmax) {  // row-max mode: a multiple of the row blocks per column
+    if (CM == 0 && CL == 1 && out.rmax && !out.pair_nt) {  // row-max mode: a multiple of the row blocks per column
         const int ibs = out.rn / kOzBM;
         if (clusters >= ibs) clusters = clusters / ibs * ibs;
     }
@@ -1292,7 +1365,7 @@ size_t dsynth_coef_bytes(int kp) { return (size_t)ds_b_bytes(kp) + kDsBN * sizeo
 
 // The digit cache from the tiled FP64 slabs: OzView mode 7, 5 digits, 128-row tiles.
 cudaError_t launch_dsynth_build(const double* slabs, int n, int l, int kp, int8_t* digits, int* exps,
-                                unsigned long long* rowmax_tmp, cudaStream_t stream) {
+                                unsigned long long* rowmax_tmp, cudaStream_t stream, int slices) {
     const int nt = (int)ceil_div(n, kTile);
     OzView v{slabs, 0, 0, (int64_t)nt * nt * kTileElems, 0, 0, (int)dsynth_cache_rows(n), (int)dsynth_cache_rows(n),
              1, kp, kp, true};
@@ -1300,7 +1373,7 @@ cudaError_t launch_dsynth_build(const double* slabs, int n, int l, int kp, int8_
     v.nt = nt;
     v.l = l;
     v.tp2 = n;
-    return launch_oz_slice(v, kDsSA, kOzBM, digits, exps, rowmax_tmp, stream);
+    return launch_oz_slice(v, slices > 0 ? slices : kDsSA, kOzBM, digits, exps, rowmax_tmp, stream);
 }
 
 // Coefficient digits for `ac` operator rows (table rows of width coef_ld, c_k at l_used + k) into
