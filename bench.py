@@ -448,7 +448,8 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     # budget: the reference count L N^2 16 B (17.2 GB) + the packed slabs (5.4 GB) the step route uses
-    cache = fg.PowerCache(cfg.f, L, memory_budget=24 << 30, device=local)
+    # + the order window's node operators (2.5 GB, secondary line)
+    cache = fg.PowerCache(cfg.f, L, memory_budget=32 << 30, device=local)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     real = cache.is_real()
@@ -622,11 +623,66 @@ def main():
     e2e_ms = max(e2e_dev_ms, t_wall * 1e3)
 
     extras = {}
+    win_out = None
     if not args.no_extras:
         try:
             extras["c2_sweep"] = c2_sweep(fg, torch, stream, local)
         except Exception as ex:  # secondary line only
             extras["c2_sweep"] = {"error": str(ex)}
+        # the same step with an order window declared (fgfrft_cache_set_order_window [0, 2]): Q, dQ/da
+        # interpolated from r exact node operators (built once, like the power cache) instead of the
+        # 64 packed powers -- a secondary line; the headline stays on the reference's series route
+        try:
+            t0 = time.perf_counter()
+            nodes = cache.set_order_window(0.0, 2.0)
+            win_build_s = time.perf_counter() - t0
+            loss_w = torch.empty(2, dtype=torch.float64, device=dev)
+            dlda_w = torch.empty(2, dtype=torch.float64, device=dev)
+
+            def step_win(i):
+                fg._check(L_.fgfrft_mse_step_dev(cache.handle, al[i & 1].ctypes.data, 1, xd.data_ptr(), xcd.data_ptr(),
+                                                 b, None, loss_w[i & 1:].data_ptr(), dlda_w[i & 1:].data_ptr()))
+
+            ms_w = timed_events(stream, step_win, args.steps, warm=args.warmup)
+            route_w = cache.route_info()
+            fg.profile_enable(True)
+            fg.profile_read(reset=True)
+            with torch.cuda.stream(stream):
+                for i in range(args.steps):
+                    step_win(i)
+            torch.cuda.synchronize()
+            prof_w = fg.profile_read(reset=True)
+            fg.profile_enable(False)
+            win_out = (loss_w.cpu().numpy().copy(), dlda_w.cpu().numpy().copy())
+            for i in range(args.warmup):
+                step_e2e(i)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            t_w = time.perf_counter()
+            for i in range(args.steps):
+                step_e2e(i)
+            e1.record(stream)
+            e1.synchronize()
+            e2e_w = max(e0.elapsed_time(e1) / args.steps, (time.perf_counter() - t_w) / args.steps * 1e3)
+            syn_w = prof_w.get("synthesis", (0.0, 0))
+            syn_ms = syn_w[0] / args.steps if syn_w[1] else None
+            wbytes = nodes * n * n * 8 + 2 * n * n * 8
+            extras["order_window_step"] = {
+                "workload": "config 3 step as the headline, order window [0, 2] declared",
+                "route": {"route": route_w[0], "nodes": route_w[1]}, "window_build_s": win_build_s,
+                "ms_per_step": ms_w, "value": n * b / (ms_w * 1e-3), "unit": UNIT,
+                "e2e": {"value": n * b / (e2e_w * 1e-3), "unit": UNIT, "ms_per_step": e2e_w},
+                "kernel_classes_ms_per_step": {k: v[0] / args.steps for k, v in prof_w.items() if v[1]},
+                "synthesis_roofline": ({"kernel": "window_synth_kernel<2> (node operators -> Q, dQ/da + row maxima)",
+                                        "algorithmic_bytes": wbytes, "achieved_gbs": wbytes / (syn_ms * 1e-3) / 1e9,
+                                        "peak": peaks["hbm_gbs"],
+                                        "frac": wbytes / (syn_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                                        "algorithmic": f"{nodes} node operators x N^2 x 8 B read + Q, dQ 2 N^2 x 8 B "
+                                                       f"written"} if syn_ms else None)}
+            cache.set_order_window(0.0, 0.0)
+        except Exception as ex:  # secondary line only
+            extras["order_window_step"] = {"error": str(ex)}
 
     # ---- parity of the timed step against the oracle (rank 0; the oracle cache is reused by the CPU
     # baseline below). After every GPU timing: the oracle's BLAS threads keep spinning for a while
@@ -641,6 +697,10 @@ def main():
         check = []
         for i, a in enumerate(ALPHAS):
             lr, dr = oracle_step(O, ocache, cfg.x, cfg.x_clean, a, cores)
+            if win_out is not None:
+                extras["order_window_step"].setdefault("parity_check", []).append(
+                    {"alpha": a, "loss_rel_err": abs(float(win_out[0][i]) - lr) / abs(lr),
+                     "dlda_rel_err": abs(float(win_out[1][i]) - dr) / max(abs(dr), 1e-300)})
             check.append({"alpha": a, "loss": float(step_out[0][i]), "loss_ref": lr,
                           "loss_rel_err": abs(float(step_out[0][i]) - lr) / abs(lr),
                           "dlda": float(step_out[1][i]), "dlda_ref": dr,

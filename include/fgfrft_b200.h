@@ -160,6 +160,15 @@ int fgfrft_cache_orthogonality(const fgfrft_cache* cache, double* residual);
 /* Build lazily-built device structures now (the INT8 digit slices of the stacked cache for the
  * power-product route); a no-op for handles that never use them. Synchronises. */
 int fgfrft_cache_prepare(fgfrft_cache* cache);
+
+// Order window (an extension, no reference counterpart): declare the orders the caller will step
+// with. Builds r exact FP64 node operators Q(x_j) - c_0(x_j) I at the Chebyshev nodes of [lo, hi]
+// (r ~ 9 + 5 (hi - lo); r n^2 8 bytes, counted against the memory budget), after which the one- /
+// two-order step and apply routes synthesise Q(a), dQ/da of orders inside [lo, hi] from them --
+// r slabs instead of the L powers (the coefficients are interpolated to 4e-15 of the largest;
+// orders outside the window take the packed route). hi <= lo clears it. Real F, n >= 512 only.
+int fgfrft_cache_set_order_window(fgfrft_cache* cache, double lo, double hi);
+int fgfrft_cache_order_window(const fgfrft_cache* cache, double* lo, double* hi, int* nodes);
 int fgfrft_cache_device_slab(fgfrft_cache* cache, int k, void** dptr);
 int fgfrft_cache_device_bytes(const fgfrft_cache* cache, uint64_t* bytes);
 

@@ -125,6 +125,8 @@ def lib() -> ctypes.CDLL:
         "fgfrft_denoise_fit": (i, [vp, i, d, d, vp, vp, vp, vp, vp, vp, vp]),
         "fgfrft_cache_orthogonality": (i, [vp, vp]),
         "fgfrft_cache_prepare": (i, [vp]),
+        "fgfrft_cache_set_order_window": (i, [vp, d, d]),
+        "fgfrft_cache_order_window": (i, [vp, vp, vp, vp]),
         "fgfrft_dgemm_int8_dev": (i, [i, i, i64, i64, i64, vp, i64, vp, i64, vp, i64, i, vp]),
         "fgfrft_spectrum_create": (i, [vp, vp, i64, i, pp]),
         "fgfrft_spectrum_decompose": (i, [vp, i64, i, pp]),
@@ -189,7 +191,7 @@ def exported_symbols():
         "fgfrft_batch_forward_dev", "fgfrft_batch_dlda_dev", "fgfrft_dgemm_int8_dev", "fgfrft_cache_set_engine",
         "fgfrft_int8_digits", "fgfrft_step_int8_digits", "fgfrft_cache_orthogonality", "fgfrft_denoise_create", "fgfrft_denoise_destroy",
         "fgfrft_denoise_eval", "fgfrft_denoise_fit",
-        "fgfrft_cache_prepare", "fgfrft_spectrum_create", "fgfrft_spectrum_decompose", "fgfrft_spectrum_destroy",
+        "fgfrft_cache_prepare", "fgfrft_cache_set_order_window", "fgfrft_cache_order_window", "fgfrft_spectrum_create", "fgfrft_spectrum_decompose", "fgfrft_spectrum_destroy",
         "fgfrft_spectrum_info", "fgfrft_spectrum_vectors", "fgfrft_spectrum_set_stream", "fgfrft_exact",
         "fgfrft_exact_dev", "fgfrft_cascade_create", "fgfrft_cascade_destroy", "fgfrft_cascade_eval",
         "fgfrft_cascade_learn", "fgfrft_cache_save", "fgfrft_cache_load", "fgfrft_shard_mse_dlda_partial_dev",
@@ -330,7 +332,8 @@ class PowerCache:
     def route_info(self):
         """(route, nodes) of the last MSE step: 0 synthesis, 1 power products, 2 node interpolation,
         3 packed (Q, dQ/da from the packed slabs + one Ozaki GEMM [Y; dY] = [Q; dQ] X), 4 the same
-        step with Q, dQ/da synthesised on the INT8 tensor cores from the digit cache."""
+        step with Q, dQ/da synthesised on the INT8 tensor cores from the digit cache, 5 the same step
+        with Q, dQ/da interpolated from the order window's node operators (nodes = their count)."""
         r, k = ctypes.c_int(), ctypes.c_int()
         _check(lib().fgfrft_cache_route_info(self._h, ctypes.addressof(r), ctypes.addressof(k)))
         return r.value, k.value
@@ -366,6 +369,20 @@ class PowerCache:
     def prepare(self) -> None:
         """Build lazily-built device structures (INT8 digit slices of the cache) now."""
         _check(lib().fgfrft_cache_prepare(self._h))
+
+    def set_order_window(self, lo: float, hi: float) -> int:
+        """Declare the orders the caller will step with (fgfrft_cache_set_order_window): r exact node
+        operators at the Chebyshev nodes of [lo, hi]; one / two-order steps and applies with orders
+        inside take them instead of the L packed powers. hi <= lo clears. Returns r."""
+        _check(lib().fgfrft_cache_set_order_window(self._h, float(lo), float(hi)))
+        return self.order_window()[2]
+
+    def order_window(self):
+        """(lo, hi, nodes) of the declared order window (nodes 0: none)."""
+        lo, hi, r = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        _check(lib().fgfrft_cache_order_window(self._h, ctypes.addressof(lo), ctypes.addressof(hi),
+                                               ctypes.addressof(r)))
+        return lo.value, hi.value, r.value
 
     def device_bytes(self) -> int:
         b = ctypes.c_uint64()

@@ -15,6 +15,37 @@
 
 namespace fgbi {
 
+// Host-side time of the per-call planning stages (FGFRFT_HOST_PROF=1: printed at exit) -- the order
+// sweeps' host work must stay under their device time or the device idles between calls.
+struct HostProf {
+    const bool on = [] {
+        const char* e = std::getenv("FGFRFT_HOST_PROF");
+        return e && std::atoi(e) == 1;
+    }();
+    double t[8] = {};
+    long n[8] = {};
+    ~HostProf() {
+        if (!on) return;
+        static const char* names[8] = {"upload_coefs", "node_plan", "node_stage", "node_products", "combine",
+                                       "mse_step_dev", "", ""};
+        for (int k = 0; k < 8; ++k)
+            if (n[k]) std::fprintf(stderr, "[fgfrft host] %-14s %8.1f us/call (%ld calls)\n", names[k], t[k] / n[k] * 1e6, n[k]);
+    }
+};
+static HostProf g_hprof;
+struct HostTimer {
+    int k;
+    std::chrono::steady_clock::time_point t0;
+    explicit HostTimer(int k_) : k(k_) {
+        if (g_hprof.on) t0 = std::chrono::steady_clock::now();
+    }
+    ~HostTimer() {
+        if (!g_hprof.on) return;
+        g_hprof.t[k] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        ++g_hprof.n[k];
+    }
+};
+
 thread_local std::string g_err;
 thread_local bool tl_internal_signals = false;
 std::atomic<uint64_t> g_launches{0};
@@ -90,14 +121,17 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
         return FGFRFT_OK;
     }
     c->coef_l = -1;
-    if (c->coef_evt) FGB_CUDA(cudaEventSynchronize(c->coef_evt));
-    if (c->coef_h_cap < count) {
-        if (c->coef_h) cudaFreeHost(c->coef_h);
-        c->coef_h = nullptr;
-        c->coef_h_cap = 0;
-        FGB_CUDA(cudaMallocHost(&c->coef_h, count * sizeof(double)));
-        c->coef_h_cap = count;
+    const int q = (c->coef_slot + 1) % fgfrft_cache::kCoefRing;
+    if (c->coef_evr[q]) FGB_CUDA(cudaEventSynchronize(c->coef_evr[q]));  // its upload, kCoefRing calls ago
+    if (c->coef_hr_cap[q] < count) {
+        if (c->coef_hr[q]) cudaFreeHost(c->coef_hr[q]);
+        c->coef_hr[q] = nullptr;
+        c->coef_hr_cap[q] = 0;
+        FGB_CUDA(cudaMallocHost(&c->coef_hr[q], count * sizeof(double)));
+        c->coef_hr_cap[q] = count;
     }
+    c->coef_slot = q;
+    c->coef_h = c->coef_hr[q];
     // 2 (2L+1) libm evaluations per order: spread an order sweep over the host cores
     const int nthr = std::min(8, std::max(1, n_alpha / 8));
 #pragma omp parallel for schedule(static) num_threads(nthr) if (nthr > 1)
@@ -105,8 +139,8 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
         host_sinc_coeffs(alphas[a], l, c->coef_h + a * width, c->coef_h + ((size_t)n_alpha + a) * width);
     FGB_CUDA(c->coef.ensure(count * sizeof(double)));
     FGB_CUDA(cudaMemcpyAsync(c->coef.p, c->coef_h, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    if (!c->coef_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->coef_evt, cudaEventDisableTiming));
-    FGB_CUDA(cudaEventRecord(c->coef_evt, c->stream));
+    if (!c->coef_evr[q]) FGB_CUDA(cudaEventCreateWithFlags(&c->coef_evr[q], cudaEventDisableTiming));
+    FGB_CUDA(cudaEventRecord(c->coef_evr[q], c->stream));
     c->coef_alphas.assign(alphas, alphas + n_alpha);
     c->coef_l = l;
     *dev = c->coef.as<double>();
@@ -243,10 +277,12 @@ void destroy_cache(fgfrft_cache* c) {
                       &c->loss, &c->dlda, &c->tmp, &c->ps, &c->pe, &c->prm, &c->xsl, &c->xex, &c->z, &c->qsl,
                       &c->qex, &c->ps3, &c->pe3, &c->plr, &c->zd, &c->zaux, &c->cdig, &c->cex, &c->bx, &c->bxc,
                       &c->by, &c->es, &c->ee, &c->erm, &c->nd_tab, &c->nd_p, &c->nd_d0, &c->nd_bsl, &c->nd_bex,
-                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ds, &c->dse, &c->dsb, &c->ydy, &c->pp, &c->ppc, &c->rb, &c->bar})
+                      &c->nd_w, &c->nd_z, &c->pk, &c->pks, &c->ds, &c->dse, &c->dsb, &c->win, &c->ydy, &c->pp, &c->ppc, &c->rb, &c->bar})
         b->release();
-    if (c->coef_h) cudaFreeHost(c->coef_h);
-    if (c->coef_evt) cudaEventDestroy(c->coef_evt);
+    for (int q = 0; q < fgfrft_cache::kCoefRing; ++q) {
+        if (c->coef_hr[q]) cudaFreeHost(c->coef_hr[q]);
+        if (c->coef_evr[q]) cudaEventDestroy(c->coef_evr[q]);
+    }
     for (int q = 0; q < fgfrft_cache::kNdRing; ++q) {
         if (c->nd_hr[q]) cudaFreeHost(c->nd_hr[q]);
         if (c->nd_evr[q]) cudaEventDestroy(c->nd_evr[q]);
@@ -490,15 +526,19 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
                    2);
         return FGFRFT_OK;
     }
-    if ((n_alpha == 1 || n_alpha == 2 || n_alpha == 4) && packed_enabled(c) && use_int8_gemm(c, b) &&
-        ensure_step_cache(c)) {
+    if ((n_alpha == 1 || n_alpha == 2 || n_alpha == 4) && packed_enabled(c) && use_int8_gemm(c, b)) {
         // Q(a)^T = Q(-a) bit-exactly (sinc.hpp coefficient mirror): the inverse synthesises Q(-a)
-        if (inverse) {
-            std::vector<double> al(alphas, alphas + n_alpha);
+        std::vector<double> al(alphas, alphas + n_alpha);
+        if (inverse)
             for (double& v : al) v = -v;
-            if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
+        WindowWeights ww;
+        const bool win = window_weights(c, al.data(), n_alpha, false, l_used, &ww);
+        if (win || ensure_step_cache(c)) {
+            if (inverse)
+                if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
+            return packed_products(c, coef, 2 * l_used + 1, n_alpha, x_dev, b, y_dev, l_used, nullptr,
+                                   win ? &ww : nullptr);
         }
-        return packed_products(c, coef, 2 * l_used + 1, n_alpha, x_dev, b, y_dev, l_used);
     }
     const int chunk = alpha_chunk(c, n_alpha);
     FGB_CUDA(c->q.ensure((size_t)chunk * sl * c->elem));
@@ -557,11 +597,15 @@ uint64_t power_slice_bytes(const fgfrft_cache* c) {
 // The node operators' A operand: element-PAIR rows by default (row = the element pair (i, j), (j, i)
 // of a tile pair, K = the L powers of both elements: half the bytes of the element-row form, whose
 // K stacked P_k(i, j) and P_k(j, i) for every element, so every power was stored twice) -- the
-// same values per row, so the same slicing error. FGFRFT_NODE_PAIRS=0: the element-row form.
+// same values per row, so the same slicing error. Measured at config 2 it reads half the bytes (427
+// vs 812 MB, ncu) but runs 0.217 vs 0.182 ms: 2r = 38 output columns need the 64-column B tile,
+// whose 6 digit-sum accumulators (384 TMEM columns) leave room for ONE buffer, so every unit's MMAs
+// wait for the previous unit's epilogue; the element-row form's 32-column tiles double-buffer. Opt-in
+// (FGFRFT_NODE_PAIRS=1) until the pair form is split into two 32-column units per tile.
 static bool node_pairs_wanted() {
     static const bool v = [] {
         const char* e = std::getenv("FGFRFT_NODE_PAIRS");
-        return !(e && std::atoi(e) == 0);
+        return e && std::atoi(e) == 1;
     }();
     return v;
 }
@@ -710,43 +754,47 @@ static bool node_plan_r(const double* alphas, int na, int l, bool need_d, const 
             if (dj) dj[j] = lj[j] * (-1.0 / (x - xn[j]) + sw2 / sw);
         }
     }
-    // check the interpolated coefficients against the exact ones on every order
-    double cmax = 0.0, dmax = 0.0, ce = 0.0, de = 0.0;
+    *rp_out = rp;
+    // The derivative weights l_j'(a) amplify the node operators' INT8 error (~5e-14 of |W_j|) by
+    // sum_j |l_j'(a)| ~ 420 / width: capped at 5000 (width >~ 0.08; the parity tests hold 1e-10 at
+    // width 0.1) -- narrower sweeps take the power route (2L products, no derivative amplification).
+    if (need_d)
+        for (int a = 0; a < na; ++a) {
+            double t = 0.0;
+            for (int j = 0; j < r; ++j) t += std::fabs(pw[(size_t)(na + a) * rp + j]);
+            if (t > 5000.0) return false;
+        }
+    // check the interpolated coefficients against the exact ones on every order, leaving at the
+    // first miss (the search tries node counts upward: only the accepted count runs the whole check)
+    double cmax = 0.0, dmax = 0.0;
+    for (int a = 0; a < na; ++a)
+        for (int q = 0; q < T; ++q) {
+            cmax = std::max(cmax, std::fabs(coef_h[(size_t)a * T + q]));
+            if (need_d) dmax = std::max(dmax, std::fabs(coef_h[(size_t)(na + a) * T + q]));
+        }
+    const double ctol = 4e-15 * cmax, dtol = 2e-12 * std::max(dmax, 1e-300);
     std::vector<double> vc((size_t)T), vd((size_t)T);
+    double* __restrict__ pc = vc.data();
+    double* __restrict__ pd = vd.data();
     for (int a = 0; a < na; ++a) {
         const double* c = coef_h + (size_t)a * T;
         const double* dc = coef_h + (size_t)(na + a) * T;
         std::fill(vc.begin(), vc.end(), 0.0);
         std::fill(vd.begin(), vd.end(), 0.0);
         for (int j = 0; j < r; ++j) {
-            const double* tj = &tab[(size_t)j * T];
-            const double pl = pw[(size_t)a * rp + j], pd = need_d ? pw[(size_t)(na + a) * rp + j] : 0.0;
+            const double* __restrict__ tj = &tab[(size_t)j * T];
+            const double pl = pw[(size_t)a * rp + j], pdj = need_d ? pw[(size_t)(na + a) * rp + j] : 0.0;
             for (int q = 0; q < T; ++q) {
-                vc[q] += pl * tj[q];
-                vd[q] += pd * tj[q];
+                pc[q] += pl * tj[q];
+                pd[q] += pdj * tj[q];
             }
         }
         for (int q = 0; q < T; ++q) {
-            cmax = std::max(cmax, std::fabs(c[q]));
-            ce = std::max(ce, std::fabs(vc[q] - c[q]));
-            if (need_d) {
-                dmax = std::max(dmax, std::fabs(dc[q]));
-                de = std::max(de, std::fabs(vd[q] - dc[q]));
-            }
+            if (std::fabs(pc[q] - c[q]) > ctol) return false;
+            if (need_d && std::fabs(pd[q] - dc[q]) > dtol) return false;
         }
     }
-    *rp_out = rp;
-    // The derivative weights l_j'(a) amplify the node operators' INT8 error (~5e-14 of |W_j|) by
-    // sum_j |l_j'(a)| ~ 420 / width: capped at 5000 (width >~ 0.08; the parity tests hold 1e-10 at
-    // width 0.1) -- narrower sweeps take the power route (2L products, no derivative amplification).
-    double lsum = 0.0;
-    if (need_d)
-        for (int a = 0; a < na; ++a) {
-            double t = 0.0;
-            for (int j = 0; j < r; ++j) t += std::fabs(pw[(size_t)(na + a) * rp + j]);
-            lsum = std::max(lsum, t);
-        }
-    return ce <= 4e-15 * cmax && (!need_d || (de <= 2e-12 * std::max(dmax, 1e-300) && lsum <= 5000.0));
+    return true;
 }
 
 bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* r_out, int* rp_out) {
@@ -770,10 +818,17 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
     if (!(w > 1e-9)) return false;
     // the element-pair node operators hold 2r <= 64 output columns (one B tile)
     const int rmax = node_pairs_wanted() ? std::min(node_max_terms(), kOzTileB / 2) : node_max_terms();
-    for (int r = std::max(6, (int)std::floor(8.0 + 4.2 * w)); r <= rmax; ++r)
+    // the search starts one below the count the last sweep of (almost) the same width needed -- the
+    // counts below it fail their first orders cheaply, but each still costs its node table
+    int r0 = std::max(6, (int)std::floor(8.0 + 4.2 * w));
+    if (p.hint_r > 0 && p.hint_need_d == need_d && std::fabs(p.hint_w - w) <= 1e-6 * w) r0 = std::max(r0, p.hint_r - 1);
+    for (int r = r0; r <= rmax; ++r)
         if (node_plan_r(alphas, na, c->l, need_d, c->coef_h, r, p.tab, p.d0, p.pw, &p.rp)) {
             p.r = r;
             p.ok = true;
+            p.hint_r = r;
+            p.hint_w = w;
+            p.hint_need_d = need_d;
             break;
         }
     *r_out = p.r;
@@ -955,14 +1010,22 @@ int mse_node_route(fgfrft_cache* c, const double* alphas, int n_alpha, const voi
                    int64_t b, void* y_dev, double* loss_dev, double* dlda_dev, bool need_d, bool* ran) {
     *ran = false;
     int r = 0, rp = 0;
-    if (!node_plan(c, alphas, n_alpha, need_d, &r, &rp)) return FGFRFT_OK;
+    {
+        HostTimer ht(1);
+        if (!node_plan(c, alphas, n_alpha, need_d, &r, &rp)) return FGFRFT_OK;
+    }
     auto& p = c->nd_plan;
     // a memoised plan's tables are still on the device from the call that staged them: no host
     // staging, no wait on that call's uploads
     const bool upload = !p.staged;
-    if (upload)
+    if (upload) {
+        HostTimer ht(2);
         if (int st = node_stage(c, p.tab, p.d0, p.pw)) return st;
-    if (int st = node_products(c, p.tab, p.d0, r, x_dev, b, upload)) return st;
+    }
+    {
+        HostTimer ht(3);
+        if (int st = node_products(c, p.tab, p.d0, r, x_dev, b, upload)) return st;
+    }
     if (upload) {
         if (int st = node_staged(c)) return st;
         p.staged = true;
@@ -1442,6 +1505,62 @@ bool packed_enabled(const fgfrft_cache* c) {
            engine_of(c) == FGFRFT_ENGINE_AUTO;
 }
 
+// ---- the order window: node operators for the orders a caller declares it will use
+//
+// Q(a) is analytic in a, and over a bounded window [lo, hi] the r-point Chebyshev interpolant of its
+// series coefficients matches them to 4e-15 of the largest (2e-12 for the derivatives) with r ~ 9 + 5
+// (hi - lo) -- the node route's criterion (node_plan_r), here checked on 513 orders of the window.
+// So Q(a) = sum_j l_j(a) W_j and dQ/da = sum_j l_j'(a) W_j with W_j = Q(x_j), exact FP64: r slabs
+// instead of L powers per step (config 3, [0, 2]: 19 x 134 MB = 2.5 GB against 5.4 GB packed).
+// The c_0 I terms stay out of W'_j = W_j - c_0(x_j) I: the product GEMM's epilogue adds the exact
+// c_0(a), c'_0(a) (the nodiag form of the packed route).
+
+// barycentric weights l_j(x) (and l_j'(x)) on the nodes xn with weights bw
+static void bary_weights(const std::vector<double>& xn, const std::vector<double>& bw, double x, double* lj,
+                         double* dj) {
+    const int r = (int)xn.size();
+    int hit = -1;
+    for (int j = 0; j < r; ++j)
+        if (std::fabs(x - xn[j]) < 1e-14 * std::max(1.0, std::fabs(x))) hit = j;
+    if (hit >= 0) {  // on a node: Kronecker weights, the derivative row of the differentiation matrix
+        for (int j = 0; j < r; ++j) lj[j] = j == hit ? 1.0 : 0.0;
+        if (dj) {
+            double diag = 0.0;
+            for (int j = 0; j < r; ++j)
+                if (j != hit) {
+                    dj[j] = (bw[j] / bw[hit]) / (xn[hit] - xn[j]);
+                    diag -= dj[j];
+                }
+            dj[hit] = diag;
+        }
+        return;
+    }
+    double sw = 0.0, sw2 = 0.0;
+    for (int j = 0; j < r; ++j) {
+        const double t = bw[j] / (x - xn[j]);
+        sw += t;
+        sw2 += t / (x - xn[j]);
+    }
+    for (int j = 0; j < r; ++j) {
+        const double t = bw[j] / (x - xn[j]);
+        lj[j] = t / sw;
+        if (dj) dj[j] = lj[j] * (-1.0 / (x - xn[j]) + sw2 / sw);
+    }
+}
+
+bool window_weights(const fgfrft_cache* c, const double* alphas, int n_alpha, bool with_d, int l_used,
+                    WindowWeights* ww) {
+    if (!c->win_r || l_used != c->l) return false;
+    const int rows = with_d ? 2 * n_alpha : n_alpha;
+    if (rows > 4) return false;
+    const double eps = 1e-12 * (1.0 + std::max(std::fabs(c->win_lo), std::fabs(c->win_hi)));
+    for (int a = 0; a < n_alpha; ++a)
+        if (!(alphas[a] >= c->win_lo - eps && alphas[a] <= c->win_hi + eps)) return false;
+    for (int a = 0; a < n_alpha; ++a)
+        bary_weights(c->win_xn, c->win_bw, alphas[a], ww->w[a], with_d ? ww->w[n_alpha + a] : nullptr);
+    return true;
+}
+
 // true when the packed slabs are resident (built on first use, counted against the budget).
 bool ensure_packed(fgfrft_cache* c) {
     if (c->pk_state) return c->pk_state > 0;
@@ -1650,7 +1769,7 @@ int ensure_pipe_streams(fgfrft_cache* c) {
 // aux stream, and the GEMM runs per chunk as its columns land, so the host->device transfer
 // overlaps the synthesis (which does not need X) and the earlier chunks' products.
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
-                    void* y, int l_used, const double* x_host) {
+                    void* y, int l_used, const double* x_host, const WindowWeights* ww) {
     const int S = step_slices();
     const int64_t n = c->n, mp = pad_rows(n), sl = n * n, kp = pad_k(n);
     const int64_t bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
@@ -1662,7 +1781,7 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         c->pk_plan = pk_plan(n, rows, b, l_used);
         c->pk_plan_key = key;
     }
-    if (x_host && c->pk_plan.size() > 1) {  // the chunked host-X form runs one shell
+    if ((x_host || ww) && c->pk_plan.size() > 1) {  // the chunked host-X form / the window run one shell
         c->pk_plan.assign(1, PkShell{0, (int)n, 0, -1});
         c->pk_plan_key = 0;
     }
@@ -1715,10 +1834,12 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
                    3);
     }
     FGB_CUDA(cudaMemsetAsync(rmax, 0, (size_t)rows * mp * sizeof(unsigned long long), c->pk_s));
-    // synthesis engine: tensor-core digits (dsynth) or the packed FP64 decode (psynth)
-    const bool tc = dsynth_wanted() && c->ds_state > 0;
+    // synthesis engine: the window's node operators, tensor-core digits (dsynth) or the packed FP64
+    // decode (psynth)
+    const bool tc = !ww && dsynth_wanted() && c->ds_state > 0;
     c->pk_tc = tc;
-    if (!tc && !ensure_packed(c)) return FGFRFT_CAPACITY;
+    c->pk_win = ww != nullptr;
+    if (!ww && !tc && !ensure_packed(c)) return FGFRFT_CAPACITY;
     const int64_t dkp = dsynth_kp(c->l);
     if (tc) {
         ProfScope ps(KC_SYNTH, c->pk_s);
@@ -1758,7 +1879,11 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         {
             ProfScope ps(KC_SYNTH, c->pk_s);
             // shell 0 runs alone (the GEMM has nothing yet): full grid; later shells share the GPU
-            if (tc)
+            if (ww)
+                FGB_LAUNCH(launch_window_synth(c->win.as<double>(), c->win_r, (int)n, *ww, rows, q, sl, rmax, mp,
+                                               c->pk_s),
+                           1);
+            else if (tc)
                 FGB_LAUNCH(launch_dsynth(c->ds.as<int8_t>(), c->dse.as<int>(), c->dsb.as<int8_t>(), (int)dkp, (int)n,
                                          sh.p0, sh.p1, coef, coef_ld, l_used, rows, q, sl, rmax, mp,
                                          s == 0 ? (int)pk_env("FGFRFT_SYN_CAP0", 0) : syn_cap, c->pk_s, 1),
@@ -1819,11 +1944,12 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
 }
 
 int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,
-                    void* y_dev, double* loss_dev, double* dlda_dev, const double* x_host, const double* xc_host) {
+                    void* y_dev, double* loss_dev, double* dlda_dev, const WindowWeights* ww, const double* x_host,
+                    const double* xc_host) {
     const int64_t n = c->n, blk = 2 * n * b;  // doubles per n x b complex block
     const int rows = 2 * n_alpha;             // table rows [c(a_0) ..][c'(a_0) ..]: Q_a then dQ_a
     FGB_CUDA(c->ydy.ensure((size_t)rows * blk * sizeof(double)));
-    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l, x_host)) return st;
+    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l, x_host, ww)) return st;
     if (xc_host) {  // Xc behind X on the aux stream: only the final loss pass needs it
         if (!c->xc_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->xc_evt, cudaEventDisableTiming));
         FGB_CUDA(cudaMemcpyAsync(const_cast<void*>(xc_dev), xc_host, (size_t)n * b * 16, cudaMemcpyHostToDevice,
@@ -1842,8 +1968,8 @@ int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void
                                  norm, loss_dev + a, dlda_dev + a, c->stream),
                    2);
     }
-    c->last_route = c->pk_tc ? 4 : 3;
-    c->last_nodes = 0;
+    c->last_route = c->pk_win ? 5 : c->pk_tc ? 4 : 3;
+    c->last_nodes = c->pk_win ? c->win_r : 0;
     return FGFRFT_OK;
 }
 
@@ -2020,6 +2146,68 @@ int fgfrft_cache_set_engine(fgfrft_cache* c, int engine) {
 int fgfrft_cache_orthogonality(const fgfrft_cache* c, double* residual) {
     if (int st = check_handle(c)) return st;
     if (residual) *residual = c->ortho_residual;
+    return FGFRFT_OK;
+}
+
+int fgfrft_cache_set_order_window(fgfrft_cache* c, double lo, double hi) {
+    FGB_GUARD_BEGIN
+    if (int st = check_handle(c)) return st;
+    if (!std::isfinite(lo) || !std::isfinite(hi)) return fail(FGFRFT_PARAMETER, "order window: bounds must be finite");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard dg(c->device);
+    if (c->win_r) {
+        c->aux_bytes -= (uint64_t)c->win_r * c->n * c->n * 8;
+        c->win.release();
+        c->win_r = 0;
+        c->win_xn.clear();
+        c->win_bw.clear();
+    }
+    if (!(hi > lo)) return FGFRFT_OK;  // cleared
+    if (!packed_enabled(c)) return fail(FGFRFT_PARAMETER, "order window: needs the packed step route (real F, n >= 512)");
+    const int l = c->l, T = 2 * l + 1, ns = 513;
+    std::vector<double> al((size_t)ns), coefs((size_t)2 * ns * T);
+    for (int i = 0; i < ns; ++i) {
+        al[i] = lo + (hi - lo) * (double)i / (double)(ns - 1);
+        host_sinc_coeffs(al[i], l, &coefs[(size_t)i * T], &coefs[(size_t)(ns + i) * T]);
+    }
+    std::vector<double> tab, d0, pw;
+    int r = 0, rp = 0;
+    for (int rr = std::max(6, (int)std::floor(8.0 + 4.2 * (hi - lo))); rr <= kWindowMaxNodes; ++rr)
+        if (node_plan_r(al.data(), ns, l, true, coefs.data(), rr, tab, d0, pw, &rp)) {
+            r = rr;
+            break;
+        }
+    if (!r) return fail(FGFRFT_PARAMETER, "order window: too wide for 48 interpolation nodes");
+    const uint64_t bytes = (uint64_t)r * c->n * c->n * 8;
+    if (!aux_fits(c, bytes)) return fail(FGFRFT_CAPACITY, "order window: node operators exceed the memory budget");
+    for (int j = 0; j < r; ++j) tab[(size_t)j * T + l] = 0.0;  // W'_j: c_0 I left out
+    DevBuf tmp;
+    FGB_CUDA(tmp.ensure(tab.size() * 8));
+    FGB_CUDA(c->win.ensure(bytes));
+    FGB_CUDA(cudaMemcpyAsync(tmp.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    if (int st = synth_into(c, tmp.as<double>(), r, l, c->win.p, true)) return st;
+    FGB_CUDA(cudaStreamSynchronize(c->stream));
+    c->win_xn.resize(r);
+    c->win_bw.resize(r);
+    const double mid = 0.5 * (lo + hi), half = 0.5 * (hi - lo);
+    for (int j = 0; j < r; ++j) {  // the nodes node_plan_r interpolated on
+        const double th = M_PI * (2.0 * j + 1.0) / (2.0 * r);
+        c->win_xn[j] = mid + half * std::cos(th);
+        c->win_bw[j] = ((j & 1) ? -1.0 : 1.0) * std::sin(th);
+    }
+    c->win_lo = lo;
+    c->win_hi = hi;
+    c->win_r = r;
+    c->aux_bytes += bytes;
+    return FGFRFT_OK;
+    FGB_GUARD_END
+}
+
+int fgfrft_cache_order_window(const fgfrft_cache* c, double* lo, double* hi, int* nodes) {
+    if (!c) return fail(FGFRFT_PARAMETER, "null cache handle");
+    if (lo) *lo = c->win_lo;
+    if (hi) *hi = c->win_hi;
+    if (nodes) *nodes = c->win_r;
     return FGFRFT_OK;
 }
 
@@ -2254,6 +2442,7 @@ int fgfrft_dlda(fgfrft_cache* c, const double* alphas, int n_alpha, const double
 
 int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, const void* x_dev, const void* xc_dev,
                         int64_t b, void* y_dev, void* loss_dev, void* dlda_dev) {
+    HostTimer ht_all(5);
     FGB_GUARD_BEGIN
     if (int st = check_handle(c)) return st;
     if (int st = check_alphas(alphas, n_alpha)) return st;
@@ -2288,7 +2477,10 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
         }
     } demote_y{c, y_c64, blk * n_alpha};
     double* coef = nullptr;
-    if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
+    {
+        HostTimer ht(0);
+        if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
+    }
     const double* dc_dev = coef + (size_t)n_alpha * width;
     if (use_power_route(c, n_alpha) && use_int8_combine(c)) {
         FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
@@ -2305,9 +2497,13 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
     c->last_route = use_power_route(c, n_alpha) ? 1 : 0;
     c->last_nodes = 0;
     if (!use_power_route(c, n_alpha) && n_alpha <= 2 && packed_enabled(c) && use_int8_gemm(c, b) &&
-        !use_fused_apply(c, n_alpha, b) && ensure_step_cache(c))
-        return mse_packed_step(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
-                               static_cast<double*>(dlda_dev));
+        !use_fused_apply(c, n_alpha, b)) {
+        WindowWeights ww;
+        const bool win = window_weights(c, alphas, n_alpha, true, c->l, &ww);
+        if (win || ensure_step_cache(c))
+            return mse_packed_step(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
+                                   static_cast<double*>(dlda_dev), win ? &ww : nullptr);
+    }
     if (use_power_route(c, n_alpha)) {
         FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
         if (int st = mse_power_route(c, coef, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
@@ -2408,8 +2604,11 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
         // overlap the synthesis and the earlier chunks' products, Xc behind it (mse_packed_step).
         std::lock_guard<std::mutex> lk(c->mu);
         DeviceGuard dg(c->device);
+        WindowWeights ww;
+        bool win = false;
         if (c->dtype == FGFRFT_C128 && !c->api_c64 && n_alpha <= 2 && packed_enabled(c) && use_int8_gemm(c, b) &&
-            !use_fused_apply(c, n_alpha, b) && !use_power_route(c, n_alpha) && ensure_step_cache(c)) {
+            !use_fused_apply(c, n_alpha, b) && !use_power_route(c, n_alpha) &&
+            ((win = window_weights(c, alphas, n_alpha, true, c->l, &ww)) || ensure_step_cache(c))) {
             const size_t xe = (size_t)c->n * b;
             FGB_CUDA(c->x.ensure(xe * 16));
             FGB_CUDA(c->xc.ensure(xe * 16));
@@ -2419,7 +2618,7 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
             if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
             double* ld = c->loss.as<double>();
             if (int st = mse_packed_step(c, coef, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha,
-                                         x, xc))
+                                         win ? &ww : nullptr, x, xc))
                 return st;
             std::vector<double> out(2 * (size_t)n_alpha);
             FGB_CUDA(cudaMemcpyAsync(out.data(), ld, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

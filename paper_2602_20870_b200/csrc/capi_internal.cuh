@@ -4,6 +4,7 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <complex>
 #include <dlfcn.h>
@@ -168,6 +169,9 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
 // packed.cu (the packed power cache and the one- / two-order step route)
 size_t packed_bytes(int n, int l);
 cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream);
+// the order window (packed.cu): Q_x = sum_j w[x][j] W'_j over r <= kWindowMaxNodes node operators
+cudaError_t launch_window_synth(const double* wops, int r, int n, const WindowWeights& ww, int rows, double* out,
+                                int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream);
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
                           int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0,
@@ -337,6 +341,9 @@ struct fgfrft_cache {
     int nd_slot = 0;
     struct NodePlan {  // memoised plan of the last sweep (a pure function of the orders)
         std::vector<double> alphas, tab, d0, pw;
+        int hint_r = 0;  // node count of the last accepted plan, its width: the next search's start
+        double hint_w = 0.0;
+        bool hint_need_d = false;
         bool need_d = false, ok = false;
         bool staged = false;  // tab / d0 / pw of this plan already resident in nd_tab / nd_d0 / nd_p
         int r = 0, rp = 0;
@@ -406,6 +413,14 @@ struct fgfrft_cache {
     // Replaces the packed slabs on the step route when it fits. 0 not built, 1 ready, -1 unavailable.
     int ds_state = 0;
     bool pk_tc = false;  // the last packed_products synthesised on the tensor cores
+    // the order window (fgfrft_cache_set_order_window): r exact FP64 node operators W'_j (c_0 I left
+    // out) at the Chebyshev nodes of [win_lo, win_hi]; the step route synthesises Q, dQ/da of orders
+    // inside it from these instead of the packed powers
+    DevBuf win;
+    int win_r = 0;
+    double win_lo = 0.0, win_hi = 0.0;
+    std::vector<double> win_xn, win_bw;
+    bool pk_win = false;  // the last packed_products synthesised from the window
     DevBuf ds, dse, dsb;
     // shell pipeline of the packed route: side streams (S synthesis + slicing, G GEMMs, high
     // priority), fork / join events, one event per shell, the memoised shell plan
@@ -415,9 +430,14 @@ struct fgfrft_cache {
     std::vector<cudaEvent_t> xh_ev;  // host-X column chunks landed (chunked host MSE step)
     std::vector<PkShell> pk_plan;
     uint64_t pk_plan_key = 0;
-    double* coef_h = nullptr;  // pinned staging for the coefficient tables
-    size_t coef_h_cap = 0;
-    cudaEvent_t coef_evt = nullptr;
+    // pinned staging for the coefficient tables: a ring of 3 (the host evaluates the next calls'
+    // tables while this call's upload is queued behind the device's work); coef_h = current slot
+    static constexpr int kCoefRing = 3;
+    double* coef_h = nullptr;
+    double* coef_hr[kCoefRing] = {};
+    size_t coef_hr_cap[kCoefRing] = {};
+    cudaEvent_t coef_evr[kCoefRing] = {};
+    int coef_slot = 0;
     std::vector<double> coef_alphas;  // orders of the tables now in `coef` / coef_h (memo)
     int coef_l = -1;
 
@@ -498,9 +518,13 @@ bool ensure_packed(fgfrft_cache* c);
 bool ensure_dsynth(fgfrft_cache* c);
 bool ensure_step_cache(fgfrft_cache* c);
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
-                    void* y, int l_used, const double* x_host = nullptr);
+                    void* y, int l_used, const double* x_host = nullptr, const WindowWeights* ww = nullptr);
+// true (and the weights rows [l_j(a) ..][l_j'(a) ..] when with_d) when every order lies in the window
+bool window_weights(const fgfrft_cache* c, const double* alphas, int n_alpha, bool with_d, int l_used,
+                    WindowWeights* ww);
 int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void* x_dev, const void* xc_dev, int64_t b,
-                    void* y_dev, double* loss_dev, double* dlda_dev, const double* x_host = nullptr,
+                    void* y_dev, double* loss_dev, double* dlda_dev, const WindowWeights* ww = nullptr,
+                    const double* x_host = nullptr,
                     const double* xc_host = nullptr);
 
 }  // namespace fgbi

@@ -186,4 +186,11 @@ __device__ __forceinline__ void pair_of_imajor(int p, int nt, int& I, int& J) {
     J = i + (int)(p - pairs_before(i, nt));
 }
 
+// The order window's per-call interpolation weights (packed.cu window_synth_kernel, passed by value):
+// rows [l_j(a) ..][l_j'(a) ..] over r <= kWindowMaxNodes node operators.
+constexpr int kWindowMaxNodes = 48;
+struct WindowWeights {
+    double w[4][kWindowMaxNodes];
+};
+
 }  // namespace fgb

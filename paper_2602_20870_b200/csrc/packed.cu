@@ -488,4 +488,84 @@ cudaError_t launch_mse_dy(const void* y, const void* dy, const void* xc, int64_t
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- the order window
+//
+// Node operators of a declared order window [lo, hi] (fgfrft_cache_set_order_window): W'_j =
+// sum_{k != 0} c_k(x_j) P_k at the r Chebyshev nodes x_j of the window, exact FP64 (synthesised
+// once by the FP64 series kernels), column-major n x n each. Per call, for orders inside the
+// window, Q(a) - c_0(a) I = sum_j l_j(a) W'_j and dQ/da - c'_0(a) I = sum_j l_j'(a) W'_j (barycentric
+// weights; the c_0 terms come back exactly in the product GEMM's epilogue): r slabs streamed instead
+// of the L packed powers. One thread per row over a 64-column chunk, all outputs per staged value;
+// row maxima of each output by atomicMax on the ordered bits (the Ozaki slicing reads them).
+namespace {
+template <int ROWS>
+__global__ void __launch_bounds__(256) window_synth_kernel(const double* __restrict__ wops, int r, int n, int64_t nn,
+                                                           WindowWeights ww, double* __restrict__ out,
+                                                           int64_t ostride, unsigned long long* __restrict__ rowmax,
+                                                           int64_t mp) {
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    const int j0 = blockIdx.y * 64, j1 = min(j0 + 64, n);
+    if (i >= n) return;
+    double mx[ROWS];
+#pragma unroll
+    for (int x = 0; x < ROWS; ++x) mx[x] = 0.0;
+    // two columns per pass, 16 node operators per batch of loads: 32 independent 8-byte loads in
+    // flight per thread before the first FMA (the first form, one load chain per column, ran at 0.60
+    // of the DRAM peak on long-scoreboard stalls)
+    for (int j = j0; j < j1; j += 2) {
+        const bool two = j + 1 < j1;
+        const double* p0 = wops + (int64_t)j * n + i;
+        const double* p1 = p0 + n;
+        double a0[ROWS], a1[ROWS];
+#pragma unroll
+        for (int x = 0; x < ROWS; ++x) a0[x] = a1[x] = 0.0;
+        for (int t0 = 0; t0 < r; t0 += 16) {
+            double v0[16], v1[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int t = t0 + u;
+                v0[u] = t < r ? __ldcs(p0 + (int64_t)t * nn) : 0.0;
+                v1[u] = (t < r && two) ? __ldcs(p1 + (int64_t)t * nn) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                if (t0 + u >= r) break;
+#pragma unroll
+                for (int x = 0; x < ROWS; ++x) {
+                    a0[x] = fma(ww.w[x][t0 + u], v0[u], a0[x]);
+                    a1[x] = fma(ww.w[x][t0 + u], v1[u], a1[x]);
+                }
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < ROWS; ++x) {
+            __stcs(out + x * ostride + (int64_t)j * n + i, a0[x]);
+            mx[x] = fmax(mx[x], fabs(a0[x]));
+            if (two) {
+                __stcs(out + x * ostride + (int64_t)(j + 1) * n + i, a1[x]);
+                mx[x] = fmax(mx[x], fabs(a1[x]));
+            }
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < ROWS; ++x)
+        if (mx[x] > 0.0) atomicMax(rowmax + x * mp + i, (unsigned long long)__double_as_longlong(mx[x]));
+}
+}  // namespace
+
+cudaError_t launch_window_synth(const double* wops, int r, int n, const WindowWeights& ww, int rows, double* out,
+                                int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream) {
+    if (r < 1 || r > kWindowMaxNodes) return cudaErrorInvalidValue;
+    const dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, 64));
+    const int64_t nn = (int64_t)n * n;
+    switch (rows) {
+        case 1: window_synth_kernel<1><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp); break;
+        case 2: window_synth_kernel<2><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp); break;
+        case 4: window_synth_kernel<4><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace fgb

@@ -189,22 +189,28 @@ def test_config3_headline_step_full_batch_dense_oracle():
     from threadpoolctl import threadpool_limits
     cfg = prep.config3()
     n, b = cfg.x.shape
-    cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=24 << 30)
+    cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=32 << 30)
     try:
         with threadpool_limits(os.cpu_count() or 1):
             o = O.PowerCache(cfg.f, cfg.l, memory_budget=1 << 40, real_recursion=True)
             for a in (0.37, -1.3):
-                loss, dl, y = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
-                assert cache.route_info()[0] in (3, 4)  # packed step: FP64-decode or tensor-core synthesis
                 q = O.fgfrft_matrix(o, a, nthreads=os.cpu_count() or 1)
                 yr = q @ cfg.x
                 r = yr - cfg.x_clean
                 lr = float(np.vdot(r, r).real) / (n * b)
                 dq = O.fgfrft_grad(o, a, nthreads=os.cpu_count() or 1)
                 dr = float(np.sum(np.conj(2.0 * r / (n * b)) * (dq @ cfg.x)).real)
-                assert rel(y[0], yr) <= 1e-10
-                assert abs(loss[0] - lr) <= 1e-10 * lr
-                assert abs(dl[0] - dr) <= 1e-10 * max(abs(dr), 1e-3)
+                # the packed route, then (a = 0.37) the order-window route over [0, 2] (node operators)
+                for window in ((None, (0.0, 2.0)) if a > 0 else (None,)):
+                    if window:
+                        assert cache.set_order_window(*window) > 0
+                    loss, dl, y = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
+                    assert cache.route_info()[0] == (5 if window else 3) or (not window and cache.route_info()[0] == 4)
+                    assert rel(y[0], yr) <= 1e-10, window
+                    assert abs(loss[0] - lr) <= 1e-10 * lr, window
+                    assert abs(dl[0] - dr) <= 1e-10 * max(abs(dr), 1e-3), window
+                    if window:
+                        cache.set_order_window(0.0, 0.0)
             # series vs exact: the GPU spectrum against the oracle's (CPU) decomposition
             a = 0.37
             eig_g = fg.eigendecompose_unitary(cfg.f)

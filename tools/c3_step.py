@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--sweep", default="", help="env settings to time in turn, e.g. "
                     "'FGFRFT_PIPE_SHELLS=1;FGFRFT_PIPE_SHELLS=4&FGFRFT_PIPE_GEMM_CTAS=100'")
     ap.add_argument("--trace", action="store_true", help="print the last step's launch timeline (sweep mode)")
+    ap.add_argument("--window", default="", help="declare an order window 'lo,hi' (node-operator route)")
     args = ap.parse_args()
     t0 = time.perf_counter()
     cfg = prep.config3() if args.config == "3" else prep.config4()
@@ -51,6 +52,10 @@ def main():
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     cache.set_stream(stream.cuda_stream)
+    if args.window and not args.pshard:
+        t1 = time.perf_counter()
+        print(json.dumps({"window": args.window, "nodes": cache.set_order_window(*map(float, args.window.split(","))),
+                          "window_build_s": time.perf_counter() - t1}), flush=True)
     al = [np.array([0.37]), np.array([0.63])]
     x = torch.from_numpy(np.ascontiguousarray(cfg.x.T)).cuda().to(ct)
     xc = torch.from_numpy(np.ascontiguousarray(cfg.x_clean.T)).cuda().to(ct)
@@ -124,7 +129,8 @@ def main():
     torch.cuda.synchronize()
     prof = {k: [v[0] / args.steps, v[1] / args.steps] for k, v in fg.profile_read(reset=True).items() if v[1]}
     fg.profile_enable(False)
-    print(json.dumps({"config": "C" + args.config, "c64": args.c64, "pshard": args.pshard, "n": n, "l": L, "b": b, "ms_per_step": ms,
+    print(json.dumps({"config": "C" + args.config, "c64": args.c64, "pshard": args.pshard, "n": n, "l": L, "b": b,
+                      "route": cache.route_info() if not args.pshard else None, "ms_per_step": ms,
                       "signal_nodes_per_s": n * b / (ms * 1e-3), "launches_per_step": launches,
                       "prep_s": prep_s, "build_s": build_s, "classes_ms_per_step": prof,
                       "loss": float(loss[0]), "dlda": float(dl[0])}), flush=True)
