@@ -9,7 +9,7 @@ SRC="$HERE/csrc"
 OBJ="$HERE/build"
 mkdir -p "$OBJ"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC
-       -Xcompiler -ffp-contract=off -Xcompiler -fopenmp -I"$ROOT/include" -I"$SRC" --expt-relaxed-constexpr)
+       -Xcompiler -ffp-contract=off -I"$ROOT/include" -I"$SRC" --expt-relaxed-constexpr)
 [ -n "${FGFRFT_PTXAS_VERBOSE:-}" ] && FLAGS+=(-Xptxas -v)
 pids=()
 for f in capi capi_shard capi_learn capi_spectral capi_store synth zgemm cgemm dots ops layout shard batch real ozgemm combine denoise spectral store packed capi_pshard; do
@@ -17,5 +17,5 @@ for f in capi capi_shard capi_learn capi_spectral capi_store synth zgemm cgemm d
 done
 "$NVCC" "${FLAGS[@]}" -x cu -c "$SRC/sinc_host.cpp" -o "$OBJ/sinc_host.o" & pids+=($!)
 for p in "${pids[@]}"; do wait "$p"; done
-"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT" "$OBJ"/*.o -lcudart -lgomp -ldl
+"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT" "$OBJ"/*.o -lcudart -ldl
 echo "built $OUT"

@@ -132,9 +132,9 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
     }
     c->coef_slot = q;
     c->coef_h = c->coef_hr[q];
-    // 2 (2L+1) libm evaluations per order: spread an order sweep over the host cores
-    const int nthr = std::min(8, std::max(1, n_alpha / 8));
-#pragma omp parallel for schedule(static) num_threads(nthr) if (nthr > 1)
+    // 2 (2L+1) libm evaluations per order, on this thread: an OpenMP team here measured 1.4 ms per
+    // call inside a process whose other OpenMP pools spin (CPU quota), against 0.05 ms alone -- and
+    // the order sweeps, whose host planning would need it, plan from host_sinc_coeffs_fast tables
     for (int a = 0; a < n_alpha; ++a)
         host_sinc_coeffs(alphas[a], l, c->coef_h + a * width, c->coef_h + ((size_t)n_alpha + a) * width);
     FGB_CUDA(c->coef.ensure(count * sizeof(double)));
@@ -499,13 +499,13 @@ int apply_device(fgfrft_cache* c, const double* alphas, int n_alpha, int l_used,
         std::vector<double> al(alphas, alphas + n_alpha);
         if (inverse)
             for (double& v : al) v = -v;
-        if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
         if (use_node_route(c, n_alpha, b)) {
             bool ran = false;
             if (int st = mse_node_route(c, al.data(), n_alpha, x_dev, nullptr, b, y_dev, nullptr, nullptr, false, &ran))
                 return st;
             if (ran) return FGFRFT_OK;
         }
+        if (int st = upload_coefs(c, al.data(), n_alpha, l_used, &coef)) return st;
         return apply_power_route(c, coef, n_alpha, x_dev, b, y_dev);
     }
     if (int st = upload_coefs(c, alphas, n_alpha, l_used, &coef)) return st;
@@ -717,7 +717,7 @@ static bool node_plan_r(const double* alphas, int na, int l, bool need_d, const 
     d0.assign((size_t)r, 0.0);
     std::vector<double> scratch((size_t)T);
     for (int j = 0; j < r; ++j) {
-        host_sinc_coeffs(xn[j], l, &tab[(size_t)j * T], scratch.data());
+        host_sinc_coeffs_fast(xn[j], l, &tab[(size_t)j * T], scratch.data());
         d0[j] = tab[(size_t)j * T + l];
     }
     const int rows = need_d ? 2 * na : na;
@@ -818,12 +818,17 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
     if (!(w > 1e-9)) return false;
     // the element-pair node operators hold 2r <= 64 output columns (one B tile)
     const int rmax = node_pairs_wanted() ? std::min(node_max_terms(), kOzTileB / 2) : node_max_terms();
+    // the orders' exact coefficient tables for the interpolation check (host only)
+    const int T = 2 * c->l + 1;
+    c->nd_ctab.resize((size_t)2 * na * T);
+    for (int a = 0; a < na; ++a)
+        host_sinc_coeffs_fast(alphas[a], c->l, &c->nd_ctab[(size_t)a * T], &c->nd_ctab[(size_t)(na + a) * T]);
     // the search starts one below the count the last sweep of (almost) the same width needed -- the
     // counts below it fail their first orders cheaply, but each still costs its node table
     int r0 = std::max(6, (int)std::floor(8.0 + 4.2 * w));
     if (p.hint_r > 0 && p.hint_need_d == need_d && std::fabs(p.hint_w - w) <= 1e-6 * w) r0 = std::max(r0, p.hint_r - 1);
     for (int r = r0; r <= rmax; ++r)
-        if (node_plan_r(alphas, na, c->l, need_d, c->coef_h, r, p.tab, p.d0, p.pw, &p.rp)) {
+        if (node_plan_r(alphas, na, c->l, need_d, c->nd_ctab.data(), r, p.tab, p.d0, p.pw, &p.rp)) {
             p.r = r;
             p.ok = true;
             p.hint_r = r;
@@ -1781,11 +1786,25 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         c->pk_plan = pk_plan(n, rows, b, l_used);
         c->pk_plan_key = key;
     }
-    if ((x_host || ww) && c->pk_plan.size() > 1) {  // the chunked host-X form / the window run one shell
+    if (x_host && c->pk_plan.size() > 1) {  // the chunked host-X form runs one shell
         c->pk_plan.assign(1, PkShell{0, (int)n, 0, -1});
         c->pk_plan_key = 0;
     }
-    const std::vector<PkShell>& plan = c->pk_plan;
+    // the window synthesis has no pair coupling: row shells are plain row ranges (FGFRFT_WIN_SHELLS
+    // equal shells; 1 = serial, the default: measured at config 3 on [0, 2], 2 / 3 / 4 shells with the
+    // GEMM capped at 100-132 CTAs took 1.44-1.75 ms against 1.45 serial -- the GEMM loses to the
+    // shared SMs what the overlap hides)
+    std::vector<PkShell> wplan;
+    if (ww) {
+        const int T = (int)ceil_div(n, kOzTileA);
+        const int k = x_host ? 1 : std::max(1, std::min(T, (int)pk_env("FGFRFT_WIN_SHELLS", 1)));
+        for (int s = 0; s < k; ++s) {
+            const int b0 = (int)((int64_t)T * s / k), b1 = (int)((int64_t)T * (s + 1) / k);
+            wplan.push_back(PkShell{(int)std::min<int64_t>(n, (int64_t)b0 * kOzTileA),
+                                    (int)std::min<int64_t>(n, (int64_t)b1 * kOzTileA), 0, 0});
+        }
+    }
+    const std::vector<PkShell>& plan = ww ? wplan : c->pk_plan;
     int64_t srows = 0;  // sliced rows over all shells (each shell padded to 128)
     for (const PkShell& sh : plan) srows += pad_rows(sh.r1 - sh.r0);
     const int64_t exps_ints = ceil_div((int64_t)rows * srows, 2) * 2;
@@ -1881,7 +1900,7 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
             // shell 0 runs alone (the GEMM has nothing yet): full grid; later shells share the GPU
             if (ww)
                 FGB_LAUNCH(launch_window_synth(c->win.as<double>(), c->win_r, (int)n, *ww, rows, q, sl, rmax, mp,
-                                               c->pk_s),
+                                               c->pk_s, sh.r0, sh.r1),
                            1);
             else if (tc)
                 FGB_LAUNCH(launch_dsynth(c->ds.as<int8_t>(), c->dse.as<int>(), c->dsb.as<int8_t>(), (int)dkp, (int)n,
@@ -2168,7 +2187,7 @@ int fgfrft_cache_set_order_window(fgfrft_cache* c, double lo, double hi) {
     std::vector<double> al((size_t)ns), coefs((size_t)2 * ns * T);
     for (int i = 0; i < ns; ++i) {
         al[i] = lo + (hi - lo) * (double)i / (double)(ns - 1);
-        host_sinc_coeffs(al[i], l, &coefs[(size_t)i * T], &coefs[(size_t)(ns + i) * T]);
+        host_sinc_coeffs_fast(al[i], l, &coefs[(size_t)i * T], &coefs[(size_t)(ns + i) * T]);
     }
     std::vector<double> tab, d0, pw;
     int r = 0, rp = 0;
@@ -2476,23 +2495,26 @@ int fgfrft_mse_step_dev(fgfrft_cache* c, const double* alphas, int n_alpha, cons
             if (dst) launch_demote(c->by.p, dst, (int64_t)cnt, c->stream);
         }
     } demote_y{c, y_c64, blk * n_alpha};
+    const bool combine = use_power_route(c, n_alpha) && use_int8_combine(c);
+    // the node route plans from its own host tables: the exact coefficient tables (bit-identical to
+    // sinc.hpp, 2 (2L + 1) libm calls per order) are only evaluated for the routes that consume them
+    if (!combine && use_node_route(c, n_alpha, b)) {
+        bool ran = false;
+        if (int st = mse_node_route(c, alphas, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
+                                    static_cast<double*>(dlda_dev), true, &ran))
+            return st;
+        if (ran) return FGFRFT_OK;
+    }
     double* coef = nullptr;
     {
         HostTimer ht(0);
         if (int st = upload_coefs(c, alphas, n_alpha, l, &coef)) return st;
     }
     const double* dc_dev = coef + (size_t)n_alpha * width;
-    if (use_power_route(c, n_alpha) && use_int8_combine(c)) {
+    if (combine) {
         FGB_CUDA(c->s.ensure((size_t)n_alpha * width * sizeof(double)));
         return mse_int8_combine(c, coef, dc_dev, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
                                 c->s.as<double>(), static_cast<double*>(dlda_dev));
-    }
-    if (use_node_route(c, n_alpha, b)) {
-        bool ran = false;
-        if (int st = mse_node_route(c, alphas, n_alpha, x_dev, xc_dev, b, y_dev, static_cast<double*>(loss_dev),
-                                    static_cast<double*>(dlda_dev), true, &ran))
-            return st;
-        if (ran) return FGFRFT_OK;
     }
     c->last_route = use_power_route(c, n_alpha) ? 1 : 0;
     c->last_nodes = 0;

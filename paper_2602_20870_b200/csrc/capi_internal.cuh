@@ -29,6 +29,7 @@ namespace fgb {
 double host_sinc(double);
 double host_sinc_deriv(double);
 void host_sinc_coeffs(double alpha, int l, double* c, double* dc);
+void host_sinc_coeffs_fast(double alpha, int l, double* c, double* dc);  // planning tables only
 uint64_t host_fnv1a64(const void* data, size_t nbytes);
 template <typename R>
 cudaError_t launch_synth(const void* slabs, int n, int l_used, const double* coef_dev, int n_alpha, void* out,
@@ -171,7 +172,8 @@ size_t packed_bytes(int n, int l);
 cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream);
 // the order window (packed.cu): Q_x = sum_j w[x][j] W'_j over r <= kWindowMaxNodes node operators
 cudaError_t launch_window_synth(const double* wops, int r, int n, const WindowWeights& ww, int rows, double* out,
-                                int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream);
+                                int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream,
+                                int row0 = 0, int row1 = -1);
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
                           int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0,
@@ -339,6 +341,7 @@ struct fgfrft_cache {
     size_t nd_hr_cap[kNdRing] = {};
     cudaEvent_t nd_evr[kNdRing] = {};
     int nd_slot = 0;
+    std::vector<double> nd_ctab;  // the sweep's [c | c'] tables for the node plan's check (host)
     struct NodePlan {  // memoised plan of the last sweep (a pure function of the orders)
         std::vector<double> alphas, tab, d0, pw;
         int hint_r = 0;  // node count of the last accepted plan, its width: the next search's start

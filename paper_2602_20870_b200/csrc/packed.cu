@@ -503,10 +503,10 @@ template <int ROWS>
 __global__ void __launch_bounds__(256) window_synth_kernel(const double* __restrict__ wops, int r, int n, int64_t nn,
                                                            WindowWeights ww, double* __restrict__ out,
                                                            int64_t ostride, unsigned long long* __restrict__ rowmax,
-                                                           int64_t mp) {
-    const int i = blockIdx.x * 256 + threadIdx.x;
+                                                           int64_t mp, int row0, int row1) {
+    const int i = row0 + blockIdx.x * 256 + threadIdx.x;
     const int j0 = blockIdx.y * 64, j1 = min(j0 + 64, n);
-    if (i >= n) return;
+    if (i >= row1) return;
     double mx[ROWS];
 #pragma unroll
     for (int x = 0; x < ROWS; ++x) mx[x] = 0.0;
@@ -555,14 +555,17 @@ __global__ void __launch_bounds__(256) window_synth_kernel(const double* __restr
 }  // namespace
 
 cudaError_t launch_window_synth(const double* wops, int r, int n, const WindowWeights& ww, int rows, double* out,
-                                int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream) {
+                                int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream,
+                                int row0, int row1) {
     if (r < 1 || r > kWindowMaxNodes) return cudaErrorInvalidValue;
-    const dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, 64));
+    if (row1 < 0 || row1 > n) row1 = n;
+    if (row1 <= row0) return cudaSuccess;
+    const dim3 grid((unsigned)ceil_div(row1 - row0, 256), (unsigned)ceil_div(n, 64));
     const int64_t nn = (int64_t)n * n;
     switch (rows) {
-        case 1: window_synth_kernel<1><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp); break;
-        case 2: window_synth_kernel<2><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp); break;
-        case 4: window_synth_kernel<4><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp); break;
+        case 1: window_synth_kernel<1><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp, row0, row1); break;
+        case 2: window_synth_kernel<2><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp, row0, row1); break;
+        case 4: window_synth_kernel<4><<<grid, 256, 0, stream>>>(wops, r, n, nn, ww, out, ostride, rowmax, mp, row0, row1); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
