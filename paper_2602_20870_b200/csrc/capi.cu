@@ -598,10 +598,12 @@ uint64_t power_slice_bytes(const fgfrft_cache* c) {
 // of a tile pair, K = the L powers of both elements: half the bytes of the element-row form, whose
 // K stacked P_k(i, j) and P_k(j, i) for every element, so every power was stored twice) -- the
 // same values per row, so the same slicing error. Measured at config 2 it reads half the bytes (427
-// vs 812 MB, ncu) but runs 0.217 vs 0.182 ms: 2r = 38 output columns need the 64-column B tile,
-// whose 6 digit-sum accumulators (384 TMEM columns) leave room for ONE buffer, so every unit's MMAs
-// wait for the previous unit's epilogue; the element-row form's 32-column tiles double-buffer. Opt-in
-// (FGFRFT_NODE_PAIRS=1) until the pair form is split into two 32-column units per tile.
+// vs 812 MB, ncu) but runs slower: 0.217 ms (vs 0.182) with the 64-column B tile (its 6 digit-sum
+// accumulators, 384 TMEM columns, leave room for ONE buffer: every unit's MMAs wait for the previous
+// unit's epilogue) and 0.30 ms as two double-buffered 32-column units per tile -- half of every
+// pair's outputs are the mirror elements, whose column-major stores scatter one 8-byte word per lane
+// (the pair's mirror rows come from 8 different units, too many to transpose through shared
+// memory). Opt-in (FGFRFT_NODE_PAIRS=1).
 static bool node_pairs_wanted() {
     static const bool v = [] {
         const char* e = std::getenv("FGFRFT_NODE_PAIRS");
@@ -847,7 +849,10 @@ bool node_plan(fgfrft_cache* c, const double* alphas, int na, bool need_d, int* 
 static int node_products_pairs(fgfrft_cache* c, const std::vector<double>& tab, const std::vector<double>& d0, int r,
                                const void* x_dev, int64_t b, bool upload) {
     const int S = c->es_slices;
+    // B: 2r rows sliced as two 32-row tiles (64 rows: the slicer's granule); the narrow,
+    // double-buffered GEMM form runs over the live tiles
     const int64_t n = c->n, rows = (int64_t)dsynth_cache_rows((int)n), kp = dsynth_kp(c->l), bp = kOzTileB;
+    const int64_t bn = ceil_div(2 * r, kOzTileNarrow) * kOzTileNarrow;
     if (upload) {
         FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
         FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
@@ -862,7 +867,7 @@ static int node_products_pairs(fgfrft_cache* c, const std::vector<double>& tab, 
         v.tiled = 8;
         v.l = c->l;
         ProfScope ps(KC_SLICE, c->stream);
-        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->nd_bsl.as<int8_t>(), be,
+        FGB_LAUNCH(launch_oz_slice(v, S, kOzTileNarrow, c->nd_bsl.as<int8_t>(), be,
                                    reinterpret_cast<unsigned long long*>(be + bp), c->stream),
                    3);
     }
@@ -887,8 +892,8 @@ static int node_products_pairs(fgfrft_cache* c, const std::vector<double>& tab, 
         out.pair_nt = (int)ceil_div(n, kTile);
         out.pair_n = (int)n;
         ProfScope ps(KC_NODEOP, c->stream);
-        FGB_LAUNCH(launch_ozgemm_ex(S, 0, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(), be,
-                                    (int)bp, (int)kp, out, c->stream),
+        FGB_LAUNCH(launch_ozgemm_narrow(S, c->es.as<int8_t>(), c->ee.as<int>(), (int)rows, c->nd_bsl.as<int8_t>(), be,
+                                        (int)bn, (int)kp, out, c->stream),
                    1);
     }
     return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, true);

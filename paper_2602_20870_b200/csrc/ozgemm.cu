@@ -52,7 +52,8 @@ template <int S, int BN = kOzBN> struct OzCfg {
     static constexpr int a_stage = S * kOzBM * bk;
     static constexpr int b_stage = S * BN * bk;
     static constexpr int stage = a_stage + b_stage;
-    static constexpr int smem = stages * stage + 1024 + 2048;  // + barriers / scratch + CM 2 exchange
+    // + barriers / scratch + CM 2 exchange (+ the narrow form's pair-mode row maxima, [2][32][32])
+    static constexpr int smem = stages * stage + 1024 + 2048 + (BN == kOzBN ? 0 : 16384);
 };
 
 
@@ -458,8 +459,9 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     // the pair's rows stay in registers across them)
     const bool pairs = CM == 0 && CL == 1 && out.pair_nt > 0;
     const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32 && !pairs;  // (the skinny epilogue)
-    const int ub = pairs ? cid * 8 : cid, ue = units, us = nclusters;
-    auto next_u = [&](int u) { return pairs ? ((u & 7) == 7 ? u + 8 * us - 7 : u + 1) : u + us; };
+    const int upp = 8 * ngroups;  // pair mode: units of one tile pair (8 M tiles x the N tiles)
+    const int ub = pairs ? cid * upp : cid, ue = units, us = nclusters;
+    auto next_u = [&](int u) { return pairs ? ((u % upp) == upp - 1 ? u + upp * us - (upp - 1) : u + 1) : u + us; };
     auto unit_mt = [&](int u) { return u / ngroups; };
     auto unit_nt = [&](int u) { return (u % ngroups) * CL + rank; };
 
@@ -534,12 +536,30 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
         // pair mode: the column scales 2^e_n and the diagonal terms in shared memory (the CM 2
         // exchange region), the next unit's row exponent prefetched, the pair's (I, J) per pair
         int ea_nx = 0, pI = 0, pJ = 0;
+        // narrow pair mode: the pair's row maxima reduced in shared memory ([mirror][node][row of the
+        // tile]) and flushed to global once per pair
+        unsigned long long* psm = reinterpret_cast<unsigned long long*>(smem + kOzStages * Cfg::stage + 1024 + 2048);
         if (CM == 0 && pairs) {
             for (int t = threadIdx.x - 64; t < kOzBN + 32; t += 32 * kOzEpiWarps)
-                xchg[t] = t < kOzBN ? pow2(eb[t]) : (t - kOzBN < out.nv / 2 ? out.dg[t - kOzBN] : 0.0);
+                xchg[t] = t < kOzBN ? (t < ngroups * BN ? pow2(eb[t]) : 0.0)
+                                    : (t - kOzBN < out.nv / 2 ? out.dg[t - kOzBN] : 0.0);
+            if (BN != kOzBN)
+                for (int t = threadIdx.x - 64; t < 2048; t += 32 * kOzEpiWarps) psm[t] = 0ull;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kOzEpiWarps) : "memory");
-            if (ub < ue) ea_nx = ea[ub * kOzBM + lrow];
+            if (ub < ue) ea_nx = ea[unit_mt(ub) * kOzBM + lrow];
         }
+        auto pair_flush = [&](int I, int J) {  // every epilogue thread, at a pair boundary
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kOzEpiWarps) : "memory");
+            for (int t = threadIdx.x - 64; t < 2048; t += 32 * kOzEpiWarps) {
+                const unsigned long long v = psm[t];
+                if (!v) continue;
+                psm[t] = 0ull;
+                const int side = t >> 10, x = (t >> 5) & 31, idx = t & 31;
+                const int row = (side ? J : I) * 32 + idx;
+                if (row < out.pair_n) atomicMax(out.rmax + (int64_t)x * out.rnp + row, v);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kOzEpiWarps) : "memory");
+        };
         double rmx[8];  // chunk mode: running row max of this thread's 8 columns over the row block
         int rib = -1;
         auto flush_rmax = [&](int live) {
@@ -553,6 +573,10 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
         for (int u = ub; u < ue; u = next_u(u), ++tcount) {
             const int mt = unit_mt(u), nt = unit_nt(u);
             const int buf = tcount % NB;
+            if (CM == 0 && pairs && BN != kOzBN && (u % upp) == 0) {
+                if (tcount > 0 && out.rmax) pair_flush(pI, pJ);
+                pair_of_imajor(mt >> 3, out.pair_nt, pI, pJ);
+            }
             mbar_wait(tfull + buf, (tcount / NB) & 1);
             tc_fence_after();
             constexpr double lo_w = 1.0 / oz_pow254(S - 3);  // weight of the low fold
@@ -586,6 +610,41 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(tempty + buf);
+                if (CM == 0 && pairs) {
+                    // element pair row m of tile pair (pI, pJ): t = 128 (mt % 8) + lrow -> (i, j) = (t % 32, t / 32)
+                    const int m = mt * kOzBM + lrow;
+                    const int t = m & 1023, pi = t & 31, pj = t >> 5;
+                    const int ri = pI * 32 + pi, cj = pJ * 32 + pj, nn = out.pair_n;
+                    const bool ok = ri < nn && cj < nn, diag = pI == pJ;
+                    const double ra = pow2(ea_nx) * kOzScale;
+                    {
+                        const int un = next_u(u);
+                        ea_nx = un < ue ? ea[unit_mt(un) * kOzBM + lrow] : 0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (q >= live) break;  // warp-uniform
+                        const int col = nt * BN + c0 + q, x = col >> 1;
+                        double w = val8[q] * ra * xchg[col];
+                        if (diag && pi == pj) w += xchg[kOzBN + x];
+                        double* o = out.c + (int64_t)x * out.ldc;
+                        if (!(col & 1)) {  // W_x[32I + i, 32J + j]: lanes along rows 32I + i
+                            if (ok) {
+                                __stcs(o + (int64_t)cj * nn + ri, w);
+                                if (out.rmax) atomicMax(psm + x * 32 + pi, (unsigned long long)__double_as_longlong(fabs(w)));
+                            }
+                        } else if (!diag) {  // the mirror W_x[32J + j, 32I + i]; row 32J + j is warp-uniform
+                            if (ok) __stcs(o + (int64_t)ri * nn + cj, w);
+                            if (out.rmax) {
+                                const unsigned hw =
+                                    (unsigned)((unsigned long long)__double_as_longlong(ok ? fabs(w) : 0.0) >> 32);
+                                const unsigned mx = __reduce_max_sync(0xffffffffu, hw);
+                                if (lane == 0 && mx) atomicMax(psm + 1024 + x * 32 + pj, (unsigned long long)mx << 32);
+                            }
+                        }
+                    }
+                    continue;
+                }
                 if (live <= 0) continue;
                 const int m = mt * kOzBM + lrow;
                 const int bm = m / out.mp, i = m - bm * out.mp;
@@ -811,6 +870,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
             }  // BN == kOzBN
         }
         if (chunk) flush_rmax(min((out.nv + 3) >> 2, out.nv - h * ((out.nv + 3) >> 2)));
+        if (CM == 0 && pairs && BN != kOzBN && tcount > 0 && out.rmax) pair_flush(pI, pJ);
         if (CM == 1 && out.scw > 0) __threadfence_system();  // peer stores visible before the barrier
         if (CM == 2) {
             double* gp = out.part + (((int64_t)blockIdx.x * kOzEpiQ + h) * kOzBM + lrow) * 3;
@@ -1305,12 +1365,15 @@ static cudaError_t oz_launch(const int8_t* a, const int* ea, int mrows, const in
 // kOzTileNarrow), nrows == 32; narrow TMEM accumulators, double-buffered.
 cudaError_t launch_ozgemm_narrow(int slices, const int8_t* a, const int* ea, int mrows, const int8_t* b,
                                  const int* eb, int nrows, int kp, const OzOut& out, cudaStream_t stream) {
-    if (mrows % kOzBM || nrows != kOzTileNarrow || kp % 64 || out.nv > kOzTileNarrow || out.npeers)
+    // pair mode (out.pair_nt): up to 2 B tiles of 32 rows (2r <= 64 output columns)
+    const int nt = nrows / kOzTileNarrow;
+    if (mrows % kOzBM || nrows % kOzTileNarrow || kp % 64 || out.npeers ||
+        (out.pair_nt ? (nt > 2 || out.nv > nrows || mrows % (8 * kOzBM)) : (nt != 1 || out.nv > kOzTileNarrow)))
         return cudaErrorInvalidValue;
     const int mtiles = mrows / kOzBM;
-    if (slices == 6) return oz_launch_cl<6, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, 1, kp, out, stream);
-    if (slices == 7) return oz_launch_cl<7, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, 1, kp, out, stream);
-    if (slices == 8) return oz_launch_cl<8, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, 1, kp, out, stream);
+    if (slices == 6) return oz_launch_cl<6, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, nt, kp, out, stream);
+    if (slices == 7) return oz_launch_cl<7, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, nt, kp, out, stream);
+    if (slices == 8) return oz_launch_cl<8, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, nt, kp, out, stream);
     return cudaErrorInvalidValue;
 }
 
