@@ -457,7 +457,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     // the same row block and the row max stays in registers until one flush at the end
     // pair mode (out.pair_nt): a CTA takes the 8 M tiles of one tile pair in a row (row maxima of
     // the pair's rows stay in registers across them)
-    const bool pairs = CM == 0 && CL == 1 && out.pair_nt > 0;
+    const bool pairs = CM == 0 && CL == 1 && BN != kOzBN && out.pair_nt > 0;  // (the narrow form only)
     const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32 && !pairs;  // (the skinny epilogue)
     const int upp = 8 * ngroups;  // pair mode: units of one tile pair (8 M tiles x the N tiles)
     const int ub = pairs ? cid * upp : cid, ue = units, us = nclusters;
@@ -530,9 +530,6 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
             for (int c = 0; c < kOzEC; ++c) lacc[c] = 0.0;
         }
-        double prm[kOzEC / 2];  // pair mode: running max of rows 32I + i over the pair's tiles
-#pragma unroll
-        for (int q = 0; q < kOzEC / 2; ++q) prm[q] = 0.0;
         // pair mode: the column scales 2^e_n and the diagonal terms in shared memory (the CM 2
         // exchange region), the next unit's row exponent prefetched, the pair's (I, J) per pair
         int ea_nx = 0, pI = 0, pJ = 0;
@@ -777,55 +774,6 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                             const double r = yv - xcp;
                             lacc[c] = fma(r, r, lacc[c]);
                         }
-                    }
-                }
-                continue;
-            }
-            if (CM == 0 && pairs) {
-                // element pair row m: tile pair p, t = 128 (mt % 8) + lrow -> (i, j) = (t % 32, t / 32)
-                const int t = m & 1023, pi = t & 31, pj = t >> 5;
-                if ((mt & 7) == 0 || tcount == 0) pair_of_imajor(m >> 10, out.pair_nt, pI, pJ);
-                const int I = pI, J = pJ;
-                const int ri = I * 32 + pi, cj = J * 32 + pj, nn = out.pair_n;
-                const bool ok = ri < nn && cj < nn, diag = I == J;
-                const double ra = pow2(ea_nx) * kOzScale;
-                {
-                    const int un = next_u(u);
-                    ea_nx = un < ue ? ea[un * kOzBM + lrow] : 0;
-                }
-                const double* sct = xchg + h * kOzEC;
-#pragma unroll
-                for (int q = 0; q < kOzEC / 2; ++q) {
-                    const int x = (nt * kOzBN + h * kOzEC) / 2 + q;
-                    if (2 * x >= out.nv) break;  // warp-uniform
-                    double w0 = val[2 * q] * ra * sct[2 * q];
-                    double w1 = val[2 * q + 1] * ra * sct[2 * q + 1];
-                    if (diag && pi == pj) {
-                        w0 += xchg[kOzBN + x];
-                        w1 += xchg[kOzBN + x];
-                    }
-                    double* o = out.c + (int64_t)x * out.ldc;
-                    if (ok) {
-                        __stcs(o + (int64_t)cj * nn + ri, w0);  // W_x[32I + i, 32J + j]: lanes along rows
-                        prm[q] = fmax(prm[q], fabs(w0));
-                    }
-                    if (!diag) {  // W_x[32J + j, 32I + i]; row 32J + j is warp-uniform
-                        if (ok) __stcs(o + (int64_t)ri * nn + cj, w1);
-                        if (out.rmax) {
-                            const unsigned hw = (unsigned)((unsigned long long)__double_as_longlong(ok ? fabs(w1) : 0.0) >> 32);
-                            const unsigned mx = __reduce_max_sync(0xffffffffu, hw);
-                            if (lane == 0 && mx && cj < nn)
-                                atomicMax(out.rmax + (int64_t)x * out.rnp + cj, (unsigned long long)mx << 32);
-                        }
-                    }
-                }
-                if ((mt & 7) == 7) {  // the pair's last tile: rows 32I + i are complete for this thread
-#pragma unroll
-                    for (int q = 0; q < kOzEC / 2; ++q) {
-                        const int x = (nt * kOzBN + h * kOzEC) / 2 + q;
-                        if (out.rmax && 2 * x < out.nv && prm[q] > 0.0 && ri < nn)
-                            atomicMax(out.rmax + (int64_t)x * out.rnp + ri, (unsigned long long)__double_as_longlong(prm[q]));
-                        prm[q] = 0.0;
                     }
                 }
                 continue;
