@@ -93,3 +93,34 @@ def test_graph_batch_persistent_tensor_core_kernels(graphs, heads):
             _, dc = O.sinc_coeffs(alphas[gi, h], l)
             assert abs(dl[gi, h] - float(np.dot(dc, s_ref))) <= 1e-4 * float(np.sum(np.abs(dc * s_ref))), (gi, h)
     batch.close()
+
+
+def test_config5_full_size_sampled():
+    """BASELINE config 5 at full size (4096 ER(64, 0.1) graphs, L = 16, 4 heads per graph with orders
+    in [0.5, 1.5], 64 complex64 channels -- prep.config5), on the persistent tcgen05 kernels: F^a X
+    and dL/da of 24 sampled graphs (first, last, across the persistent loop) against the fp64
+    oracle within 1e-4 (north-star complex64 bar)."""
+    fs, orders, feats, l = prep.config5()
+    graphs, n, ch = feats.shape
+    heads = orders.shape[1]
+    rng = np.random.default_rng(55)
+    gc = (rng.standard_normal((graphs, heads, n, ch)) + 1j * rng.standard_normal((graphs, heads, n, ch))) \
+        .astype(np.complex64)
+    batch = fg.GraphBatch(fs, l)
+    a_d = torch.from_numpy(orders).cuda()
+    x_d = torch.from_numpy(np.ascontiguousarray(feats.transpose(0, 2, 1)).astype(np.complex64)).cuda()
+    g_d = torch.from_numpy(np.ascontiguousarray(gc.transpose(0, 1, 3, 2))).cuda()
+    y = batch.forward(a_d, x_d).cpu().numpy().transpose(0, 1, 3, 2)
+    dl = batch.dlda(a_d, g_d, x_d).cpu().numpy()
+    sample = sorted(set([0, 1, 147, 148, 2047, 4094, 4095] + list(rng.choice(graphs, 17, replace=False))))
+    for gi in sample:
+        cache = O.PowerCache(fs[gi], l)
+        xg = feats[gi].astype(np.complex64).astype(np.complex128)
+        for h in range(heads):
+            q = O.fgfrft_matrix(cache, orders[gi, h])
+            assert rel(y[gi, h], q @ xg) <= 1e-4, (gi, h)
+            gg = gc[gi, h].astype(np.complex128)
+            s_ref = O.power_dots(cache, gg @ xg.conj().T)
+            _, dc = O.sinc_coeffs(orders[gi, h], l)
+            assert abs(dl[gi, h] - float(np.dot(dc, s_ref))) <= 1e-4 * float(np.sum(np.abs(dc * s_ref))), (gi, h)
+    batch.close()

@@ -260,6 +260,13 @@ def test_config4_packed_step_and_pair_shard_world1():
             cols = np.random.default_rng(int(a * 100)).choice(b, size=64, replace=False)
             yr = O.series_apply_recursive(cfg.f, a, cfg.l, np.asfortranarray(cfg.x[:, cols]))
             assert rel(y[0][:, cols], yr) <= 1e-10
+            if a == alphas[0]:  # the order-window route (19 exact node operators of [0, 2]) on the same step
+                assert cache.set_order_window(0.0, 2.0) > 0
+                lw, dw, yw = fg.mse_step(cache, [a], cfg.x, cfg.x_clean, want_y=True)
+                assert cache.route_info()[0] == 5
+                assert rel(yw[0][:, cols], yr) <= 1e-10
+                assert abs(lw[0] - loss[0]) <= 1e-11 * loss[0] and abs(dw[0] - dl[0]) <= 1e-9 * max(abs(dl[0]), 1e-3)
+                cache.set_order_window(0.0, 0.0)
     finally:
         cache.close()
     comm = ps.Comm(ps.Comm.unique_id(), 1, 0, 0)
