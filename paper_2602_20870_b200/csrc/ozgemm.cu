@@ -45,7 +45,7 @@ __host__ __device__ constexpr double oz_pow254(int k) { return k == 0 ? 1.0 : 25
 
 // Stage geometry per digit count: 6 digits -> 64-byte K blocks (two MMA K steps, 18 MMAs per
 // stage) in a 3-stage ring; 7-8 digits -> 32-byte K blocks in a 5- / 4-stage ring (<= 219 KB smem).
-template <int S, int BN = kOzBN> struct OzCfg {
+template <int S, int BN = kOzBN, bool P = false> struct OzCfg {
     static constexpr int bk = S <= 6 ? 64 : 32;        // bytes (= int8 elements) of K per stage
     static constexpr int stages = S <= 6 ? 3 : (S == 7 ? 5 : 4);
     static constexpr int sbo = bk / 16 * 128;          // bytes between 8-row groups of a slice block
@@ -53,7 +53,7 @@ template <int S, int BN = kOzBN> struct OzCfg {
     static constexpr int b_stage = S * BN * bk;
     static constexpr int stage = a_stage + b_stage;
     // + barriers / scratch + CM 2 exchange (+ the narrow form's pair-mode row maxima, [2][32][32])
-    static constexpr int smem = stages * stage + 1024 + 2048 + (BN == kOzBN ? 0 : 16384);
+    static constexpr int smem = stages * stage + 1024 + 2048 + (P ? 16384 : 0);
 };
 
 
@@ -407,12 +407,15 @@ constexpr int kOzThreads = 32 * (2 + kOzEpiWarps);    // producer warp, MMA warp
 // BN = 32 (CM 0 only): the skinny node-operator form -- B tiles of 32 rows (r <= 32 live output
 // columns), S x 32 TMEM columns per accumulator set, so two sets fit and the MMAs of unit u + 1
 // run while the epilogue drains unit u (tfull / tempty per buffer).
-template <int S, int CM, int CL, int BN = kOzBN>
+// P: the element-pair node-operator mode (OzOut::pair_nt, narrow form only) -- a separate
+// instantiation so its registers do not burden the default forms.
+template <int S, int CM, int CL, int BN = kOzBN, bool P = false>
 __global__ void __launch_bounds__(kOzThreads, 1)
 ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const int8_t* __restrict__ b,
               const int* __restrict__ eb, int kblocks, int mtiles, int ntiles, OzOut out) {
     static_assert(BN == kOzBN || (BN == 32 && CM == 0), "narrow tiles: node operators only");
-    using Cfg = OzCfg<S, BN>;
+    static_assert(!P || (BN == 32 && CM == 0 && CL == 1), "pair mode: the narrow form");
+    using Cfg = OzCfg<S, BN, P>;
     constexpr int NB = BN == kOzBN ? 1 : 2;        // TMEM accumulator buffers
     constexpr uint32_t kBufCols = BN == kOzBN ? 0 : 256;
     constexpr int kOzStages = Cfg::stages;
@@ -457,7 +460,7 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     // the same row block and the row max stays in registers until one flush at the end
     // pair mode (out.pair_nt): a CTA takes the 8 M tiles of one tile pair in a row (row maxima of
     // the pair's rows stay in registers across them)
-    const bool pairs = CM == 0 && CL == 1 && BN != kOzBN && out.pair_nt > 0;  // (the narrow form only)
+    constexpr bool pairs = P;
     const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32 && !pairs;  // (the skinny epilogue)
     const int upp = 8 * ngroups;  // pair mode: units of one tile pair (8 M tiles x the N tiles)
     const int ub = pairs ? cid * upp : cid, ue = units, us = nclusters;
@@ -1243,19 +1246,19 @@ cudaError_t launch_oz_slice_ready(const OzView& v, int slices, int tr, int8_t* d
     return cudaErrorInvalidValue;
 }
 
-template <int S, int CM, int CL, int BN = kOzBN>
+template <int S, int CM, int CL, int BN = kOzBN, bool P = false>
 static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, const int8_t* b, const int* eb, int ntiles,
                                 int kp, const OzOut& out, cudaStream_t stream) {
     static PerDeviceOnce attr;
     if (cudaError_t e = attr.run([] {
-            return cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (OzCfg<S, BN>::smem));
+            return cudaFuncSetAttribute(ozgemm_kernel<S, CM, CL, BN, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (OzCfg<S, BN, P>::smem));
         }))
         return e;
     const int units = mtiles * (ntiles / CL);
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kOzThreads);
-    cfg.dynamicSmemBytes = (OzCfg<S, BN>::smem);
+    cfg.dynamicSmemBytes = (OzCfg<S, BN, P>::smem);
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1272,7 +1275,7 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
     if (max_clusters == 0) {
         cfg.gridDim = dim3(FGFRFT_SMS / CL * CL);
         int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, ozgemm_kernel<S, CM, CL, BN>, &cfg) != cudaSuccess || mc <= 0) {
+        if (cudaOccupancyMaxActiveClusters(&mc, ozgemm_kernel<S, CM, CL, BN, P>, &cfg) != cudaSuccess || mc <= 0) {
             cudaGetLastError();
             mc = FGFRFT_SMS / CL;
         }
@@ -1286,7 +1289,7 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
         if (clusters >= ibs) clusters = clusters / ibs * ibs;
     }
     cfg.gridDim = dim3(clusters * CL);
-    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL, BN>, a, ea, b, eb, kp / OzCfg<S, BN>::bk, mtiles, ntiles, out);
+    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL, BN, P>, a, ea, b, eb, kp / OzCfg<S, BN, P>::bk, mtiles, ntiles, out);
 }
 
 template <int S, int CM>
@@ -1319,6 +1322,10 @@ cudaError_t launch_ozgemm_narrow(int slices, const int8_t* a, const int* ea, int
         (out.pair_nt ? (nt > 2 || out.nv > nrows || mrows % (8 * kOzBM)) : (nt != 1 || out.nv > kOzTileNarrow)))
         return cudaErrorInvalidValue;
     const int mtiles = mrows / kOzBM;
+    if (out.pair_nt) {
+        if (slices == 6) return oz_launch_cl<6, 0, 1, kOzTileNarrow, true>(a, ea, mtiles, b, eb, nt, kp, out, stream);
+        return cudaErrorInvalidValue;
+    }
     if (slices == 6) return oz_launch_cl<6, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, nt, kp, out, stream);
     if (slices == 7) return oz_launch_cl<7, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, nt, kp, out, stream);
     if (slices == 8) return oz_launch_cl<8, 0, 1, kOzTileNarrow>(a, ea, mtiles, b, eb, nt, kp, out, stream);
