@@ -539,11 +539,12 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
         // narrow pair mode: the pair's row maxima reduced in shared memory ([mirror][node][row of the
         // tile]) and flushed to global once per pair
         unsigned long long* psm = reinterpret_cast<unsigned long long*>(smem + kOzStages * Cfg::stage + 1024 + 2048);
-        if (CM == 0 && pairs) {
+        if (CM == 0 && BN != kOzBN) {  // narrow forms: column scales / diagonal in shared memory
+            const int ndg = pairs ? out.nv / 2 : out.nv;
             for (int t = threadIdx.x - 64; t < kOzBN + 32; t += 32 * kOzEpiWarps)
                 xchg[t] = t < kOzBN ? (t < ngroups * BN ? pow2(eb[t]) : 0.0)
-                                    : (t - kOzBN < out.nv / 2 ? out.dg[t - kOzBN] : 0.0);
-            if (BN != kOzBN)
+                                    : (out.dg && t - kOzBN < ndg ? out.dg[t - kOzBN] : 0.0);
+            if (pairs)
                 for (int t = threadIdx.x - 64; t < 2048; t += 32 * kOzEpiWarps) psm[t] = 0ull;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kOzEpiWarps) : "memory");
             if (ub < ue) ea_nx = ea[unit_mt(ub) * kOzBM + lrow];
@@ -645,13 +646,20 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                     }
                     continue;
                 }
+                double ra = 0.0;
+                if (CM == 0 && BN != kOzBN) {  // this unit's row exponent (prefetched), the next unit's load
+                    ra = pow2(ea_nx) * kOzScale;
+                    const int un = next_u(u);
+                    ea_nx = un < ue ? ea[unit_mt(un) * kOzBM + lrow] : 0;
+                }
                 if (live <= 0) continue;
                 const int m = mt * kOzBM + lrow;
                 const int bm = m / out.mp, i = m - bm * out.mp;
                 if (i >= out.mv) continue;
-                const double ra = pow2(ea[m]) * kOzScale;
+                if (!(CM == 0 && BN != kOzBN)) ra = pow2(ea[m]) * kOzScale;
                 double* cb = out.c + (int64_t)bm * out.sc + i;
                 const int* ebt = eb + nt * BN + c0;
+                const double* sct = xchg + nt * BN + c0;  // 2^e_n of these columns (narrow forms)
                 if (chunk) {
                     const int ibs = out.rn / kOzBM, rj = mt / ibs, ib = mt - rj * ibs, ri = ib * kOzBM + lrow;
                     if (ib != rib) {
@@ -663,8 +671,8 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         if (q >= live) break;
-                        double y = val8[q] * ra * pow2(ebt[q]);
-                        if (ri == rj) y += out.dg[c0 + q];  // the c_0 I term of the series
+                        double y = val8[q] * ra * (BN != kOzBN ? sct[q] : pow2(ebt[q]));
+                        if (ri == rj) y += BN != kOzBN ? xchg[kOzBN + c0 + q] : out.dg[c0 + q];  // the c_0 I term
                         rmx[q] = fmax(rmx[q], fabs(y));
                         __stcs(cb + (int64_t)(c0 + q) * out.ldc, y);
                     }
@@ -673,7 +681,8 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (q >= live) break;
-                    __stcs(cb + (int64_t)(nt * BN + c0 + q) * out.ldc, val8[q] * ra * pow2(ebt[q]));
+                    __stcs(cb + (int64_t)(nt * BN + c0 + q) * out.ldc,
+                           val8[q] * ra * (BN != kOzBN ? sct[q] : pow2(ebt[q])));
                 }
                 continue;
             }
