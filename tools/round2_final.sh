@@ -1,6 +1,6 @@
 # Round-2 final evidence on one B200 (outputs under gpurun_out/ev4/; summaries copied to profiles/).
 cd $GRAFT_REPO_ROOT
-E=gpurun_out/ev4; mkdir -p $E
+E=gpurun_out/ev6; mkdir -p $E
 timeout 1800 python -m pytest tests -m gpu -q -x > $E/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $E/pytest_gpu.log
 tail -n 2 $E/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $E/smoke.log 2>&1; tail -n 1 $E/smoke.log
