@@ -51,7 +51,10 @@ def main():
     ap.add_argument("--ns", default="1000,2000,3000,4000,5000,6000,7000,8000")
     ap.add_argument("--l", type=int, default=10)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--record", default=None, help="also write the reference CLI's bench.csv + bench.manifest "
+                    "(commands.hpp:140-165 format) under this prefix")
     args = ap.parse_args()
+    records = []
     try:
         hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
     except Exception:
@@ -87,6 +90,8 @@ def main():
                "gpu_eig_s": eig_s, "cache_build_s": build_s, "prep_s": prep_s,
                "paper_series_s": ps, "paper_exact_s": pe,
                "speedup_vs_paper_series": (ps / (t_series * 1e-3)) if ps else None}
+        records.append({"n": n, "l": args.l, "fast_s": t_series * 1e-3, "exact_s": t_exact * 1e-3,
+                        "speedup": t_exact / t_series, "repeats": 25})
         line = json.dumps(rec)
         print(line, flush=True)
         if fh:
@@ -94,6 +99,12 @@ def main():
             fh.flush()
         del q, cache, eig
         torch.cuda.empty_cache()
+    if args.record:
+        from paper_2602_20870_b200 import formats
+        formats.write_bench(args.record, records,
+                            [("n-list", args.ns), ("l", str(args.l)), ("repeats", "25"), ("warmups", "3"),
+                             ("alpha", "0.37"), ("seed", "1"), ("haar", "1"), ("out", args.record),
+                             ("device", "B200")], 1)
 
 
 def ctypes_stream(stream):
