@@ -101,3 +101,27 @@ def test_window_budget_and_validation():
     h = fg.PowerCache(prep.random_unitary(n, 3), l)  # complex F: no packed route
     with pytest.raises(fg.ParameterError):
         h.set_order_window(0.0, 1.0)
+
+
+def test_window_inverse_inside_and_truncation_fallback():
+    """A window around zero serves the inverse apply (Q(a)^H = Q(-a), -a inside the window); a
+    truncated apply cannot use the full-L node operators and falls back to the packed route."""
+    n, l, b = 512, 16, 70
+    f = prep.gft_from_shift(prep.laplacian(prep.grid_graph(16, 32)))
+    o = O.PowerCache(f, l)
+    g = fg.PowerCache(f, l, memory_budget=4 << 30)
+    assert g.set_order_window(-1.0, 1.0) > 0
+    r = np.random.default_rng(9)
+    x = r.standard_normal((n, b)) + 1j * r.standard_normal((n, b))
+    for alphas in ([0.3], [0.7, -0.45]):
+        y = fg.apply_series(g, alphas, x, inverse=True)
+        for i, a in enumerate(alphas):
+            q = O.fgfrft_matrix(o, a)
+            assert rel(y[i], q.conj().T @ x) <= 1e-10
+    yt = fg.apply_series(g, [0.3], x, truncation=9)
+    assert rel(yt[0], O.fgfrft_matrix(o, 0.3, truncation=9) @ x) <= 1e-10
+    xc = x + 0.05 * r.standard_normal((n, b))
+    loss, dl, _ = fg.mse_step(g, [-0.8], x, xc)
+    assert g.route_info()[0] == 5
+    lr, dr, _ = O.dlda_mse(o, -0.8, x, xc)
+    assert abs(loss[0] - lr) <= 1e-10 * lr
