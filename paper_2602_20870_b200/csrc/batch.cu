@@ -875,13 +875,16 @@ batch_fwd_tc_kernel(const float* __restrict__ slabs, int l, const float* __restr
                             im[2 * m + 1] = v.w;
                         }
                         const int n0 = 2 * (32 * half + cl);
-                        uint4 hi, lo;
-                        tc_split8(re, hi, lo);
-                        st_shared_v4(xhl + tc_off(128, n0, kc), hi);
-                        st_shared_v4(xhl + 16384 + tc_off(128, n0, kc), lo);
-                        tc_split8(im, hi, lo);
-                        st_shared_v4(xhl + tc_off(128, n0 + 1, kc), hi);
-                        st_shared_v4(xhl + 16384 + tc_off(128, n0 + 1, kc), lo);
+                        uint4 rh, rl, ih, il;
+                        tc_split8(re, rh, rl);
+                        tc_split8(im, ih, il);
+                        // odd kc lanes store their imaginary row first: each store instruction then
+                        // covers all 8 16-byte bank groups of a 128-byte row group (2x fewer wavefronts)
+                        const int sw = kc & 1, na = n0 + sw, nb = n0 + 1 - sw;
+                        st_shared_v4(xhl + tc_off(128, na, kc), sw ? ih : rh);
+                        st_shared_v4(xhl + 16384 + tc_off(128, na, kc), sw ? il : rl);
+                        st_shared_v4(xhl + tc_off(128, nb, kc), sw ? rh : ih);
+                        st_shared_v4(xhl + 16384 + tc_off(128, nb, kc), sw ? rl : il);
                     }
                     ring.release(rc, lane);
                     rc.next(stages);
