@@ -625,6 +625,20 @@ def main():
     t_wall = (time.perf_counter() - t_wall) / args.steps
     e2e_dev_ms = e0.elapsed_time(e1) / args.steps
     e2e_ms = max(e2e_dev_ms, t_wall * 1e3)
+    # the link floor of the e2e number: the same 2 N B complex128 bytes as one plain pinned H2D copy
+    # each (no kernels), median of 5 -- e2e / this = how close the step sits to the host link
+    h2d_dst = torch.empty(2 * n * b * 16, dtype=torch.uint8, device=f"cuda:{local}")
+    h2d_ms = []
+    for _ in range(5):
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            h2d_dst[: n * b * 16].copy_(xh.view(torch.uint8).reshape(-1), non_blocking=True)
+            h2d_dst[n * b * 16:].copy_(xch.view(torch.uint8).reshape(-1), non_blocking=True)
+            e1.record(stream)
+        e1.synchronize()
+        h2d_ms.append(e0.elapsed_time(e1))
+    h2d_ms = float(np.median(h2d_ms))
+    del h2d_dst
 
     extras = {}
     win_out = None
@@ -731,7 +745,10 @@ def main():
                                 "lazily built step structures, once per cache"},
         "e2e": {"value": n * b / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                 "device_ms": e2e_dev_ms, "wall_ms": t_wall * 1e3,
-                "h2d_bytes_per_step": 2 * n * b * 16, "d2h_bytes_per_step": 2 * 8},
+                "h2d_bytes_per_step": 2 * n * b * 16, "d2h_bytes_per_step": 2 * 8,
+                "h2d_copy_only_ms": h2d_ms, "h2d_copy_only_gbs": 2 * n * b * 16 / (h2d_ms * 1e-3) / 1e9,
+                "note": "h2d_copy_only = the step's X + Xc bytes as plain pinned H2D copies on the same stream "
+                        "(the host link's floor for this e2e; it varies box to box)"},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk,

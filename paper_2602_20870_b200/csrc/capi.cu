@@ -1778,8 +1778,14 @@ int ensure_pipe_streams(fgfrft_cache* c) {
 // x_host != nullptr: X is still on the host -- it is copied into x_dev in column chunks on the
 // aux stream, and the GEMM runs per chunk as its columns land, so the host->device transfer
 // overlaps the synthesis (which does not need X) and the earlier chunks' products.
+int64_t fused_mse_slots_per_order(int64_t n, int64_t b) {
+    return (pad_rows(n) / kOzTileA) * (ceil_div(2 * b, kOzTileB) * kOzTileB / kOzTileB) * 16;
+}
+
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
-                    void* y, int l_used, const double* x_host, const WindowWeights* ww) {
+                    void* y, int l_used, const double* x_host, const WindowWeights* ww, const double* fuse_xc,
+                    double* fuse_part, bool* fused) {
+    if (fused) *fused = false;
     const int S = step_slices();
     const int64_t n = c->n, mp = pad_rows(n), sl = n * n, kp = pad_k(n);
     const int64_t bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
@@ -1953,11 +1959,17 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         {
             ProfScope ps(KC_I8GEMM, c->pk_g);
             const bool last = s + 1 == plan.size();
+            OzOut o = gemm_out(static_cast<double*>(y) + 2 * sh.r0, rv, rp, 2 * b,
+                               static_cast<const double*>(x_dev) + 2 * sh.r0, last ? 0 : gcap);
+            // fused MSE: one shell of [Q_a; dQ_a] rows (rows = 2 n_alpha blocks), the loss pass in the
+            // epilogue (dY is never stored)
+            if (fuse_xc && fuse_part && plan.size() == 1 && rows % 2 == 0) {
+                o.lpart = fuse_part;
+                o.lxc = fuse_xc + 2 * sh.r0;
+                if (fused) *fused = true;
+            }
             FGB_LAUNCH(launch_ozgemm_ex(S, 1, dst, ex, (int)(rows * rp), c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
-                                        (int)kp,
-                                        gemm_out(static_cast<double*>(y) + 2 * sh.r0, rv, rp, 2 * b,
-                                                 static_cast<const double*>(x_dev) + 2 * sh.r0, last ? 0 : gcap),
-                                        c->pk_g),
+                                        (int)kp, o, c->pk_g),
                        1);
         }
         row_off += rp;
@@ -1973,7 +1985,29 @@ int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void
     const int64_t n = c->n, blk = 2 * n * b;  // doubles per n x b complex block
     const int rows = 2 * n_alpha;             // table rows [c(a_0) ..][c'(a_0) ..]: Q_a then dQ_a
     FGB_CUDA(c->ydy.ensure((size_t)rows * blk * sizeof(double)));
-    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l, x_host, ww)) return st;
+    // device-resident step: the loss pass rides in the product GEMM's epilogue (FGFRFT_FUSED_MSE=0:
+    // the separate mse_dy pass). The host-X form keeps the separate pass: Xc lands last there.
+    const bool want_fuse = !x_host && pk_env("FGFRFT_FUSED_MSE", 1) != 0 &&
+                           (ww ? pk_env("FGFRFT_WIN_SHELLS", 1) <= 1 : pk_env("FGFRFT_PIPE_SHELLS", 1) <= 1);
+    const int64_t per = fused_mse_slots_per_order(n, b);
+    if (want_fuse) FGB_CUDA(c->lpart.ensure((size_t)n_alpha * per * 2 * sizeof(double)));
+    bool fused = false;
+    void* yd = want_fuse && y_dev ? y_dev : c->ydy.p;  // fused: Y lands in the caller's buffer directly
+    if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, yd, c->l, x_host, ww,
+                                 want_fuse ? static_cast<const double*>(xc_dev) : nullptr,
+                                 want_fuse ? c->lpart.as<double>() : nullptr, &fused))
+        return st;
+    if (fused) {
+        const double norm = 1.0 / ((double)n * (double)b);
+        ProfScope ps(KC_ELEMWISE, c->stream);
+        FGB_LAUNCH(launch_fused_mse_finish(c->lpart.as<double>(), per, n_alpha, norm, loss_dev, dlda_dev, c->stream), 1);
+        c->last_route = c->pk_win ? 5 : c->pk_tc ? 4 : 3;
+        c->last_nodes = c->pk_win ? c->win_r : 0;
+        return FGFRFT_OK;
+    }
+    if (yd != c->ydy.p) {  // not fused after all (a multi-shell plan): Y and dY in the step buffer
+        if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l, x_host, ww)) return st;
+    }
     if (xc_host) {  // Xc behind X on the aux stream: only the final loss pass needs it
         if (!c->xc_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->xc_evt, cudaEventDisableTiming));
         FGB_CUDA(cudaMemcpyAsync(const_cast<void*>(xc_dev), xc_host, (size_t)n * b * 16, cudaMemcpyHostToDevice,

@@ -186,6 +186,10 @@ cudaError_t launch_sum_slots(const double* slots, int nslots, int64_t count, dou
 size_t packed_scale_elems(int n, int l);
 int64_t packed_pairs_before(int I, int nt);
 size_t mse_dy_part_elems();
+// The fused-MSE product GEMM's partials (OzOut::lpart): order a owns the slot run [a per, (a + 1) per)
+// of (loss, dot) pairs, per = Y tiles of one block x 16 epilogue warps; loss = sum * norm, dL/da = 2 dot norm.
+cudaError_t launch_fused_mse_finish(const double* part, int64_t per, int n_alpha, double norm, double* loss,
+                                    double* dlda, cudaStream_t stream);
 cudaError_t launch_mse_dy(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
                           double norm, double* loss, double* dlda, cudaStream_t stream);
 }  // namespace fgb
@@ -521,7 +525,10 @@ bool ensure_packed(fgfrft_cache* c);
 bool ensure_dsynth(fgfrft_cache* c);
 bool ensure_step_cache(fgfrft_cache* c);
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
-                    void* y, int l_used, const double* x_host = nullptr, const WindowWeights* ww = nullptr);
+                    void* y, int l_used, const double* x_host = nullptr, const WindowWeights* ww = nullptr,
+                    const double* fuse_xc = nullptr, double* fuse_part = nullptr, bool* fused = nullptr);
+// slots the fused-MSE product GEMM writes per order (launch_fused_mse_finish's per), in double2
+int64_t fused_mse_slots_per_order(int64_t n, int64_t b);
 // true (and the weights rows [l_j(a) ..][l_j'(a) ..] when with_d) when every order lies in the window
 bool window_weights(const fgfrft_cache* c, const double* alphas, int n_alpha, bool with_d, int l_used,
                     WindowWeights* ww);

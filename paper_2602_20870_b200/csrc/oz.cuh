@@ -98,6 +98,15 @@ struct OzOut {
     // (pair_n x pair_n); dg[x] added on the diagonal; rmax[x * rnp + row] = the row maxima (zeroed
     // by the caller). Each CTA takes the 8 M tiles of a tile pair in a row.
     int pair_nt = 0, pair_n = 0;
+    // CM 1 fused MSE + dL/da (the packed step, DESIGN 3.7): A = [Q_a blocks; dQ_a blocks] (2 n_alpha
+    // blocks of mp rows, an even number of M tiles); each CTA takes M tile mt and then mt + mtiles / 2
+    // (the dQ rows of the same Q rows) with the same N tile, so the thread that stored Y[i, j] meets
+    // dY[i, j] one unit later: the Y tile is stored and sum |Y - Xc|^2 accumulated, the dY tile is NOT
+    // stored and sum Re conj(Y - Xc) dY accumulated (Y read back from c, block bm - n_alpha). Warp
+    // sums per Y tile (mt < mtiles / 2, nt) land in lpart[((mt * ntiles + nt) * 16 + ew) * 2 + {0, 1}]
+    // (fixed order: the finish kernel's sums are deterministic). lxc: Xc, laid out as C in a block.
+    double* lpart = nullptr;
+    const double* lxc = nullptr;
 };
 
 constexpr int kOzTileA = 128;  // A operand row tile (output rows per CTA)

@@ -463,10 +463,16 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
     constexpr bool pairs = P;
     const bool chunk = CM == 0 && CL == 1 && out.rmax != nullptr && out.nv <= 32 && !pairs;  // (the skinny epilogue)
     const int upp = 8 * ngroups;  // pair mode: units of one tile pair (8 M tiles x the N tiles)
-    const int ub = pairs ? cid * upp : cid, ue = units, us = nclusters;
-    auto next_u = [&](int u) { return pairs ? ((u % upp) == upp - 1 ? u + upp * us - (upp - 1) : u + 1) : u + us; };
-    auto unit_mt = [&](int u) { return u / ngroups; };
-    auto unit_nt = [&](int u) { return (u % ngroups) * CL + rank; };
+    // fused MSE (CM 1, out.lpart): units 2 pu (Y tile) and 2 pu + 1 (its dY tile) back to back per CTA
+    const bool fmse = CM == 1 && out.lpart != nullptr;
+    const int mhalf = mtiles >> 1;
+    const int ub = pairs ? cid * upp : (fmse ? 2 * cid : cid), ue = units, us = nclusters;
+    auto next_u = [&](int u) {
+        if (fmse) return (u & 1) ? u - 1 + 2 * us : u + 1;
+        return pairs ? ((u % upp) == upp - 1 ? u + upp * us - (upp - 1) : u + 1) : u + us;
+    };
+    auto unit_mt = [&](int u) { return fmse ? (u >> 1) / ngroups + (u & 1) * mhalf : u / ngroups; };
+    auto unit_nt = [&](int u) { return ((fmse ? (u >> 1) : u) % ngroups) * CL + rank; };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -527,7 +533,8 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
         const int lrow = lg * 32 + lane;
         const uint32_t lane_addr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(h * kOzEC);
         int tcount = 0;
-        double gacc[3] = {0.0, 0.0, 0.0};  // CM 2: <X, Z_kk>, <Xc, Z_kk>, <Z_L, Z_kk> over this thread's tiles
+        double gacc[3] = {0.0, 0.0, 0.0};
+        double ls1 = 0.0, ls2 = 0.0;       // CM 1 fused MSE: sum |Y - Xc|^2, sum Re conj(Y - Xc) dY  // CM 2: <X, Z_kk>, <Xc, Z_kk>, <Z_L, Z_kk> over this thread's tiles
         double lacc[kOzEC];                // CM 3: sum (Y - Xc)^2 per order column
         if (CM == 3) {
 #pragma unroll
@@ -807,6 +814,20 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                         v0 = fma(d, xv.x, v0);
                         v1 = fma(d, xv.y, v1);
                     }
+                    if (CM == 1 && fmse) {  // fused MSE: Y tile (even unit) / its dY tile (odd unit)
+                        const int64_t o = (i + (int64_t)(n >> 1) * out.ldc) * 2;
+                        const double2 xc = *reinterpret_cast<const double2*>(out.lxc + o);
+                        if (!(u & 1)) {
+                            *reinterpret_cast<double2*>(cb + o) = make_double2(v0, v1);  // re-read by this thread
+                            const double rx = v0 - xc.x, ry = v1 - xc.y;
+                            ls1 = fma(rx, rx, fma(ry, ry, ls1));
+                        } else {
+                            const double2 yv = *reinterpret_cast<const double2*>(
+                                out.c + (int64_t)(bm - (mhalf * kOzBM) / out.mp) * out.sc + o);
+                            ls2 = fma(yv.x - xc.x, v0, fma(yv.y - xc.y, v1, ls2));
+                        }
+                        continue;
+                    }
                     if (CM == 0) {
                         const int64_t o0 = (int64_t)bm * out.sc + i + (int64_t)n * out.ldc;
                         __stcs(cb + i + (int64_t)n * out.ldc, v0);
@@ -826,6 +847,17 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
                             *reinterpret_cast<double2*>(out.peers[q] + o) = make_double2(v0, v1);
                     }
                 }
+            }
+            if (CM == 1 && fmse && (u & 1)) {  // pair unit done: warp sums in fixed order
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    ls1 += __shfl_xor_sync(0xffffffffu, ls1, o);
+                    ls2 += __shfl_xor_sync(0xffffffffu, ls2, o);
+                }
+                if (lane == 0)
+                    *reinterpret_cast<double2*>(out.lpart + ((int64_t)((mt - mhalf) * ntiles + nt) * kOzEpiWarps + ew) * 2) =
+                        make_double2(ls1, ls2);
+                ls1 = ls2 = 0.0;
             }
             }  // BN == kOzBN
         }

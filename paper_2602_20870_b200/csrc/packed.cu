@@ -478,6 +478,45 @@ __global__ void __launch_bounds__(64) mse_dy_finish_kernel(const double* __restr
 
 size_t mse_dy_part_elems() { return 2 * kMdBlocks; }
 
+// One CTA per order: fixed-order strided sums and a fixed tree (deterministic run to run).
+__global__ void __launch_bounds__(256) fused_mse_finish_kernel(const double2* __restrict__ part, int64_t per,
+                                                               double norm, double* __restrict__ loss,
+                                                               double* __restrict__ dlda) {
+    __shared__ double red[2][8];
+    const double2* p = part + (int64_t)blockIdx.x * per;
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t i = threadIdx.x; i < per; i += 256) {
+        const double2 v = p[i];
+        s1 += v.x;
+        s2 += v.y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = s1;
+        red[1][threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t1 = 0.0, t2 = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            t1 += red[0][w];
+            t2 += red[1][w];
+        }
+        loss[blockIdx.x] = t1 * norm;
+        dlda[blockIdx.x] = 2.0 * t2 * norm;
+    }
+}
+
+cudaError_t launch_fused_mse_finish(const double* part, int64_t per, int n_alpha, double norm, double* loss,
+                                    double* dlda, cudaStream_t stream) {
+    fused_mse_finish_kernel<<<n_alpha, 256, 0, stream>>>(reinterpret_cast<const double2*>(part), per, norm, loss, dlda);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_mse_dy(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
                           double norm, double* loss, double* dlda, cudaStream_t stream) {
     mse_dy_kernel<<<kMdBlocks, 256, 0, stream>>>((const double2*)y, (const double2*)dy, (const double2*)xc, count,
