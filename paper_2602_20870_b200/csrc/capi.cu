@@ -1583,16 +1583,24 @@ bool ensure_packed(fgfrft_cache* c) {
         c->pk_state = -1;
         return false;
     }
+    // the powers' row / column maxima (the digit-emitting synthesis' row bounds): 2 L N doubles, best effort
+    const uint64_t mbytes = (uint64_t)c->l * 2 * ceil_div(c->n, kTile) * kTile * sizeof(double);
+    if (!aux_fits(c, bytes + sbytes + mbytes) || c->pkm.ensure(mbytes) != cudaSuccess) {
+        cudaGetLastError();
+        c->pkm.release();
+    }
     ProfScope ps(KC_SLICE, c->stream);
-    if (launch_pack_tiles(c->slabs, (int)c->n, c->l, c->pk.p, c->pks.as<double>(), c->stream) != cudaSuccess) {
+    if (launch_pack_tiles(c->slabs, (int)c->n, c->l, c->pk.p, c->pks.as<double>(), c->stream,
+                          c->pkm.p ? c->pkm.as<unsigned long long>() : nullptr) != cudaSuccess) {
         cudaGetLastError();
         c->pk.release();
         c->pks.release();
+        c->pkm.release();
         c->pk_state = -1;
         return false;
     }
     g_launches += 1;
-    c->aux_bytes += bytes + sbytes;
+    c->aux_bytes += bytes + sbytes + (c->pkm.p ? mbytes : 0);
     c->pk_state = 1;
     return true;
 }
@@ -1863,13 +1871,18 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
                                    reinterpret_cast<unsigned long long*>(xe + bp), c->pk_g),
                    3);
     }
-    FGB_CUDA(cudaMemsetAsync(rmax, 0, (size_t)rows * mp * sizeof(unsigned long long), c->pk_s));
     // synthesis engine: the window's node operators, tensor-core digits (dsynth) or the packed FP64
     // decode (psynth)
     const bool tc = !ww && dsynth_wanted() && c->ds_state > 0;
     c->pk_tc = tc;
     c->pk_win = ww != nullptr;
     if (!ww && !tc && !ensure_packed(c)) return FGFRFT_CAPACITY;
+    // psynth emits [Q; dQ]'s digits itself (row exponents from the power maxima, prow_bound_kernel):
+    // one order, one shell, whole 128-row tiles (FGFRFT_PSYNTH_DIGITS=0: FP64 Q + the slicing pass)
+    const bool emit = !ww && !tc && plan.size() == 1 && rows == 2 && n % kOzTileA == 0 && c->pkm.p &&
+                      oz_bk(S) == 64 && pk_env("FGFRFT_PSYNTH_DIGITS", 1) != 0;
+    c->pk_emit = emit;
+    if (!emit) FGB_CUDA(cudaMemsetAsync(rmax, 0, (size_t)rows * mp * sizeof(unsigned long long), c->pk_s));
     const int64_t dkp = dsynth_kp(c->l);
     if (tc) {
         ProfScope ps(KC_SYNTH, c->pk_s);
@@ -1906,7 +1919,18 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
         const int64_t rv = sh.r1 - sh.r0, rp = pad_rows(rv);
         int8_t* dst = c->qsl.as<int8_t>() + (size_t)S * rows * row_off * kp;
         int* ex = exps + rows * row_off;
-        {
+        if (emit) {
+            {
+                ProfScope ps(KC_SLICE, c->pk_s);
+                FGB_LAUNCH(launch_prow_bound(c->pkm.as<unsigned long long>(), (int)n, l_used, coef, coef_ld, rows,
+                                             (int)rp, ex, c->pk_s),
+                           1);
+            }
+            ProfScope ps(KC_SYNTH, c->pk_s);
+            FGB_LAUNCH(launch_psynth(c->pk.p, c->pks.as<double>(), (int)n, l_used, c->l, coef, coef_ld, rows, nullptr, 0,
+                                     nullptr, 0, c->pk_s, sh.p0, sh.p1, 0, 0, 1, dst, ex, (int)rp, (int)kp, S),
+                       1);
+        } else {
             ProfScope ps(KC_SYNTH, c->pk_s);
             // shell 0 runs alone (the GEMM has nothing yet): full grid; later shells share the GPU
             if (ww)
@@ -1923,7 +1947,7 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
                                          rmax, mp, c->pk_s, sh.p0, sh.p1, s == 0 ? 0 : syn_cap, 0, 1),
                            1);
         }
-        {
+        if (!emit) {
             OzView v{q + sh.r0, 1, n, sl, 0, 0, (int)rv, (int)rp, rows, (int)n, (int)kp, true};
             v.rmb = mp;
             ProfScope ps(KC_SLICE, c->pk_s);

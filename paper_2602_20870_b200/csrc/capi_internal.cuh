@@ -169,7 +169,11 @@ cudaError_t launch_combine(int mode, const double* z, const double* x, const dou
                            double* loss, cudaStream_t stream);
 // packed.cu (the packed power cache and the one- / two-order step route)
 size_t packed_bytes(int n, int l);
-cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream);
+cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream,
+                              unsigned long long* pmax = nullptr);
+// exps[a rp + i] = the Ozaki row exponent of a bound on |(Q_a - c_0 I)[i, :]| from the power maxima
+cudaError_t launch_prow_bound(const unsigned long long* pmax, int n, int l, const double* coef, int coef_ld, int ac,
+                              int rp, int* exps, cudaStream_t stream);
 // the order window (packed.cu): Q_x = sum_j w[x][j] W'_j over r <= kWindowMaxNodes node operators
 cudaError_t launch_window_synth(const double* wops, int r, int n, const WindowWeights& ww, int rows, double* out,
                                 int64_t ostride, unsigned long long* rowmax, int64_t mp, cudaStream_t stream,
@@ -177,7 +181,8 @@ cudaError_t launch_window_synth(const double* wops, int r, int n, const WindowWe
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
                           int64_t rm_stride, cudaStream_t stream, int p0 = 0, int p1 = -1, int max_ctas = 0,
-                          int pbase = 0, int nodiag = 0);
+                          int pbase = 0, int nodiag = 0, int8_t* digits = nullptr, const int* exps = nullptr,
+                          int rp = 0, int kp = 0, int sd = 0);
 cudaError_t launch_pack_pairs_from_panels(const double* rp, int64_t ld_r, const double* cp, int64_t ld_c, int n, int I0,
                                           int pbase, int npairs_local, int k, int l, void* packed, double* scales,
                                           cudaStream_t stream);
@@ -415,11 +420,13 @@ struct fgfrft_cache {
     // two-order step and apply route (real F). 0 not built, 1 ready, -1 unavailable.
     int pk_state = 0;
     DevBuf pk, pks, ydy;
+    DevBuf pkm;  // [L][2][32 nt] row / column maxima of the powers (digit-emitting synthesis; empty: off)
     // Digit cache of the INT8 tensor-core synthesis (ozgemm.cu dsynth_kernel): pair-major element
     // rows x powers, 5 base-254 digits + one exponent per element row; the coefficient digits.
     // Replaces the packed slabs on the step route when it fits. 0 not built, 1 ready, -1 unavailable.
     int ds_state = 0;
     bool pk_tc = false;  // the last packed_products synthesised on the tensor cores
+    bool pk_emit = false;  // the last packed_products' synthesis emitted Q's digits (no slicing pass)
     // the order window (fgfrft_cache_set_order_window): r exact FP64 node operators W'_j (c_0 I left
     // out) at the Chebyshev nodes of [win_lo, win_hi]; the step route synthesises Q, dQ/da of orders
     // inside it from these instead of the packed powers

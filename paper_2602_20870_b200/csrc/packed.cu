@@ -43,10 +43,15 @@ size_t packed_scale_elems(int n, int l) {
 // A CTA walking a pair streams one contiguous L * 10 KB region, one bulk copy per power.
 
 // One CTA per tile of every power: grid = l * ntiles, 256 threads x 4 elements.
+// pmax (optional, [L][2][32 nt] ordered double bits, zeroed by the caller): max_j |P_k[i, j]| (slot 0)
+// and max_j |P_k[j, i]| (slot 1) of every power, plus the tile's quantum (so they bound the DECODED
+// values) -- the per-row bounds the digit-emitting synthesis scales Q's rows by (prow_bound_kernel).
 __global__ void __launch_bounds__(256) pack_tiles_kernel(const double* __restrict__ slabs, int64_t slab_elems,
                                                          int nt, int l, unsigned char* __restrict__ packed,
-                                                         double* __restrict__ scales) {
+                                                         double* __restrict__ scales,
+                                                         unsigned long long* __restrict__ pmax) {
     __shared__ double red[8];
+    __shared__ double ab[kTile][kTile + 1];
     const int64_t ntiles = (int64_t)nt * nt;
     const int64_t tile = blockIdx.x;
     const int64_t k = tile / ntiles, t = tile - k * ntiles;  // k = power - 1; t = J * nt + I
@@ -70,6 +75,23 @@ __global__ void __launch_bounds__(256) pack_tiles_kernel(const double* __restric
     if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
     e = max(e, -900);              // all-tiny tiles quantise to 0 instead of overflowing the scale
     const double up = ldexp(1.0, kPkFrac - e);
+    if (pmax) {  // element t = (row (t & 31) ^ (t >> 5), column t >> 5) of the swizzled tile
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int t = threadIdx.x + 256 * i, cj = t >> 5;
+            ab[(t & 31) ^ cj][cj] = fabs(v[i]);
+        }
+        __syncthreads();
+        if (threadIdx.x < 2 * kTile) {
+            const int q = threadIdx.x & 31, col = threadIdx.x >> 5;  // col 0: row q's max, 1: column q's
+            double m2 = 0.0;
+            for (int z = 0; z < kTile; ++z) m2 = fmax(m2, col ? ab[z][q] : ab[q][z]);
+            m2 += ldexp(1.0, e - kPkFrac);  // the decoded value is within one quantum
+            const int64_t npad = (int64_t)nt * kTile;
+            atomicMax(pmax + (k * 2 + col) * npad + (col ? J : I) * kTile + q,
+                      (unsigned long long)__double_as_longlong(m2));
+        }
+    }
     const int lo_i = min(I, J), hi_j = max(I, J);
     const int64_t pair = pairs_before(lo_i, nt) + (hi_j - lo_i);
     for (int slot = (I <= J ? 0 : 1); slot <= (I < J ? 0 : 1); ++slot) {  // diagonal: both slots
@@ -88,11 +110,51 @@ __global__ void __launch_bounds__(256) pack_tiles_kernel(const double* __restric
     }
 }
 
-cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream) {
+cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, double* scales, cudaStream_t stream,
+                              unsigned long long* pmax) {
     const int nt = (int)ceil_div(n, kTile);
     const int64_t ntiles = (int64_t)nt * nt;
+    if (pmax) {
+        cudaError_t e = cudaMemsetAsync(pmax, 0, (size_t)l * 2 * nt * kTile * sizeof(unsigned long long), stream);
+        if (e != cudaSuccess) return e;
+    }
     pack_tiles_kernel<<<(unsigned)(ntiles * l), 256, 0, stream>>>((const double*)slabs, ntiles * kTileElems, nt, l,
-                                                                  (unsigned char*)packed, scales);
+                                                                  (unsigned char*)packed, scales, pmax);
+    return cudaGetLastError();
+}
+
+// Row bounds of Q_a - c_0 I from the power maxima: R_i = sum_(k=1..l) |c_a(k)| max_j |P_k[i, j]| +
+// |c_a(-k)| max_j |P_k[j, i]| >= max_j |Q_a[i, j] - c_0 delta_ij| (the series' triangle inequality;
+// inflated by 2^-40 for the synthesis' own FP64 rounding), and exps[a rp + i] = e with R_i < 2^e --
+// the row exponents of the product GEMM's Ozaki slicing (|Q[i, :]| 2^(-e-1) < 1/2), known BEFORE
+// Q exists, so the synthesis can emit Q's digits directly (psynth_pairs_kernel SD > 0). A row whose
+// bound is loose by 2^b loses b bits of the ~47 the 6 digits carry (measured ~2.5 bits on graph
+// GFTs: 4-6x at N = 1024). coef rows: a * coef_ld, c_k at l + k.
+__global__ void __launch_bounds__(256) prow_bound_kernel(const unsigned long long* __restrict__ pmax, int64_t npad,
+                                                         int l, const double* __restrict__ coef, int coef_ld, int rp,
+                                                         int* __restrict__ exps) {
+    const int i = blockIdx.x * 256 + threadIdx.x, a = blockIdx.y;
+    if (i >= rp) return;
+    const double* cr = coef + (int64_t)a * coef_ld + l;
+    double r = 0.0;
+    if (i < npad) {
+        for (int k = 1; k <= l; ++k) {
+            const double mr = __longlong_as_double((long long)pmax[(int64_t)(k - 1) * 2 * npad + i]);
+            const double mc = __longlong_as_double((long long)pmax[((int64_t)(k - 1) * 2 + 1) * npad + i]);
+            r = fma(fabs(cr[k]), mr, fma(fabs(cr[-k]), mc, r));
+        }
+    }
+    r *= 1.0 + 0x1p-40;
+    int e = 0;
+    if (r > 0.0) frexp(r, &e);
+    exps[(int64_t)a * rp + i] = e;
+}
+
+cudaError_t launch_prow_bound(const unsigned long long* pmax, int n, int l, const double* coef, int coef_ld, int ac,
+                              int rp, int* exps, cudaStream_t stream) {
+    const int64_t npad = ceil_div(n, kTile) * kTile;
+    prow_bound_kernel<<<dim3((unsigned)ceil_div(rp, 256), (unsigned)ac), 256, 0, stream>>>(pmax, npad, l, coef,
+                                                                                          coef_ld, rp, exps);
     return cudaGetLastError();
 }
 
@@ -127,12 +189,53 @@ __device__ __forceinline__ void consumer_sync(int g) { asm volatile("bar.sync %0
 
 // Stage s of a pair's items is (k - 1) % S (every pair restarts at stage 0, so the consumer's
 // stage offsets are compile-time immediates); per-stage phase bits track the reuse.
-template <int AC, int G, int S>
+// SD > 0 (digit emission, n % 128 == 0): instead of FP64 Q and its row maxima, the kernel writes Q's
+// SD balanced base-254 digits straight into the product GEMM's sliced A operand (ozgemm.cu layout:
+// 128-row tiles x 64-byte K blocks, SD digit planes of 8 KB per block, 8-row core groups 512 B apart),
+// scaled per row by the exponents prow_bound_kernel derived from the power maxima -- the FP64 Q round
+// trip through HBM and the slicing pass disappear. Digit arithmetic = oz_write_digits'.
+struct PsDigits {
+    int8_t* dig = nullptr;
+    const int* exps = nullptr;  // [a * rp + row]
+    int rp = 0, kbc = 0;        // padded rows per output block, 64-byte K blocks
+};
+
+template <int SD>
+__device__ __forceinline__ void ps_digits4(double (&x)[4], int8_t* base) {  // 4 consecutive K of one row
+#pragma unroll
+    for (int s = 0; s < SD; ++s) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double y = x[i] * 254.0;
+            const double t = y + 6755399441055744.0;  // rint(y) in the low word
+            x[i] = y - (t - 6755399441055744.0);
+            w |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * i);
+        }
+        *reinterpret_cast<uint32_t*>(base + s * 8192) = w;
+    }
+}
+template <int SD>
+__device__ __forceinline__ void ps_digits1(double x, int8_t* base) {
+#pragma unroll
+    for (int s = 0; s < SD; ++s) {
+        const double y = x * 254.0;
+        const double t = y + 6755399441055744.0;
+        x = y - (t - 6755399441055744.0);
+        base[s * 8192] = (int8_t)__double2loint(t);
+    }
+}
+__device__ __forceinline__ int8_t* ps_digit_addr(int8_t* dig, int sd, int kbc, int m, int k) {
+    return dig + ((int64_t)(m >> 7) * kbc + (k >> 6)) * (sd * 8192) + ((m & 127) >> 3) * 512 + ((k >> 4) & 3) * 128 +
+           (m & 7) * 16 + (k & 15);
+}
+
+template <int AC, int G, int S, int SD = 0>
 __global__ void __launch_bounds__(G * (kPsConsumers + 32), 1)
 psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __restrict__ scales, int n, int l,
                     int lc, const double* __restrict__ coef, int coef_ld, double* __restrict__ out, int64_t out_stride,
                     unsigned long long* __restrict__ rowmax, int64_t rm_stride, int nt, int p0, int p1,
-                    int pbase, int nodiag) {
+                    int pbase, int nodiag, PsDigits pd) {
     constexpr int kStage = 2 * kPkTileBytes;
     extern __shared__ __align__(128) unsigned char smem_all[];
     const int g = threadIdx.x / (kPsConsumers + 32);
@@ -191,7 +294,9 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
         return;
     }
     // ---------------- consumer warps: thread (lane r, warp) owns elements (r, c_i) of tile (I,J)
-    // and (c_i, r) of tile (J,I), c_i = warp + 8 i; their byte offsets inside a stage are fixed
+    // and (c_i, r) of tile (J,I), c_i = 4 warp + i (4 consecutive K of a row: one 32-bit digit store
+    // per digit plane when emitting); their byte offsets inside a stage are fixed (the XOR swizzle
+    // keeps every fixed-c_i read conflict free)
     const int r = lane;
     const uint32_t* lo1p[4];  // element (r, c_i) of tile 1 and (c_i, r) of tile 2, stage 0
     const uint8_t* hi1p[4];
@@ -199,7 +304,7 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
     const uint8_t* hi2p[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const int c = warp + 8 * i;
+        const int c = 4 * warp + i;
         lo1p[i] = reinterpret_cast<const uint32_t*>(ring) + swz(r, c);
         hi1p[i] = ring + kTileElems * 4 + swz(r, c);
         lo2p[i] = reinterpret_cast<const uint32_t*>(ring + kPkTileBytes) + swz(c, r);
@@ -218,7 +323,7 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int a = 0; a < AC; ++a) {
-                q1[i][a] = (diag && r == warp + 8 * i) ? ctab[a * cw + l] : 0.0;
+                q1[i][a] = (diag && r == 4 * warp + i) ? ctab[a * cw + l] : 0.0;
                 q2[i][a] = 0.0;
             }
         for (int k0 = 1; k0 <= l; k0 += S) {
@@ -254,13 +359,34 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
                 if (lane == 0) mbar_arrive(&empty[u]);
             }
         }
-        // Q[I-tile, J-tile]: rows r (lanes), columns c = warp + 8 i; row maxima across the 8 warps
+        if constexpr (SD > 0) {  // digits of both tiles straight into the product GEMM's A operand
+#pragma unroll
+            for (int a = 0; a < AC; ++a) {
+                {  // Q[32 I + r, 32 J + 4 warp .. + 3]: one 32-bit store per digit plane
+                    const int m = a * pd.rp + I * kTile + r, k0 = J * kTile + 4 * warp;
+                    const double sc = __longlong_as_double((long long)(1022 - pd.exps[m]) << 52);  // 2^(-e-1)
+                    double x[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) x[i] = q1[i][a] * sc;
+                    ps_digits4<SD>(x, ps_digit_addr(pd.dig, SD, pd.kbc, m, k0));
+                }
+                if (!diag) {  // Q[32 J + 4 warp + i, 32 I + r]: lanes along K, byte stores
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int m = a * pd.rp + J * kTile + 4 * warp + i;
+                        const double sc = __longlong_as_double((long long)(1022 - pd.exps[m]) << 52);
+                        ps_digits1<SD>(q2[i][a] * sc, ps_digit_addr(pd.dig, SD, pd.kbc, m, I * kTile + r));
+                    }
+                }
+            }
+        } else {
+        // Q[I-tile, J-tile]: rows r (lanes), columns c = 4 warp + i; row maxima across the 8 warps
 #pragma unroll
         for (int a = 0; a < AC; ++a) {
             double mx = 0.0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int c = warp + 8 * i;
+                const int c = 4 * warp + i;
                 if (r < bi && c < bj) {
                     out[(int64_t)a * out_stride + (int64_t)(J * kTile + c) * n + I * kTile + r] = q1[i][a];
                     mx = fmax(mx, fabs(q1[i][a]));
@@ -269,13 +395,12 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
             red[(a * 8 + warp) * 32 + lane] = mx;
         }
         if (!diag) {
-            // Q[J-tile, I-tile]: thread (lane r, warp) holds Q[J*32 + warp + 8i, I*32 + r]; the stores of
-            // a 32-byte sector come from 4 warps and merge in L2
+            // Q[J-tile, I-tile]: thread (lane r, warp) holds Q[J*32 + 4 warp + i, I*32 + r]
 #pragma unroll
             for (int a = 0; a < AC; ++a)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int row = warp + 8 * i;
+                    const int row = 4 * warp + i;
                     const bool ok = r < bi && row < bj;
                     double m = ok ? fabs(q2[i][a]) : 0.0;
                     if (ok) out[(int64_t)a * out_stride + (int64_t)(I * kTile + r) * n + J * kTile + row] = q2[i][a];
@@ -296,6 +421,7 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
                 atomicMax(rowmax + (int64_t)a * rm_stride + I * kTile + r, (unsigned long long)__double_as_longlong(mx));
         }
         consumer_sync(g);
+        }  // SD == 0
     }
 }
 
@@ -305,37 +431,51 @@ psynth_pairs_kernel(const unsigned char* __restrict__ packed, const double* __re
 cudaError_t launch_psynth(const void* packed, const double* scales, int n, int l, int l_cache, const double* coef_dev,
                           int coef_ld, int n_alpha, double* out, int64_t out_stride, unsigned long long* rowmax,
                           int64_t rm_stride, cudaStream_t stream, int p0, int p1, int max_ctas, int pbase,
-                          int nodiag) {
+                          int nodiag, int8_t* digits, const int* exps, int rp, int kp, int sd) {
     const int nt = (int)ceil_div(n, kTile);
     if (p1 < 0) p1 = nt * (nt + 1) / 2;
     const int npairs = p1 - p0;
     if (npairs <= 0) return cudaSuccess;
+    // digit emission: one order's [Q; dQ] (AC = 2), whole 128-row tiles, 5 / 6 digits
+    if (digits && (n_alpha != 2 || n % 128 || rp % 128 || kp % 64 || (sd != 5 && sd != 6) || !exps))
+        return cudaErrorInvalidValue;
+    PsDigits pd;
+    if (digits) {
+        pd.dig = digits;
+        pd.exps = exps;
+        pd.rp = rp;
+        pd.kbc = kp / 64;
+    }
     const int stages = psynth_stages(l_cache, n_alpha);
     const size_t smem = psynth_smem_bytes(l_cache, n_alpha, stages);
     const int groups = psynth_groups(n_alpha);
     int grid = FGFRFT_SMS;  // one CTA (groups x 288 threads) per SM
     if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
     if (grid * groups > npairs) grid = (npairs + groups - 1) / groups;
-#define FGB_PS(ACV)                                                                                          \
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+#define FGB_PS(ACV, SDV)                                                                                     \
     {                                                                                                        \
         constexpr int GV = ACV == 4 ? 1 : 2;                                                                 \
         static PerDeviceOnce attr;                                                                           \
         cudaError_t e = attr.run([] {                                                                        \
-            cudaError_t r = cudaFuncSetAttribute(psynth_pairs_kernel<ACV, GV, kPsStages>,                    \
+            cudaError_t r = cudaFuncSetAttribute(psynth_pairs_kernel<ACV, GV, kPsStages, SDV>,               \
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);   \
             if (r != cudaSuccess) return r;                                                                  \
-            return cudaFuncSetAttribute(psynth_pairs_kernel<ACV, GV, 8>,                                     \
+            return cudaFuncSetAttribute(psynth_pairs_kernel<ACV, GV, 8, SDV>,                                \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);            \
         });                                                                                                  \
         if (e != cudaSuccess) return e;                                                                      \
-        if (smem > 227 * 1024) return cudaErrorInvalidValue;                                                 \
-        auto kern = stages == kPsStages ? psynth_pairs_kernel<ACV, GV, kPsStages> : psynth_pairs_kernel<ACV, GV, 8>; \
+        auto kern = stages == kPsStages ? psynth_pairs_kernel<ACV, GV, kPsStages, SDV>                       \
+                                        : psynth_pairs_kernel<ACV, GV, 8, SDV>;                              \
         kern<<<grid, GV * (kPsConsumers + 32), smem, stream>>>((const unsigned char*)packed,                 \
                                                               scales, n, l, l_cache,                         \
                                                               coef_dev, coef_ld, out, out_stride, rowmax,    \
-                                                              rm_stride, nt, p0, p1, pbase, nodiag);         \
+                                                              rm_stride, nt, p0, p1, pbase, nodiag, pd);     \
     }
-    if (n_alpha == 1) FGB_PS(1) else if (n_alpha == 2) FGB_PS(2) else if (n_alpha == 4) FGB_PS(4) else return cudaErrorInvalidValue;
+    if (digits) {
+        if (sd == 6) FGB_PS(2, 6) else FGB_PS(2, 5)
+    } else if (n_alpha == 1) FGB_PS(1, 0) else if (n_alpha == 2) FGB_PS(2, 0) else if (n_alpha == 4) FGB_PS(4, 0)
+    else return cudaErrorInvalidValue;
 #undef FGB_PS
     return cudaGetLastError();
 }

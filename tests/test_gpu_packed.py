@@ -185,3 +185,34 @@ def test_tensor_core_synthesis_matches_packed_synthesis():
             os.environ.pop("FGFRFT_DSYNTH", None)
         else:
             os.environ["FGFRFT_DSYNTH"] = old
+
+
+@pytest.mark.parametrize("alpha", [0.37, -1.3, 1.0])
+def test_digit_emission_matches_the_slicing_pass(problem, alpha):
+    """One order on whole 128-row tiles: psynth writes [Q; dQ]'s Ozaki digits itself, scaled per row
+    by the exponents prow_bound_kernel derives from the powers' row / column maxima (packed.cu), in
+    place of FP64 Q + row maxima + the slicing pass (FGFRFT_PSYNTH_DIGITS=0). The bound is looser
+    than the exact row maximum by a few bits, so the two differ in the last digits only; both hold
+    the oracle's 1e-10 bar."""
+    f, l, x, xc, g, o, route = problem
+    if route != 3:
+        pytest.skip("digit emission is the packed FP64-decode synthesis' (route 3)")
+    old = os.environ.get("FGFRFT_PSYNTH_DIGITS")
+    try:
+        os.environ["FGFRFT_PSYNTH_DIGITS"] = "0"
+        l0, d0, y0 = fg.mse_step(g, [alpha], x, xc, want_y=True)
+        os.environ["FGFRFT_PSYNTH_DIGITS"] = "1"
+        l1, d1, y1 = fg.mse_step(g, [alpha], x, xc, want_y=True)
+    finally:
+        if old is None:
+            os.environ.pop("FGFRFT_PSYNTH_DIGITS", None)
+        else:
+            os.environ["FGFRFT_PSYNTH_DIGITS"] = old
+    assert g.route_info()[0] == 3
+    assert rel(y1[0], y0[0]) <= 1e-11
+    lr, dr, yr = O.dlda_mse(o, alpha, x, xc)
+    assert rel(y1[0], yr) <= 1e-10
+    assert abs(l1[0] - lr) <= 1e-10 * lr
+    s = O.power_dots(o, 2.0 * (yr - xc) @ x.conj().T / x.size)
+    _, dc = O.sinc_coeffs(alpha, l)
+    assert abs(d1[0] - dr) <= 1e-10 * max(np.sum(np.abs(dc * s)), 1e-300)
