@@ -134,7 +134,8 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
-def ncu_summary(name_regex: str, files=("r02b_ncu_c3_summary.csv", "r02_ncu_c3_summary.csv", "r02_ncu_c3_gemm_summary.csv")):
+def ncu_summary(name_regex: str, files=("r02c_ncu_c3_summary.csv", "r02b_ncu_c3_summary.csv", "r02_ncu_c3_summary.csv",
+                                         "r02_ncu_c3_gemm_summary.csv")):
     """The committed ncu --set full summary row (profiles/<file>) of the kernel whose name matches
     `name_regex`: {"traffic": dram read + write bytes per launch, "duration_us", "file"} or None."""
     rx = re.compile(name_regex)
@@ -529,7 +530,11 @@ def main():
     # SURVEY 8(d) K2 algorithmic bytes: (S*e + A*16)*N^2 -- S = L stored slabs of e bytes per element,
     # A = 2 outputs (Q, dQ/da) counted at 16 B (the VERDICT r01 formula)
     fp64_bytes = (L * e + 2 * 16) * n * n
-    syn_bytes = {3: packed_bytes + 2 * 8 * n * n, 4: digit_bytes + 2 * 8 * n * n}.get(route, fp64_bytes)
+    # route 3 on whole 128-row tiles (one order): psynth writes [Q; dQ]'s S Ozaki digits directly
+    # (packed.cu SD > 0) instead of FP64 Q, dQ
+    emit = route == 3 and n % 128 == 0 and os.environ.get("FGFRFT_PSYNTH_DIGITS", "1") != "0"
+    out_bytes = 2 * S * n * n if emit else 2 * 8 * n * n
+    syn_bytes = {3: packed_bytes + out_bytes, 4: digit_bytes + 2 * 8 * n * n}.get(route, fp64_bytes)
     dom = max(classes, key=lambda k: classes[k]["ms_per_step"])
     syn = classes.get("synthesis")
     roof = None
@@ -537,9 +542,12 @@ def main():
         per_launch_ms = syn["ms_per_step"] / syn["launches_per_step"]
         ach = syn_bytes / syn["launches_per_step"] / (per_launch_ms * 1e-3) / 1e9
         fp64_ach = fp64_bytes / syn["launches_per_step"] / (per_launch_ms * 1e-3) / 1e9
-        nc = ncu_summary({3: r"psynth", 4: r"dsynth_kernel"}.get(route, r"rsynth_pairs"))
+        nc = ncu_summary({3: (rf"psynth_pairs_kernel<2, 2, 10, {S}>" if emit else r"psynth_pairs_kernel<2, 2, 10(, 0)?>"),
+                          4: r"dsynth_kernel"}.get(route, r"rsynth_pairs"))
         roof = {"bound": "hbm",
-                "kernel": {3: "psynth_pairs_kernel<2> (packed slabs -> Q and dQ/da, one pass, TMA ring)",
+                "kernel": {3: (f"psynth_pairs_kernel<2,2,10,{S}> (packed slabs -> the {S} Ozaki digits of Q and dQ/da, "
+                               f"one pass, TMA ring)" if emit else
+                               "psynth_pairs_kernel<2> (packed slabs -> Q and dQ/da, one pass, TMA ring)"),
                            4: ("dsynth_kernel<2,4> (digit cache -> Q and dQ/da on the INT8 tensor cores: TMA ring, "
                                "2 MMA-issuing warps, TMEM accumulators, mirror pairs per row)")}.get(
                                route, "rsynth_pairs_kernel (FP64 slabs -> Q and dQ/da)"),
@@ -555,7 +563,9 @@ def main():
                 "physical_bytes_per_launch": syn_bytes / syn["launches_per_step"],
                 "physical_gbs": ach, "physical_frac": ach / peaks["hbm_gbs"],
                 "physical": {3: (f"packed slabs {packed_bytes:.4g} B (npairs*L*2 tiles*5 KB + scales; 5 B per "
-                                    f"element, diagonal tiles twice) read + Q, dQ 2*N^2*8 B written = {syn_bytes:.4g} B"),
+                                    f"element, diagonal tiles twice) read + " +
+                                    (f"the {S} digits of Q, dQ 2*{S}*N^2 B written" if emit else
+                                     "Q, dQ 2*N^2*8 B written") + f" = {syn_bytes:.4g} B"),
                                 4: (f"digit cache {digit_bytes:.4g} B (npairs*1024 element-pair rows x {dk_kp} powers "
                                     f"(P_k(e) | P_k(e')) x 5 digits + 4 B exponent per row; 5 B per element and "
                                     f"power, diagonal tiles twice) read + Q, dQ 2*N^2*8 B written = {syn_bytes:.4g} B")
