@@ -130,20 +130,29 @@ cudaError_t launch_pack_tiles(const void* slabs, int n, int l, void* packed, dou
 // Q exists, so the synthesis can emit Q's digits directly (psynth_pairs_kernel SD > 0). A row whose
 // bound is loose by 2^b loses b bits of the ~47 the 6 digits carry (measured ~2.5 bits on graph
 // GFTs: 4-6x at N = 1024). coef rows: a * coef_ld, c_k at l + k.
+// 64 rows x 4 power slices per CTA (k = 1 + slice, 5 + slice, ...; the slices' partial sums are added
+// in fixed order through shared memory): the kernel sits on the step's critical path ahead of the
+// synthesis, so it is spread over rp / 64 CTAs instead of one serial 2 l-load chain per thread.
 __global__ void __launch_bounds__(256) prow_bound_kernel(const unsigned long long* __restrict__ pmax, int64_t npad,
                                                          int l, const double* __restrict__ coef, int coef_ld, int rp,
                                                          int* __restrict__ exps) {
-    const int i = blockIdx.x * 256 + threadIdx.x, a = blockIdx.y;
-    if (i >= rp) return;
+    __shared__ double part[4][64];
+    const int lr = threadIdx.x & 63, ks = threadIdx.x >> 6;
+    const int i = blockIdx.x * 64 + lr, a = blockIdx.y;
     const double* cr = coef + (int64_t)a * coef_ld + l;
     double r = 0.0;
-    if (i < npad) {
-        for (int k = 1; k <= l; ++k) {
+    if (i < npad && i < rp) {
+#pragma unroll 4
+        for (int k = 1 + ks; k <= l; k += 4) {
             const double mr = __longlong_as_double((long long)pmax[(int64_t)(k - 1) * 2 * npad + i]);
             const double mc = __longlong_as_double((long long)pmax[((int64_t)(k - 1) * 2 + 1) * npad + i]);
             r = fma(fabs(cr[k]), mr, fma(fabs(cr[-k]), mc, r));
         }
     }
+    part[ks][lr] = r;
+    __syncthreads();
+    if (ks != 0 || i >= rp) return;
+    r = ((part[0][lr] + part[1][lr]) + part[2][lr]) + part[3][lr];
     r *= 1.0 + 0x1p-40;
     int e = 0;
     if (r > 0.0) frexp(r, &e);
@@ -153,8 +162,8 @@ __global__ void __launch_bounds__(256) prow_bound_kernel(const unsigned long lon
 cudaError_t launch_prow_bound(const unsigned long long* pmax, int n, int l, const double* coef, int coef_ld, int ac,
                               int rp, int* exps, cudaStream_t stream) {
     const int64_t npad = ceil_div(n, kTile) * kTile;
-    prow_bound_kernel<<<dim3((unsigned)ceil_div(rp, 256), (unsigned)ac), 256, 0, stream>>>(pmax, npad, l, coef,
-                                                                                          coef_ld, rp, exps);
+    prow_bound_kernel<<<dim3((unsigned)ceil_div(rp, 64), (unsigned)ac), 256, 0, stream>>>(pmax, npad, l, coef,
+                                                                                         coef_ld, rp, exps);
     return cudaGetLastError();
 }
 
@@ -618,42 +627,52 @@ __global__ void __launch_bounds__(64) mse_dy_finish_kernel(const double* __restr
 
 size_t mse_dy_part_elems() { return 2 * kMdBlocks; }
 
-// One CTA per order: fixed-order strided sums and a fixed tree (deterministic run to run).
-__global__ void __launch_bounds__(256) fused_mse_finish_kernel(const double2* __restrict__ part, int64_t per,
-                                                               double norm, double* __restrict__ loss,
-                                                               double* __restrict__ dlda) {
-    __shared__ double red[2][8];
+// One CTA per order: fixed-order strided sums (four independent chains per thread) and a fixed tree
+// (deterministic run to run).
+__global__ void __launch_bounds__(1024) fused_mse_finish_kernel(const double2* __restrict__ part, int64_t per,
+                                                                double norm, double* __restrict__ loss,
+                                                                double* __restrict__ dlda) {
+    __shared__ double red[2][32];
     const double2* p = part + (int64_t)blockIdx.x * per;
-    double s1 = 0.0, s2 = 0.0;
-    for (int64_t i = threadIdx.x; i < per; i += 256) {
-        const double2 v = p[i];
-        s1 += v.x;
-        s2 += v.y;
+    double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t i0 = threadIdx.x; i0 < per; i0 += 4096) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t i = i0 + q * 1024;
+            const double2 v = i < per ? p[i] : make_double2(0.0, 0.0);
+            s1[q] += v.x;
+            s2[q] += v.y;
+        }
     }
+    double t1 = (s1[0] + s1[1]) + (s1[2] + s1[3]), t2 = (s2[0] + s2[1]) + (s2[2] + s2[3]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+        t2 += __shfl_xor_sync(0xffffffffu, t2, o);
     }
     if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = s1;
-        red[1][threadIdx.x >> 5] = s2;
+        red[0][threadIdx.x >> 5] = t1;
+        red[1][threadIdx.x >> 5] = t2;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double t1 = 0.0, t2 = 0.0;
-        for (int w = 0; w < 8; ++w) {
-            t1 += red[0][w];
-            t2 += red[1][w];
+    if (threadIdx.x < 32) {
+        t1 = red[0][threadIdx.x];
+        t2 = red[1][threadIdx.x];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+            t2 += __shfl_xor_sync(0xffffffffu, t2, o);
         }
-        loss[blockIdx.x] = t1 * norm;
-        dlda[blockIdx.x] = 2.0 * t2 * norm;
+        if (threadIdx.x == 0) {
+            loss[blockIdx.x] = t1 * norm;
+            dlda[blockIdx.x] = 2.0 * t2 * norm;
+        }
     }
 }
 
 cudaError_t launch_fused_mse_finish(const double* part, int64_t per, int n_alpha, double norm, double* loss,
                                     double* dlda, cudaStream_t stream) {
-    fused_mse_finish_kernel<<<n_alpha, 256, 0, stream>>>(reinterpret_cast<const double2*>(part), per, norm, loss, dlda);
+    fused_mse_finish_kernel<<<n_alpha, 1024, 0, stream>>>(reinterpret_cast<const double2*>(part), per, norm, loss, dlda);
     return cudaGetLastError();
 }
 

@@ -86,7 +86,10 @@ def test_window_host_and_device_steps_agree(problem):
                                            None, lo.data_ptr(), dl.data_ptr()))
     torch.cuda.synchronize()
     assert g.route_info()[0] == 5
-    assert float(lo[0]) == loss_h[0] and float(dl[0]) == dl_h[0]
+    # same products; the host form's separate loss pass and the fused epilogue sum in different
+    # (each deterministic) orders
+    assert abs(float(lo[0]) - loss_h[0]) <= 1e-14 * abs(loss_h[0])
+    assert abs(float(dl[0]) - dl_h[0]) <= 1e-12 * abs(dl_h[0])
 
 
 def test_window_budget_and_validation():
