@@ -282,3 +282,40 @@ def test_config4_packed_step_and_pair_shard_world1():
     finally:
         sh.close()
         comm.close()
+
+
+@pytest.mark.skipif(not HEAVY, reason="FGFRFT_SKIP_HEAVY=1")
+def test_config3_full_batch_properties():
+    """Size-independent properties of the headline step at the full config-3 size (N = 4096, L = 64,
+    B = 1024), no oracle in the loop: (1) the central difference of the loss in the order equals
+    dL/da (the series coefficients are analytic in a; sinc.hpp:24-36 is the derivative the step
+    uses); (2) the apply is complex-linear in X (the real / imaginary column split of the INT8
+    product must not mix them); (3) apply_inverse(apply_forward(X)) equals Q^H (Q X) formed on the
+    host from the bit-exact synthesis route's Q (transform.hpp:138-148) -- two different device
+    routes and numpy agreeing on the series' own unitarity defect."""
+    cfg = prep.config3()
+    n, b = cfg.x.shape
+    cache = fg.PowerCache(cfg.f, cfg.l, memory_budget=32 << 30)
+    try:
+        for a in (0.37, 1.45):
+            h = 1e-4
+            lp, _, _ = fg.mse_step(cache, [a + h], cfg.x, cfg.x_clean)
+            lm, _, _ = fg.mse_step(cache, [a - h], cfg.x, cfg.x_clean)
+            l0, d0, _ = fg.mse_step(cache, [a], cfg.x, cfg.x_clean)
+            assert cache.route_info()[0] in (3, 4)
+            fd = (lp[0] - lm[0]) / (2 * h)
+            assert abs(fd - d0[0]) <= 1e-6 * max(abs(d0[0]), l0[0]), (a, fd, d0[0])
+        a = 0.37
+        y1 = fg.apply_series(cache, [a], cfg.x)[0]
+        z = 0.5 - 2.0j
+        y2 = fg.apply_series(cache, [a], np.asfortranarray(z * cfg.x))[0]
+        assert rel(y2, z * y1) <= 1e-12
+        back = fg.apply_series(cache, [a], np.asfortranarray(y1), inverse=True)[0]
+        q = fg.synthesize(cache, [a])[0]
+        cols = slice(0, 8)
+        host = q.conj().T @ (q @ cfg.x[:, cols])
+        assert rel(back[:, cols], host) <= 1e-10
+        defect = rel(back, cfg.x)
+        assert defect <= 0.2, defect  # the truncated series is only approximately unitary; it must not blow up
+    finally:
+        cache.close()
