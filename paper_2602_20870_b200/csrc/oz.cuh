@@ -98,6 +98,10 @@ struct OzOut {
     // (pair_n x pair_n); dg[x] added on the diagonal; rmax[x * rnp + row] = the row maxima (zeroed
     // by the caller). Each CTA takes the 8 M tiles of a tile pair in a row.
     int pair_nt = 0, pair_n = 0;
+    // CM 1: N-band raster (set by the launcher). The unit order walks all M tiles over band 0's N
+    // groups, then band 1's, ...: a B operand larger than L2 (config 4: 151 MB of X digits) stays
+    // resident one band at a time instead of being re-streamed from HBM by every wave of M tiles.
+    int nband = 1;
     // CM 1 fused MSE + dL/da (the packed step, DESIGN 3.7): A = [Q_a blocks; dQ_a blocks] (2 n_alpha
     // blocks of mp rows, an even number of M tiles); each CTA takes M tile mt and then mt + mtiles / 2
     // (the dQ rows of the same Q rows) with the same N tile, so the thread that stored Y[i, j] meets

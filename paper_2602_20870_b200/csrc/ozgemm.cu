@@ -471,8 +471,17 @@ ozgemm_kernel(const int8_t* __restrict__ a, const int* __restrict__ ea, const in
         if (fmse) return (u & 1) ? u - 1 + 2 * us : u + 1;
         return pairs ? ((u % upp) == upp - 1 ? u + upp * us - (upp - 1) : u + 1) : u + us;
     };
-    auto unit_mt = [&](int u) { return fmse ? (u >> 1) / ngroups + (u & 1) * mhalf : u / ngroups; };
-    auto unit_nt = [&](int u) { return ((fmse ? (u >> 1) : u) % ngroups) * CL + rank; };
+    // N bands (CM 1, out.nband > 1): unit q -> band q / (M tiles x gw), then M-major inside the band
+    const int gw = (CM == 1 && out.nband > 1) ? ngroups / out.nband : ngroups;
+    const int bandu = (fmse ? mhalf : mtiles) * gw;
+    auto unit_mt = [&](int u) {
+        const int q = fmse ? (u >> 1) : u;
+        return (q % bandu) / gw + ((fmse && (u & 1)) ? mhalf : 0);
+    };
+    auto unit_nt = [&](int u) {
+        const int q = fmse ? (u >> 1) : u;
+        return ((q / bandu) * gw + q % gw) * CL + rank;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1297,6 +1306,19 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
         }))
         return e;
     const int units = mtiles * (ntiles / CL);
+    OzOut o2 = out;
+    if (CM == 1 && BN == kOzBN) {
+        // B bands: keep the B operand's band (evict_last) L2-resident beside the streaming A tiles
+        static const int forced_bands = [] {
+            const char* e = std::getenv("FGFRFT_OZ_BANDS");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int ngroups = ntiles / CL;
+        const double bbytes = (double)ntiles * BN * kp * S, cap = 56e6;
+        int nb = forced_bands > 0 ? forced_bands : (bbytes > cap ? (int)((bbytes + cap - 1) / cap) : 1);
+        while (nb < ngroups && ngroups % nb) ++nb;
+        o2.nband = (nb >= 1 && nb <= ngroups && ngroups % nb == 0) ? nb : 1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kOzThreads);
     cfg.dynamicSmemBytes = (OzCfg<S, BN, P>::smem);
@@ -1330,7 +1352,7 @@ static cudaError_t oz_launch_cl(const int8_t* a, const int* ea, int mtiles, cons
         if (clusters >= ibs) clusters = clusters / ibs * ibs;
     }
     cfg.gridDim = dim3(clusters * CL);
-    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL, BN, P>, a, ea, b, eb, kp / OzCfg<S, BN, P>::bk, mtiles, ntiles, out);
+    return cudaLaunchKernelEx(&cfg, ozgemm_kernel<S, CM, CL, BN, P>, a, ea, b, eb, kp / OzCfg<S, BN, P>::bk, mtiles, ntiles, o2);
 }
 
 template <int S, int CM>
