@@ -479,7 +479,8 @@ int download_signal(fgfrft_cache* c, const void* src, size_t elems, double* host
 // INT8 tensor-core (Ozaki) versions of the real-F synthesis route's two GEMMs (defined below).
 bool use_int8_gemm(const fgfrft_cache* c, int64_t b);
 bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b);
-int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out);
+int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out, cudaStream_t st = nullptr);
+int ensure_pipe_streams(fgfrft_cache* c);
 int int8_gx(fgfrft_cache* c, int na, const void* g, const void* x_dev, int64_t b, void* m);
 int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
                 int64_t sm);
@@ -910,6 +911,22 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
         return node_products_pairs(c, tab, d0, r, x_dev, b, upload);
     }
     const int64_t n = c->n, rows = pad_rows(n * n), kp = pad_k(2 * (int64_t)c->l), bp = kOzTileB;
+    // X's digits (the product GEMM's B operand) on the side stream, beside the node-operator GEMM
+    // (ordered after everything already on c->stream: the previous call's product GEMM read them)
+    static const bool x_side = [] {
+        const char* e = std::getenv("FGFRFT_NODE_XSIDE");
+        return !e || std::atoi(e) != 0;
+    }();
+    int64_t xbp = 0;
+    cudaEvent_t xev = nullptr;
+    if (x_side) {
+        if (int st = ensure_pipe_streams(c)) return st;
+        FGB_CUDA(cudaEventRecord(c->pk_e0, c->stream));
+        FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_e0, 0));
+        if (int st = slice_signal_rows(c, x_dev, b, &xbp, c->pk_g)) return st;
+        FGB_CUDA(cudaEventRecord(c->pk_ex, c->pk_g));
+        xev = c->pk_ex;
+    }
     if (upload) {
         FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
         FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
@@ -977,7 +994,7 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
     }
     if (!fused)
         FGB_LAUNCH(launch_add_diag(c->nd_w.as<double>(), (int)n, (int64_t)nn, c->nd_d0.as<double>(), r, c->stream), 1);
-    return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, fused);
+    return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, fused, xev, xbp);
 }
 
 // Copy the plan's tables into the next pinned staging slot (after the uploads of the call that
@@ -1302,7 +1319,8 @@ bool use_fused_apply(const fgfrft_cache* c, int n_alpha, int64_t b) {
 }
 
 // Slice the signal block X (n x b complex) as the B operand: rows 2j + comp, K = signal index.
-int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out) {
+int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp_out, cudaStream_t st) {
+    if (!st) st = c->stream;
     const int S = oz_slices_default();
     const int64_t n = c->n, kp = pad_k(n), bp = ceil_div(2 * b, kOzTileB) * kOzTileB;
     FGB_CUDA(c->xsl.ensure((size_t)S * bp * kp));
@@ -1310,9 +1328,9 @@ int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp
     int* xe = c->xex.as<int>();
     const OzView v{static_cast<const double*>(x_dev), 2 * n, 2, 0, 1, 0, (int)(2 * b), (int)bp, 1, (int)n, (int)kp,
                    false};
-    ProfScope ps(KC_SLICE, c->stream);
+    ProfScope ps(KC_SLICE, st);
     FGB_LAUNCH(launch_oz_slice(v, S, kOzTileB, c->xsl.as<int8_t>(), xe,
-                               reinterpret_cast<unsigned long long*>(xe + bp), c->stream),
+                               reinterpret_cast<unsigned long long*>(xe + bp), st),
                3);
     *bp_out = bp;
     return FGFRFT_OK;
@@ -1322,7 +1340,7 @@ int slice_signal_rows(fgfrft_cache* c, const void* x_dev, int64_t b, int64_t* bp
 // doubles), complex X (n x b); Y_a complex m x b (leading dimension ldy, stride sy doubles).
 int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
                 const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers, int npeers,
-                bool rowmax_ready) {
+                bool rowmax_ready, cudaEvent_t x_sliced, int64_t x_bp) {
     const int S = oz_slices_default();
     const int64_t n = c->n, mp = pad_rows(m), kp = pad_k(n), rows = (int64_t)na * mp;
     FGB_CUDA(c->qsl.ensure((size_t)S * rows * kp));
@@ -1342,8 +1360,12 @@ int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m,
                                        reinterpret_cast<unsigned long long*>(qe + rows), c->stream),
                        3);
     }
-    int64_t bp = 0;
-    if (int st = slice_signal_rows(c, x_dev, b, &bp)) return st;
+    int64_t bp = x_bp;
+    if (x_sliced) {  // the caller sliced X on a side stream (node route: beside the node-operator GEMM)
+        FGB_CUDA(cudaStreamWaitEvent(c->stream, x_sliced, 0));
+    } else if (int st = slice_signal_rows(c, x_dev, b, &bp)) {
+        return st;
+    }
     ProfScope ps(KC_I8GEMM, c->stream);
     FGB_LAUNCH(launch_ozgemm(S, 1, c->qsl.as<int8_t>(), qe, (int)rows, c->xsl.as<int8_t>(), c->xex.as<int>(), (int)bp,
                              (int)kp, static_cast<double*>(y), ldy, sy, (int)m, (int)mp, (int)(2 * b), c->stream, peers,
@@ -1353,9 +1375,9 @@ int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m,
 }
 
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y,
-            bool rowmax_ready) {
+            bool rowmax_ready, cudaEvent_t x_sliced, int64_t x_bp) {
     return int8_qx_gen(c, na, inverse, q, c->n, c->n, c->n * c->n, x_dev, b, y, c->n, 2 * c->n * b, nullptr, 0,
-                       rowmax_ready);
+                       rowmax_ready, x_sliced, x_bp);
 }
 
 // M_a = Re(G_a X^H) (real m x n, column-major ld m, stride sm) for na blocks G_a (m x b complex,

@@ -511,13 +511,13 @@ int upload_coefs(fgfrft_cache* c, const double* alphas, int n_alpha, int l, doub
 bool use_int8_gemm(const fgfrft_cache* c, int64_t b);
 int int8_qx_gen(fgfrft_cache* c, int na, bool inverse, const void* q, int64_t m, int64_t ldq, int64_t sq,
                 const void* x_dev, int64_t b, void* y, int64_t ldy, int64_t sy, double* const* peers = nullptr,
-                int npeers = 0, bool rowmax_ready = false);
+                int npeers = 0, bool rowmax_ready = false, cudaEvent_t x_sliced = nullptr, int64_t x_bp = 0);
 int int8_gx_gen(fgfrft_cache* c, int na, const void* g, int64_t m, const void* x_dev, int64_t b, void* out,
                 int64_t sm);
 int check_batch(const fgfrft_cache* c);
 int synth_into(fgfrft_cache* c, const double* coef_dev, int n_alpha, int l_used, void* out, bool internal = false);
 int int8_qx(fgfrft_cache* c, int na, bool inverse, const void* q, const void* x_dev, int64_t b, void* y,
-            bool rowmax_ready = false);
+            bool rowmax_ready = false, cudaEvent_t x_sliced = nullptr, int64_t x_bp = 0);
 int create_common(const double* f, int64_t n, int l, uint64_t budget, int dtype, int device, fgfrft_cache** out,
                   fgfrft_cache** made);
 int check_orthogonal(fgfrft_cache* c, const double* fr, double* scratch);

@@ -36,9 +36,15 @@ def timed(stream, fn, reps=10, warm=3):
         for i in range(reps):
             fn(i)
     torch.cuda.synchronize()
+    tr = fg.profile_trace() if os.environ.get("PROBE_TRACE") else []
     prof = {k: round(v[0] / reps, 4) for k, v in fg.profile_read(reset=True).items() if v[1]}
     fg.profile_enable(False)
-    return {"dev_ms": dev, "wall_ms": wall, "classes": prof}
+    out = {"dev_ms": dev, "wall_ms": wall, "classes": prof}
+    if tr:  # the last step's launches: (class, start, end) in ms from the step's first launch
+        per = len(tr) // reps
+        t0 = tr[-per][1]
+        out["trace"] = [(c, round(a - t0, 4), round(b - t0, 4)) for c, a, b in tr[-per:]]
+    return out
 
 
 def main():
