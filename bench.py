@@ -135,7 +135,7 @@ def cpu_model():
     return platform.processor() or "unknown"
 
 
-def ncu_summary(name_regex: str, files=("r02d_ncu_c3_summary.csv", "r02c_ncu_c3_summary.csv", "r02b_ncu_c3_summary.csv", "r02_ncu_c3_summary.csv",
+def ncu_summary(name_regex: str, files=("r02e_ncu_c3_summary.csv", "r02d_ncu_c3_summary.csv", "r02c_ncu_c3_summary.csv", "r02b_ncu_c3_summary.csv", "r02_ncu_c3_summary.csv",
                                          "r02_ncu_c3_gemm_summary.csv")):
     """The committed ncu --set full summary row (profiles/<file>) of the kernel whose name matches
     `name_regex`: {"traffic": dram read + write bytes per launch, "duration_us", "file"} or None."""

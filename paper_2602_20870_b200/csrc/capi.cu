@@ -269,7 +269,7 @@ void destroy_cache(fgfrft_cache* c) {
     for (cudaEvent_t e : c->pk_es) cudaEventDestroy(e);
     for (cudaEvent_t e : c->xh_ev) cudaEventDestroy(e);
     for (void* p : c->rb_open) cudaIpcCloseMemHandle(p);
-    for (cudaEvent_t e : {c->pk_e0, c->pk_eg, c->pk_ex})
+    for (cudaEvent_t e : {c->pk_e0, c->pk_eg, c->pk_ex, c->nd_ev_op, c->nd_ev_b})
         if (e) cudaEventDestroy(e);
     if (c->pk_s) cudaStreamSynchronize(c->pk_s);
     if (c->pk_g) cudaStreamSynchronize(c->pk_g);
@@ -927,11 +927,16 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
         FGB_CUDA(cudaEventRecord(c->pk_ex, c->pk_g));
         xev = c->pk_ex;
     }
+    // The node tables come from the host plan, not from the stream's earlier work: their upload and
+    // slicing run on the second side stream, ordered only after the previous call's node-operator
+    // GEMM (the reader of these buffers), so in back-to-back steps they overlap the previous step's tail.
+    cudaStream_t ts = x_side ? c->pk_s : c->stream;
+    if (x_side && c->nd_ev_op) FGB_CUDA(cudaStreamWaitEvent(ts, c->nd_ev_op, 0));
+    FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
+    FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
     if (upload) {
-        FGB_CUDA(c->nd_tab.ensure(tab.size() * 8));
-        FGB_CUDA(c->nd_d0.ensure(d0.size() * 8));
-        FGB_CUDA(cudaMemcpyAsync(c->nd_tab.p, c->nd_h, tab.size() * 8, cudaMemcpyHostToDevice, c->stream));
-        FGB_CUDA(cudaMemcpyAsync(c->nd_d0.p, c->nd_h + tab.size(), d0.size() * 8, cudaMemcpyHostToDevice, c->stream));
+        FGB_CUDA(cudaMemcpyAsync(c->nd_tab.p, c->nd_h, tab.size() * 8, cudaMemcpyHostToDevice, ts));
+        FGB_CUDA(cudaMemcpyAsync(c->nd_d0.p, c->nd_h + tab.size(), d0.size() * 8, cudaMemcpyHostToDevice, ts));
     }
     FGB_CUDA(c->nd_bsl.ensure((size_t)S * bp * kp));
     FGB_CUDA(c->nd_bex.ensure((size_t)bp * (sizeof(int) + sizeof(unsigned long long))));
@@ -942,10 +947,15 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
         OzView v{c->nd_tab.as<double>(), T, 0, 0, 0, 0, r, (int)bp, 1, 2 * c->l, (int)kp, false};
         v.tiled = 4;
         v.l = c->l;
-        ProfScope ps(KC_SLICE, c->stream);
+        ProfScope ps(KC_SLICE, ts);
         FGB_LAUNCH(launch_oz_slice(v, S, narrow ? kOzTileNarrow : kOzTileB, c->nd_bsl.as<int8_t>(), be,
-                                   reinterpret_cast<unsigned long long*>(be + bp), c->stream),
+                                   reinterpret_cast<unsigned long long*>(be + bp), ts),
                    3);
+    }
+    if (x_side) {
+        if (!c->nd_ev_b) FGB_CUDA(cudaEventCreateWithFlags(&c->nd_ev_b, cudaEventDisableTiming));
+        FGB_CUDA(cudaEventRecord(c->nd_ev_b, ts));
+        FGB_CUDA(cudaStreamWaitEvent(c->stream, c->nd_ev_b, 0));
     }
     const size_t nn = (size_t)n * n;
     FGB_CUDA(c->nd_w.ensure((size_t)r * nn * 8));
@@ -994,6 +1004,10 @@ int node_products(fgfrft_cache* c, const std::vector<double>& tab, const std::ve
     }
     if (!fused)
         FGB_LAUNCH(launch_add_diag(c->nd_w.as<double>(), (int)n, (int64_t)nn, c->nd_d0.as<double>(), r, c->stream), 1);
+    if (x_side) {  // the coefficient digits and the diagonal have been read
+        if (!c->nd_ev_op) FGB_CUDA(cudaEventCreateWithFlags(&c->nd_ev_op, cudaEventDisableTiming));
+        FGB_CUDA(cudaEventRecord(c->nd_ev_op, c->stream));
+    }
     return int8_qx(c, r, false, c->nd_w.p, x_dev, b, c->nd_z.p, fused, xev, xbp);
 }
 

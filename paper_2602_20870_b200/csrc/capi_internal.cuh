@@ -440,6 +440,9 @@ struct fgfrft_cache {
     // priority), fork / join events, one event per shell, the memoised shell plan
     cudaStream_t pk_s = nullptr, pk_g = nullptr;
     cudaEvent_t pk_e0 = nullptr, pk_eg = nullptr, pk_ex = nullptr;
+    // node route: the last node-operator GEMM has read the coefficient digits / diagonal (the next
+    // call's tables may overwrite them on the side stream), and this call's digits are ready
+    cudaEvent_t nd_ev_op = nullptr, nd_ev_b = nullptr;
     std::vector<cudaEvent_t> pk_es;
     std::vector<cudaEvent_t> xh_ev;  // host-X column chunks landed (chunked host MSE step)
     std::vector<PkShell> pk_plan;
