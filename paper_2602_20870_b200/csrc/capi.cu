@@ -268,6 +268,7 @@ void destroy_cache(fgfrft_cache* c) {
     if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     for (cudaEvent_t e : c->pk_es) cudaEventDestroy(e);
     for (cudaEvent_t e : c->xh_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->xch_ev) cudaEventDestroy(e);
     for (void* p : c->rb_open) cudaIpcCloseMemHandle(p);
     for (cudaEvent_t e : {c->pk_e0, c->pk_eg, c->pk_ex, c->nd_ev_op, c->nd_ev_b})
         if (e) cudaEventDestroy(e);
@@ -2068,27 +2069,54 @@ int mse_packed_step(fgfrft_cache* c, const double* coef, int n_alpha, const void
     if (yd != c->ydy.p) {  // not fused after all (a multi-shell plan): Y and dY in the step buffer
         if (int st = packed_products(c, coef, 2 * c->l + 1, rows, x_dev, b, c->ydy.p, c->l, x_host, ww)) return st;
     }
-    if (xc_host) {  // Xc behind X on the aux stream: only the final loss pass needs it
-        if (!c->xc_evt) FGB_CUDA(cudaEventCreateWithFlags(&c->xc_evt, cudaEventDisableTiming));
-        // in 4 chunks, like X: one 67 MB pinned copy measured 46 GB/s on this pool against 55 GB/s chunked
-        // (tools/probes/h2d_probe.py)
-        const int64_t ce = ceil_div(b, (int64_t)4) * n;  // complex elements per chunk (whole columns)
-        for (int64_t e0 = 0; e0 < n * b; e0 += ce)
+    const double norm = 1.0 / ((double)n * (double)b);
+    if (xc_host) {
+        // Xc behind X on the aux stream, in 4 column chunks like X (one 67 MB pinned copy measured 46 GB/s
+        // on this pool against 55 GB/s chunked, tools/probes/h2d_probe.py); the loss pass runs per chunk
+        // as it lands, so only the last chunk's quarter is left once the host link goes quiet
+        constexpr int kXcChunks = 4;
+        if (c->xch_ev.size() < (size_t)kXcChunks) {
+            const size_t have = c->xch_ev.size();
+            c->xch_ev.resize(kXcChunks, nullptr);
+            for (size_t i = have; i < (size_t)kXcChunks; ++i)
+                FGB_CUDA(cudaEventCreateWithFlags(&c->xch_ev[i], cudaEventDisableTiming));
+        }
+        const int64_t ce = ceil_div(b, (int64_t)kXcChunks) * n;  // complex elements per chunk (whole columns)
+        int nq = 0;
+        for (int64_t e0 = 0; e0 < n * b; e0 += ce, ++nq) {
             FGB_CUDA(cudaMemcpyAsync(static_cast<double*>(const_cast<void*>(xc_dev)) + 2 * e0, xc_host + 2 * e0,
                                      (size_t)std::min(ce, n * b - e0) * 16, cudaMemcpyHostToDevice, c->aux_stream));
-        FGB_CUDA(cudaEventRecord(c->xc_evt, c->aux_stream));
-        c->xc_pending = true;
-    }
-    if (int st = wait_xc(c)) return st;
-    FGB_CUDA(c->lpart.ensure(mse_dy_part_elems() * sizeof(double)));
-    const double norm = 1.0 / ((double)n * (double)b);
-    ProfScope ps(KC_ELEMWISE, c->stream);
-    for (int a = 0; a < n_alpha; ++a) {
-        const double* ya = c->ydy.as<double>() + (size_t)a * blk;
-        FGB_LAUNCH(launch_mse_dy(ya, ya + (size_t)n_alpha * blk, xc_dev, n * b,
-                                 y_dev ? static_cast<double*>(y_dev) + (size_t)a * blk : nullptr, c->lpart.as<double>(),
-                                 norm, loss_dev + a, dlda_dev + a, c->stream),
-                   2);
+            FGB_CUDA(cudaEventRecord(c->xch_ev[nq], c->aux_stream));
+        }
+        FGB_CUDA(c->lpart.ensure((size_t)n_alpha * nq * mse_dy_part_elems() * sizeof(double)));
+        ProfScope ps(KC_ELEMWISE, c->stream);
+        int q = 0;
+        for (int64_t e0 = 0; e0 < n * b; e0 += ce, ++q) {
+            const int64_t cnt = std::min(ce, n * b - e0);
+            FGB_CUDA(cudaStreamWaitEvent(c->stream, c->xch_ev[q], 0));
+            for (int a = 0; a < n_alpha; ++a) {
+                const double* ya = c->ydy.as<double>() + (size_t)a * blk + 2 * e0;
+                FGB_LAUNCH(launch_mse_dy_part(ya, ya + (size_t)n_alpha * blk, static_cast<const double*>(xc_dev) + 2 * e0,
+                                              cnt, y_dev ? static_cast<double*>(y_dev) + (size_t)a * blk + 2 * e0 : nullptr,
+                                              c->lpart.as<double>(), a * nq + q, c->stream),
+                           1);
+            }
+        }
+        for (int a = 0; a < n_alpha; ++a)
+            FGB_LAUNCH(launch_mse_dy_finish_n(c->lpart.as<double>() + (size_t)a * nq * mse_dy_part_elems(), nq, norm,
+                                              loss_dev + a, dlda_dev + a, c->stream),
+                       1);
+    } else {
+        if (int st = wait_xc(c)) return st;
+        FGB_CUDA(c->lpart.ensure(mse_dy_part_elems() * sizeof(double)));
+        ProfScope ps(KC_ELEMWISE, c->stream);
+        for (int a = 0; a < n_alpha; ++a) {
+            const double* ya = c->ydy.as<double>() + (size_t)a * blk;
+            FGB_LAUNCH(launch_mse_dy(ya, ya + (size_t)n_alpha * blk, xc_dev, n * b,
+                                     y_dev ? static_cast<double*>(y_dev) + (size_t)a * blk : nullptr,
+                                     c->lpart.as<double>(), norm, loss_dev + a, dlda_dev + a, c->stream),
+                       2);
+        }
     }
     c->last_route = c->pk_win ? 5 : c->pk_tc ? 4 : 3;
     c->last_nodes = c->pk_win ? c->win_r : 0;

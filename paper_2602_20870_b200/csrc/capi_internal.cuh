@@ -197,6 +197,10 @@ cudaError_t launch_fused_mse_finish(const double* part, int64_t per, int n_alpha
                                     double* dlda, cudaStream_t stream);
 cudaError_t launch_mse_dy(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
                           double norm, double* loss, double* dlda, cudaStream_t stream);
+cudaError_t launch_mse_dy_part(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
+                               int slot, cudaStream_t stream);
+cudaError_t launch_mse_dy_finish_n(const double* part, int nslots, double norm, double* loss, double* dlda,
+                                   cudaStream_t stream);
 }  // namespace fgb
 
 using namespace fgb;
@@ -445,6 +449,7 @@ struct fgfrft_cache {
     cudaEvent_t nd_ev_op = nullptr, nd_ev_b = nullptr;
     std::vector<cudaEvent_t> pk_es;
     std::vector<cudaEvent_t> xh_ev;  // host-X column chunks landed (chunked host MSE step)
+    std::vector<cudaEvent_t> xch_ev; // host-Xc column chunks landed (the loss pass runs per chunk)
     std::vector<PkShell> pk_plan;
     uint64_t pk_plan_key = 0;
     // pinned staging for the coefficient tables: a ring of 3 (the host evaluates the next calls'

@@ -627,6 +627,39 @@ __global__ void __launch_bounds__(64) mse_dy_finish_kernel(const double* __restr
 
 size_t mse_dy_part_elems() { return 2 * kMdBlocks; }
 
+// Chunked form (host-buffer step: the loss of a column chunk as soon as its Xc has landed): the
+// partials of chunk `slot` go to part + slot * mse_dy_part_elems(); launch_mse_dy_finish_n sums
+// `nslots` of them in fixed order.
+__global__ void __launch_bounds__(64) mse_dy_finish_n_kernel(const double* __restrict__ part, int nslots, double norm,
+                                                             double* __restrict__ loss, double* __restrict__ dlda) {
+    __shared__ double red[2];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp 0: loss, warp 1: dot
+    double t = 0.0;
+    for (int s = 0; s < nslots; ++s)
+        for (int i = lane; i < kMdBlocks; i += 32) t += part[((int64_t)s * 2 + w) * kMdBlocks + i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[w] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *loss = red[0] * norm;
+        *dlda = 2.0 * red[1] * norm;
+    }
+}
+
+cudaError_t launch_mse_dy_part(const void* y, const void* dy, const void* xc, int64_t count, void* yout, double* part,
+                               int slot, cudaStream_t stream) {
+    mse_dy_kernel<<<kMdBlocks, 256, 0, stream>>>((const double2*)y, (const double2*)dy, (const double2*)xc, count,
+                                                 (double2*)yout, part + (size_t)slot * 2 * kMdBlocks);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mse_dy_finish_n(const double* part, int nslots, double norm, double* loss, double* dlda,
+                                   cudaStream_t stream) {
+    mse_dy_finish_n_kernel<<<1, 64, 0, stream>>>(part, nslots, norm, loss, dlda);
+    return cudaGetLastError();
+}
+
 // One CTA per order: fixed-order strided sums (four independent chains per thread) and a fixed tree
 // (deterministic run to run).
 __global__ void __launch_bounds__(1024) fused_mse_finish_kernel(const double2* __restrict__ part, int64_t per,
