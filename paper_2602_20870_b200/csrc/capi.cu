@@ -1827,6 +1827,40 @@ int64_t fused_mse_slots_per_order(int64_t n, int64_t b) {
     return (pad_rows(n) / kOzTileA) * (ceil_div(2 * b, kOzTileB) * kOzTileB / kOzTileB) * 16;
 }
 
+// Host X of the chunked step: column chunks of >= 32 signals, FGFRFT_E2E_CHUNKS (4) of them.
+static void host_x_chunks(int64_t b, int* nch, int64_t* cw) {
+    *nch = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)pk_env("FGFRFT_E2E_CHUNKS", 4), ceil_div(b, 32)));
+    *cw = ceil_div(ceil_div(b, *nch), 32) * 32;
+}
+
+// The chunk copies of host X into x_dev on the aux stream (after everything already on c->stream:
+// the previous call's readers), one event per chunk. fgfrft_mse_step calls it BEFORE its host-side
+// planning (the series coefficients are ~50 us of libm on this thread), so the link starts at once.
+int enqueue_host_x(fgfrft_cache* c, const double* x_host, const void* x_dev, int64_t b) {
+    const int64_t n = c->n;
+    int nch = 0;
+    int64_t cw = b;
+    host_x_chunks(b, &nch, &cw);
+    if (int st = ensure_pipe_streams(c)) return st;
+    if (!c->aux_stream) FGB_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    FGB_CUDA(cudaEventRecord(c->pk_e0, c->stream));
+    FGB_CUDA(cudaStreamWaitEvent(c->aux_stream, c->pk_e0, 0));  // the previous call's readers are done
+    if (c->xh_ev.size() < (size_t)nch) {
+        const size_t have = c->xh_ev.size();
+        c->xh_ev.resize(nch, nullptr);
+        for (size_t i = have; i < (size_t)nch; ++i)
+            FGB_CUDA(cudaEventCreateWithFlags(&c->xh_ev[i], cudaEventDisableTiming));
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        const int64_t j0 = ch * cw, j1 = std::min<int64_t>(b, j0 + cw);
+        if (j1 <= j0) break;
+        FGB_CUDA(cudaMemcpyAsync(static_cast<double*>(const_cast<void*>(x_dev)) + j0 * 2 * n, x_host + j0 * 2 * n,
+                                 (size_t)(j1 - j0) * n * 16, cudaMemcpyHostToDevice, c->aux_stream));
+        FGB_CUDA(cudaEventRecord(c->xh_ev[ch], c->aux_stream));
+    }
+    return FGFRFT_OK;
+}
+
 int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, const void* x_dev, int64_t b,
                     void* y, int l_used, const double* x_host, const WindowWeights* ww, const double* fuse_xc,
                     double* fuse_part, bool* fused) {
@@ -1877,26 +1911,16 @@ int packed_products(fgfrft_cache* c, const double* coef, int coef_ld, int rows, 
     FGB_CUDA(cudaStreamWaitEvent(c->pk_s, c->pk_e0, 0));
     FGB_CUDA(cudaStreamWaitEvent(c->pk_g, c->pk_e0, 0));
     // host X: column chunks of >= 32 signals (64 B-operand rows) copied on the aux stream
-    const int nch = x_host ? (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)pk_env("FGFRFT_E2E_CHUNKS", 4),
-                                                                        ceil_div(b, 32)))
-                           : 0;
-    const int64_t cw = x_host ? ceil_div(ceil_div(b, nch), 32) * 32 : b;
+    int nch = 0;
+    int64_t cw = b;
     if (x_host) {
-        if (!c->aux_stream) FGB_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
-        FGB_CUDA(cudaStreamWaitEvent(c->aux_stream, c->pk_e0, 0));  // the previous call's readers are done
-        if (c->xh_ev.size() < (size_t)nch) {
-            const size_t have = c->xh_ev.size();
-            c->xh_ev.resize(nch, nullptr);
-            for (size_t i = have; i < (size_t)nch; ++i)
-                FGB_CUDA(cudaEventCreateWithFlags(&c->xh_ev[i], cudaEventDisableTiming));
+        host_x_chunks(b, &nch, &cw);
+        if (c->xh_pre == x_host) {  // fgfrft_mse_step enqueued them before its host-side planning
+            c->xh_pre = nullptr;
+        } else if (int st = enqueue_host_x(c, x_host, x_dev, b)) {
+            return st;
         }
-        for (int ch = 0; ch < nch; ++ch) {
-            const int64_t j0 = ch * cw, j1 = std::min<int64_t>(b, j0 + cw);
-            if (j1 <= j0) break;
-            FGB_CUDA(cudaMemcpyAsync(static_cast<double*>(const_cast<void*>(x_dev)) + j0 * 2 * n, x_host + j0 * 2 * n,
-                                     (size_t)(j1 - j0) * n * 16, cudaMemcpyHostToDevice, c->aux_stream));
-            FGB_CUDA(cudaEventRecord(c->xh_ev[ch], c->aux_stream));
-        }
+        c->xh_pre = nullptr;
     }
     // G: X sliced once (B operand: rows 2j + comp, K = signal index), while S synthesises shell 0
     if (!x_host) {
@@ -2767,12 +2791,19 @@ int fgfrft_mse_step(fgfrft_cache* c, const double* alphas, int n_alpha, const do
             FGB_CUDA(c->xc.ensure(xe * 16));
             FGB_CUDA(c->loss.ensure((size_t)n_alpha * 2 * sizeof(double)));
             if (y) FGB_CUDA(c->y.ensure(xe * 16 * n_alpha));
+            // X onto the link first; the coefficient tables and the step's planning follow behind it
+            if (int st = enqueue_host_x(c, x, c->x.p, b)) return st;
+            c->xh_pre = x;
             double* coef = nullptr;
-            if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) return st;
-            double* ld = c->loss.as<double>();
-            if (int st = mse_packed_step(c, coef, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld, ld + n_alpha,
-                                         win ? &ww : nullptr, x, xc))
+            if (int st = upload_coefs(c, alphas, n_alpha, c->l, &coef)) {
+                c->xh_pre = nullptr;
                 return st;
+            }
+            double* ld = c->loss.as<double>();
+            const int st_step = mse_packed_step(c, coef, n_alpha, c->x.p, c->xc.p, b, y ? c->y.p : nullptr, ld,
+                                                ld + n_alpha, win ? &ww : nullptr, x, xc);
+            c->xh_pre = nullptr;
+            if (st_step) return st_step;
             std::vector<double> out(2 * (size_t)n_alpha);
             FGB_CUDA(cudaMemcpyAsync(out.data(), ld, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
             if (y) {

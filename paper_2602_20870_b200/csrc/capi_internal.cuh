@@ -450,6 +450,7 @@ struct fgfrft_cache {
     std::vector<cudaEvent_t> pk_es;
     std::vector<cudaEvent_t> xh_ev;  // host-X column chunks landed (chunked host MSE step)
     std::vector<cudaEvent_t> xch_ev; // host-Xc column chunks landed (the loss pass runs per chunk)
+    const double* xh_pre = nullptr;  // host X whose chunk copies the caller already enqueued (enqueue_host_x)
     std::vector<PkShell> pk_plan;
     uint64_t pk_plan_key = 0;
     // pinned staging for the coefficient tables: a ring of 3 (the host evaluates the next calls'
